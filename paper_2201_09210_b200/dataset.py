@@ -1,0 +1,180 @@
+"""Dataset sources backing ``input(name, shape)``.
+
+Semantics follow the reference (pkg/src/coex/dataset.py:39-95):
+
+* ``SyntheticDataset``: the o-th occurrence of ``input(name)`` is uniform in
+  [-1, 1); element e is the e-th xorshift64* draw of the stream seeded with
+  ``seed ^ fnv1a64(name) ^ (o * 0x9E3779B97F4A7C15)``.  Cursors are the only
+  mutable state; ``snapshot``/``restore`` support step replay.
+* ``FileDataset``: JSON-lines records consumed per name in file order.
+
+B200 twist: ``SyntheticDataset.next`` returns a :class:`SyntheticTensor` -- a
+lazy descriptor (generator state + shape).  The B200 backend expands it on the
+device (``coex_tensor_synth`` / ``coex_pass_feed_synth``), bit-identical to the
+reference's Python loop, so a step's input batch never crosses PCIe.  Host code
+that needs the numbers (print, natives) calls ``materialize()``, which runs a
+vectorised host expansion with the same bits.
+"""
+
+from __future__ import annotations
+
+import json
+
+import numpy as np
+
+from .errors import DatasetExhausted, EvalError
+from .rng import MASK64, XS_MULT, seeded_state, xs_step
+from .tensor import Tensor, shape_size
+
+OCC_MIX = 0x9E3779B97F4A7C15
+
+
+def synth_values(state: int, n: int) -> np.ndarray:
+    """Host expansion of ``n`` draws from generator ``state`` mapped to [-1, 1).
+
+    Bit-identical to ``gen.next_unit() * 2.0 - 1.0`` repeated n times
+    (dataset.py:49-50): the sequential xorshift walk is done on uint64 lanes of
+    64 interleaved sub-streams (each lane jumps 64 states at a time)."""
+    out = np.empty(n, dtype=np.float64)
+    if n == 0:
+        return out
+    lanes = min(n, 64)
+    starts = np.empty(lanes, dtype=np.uint64)
+    x = state
+    for i in range(lanes):
+        x = xs_step(x)
+        starts[i] = x
+    rows = -(-n // lanes)
+    states = np.empty((rows, lanes), dtype=np.uint64)
+    states[0] = starts
+    if rows > 1:
+        from .rng import jump_columns
+        cols = np.array(jump_columns(6) if lanes == 64 else _cols_for(lanes), dtype=np.uint64)
+        cur = starts.copy()
+        for r in range(1, rows):
+            cur = _apply_matrix(cols, cur)
+            states[r] = cur
+    flat = states.reshape(-1)[:n]
+    prod = flat * np.uint64(XS_MULT)
+    out[:] = (prod >> np.uint64(11)).astype(np.float64) * (2.0 ** -53) * 2.0 - 1.0
+    return out
+
+
+def _cols_for(k: int) -> list:
+    cols = []
+    for b in range(64):
+        v = 1 << b
+        for _ in range(k):
+            v = xs_step(v)
+        cols.append(v)
+    return cols
+
+
+def _apply_matrix(cols: np.ndarray, v: np.ndarray) -> np.ndarray:
+    r = np.zeros_like(v)
+    for b in range(64):
+        bit = (v >> np.uint64(b)) & np.uint64(1)
+        r ^= cols[b] * bit
+    return r
+
+
+class SyntheticTensor:
+    """Lazy synthetic input: generator ``state`` expands to ``shape`` values."""
+
+    __slots__ = ("state", "shape", "_host")
+
+    def __init__(self, state: int, shape):
+        self.state = state & MASK64
+        self.shape = tuple(int(d) for d in shape)
+        self._host = None
+
+    def size(self) -> int:
+        return shape_size(self.shape)
+
+    def rank(self) -> int:
+        return len(self.shape)
+
+    def materialize(self) -> Tensor:
+        if self._host is None:
+            self._host = Tensor._wrap(synth_values(self.state, self.size()).reshape(self.shape))
+        return self._host
+
+    @property
+    def data(self):
+        return self.materialize().data
+
+    def to_nested(self):
+        return self.materialize().to_nested()
+
+
+class DatasetSource:
+    def next(self, name: str, shape, step: int):
+        raise NotImplementedError
+
+    def snapshot(self) -> dict:
+        raise NotImplementedError
+
+    def restore(self, snap: dict):
+        raise NotImplementedError
+
+
+class SyntheticDataset(DatasetSource):
+    """Uniform [-1, 1) tensors keyed by (seed, name, occurrence) (dataset.py:39-57)."""
+
+    def __init__(self, seed: int, lazy: bool = True):
+        self.seed = seed
+        self.lazy = lazy
+        self._cursors: dict = {}
+
+    def next(self, name: str, shape, step: int):
+        if shape is None:
+            raise EvalError(f"input({name!r}): the synthetic dataset needs an explicit shape", step)
+        occ = self._cursors.get(name, 0)
+        self._cursors[name] = occ + 1
+        st = seeded_state(self.seed, name, (occ * OCC_MIX) & MASK64)
+        t = SyntheticTensor(st, shape)
+        return t if self.lazy else t.materialize()
+
+    def snapshot(self) -> dict:
+        return dict(self._cursors)
+
+    def restore(self, snap: dict):
+        self._cursors = dict(snap)
+
+
+class FileDataset(DatasetSource):
+    """JSON-lines records ``{"name", "shape", "data"}`` consumed per name (dataset.py:60-95)."""
+
+    def __init__(self, path: str):
+        self.path = path
+        self._records: dict = {}
+        self._cursors: dict = {}
+        with open(path, "r", encoding="utf-8") as fh:
+            for lineno, raw in enumerate(fh, 1):
+                raw = raw.strip()
+                if not raw:
+                    continue
+                try:
+                    rec = json.loads(raw)
+                    t = Tensor(tuple(rec["shape"]), np.asarray(rec["data"], dtype=float))
+                    nm = rec["name"]
+                except (KeyError, ValueError, TypeError) as exc:
+                    raise EvalError(f"{path}:{lineno}: bad dataset record ({exc})") from exc
+                self._records.setdefault(nm, []).append(t)
+
+    def next(self, name: str, shape, step: int):
+        recs = self._records.get(name, [])
+        i = self._cursors.get(name, 0)
+        if i >= len(recs):
+            raise DatasetExhausted(f"input({name!r}): dataset exhausted after {i} record(s)", step)
+        self._cursors[name] = i + 1
+        t = recs[i]
+        if shape is not None and t.shape != tuple(shape):
+            raise EvalError(f"input({name!r}): record {i} has shape {list(t.shape)}, expected {list(shape)}", step)
+        return t
+
+    def snapshot(self) -> dict:
+        return dict(self._cursors)
+
+    def restore(self, snap: dict):
+        self._cursors = dict(snap)
