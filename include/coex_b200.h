@@ -1,0 +1,134 @@
+/*
+ * coex_b200.h -- C-ABI of the B200 symbolic-execution backend (libcoexb200.so).
+ *
+ * Drop-in boundary for the reference's symbolic executor.  The reference (a
+ * pure-Python package, /root/reference/pkg) has no FFI; its boundary for this
+ * path is the Python surface each entry point below replaces:
+ *
+ *   coex_exec_op            <- coex.tensor.execute_kernel     pkg/src/coex/tensor.py:246-291
+ *   coex_tensor_put/get     <- coex.tensor.Tensor marshalling pkg/src/coex/tensor.py:69-102
+ *   coex_tensor_synth       <- coex.dataset.SyntheticDataset.next  pkg/src/coex/dataset.py:44-51
+ *   coex_var_*              <- graph_runner.VariableStore / snapshot_vars / rollback
+ *   coex_prog_build         <- graph_gen.structure output (SymProgram) consumed by run_pass
+ *   coex_pass_begin/_wait   <- graph_runner.run_pass (Committed | Cancelled)
+ *   coex_pass_case/_loop    <- ChannelSet.decisions push (CaseDecision / LoopDecision)
+ *   coex_pass_feed*         <- ChannelSet.feeds push
+ *   coex_pass_fetch         <- ChannelSet.fetches pop
+ *   coex_pass_cancel        <- ChannelSet.cancel
+ *
+ * Status codes map 1:1 onto the reference's exception classes
+ * (pkg/src/coex/errors.py:6-90); coex_last_error() returns the message of the
+ * last failing call on the calling thread.  All data crosses the ABI as
+ * float64 (the reference's only dtype, tensor.py:1-11); the device stores it in
+ * the context's precision.  Every call is made from one host thread (the
+ * orchestrator/skeleton thread); the GPU plays the runner thread.
+ */
+#ifndef COEX_B200_H
+#define COEX_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum coex_status {
+  COEX_OK = 0,
+  COEX_SHAPE_MISMATCH = 1,   /* errors.ShapeMismatch */
+  COEX_BAD_ATTRS = 2,        /* errors.BadAttrs */
+  COEX_DECISION_MISMATCH = 3,/* errors.DecisionMismatch */
+  COEX_CHANNEL_CLOSED = 4,   /* errors.ChannelClosed (peer failed / timeout) */
+  COEX_CANCELLED = 5,        /* pass ended Cancelled */
+  COEX_IN_FLIGHT_PASS = 6,   /* errors.InFlightPass */
+  COEX_BUDGET = 7,           /* errors.BudgetExceeded */
+  COEX_CUDA_ERROR = 8,       /* device / driver failure */
+  COEX_SHAPE_MISS = 9,       /* fed shape differs from the graph's specialisation */
+  COEX_INVALID = 10          /* bad handle / argument */
+};
+
+/* OpKind codes (order of coex.tensor.OpKind, tensor.py:30-44). */
+enum coex_opkind {
+  COEX_MATMUL = 0, COEX_ADD, COEX_SUB, COEX_MUL, COEX_NEG, COEX_RELU, COEX_SIGMOID,
+  COEX_SUM, COEX_MEAN, COEX_TRANSPOSE, COEX_RESHAPE, COEX_FILL, COEX_READ_VAR, COEX_ASSIGN_VAR
+};
+
+/* Device storage / arithmetic precision of a context. */
+enum coex_precision {
+  COEX_F64 = 0,   /* parity mode: bitwise equal to the reference except Sigmoid (<= few ulp) */
+  COEX_F32 = 1,   /* fp32 storage and arithmetic (<= 1e-5 relative) */
+  COEX_BF16 = 2   /* fp32 storage, MatMul on tcgen05 with bf16 operands (<= 2e-2 relative) */
+};
+
+#define COEX_MAX_RANK 8
+
+typedef struct coex_ctx coex_ctx;
+typedef struct coex_prog coex_prog;
+
+/* Op attributes: perm (TRANSPOSE), target_shape (RESHAPE), shape + value (FILL). */
+typedef struct coex_attrs {
+  int32_t n;                      /* entries used in dims */
+  int64_t dims[COEX_MAX_RANK];
+  double value;                   /* FILL value */
+} coex_attrs;
+
+typedef struct coex_pass_stats {
+  int32_t committed;              /* 1 = Committed, 0 = Cancelled */
+  int32_t status;                 /* coex_status of the device side */
+  double exec_ms;                 /* device time of the pass (begin..end kernels) */
+  double stall_ms;                /* device time spent waiting on decisions/feeds */
+  int64_t ops;                    /* compute kernels executed */
+  int64_t fetches;                /* fetch entries published */
+  uint64_t dirty_mask;            /* vars committed by this pass (first 64 var indices) */
+} coex_pass_stats;
+
+const char* coex_last_error(void);
+const char* coex_version(void);
+
+/* ---- context ---- */
+int coex_ctx_create(int device, int precision, coex_ctx** out);
+int coex_ctx_destroy(coex_ctx* ctx);
+int coex_ctx_sync(coex_ctx* ctx);
+int coex_ctx_set_timeout(coex_ctx* ctx, double seconds);
+/* Number of compute kernels this context launched eagerly or replayed in graphs. */
+int64_t coex_ctx_kernel_count(coex_ctx* ctx);
+
+/* ---- tensors (eager side) ---- */
+int coex_tensor_put(coex_ctx* ctx, int ndim, const int64_t* shape, const double* data, int64_t* id);
+int coex_tensor_synth(coex_ctx* ctx, uint64_t state, int ndim, const int64_t* shape, int64_t* id);
+int coex_tensor_get(coex_ctx* ctx, int64_t id, double* out, int64_t cap, int* ndim, int64_t* shape);
+int coex_tensor_info(coex_ctx* ctx, int64_t id, int* ndim, int64_t* shape);
+int coex_tensor_free(coex_ctx* ctx, int64_t id);
+int coex_exec_op(coex_ctx* ctx, int kind, const coex_attrs* attrs, int nin, const int64_t* in_ids,
+                 int64_t* out_id);
+
+/* ---- variable store ---- */
+int coex_var_define(coex_ctx* ctx, const char* name, int64_t tensor_id, int* var_index);
+int coex_var_read(coex_ctx* ctx, int var_index, int64_t* tensor_id);
+int coex_var_assign(coex_ctx* ctx, int var_index, int64_t tensor_id);
+int coex_var_info(coex_ctx* ctx, int var_index, int* ndim, int64_t* shape);
+int coex_var_rollback(coex_ctx* ctx);
+
+/* ---- symbolic programs ---- */
+/* plan: int64 words produced by the host planner (paper_2201_09210_b200/planner.py). */
+int coex_prog_build(coex_ctx* ctx, const int64_t* plan, int64_t nwords, const double* consts,
+                    int64_t nconsts, coex_prog** out);
+int coex_prog_destroy(coex_prog* prog);
+int coex_prog_info(coex_prog* prog, int64_t* n_kernel_nodes, int64_t* n_cond_nodes, int64_t* arena_bytes);
+
+/* ---- one pass (one co-execution step) ---- */
+int coex_pass_begin(coex_prog* prog);
+int coex_pass_case(coex_prog* prog, int64_t branch_id, int32_t case_index);
+int coex_pass_loop(coex_prog* prog, int64_t loop_id, int32_t cont);
+int coex_pass_feed(coex_prog* prog, int64_t slot, int ndim, const int64_t* shape, const double* data);
+int coex_pass_feed_synth(coex_prog* prog, int64_t slot, uint64_t state, int ndim, const int64_t* shape);
+int coex_pass_feed_tensor(coex_prog* prog, int64_t slot, int64_t tensor_id);
+int coex_pass_fetch(coex_prog* prog, int64_t node_id, int64_t occurrence, double* out, int64_t cap,
+                    int* ndim, int64_t* shape);
+int coex_pass_cancel(coex_prog* prog);
+int coex_pass_wait(coex_prog* prog, coex_pass_stats* stats);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* COEX_B200_H */

@@ -1,0 +1,405 @@
+"""The B200 backend: ctypes binding of libcoexb200.so (include/coex_b200.h).
+
+* :class:`B200Backend` implements the backend protocol of :mod:`.runner_api`
+  on the device: eager ops for imperative / tracing / replay steps, the device
+  variable store, and symbolic passes.
+* :class:`B200Program` caches one CUDA graph per shape signature of a
+  SymProgram (built by :mod:`.planner`, instantiated by ``coex_prog_build``).
+* :class:`B200Pass` is the skeleton's side of one pass: decisions and feeds
+  are published to the pinned mapped rings, fetches spin on the fetch ring.
+  Lazy mode withholds publication (and the launch) until a fetch or StepEnd.
+
+There is no CPU fallback: constructing a backend without the built library or
+without a CUDA device raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+from .dataset import SyntheticTensor
+from .errors import STATUS, ChannelClosed, CoexError, DeviceError, ShapeMiss
+from .planner import Planner, slot_code
+from .runner_api import PassResult
+from .tensor import OpKind, Tensor, shape_size
+from .trace_graph import CaseDecision, LoopDecision
+
+LIB_NAME = "libcoexb200.so"
+MAX_RANK = 8
+PRECISIONS = {"f64": 0, "fp32": 1, "bf16": 2}
+
+
+class CoexAttrs(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int32), ("dims", ctypes.c_int64 * MAX_RANK), ("value", ctypes.c_double)]
+
+
+class CoexPassStats(ctypes.Structure):
+    _fields_ = [("committed", ctypes.c_int32), ("status", ctypes.c_int32), ("exec_ms", ctypes.c_double),
+                ("stall_ms", ctypes.c_double), ("ops", ctypes.c_int64), ("fetches", ctypes.c_int64),
+                ("dirty_mask", ctypes.c_uint64)]
+
+
+_P = ctypes.c_void_p
+_I64 = ctypes.c_int64
+_I64P = ctypes.POINTER(ctypes.c_int64)
+_DP = ctypes.POINTER(ctypes.c_double)
+_IP = ctypes.POINTER(ctypes.c_int)
+
+SIGNATURES = {
+    "coex_last_error": (ctypes.c_char_p, []),
+    "coex_version": (ctypes.c_char_p, []),
+    "coex_ctx_create": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.POINTER(_P)]),
+    "coex_ctx_destroy": (ctypes.c_int, [_P]),
+    "coex_ctx_sync": (ctypes.c_int, [_P]),
+    "coex_ctx_set_timeout": (ctypes.c_int, [_P, ctypes.c_double]),
+    "coex_ctx_kernel_count": (_I64, [_P]),
+    "coex_tensor_put": (ctypes.c_int, [_P, ctypes.c_int, _I64P, _DP, _I64P]),
+    "coex_tensor_synth": (ctypes.c_int, [_P, ctypes.c_uint64, ctypes.c_int, _I64P, _I64P]),
+    "coex_tensor_get": (ctypes.c_int, [_P, _I64, _DP, _I64, _IP, _I64P]),
+    "coex_tensor_info": (ctypes.c_int, [_P, _I64, _IP, _I64P]),
+    "coex_tensor_free": (ctypes.c_int, [_P, _I64]),
+    "coex_exec_op": (ctypes.c_int, [_P, ctypes.c_int, ctypes.POINTER(CoexAttrs), ctypes.c_int, _I64P, _I64P]),
+    "coex_var_define": (ctypes.c_int, [_P, ctypes.c_char_p, _I64, _IP]),
+    "coex_var_read": (ctypes.c_int, [_P, ctypes.c_int, _I64P]),
+    "coex_var_assign": (ctypes.c_int, [_P, ctypes.c_int, _I64]),
+    "coex_var_info": (ctypes.c_int, [_P, ctypes.c_int, _IP, _I64P]),
+    "coex_var_rollback": (ctypes.c_int, [_P]),
+    "coex_prog_build": (ctypes.c_int, [_P, _I64P, _I64, _DP, _I64, ctypes.POINTER(_P)]),
+    "coex_prog_destroy": (ctypes.c_int, [_P]),
+    "coex_prog_info": (ctypes.c_int, [_P, _I64P, _I64P, _I64P]),
+    "coex_pass_begin": (ctypes.c_int, [_P]),
+    "coex_pass_case": (ctypes.c_int, [_P, _I64, ctypes.c_int32]),
+    "coex_pass_loop": (ctypes.c_int, [_P, _I64, ctypes.c_int32]),
+    "coex_pass_feed": (ctypes.c_int, [_P, _I64, ctypes.c_int, _I64P, _DP]),
+    "coex_pass_feed_synth": (ctypes.c_int, [_P, _I64, ctypes.c_uint64, ctypes.c_int, _I64P]),
+    "coex_pass_feed_tensor": (ctypes.c_int, [_P, _I64, _I64]),
+    "coex_pass_fetch": (ctypes.c_int, [_P, _I64, _I64, _DP, _I64, _IP, _I64P]),
+    "coex_pass_cancel": (ctypes.c_int, [_P]),
+    "coex_pass_wait": (ctypes.c_int, [_P, ctypes.POINTER(CoexPassStats)]),
+}
+
+_LIB = None
+
+
+def lib_path() -> str:
+    return os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
+
+
+def load_library():
+    """Load the in-tree libcoexb200.so; raise (no fallback) when it is missing."""
+    global _LIB
+    if _LIB is None:
+        path = lib_path()
+        if not os.path.exists(path):
+            raise DeviceError(f"{path} is not built; run __graft_entry__.build() "
+                              "(there is no CPU fallback for the B200 backend)")
+        lib = ctypes.CDLL(path)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _LIB = lib
+    return _LIB
+
+
+def _check(rc: int):
+    if rc != 0:
+        msg = _LIB.coex_last_error().decode(errors="replace")
+        raise STATUS.get(rc, CoexError)(msg)
+
+
+def _shape_arr(shape):
+    a = (ctypes.c_int64 * MAX_RANK)()
+    for i, d in enumerate(shape):
+        a[i] = int(d)
+    return a
+
+
+class DevTensor:
+    """A device tensor handle owned by a context (freed on GC)."""
+
+    __slots__ = ("be", "id", "shape", "__weakref__")
+
+    def __init__(self, be, tid: int, shape: tuple):
+        self.be = be
+        self.id = tid
+        self.shape = tuple(shape)
+
+    def __del__(self):
+        be = self.be
+        if be is not None and be.ctx is not None and _LIB is not None:
+            _LIB.coex_tensor_free(be.ctx, self.id)
+
+    def size(self):
+        return shape_size(self.shape)
+
+
+class B200Backend:
+    """Backend protocol (runner_api.py) on one B200 through libcoexb200.so."""
+
+    name = "b200"
+
+    def __init__(self, device: int = 0, precision: str = "f64", timeout_s: float = 120.0):
+        self.lib = load_library()
+        if precision not in PRECISIONS:
+            raise ValueError(f"precision must be one of {sorted(PRECISIONS)}")
+        self.precision = precision
+        self.esize = 8 if precision == "f64" else 4
+        ctx = _P()
+        _check(self.lib.coex_ctx_create(device, PRECISIONS[precision], ctypes.byref(ctx)))
+        self.ctx = ctx
+        self.lib.coex_ctx_set_timeout(ctx, timeout_s)
+        self.var_idx: dict = {}
+        self._vshape: dict = {}
+        self.active = None
+
+    def close(self):
+        if self.ctx is not None:
+            self.lib.coex_ctx_destroy(self.ctx)
+            self.ctx = None
+
+    def kernel_count(self) -> int:
+        return int(self.lib.coex_ctx_kernel_count(self.ctx))
+
+    def sync(self):
+        _check(self.lib.coex_ctx_sync(self.ctx))
+
+    # ------------------------------------------------------------ eager side
+    def put(self, t) -> DevTensor:
+        if isinstance(t, DevTensor):
+            return t
+        tid = ctypes.c_int64()
+        if isinstance(t, SyntheticTensor):
+            _check(self.lib.coex_tensor_synth(self.ctx, t.state, len(t.shape), _shape_arr(t.shape), ctypes.byref(tid)))
+            return DevTensor(self, tid.value, t.shape)
+        if not isinstance(t, Tensor):
+            raise TypeError(f"cannot put {type(t).__name__}")
+        data = np.ascontiguousarray(t.data, dtype=np.float64)
+        _check(self.lib.coex_tensor_put(self.ctx, len(t.shape), _shape_arr(t.shape),
+                                        data.ctypes.data_as(_DP), ctypes.byref(tid)))
+        return DevTensor(self, tid.value, t.shape)
+
+    def get(self, v) -> Tensor:
+        if isinstance(v, Tensor):
+            return v
+        if isinstance(v, SyntheticTensor):
+            return v.materialize()
+        out = np.empty(max(shape_size(v.shape), 1), dtype=np.float64)
+        nd = ctypes.c_int()
+        shp = (ctypes.c_int64 * MAX_RANK)()
+        _check(self.lib.coex_tensor_get(self.ctx, v.id, out.ctypes.data_as(_DP), out.size, ctypes.byref(nd), shp))
+        return Tensor._wrap(out[:shape_size(v.shape)].reshape(v.shape))
+
+    def exec_op(self, kind: OpKind, attrs: dict, values: list) -> DevTensor:
+        devs = [self.put(v) for v in values]
+        at = CoexAttrs()
+        if kind is OpKind.TRANSPOSE:
+            dims = attrs["perm"]
+        elif kind is OpKind.RESHAPE:
+            dims = attrs["target_shape"]
+        elif kind is OpKind.FILL:
+            dims = attrs["shape"]
+            at.value = float(attrs["value"])
+        else:
+            dims = ()
+        if len(dims) > MAX_RANK:
+            raise CoexError(f"rank {len(dims)} exceeds {MAX_RANK}")
+        at.n = len(dims)
+        for i, d in enumerate(dims):
+            at.dims[i] = int(d)
+        ids = (ctypes.c_int64 * 2)(*[d.id for d in devs], *([0] * (2 - len(devs))))
+        out = ctypes.c_int64()
+        _check(self.lib.coex_exec_op(self.ctx, kind.code, ctypes.byref(at), len(devs), ids, ctypes.byref(out)))
+        nd = ctypes.c_int()
+        shp = (ctypes.c_int64 * MAX_RANK)()
+        _check(self.lib.coex_tensor_info(self.ctx, out.value, ctypes.byref(nd), shp))
+        return DevTensor(self, out.value, tuple(shp[i] for i in range(nd.value)))
+
+    # ------------------------------------------------------------ variables
+    def var_define(self, name: str, value):
+        d = self.put(value)
+        idx = ctypes.c_int()
+        _check(self.lib.coex_var_define(self.ctx, name.encode(), d.id, ctypes.byref(idx)))
+        self.var_idx[name] = idx.value
+        self._vshape[name] = tuple(d.shape)
+
+    def var_read(self, name: str) -> DevTensor:
+        tid = ctypes.c_int64()
+        _check(self.lib.coex_var_read(self.ctx, self.var_idx[name], ctypes.byref(tid)))
+        return DevTensor(self, tid.value, self._vshape[name])
+
+    def var_assign(self, name: str, value):
+        d = self.put(value)
+        _check(self.lib.coex_var_assign(self.ctx, self.var_idx[name], d.id))
+        self._vshape[name] = tuple(d.shape)
+
+    def var_shape(self, name: str) -> tuple:
+        return self._vshape[name]
+
+    def var_shapes(self) -> dict:
+        return dict(self._vshape)
+
+    def snapshot_vars(self) -> dict:
+        if self.active is not None:
+            from .errors import InFlightPass
+            raise InFlightPass("snapshot_vars during an in-flight pass")
+        return {name: self.get(self.var_read(name)) for name in self.var_idx}
+
+    def rollback(self):
+        _check(self.lib.coex_var_rollback(self.ctx))
+
+    # ------------------------------------------------------------ symbolic side
+    def compile(self, sp, tg) -> "B200Program":
+        return B200Program(self, sp, tg)
+
+    def begin_pass(self, prog: "B200Program", lazy: bool = False) -> "B200Pass":
+        return B200Pass(self, prog, lazy)
+
+
+class B200Program:
+    """A SymProgram with its CUDA graphs, one per shape signature."""
+
+    def __init__(self, be: B200Backend, sp, tg):
+        self.be = be
+        self.sp = sp
+        self.tg = tg
+        self.graphs: dict = {}
+        self.feed_shape: dict = {}       # slot -> expected shape (observed hints, updated on misses)
+        self.node_of_slot = {}
+        for n in tg.all_nodes():
+            if n.typ == "op":
+                for pos, s in n.feed_shapes.items():
+                    self.feed_shape[(n.id, pos)] = tuple(s)
+        self.last_plan = None
+
+    def specialise(self):
+        """The (graph handle, plan) for the current variable shapes."""
+        vsh = {n: self.be.var_shape(n) for n in self.be.var_idx}
+        key = (tuple(sorted(vsh.items())), tuple(sorted(self.feed_shape.items())))
+        hit = self.graphs.get(key)
+        if hit is not None:
+            return hit
+        plan = Planner(self.sp, self.tg, self.be.var_idx, vsh, self.feed_shape, self.be.esize).build()
+        words = np.asarray(plan.words, dtype=np.int64)
+        consts = np.asarray(plan.consts if plan.consts else [0.0], dtype=np.float64)
+        handle = _P()
+        _check(self.be.lib.coex_prog_build(self.be.ctx, words.ctypes.data_as(_I64P), words.size,
+                                           consts.ctypes.data_as(_DP), len(plan.consts), ctypes.byref(handle)))
+        self.graphs[key] = (handle, plan)
+        self.last_plan = plan
+        return handle, plan
+
+    def info(self, handle) -> dict:
+        nk, nc, ab = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        self.be.lib.coex_prog_info(handle, ctypes.byref(nk), ctypes.byref(nc), ctypes.byref(ab))
+        return {"kernel_nodes": nk.value, "conditional_nodes": nc.value, "arena_bytes": ab.value}
+
+    def close(self):
+        for handle, _ in self.graphs.values():
+            self.be.lib.coex_prog_destroy(handle)
+        self.graphs.clear()
+
+
+class B200Pass:
+    """Skeleton-side channel of one in-flight pass (ChannelSet)."""
+
+    def __init__(self, be: B200Backend, prog: B200Program, lazy: bool):
+        self.be = be
+        self.lib = be.lib
+        self.prog = prog
+        self.lazy = lazy
+        self.handle, self.plan = prog.specialise()
+        self.launched = False
+        self.pending: list = []
+        self.keep: list = []             # device tensors fed by pointer must outlive the pass
+        self.cancelled = False
+        self.result = None
+        if not lazy:
+            self._launch()
+
+    def _launch(self):
+        if self.be.active is not None:
+            raise ChannelClosed("another pass is in flight")
+        _check(self.lib.coex_pass_begin(self.handle))
+        self.be.active = self
+        self.launched = True
+
+    def _flush(self):
+        if not self.launched:
+            self._launch()
+        for fn, args in self.pending:
+            _check(fn(*args))
+        self.pending.clear()
+
+    def _do(self, fn, *args):
+        if self.lazy:
+            self.pending.append((fn, (self.handle,) + args))
+        else:
+            _check(fn(self.handle, *args))
+
+    def decide(self, d):
+        if isinstance(d, CaseDecision):
+            self._do(self.lib.coex_pass_case, d.branch_id, d.case_index)
+        elif isinstance(d, LoopDecision):
+            self._do(self.lib.coex_pass_loop, d.loop_id, 1 if d.cont else 0)
+        else:
+            raise CoexError(f"unknown decision {d!r}")
+
+    def feed(self, slot, v):
+        want = self.plan.feed_shapes.get(slot)
+        shape = tuple(v.shape)
+        if want is None or tuple(want) != shape:
+            self.prog.feed_shape[slot] = shape           # next specialisation uses the observed shape
+            raise ShapeMiss(f"feed slot {slot}: shape {shape} but the graph expects {want}")
+        code = slot_code(slot)
+        if isinstance(v, DevTensor):
+            self.keep.append(v)
+            self._do(self.lib.coex_pass_feed_tensor, code, v.id)
+        elif isinstance(v, SyntheticTensor):
+            self._do(self.lib.coex_pass_feed_synth, code, ctypes.c_uint64(v.state), len(shape), _shape_arr(shape))
+        else:
+            data = np.ascontiguousarray(v.data, dtype=np.float64)
+            self.keep.append(data)
+            self._do(self.lib.coex_pass_feed, code, len(shape), _shape_arr(shape), data.ctypes.data_as(_DP))
+
+    def fetch(self, nid: int, k: int) -> Tensor:
+        if self.lazy:
+            self._flush()
+        shp_expect = self.plan.node_shapes[nid]
+        out = np.empty(max(shape_size(shp_expect), 1), dtype=np.float64)
+        nd = ctypes.c_int()
+        shp = (ctypes.c_int64 * MAX_RANK)()
+        _check(self.lib.coex_pass_fetch(self.handle, nid, k, out.ctypes.data_as(_DP), out.size, ctypes.byref(nd), shp))
+        shape = tuple(shp[i] for i in range(nd.value))
+        return Tensor._wrap(out[:shape_size(shape)].reshape(shape))
+
+    def cancel(self):
+        self.cancelled = True
+        if self.launched:
+            self.lib.coex_pass_cancel(self.handle)
+
+    def wait(self) -> PassResult:
+        if self.result is not None:
+            return self.result
+        if not self.launched:
+            if self.cancelled:
+                self.result = PassResult(False)
+                return self.result
+            self._flush()
+        elif self.lazy:
+            self._flush()
+        st = CoexPassStats()
+        rc = self.lib.coex_pass_wait(self.handle, ctypes.byref(st))
+        self.be.active = None
+        self.keep.clear()
+        if rc not in (0, 5):
+            msg = self.lib.coex_last_error().decode(errors="replace")
+            self.result = PassResult(False, st.exec_ms, st.stall_ms, st.ops, st.fetches, error=msg)
+            if rc == 3:
+                raise STATUS[rc](msg)
+            return self.result
+        self.result = PassResult(bool(st.committed), st.exec_ms, st.stall_ms, st.ops, st.fetches)
+        return self.result

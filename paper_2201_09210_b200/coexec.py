@@ -155,7 +155,13 @@ class Orchestrator:
         """SPEC.md:525-533 (and the lazy variant)."""
         snap = self.ds.snapshot()
         lines_before = len(self.it.out)
-        ch = self.be.begin_pass(self.compiled, lazy=lazy)
+        try:
+            ch = self.be.begin_pass(self.compiled, lazy=lazy)
+        except ShapeMiss:
+            # no graph for this shape signature yet and no hint to build one: run inline
+            self.stats.shape_replays += 1
+            self._imperative_step(step)
+            return
         rec = _DecisionRecorder(ch)
         cursor = Cursor(self.tg, self.sp.unrolled)
         ctx = SkeletonCtx(self.be, step, cursor, rec, check=self.mode is Mode.skeleton_check, stats=self.stats)

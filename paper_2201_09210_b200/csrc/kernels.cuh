@@ -1,0 +1,811 @@
+// kernels.cuh -- sm_100a device code of the B200 symbolic-execution backend.
+//
+// Every compute kernel serves both execution paths:
+//   * eager (coex_exec_op: imperative / tracing / replay steps) -- operands are
+//     passed as direct device pointers;
+//   * graph (one CUDA Graph per SymProgram specialisation) -- operands are read
+//     through *cells*: device words holding the pointer of the latest execution
+//     of the producing node (phi semantics for branch merges / loop-carried
+//     values).
+// Reference semantics (float64, pinned orders) are in pkg/src/coex/tensor.py;
+// each kernel cites the lines it reproduces.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace coex {
+
+constexpr int kMaxRank = 8;
+constexpr int kMaxPub = 6;
+
+// ------------------------------------------------------------------ pass state
+// One per context, in device memory.  Reset by k_pass_begin.
+struct DevState {
+  int cancelled;                  // later kernels become no-ops
+  int status;                     // coex_status of a device-detected failure
+  unsigned long long pass_id;
+  long long dec_head;             // decisions consumed this pass
+  long long feed_head;            // feeds consumed this pass
+  long long fetch_head;           // fetch entries published this pass
+  unsigned long long fetch_bytes; // fetch payload arena bump pointer
+  unsigned long long stall_ns;    // time spent spinning on the host
+  long long ops;                  // compute kernels executed (not skipped)
+  unsigned long long t_begin;
+};
+
+// Host <-> device rings in pinned, mapped host memory.
+constexpr int kDecCap = 1024;
+constexpr int kFeedCap = 1024;
+constexpr int kFetchCap = 4096;
+
+struct DecEntry {
+  volatile unsigned long long seq;
+  long long id;
+  int kind;     // 0 = case, 1 = loop
+  int value;    // case index / continue flag
+};
+
+enum FeedType { FEED_SCALAR = 0, FEED_HOST = 1, FEED_SYNTH = 2, FEED_DEVICE = 3 };
+
+struct FeedEntry {
+  volatile unsigned long long seq;
+  long long slot;
+  int type;
+  int ndim;
+  long long shape[kMaxRank];
+  unsigned long long state;    // FEED_SYNTH generator state
+  double scalar;               // FEED_SCALAR value
+  unsigned long long off;      // FEED_HOST payload offset in the feed arena (doubles)
+  const void* dptr;            // FEED_DEVICE pointer (already in the context precision)
+};
+
+struct FetchEntry {
+  volatile unsigned long long seq;
+  long long node;
+  unsigned long long off;      // payload offset (bytes) in the fetch arena
+  long long numel;
+  int ndim;
+  int pad;
+  long long shape[kMaxRank];
+};
+
+struct Mailbox {
+  volatile unsigned long long pass_id;   // host: set before launch
+  volatile unsigned long long cancel;    // host: = pass_id to cancel
+  volatile unsigned long long done;      // device: = pass_id when the pass ended
+  volatile int status;
+  volatile int committed;
+  volatile long long dec_consumed;
+  volatile long long feed_consumed;
+  volatile unsigned long long exec_ns;
+  volatile unsigned long long stall_ns;
+  volatile long long ops;
+  volatile long long fetches;
+  volatile unsigned long long dirty_mask;
+  volatile int var_shape_id[64];
+  DecEntry dec[kDecCap];
+  FeedEntry feed[kFeedCap];
+  FetchEntry fetch[kFetchCap];
+};
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const volatile unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(volatile unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__host__ __device__ __forceinline__ unsigned long long seq_of(unsigned long long pass_id, long long idx) {
+  return (pass_id << 24) + (unsigned long long)idx + 1ull;
+}
+
+// ------------------------------------------------------------------ operands
+struct In {
+  const void* direct;
+  void* const* cell;
+};
+template <typename T>
+__device__ __forceinline__ const T* res(const In& x) {
+  return (const T*)(x.cell ? *x.cell : x.direct);
+}
+
+struct Out {
+  void* buf[2];          // buf[1] used only when pingpong
+  int pingpong;          // node may read its own previous output
+  int npub;
+  void** pub[kMaxPub];   // cells that receive the chosen output pointer
+  unsigned int* late;    // non-null: publish from the last block (node reads a cell it publishes)
+};
+
+template <typename T>
+__device__ __forceinline__ T* pick_out(const Out& o, const void* a, const void* b) {
+  if (!o.pingpong) return (T*)o.buf[0];
+  return (T*)((a == o.buf[0] || b == o.buf[0]) ? o.buf[1] : o.buf[0]);
+}
+
+// Early publication: block 0 / thread 0, before compute (safe when no block reads a published cell).
+__device__ __forceinline__ void publish_early(const Out& o, void* out) {
+  if (o.late == nullptr && blockIdx.x == 0 && threadIdx.x == 0)
+    for (int i = 0; i < o.npub; ++i) *o.pub[i] = out;
+}
+// Late publication: the last block to finish writes the cells.
+__device__ __forceinline__ void publish_late(const Out& o, void* out) {
+  if (o.late == nullptr) return;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    unsigned int prev = atomicAdd(o.late, 1u);
+    if (prev == gridDim.x - 1) {
+      for (int i = 0; i < o.npub; ++i) *o.pub[i] = out;
+      *o.late = 0u;
+    }
+  }
+}
+
+__device__ __forceinline__ bool skip(const DevState* ds) {
+  return ds != nullptr && *(volatile const int*)&ds->cancelled;
+}
+__device__ __forceinline__ void count_op(DevState* ds) {
+  if (ds != nullptr && blockIdx.x == 0 && threadIdx.x == 0) ds->ops += 1;
+}
+
+// ------------------------------------------------------------------ elementwise
+// ADD/SUB/MUL with rank-0 broadcast (tensor.py:121-128, 261-263); NEG/RELU/SIGMOID (tensor.py:264-270).
+enum EwOp { EW_ADD = 0, EW_SUB = 1, EW_MUL = 2, EW_NEG = 3, EW_RELU = 4, EW_SIGMOID = 5, EW_COPY = 6 };
+
+__device__ __forceinline__ double ew_apply(int op, double a, double b) {
+  switch (op) {
+    case EW_ADD: return __dadd_rn(a, b);
+    case EW_SUB: return __dsub_rn(a, b);
+    case EW_MUL: return __dmul_rn(a, b);
+    case EW_NEG: return -a;
+    case EW_RELU: return (a > 0.0 || a != a) ? a : 0.0;        // np.maximum(x, 0): NaN kept, -0 -> +0
+    case EW_SIGMOID: return __ddiv_rn(1.0, __dadd_rn(1.0, exp(-a)));
+    default: return a;
+  }
+}
+__device__ __forceinline__ float ew_apply(int op, float a, float b) {
+  switch (op) {
+    case EW_ADD: return __fadd_rn(a, b);
+    case EW_SUB: return __fsub_rn(a, b);
+    case EW_MUL: return __fmul_rn(a, b);
+    case EW_NEG: return -a;
+    case EW_RELU: return (a > 0.0f || a != a) ? a : 0.0f;
+    case EW_SIGMOID: return __fdiv_rn(1.0f, __fadd_rn(1.0f, expf(-a)));
+    default: return a;
+  }
+}
+
+struct EwParams {
+  DevState* ds;
+  In a, b;
+  int op;
+  int a_scalar, b_scalar;   // broadcast rank-0 operand
+  long long n;
+  Out out;
+};
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_elementwise(EwParams p) {
+  if (skip(p.ds)) return;
+  const T* a = res<T>(p.a);
+  const T* b = (p.op <= EW_MUL) ? res<T>(p.b) : nullptr;
+  T* o = pick_out<T>(p.out, a, b);
+  publish_early(p.out, o);
+  count_op(p.ds);
+  const long long n = p.n;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const T as = p.a_scalar ? a[0] : T(0);
+  const T bs = (b != nullptr && p.b_scalar) ? b[0] : T(0);
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    T x = p.a_scalar ? as : a[i];
+    T y = (b == nullptr) ? T(0) : (p.b_scalar ? bs : b[i]);
+    o[i] = ew_apply(p.op, x, y);
+  }
+  publish_late(p.out, o);
+}
+
+// ------------------------------------------------------------------ reductions
+// SUM / MEAN (tensor.py:239-243, 271-277): sequential row-major sum from +0.0.
+struct ReduceParams {
+  DevState* ds;
+  In a;
+  long long n;
+  int mean;
+  Out out;
+};
+
+// Parity path: one warp streams the data, lane 0 accumulates strictly in order.
+template <typename T>
+__global__ void __launch_bounds__(32) k_reduce_seq(ReduceParams p) {
+  if (skip(p.ds)) return;
+  const T* a = res<T>(p.a);
+  T* o = pick_out<T>(p.out, a, nullptr);
+  publish_early(p.out, o);
+  count_op(p.ds);
+  const int lane = threadIdx.x;
+  double acc = 0.0;
+  for (long long base = 0; base < p.n; base += 32) {
+    long long i = base + lane;
+    double v = (i < p.n) ? (double)a[i] : 0.0;
+    int cnt = (int)min(32ll, p.n - base);
+    for (int j = 0; j < cnt; ++j) {
+      double x = __shfl_sync(0xffffffffu, v, j);
+      acc = __dadd_rn(acc, x);
+    }
+  }
+  if (lane == 0) o[0] = (T)(p.mean ? __ddiv_rn(acc, (double)p.n) : acc);
+  publish_late(p.out, o);
+}
+
+// Tolerance path (fp32 / bf16 contexts): warp-shuffle tree in double, one block.
+template <typename T>
+__global__ void __launch_bounds__(1024) k_reduce_tree(ReduceParams p) {
+  if (skip(p.ds)) return;
+  const T* a = res<T>(p.a);
+  T* o = pick_out<T>(p.out, a, nullptr);
+  publish_early(p.out, o);
+  count_op(p.ds);
+  __shared__ double part[32];
+  double acc = 0.0;
+  for (long long i = threadIdx.x; i < p.n; i += blockDim.x) acc += (double)a[i];
+  for (int s = 16; s > 0; s >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, s);
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double v = (threadIdx.x < (blockDim.x >> 5)) ? part[threadIdx.x] : 0.0;
+    for (int s = 16; s > 0; s >>= 1) v += __shfl_xor_sync(0xffffffffu, v, s);
+    if (threadIdx.x == 0) o[0] = (T)(p.mean ? v / (double)p.n : v);
+  }
+  publish_late(p.out, o);
+}
+
+// ------------------------------------------------------------------ transpose
+// TRANSPOSE (tensor.py:156-161, 278-279): out[o] = in[sum idx_d * in_stride[perm[d]]], materialised.
+struct TransposeParams {
+  DevState* ds;
+  In a;
+  int rank;
+  long long n;
+  long long out_shape[kMaxRank];
+  long long src_stride[kMaxRank];   // input stride of the axis that out-dim d reads
+  Out out;
+};
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_transpose(TransposeParams p) {
+  if (skip(p.ds)) return;
+  const T* a = res<T>(p.a);
+  T* o = pick_out<T>(p.out, a, nullptr);
+  publish_early(p.out, o);
+  count_op(p.ds);
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < p.n; i += stride) {
+    long long rem = i, src = 0;
+    for (int d = p.rank - 1; d >= 0; --d) {
+      long long q = rem / p.out_shape[d];
+      long long r = rem - q * p.out_shape[d];
+      src += r * p.src_stride[d];
+      rem = q;
+    }
+    o[i] = a[src];
+  }
+  publish_late(p.out, o);
+}
+
+// 2-D transpose through a padded shared-memory tile (coalesced on both sides).
+template <typename T>
+__global__ void __launch_bounds__(256) k_transpose2d(TransposeParams p) {
+  if (skip(p.ds)) return;
+  const T* a = res<T>(p.a);
+  T* o = pick_out<T>(p.out, a, nullptr);
+  publish_early(p.out, o);
+  count_op(p.ds);
+  __shared__ T tile[32][33];
+  const long long R = p.out_shape[1], C = p.out_shape[0];   // input is R x C, output C x R
+  const long long tiles_c = (C + 31) / 32;
+  for (long long t = blockIdx.x; t < ((R + 31) / 32) * tiles_c; t += gridDim.x) {
+    long long r0 = (t / tiles_c) * 32, c0 = (t % tiles_c) * 32;
+    for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+      long long r = r0 + k, c = c0 + threadIdx.x;
+      if (r < R && c < C) tile[k][threadIdx.x] = a[r * C + c];
+    }
+    __syncthreads();
+    for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+      long long c = c0 + k, r = r0 + threadIdx.x;
+      if (r < R && c < C) o[c * R + r] = tile[threadIdx.x][k];
+    }
+    __syncthreads();
+  }
+  publish_late(p.out, o);
+}
+
+// ------------------------------------------------------------------ matmul
+// MATMUL (tensor.py:228-236): out[i,j] = (((+0 + a[i,0]*b[0,j]) + a[i,1]*b[1,j]) + ...),
+// every product and every sum rounded separately, k strictly increasing.
+// Parity SIMT kernel: a k-panel of A and B is staged in shared memory; each
+// thread owns RM x RN outputs and walks k in order -> bitwise equal to the
+// reference for any tiling.  ``trans_a``/``trans_b`` read a transposed operand
+// in place (TRANSPOSE folded into the consumer).
+struct MatmulParams {
+  DevState* ds;
+  In a, b;
+  long long M, N, K;
+  int trans_a, trans_b;
+  long long lda, ldb;       // row stride of the stored operand
+  Out out;
+};
+
+template <typename T, int BM, int BN, int BK, int RM, int RN, bool EXACT>
+__global__ void __launch_bounds__((BM / RM) * (BN / RN)) k_matmul_simt(MatmulParams p) {
+  if (skip(p.ds)) return;
+  const T* A = res<T>(p.a);
+  const T* B = res<T>(p.b);
+  T* C = pick_out<T>(p.out, A, B);
+  publish_early(p.out, C);
+  count_op(p.ds);
+  constexpr int TX = BN / RN, TY = BM / RM, NT = TX * TY;
+  __shared__ T sA[BK][BM + 1];
+  __shared__ T sB[BK][BN + 1];
+  const int tx = threadIdx.x % TX, ty = threadIdx.x / TX;
+  const long long tiles_n = (p.N + BN - 1) / BN;
+  const long long tiles = ((p.M + BM - 1) / BM) * tiles_n;
+  for (long long tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+    const long long m0 = (tile / tiles_n) * BM, n0 = (tile % tiles_n) * BN;
+    T acc[RM][RN];
+#pragma unroll
+    for (int i = 0; i < RM; ++i)
+#pragma unroll
+      for (int j = 0; j < RN; ++j) acc[i][j] = T(0);
+    for (long long k0 = 0; k0 < p.K; k0 += BK) {
+      for (int e = threadIdx.x; e < BM * BK; e += NT) {
+        int mm, kk;
+        if (p.trans_a) { mm = e % BM; kk = e / BM; } else { kk = e % BK; mm = e / BK; }
+        long long gm = m0 + mm, gk = k0 + kk;
+        T v = T(0);
+        if (gm < p.M && gk < p.K) v = p.trans_a ? A[gk * p.lda + gm] : A[gm * p.lda + gk];
+        sA[kk][mm] = v;
+      }
+      for (int e = threadIdx.x; e < BK * BN; e += NT) {
+        int kk, nn;
+        if (p.trans_b) { kk = e % BK; nn = e / BK; } else { nn = e % BN; kk = e / BN; }
+        long long gk = k0 + kk, gn = n0 + nn;
+        T v = T(0);
+        if (gk < p.K && gn < p.N) v = p.trans_b ? B[gn * p.ldb + gk] : B[gk * p.ldb + gn];
+        sB[kk][nn] = v;
+      }
+      __syncthreads();
+      const int kmax = (int)min((long long)BK, p.K - k0);
+      for (int kk = 0; kk < kmax; ++kk) {
+        T av[RM], bv[RN];
+#pragma unroll
+        for (int i = 0; i < RM; ++i) av[i] = sA[kk][ty + i * TY];
+#pragma unroll
+        for (int j = 0; j < RN; ++j) bv[j] = sB[kk][tx + j * TX];
+#pragma unroll
+        for (int i = 0; i < RM; ++i)
+#pragma unroll
+          for (int j = 0; j < RN; ++j) {
+            if constexpr (EXACT) {
+              acc[i][j] = ew_apply(EW_ADD, acc[i][j], ew_apply(EW_MUL, av[i], bv[j]));
+            } else {
+              acc[i][j] = fma(av[i], bv[j], acc[i][j]);
+            }
+          }
+      }
+      __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < RM; ++i)
+#pragma unroll
+      for (int j = 0; j < RN; ++j) {
+        long long gm = m0 + ty + i * TY, gn = n0 + tx + j * TX;
+        if (gm < p.M && gn < p.N) C[gm * p.N + gn] = acc[i][j];
+      }
+  }
+  publish_late(p.out, C);
+}
+
+// ------------------------------------------------------------------ fill / copy / pointer ops
+struct FillParams {
+  DevState* ds;
+  double value;
+  long long n;
+  Out out;
+};
+template <typename T>
+__global__ void __launch_bounds__(256) k_fill(FillParams p) {
+  if (skip(p.ds)) return;
+  T* o = (T*)p.out.buf[0];
+  publish_early(p.out, o);
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < p.n; i += stride) o[i] = (T)p.value;
+}
+
+// Convert float64 host payload (mapped) into the context precision.
+template <typename T>
+__global__ void __launch_bounds__(256) k_from_f64(const double* src, T* dst, long long n) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) dst[i] = (T)src[i];
+}
+template <typename T>
+__global__ void __launch_bounds__(256) k_to_f64(const T* src, double* dst, long long n) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) dst[i] = (double)src[i];
+}
+
+// Pointer-only ops (RESHAPE view, READ_VAR, ASSIGN_VAR): no data movement.
+enum PtrOp { PTR_ALIAS = 0, PTR_READ_VAR = 1, PTR_ASSIGN_VAR = 2 };
+struct PtrParams {
+  DevState* ds;
+  int op;
+  In a;
+  void** var_cur;      // committed pointer table entry of the variable
+  void** var_ovl;      // overlay table entry (null = not assigned this pass)
+  int* var_ovl_shape;
+  int shape_id;
+  Out out;
+};
+__global__ void k_ptr(PtrParams p) {
+  if (skip(p.ds)) return;
+  void* v;
+  if (p.op == PTR_READ_VAR) {
+    v = *p.var_ovl;                            // overlay first, then committed
+    if (v == nullptr) v = *p.var_cur;
+  } else {
+    v = (void*)res<char>(p.a);
+    if (p.op == PTR_ASSIGN_VAR) {              // AssignVar writes the overlay
+      *p.var_ovl = v;
+      *p.var_ovl_shape = p.shape_id;
+    }
+  }
+  for (int i = 0; i < p.out.npub; ++i) *p.out.pub[i] = v;
+}
+
+// ------------------------------------------------------------------ synthetic data
+// SyntheticDataset.next (dataset.py:44-51): element e = (e-th xorshift64* draw) * 2 - 1.
+// Each thread owns a run of kSynthRun consecutive elements; it jumps to the
+// run's first state with GF(2) matrices J_j = T^(kSynthRun * 2^j), walks the
+// run, and the block stores through shared memory so global writes coalesce.
+constexpr int kSynthRun = 16;
+constexpr int kSynthThreads = 256;
+constexpr int kJumpBits = 40;
+
+__device__ __forceinline__ unsigned long long xs_next(unsigned long long x) {
+  x ^= x >> 12;
+  x ^= x << 25;
+  x ^= x >> 27;
+  return x;
+}
+__device__ __forceinline__ double xs_unit_pm1(unsigned long long x) {
+  unsigned long long r = (x * 0x2545F4914F6CDD1Dull) >> 11;
+  return __dsub_rn(__dmul_rn(__dmul_rn((double)r, 0x1p-53), 2.0), 1.0);
+}
+__device__ __forceinline__ unsigned long long gf2_apply(const unsigned long long* cols, unsigned long long v) {
+  unsigned long long r = 0;
+#pragma unroll 8
+  for (int b = 0; b < 64; ++b) r ^= cols[b] & (0ull - ((v >> b) & 1ull));
+  return r;
+}
+
+struct SynthParams {
+  DevState* ds;
+  const unsigned long long* jump;   // kJumpBits matrices x 64 columns
+  const unsigned long long* state_ptr;  // graph mode: state from the feed record (null = use state)
+  unsigned long long state;
+  long long n;
+  Out out;
+};
+
+template <typename T>
+__global__ void __launch_bounds__(kSynthThreads) k_synth(SynthParams p) {
+  if (skip(p.ds)) return;
+  T* o = (T*)p.out.buf[0];
+  publish_early(p.out, o);
+  __shared__ T stage[kSynthThreads * kSynthRun];
+  const unsigned long long s0 = p.state_ptr ? *p.state_ptr : p.state;
+  const long long per_block = (long long)kSynthThreads * kSynthRun;
+  for (long long base = (long long)blockIdx.x * per_block; base < p.n; base += (long long)gridDim.x * per_block) {
+    long long run = base / kSynthRun + threadIdx.x;
+    unsigned long long s = s0;
+    for (int j = 0; j < kJumpBits && (run >> j) != 0; ++j)
+      if ((run >> j) & 1) s = gf2_apply(p.jump + 64 * j, s);
+#pragma unroll
+    for (int i = 0; i < kSynthRun; ++i) {
+      s = xs_next(s);
+      stage[threadIdx.x * kSynthRun + i] = (T)xs_unit_pm1(s);
+    }
+    __syncthreads();
+    long long lim = min(per_block, p.n - base);
+    for (long long i = threadIdx.x; i < lim; i += kSynthThreads) o[base + i] = stage[i];
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------------ handshake
+// Device side of ChannelSet over pinned mapped host rings.
+
+// Spin until the next ring entry is published, the pass is cancelled, or (never) forever.
+// Returns false on cancel.  Accumulates spin time as graph stall.
+__device__ __forceinline__ bool wait_seq(DevState* ds, const Mailbox* mb, const volatile unsigned long long* seqp,
+                                         unsigned long long want) {
+  unsigned long long t0 = 0;
+  int polls = 0;
+  while (ld_acquire_sys(seqp) != want) {
+    if (t0 == 0) t0 = globaltimer();
+    if (mb->cancel == ds->pass_id) {
+      ds->cancelled = 1;
+      ds->stall_ns += globaltimer() - t0;
+      return false;
+    }
+    if (++polls > 64) __nanosleep(200);
+  }
+  if (t0 != 0) ds->stall_ns += globaltimer() - t0;
+  return true;
+}
+
+struct DecideParams {
+  DevState* ds;
+  Mailbox* mb;
+  cudaGraphConditionalHandle handle;
+  long long id;        // expected branch node id / loop id
+  int kind;            // 0 = case (SWITCH), 1 = loop (WHILE)
+  int skip_value;      // value that runs no body: ncases for SWITCH, 0 for WHILE
+};
+
+__global__ void k_decide(DecideParams p) {
+  DevState* ds = p.ds;
+  if (ds->cancelled) {
+    cudaGraphSetConditional(p.handle, (unsigned)p.skip_value);
+    return;
+  }
+  long long idx = ds->dec_head;
+  const DecEntry* e = &p.mb->dec[idx % kDecCap];
+  if (!wait_seq(ds, p.mb, &e->seq, seq_of(ds->pass_id, idx))) {
+    cudaGraphSetConditional(p.handle, (unsigned)p.skip_value);
+    return;
+  }
+  if (e->kind != p.kind || e->id != p.id) {      // DecisionMismatch, fatal
+    ds->status = 3;
+    ds->cancelled = 1;
+    cudaGraphSetConditional(p.handle, (unsigned)p.skip_value);
+    return;
+  }
+  int v = e->value;
+  ds->dec_head = idx + 1;
+  p.mb->dec_consumed = idx + 1;
+  cudaGraphSetConditional(p.handle, (unsigned)v);
+}
+
+// Feed: wait for the slot's next entry; scalar / device-pointer feeds complete here,
+// host-payload and synthetic feeds are expanded by the following k_feed_fill.
+struct FeedRecord {
+  int type;
+  unsigned long long state;
+  unsigned long long off;
+  const void* dptr;
+};
+struct FeedWaitParams {
+  DevState* ds;
+  Mailbox* mb;
+  long long slot;
+  long long numel;       // static element count of the specialisation
+  int ndim;
+  long long shape[kMaxRank];
+  FeedRecord* rec;       // device scratch for k_feed_fill
+  void* buf;             // slot buffer
+  void** cell;           // slot cell (re-pointed for device-resident feeds)
+  int is_f64;
+};
+
+__global__ void k_feed_wait(FeedWaitParams p) {
+  DevState* ds = p.ds;
+  if (ds->cancelled) return;
+  long long idx = ds->feed_head;
+  const FeedEntry* e = &p.mb->feed[idx % kFeedCap];
+  if (!wait_seq(ds, p.mb, &e->seq, seq_of(ds->pass_id, idx))) return;
+  bool ok = (e->slot == p.slot) && (e->ndim == p.ndim);
+  for (int d = 0; ok && d < p.ndim; ++d) ok = (e->shape[d] == p.shape[d]);
+  if (!ok) {                      // orchestrator bug or shape miss: cancel (host reports it)
+    ds->status = (e->slot == p.slot) ? 9 : 3;
+    ds->cancelled = 1;
+    return;
+  }
+  ds->feed_head = idx + 1;
+  p.mb->feed_consumed = idx + 1;
+  p.rec->type = e->type;
+  p.rec->state = e->state;
+  p.rec->off = e->off;
+  p.rec->dptr = e->dptr;
+  if (e->type == FEED_SCALAR) {
+    if (p.is_f64) *(double*)p.buf = e->scalar; else *(float*)p.buf = (float)e->scalar;
+    *p.cell = p.buf;
+  } else if (e->type == FEED_DEVICE) {
+    *p.cell = (void*)e->dptr;      // bind by pointer, no copy
+  } else {
+    *p.cell = p.buf;
+  }
+}
+
+struct FeedFillParams {
+  DevState* ds;
+  const FeedRecord* rec;
+  const double* arena;   // mapped host feed payload arena
+  const unsigned long long* jump;
+  long long n;
+  void* buf;
+};
+
+template <typename T>
+__global__ void __launch_bounds__(kSynthThreads) k_feed_fill(FeedFillParams p) {
+  if (skip(p.ds)) return;
+  const int type = p.rec->type;
+  T* o = (T*)p.buf;
+  if (type == FEED_HOST) {
+    const double* src = p.arena + p.rec->off;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < p.n; i += stride) o[i] = (T)src[i];
+  } else if (type == FEED_SYNTH) {
+    __shared__ T stage[kSynthThreads * kSynthRun];
+    const unsigned long long s0 = p.rec->state;
+    const long long per_block = (long long)kSynthThreads * kSynthRun;
+    for (long long base = (long long)blockIdx.x * per_block; base < p.n; base += (long long)gridDim.x * per_block) {
+      long long run = base / kSynthRun + threadIdx.x;
+      unsigned long long s = s0;
+      for (int j = 0; j < kJumpBits && (run >> j) != 0; ++j)
+        if ((run >> j) & 1) s = gf2_apply(p.jump + 64 * j, s);
+#pragma unroll
+      for (int i = 0; i < kSynthRun; ++i) {
+        s = xs_next(s);
+        stage[threadIdx.x * kSynthRun + i] = (T)xs_unit_pm1(s);
+      }
+      __syncthreads();
+      long long lim = min(per_block, p.n - base);
+      for (long long i = threadIdx.x; i < lim; i += kSynthThreads) o[base + i] = stage[i];
+      __syncthreads();
+    }
+  }
+}
+
+// Fetch: copy the node's latest output into the mapped fetch arena, then publish.
+struct FetchParams {
+  DevState* ds;
+  Mailbox* mb;
+  In a;
+  long long node;
+  long long numel;
+  int ndim;
+  long long shape[kMaxRank];
+  char* arena;                 // mapped host fetch payload arena (device view)
+  unsigned long long arena_cap;
+  int elsize;
+};
+
+__global__ void __launch_bounds__(256) k_fetch(FetchParams p) {
+  DevState* ds = p.ds;
+  if (ds->cancelled) return;
+  __shared__ unsigned long long off;
+  __shared__ long long idx;
+  const char* src = res<char>(p.a);
+  const unsigned long long bytes = (unsigned long long)p.numel * p.elsize;
+  if (threadIdx.x == 0) {
+    idx = ds->fetch_head;
+    off = (ds->fetch_bytes + 15ull) & ~15ull;
+    if (off + bytes > p.arena_cap) off = 0;     // ring wrap (host copies payloads out promptly)
+    ds->fetch_bytes = off + bytes;
+    ds->fetch_head = idx + 1;
+  }
+  __syncthreads();
+  // 16-byte vector copy when possible
+  if ((bytes & 15ull) == 0 && (((uintptr_t)src) & 15) == 0) {
+    const uint4* s4 = (const uint4*)src;
+    uint4* d4 = (uint4*)(p.arena + off);
+    for (unsigned long long i = threadIdx.x; i < bytes / 16; i += blockDim.x) d4[i] = s4[i];
+  } else {
+    for (unsigned long long i = threadIdx.x; i < bytes; i += blockDim.x) p.arena[off + i] = src[i];
+  }
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    FetchEntry* e = &p.mb->fetch[idx % kFetchCap];
+    e->node = p.node;
+    e->off = off;
+    e->numel = p.numel;
+    e->ndim = p.ndim;
+    for (int d = 0; d < p.ndim; ++d) e->shape[d] = p.shape[d];
+    __threadfence_system();
+    st_release_sys(&e->seq, seq_of(ds->pass_id, idx));
+  }
+}
+
+// Pass begin / end (+ commit of the overlay into the variable store).
+struct BeginParams {
+  DevState* ds;
+  Mailbox* mb;
+  void** var_ovl;
+  int nvars;
+};
+__global__ void k_pass_begin(BeginParams p) {
+  DevState* ds = p.ds;
+  for (int i = threadIdx.x; i < p.nvars; i += blockDim.x) p.var_ovl[i] = nullptr;
+  if (threadIdx.x == 0) {
+    ds->cancelled = 0;
+    ds->status = 0;
+    ds->pass_id = p.mb->pass_id;
+    ds->dec_head = ds->feed_head = ds->fetch_head = 0;
+    ds->fetch_bytes = 0;
+    ds->stall_ns = 0;
+    ds->ops = 0;
+    ds->t_begin = globaltimer();
+  }
+}
+
+constexpr int kMaxCommit = 64;
+struct CommitParams {
+  DevState* ds;
+  int n;
+  int var_index[kMaxCommit];
+  void** var_cur;             // committed pointer table
+  void** var_ovl;             // overlay table
+  void** var_spare;           // per-pass spare buffers provided by the host
+  long long bytes[kMaxCommit];
+};
+// One block per assigned variable: copy the overlay value into the variable's
+// spare buffer and make it the committed value.
+__global__ void __launch_bounds__(256) k_commit(CommitParams p) {
+  if (p.ds->cancelled) return;
+  const int j = blockIdx.x;
+  if (j >= p.n) return;
+  const int v = p.var_index[j];
+  const char* src = (const char*)p.var_ovl[v];
+  if (src == nullptr) return;
+  char* dst = (char*)p.var_spare[v];
+  const long long bytes = p.bytes[j];
+  if ((bytes & 15) == 0) {
+    const uint4* s4 = (const uint4*)src;
+    uint4* d4 = (uint4*)dst;
+    for (long long i = threadIdx.x; i < bytes / 16; i += blockDim.x) d4[i] = s4[i];
+  } else {
+    for (long long i = threadIdx.x; i < bytes; i += blockDim.x) dst[i] = src[i];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) p.var_cur[v] = dst;
+}
+
+struct EndParams {
+  DevState* ds;
+  Mailbox* mb;
+  void** var_ovl;
+  int* var_ovl_shape;
+  int nvars;
+};
+__global__ void k_pass_end(EndParams p) {
+  DevState* ds = p.ds;
+  if (threadIdx.x != 0) return;
+  unsigned long long mask = 0;
+  if (!ds->cancelled) {
+    for (int i = 0; i < p.nvars && i < 64; ++i)
+      if (p.var_ovl[i] != nullptr) {
+        mask |= 1ull << i;
+        p.mb->var_shape_id[i] = p.var_ovl_shape[i];
+      }
+  }
+  p.mb->dirty_mask = mask;
+  p.mb->committed = ds->cancelled ? 0 : 1;
+  p.mb->status = ds->status;
+  p.mb->exec_ns = globaltimer() - ds->t_begin;
+  p.mb->stall_ns = ds->stall_ns;
+  p.mb->ops = ds->ops;
+  p.mb->fetches = ds->fetch_head;
+  __threadfence_system();
+  st_release_sys(&p.mb->done, ds->pass_id);
+}
+
+}  // namespace coex

@@ -1,0 +1,1344 @@
+// runtime.cu -- host side of libcoexb200.so (C-ABI in include/coex_b200.h).
+//
+// * Context: device, one execution stream, stream-ordered allocator, the
+//   device pass state, and the pinned+mapped mailbox (decision / feed / fetch
+//   rings, cancel word, done word) shared with the device.
+// * Eager side: refcounted device tensors; coex_exec_op launches one kernel
+//   from kernels.cuh (execute_kernel, pkg/src/coex/tensor.py:246-291).
+// * Symbolic side: coex_prog_build turns the host planner's plan (a SymProgram
+//   specialised to one shape signature) into ONE CUDA graph: compute kernels
+//   become kernel nodes, SwitchCase / While become SWITCH / WHILE conditional
+//   nodes driven by k_decide kernels that spin on the mapped decision ring,
+//   InputFeed / OutputFetch become feed / fetch kernels on the mapped rings.
+//   A co-execution step is one cudaGraphLaunch; the host only publishes
+//   decisions and fed values.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <chrono>
+#include <cstdio>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <thread>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/coex_b200.h"
+#include "kernels.cuh"
+
+using namespace coex;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CK(call)                                                                                  \
+  do {                                                                                            \
+    cudaError_t e_ = (call);                                                                      \
+    if (e_ != cudaSuccess)                                                                        \
+      return fail(COEX_CUDA_ERROR, std::string(#call) + ": " + cudaGetErrorString(e_) + " @" +    \
+                                       std::to_string(__LINE__));                                 \
+  } while (0)
+
+constexpr int kMaxVars = 1024;
+constexpr int kNumSMs = 148;
+
+struct Buf {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  int refs = 0;
+};
+
+struct TRec {
+  Buf* buf = nullptr;
+  int ndim = 0;
+  int64_t shape[COEX_MAX_RANK] = {0};
+  int64_t numel = 1;
+};
+
+struct Var {
+  std::string name;
+  TRec t;
+  Buf* spare = nullptr;   // var-owned buffer the next commit writes into
+};
+
+int64_t numel_of(int ndim, const int64_t* shape) {
+  int64_t n = 1;
+  for (int i = 0; i < ndim; ++i) n *= shape[i];
+  return n;
+}
+
+// A kernel launch, usable both eagerly and as a graph kernel node.
+struct Launch {
+  void* fn = nullptr;
+  dim3 grid{1}, block{1};
+  size_t smem = 0;
+  alignas(16) unsigned char params[2048];
+  size_t psize = 0;
+  void* args[1];
+  template <typename P>
+  void set(void* f, dim3 g, dim3 b, const P& p) {
+    static_assert(sizeof(P) <= sizeof(params), "kernel params too large");
+    fn = f;
+    grid = g;
+    block = b;
+    memcpy(params, &p, sizeof(P));
+    psize = sizeof(P);
+  }
+  void** argv() {
+    args[0] = params;
+    return args;
+  }
+};
+
+dim3 grid_for(int64_t n, int threads = 256, int max_per_sm = 8) {
+  int64_t b = (n + threads - 1) / threads;
+  if (b < 1) b = 1;
+  int64_t cap = (int64_t)kNumSMs * max_per_sm;
+  return dim3((unsigned)(b < cap ? b : cap));
+}
+
+}  // namespace
+
+struct coex_ctx {
+  int device = 0;
+  int prec = COEX_F64;
+  size_t esize = 8;
+  cudaStream_t stream = nullptr;
+  std::unordered_map<int64_t, TRec> tensors;
+  int64_t next_id = 1;
+  std::vector<Var> vars;
+  std::unordered_map<std::string, int> var_index;
+  void** d_var_cur = nullptr;
+  void** d_var_ovl = nullptr;
+  int* d_var_ovl_shape = nullptr;
+  void** d_var_spare = nullptr;
+  void** h_var_cur = nullptr;     // pinned mirror
+  void** h_var_spare = nullptr;   // pinned mirror
+  DevState* d_state = nullptr;
+  Mailbox* mb = nullptr;
+  Mailbox* d_mb = nullptr;
+  double* feed_arena = nullptr;
+  double* d_feed_arena = nullptr;
+  size_t feed_cap = 0;            // doubles
+  char* fetch_arena = nullptr;
+  char* d_fetch_arena = nullptr;
+  size_t fetch_cap = 0;           // bytes
+  unsigned long long* d_jump = nullptr;
+  double* h_stage = nullptr;      // pinned staging for put/get
+  size_t stage_cap = 0;
+  double timeout_s = 120.0;
+  int64_t kernel_count = 0;
+  coex_prog* active = nullptr;
+  unsigned long long pass_counter = 0;
+};
+
+namespace {
+
+bool is_f64(const coex_ctx* c) { return c->prec == COEX_F64; }
+
+int alloc_buf(coex_ctx* c, size_t bytes, Buf** out) {
+  Buf* b = new Buf();
+  b->bytes = bytes;
+  b->refs = 1;
+  if (bytes > 0) {
+    cudaError_t e = cudaMallocAsync(&b->ptr, bytes < 16 ? 16 : bytes, c->stream);
+    if (e != cudaSuccess) {
+      delete b;
+      return fail(COEX_CUDA_ERROR, std::string("cudaMallocAsync: ") + cudaGetErrorString(e));
+    }
+  }
+  *out = b;
+  return COEX_OK;
+}
+
+void release(coex_ctx* c, Buf* b) {
+  if (b == nullptr) return;
+  if (--b->refs == 0) {
+    if (b->ptr) cudaFreeAsync(b->ptr, c->stream);
+    delete b;
+  }
+}
+
+int64_t new_handle(coex_ctx* c, const TRec& t) {
+  int64_t id = c->next_id++;
+  c->tensors[id] = t;
+  return id;
+}
+
+int ensure_stage(coex_ctx* c, size_t doubles) {
+  if (doubles <= c->stage_cap) return COEX_OK;
+  if (c->h_stage) {
+    CK(cudaStreamSynchronize(c->stream));
+    cudaFreeHost(c->h_stage);
+  }
+  size_t cap = doubles < 4096 ? 4096 : doubles;
+  CK(cudaHostAlloc((void**)&c->h_stage, cap * sizeof(double), cudaHostAllocDefault));
+  c->stage_cap = cap;
+  return COEX_OK;
+}
+
+// ---- GF(2) jump matrices for the synthetic-data generator ----
+unsigned long long xs_step_host(unsigned long long x) {
+  x ^= x >> 12;
+  x ^= x << 25;
+  x ^= x >> 27;
+  return x;
+}
+void mat_apply(const unsigned long long* cols, unsigned long long v, unsigned long long* r) {
+  unsigned long long acc = 0;
+  for (int b = 0; b < 64; ++b)
+    if ((v >> b) & 1ull) acc ^= cols[b];
+  *r = acc;
+}
+void mat_square(const unsigned long long* in, unsigned long long* out) {
+  for (int b = 0; b < 64; ++b) mat_apply(in, in[b], &out[b]);
+}
+
+// ---- shape inference (tensor.py:131-187) ----
+int infer(int kind, const coex_attrs* at, int nin, const TRec* in, int* ndim, int64_t* shape) {
+  static const int arity[] = {2, 2, 2, 2, 1, 1, 1, 1, 1, 1, 1, 0, 0, 1};
+  if (kind < 0 || kind > COEX_ASSIGN_VAR) return fail(COEX_BAD_ATTRS, "unknown op kind");
+  if (nin != arity[kind]) return fail(COEX_BAD_ATTRS, "wrong number of tensor inputs");
+  switch (kind) {
+    case COEX_ADD: case COEX_SUB: case COEX_MUL: {
+      const TRec &a = in[0], &b = in[1];
+      bool same = a.ndim == b.ndim;
+      for (int i = 0; same && i < a.ndim; ++i) same = a.shape[i] == b.shape[i];
+      const TRec& r = (same || b.ndim == 0) ? a : (a.ndim == 0 ? b : a);
+      if (!(same || a.ndim == 0 || b.ndim == 0)) return fail(COEX_SHAPE_MISMATCH, "elementwise: incompatible shapes");
+      *ndim = r.ndim;
+      memcpy(shape, r.shape, sizeof(int64_t) * r.ndim);
+      return COEX_OK;
+    }
+    case COEX_NEG: case COEX_RELU: case COEX_SIGMOID: case COEX_ASSIGN_VAR:
+      *ndim = in[0].ndim;
+      memcpy(shape, in[0].shape, sizeof(int64_t) * in[0].ndim);
+      return COEX_OK;
+    case COEX_SUM: case COEX_MEAN:
+      if (kind == COEX_MEAN && in[0].numel == 0) return fail(COEX_SHAPE_MISMATCH, "mean of an empty tensor");
+      *ndim = 0;
+      return COEX_OK;
+    case COEX_MATMUL:
+      if (in[0].ndim != 2 || in[1].ndim != 2) return fail(COEX_SHAPE_MISMATCH, "matmul: rank-2 operands required");
+      if (in[0].shape[1] != in[1].shape[0]) return fail(COEX_SHAPE_MISMATCH, "matmul: inner dimensions differ");
+      *ndim = 2;
+      shape[0] = in[0].shape[0];
+      shape[1] = in[1].shape[1];
+      return COEX_OK;
+    case COEX_TRANSPOSE: {
+      if (at == nullptr || at->n != in[0].ndim) return fail(COEX_BAD_ATTRS, "transpose: perm is not a permutation");
+      bool seen[COEX_MAX_RANK] = {false};
+      for (int i = 0; i < at->n; ++i) {
+        int64_t p = at->dims[i];
+        if (p < 0 || p >= at->n || seen[p]) return fail(COEX_BAD_ATTRS, "transpose: perm is not a permutation");
+        seen[p] = true;
+        shape[i] = in[0].shape[p];
+      }
+      *ndim = at->n;
+      return COEX_OK;
+    }
+    case COEX_RESHAPE: {
+      if (at == nullptr || at->n < 0 || at->n > COEX_MAX_RANK) return fail(COEX_BAD_ATTRS, "reshape: bad target shape");
+      if (numel_of(at->n, at->dims) != in[0].numel) return fail(COEX_BAD_ATTRS, "reshape: size mismatch");
+      *ndim = at->n;
+      memcpy(shape, at->dims, sizeof(int64_t) * at->n);
+      return COEX_OK;
+    }
+    case COEX_FILL:
+      if (at == nullptr || at->n < 0 || at->n > COEX_MAX_RANK) return fail(COEX_BAD_ATTRS, "fill: bad shape");
+      for (int i = 0; i < at->n; ++i)
+        if (at->dims[i] < 0) return fail(COEX_BAD_ATTRS, "fill: bad shape");
+      *ndim = at->n;
+      memcpy(shape, at->dims, sizeof(int64_t) * at->n);
+      return COEX_OK;
+    default:
+      return fail(COEX_BAD_ATTRS, "read_var is executed against the variable store");
+  }
+}
+
+// ---- kernel selection, shared by eager launches and graph nodes ----
+struct OpSpec {
+  int kind = 0;
+  In in[2] = {{nullptr, nullptr}, {nullptr, nullptr}};
+  int in_ndim[2] = {0, 0};
+  int64_t in_shape[2][COEX_MAX_RANK] = {{0}};
+  int out_ndim = 0;
+  int64_t out_shape[COEX_MAX_RANK] = {0};
+  int attr_n = 0;
+  int64_t attr_dims[COEX_MAX_RANK] = {0};
+  double value = 0.0;
+  int trans_a = 0, trans_b = 0;
+  Out out{};
+  DevState* ds = nullptr;
+};
+
+template <typename T>
+int build_launch_t(coex_ctx* c, const OpSpec& s, Launch* L) {
+  const int64_t n = numel_of(s.out_ndim, s.out_shape);
+  switch (s.kind) {
+    case COEX_ADD: case COEX_SUB: case COEX_MUL: case COEX_NEG: case COEX_RELU: case COEX_SIGMOID: {
+      EwParams p{};
+      p.ds = s.ds;
+      p.a = s.in[0];
+      p.b = s.in[1];
+      p.op = s.kind == COEX_ADD ? EW_ADD : s.kind == COEX_SUB ? EW_SUB : s.kind == COEX_MUL ? EW_MUL
+           : s.kind == COEX_NEG ? EW_NEG : s.kind == COEX_RELU ? EW_RELU : EW_SIGMOID;
+      int binary = s.kind <= COEX_MUL;
+      p.a_scalar = binary && s.in_ndim[0] == 0 && n != 1;
+      p.b_scalar = binary && s.in_ndim[1] == 0 && n != 1;
+      p.n = n;
+      p.out = s.out;
+      L->set((void*)k_elementwise<T>, grid_for(n), dim3(256), p);
+      return COEX_OK;
+    }
+    case COEX_SUM: case COEX_MEAN: {
+      ReduceParams p{};
+      p.ds = s.ds;
+      p.a = s.in[0];
+      p.n = numel_of(s.in_ndim[0], s.in_shape[0]);
+      p.mean = s.kind == COEX_MEAN;
+      p.out = s.out;
+      if (is_f64(c)) L->set((void*)k_reduce_seq<T>, dim3(1), dim3(32), p);
+      else L->set((void*)k_reduce_tree<T>, dim3(1), dim3(1024), p);
+      return COEX_OK;
+    }
+    case COEX_TRANSPOSE: {
+      TransposeParams p{};
+      p.ds = s.ds;
+      p.a = s.in[0];
+      p.rank = s.out_ndim;
+      p.n = n;
+      int64_t istr[COEX_MAX_RANK];
+      int64_t acc = 1;
+      for (int d = s.in_ndim[0] - 1; d >= 0; --d) {
+        istr[d] = acc;
+        acc *= s.in_shape[0][d];
+      }
+      for (int d = 0; d < s.out_ndim; ++d) {
+        p.out_shape[d] = s.out_shape[d];
+        p.src_stride[d] = istr[s.attr_dims[d]];
+      }
+      p.out = s.out;
+      if (s.out_ndim == 2 && s.attr_dims[0] == 1) {
+        int64_t tiles = ((s.out_shape[1] + 31) / 32) * ((s.out_shape[0] + 31) / 32);
+        L->set((void*)k_transpose2d<T>, dim3((unsigned)(tiles < kNumSMs * 8 ? (tiles < 1 ? 1 : tiles) : kNumSMs * 8)),
+               dim3(32, 8), p);
+      } else {
+        L->set((void*)k_transpose<T>, grid_for(n), dim3(256), p);
+      }
+      return COEX_OK;
+    }
+    case COEX_MATMUL: {
+      MatmulParams p{};
+      p.ds = s.ds;
+      p.a = s.in[0];
+      p.b = s.in[1];
+      p.trans_a = s.trans_a;
+      p.trans_b = s.trans_b;
+      // logical shapes: A [M,K], B [K,N]; stored transposed when trans_*
+      p.M = s.trans_a ? s.in_shape[0][1] : s.in_shape[0][0];
+      p.K = s.trans_a ? s.in_shape[0][0] : s.in_shape[0][1];
+      p.N = s.trans_b ? s.in_shape[1][0] : s.in_shape[1][1];
+      p.lda = s.in_shape[0][1];
+      p.ldb = s.in_shape[1][1];
+      p.out = s.out;
+      const int64_t tiles_big = ((p.M + 63) / 64) * ((p.N + 63) / 64);
+      const bool exact = is_f64(c);
+      if (tiles_big >= kNumSMs) {
+        dim3 g((unsigned)(tiles_big < kNumSMs * 4 ? tiles_big : kNumSMs * 4));
+        if (exact) L->set((void*)k_matmul_simt<T, 64, 64, 16, 4, 4, true>, g, dim3(256), p);
+        else L->set((void*)k_matmul_simt<T, 64, 64, 16, 4, 4, false>, g, dim3(256), p);
+      } else {
+        int64_t tiles = ((p.M + 15) / 16) * ((p.N + 15) / 16);
+        dim3 g((unsigned)(tiles < kNumSMs * 8 ? (tiles < 1 ? 1 : tiles) : kNumSMs * 8));
+        if (exact) L->set((void*)k_matmul_simt<T, 16, 16, 32, 1, 1, true>, g, dim3(256), p);
+        else L->set((void*)k_matmul_simt<T, 16, 16, 32, 1, 1, false>, g, dim3(256), p);
+      }
+      return COEX_OK;
+    }
+    case COEX_FILL: {
+      FillParams p{};
+      p.ds = s.ds;
+      p.value = s.value;
+      p.n = n;
+      p.out = s.out;
+      L->set((void*)k_fill<T>, grid_for(n), dim3(256), p);
+      return COEX_OK;
+    }
+    default:
+      return fail(COEX_BAD_ATTRS, "op kind has no kernel");
+  }
+}
+
+int build_launch(coex_ctx* c, const OpSpec& s, Launch* L) {
+  return is_f64(c) ? build_launch_t<double>(c, s, L) : build_launch_t<float>(c, s, L);
+}
+
+int launch_now(coex_ctx* c, Launch& L) {
+  CK(cudaLaunchKernel(L.fn, L.grid, L.block, L.argv(), L.smem, c->stream));
+  c->kernel_count++;
+  return COEX_OK;
+}
+
+TRec* get_t(coex_ctx* c, int64_t id) {
+  auto it = c->tensors.find(id);
+  return it == c->tensors.end() ? nullptr : &it->second;
+}
+
+int set_var_cur(coex_ctx* c, int idx) {
+  c->h_var_cur[idx] = c->vars[idx].t.buf ? c->vars[idx].t.buf->ptr : nullptr;
+  CK(cudaMemcpyAsync(c->d_var_cur + idx, c->h_var_cur + idx, sizeof(void*), cudaMemcpyHostToDevice, c->stream));
+  return COEX_OK;
+}
+
+}  // namespace
+
+// =============================================================== C-ABI: context
+extern "C" {
+
+const char* coex_last_error(void) { return g_err.c_str(); }
+const char* coex_version(void) { return "coexb200 0.1.0 sm_100a"; }
+
+int coex_ctx_create(int device, int precision, coex_ctx** out) {
+  if (precision < COEX_F64 || precision > COEX_BF16) return fail(COEX_INVALID, "bad precision");
+  CK(cudaSetDevice(device));
+  coex_ctx* c = new coex_ctx();
+  c->device = device;
+  c->prec = precision;
+  c->esize = precision == COEX_F64 ? 8 : 4;
+  CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  cudaMemPool_t pool;
+  CK(cudaDeviceGetDefaultMemPool(&pool, device));
+  uint64_t thresh = ~0ull;
+  CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thresh));
+  CK(cudaMalloc(&c->d_var_cur, kMaxVars * sizeof(void*)));
+  CK(cudaMalloc(&c->d_var_ovl, kMaxVars * sizeof(void*)));
+  CK(cudaMalloc(&c->d_var_ovl_shape, kMaxVars * sizeof(int)));
+  CK(cudaMalloc(&c->d_var_spare, kMaxVars * sizeof(void*)));
+  CK(cudaMemset(c->d_var_cur, 0, kMaxVars * sizeof(void*)));
+  CK(cudaMemset(c->d_var_ovl, 0, kMaxVars * sizeof(void*)));
+  CK(cudaMemset(c->d_var_spare, 0, kMaxVars * sizeof(void*)));
+  CK(cudaHostAlloc((void**)&c->h_var_cur, kMaxVars * sizeof(void*), cudaHostAllocDefault));
+  CK(cudaHostAlloc((void**)&c->h_var_spare, kMaxVars * sizeof(void*), cudaHostAllocDefault));
+  memset(c->h_var_cur, 0, kMaxVars * sizeof(void*));
+  memset(c->h_var_spare, 0, kMaxVars * sizeof(void*));
+  CK(cudaMalloc(&c->d_state, sizeof(DevState)));
+  CK(cudaMemset(c->d_state, 0, sizeof(DevState)));
+  CK(cudaHostAlloc((void**)&c->mb, sizeof(Mailbox), cudaHostAllocMapped));
+  memset((void*)c->mb, 0, sizeof(Mailbox));
+  CK(cudaHostGetDevicePointer((void**)&c->d_mb, c->mb, 0));
+  c->feed_cap = (size_t)32 << 20;   // doubles (256 MiB)
+  CK(cudaHostAlloc((void**)&c->feed_arena, c->feed_cap * sizeof(double), cudaHostAllocMapped));
+  CK(cudaHostGetDevicePointer((void**)&c->d_feed_arena, c->feed_arena, 0));
+  c->fetch_cap = (size_t)64 << 20;  // bytes
+  CK(cudaHostAlloc((void**)&c->fetch_arena, c->fetch_cap, cudaHostAllocMapped));
+  CK(cudaHostGetDevicePointer((void**)&c->d_fetch_arena, c->fetch_arena, 0));
+  // jump matrices J_j = T^(kSynthRun * 2^j)
+  std::vector<unsigned long long> jm(64 * kJumpBits), cur(64), tmp(64);
+  for (int b = 0; b < 64; ++b) cur[b] = xs_step_host(1ull << b);
+  for (int s = 1; s < kSynthRun; s <<= 1) {      // T^16 by repeated squaring
+    mat_square(cur.data(), tmp.data());
+    cur.swap(tmp);
+  }
+  for (int j = 0; j < kJumpBits; ++j) {
+    memcpy(&jm[64 * j], cur.data(), 64 * sizeof(unsigned long long));
+    mat_square(cur.data(), tmp.data());
+    cur.swap(tmp);
+  }
+  CK(cudaMalloc(&c->d_jump, jm.size() * sizeof(unsigned long long)));
+  CK(cudaMemcpy(c->d_jump, jm.data(), jm.size() * sizeof(unsigned long long), cudaMemcpyHostToDevice));
+  *out = c;
+  return COEX_OK;
+}
+
+int coex_ctx_destroy(coex_ctx* c) {
+  if (c == nullptr) return COEX_OK;
+  cudaStreamSynchronize(c->stream);
+  for (auto& kv : c->tensors) release(c, kv.second.buf);
+  for (auto& v : c->vars) {
+    release(c, v.t.buf);
+    release(c, v.spare);
+  }
+  cudaStreamSynchronize(c->stream);
+  cudaFree(c->d_var_cur);
+  cudaFree(c->d_var_ovl);
+  cudaFree(c->d_var_ovl_shape);
+  cudaFree(c->d_var_spare);
+  cudaFreeHost(c->h_var_cur);
+  cudaFreeHost(c->h_var_spare);
+  cudaFree(c->d_state);
+  cudaFreeHost((void*)c->mb);
+  cudaFreeHost(c->feed_arena);
+  cudaFreeHost(c->fetch_arena);
+  cudaFree(c->d_jump);
+  if (c->h_stage) cudaFreeHost(c->h_stage);
+  cudaStreamDestroy(c->stream);
+  delete c;
+  return COEX_OK;
+}
+
+int coex_ctx_sync(coex_ctx* c) {
+  CK(cudaStreamSynchronize(c->stream));
+  return COEX_OK;
+}
+
+int coex_ctx_set_timeout(coex_ctx* c, double seconds) {
+  c->timeout_s = seconds;
+  return COEX_OK;
+}
+
+int64_t coex_ctx_kernel_count(coex_ctx* c) { return c ? c->kernel_count : 0; }
+
+// =============================================================== tensors
+int coex_tensor_put(coex_ctx* c, int ndim, const int64_t* shape, const double* data, int64_t* id) {
+  if (ndim < 0 || ndim > COEX_MAX_RANK) return fail(COEX_INVALID, "rank out of range");
+  TRec t;
+  t.ndim = ndim;
+  for (int i = 0; i < ndim; ++i) t.shape[i] = shape[i];
+  t.numel = numel_of(ndim, shape);
+  int rc = alloc_buf(c, t.numel * c->esize, &t.buf);
+  if (rc) return rc;
+  if (t.numel > 0) {
+    rc = ensure_stage(c, t.numel);
+    if (rc) return rc;
+    CK(cudaStreamSynchronize(c->stream));        // staging buffer reuse
+    memcpy(c->h_stage, data, t.numel * sizeof(double));
+    if (is_f64(c)) {
+      CK(cudaMemcpyAsync(t.buf->ptr, c->h_stage, t.numel * 8, cudaMemcpyHostToDevice, c->stream));
+    } else {
+      double* dtmp;
+      CK(cudaMallocAsync(&dtmp, t.numel * 8, c->stream));
+      CK(cudaMemcpyAsync(dtmp, c->h_stage, t.numel * 8, cudaMemcpyHostToDevice, c->stream));
+      k_from_f64<float><<<grid_for(t.numel), 256, 0, c->stream>>>(dtmp, (float*)t.buf->ptr, t.numel);
+      CK(cudaGetLastError());
+      CK(cudaFreeAsync(dtmp, c->stream));
+    }
+  }
+  *id = new_handle(c, t);
+  return COEX_OK;
+}
+
+int coex_tensor_synth(coex_ctx* c, uint64_t state, int ndim, const int64_t* shape, int64_t* id) {
+  if (ndim < 0 || ndim > COEX_MAX_RANK) return fail(COEX_INVALID, "rank out of range");
+  TRec t;
+  t.ndim = ndim;
+  for (int i = 0; i < ndim; ++i) t.shape[i] = shape[i];
+  t.numel = numel_of(ndim, shape);
+  int rc = alloc_buf(c, t.numel * c->esize, &t.buf);
+  if (rc) return rc;
+  if (t.numel > 0) {
+    SynthParams p{};
+    p.jump = c->d_jump;
+    p.state = state;
+    p.n = t.numel;
+    p.out.buf[0] = t.buf->ptr;
+    const int64_t per_block = (int64_t)kSynthThreads * kSynthRun;
+    int64_t blocks = (t.numel + per_block - 1) / per_block;
+    dim3 g((unsigned)(blocks < kNumSMs * 4 ? blocks : kNumSMs * 4));
+    Launch L;
+    if (is_f64(c)) L.set((void*)k_synth<double>, g, dim3(kSynthThreads), p);
+    else L.set((void*)k_synth<float>, g, dim3(kSynthThreads), p);
+    rc = launch_now(c, L);
+    if (rc) return rc;
+  }
+  *id = new_handle(c, t);
+  return COEX_OK;
+}
+
+int coex_tensor_info(coex_ctx* c, int64_t id, int* ndim, int64_t* shape) {
+  TRec* t = get_t(c, id);
+  if (!t) return fail(COEX_INVALID, "unknown tensor id");
+  *ndim = t->ndim;
+  for (int i = 0; i < t->ndim; ++i) shape[i] = t->shape[i];
+  return COEX_OK;
+}
+
+static int read_buf(coex_ctx* c, const void* dptr, int64_t numel, double* out) {
+  if (numel == 0) return COEX_OK;
+  int rc = ensure_stage(c, numel);
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(c->h_stage, dptr, numel * c->esize, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  if (is_f64(c)) {
+    memcpy(out, c->h_stage, numel * 8);
+  } else {
+    const float* f = (const float*)c->h_stage;
+    for (int64_t i = 0; i < numel; ++i) out[i] = (double)f[i];
+  }
+  return COEX_OK;
+}
+
+int coex_tensor_get(coex_ctx* c, int64_t id, double* out, int64_t cap, int* ndim, int64_t* shape) {
+  TRec* t = get_t(c, id);
+  if (!t) return fail(COEX_INVALID, "unknown tensor id");
+  if (cap < t->numel) return fail(COEX_INVALID, "output buffer too small");
+  *ndim = t->ndim;
+  for (int i = 0; i < t->ndim; ++i) shape[i] = t->shape[i];
+  return read_buf(c, t->buf ? t->buf->ptr : nullptr, t->numel, out);
+}
+
+int coex_tensor_free(coex_ctx* c, int64_t id) {
+  auto it = c->tensors.find(id);
+  if (it == c->tensors.end()) return fail(COEX_INVALID, "unknown tensor id");
+  release(c, it->second.buf);
+  c->tensors.erase(it);
+  return COEX_OK;
+}
+
+int coex_exec_op(coex_ctx* c, int kind, const coex_attrs* attrs, int nin, const int64_t* in_ids,
+                 int64_t* out_id) {
+  if (c->active) return fail(COEX_IN_FLIGHT_PASS, "eager op while a pass is in flight");
+  TRec in[2];
+  for (int i = 0; i < nin && i < 2; ++i) {
+    TRec* t = get_t(c, in_ids[i]);
+    if (!t) return fail(COEX_INVALID, "unknown input tensor id");
+    in[i] = *t;
+  }
+  TRec o;
+  int rc = infer(kind, attrs, nin, in, &o.ndim, o.shape);
+  if (rc) return rc;
+  o.numel = numel_of(o.ndim, o.shape);
+  if (kind == COEX_RESHAPE || kind == COEX_ASSIGN_VAR) {       // views: share the buffer
+    o.buf = in[0].buf;
+    o.buf->refs++;
+    *out_id = new_handle(c, o);
+    return COEX_OK;
+  }
+  rc = alloc_buf(c, o.numel * c->esize, &o.buf);
+  if (rc) return rc;
+  OpSpec s;
+  s.kind = kind;
+  for (int i = 0; i < nin; ++i) {
+    s.in[i].direct = in[i].buf->ptr;
+    s.in_ndim[i] = in[i].ndim;
+    memcpy(s.in_shape[i], in[i].shape, sizeof(int64_t) * in[i].ndim);
+  }
+  s.out_ndim = o.ndim;
+  memcpy(s.out_shape, o.shape, sizeof(int64_t) * o.ndim);
+  if (attrs) {
+    s.attr_n = attrs->n;
+    memcpy(s.attr_dims, attrs->dims, sizeof(int64_t) * COEX_MAX_RANK);
+    s.value = attrs->value;
+  }
+  s.out.buf[0] = o.buf->ptr;
+  if (o.numel > 0 || kind == COEX_SUM || kind == COEX_MEAN) {
+    Launch L;
+    rc = build_launch(c, s, &L);
+    if (rc == COEX_OK) rc = launch_now(c, L);
+    if (rc) {
+      release(c, o.buf);
+      return rc;
+    }
+  }
+  *out_id = new_handle(c, o);
+  return COEX_OK;
+}
+
+// =============================================================== variables
+int coex_var_define(coex_ctx* c, const char* name, int64_t tid, int* var_index) {
+  TRec* t = get_t(c, tid);
+  if (!t) return fail(COEX_INVALID, "unknown tensor id");
+  auto it = c->var_index.find(name);
+  int idx;
+  if (it == c->var_index.end()) {
+    if ((int)c->vars.size() >= kMaxVars) return fail(COEX_INVALID, "too many variables");
+    idx = (int)c->vars.size();
+    c->vars.push_back(Var());
+    c->vars[idx].name = name;
+    c->var_index[name] = idx;
+  } else {
+    idx = it->second;
+    release(c, c->vars[idx].t.buf);
+  }
+  c->vars[idx].t = *t;
+  c->vars[idx].t.buf->refs++;
+  *var_index = idx;
+  return set_var_cur(c, idx);
+}
+
+int coex_var_read(coex_ctx* c, int idx, int64_t* tid) {
+  if (idx < 0 || idx >= (int)c->vars.size()) return fail(COEX_BAD_ATTRS, "unknown variable");
+  if (c->active) return fail(COEX_IN_FLIGHT_PASS, "variable read during a pass");
+  TRec t = c->vars[idx].t;
+  t.buf->refs++;
+  *tid = new_handle(c, t);
+  return COEX_OK;
+}
+
+int coex_var_assign(coex_ctx* c, int idx, int64_t tid) {
+  if (idx < 0 || idx >= (int)c->vars.size()) return fail(COEX_BAD_ATTRS, "unknown variable");
+  if (c->active) return fail(COEX_IN_FLIGHT_PASS, "variable assign during a pass");
+  TRec* t = get_t(c, tid);
+  if (!t) return fail(COEX_INVALID, "unknown tensor id");
+  Buf* old = c->vars[idx].t.buf;
+  c->vars[idx].t = *t;
+  c->vars[idx].t.buf->refs++;
+  release(c, old);
+  return set_var_cur(c, idx);
+}
+
+int coex_var_info(coex_ctx* c, int idx, int* ndim, int64_t* shape) {
+  if (idx < 0 || idx >= (int)c->vars.size()) return fail(COEX_BAD_ATTRS, "unknown variable");
+  *ndim = c->vars[idx].t.ndim;
+  for (int i = 0; i < *ndim; ++i) shape[i] = c->vars[idx].t.shape[i];
+  return COEX_OK;
+}
+
+int coex_var_rollback(coex_ctx* c) {
+  if (c->active) return fail(COEX_IN_FLIGHT_PASS, "rollback during a pass");
+  return COEX_OK;   // the overlay lives only inside a pass; a cancelled pass never commits
+}
+
+}  // extern "C"
+
+// =============================================================== symbolic programs
+namespace {
+
+enum PlanTag : int64_t { T_SEQ = 1, T_OP = 2, T_PTR = 3, T_FEED = 4, T_FETCH = 5, T_SWITCH = 6, T_WHILE = 7 };
+constexpr int64_t kPlanMagic = 0xC0E8B200;
+constexpr int64_t kPlanVersion = 1;
+
+struct FeedSlot {
+  int64_t slot;
+  void* buf;
+  void** cell;
+  FeedRecord* rec;
+};
+
+}  // namespace
+
+struct coex_prog {
+  coex_ctx* ctx = nullptr;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  char* arena = nullptr;              // node / slot buffers
+  size_t arena_bytes = 0;
+  void** cells = nullptr;             // device pointer cells
+  int64_t ncells = 0;
+  FeedRecord* recs = nullptr;
+  unsigned int* late = nullptr;       // late-publication counters
+  int64_t n_kernel_nodes = 0, n_cond_nodes = 0, n_compute = 0;
+  std::vector<int> commit_vars;
+  std::vector<int64_t> commit_bytes;
+  std::unordered_map<int, std::vector<int64_t>> var_shapes;   // shape id -> dims
+  // pass state (host side)
+  bool running = false;
+  unsigned long long pass_id = 0;
+  int64_t dec_n = 0, feed_n = 0;
+  size_t feed_off = 0;
+  int64_t fetch_read = 0;
+  std::unordered_map<int64_t, int64_t> fetch_count;             // node -> entries seen
+  std::unordered_map<int64_t, std::vector<int64_t>> fetch_idx;  // node -> ring indices
+  std::vector<std::vector<double>> fetch_copy;                  // payload snapshots
+};
+
+namespace {
+
+struct Builder {
+  coex_ctx* c;
+  coex_prog* p;
+  const int64_t* w;
+  int64_t n;
+  int64_t pos = 0;
+  std::vector<char*> bufs;
+  int64_t n_late = 0;
+  std::string err;
+
+  int64_t next() {
+    if (pos >= n) throw std::runtime_error("plan truncated");
+    return w[pos++];
+  }
+  void** cell(int64_t i) {
+    if (i < 0 || i >= p->ncells) throw std::runtime_error("bad cell index");
+    return p->cells + i;
+  }
+  char* buf(int64_t i) {
+    if (i < 0) return nullptr;
+    if (i >= (int64_t)bufs.size()) throw std::runtime_error("bad buffer index");
+    return bufs[i];
+  }
+
+  int add_kernel(cudaGraph_t g, cudaGraphNode_t* prev, Launch& L) {
+    cudaKernelNodeParams kp = {};
+    kp.func = L.fn;
+    kp.gridDim = L.grid;
+    kp.blockDim = L.block;
+    kp.sharedMemBytes = (unsigned)L.smem;
+    kp.kernelParams = L.argv();
+    cudaGraphNode_t node;
+    CK(cudaGraphAddKernelNode(&node, g, *prev ? prev : nullptr, *prev ? 1 : 0, &kp));
+    *prev = node;
+    p->n_kernel_nodes++;
+    return COEX_OK;
+  }
+
+  void read_out(Out& o) {
+    int64_t b0 = next(), b1 = next();
+    o.buf[0] = buf(b0);
+    o.buf[1] = buf(b1);
+    o.pingpong = (int)next();
+    int64_t late = next();
+    int64_t np = next();
+    if (np > kMaxPub) throw std::runtime_error("too many publish cells");
+    o.npub = (int)np;
+    for (int i = 0; i < kMaxPub; ++i) {
+      int64_t ci = next();
+      o.pub[i] = (i < np) ? cell(ci) : nullptr;
+    }
+    o.late = late ? p->late + (n_late++) : nullptr;
+  }
+
+  int seq(cudaGraph_t g, cudaGraphNode_t* prev) {
+    if (next() != T_SEQ) throw std::runtime_error("expected SEQ");
+    int64_t items = next();
+    for (int64_t i = 0; i < items; ++i) {
+      int rc = item(g, prev);
+      if (rc) return rc;
+    }
+    return COEX_OK;
+  }
+
+  int item(cudaGraph_t g, cudaGraphNode_t* prev) {
+    int64_t tag = next();
+    switch (tag) {
+      case T_OP: {
+        OpSpec s;
+        s.ds = c->d_state;
+        s.kind = (int)next();
+        next();  // node id (diagnostics)
+        for (int i = 0; i < 2; ++i) {
+          int64_t ci = next();
+          s.in[i].cell = ci >= 0 ? cell(ci) : nullptr;
+          s.in[i].direct = nullptr;
+        }
+        for (int i = 0; i < 2; ++i) {
+          s.in_ndim[i] = (int)next();
+          for (int d = 0; d < COEX_MAX_RANK; ++d) s.in_shape[i][d] = next();
+        }
+        s.out_ndim = (int)next();
+        for (int d = 0; d < COEX_MAX_RANK; ++d) s.out_shape[d] = next();
+        s.attr_n = (int)next();
+        for (int d = 0; d < COEX_MAX_RANK; ++d) s.attr_dims[d] = next();
+        int64_t vbits = next();
+        memcpy(&s.value, &vbits, 8);
+        s.trans_a = (int)next();
+        s.trans_b = (int)next();
+        read_out(s.out);
+        Launch L;
+        int rc = build_launch(c, s, &L);
+        if (rc) return rc;
+        p->n_compute++;
+        return add_kernel(g, prev, L);
+      }
+      case T_PTR: {
+        PtrParams q{};
+        q.ds = c->d_state;
+        q.op = (int)next();
+        next();  // node id
+        int64_t ci = next();
+        q.a.cell = ci >= 0 ? cell(ci) : nullptr;
+        int64_t vi = next();
+        q.shape_id = (int)next();
+        if (vi >= 0) {
+          q.var_cur = c->d_var_cur + vi;
+          q.var_ovl = c->d_var_ovl + vi;
+          q.var_ovl_shape = c->d_var_ovl_shape + vi;
+        }
+        read_out(q.out);
+        Launch L;
+        L.set((void*)k_ptr, dim3(1), dim3(1), q);
+        return add_kernel(g, prev, L);
+      }
+      case T_FEED: {
+        FeedWaitParams q{};
+        q.ds = c->d_state;
+        q.mb = c->d_mb;
+        q.slot = next();
+        q.numel = next();
+        q.ndim = (int)next();
+        for (int d = 0; d < COEX_MAX_RANK; ++d) q.shape[d] = next();
+        q.buf = buf(next());
+        q.cell = cell(next());
+        q.rec = p->recs + (int64_t)next();
+        q.is_f64 = is_f64(c);
+        Launch L;
+        L.set((void*)k_feed_wait, dim3(1), dim3(1), q);
+        int rc = add_kernel(g, prev, L);
+        if (rc) return rc;
+        if (q.numel > 1 || q.ndim > 0) {
+          FeedFillParams f{};
+          f.ds = c->d_state;
+          f.rec = q.rec;
+          f.arena = c->d_feed_arena;
+          f.jump = c->d_jump;
+          f.n = q.numel;
+          f.buf = q.buf;
+          const int64_t per_block = (int64_t)kSynthThreads * kSynthRun;
+          int64_t blocks = (q.numel + per_block - 1) / per_block;
+          if (blocks < 1) blocks = 1;
+          dim3 gd((unsigned)(blocks < kNumSMs * 4 ? blocks : kNumSMs * 4));
+          Launch F;
+          if (is_f64(c)) F.set((void*)k_feed_fill<double>, gd, dim3(kSynthThreads), f);
+          else F.set((void*)k_feed_fill<float>, gd, dim3(kSynthThreads), f);
+          rc = add_kernel(g, prev, F);
+        }
+        return rc;
+      }
+      case T_FETCH: {
+        FetchParams q{};
+        q.ds = c->d_state;
+        q.mb = c->d_mb;
+        q.node = next();
+        q.a.cell = cell(next());
+        q.numel = next();
+        q.ndim = (int)next();
+        for (int d = 0; d < COEX_MAX_RANK; ++d) q.shape[d] = next();
+        q.arena = c->d_fetch_arena;
+        q.arena_cap = c->fetch_cap;
+        q.elsize = (int)c->esize;
+        Launch L;
+        L.set((void*)k_fetch, dim3(1), dim3(256), q);
+        return add_kernel(g, prev, L);
+      }
+      case T_SWITCH: {
+        int64_t branch = next();
+        int64_t ncases = next();
+        cudaGraphConditionalHandle h;
+        CK(cudaGraphConditionalHandleCreate(&h, g, 0, 0));
+        DecideParams d{};
+        d.ds = c->d_state;
+        d.mb = c->d_mb;
+        d.handle = h;
+        d.id = branch;
+        d.kind = 0;
+        d.skip_value = (int)ncases;
+        Launch L;
+        L.set((void*)k_decide, dim3(1), dim3(1), d);
+        int rc = add_kernel(g, prev, L);
+        if (rc) return rc;
+        cudaGraphNodeParams cp = {};
+        cp.type = cudaGraphNodeTypeConditional;
+        cp.conditional.handle = h;
+        cp.conditional.type = cudaGraphCondTypeSwitch;
+        cp.conditional.size = (unsigned)ncases;
+        cudaGraphNode_t node;
+        CK(cudaGraphAddNode(&node, g, prev, 1, &cp));
+        p->n_cond_nodes++;
+        for (int64_t k = 0; k < ncases; ++k) {
+          cudaGraphNode_t bprev = nullptr;
+          rc = seq(cp.conditional.phGraph_out[k], &bprev);
+          if (rc) return rc;
+        }
+        *prev = node;
+        return COEX_OK;
+      }
+      case T_WHILE: {
+        int64_t loop = next();
+        cudaGraphConditionalHandle h;
+        CK(cudaGraphConditionalHandleCreate(&h, g, 0, 0));
+        DecideParams d{};
+        d.ds = c->d_state;
+        d.mb = c->d_mb;
+        d.handle = h;
+        d.id = loop;
+        d.kind = 1;
+        d.skip_value = 0;
+        Launch L;
+        L.set((void*)k_decide, dim3(1), dim3(1), d);
+        int rc = add_kernel(g, prev, L);
+        if (rc) return rc;
+        cudaGraphNodeParams cp = {};
+        cp.type = cudaGraphNodeTypeConditional;
+        cp.conditional.handle = h;
+        cp.conditional.type = cudaGraphCondTypeWhile;
+        cp.conditional.size = 1;
+        cudaGraphNode_t node;
+        CK(cudaGraphAddNode(&node, g, prev, 1, &cp));
+        p->n_cond_nodes++;
+        cudaGraph_t body = cp.conditional.phGraph_out[0];
+        cudaGraphNode_t bprev = nullptr;
+        rc = seq(body, &bprev);
+        if (rc) return rc;
+        Launch L2;    // Loop-Cond at the end of the body: next LoopDecision
+        L2.set((void*)k_decide, dim3(1), dim3(1), d);
+        rc = add_kernel(body, &bprev, L2);
+        if (rc) return rc;
+        *prev = node;
+        return COEX_OK;
+      }
+      default:
+        throw std::runtime_error("unknown plan tag " + std::to_string(tag));
+    }
+  }
+};
+
+}  // namespace
+
+extern "C" {
+
+int coex_prog_build(coex_ctx* c, const int64_t* plan, int64_t nwords, const double* consts, int64_t nconsts,
+                    coex_prog** out) {
+  if (c->active) return fail(COEX_IN_FLIGHT_PASS, "prog_build during a pass");
+  coex_prog* p = new coex_prog();
+  p->ctx = c;
+  Builder b{c, p, plan, nwords};
+  try {
+    if (b.next() != kPlanMagic || b.next() != kPlanVersion) throw std::runtime_error("bad plan header");
+    const int64_t nbufs = b.next();
+    std::vector<int64_t> sizes(nbufs);
+    size_t total = 0;
+    for (int64_t i = 0; i < nbufs; ++i) {
+      sizes[i] = b.next();
+      total += ((size_t)sizes[i] + 255) & ~(size_t)255;
+    }
+    p->arena_bytes = total;
+    if (total) CK(cudaMalloc(&p->arena, total));
+    size_t off = 0;
+    for (int64_t i = 0; i < nbufs; ++i) {
+      b.bufs.push_back(p->arena + off);
+      off += ((size_t)sizes[i] + 255) & ~(size_t)255;
+    }
+    p->ncells = b.next();
+    std::vector<void*> init(p->ncells > 0 ? p->ncells : 1, nullptr);
+    for (int64_t i = 0; i < p->ncells; ++i) init[i] = b.buf(b.next());
+    CK(cudaMalloc(&p->cells, sizeof(void*) * (p->ncells > 0 ? p->ncells : 1)));
+    CK(cudaMemcpy(p->cells, init.data(), sizeof(void*) * p->ncells, cudaMemcpyHostToDevice));
+    const int64_t nrecs = b.next();
+    CK(cudaMalloc(&p->recs, sizeof(FeedRecord) * (nrecs > 0 ? nrecs : 1)));
+    const int64_t nlate = b.next();
+    CK(cudaMalloc(&p->late, sizeof(unsigned int) * (nlate > 0 ? nlate : 1)));
+    CK(cudaMemset(p->late, 0, sizeof(unsigned int) * (nlate > 0 ? nlate : 1)));
+    // constant buffers (FILL nodes are evaluated once here)
+    const int64_t nfill = b.next();
+    for (int64_t i = 0; i < nfill; ++i) {
+      int64_t bi = b.next(), cnt = b.next(), ci = b.next();
+      if (ci < 0 || ci >= nconsts) throw std::runtime_error("bad const index");
+      OpSpec s;
+      s.kind = COEX_FILL;
+      s.out_ndim = 1;
+      s.out_shape[0] = cnt;
+      s.value = consts[ci];
+      s.out.buf[0] = b.buf(bi);
+      if (cnt > 0) {
+        Launch L;
+        int rc = build_launch(c, s, &L);
+        if (rc == COEX_OK) rc = launch_now(c, L);
+        if (rc) throw std::runtime_error(g_err);
+      }
+    }
+    // variables committed by this program
+    const int64_t ncommit = b.next();
+    if (ncommit > kMaxCommit) throw std::runtime_error("too many assigned variables");
+    for (int64_t i = 0; i < ncommit; ++i) {
+      p->commit_vars.push_back((int)b.next());
+      p->commit_bytes.push_back(b.next());
+    }
+    const int64_t nshapes = b.next();
+    for (int64_t i = 0; i < nshapes; ++i) {
+      int sid = (int)b.next();
+      int64_t nd = b.next();
+      std::vector<int64_t> dims;
+      for (int64_t d = 0; d < nd; ++d) dims.push_back(b.next());
+      p->var_shapes[sid] = dims;
+    }
+    CK(cudaGraphCreate(&p->graph, 0));
+    cudaGraphNode_t prev = nullptr;
+    {
+      BeginParams bp{c->d_state, c->d_mb, c->d_var_ovl, (int)c->vars.size() > 0 ? (int)kMaxVars : 0};
+      bp.nvars = kMaxVars;
+      Launch L;
+      L.set((void*)k_pass_begin, dim3(1), dim3(256), bp);
+      int rc = b.add_kernel(p->graph, &prev, L);
+      if (rc) throw std::runtime_error(g_err);
+    }
+    int rc = b.seq(p->graph, &prev);
+    if (rc) throw std::runtime_error(g_err);
+    if (!p->commit_vars.empty()) {
+      CommitParams cp{};
+      cp.ds = c->d_state;
+      cp.n = (int)p->commit_vars.size();
+      for (int i = 0; i < cp.n; ++i) {
+        cp.var_index[i] = p->commit_vars[i];
+        cp.bytes[i] = p->commit_bytes[i];
+      }
+      cp.var_cur = c->d_var_cur;
+      cp.var_ovl = c->d_var_ovl;
+      cp.var_spare = c->d_var_spare;
+      Launch L;
+      L.set((void*)k_commit, dim3(cp.n), dim3(256), cp);
+      rc = b.add_kernel(p->graph, &prev, L);
+      if (rc) throw std::runtime_error(g_err);
+    }
+    {
+      EndParams ep{c->d_state, c->d_mb, c->d_var_ovl, c->d_var_ovl_shape, (int)kMaxVars};
+      Launch L;
+      L.set((void*)k_pass_end, dim3(1), dim3(32), ep);
+      rc = b.add_kernel(p->graph, &prev, L);
+      if (rc) throw std::runtime_error(g_err);
+    }
+    if (b.pos != nwords) throw std::runtime_error("trailing plan words");
+    cudaError_t e = cudaGraphInstantiate(&p->exec, p->graph, 0);
+    if (e != cudaSuccess) throw std::runtime_error(std::string("cudaGraphInstantiate: ") + cudaGetErrorString(e));
+    e = cudaStreamSynchronize(c->stream);
+    if (e != cudaSuccess) throw std::runtime_error(std::string("build sync: ") + cudaGetErrorString(e));
+  } catch (const std::exception& ex) {
+    coex_prog_destroy(p);
+    return fail(COEX_INVALID, std::string("coex_prog_build: ") + ex.what() + (g_err.empty() ? "" : " / " + g_err));
+  }
+  *out = p;
+  return COEX_OK;
+}
+
+int coex_prog_destroy(coex_prog* p) {
+  if (p == nullptr) return COEX_OK;
+  coex_ctx* c = p->ctx;
+  if (c && c->active == p) return fail(COEX_IN_FLIGHT_PASS, "destroying a running program");
+  if (c) cudaStreamSynchronize(c->stream);
+  if (p->exec) cudaGraphExecDestroy(p->exec);
+  if (p->graph) cudaGraphDestroy(p->graph);
+  if (p->arena) cudaFree(p->arena);
+  if (p->cells) cudaFree(p->cells);
+  if (p->recs) cudaFree(p->recs);
+  if (p->late) cudaFree(p->late);
+  delete p;
+  return COEX_OK;
+}
+
+int coex_prog_info(coex_prog* p, int64_t* nk, int64_t* nc, int64_t* ab) {
+  *nk = p->n_kernel_nodes;
+  *nc = p->n_cond_nodes;
+  *ab = (int64_t)p->arena_bytes;
+  return COEX_OK;
+}
+
+// =============================================================== passes
+static double now_s() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+int coex_pass_begin(coex_prog* p) {
+  coex_ctx* c = p->ctx;
+  if (c->active) return fail(COEX_IN_FLIGHT_PASS, "a pass is already in flight");
+  // spare buffers for the variables this program may commit
+  for (size_t i = 0; i < p->commit_vars.size(); ++i) {
+    Var& v = c->vars[p->commit_vars[i]];
+    size_t need = (size_t)p->commit_bytes[i];
+    if (v.spare && (v.spare->refs != 1 || v.spare->bytes < need)) {
+      release(c, v.spare);
+      v.spare = nullptr;
+    }
+    if (!v.spare) {
+      int rc = alloc_buf(c, need, &v.spare);
+      if (rc) return rc;
+    }
+    c->h_var_spare[p->commit_vars[i]] = v.spare->ptr;
+  }
+  if (!p->commit_vars.empty())
+    CK(cudaMemcpyAsync(c->d_var_spare, c->h_var_spare, sizeof(void*) * c->vars.size(), cudaMemcpyHostToDevice,
+                       c->stream));
+  p->pass_id = ++c->pass_counter;
+  p->dec_n = p->feed_n = 0;
+  p->feed_off = 0;
+  p->fetch_read = 0;
+  p->fetch_count.clear();
+  p->fetch_idx.clear();
+  p->fetch_copy.clear();
+  c->mb->done = 0;
+  c->mb->dec_consumed = 0;
+  c->mb->feed_consumed = 0;
+  c->mb->pass_id = p->pass_id;
+  std::atomic_thread_fence(std::memory_order_seq_cst);
+  CK(cudaGraphLaunch(p->exec, c->stream));
+  c->kernel_count += p->n_compute;
+  c->active = p;
+  p->running = true;
+  return COEX_OK;
+}
+
+static int device_failed(coex_prog* p) {
+  coex_ctx* c = p->ctx;
+  if (c->mb->done == p->pass_id && c->mb->status != 0) return c->mb->status;
+  return 0;
+}
+
+static int publish_wait(coex_prog* p, volatile long long* consumed, int64_t next_idx, int cap) {
+  coex_ctx* c = p->ctx;
+  double t0 = 0;
+  while (next_idx - *consumed >= cap) {
+    if (t0 == 0) t0 = now_s();
+    if (c->mb->done == p->pass_id) return fail(COEX_CHANNEL_CLOSED, "pass ended while the host was publishing");
+    if (now_s() - t0 > c->timeout_s) return fail(COEX_CHANNEL_CLOSED, "ring full: device not consuming");
+  }
+  return COEX_OK;
+}
+
+static int push_decision(coex_prog* p, int kind, int64_t id, int value) {
+  coex_ctx* c = p->ctx;
+  if (c->active != p) return fail(COEX_CHANNEL_CLOSED, "no pass in flight");
+  int rc = publish_wait(p, &c->mb->dec_consumed, p->dec_n, kDecCap);
+  if (rc) return rc;
+  DecEntry* e = &c->mb->dec[p->dec_n % kDecCap];
+  e->id = id;
+  e->kind = kind;
+  e->value = value;
+  std::atomic_thread_fence(std::memory_order_release);
+  e->seq = seq_of(p->pass_id, p->dec_n);
+  p->dec_n++;
+  return COEX_OK;
+}
+
+int coex_pass_case(coex_prog* p, int64_t branch_id, int32_t case_index) {
+  return push_decision(p, 0, branch_id, case_index);
+}
+int coex_pass_loop(coex_prog* p, int64_t loop_id, int32_t cont) { return push_decision(p, 1, loop_id, cont ? 1 : 0); }
+
+static int push_feed(coex_prog* p, int64_t slot, int type, int ndim, const int64_t* shape, const double* data,
+                     uint64_t state, const void* dptr) {
+  coex_ctx* c = p->ctx;
+  if (c->active != p) return fail(COEX_CHANNEL_CLOSED, "no pass in flight");
+  if (ndim < 0 || ndim > COEX_MAX_RANK) return fail(COEX_INVALID, "rank out of range");
+  int rc = publish_wait(p, &c->mb->feed_consumed, p->feed_n, kFeedCap);
+  if (rc) return rc;
+  FeedEntry* e = &c->mb->feed[p->feed_n % kFeedCap];
+  const int64_t n = numel_of(ndim, shape);
+  e->slot = slot;
+  e->ndim = ndim;
+  for (int d = 0; d < ndim; ++d) e->shape[d] = shape[d];
+  e->type = type;
+  e->state = state;
+  e->dptr = dptr;
+  if (type == FEED_HOST && n == 1 && ndim == 0) {
+    e->type = FEED_SCALAR;
+    e->scalar = data[0];
+  } else if (type == FEED_HOST) {
+    if (p->feed_off + (size_t)n > c->feed_cap) return fail(COEX_CHANNEL_CLOSED, "feed arena exhausted this pass");
+    memcpy(c->feed_arena + p->feed_off, data, n * sizeof(double));
+    e->off = p->feed_off;
+    p->feed_off += ((size_t)n + 1) & ~(size_t)1;
+  }
+  std::atomic_thread_fence(std::memory_order_release);
+  e->seq = seq_of(p->pass_id, p->feed_n);
+  p->feed_n++;
+  return COEX_OK;
+}
+
+int coex_pass_feed(coex_prog* p, int64_t slot, int ndim, const int64_t* shape, const double* data) {
+  return push_feed(p, slot, FEED_HOST, ndim, shape, data, 0, nullptr);
+}
+int coex_pass_feed_synth(coex_prog* p, int64_t slot, uint64_t state, int ndim, const int64_t* shape) {
+  return push_feed(p, slot, FEED_SYNTH, ndim, shape, nullptr, state, nullptr);
+}
+int coex_pass_feed_tensor(coex_prog* p, int64_t slot, int64_t tid) {
+  TRec* t = get_t(p->ctx, tid);
+  if (!t) return fail(COEX_INVALID, "unknown tensor id");
+  return push_feed(p, slot, FEED_DEVICE, t->ndim, t->shape, nullptr, 0, t->buf ? t->buf->ptr : nullptr);
+}
+
+int coex_pass_fetch(coex_prog* p, int64_t node, int64_t occ, double* out, int64_t cap, int* ndim, int64_t* shape) {
+  coex_ctx* c = p->ctx;
+  if (c->active != p) return fail(COEX_CHANNEL_CLOSED, "no pass in flight");
+  double t0 = 0;
+  while (true) {
+    auto it = p->fetch_idx.find(node);
+    if (it != p->fetch_idx.end() && (int64_t)it->second.size() > occ) {
+      const FetchEntry* e = &c->mb->fetch[it->second[occ] % kFetchCap];
+      const std::vector<double>& data = p->fetch_copy[it->second[occ]];
+      if (cap < e->numel) return fail(COEX_INVALID, "fetch buffer too small");
+      *ndim = e->ndim;
+      for (int d = 0; d < e->ndim; ++d) shape[d] = e->shape[d];
+      memcpy(out, data.data(), sizeof(double) * e->numel);
+      return COEX_OK;
+    }
+    // drain newly published entries in order
+    const FetchEntry* e = &c->mb->fetch[p->fetch_read % kFetchCap];
+    if (e->seq == seq_of(p->pass_id, p->fetch_read)) {
+      std::atomic_thread_fence(std::memory_order_acquire);
+      std::vector<double> v(e->numel);
+      if (c->prec == COEX_F64) {
+        memcpy(v.data(), c->fetch_arena + e->off, sizeof(double) * e->numel);
+      } else {
+        const float* f = (const float*)(c->fetch_arena + e->off);
+        for (int64_t i = 0; i < e->numel; ++i) v[i] = (double)f[i];
+      }
+      p->fetch_copy.push_back(std::move(v));
+      p->fetch_idx[e->node].push_back(p->fetch_read);
+      p->fetch_read++;
+      continue;
+    }
+    if (c->mb->done == p->pass_id) {
+      int st = c->mb->status;
+      if (st == 3) return fail(COEX_DECISION_MISMATCH, "device reported a decision mismatch");
+      if (st == 9) return fail(COEX_SHAPE_MISS, "fed shape differs from the graph specialisation");
+      return fail(COEX_CHANNEL_CLOSED, "pass ended without the requested fetch");
+    }
+    if (t0 == 0) t0 = now_s();
+    else if (now_s() - t0 > c->timeout_s) return fail(COEX_CHANNEL_CLOSED, "fetch timed out");
+  }
+}
+
+int coex_pass_cancel(coex_prog* p) {
+  coex_ctx* c = p->ctx;
+  if (c->active != p) return COEX_OK;
+  c->mb->cancel = p->pass_id;
+  std::atomic_thread_fence(std::memory_order_seq_cst);
+  return COEX_OK;
+}
+
+int coex_pass_wait(coex_prog* p, coex_pass_stats* st) {
+  coex_ctx* c = p->ctx;
+  if (c->active != p) return fail(COEX_CHANNEL_CLOSED, "no pass in flight");
+  double t0 = now_s();
+  while (c->mb->done != p->pass_id) {
+    if (now_s() - t0 > c->timeout_s) {
+      c->mb->cancel = p->pass_id;     // unblock any spinner, then report
+      cudaStreamSynchronize(c->stream);
+      c->active = nullptr;
+      p->running = false;
+      return fail(COEX_CHANNEL_CLOSED, "pass did not finish before the timeout");
+    }
+  }
+  std::atomic_thread_fence(std::memory_order_acquire);
+  CK(cudaStreamSynchronize(c->stream));
+  c->active = nullptr;
+  p->running = false;
+  const Mailbox* mb = c->mb;
+  if (st) {
+    st->committed = mb->committed;
+    st->status = mb->status;
+    st->exec_ms = mb->exec_ns * 1e-6;
+    st->stall_ms = mb->stall_ns * 1e-6;
+    st->ops = mb->ops;
+    st->fetches = mb->fetches;
+    st->dirty_mask = mb->dirty_mask;
+  }
+  if (mb->committed) {
+    // host bookkeeping of committed variables: the spare became the value
+    for (size_t i = 0; i < p->commit_vars.size(); ++i) {
+      int vi = p->commit_vars[i];
+      if (vi >= 64 || !((mb->dirty_mask >> vi) & 1ull)) continue;
+      Var& v = c->vars[vi];
+      Buf* old = v.t.buf;
+      v.t.buf = v.spare;
+      v.spare = (old && old->refs == 1) ? old : nullptr;
+      if (v.spare == nullptr) release(c, old);
+      auto sh = p->var_shapes.find((int)mb->var_shape_id[vi]);
+      if (sh != p->var_shapes.end()) {
+        v.t.ndim = (int)sh->second.size();
+        for (int d = 0; d < v.t.ndim; ++d) v.t.shape[d] = sh->second[d];
+        v.t.numel = numel_of(v.t.ndim, v.t.shape);
+      }
+      c->h_var_cur[vi] = v.t.buf->ptr;
+    }
+  }
+  if (mb->status == 3) return fail(COEX_DECISION_MISMATCH, "device reported a decision mismatch");
+  return mb->committed ? COEX_OK : COEX_CANCELLED;
+}
+
+}  // extern "C"

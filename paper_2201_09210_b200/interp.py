@@ -103,12 +103,12 @@ class EagerCtx:
             refs.append(External((loc.stmt_id, pos)))
             devs.append(v.dev if isinstance(v, Val) else self.be.put(lift_host_value(v) if not is_tensor(v) else v))
 
-    def _emit(self, kind, attrs, loc, refs, dev, shape) -> Val:
+    def _emit(self, kind, attrs, loc, refs, dev, shape, in_shapes=()) -> Val:
         hid = self.next_hid
         self.next_hid += 1
         if self.trace is not None:
             self.producer[hid] = len(self.trace)
-            self.trace.append(OpEvent(kind, attrs, loc, refs, [hid]))
+            self.trace.append(OpEvent(kind, attrs, loc, refs, [hid], False, tuple(shape), tuple(in_shapes)))
         return Val(dev, hid, self.epoch, shape)
 
     def op(self, kind: OpKind, attrs: dict, args: list, loc, shapes: list) -> Val:
@@ -117,7 +117,7 @@ class EagerCtx:
         for p, v in enumerate(args):
             self._arg(v, loc, p, refs, devs)
         dev = self.be.exec_op(kind, attrs, devs)
-        return self._emit(kind, attrs, loc, refs, dev, out_shape)
+        return self._emit(kind, attrs, loc, refs, dev, out_shape, [tuple(s) for s in shapes])
 
     def read_var(self, name: str, loc) -> Val:
         dev = self.be.var_read(name)
@@ -127,7 +127,7 @@ class EagerCtx:
         refs, devs = [], []
         self._arg(v, loc, 0, refs, devs)
         self.be.var_assign(name, devs[0])
-        return self._emit(OpKind.ASSIGN_VAR, {"var_name": name}, loc, refs, devs[0], shape)
+        return self._emit(OpKind.ASSIGN_VAR, {"var_name": name}, loc, refs, devs[0], shape, [tuple(shape)])
 
     def var_shape(self, name: str) -> tuple:
         return self.be.var_shape(name)
@@ -425,8 +425,8 @@ class Interp:
             return -v
         if isinstance(e, ast.BinOp):
             return self._binop(e, ctx, env, loc)
-        if isinstance(e, ast.ShapeLit):
-            return list(self._shape(e, ctx, env, loc))
+        if isinstance(e, ast.ShapeLit):     # a bracket literal outside a shape position: host list
+            return [self._host(self._expr(d, ctx, env, loc), ctx, d) for d in e.dims]
         raise self._err(f"unknown expression {type(e).__name__}", e)
 
     def _native_arg(self, v, ctx):

@@ -1,0 +1,410 @@
+"""Device plan for one SymProgram specialisation.
+
+Turns a :class:`~.graph_gen.SymProgram` plus a shape signature (variable shapes
+at pass begin, fed shapes per feed slot) into the int64 plan consumed by
+``coex_prog_build`` (csrc/runtime.cu ``Builder``), which builds one CUDA graph.
+
+Memory model:
+* every ExecOp node id owns one output buffer (two when the node can read its
+  own previous output, e.g. a loop-carried ``x = matmul(x, w)``); tail-duplicated
+  instances of a node share it, since at most one instance runs per position;
+* every value is reached through a *cell* (a device word holding a pointer):
+  ``vcell[node]`` holds the node's latest output; an input with several
+  candidate producers reads ``bcell[candidate set]``, which every candidate
+  writes when it executes -- "latest candidate wins", the phi rule the cursor
+  enforces on the host;
+* RESHAPE / READ_VAR / ASSIGN_VAR only move pointers; FILL nodes are constants
+  evaluated once at build time;
+* each feed slot owns a buffer and a cell (re-pointed for device-resident feeds).
+
+Transpose folding: a 2-D TRANSPOSE whose only consumers are MatMuls (and which
+is not fetched) is not materialised -- the MatMul reads the operand transposed.
+"""
+
+from __future__ import annotations
+
+import struct
+from dataclasses import dataclass, field
+
+from .errors import ShapeMiss
+from .graph_gen import ExecOp, InputFeed, OutputFetch, SwitchCase, SymProgram, UnrolledLoop, While
+from .tensor import OpKind, infer_shape, shape_size
+
+MAGIC = 0xC0E8B200
+VERSION = 1
+T_SEQ, T_OP, T_PTR, T_FEED, T_FETCH, T_SWITCH, T_WHILE = 1, 2, 3, 4, 5, 6, 7
+PTR_ALIAS, PTR_READ_VAR, PTR_ASSIGN_VAR = 0, 1, 2
+MAX_RANK = 8
+MAX_PUB = 6
+COMPUTE = {OpKind.MATMUL, OpKind.ADD, OpKind.SUB, OpKind.MUL, OpKind.NEG, OpKind.RELU,
+           OpKind.SIGMOID, OpKind.SUM, OpKind.MEAN, OpKind.TRANSPOSE}
+
+
+def slot_code(slot: tuple) -> int:
+    return slot[0] * 4 + slot[1]
+
+
+def _pad(shape, n=MAX_RANK) -> list:
+    s = list(shape)
+    if len(s) > n:
+        raise ShapeMiss(f"rank {len(s)} exceeds {n}")
+    return s + [0] * (n - len(s))
+
+
+def _f64_bits(x: float) -> int:
+    return struct.unpack("<q", struct.pack("<d", float(x)))[0]
+
+
+def walk(insts):
+    """Yield every instruction (pre-order), descending into cases and loop bodies."""
+    for x in insts:
+        yield x
+        if isinstance(x, SwitchCase):
+            for c in x.cases:
+                yield from walk(c)
+        elif isinstance(x, While):
+            yield from walk(x.body)
+        elif isinstance(x, UnrolledLoop):
+            if x.bodies:
+                yield from walk(x.bodies[0])
+
+
+@dataclass
+class Plan:
+    words: list
+    consts: list
+    signature: tuple
+    n_compute: int = 0
+    flops: int = 0                       # algorithmic FLOPs if every instruction ran once
+    node_shapes: dict = field(default_factory=dict)
+    feed_shapes: dict = field(default_factory=dict)
+    folded: set = field(default_factory=set)
+
+
+class Planner:
+    def __init__(self, sp: SymProgram, tg, var_index: dict, var_shapes: dict, feed_shapes: dict, esize: int):
+        self.sp = sp
+        self.tg = tg
+        self.var_index = var_index
+        self.var_shapes = dict(var_shapes)
+        self.feed_shapes = dict(feed_shapes)
+        self.esize = esize
+        self.ops = {}           # node id -> ExecOp (first instance)
+        for x in walk(sp.body):
+            if isinstance(x, ExecOp) and x.node_id not in self.ops:
+                self.ops[x.node_id] = x
+
+    # ------------------------------------------------------------ shapes
+    def infer_shapes(self) -> dict:
+        shapes: dict = {}
+        vsh = dict(self.var_shapes)
+
+        def in_shape(b):
+            if b.fed:
+                s = self.feed_shapes.get(b.slot)
+                if s is None:
+                    raise ShapeMiss(f"no shape known for feed slot {b.slot}")
+                return tuple(s)
+            known = [shapes[c] for c in b.cands if c in shapes]
+            if not known:
+                return None
+            if any(k != known[0] for k in known):
+                raise ShapeMiss(f"candidates {b.cands} disagree on shape")
+            return known[0]
+
+        def go(insts, final):
+            for x in insts:
+                if isinstance(x, ExecOp):
+                    if x.kind is OpKind.READ_VAR:
+                        name = x.attrs["var_name"]
+                        if name not in vsh:
+                            raise ShapeMiss(f"unknown variable {name!r}")
+                        s = tuple(vsh[name])
+                    else:
+                        ins = [in_shape(b) for b in x.inputs]
+                        if any(i is None for i in ins):
+                            if final:
+                                raise ShapeMiss(f"node {x.node_id}: input shape unknown")
+                            continue
+                        s = tuple(infer_shape(x.kind, x.attrs, ins)[0])
+                        if x.kind is OpKind.ASSIGN_VAR:
+                            name = x.attrs["var_name"]
+                            if name in self.var_shapes and tuple(self.var_shapes[name]) != s:
+                                raise ShapeMiss(f"assignment changes the shape of {name!r}")
+                            vsh[name] = s
+                    if x.node_id in shapes and shapes[x.node_id] != s:
+                        raise ShapeMiss(f"node {x.node_id} has a path-dependent shape")
+                    shapes[x.node_id] = s
+                elif isinstance(x, SwitchCase):
+                    for c in x.cases:
+                        go(c, final)
+                elif isinstance(x, While):
+                    go(x.body, final)
+                    go(x.body, final)
+                elif isinstance(x, UnrolledLoop):
+                    for b in x.bodies:
+                        go(b, final)
+
+        go(self.sp.body, False)
+        go(self.sp.body, True)
+        return shapes
+
+    # ------------------------------------------------------------ plan
+    def build(self) -> Plan:
+        shapes = self.infer_shapes()
+        ops = self.ops
+        # consumers of every node id (over all bindings)
+        consumers: dict = {}
+        multi: dict = {}          # frozenset(cands) -> bcell index (assigned later)
+        for x in walk(self.sp.body):
+            if isinstance(x, ExecOp):
+                for b in x.inputs:
+                    if not b.fed:
+                        for c in b.cands:
+                            consumers.setdefault(c, []).append(x)
+                        if len(b.cands) > 1:
+                            multi.setdefault(frozenset(b.cands), None)
+        # transpose folding: 2-D transpose consumed only (single-candidate) by matmuls, not fetched
+        folded = set()
+        for nid, x in ops.items():
+            if x.kind is OpKind.TRANSPOSE and tuple(x.attrs["perm"]) == (1, 0) and nid not in self.sp.fetch_nodes:
+                cons = consumers.get(nid, [])
+                if cons and all(c.kind is OpKind.MATMUL for c in cons) and \
+                        not any(nid in s for s in multi) and not x.inputs[0].fed and len(x.inputs[0].cands) == 1 \
+                        and _fold_is_local(self.sp.body, nid, x.inputs[0].cands[0]):
+                    folded.add(nid)
+        self.folded = folded
+
+        bufs: list = []
+
+        def new_buf(nbytes):
+            bufs.append(max(int(nbytes), 16))
+            return len(bufs) - 1
+
+        cell_init: list = []
+
+        def new_cell(buf_idx=-1):
+            cell_init.append(buf_idx)
+            return len(cell_init) - 1
+
+        node_buf: dict = {}
+        vcell: dict = {}
+        fills: list = []
+        consts: list = []
+        for nid, x in ops.items():
+            n = shape_size(shapes[nid])
+            if x.kind in COMPUTE and nid not in folded:
+                self_dep = any((not b.fed) and nid in b.cands for b in x.inputs)
+                b0 = new_buf(n * self.esize)
+                b1 = new_buf(n * self.esize) if self_dep else -1
+                node_buf[nid] = (b0, b1, self_dep)
+                vcell[nid] = new_cell(b0)
+            elif x.kind is OpKind.FILL:
+                b0 = new_buf(n * self.esize)
+                consts.append(float(x.attrs["value"]))
+                fills.append((b0, n, len(consts) - 1))
+                vcell[nid] = new_cell(b0)
+            else:
+                vcell[nid] = new_cell(-1)
+        for s in list(multi):
+            multi[s] = new_cell(-1)
+        slot_buf: dict = {}
+        slot_cell: dict = {}
+        slot_rec: dict = {}
+        for slot in sorted(self.sp.feed_slots):
+            shp = self.feed_shapes.get(slot)
+            if shp is None:
+                raise ShapeMiss(f"no shape known for feed slot {slot}")
+            slot_buf[slot] = new_buf(shape_size(shp) * self.esize)
+            slot_cell[slot] = new_cell(slot_buf[slot])
+            slot_rec[slot] = len(slot_rec)
+        pubs: dict = {}
+        for nid in ops:
+            lst = [vcell[nid]] + [c for s, c in multi.items() if nid in s]
+            if len(lst) > MAX_PUB:
+                raise ShapeMiss(f"node {nid} publishes to {len(lst)} cells (max {MAX_PUB})")
+            pubs[nid] = lst
+
+        def in_cell(b):
+            if b.fed:
+                return slot_cell[b.slot]
+            if len(b.cands) == 1:
+                return vcell[b.cands[0]]
+            return multi[frozenset(b.cands)]
+
+        # variables assigned by the program (committed at pass end)
+        assigned: dict = {}
+        shape_ids: dict = {}
+        for x in walk(self.sp.body):
+            if isinstance(x, ExecOp) and x.kind is OpKind.ASSIGN_VAR:
+                name = x.attrs["var_name"]
+                s = shapes[x.node_id]
+                assigned[name] = shape_size(s) * self.esize
+                shape_ids.setdefault(s, len(shape_ids))
+        self._sids = shape_ids
+        late_count = [0]
+        n_compute = [0]
+        flops = [0]
+        w: list = []
+
+        def out_words(nid, late):
+            b0, b1, pp = node_buf.get(nid, (-1, -1, False))
+            p = pubs[nid]
+            if late:
+                late_count[0] += 1
+            return [b0, b1, int(pp), int(late), len(p)] + p + [0] * (MAX_PUB - len(p))
+
+        def ptr_item(op, nid, cin, var_idx, shape_id):
+            return [T_PTR, op, nid, cin, var_idx, shape_id] + out_words(nid, False)
+
+        def emit(insts) -> list:
+            items = []
+            for x in insts:
+                if isinstance(x, InputFeed):
+                    shp = tuple(self.feed_shapes[x.slot])
+                    items.append([T_FEED, slot_code(x.slot), shape_size(shp), len(shp)] + _pad(shp)
+                                 + [slot_buf[x.slot], slot_cell[x.slot], slot_rec[x.slot]])
+                elif isinstance(x, OutputFetch):
+                    shp = shapes[x.node_id]
+                    items.append([T_FETCH, x.node_id, vcell[x.node_id], shape_size(shp), len(shp)] + _pad(shp))
+                elif isinstance(x, ExecOp):
+                    items.extend(self._exec(x, shapes, in_cell, out_words, ptr_item, pubs, multi,
+                                            folded, n_compute, flops))
+                elif isinstance(x, SwitchCase):
+                    it = [T_SWITCH, x.branch_id, len(x.cases)]
+                    for c in x.cases:
+                        it += seq(c)
+                    items.append(it)
+                elif isinstance(x, While):
+                    items.append([T_WHILE, x.loop_id] + seq(x.body))
+                elif isinstance(x, UnrolledLoop):
+                    for b in x.bodies:
+                        items.extend(emit(b))
+            return items
+
+        def seq(insts) -> list:
+            items = emit(insts)
+            out = [T_SEQ, len(items)]
+            for it in items:
+                out += it
+            return out
+
+        body = seq(self.sp.body)
+        w += [MAGIC, VERSION, len(bufs)] + bufs
+        w += [len(cell_init)] + cell_init
+        w += [len(slot_rec), late_count[0]]
+        w += [len(fills)]
+        for b0, n, ci in fills:
+            w += [b0, n, ci]
+        w += [len(assigned)]
+        for name, nbytes in assigned.items():
+            w += [self.var_index[name], nbytes]
+        w += [len(shape_ids)]
+        for s, sid in shape_ids.items():
+            w += [sid, len(s)] + list(s)
+        w += body
+        sig = (tuple(sorted((k, tuple(v)) for k, v in self.var_shapes.items())),
+               tuple(sorted((k, tuple(v)) for k, v in self.feed_shapes.items())))
+        return Plan(w, consts, sig, n_compute[0], flops[0], shapes, dict(self.feed_shapes), folded)
+
+    def _exec(self, x, shapes, in_cell, out_words, ptr_item, pubs, multi, folded, n_compute, flops) -> list:
+        nid = x.node_id
+        k = x.kind
+        if k is OpKind.FILL:
+            if any(nid in s for s in multi):
+                return [ptr_item(PTR_ALIAS, nid, in_cell_const(nid, pubs), -1, -1)]
+            return []
+        if k is OpKind.RESHAPE:
+            return [ptr_item(PTR_ALIAS, nid, in_cell(x.inputs[0]), -1, -1)]
+        if k is OpKind.READ_VAR:
+            return [ptr_item(PTR_READ_VAR, nid, -1, self.var_index[x.attrs["var_name"]], -1)]
+        if k is OpKind.ASSIGN_VAR:
+            s = shapes[nid]
+            return [ptr_item(PTR_ASSIGN_VAR, nid, in_cell(x.inputs[0]), self.var_index[x.attrs["var_name"]],
+                             self._shape_id(s))]
+        if nid in folded:
+            return []
+        ins = list(x.inputs)
+        trans = [0, 0]
+        cells = []
+        in_shapes = []
+        for i, b in enumerate(ins):
+            if k is OpKind.MATMUL and not b.fed and len(b.cands) == 1 and b.cands[0] in folded:
+                tnode = self.ops[b.cands[0]]
+                cells.append(in_cell(tnode.inputs[0]))
+                in_shapes.append(shapes[tnode.inputs[0].cands[0]])
+                trans[i] = 1
+            else:
+                cells.append(in_cell(b))
+                in_shapes.append(self._in_shape(b, shapes))
+        while len(cells) < 2:
+            cells.append(-1)
+            in_shapes.append(())
+        late = any(c in pubs[nid] for c in cells if c >= 0)
+        attr_dims = list(x.attrs.get("perm", ()))
+        out_shape = shapes[nid]
+        n_compute[0] += 1
+        if k is OpKind.MATMUL:
+            m, kk = (in_shapes[0][1], in_shapes[0][0]) if trans[0] else in_shapes[0]
+            nn = in_shapes[1][0] if trans[1] else in_shapes[1][1]
+            flops[0] += 2 * m * nn * kk
+        word = [T_OP, k.code, nid, cells[0], cells[1]]
+        for s in in_shapes:
+            word += [len(s)] + _pad(s)
+        word += [len(out_shape)] + _pad(out_shape)
+        word += [len(attr_dims)] + _pad(attr_dims) + [_f64_bits(0.0), trans[0], trans[1]]
+        word += out_words(nid, late)
+        return [word]
+
+    def _in_shape(self, b, shapes):
+        if b.fed:
+            return tuple(self.feed_shapes[b.slot])
+        return shapes[b.cands[0]]
+
+    def _shape_id(self, s):
+        return self._sids[tuple(s)]
+
+
+def in_cell_const(nid, pubs):
+    return pubs[nid][0]
+
+
+def _mentions(x, nid) -> bool:
+    return any(isinstance(y, ExecOp) and y.node_id == nid for y in walk([x]))
+
+
+def _fold_is_local(insts, tnid: int, producer: int) -> bool:
+    """A transpose may be read in place by its MatMul consumer only if, in every
+    instruction list holding the transpose, a consuming MatMul follows in the
+    same list and nothing in between can re-execute the transpose's producer."""
+    ok = True
+    found = False
+
+    def scan(lst):
+        nonlocal ok, found
+        for i, x in enumerate(lst):
+            if isinstance(x, ExecOp) and x.node_id == tnid:
+                found = True
+                j = i + 1
+                hit = False
+                while j < len(lst):
+                    y = lst[j]
+                    if isinstance(y, ExecOp) and y.kind is OpKind.MATMUL and \
+                            any((not b.fed) and tnid in b.cands for b in y.inputs):
+                        hit = True
+                        break
+                    if _mentions(y, producer) or not isinstance(y, (ExecOp, InputFeed, OutputFetch)):
+                        break
+                    j += 1
+                ok = ok and hit
+            elif isinstance(x, SwitchCase):
+                for c in x.cases:
+                    scan(c)
+            elif isinstance(x, While):
+                scan(x.body)
+            elif isinstance(x, UnrolledLoop):
+                for b in x.bodies:
+                    scan(b)
+
+    scan(insts)
+    return ok and found

@@ -58,6 +58,8 @@ class OpEvent:
     inputs: list
     outputs: list
     fetch_after: bool = False
+    out_shape: tuple | None = None      # observed shapes: specialisation hints, not part of the key
+    in_shapes: tuple | None = None
 
     def key(self) -> tuple:
         return op_key(self.kind, self.attrs, self.loc, self.in_kinds())
@@ -116,6 +118,8 @@ class Node:
     loop_id: int = -1
     body: "TraceGraph | None" = None
     trip_counts: set = field(default_factory=set)
+    out_shape: tuple | None = None      # last observed output shape (planner hint)
+    feed_shapes: dict = field(default_factory=dict)   # input pos -> last observed fed shape
 
     def key(self) -> tuple:
         if self.typ == "op":
@@ -303,6 +307,12 @@ class _Merger:
         if e.fetch_after and not node.fetch:
             node.fetch = True
             self.rep.annotations_added += 1
+        if e.out_shape is not None:
+            node.out_shape = tuple(e.out_shape)
+        if e.in_shapes is not None:
+            for pos, k in enumerate(kinds):
+                if k == "e":
+                    node.feed_shapes[pos] = tuple(e.in_shapes[pos])
         for o in e.outputs:
             self.hmap[o] = nid
         return nid
