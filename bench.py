@@ -1,0 +1,323 @@
+"""Benchmark: C1 tiny-MLP training iterations/s under B200 co-execution.
+
+Metric (BASELINE.json): training iterations/s at 1/2/4/8 B200, next to the
+reference CPU co-execution path, with the dominant kernel's roofline fraction.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--precision f64|fp32|bf16] [--impl b200|reference]
+
+A *step* is one training iteration of C1 (paper_2201_09210_b200/workloads.py)
+run by the co-execution orchestrator: the Python skeleton walks the step while
+the B200 executes the step's CUDA graph (one cudaGraphLaunch; SWITCH / WHILE
+conditional nodes driven by the skeleton's decisions over pinned mapped memory).
+
+* ``value``: K / (sum of per-step device time), CUDA events on the context's
+  stream bracketing each step; synthetic inputs expanded on the device from the
+  generator state (no host data), L2 flushed (256 MiB write) between steps
+  outside the timed region.
+* ``e2e``: the same metric through the public API with host-resident inputs
+  (``InMemoryDataset``): every step copies x and y host->device through the C-ABI
+  feed path and reads the loss back.
+* ``roofline``: the dominant compute kernel of the step, re-launched eagerly with
+  the step's shapes between CUDA events on the same stream.
+* ``cpu_baseline``: the CPU oracle co-execution (oracle/, SPEC-faithful runner +
+  reference kernels + reference Python dataset) on a bounded sample, rank 0 only.
+
+Multi-GPU: one process per GPU (torchrun); each rank runs its own C1 replica on
+its own data stream (weak scaling).  Time = max over ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2201_09210_b200 import coexec, lang  # noqa: E402
+from paper_2201_09210_b200.coexec import Phase  # noqa: E402
+from paper_2201_09210_b200.dataset import SyntheticDataset  # noqa: E402
+from paper_2201_09210_b200.tensor import OpKind, Tensor, shape_size  # noqa: E402
+from paper_2201_09210_b200.workloads import C1, InMemoryDataset, c1_flops, c1_program  # noqa: E402
+
+METRIC = "training iterations/sec at 1/2/4/8 B200 vs ref CPU co-exec; % HBM/tensor roofline"
+UNIT = "it/s"
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), float(p["bf16_tflops"]), "measured"
+    except Exception:
+        return 6650.0, 1590.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.samples = []
+        self.stop = threading.Event()
+        self.t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        while not self.stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}", "--format=csv,noheader,nounits"],
+                                     capture_output=True, text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self.stop.wait(0.2)
+
+    def __enter__(self):
+        self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self.stop.set()
+        self.t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = sorted(float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit())
+        mx = max((float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()), default=None)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if len(s) > 2 + i and "Active" in s[2 + i]})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def make_orch(src, dataset, backend):
+    o = coexec.Orchestrator(lang.parse(src), dataset, coexec.Mode.coexec, coexec.RunConfig(), backend)
+    o.start()
+    return o
+
+
+def reach_coexec(o, budget: int = 40):
+    """Untimed steps until the phase machine has generated a graph and runs CoExec."""
+    n = 0
+    while o.phase is not Phase.CoExec and n < budget:
+        o.step()
+        n += 1
+    return n
+
+
+def flush_l2():
+    import torch
+    buf = getattr(flush_l2, "buf", None)
+    if buf is None:
+        buf = flush_l2.buf = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    buf.fill_(1)
+    torch.cuda.synchronize()
+
+
+def timed_steps(o, be, k: int, flush: bool = True):
+    """Run k steps; device time per step from CUDA events on the context stream."""
+    tot = 0.0
+    ops0 = be.kernel_count()
+    for _ in range(k):
+        if flush:
+            flush_l2()
+        be.event(0)
+        o.step()
+        be.event(1)
+        tot += be.elapsed_ms(0, 1)
+    return tot, be.kernel_count() - ops0
+
+
+def roofline(be, hbm_peak, tflops_peak, peak_kind):
+    """Time every compute kernel of the C1 step eagerly (same shapes, same stream)."""
+    import numpy as np
+    b, h, din, dout = C1["batch"], C1["hidden"], C1["din"], C1["dout"]
+    r = np.random.default_rng(0)
+
+    def t(*s):
+        return Tensor(s, r.standard_normal(s))
+
+    kernels = {
+        "matmul x.w1 [64x784]x[784x128]": (OpKind.MATMUL, {}, [t(b, din), t(din, h)]),
+        "matmul x^T.dh [784x64]x[64x128]": (OpKind.MATMUL, {}, [t(din, b), t(b, h)]),
+        "matmul h.w2 [64x128]x[128x10]": (OpKind.MATMUL, {}, [t(b, h), t(h, dout)]),
+        "sigmoid [64x128]": (OpKind.SIGMOID, {}, [t(b, h)]),
+        "sub w1 update [784x128]": (OpKind.SUB, {}, [t(din, h), t(din, h)]),
+        "mean [64x10]": (OpKind.MEAN, {}, [t(b, dout)]),
+    }
+    times = {name: be.time_op(*spec, reps=200) for name, spec in kernels.items()}
+    top = max(times, key=times.get)
+    kind, _, ins = kernels[top]
+    es = be.esize
+    byts = sum(x.size() for x in ins) * es
+    if kind is OpKind.MATMUL:
+        (m, kk), (_, n) = ins[0].shape, ins[1].shape
+        byts += m * n * es
+        flops = 2 * m * n * kk
+    else:
+        byts += ins[0].size() * es
+        flops = ins[0].size()
+    ms = times[top]
+    achieved = byts / (ms * 1e-3) / 1e9
+    return {"bound": "hbm", "kernel": top, "achieved": round(achieved, 3), "peak": hbm_peak, "unit": "GB/s",
+            "frac": round(achieved / hbm_peak, 6), "traffic": None, "peak_source": peak_kind,
+            "kernel_ms": round(ms, 5), "algorithmic_bytes": byts, "flops": flops,
+            "achieved_tflops": round(flops / (ms * 1e-3) / 1e12, 4),
+            "all_kernels_ms": {k: round(v, 5) for k, v in times.items()}}
+
+
+def cpu_baseline(steps: int = 12):
+    """CPU oracle co-execution of C1 on this host (bounded sample)."""
+    from oracle.cpu_backend import CpuBackend
+    from oracle.ref_dataset import RefSyntheticDataset
+    src = c1_program(steps=10_000, **C1)
+    o = make_orch(src, RefSyntheticDataset(0), CpuBackend())
+    reach_coexec(o)
+    o.step()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        o.step()
+    dt = time.perf_counter() - t0
+    return {"value": round(steps / dt, 4), "unit": UNIT, "cores": 2, "kind": "port",
+            "sample": f"C1 co-exec, {steps} steps after tracing+1 warm step; oracle runner+kernels+reference "
+                      f"per-element Python dataset; host cpu_count={os.cpu_count()}"}
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    k = max(1, min(args.steps, 30))
+    base = cpu_baseline(k)
+    line = {"impl": "reference", "metric": METRIC, "value": base["value"], "unit": UNIT, "n_gpus": 0,
+            "steps": k, "warmup": args.warmup, "ms_per_step": round(1e3 / base["value"], 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (reference SyntheticDataset, seed 0)",
+            "config": {"workload": "C1 tiny MLP 784-128-10, batch 64, coexec (CPU oracle runner)",
+                       "global_batch": 64},
+            "cpu_baseline": base,
+            "e2e": {"value": base["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+def run_b200(args):
+    rank, world, local = dist_env()
+    import torch
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    from paper_2201_09210_b200.b200 import B200Backend
+    be = B200Backend(device=local if world > 1 else 0, precision=args.precision)
+    total_steps = 100_000
+    src = c1_program(steps=total_steps, **C1)
+    # each rank trains its own replica on its own data stream (weak scaling)
+    o = make_orch(src, SyntheticDataset(1000 + rank), be)
+    pre = reach_coexec(o)
+    for _ in range(args.warmup):
+        o.step()
+    if world > 1:
+        torch.distributed.barrier()
+    be.sync()
+    hbm, tfl, peak_kind = load_peaks()
+    replays0 = o.stats.steps_replayed
+    with ClockSampler(local) as clk:
+        dev_ms, launches = timed_steps(o, be, args.steps)
+    be.sync()
+    replays = o.stats.steps_replayed - replays0
+    t_max = dev_ms
+    if world > 1:
+        tt = torch.tensor([dev_ms], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        t_max = float(tt.item())
+    value = world * args.steps / (t_max * 1e-3)
+
+    # e2e: host-resident inputs through the public API (H2D each step, loss D2H)
+    import numpy as np
+    rr = np.random.default_rng(7 + rank)
+    b, din, dout, h = C1["batch"], C1["din"], C1["dout"], C1["hidden"]
+    recs = {"x": [Tensor((b, din), rr.uniform(-1, 1, (b, din))) for _ in range(4)],
+            "y": [Tensor((b, dout), rr.uniform(-1, 1, (b, dout))) for _ in range(4)],
+            "w1_init": [Tensor((din, h), rr.uniform(-1, 1, (din, h)))],
+            "w2_init": [Tensor((h, dout), rr.uniform(-1, 1, (h, dout)))]}
+    be2 = B200Backend(device=local if world > 1 else 0, precision=args.precision)
+    o2 = make_orch(src, InMemoryDataset(recs), be2)
+    reach_coexec(o2)
+    for _ in range(args.warmup):
+        o2.step()
+    e2e_ms, _ = timed_steps(o2, be2, args.steps)
+    e2e_max = e2e_ms
+    if world > 1:
+        tt = torch.tensor([e2e_ms], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        e2e_max = float(tt.item())
+    esz = 8
+    h2d = (b * din + b * dout) * esz
+    d2h = 8
+
+    if rank == 0:
+        roof = roofline(be, hbm, tfl, peak_kind)
+        base = cpu_baseline(12) if world == 1 and not args.no_cpu_baseline else None
+        st = o.stats
+        line = {
+            "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(t_max / args.steps, 5), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": args.precision,
+            "data": "synthetic (SyntheticDataset seed 1000+rank, expanded on device from xorshift64* state)",
+            "config": {"workload": "C1 tiny MLP 784-128-10 (sigmoid, MSE, hand-written backward, "
+                                   "loss-driven branch, native clip, choice-driven while), coexec mode",
+                       "global_batch": C1["batch"] * world, "per_gpu_batch": C1["batch"],
+                       "parallelism": f"replicas{world}", "l2": "flushed (256 MiB write) between timed steps",
+                       "tracing_steps_before_coexec": pre, "steps_replayed_in_timed_region": replays,
+                       "algorithmic_flops_per_step": c1_flops(**C1)},
+            "roofline": roof,
+            "cpu_baseline": base,
+            "e2e": {"value": round(world * args.steps / (e2e_max * 1e-3), 3), "unit": UNIT,
+                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "data": "InMemoryDataset host tensors, copied through coex_pass_feed each step"},
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+            "stats": {"graph_exec_ms": round(st.graph_exec_ms, 3), "graph_stall_ms": round(st.graph_stall_ms, 3),
+                      "python_exec_ms": round(st.python_exec_ms, 3), "python_stall_ms": round(st.python_stall_ms, 3),
+                      "counters": list(st.counters())},
+        }
+        print(json.dumps(line))
+    be2.close()
+    be.close()
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--precision", default="f64", choices=["f64", "fp32", "bf16"])
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

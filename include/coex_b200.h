@@ -93,6 +93,13 @@ int coex_ctx_set_timeout(coex_ctx* ctx, double seconds);
 /* Number of compute kernels this context launched eagerly or replayed in graphs. */
 int64_t coex_ctx_kernel_count(coex_ctx* ctx);
 
+/* ---- timing on the context's stream (bench.py; CUDA events, not host clocks) ---- */
+int coex_ctx_event_record(coex_ctx* ctx, int slot);               /* slot in [0, 64) */
+int coex_ctx_event_elapsed(coex_ctx* ctx, int a, int b, double* ms);
+/* Launch one op `reps` times back to back between two events; average device ms per launch. */
+int coex_exec_op_timed(coex_ctx* ctx, int kind, const coex_attrs* attrs, int nin, const int64_t* in_ids,
+                       int reps, double* avg_ms);
+
 /* ---- tensors (eager side) ---- */
 int coex_tensor_put(coex_ctx* ctx, int ndim, const int64_t* shape, const double* data, int64_t* id);
 int coex_tensor_synth(coex_ctx* ctx, uint64_t state, int ndim, const int64_t* shape, int64_t* id);

@@ -47,6 +47,7 @@ class ChannelSet:
         self.decisions = deque()
         self.feeds = defaultdict(deque)
         self.fetches = defaultdict(deque)
+        self.commit = deque()          # commit token: the skeleton reached StepEnd
         self.cancelled = False
 
     def _push(self, q, item, bounded=True):
@@ -187,6 +188,9 @@ class _Runner:
 
     def whole(self):
         yield from self.run(self.sp.body)
+        # never commit before the skeleton confirms StepEnd: a pass that ran to
+        # its end ahead of a late divergence must still be cancellable
+        yield from self._pop(self.ch.commit)
 
 
 def run_pass(sp, ch: ChannelSet, vs: VariableStore) -> PassResult:
@@ -303,6 +307,8 @@ class CpuPass:
         self.ch.cancel()
 
     def wait(self) -> PassResult:
+        if not self.ch.cancelled:
+            self.ch._push(self.ch.commit, True, bounded=False)
         if self.lazy:
             if not self.done and self.ch.cancelled:
                 self._finish(False)

@@ -56,6 +56,10 @@ SIGNATURES = {
     "coex_ctx_sync": (ctypes.c_int, [_P]),
     "coex_ctx_set_timeout": (ctypes.c_int, [_P, ctypes.c_double]),
     "coex_ctx_kernel_count": (_I64, [_P]),
+    "coex_ctx_event_record": (ctypes.c_int, [_P, ctypes.c_int]),
+    "coex_ctx_event_elapsed": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int, _DP]),
+    "coex_exec_op_timed": (ctypes.c_int, [_P, ctypes.c_int, ctypes.POINTER(CoexAttrs), ctypes.c_int, _I64P,
+                                          ctypes.c_int, _DP]),
     "coex_tensor_put": (ctypes.c_int, [_P, ctypes.c_int, _I64P, _DP, _I64P]),
     "coex_tensor_synth": (ctypes.c_int, [_P, ctypes.c_uint64, ctypes.c_int, _I64P, _I64P]),
     "coex_tensor_get": (ctypes.c_int, [_P, _I64, _DP, _I64, _IP, _I64P]),
@@ -118,6 +122,25 @@ def _shape_arr(shape):
     return a
 
 
+def _attrs(kind: OpKind, attrs: dict) -> CoexAttrs:
+    at = CoexAttrs()
+    if kind is OpKind.TRANSPOSE:
+        dims = attrs["perm"]
+    elif kind is OpKind.RESHAPE:
+        dims = attrs["target_shape"]
+    elif kind is OpKind.FILL:
+        dims = attrs["shape"]
+        at.value = float(attrs["value"])
+    else:
+        dims = ()
+    if len(dims) > MAX_RANK:
+        raise CoexError(f"rank {len(dims)} exceeds {MAX_RANK}")
+    at.n = len(dims)
+    for i, d in enumerate(dims):
+        at.dims[i] = int(d)
+    return at
+
+
 class DevTensor:
     """A device tensor handle owned by a context (freed on GC)."""
 
@@ -167,6 +190,25 @@ class B200Backend:
     def sync(self):
         _check(self.lib.coex_ctx_sync(self.ctx))
 
+    def event(self, slot: int):
+        """Record CUDA event ``slot`` on the context's stream."""
+        _check(self.lib.coex_ctx_event_record(self.ctx, slot))
+
+    def elapsed_ms(self, a: int, b: int) -> float:
+        ms = ctypes.c_double()
+        _check(self.lib.coex_ctx_event_elapsed(self.ctx, a, b, ctypes.byref(ms)))
+        return ms.value
+
+    def time_op(self, kind: OpKind, attrs: dict, values: list, reps: int = 50) -> float:
+        """Average device ms of one launch of ``kind`` (CUDA events on the context stream)."""
+        devs = [self.put(v) for v in values]
+        at = _attrs(kind, attrs)
+        ids = (ctypes.c_int64 * 2)(*[d.id for d in devs], *([0] * (2 - len(devs))))
+        ms = ctypes.c_double()
+        _check(self.lib.coex_exec_op_timed(self.ctx, kind.code, ctypes.byref(at), len(devs), ids, reps,
+                                           ctypes.byref(ms)))
+        return ms.value
+
     # ------------------------------------------------------------ eager side
     def put(self, t) -> DevTensor:
         if isinstance(t, DevTensor):
@@ -195,21 +237,7 @@ class B200Backend:
 
     def exec_op(self, kind: OpKind, attrs: dict, values: list) -> DevTensor:
         devs = [self.put(v) for v in values]
-        at = CoexAttrs()
-        if kind is OpKind.TRANSPOSE:
-            dims = attrs["perm"]
-        elif kind is OpKind.RESHAPE:
-            dims = attrs["target_shape"]
-        elif kind is OpKind.FILL:
-            dims = attrs["shape"]
-            at.value = float(attrs["value"])
-        else:
-            dims = ()
-        if len(dims) > MAX_RANK:
-            raise CoexError(f"rank {len(dims)} exceeds {MAX_RANK}")
-        at.n = len(dims)
-        for i, d in enumerate(dims):
-            at.dims[i] = int(d)
+        at = _attrs(kind, attrs)
         ids = (ctypes.c_int64 * 2)(*[d.id for d in devs], *([0] * (2 - len(devs))))
         out = ctypes.c_int64()
         _check(self.lib.coex_exec_op(self.ctx, kind.code, ctypes.byref(at), len(devs), ids, ctypes.byref(out)))

@@ -211,29 +211,42 @@ class Orchestrator:
         self.stats.graph_stall_ms += res.stall_ms
 
     # ---- main loop -----------------------------------------------------------
-    def run(self):
+    def start(self):
+        """Run the prologue imperatively."""
         self.it.run_prologue()
+        self.next_step = 0
+
+    def step(self) -> Phase:
+        """Run the next step in the current phase; returns the phase it ran in."""
+        step = self.next_step
+        self.next_step += 1
+        t0 = time.perf_counter()
+        phase = self.phase
+        if self.mode is Mode.imperative or phase is Phase.ImperativeOnly:
+            self._imperative_step(step)
+            self.stats.python_exec_ms += (time.perf_counter() - t0) * 1e3
+        elif phase is Phase.Tracing:
+            self.step_tracing(step)
+            self.stats.python_exec_ms += (time.perf_counter() - t0) * 1e3
+        else:
+            self.step_coexec(step, lazy=self.mode is Mode.lazy)
+        dt = time.perf_counter() - t0
+        self.step_times.append(dt)
+        self.stats.per_step.append({"step": step, "phase": phase.value, "ms": dt * 1e3})
+        return phase
+
+    def result(self) -> RunResult:
+        return RunResult(list(self.it.out), self.be.snapshot_vars(), self.step_times)
+
+    def run(self):
+        self.start()
         t_run = time.perf_counter()
-        for step in range(self.prog.step_count):
-            t0 = time.perf_counter()
-            phase = self.phase
-            if self.mode is Mode.imperative or phase is Phase.ImperativeOnly:
-                ts = time.perf_counter()
-                self._imperative_step(step)
-                self.stats.python_exec_ms += (time.perf_counter() - ts) * 1e3
-            elif phase is Phase.Tracing:
-                ts = time.perf_counter()
-                self.step_tracing(step)
-                self.stats.python_exec_ms += (time.perf_counter() - ts) * 1e3
-            else:
-                self.step_coexec(step, lazy=self.mode is Mode.lazy)
-            dt = time.perf_counter() - t0
-            self.step_times.append(dt)
-            self.stats.per_step.append({"step": step, "phase": phase.value, "ms": dt * 1e3})
+        while self.next_step < self.prog.step_count:
+            self.step()
         total = time.perf_counter() - t_run
         self.stats.steps = self.prog.step_count
         self.stats.throughput = self.prog.step_count / total if total > 0 else 0.0
-        return RunResult(list(self.it.out), self.be.snapshot_vars(), self.step_times), self.stats
+        return self.result(), self.stats
 
 
 def default_backend():

@@ -584,6 +584,29 @@ __global__ void k_decide(DecideParams p) {
   cudaGraphSetConditional(p.handle, (unsigned)v);
 }
 
+// Commit gate: the overlay may only be committed once the skeleton has
+// reached StepEnd without diverging.  The host publishes a
+// commit token (decision kind 2) from coex_pass_wait; a cancel instead leaves
+// the pass uncommitted even when the device already finished every op.
+struct GateParams {
+  DevState* ds;
+  Mailbox* mb;
+};
+__global__ void k_commit_gate(GateParams p) {
+  DevState* ds = p.ds;
+  if (ds->cancelled) return;
+  long long idx = ds->dec_head;
+  const DecEntry* e = &p.mb->dec[idx % kDecCap];
+  if (!wait_seq(ds, p.mb, &e->seq, seq_of(ds->pass_id, idx))) return;
+  if (e->kind != 2) {
+    ds->status = 3;
+    ds->cancelled = 1;
+    return;
+  }
+  ds->dec_head = idx + 1;
+  p.mb->dec_consumed = idx + 1;
+}
+
 // Feed: wait for the slot's next entry; scalar / device-pointer feeds complete here,
 // host-payload and synthetic feeds are expanded by the following k_feed_fill.
 struct FeedRecord {

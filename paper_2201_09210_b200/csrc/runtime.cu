@@ -137,6 +137,7 @@ struct coex_ctx {
   int64_t kernel_count = 0;
   coex_prog* active = nullptr;
   unsigned long long pass_counter = 0;
+  cudaEvent_t events[64] = {nullptr};
 };
 
 namespace {
@@ -479,6 +480,8 @@ int coex_ctx_destroy(coex_ctx* c) {
   cudaFreeHost(c->fetch_arena);
   cudaFree(c->d_jump);
   if (c->h_stage) cudaFreeHost(c->h_stage);
+  for (auto& ev : c->events)
+    if (ev) cudaEventDestroy(ev);
   cudaStreamDestroy(c->stream);
   delete c;
   return COEX_OK;
@@ -495,6 +498,23 @@ int coex_ctx_set_timeout(coex_ctx* c, double seconds) {
 }
 
 int64_t coex_ctx_kernel_count(coex_ctx* c) { return c ? c->kernel_count : 0; }
+
+int coex_ctx_event_record(coex_ctx* c, int slot) {
+  if (slot < 0 || slot >= 64) return fail(COEX_INVALID, "event slot out of range");
+  if (!c->events[slot]) CK(cudaEventCreate(&c->events[slot]));
+  CK(cudaEventRecord(c->events[slot], c->stream));
+  return COEX_OK;
+}
+
+int coex_ctx_event_elapsed(coex_ctx* c, int a, int b, double* ms) {
+  if (a < 0 || a >= 64 || b < 0 || b >= 64 || !c->events[a] || !c->events[b])
+    return fail(COEX_INVALID, "event slot not recorded");
+  CK(cudaEventSynchronize(c->events[b]));
+  float f = 0.f;
+  CK(cudaEventElapsedTime(&f, c->events[a], c->events[b]));
+  *ms = f;
+  return COEX_OK;
+}
 
 // =============================================================== tensors
 int coex_tensor_put(coex_ctx* c, int ndim, const int64_t* shape, const double* data, int64_t* id) {
@@ -639,6 +659,48 @@ int coex_exec_op(coex_ctx* c, int kind, const coex_attrs* attrs, int nin, const 
   }
   *out_id = new_handle(c, o);
   return COEX_OK;
+}
+
+int coex_exec_op_timed(coex_ctx* c, int kind, const coex_attrs* attrs, int nin, const int64_t* in_ids, int reps,
+                       double* avg_ms) {
+  if (reps < 1) return fail(COEX_INVALID, "reps must be >= 1");
+  int64_t out;
+  int rc = coex_exec_op(c, kind, attrs, nin, in_ids, &out);     // warm-up + output buffer
+  if (rc) return rc;
+  TRec in[2];
+  for (int i = 0; i < nin; ++i) in[i] = *get_t(c, in_ids[i]);
+  TRec* o = get_t(c, out);
+  OpSpec s;
+  s.kind = kind;
+  for (int i = 0; i < nin; ++i) {
+    s.in[i].direct = in[i].buf->ptr;
+    s.in_ndim[i] = in[i].ndim;
+    memcpy(s.in_shape[i], in[i].shape, sizeof(int64_t) * in[i].ndim);
+  }
+  s.out_ndim = o->ndim;
+  memcpy(s.out_shape, o->shape, sizeof(int64_t) * o->ndim);
+  if (attrs) {
+    s.attr_n = attrs->n;
+    memcpy(s.attr_dims, attrs->dims, sizeof(int64_t) * COEX_MAX_RANK);
+    s.value = attrs->value;
+  }
+  s.out.buf[0] = o->buf->ptr;
+  Launch L;
+  rc = build_launch(c, s, &L);
+  if (rc) return rc;
+  rc = coex_ctx_event_record(c, 62);
+  if (rc) return rc;
+  for (int r = 0; r < reps; ++r) {
+    rc = launch_now(c, L);
+    if (rc) return rc;
+  }
+  rc = coex_ctx_event_record(c, 63);
+  if (rc) return rc;
+  double ms = 0;
+  rc = coex_ctx_event_elapsed(c, 62, 63, &ms);
+  *avg_ms = ms / reps;
+  coex_tensor_free(c, out);
+  return rc;
 }
 
 // =============================================================== variables
@@ -1060,6 +1122,13 @@ int coex_prog_build(coex_ctx* c, const int64_t* plan, int64_t nwords, const doub
     }
     int rc = b.seq(p->graph, &prev);
     if (rc) throw std::runtime_error(g_err);
+    {
+      GateParams gp{c->d_state, c->d_mb};
+      Launch L;
+      L.set((void*)k_commit_gate, dim3(1), dim3(1), gp);
+      rc = b.add_kernel(p->graph, &prev, L);
+      if (rc) throw std::runtime_error(g_err);
+    }
     if (!p->commit_vars.empty()) {
       CommitParams cp{};
       cp.ds = c->d_state;
@@ -1160,12 +1229,6 @@ int coex_pass_begin(coex_prog* p) {
   c->active = p;
   p->running = true;
   return COEX_OK;
-}
-
-static int device_failed(coex_prog* p) {
-  coex_ctx* c = p->ctx;
-  if (c->mb->done == p->pass_id && c->mb->status != 0) return c->mb->status;
-  return 0;
 }
 
 static int publish_wait(coex_prog* p, volatile long long* consumed, int64_t next_idx, int cap) {
@@ -1294,6 +1357,10 @@ int coex_pass_cancel(coex_prog* p) {
 int coex_pass_wait(coex_prog* p, coex_pass_stats* st) {
   coex_ctx* c = p->ctx;
   if (c->active != p) return fail(COEX_CHANNEL_CLOSED, "no pass in flight");
+  if (c->mb->cancel != p->pass_id && c->mb->done != p->pass_id) {
+    int rc = push_decision(p, 2, -1, 0);          // commit token: the skeleton reached StepEnd
+    if (rc) return rc;
+  }
   double t0 = now_s();
   while (c->mb->done != p->pass_id) {
     if (now_s() - t0 > c->timeout_s) {
