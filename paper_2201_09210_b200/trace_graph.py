@@ -321,8 +321,8 @@ class _Merger:
         lid = events[i].loop
         exit_i, iters, has_ops = _loop_extent(events, i)
         key = ("loop", lid)
-        if not has_ops and g.child_with_key(cur, key) is None:
-            return cur, exit_i + 1                      # op-free loop: dropped
+        if not has_ops:
+            return cur, exit_i + 1                      # op-free loop occurrence: dropped
         nid = self._locate(g, cur, key, lambda: Node(g.ids(), "loop", loop_id=lid, body=TraceGraph(g.ids)))
         node = g.nodes[nid]
         for s in iters:
@@ -400,7 +400,8 @@ class Cursor:
     def __init__(self, tg: TraceGraph, unrolled: dict | None = None):
         self.tg = tg
         self.stack = [_Frame(tg, tg.start)]
-        self.skip_depth = 0             # >0 while inside an op-free loop being dropped
+        self.pending: list = []         # loop markers of a loop not yet known to contain ops
+        self.pending_depth = 0
         self.execs: dict = {}           # node id -> executions so far this step
         self.clock = 0
         self.last: dict = {}            # node id -> clock of its latest execution
@@ -417,9 +418,16 @@ class Cursor:
             decisions.append(CaseDecision(f.cur, succ.index(to)))
         f.cur = to
 
+    def _replay_pending(self) -> list:
+        """The buffered loop turned out to contain ops: enter it for real."""
+        marks, self.pending, self.pending_depth = self.pending, [], 0
+        decisions: list = []
+        for kind, lid in marks:
+            decisions += (self._enter if kind == 0 else self._iter if kind == 1 else self._exit)(lid)
+        return decisions
+
     def advance_op(self, e: OpEvent) -> Advance:
-        if self.skip_depth:
-            raise Diverged("op inside a loop the graph does not contain")
+        decisions = self._replay_pending() if self.pending else []
         f = self.top
         c = f.g.child_with_key(f.cur, e.key())
         if c is None:
@@ -434,7 +442,6 @@ class Cursor:
                 latest = max(cs, key=lambda p: self.last.get(p, -1))
                 if latest != prod or self.last.get(prod) != tick:
                     raise Diverged(f"node {c} input {pos}: producer is not the latest candidate")
-        decisions: list = []
         self._leave(f, c, decisions)
         k = self.execs.get(c, 0)
         self.execs[c] = k + 1
@@ -448,15 +455,33 @@ class Cursor:
         nid, k, _ = self.handles[handle_id]
         return nid, k
 
+    # Loop markers are buffered until the loop's first op: an occurrence without
+    # ops is dropped by the merge, so it must not reach the graph.
     def loop_enter(self, lid: int) -> list:
-        if self.skip_depth:
-            self.skip_depth += 1
+        self.pending.append((0, lid))
+        self.pending_depth += 1
+        return []
+
+    def loop_iter(self, lid: int) -> list:
+        if self.pending:
+            self.pending.append((1, lid))
             return []
+        return self._iter(lid)
+
+    def loop_exit(self, lid: int) -> list:
+        if self.pending:
+            self.pending.append((2, lid))
+            self.pending_depth -= 1
+            if self.pending_depth == 0:
+                self.pending = []        # the whole buffered loop was op-free
+            return []
+        return self._exit(lid)
+
+    def _enter(self, lid: int) -> list:
         f = self.top
         c = f.g.child_with_key(f.cur, ("loop", lid))
         if c is None:
-            self.skip_depth = 1          # dropped unless it turns out to contain ops
-            return []
+            raise Diverged(f"no loop {lid} successor at node {f.cur}")
         decisions: list = []
         self._leave(f, c, decisions)
         self.stack.append(_Frame(f.g.nodes[c].body, -1, f.g.nodes[c]))
@@ -468,9 +493,7 @@ class Cursor:
                 raise Diverged(f"loop {f.loop.loop_id}: iteration ends where the body cannot")
             self._leave(f, f.g.end, decisions)
 
-    def loop_iter(self, lid: int) -> list:
-        if self.skip_depth:
-            return []
+    def _iter(self, lid: int) -> list:
         f = self.top
         decisions: list = []
         self._end_iteration(f, decisions)
@@ -485,10 +508,7 @@ class Cursor:
         f.in_body = True
         return decisions
 
-    def loop_exit(self, lid: int) -> list:
-        if self.skip_depth:
-            self.skip_depth -= 1
-            return []
+    def _exit(self, lid: int) -> list:
         f = self.top
         decisions: list = []
         self._end_iteration(f, decisions)
@@ -503,7 +523,7 @@ class Cursor:
 
     def step_end(self) -> list:
         f = self.top
-        if len(self.stack) != 1 or self.skip_depth:
+        if len(self.stack) != 1 or self.pending:
             raise MalformedTrace("StepEnd inside a loop")
         if not f.g.has_edge(f.cur, f.g.end):
             raise Diverged("step ends where the graph cannot")
