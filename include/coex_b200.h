@@ -100,6 +100,11 @@ int coex_ctx_event_elapsed(coex_ctx* ctx, int a, int b, double* ms);
 int coex_exec_op_timed(coex_ctx* ctx, int kind, const coex_attrs* attrs, int nin, const int64_t* in_ids,
                        int reps, double* avg_ms);
 
+/* Device-side per-kernel stamps (%globaltimer, kernel kind) for the next passes (0 = off).
+ * coex_ctx_read_trace returns n (time_ns, kind) pairs of the last pass. */
+int coex_ctx_set_trace(coex_ctx* ctx, int capacity);
+int coex_ctx_read_trace(coex_ctx* ctx, uint64_t* out_pairs, int64_t cap, int64_t* n);
+
 /* ---- tensors (eager side) ---- */
 int coex_tensor_put(coex_ctx* ctx, int ndim, const int64_t* shape, const double* data, int64_t* id);
 int coex_tensor_synth(coex_ctx* ctx, uint64_t state, int ndim, const int64_t* shape, int64_t* id);

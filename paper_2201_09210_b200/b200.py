@@ -60,6 +60,8 @@ SIGNATURES = {
     "coex_ctx_event_elapsed": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int, _DP]),
     "coex_exec_op_timed": (ctypes.c_int, [_P, ctypes.c_int, ctypes.POINTER(CoexAttrs), ctypes.c_int, _I64P,
                                           ctypes.c_int, _DP]),
+    "coex_ctx_set_trace": (ctypes.c_int, [_P, ctypes.c_int]),
+    "coex_ctx_read_trace": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_uint64), _I64, _I64P]),
     "coex_tensor_put": (ctypes.c_int, [_P, ctypes.c_int, _I64P, _DP, _I64P]),
     "coex_tensor_synth": (ctypes.c_int, [_P, ctypes.c_uint64, ctypes.c_int, _I64P, _I64P]),
     "coex_tensor_get": (ctypes.c_int, [_P, _I64, _DP, _I64, _IP, _I64P]),
@@ -198,6 +200,22 @@ class B200Backend:
         ms = ctypes.c_double()
         _check(self.lib.coex_ctx_event_elapsed(self.ctx, a, b, ctypes.byref(ms)))
         return ms.value
+
+    STAMP_KINDS = {0: "begin", 1: "elementwise", 2: "reduce", 3: "transpose", 4: "matmul", 5: "ptr-op",
+                   6: "decide", 7: "feed-wait", 8: "feed-fill", 9: "fetch", 10: "commit-gate", 11: "commit",
+                   12: "end", 13: "fused"}
+
+    def set_trace(self, capacity: int):
+        """Enable device-side per-kernel stamps (0 disables)."""
+        _check(self.lib.coex_ctx_set_trace(self.ctx, capacity))
+
+    def read_trace(self) -> list:
+        """[(t_ns, kind, after_wait)] of the last pass."""
+        cap = 8192
+        buf = (ctypes.c_uint64 * (2 * cap))()
+        n = ctypes.c_int64()
+        _check(self.lib.coex_ctx_read_trace(self.ctx, buf, cap, ctypes.byref(n)))
+        return [(buf[2 * i], buf[2 * i + 1] & 63, bool(buf[2 * i + 1] & 64)) for i in range(n.value)]
 
     def time_op(self, kind: OpKind, attrs: dict, values: list, reps: int = 50) -> float:
         """Average device ms of one launch of ``kind`` (CUDA events on the context stream)."""

@@ -31,6 +31,16 @@ struct DevState {
   unsigned long long stall_ns;    // time spent spinning on the host
   long long ops;                  // compute kernels executed (not skipped)
   unsigned long long t_begin;
+  unsigned long long* trace;      // optional per-kernel stamps: (globaltimer, kind) pairs
+  int trace_cap;
+  int trace_n;
+};
+
+// Kernel kinds recorded by stamp() (profiling: share of each kernel kind in a pass).
+enum StampKind {
+  SK_BEGIN = 0, SK_EW = 1, SK_REDUCE = 2, SK_TRANSPOSE = 3, SK_MATMUL = 4, SK_PTR = 5, SK_DECIDE = 6,
+  SK_FEED_WAIT = 7, SK_FEED_FILL = 8, SK_FETCH = 9, SK_GATE = 10, SK_COMMIT = 11, SK_END = 12,
+  SK_AFTER_WAIT = 64, SK_FUSED = 13
 };
 
 // Host <-> device rings in pinned, mapped host memory.
@@ -100,6 +110,17 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
+}
+
+__device__ __forceinline__ void stamp(DevState* ds, int kind) {
+  if (ds != nullptr && blockIdx.x == 0 && threadIdx.x == 0 && threadIdx.y == 0 && ds->trace != nullptr) {
+    int i = ds->trace_n;
+    if (i < ds->trace_cap) {
+      ds->trace[2 * i] = globaltimer();
+      ds->trace[2 * i + 1] = (unsigned long long)kind;
+      ds->trace_n = i + 1;
+    }
+  }
 }
 
 __host__ __device__ __forceinline__ unsigned long long seq_of(unsigned long long pass_id, long long idx) {
@@ -194,6 +215,7 @@ struct EwParams {
 
 template <typename T>
 __global__ void __launch_bounds__(256) k_elementwise(EwParams p) {
+  stamp(p.ds, SK_EW);
   if (skip(p.ds)) return;
   const T* a = res<T>(p.a);
   const T* b = (p.op <= EW_MUL) ? res<T>(p.b) : nullptr;
@@ -225,6 +247,7 @@ struct ReduceParams {
 // Parity path: one warp streams the data, lane 0 accumulates strictly in order.
 template <typename T>
 __global__ void __launch_bounds__(32) k_reduce_seq(ReduceParams p) {
+  stamp(p.ds, SK_REDUCE);
   if (skip(p.ds)) return;
   const T* a = res<T>(p.a);
   T* o = pick_out<T>(p.out, a, nullptr);
@@ -248,6 +271,7 @@ __global__ void __launch_bounds__(32) k_reduce_seq(ReduceParams p) {
 // Tolerance path (fp32 / bf16 contexts): warp-shuffle tree in double, one block.
 template <typename T>
 __global__ void __launch_bounds__(1024) k_reduce_tree(ReduceParams p) {
+  stamp(p.ds, SK_REDUCE);
   if (skip(p.ds)) return;
   const T* a = res<T>(p.a);
   T* o = pick_out<T>(p.out, a, nullptr);
@@ -281,6 +305,7 @@ struct TransposeParams {
 
 template <typename T>
 __global__ void __launch_bounds__(256) k_transpose(TransposeParams p) {
+  stamp(p.ds, SK_TRANSPOSE);
   if (skip(p.ds)) return;
   const T* a = res<T>(p.a);
   T* o = pick_out<T>(p.out, a, nullptr);
@@ -303,6 +328,7 @@ __global__ void __launch_bounds__(256) k_transpose(TransposeParams p) {
 // 2-D transpose through a padded shared-memory tile (coalesced on both sides).
 template <typename T>
 __global__ void __launch_bounds__(256) k_transpose2d(TransposeParams p) {
+  stamp(p.ds, SK_TRANSPOSE);
   if (skip(p.ds)) return;
   const T* a = res<T>(p.a);
   T* o = pick_out<T>(p.out, a, nullptr);
@@ -345,6 +371,7 @@ struct MatmulParams {
 
 template <typename T, int BM, int BN, int BK, int RM, int RN, bool EXACT>
 __global__ void __launch_bounds__((BM / RM) * (BN / RN)) k_matmul_simt(MatmulParams p) {
+  stamp(p.ds, SK_MATMUL);
   if (skip(p.ds)) return;
   const T* A = res<T>(p.a);
   const T* B = res<T>(p.b);
@@ -454,6 +481,7 @@ struct PtrParams {
   Out out;
 };
 __global__ void k_ptr(PtrParams p) {
+  stamp(p.ds, SK_PTR);
   if (skip(p.ds)) return;
   void* v;
   if (p.op == PTR_READ_VAR) {
@@ -562,6 +590,7 @@ struct DecideParams {
 
 __global__ void k_decide(DecideParams p) {
   DevState* ds = p.ds;
+  stamp(ds, SK_DECIDE);
   if (ds->cancelled) {
     cudaGraphSetConditional(p.handle, (unsigned)p.skip_value);
     return;
@@ -578,6 +607,7 @@ __global__ void k_decide(DecideParams p) {
     cudaGraphSetConditional(p.handle, (unsigned)p.skip_value);
     return;
   }
+  stamp(ds, SK_AFTER_WAIT | SK_DECIDE);
   int v = e->value;
   ds->dec_head = idx + 1;
   p.mb->dec_consumed = idx + 1;
@@ -594,6 +624,7 @@ struct GateParams {
 };
 __global__ void k_commit_gate(GateParams p) {
   DevState* ds = p.ds;
+  stamp(ds, SK_GATE);
   if (ds->cancelled) return;
   long long idx = ds->dec_head;
   const DecEntry* e = &p.mb->dec[idx % kDecCap];
@@ -603,6 +634,7 @@ __global__ void k_commit_gate(GateParams p) {
     ds->cancelled = 1;
     return;
   }
+  stamp(ds, SK_AFTER_WAIT | SK_GATE);
   ds->dec_head = idx + 1;
   p.mb->dec_consumed = idx + 1;
 }
@@ -630,6 +662,7 @@ struct FeedWaitParams {
 
 __global__ void k_feed_wait(FeedWaitParams p) {
   DevState* ds = p.ds;
+  stamp(ds, SK_FEED_WAIT);
   if (ds->cancelled) return;
   long long idx = ds->feed_head;
   const FeedEntry* e = &p.mb->feed[idx % kFeedCap];
@@ -641,6 +674,7 @@ __global__ void k_feed_wait(FeedWaitParams p) {
     ds->cancelled = 1;
     return;
   }
+  stamp(ds, SK_AFTER_WAIT | SK_FEED_WAIT);
   ds->feed_head = idx + 1;
   p.mb->feed_consumed = idx + 1;
   p.rec->type = e->type;
@@ -668,6 +702,7 @@ struct FeedFillParams {
 
 template <typename T>
 __global__ void __launch_bounds__(kSynthThreads) k_feed_fill(FeedFillParams p) {
+  stamp(p.ds, SK_FEED_FILL);
   if (skip(p.ds)) return;
   const int type = p.rec->type;
   T* o = (T*)p.buf;
@@ -713,6 +748,7 @@ struct FetchParams {
 
 __global__ void __launch_bounds__(256) k_fetch(FetchParams p) {
   DevState* ds = p.ds;
+  stamp(ds, SK_FETCH);
   if (ds->cancelled) return;
   __shared__ unsigned long long off;
   __shared__ long long idx;
@@ -766,8 +802,11 @@ __global__ void k_pass_begin(BeginParams p) {
     ds->fetch_bytes = 0;
     ds->stall_ns = 0;
     ds->ops = 0;
+    ds->trace_n = 0;
     ds->t_begin = globaltimer();
   }
+  __syncthreads();
+  stamp(ds, SK_BEGIN);
 }
 
 constexpr int kMaxCommit = 64;
@@ -780,26 +819,29 @@ struct CommitParams {
   void** var_spare;           // per-pass spare buffers provided by the host
   long long bytes[kMaxCommit];
 };
-// One block per assigned variable: copy the overlay value into the variable's
-// spare buffer and make it the committed value.
+// Grid (x: chunks, y: assigned variable): copy the overlay value into the
+// variable's spare buffer with 16-byte vector stores; block (0, v) flips the
+// committed pointer (nothing reads var_cur until the next pass).
 __global__ void __launch_bounds__(256) k_commit(CommitParams p) {
+  stamp(p.ds, SK_COMMIT);
   if (p.ds->cancelled) return;
-  const int j = blockIdx.x;
+  const int j = blockIdx.y;
   if (j >= p.n) return;
   const int v = p.var_index[j];
   const char* src = (const char*)p.var_ovl[v];
   if (src == nullptr) return;
   char* dst = (char*)p.var_spare[v];
   const long long bytes = p.bytes[j];
-  if ((bytes & 15) == 0) {
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long nth = (long long)gridDim.x * blockDim.x;
+  if ((bytes & 15) == 0 && ((uintptr_t)src & 15) == 0 && ((uintptr_t)dst & 15) == 0) {
     const uint4* s4 = (const uint4*)src;
     uint4* d4 = (uint4*)dst;
-    for (long long i = threadIdx.x; i < bytes / 16; i += blockDim.x) d4[i] = s4[i];
+    for (long long i = tid; i < bytes / 16; i += nth) d4[i] = s4[i];
   } else {
-    for (long long i = threadIdx.x; i < bytes; i += blockDim.x) dst[i] = src[i];
+    for (long long i = tid; i < bytes; i += nth) dst[i] = src[i];
   }
-  __syncthreads();
-  if (threadIdx.x == 0) p.var_cur[v] = dst;
+  if (blockIdx.x == 0 && threadIdx.x == 0) p.var_cur[v] = dst;
 }
 
 struct EndParams {
@@ -812,6 +854,7 @@ struct EndParams {
 __global__ void k_pass_end(EndParams p) {
   DevState* ds = p.ds;
   if (threadIdx.x != 0) return;
+  stamp(ds, SK_END);
   unsigned long long mask = 0;
   if (!ds->cancelled) {
     for (int i = 0; i < p.nvars && i < 64; ++i)

@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <cstddef>
 #include <chrono>
 #include <cstdio>
 #include <cstring>
@@ -138,6 +139,8 @@ struct coex_ctx {
   coex_prog* active = nullptr;
   unsigned long long pass_counter = 0;
   cudaEvent_t events[64] = {nullptr};
+  unsigned long long* d_trace = nullptr;
+  int trace_cap = 0;
 };
 
 namespace {
@@ -498,6 +501,34 @@ int coex_ctx_set_timeout(coex_ctx* c, double seconds) {
 }
 
 int64_t coex_ctx_kernel_count(coex_ctx* c) { return c ? c->kernel_count : 0; }
+
+int coex_ctx_set_trace(coex_ctx* c, int capacity) {
+  if (c->active) return fail(COEX_IN_FLIGHT_PASS, "set_trace during a pass");
+  CK(cudaStreamSynchronize(c->stream));
+  if (c->d_trace) {
+    cudaFree(c->d_trace);
+    c->d_trace = nullptr;
+  }
+  c->trace_cap = capacity > 0 ? capacity : 0;
+  if (c->trace_cap) CK(cudaMalloc(&c->d_trace, sizeof(unsigned long long) * 2 * c->trace_cap));
+  unsigned long long* tp = c->d_trace;
+  int cap = c->trace_cap;
+  CK(cudaMemcpy((char*)c->d_state + offsetof(DevState, trace), &tp, sizeof(tp), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy((char*)c->d_state + offsetof(DevState, trace_cap), &cap, sizeof(cap), cudaMemcpyHostToDevice));
+  return COEX_OK;
+}
+
+int coex_ctx_read_trace(coex_ctx* c, uint64_t* out, int64_t cap, int64_t* n) {
+  if (c->active) return fail(COEX_IN_FLIGHT_PASS, "read_trace during a pass");
+  int tn = 0;
+  CK(cudaStreamSynchronize(c->stream));
+  CK(cudaMemcpy(&tn, (char*)c->d_state + offsetof(DevState, trace_n), sizeof(int), cudaMemcpyDeviceToHost));
+  if (tn > c->trace_cap) tn = c->trace_cap;
+  int64_t m = tn < cap ? tn : cap;
+  if (m > 0) CK(cudaMemcpy(out, c->d_trace, sizeof(uint64_t) * 2 * m, cudaMemcpyDeviceToHost));
+  *n = m;
+  return COEX_OK;
+}
 
 int coex_ctx_event_record(coex_ctx* c, int slot) {
   if (slot < 0 || slot >= 64) return fail(COEX_INVALID, "event slot out of range");
@@ -1141,7 +1172,11 @@ int coex_prog_build(coex_ctx* c, const int64_t* plan, int64_t nwords, const doub
       cp.var_ovl = c->d_var_ovl;
       cp.var_spare = c->d_var_spare;
       Launch L;
-      L.set((void*)k_commit, dim3(cp.n), dim3(256), cp);
+      int64_t maxb = 0;
+      for (int i = 0; i < cp.n; ++i) maxb = cp.bytes[i] > maxb ? cp.bytes[i] : maxb;
+      int64_t gx = (maxb / 16 + 255) / 256;
+      gx = gx < 1 ? 1 : (gx > kNumSMs ? kNumSMs : gx);
+      L.set((void*)k_commit, dim3((unsigned)gx, cp.n), dim3(256), cp);
       rc = b.add_kernel(p->graph, &prev, L);
       if (rc) throw std::runtime_error(g_err);
     }

@@ -65,7 +65,7 @@ class OpEvent:
         return op_key(self.kind, self.attrs, self.loc, self.in_kinds())
 
     def in_kinds(self) -> tuple:
-        return tuple("h" if isinstance(r, Handle) else "e" for r in self.inputs)
+        return tuple(["h" if type(r) is Handle else "e" for r in self.inputs])
 
 
 @dataclass(frozen=True)
@@ -89,7 +89,7 @@ class StepEnd:
 
 
 def op_key(kind, attrs, loc, in_kinds) -> tuple:
-    return ("op", kind.value, canonical_attrs(attrs), loc.key(), tuple(in_kinds))
+    return ("op", kind.value, canonical_attrs(attrs) if attrs else (), (loc.stmt_id, loc.loop_path), in_kinds)
 
 
 # ---------------------------------------------------------------- the graph
@@ -122,11 +122,16 @@ class Node:
     feed_shapes: dict = field(default_factory=dict)   # input pos -> last observed fed shape
 
     def key(self) -> tuple:
-        if self.typ == "op":
-            return op_key(self.kind, self.attrs, self.loc, self.in_kinds)
-        if self.typ == "loop":
-            return ("loop", self.loop_id)
-        return (self.typ,)
+        k = self.__dict__.get("_key")
+        if k is None:
+            if self.typ == "op":
+                k = op_key(self.kind, self.attrs, self.loc, tuple(self.in_kinds))
+            elif self.typ == "loop":
+                k = ("loop", self.loop_id)
+            else:
+                k = (self.typ,)
+            self.__dict__["_key"] = k
+        return k
 
     def feed_slots(self) -> list:
         return [(self.id, p) for p, k in enumerate(self.in_kinds) if k == "e"]
@@ -140,6 +145,7 @@ class TraceGraph:
         self.nodes: dict = {}
         self.succ: dict = {}
         self.pred: dict = {}
+        self.kids: dict = {}       # node id -> {child key: child id} (child-distinctness makes it a map)
         self.start = self._add(Node(self.ids(), "start"))
         self.end = self._add(Node(self.ids(), "end"))
 
@@ -147,20 +153,19 @@ class TraceGraph:
         self.nodes[n.id] = n
         self.succ[n.id] = []
         self.pred[n.id] = []
+        self.kids[n.id] = {}
         return n.id
 
     def add_edge(self, a: int, b: int):
         self.succ[a].append(b)
         self.pred[b].append(a)
+        self.kids[a].setdefault(self.nodes[b].key(), b)
 
     def has_edge(self, a: int, b: int) -> bool:
         return b in self.succ[a]
 
     def child_with_key(self, a: int, key: tuple):
-        for c in self.succ[a]:
-            if self.nodes[c].key() == key:
-                return c
-        return None
+        return self.kids[a].get(key)
 
     def ancestors(self, n: int) -> set:
         seen = {n}
