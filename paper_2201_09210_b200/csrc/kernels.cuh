@@ -440,6 +440,152 @@ __global__ void __launch_bounds__((BM / RM) * (BN / RN)) k_matmul_simt(MatmulPar
   publish_late(p.out, C);
 }
 
+// Pipelined variant: STAGES-deep cp.async ring of k-panels so the global loads
+// of panel t+STAGES-1 overlap the (sequential-k) arithmetic on panel t.  Same
+// per-output accumulation order as k_matmul_simt -> bitwise identical.
+__device__ __forceinline__ void cp_async_el(void* smem, const void* gmem, bool valid, int bytes) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  int src = valid ? bytes : 0;
+  if (bytes == 8)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(s), "l"(gmem), "r"(src) : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(s), "l"(gmem), "r"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+template <typename T, int BM, int BN, int BK, int RM, int RN, bool EXACT, int STAGES>
+__global__ void __launch_bounds__((BM / RM) * (BN / RN)) k_matmul_pipe(MatmulParams p) {
+  stamp(p.ds, SK_MATMUL);
+  if (skip(p.ds)) return;
+  const T* A = res<T>(p.a);
+  const T* B = res<T>(p.b);
+  T* C = pick_out<T>(p.out, A, B);
+  publish_early(p.out, C);
+  count_op(p.ds);
+  constexpr int TX = BN / RN, TY = BM / RM, NT = TX * TY;
+  __shared__ __align__(16) T sA[STAGES][BK][BM + 1];
+  __shared__ __align__(16) T sB[STAGES][BK][BN + 1];
+  const int tx = threadIdx.x % TX, ty = threadIdx.x / TX;
+  const long long tiles_n = (p.N + BN - 1) / BN;
+  const long long tiles = ((p.M + BM - 1) / BM) * tiles_n;
+  const long long nk = (p.K + BK - 1) / BK;
+  const T* zero_src = A != nullptr ? A : B;
+  for (long long tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+    const long long m0 = (tile / tiles_n) * BM, n0 = (tile % tiles_n) * BN;
+    auto load = [&](int st, long long k0) {
+      for (int e = threadIdx.x; e < BM * BK; e += NT) {
+        int mm, kk;
+        if (p.trans_a) { mm = e % BM; kk = e / BM; } else { kk = e % BK; mm = e / BK; }
+        long long gm = m0 + mm, gk = k0 + kk;
+        bool ok = gm < p.M && gk < p.K;
+        const T* src = ok ? (p.trans_a ? A + gk * p.lda + gm : A + gm * p.lda + gk) : zero_src;
+        cp_async_el(&sA[st][kk][mm], src, ok, (int)sizeof(T));
+      }
+      for (int e = threadIdx.x; e < BK * BN; e += NT) {
+        int kk, nn;
+        if (p.trans_b) { kk = e % BK; nn = e / BK; } else { nn = e % BN; kk = e / BN; }
+        long long gk = k0 + kk, gn = n0 + nn;
+        bool ok = gk < p.K && gn < p.N;
+        const T* src = ok ? (p.trans_b ? B + gn * p.ldb + gk : B + gk * p.ldb + gn) : zero_src;
+        cp_async_el(&sB[st][kk][nn], src, ok, (int)sizeof(T));
+      }
+      cp_async_commit();
+    };
+    T acc[RM][RN];
+#pragma unroll
+    for (int i = 0; i < RM; ++i)
+#pragma unroll
+      for (int j = 0; j < RN; ++j) acc[i][j] = T(0);
+#pragma unroll
+    for (int st = 0; st < STAGES - 1; ++st) {
+      if (st < nk) load(st, st * BK);
+      else cp_async_commit();
+    }
+    for (long long t = 0; t < nk; ++t) {
+      cp_async_wait<STAGES - 2>();
+      __syncthreads();
+      if (t + STAGES - 1 < nk) load((int)((t + STAGES - 1) % STAGES), (t + STAGES - 1) * BK);
+      else cp_async_commit();
+      const int st = (int)(t % STAGES);
+      const long long k0 = t * BK;
+      auto step = [&](int kk) {
+        T av[RM], bv[RN];
+#pragma unroll
+        for (int i = 0; i < RM; ++i) av[i] = sA[st][kk][ty + i * TY];
+#pragma unroll
+        for (int j = 0; j < RN; ++j) bv[j] = sB[st][kk][tx + j * TX];
+#pragma unroll
+        for (int i = 0; i < RM; ++i)
+#pragma unroll
+          for (int j = 0; j < RN; ++j) {
+            if constexpr (EXACT) acc[i][j] = ew_apply(EW_ADD, acc[i][j], ew_apply(EW_MUL, av[i], bv[j]));
+            else acc[i][j] = fma(av[i], bv[j], acc[i][j]);
+          }
+      };
+      if (k0 + BK <= p.K) {
+#pragma unroll
+        for (int kk = 0; kk < BK; ++kk) step(kk);
+      } else {
+        const int kmax = (int)(p.K - k0);
+        for (int kk = 0; kk < kmax; ++kk) step(kk);
+      }
+    }
+    cp_async_wait<0>();
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < RM; ++i)
+#pragma unroll
+      for (int j = 0; j < RN; ++j) {
+        long long gm = m0 + ty + i * TY, gn = n0 + tx + j * TX;
+        if (gm < p.M && gn < p.N) C[gm * p.N + gn] = acc[i][j];
+      }
+  }
+  publish_late(p.out, C);
+}
+
+// Parity SUM / MEAN with shared-memory staging: all threads stream 2048-element
+// chunks into a double buffer while thread 0 adds the previous chunk strictly in
+// order (unrolled so loads run ahead of the dependent add chain).
+template <typename T>
+__global__ void __launch_bounds__(256) k_reduce_seq_smem(ReduceParams p) {
+  stamp(p.ds, SK_REDUCE);
+  if (skip(p.ds)) return;
+  constexpr int CH = 2048;
+  __shared__ T buf[2][CH];
+  const T* a = res<T>(p.a);
+  T* o = pick_out<T>(p.out, a, nullptr);
+  publish_early(p.out, o);
+  count_op(p.ds);
+  double acc = 0.0;
+  const long long nch = (p.n + CH - 1) / CH;
+  for (int i = threadIdx.x; i < CH; i += blockDim.x) buf[0][i] = (i < p.n) ? a[i] : T(0);
+  __syncthreads();
+  for (long long c = 0; c < nch; ++c) {
+    const int cur = (int)(c & 1);
+    if (c + 1 < nch) {
+      const long long base = (c + 1) * CH;
+      for (int i = threadIdx.x; i < CH; i += blockDim.x)
+        buf[cur ^ 1][i] = (base + i < p.n) ? a[base + i] : T(0);
+    }
+    if (threadIdx.x == 0) {
+      const int cnt = (int)min((long long)CH, p.n - c * CH);
+      int i = 0;
+      for (; i + 8 <= cnt; i += 8) {
+        double v0 = buf[cur][i], v1 = buf[cur][i + 1], v2 = buf[cur][i + 2], v3 = buf[cur][i + 3];
+        double v4 = buf[cur][i + 4], v5 = buf[cur][i + 5], v6 = buf[cur][i + 6], v7 = buf[cur][i + 7];
+        acc = __dadd_rn(acc, v0); acc = __dadd_rn(acc, v1); acc = __dadd_rn(acc, v2); acc = __dadd_rn(acc, v3);
+        acc = __dadd_rn(acc, v4); acc = __dadd_rn(acc, v5); acc = __dadd_rn(acc, v6); acc = __dadd_rn(acc, v7);
+      }
+      for (; i < cnt; ++i) acc = __dadd_rn(acc, (double)buf[cur][i]);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) o[0] = (T)(p.mean ? __ddiv_rn(acc, (double)p.n) : acc);
+  publish_late(p.out, o);
+}
+
 // ------------------------------------------------------------------ fill / copy / pointer ops
 struct FillParams {
   DevState* ds;
@@ -502,9 +648,12 @@ __global__ void k_ptr(PtrParams p) {
 // Each thread owns a run of kSynthRun consecutive elements; it jumps to the
 // run's first state with GF(2) matrices J_j = T^(kSynthRun * 2^j), walks the
 // run, and the block stores through shared memory so global writes coalesce.
-constexpr int kSynthRun = 16;
-constexpr int kSynthThreads = 256;
+constexpr int kSynthRun = 32;
+constexpr int kSynthThreads = 128;
 constexpr int kJumpBits = 40;
+// Jump matrices are stored as 4-bit lookup tables: tab[j][nibble][value] =
+// J_j applied to (value << 4*nibble); one application = 16 independent loads.
+constexpr int kJumpTabWords = 16 * 16;
 
 __device__ __forceinline__ unsigned long long xs_next(unsigned long long x) {
   x ^= x >> 12;
@@ -516,16 +665,23 @@ __device__ __forceinline__ double xs_unit_pm1(unsigned long long x) {
   unsigned long long r = (x * 0x2545F4914F6CDD1Dull) >> 11;
   return __dsub_rn(__dmul_rn(__dmul_rn((double)r, 0x1p-53), 2.0), 1.0);
 }
-__device__ __forceinline__ unsigned long long gf2_apply(const unsigned long long* cols, unsigned long long v) {
+__device__ __forceinline__ unsigned long long gf2_apply(const unsigned long long* tab, unsigned long long v) {
   unsigned long long r = 0;
-#pragma unroll 8
-  for (int b = 0; b < 64; ++b) r ^= cols[b] & (0ull - ((v >> b) & 1ull));
+#pragma unroll
+  for (int nib = 0; nib < 16; ++nib) r ^= __ldg(tab + nib * 16 + ((v >> (4 * nib)) & 15ull));
   return r;
+}
+// State at the start of run `run` (each run = kSynthRun draws) from s0.
+__device__ __forceinline__ unsigned long long jump_to_run(const unsigned long long* tabs, unsigned long long s,
+                                                          long long run) {
+  for (int j = 0; j < kJumpBits && (run >> j) != 0; ++j)
+    if ((run >> j) & 1) s = gf2_apply(tabs + kJumpTabWords * j, s);
+  return s;
 }
 
 struct SynthParams {
   DevState* ds;
-  const unsigned long long* jump;   // kJumpBits matrices x 64 columns
+  const unsigned long long* jump;   // kJumpBits nibble tables (kJumpTabWords each)
   const unsigned long long* state_ptr;  // graph mode: state from the feed record (null = use state)
   unsigned long long state;
   long long n;
@@ -541,10 +697,7 @@ __global__ void __launch_bounds__(kSynthThreads) k_synth(SynthParams p) {
   const unsigned long long s0 = p.state_ptr ? *p.state_ptr : p.state;
   const long long per_block = (long long)kSynthThreads * kSynthRun;
   for (long long base = (long long)blockIdx.x * per_block; base < p.n; base += (long long)gridDim.x * per_block) {
-    long long run = base / kSynthRun + threadIdx.x;
-    unsigned long long s = s0;
-    for (int j = 0; j < kJumpBits && (run >> j) != 0; ++j)
-      if ((run >> j) & 1) s = gf2_apply(p.jump + 64 * j, s);
+    unsigned long long s = jump_to_run(p.jump, s0, base / kSynthRun + threadIdx.x);
 #pragma unroll
     for (int i = 0; i < kSynthRun; ++i) {
       s = xs_next(s);
@@ -715,10 +868,7 @@ __global__ void __launch_bounds__(kSynthThreads) k_feed_fill(FeedFillParams p) {
     const unsigned long long s0 = p.rec->state;
     const long long per_block = (long long)kSynthThreads * kSynthRun;
     for (long long base = (long long)blockIdx.x * per_block; base < p.n; base += (long long)gridDim.x * per_block) {
-      long long run = base / kSynthRun + threadIdx.x;
-      unsigned long long s = s0;
-      for (int j = 0; j < kJumpBits && (run >> j) != 0; ++j)
-        if ((run >> j) & 1) s = gf2_apply(p.jump + 64 * j, s);
+      unsigned long long s = jump_to_run(p.jump, s0, base / kSynthRun + threadIdx.x);
 #pragma unroll
       for (int i = 0; i < kSynthRun; ++i) {
         s = xs_next(s);

@@ -309,7 +309,7 @@ int build_launch_t(coex_ctx* c, const OpSpec& s, Launch* L) {
       p.n = numel_of(s.in_ndim[0], s.in_shape[0]);
       p.mean = s.kind == COEX_MEAN;
       p.out = s.out;
-      if (is_f64(c)) L->set((void*)k_reduce_seq<T>, dim3(1), dim3(32), p);
+      if (is_f64(c)) L->set((void*)k_reduce_seq_smem<T>, dim3(1), dim3(256), p);
       else L->set((void*)k_reduce_tree<T>, dim3(1), dim3(1024), p);
       return COEX_OK;
     }
@@ -357,13 +357,13 @@ int build_launch_t(coex_ctx* c, const OpSpec& s, Launch* L) {
       const bool exact = is_f64(c);
       if (tiles_big >= kNumSMs) {
         dim3 g((unsigned)(tiles_big < kNumSMs * 4 ? tiles_big : kNumSMs * 4));
-        if (exact) L->set((void*)k_matmul_simt<T, 64, 64, 16, 4, 4, true>, g, dim3(256), p);
-        else L->set((void*)k_matmul_simt<T, 64, 64, 16, 4, 4, false>, g, dim3(256), p);
+        if (exact) L->set((void*)k_matmul_pipe<T, 64, 64, 16, 4, 4, true, 3>, g, dim3(256), p);
+        else L->set((void*)k_matmul_pipe<T, 64, 64, 16, 4, 4, false, 3>, g, dim3(256), p);
       } else {
         int64_t tiles = ((p.M + 15) / 16) * ((p.N + 15) / 16);
         dim3 g((unsigned)(tiles < kNumSMs * 8 ? (tiles < 1 ? 1 : tiles) : kNumSMs * 8));
-        if (exact) L->set((void*)k_matmul_simt<T, 16, 16, 32, 1, 1, true>, g, dim3(256), p);
-        else L->set((void*)k_matmul_simt<T, 16, 16, 32, 1, 1, false>, g, dim3(256), p);
+        if (exact) L->set((void*)k_matmul_pipe<T, 16, 16, 32, 1, 1, true, 4>, g, dim3(256), p);
+        else L->set((void*)k_matmul_pipe<T, 16, 16, 32, 1, 1, false, 4>, g, dim3(256), p);
       }
       return COEX_OK;
     }
@@ -444,15 +444,20 @@ int coex_ctx_create(int device, int precision, coex_ctx** out) {
   c->fetch_cap = (size_t)64 << 20;  // bytes
   CK(cudaHostAlloc((void**)&c->fetch_arena, c->fetch_cap, cudaHostAllocMapped));
   CK(cudaHostGetDevicePointer((void**)&c->d_fetch_arena, c->fetch_arena, 0));
-  // jump matrices J_j = T^(kSynthRun * 2^j)
-  std::vector<unsigned long long> jm(64 * kJumpBits), cur(64), tmp(64);
+  // jump matrices J_j = T^(kSynthRun * 2^j), stored as 4-bit lookup tables
+  std::vector<unsigned long long> jm(kJumpTabWords * kJumpBits), cur(64), tmp(64);
   for (int b = 0; b < 64; ++b) cur[b] = xs_step_host(1ull << b);
-  for (int s = 1; s < kSynthRun; s <<= 1) {      // T^16 by repeated squaring
+  for (int s = 1; s < kSynthRun; s <<= 1) {      // T^kSynthRun by repeated squaring
     mat_square(cur.data(), tmp.data());
     cur.swap(tmp);
   }
   for (int j = 0; j < kJumpBits; ++j) {
-    memcpy(&jm[64 * j], cur.data(), 64 * sizeof(unsigned long long));
+    for (int nib = 0; nib < 16; ++nib)
+      for (int v = 0; v < 16; ++v) {
+        unsigned long long r;
+        mat_apply(cur.data(), (unsigned long long)v << (4 * nib), &r);
+        jm[kJumpTabWords * j + nib * 16 + v] = r;
+      }
     mat_square(cur.data(), tmp.data());
     cur.swap(tmp);
   }
