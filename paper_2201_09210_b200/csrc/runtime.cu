@@ -357,8 +357,8 @@ int build_launch_t(coex_ctx* c, const OpSpec& s, Launch* L) {
       const bool exact = is_f64(c);
       if (tiles_big >= kNumSMs) {
         dim3 g((unsigned)(tiles_big < kNumSMs * 4 ? tiles_big : kNumSMs * 4));
-        if (exact) L->set((void*)k_matmul_pipe<T, 64, 64, 16, 4, 4, true, 3>, g, dim3(256), p);
-        else L->set((void*)k_matmul_pipe<T, 64, 64, 16, 4, 4, false, 3>, g, dim3(256), p);
+        if (exact) L->set((void*)k_matmul_pipe<T, 64, 64, 16, 4, 4, true, sizeof(T) == 8 ? 2 : 3>, g, dim3(256), p);
+        else L->set((void*)k_matmul_pipe<T, 64, 64, 16, 4, 4, false, sizeof(T) == 8 ? 2 : 3>, g, dim3(256), p);
       } else {
         int64_t tiles = ((p.M + 15) / 16) * ((p.N + 15) / 16);
         dim3 g((unsigned)(tiles < kNumSMs * 8 ? (tiles < 1 ? 1 : tiles) : kNumSMs * 8));
