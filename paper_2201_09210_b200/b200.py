@@ -328,7 +328,8 @@ class B200Program:
         hit = self.graphs.get(key)
         if hit is not None:
             return hit
-        plan = Planner(self.sp, self.tg, self.be.var_idx, vsh, self.feed_shape, self.be.esize).build()
+        plan = Planner(self.sp, self.tg, self.be.var_idx, vsh, self.feed_shape, self.be.esize,
+                       bf16=self.be.precision == "bf16").build()
         words = np.asarray(plan.words, dtype=np.int64)
         consts = np.asarray(plan.consts if plan.consts else [0.0], dtype=np.float64)
         handle = _P()

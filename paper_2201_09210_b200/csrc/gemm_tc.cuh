@@ -1,0 +1,247 @@
+// gemm_tc.cuh -- MATMUL on the 5th-generation tensor cores (tcgen05) for the
+// bf16 precision mode: C[M,N] (fp32) = A[M,K] . B[K,N], operands rounded to
+// bf16, fp32 accumulation in TMEM (reference op: tensor.py:228-236; tolerance
+// 2e-2 relative per BASELINE.json north_star).
+//
+// Two kernels per MatMul node:
+//   k_cvt_bf16  -- fp32 operand (read through its cell, optionally stored
+//                  transposed) -> bf16 K-major copy with a 16-byte-multiple row
+//                  pitch (the TMA source); B is written as B^T [N][K].
+//   k_gemm_tc   -- warp-specialised tcgen05 GEMM, one 128 x BN tile per CTA:
+//                  warp 0 = TMA producer (cp.async.bulk.tensor, SWIZZLE_128B),
+//                  warp 1 = TMEM allocator + single-thread MMA issuer
+//                  (tcgen05.mma.cta_group::1.kind::f16, M=128, N=BN, K=16),
+//                  warps 2-5 = epilogue (tcgen05.ld 32x32b -> fp32 stores).
+//                  4-stage smem ring with full/empty mbarriers; tcgen05.commit
+//                  frees a stage when its MMAs retire.
+#pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include "kernels.cuh"
+
+namespace coex {
+
+constexpr int TC_BM = 128;
+constexpr int TC_BN = 128;
+constexpr int TC_BK = 64;          // 64 bf16 = 128 B = one SWIZZLE_128B row
+constexpr int TC_STAGES = 4;
+constexpr int TC_THREADS = 192;
+constexpr int TC_A_BYTES = TC_BM * TC_BK * 2;
+constexpr int TC_B_BYTES = TC_BN * TC_BK * 2;
+constexpr int TC_SMEM = TC_STAGES * (TC_A_BYTES + TC_B_BYTES) + 1024 /*align*/ + 256 /*barriers*/;
+
+struct CvtParams {
+  DevState* ds;
+  In src[2];                 // fp32 operands
+  long long rows[2];         // rows of the K-major output (M for A, N for B)
+  long long K;
+  long long ld;              // padded K pitch (elements, multiple of 8)
+  int trans[2];              // 1: element (r, k) is src[k * rows + r]; 0: src[r * K + k]
+  __nv_bfloat16* dst[2];
+};
+
+// Operand conversion: grid.y selects the operand.
+__global__ void __launch_bounds__(256) k_cvt_bf16(CvtParams p) {
+  stamp(p.ds, SK_FUSED);
+  if (skip(p.ds)) return;
+  const int w = blockIdx.y;
+  const float* s = res<float>(p.src[w]);
+  __nv_bfloat16* d = p.dst[w];
+  const long long R = p.rows[w], K = p.K, ld = p.ld;
+  const long long n = R * ld;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const long long r = i / ld, k = i - r * ld;
+    float v = 0.f;
+    if (k < K) v = p.trans[w] ? s[k * R + r] : s[r * K + k];
+    d[i] = __float2bfloat16_rn(v);
+  }
+}
+
+struct TcGemmParams {
+  CUtensorMap tmA;           // bf16 [M][ld], box {64, 128}, SWIZZLE_128B
+  CUtensorMap tmB;           // bf16 [N][ld], box {64, BN}
+  DevState* ds;
+  In a, b;                   // original operands (ping-pong output choice only)
+  long long M, N, K;
+  Out out;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(a), "r"(parity)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::
+          "r"(smem_u32(dst)),
+      "l"((uint64_t)map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+// SMEM matrix descriptor, K-major, SWIZZLE_128B (cute UMMA::SmemDescriptor):
+// start>>4 [0,14), LBO=1 [16,30), SBO=1024>>4 [32,46), version=1 [46,48), layout=2 [61,64).
+__device__ __forceinline__ uint64_t smem_desc_k_sw128(const void* p) {
+  uint64_t d = 0;
+  d |= (uint64_t)((smem_u32(p) & 0x3FFFF) >> 4);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+
+// Instruction descriptor kind::f16: D=F32 (bit 4), A=BF16 (bits 7-9), B=BF16 (bits 10-12),
+// K-major A/B, N>>3 at [17,23), M>>4 at [24,29).
+__host__ __device__ constexpr uint32_t idesc_bf16_f32(int M, int N) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+__global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc(const __grid_constant__ TcGemmParams p) {
+  stamp(p.ds, SK_MATMUL);
+  if (skip(p.ds)) return;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  unsigned char* sA = smem;
+  unsigned char* sB = smem + TC_STAGES * TC_A_BYTES;
+  uint64_t* full = (uint64_t*)(sB + TC_STAGES * TC_B_BYTES);
+  uint64_t* empty = full + TC_STAGES;
+  uint64_t* tmem_full = empty + TC_STAGES;
+  uint32_t* tmem_slot = (uint32_t*)(tmem_full + 1);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const long long tiles_n = (p.N + TC_BN - 1) / TC_BN;
+  const int m0 = (int)((blockIdx.x / tiles_n) * TC_BM);
+  const int n0 = (int)((blockIdx.x % tiles_n) * TC_BN);
+  const int nk = (int)((p.K + TC_BK - 1) / TC_BK);
+
+  float* C = pick_out<float>(p.out, res<float>(p.a), res<float>(p.b));
+  publish_early(p.out, C);
+  count_op(p.ds);
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < TC_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tmem_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&p.tmA) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&p.tmB) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(TC_BN)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int kb = 0; kb < nk; ++kb) {
+        const int s = kb % TC_STAGES;
+        const uint32_t ph = (uint32_t)((kb / TC_STAGES) & 1);
+        mbar_wait(&empty[s], ph ^ 1u);
+        mbar_expect_tx(&full[s], TC_A_BYTES + TC_B_BYTES);
+        tma_load_2d(sA + s * TC_A_BYTES, &p.tmA, &full[s], kb * TC_BK, m0);
+        tma_load_2d(sB + s * TC_B_BYTES, &p.tmB, &full[s], kb * TC_BK, n0);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_bf16_f32(TC_BM, TC_BN);
+      for (int kb = 0; kb < nk; ++kb) {
+        const int s = kb % TC_STAGES;
+        const uint32_t ph = (uint32_t)((kb / TC_STAGES) & 1);
+        mbar_wait(&full[s], ph);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint64_t da = smem_desc_k_sw128(sA + s * TC_A_BYTES);
+        const uint64_t db = smem_desc_k_sw128(sB + s * TC_B_BYTES);
+#pragma unroll
+        for (int k = 0; k < TC_BK / 16; ++k) {
+          const uint32_t acc = (kb > 0 || k > 0) ? 1u : 0u;
+          // advance 16 elements (32 B) along K inside the 128-B swizzle atom
+          asm volatile(
+              "{\n\t.reg .pred p;\n\t"
+              "setp.ne.b32 p, %4, 0;\n\t"
+              "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
+              "l"(da + (uint64_t)(2 * k)), "l"(db + (uint64_t)(2 * k)), "r"(idesc), "r"(acc)
+              : "memory");
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                         smem_u32(&empty[s]))
+                     : "memory");
+      }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                       smem_u32(tmem_full))
+                   : "memory");
+    }
+  } else {
+    // epilogue: warps 2..5 own TMEM lanes 32*(warp%4) .. +31
+    const int lane_base = 32 * (warp % 4);
+    const int row = m0 + lane_base + lane;
+    if (nk > 0) {
+      mbar_wait(tmem_full, 0);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    }
+#pragma unroll 1
+    for (int c = 0; c < TC_BN; c += 16) {
+      uint32_t r[16];
+      if (nk > 0) {
+        const uint32_t taddr = tmem + ((uint32_t)lane_base << 16) + (uint32_t)c;
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+              "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      } else {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) r[i] = 0u;
+      }
+      if (row < p.M) {
+        float* dst = C + (long long)row * p.N + n0 + c;
+        const int valid = (int)min((long long)16, p.N - (n0 + c));
+        if (valid == 16 && (((uintptr_t)dst) & 15) == 0) {
+#pragma unroll
+          for (int i = 0; i < 16; i += 4)
+            *(float4*)(dst + i) = make_float4(__uint_as_float(r[i]), __uint_as_float(r[i + 1]),
+                                              __uint_as_float(r[i + 2]), __uint_as_float(r[i + 3]));
+        } else {
+          for (int i = 0; i < valid; ++i) dst[i] = __uint_as_float(r[i]);
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TC_BN) : "memory");
+  }
+  publish_late(p.out, C);
+}
+
+}  // namespace coex

@@ -27,6 +27,9 @@
 
 #include "../../include/coex_b200.h"
 #include "kernels.cuh"
+#include "gemm_tc.cuh"
+
+#include <cudaTypedefs.h>
 
 using namespace coex;
 
@@ -80,7 +83,7 @@ struct Launch {
   void* fn = nullptr;
   dim3 grid{1}, block{1};
   size_t smem = 0;
-  alignas(16) unsigned char params[2048];
+  alignas(64) unsigned char params[2048];
   size_t psize = 0;
   void* args[1];
   template <typename P>
@@ -279,9 +282,40 @@ struct OpSpec {
   int64_t attr_dims[COEX_MAX_RANK] = {0};
   double value = 0.0;
   int trans_a = 0, trans_b = 0;
+  void* scratch[2] = {nullptr, nullptr};   // bf16 K-major operand copies (tcgen05 path)
   Out out{};
   DevState* ds = nullptr;
 };
+
+// ---- TMA tensor maps (driver entry point; no -lcuda link dependency) ----
+PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (fn == nullptr) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
+  }
+  return fn;
+}
+
+int64_t bf16_pitch(int64_t K) { return (K + 7) / 8 * 8; }
+
+// bf16 [rows][pitch] K-major tile source: box {64, box_rows}, 128-byte swizzle, OOB -> 0.
+int make_tmap(CUtensorMap* m, void* base, int64_t rows, int64_t K, int box_rows) {
+  auto enc = tmap_encoder();
+  if (!enc) return fail(COEX_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {(cuuint64_t)(K > 0 ? K : 1), (cuuint64_t)(rows > 0 ? rows : 1)};
+  cuuint64_t strides[1] = {(cuuint64_t)bf16_pitch(K > 0 ? K : 1) * 2};
+  cuuint32_t box[2] = {(cuuint32_t)TC_BK, (cuuint32_t)box_rows};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base, dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(COEX_CUDA_ERROR, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  return COEX_OK;
+}
 
 template <typename T>
 int build_launch_t(coex_ctx* c, const OpSpec& s, Launch* L) {
@@ -340,6 +374,7 @@ int build_launch_t(coex_ctx* c, const OpSpec& s, Launch* L) {
       return COEX_OK;
     }
     case COEX_MATMUL: {
+      if (c->prec == COEX_BF16) return fail(COEX_INVALID, "bf16 matmul is lowered by build_launches");
       MatmulParams p{};
       p.ds = s.ds;
       p.a = s.in[0];
@@ -383,6 +418,66 @@ int build_launch_t(coex_ctx* c, const OpSpec& s, Launch* L) {
 
 int build_launch(coex_ctx* c, const OpSpec& s, Launch* L) {
   return is_f64(c) ? build_launch_t<double>(c, s, L) : build_launch_t<float>(c, s, L);
+}
+
+bool needs_scratch(const coex_ctx* c, int kind) { return c->prec == COEX_BF16 && kind == COEX_MATMUL; }
+
+void scratch_bytes(const OpSpec& s, size_t* a, size_t* b) {
+  const int64_t M = s.trans_a ? s.in_shape[0][1] : s.in_shape[0][0];
+  const int64_t K = s.trans_a ? s.in_shape[0][0] : s.in_shape[0][1];
+  const int64_t N = s.trans_b ? s.in_shape[1][0] : s.in_shape[1][1];
+  *a = (size_t)(M > 0 ? M : 1) * bf16_pitch(K > 0 ? K : 1) * 2;
+  *b = (size_t)(N > 0 ? N : 1) * bf16_pitch(K > 0 ? K : 1) * 2;
+}
+
+// One op -> one or two launches (bf16 MatMul = operand conversion + tcgen05 GEMM).
+int build_launches(coex_ctx* c, const OpSpec& s, Launch* L, int* nL) {
+  if (!needs_scratch(c, s.kind)) {
+    *nL = 1;
+    return build_launch(c, s, L);
+  }
+  const int64_t M = s.trans_a ? s.in_shape[0][1] : s.in_shape[0][0];
+  const int64_t K = s.trans_a ? s.in_shape[0][0] : s.in_shape[0][1];
+  const int64_t N = s.trans_b ? s.in_shape[1][0] : s.in_shape[1][1];
+  CvtParams cv{};
+  cv.ds = s.ds;
+  cv.src[0] = s.in[0];
+  cv.src[1] = s.in[1];
+  cv.rows[0] = M;
+  cv.rows[1] = N;
+  cv.K = K;
+  cv.ld = bf16_pitch(K);
+  cv.trans[0] = s.trans_a ? 1 : 0;     // A stored [K][M] when folded from a transpose
+  cv.trans[1] = s.trans_b ? 0 : 1;     // B stored [K][N] -> B^T read; folded: stored [N][K]
+  cv.dst[0] = (__nv_bfloat16*)s.scratch[0];
+  cv.dst[1] = (__nv_bfloat16*)s.scratch[1];
+  const int64_t big = (M > N ? M : N) * cv.ld;
+  dim3 g = grid_for(big);
+  g.y = 2;
+  L[0].set((void*)k_cvt_bf16, g, dim3(256), cv);
+  TcGemmParams gp;
+  memset(&gp, 0, sizeof(gp));
+  int rc = make_tmap(&gp.tmA, s.scratch[0], M, K, TC_BM);
+  if (rc) return rc;
+  rc = make_tmap(&gp.tmB, s.scratch[1], N, K, TC_BN);
+  if (rc) return rc;
+  gp.ds = s.ds;
+  gp.a = s.in[0];
+  gp.b = s.in[1];
+  gp.M = M;
+  gp.N = N;
+  gp.K = K;
+  gp.out = s.out;
+  const int64_t tiles = ((M + TC_BM - 1) / TC_BM) * ((N + TC_BN - 1) / TC_BN);
+  L[1].set((void*)k_gemm_tc, dim3((unsigned)(tiles > 0 ? tiles : 1)), dim3(TC_THREADS), gp);
+  L[1].smem = TC_SMEM;
+  static bool attr = false;
+  if (!attr) {
+    CK(cudaFuncSetAttribute((const void*)k_gemm_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM));
+    attr = true;
+  }
+  *nL = 2;
+  return COEX_OK;
 }
 
 int launch_now(coex_ctx* c, Launch& L) {
@@ -685,9 +780,18 @@ int coex_exec_op(coex_ctx* c, int kind, const coex_attrs* attrs, int nin, const 
   }
   s.out.buf[0] = o.buf->ptr;
   if (o.numel > 0 || kind == COEX_SUM || kind == COEX_MEAN) {
-    Launch L;
-    rc = build_launch(c, s, &L);
-    if (rc == COEX_OK) rc = launch_now(c, L);
+    if (needs_scratch(c, kind)) {
+      size_t ba, bb;
+      scratch_bytes(s, &ba, &bb);
+      CK(cudaMallocAsync(&s.scratch[0], ba, c->stream));
+      CK(cudaMallocAsync(&s.scratch[1], bb, c->stream));
+    }
+    Launch L[2];
+    int nL = 0;
+    rc = build_launches(c, s, L, &nL);
+    for (int i = 0; rc == COEX_OK && i < nL; ++i) rc = launch_now(c, L[i]);
+    if (s.scratch[0]) cudaFreeAsync(s.scratch[0], c->stream);
+    if (s.scratch[1]) cudaFreeAsync(s.scratch[1], c->stream);
     if (rc) {
       release(c, o.buf);
       return rc;
@@ -721,20 +825,31 @@ int coex_exec_op_timed(coex_ctx* c, int kind, const coex_attrs* attrs, int nin, 
     s.value = attrs->value;
   }
   s.out.buf[0] = o->buf->ptr;
-  Launch L;
-  rc = build_launch(c, s, &L);
+  if (needs_scratch(c, kind)) {
+    size_t ba, bb;
+    scratch_bytes(s, &ba, &bb);
+    CK(cudaMallocAsync(&s.scratch[0], ba, c->stream));
+    CK(cudaMallocAsync(&s.scratch[1], bb, c->stream));
+  }
+  Launch L[2];
+  int nL = 0;
+  rc = build_launches(c, s, L, &nL);
   if (rc) return rc;
   rc = coex_ctx_event_record(c, 62);
   if (rc) return rc;
   for (int r = 0; r < reps; ++r) {
-    rc = launch_now(c, L);
-    if (rc) return rc;
+    for (int i = 0; i < nL; ++i) {
+      rc = launch_now(c, L[i]);
+      if (rc) return rc;
+    }
   }
   rc = coex_ctx_event_record(c, 63);
   if (rc) return rc;
   double ms = 0;
   rc = coex_ctx_event_elapsed(c, 62, 63, &ms);
   *avg_ms = ms / reps;
+  if (s.scratch[0]) cudaFreeAsync(s.scratch[0], c->stream);
+  if (s.scratch[1]) cudaFreeAsync(s.scratch[1], c->stream);
   coex_tensor_free(c, out);
   return rc;
 }
@@ -801,7 +916,7 @@ namespace {
 
 enum PlanTag : int64_t { T_SEQ = 1, T_OP = 2, T_PTR = 3, T_FEED = 4, T_FETCH = 5, T_SWITCH = 6, T_WHILE = 7 };
 constexpr int64_t kPlanMagic = 0xC0E8B200;
-constexpr int64_t kPlanVersion = 1;
+constexpr int64_t kPlanVersion = 2;
 
 struct FeedSlot {
   int64_t slot;
@@ -928,12 +1043,19 @@ struct Builder {
         memcpy(&s.value, &vbits, 8);
         s.trans_a = (int)next();
         s.trans_b = (int)next();
+        s.scratch[0] = buf(next());
+        s.scratch[1] = buf(next());
         read_out(s.out);
-        Launch L;
-        int rc = build_launch(c, s, &L);
+        Launch L[2];
+        int nL = 0;
+        int rc = build_launches(c, s, L, &nL);
         if (rc) return rc;
-        p->n_compute++;
-        return add_kernel(g, prev, L);
+        p->n_compute += nL;
+        for (int i = 0; i < nL; ++i) {
+          rc = add_kernel(g, prev, L[i]);
+          if (rc) return rc;
+        }
+        return COEX_OK;
       }
       case T_PTR: {
         PtrParams q{};

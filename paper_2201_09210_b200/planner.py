@@ -31,7 +31,7 @@ from .graph_gen import ExecOp, InputFeed, OutputFetch, SwitchCase, SymProgram, U
 from .tensor import OpKind, infer_shape, shape_size
 
 MAGIC = 0xC0E8B200
-VERSION = 1
+VERSION = 2
 T_SEQ, T_OP, T_PTR, T_FEED, T_FETCH, T_SWITCH, T_WHILE = 1, 2, 3, 4, 5, 6, 7
 PTR_ALIAS, PTR_READ_VAR, PTR_ASSIGN_VAR = 0, 1, 2
 MAX_RANK = 8
@@ -82,7 +82,9 @@ class Plan:
 
 
 class Planner:
-    def __init__(self, sp: SymProgram, tg, var_index: dict, var_shapes: dict, feed_shapes: dict, esize: int):
+    def __init__(self, sp: SymProgram, tg, var_index: dict, var_shapes: dict, feed_shapes: dict, esize: int,
+                 bf16: bool = False):
+        self.bf16 = bf16
         self.sp = sp
         self.tg = tg
         self.var_index = var_index
@@ -180,6 +182,8 @@ class Planner:
         def new_buf(nbytes):
             bufs.append(max(int(nbytes), 16))
             return len(bufs) - 1
+
+        self.new_buf = new_buf
 
         cell_init: list = []
 
@@ -353,6 +357,11 @@ class Planner:
             word += [len(s)] + _pad(s)
         word += [len(out_shape)] + _pad(out_shape)
         word += [len(attr_dims)] + _pad(attr_dims) + [_f64_bits(0.0), trans[0], trans[1]]
+        if k is OpKind.MATMUL and self.bf16:
+            pitch = (kk + 7) // 8 * 8
+            word += [self.new_buf(max(m, 1) * pitch * 2), self.new_buf(max(nn, 1) * pitch * 2)]
+        else:
+            word += [-1, -1]
         word += out_words(nid, late)
         return [word]
 
