@@ -524,7 +524,23 @@ __global__ void __launch_bounds__((BM / RM) * (BN / RN)) k_matmul_pipe(MatmulPar
             else acc[i][j] = fma(av[i], bv[j], acc[i][j]);
           }
       };
-      if (k0 + BK <= p.K) {
+      if constexpr (RM == 1 && RN == 1) {
+        // One output per thread: form all BK products first (independent, fully
+        // pipelined), then add them in k order.  Zero-filled padding contributes
+        // +0 products, and the accumulator (started at +0.0) can never be -0.0,
+        // so adding them is exact -- same bits as the reference's k loop.
+        T prod[BK];
+#pragma unroll
+        for (int kk = 0; kk < BK; ++kk) {
+          if constexpr (EXACT) prod[kk] = ew_apply(EW_MUL, sA[st][kk][ty], sB[st][kk][tx]);
+          else prod[kk] = sA[st][kk][ty] * sB[st][kk][tx];
+        }
+#pragma unroll
+        for (int kk = 0; kk < BK; ++kk) {
+          if constexpr (EXACT) acc[0][0] = ew_apply(EW_ADD, acc[0][0], prod[kk]);
+          else acc[0][0] += prod[kk];
+        }
+      } else if (k0 + BK <= p.K) {
 #pragma unroll
         for (int kk = 0; kk < BK; ++kk) step(kk);
       } else {

@@ -49,8 +49,10 @@ steps 5 {
   let x = input("x", [200, 96])
   let h = matmul(x, w)
   let g = matmul(transpose(x), h)
-  w = sub(w, mul(matmul(g, transpose(transpose(w))), 0.0001))
+  let z = matmul(h, transpose(w))
+  w = sub(w, mul(g, 0.0001))
   print(sum(h))
+  print(mean(z))
 }
 """
     res = {}
