@@ -602,6 +602,147 @@ __global__ void __launch_bounds__(256) k_reduce_seq_smem(ReduceParams p) {
   publish_late(p.out, o);
 }
 
+// ------------------------------------------------------------------ fused chains
+// A run of consecutive elementwise ExecOps of one element count, optionally
+// closed by SUM / MEAN, executed as ONE kernel: a micro-op program interpreted
+// per element over a small register file.  Each op rounds exactly like its
+// standalone kernel (ew_apply), and every element is read and written by one
+// thread in program order, so fusion is bit-identical to the unfused sequence
+// (in-place reuse of a node's buffer is safe element by element).
+constexpr int kChainIn = 8, kChainOps = 16, kChainOut = 8, kChainPub = 4, kChainRegs = 16;
+
+struct ChainOp {
+  unsigned char op, dst, a, b;   // a, b: < 16 register, >= 16 input (x - 16)
+};
+struct ChainParams {
+  DevState* ds;
+  long long n;
+  int nin, nops, nout;
+  In in[kChainIn];
+  unsigned char in_scalar[kChainIn];
+  ChainOp ops[kChainOps];
+  unsigned char out_reg[kChainOut];
+  void* out_buf[kChainOut];
+  unsigned char npub[kChainOut];
+  void** pub[kChainOut][kChainPub];
+  unsigned int* late;            // non-null: publish after every block read its inputs
+  int red;                       // 0 = none, 1 = SUM, 2 = MEAN of register red_reg
+  int red_reg;
+  void* red_buf;
+  int red_npub;
+  void** red_pub[kChainPub];
+};
+
+template <typename T>
+__device__ __forceinline__ T chain_src(const ChainParams& p, const T* r, const T* const* ip, const T* sv,
+                                       int x, long long i) {
+  if (x < kChainRegs) return r[x];
+  const int k = x - kChainRegs;
+  return p.in_scalar[k] ? sv[k] : ip[k][i];
+}
+
+template <typename T>
+__device__ __forceinline__ void chain_eval(const ChainParams& p, T* r, const T* const* ip, const T* sv, long long i) {
+  for (int k = 0; k < p.nops; ++k) {
+    const ChainOp o = p.ops[k];
+    r[o.dst] = ew_apply((int)o.op, chain_src(p, r, ip, sv, o.a, i),
+                        o.op <= EW_MUL ? chain_src(p, r, ip, sv, o.b, i) : T(0));
+  }
+}
+
+__device__ __forceinline__ void chain_publish(const ChainParams& p) {
+  for (int j = 0; j < p.nout; ++j)
+    for (int q = 0; q < p.npub[j]; ++q) *p.pub[j][q] = p.out_buf[j];
+  if (p.red)
+    for (int q = 0; q < p.red_npub; ++q) *p.red_pub[q] = p.red_buf;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_chain(ChainParams p) {
+  stamp(p.ds, SK_FUSED);
+  if (skip(p.ds)) return;
+  const T* ip[kChainIn];
+  T sv[kChainIn];
+  for (int k = 0; k < p.nin; ++k) {
+    ip[k] = res<T>(p.in[k]);
+    sv[k] = p.in_scalar[k] ? ip[k][0] : T(0);
+  }
+  if (p.late == nullptr && blockIdx.x == 0 && threadIdx.x == 0) chain_publish(p);
+  count_op(p.ds);
+  T r[kChainRegs];
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < p.n; i += stride) {
+    chain_eval(p, r, ip, sv, i);
+    for (int j = 0; j < p.nout; ++j) ((T*)p.out_buf[j])[i] = r[p.out_reg[j]];
+  }
+  if (p.late != nullptr) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      if (atomicAdd(p.late, 1u) == gridDim.x - 1) {
+        chain_publish(p);
+        *p.late = 0u;
+      }
+    }
+  }
+}
+
+// Chain closed by SUM / MEAN: one block evaluates the chain in 2048-element
+// chunks into shared memory; the parity path (EXACT) adds in row-major order on
+// one thread, the tolerance path reduces with warp shuffles in double.
+template <typename T, bool EXACT>
+__global__ void __launch_bounds__(256) k_chain_reduce(ChainParams p) {
+  stamp(p.ds, SK_FUSED);
+  if (skip(p.ds)) return;
+  constexpr int CH = 2048;
+  __shared__ T vals[CH];
+  __shared__ double part[8];
+  const T* ip[kChainIn];
+  T sv[kChainIn];
+  for (int k = 0; k < p.nin; ++k) {
+    ip[k] = res<T>(p.in[k]);
+    sv[k] = p.in_scalar[k] ? ip[k][0] : T(0);
+  }
+  count_op(p.ds);
+  T r[kChainRegs];
+  double acc = 0.0;
+  for (long long base = 0; base < p.n; base += CH) {
+    const int cnt = (int)min((long long)CH, p.n - base);
+    for (int t = threadIdx.x; t < cnt; t += blockDim.x) {
+      const long long i = base + t;
+      chain_eval(p, r, ip, sv, i);
+      for (int j = 0; j < p.nout; ++j) ((T*)p.out_buf[j])[i] = r[p.out_reg[j]];
+      vals[t] = r[p.red_reg];
+    }
+    __syncthreads();
+    if constexpr (EXACT) {
+      if (threadIdx.x == 0) {
+        int t = 0;
+        for (; t + 8 <= cnt; t += 8) {
+          double v0 = vals[t], v1 = vals[t + 1], v2 = vals[t + 2], v3 = vals[t + 3];
+          double v4 = vals[t + 4], v5 = vals[t + 5], v6 = vals[t + 6], v7 = vals[t + 7];
+          acc = __dadd_rn(acc, v0); acc = __dadd_rn(acc, v1); acc = __dadd_rn(acc, v2); acc = __dadd_rn(acc, v3);
+          acc = __dadd_rn(acc, v4); acc = __dadd_rn(acc, v5); acc = __dadd_rn(acc, v6); acc = __dadd_rn(acc, v7);
+        }
+        for (; t < cnt; ++t) acc = __dadd_rn(acc, (double)vals[t]);
+      }
+    } else {
+      double s = 0.0;
+      for (int t = threadIdx.x; t < cnt; t += blockDim.x) s += (double)vals[t];
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = s;
+      __syncthreads();
+      if (threadIdx.x == 0)
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) acc += part[w];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    ((T*)p.red_buf)[0] = (T)(p.red == 2 ? __ddiv_rn(acc, (double)p.n) : acc);
+    chain_publish(p);     // single block: every input has been read
+  }
+}
+
 // ------------------------------------------------------------------ fill / copy / pointer ops
 struct FillParams {
   DevState* ds;

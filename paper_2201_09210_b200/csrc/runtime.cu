@@ -914,7 +914,7 @@ int coex_var_rollback(coex_ctx* c) {
 // =============================================================== symbolic programs
 namespace {
 
-enum PlanTag : int64_t { T_SEQ = 1, T_OP = 2, T_PTR = 3, T_FEED = 4, T_FETCH = 5, T_SWITCH = 6, T_WHILE = 7 };
+enum PlanTag : int64_t { T_SEQ = 1, T_OP = 2, T_PTR = 3, T_FEED = 4, T_FETCH = 5, T_SWITCH = 6, T_WHILE = 7, T_CHAIN = 8 };
 constexpr int64_t kPlanMagic = 0xC0E8B200;
 constexpr int64_t kPlanVersion = 2;
 
@@ -1056,6 +1056,57 @@ struct Builder {
           if (rc) return rc;
         }
         return COEX_OK;
+      }
+      case T_CHAIN: {
+        ChainParams q;
+        memset(&q, 0, sizeof(q));
+        q.ds = c->d_state;
+        q.n = next();
+        q.red = (int)next();
+        q.red_reg = (int)next();
+        q.red_buf = buf(next());
+        q.red_npub = (int)next();
+        for (int i = 0; i < kChainPub; ++i) {
+          int64_t ci = next();
+          q.red_pub[i] = i < q.red_npub ? cell(ci) : nullptr;
+        }
+        const int64_t late = next();
+        q.nin = (int)next();
+        for (int i = 0; i < kChainIn; ++i) {
+          int64_t ci = next();
+          q.in[i].cell = (i < q.nin) ? cell(ci) : nullptr;
+          q.in[i].direct = nullptr;
+          q.in_scalar[i] = (unsigned char)next();
+        }
+        q.nops = (int)next();
+        for (int i = 0; i < kChainOps; ++i) {
+          q.ops[i].op = (unsigned char)next();
+          q.ops[i].dst = (unsigned char)next();
+          q.ops[i].a = (unsigned char)next();
+          q.ops[i].b = (unsigned char)next();
+        }
+        q.nout = (int)next();
+        for (int j = 0; j < kChainOut; ++j) {
+          q.out_reg[j] = (unsigned char)next();
+          q.out_buf[j] = buf(next());
+          q.npub[j] = (unsigned char)next();
+          for (int i = 0; i < kChainPub; ++i) {
+            int64_t ci = next();
+            q.pub[j][i] = (j < q.nout && i < q.npub[j]) ? cell(ci) : nullptr;
+          }
+        }
+        if (q.nin > kChainIn || q.nops > kChainOps || q.nout > kChainOut) throw std::runtime_error("chain too wide");
+        q.late = late ? p->late + (n_late++) : nullptr;
+        Launch L;
+        if (q.red) {
+          if (is_f64(c)) L.set((void*)k_chain_reduce<double, true>, dim3(1), dim3(256), q);
+          else L.set((void*)k_chain_reduce<float, false>, dim3(1), dim3(256), q);
+        } else {
+          if (is_f64(c)) L.set((void*)k_chain<double>, grid_for(q.n), dim3(256), q);
+          else L.set((void*)k_chain<float>, grid_for(q.n), dim3(256), q);
+        }
+        p->n_compute++;
+        return add_kernel(g, prev, L);
       }
       case T_PTR: {
         PtrParams q{};

@@ -32,12 +32,14 @@ from .tensor import OpKind, infer_shape, shape_size
 
 MAGIC = 0xC0E8B200
 VERSION = 2
-T_SEQ, T_OP, T_PTR, T_FEED, T_FETCH, T_SWITCH, T_WHILE = 1, 2, 3, 4, 5, 6, 7
+T_SEQ, T_OP, T_PTR, T_FEED, T_FETCH, T_SWITCH, T_WHILE, T_CHAIN = 1, 2, 3, 4, 5, 6, 7, 8
 PTR_ALIAS, PTR_READ_VAR, PTR_ASSIGN_VAR = 0, 1, 2
 MAX_RANK = 8
 MAX_PUB = 6
 COMPUTE = {OpKind.MATMUL, OpKind.ADD, OpKind.SUB, OpKind.MUL, OpKind.NEG, OpKind.RELU,
            OpKind.SIGMOID, OpKind.SUM, OpKind.MEAN, OpKind.TRANSPOSE}
+EW_CODE = {OpKind.ADD: 0, OpKind.SUB: 1, OpKind.MUL: 2, OpKind.NEG: 3, OpKind.RELU: 4, OpKind.SIGMOID: 5}
+CHAIN_IN, CHAIN_OPS, CHAIN_OUT, CHAIN_PUB, CHAIN_REGS = 8, 16, 8, 4, 16
 
 
 def slot_code(slot: tuple) -> int:
@@ -83,8 +85,9 @@ class Plan:
 
 class Planner:
     def __init__(self, sp: SymProgram, tg, var_index: dict, var_shapes: dict, feed_shapes: dict, esize: int,
-                 bf16: bool = False):
+                 bf16: bool = False, fuse: bool = True):
         self.bf16 = bf16
+        self.fuse = fuse
         self.sp = sp
         self.tg = tg
         self.var_index = var_index
@@ -261,13 +264,34 @@ class Planner:
         def ptr_item(op, nid, cin, var_idx, shape_id):
             return [T_PTR, op, nid, cin, var_idx, shape_id] + out_words(nid, False)
 
+        self.consumers = consumers
+        self.n_chains = 0
+        self.chain_lates = 0
+
+        def feed_item(x):
+            shp = tuple(self.feed_shapes[x.slot])
+            return ([T_FEED, slot_code(x.slot), shape_size(shp), len(shp)] + _pad(shp)
+                    + [slot_buf[x.slot], slot_cell[x.slot], slot_rec[x.slot]])
+
         def emit(insts) -> list:
             items = []
-            for x in insts:
+            if self.fuse:
+                segs = self._segments(insts, shapes, folded)
+            else:
+                segs = [("inst", x) for x in insts]
+            for kind_, seg in segs:
+                if kind_ == "chain":
+                    run, feeds = seg
+                    for f in feeds:
+                        items.append(feed_item(f))
+                    try:
+                        items.append(self._chain_item(run, shapes, in_cell, node_buf, pubs, multi, n_compute))
+                    except _TooWide:
+                        items.extend(emit(run))
+                    continue
+                x = seg
                 if isinstance(x, InputFeed):
-                    shp = tuple(self.feed_shapes[x.slot])
-                    items.append([T_FEED, slot_code(x.slot), shape_size(shp), len(shp)] + _pad(shp)
-                                 + [slot_buf[x.slot], slot_cell[x.slot], slot_rec[x.slot]])
+                    items.append(feed_item(x))
                 elif isinstance(x, OutputFetch):
                     shp = shapes[x.node_id]
                     items.append([T_FETCH, x.node_id, vcell[x.node_id], shape_size(shp), len(shp)] + _pad(shp))
@@ -296,7 +320,7 @@ class Planner:
         body = seq(self.sp.body)
         w += [MAGIC, VERSION, len(bufs)] + bufs
         w += [len(cell_init)] + cell_init
-        w += [len(slot_rec), late_count[0]]
+        w += [len(slot_rec), late_count[0] + self.chain_lates]
         w += [len(fills)]
         for b0, n, ci in fills:
             w += [b0, n, ci]
@@ -365,6 +389,144 @@ class Planner:
         word += out_words(nid, late)
         return [word]
 
+    # ------------------------------------------------------------ fusion
+    def _segments(self, insts, shapes, folded) -> list:
+        """Split one instruction list into fused runs and plain instructions.  A run is a
+        maximal sequence of same-size elementwise ExecOps (InputFeeds in between are
+        hoisted in order), optionally closed by SUM / MEAN of a value computed in the run;
+        an OutputFetch or any other instruction ends it."""
+        segs: list = []
+        run: list = []
+        feeds: list = []
+        n_run = [None]
+
+        def flush():
+            if len(run) >= 2:
+                segs.append(("chain", (list(run), list(feeds))))
+            else:
+                segs.extend(("inst", f) for f in feeds)
+                segs.extend(("inst", r) for r in run)
+            run.clear()
+            feeds.clear()
+            n_run[0] = None
+
+        def in_run(nid):
+            return any(r.node_id == nid for r in run)
+
+        for x in insts:
+            if isinstance(x, InputFeed) and run:
+                feeds.append(x)
+                continue
+            if isinstance(x, ExecOp) and x.kind in EW_CODE and x.node_id not in folded:
+                n = shape_size(shapes[x.node_id])
+                if run and n != n_run[0] or len(run) >= CHAIN_OPS:
+                    flush()
+                if not run:
+                    n_run[0] = n
+                run.append(x)
+                continue
+            if (isinstance(x, ExecOp) and x.kind in (OpKind.SUM, OpKind.MEAN) and run
+                    and not x.inputs[0].fed and len(x.inputs[0].cands) == 1 and in_run(x.inputs[0].cands[0])
+                    and len(run) < CHAIN_OPS):
+                run.append(x)
+                flush()
+                continue
+            flush()
+            segs.append(("inst", x))
+        flush()
+        return segs
+
+    def _chain_item(self, run, shapes, in_cell, node_buf, pubs, multi, n_compute) -> list:
+        red = run[-1] if run[-1].kind in (OpKind.SUM, OpKind.MEAN) else None
+        ew = run[:-1] if red is not None else run
+        n = shape_size(shapes[ew[0].node_id])
+        inputs: list = []          # (cell, scalar)
+        ops: list = []
+        reg_of: dict = {}          # position in run -> register
+
+        def src(pos, b):
+            if not b.fed:
+                for q in range(pos - 1, -1, -1):
+                    if run[q].node_id in b.cands:
+                        return reg_of[q]
+            cell = in_cell(b)
+            scal = 1 if (n > 1 and shape_size(self._in_shape_any(b, shapes)) == 1) else 0
+            key = (cell, scal)
+            if key not in inputs:
+                inputs.append(key)
+            return CHAIN_REGS + inputs.index(key)
+
+        for pos, x in enumerate(ew):
+            a = src(pos, x.inputs[0])
+            b = src(pos, x.inputs[1]) if len(x.inputs) > 1 else 0
+            reg_of[pos] = pos
+            ops.append((EW_CODE[x.kind], pos, a, b))
+        red_reg = src(len(ew), red.inputs[0]) if red is not None else 0
+        if len(inputs) > CHAIN_IN:
+            raise _TooWide()
+        outs: list = []
+        for pos, x in enumerate(ew):
+            if self._must_store(x.node_id, run, pos):
+                p = pubs[x.node_id]
+                if len(p) > CHAIN_PUB or len(outs) >= CHAIN_OUT:
+                    raise _TooWide()
+                outs.append((pos, node_buf[x.node_id][0], p))
+        pub_cells = {c for _, _, p in outs for c in p}
+        if red is not None:
+            pub_cells |= set(pubs[red.node_id])
+        late = int(any(c in pub_cells for c, _ in inputs))
+        self.chain_lates += late
+        n_compute[0] += 1
+        self.n_chains += 1
+        w = [T_CHAIN, n]
+        if red is not None:
+            rp = pubs[red.node_id]
+            if len(rp) > CHAIN_PUB:
+                raise _TooWide()
+            w += [1 if red.kind is OpKind.SUM else 2, red_reg, node_buf[red.node_id][0], len(rp)] + rp + \
+                [0] * (CHAIN_PUB - len(rp))
+        else:
+            w += [0, 0, -1, 0] + [0] * CHAIN_PUB
+        w += [late, len(inputs)]
+        for cell, scal in inputs + [(-1, 0)] * (CHAIN_IN - len(inputs)):
+            w += [cell, scal]
+        w += [len(ops)]
+        for op in ops + [(0, 0, 0, 0)] * (CHAIN_OPS - len(ops)):
+            w += list(op)
+        w += [len(outs)]
+        for reg, buf, p in outs + [(0, -1, [])] * (CHAIN_OUT - len(outs)):
+            w += [reg, buf, len(p)] + list(p) + [0] * (CHAIN_PUB - len(p))
+        return w
+
+    def _must_store(self, nid, run, pos) -> bool:
+        """A value computed in a run stays in registers only if every consumer anywhere in the
+        program is a later op of this run that reads it as its latest candidate."""
+        if nid in self.sp.fetch_nodes or any(nid in s for s in self._multi_sets()):
+            return True
+        later = {id(x): q for q, x in enumerate(run) if q > pos}
+        for c in self.consumers.get(nid, []):
+            q = later.get(id(c))
+            if q is None:
+                return True
+            for b in c.inputs:
+                if not b.fed and nid in b.cands:
+                    last = max((r for r in range(q) if run[r].node_id in b.cands), default=None)
+                    if last != pos:
+                        return True
+        return False
+
+    def _multi_sets(self):
+        ms = getattr(self, "_ms", None)
+        if ms is None:
+            ms = self._ms = [frozenset(b.cands) for x in walk(self.sp.body) if isinstance(x, ExecOp)
+                             for b in x.inputs if not b.fed and len(b.cands) > 1]
+        return ms
+
+    def _in_shape_any(self, b, shapes):
+        if b.fed:
+            return tuple(self.feed_shapes[b.slot])
+        return shapes[b.cands[0]]
+
     def _in_shape(self, b, shapes):
         if b.fed:
             return tuple(self.feed_shapes[b.slot])
@@ -417,3 +579,7 @@ def _fold_is_local(insts, tnid: int, producer: int) -> bool:
 
     scan(insts)
     return ok and found
+
+
+class _TooWide(Exception):
+    """A fused run needs more inputs / outputs / publish cells than the chain kernel holds."""
