@@ -22,8 +22,10 @@ conditional nodes driven by the skeleton's decisions over pinned mapped memory).
 * ``cpu_baseline``: the CPU oracle co-execution (oracle/, SPEC-faithful runner +
   reference kernels + reference Python dataset) on a bounded sample, rank 0 only.
 
-Multi-GPU: one process per GPU (torchrun); each rank runs its own C1 replica on
-its own data stream (weak scaling).  Time = max over ranks.
+Multi-GPU: one process per GPU (torchrun), data parallel: global batch 64*N, every
+rank runs the host program on global shapes while its device expands and trains on
+its own 64-row shard; gradients and the loss are all-reduced by NCCL nodes inside
+the pass graph (paper_2201_09210_b200/dp.py).  Weak scaling; time = max over ranks.
 """
 
 from __future__ import annotations
@@ -223,11 +225,16 @@ def run_b200(args):
     else:
         torch.cuda.set_device(0)
     from paper_2201_09210_b200.b200 import B200Backend
-    be = B200Backend(device=local if world > 1 else 0, precision=args.precision)
+    from paper_2201_09210_b200.dp import DPGroup
+    gbatch = C1["batch"] * world
+    dp = DPGroup(rank, world, gbatch) if world > 1 else None
+    be = B200Backend(device=local if world > 1 else 0, precision=args.precision, dp=dp)
     total_steps = 100_000
-    src = c1_program(steps=total_steps, **C1)
-    # each rank trains its own replica on its own data stream (weak scaling)
-    o = make_orch(src, SyntheticDataset(1000 + rank), be)
+    cfg = dict(C1, batch=gbatch)
+    src = c1_program(steps=total_steps, **cfg)
+    # data parallel: every rank runs the host program on the global batch; its device
+    # expands and trains on its own 64-row shard; gradients are all-reduced in the graph
+    o = make_orch(src, SyntheticDataset(1000), be)
     pre = reach_coexec(o)
     for _ in range(args.warmup):
         o.step()
@@ -249,13 +256,13 @@ def run_b200(args):
 
     # e2e: host-resident inputs through the public API (H2D each step, loss D2H)
     import numpy as np
-    rr = np.random.default_rng(7 + rank)
-    b, din, dout, h = C1["batch"], C1["din"], C1["dout"], C1["hidden"]
+    rr = np.random.default_rng(7)
+    b, din, dout, h = gbatch, C1["din"], C1["dout"], C1["hidden"]
     recs = {"x": [Tensor((b, din), rr.uniform(-1, 1, (b, din))) for _ in range(4)],
             "y": [Tensor((b, dout), rr.uniform(-1, 1, (b, dout))) for _ in range(4)],
             "w1_init": [Tensor((din, h), rr.uniform(-1, 1, (din, h)))],
             "w2_init": [Tensor((h, dout), rr.uniform(-1, 1, (h, dout)))]}
-    be2 = B200Backend(device=local if world > 1 else 0, precision=args.precision)
+    be2 = B200Backend(device=local if world > 1 else 0, precision=args.precision, dp=dp)
     o2 = make_orch(src, InMemoryDataset(recs), be2)
     reach_coexec(o2)
     for _ in range(args.warmup):
@@ -267,7 +274,7 @@ def run_b200(args):
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
         e2e_max = float(tt.item())
     esz = 8
-    h2d = (b * din + b * dout) * esz
+    h2d = (C1["batch"] * din + C1["batch"] * dout) * esz      # this rank's shard of x and y
     d2h = 8
 
     if rank == 0:
@@ -278,11 +285,13 @@ def run_b200(args):
             "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(t_max / args.steps, 5), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": args.precision,
-            "data": "synthetic (SyntheticDataset seed 1000+rank, expanded on device from xorshift64* state)",
+            "data": "synthetic (SyntheticDataset seed 1000; each rank expands its batch shard on device "
+                    "from the jumped-ahead xorshift64* state)",
             "config": {"workload": "C1 tiny MLP 784-128-10 (sigmoid, MSE, hand-written backward, "
                                    "loss-driven branch, native clip, choice-driven while), coexec mode",
                        "global_batch": C1["batch"] * world, "per_gpu_batch": C1["batch"],
-                       "parallelism": f"replicas{world}", "l2": "flushed (256 MiB write) between timed steps",
+                       "parallelism": f"dp{world}" + ("" if world == 1 else " (NCCL all-reduce in the pass graph)"),
+                       "l2": "flushed (256 MiB write) between timed steps",
                        "tracing_steps_before_coexec": pre, "steps_replayed_in_timed_region": replays,
                        "algorithmic_flops_per_step": c1_flops(**C1)},
             "roofline": roof,

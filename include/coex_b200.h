@@ -93,6 +93,13 @@ int coex_ctx_set_timeout(coex_ctx* ctx, double seconds);
 /* Number of compute kernels this context launched eagerly or replayed in graphs. */
 int64_t coex_ctx_kernel_count(coex_ctx* ctx);
 
+/* ---- data parallelism (one process per GPU; NCCL over NVLink, loaded at run time) ----
+ * Rank 0 calls coex_nccl_unique_id, the host plumbing (torch.distributed) broadcasts the 128
+ * bytes, every rank calls coex_ctx_init_comm.  Plans of a sharded SymProgram then contain
+ * all-reduce nodes (ncclAllReduce captured into the pass graph). */
+int coex_nccl_unique_id(uint8_t* out128);
+int coex_ctx_init_comm(coex_ctx* ctx, int rank, int world, const uint8_t* uid128);
+
 /* ---- timing on the context's stream (bench.py; CUDA events, not host clocks) ---- */
 int coex_ctx_event_record(coex_ctx* ctx, int slot);               /* slot in [0, 64) */
 int coex_ctx_event_elapsed(coex_ctx* ctx, int a, int b, double* ms);

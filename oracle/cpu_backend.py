@@ -30,6 +30,7 @@ from paper_2201_09210_b200.errors import (ChannelClosed, DecisionMismatch, InFli
                                           PassCancelled)
 from paper_2201_09210_b200.graph_gen import (ExecOp, InputFeed, OutputFetch, SwitchCase,
                                              UnrolledLoop, While)
+from paper_2201_09210_b200.dp import AllReduce, shard_program, shard_value
 from paper_2201_09210_b200.runner_api import PassResult
 from paper_2201_09210_b200.tensor import OpKind, Tensor
 from paper_2201_09210_b200.trace_graph import CaseDecision, LoopDecision
@@ -104,10 +105,11 @@ def _host(v) -> Tensor:
 class _Runner:
     """One pass over a SymProgram as a generator: yields _NEED when it must block."""
 
-    def __init__(self, sp, ch: ChannelSet, vs: VariableStore):
+    def __init__(self, sp, ch: ChannelSet, vs: VariableStore, dp=None):
         self.sp = sp
         self.ch = ch
         self.vs = vs
+        self.dp = dp
         self.vals: dict = {}       # node id -> (tick, Tensor)
         self.fed: dict = {}        # slot -> Tensor
         self.tick = 0
@@ -169,6 +171,9 @@ class _Runner:
             elif isinstance(x, OutputFetch):
                 self.ch.push_fetch(x.node_id, self.vals[x.node_id][1])
                 self.fetches += 1
+            elif isinstance(x, AllReduce):
+                tick, t = self.vals[x.node_id]
+                self.vals[x.node_id] = (tick, Tensor(t.shape, self.dp.allreduce(t.data, x.avg)))
             elif isinstance(x, SwitchCase):
                 d = yield from self._pop(self.ch.decisions)
                 if not isinstance(d, CaseDecision) or d.branch_id != x.branch_id:
@@ -193,9 +198,9 @@ class _Runner:
         yield from self._pop(self.ch.commit)
 
 
-def run_pass(sp, ch: ChannelSet, vs: VariableStore) -> PassResult:
+def run_pass(sp, ch: ChannelSet, vs: VariableStore, dp=None) -> PassResult:
     """Blocking structured execution of ``sp``."""
-    r = _Runner(sp, ch, vs)
+    r = _Runner(sp, ch, vs, dp)
     gen = r.whole()
     vs.in_flight = True
     try:
@@ -221,7 +226,9 @@ def snapshot_vars(vs: VariableStore) -> dict:
 class CpuPass:
     """The skeleton-facing side of one pass (threaded, or lazy on the caller's thread)."""
 
-    def __init__(self, sp, vs: VariableStore, capacity: int, lazy: bool):
+    def __init__(self, sp, vs: VariableStore, capacity: int, lazy: bool, dp=None, sharded=()):
+        self.dp = dp
+        self.sharded = set(sharded)
         self.ch = ChannelSet(capacity, lazy)
         self.vs = vs
         self.lazy = lazy
@@ -230,7 +237,7 @@ class CpuPass:
         self.done = False
         self.consumed: dict = {}    # node id -> fetch entries already taken
         if lazy:
-            self.runner = _Runner(sp, self.ch, vs)
+            self.runner = _Runner(sp, self.ch, vs, dp)
             self.gen = self.runner.whole()
             vs.in_flight = True
         else:
@@ -239,7 +246,7 @@ class CpuPass:
 
     def _thread_main(self, sp):
         try:
-            self.result = run_pass(sp, self.ch, self.vs)
+            self.result = run_pass(sp, self.ch, self.vs, self.dp)
         except BaseException as e:  # surfaced as ChannelClosed to the skeleton
             self.error = e
             self.ch.cancel()
@@ -278,6 +285,8 @@ class CpuPass:
         self.ch.push_decision(d)
 
     def feed(self, slot, v):
+        if slot in self.sharded:
+            v = shard_value(_host(v) if not hasattr(v, "state") else v, self.dp.rank, self.dp.world)
         self.ch.push_feed(slot, v)
 
     def _take(self, nid: int, k: int):
@@ -326,9 +335,11 @@ class CpuBackend:
     name = "cpu-oracle"
     precision = "f64"
 
-    def __init__(self, capacity: int = 64):
+    def __init__(self, capacity: int = 64, dp=None):
         self.vs = VariableStore()
         self.capacity = capacity
+        self.dp = dp
+        self.dp_plans: list = []
 
     # ---- eager
     def put(self, t):
@@ -363,7 +374,15 @@ class CpuBackend:
 
     # ---- symbolic
     def compile(self, sp, tg):
-        return sp
+        if self.dp is None or self.dp.world <= 1:
+            return (sp, ())
+        from paper_2201_09210_b200.planner import Planner
+        feed_shapes = {(n.id, p): tuple(s) for n in tg.all_nodes() if n.typ == "op" for p, s in n.feed_shapes.items()}
+        node_shapes = Planner(sp, tg, {}, self.var_shapes(), feed_shapes, 8).infer_shapes()
+        plan = shard_program(sp, feed_shapes, node_shapes, self.dp.batch, self.dp.world)
+        self.dp_plans.append(plan)
+        return (plan.sp, plan.sharded_slots)
 
-    def begin_pass(self, sp, lazy: bool = False) -> CpuPass:
-        return CpuPass(sp, self.vs, self.capacity, lazy)
+    def begin_pass(self, prog, lazy: bool = False) -> CpuPass:
+        sp, sharded = prog
+        return CpuPass(sp, self.vs, self.capacity, lazy, self.dp, sharded)

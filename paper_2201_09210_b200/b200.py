@@ -60,6 +60,8 @@ SIGNATURES = {
     "coex_ctx_event_elapsed": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int, _DP]),
     "coex_exec_op_timed": (ctypes.c_int, [_P, ctypes.c_int, ctypes.POINTER(CoexAttrs), ctypes.c_int, _I64P,
                                           ctypes.c_int, _DP]),
+    "coex_nccl_unique_id": (ctypes.c_int, [ctypes.c_char_p]),
+    "coex_ctx_init_comm": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int, ctypes.c_char_p]),
     "coex_ctx_set_trace": (ctypes.c_int, [_P, ctypes.c_int]),
     "coex_ctx_read_trace": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_uint64), _I64, _I64P]),
     "coex_tensor_put": (ctypes.c_int, [_P, ctypes.c_int, _I64P, _DP, _I64P]),
@@ -167,8 +169,9 @@ class B200Backend:
 
     name = "b200"
 
-    def __init__(self, device: int = 0, precision: str = "f64", timeout_s: float = 120.0):
+    def __init__(self, device: int = 0, precision: str = "f64", timeout_s: float = 120.0, dp=None):
         self.lib = load_library()
+        self.dp = dp
         if precision not in PRECISIONS:
             raise ValueError(f"precision must be one of {sorted(PRECISIONS)}")
         self.precision = precision
@@ -180,6 +183,22 @@ class B200Backend:
         self.var_idx: dict = {}
         self._vshape: dict = {}
         self.active = None
+        if dp is not None and (dp.world > 1 or dp.force):
+            self._init_comm()
+
+    def _init_comm(self):
+        """NCCL communicator over the caller's torch.distributed group (rank 0 makes the id)."""
+        uid = ctypes.create_string_buffer(128)
+        if self.dp.world > 1:
+            import torch.distributed as dist
+            if self.dp.rank == 0:
+                _check(self.lib.coex_nccl_unique_id(uid))
+            obj = [bytes(uid.raw)]
+            dist.broadcast_object_list(obj, src=0)
+            uid = ctypes.create_string_buffer(obj[0], 128)
+        else:
+            _check(self.lib.coex_nccl_unique_id(uid))
+        _check(self.lib.coex_ctx_init_comm(self.ctx, self.dp.rank, self.dp.world, uid))
 
     def close(self):
         if self.ctx is not None:
@@ -314,7 +333,7 @@ class B200Program:
         self.tg = tg
         self.graphs: dict = {}
         self.feed_shape: dict = {}       # slot -> expected shape (observed hints, updated on misses)
-        self.node_of_slot = {}
+        self.dp_plan = None
         for n in tg.all_nodes():
             if n.typ == "op":
                 for pos, s in n.feed_shapes.items():
@@ -328,8 +347,7 @@ class B200Program:
         hit = self.graphs.get(key)
         if hit is not None:
             return hit
-        plan = Planner(self.sp, self.tg, self.be.var_idx, vsh, self.feed_shape, self.be.esize,
-                       bf16=self.be.precision == "bf16").build()
+        plan = self._plan(vsh)
         words = np.asarray(plan.words, dtype=np.int64)
         consts = np.asarray(plan.consts if plan.consts else [0.0], dtype=np.float64)
         handle = _P()
@@ -338,6 +356,28 @@ class B200Program:
         self.graphs[key] = (handle, plan)
         self.last_plan = plan
         return handle, plan
+
+    def _plan(self, vsh):
+        be = self.be
+        bf16 = be.precision == "bf16"
+        dp = be.dp
+        if dp is not None and (dp.world > 1 or dp.force):
+            from .dp import local_feed_shapes, shard_program
+            from .planner import NeedsReplicated
+            gshapes = Planner(self.sp, self.tg, be.var_idx, vsh, self.feed_shape, be.esize).infer_shapes()
+            dplan = shard_program(self.sp, self.feed_shape, gshapes, dp.batch, dp.world, force=dp.force)
+            self.dp_plan = dplan
+            if not dplan.replicated:
+                try:
+                    plan = Planner(dplan.sp, self.tg, be.var_idx, vsh, local_feed_shapes(self.feed_shape, dplan),
+                                   be.esize, bf16=bf16, force_store=dplan.allreduce_nodes).build()
+                    plan.feed_shapes = dict(self.feed_shape)        # host checks global shapes
+                    plan.sharded = set(dplan.sharded_slots)
+                    plan.dp = dplan
+                    return plan
+                except NeedsReplicated as e:
+                    dplan.replicated, dplan.reason = True, str(e)
+        return Planner(self.sp, self.tg, be.var_idx, vsh, self.feed_shape, be.esize, bf16=bf16).build()
 
     def info(self, handle) -> dict:
         nk, nc, ab = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
@@ -402,6 +442,13 @@ class B200Pass:
             self.prog.feed_shape[slot] = shape           # next specialisation uses the observed shape
             raise ShapeMiss(f"feed slot {slot}: shape {shape} but the graph expects {want}")
         code = slot_code(slot)
+        if slot in getattr(self.plan, "sharded", ()):
+            from .dp import shard_value
+            dp = self.be.dp
+            if isinstance(v, DevTensor):
+                v = self.be.get(v)
+            v = shard_value(v, dp.rank, dp.world)
+            shape = tuple(v.shape)
         if isinstance(v, DevTensor):
             self.keep.append(v)
             self._do(self.lib.coex_pass_feed_tensor, code, v.id)

@@ -30,6 +30,7 @@
 #include "gemm_tc.cuh"
 
 #include <cudaTypedefs.h>
+#include <dlfcn.h>
 
 using namespace coex;
 
@@ -144,6 +145,9 @@ struct coex_ctx {
   cudaEvent_t events[64] = {nullptr};
   unsigned long long* d_trace = nullptr;
   int trace_cap = 0;
+  void* comm = nullptr;                  // ncclComm_t
+  int rank = 0, world = 1;
+  cudaStream_t cap_stream = nullptr;     // side stream used to capture collectives into graphs
 };
 
 namespace {
@@ -301,6 +305,38 @@ PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
 }
 
 int64_t bf16_pitch(int64_t K) { return (K + 7) / 8 * 8; }
+
+// ---- NCCL, bound at run time (single-GPU use needs no NCCL at all) ----
+typedef struct { char internal[128]; } nccl_uid_t;
+typedef void* nccl_comm_t;
+enum { kNcclFloat = 7, kNcclDouble = 8, kNcclSum = 0, kNcclAvg = 4 };   // nccl.h ncclDataType_t / ncclRedOp_t
+struct NcclApi {
+  int (*get_unique_id)(nccl_uid_t*) = nullptr;
+  int (*comm_init_rank)(nccl_comm_t*, int, nccl_uid_t, int) = nullptr;
+  int (*all_reduce)(const void*, void*, size_t, int, int, nccl_comm_t, cudaStream_t) = nullptr;
+  int (*comm_destroy)(nccl_comm_t) = nullptr;
+  const char* (*error_string)(int) = nullptr;
+  bool ok = false;
+};
+NcclApi& nccl() {
+  static NcclApi api;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);     // reuse torch's copy if loaded
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (h) {
+      api.get_unique_id = (int (*)(nccl_uid_t*))dlsym(h, "ncclGetUniqueId");
+      api.comm_init_rank = (int (*)(nccl_comm_t*, int, nccl_uid_t, int))dlsym(h, "ncclCommInitRank");
+      api.all_reduce = (int (*)(const void*, void*, size_t, int, int, nccl_comm_t, cudaStream_t))dlsym(h, "ncclAllReduce");
+      api.comm_destroy = (int (*)(nccl_comm_t))dlsym(h, "ncclCommDestroy");
+      api.error_string = (const char* (*)(int))dlsym(h, "ncclGetErrorString");
+      api.ok = api.get_unique_id && api.comm_init_rank && api.all_reduce && api.comm_destroy;
+    }
+  }
+  return api;
+}
 
 // bf16 [rows][pitch] K-major tile source: box {64, box_rows}, 128-byte swizzle, OOB -> 0.
 int make_tmap(CUtensorMap* m, void* base, int64_t rows, int64_t K, int box_rows) {
@@ -585,6 +621,8 @@ int coex_ctx_destroy(coex_ctx* c) {
   if (c->h_stage) cudaFreeHost(c->h_stage);
   for (auto& ev : c->events)
     if (ev) cudaEventDestroy(ev);
+  if (c->comm && nccl().ok) nccl().comm_destroy(c->comm);
+  if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   cudaStreamDestroy(c->stream);
   delete c;
   return COEX_OK;
@@ -601,6 +639,30 @@ int coex_ctx_set_timeout(coex_ctx* c, double seconds) {
 }
 
 int64_t coex_ctx_kernel_count(coex_ctx* c) { return c ? c->kernel_count : 0; }
+
+int coex_nccl_unique_id(uint8_t* out128) {
+  NcclApi& n = nccl();
+  if (!n.ok) return fail(COEX_CUDA_ERROR, "libnccl.so.2 not found");
+  nccl_uid_t id;
+  int r = n.get_unique_id(&id);
+  if (r) return fail(COEX_CUDA_ERROR, std::string("ncclGetUniqueId: ") + (n.error_string ? n.error_string(r) : ""));
+  memcpy(out128, id.internal, 128);
+  return COEX_OK;
+}
+
+int coex_ctx_init_comm(coex_ctx* c, int rank, int world, const uint8_t* uid128) {
+  NcclApi& n = nccl();
+  if (!n.ok) return fail(COEX_CUDA_ERROR, "libnccl.so.2 not found");
+  nccl_uid_t id;
+  memcpy(id.internal, uid128, 128);
+  CK(cudaSetDevice(c->device));
+  int r = n.comm_init_rank(&c->comm, world, id, rank);
+  if (r) return fail(COEX_CUDA_ERROR, std::string("ncclCommInitRank: ") + (n.error_string ? n.error_string(r) : ""));
+  c->rank = rank;
+  c->world = world;
+  if (!c->cap_stream) CK(cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
+  return COEX_OK;
+}
 
 int coex_ctx_set_trace(coex_ctx* c, int capacity) {
   if (c->active) return fail(COEX_IN_FLIGHT_PASS, "set_trace during a pass");
@@ -914,7 +976,8 @@ int coex_var_rollback(coex_ctx* c) {
 // =============================================================== symbolic programs
 namespace {
 
-enum PlanTag : int64_t { T_SEQ = 1, T_OP = 2, T_PTR = 3, T_FEED = 4, T_FETCH = 5, T_SWITCH = 6, T_WHILE = 7, T_CHAIN = 8 };
+enum PlanTag : int64_t { T_SEQ = 1, T_OP = 2, T_PTR = 3, T_FEED = 4, T_FETCH = 5, T_SWITCH = 6, T_WHILE = 7, T_CHAIN = 8,
+                         T_ALLREDUCE = 9 };
 constexpr int64_t kPlanMagic = 0xC0E8B200;
 constexpr int64_t kPlanVersion = 2;
 
@@ -937,7 +1000,7 @@ struct coex_prog {
   int64_t ncells = 0;
   FeedRecord* recs = nullptr;
   unsigned int* late = nullptr;       // late-publication counters
-  int64_t n_kernel_nodes = 0, n_cond_nodes = 0, n_compute = 0;
+  int64_t n_kernel_nodes = 0, n_cond_nodes = 0, n_compute = 0, n_collectives = 0;
   std::vector<int> commit_vars;
   std::vector<int64_t> commit_bytes;
   std::unordered_map<int, std::vector<int64_t>> var_shapes;   // shape id -> dims
@@ -1107,6 +1170,28 @@ struct Builder {
         }
         p->n_compute++;
         return add_kernel(g, prev, L);
+      }
+      case T_ALLREDUCE: {
+        void* b = buf(next());
+        const int64_t count = next();
+        const int64_t avg = next();
+        NcclApi& n = nccl();
+        if (!n.ok || c->comm == nullptr) throw std::runtime_error("all-reduce in a plan without a communicator");
+        // Capture the collective on a side stream into a child graph (stream capture into
+        // an existing graph would also work; a child node keeps conditional bodies simple).
+        cudaGraph_t child;
+        CK(cudaStreamBeginCapture(c->cap_stream, cudaStreamCaptureModeRelaxed));
+        int r = n.all_reduce(b, b, (size_t)count, is_f64(c) ? kNcclDouble : kNcclFloat, avg ? kNcclAvg : kNcclSum,
+                             c->comm, c->cap_stream);
+        cudaError_t ce = cudaStreamEndCapture(c->cap_stream, &child);
+        if (r || ce != cudaSuccess) throw std::runtime_error("capturing ncclAllReduce failed");
+        cudaGraphNode_t node;
+        ce = cudaGraphAddChildGraphNode(&node, g, *prev ? prev : nullptr, *prev ? 1 : 0, child);
+        cudaGraphDestroy(child);
+        if (ce != cudaSuccess) throw std::runtime_error(std::string("child graph node: ") + cudaGetErrorString(ce));
+        *prev = node;
+        p->n_collectives++;
+        return COEX_OK;
       }
       case T_PTR: {
         PtrParams q{};

@@ -1,0 +1,329 @@
+"""Data-parallel co-execution: shard a SymProgram over R ranks.
+
+Every rank runs the same host program (skeleton, natives, decisions) on global
+shapes; only the device pass is sharded.  Feed slots whose leading dimension is
+the global batch are fed row shards; a propagation pass over the SymProgram
+tags every value
+
+    R   replicated            (variables, fills, host scalars, all-reduced values)
+    S0  rows sharded          (batch inputs and row-wise functions of them)
+    S1  columns sharded       (transpose of S0)
+    P+  partial sum           (Sum over S0, MatMul contracting the sharded dim)
+    P~  partial mean          (Mean over S0 -- equal shards make the mean of
+                               local means the global mean)
+
+and inserts ``AllReduce(node, op)`` right after a Partial producer when any
+consumer needs a replicated value: AssignVar, OutputFetch, a nonlinear op, or
+mixing with R / another Partial kind.  After the all-reduce the node is R for
+all consumers, so fetched values -- and hence every rank's decisions -- are
+identical.  Anything outside these rules (e.g. fetching a sharded activation,
+assigning a sharded value to a variable, slicing a replicated batch tensor)
+makes the program run replicated: every rank computes the global batch, no
+collective, still correct.
+
+Parity: DP results equal the single-device run up to summation order
+(tolerance, not bitwise) -- tests/test_dp_gloo.py checks world size 2 on CPU.
+"""
+
+from __future__ import annotations
+
+import copy
+from dataclasses import dataclass, field
+
+from .graph_gen import ExecOp, InputFeed, OutputFetch, SwitchCase, SymProgram, UnrolledLoop, While
+from .rng import jump_state
+from .tensor import OpKind, Tensor, shape_size
+
+R, S0, S1, PSUM, PAVG = "R", "S0", "S1", "P+", "P~"
+PARTIAL = (PSUM, PAVG)
+ELEMENTWISE = (OpKind.ADD, OpKind.SUB, OpKind.MUL)
+LINEAR_UNARY = (OpKind.NEG,)
+NONLINEAR = (OpKind.RELU, OpKind.SIGMOID)
+
+
+@dataclass
+class AllReduce:
+    """Sum (``avg=False``) or average the node's latest output across ranks, in place."""
+
+    node_id: int
+    avg: bool
+
+
+class Unshardable(Exception):
+    pass
+
+
+@dataclass
+class DPPlan:
+    sp: SymProgram                  # transformed program (AllReduce inserted, local reshape attrs)
+    sharded_slots: set              # feed slots fed row shards
+    state: dict                     # node id -> state
+    world: int
+    replicated: bool = False        # True: program runs unsharded on every rank
+    reason: str = ""
+    allreduce_nodes: list = field(default_factory=list)
+
+
+def _iter(insts):
+    for x in insts:
+        yield x
+        if isinstance(x, SwitchCase):
+            for c in x.cases:
+                yield from _iter(c)
+        elif isinstance(x, While):
+            yield from _iter(x.body)
+        elif isinstance(x, UnrolledLoop):
+            for b in x.bodies:
+                yield from _iter(b)
+
+
+class _Prop:
+    def __init__(self, sp: SymProgram, feed_shapes: dict, node_shapes: dict, batch: int, world: int):
+        self.sp = sp
+        self.feed_shapes = feed_shapes
+        self.node_shapes = node_shapes
+        self.batch = batch
+        self.world = world
+        self.sharded = {s for s, shp in feed_shapes.items()
+                        if len(shp) >= 1 and shp[0] == batch and batch % world == 0}
+        self.state: dict = {}
+        self.reduce_at: dict = {}       # node id -> avg flag
+        self.kind: dict = {}
+        for x in _iter(sp.body):
+            if isinstance(x, ExecOp):
+                self.kind[x.node_id] = x
+
+    def bind(self, b):
+        if b.fed:
+            return S0 if b.slot in self.sharded else R
+        sts = {self.eff(c) for c in b.cands if c in self.state}
+        if not sts:
+            return None
+        if len(sts) > 1:
+            raise Unshardable(f"candidates {b.cands} disagree on sharding {sorted(sts)}")
+        return sts.pop()
+
+    def eff(self, nid):
+        """State a consumer sees: all-reduced Partials read as R."""
+        st = self.state[nid]
+        return R if (st in PARTIAL and nid in self.reduce_at) else st
+
+    def need_r(self, nid):
+        """A consumer needs node ``nid`` replicated: schedule its all-reduce."""
+        st = self.state.get(nid)
+        if st in PARTIAL:
+            self.reduce_at[nid] = st == PAVG
+            return True
+        if st in (S0, S1):
+            raise Unshardable(f"node {nid}: a sharded value is needed replicated")
+        return False
+
+    def needs_r_binding(self, b):
+        if not b.fed:
+            for c in b.cands:
+                if c in self.state:
+                    self.need_r(c)
+
+    def op(self, x: ExecOp):
+        k = x.kind
+        ins = [self.bind(b) for b in x.inputs]
+        if any(s is None for s in ins):
+            return None                      # loop-carried input not known yet
+        if k in (OpKind.READ_VAR, OpKind.FILL):
+            return R
+        if k is OpKind.ASSIGN_VAR:
+            if ins[0] in PARTIAL:
+                self.needs_r_binding(x.inputs[0])
+                return R
+            if ins[0] != R:
+                raise Unshardable("assigning a sharded value to a variable")
+            return R
+        if k in NONLINEAR:
+            if ins[0] in PARTIAL:
+                self.needs_r_binding(x.inputs[0])
+                return R
+            return ins[0]
+        if k in LINEAR_UNARY:
+            return ins[0]
+        if k in ELEMENTWISE:
+            a, b = ins
+            scalar = [self._rank0(bb) for bb in x.inputs]
+            if a == b:
+                if a in PARTIAL and k is OpKind.MUL:
+                    self.needs_r_binding(x.inputs[0])
+                    self.needs_r_binding(x.inputs[1])
+                    return R
+                return a
+            pa, pb = a in PARTIAL, b in PARTIAL
+            if pa and pb:                       # P+ with P~
+                self.needs_r_binding(x.inputs[0])
+                self.needs_r_binding(x.inputs[1])
+                return R
+            if pa or pb:
+                other = b if pa else a
+                if k is OpKind.MUL and other == R:
+                    return a if pa else b       # scaling by a replicated value is linear
+                self.needs_r_binding(x.inputs[0 if pa else 1])
+                a, b = (R, b) if pa else (a, R)
+                if a == b:
+                    return R
+            # now no partials: combine R with S0/S1
+            if a != R and b != R:
+                raise Unshardable(f"node {x.node_id}: {a} meets {b}")
+            sh = a if a != R else b
+            r_side = 1 if a != R else 0
+            if not scalar[r_side]:
+                raise Unshardable(f"node {x.node_id}: replicated tensor meets a sharded one")
+            return sh
+        if k in (OpKind.SUM, OpKind.MEAN):
+            a = ins[0]
+            if a in (S0, S1):
+                return PSUM if k is OpKind.SUM else PAVG
+            if a in PARTIAL:
+                if k is OpKind.MEAN and a == PSUM or k is OpKind.SUM and a == PAVG:
+                    return a                    # linear: keeps the partial kind
+                return a
+            return R
+        if k is OpKind.TRANSPOSE:
+            a = ins[0]
+            if a in (S0, S1):
+                if tuple(x.attrs["perm"]) != (1, 0):
+                    raise Unshardable("transpose of a sharded tensor beyond 2-D")
+                return S1 if a == S0 else S0
+            return a
+        if k is OpKind.RESHAPE:
+            a = ins[0]
+            if a == S1:
+                raise Unshardable("reshape of a column-sharded tensor")
+            if a == S0:
+                tgt = x.attrs["target_shape"]
+                if not tgt or tgt[0] != self.batch:
+                    raise Unshardable("reshape that moves the batch dimension")
+            return a
+        if k is OpKind.MATMUL:
+            a, b = ins
+            if a == S0 and b == R:
+                return S0
+            if a == S1 and b == S0:
+                return PSUM
+            if a == R and b == R:
+                return R
+            if a in PARTIAL and b == R:
+                return a
+            if a == R and b in PARTIAL:
+                return b
+            if a in PARTIAL or b in PARTIAL:
+                for i, s in enumerate(ins):
+                    if s in PARTIAL:
+                        self.needs_r_binding(x.inputs[i])
+                return self.op(x)
+            raise Unshardable(f"matmul of {a} x {b}")
+        raise Unshardable(f"no sharding rule for {k.value}")
+
+    def _rank0(self, b):
+        shp = self.feed_shapes.get(b.slot) if b.fed else self.node_shapes.get(b.cands[0])
+        return shp is not None and shape_size(shp) == 1
+
+    def walk(self, insts):
+        changed = False
+        for x in insts:
+            if isinstance(x, ExecOp):
+                st = self.op(x)
+                if st is not None and self.state.get(x.node_id) != st:
+                    self.state[x.node_id] = st
+                    changed = True
+            elif isinstance(x, OutputFetch):
+                if x.node_id in self.state:
+                    before = x.node_id in self.reduce_at
+                    self.need_r(x.node_id)
+                    changed |= (x.node_id in self.reduce_at) != before
+            elif isinstance(x, SwitchCase):
+                for c in x.cases:
+                    changed |= self.walk(c)
+            elif isinstance(x, While):
+                changed |= self.walk(x.body)
+            elif isinstance(x, UnrolledLoop):
+                for b in x.bodies:
+                    changed |= self.walk(b)
+        return changed
+
+    def run(self):
+        for _ in range(8):
+            n_red = len(self.reduce_at)
+            if not self.walk(self.sp.body) and len(self.reduce_at) == n_red:
+                return
+        raise Unshardable("sharding states did not converge")
+
+
+def _rewrite(insts, prop: _Prop) -> list:
+    out = []
+    for x in insts:
+        if isinstance(x, ExecOp):
+            y = x
+            if x.kind is OpKind.RESHAPE and prop.state.get(x.node_id) == S0:
+                tgt = list(x.attrs["target_shape"])
+                tgt[0] //= prop.world
+                y = ExecOp(x.node_id, x.kind, dict(x.attrs, target_shape=tuple(tgt)), x.inputs)
+            out.append(y)
+            if x.node_id in prop.reduce_at:
+                out.append(AllReduce(x.node_id, prop.reduce_at[x.node_id]))
+        elif isinstance(x, SwitchCase):
+            out.append(SwitchCase(x.branch_id, [_rewrite(c, prop) for c in x.cases]))
+        elif isinstance(x, While):
+            out.append(While(x.loop_id, x.node_id, _rewrite(x.body, prop)))
+        elif isinstance(x, UnrolledLoop):
+            body = _rewrite(x.bodies[0], prop) if x.bodies else []
+            out.append(UnrolledLoop(x.loop_id, x.node_id, [body] * len(x.bodies)))
+        else:
+            out.append(x)
+    return out
+
+
+def shard_program(sp: SymProgram, feed_shapes: dict, node_shapes: dict, batch: int, world: int,
+                  force: bool = False) -> DPPlan:
+    """Shard ``sp`` for ``world`` ranks with global batch ``batch`` (feeds with dim0 == batch).
+    ``node_shapes`` are the global shapes of the specialisation (Planner.infer_shapes)."""
+    if world <= 1 and not force:
+        return DPPlan(sp, set(), {}, world, replicated=True, reason="world size 1")
+    prop = _Prop(sp, feed_shapes, node_shapes, batch, world)
+    if not prop.sharded:
+        return DPPlan(sp, set(), {}, world, replicated=True, reason="no batch-sized feed")
+    try:
+        prop.run()
+    except Unshardable as e:
+        return DPPlan(sp, set(), {}, world, replicated=True, reason=str(e))
+    new = copy.copy(sp)
+    new.body = _rewrite(sp.body, prop)
+    return DPPlan(new, prop.sharded, prop.state, world, False, "", sorted(prop.reduce_at))
+
+
+def local_feed_shapes(feed_shapes: dict, plan: DPPlan) -> dict:
+    out = dict(feed_shapes)
+    for s in plan.sharded_slots:
+        shp = list(out[s])
+        shp[0] //= plan.world
+        out[s] = tuple(shp)
+    return out
+
+
+def shard_value(v, rank: int, world: int):
+    """Rank ``rank``'s row shard of a fed batch value (host tensor or synthetic descriptor)."""
+    from .dataset import SyntheticTensor
+    rows = v.shape[0] // world
+    if isinstance(v, SyntheticTensor):
+        row_elems = shape_size(v.shape[1:])
+        st = jump_state(v.state, rank * rows * row_elems)
+        return SyntheticTensor(st, (rows,) + tuple(v.shape[1:]))
+    data = v.data if hasattr(v, "data") else v
+    return Tensor((rows,) + tuple(v.shape[1:]), data[rank * rows:(rank + 1) * rows])
+
+
+@dataclass
+class DPGroup:
+    """This process's place in the data-parallel job."""
+
+    rank: int
+    world: int
+    batch: int                      # global batch: feeds with this leading dim are sharded
+    allreduce: object = None        # callable(numpy array, avg) -> numpy array (CPU oracle only)
+    force: bool = False             # shard (and all-reduce over NCCL) even at world size 1 (tests)

@@ -32,7 +32,7 @@ from .tensor import OpKind, infer_shape, shape_size
 
 MAGIC = 0xC0E8B200
 VERSION = 2
-T_SEQ, T_OP, T_PTR, T_FEED, T_FETCH, T_SWITCH, T_WHILE, T_CHAIN = 1, 2, 3, 4, 5, 6, 7, 8
+T_SEQ, T_OP, T_PTR, T_FEED, T_FETCH, T_SWITCH, T_WHILE, T_CHAIN, T_ALLREDUCE = 1, 2, 3, 4, 5, 6, 7, 8, 9
 PTR_ALIAS, PTR_READ_VAR, PTR_ASSIGN_VAR = 0, 1, 2
 MAX_RANK = 8
 MAX_PUB = 6
@@ -85,7 +85,8 @@ class Plan:
 
 class Planner:
     def __init__(self, sp: SymProgram, tg, var_index: dict, var_shapes: dict, feed_shapes: dict, esize: int,
-                 bf16: bool = False, fuse: bool = True):
+                 bf16: bool = False, fuse: bool = True, force_store=()):
+        self.force_store = set(force_store)
         self.bf16 = bf16
         self.fuse = fuse
         self.sp = sp
@@ -308,6 +309,11 @@ class Planner:
                 elif isinstance(x, UnrolledLoop):
                     for b in x.bodies:
                         items.extend(emit(b))
+                elif type(x).__name__ == "AllReduce":
+                    b0, b1, pp = node_buf.get(x.node_id, (-1, -1, True))
+                    if b0 < 0 or pp:
+                        raise NeedsReplicated(f"node {x.node_id} has no static buffer to all-reduce")
+                    items.append([T_ALLREDUCE, b0, shape_size(shapes[x.node_id]), int(x.avg)])
             return items
 
         def seq(insts) -> list:
@@ -501,7 +507,7 @@ class Planner:
     def _must_store(self, nid, run, pos) -> bool:
         """A value computed in a run stays in registers only if every consumer anywhere in the
         program is a later op of this run that reads it as its latest candidate."""
-        if nid in self.sp.fetch_nodes or any(nid in s for s in self._multi_sets()):
+        if nid in self.sp.fetch_nodes or nid in self.force_store or any(nid in s for s in self._multi_sets()):
             return True
         later = {id(x): q for q, x in enumerate(run) if q > pos}
         for c in self.consumers.get(nid, []):
@@ -583,3 +589,7 @@ def _fold_is_local(insts, tnid: int, producer: int) -> bool:
 
 class _TooWide(Exception):
     """A fused run needs more inputs / outputs / publish cells than the chain kernel holds."""
+
+
+class NeedsReplicated(Exception):
+    """A sharded plan cannot be lowered (e.g. all-reduce of a pointer-only value)."""

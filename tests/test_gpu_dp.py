@@ -1,0 +1,32 @@
+"""Data-parallel device path on one GPU: a forced 1-rank sharding puts NCCL all-reduce
+nodes into the pass graph (captured ncclAllReduce child graphs, incl. inside a WHILE
+body) -- results must stay bit-identical to the oracle (a 1-rank all-reduce is exact)."""
+
+import pytest
+
+from oracle.cpu_backend import CpuBackend
+from paper_2201_09210_b200 import coexec, lang
+from paper_2201_09210_b200.b200 import B200Backend
+from paper_2201_09210_b200.dataset import SyntheticDataset
+from paper_2201_09210_b200.dp import DPGroup
+from paper_2201_09210_b200.workloads import c1_program
+
+pytestmark = pytest.mark.gpu
+
+
+def test_forced_dp_nccl_in_graph_bitwise():
+    src = c1_program(steps=10, batch=8, hidden=16, din=12, dout=3)
+    ref, ref_st = coexec.run(lang.parse(src), SyntheticDataset(0), "coexec", backend=CpuBackend())
+    be = B200Backend(precision="f64", dp=DPGroup(0, 1, 8, force=True))
+    try:
+        o = coexec.Orchestrator(lang.parse(src), SyntheticDataset(0), coexec.Mode.coexec, coexec.RunConfig(), be)
+        got, st = o.run()
+        plan = o.compiled.last_plan
+        assert plan.dp is not None and not plan.dp.replicated, plan.dp and plan.dp.reason
+        assert len(plan.dp.allreduce_nodes) >= 3
+    finally:
+        be.close()
+    assert st.counters() == ref_st.counters()
+    assert [float(x) for x in got.lines] == pytest.approx([float(x) for x in ref.lines], rel=1e-12)
+    for k, t in ref.vars.items():
+        assert abs(got.vars[k].data - t.data).max() <= 1e-12 * max(1.0, abs(t.data).max())
