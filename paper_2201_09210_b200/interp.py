@@ -29,7 +29,7 @@ from . import lang
 from .errors import CoexError, EvalError
 from .lang import ast
 from .natives import eval_native
-from .tensor import OpKind, Tensor, infer_shape, lift_host_value, shape_size
+from .tensor import OpKind, Tensor, canonical_attrs, infer_shape, lift_host_value, shape_size
 from .dataset import SyntheticTensor
 from .trace_graph import (Diverged, External, Handle, LoopEnter, LoopExit,
                           LoopIterStart, OpEvent, StepEnd)
@@ -80,6 +80,20 @@ class StepDiverged(Exception):
         self.pending = pending
 
 
+_KIND_VAL = {k: k.value for k in OpKind}
+_IN_KINDS = {(): (), (True,): ("h",), (False,): ("e",), (True, True): ("h", "h"), (True, False): ("h", "e"),
+             (False, True): ("e", "h"), (False, False): ("e", "e")}
+_SHAPE_CACHE: dict = {}
+_LOC_KEYS: dict = {}
+
+
+def _loc_key(loc) -> tuple:
+    k = _LOC_KEYS.get(loc)
+    if k is None:
+        k = _LOC_KEYS[loc] = (loc.stmt_id, loc.loop_path)
+    return k
+
+
 # ======================================================================= contexts
 
 
@@ -110,6 +124,9 @@ class EagerCtx:
             self.producer[hid] = len(self.trace)
             self.trace.append(OpEvent(kind, attrs, loc, refs, [hid], False, tuple(shape), tuple(in_shapes)))
         return Val(dev, hid, self.epoch, shape)
+
+    def op_site(self, site, args, shapes) -> Val:
+        return self.op(site[0], _NOATTRS, args, site[2], shapes)
 
     def op(self, kind: OpKind, attrs: dict, args: list, loc, shapes: list) -> Val:
         out_shape = infer_shape(kind, attrs, shapes)[0]
@@ -187,35 +204,84 @@ class SkeletonCtx:
             self.tg_nodes[nid] = n
         return n
 
-    def _advance(self, ev: OpEvent):
-        try:
-            adv = self.cursor.advance_op(ev)
-        except Diverged as d:
-            raise StepDiverged(d.why, ev) from None
-        for d in adv.decisions:
-            self.ch.decide(d)
-        return adv
-
     def _op(self, kind, attrs, loc, args, shape) -> Val:
-        refs, feeds = [], []
+        epoch = self.epoch
+        hids = []
+        feeds = None
         for p, v in enumerate(args):
-            if isinstance(v, Val) and v.epoch == self.epoch:
-                refs.append(Handle(v.hid))
+            if type(v) is Val and v.epoch == epoch:
+                hids.append(v.hid)
             else:
-                refs.append(External((loc.stmt_id, p)))
+                hids.append(None)
+                if feeds is None:
+                    feeds = []
                 feeds.append((p, v))
         hid = self.next_hid
-        self.next_hid += 1
-        adv = self._advance(OpEvent(kind, attrs, loc, refs, [hid]))
-        for p, v in feeds:
-            if isinstance(v, Val):
-                self.ch.feed((adv.node_id, p), v.dev)
-            else:
-                self.ch.feed((adv.node_id, p), v if is_tensor(v) else lift_host_value(v))
-        return Val(None, hid, self.epoch, shape)
+        self.next_hid = hid + 1
+        in_kinds = _IN_KINDS[tuple(h is not None for h in hids)]
+        key = ("op", _KIND_VAL[kind], canonical_attrs(attrs) if attrs else (), _loc_key(loc), in_kinds)
+        try:
+            nid, _, decisions = self.cursor.advance(key, hids, hid)
+        except Diverged as d:
+            refs = [Handle(h) if h is not None else External((loc.stmt_id, p)) for p, h in enumerate(hids)]
+            raise StepDiverged(d.why, OpEvent(kind, attrs, loc, refs, [hid])) from None
+        ch = self.ch
+        for d in decisions:
+            ch.decide(d)
+        if feeds is not None:
+            for p, v in feeds:
+                if isinstance(v, Val):
+                    ch.feed((nid, p), v.dev)
+                else:
+                    ch.feed((nid, p), v if is_tensor(v) else lift_host_value(v))
+        return Val(None, hid, epoch, shape)
+
+    def op_site(self, site, args, shapes) -> Val:
+        """Attr-less op from a compiled call site ``(kind, kind value, loc, loc key)``."""
+        kind, kval, loc, lkey = site
+        ck = (kval, tuple(shapes))
+        shape = _SHAPE_CACHE.get(ck)
+        if shape is None:
+            shape = _SHAPE_CACHE[ck] = infer_shape(kind, _NOATTRS, shapes)[0]
+        epoch = self.epoch
+        a0 = args[0]
+        h0 = a0.hid if (type(a0) is Val and a0.epoch == epoch) else None
+        if len(args) == 2:
+            a1 = args[1]
+            h1 = a1.hid if (type(a1) is Val and a1.epoch == epoch) else None
+            hids = [h0, h1]
+            in_kinds = ("h" if h0 is not None else "e", "h" if h1 is not None else "e")
+        else:
+            hids = [h0]
+            in_kinds = ("h",) if h0 is not None else ("e",)
+        hid = self.next_hid
+        self.next_hid = hid + 1
+        try:
+            nid, _, decisions = self.cursor.advance(("op", kval, (), lkey, in_kinds), hids, hid)
+        except Diverged as d:
+            refs = [Handle(h) if h is not None else External((loc.stmt_id, p)) for p, h in enumerate(hids)]
+            raise StepDiverged(d.why, OpEvent(kind, {}, loc, refs, [hid])) from None
+        ch = self.ch
+        for d in decisions:
+            ch.decide(d)
+        for p, h in enumerate(hids):
+            if h is None:
+                v = args[p]
+                if isinstance(v, Val):
+                    ch.feed((nid, p), v.dev)
+                else:
+                    ch.feed((nid, p), v if is_tensor(v) else lift_host_value(v))
+        return Val(None, hid, epoch, shape)
 
     def op(self, kind, attrs, args, loc, shapes) -> Val:
-        return self._op(kind, attrs, loc, args, infer_shape(kind, attrs, shapes)[0])
+        if attrs:
+            shape = infer_shape(kind, attrs, shapes)[0]
+        else:
+            ck = (kind, tuple(shapes))
+            shape = _SHAPE_CACHE.get(ck)
+            if shape is None:
+                shape = _SHAPE_CACHE[ck] = infer_shape(kind, attrs, shapes)[0]
+        return self._op(kind, attrs, loc, args, shape)
 
     def read_var(self, name, loc) -> Val:
         return self._op(OpKind.READ_VAR, {"var_name": name}, loc, [], self.var_shapes[name])
@@ -280,7 +346,13 @@ class SkeletonCtx:
 
 
 class Interp:
-    """Evaluator over a parsed :class:`~.lang.ast.Program`."""
+    """Evaluator over a parsed :class:`~.lang.ast.Program`.
+
+    Each AST node is compiled once into a Python closure ``f(ctx, env)``; a step
+    runs the closures of the step body.  Compilation resolves everything that
+    does not change between steps (variable vs local names, op kinds, constant
+    literals, prologue vs body), so the per-op host cost of the skeleton -- the
+    part that overlaps the device pass -- is a few closure calls."""
 
     def __init__(self, program: ast.Program, dataset, backend, seed: int = 0):
         self.prog = program
@@ -291,235 +363,353 @@ class Interp:
         self.out: list = []            # flushed printed lines
         self.prologue_env: dict = {}
         self.step = -1
+        self._body = self._c_block(program.body, False)
 
     # ------------------------------------------------------------------ driver API
     def run_prologue(self):
         self.step = -1
         env: dict = {}
         ctx = EagerCtx(self.be, -1, None)
-        self._block(self.prog.prologue, ctx, env, prologue=True)
+        for f in self._c_block(self.prog.prologue, True):
+            f(ctx, env)
         self.prologue_env = env
 
     def run_step(self, step: int, ctx) -> None:
         """Run the step body under ``ctx`` (raises StepDiverged in skeleton mode)."""
         self.step = step
         env = dict(self.prologue_env)
-        self._block(self.prog.body, ctx, env, prologue=False)
+        for f in self._body:
+            f(ctx, env)
         ctx.finish()
 
-    # ------------------------------------------------------------------ statements
     def _err(self, msg, node) -> EvalError:
         return EvalError(msg, self.step, node.pos.line, node.pos.col)
 
-    def _block(self, stmts, ctx, env, prologue):
-        for st in stmts:
-            self._stmt(st, ctx, env, prologue)
+    # ------------------------------------------------------------------ statements
+    def _c_block(self, stmts, prologue) -> list:
+        return [self._c_stmt(st, prologue) for st in stmts]
 
-    def _stmt(self, st, ctx, env, prologue):
+    def _wrap(self, st, body):
+        it = self
+
+        def run(ctx, env):
+            try:
+                body(ctx, env)
+            except (EvalError, StepDiverged):
+                raise
+            except CoexError as e:
+                raise it._err(str(e), st) from e
+
+        return run
+
+    def _c_cond(self, e, loc, st):
+        f = self._c_expr(e, loc)
+        it = self
+
+        def cond(ctx, env):
+            v = f(ctx, env)
+            if v is True or v is False:
+                return v
+            raise it._err(f"non-boolean condition ({fmt_value(v)})", st)
+
+        return cond
+
+    def _c_stmt(self, st, prologue):
         loc = st.loc()
-        try:
-            if isinstance(st, ast.VarDecl):
-                v = self._expr(st.expr, ctx, env, loc)
-                self.be.var_define(st.name, v.dev if isinstance(v, Val) else
-                                   (v if is_tensor(v) else lift_host_value(v)))
-            elif isinstance(st, (ast.LetDecl, ast.Assign)):
-                v = self._expr(st.expr, ctx, env, loc)
-                if isinstance(st, ast.Assign) and st.name in self.var_names:
-                    if not is_tensor(v):
-                        v = lift_host_value(v)
-                    if prologue:
-                        self.be.var_assign(st.name, v.dev if isinstance(v, Val) else self.be.put(v))
-                    else:
-                        ctx.assign_var(st.name, v, loc, tuple(v.shape))
+        be = self.be
+        if isinstance(st, ast.VarDecl):
+            f = self._c_expr(st.expr, loc)
+            name = st.name
+
+            def body(ctx, env):
+                v = f(ctx, env)
+                be.var_define(name, v.dev if isinstance(v, Val) else (v if is_tensor(v) else lift_host_value(v)))
+        elif isinstance(st, (ast.LetDecl, ast.Assign)):
+            f = self._c_expr(st.expr, loc)
+            name = st.name
+            if isinstance(st, ast.Assign) and name in self.var_names:
+                if prologue:
+                    def body(ctx, env):
+                        v = f(ctx, env)
+                        if not is_tensor(v):
+                            v = lift_host_value(v)
+                        be.var_assign(name, v.dev if isinstance(v, Val) else be.put(v))
                 else:
-                    env[st.name] = v
-            elif isinstance(st, ast.Print):
-                v = self._expr(st.expr, ctx, env, loc)
+                    def body(ctx, env):
+                        v = f(ctx, env)
+                        if not is_tensor(v):
+                            v = lift_host_value(v)
+                        ctx.assign_var(name, v, loc, tuple(v.shape))
+            else:
+                def body(ctx, env):
+                    env[name] = f(ctx, env)
+        elif isinstance(st, ast.Print):
+            f = self._c_expr(st.expr, loc)
+            it = self
+
+            def body(ctx, env):
+                v = f(ctx, env)
                 if is_tensor(v):
                     v = ctx.materialize(v).to_nested()
-                ctx.emit_print(self, fmt_value(v))
-            elif isinstance(st, ast.If):
-                if self._cond(st.cond, ctx, env, loc, st):
-                    self._block(st.then, ctx, env, prologue)
-                    return
-                for c, blk in st.elifs:
-                    if self._cond(c, ctx, env, loc, st):
-                        self._block(blk, ctx, env, prologue)
+                ctx.emit_print(it, fmt_value(v))
+        elif isinstance(st, ast.If):
+            arms = [(self._c_cond(st.cond, loc, st), self._c_block(st.then, prologue))]
+            arms += [(self._c_cond(c, loc, st), self._c_block(blk, prologue)) for c, blk in st.elifs]
+            orelse = self._c_block(st.orelse, prologue) if st.orelse is not None else None
+
+            def body(ctx, env):
+                for cond, blk in arms:
+                    if cond(ctx, env):
+                        for g in blk:
+                            g(ctx, env)
                         return
-                if st.orelse is not None:
-                    self._block(st.orelse, ctx, env, prologue)
-            elif isinstance(st, ast.While):
-                ctx.loop_enter(st.loop_id)
-                while self._cond(st.cond, ctx, env, loc, st):
-                    ctx.loop_iter(st.loop_id)
-                    self._block(st.body, ctx, env, prologue)
-                ctx.loop_exit(st.loop_id)
-            elif isinstance(st, ast.For):
-                n = self._expr(st.count, ctx, env, loc)
+                if orelse is not None:
+                    for g in orelse:
+                        g(ctx, env)
+        elif isinstance(st, ast.While):
+            cond = self._c_cond(st.cond, loc, st)
+            blk = self._c_block(st.body, prologue)
+            lid = st.loop_id
+
+            def body(ctx, env):
+                ctx.loop_enter(lid)
+                while cond(ctx, env):
+                    ctx.loop_iter(lid)
+                    for g in blk:
+                        g(ctx, env)
+                ctx.loop_exit(lid)
+        elif isinstance(st, ast.For):
+            cnt = self._c_expr(st.count, loc)
+            blk = self._c_block(st.body, prologue)
+            lid = st.loop_id
+            var = st.var
+            it = self
+
+            def body(ctx, env):
+                n = cnt(ctx, env)
                 if isinstance(n, float) and n.is_integer():
                     n = int(n)
                 if isinstance(n, bool) or not isinstance(n, int):
-                    raise self._err(f"range() count must be an integer, got {fmt_value(n)}", st)
-                ctx.loop_enter(st.loop_id)
+                    raise it._err(f"range() count must be an integer, got {fmt_value(n)}", st)
+                ctx.loop_enter(lid)
                 for i in range(n):
-                    ctx.loop_iter(st.loop_id)
-                    env[st.var] = i
-                    self._block(st.body, ctx, env, prologue)
-                ctx.loop_exit(st.loop_id)
-            else:  # pragma: no cover
-                raise self._err(f"unknown statement {type(st).__name__}", st)
-        except (EvalError, StepDiverged):
-            raise
-        except CoexError as e:
-            raise self._err(str(e), st) from e
-
-    def _cond(self, e, ctx, env, loc, st) -> bool:
-        v = self._expr(e, ctx, env, loc)
-        if not isinstance(v, bool):
-            raise self._err(f"non-boolean condition ({fmt_value(v)})", st)
-        return v
+                    ctx.loop_iter(lid)
+                    env[var] = i
+                    for g in blk:
+                        g(ctx, env)
+                ctx.loop_exit(lid)
+        else:  # pragma: no cover
+            raise self._err(f"unknown statement {type(st).__name__}", st)
+        return self._wrap(st, body)
 
     # ------------------------------------------------------------------ expressions
-    def _host(self, v, ctx, e):
-        if is_tensor(v):
-            raise self._err("tensor value in a host expression; use item()", e)
-        return v
+    def _host_fn(self, f, e):
+        it = self
 
-    def _expr(self, e, ctx, env, loc):
-        if isinstance(e, ast.Num):
-            return e.value
-        if isinstance(e, ast.Str):
-            return e.value
-        if isinstance(e, ast.Bool):
-            return e.value
+        def g(ctx, env):
+            v = f(ctx, env)
+            if isinstance(v, (Val, Tensor, SyntheticTensor)):
+                raise it._err("tensor value in a host expression; use item()", e)
+            return v
+
+        return g
+
+    def _c_expr(self, e, loc):
+        it = self
+        if isinstance(e, (ast.Num, ast.Str, ast.Bool)):
+            c = e.value
+            return lambda ctx, env: c
         if isinstance(e, ast.Ident):
-            if e.name in self.var_names:
-                if self.step < 0:
-                    return Val(self.be.var_read(e.name), -1, -1, self.be.var_shape(e.name))
-                return ctx.read_var(e.name, loc)
-            if e.name == "step":
-                return max(self.step, 0)
-            if e.name not in env:
-                raise self._err(f"undefined name {e.name!r}", e)
-            return env[e.name]
+            name = e.name
+            if name in self.var_names:
+                be = self.be
+
+                def var(ctx, env):
+                    if it.step < 0:
+                        return Val(be.var_read(name), -1, -1, be.var_shape(name))
+                    return ctx.read_var(name, loc)
+                return var
+            if name == "step":
+                return lambda ctx, env: max(it.step, 0)
+
+            def ident(ctx, env):
+                try:
+                    return env[name]
+                except KeyError:
+                    raise it._err(f"undefined name {name!r}", e) from None
+            return ident
         if isinstance(e, ast.OpCall):
-            return self._opcall(e, ctx, env, loc)
+            return self._c_opcall(e, loc)
         if isinstance(e, ast.Input):
-            shape = None if e.shape is None else self._shape(e.shape, ctx, env, loc)
-            return self.ds.next(e.name, shape, self.step)
+            shp = None if e.shape is None else self._c_shape(e.shape, loc)
+            name = e.name
+            ds = self.ds
+            if shp is None:
+                return lambda ctx, env: ds.next(name, None, it.step)
+            return lambda ctx, env: ds.next(name, shp(ctx, env), it.step)
         if isinstance(e, ast.Native):
-            args = [self._native_arg(self._expr(a, ctx, env, loc), ctx) for a in e.args]
-            return eval_native(e.name, args, self.seed, self.step)
+            fs = [self._c_expr(a, loc) for a in e.args]
+            name = e.name
+
+            def native(ctx, env):
+                args = []
+                for f in fs:
+                    v = f(ctx, env)
+                    args.append(ctx.materialize(v).to_nested() if is_tensor(v) else v)
+                return eval_native(name, args, it.seed, it.step)
+            return native
         if isinstance(e, ast.Item):
-            v = self._expr(e.operand, ctx, env, loc)
-            return ctx.materialize(v).to_nested() if is_tensor(v) else v
+            f = self._c_expr(e.operand, loc)
+
+            def item(ctx, env):
+                v = f(ctx, env)
+                return ctx.materialize(v).to_nested() if is_tensor(v) else v
+            return item
         if isinstance(e, ast.Not):
-            v = self._host(self._expr(e.operand, ctx, env, loc), ctx, e)
-            if not isinstance(v, bool):
-                raise self._err("'not' needs a boolean", e)
-            return not v
+            f = self._host_fn(self._c_expr(e.operand, loc), e)
+
+            def not_(ctx, env):
+                v = f(ctx, env)
+                if not isinstance(v, bool):
+                    raise it._err("'not' needs a boolean", e)
+                return not v
+            return not_
         if isinstance(e, ast.NegOp):
-            v = self._host(self._expr(e.operand, ctx, env, loc), ctx, e)
-            if isinstance(v, bool) or not isinstance(v, (int, float)):
-                raise self._err("unary '-' needs a number", e)
-            return -v
+            f = self._host_fn(self._c_expr(e.operand, loc), e)
+
+            def neg(ctx, env):
+                v = f(ctx, env)
+                if isinstance(v, bool) or not isinstance(v, (int, float)):
+                    raise it._err("unary '-' needs a number", e)
+                return -v
+            return neg
         if isinstance(e, ast.BinOp):
-            return self._binop(e, ctx, env, loc)
+            return self._c_binop(e, loc)
         if isinstance(e, ast.ShapeLit):     # a bracket literal outside a shape position: host list
-            return [self._host(self._expr(d, ctx, env, loc), ctx, d) for d in e.dims]
+            fs = [self._host_fn(self._c_expr(d, loc), d) for d in e.dims]
+            return lambda ctx, env: [f(ctx, env) for f in fs]
         raise self._err(f"unknown expression {type(e).__name__}", e)
 
-    def _native_arg(self, v, ctx):
-        if is_tensor(v):
-            return ctx.materialize(v).to_nested()
-        return v
-
-    def _binop(self, e, ctx, env, loc):
+    def _c_binop(self, e, loc):
+        it = self
         op = e.op
-        a = self._host(self._expr(e.left, ctx, env, loc), ctx, e)
+        fa = self._host_fn(self._c_expr(e.left, loc), e)
+        fb = self._host_fn(self._c_expr(e.right, loc), e)
         if op in ("and", "or"):
-            if not isinstance(a, bool):
-                raise self._err(f"'{op}' needs booleans", e)
-            if (op == "and" and not a) or (op == "or" and a):
-                return a
-            b = self._host(self._expr(e.right, ctx, env, loc), ctx, e)
-            if not isinstance(b, bool):
-                raise self._err(f"'{op}' needs booleans", e)
-            return b
-        b = self._host(self._expr(e.right, ctx, env, loc), ctx, e)
-        if op == "==":
-            return a == b
-        if op == "!=":
-            return a != b
-        num = (int, float)
-        if op == "+" and isinstance(a, str) and isinstance(b, str):
-            return a + b
-        if isinstance(a, bool) or isinstance(b, bool) or not isinstance(a, num) or not isinstance(b, num):
-            if op in ("<", "<=", ">", ">=") and isinstance(a, str) and isinstance(b, str):
-                pass
-            else:
-                raise self._err(f"operator '{op}' needs numbers, got {fmt_value(a)} and {fmt_value(b)}", e)
-        if op == "+":
-            return a + b
-        if op == "-":
-            return a - b
-        if op == "*":
-            return a * b
-        if op == "/":
-            if b == 0:
-                raise self._err("division by zero", e)
-            return a / b
-        if op == "<":
-            return a < b
-        if op == "<=":
-            return a <= b
-        if op == ">":
-            return a > b
-        if op == ">=":
-            return a >= b
-        raise self._err(f"unknown operator {op!r}", e)
+            want = op == "or"
 
-    def _shape(self, s: ast.ShapeLit, ctx, env, loc) -> tuple:
-        dims = []
-        for d in s.dims:
-            v = self._host(self._expr(d, ctx, env, loc), ctx, d)
-            if isinstance(v, float) and v.is_integer():
-                v = int(v)
-            if isinstance(v, bool) or not isinstance(v, int) or v < 0:
-                raise self._err(f"shape dimension must be a non-negative integer, got {fmt_value(v)}", d)
-            dims.append(v)
-        return tuple(dims)
+            def logic(ctx, env):
+                a = fa(ctx, env)
+                if not isinstance(a, bool):
+                    raise it._err(f"'{op}' needs booleans", e)
+                if a is want:
+                    return a
+                b = fb(ctx, env)
+                if not isinstance(b, bool):
+                    raise it._err(f"'{op}' needs booleans", e)
+                return b
+            return logic
+        if op == "==":
+            return lambda ctx, env: fa(ctx, env) == fb(ctx, env)
+        if op == "!=":
+            return lambda ctx, env: fa(ctx, env) != fb(ctx, env)
+        impl = _BINOPS[op]
+
+        def arith(ctx, env):
+            a = fa(ctx, env)
+            b = fb(ctx, env)
+            ta, tb = type(a), type(b)
+            if (ta is int or ta is float) and (tb is int or tb is float):
+                if op == "/" and b == 0:
+                    raise it._err("division by zero", e)
+                return impl(a, b)
+            if ta is str and tb is str and op in ("+", "<", "<=", ">", ">="):
+                return impl(a, b)
+            raise it._err(f"operator '{op}' needs numbers, got {fmt_value(a)} and {fmt_value(b)}", e)
+        return arith
+
+    def _c_shape(self, s: ast.ShapeLit, loc):
+        it = self
+        fs = [(self._host_fn(self._c_expr(d, loc), d), d) for d in s.dims]
+
+        def shape(ctx, env):
+            dims = []
+            for f, d in fs:
+                v = f(ctx, env)
+                if isinstance(v, float) and v.is_integer():
+                    v = int(v)
+                if isinstance(v, bool) or not isinstance(v, int) or v < 0:
+                    raise it._err(f"shape dimension must be a non-negative integer, got {fmt_value(v)}", d)
+                dims.append(v)
+            return tuple(dims)
+        return shape
 
     @staticmethod
     def _shape_of(v) -> tuple:
-        if isinstance(v, (Val, Tensor, SyntheticTensor)):
-            return tuple(v.shape)
+        t = type(v)
+        if t is Val or t is Tensor or t is SyntheticTensor:
+            return v.shape
         if isinstance(v, list):
             return lift_host_value(v).shape
         return ()
 
-    def _opcall(self, e: ast.OpCall, ctx, env, loc):
+    def _c_opcall(self, e: ast.OpCall, loc):
+        it = self
         name = e.name
         kind = OP_BY_NAME[name]
+        shape_of = self._shape_of
         if name == "fill":
-            shape = self._shape(e.args[0], ctx, env, loc)
-            val = self._host(self._expr(e.args[1], ctx, env, loc), ctx, e)
-            if isinstance(val, bool) or not isinstance(val, (int, float)):
-                raise self._err("fill value must be a number", e)
-            return ctx.op(kind, {"shape": shape, "value": float(val)}, [], loc, [])
-        x = self._expr(e.args[0], ctx, env, loc)
+            shp = self._c_shape(e.args[0], loc)
+            fv = self._host_fn(self._c_expr(e.args[1], loc), e)
+
+            def fill(ctx, env):
+                shape = shp(ctx, env)
+                val = fv(ctx, env)
+                if isinstance(val, bool) or not isinstance(val, (int, float)):
+                    raise it._err("fill value must be a number", e)
+                return ctx.op(kind, {"shape": shape, "value": float(val)}, [], loc, [])
+            return fill
+        fx = self._c_expr(e.args[0], loc)
         if name == "reshape":
-            tgt = self._shape(e.args[1], ctx, env, loc)
-            return ctx.op(kind, {"target_shape": tgt}, [x], loc, [self._shape_of(x)])
+            tgt = self._c_shape(e.args[1], loc)
+
+            def reshape(ctx, env):
+                x = fx(ctx, env)
+                return ctx.op(kind, {"target_shape": tgt(ctx, env)}, [x], loc, [shape_of(x)])
+            return reshape
         if name == "transpose":
-            shp = self._shape_of(x)
-            perm = self._shape(e.args[1], ctx, env, loc) if len(e.args) == 2 else tuple(reversed(range(len(shp))))
-            return ctx.op(kind, {"perm": tuple(perm)}, [x], loc, [shp])
-        args = [x] + [self._expr(a, ctx, env, loc) for a in e.args[1:]]
-        for a in args:
-            if isinstance(a, str):
-                raise self._err(f"{name}: string operand", e)
-        return ctx.op(kind, {}, args, loc, [self._shape_of(a) for a in args])
+            perm_f = self._c_shape(e.args[1], loc) if len(e.args) == 2 else None
+
+            def transpose(ctx, env):
+                x = fx(ctx, env)
+                shp = shape_of(x)
+                perm = perm_f(ctx, env) if perm_f is not None else tuple(range(len(shp) - 1, -1, -1))
+                return ctx.op(kind, {"perm": tuple(perm)}, [x], loc, [shp])
+            return transpose
+        site = (kind, kind.value, loc, (loc.stmt_id, loc.loop_path))
+        if len(e.args) == 1:
+            def unary(ctx, env):
+                x = fx(ctx, env)
+                if isinstance(x, str):
+                    raise it._err(f"{name}: string operand", e)
+                return ctx.op_site(site, [x], [shape_of(x)])
+            return unary
+        fy = self._c_expr(e.args[1], loc)
+
+        def binary(ctx, env):
+            x = fx(ctx, env)
+            y = fy(ctx, env)
+            if isinstance(x, str) or isinstance(y, str):
+                raise it._err(f"{name}: string operand", e)
+            return ctx.op_site(site, [x, y], [shape_of(x), shape_of(y)])
+        return binary
+
+
+_NOATTRS: dict = {}
+_BINOPS = {
+    "+": lambda a, b: a + b, "-": lambda a, b: a - b, "*": lambda a, b: a * b, "/": lambda a, b: a / b,
+    "<": lambda a, b: a < b, "<=": lambda a, b: a <= b, ">": lambda a, b: a > b, ">=": lambda a, b: a >= b,
+}
 
 
 def run_imperative(program, dataset, backend, config=None) -> "RunResult":

@@ -432,29 +432,54 @@ class Cursor:
         return decisions
 
     def advance_op(self, e: OpEvent) -> Advance:
+        hids = [r.id if isinstance(r, Handle) else None for r in e.inputs]
+        c, k, decisions = self.advance(e.key(), hids, e.outputs[0] if e.outputs else None)
+        for o in e.outputs[1:]:
+            self.handles[o] = self.handles[e.outputs[0]]
+        return Advance(c, k, decisions)
+
+    def advance(self, key: tuple, hids: list, out_hid) -> tuple:
+        """Fast path used by the skeleton: ``key`` is the op's equality key, ``hids`` the
+        handle id of each produced input (None for fed inputs).  Returns
+        (node id, execution index, decisions)."""
         decisions = self._replay_pending() if self.pending else []
-        f = self.top
-        c = f.g.child_with_key(f.cur, e.key())
+        f = self.stack[-1]
+        g = f.g
+        c = g.kids[f.cur].get(key)
         if c is None:
-            raise Diverged(f"no successor of node {f.cur} matches {e.kind.value}@{e.loc.stmt_id}")
-        node = f.g.nodes[c]
-        for pos, r in enumerate(e.inputs):
-            if isinstance(r, Handle):
-                prod, _, tick = self.handles[r.id]
+            raise Diverged(f"no successor of node {f.cur} matches {key[1]}@{key[3][0]}")
+        node = g.nodes[c]
+        last = self.last
+        for pos, h in enumerate(hids):
+            if h is not None:
+                prod, _, tick = self.handles[h]
                 cs = node.cands[pos]
-                if prod not in cs:
-                    raise Diverged(f"node {c} input {pos}: unseen producer {prod}")
-                latest = max(cs, key=lambda p: self.last.get(p, -1))
-                if latest != prod or self.last.get(prod) != tick:
+                if len(cs) == 1:
+                    if prod not in cs:
+                        raise Diverged(f"node {c} input {pos}: unseen producer {prod}")
+                else:
+                    if prod not in cs:
+                        raise Diverged(f"node {c} input {pos}: unseen producer {prod}")
+                    best = -1
+                    for q in cs:
+                        t = last.get(q, -1)
+                        if t > best:
+                            best = t
+                    if last.get(prod) != best:
+                        raise Diverged(f"node {c} input {pos}: producer is not the latest candidate")
+                if last.get(prod) != tick:
                     raise Diverged(f"node {c} input {pos}: producer is not the latest candidate")
-        self._leave(f, c, decisions)
+        succ = g.succ[f.cur]
+        if len(succ) > 1:
+            decisions.append(CaseDecision(f.cur, succ.index(c)))
+        f.cur = c
         k = self.execs.get(c, 0)
         self.execs[c] = k + 1
         self.clock += 1
-        self.last[c] = self.clock
-        for o in e.outputs:
-            self.handles[o] = (c, k, self.clock)
-        return Advance(c, k, decisions)
+        last[c] = self.clock
+        if out_hid is not None:
+            self.handles[out_hid] = (c, k, self.clock)
+        return c, k, decisions
 
     def producer_of(self, handle_id: int) -> tuple:
         nid, k, _ = self.handles[handle_id]
