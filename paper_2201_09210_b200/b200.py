@@ -17,6 +17,7 @@ from __future__ import annotations
 
 import ctypes
 import os
+import struct
 
 import numpy as np
 
@@ -27,6 +28,7 @@ from .runner_api import PassResult
 from .tensor import OpKind, Tensor, shape_size
 from .trace_graph import CaseDecision, LoopDecision
 
+_F64 = struct.Struct("<d")
 LIB_NAME = "libcoexb200.so"
 MAX_RANK = 8
 PRECISIONS = {"f64": 0, "fp32": 1, "bf16": 2}
@@ -334,6 +336,7 @@ class B200Program:
         self.graphs: dict = {}
         self.feed_shape: dict = {}       # slot -> expected shape (observed hints, updated on misses)
         self.dp_plan = None
+        self.varying: set = set()        # feed slots whose speculated constant missed
         for n in tg.all_nodes():
             if n.typ == "op":
                 for pos, s in n.feed_shapes.items():
@@ -343,7 +346,9 @@ class B200Program:
     def specialise(self):
         """The (graph handle, plan) for the current variable shapes."""
         vsh = {n: self.be.var_shape(n) for n in self.be.var_idx}
-        key = (tuple(sorted(vsh.items())), tuple(sorted(self.feed_shape.items())))
+        self.consts = self._const_slots()
+        key = (tuple(sorted(vsh.items())), tuple(sorted(self.feed_shape.items())),
+               tuple(sorted(self.consts.items())))
         hit = self.graphs.get(key)
         if hit is not None:
             return hit
@@ -356,6 +361,19 @@ class B200Program:
         self.graphs[key] = (handle, plan)
         self.last_plan = plan
         return handle, plan
+
+    def _const_slots(self) -> dict:
+        """Fed rank-0 host scalars that had one value in every trace: baked into the graph."""
+        from .trace_graph import VARIES
+        out = {}
+        for n in self.tg.all_nodes():
+            if n.typ != "op":
+                continue
+            for pos, v in n.feed_values.items():
+                slot = (n.id, pos)
+                if v is not VARIES and slot not in self.varying and tuple(n.feed_shapes.get(pos, (0,))) == ():
+                    out[slot] = v
+        return out
 
     def _plan(self, vsh):
         be = self.be
@@ -370,14 +388,16 @@ class B200Program:
             if not dplan.replicated:
                 try:
                     plan = Planner(dplan.sp, self.tg, be.var_idx, vsh, local_feed_shapes(self.feed_shape, dplan),
-                                   be.esize, bf16=bf16, force_store=dplan.allreduce_nodes).build()
+                                   be.esize, bf16=bf16, force_store=dplan.allreduce_nodes,
+                                   const_slots=self.consts).build()
                     plan.feed_shapes = dict(self.feed_shape)        # host checks global shapes
                     plan.sharded = set(dplan.sharded_slots)
                     plan.dp = dplan
                     return plan
                 except NeedsReplicated as e:
                     dplan.replicated, dplan.reason = True, str(e)
-        return Planner(self.sp, self.tg, be.var_idx, vsh, self.feed_shape, be.esize, bf16=bf16).build()
+        return Planner(self.sp, self.tg, be.var_idx, vsh, self.feed_shape, be.esize, bf16=bf16,
+                       const_slots=self.consts).build()
 
     def info(self, handle) -> dict:
         nk, nc, ab = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
@@ -436,6 +456,12 @@ class B200Pass:
             raise CoexError(f"unknown decision {d!r}")
 
     def feed(self, slot, v):
+        c = self.plan.const_slots.get(slot)
+        if c is not None:
+            if isinstance(v, Tensor) and v.shape == () and v.data.tobytes() == _F64.pack(c):
+                return                                     # speculated constant holds: nothing to send
+            self.prog.varying.add(slot)
+            raise ShapeMiss(f"feed slot {slot}: value differs from the constant baked into the graph")
         want = self.plan.feed_shapes.get(slot)
         shape = tuple(v.shape)
         if want is None or tuple(want) != shape:

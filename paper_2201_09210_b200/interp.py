@@ -117,12 +117,13 @@ class EagerCtx:
             refs.append(External((loc.stmt_id, pos)))
             devs.append(v.dev if isinstance(v, Val) else self.be.put(lift_host_value(v) if not is_tensor(v) else v))
 
-    def _emit(self, kind, attrs, loc, refs, dev, shape, in_shapes=()) -> Val:
+    def _emit(self, kind, attrs, loc, refs, dev, shape, in_shapes=(), in_values=None) -> Val:
         hid = self.next_hid
         self.next_hid += 1
         if self.trace is not None:
             self.producer[hid] = len(self.trace)
-            self.trace.append(OpEvent(kind, attrs, loc, refs, [hid], False, tuple(shape), tuple(in_shapes)))
+            self.trace.append(OpEvent(kind, attrs, loc, refs, [hid], False, tuple(shape), tuple(in_shapes),
+                                      in_values))
         return Val(dev, hid, self.epoch, shape)
 
     def op_site(self, site, args, shapes) -> Val:
@@ -134,7 +135,9 @@ class EagerCtx:
         for p, v in enumerate(args):
             self._arg(v, loc, p, refs, devs)
         dev = self.be.exec_op(kind, attrs, devs)
-        return self._emit(kind, attrs, loc, refs, dev, out_shape, [tuple(s) for s in shapes])
+        vals = tuple(float(v) if isinstance(v, (int, float)) else None for v in args) if self.trace is not None \
+            else None
+        return self._emit(kind, attrs, loc, refs, dev, out_shape, [tuple(s) for s in shapes], vals)
 
     def read_var(self, name: str, loc) -> Val:
         dev = self.be.var_read(name)

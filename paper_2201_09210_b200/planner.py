@@ -85,8 +85,9 @@ class Plan:
 
 class Planner:
     def __init__(self, sp: SymProgram, tg, var_index: dict, var_shapes: dict, feed_shapes: dict, esize: int,
-                 bf16: bool = False, fuse: bool = True, force_store=()):
+                 bf16: bool = False, fuse: bool = True, force_store=(), const_slots=None):
         self.force_store = set(force_store)
+        self.const_slots = dict(const_slots or {})
         self.bf16 = bf16
         self.fuse = fuse
         self.sp = sp
@@ -226,6 +227,9 @@ class Planner:
             slot_buf[slot] = new_buf(shape_size(shp) * self.esize)
             slot_cell[slot] = new_cell(slot_buf[slot])
             slot_rec[slot] = len(slot_rec)
+            if slot in self.const_slots:              # speculative constant: prefilled, never fed
+                consts.append(float(self.const_slots[slot]))
+                fills.append((slot_buf[slot], 1, len(consts) - 1))
         pubs: dict = {}
         for nid in ops:
             lst = [vcell[nid]] + [c for s, c in multi.items() if nid in s]
@@ -270,6 +274,8 @@ class Planner:
         self.chain_lates = 0
 
         def feed_item(x):
+            if x.slot in self.const_slots:
+                return None
             shp = tuple(self.feed_shapes[x.slot])
             return ([T_FEED, slot_code(x.slot), shape_size(shp), len(shp)] + _pad(shp)
                     + [slot_buf[x.slot], slot_cell[x.slot], slot_rec[x.slot]])
@@ -284,7 +290,9 @@ class Planner:
                 if kind_ == "chain":
                     run, feeds = seg
                     for f in feeds:
-                        items.append(feed_item(f))
+                        it = feed_item(f)
+                        if it is not None:
+                            items.append(it)
                     try:
                         items.append(self._chain_item(run, shapes, in_cell, node_buf, pubs, multi, n_compute))
                     except _TooWide:
@@ -292,7 +300,9 @@ class Planner:
                     continue
                 x = seg
                 if isinstance(x, InputFeed):
-                    items.append(feed_item(x))
+                    it = feed_item(x)
+                    if it is not None:
+                        items.append(it)
                 elif isinstance(x, OutputFetch):
                     shp = shapes[x.node_id]
                     items.append([T_FETCH, x.node_id, vcell[x.node_id], shape_size(shp), len(shp)] + _pad(shp))
@@ -339,7 +349,9 @@ class Planner:
         w += body
         sig = (tuple(sorted((k, tuple(v)) for k, v in self.var_shapes.items())),
                tuple(sorted((k, tuple(v)) for k, v in self.feed_shapes.items())))
-        return Plan(w, consts, sig, n_compute[0], flops[0], shapes, dict(self.feed_shapes), folded)
+        plan = Plan(w, consts, sig, n_compute[0], flops[0], shapes, dict(self.feed_shapes), folded)
+        plan.const_slots = dict(self.const_slots)
+        return plan
 
     def _exec(self, x, shapes, in_cell, out_words, ptr_item, pubs, multi, folded, n_compute, flops) -> list:
         nid = x.node_id

@@ -60,6 +60,7 @@ class OpEvent:
     fetch_after: bool = False
     out_shape: tuple | None = None      # observed shapes: specialisation hints, not part of the key
     in_shapes: tuple | None = None
+    in_values: tuple | None = None      # fed host scalars (float) per input, else None
 
     def key(self) -> tuple:
         return op_key(self.kind, self.attrs, self.loc, self.in_kinds())
@@ -86,6 +87,15 @@ class LoopExit:
 @dataclass(frozen=True)
 class StepEnd:
     pass
+
+
+VARIES = "varies"        # feed_values marker: the fed scalar changed between traces
+_UNSEEN = object()
+
+
+def _bits(v: float) -> bytes:
+    import struct
+    return struct.pack("<d", v)
 
 
 def op_key(kind, attrs, loc, in_kinds) -> tuple:
@@ -120,6 +130,7 @@ class Node:
     trip_counts: set = field(default_factory=set)
     out_shape: tuple | None = None      # last observed output shape (planner hint)
     feed_shapes: dict = field(default_factory=dict)   # input pos -> last observed fed shape
+    feed_values: dict = field(default_factory=dict)   # input pos -> the one host scalar ever fed, or VARIES
 
     def key(self) -> tuple:
         k = self.__dict__.get("_key")
@@ -318,6 +329,15 @@ class _Merger:
             for pos, k in enumerate(kinds):
                 if k == "e":
                     node.feed_shapes[pos] = tuple(e.in_shapes[pos])
+        if e.in_values is not None:
+            for pos, k in enumerate(kinds):
+                if k == "e":
+                    v = e.in_values[pos]
+                    old = node.feed_values.get(pos, _UNSEEN)
+                    if old is _UNSEEN:
+                        node.feed_values[pos] = v if v is not None else VARIES
+                    elif old is not VARIES and (v is None or _bits(v) != _bits(old)):
+                        node.feed_values[pos] = VARIES
         for o in e.outputs:
             self.hmap[o] = nid
         return nid
