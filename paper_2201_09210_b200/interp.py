@@ -26,7 +26,7 @@ from __future__ import annotations
 import time
 
 from . import lang
-from .errors import CoexError, EvalError
+from .errors import CoexError, EvalError, ShapeMiss
 from .lang import ast
 from .natives import eval_native
 from .tensor import OpKind, Tensor, canonical_attrs, infer_shape, lift_host_value, shape_size
@@ -398,7 +398,7 @@ class Interp:
         def run(ctx, env):
             try:
                 body(ctx, env)
-            except (EvalError, StepDiverged):
+            except (EvalError, StepDiverged, ShapeMiss):
                 raise
             except CoexError as e:
                 raise it._err(str(e), st) from e
