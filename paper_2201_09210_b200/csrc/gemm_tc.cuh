@@ -23,13 +23,14 @@
 namespace coex {
 
 constexpr int TC_BM = 128;
-constexpr int TC_BN = 128;
+constexpr int TC_BN = 256;          // 128 x 256 tile: 85 FLOP per operand byte (L2-bandwidth headroom)
 constexpr int TC_BK = 64;          // 64 bf16 = 128 B = one SWIZZLE_128B row
 constexpr int TC_STAGES = 4;
 constexpr int TC_THREADS = 192;
 constexpr int TC_A_BYTES = TC_BM * TC_BK * 2;
 constexpr int TC_B_BYTES = TC_BN * TC_BK * 2;
 constexpr int TC_SMEM = TC_STAGES * (TC_A_BYTES + TC_B_BYTES) + 1024 /*align*/ + 256 /*barriers*/;
+constexpr int TC_GROUP_M = 16;      // tile rasterisation: 16 M-tiles sweep N together (L2 reuse)
 
 struct CvtParams {
   DevState* ds;
@@ -129,8 +130,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc(const __grid_constant
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const long long tiles_n = (p.N + TC_BN - 1) / TC_BN;
-  const int m0 = (int)((blockIdx.x / tiles_n) * TC_BM);
-  const int n0 = (int)((blockIdx.x % tiles_n) * TC_BN);
+  const long long tiles_m = (p.M + TC_BM - 1) / TC_BM;
+  // grouped rasterisation: consecutive CTAs cover a TC_GROUP_M x tiles_n band
+  const long long t = blockIdx.x;
+  const long long group = (long long)TC_GROUP_M * tiles_n;
+  const long long first_m = (t / group) * TC_GROUP_M;
+  const long long gm = min((long long)TC_GROUP_M, tiles_m - first_m);
+  const int m0 = (int)((first_m + (t % group) % gm) * TC_BM);
+  const int n0 = (int)(((t % group) / gm) * TC_BN);
   const int nk = (int)((p.K + TC_BK - 1) / TC_BK);
 
   float* C = pick_out<float>(p.out, res<float>(p.a), res<float>(p.b));
