@@ -42,7 +42,9 @@ struct CvtParams {
   __nv_bfloat16* dst[2];
 };
 
-// Operand conversion: grid.y selects the operand.
+// Operand conversion: grid.y selects the operand.  Direct operands stream rows
+// (coalesced on both sides); transposed operands go through a 32x33 shared-memory
+// tile so both the strided read and the K-major write stay coalesced.
 __global__ void __launch_bounds__(256) k_cvt_bf16(CvtParams p) {
   stamp(p.ds, SK_FUSED);
   if (skip(p.ds)) return;
@@ -50,13 +52,31 @@ __global__ void __launch_bounds__(256) k_cvt_bf16(CvtParams p) {
   const float* s = res<float>(p.src[w]);
   __nv_bfloat16* d = p.dst[w];
   const long long R = p.rows[w], K = p.K, ld = p.ld;
-  const long long n = R * ld;
-  const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-    const long long r = i / ld, k = i - r * ld;
-    float v = 0.f;
-    if (k < K) v = p.trans[w] ? s[k * R + r] : s[r * K + k];
-    d[i] = __float2bfloat16_rn(v);
+  if (!p.trans[w]) {
+    const long long n = R * ld;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+      const long long r = i / ld, k = i - r * ld;
+      d[i] = __float2bfloat16_rn(k < K ? s[r * K + k] : 0.f);
+    }
+    return;
+  }
+  // element (r, k) = s[k * R + r]: tiles of 32 k x 32 r
+  __shared__ float tile[32][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;   // 32 x 8
+  const long long tr = (R + 31) / 32, tk = (ld + 31) / 32;
+  for (long long t = blockIdx.x; t < tr * tk; t += gridDim.x) {
+    const long long r0 = (t % tr) * 32, k0 = (t / tr) * 32;
+    for (int j = ty; j < 32; j += 8) {
+      const long long k = k0 + j, r = r0 + tx;
+      tile[j][tx] = (k < K && r < R) ? s[k * R + r] : 0.f;
+    }
+    __syncthreads();
+    for (int j = ty; j < 32; j += 8) {
+      const long long r = r0 + j, k = k0 + tx;
+      if (r < R && k < ld) d[r * ld + k] = __float2bfloat16_rn(tile[tx][j]);
+    }
+    __syncthreads();
   }
 }
 
