@@ -53,11 +53,16 @@ __global__ void __launch_bounds__(256) k_cvt_bf16(CvtParams p) {
   __nv_bfloat16* d = p.dst[w];
   const long long R = p.rows[w], K = p.K, ld = p.ld;
   if (!p.trans[w]) {
-    const long long n = R * ld;
-    const long long stride = (long long)gridDim.x * blockDim.x;
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-      const long long r = i / ld, k = i - r * ld;
-      d[i] = __float2bfloat16_rn(k < K ? s[r * K + k] : 0.f);
+    // one row per block iteration, 8 consecutive k per thread, one 16-byte store
+    for (long long r = blockIdx.x; r < R; r += gridDim.x) {
+      const float* src = s + r * K;
+      __nv_bfloat16* dst = d + r * ld;
+      for (long long k = (long long)threadIdx.x * 8; k < ld; k += (long long)blockDim.x * 8) {
+        __align__(16) __nv_bfloat16 v[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = __float2bfloat16_rn(k + j < K ? src[k + j] : 0.f);
+        *(uint4*)(dst + k) = *(const uint4*)v;
+      }
     }
     return;
   }

@@ -487,9 +487,12 @@ int build_launches(coex_ctx* c, const OpSpec& s, Launch* L, int* nL) {
   cv.trans[1] = s.trans_b ? 0 : 1;     // B stored [K][N] -> B^T read; folded: stored [N][K]
   cv.dst[0] = (__nv_bfloat16*)s.scratch[0];
   cv.dst[1] = (__nv_bfloat16*)s.scratch[1];
-  const int64_t big = (M > N ? M : N) * cv.ld;
-  dim3 g = grid_for(big);
-  g.y = 2;
+  // direct operands: one row per block; transposed operands: one 32x32 tile per block
+  const int64_t rows_max = M > N ? M : N;
+  const int64_t tiles_max = ((rows_max + 31) / 32) * ((cv.ld + 31) / 32);
+  int64_t gx = rows_max > tiles_max ? rows_max : tiles_max;
+  if (gx > (int64_t)kNumSMs * 16) gx = (int64_t)kNumSMs * 16;
+  dim3 g((unsigned)(gx > 0 ? gx : 1), 2);
   L[0].set((void*)k_cvt_bf16, g, dim3(256), cv);
   TcGemmParams gp;
   memset(&gp, 0, sizeof(gp));
