@@ -181,6 +181,26 @@ def roofline(be, hbm_peak, tflops_peak, peak_kind):
             "all_kernels_ms": {k: round(v, 5) for k, v in times.items()}}
 
 
+def tensor_gemm(peak_tflops, peak_kind, size: int = 8192):
+    """The tcgen05 bf16 GEMM of the bf16 precision mode (the path's dense contraction on the
+    tensor cores), timed through the C-ABI with CUDA events, fp32->bf16 operand conversion
+    included.  Reported beside the C1 line: C1 itself runs the f64 parity path."""
+    import numpy as np
+    from paper_2201_09210_b200.b200 import B200Backend
+    be = B200Backend(precision="bf16")
+    try:
+        r = np.random.default_rng(size)
+        a = be.put(Tensor((size, size), r.uniform(-1, 1, (size, size))))
+        b = be.put(Tensor((size, size), r.uniform(-1, 1, (size, size))))
+        ms = be.time_op(OpKind.MATMUL, {}, [a, b], reps=10)
+    finally:
+        be.close()
+    tf = 2 * size ** 3 / (ms * 1e-3) / 1e12
+    return {"bound": "tensor", "kernel": f"k_cvt_bf16 + k_gemm_tc {size}^3 bf16->fp32", "achieved": round(tf, 2),
+            "peak": peak_tflops, "unit": "TFLOP/s", "frac": round(tf / peak_tflops, 4), "peak_source": peak_kind,
+            "ms": round(ms, 4)}
+
+
 def cpu_baseline(steps: int = 12):
     """CPU oracle co-execution of C1 on this host (bounded sample)."""
     from oracle.cpu_backend import CpuBackend
@@ -280,6 +300,7 @@ def run_b200(args):
     if rank == 0:
         roof = roofline(be, hbm, tfl, peak_kind)
         base = cpu_baseline(12) if world == 1 and not args.no_cpu_baseline else None
+        tgemm = tensor_gemm(tfl, peak_kind) if not args.no_tensor_gemm else None
         st = o.stats
         line = {
             "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -295,6 +316,7 @@ def run_b200(args):
                        "tracing_steps_before_coexec": pre, "steps_replayed_in_timed_region": replays,
                        "algorithmic_flops_per_step": c1_flops(**C1)},
             "roofline": roof,
+            "tensor_gemm": tgemm,
             "cpu_baseline": base,
             "e2e": {"value": round(world * args.steps / (e2e_max * 1e-3), 3), "unit": UNIT,
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
@@ -320,6 +342,7 @@ def main():
     ap.add_argument("--precision", default="f64", choices=["f64", "fp32", "bf16"])
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-tensor-gemm", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
