@@ -131,9 +131,14 @@ __host__ __device__ __forceinline__ unsigned long long seq_of(unsigned long long
 struct In {
   const void* direct;
   void* const* cell;
+  void* const* ovl;      // variable operand: overlay slot (set by an in-pass AssignVar) read first
 };
 template <typename T>
 __device__ __forceinline__ const T* res(const In& x) {
+  if (x.ovl != nullptr) {
+    const void* o = *x.ovl;
+    if (o != nullptr) return (const T*)o;
+  }
   return (const T*)(x.cell ? *x.cell : x.direct);
 }
 

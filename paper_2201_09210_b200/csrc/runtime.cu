@@ -1038,6 +1038,31 @@ struct Builder {
     if (i < 0 || i >= p->ncells) throw std::runtime_error("bad cell index");
     return p->cells + i;
   }
+  // operand codes: >= 0 program cell; -1 none; -(1000 + v) variable v (overlay, then committed)
+  In operand(int64_t ci) {
+    In x{nullptr, nullptr, nullptr};
+    if (ci >= 0) {
+      x.cell = cell(ci);
+    } else if (ci <= -1000 && ci > -2000) {
+      const int64_t v = -1000 - ci;
+      if (v >= kMaxVars) throw std::runtime_error("bad variable operand");
+      x.cell = c->d_var_cur + v;
+      x.ovl = c->d_var_ovl + v;
+    } else if (ci != -1) {
+      throw std::runtime_error("bad operand code");
+    }
+    return x;
+  }
+  // publish codes: >= 0 program cell; -(2000 + v) variable v's overlay slot (a folded AssignVar)
+  void** pubcell(int64_t ci) {
+    if (ci >= 0) return cell(ci);
+    if (ci <= -2000) {
+      const int64_t v = -2000 - ci;
+      if (v >= kMaxVars) throw std::runtime_error("bad variable publish code");
+      return c->d_var_ovl + v;
+    }
+    throw std::runtime_error("bad publish code");
+  }
   char* buf(int64_t i) {
     if (i < 0) return nullptr;
     if (i >= (int64_t)bufs.size()) throw std::runtime_error("bad buffer index");
@@ -1069,7 +1094,7 @@ struct Builder {
     o.npub = (int)np;
     for (int i = 0; i < kMaxPub; ++i) {
       int64_t ci = next();
-      o.pub[i] = (i < np) ? cell(ci) : nullptr;
+      o.pub[i] = (i < np) ? pubcell(ci) : nullptr;
     }
     o.late = late ? p->late + (n_late++) : nullptr;
   }
@@ -1094,8 +1119,7 @@ struct Builder {
         next();  // node id (diagnostics)
         for (int i = 0; i < 2; ++i) {
           int64_t ci = next();
-          s.in[i].cell = ci >= 0 ? cell(ci) : nullptr;
-          s.in[i].direct = nullptr;
+          s.in[i] = operand(ci);
         }
         for (int i = 0; i < 2; ++i) {
           s.in_ndim[i] = (int)next();
@@ -1134,14 +1158,13 @@ struct Builder {
         q.red_npub = (int)next();
         for (int i = 0; i < kChainPub; ++i) {
           int64_t ci = next();
-          q.red_pub[i] = i < q.red_npub ? cell(ci) : nullptr;
+          q.red_pub[i] = i < q.red_npub ? pubcell(ci) : nullptr;
         }
         const int64_t late = next();
         q.nin = (int)next();
         for (int i = 0; i < kChainIn; ++i) {
           int64_t ci = next();
-          q.in[i].cell = (i < q.nin) ? cell(ci) : nullptr;
-          q.in[i].direct = nullptr;
+          q.in[i] = (i < q.nin) ? operand(ci) : In{nullptr, nullptr, nullptr};
           q.in_scalar[i] = (unsigned char)next();
         }
         q.nops = (int)next();
@@ -1158,7 +1181,7 @@ struct Builder {
           q.npub[j] = (unsigned char)next();
           for (int i = 0; i < kChainPub; ++i) {
             int64_t ci = next();
-            q.pub[j][i] = (j < q.nout && i < q.npub[j]) ? cell(ci) : nullptr;
+            q.pub[j][i] = (j < q.nout && i < q.npub[j]) ? pubcell(ci) : nullptr;
           }
         }
         if (q.nin > kChainIn || q.nops > kChainOps || q.nout > kChainOut) throw std::runtime_error("chain too wide");
@@ -1202,7 +1225,7 @@ struct Builder {
         q.op = (int)next();
         next();  // node id
         int64_t ci = next();
-        q.a.cell = ci >= 0 ? cell(ci) : nullptr;
+        q.a = operand(ci);
         int64_t vi = next();
         q.shape_id = (int)next();
         if (vi >= 0) {
@@ -1255,7 +1278,7 @@ struct Builder {
         q.ds = c->d_state;
         q.mb = c->d_mb;
         q.node = next();
-        q.a.cell = cell(next());
+        q.a = operand(next());
         q.numel = next();
         q.ndim = (int)next();
         for (int d = 0; d < COEX_MAX_RANK; ++d) q.shape[d] = next();
@@ -1696,12 +1719,7 @@ int coex_pass_wait(coex_prog* p, coex_pass_stats* st) {
       v.t.buf = v.spare;
       v.spare = (old && old->refs == 1) ? old : nullptr;
       if (v.spare == nullptr) release(c, old);
-      auto sh = p->var_shapes.find((int)mb->var_shape_id[vi]);
-      if (sh != p->var_shapes.end()) {
-        v.t.ndim = (int)sh->second.size();
-        for (int d = 0; d < v.t.ndim; ++d) v.t.shape[d] = sh->second[d];
-        v.t.numel = numel_of(v.t.ndim, v.t.shape);
-      }
+      // graph-mode assignments are shape-stable (the planner rejects shape changes)
       c->h_var_cur[vi] = v.t.buf->ptr;
     }
   }

@@ -181,6 +181,7 @@ class Planner:
                         and _fold_is_local(self.sp.body, nid, x.inputs[0].cands[0]):
                     folded.add(nid)
         self.folded = folded
+        self.elided_reads, self.folded_assigns = self._pointer_rewrites(consumers, multi, folded)
 
         bufs: list = []
 
@@ -232,16 +233,22 @@ class Planner:
                 fills.append((slot_buf[slot], 1, len(consts) - 1))
         pubs: dict = {}
         for nid in ops:
-            lst = [vcell[nid]] + [c for s, c in multi.items() if nid in s]
+            pubs[nid] = [vcell[nid]] + [c for s, c in multi.items() if nid in s]
+        for a_nid, p_nid in self.folded_assigns.items():
+            v = self.var_index[ops[a_nid].attrs["var_name"]]
+            pubs[p_nid] = pubs[p_nid] + [-(2000 + v)] + pubs[a_nid]
+        for nid, lst in pubs.items():
             if len(lst) > MAX_PUB:
                 raise ShapeMiss(f"node {nid} publishes to {len(lst)} cells (max {MAX_PUB})")
-            pubs[nid] = lst
 
         def in_cell(b):
             if b.fed:
                 return slot_cell[b.slot]
             if len(b.cands) == 1:
-                return vcell[b.cands[0]]
+                c = b.cands[0]
+                if c in self.elided_reads:
+                    return -(1000 + self.var_index[ops[c].attrs["var_name"]])
+                return vcell[c]
             return multi[frozenset(b.cands)]
 
         # variables assigned by the program (committed at pass end)
@@ -363,7 +370,11 @@ class Planner:
         if k is OpKind.RESHAPE:
             return [ptr_item(PTR_ALIAS, nid, in_cell(x.inputs[0]), -1, -1)]
         if k is OpKind.READ_VAR:
+            if nid in self.elided_reads:
+                return []
             return [ptr_item(PTR_READ_VAR, nid, -1, self.var_index[x.attrs["var_name"]], -1)]
+        if k is OpKind.ASSIGN_VAR and nid in self.folded_assigns:
+            return []
         if k is OpKind.ASSIGN_VAR:
             s = shapes[nid]
             return [ptr_item(PTR_ASSIGN_VAR, nid, in_cell(x.inputs[0]), self.var_index[x.attrs["var_name"]],
@@ -386,7 +397,7 @@ class Planner:
         while len(cells) < 2:
             cells.append(-1)
             in_shapes.append(())
-        late = any(c in pubs[nid] for c in cells if c >= 0)
+        late = _conflicts(cells, pubs[nid])
         attr_dims = list(x.attrs.get("perm", ()))
         out_shape = shapes[nid]
         n_compute[0] += 1
@@ -406,6 +417,38 @@ class Planner:
             word += [-1, -1]
         word += out_words(nid, late)
         return [word]
+
+    # ------------------------------------------------------------ pointer-op rewrites
+    def _pointer_rewrites(self, consumers, multi, folded):
+        """ReadVar nodes whose consumers all follow them in the same instruction list with no
+        assignment to the variable in between read the variable directly (no pointer kernel);
+        an AssignVar that directly follows its producer is folded into the producer's publish
+        list (the producer writes the variable's overlay slot)."""
+        ops = self.ops
+        multi_nodes = {n for s_ in multi for n in s_}
+        elided, fold = set(), {}
+        lists = list(_lists(self.sp.body))
+        for nid, x in ops.items():
+            if x.kind is OpKind.READ_VAR and nid not in self.sp.fetch_nodes and nid not in multi_nodes \
+                    and nid not in self.force_store:
+                var = x.attrs["var_name"]
+                cons = consumers.get(nid, [])
+                if not cons or any(len(b.cands) != 1 for c in cons for b in c.inputs if not b.fed and nid in b.cands):
+                    continue
+                cids = {c.node_id for c in cons}
+                if all(_reads_local(L, nid, cids, var) for L in lists):
+                    elided.add(nid)
+        for nid, x in ops.items():
+            if x.kind is not OpKind.ASSIGN_VAR or x.inputs[0].fed or len(x.inputs[0].cands) != 1:
+                continue
+            p = x.inputs[0].cands[0]
+            px = ops.get(p)
+            if px is None or px.kind not in COMPUTE or p in folded or p in self.force_store:
+                continue
+            var = x.attrs["var_name"]
+            if all(_assign_local(L, p, nid, var) for L in lists):
+                fold[nid] = p
+        return elided, fold
 
     # ------------------------------------------------------------ fusion
     def _segments(self, insts, shapes, folded) -> list:
@@ -492,7 +535,7 @@ class Planner:
         pub_cells = {c for _, _, p in outs for c in p}
         if red is not None:
             pub_cells |= set(pubs[red.node_id])
-        late = int(any(c in pub_cells for c, _ in inputs))
+        late = int(_conflicts([c for c, _ in inputs], pub_cells))
         self.chain_lates += late
         n_compute[0] += 1
         self.n_chains += 1
@@ -605,3 +648,79 @@ class _TooWide(Exception):
 
 class NeedsReplicated(Exception):
     """A sharded plan cannot be lowered (e.g. all-reduce of a pointer-only value)."""
+
+
+def _conflicts(in_codes, pub_codes) -> bool:
+    """A kernel must publish late if it reads a cell it publishes, or reads a variable whose
+    overlay slot it publishes (a folded AssignVar of a variable the op itself reads)."""
+    pubs = set(pub_codes)
+    for c in in_codes:
+        if c is None or c == -1:
+            continue
+        if c >= 0 and c in pubs:
+            return True
+        if -2000 < c <= -1000 and -(2000 + (-1000 - c)) in pubs:
+            return True
+    return False
+
+
+def _lists(insts):
+    yield insts
+    for x in insts:
+        if isinstance(x, SwitchCase):
+            for c in x.cases:
+                yield from _lists(c)
+        elif isinstance(x, While):
+            yield from _lists(x.body)
+        elif isinstance(x, UnrolledLoop):
+            for b in x.bodies:
+                yield from _lists(b)
+
+
+def _touches_var(x, var) -> bool:
+    return any(isinstance(y, ExecOp) and y.kind in (OpKind.READ_VAR, OpKind.ASSIGN_VAR)
+               and y.attrs.get("var_name") == var for y in walk([x]))
+
+
+def _assigns_var(x, var) -> bool:
+    return any(isinstance(y, ExecOp) and y.kind is OpKind.ASSIGN_VAR and y.attrs.get("var_name") == var
+               for y in walk([x]))
+
+
+def _reads_local(L, rid, cids, var) -> bool:
+    """Every consumer instance in list L has an instance of ReadVar ``rid`` earlier in L with
+    no assignment to ``var`` in between; consumers nested below L are checked in their lists."""
+    last = None
+    for j, x in enumerate(L):
+        if isinstance(x, ExecOp) and x.node_id == rid:
+            last = j
+        elif _assigns_var(x, var):
+            last = None
+        if isinstance(x, ExecOp) and x.node_id in cids:
+            if last is None:
+                return False
+    return True
+
+
+def _assign_local(L, pid, aid, var) -> bool:
+    """In list L every instance of producer ``pid`` is followed by AssignVar ``aid`` and every
+    instance of ``aid`` is preceded by ``pid`` with only plain ops (none touching ``var``) between."""
+    pending = None
+    for j, x in enumerate(L):
+        if isinstance(x, ExecOp) and x.node_id == pid:
+            if pending is not None:
+                return False
+            pending = j
+            continue
+        if isinstance(x, ExecOp) and x.node_id == aid:
+            if pending is None:
+                return False
+            pending = None
+            continue
+        if pending is not None:
+            if not isinstance(x, (ExecOp, InputFeed, OutputFetch)) or _touches_var(x, var):
+                return False
+        elif any(isinstance(y, ExecOp) and y.node_id in (pid, aid) for y in walk([x])) and \
+                not isinstance(x, ExecOp):
+            pass                      # nested instances are checked in their own list
+    return pending is None
