@@ -47,10 +47,22 @@ enum coex_status {
   COEX_INVALID = 10          /* bad handle / argument */
 };
 
-/* OpKind codes (order of coex.tensor.OpKind, tensor.py:30-44). */
+/* OpKind codes (order of coex.tensor.OpKind, tensor.py:30-44), followed by the extension
+ * op set for configs C2-C5 (no reference counterpart -- semantics in
+ * oracle/kernels.py).  Extension ops take up to 3 tensor inputs; convolutions carry
+ * [kernel, stride, pad] in coex_attrs.dims[0..2]; NHWC layout, weights [k*k*Cin, Cout]. */
 enum coex_opkind {
   COEX_MATMUL = 0, COEX_ADD, COEX_SUB, COEX_MUL, COEX_NEG, COEX_RELU, COEX_SIGMOID,
-  COEX_SUM, COEX_MEAN, COEX_TRANSPOSE, COEX_RESHAPE, COEX_FILL, COEX_READ_VAR, COEX_ASSIGN_VAR
+  COEX_SUM, COEX_MEAN, COEX_TRANSPOSE, COEX_RESHAPE, COEX_FILL, COEX_READ_VAR, COEX_ASSIGN_VAR,
+  COEX_CONV2D = 14,        /* (x [N,H,W,C], w [k*k*C, F]) -> [N,Ho,Wo,F] */
+  COEX_CONV2D_T,           /* (x [N,H,W,C], w [k*k*F, C]) -> [N,(H-1)s-2p+k,..,F] (conv2d input grad) */
+  COEX_CONV2D_DW,          /* (x [N,H,W,C], dy [N,Ho,Wo,F]) -> [k*k*C, F] (conv2d weight grad) */
+  COEX_BATCHNORM,          /* (x [..,C], gamma [C], beta [C]) -> batch-statistics normalisation */
+  COEX_BATCHNORM_DX,       /* (x, gamma, dy) -> dx */
+  COEX_BN_DGAMMA,          /* (x, dy) -> [C] = sum_rows(dy * xhat) */
+  COEX_SUM_ROWS,           /* (x [..,C]) -> [C] */
+  COEX_TANH, COEX_LEAKY_RELU, COEX_RELU_GRAD, COEX_LEAKY_RELU_GRAD, COEX_BCE_TERM,
+  COEX_NUM_KINDS
 };
 
 /* Device storage / arithmetic precision of a context. */

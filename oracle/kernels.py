@@ -10,6 +10,20 @@ Follows pkg/src/coex/tensor.py:228-291 operation by operation:
 * ADD/SUB/MUL with rank-0 broadcast, NEG, RELU (np.maximum: NaN kept, -0 -> +0),
   SIGMOID as 1/(1+exp(-x)) with overflow ignored (tensor.py:261-270).
 * TRANSPOSE materialised, RESHAPE, FILL, ASSIGN_VAR identity (tensor.py:278-285).
+
+Extension op set (configs C2-C5, SURVEY §2.4 / §8(a) row a*): the reference has no
+such ops, so these are the builder's f64 definitions -- parity UNPINNED by the
+reference; written in tensor.py's style (explicit orders):
+
+* CONV2D = MATMUL(im2col(x), w) with the im2col column order (ky, kx, c) and
+  zero padding; CONV2D_T = col2im(MATMUL(x, w^T)) summing the (ky, kx)
+  contributions in ascending order from +0.0; CONV2D_DW =
+  MATMUL(im2col(x)^T, dy) (sequential over output pixels).
+* BATCHNORM / BATCHNORM_DX / BN_DGAMMA / SUM_ROWS: per-channel (last axis)
+  statistics over all leading rows, sequential row order from +0.0; biased
+  variance of the centred values, eps = 1e-5.
+* TANH, LEAKY_RELU (slope 0.2), RELU_GRAD, LEAKY_RELU_GRAD, BCE_TERM
+  (max(x,0) - x*t + log1p(exp(-|x|))) elementwise.
 """
 
 from __future__ import annotations
@@ -17,7 +31,7 @@ from __future__ import annotations
 import numpy as np
 
 from paper_2201_09210_b200.errors import BadAttrs, ShapeMismatch
-from paper_2201_09210_b200.tensor import OpKind, Tensor, infer_shape
+from paper_2201_09210_b200.tensor import BN_EPS, LEAKY_SLOPE, OpKind, Tensor, infer_shape
 
 
 def matmul_seq(a: np.ndarray, b: np.ndarray) -> np.ndarray:
@@ -35,7 +49,107 @@ def sum_seq(x: np.ndarray) -> float:
     return float(np.cumsum(flat)[-1]) + 0.0
 
 
+def im2col(x: np.ndarray, k: int, s: int, p: int) -> np.ndarray:
+    """[N,H,W,C] -> [N*Ho*Wo, k*k*C], column (ky, kx, c), zero padding."""
+    n, h, w, c = x.shape
+    ho, wo = (h + 2 * p - k) // s + 1, (w + 2 * p - k) // s + 1
+    xp = np.zeros((n, h + 2 * p, w + 2 * p, c), dtype=np.float64)
+    xp[:, p:p + h, p:p + w, :] = x
+    cols = np.empty((n, ho, wo, k, k, c), dtype=np.float64)
+    for ky in range(k):
+        for kx in range(k):
+            cols[:, :, :, ky, kx, :] = xp[:, ky:ky + s * (ho - 1) + 1:s, kx:kx + s * (wo - 1) + 1:s, :]
+    return cols.reshape(n * ho * wo, k * k * c)
+
+
+def col2im(cols: np.ndarray, x_shape, k: int, s: int, p: int, out_shape) -> np.ndarray:
+    """Adjoint of im2col for conv2d_t: cols [N*H*W, k*k*F] -> [N,Ho,Wo,F]; output
+    (oy, ox) sums cols[(iy, ix), (ky, kx)] with oy = iy*s - p + ky, (ky, kx) ascending."""
+    n, h, w, _ = x_shape
+    _, ho, wo, f = out_shape
+    c6 = cols.reshape(n, h, w, k, k, f)
+    out = np.zeros((n, ho, wo, f), dtype=np.float64)
+    for ky in range(k):
+        for kx in range(k):
+            # input pixel iy lands on output row iy*s - p + ky
+            oy0, ox0 = ky - p, kx - p
+            iy = [i for i in range(h) if 0 <= i * s + oy0 < ho]
+            ix = [i for i in range(w) if 0 <= i * s + ox0 < wo]
+            if not iy or not ix:
+                continue
+            iy_lo, iy_hi, ix_lo, ix_hi = iy[0], iy[-1] + 1, ix[0], ix[-1] + 1
+            oys = slice(iy_lo * s + oy0, (iy_hi - 1) * s + oy0 + 1, s)
+            oxs = slice(ix_lo * s + ox0, (ix_hi - 1) * s + ox0 + 1, s)
+            out[:, oys, oxs, :] += c6[:, iy_lo:iy_hi, ix_lo:ix_hi, ky, kx, :]
+    return out + 0.0
+
+
+def col_sum_seq(x2: np.ndarray) -> np.ndarray:
+    """Per-column sum over rows in row order from +0.0 (np.cumsum along axis 0 is sequential)."""
+    if x2.shape[0] == 0:
+        return np.zeros(x2.shape[1])
+    return np.cumsum(x2, axis=0)[-1] + 0.0
+
+
+def bn_stats(x2: np.ndarray):
+    r = x2.shape[0]
+    mean = col_sum_seq(x2) / r
+    d = x2 - mean
+    var = col_sum_seq(d * d) / r
+    rstd = 1.0 / np.sqrt(var + BN_EPS)
+    return d, rstd
+
+
+def ext_kernel(kind: OpKind, attrs: dict, x: list, out_shape) -> np.ndarray:
+    if kind is OpKind.CONV2D:
+        k, s, p = attrs["conv"]
+        return matmul_seq(im2col(x[0], k, s, p), x[1]).reshape(out_shape)
+    if kind is OpKind.CONV2D_T:
+        k, s, p = attrs["conv"]
+        n, h, w, c = x[0].shape
+        cols = matmul_seq(x[0].reshape(n * h * w, c), np.ascontiguousarray(x[1].T))
+        return col2im(cols, x[0].shape, k, s, p, out_shape)
+    if kind is OpKind.CONV2D_DW:
+        k, s, p = attrs["conv"]
+        a = im2col(x[0], k, s, p)
+        f = x[1].shape[3]
+        return matmul_seq(np.ascontiguousarray(a.T), x[1].reshape(-1, f))
+    if kind in (OpKind.BATCHNORM, OpKind.BATCHNORM_DX, OpKind.BN_DGAMMA, OpKind.SUM_ROWS):
+        c = x[0].shape[-1]
+        x2 = x[0].reshape(-1, c)
+        if kind is OpKind.SUM_ROWS:
+            return col_sum_seq(x2)
+        d, rstd = bn_stats(x2)
+        xhat = d * rstd
+        if kind is OpKind.BATCHNORM:
+            return ((xhat * x[1]) + x[2]).reshape(out_shape)
+        dy = x[-1].reshape(-1, c)
+        if kind is OpKind.BN_DGAMMA:
+            return col_sum_seq(dy * xhat)
+        r = x2.shape[0]
+        t = dy - col_sum_seq(dy) / r
+        t = t - xhat * (col_sum_seq(dy * xhat) / r)
+        return (t * (x[1] * rstd)).reshape(out_shape)
+    a = x[0]
+    if kind is OpKind.TANH:
+        return np.tanh(a)
+    if kind is OpKind.LEAKY_RELU:
+        return np.where(a > 0.0, a, a * LEAKY_SLOPE)
+    b = x[1]
+    if kind is OpKind.RELU_GRAD:
+        return np.broadcast_to(np.where(a > 0.0, b, 0.0), out_shape)
+    if kind is OpKind.LEAKY_RELU_GRAD:
+        return np.broadcast_to(np.where(a > 0.0, b, b * LEAKY_SLOPE), out_shape)
+    if kind is OpKind.BCE_TERM:
+        with np.errstate(over="ignore"):
+            return np.broadcast_to((np.maximum(a, 0.0) - a * b) + np.log1p(np.exp(-np.abs(a))), out_shape)
+    raise BadAttrs(f"unknown op kind {kind!r}")  # pragma: no cover
+
+
 _BINARY = {OpKind.ADD: np.add, OpKind.SUB: np.subtract, OpKind.MUL: np.multiply}
+
+
+EXT = frozenset(tuple(OpKind)[14:])
 
 
 def execute_kernel(kind: OpKind, attrs: dict, inputs: list, var_shapes=None) -> list:
@@ -70,6 +184,8 @@ def execute_kernel(kind: OpKind, attrs: dict, inputs: list, var_shapes=None) -> 
         r = np.full(attrs["shape"], attrs["value"], dtype=np.float64)
     elif kind is OpKind.ASSIGN_VAR:
         return [inputs[0]]
+    elif kind in EXT:
+        r = ext_kernel(kind, attrs, x, out_shape)
     else:  # pragma: no cover
         raise BadAttrs(f"unknown op kind {kind!r}")
     return [Tensor(out_shape, r)]

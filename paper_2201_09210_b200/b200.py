@@ -25,7 +25,7 @@ from .dataset import SyntheticTensor
 from .errors import STATUS, ChannelClosed, CoexError, DeviceError, ShapeMiss
 from .planner import Planner, slot_code
 from .runner_api import PassResult
-from .tensor import OpKind, Tensor, shape_size
+from .tensor import CONV_KINDS, OpKind, Tensor, shape_size
 from .trace_graph import CaseDecision, LoopDecision
 
 _F64 = struct.Struct("<d")
@@ -137,6 +137,8 @@ def _attrs(kind: OpKind, attrs: dict) -> CoexAttrs:
     elif kind is OpKind.FILL:
         dims = attrs["shape"]
         at.value = float(attrs["value"])
+    elif kind in CONV_KINDS:
+        dims = attrs["conv"]
     else:
         dims = ()
     if len(dims) > MAX_RANK:
@@ -242,7 +244,7 @@ class B200Backend:
         """Average device ms of one launch of ``kind`` (CUDA events on the context stream)."""
         devs = [self.put(v) for v in values]
         at = _attrs(kind, attrs)
-        ids = (ctypes.c_int64 * 2)(*[d.id for d in devs], *([0] * (2 - len(devs))))
+        ids = (ctypes.c_int64 * 3)(*[d.id for d in devs], *([0] * (3 - len(devs))))
         ms = ctypes.c_double()
         _check(self.lib.coex_exec_op_timed(self.ctx, kind.code, ctypes.byref(at), len(devs), ids, reps,
                                            ctypes.byref(ms)))
@@ -277,7 +279,7 @@ class B200Backend:
     def exec_op(self, kind: OpKind, attrs: dict, values: list) -> DevTensor:
         devs = [self.put(v) for v in values]
         at = _attrs(kind, attrs)
-        ids = (ctypes.c_int64 * 2)(*[d.id for d in devs], *([0] * (2 - len(devs))))
+        ids = (ctypes.c_int64 * 3)(*[d.id for d in devs], *([0] * (3 - len(devs))))
         out = ctypes.c_int64()
         _check(self.lib.coex_exec_op(self.ctx, kind.code, ctypes.byref(at), len(devs), ids, ctypes.byref(out)))
         nd = ctypes.c_int()

@@ -25,12 +25,19 @@ namespace coex {
 constexpr int TC_BM = 128;
 constexpr int TC_BN = 256;          // 128 x 256 tile: 85 FLOP per operand byte (L2-bandwidth headroom)
 constexpr int TC_BK = 64;          // 64 bf16 = 128 B = one SWIZZLE_128B row
-constexpr int TC_STAGES = 4;
 constexpr int TC_THREADS = 192;
 constexpr int TC_A_BYTES = TC_BM * TC_BK * 2;
-constexpr int TC_B_BYTES = TC_BN * TC_BK * 2;
-constexpr int TC_SMEM = TC_STAGES * (TC_A_BYTES + TC_B_BYTES) + 1024 /*align*/ + 256 /*barriers*/;
 constexpr int TC_GROUP_M = 16;      // tile rasterisation: 16 M-tiles sweep N together (L2 reuse)
+// Narrow-N variants (convolution GEMMs have N = Cout in 64..512): BN in {64, 128, 256};
+// the stage count grows as the B tile shrinks so every variant keeps ~192 KB in flight.
+template <int BN> struct TcCfg {
+  static constexpr int STAGES = BN == 256 ? 4 : BN == 128 ? 6 : 8;
+  static constexpr int B_BYTES = BN * TC_BK * 2;
+  static constexpr int SMEM = STAGES * (TC_A_BYTES + B_BYTES) + 1024 /*align*/ + 256 /*barriers*/;
+};
+constexpr int TC_STAGES = TcCfg<TC_BN>::STAGES;
+constexpr int TC_B_BYTES = TcCfg<TC_BN>::B_BYTES;
+constexpr int TC_SMEM = TcCfg<TC_BN>::SMEM;
 
 struct CvtParams {
   DevState* ds;
@@ -92,6 +99,8 @@ struct TcGemmParams {
   In a, b;                   // original operands (ping-pong output choice only)
   long long M, N, K;
   Out out;
+  float* raw;                // non-null: write here (no publication) -- scratch / split-K slices
+  int splits;                // split-K: CTA (tile, split) covers k-blocks of its slice, raw + split*M*N
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -141,36 +150,48 @@ __host__ __device__ constexpr uint32_t idesc_bf16_f32(int M, int N) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
+template <int BN>
 __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc(const __grid_constant__ TcGemmParams p) {
+  constexpr int STAGES = TcCfg<BN>::STAGES;
+  constexpr int B_BYTES = TcCfg<BN>::B_BYTES;
   stamp(p.ds, SK_MATMUL);
   if (skip(p.ds)) return;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   unsigned char* sA = smem;
-  unsigned char* sB = smem + TC_STAGES * TC_A_BYTES;
-  uint64_t* full = (uint64_t*)(sB + TC_STAGES * TC_B_BYTES);
-  uint64_t* empty = full + TC_STAGES;
-  uint64_t* tmem_full = empty + TC_STAGES;
+  unsigned char* sB = smem + STAGES * TC_A_BYTES;
+  uint64_t* full = (uint64_t*)(sB + STAGES * B_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tmem_full = empty + STAGES;
   uint32_t* tmem_slot = (uint32_t*)(tmem_full + 1);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const long long tiles_n = (p.N + TC_BN - 1) / TC_BN;
+  const long long tiles_n = (p.N + BN - 1) / BN;
   const long long tiles_m = (p.M + TC_BM - 1) / TC_BM;
   // grouped rasterisation: consecutive CTAs cover a TC_GROUP_M x tiles_n band
-  const long long t = blockIdx.x;
+  const int splits = p.splits > 1 ? p.splits : 1;
+  const int split = (int)(blockIdx.x % splits);
+  const long long t = blockIdx.x / splits;
   const long long group = (long long)TC_GROUP_M * tiles_n;
   const long long first_m = (t / group) * TC_GROUP_M;
   const long long gm = min((long long)TC_GROUP_M, tiles_m - first_m);
   const int m0 = (int)((first_m + (t % group) % gm) * TC_BM);
-  const int n0 = (int)(((t % group) / gm) * TC_BN);
-  const int nk = (int)((p.K + TC_BK - 1) / TC_BK);
+  const int n0 = (int)(((t % group) / gm) * BN);
+  const int nk_all = (int)((p.K + TC_BK - 1) / TC_BK);
+  const int kb0 = (int)((long long)nk_all * split / splits);
+  const int nk = (int)((long long)nk_all * (split + 1) / splits) - kb0;
 
-  float* C = pick_out<float>(p.out, res<float>(p.a), res<float>(p.b));
-  publish_early(p.out, C);
-  count_op(p.ds);
+  float* C;
+  if (p.raw != nullptr) {
+    C = p.raw + (long long)split * p.M * p.N;
+  } else {
+    C = pick_out<float>(p.out, res<float>(p.a), res<float>(p.b));
+    publish_early(p.out, C);
+  }
+  if (split == 0) count_op(p.ds);
 
   if (warp == 0 && lane == 0) {
-    for (int s = 0; s < TC_STAGES; ++s) {
+    for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
@@ -181,7 +202,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc(const __grid_constant
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(TC_BN)
+                 "r"(BN)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
@@ -193,24 +214,24 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc(const __grid_constant
   if (warp == 0) {
     if (lane == 0) {
       for (int kb = 0; kb < nk; ++kb) {
-        const int s = kb % TC_STAGES;
-        const uint32_t ph = (uint32_t)((kb / TC_STAGES) & 1);
+        const int s = kb % STAGES;
+        const uint32_t ph = (uint32_t)((kb / STAGES) & 1);
         mbar_wait(&empty[s], ph ^ 1u);
-        mbar_expect_tx(&full[s], TC_A_BYTES + TC_B_BYTES);
-        tma_load_2d(sA + s * TC_A_BYTES, &p.tmA, &full[s], kb * TC_BK, m0);
-        tma_load_2d(sB + s * TC_B_BYTES, &p.tmB, &full[s], kb * TC_BK, n0);
+        mbar_expect_tx(&full[s], TC_A_BYTES + B_BYTES);
+        tma_load_2d(sA + s * TC_A_BYTES, &p.tmA, &full[s], (kb0 + kb) * TC_BK, m0);
+        tma_load_2d(sB + s * B_BYTES, &p.tmB, &full[s], (kb0 + kb) * TC_BK, n0);
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      constexpr uint32_t idesc = idesc_bf16_f32(TC_BM, TC_BN);
+      constexpr uint32_t idesc = idesc_bf16_f32(TC_BM, BN);
       for (int kb = 0; kb < nk; ++kb) {
-        const int s = kb % TC_STAGES;
-        const uint32_t ph = (uint32_t)((kb / TC_STAGES) & 1);
+        const int s = kb % STAGES;
+        const uint32_t ph = (uint32_t)((kb / STAGES) & 1);
         mbar_wait(&full[s], ph);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint64_t da = smem_desc_k_sw128(sA + s * TC_A_BYTES);
-        const uint64_t db = smem_desc_k_sw128(sB + s * TC_B_BYTES);
+        const uint64_t db = smem_desc_k_sw128(sB + s * B_BYTES);
 #pragma unroll
         for (int k = 0; k < TC_BK / 16; ++k) {
           const uint32_t acc = (kb > 0 || k > 0) ? 1u : 0u;
@@ -239,7 +260,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc(const __grid_constant
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     }
 #pragma unroll 1
-    for (int c = 0; c < TC_BN; c += 16) {
+    for (int c = 0; c < BN; c += 16) {
       uint32_t r[16];
       if (nk > 0) {
         const uint32_t taddr = tmem + ((uint32_t)lane_base << 16) + (uint32_t)c;
@@ -271,9 +292,41 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc(const __grid_constant
   __syncthreads();
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TC_BN) : "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BN) : "memory");
   }
-  publish_late(p.out, C);
+  if (p.raw == nullptr) publish_late(p.out, C);
+}
+
+// Split-K reduction: out[i] = sum of the S fp32 slices in slice order (deterministic).
+struct SplitReduceParams {
+  DevState* ds;
+  const float* ws;
+  long long n;               // M * N
+  int splits;
+  In a, b;                   // node operands (ping-pong output choice only)
+  Out out;
+};
+__global__ void __launch_bounds__(256) k_splitk_reduce(SplitReduceParams p) {
+  stamp(p.ds, SK_MATMUL);
+  if (skip(p.ds)) return;
+  float* o = pick_out<float>(p.out, res<float>(p.a), p.b.cell || p.b.direct ? res<float>(p.b) : nullptr);
+  publish_early(p.out, o);
+  const long long n4 = p.n / 4;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
+    float4 acc = ((const float4*)p.ws)[i];
+    for (int s = 1; s < p.splits; ++s) {
+      const float4 v = ((const float4*)(p.ws + (long long)s * p.n))[i];
+      acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+    }
+    ((float4*)o)[i] = acc;
+  }
+  for (long long i = n4 * 4 + (long long)blockIdx.x * blockDim.x + threadIdx.x; i < p.n; i += stride) {
+    float acc = p.ws[i];
+    for (int s = 1; s < p.splits; ++s) acc += p.ws[(long long)s * p.n + i];
+    o[i] = acc;
+  }
+  publish_late(p.out, o);
 }
 
 }  // namespace coex

@@ -184,7 +184,13 @@ __device__ __forceinline__ void count_op(DevState* ds) {
 
 // ------------------------------------------------------------------ elementwise
 // ADD/SUB/MUL with rank-0 broadcast (tensor.py:121-128, 261-263); NEG/RELU/SIGMOID (tensor.py:264-270).
-enum EwOp { EW_ADD = 0, EW_SUB = 1, EW_MUL = 2, EW_NEG = 3, EW_RELU = 4, EW_SIGMOID = 5, EW_COPY = 6 };
+// Extension elementwise ops (configs C2-C5, oracle/kernels.py ext_kernel): TANH, LEAKY_RELU
+// (slope 0.2), RELU_GRAD(x, dy), LEAKY_RELU_GRAD(x, dy), BCE_TERM(x, t).
+enum EwOp { EW_ADD = 0, EW_SUB = 1, EW_MUL = 2, EW_NEG = 3, EW_RELU = 4, EW_SIGMOID = 5, EW_COPY = 6,
+            EW_TANH = 7, EW_LRELU = 8, EW_RELU_GRAD = 9, EW_LRELU_GRAD = 10, EW_BCE = 11 };
+constexpr double kLeakySlope = 0.2;
+
+__host__ __device__ __forceinline__ bool ew_binary(int op) { return op <= EW_MUL || op >= EW_RELU_GRAD; }
 
 __device__ __forceinline__ double ew_apply(int op, double a, double b) {
   switch (op) {
@@ -194,6 +200,11 @@ __device__ __forceinline__ double ew_apply(int op, double a, double b) {
     case EW_NEG: return -a;
     case EW_RELU: return (a > 0.0 || a != a) ? a : 0.0;        // np.maximum(x, 0): NaN kept, -0 -> +0
     case EW_SIGMOID: return __ddiv_rn(1.0, __dadd_rn(1.0, exp(-a)));
+    case EW_TANH: return tanh(a);
+    case EW_LRELU: return a > 0.0 ? a : __dmul_rn(a, kLeakySlope);
+    case EW_RELU_GRAD: return a > 0.0 ? b : 0.0;
+    case EW_LRELU_GRAD: return a > 0.0 ? b : __dmul_rn(b, kLeakySlope);
+    case EW_BCE: return __dadd_rn(__dsub_rn(a > 0.0 ? a : 0.0, __dmul_rn(a, b)), log1p(exp(-fabs(a))));
     default: return a;
   }
 }
@@ -205,6 +216,11 @@ __device__ __forceinline__ float ew_apply(int op, float a, float b) {
     case EW_NEG: return -a;
     case EW_RELU: return (a > 0.0f || a != a) ? a : 0.0f;
     case EW_SIGMOID: return __fdiv_rn(1.0f, __fadd_rn(1.0f, expf(-a)));
+    case EW_TANH: return tanhf(a);
+    case EW_LRELU: return a > 0.0f ? a : __fmul_rn(a, (float)kLeakySlope);
+    case EW_RELU_GRAD: return a > 0.0f ? b : 0.0f;
+    case EW_LRELU_GRAD: return a > 0.0f ? b : __fmul_rn(b, (float)kLeakySlope);
+    case EW_BCE: return __fadd_rn(__fsub_rn(a > 0.0f ? a : 0.0f, __fmul_rn(a, b)), log1pf(expf(-fabsf(a))));
     default: return a;
   }
 }
@@ -223,7 +239,7 @@ __global__ void __launch_bounds__(256) k_elementwise(EwParams p) {
   stamp(p.ds, SK_EW);
   if (skip(p.ds)) return;
   const T* a = res<T>(p.a);
-  const T* b = (p.op <= EW_MUL) ? res<T>(p.b) : nullptr;
+  const T* b = ew_binary(p.op) ? res<T>(p.b) : nullptr;
   T* o = pick_out<T>(p.out, a, b);
   publish_early(p.out, o);
   count_op(p.ds);
@@ -651,7 +667,7 @@ __device__ __forceinline__ void chain_eval(const ChainParams& p, T* r, const T* 
   for (int k = 0; k < p.nops; ++k) {
     const ChainOp o = p.ops[k];
     r[o.dst] = ew_apply((int)o.op, chain_src(p, r, ip, sv, o.a, i),
-                        o.op <= EW_MUL ? chain_src(p, r, ip, sv, o.b, i) : T(0));
+                        ew_binary(o.op) ? chain_src(p, r, ip, sv, o.b, i) : T(0));
   }
 }
 

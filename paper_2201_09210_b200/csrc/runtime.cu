@@ -28,6 +28,7 @@
 #include "../../include/coex_b200.h"
 #include "kernels.cuh"
 #include "gemm_tc.cuh"
+#include "ext_ops.cuh"
 
 #include <cudaTypedefs.h>
 #include <dlfcn.h>
@@ -213,10 +214,15 @@ void mat_square(const unsigned long long* in, unsigned long long* out) {
 }
 
 // ---- shape inference (tensor.py:131-187) ----
+int infer_ext(int kind, const coex_attrs* at, const TRec* in, int* ndim, int64_t* shape);
+
 int infer(int kind, const coex_attrs* at, int nin, const TRec* in, int* ndim, int64_t* shape) {
-  static const int arity[] = {2, 2, 2, 2, 1, 1, 1, 1, 1, 1, 1, 0, 0, 1};
-  if (kind < 0 || kind > COEX_ASSIGN_VAR) return fail(COEX_BAD_ATTRS, "unknown op kind");
+  static const int arity[] = {2, 2, 2, 2, 1, 1, 1, 1, 1, 1, 1, 0, 0, 1,
+                              2, 2, 2, 3, 3, 2, 1, 1, 1, 2, 2, 2};
+  static_assert(sizeof(arity) / sizeof(arity[0]) == COEX_NUM_KINDS, "arity table");
+  if (kind < 0 || kind >= COEX_NUM_KINDS) return fail(COEX_BAD_ATTRS, "unknown op kind");
   if (nin != arity[kind]) return fail(COEX_BAD_ATTRS, "wrong number of tensor inputs");
+  if (kind >= COEX_CONV2D) return infer_ext(kind, at, in, ndim, shape);
   switch (kind) {
     case COEX_ADD: case COEX_SUB: case COEX_MUL: {
       const TRec &a = in[0], &b = in[1];
@@ -274,12 +280,86 @@ int infer(int kind, const coex_attrs* at, int nin, const TRec* in, int* ndim, in
   }
 }
 
+// Extension op shapes (paper_2201_09210_b200/tensor.py _conv_shape / infer_shape).
+int infer_ext(int kind, const coex_attrs* at, const TRec* in, int* ndim, int64_t* shape) {
+  auto same = [](const TRec& a, const TRec& b) {
+    if (a.ndim != b.ndim) return false;
+    for (int i = 0; i < a.ndim; ++i)
+      if (a.shape[i] != b.shape[i]) return false;
+    return true;
+  };
+  switch (kind) {
+    case COEX_TANH: case COEX_LEAKY_RELU:
+      *ndim = in[0].ndim;
+      memcpy(shape, in[0].shape, sizeof(int64_t) * in[0].ndim);
+      return COEX_OK;
+    case COEX_RELU_GRAD: case COEX_LEAKY_RELU_GRAD: case COEX_BCE_TERM: {
+      const TRec &a = in[0], &b = in[1];
+      if (!(same(a, b) || a.ndim == 0 || b.ndim == 0)) return fail(COEX_SHAPE_MISMATCH, "elementwise: incompatible shapes");
+      const TRec& r = (same(a, b) || b.ndim == 0) ? a : b;
+      *ndim = r.ndim;
+      memcpy(shape, r.shape, sizeof(int64_t) * r.ndim);
+      return COEX_OK;
+    }
+    case COEX_BATCHNORM: case COEX_BATCHNORM_DX: case COEX_BN_DGAMMA: case COEX_SUM_ROWS: {
+      const TRec& x = in[0];
+      if (x.ndim < 1 || x.numel == 0) return fail(COEX_SHAPE_MISMATCH, "column op: non-empty operand of rank >= 1 required");
+      const int64_t C = x.shape[x.ndim - 1];
+      if (C > (int64_t)kColMaxSlots * 256) return fail(COEX_SHAPE_MISMATCH, "column op: more than 2048 channels");
+      if (kind == COEX_SUM_ROWS || kind == COEX_BN_DGAMMA) {
+        if (kind == COEX_BN_DGAMMA && !same(x, in[1])) return fail(COEX_SHAPE_MISMATCH, "bn_dgamma: dy differs from x");
+        *ndim = 1;
+        shape[0] = C;
+        return COEX_OK;
+      }
+      if (in[1].ndim != 1 || in[1].shape[0] != C) return fail(COEX_SHAPE_MISMATCH, "batchnorm: gamma must be [C]");
+      if (kind == COEX_BATCHNORM && (in[2].ndim != 1 || in[2].shape[0] != C))
+        return fail(COEX_SHAPE_MISMATCH, "batchnorm: beta must be [C]");
+      if (kind == COEX_BATCHNORM_DX && !same(x, in[2])) return fail(COEX_SHAPE_MISMATCH, "batchnorm_dx: dy differs from x");
+      *ndim = x.ndim;
+      memcpy(shape, x.shape, sizeof(int64_t) * x.ndim);
+      return COEX_OK;
+    }
+    default: break;
+  }
+  // convolutions
+  if (at == nullptr || at->n != 3 || at->dims[0] < 1 || at->dims[1] < 1 || at->dims[2] < 0)
+    return fail(COEX_BAD_ATTRS, "conv: attribute [kernel, stride, pad] expected");
+  const int64_t k = at->dims[0], st = at->dims[1], pd = at->dims[2];
+  const TRec &x = in[0], &w = in[1];
+  if (x.ndim != 4) return fail(COEX_SHAPE_MISMATCH, "conv: rank-4 NHWC input required");
+  const int64_t N = x.shape[0], H = x.shape[1], W = x.shape[2], C = x.shape[3];
+  *ndim = 4;
+  if (kind == COEX_CONV2D_T) {
+    if (w.ndim != 2 || w.shape[1] != C || w.shape[0] % (k * k)) return fail(COEX_SHAPE_MISMATCH, "conv2d_t: weight mismatch");
+    const int64_t Ho = (H - 1) * st - 2 * pd + k, Wo = (W - 1) * st - 2 * pd + k;
+    if (H < 1 || W < 1 || Ho < 1 || Wo < 1) return fail(COEX_SHAPE_MISMATCH, "conv2d_t: empty output");
+    shape[0] = N; shape[1] = Ho; shape[2] = Wo; shape[3] = w.shape[0] / (k * k);
+    return COEX_OK;
+  }
+  if (H + 2 * pd < k || W + 2 * pd < k) return fail(COEX_SHAPE_MISMATCH, "conv: kernel larger than padded input");
+  const int64_t Ho = (H + 2 * pd - k) / st + 1, Wo = (W + 2 * pd - k) / st + 1;
+  if (kind == COEX_CONV2D) {
+    if (w.ndim != 2 || w.shape[0] != k * k * C) return fail(COEX_SHAPE_MISMATCH, "conv2d: weight mismatch");
+    shape[0] = N; shape[1] = Ho; shape[2] = Wo; shape[3] = w.shape[1];
+    return COEX_OK;
+  }
+  if (w.ndim != 4 || w.shape[0] != N || w.shape[1] != Ho || w.shape[2] != Wo)
+    return fail(COEX_SHAPE_MISMATCH, "conv2d_dw: gradient does not match the output geometry");
+  *ndim = 2;
+  shape[0] = k * k * C;
+  shape[1] = w.shape[3];
+  return COEX_OK;
+}
+
 // ---- kernel selection, shared by eager launches and graph nodes ----
+constexpr int kMaxIn = 3;
 struct OpSpec {
   int kind = 0;
-  In in[2] = {{nullptr, nullptr}, {nullptr, nullptr}};
-  int in_ndim[2] = {0, 0};
-  int64_t in_shape[2][COEX_MAX_RANK] = {{0}};
+  int nin = 0;
+  In in[kMaxIn] = {{nullptr, nullptr, nullptr}, {nullptr, nullptr, nullptr}, {nullptr, nullptr, nullptr}};
+  int in_ndim[kMaxIn] = {0, 0, 0};
+  int64_t in_shape[kMaxIn][COEX_MAX_RANK] = {{0}};
   int out_ndim = 0;
   int64_t out_shape[COEX_MAX_RANK] = {0};
   int attr_n = 0;
@@ -287,9 +367,27 @@ struct OpSpec {
   double value = 0.0;
   int trans_a = 0, trans_b = 0;
   void* scratch[2] = {nullptr, nullptr};   // bf16 K-major operand copies (tcgen05 path)
+  char* ws = nullptr;                      // extension ops: workspace base (nullptr = size query)
   Out out{};
   DevState* ds = nullptr;
 };
+
+bool is_ext_compute(int kind) { return kind >= COEX_CONV2D && kind <= COEX_SUM_ROWS; }
+int ew_code(int kind) {
+  switch (kind) {
+    case COEX_ADD: return EW_ADD;
+    case COEX_SUB: return EW_SUB;
+    case COEX_MUL: return EW_MUL;
+    case COEX_NEG: return EW_NEG;
+    case COEX_RELU: return EW_RELU;
+    case COEX_SIGMOID: return EW_SIGMOID;
+    case COEX_TANH: return EW_TANH;
+    case COEX_LEAKY_RELU: return EW_LRELU;
+    case COEX_RELU_GRAD: return EW_RELU_GRAD;
+    case COEX_LEAKY_RELU_GRAD: return EW_LRELU_GRAD;
+    default: return EW_BCE;
+  }
+}
 
 // ---- TMA tensor maps (driver entry point; no -lcuda link dependency) ----
 PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
@@ -353,18 +451,35 @@ int make_tmap(CUtensorMap* m, void* base, int64_t rows, int64_t K, int box_rows)
   return COEX_OK;
 }
 
+// SIMT MatMul kernel choice (parity / fp32 paths): 64x64 tiles when they fill the SMs.
+template <typename T>
+void simt_matmul_launch(coex_ctx* c, const MatmulParams& p, Launch* L) {
+  const int64_t tiles_big = ((p.M + 63) / 64) * ((p.N + 63) / 64);
+  const bool exact = is_f64(c);
+  if (tiles_big >= kNumSMs) {
+    dim3 g((unsigned)(tiles_big < kNumSMs * 4 ? tiles_big : kNumSMs * 4));
+    if (exact) L->set((void*)k_matmul_pipe<T, 64, 64, 16, 4, 4, true, sizeof(T) == 8 ? 2 : 3>, g, dim3(256), p);
+    else L->set((void*)k_matmul_pipe<T, 64, 64, 16, 4, 4, false, sizeof(T) == 8 ? 2 : 3>, g, dim3(256), p);
+  } else {
+    int64_t tiles = ((p.M + 15) / 16) * ((p.N + 15) / 16);
+    dim3 g((unsigned)(tiles < kNumSMs * 8 ? (tiles < 1 ? 1 : tiles) : kNumSMs * 8));
+    if (exact) L->set((void*)k_matmul_pipe<T, 16, 16, 32, 1, 1, true, 4>, g, dim3(256), p);
+    else L->set((void*)k_matmul_pipe<T, 16, 16, 32, 1, 1, false, 4>, g, dim3(256), p);
+  }
+}
+
 template <typename T>
 int build_launch_t(coex_ctx* c, const OpSpec& s, Launch* L) {
   const int64_t n = numel_of(s.out_ndim, s.out_shape);
   switch (s.kind) {
-    case COEX_ADD: case COEX_SUB: case COEX_MUL: case COEX_NEG: case COEX_RELU: case COEX_SIGMOID: {
+    case COEX_ADD: case COEX_SUB: case COEX_MUL: case COEX_NEG: case COEX_RELU: case COEX_SIGMOID:
+    case COEX_TANH: case COEX_LEAKY_RELU: case COEX_RELU_GRAD: case COEX_LEAKY_RELU_GRAD: case COEX_BCE_TERM: {
       EwParams p{};
       p.ds = s.ds;
       p.a = s.in[0];
       p.b = s.in[1];
-      p.op = s.kind == COEX_ADD ? EW_ADD : s.kind == COEX_SUB ? EW_SUB : s.kind == COEX_MUL ? EW_MUL
-           : s.kind == COEX_NEG ? EW_NEG : s.kind == COEX_RELU ? EW_RELU : EW_SIGMOID;
-      int binary = s.kind <= COEX_MUL;
+      p.op = ew_code(s.kind);
+      int binary = ew_binary(p.op);
       p.a_scalar = binary && s.in_ndim[0] == 0 && n != 1;
       p.b_scalar = binary && s.in_ndim[1] == 0 && n != 1;
       p.n = n;
@@ -424,18 +539,7 @@ int build_launch_t(coex_ctx* c, const OpSpec& s, Launch* L) {
       p.lda = s.in_shape[0][1];
       p.ldb = s.in_shape[1][1];
       p.out = s.out;
-      const int64_t tiles_big = ((p.M + 63) / 64) * ((p.N + 63) / 64);
-      const bool exact = is_f64(c);
-      if (tiles_big >= kNumSMs) {
-        dim3 g((unsigned)(tiles_big < kNumSMs * 4 ? tiles_big : kNumSMs * 4));
-        if (exact) L->set((void*)k_matmul_pipe<T, 64, 64, 16, 4, 4, true, sizeof(T) == 8 ? 2 : 3>, g, dim3(256), p);
-        else L->set((void*)k_matmul_pipe<T, 64, 64, 16, 4, 4, false, sizeof(T) == 8 ? 2 : 3>, g, dim3(256), p);
-      } else {
-        int64_t tiles = ((p.M + 15) / 16) * ((p.N + 15) / 16);
-        dim3 g((unsigned)(tiles < kNumSMs * 8 ? (tiles < 1 ? 1 : tiles) : kNumSMs * 8));
-        if (exact) L->set((void*)k_matmul_pipe<T, 16, 16, 32, 1, 1, true, 4>, g, dim3(256), p);
-        else L->set((void*)k_matmul_pipe<T, 16, 16, 32, 1, 1, false, 4>, g, dim3(256), p);
-      }
+      simt_matmul_launch<T>(c, p, L);
       return COEX_OK;
     }
     case COEX_FILL: {
@@ -456,6 +560,260 @@ int build_launch(coex_ctx* c, const OpSpec& s, Launch* L) {
   return is_f64(c) ? build_launch_t<double>(c, s, L) : build_launch_t<float>(c, s, L);
 }
 
+// ---- tcgen05 GEMM launch: C[M,N] = A[M,K] . B^T where A / B are bf16 K-major [rows][pitch(K)] ----
+// BN = 64 / 128 / 256 by N; split-K (deterministic slice reduction) when the tile grid cannot
+// fill the SMs.  Output: the node's Out (publishes) or `raw` scratch.
+struct TcPlan {
+  int bn = 256, splits = 1;
+  int64_t tiles = 1;
+};
+TcPlan tc_plan(int64_t M, int64_t N, int64_t K, bool allow_split) {
+  TcPlan t;
+  t.bn = N <= 64 ? 64 : N <= 128 ? 128 : 256;
+  t.tiles = ((M + TC_BM - 1) / TC_BM) * ((N + t.bn - 1) / t.bn);
+  if (t.tiles < 1) t.tiles = 1;
+  const int64_t nk = (K + TC_BK - 1) / TC_BK;
+  if (allow_split && t.tiles < kNumSMs && nk >= 8) {
+    int64_t s = (kNumSMs + t.tiles - 1) / t.tiles;
+    if (s > nk / 4) s = nk / 4;
+    if (s > 32) s = 32;
+    t.splits = (int)(s < 1 ? 1 : s);
+  }
+  return t;
+}
+
+template <int BN>
+int tc_attr() {
+  static bool done = false;
+  if (!done) {
+    CK(cudaFuncSetAttribute((const void*)k_gemm_tc<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, TcCfg<BN>::SMEM));
+    done = true;
+  }
+  return COEX_OK;
+}
+
+// Appends the GEMM (and its split-K reduction) to L.  `ws` = fp32 split slices (splits > 1).
+int tc_gemm_launches(coex_ctx* c, DevState* ds, void* a16, void* b16, int64_t M, int64_t N, int64_t K,
+                     const TcPlan& t, In na, In nb, const Out& out, float* raw, float* ws, Launch* L, int* nL) {
+  TcGemmParams gp;
+  memset(&gp, 0, sizeof(gp));
+  int rc = make_tmap(&gp.tmA, a16, M, K, TC_BM);
+  if (rc) return rc;
+  rc = make_tmap(&gp.tmB, b16, N, K, t.bn);
+  if (rc) return rc;
+  gp.ds = ds;
+  gp.a = na;
+  gp.b = nb;
+  gp.M = M;
+  gp.N = N;
+  gp.K = K;
+  gp.out = out;
+  gp.splits = t.splits;
+  gp.raw = t.splits > 1 ? ws : raw;
+  Launch& G = L[(*nL)++];
+  void* fn = t.bn == 64 ? (void*)k_gemm_tc<64> : t.bn == 128 ? (void*)k_gemm_tc<128> : (void*)k_gemm_tc<256>;
+  G.set(fn, dim3((unsigned)(t.tiles * t.splits)), dim3(TC_THREADS), gp);
+  G.smem = t.bn == 64 ? TcCfg<64>::SMEM : t.bn == 128 ? TcCfg<128>::SMEM : TcCfg<256>::SMEM;
+  rc = t.bn == 64 ? tc_attr<64>() : t.bn == 128 ? tc_attr<128>() : tc_attr<256>();
+  if (rc) return rc;
+  if (t.splits > 1) {
+    SplitReduceParams r{};
+    r.ds = ds;
+    r.ws = ws;
+    r.n = M * N;
+    r.splits = t.splits;
+    r.a = na;
+    r.b = nb;
+    if (raw != nullptr) {            // reduce into scratch: a private, never-published Out
+      r.out = Out{};
+      r.out.buf[0] = raw;
+    } else {
+      r.out = out;
+    }
+    L[(*nL)++].set((void*)k_splitk_reduce, grid_for(M * N / 4 + 1), dim3(256), r);
+  }
+  return COEX_OK;
+}
+
+struct Carve {
+  char* base;
+  size_t off = 0;
+  explicit Carve(char* b) : base(b) {}
+  void* take(size_t bytes) {
+    off = (off + 255) & ~(size_t)255;
+    void* r = base ? base + off : nullptr;
+    off += bytes < 16 ? 16 : bytes;
+    return r;
+  }
+};
+
+Out private_out(void* buf) {
+  Out o{};
+  o.buf[0] = buf;
+  return o;
+}
+
+// Extension ops (conv family, batch-norm family): up to 5 launches per op, workspace carved
+// from s.ws.  With s.ws == nullptr only the workspace size is computed (*ws_bytes).
+template <typename T>
+int build_xop_t(coex_ctx* c, const OpSpec& s, Launch* L, int* nL, size_t* ws_bytes) {
+  Carve cv(s.ws);
+  const bool build = s.ws != nullptr;
+  const bool bf16 = c->prec == COEX_BF16;
+  const size_t es = sizeof(T);
+  *nL = 0;
+  const int64_t k = s.attr_dims[0], st = s.attr_dims[1], pd = s.attr_dims[2];
+  switch (s.kind) {
+    case COEX_CONV2D: {
+      const int64_t N = s.in_shape[0][0], H = s.in_shape[0][1], W = s.in_shape[0][2], C = s.in_shape[0][3];
+      const int64_t Ho = s.out_shape[1], Wo = s.out_shape[2], F = s.out_shape[3];
+      const int64_t M = N * Ho * Wo, Kc = k * k * C;
+      Im2colParams ip{};
+      ip.ds = s.ds; ip.x = s.in[0];
+      ip.N = N; ip.H = H; ip.W = W; ip.C = C; ip.Ho = Ho; ip.Wo = Wo;
+      ip.k = (int)k; ip.s = (int)st; ip.p = (int)pd;
+      if (bf16) {
+        const TcPlan t = tc_plan(M, F, Kc, true);
+        void* A = cv.take((size_t)M * bf16_pitch(Kc) * 2);
+        void* B = cv.take((size_t)F * bf16_pitch(Kc) * 2);
+        float* ws = t.splits > 1 ? (float*)cv.take((size_t)t.splits * M * F * 4) : nullptr;
+        if (!build) break;
+        ip.dst = A; ip.ld = bf16_pitch(Kc); ip.trans = 0;
+        L[(*nL)++].set((void*)k_im2col<float, __nv_bfloat16>, grid_for(M * ip.ld / 8), dim3(256), ip);
+        CvtParams q{};
+        q.ds = s.ds; q.src[0] = s.in[1]; q.rows[0] = F; q.K = Kc; q.ld = bf16_pitch(Kc); q.trans[0] = 1;
+        q.dst[0] = (__nv_bfloat16*)B;
+        const int64_t tiles = ((F + 31) / 32) * ((q.ld + 31) / 32);
+        L[(*nL)++].set((void*)k_cvt_bf16, dim3((unsigned)(tiles < kNumSMs * 16 ? tiles : kNumSMs * 16), 1), dim3(256), q);
+        return tc_gemm_launches(c, s.ds, A, B, M, F, Kc, t, s.in[0], s.in[1], s.out, nullptr, ws, L, nL);
+      }
+      void* A = cv.take((size_t)M * Kc * es);
+      if (!build) break;
+      ip.dst = A; ip.ld = Kc; ip.trans = 0;
+      L[(*nL)++].set((void*)k_im2col<T, T>, grid_for(M * Kc), dim3(256), ip);
+      MatmulParams mp{};
+      mp.ds = s.ds; mp.a = In{A, nullptr, nullptr}; mp.b = s.in[1];
+      mp.M = M; mp.K = Kc; mp.N = F; mp.lda = Kc; mp.ldb = F; mp.out = s.out;
+      simt_matmul_launch<T>(c, mp, &L[(*nL)++]);
+      return COEX_OK;
+    }
+    case COEX_CONV2D_T: {
+      const int64_t N = s.in_shape[0][0], H = s.in_shape[0][1], W = s.in_shape[0][2], C = s.in_shape[0][3];
+      const int64_t Ho = s.out_shape[1], Wo = s.out_shape[2], F = s.out_shape[3];
+      const int64_t M = N * H * W, Nc = k * k * F;
+      Col2imParams cp{};
+      cp.ds = s.ds; cp.N = N; cp.H = H; cp.W = W; cp.F = F; cp.Ho = Ho; cp.Wo = Wo;
+      cp.k = (int)k; cp.s = (int)st; cp.p = (int)pd; cp.a = s.in[0]; cp.b = s.in[1]; cp.out = s.out;
+      if (bf16) {
+        const TcPlan t = tc_plan(M, Nc, C, true);
+        void* A = cv.take((size_t)M * bf16_pitch(C) * 2);
+        void* B = cv.take((size_t)Nc * bf16_pitch(C) * 2);
+        float* cols = (float*)cv.take((size_t)M * Nc * 4);
+        float* ws = t.splits > 1 ? (float*)cv.take((size_t)t.splits * M * Nc * 4) : nullptr;
+        if (!build) break;
+        CvtParams q{};
+        q.ds = s.ds; q.src[0] = s.in[0]; q.src[1] = s.in[1]; q.rows[0] = M; q.rows[1] = Nc; q.K = C;
+        q.ld = bf16_pitch(C); q.trans[0] = 0; q.trans[1] = 0;
+        q.dst[0] = (__nv_bfloat16*)A; q.dst[1] = (__nv_bfloat16*)B;
+        const int64_t rows_max = M > Nc ? M : Nc;
+        L[(*nL)++].set((void*)k_cvt_bf16, dim3((unsigned)(rows_max < kNumSMs * 16 ? rows_max : kNumSMs * 16), 2),
+                       dim3(256), q);
+        int rc = tc_gemm_launches(c, s.ds, A, B, M, Nc, C, t, s.in[0], s.in[1], s.out, cols, ws, L, nL);
+        if (rc) return rc;
+        cp.cols = cols;
+        L[(*nL)++].set((void*)k_col2im<float, float>, grid_for(N * Ho * Wo * F), dim3(256), cp);
+        return COEX_OK;
+      }
+      void* cols = cv.take((size_t)M * Nc * es);
+      if (!build) break;
+      MatmulParams mp{};
+      mp.ds = s.ds; mp.a = s.in[0]; mp.b = s.in[1]; mp.trans_b = 1;
+      mp.M = M; mp.K = C; mp.N = Nc; mp.lda = C; mp.ldb = C; mp.out = private_out(cols);
+      simt_matmul_launch<T>(c, mp, &L[(*nL)++]);
+      cp.cols = cols;
+      L[(*nL)++].set((void*)k_col2im<T, T>, grid_for(N * Ho * Wo * F), dim3(256), cp);
+      return COEX_OK;
+    }
+    case COEX_CONV2D_DW: {
+      const int64_t N = s.in_shape[0][0], H = s.in_shape[0][1], W = s.in_shape[0][2], C = s.in_shape[0][3];
+      const int64_t Ho = s.in_shape[1][1], Wo = s.in_shape[1][2], F = s.in_shape[1][3];
+      const int64_t P = N * Ho * Wo, Kc = k * k * C;
+      Im2colParams ip{};
+      ip.ds = s.ds; ip.x = s.in[0];
+      ip.N = N; ip.H = H; ip.W = W; ip.C = C; ip.Ho = Ho; ip.Wo = Wo;
+      ip.k = (int)k; ip.s = (int)st; ip.p = (int)pd;
+      if (bf16) {
+        const TcPlan t = tc_plan(Kc, F, P, true);
+        void* A = cv.take((size_t)Kc * bf16_pitch(P) * 2);
+        void* B = cv.take((size_t)F * bf16_pitch(P) * 2);
+        float* ws = t.splits > 1 ? (float*)cv.take((size_t)t.splits * Kc * F * 4) : nullptr;
+        if (!build) break;
+        ip.dst = A; ip.ld = bf16_pitch(P); ip.trans = 1;
+        const int64_t tiles = ((ip.ld + 31) / 32) * ((Kc + 31) / 32);
+        L[(*nL)++].set((void*)k_im2col<float, __nv_bfloat16>,
+                       dim3((unsigned)(tiles < kNumSMs * 16 ? tiles : kNumSMs * 16)), dim3(256), ip);
+        CvtParams q{};
+        q.ds = s.ds; q.src[0] = s.in[1]; q.rows[0] = F; q.K = P; q.ld = bf16_pitch(P); q.trans[0] = 1;
+        q.dst[0] = (__nv_bfloat16*)B;
+        const int64_t ct = ((F + 31) / 32) * ((q.ld + 31) / 32);
+        L[(*nL)++].set((void*)k_cvt_bf16, dim3((unsigned)(ct < kNumSMs * 16 ? ct : kNumSMs * 16), 1), dim3(256), q);
+        return tc_gemm_launches(c, s.ds, A, B, Kc, F, P, t, s.in[0], s.in[1], s.out, nullptr, ws, L, nL);
+      }
+      void* A = cv.take((size_t)P * Kc * es);
+      if (!build) break;
+      ip.dst = A; ip.ld = Kc; ip.trans = 0;
+      L[(*nL)++].set((void*)k_im2col<T, T>, grid_for(P * Kc), dim3(256), ip);
+      MatmulParams mp{};
+      mp.ds = s.ds; mp.a = In{A, nullptr, nullptr}; mp.b = s.in[1]; mp.trans_a = 1;
+      mp.M = Kc; mp.K = P; mp.N = F; mp.lda = Kc; mp.ldb = F; mp.out = s.out;
+      simt_matmul_launch<T>(c, mp, &L[(*nL)++]);
+      return COEX_OK;
+    }
+    case COEX_BATCHNORM: case COEX_BATCHNORM_DX: case COEX_BN_DGAMMA: case COEX_SUM_ROWS: {
+      const int64_t C = s.in_shape[0][s.in_ndim[0] - 1];
+      const int64_t n = numel_of(s.in_ndim[0], s.in_shape[0]);
+      const int64_t R = n / C;
+      int64_t G = n / 16384;
+      if (G > kNumSMs * 2) G = kNumSMs * 2;
+      if (G > R) G = R;
+      if (G < 1) G = 1;
+      ColStatsParams cp{};
+      cp.ds = s.ds; cp.x = s.in[0]; cp.R = R; cp.C = C;
+      cp.part = (double*)cv.take((size_t)G * C * 4 * 8);
+      cp.stats = (double*)cv.take((size_t)C * 4 * 8);
+      cp.counter = (unsigned int*)cv.take(16);
+      cp.a = s.in[0];
+      cp.b = s.nin > 1 ? s.in[1] : In{nullptr, nullptr, nullptr};
+      if (!build) break;
+      if (s.kind == COEX_SUM_ROWS || s.kind == COEX_BN_DGAMMA) {
+        cp.mode = s.kind == COEX_SUM_ROWS ? COL_SUM_ROWS : COL_BN_DGAMMA;
+        if (s.kind == COEX_BN_DGAMMA) cp.dy = s.in[1];
+        cp.out = s.out;
+        L[(*nL)++].set((void*)k_colstats<T>, dim3((unsigned)G), dim3(256), cp);
+        return COEX_OK;
+      }
+      cp.mode = s.kind == COEX_BATCHNORM ? COL_BN : COL_BN_DX;
+      if (s.kind == COEX_BATCHNORM_DX) cp.dy = s.in[2];
+      cp.out = Out{};
+      L[(*nL)++].set((void*)k_colstats<T>, dim3((unsigned)G), dim3(256), cp);
+      BnApplyParams ap{};
+      ap.ds = s.ds; ap.x = s.in[0]; ap.g = s.in[1]; ap.third = s.in[2]; ap.stats = cp.stats;
+      ap.n = n; ap.C = C; ap.dx = s.kind == COEX_BATCHNORM_DX; ap.out = s.out;
+      L[(*nL)++].set((void*)k_bn_apply<T>, grid_for(n), dim3(256), ap);
+      return COEX_OK;
+    }
+    default:
+      return fail(COEX_BAD_ATTRS, "op kind has no extension kernel");
+  }
+  *ws_bytes = cv.off;
+  return COEX_OK;
+}
+
+int build_xop(coex_ctx* c, const OpSpec& s, Launch* L, int* nL, size_t* ws_bytes) {
+  return is_f64(c) ? build_xop_t<double>(c, s, L, nL, ws_bytes) : build_xop_t<float>(c, s, L, nL, ws_bytes);
+}
+constexpr int kMaxLaunches = 6;
+
 bool needs_scratch(const coex_ctx* c, int kind) { return c->prec == COEX_BF16 && kind == COEX_MATMUL; }
 
 void scratch_bytes(const OpSpec& s, size_t* a, size_t* b) {
@@ -466,8 +824,13 @@ void scratch_bytes(const OpSpec& s, size_t* a, size_t* b) {
   *b = (size_t)(N > 0 ? N : 1) * bf16_pitch(K > 0 ? K : 1) * 2;
 }
 
-// One op -> one or two launches (bf16 MatMul = operand conversion + tcgen05 GEMM).
+// One op -> its launches (bf16 MatMul = operand conversion + tcgen05 GEMM; extension ops
+// up to kMaxLaunches, see build_xop).
 int build_launches(coex_ctx* c, const OpSpec& s, Launch* L, int* nL) {
+  if (is_ext_compute(s.kind)) {
+    size_t wb = 0;
+    return build_xop(c, s, L, nL, &wb);
+  }
   if (!needs_scratch(c, s.kind)) {
     *nL = 1;
     return build_launch(c, s, L);
@@ -494,29 +857,9 @@ int build_launches(coex_ctx* c, const OpSpec& s, Launch* L, int* nL) {
   if (gx > (int64_t)kNumSMs * 16) gx = (int64_t)kNumSMs * 16;
   dim3 g((unsigned)(gx > 0 ? gx : 1), 2);
   L[0].set((void*)k_cvt_bf16, g, dim3(256), cv);
-  TcGemmParams gp;
-  memset(&gp, 0, sizeof(gp));
-  int rc = make_tmap(&gp.tmA, s.scratch[0], M, K, TC_BM);
-  if (rc) return rc;
-  rc = make_tmap(&gp.tmB, s.scratch[1], N, K, TC_BN);
-  if (rc) return rc;
-  gp.ds = s.ds;
-  gp.a = s.in[0];
-  gp.b = s.in[1];
-  gp.M = M;
-  gp.N = N;
-  gp.K = K;
-  gp.out = s.out;
-  const int64_t tiles = ((M + TC_BM - 1) / TC_BM) * ((N + TC_BN - 1) / TC_BN);
-  L[1].set((void*)k_gemm_tc, dim3((unsigned)(tiles > 0 ? tiles : 1)), dim3(TC_THREADS), gp);
-  L[1].smem = TC_SMEM;
-  static bool attr = false;
-  if (!attr) {
-    CK(cudaFuncSetAttribute((const void*)k_gemm_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM));
-    attr = true;
-  }
-  *nL = 2;
-  return COEX_OK;
+  *nL = 1;
+  return tc_gemm_launches(c, s.ds, s.scratch[0], s.scratch[1], M, N, K, tc_plan(M, N, K, false), s.in[0], s.in[1],
+                          s.out, nullptr, nullptr, L, nL);
 }
 
 int launch_now(coex_ctx* c, Launch& L) {
@@ -808,11 +1151,66 @@ int coex_tensor_free(coex_ctx* c, int64_t id) {
   return COEX_OK;
 }
 
+}  // extern "C"
+
+namespace {
+// Eager op: spec from tensor records; scratch (bf16 MatMul operands) and extension-op
+// workspace allocated stream-ordered around the launches.
+int eager_spec(coex_ctx* c, int kind, const coex_attrs* attrs, int nin, const TRec* in, const TRec& o, OpSpec* s) {
+  s->kind = kind;
+  s->nin = nin;
+  for (int i = 0; i < nin; ++i) {
+    s->in[i].direct = in[i].buf ? in[i].buf->ptr : nullptr;
+    s->in_ndim[i] = in[i].ndim;
+    memcpy(s->in_shape[i], in[i].shape, sizeof(int64_t) * in[i].ndim);
+  }
+  s->out_ndim = o.ndim;
+  memcpy(s->out_shape, o.shape, sizeof(int64_t) * o.ndim);
+  if (attrs) {
+    s->attr_n = attrs->n;
+    memcpy(s->attr_dims, attrs->dims, sizeof(int64_t) * COEX_MAX_RANK);
+    s->value = attrs->value;
+  }
+  s->out.buf[0] = o.buf->ptr;
+  return COEX_OK;
+}
+
+int eager_scratch(coex_ctx* c, OpSpec* s) {
+  if (needs_scratch(c, s->kind)) {
+    size_t ba, bb;
+    scratch_bytes(*s, &ba, &bb);
+    CK(cudaMallocAsync(&s->scratch[0], ba, c->stream));
+    CK(cudaMallocAsync(&s->scratch[1], bb, c->stream));
+  }
+  if (is_ext_compute(s->kind)) {
+    Launch tmp[kMaxLaunches];
+    int n = 0;
+    size_t wb = 0;
+    int rc = build_xop(c, *s, tmp, &n, &wb);
+    if (rc) return rc;
+    CK(cudaMallocAsync((void**)&s->ws, wb, c->stream));
+    CK(cudaMemsetAsync(s->ws, 0, wb, c->stream));
+  }
+  return COEX_OK;
+}
+
+void eager_free(coex_ctx* c, OpSpec* s) {
+  if (s->scratch[0]) cudaFreeAsync(s->scratch[0], c->stream);
+  if (s->scratch[1]) cudaFreeAsync(s->scratch[1], c->stream);
+  if (s->ws) cudaFreeAsync(s->ws, c->stream);
+  s->scratch[0] = s->scratch[1] = nullptr;
+  s->ws = nullptr;
+}
+}  // namespace
+
+extern "C" {
+
 int coex_exec_op(coex_ctx* c, int kind, const coex_attrs* attrs, int nin, const int64_t* in_ids,
                  int64_t* out_id) {
   if (c->active) return fail(COEX_IN_FLIGHT_PASS, "eager op while a pass is in flight");
-  TRec in[2];
-  for (int i = 0; i < nin && i < 2; ++i) {
+  if (nin < 0 || nin > kMaxIn) return fail(COEX_BAD_ATTRS, "wrong number of tensor inputs");
+  TRec in[kMaxIn];
+  for (int i = 0; i < nin; ++i) {
     TRec* t = get_t(c, in_ids[i]);
     if (!t) return fail(COEX_INVALID, "unknown input tensor id");
     in[i] = *t;
@@ -830,33 +1228,14 @@ int coex_exec_op(coex_ctx* c, int kind, const coex_attrs* attrs, int nin, const 
   rc = alloc_buf(c, o.numel * c->esize, &o.buf);
   if (rc) return rc;
   OpSpec s;
-  s.kind = kind;
-  for (int i = 0; i < nin; ++i) {
-    s.in[i].direct = in[i].buf->ptr;
-    s.in_ndim[i] = in[i].ndim;
-    memcpy(s.in_shape[i], in[i].shape, sizeof(int64_t) * in[i].ndim);
-  }
-  s.out_ndim = o.ndim;
-  memcpy(s.out_shape, o.shape, sizeof(int64_t) * o.ndim);
-  if (attrs) {
-    s.attr_n = attrs->n;
-    memcpy(s.attr_dims, attrs->dims, sizeof(int64_t) * COEX_MAX_RANK);
-    s.value = attrs->value;
-  }
-  s.out.buf[0] = o.buf->ptr;
+  eager_spec(c, kind, attrs, nin, in, o, &s);
   if (o.numel > 0 || kind == COEX_SUM || kind == COEX_MEAN) {
-    if (needs_scratch(c, kind)) {
-      size_t ba, bb;
-      scratch_bytes(s, &ba, &bb);
-      CK(cudaMallocAsync(&s.scratch[0], ba, c->stream));
-      CK(cudaMallocAsync(&s.scratch[1], bb, c->stream));
-    }
-    Launch L[2];
+    rc = eager_scratch(c, &s);
+    Launch L[kMaxLaunches];
     int nL = 0;
-    rc = build_launches(c, s, L, &nL);
+    if (rc == COEX_OK) rc = build_launches(c, s, L, &nL);
     for (int i = 0; rc == COEX_OK && i < nL; ++i) rc = launch_now(c, L[i]);
-    if (s.scratch[0]) cudaFreeAsync(s.scratch[0], c->stream);
-    if (s.scratch[1]) cudaFreeAsync(s.scratch[1], c->stream);
+    eager_free(c, &s);
     if (rc) {
       release(c, o.buf);
       return rc;
@@ -872,31 +1251,14 @@ int coex_exec_op_timed(coex_ctx* c, int kind, const coex_attrs* attrs, int nin, 
   int64_t out;
   int rc = coex_exec_op(c, kind, attrs, nin, in_ids, &out);     // warm-up + output buffer
   if (rc) return rc;
-  TRec in[2];
+  TRec in[kMaxIn];
   for (int i = 0; i < nin; ++i) in[i] = *get_t(c, in_ids[i]);
   TRec* o = get_t(c, out);
   OpSpec s;
-  s.kind = kind;
-  for (int i = 0; i < nin; ++i) {
-    s.in[i].direct = in[i].buf->ptr;
-    s.in_ndim[i] = in[i].ndim;
-    memcpy(s.in_shape[i], in[i].shape, sizeof(int64_t) * in[i].ndim);
-  }
-  s.out_ndim = o->ndim;
-  memcpy(s.out_shape, o->shape, sizeof(int64_t) * o->ndim);
-  if (attrs) {
-    s.attr_n = attrs->n;
-    memcpy(s.attr_dims, attrs->dims, sizeof(int64_t) * COEX_MAX_RANK);
-    s.value = attrs->value;
-  }
-  s.out.buf[0] = o->buf->ptr;
-  if (needs_scratch(c, kind)) {
-    size_t ba, bb;
-    scratch_bytes(s, &ba, &bb);
-    CK(cudaMallocAsync(&s.scratch[0], ba, c->stream));
-    CK(cudaMallocAsync(&s.scratch[1], bb, c->stream));
-  }
-  Launch L[2];
+  eager_spec(c, kind, attrs, nin, in, *o, &s);
+  rc = eager_scratch(c, &s);
+  if (rc) return rc;
+  Launch L[kMaxLaunches];
   int nL = 0;
   rc = build_launches(c, s, L, &nL);
   if (rc) return rc;
@@ -913,8 +1275,7 @@ int coex_exec_op_timed(coex_ctx* c, int kind, const coex_attrs* attrs, int nin, 
   double ms = 0;
   rc = coex_ctx_event_elapsed(c, 62, 63, &ms);
   *avg_ms = ms / reps;
-  if (s.scratch[0]) cudaFreeAsync(s.scratch[0], c->stream);
-  if (s.scratch[1]) cudaFreeAsync(s.scratch[1], c->stream);
+  eager_free(c, &s);
   coex_tensor_free(c, out);
   return rc;
 }
@@ -980,7 +1341,7 @@ int coex_var_rollback(coex_ctx* c) {
 namespace {
 
 enum PlanTag : int64_t { T_SEQ = 1, T_OP = 2, T_PTR = 3, T_FEED = 4, T_FETCH = 5, T_SWITCH = 6, T_WHILE = 7, T_CHAIN = 8,
-                         T_ALLREDUCE = 9 };
+                         T_ALLREDUCE = 9, T_XOP = 10 };
 constexpr int64_t kPlanMagic = 0xC0E8B200;
 constexpr int64_t kPlanVersion = 2;
 
@@ -1016,6 +1377,8 @@ struct coex_prog {
   std::unordered_map<int64_t, int64_t> fetch_count;             // node -> entries seen
   std::unordered_map<int64_t, std::vector<int64_t>> fetch_idx;  // node -> ring indices
   std::vector<std::vector<double>> fetch_copy;                  // payload snapshots
+  std::vector<void*> workspaces;                                // extension-op workspaces
+  size_t ws_bytes = 0;
 };
 
 namespace {
@@ -1136,9 +1499,52 @@ struct Builder {
         s.scratch[0] = buf(next());
         s.scratch[1] = buf(next());
         read_out(s.out);
-        Launch L[2];
+        s.nin = 2;
+        Launch L[kMaxLaunches];
         int nL = 0;
         int rc = build_launches(c, s, L, &nL);
+        if (rc) return rc;
+        p->n_compute += nL;
+        for (int i = 0; i < nL; ++i) {
+          rc = add_kernel(g, prev, L[i]);
+          if (rc) return rc;
+        }
+        return COEX_OK;
+      }
+      case T_XOP: {
+        OpSpec s;
+        s.ds = c->d_state;
+        s.kind = (int)next();
+        next();  // node id (diagnostics)
+        s.nin = (int)next();
+        if (s.nin < 1 || s.nin > kMaxIn || !is_ext_compute(s.kind)) throw std::runtime_error("bad extension op");
+        for (int i = 0; i < kMaxIn; ++i) {
+          int64_t ci = next();
+          s.in[i] = i < s.nin ? operand(ci) : In{nullptr, nullptr, nullptr};
+        }
+        for (int i = 0; i < kMaxIn; ++i) {
+          s.in_ndim[i] = (int)next();
+          for (int d = 0; d < COEX_MAX_RANK; ++d) s.in_shape[i][d] = next();
+        }
+        s.out_ndim = (int)next();
+        for (int d = 0; d < COEX_MAX_RANK; ++d) s.out_shape[d] = next();
+        s.attr_n = (int)next();
+        for (int d = 0; d < COEX_MAX_RANK; ++d) s.attr_dims[d] = next();
+        int64_t vbits = next();
+        memcpy(&s.value, &vbits, 8);
+        read_out(s.out);
+        Launch L[kMaxLaunches];
+        int nL = 0;
+        size_t wb = 0;
+        int rc = build_xop(c, s, L, &nL, &wb);
+        if (rc) return rc;
+        void* ws = nullptr;
+        CK(cudaMalloc(&ws, wb));
+        CK(cudaMemset(ws, 0, wb));
+        p->workspaces.push_back(ws);
+        p->ws_bytes += wb;
+        s.ws = (char*)ws;
+        rc = build_xop(c, s, L, &nL, &wb);
         if (rc) return rc;
         p->n_compute += nL;
         for (int i = 0; i < nL; ++i) {
@@ -1500,6 +1906,7 @@ int coex_prog_destroy(coex_prog* p) {
   if (p->cells) cudaFree(p->cells);
   if (p->recs) cudaFree(p->recs);
   if (p->late) cudaFree(p->late);
+  for (void* w : p->workspaces) cudaFree(w);
   delete p;
   return COEX_OK;
 }
@@ -1507,7 +1914,7 @@ int coex_prog_destroy(coex_prog* p) {
 int coex_prog_info(coex_prog* p, int64_t* nk, int64_t* nc, int64_t* ab) {
   *nk = p->n_kernel_nodes;
   *nc = p->n_cond_nodes;
-  *ab = (int64_t)p->arena_bytes;
+  *ab = (int64_t)(p->arena_bytes + p->ws_bytes);
   return COEX_OK;
 }
 

@@ -35,6 +35,7 @@ from .trace_graph import (Diverged, External, Handle, LoopEnter, LoopExit,
                           LoopIterStart, OpEvent, StepEnd)
 
 OP_BY_NAME = {k.value: k for k in OpKind if k not in (OpKind.READ_VAR, OpKind.ASSIGN_VAR)}
+CONV_NAMES = frozenset(("conv2d", "conv2d_t", "conv2d_dw"))
 
 
 class Val:
@@ -81,8 +82,8 @@ class StepDiverged(Exception):
 
 
 _KIND_VAL = {k: k.value for k in OpKind}
-_IN_KINDS = {(): (), (True,): ("h",), (False,): ("e",), (True, True): ("h", "h"), (True, False): ("h", "e"),
-             (False, True): ("e", "h"), (False, False): ("e", "e")}
+_IN_KINDS = {k: tuple("h" if b else "e" for b in k)
+             for n in range(4) for k in __import__("itertools").product((True, False), repeat=n)}
 _SHAPE_CACHE: dict = {}
 _LOC_KEYS: dict = {}
 
@@ -689,7 +690,29 @@ class Interp:
                 perm = perm_f(ctx, env) if perm_f is not None else tuple(range(len(shp) - 1, -1, -1))
                 return ctx.op(kind, {"perm": tuple(perm)}, [x], loc, [shp])
             return transpose
+        if name in CONV_NAMES:
+            # extension convolutions: two tensor operands + the [k, s, p] shape literal
+            fy = self._c_expr(e.args[1], loc)
+            geo = self._c_shape(e.args[2], loc)
+
+            def conv(ctx, env):
+                x = fx(ctx, env)
+                y = fy(ctx, env)
+                if isinstance(x, str) or isinstance(y, str):
+                    raise it._err(f"{name}: string operand", e)
+                return ctx.op(kind, {"conv": tuple(geo(ctx, env))}, [x, y], loc, [shape_of(x), shape_of(y)])
+            return conv
         site = (kind, kind.value, loc, (loc.stmt_id, loc.loop_path))
+        if len(e.args) == 3:
+            fy = self._c_expr(e.args[1], loc)
+            fz = self._c_expr(e.args[2], loc)
+
+            def ternary(ctx, env):
+                x, y, z = fx(ctx, env), fy(ctx, env), fz(ctx, env)
+                if isinstance(x, str) or isinstance(y, str) or isinstance(z, str):
+                    raise it._err(f"{name}: string operand", e)
+                return ctx.op_site(site, [x, y, z], [shape_of(x), shape_of(y), shape_of(z)])
+            return ternary
         if len(e.args) == 1:
             def unary(ctx, env):
                 x = fx(ctx, env)

@@ -28,17 +28,22 @@ from dataclasses import dataclass, field
 
 from .errors import ShapeMiss
 from .graph_gen import ExecOp, InputFeed, OutputFetch, SwitchCase, SymProgram, UnrolledLoop, While
-from .tensor import OpKind, infer_shape, shape_size
+from .tensor import CONV_KINDS, OpKind, flops_of, infer_shape, shape_size
 
 MAGIC = 0xC0E8B200
 VERSION = 2
-T_SEQ, T_OP, T_PTR, T_FEED, T_FETCH, T_SWITCH, T_WHILE, T_CHAIN, T_ALLREDUCE = 1, 2, 3, 4, 5, 6, 7, 8, 9
+T_SEQ, T_OP, T_PTR, T_FEED, T_FETCH, T_SWITCH, T_WHILE, T_CHAIN, T_ALLREDUCE, T_XOP = 1, 2, 3, 4, 5, 6, 7, 8, 9, 10
 PTR_ALIAS, PTR_READ_VAR, PTR_ASSIGN_VAR = 0, 1, 2
 MAX_RANK = 8
 MAX_PUB = 6
-COMPUTE = {OpKind.MATMUL, OpKind.ADD, OpKind.SUB, OpKind.MUL, OpKind.NEG, OpKind.RELU,
-           OpKind.SIGMOID, OpKind.SUM, OpKind.MEAN, OpKind.TRANSPOSE}
-EW_CODE = {OpKind.ADD: 0, OpKind.SUB: 1, OpKind.MUL: 2, OpKind.NEG: 3, OpKind.RELU: 4, OpKind.SIGMOID: 5}
+# extension compute ops (conv / batch-norm families) lowered by csrc/ext_ops.cuh: T_XOP items
+XOP = {OpKind.CONV2D, OpKind.CONV2D_T, OpKind.CONV2D_DW, OpKind.BATCHNORM, OpKind.BATCHNORM_DX,
+       OpKind.BN_DGAMMA, OpKind.SUM_ROWS}
+EW_CODE = {OpKind.ADD: 0, OpKind.SUB: 1, OpKind.MUL: 2, OpKind.NEG: 3, OpKind.RELU: 4, OpKind.SIGMOID: 5,
+           OpKind.TANH: 7, OpKind.LEAKY_RELU: 8, OpKind.RELU_GRAD: 9, OpKind.LEAKY_RELU_GRAD: 10,
+           OpKind.BCE_TERM: 11}
+COMPUTE = {OpKind.MATMUL, OpKind.SUM, OpKind.MEAN, OpKind.TRANSPOSE} | set(EW_CODE) | XOP
+MAX_XIN = 3
 CHAIN_IN, CHAIN_OPS, CHAIN_OUT, CHAIN_PUB, CHAIN_REGS = 8, 16, 8, 4, 16
 
 
@@ -381,6 +386,8 @@ class Planner:
                              self._shape_id(s))]
         if nid in folded:
             return []
+        if k in XOP:
+            return [self._xop_word(x, shapes, in_cell, out_words, pubs, n_compute, flops)]
         ins = list(x.inputs)
         trans = [0, 0]
         cells = []
@@ -417,6 +424,24 @@ class Planner:
             word += [-1, -1]
         word += out_words(nid, late)
         return [word]
+
+    def _xop_word(self, x, shapes, in_cell, out_words, pubs, n_compute, flops) -> list:
+        nid = x.node_id
+        cells = [in_cell(b) for b in x.inputs]
+        in_shapes = [self._in_shape(b, shapes) for b in x.inputs]
+        late = _conflicts(cells, pubs[nid])
+        n_compute[0] += 1
+        attr = list(x.attrs["conv"]) if x.kind in CONV_KINDS else []
+        if x.kind in CONV_KINDS:
+            flops[0] += flops_of(x.kind, in_shapes, x.attrs)
+        out_shape = shapes[nid]
+        word = [T_XOP, x.kind.code, nid, len(cells)] + cells + [-1] * (MAX_XIN - len(cells))
+        for s_ in in_shapes + [()] * (MAX_XIN - len(in_shapes)):
+            word += [len(s_)] + _pad(s_)
+        word += [len(out_shape)] + _pad(out_shape)
+        word += [len(attr)] + _pad(attr) + [_f64_bits(0.0)]
+        word += out_words(nid, late)
+        return word
 
     # ------------------------------------------------------------ pointer-op rewrites
     def _pointer_rewrites(self, consumers, multi, folded):

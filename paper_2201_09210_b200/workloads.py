@@ -45,6 +45,140 @@ steps {steps} {{
 C1 = dict(batch=64, hidden=128, din=784, dout=10)
 
 
+def dcgan_program(steps: int = 20, batch: int = 128, nz: int = 100, ngf: int = 64, ndf: int = 64,
+                  img: int = 64, lr: float = 0.01) -> str:
+    """BASELINE.json configs[1]: DCGAN on synthetic NHWC images.
+
+    Generator: z -> dense to [4,4,C0] -> (batchnorm, relu, conv2d_t k4 s2 p1) x L -> tanh.
+    Discriminator: (conv2d k4 s2 p1, [batchnorm], leaky_relu) down to 4x4 -> dense logit,
+    binary cross-entropy on logits.  ``native mod(step, 2)`` alternates a discriminator
+    step (real -> 1, fake -> 0, D weights updated) and a generator step (fake -> 1 through
+    D, G weights updated): a SwitchCase whose two bodies hold the two backward passes.
+    Backward passes are written out (the language has no autodiff); SGD.
+    Extension ops; parity is against the builder's f64 restatement.
+    """
+    L = 0
+    while 4 << L < img:
+        L += 1
+    if 4 << L != img or L < 1:
+        raise ValueError("img must be 4 * 2^L, L >= 1")
+    gch = [ngf << (L - 1 - i) for i in range(L)] + [3]          # G channels per resolution 4 .. img
+    dch = [3] + [ndf << i for i in range(L)]                     # D channels per resolution img .. 4
+    N = batch
+    v = []
+    v.append(f"var gw0 = mul(input(\"gw0_init\", [{nz}, {16 * gch[0]}]), 0.02)")
+    for i in range(L):
+        v.append(f"var gg{i} = fill([{gch[i]}], 1.0)")
+        v.append(f"var gb{i} = fill([{gch[i]}], 0.0)")
+        v.append(f"var gw{i + 1} = mul(input(\"gw{i + 1}_init\", [{16 * gch[i + 1]}, {gch[i]}]), 0.02)")
+    for i in range(L):
+        v.append(f"var dw{i + 1} = mul(input(\"dw{i + 1}_init\", [{16 * dch[i]}, {dch[i + 1]}]), 0.02)")
+        if i > 0:
+            v.append(f"var dg{i + 1} = fill([{dch[i + 1]}], 1.0)")
+            v.append(f"var db{i + 1} = fill([{dch[i + 1]}], 0.0)")
+    v.append(f"var dwo = mul(input(\"dwo_init\", [{16 * dch[L]}, 1]), 0.02)")
+    geo = "[4, 2, 1]"
+    b = []
+    b.append(f"let z = input(\"z\", [{N}, {nz}])")
+    b.append(f"let real = input(\"img\", [{N}, {img}, {img}, 3])")
+    b.append(f"let ga0 = reshape(matmul(z, gw0), [{N}, 4, 4, {gch[0]}])")
+    for i in range(L):
+        b.append(f"let gn{i} = batchnorm(ga{i}, gg{i}, gb{i})")
+        b.append(f"let gh{i} = relu(gn{i})")
+        b.append(f"let ga{i + 1} = conv2d_t(gh{i}, gw{i + 1}, {geo})")
+    b.append(f"let fake = tanh(ga{L})")
+
+    def d_forward(x, p):
+        out = [f"let {p}a1 = conv2d({x}, dw1, {geo})", f"let {p}h1 = leaky_relu({p}a1)"]
+        for i in range(2, L + 1):
+            out += [f"let {p}a{i} = conv2d({p}h{i - 1}, dw{i}, {geo})",
+                    f"let {p}n{i} = batchnorm({p}a{i}, dg{i}, db{i})",
+                    f"let {p}h{i} = leaky_relu({p}n{i})"]
+        out += [f"let {p}f = reshape({p}h{L}, [{N}, {16 * dch[L]}])",
+                f"let {p}logit = matmul({p}f, dwo)"]
+        return out
+
+    def d_backward(x, p, target, need_dx):
+        out = [f"let {p}dl = mul(sub(sigmoid({p}logit), {target}), {1.0 / N})",
+               f"let {p}dwo = matmul(transpose({p}f), {p}dl)",
+               f"let {p}dh{L} = reshape(matmul({p}dl, transpose(dwo)), [{N}, 4, 4, {dch[L]}])"]
+        for i in range(L, 1, -1):
+            out += [f"let {p}dn{i} = leaky_relu_grad({p}n{i}, {p}dh{i})",
+                    f"let {p}ddg{i} = bn_dgamma({p}a{i}, {p}dn{i})",
+                    f"let {p}ddb{i} = sum_rows({p}dn{i})",
+                    f"let {p}da{i} = batchnorm_dx({p}a{i}, dg{i}, {p}dn{i})",
+                    f"let {p}dw{i} = conv2d_dw({p}h{i - 1}, {p}da{i}, {geo})",
+                    f"let {p}dh{i - 1} = conv2d_t({p}da{i}, dw{i}, {geo})"]
+        out += [f"let {p}da1 = leaky_relu_grad({p}a1, {p}dh1)",
+                f"let {p}dw1 = conv2d_dw({x}, {p}da1, {geo})"]
+        if need_dx:
+            out += [f"let {p}dx = conv2d_t({p}da1, dw1, {geo})"]
+        return out
+
+    dstep = d_forward("real", "r") + d_forward("fake", "f")
+    dstep += d_backward("real", "r", "1.0", False) + d_backward("fake", "f", "0.0", False)
+    dstep += [f"let loss = add(mean(bce_term(rlogit, 1.0)), mean(bce_term(flogit, 0.0)))"]
+    dstep += [f"dwo = sub(dwo, mul(add(rdwo, fdwo), {lr}))"]
+    for i in range(1, L + 1):
+        dstep += [f"dw{i} = sub(dw{i}, mul(add(rdw{i}, fdw{i}), {lr}))"]
+        if i > 1:
+            dstep += [f"dg{i} = sub(dg{i}, mul(add(rddg{i}, fddg{i}), {lr}))",
+                      f"db{i} = sub(db{i}, mul(add(rddb{i}, fddb{i}), {lr}))"]
+    dstep += ["print(item(loss))"]
+
+    gstep = d_forward("fake", "f") + d_backward("fake", "f", "1.0", True)
+    gstep += [f"let gloss = mean(bce_term(flogit, 1.0))",
+              f"let gd{L} = mul(fdx, sub(1.0, mul(fake, fake)))"]
+    for i in range(L, 0, -1):
+        gstep += [f"let gdw{i} = conv2d_dw(gd{i}, gh{i - 1}, {geo})",
+                  f"let gdh{i - 1} = conv2d(gd{i}, gw{i}, {geo})",
+                  f"let gdn{i - 1} = relu_grad(gn{i - 1}, gdh{i - 1})",
+                  f"let gdg{i - 1} = bn_dgamma(ga{i - 1}, gdn{i - 1})",
+                  f"let gdb{i - 1} = sum_rows(gdn{i - 1})",
+                  f"let gd{i - 1} = batchnorm_dx(ga{i - 1}, gg{i - 1}, gdn{i - 1})"]
+    gstep += [f"let gdw0 = matmul(transpose(z), reshape(gd0, [{N}, {16 * gch[0]}]))",
+              f"gw0 = sub(gw0, mul(gdw0, {lr}))"]
+    for i in range(L):
+        gstep += [f"gw{i + 1} = sub(gw{i + 1}, mul(gdw{i + 1}, {lr}))",
+                  f"gg{i} = sub(gg{i}, mul(gdg{i}, {lr}))",
+                  f"gb{i} = sub(gb{i}, mul(gdb{i}, {lr}))"]
+    gstep += ["print(item(gloss))"]
+
+    ind = "\n    "
+    body = "\n  ".join(b)
+    return ("\n".join(v) + f"\nsteps {steps} {{\n  " + body +
+            f"\n  if native mod(step, 2) == 0 {{\n    " + ind.join(dstep) +
+            f"\n  }} else {{\n    " + ind.join(gstep) + "\n  }\n}\n")
+
+
+C2 = dict(batch=128, nz=100, ngf=64, ndf=64, img=64)
+C2_SMALL = dict(batch=4, nz=8, ngf=4, ndf=4, img=16)
+
+
+def dcgan_flops(batch=128, nz=100, ngf=64, ndf=64, img=64, **_) -> dict:
+    """Implicit-GEMM FLOPs of one D step and one G step (2*M*N*K per MatMul / conv)."""
+    L = 0
+    while 4 << L < img:
+        L += 1
+    gch = [ngf << (L - 1 - i) for i in range(L)] + [3]
+    dch = [3] + [ndf << i for i in range(L)]
+    N = batch
+    g_fwd = 2 * N * nz * 16 * gch[0]
+    for i in range(L):
+        h = 4 << i
+        g_fwd += 2 * N * h * h * gch[i] * 16 * gch[i + 1]          # conv2d_t: [NHW, C] x [C, 16F]
+    d_fwd = 2 * N * 16 * dch[L]
+    for i in range(L):
+        ho = img >> (i + 1)
+        d_fwd += 2 * N * ho * ho * 16 * dch[i] * dch[i + 1]
+    d_bwd_w = d_fwd                                                  # weight grads
+    d_bwd_x = d_fwd - 2 * N * (img >> 1) ** 2 * 16 * dch[0] * dch[1]  # no dx for the first layer
+    g_bwd = 2 * g_fwd                                                # dw + dx of every G layer
+    d_step = g_fwd + 2 * (d_fwd + d_bwd_w + d_bwd_x)
+    g_step = g_fwd + d_fwd + d_bwd_w + d_bwd_x + d_fwd - d_bwd_x + g_bwd
+    return {"d_step": d_step, "g_step": g_step}
+
+
 def c1_flops(batch=64, hidden=128, din=784, dout=10) -> int:
     """MatMul FLOPs of one C1 step (forward, backward, and the dw1 scaling ignored)."""
     fwd = 2 * batch * din * hidden + 2 * batch * hidden * dout

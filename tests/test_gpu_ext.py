@@ -1,0 +1,140 @@
+"""Extension op set (configs C2-C5, SURVEY §2.4 / §8(a) row a*) through the C-ABI
+against the builder's f64 restatement in oracle/kernels.py.
+
+Tolerances (stated per precision; parity for these ops is unpinned by the reference):
+* f64: convolutions and the piecewise-linear ops bit-exact (im2col + the sequential-k
+  parity GEMM + ordered col2im); tanh / bce_term <= 4 ulp-ish (1e-14 relative);
+  batch-norm family 1e-12 relative (parallel column reductions).
+* fp32: 1e-5 relative, norm-wise.
+* bf16: convolutions on tcgen05 with bf16 operands 2e-2 relative, norm-wise; the other
+  ops run in fp32 (1e-5).
+"""
+
+import numpy as np
+import pytest
+
+from oracle.kernels import execute_kernel
+from paper_2201_09210_b200.tensor import OpKind, Tensor
+
+pytestmark = pytest.mark.gpu
+
+RNG = np.random.default_rng(2201)
+
+
+def rt(*shape, scale=1.0):
+    return Tensor(shape, RNG.standard_normal(shape) * scale)
+
+
+CONV = [
+    (OpKind.CONV2D, {"conv": (4, 2, 1)}, [rt(2, 8, 8, 3), rt(48, 5)]),
+    (OpKind.CONV2D, {"conv": (3, 1, 1)}, [rt(3, 5, 5, 7), rt(63, 16)]),
+    (OpKind.CONV2D, {"conv": (3, 2, 0)}, [rt(2, 7, 7, 4), rt(36, 3)]),
+    (OpKind.CONV2D, {"conv": (4, 2, 1)}, [rt(8, 16, 16, 64), rt(1024, 128)]),
+    (OpKind.CONV2D, {"conv": (4, 2, 1)}, [rt(4, 8, 8, 256), rt(4096, 512)]),
+    (OpKind.CONV2D_T, {"conv": (4, 2, 1)}, [rt(2, 4, 4, 8), rt(48, 8)]),
+    (OpKind.CONV2D_T, {"conv": (3, 1, 1)}, [rt(2, 5, 5, 6), rt(36, 6)]),
+    (OpKind.CONV2D_T, {"conv": (4, 2, 1)}, [rt(4, 8, 8, 64), rt(512, 64)]),
+    (OpKind.CONV2D_T, {"conv": (4, 2, 1)}, [rt(8, 16, 16, 128), rt(48, 128)]),
+    (OpKind.CONV2D_DW, {"conv": (4, 2, 1)}, [rt(2, 8, 8, 3), rt(2, 4, 4, 5)]),
+    (OpKind.CONV2D_DW, {"conv": (3, 1, 1)}, [rt(3, 5, 5, 7), rt(3, 5, 5, 16)]),
+    (OpKind.CONV2D_DW, {"conv": (4, 2, 1)}, [rt(8, 16, 16, 64), rt(8, 8, 8, 128)]),
+    (OpKind.CONV2D_DW, {"conv": (4, 2, 1)}, [rt(16, 32, 32, 3), rt(16, 16, 16, 64)]),
+]
+
+BN = [
+    (OpKind.BATCHNORM, {}, [rt(4, 4, 4, 8, scale=3.0), rt(8), rt(8)]),
+    (OpKind.BATCHNORM, {}, [rt(64, 300), rt(300), rt(300)]),
+    (OpKind.BATCHNORM, {}, [rt(1000, 7), rt(7), rt(7)]),
+    (OpKind.BATCHNORM, {}, [Tensor((2, 3, 3, 512), RNG.standard_normal((2, 3, 3, 512)) + 5.0), rt(512), rt(512)]),
+    (OpKind.BATCHNORM_DX, {}, [rt(4, 4, 4, 8), rt(8), rt(4, 4, 4, 8)]),
+    (OpKind.BATCHNORM_DX, {}, [rt(64, 300), rt(300), rt(64, 300)]),
+    (OpKind.BATCHNORM_DX, {}, [rt(128, 16, 16, 64), rt(64), rt(128, 16, 16, 64)]),
+    (OpKind.BN_DGAMMA, {}, [rt(4, 4, 4, 8), rt(4, 4, 4, 8)]),
+    (OpKind.BN_DGAMMA, {}, [rt(1000, 7), rt(1000, 7)]),
+    (OpKind.SUM_ROWS, {}, [rt(4, 4, 4, 8)]),
+    (OpKind.SUM_ROWS, {}, [rt(3000, 513)]),
+    (OpKind.SUM_ROWS, {}, [rt(5)]),
+]
+
+EDGE = np.array([-800.0, -30.0, -1.0, -0.0, 0.0, 1e-30, 0.5, 30.0, 800.0, np.nan])
+EW = [
+    (OpKind.TANH, {}, [Tensor(EDGE.shape, EDGE)]),
+    (OpKind.TANH, {}, [rt(37, 41, scale=3.0)]),
+    (OpKind.LEAKY_RELU, {}, [Tensor(EDGE.shape, EDGE)]),
+    (OpKind.LEAKY_RELU, {}, [rt(1000)]),
+    (OpKind.RELU_GRAD, {}, [Tensor(EDGE.shape, EDGE), rt(10)]),
+    (OpKind.RELU_GRAD, {}, [rt(7, 9), rt()]),
+    (OpKind.LEAKY_RELU_GRAD, {}, [Tensor(EDGE.shape, EDGE), rt(10)]),
+    (OpKind.BCE_TERM, {}, [Tensor(EDGE.shape, EDGE), Tensor((), 1.0)]),
+    (OpKind.BCE_TERM, {}, [rt(64, 1, scale=4.0), Tensor((), 0.0)]),
+]
+
+
+def nrel(got, want):
+    g, w = got.data.ravel(), want.data.ravel()
+    ok = ~np.isnan(w)
+    assert np.array_equal(np.isnan(g), np.isnan(w))
+    den = np.linalg.norm(w[ok])
+    return np.linalg.norm(g[ok] - w[ok]) / (den if den > 0 else 1.0)
+
+
+def run(be, kind, attrs, ins):
+    want = execute_kernel(kind, attrs, ins)[0]
+    got = be.get(be.exec_op(kind, attrs, ins))
+    assert got.shape == want.shape, (got.shape, want.shape)
+    return got, want
+
+
+@pytest.mark.parametrize("i", range(len(CONV)))
+def test_conv_f64_bitwise(b200_factory, i):
+    got, want = run(b200_factory("f64"), *CONV[i])
+    assert got.data.tobytes() == want.data.tobytes(), np.max(np.abs(got.data - want.data))
+
+
+@pytest.mark.parametrize("prec,tol", [("fp32", 1e-5), ("bf16", 2e-2)])
+@pytest.mark.parametrize("i", range(len(CONV)))
+def test_conv_tolerance(b200_factory, prec, tol, i):
+    got, want = run(b200_factory(prec), *CONV[i])
+    assert nrel(got, want) <= tol
+
+
+@pytest.mark.parametrize("prec,tol", [("f64", 1e-12), ("fp32", 1e-5), ("bf16", 1e-5)])
+@pytest.mark.parametrize("i", range(len(BN)))
+def test_batchnorm_family(b200_factory, prec, tol, i):
+    got, want = run(b200_factory(prec), *BN[i])
+    assert nrel(got, want) <= tol
+
+
+@pytest.mark.parametrize("prec,tol", [("f64", 1e-14), ("fp32", 1e-6), ("bf16", 1e-6)])
+@pytest.mark.parametrize("i", range(len(EW)))
+def test_elementwise_ext(b200_factory, prec, tol, i):
+    kind, attrs, ins = EW[i]
+    got, want = run(b200_factory(prec), kind, attrs, ins)
+    if prec == "f64" and kind in (OpKind.LEAKY_RELU, OpKind.RELU_GRAD, OpKind.LEAKY_RELU_GRAD):
+        assert got.data.tobytes() == want.data.tobytes()
+    else:
+        assert nrel(got, want) <= tol
+
+
+def test_bn_gradient_consistency(b200_factory):
+    """batchnorm_dx / bn_dgamma / sum_rows are the gradients of sum(batchnorm(x,g,b) * dy)."""
+    be = b200_factory("f64")
+    x, g, b, dy = rt(6, 5, 4), rt(4), rt(4), rt(6, 5, 4)
+    dx = be.get(be.exec_op(OpKind.BATCHNORM_DX, {}, [x, g, dy])).data
+    dg = be.get(be.exec_op(OpKind.BN_DGAMMA, {}, [x, dy])).data
+    db = be.get(be.exec_op(OpKind.SUM_ROWS, {}, [dy])).data
+
+    def f(xx, gg, bb):
+        y = be.get(be.exec_op(OpKind.BATCHNORM, {}, [Tensor(xx.shape, xx), Tensor(gg.shape, gg),
+                                                     Tensor(bb.shape, bb)])).data
+        return float(np.sum(y * dy.data))
+
+    h = 1e-6
+    for (arr, grad, which) in ((x.data, dx, 0), (g.data, dg, 1), (b.data, db, 2)):
+        flat = arr.ravel()
+        for j in (0, flat.size // 2, flat.size - 1):
+            p, m = [x.data.copy(), g.data.copy(), b.data.copy()], [x.data.copy(), g.data.copy(), b.data.copy()]
+            p[which].ravel()[j] += h
+            m[which].ravel()[j] -= h
+            num = (f(*p) - f(*m)) / (2 * h)
+            assert abs(num - grad.ravel()[j]) <= 1e-6 * max(1.0, abs(num)), (which, j, num, grad.ravel()[j])
