@@ -119,6 +119,11 @@ int coex_ctx_event_elapsed(coex_ctx* ctx, int a, int b, double* ms);
 int coex_exec_op_timed(coex_ctx* ctx, int kind, const coex_attrs* attrs, int nin, const int64_t* in_ids,
                        int reps, double* avg_ms);
 
+/* Per-launch profile of one op's lowering (up to 6 launches): average device ms of each launch
+ * repeated `reps` times; kernel names into names[j * name_cap]. */
+int coex_exec_op_profile(coex_ctx* ctx, int kind, const coex_attrs* attrs, int nin, const int64_t* in_ids,
+                         int reps, double* ms, int* nlaunch, char* names, int name_cap);
+
 /* Device-side per-kernel stamps (%globaltimer, kernel kind) for the next passes (0 = off).
  * coex_ctx_read_trace returns n (time_ns, kind) pairs of the last pass. */
 int coex_ctx_set_trace(coex_ctx* ctx, int capacity);

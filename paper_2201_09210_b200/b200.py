@@ -62,6 +62,9 @@ SIGNATURES = {
     "coex_ctx_event_elapsed": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int, _DP]),
     "coex_exec_op_timed": (ctypes.c_int, [_P, ctypes.c_int, ctypes.POINTER(CoexAttrs), ctypes.c_int, _I64P,
                                           ctypes.c_int, _DP]),
+    "coex_exec_op_profile": (ctypes.c_int, [_P, ctypes.c_int, ctypes.POINTER(CoexAttrs), ctypes.c_int, _I64P,
+                                            ctypes.c_int, _DP, ctypes.POINTER(ctypes.c_int), ctypes.c_char_p,
+                                            ctypes.c_int]),
     "coex_nccl_unique_id": (ctypes.c_int, [ctypes.c_char_p]),
     "coex_ctx_init_comm": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int, ctypes.c_char_p]),
     "coex_ctx_set_trace": (ctypes.c_int, [_P, ctypes.c_int]),
@@ -187,6 +190,7 @@ class B200Backend:
         self.var_idx: dict = {}
         self._vshape: dict = {}
         self.active = None
+        self.op_log = None            # list: record (kind, attrs, input shapes) of eager ops
         if dp is not None and (dp.world > 1 or dp.force):
             self._init_comm()
 
@@ -250,6 +254,25 @@ class B200Backend:
                                            ctypes.byref(ms)))
         return ms.value
 
+    def profile_op(self, kind: OpKind, attrs: dict, values: list, reps: int = 20) -> list:
+        """[(kernel name, average device ms)] for every launch of the op's lowering."""
+        import re
+        devs = [self.put(v) for v in values]
+        at = _attrs(kind, attrs)
+        ids = (ctypes.c_int64 * 3)(*[d.id for d in devs], *([0] * (3 - len(devs))))
+        ms = (ctypes.c_double * 8)()
+        n = ctypes.c_int()
+        cap = 256
+        names = ctypes.create_string_buffer(8 * cap)
+        _check(self.lib.coex_exec_op_profile(self.ctx, kind.code, ctypes.byref(at), len(devs), ids, reps, ms,
+                                             ctypes.byref(n), names, cap))
+        out = []
+        for j in range(n.value):
+            raw = names.raw[j * cap:(j + 1) * cap].split(b"\0", 1)[0].decode(errors="replace")
+            m = re.search(r"(k_[A-Za-z0-9_]+)", raw)
+            out.append((m.group(1) if m else raw, ms[j]))
+        return out
+
     # ------------------------------------------------------------ eager side
     def put(self, t) -> DevTensor:
         if isinstance(t, DevTensor):
@@ -278,6 +301,8 @@ class B200Backend:
 
     def exec_op(self, kind: OpKind, attrs: dict, values: list) -> DevTensor:
         devs = [self.put(v) for v in values]
+        if self.op_log is not None:
+            self.op_log.append((kind, dict(attrs), tuple(tuple(d.shape) for d in devs)))
         at = _attrs(kind, attrs)
         ids = (ctypes.c_int64 * 3)(*[d.id for d in devs], *([0] * (3 - len(devs))))
         out = ctypes.c_int64()

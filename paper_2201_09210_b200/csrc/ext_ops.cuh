@@ -101,6 +101,118 @@ __global__ void __launch_bounds__(256) k_im2col(Im2colParams p) {
   }
 }
 
+// Vectorised bf16 im2col (C % 8 == 0): one thread = 8 consecutive channels of one
+// (pixel, ky, kx) = two float4 loads, one 16-byte store; 32-bit index arithmetic.
+__global__ void __launch_bounds__(256) k_im2col_bf16v(Im2colParams p) {
+  stamp(p.ds, SK_FUSED);
+  if (skip(p.ds)) return;
+  const float* x = res<float>(p.x);
+  const int C8 = (int)(p.C / 8), k = p.k, H = (int)p.H, W = (int)p.W, Ho = (int)p.Ho, Wo = (int)p.Wo;
+  const int Q = k * k * C8;                       // 16-byte units per row (ld == Kc)
+  const long long M = p.N * p.Ho * p.Wo;
+  const long long total = M * Q;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long u = (long long)blockIdx.x * blockDim.x + threadIdx.x; u < total; u += stride) {
+    const unsigned m = (unsigned)(u / Q);          // host guarantees M < 2^31
+    const int q = (int)(u - (long long)m * Q);
+    const int ky = q / (k * C8), r2 = q - ky * k * C8, kx = r2 / C8, cg = r2 - kx * C8;
+    const int ox = (int)(m % (unsigned)Wo);
+    const unsigned t = m / (unsigned)Wo;
+    const int oy = (int)(t % (unsigned)Ho);
+    const long long n = t / (unsigned)Ho;
+    const int iy = oy * p.s - p.p + ky, ix = ox * p.s - p.p + kx;
+    uint4 out = make_uint4(0u, 0u, 0u, 0u);
+    if (iy >= 0 && iy < H && ix >= 0 && ix < W) {
+      const float4* src = (const float4*)(x + ((n * H + iy) * W + ix) * p.C + cg * 8);
+      const float4 a = src[0], b = src[1];
+      __nv_bfloat162 v0 = __floats2bfloat162_rn(a.x, a.y), v1 = __floats2bfloat162_rn(a.z, a.w);
+      __nv_bfloat162 v2 = __floats2bfloat162_rn(b.x, b.y), v3 = __floats2bfloat162_rn(b.z, b.w);
+      out.x = *(uint32_t*)&v0; out.y = *(uint32_t*)&v1; out.z = *(uint32_t*)&v2; out.w = *(uint32_t*)&v3;
+    }
+    *(uint4*)((__nv_bfloat16*)p.dst + (long long)m * p.ld + (long long)q * 8) = out;
+  }
+}
+
+// Transposed bf16 im2col dst[kk][m] (weight-gradient operand, K = output pixels), C % 4 == 0:
+// 64 m x 32 kk tiles; each thread loads float4 runs of channels (8 threads per pixel row)
+// and the tile is written back along pixels as bf16 pairs.
+__global__ void __launch_bounds__(256) k_im2col_bf16t(Im2colParams p) {
+  stamp(p.ds, SK_FUSED);
+  if (skip(p.ds)) return;
+  const float* x = res<float>(p.x);
+  __shared__ float tile[64][33];
+  const int t = threadIdx.x;
+  const int C = (int)p.C, k = p.k, H = (int)p.H, W = (int)p.W, Ho = (int)p.Ho, Wo = (int)p.Wo;
+  const long long Kc = (long long)k * k * C;
+  const unsigned M = (unsigned)(p.N * p.Ho * p.Wo);
+  const long long tm = (p.ld + 63) / 64, tk = (Kc + 31) / 32;
+  const int kq = t & 7, rl = t >> 3;                 // 8 float4 groups x 32 rows per pass
+  const int tx = t & 31, ty = t >> 5;
+  for (long long tt = blockIdx.x; tt < tm * tk; tt += gridDim.x) {
+    const long long m0 = (tt % tm) * 64, k0 = (tt / tm) * 32;
+    const long long kk = k0 + 4 * kq;
+    const int c = (int)(kk % C), kx = (int)((kk / C) % k), ky = (int)(kk / ((long long)C * k));
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int j = rl + 32 * h;
+      const unsigned m = (unsigned)(m0 + j);
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (m < M && kk < Kc) {
+        const int ox = (int)(m % (unsigned)Wo);
+        const unsigned r = m / (unsigned)Wo;
+        const int oy = (int)(r % (unsigned)Ho);
+        const long long n = r / (unsigned)Ho;
+        const int iy = oy * p.s - p.p + ky, ix = ox * p.s - p.p + kx;
+        if (iy >= 0 && iy < H && ix >= 0 && ix < W) v = *(const float4*)(x + ((n * H + iy) * W + ix) * C + c);
+      }
+      tile[j][4 * kq] = v.x; tile[j][4 * kq + 1] = v.y; tile[j][4 * kq + 2] = v.z; tile[j][4 * kq + 3] = v.w;
+    }
+    __syncthreads();
+    for (int j = ty; j < 32; j += 8) {
+      const long long kr = k0 + j, m = m0 + 2 * tx;
+      if (kr < Kc && m < p.ld) {
+        __nv_bfloat162 v = __floats2bfloat162_rn(tile[2 * tx][j], tile[2 * tx + 1][j]);
+        *(__nv_bfloat162*)((__nv_bfloat16*)p.dst + kr * p.ld + m) = v;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// Scalar bf16 im2col for C % 8 != 0 (e.g. the 3-channel image layer): one thread = one
+// 8-element unit of a row, 32-bit index arithmetic.
+__global__ void __launch_bounds__(256) k_im2col_bf16s(Im2colParams p) {
+  stamp(p.ds, SK_FUSED);
+  if (skip(p.ds)) return;
+  const float* x = res<float>(p.x);
+  const int C = (int)p.C, k = p.k, H = (int)p.H, W = (int)p.W, Ho = (int)p.Ho, Wo = (int)p.Wo;
+  const int Kc = k * k * C;
+  const int Q = (int)(p.ld / 8);
+  const long long total = p.N * p.Ho * p.Wo * Q;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long u = (long long)blockIdx.x * blockDim.x + threadIdx.x; u < total; u += stride) {
+    const unsigned m = (unsigned)(u / Q);
+    const int q = (int)(u - (long long)m * Q);
+    const int ox = (int)(m % (unsigned)Wo);
+    const unsigned r = m / (unsigned)Wo;
+    const int oy = (int)(r % (unsigned)Ho);
+    const long long n = r / (unsigned)Ho;
+    __align__(16) __nv_bfloat16 v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int kk = q * 8 + j;
+      float val = 0.f;
+      if (kk < Kc) {
+        const int c = kk % C, kx = (kk / C) % k, ky = kk / (C * k);
+        const int iy = oy * p.s - p.p + ky, ix = ox * p.s - p.p + kx;
+        if (iy >= 0 && iy < H && ix >= 0 && ix < W) val = x[((n * H + iy) * W + ix) * C + c];
+      }
+      v[j] = __float2bfloat16_rn(val);
+    }
+    *(uint4*)((__nv_bfloat16*)p.dst + (long long)m * p.ld + (long long)q * 8) = *(const uint4*)v;
+  }
+}
+
 // f64 parity path for the transposed operand is not needed: the SIMT GEMM reads the
 // row-major im2col buffer with trans_a (element-exact), so only float tiles go through smem.
 
@@ -153,6 +265,53 @@ __global__ void __launch_bounds__(256) k_col2im(Col2imParams p) {
   publish_late(p.out, o);
 }
 
+// Vectorised col2im (F % V == 0, V = 4 or 1): one thread = V channels of one output pixel;
+// only the (ky, kx) taps congruent with the output position are visited, ascending.
+template <int V>
+__global__ void __launch_bounds__(256) k_col2im_v(Col2imParams p) {
+  stamp(p.ds, SK_FUSED);
+  if (skip(p.ds)) return;
+  float* o = pick_out<float>(p.out, res<float>(p.a), res<float>(p.b));
+  publish_early(p.out, o);
+  count_op(p.ds);
+  const float* cols = (const float*)p.cols;
+  const int F4 = (int)(p.F / V), k = p.k, s = p.s, pd = p.p, H = (int)p.H, W = (int)p.W;
+  const int Ho = (int)p.Ho, Wo = (int)p.Wo;
+  const long long kkF = (long long)k * k * p.F;
+  const long long total = p.N * p.Ho * p.Wo * F4;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long u = (long long)blockIdx.x * blockDim.x + threadIdx.x; u < total; u += stride) {
+    const unsigned pix = (unsigned)(u / F4);        // host guarantees N*Ho*Wo < 2^31
+    const int f4 = (int)(u - (long long)pix * F4);
+    const int ox = (int)(pix % (unsigned)Wo);
+    const unsigned r = pix / (unsigned)Wo;
+    const int oy = (int)(r % (unsigned)Ho);
+    const long long n = r / (unsigned)Ho;
+    float acc[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) acc[v] = 0.f;
+    for (int ky = (oy + pd) % s; ky < k; ky += s) {
+      const int iy = (oy + pd - ky) / s;
+      if (oy + pd - ky < 0 || iy >= H) continue;
+      for (int kx = (ox + pd) % s; kx < k; kx += s) {
+        const int ix = (ox + pd - kx) / s;
+        if (ox + pd - kx < 0 || ix >= W) continue;
+        const float* src = cols + ((n * H + iy) * W + ix) * kkF + ((long long)ky * k + kx) * p.F + f4 * V;
+        if constexpr (V == 4) {
+          const float4 v = *(const float4*)src;
+          acc[0] = __fadd_rn(acc[0], v.x); acc[1] = __fadd_rn(acc[1], v.y);
+          acc[2] = __fadd_rn(acc[2], v.z); acc[3] = __fadd_rn(acc[3], v.w);
+        } else {
+          acc[0] = __fadd_rn(acc[0], src[0]);
+        }
+      }
+    }
+    if constexpr (V == 4) *(float4*)(o + (long long)pix * p.F + f4 * 4) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+    else o[(long long)pix * p.F + f4] = acc[0];
+  }
+  publish_late(p.out, o);
+}
+
 // ------------------------------------------------------------------ column statistics
 // Per-channel (last axis) sums over all leading rows, in double, with a per-channel shift
 // K_c = x[0, c] (numerically a centred one-pass): S1 = sum(x-K), S2 = sum((x-K)^2),
@@ -166,14 +325,17 @@ struct ColStatsParams {
   In x, dy;
   long long R, C;
   int mode;
-  double* part;              // [gridDim.x][C][4]
+  double* part;              // [gridDim.x][C][4] partials, or [C][4] accumulator when atomic
+  int atomic;
   double* stats;             // [C][4]: mean, rstd, mean(dy), mean(dy*xhat)   (COL_BN, COL_BN_DX)
   unsigned int* counter;     // zero-initialised; reset by the last block
   In a, b;                   // node operands (ping-pong output choice only)
   Out out;                   // [C] result (COL_SUM_ROWS, COL_BN_DGAMMA)
 };
 
-template <typename T>
+// V = channels per thread (4: float4 loads when C % 4 == 0 and T = float; else 1); rows
+// unrolled by 4 so each thread keeps several independent loads in flight.
+template <typename T, int V>
 __global__ void __launch_bounds__(256) k_colstats(ColStatsParams p) {
   stamp(p.ds, SK_REDUCE);
   if (skip(p.ds)) return;
@@ -188,50 +350,95 @@ __global__ void __launch_bounds__(256) k_colstats(ColStatsParams p) {
   }
   count_op(p.ds);
   const long long C = p.C, R = p.R;
-  const int L = (int)(C < 256 ? C : 256);          // lanes per row
-  const int rpi = 256 / L;                         // rows per iteration
+  const long long CV = C / V;                      // vector lanes per row
+  const int L = (int)(CV < 256 ? CV : 256);
+  const int rpi = 256 / L;
   const int t = threadIdx.x, cc = t % L, rr = t / L;
-  const int slots = (int)((C + L - 1) / L);
-  // row range of this block
+  const int slots = (int)((CV + L - 1) / L);
   const long long r_begin = R * blockIdx.x / gridDim.x, r_end = R * (blockIdx.x + 1) / gridDim.x;
-  double a1[kColMaxSlots], a2[kColMaxSlots], a3[kColMaxSlots], a4[kColMaxSlots], sh[kColMaxSlots];
+  constexpr int S = kColMaxSlots / V > 0 ? kColMaxSlots / V : 1;
+  double a1[S][V], a2[S][V], a3[S][V], a4[S][V], sh[S][V];
 #pragma unroll
-  for (int j = 0; j < kColMaxSlots; ++j) {
-    a1[j] = a2[j] = a3[j] = a4[j] = 0.0;
-    const long long c = cc + (long long)j * L;
-    sh[j] = (p.mode != COL_SUM_ROWS && j < slots && c < C) ? (double)x[c] : 0.0;
-  }
+  for (int j = 0; j < S; ++j)
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      a1[j][v] = a2[j][v] = a3[j][v] = a4[j][v] = 0.0;
+      const long long c = (cc + (long long)j * L) * V + v;
+      sh[j][v] = (p.mode != COL_SUM_ROWS && j < slots && c < C) ? (double)x[c] : 0.0;
+    }
   if (rr < rpi) {
-    for (long long r = r_begin + rr; r < r_end; r += rpi) {
 #pragma unroll
-      for (int j = 0; j < kColMaxSlots; ++j) {
-        const long long c = cc + (long long)j * L;
-        if (j < slots && c < C) {
-          const double v = (double)x[r * C + c] - sh[j];
-          a1[j] += v;
-          a2[j] += v * v;
+    for (int j = 0; j < S; ++j) {
+      if (j >= slots) break;
+      const long long c0 = (cc + (long long)j * L) * V;
+      if (c0 >= C) break;
+      long long r = r_begin + rr;
+      for (; r + 3 * rpi < r_end; r += 4 * rpi) {
+        T xv[4][V], gv[4][V];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const long long off = (r + (long long)q * rpi) * C + c0;
+          if constexpr (V == 4) {
+            const float4 f = *(const float4*)(x + off);
+            xv[q][0] = f.x; xv[q][1] = f.y; xv[q][2] = f.z; xv[q][3] = f.w;
+            if (with_dy) {
+              const float4 g = *(const float4*)(dy + off);
+              gv[q][0] = g.x; gv[q][1] = g.y; gv[q][2] = g.z; gv[q][3] = g.w;
+            }
+          } else {
+            xv[q][0] = x[off];
+            if (with_dy) gv[q][0] = dy[off];
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+          for (int v = 0; v < V; ++v) {
+            const double d = (double)xv[q][v] - sh[j][v];
+            a1[j][v] += d;
+            a2[j][v] += d * d;
+            if (with_dy) {
+              const double g = (double)gv[q][v];
+              a3[j][v] += g;
+              a4[j][v] += g * d;
+            }
+          }
+      }
+      for (; r < r_end; r += rpi) {
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          const long long off = r * C + c0 + v;
+          const double d = (double)x[off] - sh[j][v];
+          a1[j][v] += d;
+          a2[j][v] += d * d;
           if (with_dy) {
-            const double g = (double)dy[r * C + c];
-            a3[j] += g;
-            a4[j] += g * v;
+            const double g = (double)dy[off];
+            a3[j][v] += g;
+            a4[j][v] += g * d;
           }
         }
       }
     }
   }
   __shared__ double sm[256][4];
-  for (int j = 0; j < slots; ++j) {
-    sm[t][0] = a1[j]; sm[t][1] = a2[j]; sm[t][2] = a3[j]; sm[t][3] = a4[j];
-    __syncthreads();
-    const long long c = t + (long long)j * L;
-    if (t < L && c < C) {
-      double s[4] = {0.0, 0.0, 0.0, 0.0};
-      for (int q = 0; q < rpi; ++q)
-        for (int u = 0; u < 4; ++u) s[u] += sm[q * L + t][u];
-      double* dst = p.part + ((long long)blockIdx.x * C + c) * 4;
-      for (int u = 0; u < 4; ++u) dst[u] = s[u];
+  for (int j = 0; j < slots && j < S; ++j) {
+    for (int v = 0; v < V; ++v) {
+      sm[t][0] = a1[j][v]; sm[t][1] = a2[j][v]; sm[t][2] = a3[j][v]; sm[t][3] = a4[j][v];
+      __syncthreads();
+      const long long c = (t + (long long)j * L) * V + v;
+      if (t < L && c < C) {
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int q = 0; q < rpi; ++q)
+          for (int u = 0; u < 4; ++u) acc[u] += sm[q * L + t][u];
+        if (p.atomic) {        // tolerance modes: fp64 atomics into the [C][4] accumulator
+          for (int u = 0; u < 4; ++u) atomicAdd(p.part + c * 4 + u, acc[u]);
+        } else {               // parity mode: per-block partials merged in block order
+          double* dst = p.part + ((long long)blockIdx.x * C + c) * 4;
+          for (int u = 0; u < 4; ++u) dst[u] = acc[u];
+        }
+      }
+      __syncthreads();
     }
-    __syncthreads();
   }
   // last block: combine partials (block order) and finalise
   __shared__ unsigned int last;
@@ -241,11 +448,33 @@ __global__ void __launch_bounds__(256) k_colstats(ColStatsParams p) {
   if (!last) return;
   __threadfence();
   for (long long c = t; c < C; c += blockDim.x) {
-    double s1 = 0.0, s2 = 0.0, d1 = 0.0, d2 = 0.0;
-    for (unsigned int b = 0; b < gridDim.x; ++b) {
-      const double* q = p.part + ((long long)b * C + c) * 4;
-      s1 += q[0]; s2 += q[1]; d1 += q[2]; d2 += q[3];
+    // four interleaved accumulators (fixed combination order: deterministic), L2 loads
+    // (the partials were written by other blocks; this SM never cached them)
+    double acc[4][4] = {{0.0}};
+    const double2* q = (const double2*)(p.part + c * 4);
+    const long long stride2 = 2 * C;                // two double2 per channel per block
+    const unsigned int nb = p.atomic ? 1u : gridDim.x;
+    unsigned int b = 0;
+    for (; b + 4 <= nb; b += 4) {
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        const double2 u = __ldcg(q + (long long)(b + w) * stride2), v = __ldcg(q + (long long)(b + w) * stride2 + 1);
+        acc[w][0] += u.x; acc[w][1] += u.y; acc[w][2] += v.x; acc[w][3] += v.y;
+      }
     }
+    for (; b < nb; ++b) {
+      const double2 u = __ldcg(q + (long long)b * stride2), v = __ldcg(q + (long long)b * stride2 + 1);
+      acc[0][0] += u.x; acc[0][1] += u.y; acc[0][2] += v.x; acc[0][3] += v.y;
+    }
+    if (p.atomic) {                                 // leave the accumulator zeroed for the next launch
+      double2* z = (double2*)(p.part + c * 4);
+      z[0] = make_double2(0.0, 0.0);
+      z[1] = make_double2(0.0, 0.0);
+    }
+    const double s1 = (acc[0][0] + acc[1][0]) + (acc[2][0] + acc[3][0]);
+    const double s2 = (acc[0][1] + acc[1][1]) + (acc[2][1] + acc[3][1]);
+    const double d1 = (acc[0][2] + acc[1][2]) + (acc[2][2] + acc[3][2]);
+    const double d2 = (acc[0][3] + acc[1][3]) + (acc[2][3] + acc[3][3]);
     if (p.mode == COL_SUM_ROWS) {
       o[c] = (T)s1;
       continue;

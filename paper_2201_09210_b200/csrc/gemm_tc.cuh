@@ -55,21 +55,33 @@ struct CvtParams {
 __global__ void __launch_bounds__(256) k_cvt_bf16(CvtParams p) {
   stamp(p.ds, SK_FUSED);
   if (skip(p.ds)) return;
-  const int w = blockIdx.y;
-  const float* s = res<float>(p.src[w]);
-  __nv_bfloat16* d = p.dst[w];
-  const long long R = p.rows[w], K = p.K, ld = p.ld;
-  if (!p.trans[w]) {
-    // one row per block iteration, 8 consecutive k per thread, one 16-byte store
-    for (long long r = blockIdx.x; r < R; r += gridDim.x) {
+  // operand select without dynamic indexing of the parameter arrays (that would copy the
+  // whole parameter block to local memory in every thread)
+  const bool w1 = blockIdx.y != 0;
+  const float* s = res<float>(w1 ? p.src[1] : p.src[0]);
+  __nv_bfloat16* d = w1 ? p.dst[1] : p.dst[0];
+  const long long R = w1 ? p.rows[1] : p.rows[0], K = p.K, ld = p.ld;
+  if (!(w1 ? p.trans[1] : p.trans[0])) {
+    // flattened over 8-element units of every row: 8 consecutive k per thread, one 16-byte store
+    const long long per_row = ld / 8, total = R * per_row;
+    const bool vec = (K % 4) == 0 && ld == K && ((uintptr_t)s & 15) == 0;
+    for (long long u = (long long)blockIdx.x * blockDim.x + threadIdx.x; u < total;
+         u += (long long)gridDim.x * blockDim.x) {
+      const long long r = u / per_row, k = (u - r * per_row) * 8;
       const float* src = s + r * K;
-      __nv_bfloat16* dst = d + r * ld;
-      for (long long k = (long long)threadIdx.x * 8; k < ld; k += (long long)blockDim.x * 8) {
+      uint4 o;
+      if (vec) {
+        const float4 a = *(const float4*)(src + k), b = *(const float4*)(src + k + 4);
+        __nv_bfloat162 v0 = __floats2bfloat162_rn(a.x, a.y), v1 = __floats2bfloat162_rn(a.z, a.w);
+        __nv_bfloat162 v2 = __floats2bfloat162_rn(b.x, b.y), v3 = __floats2bfloat162_rn(b.z, b.w);
+        o.x = *(uint32_t*)&v0; o.y = *(uint32_t*)&v1; o.z = *(uint32_t*)&v2; o.w = *(uint32_t*)&v3;
+      } else {
         __align__(16) __nv_bfloat16 v[8];
 #pragma unroll
         for (int j = 0; j < 8; ++j) v[j] = __float2bfloat16_rn(k + j < K ? src[k + j] : 0.f);
-        *(uint4*)(dst + k) = *(const uint4*)v;
+        o = *(const uint4*)v;
       }
+      *(uint4*)(d + r * ld + k) = o;
     }
     return;
   }
@@ -283,7 +295,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc(const __grid_constant
             *(float4*)(dst + i) = make_float4(__uint_as_float(r[i]), __uint_as_float(r[i + 1]),
                                               __uint_as_float(r[i + 2]), __uint_as_float(r[i + 3]));
         } else {
-          for (int i = 0; i < valid; ++i) dst[i] = __uint_as_float(r[i]);
+#pragma unroll
+          for (int i = 0; i < 16; ++i)
+            if (i < valid) dst[i] = __uint_as_float(r[i]);
         }
       }
     }

@@ -654,47 +654,83 @@ struct ChainParams {
   void** red_pub[kChainPub];
 };
 
+// The chain program, its operand pointers and every thread's register file live in shared
+// memory: the interpreter indexes them dynamically, which on registers / kernel parameters
+// would force per-thread local-memory copies.  Register file layout [reg][thread].
 template <typename T>
-__device__ __forceinline__ T chain_src(const ChainParams& p, const T* r, const T* const* ip, const T* sv,
-                                       int x, long long i) {
-  if (x < kChainRegs) return r[x];
-  const int k = x - kChainRegs;
-  return p.in_scalar[k] ? sv[k] : ip[k][i];
+struct ChainSmem {
+  ChainOp ops[kChainOps];
+  const T* ip[kChainIn];
+  T sv[kChainIn];
+  unsigned char in_scalar[kChainIn];
+  unsigned char out_reg[kChainOut];
+  T* out_buf[kChainOut];
+  T r[kChainRegs][256];
+};
+
+template <typename T>
+__device__ __forceinline__ void chain_load(const ChainParams& p, ChainSmem<T>& S) {
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < kChainOps; ++k) S.ops[k] = p.ops[k];
+#pragma unroll
+    for (int k = 0; k < kChainIn; ++k) {
+      const T* ptr = k < p.nin ? res<T>(p.in[k]) : nullptr;
+      S.ip[k] = ptr;
+      S.in_scalar[k] = p.in_scalar[k];
+      S.sv[k] = (k < p.nin && p.in_scalar[k]) ? ptr[0] : T(0);
+    }
+#pragma unroll
+    for (int j = 0; j < kChainOut; ++j) {
+      S.out_reg[j] = p.out_reg[j];
+      S.out_buf[j] = (T*)p.out_buf[j];
+    }
+  }
+  __syncthreads();
 }
 
 template <typename T>
-__device__ __forceinline__ void chain_eval(const ChainParams& p, T* r, const T* const* ip, const T* sv, long long i) {
-  for (int k = 0; k < p.nops; ++k) {
-    const ChainOp o = p.ops[k];
-    r[o.dst] = ew_apply((int)o.op, chain_src(p, r, ip, sv, o.a, i),
-                        ew_binary(o.op) ? chain_src(p, r, ip, sv, o.b, i) : T(0));
+__device__ __forceinline__ T chain_src(const ChainSmem<T>& S, int x, long long i) {
+  if (x < kChainRegs) return S.r[x][threadIdx.x];
+  const int k = x - kChainRegs;
+  return S.in_scalar[k] ? S.sv[k] : S.ip[k][i];
+}
+
+template <typename T>
+__device__ __forceinline__ void chain_eval(const ChainSmem<T>& Sc, int nops, long long i) {
+  ChainSmem<T>& S = const_cast<ChainSmem<T>&>(Sc);
+  for (int k = 0; k < nops; ++k) {
+    const ChainOp o = S.ops[k];
+    S.r[o.dst][threadIdx.x] = ew_apply((int)o.op, chain_src(S, o.a, i), ew_binary(o.op) ? chain_src(S, o.b, i) : T(0));
   }
 }
 
 __device__ __forceinline__ void chain_publish(const ChainParams& p) {
-  for (int j = 0; j < p.nout; ++j)
-    for (int q = 0; q < p.npub[j]; ++q) *p.pub[j][q] = p.out_buf[j];
-  if (p.red)
-    for (int q = 0; q < p.red_npub; ++q) *p.red_pub[q] = p.red_buf;
+#pragma unroll
+  for (int j = 0; j < kChainOut; ++j)
+#pragma unroll
+    for (int q = 0; q < kChainPub; ++q)
+      if (j < p.nout && q < p.npub[j]) *p.pub[j][q] = p.out_buf[j];
+  if (p.red) {
+#pragma unroll
+    for (int q = 0; q < kChainPub; ++q)
+      if (q < p.red_npub) *p.red_pub[q] = p.red_buf;
+  }
 }
 
 template <typename T>
 __global__ void __launch_bounds__(256) k_chain(ChainParams p) {
   stamp(p.ds, SK_FUSED);
   if (skip(p.ds)) return;
-  const T* ip[kChainIn];
-  T sv[kChainIn];
-  for (int k = 0; k < p.nin; ++k) {
-    ip[k] = res<T>(p.in[k]);
-    sv[k] = p.in_scalar[k] ? ip[k][0] : T(0);
-  }
+  __shared__ ChainSmem<T> S;
+  chain_load(p, S);
   if (p.late == nullptr && blockIdx.x == 0 && threadIdx.x == 0) chain_publish(p);
   count_op(p.ds);
-  T r[kChainRegs];
+  const int nops = p.nops, nout = p.nout;
   const long long stride = (long long)gridDim.x * blockDim.x;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < p.n; i += stride) {
-    chain_eval(p, r, ip, sv, i);
-    for (int j = 0; j < p.nout; ++j) ((T*)p.out_buf[j])[i] = r[p.out_reg[j]];
+    chain_eval(S, nops, i);
+    for (int j = 0; j < nout; ++j) S.out_buf[j][i] = S.r[S.out_reg[j]][threadIdx.x];
   }
   if (p.late != nullptr) {
     __syncthreads();
@@ -715,25 +751,21 @@ template <typename T, bool EXACT>
 __global__ void __launch_bounds__(256) k_chain_reduce(ChainParams p) {
   stamp(p.ds, SK_FUSED);
   if (skip(p.ds)) return;
-  constexpr int CH = 2048;
+  constexpr int CH = 1024;
   __shared__ T vals[CH];
   __shared__ double part[8];
-  const T* ip[kChainIn];
-  T sv[kChainIn];
-  for (int k = 0; k < p.nin; ++k) {
-    ip[k] = res<T>(p.in[k]);
-    sv[k] = p.in_scalar[k] ? ip[k][0] : T(0);
-  }
+  __shared__ ChainSmem<T> S;
+  chain_load(p, S);
   count_op(p.ds);
-  T r[kChainRegs];
+  const int nops = p.nops, nout = p.nout, red_reg = p.red_reg;
   double acc = 0.0;
   for (long long base = 0; base < p.n; base += CH) {
     const int cnt = (int)min((long long)CH, p.n - base);
     for (int t = threadIdx.x; t < cnt; t += blockDim.x) {
       const long long i = base + t;
-      chain_eval(p, r, ip, sv, i);
-      for (int j = 0; j < p.nout; ++j) ((T*)p.out_buf[j])[i] = r[p.out_reg[j]];
-      vals[t] = r[p.red_reg];
+      chain_eval(S, nops, i);
+      for (int j = 0; j < nout; ++j) S.out_buf[j][i] = S.r[S.out_reg[j]][threadIdx.x];
+      vals[t] = chain_src(S, red_reg, i);
     }
     __syncthreads();
     if constexpr (EXACT) {

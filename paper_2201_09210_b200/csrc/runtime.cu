@@ -567,19 +567,42 @@ struct TcPlan {
   int bn = 256, splits = 1;
   int64_t tiles = 1;
 };
+// Tile width and split-K count from a small cost model of one launch: waves of CTAs, each
+// bounded by its MMA time or its L2->SMEM operand stream, plus the fp32 epilogue store and a
+// fixed prologue; split-K adds the slice reduction.  (Per-SM figures: 1/148 of the measured
+// bf16 peak, ~135 GB/s of L2 operand bandwidth, ~44 GB/s of concurrent store bandwidth.)
 TcPlan tc_plan(int64_t M, int64_t N, int64_t K, bool allow_split) {
-  TcPlan t;
-  t.bn = N <= 64 ? 64 : N <= 128 ? 128 : 256;
-  t.tiles = ((M + TC_BM - 1) / TC_BM) * ((N + t.bn - 1) / t.bn);
-  if (t.tiles < 1) t.tiles = 1;
+  TcPlan best;
+  double best_t = 1e30;
   const int64_t nk = (K + TC_BK - 1) / TC_BK;
-  if (allow_split && t.tiles < kNumSMs && nk >= 8) {
-    int64_t s = (kNumSMs + t.tiles - 1) / t.tiles;
-    if (s > nk / 4) s = nk / 4;
-    if (s > 32) s = 32;
-    t.splits = (int)(s < 1 ? 1 : s);
+  const int bns[3] = {64, 128, 256};
+  for (int bn : bns) {
+    if (bn > 64 && N <= bn / 2) continue;
+    const int64_t tiles = ((M + TC_BM - 1) / TC_BM) * ((N + bn - 1) / bn);
+    const int64_t smax = allow_split ? (nk / 2 < 32 ? (nk / 2 > 1 ? nk / 2 : 1) : 32) : 1;
+    for (int64_t sp = 1; sp <= smax; ++sp) {
+      const int64_t ctas = (tiles < 1 ? 1 : tiles) * sp;
+      const int64_t waves = (ctas + kNumSMs - 1) / kNumSMs;
+      const double kper = (double)((nk + sp - 1) / sp);
+      const double mma = kper * 2.0 * TC_BM * bn * TC_BK / 10.7e12;
+      const double feed = kper * (double)(TC_BM + bn) * TC_BK * 2 / 135e9;
+      const double epi = (double)TC_BM * bn * 4 / 44e9;
+      double t = waves * ((mma > feed ? mma : feed) + epi + 2e-6);
+      if (sp > 1) t += (double)(sp + 1) * M * N * 4 / 5.5e12 + 2e-6;
+      if (t < best_t * 0.98) {
+        best_t = t;
+        best.bn = bn;
+        best.splits = (int)sp;
+        best.tiles = tiles < 1 ? 1 : tiles;
+      }
+    }
   }
-  return t;
+  return best;
+}
+
+size_t matmul_split_ws(int64_t M, int64_t N, int64_t K) {
+  const TcPlan t = tc_plan(M, N, K, true);
+  return t.splits > 1 ? (size_t)t.splits * M * N * 4 : 0;
 }
 
 template <int BN>
@@ -679,7 +702,12 @@ int build_xop_t(coex_ctx* c, const OpSpec& s, Launch* L, int* nL, size_t* ws_byt
         float* ws = t.splits > 1 ? (float*)cv.take((size_t)t.splits * M * F * 4) : nullptr;
         if (!build) break;
         ip.dst = A; ip.ld = bf16_pitch(Kc); ip.trans = 0;
-        L[(*nL)++].set((void*)k_im2col<float, __nv_bfloat16>, grid_for(M * ip.ld / 8), dim3(256), ip);
+        if (C % 8 == 0 && M < (1ll << 31))
+          L[(*nL)++].set((void*)k_im2col_bf16v, grid_for(M * Kc / 8), dim3(256), ip);
+        else if (M < (1ll << 31))
+          L[(*nL)++].set((void*)k_im2col_bf16s, grid_for(M * ip.ld / 8), dim3(256), ip);
+        else
+          L[(*nL)++].set((void*)k_im2col<float, __nv_bfloat16>, grid_for(M * ip.ld / 8), dim3(256), ip);
         CvtParams q{};
         q.ds = s.ds; q.src[0] = s.in[1]; q.rows[0] = F; q.K = Kc; q.ld = bf16_pitch(Kc); q.trans[0] = 1;
         q.dst[0] = (__nv_bfloat16*)B;
@@ -721,7 +749,12 @@ int build_xop_t(coex_ctx* c, const OpSpec& s, Launch* L, int* nL, size_t* ws_byt
         int rc = tc_gemm_launches(c, s.ds, A, B, M, Nc, C, t, s.in[0], s.in[1], s.out, cols, ws, L, nL);
         if (rc) return rc;
         cp.cols = cols;
-        L[(*nL)++].set((void*)k_col2im<float, float>, grid_for(N * Ho * Wo * F), dim3(256), cp);
+        if (F % 4 == 0 && N * Ho * Wo < (1ll << 31))
+          L[(*nL)++].set((void*)k_col2im_v<4>, grid_for(N * Ho * Wo * F / 4), dim3(256), cp);
+        else if (N * Ho * Wo < (1ll << 31))
+          L[(*nL)++].set((void*)k_col2im_v<1>, grid_for(N * Ho * Wo * F), dim3(256), cp);
+        else
+          L[(*nL)++].set((void*)k_col2im<float, float>, grid_for(N * Ho * Wo * F), dim3(256), cp);
         return COEX_OK;
       }
       void* cols = cv.take((size_t)M * Nc * es);
@@ -749,9 +782,15 @@ int build_xop_t(coex_ctx* c, const OpSpec& s, Launch* L, int* nL, size_t* ws_byt
         float* ws = t.splits > 1 ? (float*)cv.take((size_t)t.splits * Kc * F * 4) : nullptr;
         if (!build) break;
         ip.dst = A; ip.ld = bf16_pitch(P); ip.trans = 1;
-        const int64_t tiles = ((ip.ld + 31) / 32) * ((Kc + 31) / 32);
-        L[(*nL)++].set((void*)k_im2col<float, __nv_bfloat16>,
-                       dim3((unsigned)(tiles < kNumSMs * 16 ? tiles : kNumSMs * 16)), dim3(256), ip);
+        if (P < (1ll << 31) && C % 4 == 0) {
+          const int64_t tiles = ((ip.ld + 63) / 64) * ((Kc + 31) / 32);
+          L[(*nL)++].set((void*)k_im2col_bf16t, dim3((unsigned)(tiles < kNumSMs * 16 ? tiles : kNumSMs * 16)),
+                         dim3(256), ip);
+        } else {
+          const int64_t tiles = ((ip.ld + 31) / 32) * ((Kc + 31) / 32);
+          L[(*nL)++].set((void*)k_im2col<float, __nv_bfloat16>,
+                         dim3((unsigned)(tiles < kNumSMs * 16 ? tiles : kNumSMs * 16)), dim3(256), ip);
+        }
         CvtParams q{};
         q.ds = s.ds; q.src[0] = s.in[1]; q.rows[0] = F; q.K = P; q.ld = bf16_pitch(P); q.trans[0] = 1;
         q.dst[0] = (__nv_bfloat16*)B;
@@ -773,13 +812,21 @@ int build_xop_t(coex_ctx* c, const OpSpec& s, Launch* L, int* nL, size_t* ws_byt
       const int64_t C = s.in_shape[0][s.in_ndim[0] - 1];
       const int64_t n = numel_of(s.in_ndim[0], s.in_shape[0]);
       const int64_t R = n / C;
-      int64_t G = n / 16384;
-      if (G > kNumSMs * 2) G = kNumSMs * 2;
+      // partial blocks: enough to stream x at full bandwidth, few enough that the last block's
+      // merge of G x C partials stays small
+      // tolerance modes accumulate with fp64 atomics (no merge of per-block partials)
+      const bool atomic = !is_f64(c);
+      int64_t G = n / 8192;
+      if (!atomic && G > 32768 / C) G = 32768 / C;
+      if (G > kNumSMs * 4) G = kNumSMs * 4;
       if (G > R) G = R;
       if (G < 1) G = 1;
+      const bool v4 = !is_f64(c) && C % 4 == 0;
+      void* colfn = v4 ? (void*)k_colstats<float, 4> : (void*)k_colstats<T, 1>;
       ColStatsParams cp{};
       cp.ds = s.ds; cp.x = s.in[0]; cp.R = R; cp.C = C;
-      cp.part = (double*)cv.take((size_t)G * C * 4 * 8);
+      cp.atomic = atomic ? 1 : 0;
+      cp.part = (double*)cv.take((size_t)(atomic ? 1 : G) * C * 4 * 8);
       cp.stats = (double*)cv.take((size_t)C * 4 * 8);
       cp.counter = (unsigned int*)cv.take(16);
       cp.a = s.in[0];
@@ -789,13 +836,13 @@ int build_xop_t(coex_ctx* c, const OpSpec& s, Launch* L, int* nL, size_t* ws_byt
         cp.mode = s.kind == COEX_SUM_ROWS ? COL_SUM_ROWS : COL_BN_DGAMMA;
         if (s.kind == COEX_BN_DGAMMA) cp.dy = s.in[1];
         cp.out = s.out;
-        L[(*nL)++].set((void*)k_colstats<T>, dim3((unsigned)G), dim3(256), cp);
+        L[(*nL)++].set(colfn, dim3((unsigned)G), dim3(256), cp);
         return COEX_OK;
       }
       cp.mode = s.kind == COEX_BATCHNORM ? COL_BN : COL_BN_DX;
       if (s.kind == COEX_BATCHNORM_DX) cp.dy = s.in[2];
       cp.out = Out{};
-      L[(*nL)++].set((void*)k_colstats<T>, dim3((unsigned)G), dim3(256), cp);
+      L[(*nL)++].set(colfn, dim3((unsigned)G), dim3(256), cp);
       BnApplyParams ap{};
       ap.ds = s.ds; ap.x = s.in[0]; ap.g = s.in[1]; ap.third = s.in[2]; ap.stats = cp.stats;
       ap.n = n; ap.C = C; ap.dx = s.kind == COEX_BATCHNORM_DX; ap.out = s.out;
@@ -858,8 +905,8 @@ int build_launches(coex_ctx* c, const OpSpec& s, Launch* L, int* nL) {
   dim3 g((unsigned)(gx > 0 ? gx : 1), 2);
   L[0].set((void*)k_cvt_bf16, g, dim3(256), cv);
   *nL = 1;
-  return tc_gemm_launches(c, s.ds, s.scratch[0], s.scratch[1], M, N, K, tc_plan(M, N, K, false), s.in[0], s.in[1],
-                          s.out, nullptr, nullptr, L, nL);
+  return tc_gemm_launches(c, s.ds, s.scratch[0], s.scratch[1], M, N, K, tc_plan(M, N, K, s.ws != nullptr), s.in[0],
+                          s.in[1], s.out, nullptr, (float*)s.ws, L, nL);
 }
 
 int launch_now(coex_ctx* c, Launch& L) {
@@ -1181,6 +1228,11 @@ int eager_scratch(coex_ctx* c, OpSpec* s) {
     scratch_bytes(*s, &ba, &bb);
     CK(cudaMallocAsync(&s->scratch[0], ba, c->stream));
     CK(cudaMallocAsync(&s->scratch[1], bb, c->stream));
+    const int64_t M = s->trans_a ? s->in_shape[0][1] : s->in_shape[0][0];
+    const int64_t K = s->trans_a ? s->in_shape[0][0] : s->in_shape[0][1];
+    const int64_t N = s->trans_b ? s->in_shape[1][0] : s->in_shape[1][1];
+    const size_t wb = matmul_split_ws(M, N, K);
+    if (wb) CK(cudaMallocAsync((void**)&s->ws, wb, c->stream));
   }
   if (is_ext_compute(s->kind)) {
     Launch tmp[kMaxLaunches];
@@ -1275,6 +1327,45 @@ int coex_exec_op_timed(coex_ctx* c, int kind, const coex_attrs* attrs, int nin, 
   double ms = 0;
   rc = coex_ctx_event_elapsed(c, 62, 63, &ms);
   *avg_ms = ms / reps;
+  eager_free(c, &s);
+  coex_tensor_free(c, out);
+  return rc;
+}
+
+// Per-launch device time of one op (roofline evidence for multi-kernel ops): every launch of
+// the op's lowering is repeated `reps` times back to back between CUDA events on the context
+// stream, after one full warm run that fills the op's scratch.
+int coex_exec_op_profile(coex_ctx* c, int kind, const coex_attrs* attrs, int nin, const int64_t* in_ids, int reps,
+                         double* ms, int* nlaunch, char* names, int name_cap) {
+  if (reps < 1) return fail(COEX_INVALID, "reps must be >= 1");
+  int64_t out;
+  int rc = coex_exec_op(c, kind, attrs, nin, in_ids, &out);
+  if (rc) return rc;
+  TRec in[kMaxIn];
+  for (int i = 0; i < nin; ++i) in[i] = *get_t(c, in_ids[i]);
+  TRec* o = get_t(c, out);
+  OpSpec s;
+  eager_spec(c, kind, attrs, nin, in, *o, &s);
+  rc = eager_scratch(c, &s);
+  if (rc) return rc;
+  Launch L[kMaxLaunches];
+  int nL = 0;
+  rc = build_launches(c, s, L, &nL);
+  for (int i = 0; rc == COEX_OK && i < nL; ++i) rc = launch_now(c, L[i]);
+  for (int j = 0; rc == COEX_OK && j < nL; ++j) {
+    rc = coex_ctx_event_record(c, 62);
+    for (int r = 0; rc == COEX_OK && r < reps; ++r) rc = launch_now(c, L[j]);
+    if (rc == COEX_OK) rc = coex_ctx_event_record(c, 63);
+    double t = 0;
+    if (rc == COEX_OK) rc = coex_ctx_event_elapsed(c, 62, 63, &t);
+    ms[j] = t / reps;
+    const char* nm = nullptr;
+    if (names != nullptr && name_cap > 0) {
+      if (cudaFuncGetName(&nm, L[j].fn) != cudaSuccess || nm == nullptr) nm = "?";
+      snprintf(names + (size_t)j * name_cap, name_cap, "%s", nm);
+    }
+  }
+  *nlaunch = nL;
   eager_free(c, &s);
   coex_tensor_free(c, out);
   return rc;
@@ -1500,6 +1591,19 @@ struct Builder {
         s.scratch[1] = buf(next());
         read_out(s.out);
         s.nin = 2;
+        if (needs_scratch(c, s.kind)) {           // bf16 MatMul: split-K slices when the tile grid is small
+          const int64_t M = s.trans_a ? s.in_shape[0][1] : s.in_shape[0][0];
+          const int64_t K = s.trans_a ? s.in_shape[0][0] : s.in_shape[0][1];
+          const int64_t N = s.trans_b ? s.in_shape[1][0] : s.in_shape[1][1];
+          const size_t wb = matmul_split_ws(M, N, K);
+          if (wb) {
+            void* ws = nullptr;
+            CK(cudaMalloc(&ws, wb));
+            p->workspaces.push_back(ws);
+            p->ws_bytes += wb;
+            s.ws = (char*)ws;
+          }
+        }
         Launch L[kMaxLaunches];
         int nL = 0;
         int rc = build_launches(c, s, L, &nL);

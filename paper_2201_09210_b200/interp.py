@@ -255,6 +255,9 @@ class SkeletonCtx:
             h1 = a1.hid if (type(a1) is Val and a1.epoch == epoch) else None
             hids = [h0, h1]
             in_kinds = ("h" if h0 is not None else "e", "h" if h1 is not None else "e")
+        elif len(args) > 2:
+            hids = [a.hid if (type(a) is Val and a.epoch == epoch) else None for a in args]
+            in_kinds = _IN_KINDS[tuple(h is not None for h in hids)]
         else:
             hids = [h0]
             in_kinds = ("h",) if h0 is not None else ("e",)

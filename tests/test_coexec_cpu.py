@@ -184,3 +184,14 @@ def test_lazy_and_coexec_stats_shape():
     for k in ("python_exec_ms", "python_stall_ms", "graph_exec_ms", "graph_stall_ms", "phase_transitions",
               "traces_collected", "graph_regens", "steps_replayed", "throughput"):
         assert k in d
+
+
+def test_dcgan_reaches_steady_coexec():
+    """C2 alternates D / G steps through one SwitchCase: after both paths are traced
+    every step runs co-executed (no divergence, no replay) -- ternary extension ops
+    (batchnorm) must key identically in traced and skeleton steps."""
+    from paper_2201_09210_b200.workloads import C2_SMALL, dcgan_program
+    o = coexec.Orchestrator(lang.parse(dcgan_program(steps=12, **C2_SMALL)), SyntheticDataset(0),
+                            coexec.Mode.coexec, coexec.RunConfig(), CpuBackend())
+    o.run()
+    assert o.stats.counters() == (1, 3, 1, 0)

@@ -39,6 +39,15 @@ CONV = [
     (OpKind.CONV2D_DW, {"conv": (3, 1, 1)}, [rt(3, 5, 5, 7), rt(3, 5, 5, 16)]),
     (OpKind.CONV2D_DW, {"conv": (4, 2, 1)}, [rt(8, 16, 16, 64), rt(8, 8, 8, 128)]),
     (OpKind.CONV2D_DW, {"conv": (4, 2, 1)}, [rt(16, 32, 32, 3), rt(16, 16, 16, 64)]),
+    (OpKind.CONV2D_DW, {"conv": (4, 2, 1)}, [rt(2, 6, 6, 4), rt(2, 3, 3, 12)]),
+    (OpKind.CONV2D, {"conv": (4, 2, 1)}, [rt(2, 6, 6, 4), rt(64, 12)]),
+    (OpKind.CONV2D_T, {"conv": (4, 2, 1)}, [rt(2, 3, 3, 12), rt(64, 12)]),
+]
+MATMUL_SPLIT = [  # bf16 MatMuls whose tile grid is too small: split-K slices
+    (OpKind.MATMUL, {}, [rt(128, 8192), rt(8192, 1)]),
+    (OpKind.MATMUL, {}, [rt(8192, 128), rt(128, 1)]),
+    (OpKind.MATMUL, {}, [rt(100, 128), rt(128, 8192)]),
+    (OpKind.MATMUL, {}, [rt(256, 4096), rt(4096, 96)]),
 ]
 
 BN = [
@@ -96,6 +105,12 @@ def test_conv_f64_bitwise(b200_factory, i):
 def test_conv_tolerance(b200_factory, prec, tol, i):
     got, want = run(b200_factory(prec), *CONV[i])
     assert nrel(got, want) <= tol
+
+
+@pytest.mark.parametrize("i", range(len(MATMUL_SPLIT)))
+def test_matmul_bf16_split(b200_factory, i):
+    got, want = run(b200_factory("bf16"), *MATMUL_SPLIT[i])
+    assert nrel(got, want) <= 2e-2
 
 
 @pytest.mark.parametrize("prec,tol", [("f64", 1e-12), ("fp32", 1e-5), ("bf16", 1e-5)])

@@ -1,0 +1,34 @@
+"""Eager launches of selected C2 ops for ncu captures (one op per invocation argument).
+
+    ncu --set full -k regex:<kernel> python tools/ncu_ops.py <name> [...]
+"""
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_2201_09210_b200.b200 import B200Backend  # noqa: E402
+from paper_2201_09210_b200.tensor import OpKind, Tensor  # noqa: E402
+
+OPS = {
+    "convt_4x4x512": (OpKind.CONV2D_T, {"conv": (4, 2, 1)}, [(128, 4, 4, 512), (4096, 512)]),
+    "convt_16x16x128": (OpKind.CONV2D_T, {"conv": (4, 2, 1)}, [(128, 16, 16, 128), (1024, 128)]),
+    "conv_32x32x64": (OpKind.CONV2D, {"conv": (4, 2, 1)}, [(128, 32, 32, 64), (1024, 128)]),
+    "dw_32x32x64": (OpKind.CONV2D_DW, {"conv": (4, 2, 1)}, [(128, 32, 32, 64), (128, 16, 16, 128)]),
+    "conv_16x16x128": (OpKind.CONV2D, {"conv": (4, 2, 1)}, [(128, 16, 16, 128), (2048, 256)]),
+    "bn_16x16x128": (OpKind.BATCHNORM, {}, [(128, 16, 16, 128), (128,), (128,)]),
+    "mm_8192x128x1": (OpKind.MATMUL, {}, [(8192, 128), (128, 1)]),
+    "gemm_8192": (OpKind.MATMUL, {}, [(8192, 8192), (8192, 8192)]),
+}
+
+be = B200Backend(precision=os.environ.get("PREC", "bf16"))
+r = np.random.default_rng(0)
+for name in sys.argv[1:]:
+    kind, attrs, shapes = OPS[name]
+    ins = [be.put(Tensor(s, r.uniform(-1, 1, s))) for s in shapes]
+    for _ in range(3):
+        be.exec_op(kind, attrs, ins)
+    print(name, be.profile_op(kind, attrs, ins, reps=5))
+be.sync()
