@@ -230,7 +230,8 @@ class B200Backend:
 
     STAMP_KINDS = {0: "begin", 1: "elementwise", 2: "reduce", 3: "transpose", 4: "matmul", 5: "ptr-op",
                    6: "decide", 7: "feed-wait", 8: "feed-fill", 9: "fetch", 10: "commit-gate", 11: "commit",
-                   12: "end", 13: "fused"}
+                   12: "end", 13: "fused chain", 14: "im2col", 15: "col2im", 16: "bf16 cvt", 17: "colstats",
+                   18: "bn apply", 19: "split-K reduce"}
 
     def set_trace(self, capacity: int):
         """Enable device-side per-kernel stamps (0 disables)."""

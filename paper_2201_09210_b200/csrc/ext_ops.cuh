@@ -58,7 +58,7 @@ template <> __device__ __forceinline__ __nv_bfloat16 cvt_to<__nv_bfloat16>(doubl
 // of one (ky, kx) run are contiguous channels).  bf16 destinations store 8 per thread.
 template <typename Tin, typename Tout>
 __global__ void __launch_bounds__(256) k_im2col(Im2colParams p) {
-  stamp(p.ds, SK_FUSED);
+  stamp(p.ds, SK_IM2COL);
   if (skip(p.ds)) return;
   const Tin* x = res<Tin>(p.x);
   const long long M = p.N * p.Ho * p.Wo;
@@ -104,7 +104,7 @@ __global__ void __launch_bounds__(256) k_im2col(Im2colParams p) {
 // Vectorised bf16 im2col (C % 8 == 0): one thread = 8 consecutive channels of one
 // (pixel, ky, kx) = two float4 loads, one 16-byte store; 32-bit index arithmetic.
 __global__ void __launch_bounds__(256) k_im2col_bf16v(Im2colParams p) {
-  stamp(p.ds, SK_FUSED);
+  stamp(p.ds, SK_IM2COL);
   if (skip(p.ds)) return;
   const float* x = res<float>(p.x);
   const int C8 = (int)(p.C / 8), k = p.k, H = (int)p.H, W = (int)p.W, Ho = (int)p.Ho, Wo = (int)p.Wo;
@@ -137,7 +137,7 @@ __global__ void __launch_bounds__(256) k_im2col_bf16v(Im2colParams p) {
 // 64 m x 32 kk tiles; each thread loads float4 runs of channels (8 threads per pixel row)
 // and the tile is written back along pixels as bf16 pairs.
 __global__ void __launch_bounds__(256) k_im2col_bf16t(Im2colParams p) {
-  stamp(p.ds, SK_FUSED);
+  stamp(p.ds, SK_IM2COL);
   if (skip(p.ds)) return;
   const float* x = res<float>(p.x);
   __shared__ float tile[64][33];
@@ -182,7 +182,7 @@ __global__ void __launch_bounds__(256) k_im2col_bf16t(Im2colParams p) {
 // Scalar bf16 im2col for C % 8 != 0 (e.g. the 3-channel image layer): one thread = one
 // 8-element unit of a row, 32-bit index arithmetic.
 __global__ void __launch_bounds__(256) k_im2col_bf16s(Im2colParams p) {
-  stamp(p.ds, SK_FUSED);
+  stamp(p.ds, SK_IM2COL);
   if (skip(p.ds)) return;
   const float* x = res<float>(p.x);
   const int C = (int)p.C, k = p.k, H = (int)p.H, W = (int)p.W, Ho = (int)p.Ho, Wo = (int)p.Wo;
@@ -230,7 +230,7 @@ struct Col2imParams {
 
 template <typename Tc, typename T>
 __global__ void __launch_bounds__(256) k_col2im(Col2imParams p) {
-  stamp(p.ds, SK_FUSED);
+  stamp(p.ds, SK_COL2IM);
   if (skip(p.ds)) return;
   T* o = pick_out<T>(p.out, res<T>(p.a), res<T>(p.b));
   publish_early(p.out, o);
@@ -269,7 +269,7 @@ __global__ void __launch_bounds__(256) k_col2im(Col2imParams p) {
 // only the (ky, kx) taps congruent with the output position are visited, ascending.
 template <int V>
 __global__ void __launch_bounds__(256) k_col2im_v(Col2imParams p) {
-  stamp(p.ds, SK_FUSED);
+  stamp(p.ds, SK_COL2IM);
   if (skip(p.ds)) return;
   float* o = pick_out<float>(p.out, res<float>(p.a), res<float>(p.b));
   publish_early(p.out, o);
@@ -319,6 +319,7 @@ __global__ void __launch_bounds__(256) k_col2im_v(Col2imParams p) {
 // combines them in block order (deterministic) and finalises.
 enum ColMode { COL_SUM_ROWS = 0, COL_BN = 1, COL_BN_DX = 2, COL_BN_DGAMMA = 3 };
 constexpr int kColMaxSlots = 8;    // channels per thread (C <= 8 * 256)
+constexpr int kColReplicas = 8;    // atomic accumulators (spreads same-address contention)
 
 struct ColStatsParams {
   DevState* ds;
@@ -335,12 +336,12 @@ struct ColStatsParams {
 
 // V = channels per thread (4: float4 loads when C % 4 == 0 and T = float; else 1); rows
 // unrolled by 4 so each thread keeps several independent loads in flight.
-template <typename T, int V>
+template <typename T, int V, int S, bool DY>
 __global__ void __launch_bounds__(256) k_colstats(ColStatsParams p) {
-  stamp(p.ds, SK_REDUCE);
+  stamp(p.ds, SK_COLSTATS);
   if (skip(p.ds)) return;
   const T* x = res<T>(p.x);
-  const bool with_dy = p.mode == COL_BN_DX || p.mode == COL_BN_DGAMMA;
+  constexpr bool with_dy = DY;
   const T* dy = with_dy ? res<T>(p.dy) : nullptr;
   const bool final_out = p.mode == COL_SUM_ROWS || p.mode == COL_BN_DGAMMA;
   T* o = nullptr;
@@ -356,7 +357,6 @@ __global__ void __launch_bounds__(256) k_colstats(ColStatsParams p) {
   const int t = threadIdx.x, cc = t % L, rr = t / L;
   const int slots = (int)((CV + L - 1) / L);
   const long long r_begin = R * blockIdx.x / gridDim.x, r_end = R * (blockIdx.x + 1) / gridDim.x;
-  constexpr int S = kColMaxSlots / V > 0 ? kColMaxSlots / V : 1;
   double a1[S][V], a2[S][V], a3[S][V], a4[S][V], sh[S][V];
 #pragma unroll
   for (int j = 0; j < S; ++j)
@@ -430,8 +430,9 @@ __global__ void __launch_bounds__(256) k_colstats(ColStatsParams p) {
         double acc[4] = {0.0, 0.0, 0.0, 0.0};
         for (int q = 0; q < rpi; ++q)
           for (int u = 0; u < 4; ++u) acc[u] += sm[q * L + t][u];
-        if (p.atomic) {        // tolerance modes: fp64 atomics into the [C][4] accumulator
-          for (int u = 0; u < 4; ++u) atomicAdd(p.part + c * 4 + u, acc[u]);
+        if (p.atomic) {        // tolerance modes: fp64 atomics into one of kColReplicas [C][4] accumulators
+          double* dst = p.part + ((long long)(blockIdx.x % kColReplicas) * C + c) * 4;
+          for (int u = 0; u < 4; ++u) atomicAdd(dst + u, acc[u]);
         } else {               // parity mode: per-block partials merged in block order
           double* dst = p.part + ((long long)blockIdx.x * C + c) * 4;
           for (int u = 0; u < 4; ++u) dst[u] = acc[u];
@@ -440,20 +441,25 @@ __global__ void __launch_bounds__(256) k_colstats(ColStatsParams p) {
       __syncthreads();
     }
   }
-  // last block: combine partials (block order) and finalise
+  // last block: combine partials (block order) and finalise.  The CTA barrier orders every
+  // thread's partial writes before thread 0's cumulative gpu-scope fence and arrival.
   __shared__ unsigned int last;
-  __threadfence();
-  if (t == 0) last = (atomicAdd(p.counter, 1u) == gridDim.x - 1) ? 1u : 0u;
+  __syncthreads();
+  if (t == 0) {
+    __threadfence();
+    last = (atomicAdd(p.counter, 1u) == gridDim.x - 1) ? 1u : 0u;
+    if (last) __threadfence();
+  }
   __syncthreads();
   if (!last) return;
-  __threadfence();
   for (long long c = t; c < C; c += blockDim.x) {
     // four interleaved accumulators (fixed combination order: deterministic), L2 loads
     // (the partials were written by other blocks; this SM never cached them)
     double acc[4][4] = {{0.0}};
     const double2* q = (const double2*)(p.part + c * 4);
     const long long stride2 = 2 * C;                // two double2 per channel per block
-    const unsigned int nb = p.atomic ? 1u : gridDim.x;
+    const unsigned int nb = p.atomic ? (gridDim.x < (unsigned)kColReplicas ? gridDim.x : (unsigned)kColReplicas)
+                                     : gridDim.x;
     unsigned int b = 0;
     for (; b + 4 <= nb; b += 4) {
 #pragma unroll
@@ -466,10 +472,12 @@ __global__ void __launch_bounds__(256) k_colstats(ColStatsParams p) {
       const double2 u = __ldcg(q + (long long)b * stride2), v = __ldcg(q + (long long)b * stride2 + 1);
       acc[0][0] += u.x; acc[0][1] += u.y; acc[0][2] += v.x; acc[0][3] += v.y;
     }
-    if (p.atomic) {                                 // leave the accumulator zeroed for the next launch
-      double2* z = (double2*)(p.part + c * 4);
-      z[0] = make_double2(0.0, 0.0);
-      z[1] = make_double2(0.0, 0.0);
+    if (p.atomic) {                                 // leave the accumulators zeroed for the next launch
+      for (unsigned int r = 0; r < nb; ++r) {
+        double2* z = (double2*)(p.part + ((long long)r * C + c) * 4);
+        z[0] = make_double2(0.0, 0.0);
+        z[1] = make_double2(0.0, 0.0);
+      }
     }
     const double s1 = (acc[0][0] + acc[1][0]) + (acc[2][0] + acc[3][0]);
     const double s2 = (acc[0][1] + acc[1][1]) + (acc[2][1] + acc[3][1]);
@@ -515,7 +523,7 @@ struct BnApplyParams {
 
 template <typename T>
 __global__ void __launch_bounds__(256) k_bn_apply(BnApplyParams p) {
-  stamp(p.ds, SK_EW);
+  stamp(p.ds, SK_BNAPPLY);
   if (skip(p.ds)) return;
   const T* x = res<T>(p.x);
   const T* g = res<T>(p.g);
@@ -532,6 +540,57 @@ __global__ void __launch_bounds__(256) k_bn_apply(BnApplyParams p) {
     if (!p.dx) r = xhat * (double)g[c] + (double)z[c];
     else r = (((double)z[i] - st[2]) - xhat * st[3]) * ((double)g[c] * st[1]);
     o[i] = (T)r;
+  }
+  publish_late(p.out, o);
+}
+
+// Vectorised apply (float, C % 4 == 0): per-channel affine coefficients in shared memory,
+// one float4 per thread.  BATCHNORM: y = x*A + B;  BATCHNORM_DX: dx = dy*A + x*B + D with
+// A = g*rstd, B = -g*rstd^2*mean(dy*xhat), D = g*rstd*(rstd*mean*mean(dy*xhat) - mean(dy)).
+__global__ void __launch_bounds__(256) k_bn_apply_v4(BnApplyParams p) {
+  stamp(p.ds, SK_BNAPPLY);
+  if (skip(p.ds)) return;
+  extern __shared__ float coef[];                    // [3][C]
+  const float* x = res<float>(p.x);
+  const float* g = res<float>(p.g);
+  const float* z = res<float>(p.third);
+  float* o = pick_out<float>(p.out, x, g);
+  publish_early(p.out, o);
+  count_op(p.ds);
+  const int C = (int)p.C;
+  for (int c = threadIdx.x; c < C; c += blockDim.x) {
+    const double* st = p.stats + (long long)c * 4;
+    const double gr = (double)g[c] * st[1];
+    if (!p.dx) {
+      coef[c] = (float)gr;
+      coef[C + c] = (float)((double)z[c] - st[0] * gr);
+    } else {
+      coef[c] = (float)gr;
+      coef[C + c] = (float)(-gr * st[1] * st[3]);
+      coef[2 * C + c] = (float)(gr * (st[1] * st[0] * st[3] - st[2]));
+    }
+  }
+  __syncthreads();
+  const long long n4 = p.n / 4;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const int C4 = C / 4;
+  for (long long u = (long long)blockIdx.x * blockDim.x + threadIdx.x; u < n4; u += stride) {
+    const int c = (int)(u % C4) * 4;
+    const float4 xv = ((const float4*)x)[u];
+    float4 r;
+    if (!p.dx) {
+      r.x = fmaf(xv.x, coef[c], coef[C + c]);
+      r.y = fmaf(xv.y, coef[c + 1], coef[C + c + 1]);
+      r.z = fmaf(xv.z, coef[c + 2], coef[C + c + 2]);
+      r.w = fmaf(xv.w, coef[c + 3], coef[C + c + 3]);
+    } else {
+      const float4 gv = ((const float4*)z)[u];
+      r.x = fmaf(gv.x, coef[c], fmaf(xv.x, coef[C + c], coef[2 * C + c]));
+      r.y = fmaf(gv.y, coef[c + 1], fmaf(xv.y, coef[C + c + 1], coef[2 * C + c + 1]));
+      r.z = fmaf(gv.z, coef[c + 2], fmaf(xv.z, coef[C + c + 2], coef[2 * C + c + 2]));
+      r.w = fmaf(gv.w, coef[c + 3], fmaf(xv.w, coef[C + c + 3], coef[2 * C + c + 3]));
+    }
+    ((float4*)o)[u] = r;
   }
   publish_late(p.out, o);
 }

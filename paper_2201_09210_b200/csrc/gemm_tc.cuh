@@ -53,7 +53,7 @@ struct CvtParams {
 // (coalesced on both sides); transposed operands go through a 32x33 shared-memory
 // tile so both the strided read and the K-major write stay coalesced.
 __global__ void __launch_bounds__(256) k_cvt_bf16(CvtParams p) {
-  stamp(p.ds, SK_FUSED);
+  stamp(p.ds, SK_CVT);
   if (skip(p.ds)) return;
   // operand select without dynamic indexing of the parameter arrays (that would copy the
   // whole parameter block to local memory in every thread)
@@ -321,7 +321,7 @@ struct SplitReduceParams {
   Out out;
 };
 __global__ void __launch_bounds__(256) k_splitk_reduce(SplitReduceParams p) {
-  stamp(p.ds, SK_MATMUL);
+  stamp(p.ds, SK_SPLITK);
   if (skip(p.ds)) return;
   float* o = pick_out<float>(p.out, res<float>(p.a), p.b.cell || p.b.direct ? res<float>(p.b) : nullptr);
   publish_early(p.out, o);

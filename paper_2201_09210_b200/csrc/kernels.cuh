@@ -40,7 +40,8 @@ struct DevState {
 enum StampKind {
   SK_BEGIN = 0, SK_EW = 1, SK_REDUCE = 2, SK_TRANSPOSE = 3, SK_MATMUL = 4, SK_PTR = 5, SK_DECIDE = 6,
   SK_FEED_WAIT = 7, SK_FEED_FILL = 8, SK_FETCH = 9, SK_GATE = 10, SK_COMMIT = 11, SK_END = 12,
-  SK_AFTER_WAIT = 64, SK_FUSED = 13
+  SK_AFTER_WAIT = 64, SK_FUSED = 13, SK_IM2COL = 14, SK_COL2IM = 15, SK_CVT = 16, SK_COLSTATS = 17,
+  SK_BNAPPLY = 18, SK_SPLITK = 19
 };
 
 // Host <-> device rings in pinned, mapped host memory.

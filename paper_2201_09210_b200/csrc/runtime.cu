@@ -816,17 +816,21 @@ int build_xop_t(coex_ctx* c, const OpSpec& s, Launch* L, int* nL, size_t* ws_byt
       // merge of G x C partials stays small
       // tolerance modes accumulate with fp64 atomics (no merge of per-block partials)
       const bool atomic = !is_f64(c);
-      int64_t G = n / 8192;
+      int64_t G = n / 16384;
       if (!atomic && G > 32768 / C) G = 32768 / C;
-      if (G > kNumSMs * 4) G = kNumSMs * 4;
+      if (G > kNumSMs * 2) G = kNumSMs * 2;
       if (G > R) G = R;
       if (G < 1) G = 1;
       const bool v4 = !is_f64(c) && C % 4 == 0;
-      void* colfn = v4 ? (void*)k_colstats<float, 4> : (void*)k_colstats<T, 1>;
+      const bool dy = s.kind == COEX_BATCHNORM_DX || s.kind == COEX_BN_DGAMMA;
+      void* colfn;
+      if (v4 && C <= 1024) colfn = dy ? (void*)k_colstats<float, 4, 1, true> : (void*)k_colstats<float, 4, 1, false>;
+      else if (v4) colfn = dy ? (void*)k_colstats<float, 4, 2, true> : (void*)k_colstats<float, 4, 2, false>;
+      else colfn = dy ? (void*)k_colstats<T, 1, kColMaxSlots, true> : (void*)k_colstats<T, 1, kColMaxSlots, false>;
       ColStatsParams cp{};
       cp.ds = s.ds; cp.x = s.in[0]; cp.R = R; cp.C = C;
       cp.atomic = atomic ? 1 : 0;
-      cp.part = (double*)cv.take((size_t)(atomic ? 1 : G) * C * 4 * 8);
+      cp.part = (double*)cv.take((size_t)(atomic ? kColReplicas : G) * C * 4 * 8);
       cp.stats = (double*)cv.take((size_t)C * 4 * 8);
       cp.counter = (unsigned int*)cv.take(16);
       cp.a = s.in[0];
@@ -846,7 +850,12 @@ int build_xop_t(coex_ctx* c, const OpSpec& s, Launch* L, int* nL, size_t* ws_byt
       BnApplyParams ap{};
       ap.ds = s.ds; ap.x = s.in[0]; ap.g = s.in[1]; ap.third = s.in[2]; ap.stats = cp.stats;
       ap.n = n; ap.C = C; ap.dx = s.kind == COEX_BATCHNORM_DX; ap.out = s.out;
-      L[(*nL)++].set((void*)k_bn_apply<T>, grid_for(n), dim3(256), ap);
+      if (v4) {
+        L[*nL].set((void*)k_bn_apply_v4, grid_for(n / 4), dim3(256), ap);
+        L[(*nL)++].smem = (size_t)3 * C * sizeof(float);
+      } else {
+        L[(*nL)++].set((void*)k_bn_apply<T>, grid_for(n), dim3(256), ap);
+      }
       return COEX_OK;
     }
     default:
