@@ -28,12 +28,15 @@ constexpr int TC_BK = 64;          // 64 bf16 = 128 B = one SWIZZLE_128B row
 constexpr int TC_THREADS = 192;
 constexpr int TC_A_BYTES = TC_BM * TC_BK * 2;
 constexpr int TC_GROUP_M = 16;      // tile rasterisation: 16 M-tiles sweep N together (L2 reuse)
+constexpr int TC_EPI_LD = 36;       // epilogue staging row pitch (floats): 32 columns + 16-byte pad
+constexpr int TC_EPI_BYTES = 4 * 32 * TC_EPI_LD * 4;   // four epilogue warps x 32 rows
 // Narrow-N variants (convolution GEMMs have N = Cout in 64..512): BN in {64, 128, 256};
 // the stage count grows as the B tile shrinks so every variant keeps ~192 KB in flight.
 template <int BN> struct TcCfg {
   static constexpr int STAGES = BN == 256 ? 4 : BN == 128 ? 6 : 8;
   static constexpr int B_BYTES = BN * TC_BK * 2;
-  static constexpr int SMEM = STAGES * (TC_A_BYTES + B_BYTES) + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int SMEM = STAGES * (TC_A_BYTES + B_BYTES) + 1024 /*align*/ + 256 /*barriers, tmem slot*/ +
+                               TC_EPI_BYTES;
 };
 constexpr int TC_STAGES = TcCfg<TC_BN>::STAGES;
 constexpr int TC_B_BYTES = TcCfg<TC_BN>::B_BYTES;
@@ -156,16 +159,42 @@ __device__ __forceinline__ uint64_t smem_desc_k_sw128(const void* p) {
   return d;
 }
 
-// Instruction descriptor kind::f16: D=F32 (bit 4), A=BF16 (bits 7-9), B=BF16 (bits 10-12),
-// K-major A/B, N>>3 at [17,23), M>>4 at [24,29).
-__host__ __device__ constexpr uint32_t idesc_bf16_f32(int M, int N) {
-  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+// SMEM matrix descriptor, MN-major, SWIZZLE_128B: the tile is a stack of TMA boxes of 64
+// MN-elements x 64 K-rows (8 KB each, 128-B rows); canonical layout ((8,n),(8,k)) in 16-byte
+// units with LBO = 8192 B (next 64 MN-elements), SBO = 1024 B (next 8 K-rows).
+__device__ __forceinline__ uint64_t smem_desc_mn_sw128(const void* p) {
+  uint64_t d = 0;
+  d |= (uint64_t)((smem_u32(p) & 0x3FFFF) >> 4);
+  d |= (uint64_t)(8192 >> 4) << 16;
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
 }
 
-template <int BN>
+// Instruction descriptor kind::f16: D=F32 (bit 4), A=BF16 (bits 7-9), B=BF16 (bits 10-12),
+// K-major A/B, N>>3 at [17,23), M>>4 at [24,29).
+__host__ __device__ constexpr uint32_t idesc_bf16_f32(int M, int N, bool a_mn = false, bool b_mn = false) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(a_mn ? 1 : 0) << 15) | ((uint32_t)(b_mn ? 1 : 0) << 16) |
+         ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Persistent warp-specialised GEMM.  Work items = (output tile, K slice), strided over the
+// grid; three pipelines: the smem ring (TMA -> MMA, `full`/`empty`), two TMEM accumulator
+// buffers (MMA -> epilogue, `tfull`/`tempty`) so the epilogue of item i overlaps the MMAs of
+// item i+1, and the static round-robin item schedule shared by all roles.
+// A_MN / B_MN: operand stored MN-major in global memory ([K][M] / [K][N] rows, e.g. an
+// im2col matrix used as A^T) -- loaded as 64 x 64 boxes and consumed through MN-major
+// descriptors, so no transposition pass is needed.
+template <int BN, bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc(const __grid_constant__ TcGemmParams p) {
   constexpr int STAGES = TcCfg<BN>::STAGES;
   constexpr int B_BYTES = TcCfg<BN>::B_BYTES;
+  constexpr uint32_t TMEM_COLS = 2 * BN;            // two accumulator buffers
   stamp(p.ds, SK_MATMUL);
   if (skip(p.ds)) return;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -174,47 +203,53 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc(const __grid_constant
   unsigned char* sB = smem + STAGES * TC_A_BYTES;
   uint64_t* full = (uint64_t*)(sB + STAGES * B_BYTES);
   uint64_t* empty = full + STAGES;
-  uint64_t* tmem_full = empty + STAGES;
-  uint32_t* tmem_slot = (uint32_t*)(tmem_full + 1);
+  uint64_t* tfull = empty + STAGES;                 // [2]
+  uint64_t* tempty = tfull + 2;                     // [2]
+  uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const long long tiles_n = (p.N + BN - 1) / BN;
   const long long tiles_m = (p.M + TC_BM - 1) / TC_BM;
-  // grouped rasterisation: consecutive CTAs cover a TC_GROUP_M x tiles_n band
   const int splits = p.splits > 1 ? p.splits : 1;
-  const int split = (int)(blockIdx.x % splits);
-  const long long t = blockIdx.x / splits;
-  const long long group = (long long)TC_GROUP_M * tiles_n;
-  const long long first_m = (t / group) * TC_GROUP_M;
-  const long long gm = min((long long)TC_GROUP_M, tiles_m - first_m);
-  const int m0 = (int)((first_m + (t % group) % gm) * TC_BM);
-  const int n0 = (int)(((t % group) / gm) * BN);
+  const long long items = tiles_m * tiles_n * splits;
   const int nk_all = (int)((p.K + TC_BK - 1) / TC_BK);
-  const int kb0 = (int)((long long)nk_all * split / splits);
-  const int nk = (int)((long long)nk_all * (split + 1) / splits) - kb0;
+  const long long group = (long long)TC_GROUP_M * tiles_n;
 
-  float* C;
-  if (p.raw != nullptr) {
-    C = p.raw + (long long)split * p.M * p.N;
-  } else {
-    C = pick_out<float>(p.out, res<float>(p.a), res<float>(p.b));
-    publish_early(p.out, C);
+  // item -> (m0, n0, split, first k-block, k-block count); grouped rasterisation of tiles
+  auto decode = [&](long long it, int& m0, int& n0, int& split, int& kb0, int& nk) {
+    split = (int)(it % splits);
+    const long long t = it / splits;
+    const long long first_m = (t / group) * TC_GROUP_M;
+    const long long gm = min((long long)TC_GROUP_M, tiles_m - first_m);
+    m0 = (int)((first_m + (t % group) % gm) * TC_BM);
+    n0 = (int)(((t % group) / gm) * BN);
+    kb0 = (int)((long long)nk_all * split / splits);
+    nk = (int)((long long)nk_all * (split + 1) / splits) - kb0;
+  };
+
+  float* Cout = nullptr;
+  if (p.raw == nullptr) {
+    Cout = pick_out<float>(p.out, res<float>(p.a), res<float>(p.b));
+    publish_early(p.out, Cout);
   }
-  if (split == 0) count_op(p.ds);
+  count_op(p.ds);
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(tmem_full, 1);
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);                     // one arrival per epilogue warp
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&p.tmA) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&p.tmB) : "memory");
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(BN)
+                 "r"(TMEM_COLS)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
@@ -224,91 +259,152 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc(const __grid_constant
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
-    if (lane == 0) {
-      for (int kb = 0; kb < nk; ++kb) {
-        const int s = kb % STAGES;
-        const uint32_t ph = (uint32_t)((kb / STAGES) & 1);
-        mbar_wait(&empty[s], ph ^ 1u);
-        mbar_expect_tx(&full[s], TC_A_BYTES + B_BYTES);
-        tma_load_2d(sA + s * TC_A_BYTES, &p.tmA, &full[s], (kb0 + kb) * TC_BK, m0);
-        tma_load_2d(sB + s * B_BYTES, &p.tmB, &full[s], (kb0 + kb) * TC_BK, n0);
+    if (lane == 0) {                                // ===== TMA producer
+      long long kbg = 0;                            // k-blocks issued by this CTA (ring position)
+      for (long long it = blockIdx.x; it < items; it += gridDim.x) {
+        int m0, n0, split, kb0, nk;
+        decode(it, m0, n0, split, kb0, nk);
+        for (int kb = 0; kb < nk; ++kb, ++kbg) {
+          const int s = (int)(kbg % STAGES);
+          const uint32_t ph = (uint32_t)((kbg / STAGES) & 1);
+          mbar_wait(&empty[s], ph ^ 1u);
+          mbar_expect_tx(&full[s], TC_A_BYTES + B_BYTES);
+          if constexpr (A_MN) {
+#pragma unroll
+            for (int h = 0; h < TC_BM / 64; ++h)
+              tma_load_2d(sA + s * TC_A_BYTES + h * 8192, &p.tmA, &full[s], m0 + 64 * h, (kb0 + kb) * TC_BK);
+          } else {
+            tma_load_2d(sA + s * TC_A_BYTES, &p.tmA, &full[s], (kb0 + kb) * TC_BK, m0);
+          }
+          if constexpr (B_MN) {
+#pragma unroll
+            for (int h = 0; h < BN / 64; ++h)
+              tma_load_2d(sB + s * B_BYTES + h * 8192, &p.tmB, &full[s], n0 + 64 * h, (kb0 + kb) * TC_BK);
+          } else {
+            tma_load_2d(sB + s * B_BYTES, &p.tmB, &full[s], (kb0 + kb) * TC_BK, n0);
+          }
+        }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t idesc = idesc_bf16_f32(TC_BM, BN);
-      for (int kb = 0; kb < nk; ++kb) {
-        const int s = kb % STAGES;
-        const uint32_t ph = (uint32_t)((kb / STAGES) & 1);
-        mbar_wait(&full[s], ph);
+    if (lane == 0) {                                // ===== MMA issuer
+      constexpr uint32_t idesc = idesc_bf16_f32(TC_BM, BN, A_MN, B_MN);
+      long long kbg = 0;
+      int li = 0;                                   // local item index
+      for (long long it = blockIdx.x; it < items; it += gridDim.x, ++li) {
+        int m0, n0, split, kb0, nk;
+        decode(it, m0, n0, split, kb0, nk);
+        const int a = li & 1;
+        const uint32_t aph = (uint32_t)((li >> 1) & 1);
+        mbar_wait(&tempty[a], aph ^ 1u);            // epilogue drained this accumulator
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint64_t da = smem_desc_k_sw128(sA + s * TC_A_BYTES);
-        const uint64_t db = smem_desc_k_sw128(sB + s * B_BYTES);
+        const uint32_t acc_addr = tmem + (uint32_t)(a * BN);
+        for (int kb = 0; kb < nk; ++kb, ++kbg) {
+          const int s = (int)(kbg % STAGES);
+          const uint32_t ph = (uint32_t)((kbg / STAGES) & 1);
+          mbar_wait(&full[s], ph);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint64_t da = A_MN ? smem_desc_mn_sw128(sA + s * TC_A_BYTES) : smem_desc_k_sw128(sA + s * TC_A_BYTES);
+          const uint64_t db = B_MN ? smem_desc_mn_sw128(sB + s * B_BYTES) : smem_desc_k_sw128(sB + s * B_BYTES);
+          // one K=16 step: K-major advances 32 B inside the 128-B swizzle atom; MN-major
+          // advances two 8-row groups (2 x 1024 B)
+          constexpr uint64_t stepA = A_MN ? 128 : 2, stepB = B_MN ? 128 : 2;
 #pragma unroll
-        for (int k = 0; k < TC_BK / 16; ++k) {
-          const uint32_t acc = (kb > 0 || k > 0) ? 1u : 0u;
-          // advance 16 elements (32 B) along K inside the 128-B swizzle atom
-          asm volatile(
-              "{\n\t.reg .pred p;\n\t"
-              "setp.ne.b32 p, %4, 0;\n\t"
-              "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
-              "l"(da + (uint64_t)(2 * k)), "l"(db + (uint64_t)(2 * k)), "r"(idesc), "r"(acc)
-              : "memory");
+          for (int k = 0; k < TC_BK / 16; ++k) {
+            const uint32_t acc = (kb > 0 || k > 0) ? 1u : 0u;
+            asm volatile(
+                "{\n\t.reg .pred p;\n\t"
+                "setp.ne.b32 p, %4, 0;\n\t"
+                "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(acc_addr),
+                "l"(da + stepA * k), "l"(db + stepB * k), "r"(idesc), "r"(acc)
+                : "memory");
+          }
+          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                           smem_u32(&empty[s]))
+                       : "memory");
         }
-        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                         smem_u32(&empty[s]))
-                     : "memory");
+        if (nk > 0)
+          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                           smem_u32(&tfull[a]))
+                       : "memory");
+        else
+          mbar_arrive(&tfull[a]);                   // empty K slice: the epilogue writes zeros
       }
-      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                       smem_u32(tmem_full))
-                   : "memory");
     }
-  } else {
-    // epilogue: warps 2..5 own TMEM lanes 32*(warp%4) .. +31
-    const int lane_base = 32 * (warp % 4);
-    const int row = m0 + lane_base + lane;
-    if (nk > 0) {
-      mbar_wait(tmem_full, 0);
+  } else {                                          // ===== epilogue: warps 2..5
+    // TMEM -> registers -> per-warp smem transpose -> coalesced row-segment stores:
+    // each 32-column chunk of the warp's 32 rows leaves as 128-byte row segments.
+    const int lane_base = 32 * (warp % 4);          // TMEM lanes of this warp
+    float* stage = (float*)(tmem_slot + 4) + (warp - 2) * (32 * TC_EPI_LD);
+    const bool vec_ok = (p.N % 4) == 0;
+    int li = 0;
+    for (long long it = blockIdx.x; it < items; it += gridDim.x, ++li) {
+      int m0, n0, split, kb0, nk;
+      decode(it, m0, n0, split, kb0, nk);
+      const int a = li & 1;
+      const uint32_t aph = (uint32_t)((li >> 1) & 1);
+      float* C = p.raw != nullptr ? p.raw + (long long)split * p.M * p.N : Cout;
+      mbar_wait(&tfull[a], aph);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    }
 #pragma unroll 1
-    for (int c = 0; c < BN; c += 16) {
-      uint32_t r[16];
-      if (nk > 0) {
-        const uint32_t taddr = tmem + ((uint32_t)lane_base << 16) + (uint32_t)c;
-        asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-              "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-            : "r"(taddr));
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      } else {
-#pragma unroll
-        for (int i = 0; i < 16; ++i) r[i] = 0u;
-      }
-      if (row < p.M) {
-        float* dst = C + (long long)row * p.N + n0 + c;
-        const int valid = (int)min((long long)16, p.N - (n0 + c));
-        if (valid == 16 && (((uintptr_t)dst) & 15) == 0) {
-#pragma unroll
-          for (int i = 0; i < 16; i += 4)
-            *(float4*)(dst + i) = make_float4(__uint_as_float(r[i]), __uint_as_float(r[i + 1]),
-                                              __uint_as_float(r[i + 2]), __uint_as_float(r[i + 3]));
+      for (int c = 0; c < BN; c += 32) {
+        uint32_t r[32];
+        if (nk > 0) {
+          const uint32_t taddr = tmem + ((uint32_t)lane_base << 16) + (uint32_t)(a * BN + c);
+          asm volatile(
+              "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+              "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+              : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+                "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]),
+                "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]),
+                "=r"(r[30]), "=r"(r[31])
+              : "r"(taddr));
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         } else {
 #pragma unroll
-          for (int i = 0; i < 16; ++i)
-            if (i < valid) dst[i] = __uint_as_float(r[i]);
+          for (int i = 0; i < 32; ++i) r[i] = 0u;
         }
+        if (n0 + c >= p.N) break;                    // chunk entirely past the last column
+        float* srow = stage + lane * TC_EPI_LD;
+#pragma unroll
+        for (int i = 0; i < 32; i += 4)
+          *(float4*)(srow + i) = make_float4(__uint_as_float(r[i]), __uint_as_float(r[i + 1]),
+                                             __uint_as_float(r[i + 2]), __uint_as_float(r[i + 3]));
+        __syncwarp();
+        const int sub = lane >> 3, col = (lane & 7) * 4;   // 4 rows x 8 float4 per instruction
+        const long long gcol = (long long)n0 + c + col;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int rr = q * 4 + sub;
+          const long long grow = (long long)m0 + lane_base + rr;
+          if (grow < p.M && gcol < p.N) {
+            const float4 v = *(const float4*)(stage + rr * TC_EPI_LD + col);
+            float* dst = C + grow * p.N + gcol;
+            if (vec_ok && gcol + 4 <= p.N) {
+              *(float4*)dst = v;
+            } else {
+              dst[0] = v.x;
+              if (gcol + 1 < p.N) dst[1] = v.y;
+              if (gcol + 2 < p.N) dst[2] = v.z;
+              if (gcol + 3 < p.N) dst[3] = v.w;
+            }
+          }
+        }
+        __syncwarp();
       }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[a]);       // accumulator buffer free for item li + 2
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BN) : "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS) : "memory");
   }
-  if (p.raw == nullptr) publish_late(p.out, C);
+  if (p.raw == nullptr) publish_late(p.out, Cout);
 }
 
 // Split-K reduction: out[i] = sum of the S fp32 slices in slice order (deterministic).

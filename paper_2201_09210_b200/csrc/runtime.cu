@@ -468,6 +468,21 @@ void simt_matmul_launch(coex_ctx* c, const MatmulParams& p, Launch* L) {
   }
 }
 
+// bf16 [K rows][pitch(MN)] MN-major operand: box {64 MN, 64 K}, 128-byte swizzle, OOB -> 0.
+int make_tmap_mn(CUtensorMap* m, void* base, int64_t mn, int64_t K) {
+  auto enc = tmap_encoder();
+  if (!enc) return fail(COEX_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {(cuuint64_t)(mn > 0 ? mn : 1), (cuuint64_t)(K > 0 ? K : 1)};
+  cuuint64_t strides[1] = {(cuuint64_t)bf16_pitch(mn > 0 ? mn : 1) * 2};
+  cuuint32_t box[2] = {64, (cuuint32_t)TC_BK};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base, dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(COEX_CUDA_ERROR, "cuTensorMapEncodeTiled (MN) failed: " + std::to_string((int)r));
+  return COEX_OK;
+}
+
 template <typename T>
 int build_launch_t(coex_ctx* c, const OpSpec& s, Launch* L) {
   const int64_t n = numel_of(s.out_ndim, s.out_shape);
@@ -581,13 +596,17 @@ TcPlan tc_plan(int64_t M, int64_t N, int64_t K, bool allow_split) {
     const int64_t tiles = ((M + TC_BM - 1) / TC_BM) * ((N + bn - 1) / bn);
     const int64_t smax = allow_split ? (nk / 2 < 32 ? (nk / 2 > 1 ? nk / 2 : 1) : 32) : 1;
     for (int64_t sp = 1; sp <= smax; ++sp) {
-      const int64_t ctas = (tiles < 1 ? 1 : tiles) * sp;
-      const int64_t waves = (ctas + kNumSMs - 1) / kNumSMs;
+      // persistent CTAs: items per CTA run back to back, the epilogue of one item overlapping
+      // the MMAs of the next (two TMEM accumulators)
+      const int64_t items = (tiles < 1 ? 1 : tiles) * sp;
+      const int64_t rounds = (items + kNumSMs - 1) / kNumSMs;
       const double kper = (double)((nk + sp - 1) / sp);
       const double mma = kper * 2.0 * TC_BM * bn * TC_BK / 10.7e12;
       const double feed = kper * (double)(TC_BM + bn) * TC_BK * 2 / 135e9;
       const double epi = (double)TC_BM * bn * 4 / 44e9;
-      double t = waves * ((mma > feed ? mma : feed) + epi + 2e-6);
+      double body = mma > feed ? mma : feed;
+      if (epi > body) body = epi;
+      double t = rounds * body + epi + 2e-6;
       if (sp > 1) t += (double)(sp + 1) * M * N * 4 / 5.5e12 + 2e-6;
       if (t < best_t * 0.98) {
         best_t = t;
@@ -605,24 +624,34 @@ size_t matmul_split_ws(int64_t M, int64_t N, int64_t K) {
   return t.splits > 1 ? (size_t)t.splits * M * N * 4 : 0;
 }
 
+// Appends the GEMM (and its split-K reduction) to L.  `ws` = fp32 split slices (splits > 1).
 template <int BN>
-int tc_attr() {
-  static bool done = false;
-  if (!done) {
-    CK(cudaFuncSetAttribute((const void*)k_gemm_tc<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, TcCfg<BN>::SMEM));
-    done = true;
+int tc_attr3(bool amn, bool bmn) {
+  static bool done[4] = {false, false, false, false};
+  const int i = (amn ? 2 : 0) + (bmn ? 1 : 0);
+  if (!done[i]) {
+    const void* fn = amn ? (bmn ? (const void*)k_gemm_tc<BN, true, true> : (const void*)k_gemm_tc<BN, true, false>)
+                         : (bmn ? (const void*)k_gemm_tc<BN, false, true> : (const void*)k_gemm_tc<BN, false, false>);
+    CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, TcCfg<BN>::SMEM));
+    done[i] = true;
   }
   return COEX_OK;
 }
+template <int BN>
+void* tc_fn(bool amn, bool bmn) {
+  return amn ? (bmn ? (void*)k_gemm_tc<BN, true, true> : (void*)k_gemm_tc<BN, true, false>)
+             : (bmn ? (void*)k_gemm_tc<BN, false, true> : (void*)k_gemm_tc<BN, false, false>);
+}
 
-// Appends the GEMM (and its split-K reduction) to L.  `ws` = fp32 split slices (splits > 1).
+// a_mn / b_mn: operand stored MN-major ([K][pitch(M)] / [K][pitch(N)]) instead of K-major.
 int tc_gemm_launches(coex_ctx* c, DevState* ds, void* a16, void* b16, int64_t M, int64_t N, int64_t K,
-                     const TcPlan& t, In na, In nb, const Out& out, float* raw, float* ws, Launch* L, int* nL) {
+                     const TcPlan& t, In na, In nb, const Out& out, float* raw, float* ws, Launch* L, int* nL,
+                     bool a_mn = false, bool b_mn = false) {
   TcGemmParams gp;
   memset(&gp, 0, sizeof(gp));
-  int rc = make_tmap(&gp.tmA, a16, M, K, TC_BM);
+  int rc = a_mn ? make_tmap_mn(&gp.tmA, a16, M, K) : make_tmap(&gp.tmA, a16, M, K, TC_BM);
   if (rc) return rc;
-  rc = make_tmap(&gp.tmB, b16, N, K, t.bn);
+  rc = b_mn ? make_tmap_mn(&gp.tmB, b16, N, K) : make_tmap(&gp.tmB, b16, N, K, t.bn);
   if (rc) return rc;
   gp.ds = ds;
   gp.a = na;
@@ -634,10 +663,11 @@ int tc_gemm_launches(coex_ctx* c, DevState* ds, void* a16, void* b16, int64_t M,
   gp.splits = t.splits;
   gp.raw = t.splits > 1 ? ws : raw;
   Launch& G = L[(*nL)++];
-  void* fn = t.bn == 64 ? (void*)k_gemm_tc<64> : t.bn == 128 ? (void*)k_gemm_tc<128> : (void*)k_gemm_tc<256>;
-  G.set(fn, dim3((unsigned)(t.tiles * t.splits)), dim3(TC_THREADS), gp);
+  void* fn = t.bn == 64 ? tc_fn<64>(a_mn, b_mn) : t.bn == 128 ? tc_fn<128>(a_mn, b_mn) : tc_fn<256>(a_mn, b_mn);
+  const int64_t items = t.tiles * t.splits;
+  G.set(fn, dim3((unsigned)(items < kNumSMs ? items : kNumSMs)), dim3(TC_THREADS), gp);
   G.smem = t.bn == 64 ? TcCfg<64>::SMEM : t.bn == 128 ? TcCfg<128>::SMEM : TcCfg<256>::SMEM;
-  rc = t.bn == 64 ? tc_attr<64>() : t.bn == 128 ? tc_attr<128>() : tc_attr<256>();
+  rc = t.bn == 64 ? tc_attr3<64>(a_mn, b_mn) : t.bn == 128 ? tc_attr3<128>(a_mn, b_mn) : tc_attr3<256>(a_mn, b_mn);
   if (rc) return rc;
   if (t.splits > 1) {
     SplitReduceParams r{};
@@ -698,7 +728,7 @@ int build_xop_t(coex_ctx* c, const OpSpec& s, Launch* L, int* nL, size_t* ws_byt
       if (bf16) {
         const TcPlan t = tc_plan(M, F, Kc, true);
         void* A = cv.take((size_t)M * bf16_pitch(Kc) * 2);
-        void* B = cv.take((size_t)F * bf16_pitch(Kc) * 2);
+        void* B = cv.take((size_t)Kc * bf16_pitch(F) * 2);       // w as stored: [Kc][F], MN-major B
         float* ws = t.splits > 1 ? (float*)cv.take((size_t)t.splits * M * F * 4) : nullptr;
         if (!build) break;
         ip.dst = A; ip.ld = bf16_pitch(Kc); ip.trans = 0;
@@ -709,11 +739,12 @@ int build_xop_t(coex_ctx* c, const OpSpec& s, Launch* L, int* nL, size_t* ws_byt
         else
           L[(*nL)++].set((void*)k_im2col<float, __nv_bfloat16>, grid_for(M * ip.ld / 8), dim3(256), ip);
         CvtParams q{};
-        q.ds = s.ds; q.src[0] = s.in[1]; q.rows[0] = F; q.K = Kc; q.ld = bf16_pitch(Kc); q.trans[0] = 1;
+        q.ds = s.ds; q.src[0] = s.in[1]; q.rows[0] = Kc; q.K = F; q.ld = bf16_pitch(F); q.trans[0] = 0;
         q.dst[0] = (__nv_bfloat16*)B;
-        const int64_t tiles = ((F + 31) / 32) * ((q.ld + 31) / 32);
-        L[(*nL)++].set((void*)k_cvt_bf16, dim3((unsigned)(tiles < kNumSMs * 16 ? tiles : kNumSMs * 16), 1), dim3(256), q);
-        return tc_gemm_launches(c, s.ds, A, B, M, F, Kc, t, s.in[0], s.in[1], s.out, nullptr, ws, L, nL);
+        const int64_t gx = (Kc * q.ld / 8 + 255) / 256;
+        L[(*nL)++].set((void*)k_cvt_bf16, dim3((unsigned)(gx < kNumSMs * 16 ? (gx < 1 ? 1 : gx) : kNumSMs * 16), 1),
+                       dim3(256), q);
+        return tc_gemm_launches(c, s.ds, A, B, M, F, Kc, t, s.in[0], s.in[1], s.out, nullptr, ws, L, nL, false, true);
       }
       void* A = cv.take((size_t)M * Kc * es);
       if (!build) break;
@@ -776,27 +807,28 @@ int build_xop_t(coex_ctx* c, const OpSpec& s, Launch* L, int* nL, size_t* ws_byt
       ip.N = N; ip.H = H; ip.W = W; ip.C = C; ip.Ho = Ho; ip.Wo = Wo;
       ip.k = (int)k; ip.s = (int)st; ip.p = (int)pd;
       if (bf16) {
+        // dW = im2col(x)^T . dy with both operands MN-major: A = im2col(x) [P][pitch(Kc)],
+        // B = dy [P][pitch(F)] in bf16 -- no transposition pass
         const TcPlan t = tc_plan(Kc, F, P, true);
-        void* A = cv.take((size_t)Kc * bf16_pitch(P) * 2);
-        void* B = cv.take((size_t)F * bf16_pitch(P) * 2);
+        void* A = cv.take((size_t)P * bf16_pitch(Kc) * 2);
+        void* B = cv.take((size_t)P * bf16_pitch(F) * 2);
         float* ws = t.splits > 1 ? (float*)cv.take((size_t)t.splits * Kc * F * 4) : nullptr;
         if (!build) break;
-        ip.dst = A; ip.ld = bf16_pitch(P); ip.trans = 1;
-        if (P < (1ll << 31) && C % 4 == 0) {
-          const int64_t tiles = ((ip.ld + 63) / 64) * ((Kc + 31) / 32);
-          L[(*nL)++].set((void*)k_im2col_bf16t, dim3((unsigned)(tiles < kNumSMs * 16 ? tiles : kNumSMs * 16)),
-                         dim3(256), ip);
-        } else {
-          const int64_t tiles = ((ip.ld + 31) / 32) * ((Kc + 31) / 32);
-          L[(*nL)++].set((void*)k_im2col<float, __nv_bfloat16>,
-                         dim3((unsigned)(tiles < kNumSMs * 16 ? tiles : kNumSMs * 16)), dim3(256), ip);
-        }
+        ip.dst = A; ip.ld = bf16_pitch(Kc); ip.trans = 0;
+        if (C % 8 == 0 && P < (1ll << 31))
+          L[(*nL)++].set((void*)k_im2col_bf16v, grid_for(P * Kc / 8), dim3(256), ip);
+        else if (P < (1ll << 31))
+          L[(*nL)++].set((void*)k_im2col_bf16s, grid_for(P * ip.ld / 8), dim3(256), ip);
+        else
+          L[(*nL)++].set((void*)k_im2col<float, __nv_bfloat16>, grid_for(P * ip.ld / 8), dim3(256), ip);
         CvtParams q{};
-        q.ds = s.ds; q.src[0] = s.in[1]; q.rows[0] = F; q.K = P; q.ld = bf16_pitch(P); q.trans[0] = 1;
+        q.ds = s.ds; q.src[0] = s.in[1]; q.rows[0] = P; q.K = F; q.ld = bf16_pitch(F); q.trans[0] = 0;
         q.dst[0] = (__nv_bfloat16*)B;
-        const int64_t ct = ((F + 31) / 32) * ((q.ld + 31) / 32);
-        L[(*nL)++].set((void*)k_cvt_bf16, dim3((unsigned)(ct < kNumSMs * 16 ? ct : kNumSMs * 16), 1), dim3(256), q);
-        return tc_gemm_launches(c, s.ds, A, B, Kc, F, P, t, s.in[0], s.in[1], s.out, nullptr, ws, L, nL);
+        const int64_t units = P * q.ld / 8;
+        const int64_t gx = (units + 255) / 256;
+        L[(*nL)++].set((void*)k_cvt_bf16, dim3((unsigned)(gx < kNumSMs * 16 ? (gx < 1 ? 1 : gx) : kNumSMs * 16), 1),
+                       dim3(256), q);
+        return tc_gemm_launches(c, s.ds, A, B, Kc, F, P, t, s.in[0], s.in[1], s.out, nullptr, ws, L, nL, true, true);
       }
       void* A = cv.take((size_t)P * Kc * es);
       if (!build) break;
