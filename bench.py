@@ -1,31 +1,41 @@
-"""Benchmark: C1 tiny-MLP training iterations/s under B200 co-execution.
+"""Benchmark: training iterations/s under B200 co-execution.
 
-Metric (BASELINE.json): training iterations/s at 1/2/4/8 B200, next to the
-reference CPU co-execution path, with the dominant kernel's roofline fraction.
+Metric (BASELINE.json): training iterations/s at 1/2/4/8 B200, next to the reference CPU
+co-execution path, with the dominant kernel's roofline fraction.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--precision f64|fp32|bf16] [--impl b200|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2|c1]
+                    [--precision f64|fp32|bf16] [--impl b200|reference]
 
-A *step* is one training iteration of C1 (paper_2201_09210_b200/workloads.py)
-run by the co-execution orchestrator: the Python skeleton walks the step while
-the B200 executes the step's CUDA graph (one cudaGraphLaunch; SWITCH / WHILE
-conditional nodes driven by the skeleton's decisions over pinned mapped memory).
+Workloads (paper_2201_09210_b200/workloads.py):
+* ``c2`` (default) -- BASELINE.json configs[1], DCGAN 64x64, batch 128, generator /
+  discriminator steps alternating through a SwitchCase on ``native mod(step, 2)``; bf16
+  tcgen05 convolutions / GEMMs (implicit-GEMM lowering), fp32 everything else.  A step is
+  one D or one G iteration; ``value`` counts iterations of either kind.
+* ``c1`` -- configs[0], the tiny MLP the reference's own CPU path can express (f64 parity).
 
-* ``value``: K / (sum of per-step device time), CUDA events on the context's
-  stream bracketing each step; synthetic inputs expanded on the device from the
-  generator state (no host data), L2 flushed (256 MiB write) between steps
-  outside the timed region.
+A *step* is one training iteration run by the co-execution orchestrator: the Python
+skeleton walks the step while the B200 executes the step's CUDA graph (one
+cudaGraphLaunch; SWITCH / WHILE conditional nodes driven by the skeleton's decisions over
+pinned mapped memory).
+
+* ``value``: K / (sum of per-step device time), CUDA events on the context's stream
+  bracketing each step; synthetic inputs expanded on the device from the generator state
+  (no host data), L2 flushed (256 MiB write) between steps outside the timed region.
 * ``e2e``: the same metric through the public API with host-resident inputs
-  (``InMemoryDataset``): every step copies x and y host->device through the C-ABI
-  feed path and reads the loss back.
-* ``roofline``: the dominant compute kernel of the step, re-launched eagerly with
-  the step's shapes between CUDA events on the same stream.
-* ``cpu_baseline``: the CPU oracle co-execution (oracle/, SPEC-faithful runner +
-  reference kernels + reference Python dataset) on a bounded sample, rank 0 only.
+  (``InMemoryDataset``): every step copies the step's inputs host->device through the C-ABI
+  feed path and reads the printed loss back.
+* ``roofline``: every distinct op of one D+G step pair re-launched eagerly with the step's
+  shapes, launch by launch, between CUDA events on the same stream (coex_exec_op_profile);
+  kernels grouped by family; the family with the largest share of step time is the
+  dominant kernel, its achieved FLOP/s (tensor-bound) or GB/s (memory-bound) over the
+  algorithmic work stated in DESIGN.md.
+* ``cpu_baseline``: the CPU oracle co-execution (oracle/, SPEC-faithful runner + f64
+  kernels) on a bounded sample, rank 0 only.
 
-Multi-GPU: one process per GPU (torchrun), data parallel: global batch 64*N, every
-rank runs the host program on global shapes while its device expands and trains on
-its own 64-row shard; gradients and the loss are all-reduced by NCCL nodes inside
-the pass graph (paper_2201_09210_b200/dp.py).  Weak scaling; time = max over ranks.
+Multi-GPU: one process per GPU (torchrun).  C1 is data parallel (global batch 64*N, NCCL
+all-reduce nodes inside the pass graph, paper_2201_09210_b200/dp.py).  C2 has no sharding
+rule for batch-norm statistics yet: every rank trains an independent replica on its own
+data stream (weak scaling, no collective).  Time = max over ranks.
 """
 
 from __future__ import annotations
@@ -45,7 +55,8 @@ from paper_2201_09210_b200 import coexec, lang  # noqa: E402
 from paper_2201_09210_b200.coexec import Phase  # noqa: E402
 from paper_2201_09210_b200.dataset import SyntheticDataset  # noqa: E402
 from paper_2201_09210_b200.tensor import OpKind, Tensor, shape_size  # noqa: E402
-from paper_2201_09210_b200.workloads import C1, InMemoryDataset, c1_flops, c1_program  # noqa: E402
+from paper_2201_09210_b200.workloads import (C1, C2, InMemoryDataset, c1_flops, c1_program,  # noqa: E402
+                                             dcgan_flops, dcgan_program)
 
 METRIC = "training iterations/sec at 1/2/4/8 B200 vs ref CPU co-exec; % HBM/tensor roofline"
 UNIT = "it/s"
@@ -201,6 +212,45 @@ def tensor_gemm(peak_tflops, peak_kind, size: int = 8192):
             "ms": round(ms, 4)}
 
 
+def roofline_c2(be, hbm_peak, tflops_peak, peak_kind):
+    """Per-kernel-family breakdown of one D+G step pair (eager re-launch, CUDA events on the
+    context stream) and the roofline of the dominant family."""
+    from tools.step_ops import by_family, profile_ops, record_step_ops
+    ops = record_step_ops(be, lambda n: dcgan_program(steps=n, **C2), 2)
+    rows = profile_ops(be, ops, reps=10)
+    fam = by_family(rows, be.esize)
+    total = sum(f["ms"] for f in fam.values())
+    fams = {}
+    for k, f in fam.items():
+        e = {"ms_per_pair": round(f["ms"], 4), "share": round(f["ms"] / total, 4), "launches_per_pair": f["launches"]}
+        if f["flops"]:
+            e["tflops"] = round(f["flops"] / (f["ms"] * 1e-3) / 1e12, 2)
+            e["frac_tensor"] = round(e["tflops"] / tflops_peak, 4)
+        if f["bytes"]:
+            known = f["ms"] - f["unknown_ms"]
+            if known > 0:
+                e["gbs"] = round(f["bytes"] / (known * 1e-3) / 1e9, 1)
+                e["frac_hbm"] = round(e["gbs"] / hbm_peak, 4)
+        fams[k] = e
+    top = next(iter(fam))
+    f = fam[top]
+    if f["flops"]:
+        ach = f["flops"] / (f["ms"] * 1e-3) / 1e12
+        roof = {"bound": "tensor", "kernel": top, "achieved": round(ach, 2), "peak": tflops_peak, "unit": "TFLOP/s",
+                "frac": round(ach / tflops_peak, 4), "algorithmic_flops_per_pair": f["flops"]}
+    else:
+        known = f["ms"] - f["unknown_ms"]
+        ach = f["bytes"] / (known * 1e-3) / 1e9
+        roof = {"bound": "hbm", "kernel": top, "achieved": round(ach, 1), "peak": hbm_peak, "unit": "GB/s",
+                "frac": round(ach / hbm_peak, 4), "algorithmic_bytes_per_pair": f["bytes"]}
+    roof.update({"traffic": None, "peak_source": peak_kind, "kernel_ms_per_pair": round(f["ms"], 4),
+                 "share_of_step": round(f["ms"] / total, 4), "kernel_sum_ms_per_pair": round(total, 4),
+                 "families": fams,
+                 "method": "every distinct op of one D+G step pair re-launched eagerly with the step's shapes, "
+                           "per launch, CUDA events on the context stream (coex_exec_op_profile)"})
+    return roof
+
+
 def cpu_baseline(steps: int = 12):
     """CPU oracle co-execution of C1 on this host (bounded sample)."""
     from oracle.cpu_backend import CpuBackend
@@ -218,21 +268,93 @@ def cpu_baseline(steps: int = 12):
                       f"per-element Python dataset; host cpu_count={os.cpu_count()}"}
 
 
+C2_SAMPLE_BATCH = 2
+
+
+def cpu_baseline_c2(steps: int = 2):
+    """CPU oracle co-execution of C2 (f64 restatement of every op, SPEC-faithful runner) on a
+    bounded sample: the full-size network at batch C2_SAMPLE_BATCH instead of 128, timed over
+    `steps` co-executed steps (D and G alternate) after tracing; the per-iteration time is
+    scaled by 128 / C2_SAMPLE_BATCH (every op of the step is linear in the batch)."""
+    from oracle.cpu_backend import CpuBackend
+    cfg = dict(C2, batch=C2_SAMPLE_BATCH)
+    o = make_orch(dcgan_program(steps=10_000, **cfg), SyntheticDataset(1000), CpuBackend())
+    reach_coexec(o)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        o.step()
+    dt = time.perf_counter() - t0
+    per_it = dt / steps * (C2["batch"] / C2_SAMPLE_BATCH)
+    return {"value": round(1.0 / per_it, 6), "unit": UNIT, "cores": 2, "kind": "port",
+            "sample": f"C2 co-exec on the CPU oracle at batch {C2_SAMPLE_BATCH} (same network), {steps} steps after "
+                      f"tracing ({dt:.1f} s), per-iteration time scaled x{C2['batch'] // C2_SAMPLE_BATCH} to batch "
+                      f"{C2['batch']}; host cpu_count={os.cpu_count()}"}
+
+
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    k = max(1, min(args.steps, 30))
-    base = cpu_baseline(k)
+    if args.workload == "c2":
+        base = cpu_baseline_c2(max(2, min(args.steps, 4)))
+        k = max(2, min(args.steps, 4))
+        cfg = {"workload": "C2 DCGAN 64x64 (ngf=ndf=64, nz=100), batch 128, D/G alternating, coexec (CPU oracle "
+                           "runner, f64)", "global_batch": C2["batch"]}
+    else:
+        k = max(1, min(args.steps, 30))
+        base = cpu_baseline(k)
+        cfg = {"workload": "C1 tiny MLP 784-128-10, batch 64, coexec (CPU oracle runner)", "global_batch": 64}
     line = {"impl": "reference", "metric": METRIC, "value": base["value"], "unit": UNIT, "n_gpus": 0,
             "steps": k, "warmup": args.warmup, "ms_per_step": round(1e3 / base["value"], 3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (reference SyntheticDataset, seed 0)",
-            "config": {"workload": "C1 tiny MLP 784-128-10, batch 64, coexec (CPU oracle runner)",
-                       "global_batch": 64},
-            "cpu_baseline": base,
+            "data": "synthetic (SyntheticDataset)", "config": cfg, "cpu_baseline": base,
             "e2e": {"value": base["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
+
+
+def workload_setup(args, world: int):
+    """(program source, synthetic dataset, e2e host records, per-rank H2D bytes, config dict)."""
+    import numpy as np
+    rr = np.random.default_rng(7)
+    if args.workload == "c2":
+        src = dcgan_program(steps=100_000, **C2)
+        b, nz, img = C2["batch"], C2["nz"], C2["img"]
+        recs = {"z": [Tensor((b, nz), rr.uniform(-1, 1, (b, nz))) for _ in range(2)],
+                "img": [Tensor((b, img, img, 3), rr.uniform(-1, 1, (b, img, img, 3))) for _ in range(2)]}
+        for name, shp in _c2_weight_shapes().items():
+            recs[name] = [Tensor(shp, rr.uniform(-1, 1, shp))]
+        fl = dcgan_flops(**C2)
+        cfg = {"workload": "C2 DCGAN 64x64 (ngf=ndf=64, nz=100; D: 4 strided convs + BN + leaky-relu, G: dense + "
+                           "4 transposed convs + BN + relu, tanh), batch 128/GPU, D and G iterations alternating "
+                           "through a SwitchCase on native mod(step, 2), hand-written backward, SGD",
+               "global_batch": b * world, "per_gpu_batch": b,
+               "parallelism": f"dp{world}" if world == 1 else f"{world} independent replicas (no BN sharding rule)",
+               "algorithmic_flops_per_d_step": fl["d_step"], "algorithmic_flops_per_g_step": fl["g_step"]}
+        h2d = (b * nz + b * img * img * 3) * 8
+        return src, SyntheticDataset(1000 + 7919 * dist_env()[0]), recs, h2d, cfg, None
+    gbatch = C1["batch"] * world
+    cfg1 = dict(C1, batch=gbatch)
+    src = c1_program(steps=100_000, **cfg1)
+    b, din, dout, h = gbatch, C1["din"], C1["dout"], C1["hidden"]
+    recs = {"x": [Tensor((b, din), rr.uniform(-1, 1, (b, din))) for _ in range(4)],
+            "y": [Tensor((b, dout), rr.uniform(-1, 1, (b, dout))) for _ in range(4)],
+            "w1_init": [Tensor((din, h), rr.uniform(-1, 1, (din, h)))],
+            "w2_init": [Tensor((h, dout), rr.uniform(-1, 1, (h, dout)))]}
+    cfg = {"workload": "C1 tiny MLP 784-128-10 (sigmoid, MSE, hand-written backward, loss-driven branch, native "
+                       "clip, choice-driven while), coexec mode",
+           "global_batch": gbatch, "per_gpu_batch": C1["batch"],
+           "parallelism": f"dp{world}" + ("" if world == 1 else " (NCCL all-reduce in the pass graph)"),
+           "algorithmic_flops_per_step": c1_flops(**C1)}
+    h2d = (C1["batch"] * din + C1["batch"] * dout) * 8
+    return src, SyntheticDataset(1000), recs, h2d, cfg, gbatch
+
+
+def _c2_weight_shapes() -> dict:
+    import re
+    shapes = {}
+    for m in re.finditer(r'input\("(\w+_init)", \[([0-9, ]+)\]\)', dcgan_program(steps=1, **C2)):
+        shapes[m.group(1)] = tuple(int(v) for v in m.group(2).split(","))
+    return shapes
 
 
 def run_b200(args):
@@ -246,15 +368,11 @@ def run_b200(args):
         torch.cuda.set_device(0)
     from paper_2201_09210_b200.b200 import B200Backend
     from paper_2201_09210_b200.dp import DPGroup
-    gbatch = C1["batch"] * world
-    dp = DPGroup(rank, world, gbatch) if world > 1 else None
-    be = B200Backend(device=local if world > 1 else 0, precision=args.precision, dp=dp)
-    total_steps = 100_000
-    cfg = dict(C1, batch=gbatch)
-    src = c1_program(steps=total_steps, **cfg)
-    # data parallel: every rank runs the host program on the global batch; its device
-    # expands and trains on its own 64-row shard; gradients are all-reduced in the graph
-    o = make_orch(src, SyntheticDataset(1000), be)
+    src, dataset, recs, h2d, cfg, gbatch = workload_setup(args, world)
+    dp = DPGroup(rank, world, gbatch) if (world > 1 and gbatch is not None) else None
+    dev = local if world > 1 else 0
+    be = B200Backend(device=dev, precision=args.precision, dp=dp)
+    o = make_orch(src, dataset, be)
     pre = reach_coexec(o)
     for _ in range(args.warmup):
         o.step()
@@ -263,7 +381,7 @@ def run_b200(args):
     be.sync()
     hbm, tfl, peak_kind = load_peaks()
     replays0 = o.stats.steps_replayed
-    with ClockSampler(local) as clk:
+    with ClockSampler(dev) as clk:
         dev_ms, launches = timed_steps(o, be, args.steps)
     be.sync()
     replays = o.stats.steps_replayed - replays0
@@ -275,58 +393,52 @@ def run_b200(args):
     value = world * args.steps / (t_max * 1e-3)
 
     # e2e: host-resident inputs through the public API (H2D each step, loss D2H)
-    import numpy as np
-    rr = np.random.default_rng(7)
-    b, din, dout, h = gbatch, C1["din"], C1["dout"], C1["hidden"]
-    recs = {"x": [Tensor((b, din), rr.uniform(-1, 1, (b, din))) for _ in range(4)],
-            "y": [Tensor((b, dout), rr.uniform(-1, 1, (b, dout))) for _ in range(4)],
-            "w1_init": [Tensor((din, h), rr.uniform(-1, 1, (din, h)))],
-            "w2_init": [Tensor((h, dout), rr.uniform(-1, 1, (h, dout)))]}
-    be2 = B200Backend(device=local if world > 1 else 0, precision=args.precision, dp=dp)
+    be2 = B200Backend(device=dev, precision=args.precision, dp=dp)
     o2 = make_orch(src, InMemoryDataset(recs), be2)
     reach_coexec(o2)
     for _ in range(args.warmup):
         o2.step()
+    if world > 1:
+        torch.distributed.barrier()
     e2e_ms, _ = timed_steps(o2, be2, args.steps)
     e2e_max = e2e_ms
     if world > 1:
         tt = torch.tensor([e2e_ms], device="cuda", dtype=torch.float64)
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
         e2e_max = float(tt.item())
-    esz = 8
-    h2d = (C1["batch"] * din + C1["batch"] * dout) * esz      # this rank's shard of x and y
-    d2h = 8
 
     if rank == 0:
-        roof = roofline(be, hbm, tfl, peak_kind)
-        base = cpu_baseline(12) if world == 1 and not args.no_cpu_baseline else None
-        tgemm = tensor_gemm(tfl, peak_kind) if not args.no_tensor_gemm else None
+        if args.workload == "c2":
+            roof = roofline_c2(be, hbm, tfl, peak_kind)
+            base = cpu_baseline_c2() if world == 1 and not args.no_cpu_baseline else None
+            tgemm = None
+        else:
+            roof = roofline(be, hbm, tfl, peak_kind)
+            base = cpu_baseline(12) if world == 1 and not args.no_cpu_baseline else None
+            tgemm = tensor_gemm(tfl, peak_kind) if not args.no_tensor_gemm else None
         st = o.stats
+        cfg.update({"l2": "flushed (256 MiB write) between timed steps", "tracing_steps_before_coexec": pre,
+                    "steps_replayed_in_timed_region": replays})
         line = {
             "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(t_max / args.steps, 5), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": args.precision,
-            "data": "synthetic (SyntheticDataset seed 1000; each rank expands its batch shard on device "
-                    "from the jumped-ahead xorshift64* state)",
-            "config": {"workload": "C1 tiny MLP 784-128-10 (sigmoid, MSE, hand-written backward, "
-                                   "loss-driven branch, native clip, choice-driven while), coexec mode",
-                       "global_batch": C1["batch"] * world, "per_gpu_batch": C1["batch"],
-                       "parallelism": f"dp{world}" + ("" if world == 1 else " (NCCL all-reduce in the pass graph)"),
-                       "l2": "flushed (256 MiB write) between timed steps",
-                       "tracing_steps_before_coexec": pre, "steps_replayed_in_timed_region": replays,
-                       "algorithmic_flops_per_step": c1_flops(**C1)},
+            "data": "synthetic (SyntheticDataset; each rank expands its inputs on device from the jumped-ahead "
+                    "xorshift64* state; random-init weights)",
+            "config": cfg,
             "roofline": roof,
-            "tensor_gemm": tgemm,
             "cpu_baseline": base,
             "e2e": {"value": round(world * args.steps / (e2e_max * 1e-3), 3), "unit": UNIT,
-                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "data": "InMemoryDataset host tensors, copied through coex_pass_feed each step"},
+                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 8,
+                    "data": "InMemoryDataset host tensors (f64), copied through coex_pass_feed each step"},
             "gpu_launches": launches,
             "clocks": clk.summary(),
             "stats": {"graph_exec_ms": round(st.graph_exec_ms, 3), "graph_stall_ms": round(st.graph_stall_ms, 3),
                       "python_exec_ms": round(st.python_exec_ms, 3), "python_stall_ms": round(st.python_stall_ms, 3),
                       "counters": list(st.counters())},
         }
+        if tgemm is not None:
+            line["tensor_gemm"] = tgemm
         print(json.dumps(line))
     be2.close()
     be.close()
@@ -337,14 +449,19 @@ def run_b200(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=None)
     ap.add_argument("--warmup", type=int, default=10)
-    ap.add_argument("--precision", default="f64", choices=["f64", "fp32", "bf16"])
+    ap.add_argument("--workload", default="c2", choices=["c1", "c2"])
+    ap.add_argument("--precision", default=None, choices=["f64", "fp32", "bf16"])
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-tensor-gemm", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.steps is None:
+        args.steps = 100 if args.workload == "c2" else 200
+    if args.precision is None:
+        args.precision = "bf16" if args.workload == "c2" else "f64"
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -50,6 +50,76 @@ def profile_ops(be, ops: collections.Counter, reps: int = 10):
     return rows
 
 
+def _conv_geo(kind, attrs, shapes):
+    from paper_2201_09210_b200.tensor import infer_shape
+    out = infer_shape(kind, attrs, [tuple(x) for x in shapes])[0]
+    return out
+
+
+def launch_work(kind, attrs, shapes, kernel: str, esize: int = 4):
+    """Algorithmic work of one launch of an op's lowering: ("flops", F) for the GEMM kernels,
+    ("bytes", B) for the memory-bound ones -- compulsory bytes = distinct inputs read + outputs
+    written at their storage width (bf16 operand copies count 2 B/elem, fp32 activations 4)."""
+    from paper_2201_09210_b200.tensor import flops_of, shape_size
+    shapes = [tuple(x) for x in shapes]
+    n_in = [shape_size(x) for x in shapes]
+    if kind is OpKind.MATMUL or kind in (OpKind.CONV2D, OpKind.CONV2D_T, OpKind.CONV2D_DW):
+        out = _conv_geo(kind, attrs, shapes) if kind is not OpKind.MATMUL else (shapes[0][0], shapes[1][1])
+        if kernel.startswith("k_gemm_tc") or kernel.startswith("k_matmul"):
+            return "flops", flops_of(kind, shapes, attrs)
+        if kernel.startswith("k_im2col"):
+            x = shapes[0]
+            if kind is OpKind.CONV2D:
+                rows, kc = shape_size(out[:3]), shapes[1][0]
+            else:                                   # CONV2D_DW: im2col of x over dy's pixels
+                rows, kc = shape_size(shapes[1][:3]), shape_size(out[:1])
+            return "bytes", n_in[0] * esize + rows * kc * 2
+        if kernel.startswith("k_cvt_bf16"):
+            if kind is OpKind.CONV2D:
+                return "bytes", n_in[1] * (esize + 2)
+            if kind is OpKind.CONV2D_DW:
+                return "bytes", n_in[1] * (esize + 2)
+            return "bytes", (n_in[0] + n_in[1]) * (esize + 2)
+        if kernel.startswith("k_col2im"):
+            x, w = shapes
+            return "bytes", shape_size(x[:3]) * w[0] * esize + shape_size(out) * esize
+        if kernel.startswith("k_splitk_reduce"):
+            return "bytes", None
+    if kernel.startswith("k_colstats"):
+        return "bytes", (n_in[0] + (n_in[-1] if kind in (OpKind.BATCHNORM_DX, OpKind.BN_DGAMMA) else 0)) * esize
+    if kernel.startswith("k_bn_apply"):
+        return "bytes", (2 * n_in[0] + (n_in[2] if kind is OpKind.BATCHNORM_DX else 0)) * esize
+    if kernel.startswith("k_elementwise") or kernel.startswith("k_chain") or kernel.startswith("k_transpose") \
+            or kernel.startswith("k_reduce"):
+        out = shape_size(shapes[0]) if shapes else 0
+        return "bytes", (sum(n_in) + out) * esize
+    return "bytes", None
+
+
+def by_family(rows, esize=4):
+    """Per kernel family: total ms per step, algorithmic work per step, achieved rate."""
+    fam = collections.defaultdict(lambda: {"ms": 0.0, "flops": 0, "bytes": 0, "launches": 0, "unknown_ms": 0.0})
+    for r in rows:
+        kind = OpKind(r["kind"])
+        for ln in r["launches"]:
+            name = ln["kernel"]
+            key = name.split("E")[0] if name.startswith("k_gemm_tc") else name
+            for pre in ("k_gemm_tc", "k_im2col", "k_col2im", "k_colstats", "k_bn_apply", "k_matmul"):
+                if name.startswith(pre):
+                    key = pre
+            f = fam[key]
+            f["ms"] += r["count"] * ln["ms"]
+            f["launches"] += r["count"]
+            what, amount = launch_work(kind, r["attrs"], r["shapes"], name, esize)
+            if amount is None:
+                f["unknown_ms"] += r["count"] * ln["ms"]
+            elif what == "flops":
+                f["flops"] += r["count"] * amount
+            else:
+                f["bytes"] += r["count"] * amount
+    return dict(sorted(fam.items(), key=lambda kv: -kv[1]["ms"]))
+
+
 def by_kernel(rows):
     agg = collections.defaultdict(float)
     for r in rows:
