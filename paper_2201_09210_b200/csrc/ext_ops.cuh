@@ -332,6 +332,8 @@ struct ColStatsParams {
   unsigned int* counter;     // zero-initialised; reset by the last block
   In a, b;                   // node operands (ping-pong output choice only)
   Out out;                   // [C] result (COL_SUM_ROWS, COL_BN_DGAMMA)
+  int extra;                 // COL_BN_DX fused backward: also write dgamma / dbeta [C]
+  Out out_g, out_b;
 };
 
 // V = channels per thread (4: float4 loads when C % 4 == 0 and T = float; else 1); rows
@@ -497,6 +499,12 @@ __global__ void __launch_bounds__(256) k_colstats(ColStatsParams p) {
       o[c] = (T)sdx;
       continue;
     }
+    if (p.extra) {                                  // fused backward: dgamma = sum(dy*xhat), dbeta = sum(dy)
+      T* og = pick_out<T>(p.out_g, x, dy);
+      T* ob = pick_out<T>(p.out_b, x, dy);
+      og[c] = (T)sdx;
+      ob[c] = (T)d1;
+    }
     double* st = p.stats + c * 4;
     st[0] = mean;
     st[1] = rstd;
@@ -504,6 +512,15 @@ __global__ void __launch_bounds__(256) k_colstats(ColStatsParams p) {
     st[3] = sdx / (double)R;
   }
   if (t == 0) *p.counter = 0u;
+  if (p.extra) {
+    __syncthreads();
+    if (t == 0) {                                   // the finishing block publishes both
+      T* og = pick_out<T>(p.out_g, x, dy);
+      T* ob = pick_out<T>(p.out_b, x, dy);
+      for (int i = 0; i < p.out_g.npub; ++i) *p.out_g.pub[i] = og;
+      for (int i = 0; i < p.out_b.npub; ++i) *p.out_b.pub[i] = ob;
+    }
+  }
   if (final_out) {
     __syncthreads();
     if (t == 0 && p.out.late != nullptr)   // single finishing block publishes

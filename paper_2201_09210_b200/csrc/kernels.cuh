@@ -248,6 +248,26 @@ __global__ void __launch_bounds__(256) k_elementwise(EwParams p) {
   const long long stride = (long long)gridDim.x * blockDim.x;
   const T as = p.a_scalar ? a[0] : T(0);
   const T bs = (b != nullptr && p.b_scalar) ? b[0] : T(0);
+  if constexpr (sizeof(T) == 4) {
+    // float4 path: four independent elements per thread (same per-element rounding)
+    const bool va = p.a_scalar || (((uintptr_t)a & 15) == 0);
+    const bool vb = b == nullptr || p.b_scalar || (((uintptr_t)b & 15) == 0);
+    if ((n & 3) == 0 && va && vb && (((uintptr_t)o & 15) == 0)) {
+      for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n / 4; i += stride) {
+        const float4 x4 = p.a_scalar ? make_float4(as, as, as, as) : ((const float4*)a)[i];
+        float4 y4 = make_float4(bs, bs, bs, bs);
+        if (b != nullptr && !p.b_scalar) y4 = ((const float4*)b)[i];
+        float4 r;
+        r.x = ew_apply(p.op, x4.x, y4.x);
+        r.y = ew_apply(p.op, x4.y, y4.y);
+        r.z = ew_apply(p.op, x4.z, y4.z);
+        r.w = ew_apply(p.op, x4.w, y4.w);
+        ((float4*)o)[i] = r;
+      }
+      publish_late(p.out, o);
+      return;
+    }
+  }
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
     T x = p.a_scalar ? as : a[i];
     T y = (b == nullptr) ? T(0) : (p.b_scalar ? bs : b[i]);

@@ -369,10 +369,14 @@ struct OpSpec {
   void* scratch[2] = {nullptr, nullptr};   // bf16 K-major operand copies (tcgen05 path)
   char* ws = nullptr;                      // extension ops: workspace base (nullptr = size query)
   Out out{};
+  Out out2{}, out3{};                      // fused batch-norm backward: dgamma, dbeta
   DevState* ds = nullptr;
 };
 
-bool is_ext_compute(int kind) { return kind >= COEX_CONV2D && kind <= COEX_SUM_ROWS; }
+// Plan-only kind: batchnorm_dx + bn_dgamma + sum_rows over the same (x, dy) fused into one
+// column-statistics pass (planner.py _bn_bwd_groups); three outputs dx, dgamma, dbeta.
+constexpr int kBnBwdFused = 100;
+bool is_ext_compute(int kind) { return (kind >= COEX_CONV2D && kind <= COEX_SUM_ROWS) || kind == kBnBwdFused; }
 int ew_code(int kind) {
   switch (kind) {
     case COEX_ADD: return EW_ADD;
@@ -499,7 +503,7 @@ int build_launch_t(coex_ctx* c, const OpSpec& s, Launch* L) {
       p.b_scalar = binary && s.in_ndim[1] == 0 && n != 1;
       p.n = n;
       p.out = s.out;
-      L->set((void*)k_elementwise<T>, grid_for(n), dim3(256), p);
+      L->set((void*)k_elementwise<T>, grid_for(sizeof(T) == 4 && n % 4 == 0 ? n / 4 : n), dim3(256), p);
       return COEX_OK;
     }
     case COEX_SUM: case COEX_MEAN: {
@@ -840,7 +844,7 @@ int build_xop_t(coex_ctx* c, const OpSpec& s, Launch* L, int* nL, size_t* ws_byt
       simt_matmul_launch<T>(c, mp, &L[(*nL)++]);
       return COEX_OK;
     }
-    case COEX_BATCHNORM: case COEX_BATCHNORM_DX: case COEX_BN_DGAMMA: case COEX_SUM_ROWS: {
+    case COEX_BATCHNORM: case COEX_BATCHNORM_DX: case COEX_BN_DGAMMA: case COEX_SUM_ROWS: case kBnBwdFused: {
       const int64_t C = s.in_shape[0][s.in_ndim[0] - 1];
       const int64_t n = numel_of(s.in_ndim[0], s.in_shape[0]);
       const int64_t R = n / C;
@@ -854,7 +858,7 @@ int build_xop_t(coex_ctx* c, const OpSpec& s, Launch* L, int* nL, size_t* ws_byt
       if (G > R) G = R;
       if (G < 1) G = 1;
       const bool v4 = !is_f64(c) && C % 4 == 0;
-      const bool dy = s.kind == COEX_BATCHNORM_DX || s.kind == COEX_BN_DGAMMA;
+      const bool dy = s.kind == COEX_BATCHNORM_DX || s.kind == COEX_BN_DGAMMA || s.kind == kBnBwdFused;
       void* colfn;
       if (v4 && C <= 1024) colfn = dy ? (void*)k_colstats<float, 4, 1, true> : (void*)k_colstats<float, 4, 1, false>;
       else if (v4) colfn = dy ? (void*)k_colstats<float, 4, 2, true> : (void*)k_colstats<float, 4, 2, false>;
@@ -876,12 +880,17 @@ int build_xop_t(coex_ctx* c, const OpSpec& s, Launch* L, int* nL, size_t* ws_byt
         return COEX_OK;
       }
       cp.mode = s.kind == COEX_BATCHNORM ? COL_BN : COL_BN_DX;
-      if (s.kind == COEX_BATCHNORM_DX) cp.dy = s.in[2];
+      if (s.kind == COEX_BATCHNORM_DX || s.kind == kBnBwdFused) cp.dy = s.in[2];
       cp.out = Out{};
+      if (s.kind == kBnBwdFused) {
+        cp.extra = 1;
+        cp.out_g = s.out2;
+        cp.out_b = s.out3;
+      }
       L[(*nL)++].set(colfn, dim3((unsigned)G), dim3(256), cp);
       BnApplyParams ap{};
       ap.ds = s.ds; ap.x = s.in[0]; ap.g = s.in[1]; ap.third = s.in[2]; ap.stats = cp.stats;
-      ap.n = n; ap.C = C; ap.dx = s.kind == COEX_BATCHNORM_DX; ap.out = s.out;
+      ap.n = n; ap.C = C; ap.dx = s.kind != COEX_BATCHNORM; ap.out = s.out;
       if (v4) {
         L[*nL].set((void*)k_bn_apply_v4, grid_for(n / 4), dim3(256), ap);
         L[(*nL)++].smem = (size_t)3 * C * sizeof(float);
@@ -1678,6 +1687,10 @@ struct Builder {
         int64_t vbits = next();
         memcpy(&s.value, &vbits, 8);
         read_out(s.out);
+        if (s.kind == kBnBwdFused) {
+          read_out(s.out2);
+          read_out(s.out3);
+        }
         Launch L[kMaxLaunches];
         int nL = 0;
         size_t wb = 0;

@@ -44,6 +44,7 @@ EW_CODE = {OpKind.ADD: 0, OpKind.SUB: 1, OpKind.MUL: 2, OpKind.NEG: 3, OpKind.RE
            OpKind.BCE_TERM: 11}
 COMPUTE = {OpKind.MATMUL, OpKind.SUM, OpKind.MEAN, OpKind.TRANSPOSE} | set(EW_CODE) | XOP
 MAX_XIN = 3
+XOP_BN_BWD = 100          # fused batchnorm_dx + bn_dgamma + sum_rows (csrc COEX_BN_BWD_FUSED)
 CHAIN_IN, CHAIN_OPS, CHAIN_OUT, CHAIN_PUB, CHAIN_REGS = 8, 16, 8, 4, 16
 
 
@@ -294,11 +295,19 @@ class Planner:
 
         def emit(insts) -> list:
             items = []
+            bn_groups, bn_skip = self._bn_bwd_groups(insts) if self.fuse else ({}, set())
             if self.fuse:
                 segs = self._segments(insts, shapes, folded)
             else:
                 segs = [("inst", x) for x in insts]
             for kind_, seg in segs:
+                if kind_ == "inst" and isinstance(seg, ExecOp):
+                    if seg.node_id in bn_skip:
+                        continue
+                    if seg.node_id in bn_groups:
+                        items.append(self._bn_bwd_word(bn_groups[seg.node_id], shapes, in_cell, out_words, pubs,
+                                                       n_compute))
+                        continue
                 if kind_ == "chain":
                     run, feeds = seg
                     for f in feeds:
@@ -424,6 +433,76 @@ class Planner:
             word += [-1, -1]
         word += out_words(nid, late)
         return [word]
+
+    def _bn_bwd_groups(self, insts):
+        """Batch-norm backward triples in one instruction list -- batchnorm_dx(x, g, dy),
+        bn_dgamma(x, dy), sum_rows(dy) with identical x / dy bindings -- run as ONE column-
+        statistics pass (all three need sum(dy) and sum(dy * xhat)).  The fused op sits at the
+        position of the last member; legal when nothing in between consumes an earlier member's
+        output or re-produces an input, and no member is fetched / merged / pinned."""
+        groups, skip = {}, set()
+        pos = {}
+        for i, x in enumerate(insts):
+            if isinstance(x, ExecOp):
+                pos.setdefault(x.node_id, i)
+        multi_nodes = {n for s_ in self._multi_sets() for n in s_}
+        dxs = [x for x in insts if isinstance(x, ExecOp) and x.kind is OpKind.BATCHNORM_DX]
+        used = set()
+        for d in dxs:
+            xb, gb, dyb = d.inputs
+            if xb.fed or dyb.fed:
+                continue
+            g = next((y for y in insts if isinstance(y, ExecOp) and y.kind is OpKind.BN_DGAMMA
+                      and y.node_id not in used and y.inputs[0] == xb and y.inputs[1] == dyb), None)
+            sr = next((y for y in insts if isinstance(y, ExecOp) and y.kind is OpKind.SUM_ROWS
+                       and y.node_id not in used and y.inputs[0] == dyb), None)
+            if g is None or sr is None:
+                continue
+            mem = [d, g, sr]
+            ids = {m.node_id for m in mem}
+            if any(n in self.sp.fetch_nodes or n in multi_nodes or n in self.force_store for n in ids):
+                continue
+            lo = min(pos[m.node_id] for m in mem)
+            hi = max(pos[m.node_id] for m in mem)
+            ok = True
+            for i in range(lo, hi + 1):
+                y = insts[i]
+                if isinstance(y, ExecOp) and y.node_id in ids:
+                    continue
+                if not isinstance(y, (ExecOp, InputFeed)):
+                    ok = False
+                    break
+                if any((not b.fed) and (set(b.cands) & ids) for b in y.inputs):
+                    ok = False                      # consumes a member's output before the fused op
+                    break
+                # re-producing an input of a member that already ran (e.g. its gamma ReadVar
+                # is fine for the last member, which the fused op replaces in place)
+                if any(pos[m.node_id] < i and any((not b.fed) and y.node_id in b.cands for b in m.inputs)
+                       for m in mem):
+                    ok = False
+                    break
+            if not ok:
+                continue
+            last = insts[hi]
+            groups[last.node_id] = (d, g, sr)
+            skip |= ids - {last.node_id}
+            used |= ids
+        return groups, skip
+
+    def _bn_bwd_word(self, grp, shapes, in_cell, out_words, pubs, n_compute) -> list:
+        d, g, sr = grp
+        cells = [in_cell(b) for b in d.inputs]
+        in_shapes = [self._in_shape(b, shapes) for b in d.inputs]
+        late = _conflicts(cells, pubs[d.node_id] + pubs[g.node_id] + pubs[sr.node_id])
+        n_compute[0] += 1
+        out_shape = shapes[d.node_id]
+        word = [T_XOP, XOP_BN_BWD, d.node_id, 3] + cells
+        for s_ in in_shapes:
+            word += [len(s_)] + _pad(s_)
+        word += [len(out_shape)] + _pad(out_shape)
+        word += [0] + _pad([]) + [_f64_bits(0.0)]
+        word += out_words(d.node_id, late) + out_words(g.node_id, late) + out_words(sr.node_id, late)
+        return word
 
     def _xop_word(self, x, shapes, in_cell, out_words, pubs, n_compute, flops) -> list:
         nid = x.node_id
