@@ -58,6 +58,7 @@ template <> __device__ __forceinline__ __nv_bfloat16 cvt_to<__nv_bfloat16>(doubl
 // of one (ky, kx) run are contiguous channels).  bf16 destinations store 8 per thread.
 template <typename Tin, typename Tout>
 __global__ void __launch_bounds__(256) k_im2col(Im2colParams p) {
+  COEX_PDL_ENTER();
   stamp(p.ds, SK_IM2COL);
   if (skip(p.ds)) return;
   const Tin* x = res<Tin>(p.x);
@@ -102,34 +103,50 @@ __global__ void __launch_bounds__(256) k_im2col(Im2colParams p) {
 }
 
 // Vectorised bf16 im2col (C % 8 == 0): one thread = 8 consecutive channels of one
-// (pixel, ky, kx) = two float4 loads, one 16-byte store; 32-bit index arithmetic.
+// (pixel, ky, kx) = two float4 loads, one 16-byte store.  Each block owns a contiguous range
+// of output pixels; a thread keeps its (ky, kx, channel-group) fixed and walks pixels with
+// incremental (n, oy, ox) arithmetic -- no divisions in the loop.
 __global__ void __launch_bounds__(256) k_im2col_bf16v(Im2colParams p) {
+  COEX_PDL_ENTER();
   stamp(p.ds, SK_IM2COL);
   if (skip(p.ds)) return;
   const float* x = res<float>(p.x);
   const int C8 = (int)(p.C / 8), k = p.k, H = (int)p.H, W = (int)p.W, Ho = (int)p.Ho, Wo = (int)p.Wo;
-  const int Q = k * k * C8;                       // 16-byte units per row (ld == Kc)
+  const int Q = k * k * C8;                         // 16-byte units per row (ld == Kc)
   const long long M = p.N * p.Ho * p.Wo;
-  const long long total = M * Q;
-  const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long u = (long long)blockIdx.x * blockDim.x + threadIdx.x; u < total; u += stride) {
-    const unsigned m = (unsigned)(u / Q);          // host guarantees M < 2^31
-    const int q = (int)(u - (long long)m * Q);
+  const int t = threadIdx.x;
+  const int rpi = Q >= 256 ? 1 : 256 / Q;           // rows per block iteration
+  const int qpt = (Q + 255) / 256;                  // units per thread and row
+  const int lane_q = Q >= 256 ? t : t % Q, lane_r = Q >= 256 ? 0 : t / Q;
+  if (lane_r >= rpi) return;
+  const long long r_begin = M * blockIdx.x / gridDim.x, r_end = M * (blockIdx.x + 1) / gridDim.x;
+  for (int qi = 0; qi < qpt; ++qi) {
+    const int q = lane_q + qi * 256;
+    if (q >= Q) break;
     const int ky = q / (k * C8), r2 = q - ky * k * C8, kx = r2 / C8, cg = r2 - kx * C8;
-    const int ox = (int)(m % (unsigned)Wo);
-    const unsigned t = m / (unsigned)Wo;
-    const int oy = (int)(t % (unsigned)Ho);
-    const long long n = t / (unsigned)Ho;
-    const int iy = oy * p.s - p.p + ky, ix = ox * p.s - p.p + kx;
-    uint4 out = make_uint4(0u, 0u, 0u, 0u);
-    if (iy >= 0 && iy < H && ix >= 0 && ix < W) {
-      const float4* src = (const float4*)(x + ((n * H + iy) * W + ix) * p.C + cg * 8);
-      const float4 a = src[0], b = src[1];
-      __nv_bfloat162 v0 = __floats2bfloat162_rn(a.x, a.y), v1 = __floats2bfloat162_rn(a.z, a.w);
-      __nv_bfloat162 v2 = __floats2bfloat162_rn(b.x, b.y), v3 = __floats2bfloat162_rn(b.z, b.w);
-      out.x = *(uint32_t*)&v0; out.y = *(uint32_t*)&v1; out.z = *(uint32_t*)&v2; out.w = *(uint32_t*)&v3;
+    long long m = r_begin + lane_r;
+    if (m >= r_end) continue;
+    int ox = (int)(m % Wo);
+    long long tq = m / Wo;
+    int oy = (int)(tq % Ho);
+    long long n = tq / Ho;
+    for (; m < r_end; m += rpi) {
+      const int iy = oy * p.s - p.p + ky, ix = ox * p.s - p.p + kx;
+      uint4 out = make_uint4(0u, 0u, 0u, 0u);
+      if (iy >= 0 && iy < H && ix >= 0 && ix < W) {
+        const float4* src = (const float4*)(x + ((n * H + iy) * W + ix) * p.C + cg * 8);
+        const float4 a = __ldg(src), b = __ldg(src + 1);
+        __nv_bfloat162 v0 = __floats2bfloat162_rn(a.x, a.y), v1 = __floats2bfloat162_rn(a.z, a.w);
+        __nv_bfloat162 v2 = __floats2bfloat162_rn(b.x, b.y), v3 = __floats2bfloat162_rn(b.z, b.w);
+        out.x = *(uint32_t*)&v0; out.y = *(uint32_t*)&v1; out.z = *(uint32_t*)&v2; out.w = *(uint32_t*)&v3;
+      }
+      *(uint4*)((__nv_bfloat16*)p.dst + m * p.ld + (long long)q * 8) = out;
+      ox += rpi;
+      while (ox >= Wo) {
+        ox -= Wo;
+        if (++oy == Ho) { oy = 0; ++n; }
+      }
     }
-    *(uint4*)((__nv_bfloat16*)p.dst + (long long)m * p.ld + (long long)q * 8) = out;
   }
 }
 
@@ -137,6 +154,7 @@ __global__ void __launch_bounds__(256) k_im2col_bf16v(Im2colParams p) {
 // 64 m x 32 kk tiles; each thread loads float4 runs of channels (8 threads per pixel row)
 // and the tile is written back along pixels as bf16 pairs.
 __global__ void __launch_bounds__(256) k_im2col_bf16t(Im2colParams p) {
+  COEX_PDL_ENTER();
   stamp(p.ds, SK_IM2COL);
   if (skip(p.ds)) return;
   const float* x = res<float>(p.x);
@@ -182,6 +200,7 @@ __global__ void __launch_bounds__(256) k_im2col_bf16t(Im2colParams p) {
 // Scalar bf16 im2col for C % 8 != 0 (e.g. the 3-channel image layer): one thread = one
 // 8-element unit of a row, 32-bit index arithmetic.
 __global__ void __launch_bounds__(256) k_im2col_bf16s(Im2colParams p) {
+  COEX_PDL_ENTER();
   stamp(p.ds, SK_IM2COL);
   if (skip(p.ds)) return;
   const float* x = res<float>(p.x);
@@ -230,6 +249,7 @@ struct Col2imParams {
 
 template <typename Tc, typename T>
 __global__ void __launch_bounds__(256) k_col2im(Col2imParams p) {
+  COEX_PDL_ENTER();
   stamp(p.ds, SK_COL2IM);
   if (skip(p.ds)) return;
   T* o = pick_out<T>(p.out, res<T>(p.a), res<T>(p.b));
@@ -266,9 +286,12 @@ __global__ void __launch_bounds__(256) k_col2im(Col2imParams p) {
 }
 
 // Vectorised col2im (F % V == 0, V = 4 or 1): one thread = V channels of one output pixel;
-// only the (ky, kx) taps congruent with the output position are visited, ascending.
+// only the (ky, kx) taps congruent with the output position are visited, ascending.  Blocks
+// own contiguous pixel ranges; threads keep their channel group and walk pixels
+// incrementally (no divisions in the loop).
 template <int V>
 __global__ void __launch_bounds__(256) k_col2im_v(Col2imParams p) {
+  COEX_PDL_ENTER();
   stamp(p.ds, SK_COL2IM);
   if (skip(p.ds)) return;
   float* o = pick_out<float>(p.out, res<float>(p.a), res<float>(p.b));
@@ -278,36 +301,52 @@ __global__ void __launch_bounds__(256) k_col2im_v(Col2imParams p) {
   const int F4 = (int)(p.F / V), k = p.k, s = p.s, pd = p.p, H = (int)p.H, W = (int)p.W;
   const int Ho = (int)p.Ho, Wo = (int)p.Wo;
   const long long kkF = (long long)k * k * p.F;
-  const long long total = p.N * p.Ho * p.Wo * F4;
-  const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long u = (long long)blockIdx.x * blockDim.x + threadIdx.x; u < total; u += stride) {
-    const unsigned pix = (unsigned)(u / F4);        // host guarantees N*Ho*Wo < 2^31
-    const int f4 = (int)(u - (long long)pix * F4);
-    const int ox = (int)(pix % (unsigned)Wo);
-    const unsigned r = pix / (unsigned)Wo;
-    const int oy = (int)(r % (unsigned)Ho);
-    const long long n = r / (unsigned)Ho;
-    float acc[V];
+  const long long P = p.N * p.Ho * p.Wo;
+  const int t = threadIdx.x;
+  const int rpi = F4 >= 256 ? 1 : 256 / F4;
+  const int fpt = (F4 + 255) / 256;
+  const int lane_f = F4 >= 256 ? t : t % F4, lane_r = F4 >= 256 ? 0 : t / F4;
+  if (lane_r < rpi) {
+    const long long r_begin = P * blockIdx.x / gridDim.x, r_end = P * (blockIdx.x + 1) / gridDim.x;
+    for (int fi = 0; fi < fpt; ++fi) {
+      const int f4 = lane_f + fi * 256;
+      if (f4 >= F4) break;
+      long long pix = r_begin + lane_r;
+      if (pix >= r_end) continue;
+      int ox = (int)(pix % Wo);
+      long long tq = pix / Wo;
+      int oy = (int)(tq % Ho);
+      long long n = tq / Ho;
+      for (; pix < r_end; pix += rpi) {
+        float acc[V];
 #pragma unroll
-    for (int v = 0; v < V; ++v) acc[v] = 0.f;
-    for (int ky = (oy + pd) % s; ky < k; ky += s) {
-      const int iy = (oy + pd - ky) / s;
-      if (oy + pd - ky < 0 || iy >= H) continue;
-      for (int kx = (ox + pd) % s; kx < k; kx += s) {
-        const int ix = (ox + pd - kx) / s;
-        if (ox + pd - kx < 0 || ix >= W) continue;
-        const float* src = cols + ((n * H + iy) * W + ix) * kkF + ((long long)ky * k + kx) * p.F + f4 * V;
-        if constexpr (V == 4) {
-          const float4 v = *(const float4*)src;
-          acc[0] = __fadd_rn(acc[0], v.x); acc[1] = __fadd_rn(acc[1], v.y);
-          acc[2] = __fadd_rn(acc[2], v.z); acc[3] = __fadd_rn(acc[3], v.w);
-        } else {
-          acc[0] = __fadd_rn(acc[0], src[0]);
+        for (int v = 0; v < V; ++v) acc[v] = 0.f;
+        const int ty0 = oy + pd, tx0 = ox + pd;
+        for (int ky = ty0 % s; ky < k; ky += s) {
+          const int iy = (ty0 - ky) / s;
+          if (ty0 - ky < 0 || iy >= H) continue;
+          for (int kx = tx0 % s; kx < k; kx += s) {
+            const int ix = (tx0 - kx) / s;
+            if (tx0 - kx < 0 || ix >= W) continue;
+            const float* src = cols + ((n * H + iy) * W + ix) * kkF + ((long long)ky * k + kx) * p.F + f4 * V;
+            if constexpr (V == 4) {
+              const float4 v = __ldg((const float4*)src);
+              acc[0] = __fadd_rn(acc[0], v.x); acc[1] = __fadd_rn(acc[1], v.y);
+              acc[2] = __fadd_rn(acc[2], v.z); acc[3] = __fadd_rn(acc[3], v.w);
+            } else {
+              acc[0] = __fadd_rn(acc[0], __ldg(src));
+            }
+          }
+        }
+        if constexpr (V == 4) *(float4*)(o + pix * p.F + f4 * 4) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+        else o[pix * p.F + f4] = acc[0];
+        ox += rpi;
+        while (ox >= Wo) {
+          ox -= Wo;
+          if (++oy == Ho) { oy = 0; ++n; }
         }
       }
     }
-    if constexpr (V == 4) *(float4*)(o + (long long)pix * p.F + f4 * 4) = make_float4(acc[0], acc[1], acc[2], acc[3]);
-    else o[(long long)pix * p.F + f4] = acc[0];
   }
   publish_late(p.out, o);
 }
@@ -340,6 +379,7 @@ struct ColStatsParams {
 // unrolled by 4 so each thread keeps several independent loads in flight.
 template <typename T, int V, int S, bool DY>
 __global__ void __launch_bounds__(256) k_colstats(ColStatsParams p) {
+  COEX_PDL_ENTER();
   stamp(p.ds, SK_COLSTATS);
   if (skip(p.ds)) return;
   const T* x = res<T>(p.x);
@@ -540,6 +580,7 @@ struct BnApplyParams {
 
 template <typename T>
 __global__ void __launch_bounds__(256) k_bn_apply(BnApplyParams p) {
+  COEX_PDL_ENTER();
   stamp(p.ds, SK_BNAPPLY);
   if (skip(p.ds)) return;
   const T* x = res<T>(p.x);
@@ -565,6 +606,7 @@ __global__ void __launch_bounds__(256) k_bn_apply(BnApplyParams p) {
 // one float4 per thread.  BATCHNORM: y = x*A + B;  BATCHNORM_DX: dx = dy*A + x*B + D with
 // A = g*rstd, B = -g*rstd^2*mean(dy*xhat), D = g*rstd*(rstd*mean*mean(dy*xhat) - mean(dy)).
 __global__ void __launch_bounds__(256) k_bn_apply_v4(BnApplyParams p) {
+  COEX_PDL_ENTER();
   stamp(p.ds, SK_BNAPPLY);
   if (skip(p.ds)) return;
   extern __shared__ float coef[];                    // [3][C]

@@ -56,6 +56,7 @@ struct CvtParams {
 // (coalesced on both sides); transposed operands go through a 32x33 shared-memory
 // tile so both the strided read and the K-major write stay coalesced.
 __global__ void __launch_bounds__(256) k_cvt_bf16(CvtParams p) {
+  COEX_PDL_ENTER();
   stamp(p.ds, SK_CVT);
   if (skip(p.ds)) return;
   // operand select without dynamic indexing of the parameter arrays (that would copy the
@@ -192,6 +193,7 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 // descriptors, so no transposition pass is needed.
 template <int BN, bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc(const __grid_constant__ TcGemmParams p) {
+  COEX_PDL_ENTER();
   constexpr int STAGES = TcCfg<BN>::STAGES;
   constexpr int B_BYTES = TcCfg<BN>::B_BYTES;
   constexpr uint32_t TMEM_COLS = 2 * BN;            // two accumulator buffers
@@ -417,6 +419,7 @@ struct SplitReduceParams {
   Out out;
 };
 __global__ void __launch_bounds__(256) k_splitk_reduce(SplitReduceParams p) {
+  COEX_PDL_ENTER();
   stamp(p.ds, SK_SPLITK);
   if (skip(p.ds)) return;
   float* o = pick_out<float>(p.out, res<float>(p.a), p.b.cell || p.b.direct ? res<float>(p.b) : nullptr);

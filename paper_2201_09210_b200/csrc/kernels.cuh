@@ -15,6 +15,16 @@
 
 namespace coex {
 
+// Programmatic dependent launch: every kernel of a pass graph is linked to its predecessor by a
+// programmatic edge (runtime.cu add_kernel), so it is scheduled while the predecessor's last
+// wave drains; it waits here until the predecessor grid has completed and its writes are
+// visible, then lets its own successor launch early.  Outside PDL both are no-ops.
+#define COEX_PDL_ENTER()                                        \
+  do {                                                          \
+    asm volatile("griddepcontrol.wait;" ::: "memory");          \
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); \
+  } while (0)
+
 constexpr int kMaxRank = 8;
 constexpr int kMaxPub = 6;
 
@@ -237,6 +247,7 @@ struct EwParams {
 
 template <typename T>
 __global__ void __launch_bounds__(256) k_elementwise(EwParams p) {
+  COEX_PDL_ENTER();
   stamp(p.ds, SK_EW);
   if (skip(p.ds)) return;
   const T* a = res<T>(p.a);
@@ -289,6 +300,7 @@ struct ReduceParams {
 // Parity path: one warp streams the data, lane 0 accumulates strictly in order.
 template <typename T>
 __global__ void __launch_bounds__(32) k_reduce_seq(ReduceParams p) {
+  COEX_PDL_ENTER();
   stamp(p.ds, SK_REDUCE);
   if (skip(p.ds)) return;
   const T* a = res<T>(p.a);
@@ -313,6 +325,7 @@ __global__ void __launch_bounds__(32) k_reduce_seq(ReduceParams p) {
 // Tolerance path (fp32 / bf16 contexts): warp-shuffle tree in double, one block.
 template <typename T>
 __global__ void __launch_bounds__(1024) k_reduce_tree(ReduceParams p) {
+  COEX_PDL_ENTER();
   stamp(p.ds, SK_REDUCE);
   if (skip(p.ds)) return;
   const T* a = res<T>(p.a);
@@ -347,6 +360,7 @@ struct TransposeParams {
 
 template <typename T>
 __global__ void __launch_bounds__(256) k_transpose(TransposeParams p) {
+  COEX_PDL_ENTER();
   stamp(p.ds, SK_TRANSPOSE);
   if (skip(p.ds)) return;
   const T* a = res<T>(p.a);
@@ -370,6 +384,7 @@ __global__ void __launch_bounds__(256) k_transpose(TransposeParams p) {
 // 2-D transpose through a padded shared-memory tile (coalesced on both sides).
 template <typename T>
 __global__ void __launch_bounds__(256) k_transpose2d(TransposeParams p) {
+  COEX_PDL_ENTER();
   stamp(p.ds, SK_TRANSPOSE);
   if (skip(p.ds)) return;
   const T* a = res<T>(p.a);
@@ -413,6 +428,7 @@ struct MatmulParams {
 
 template <typename T, int BM, int BN, int BK, int RM, int RN, bool EXACT>
 __global__ void __launch_bounds__((BM / RM) * (BN / RN)) k_matmul_simt(MatmulParams p) {
+  COEX_PDL_ENTER();
   stamp(p.ds, SK_MATMUL);
   if (skip(p.ds)) return;
   const T* A = res<T>(p.a);
@@ -499,6 +515,7 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 
 template <typename T, int BM, int BN, int BK, int RM, int RN, bool EXACT, int STAGES>
 __global__ void __launch_bounds__((BM / RM) * (BN / RN)) k_matmul_pipe(MatmulParams p) {
+  COEX_PDL_ENTER();
   stamp(p.ds, SK_MATMUL);
   if (skip(p.ds)) return;
   const T* A = res<T>(p.a);
@@ -608,6 +625,7 @@ __global__ void __launch_bounds__((BM / RM) * (BN / RN)) k_matmul_pipe(MatmulPar
 // order (unrolled so loads run ahead of the dependent add chain).
 template <typename T>
 __global__ void __launch_bounds__(256) k_reduce_seq_smem(ReduceParams p) {
+  COEX_PDL_ENTER();
   stamp(p.ds, SK_REDUCE);
   if (skip(p.ds)) return;
   constexpr int CH = 2048;
@@ -741,6 +759,7 @@ __device__ __forceinline__ void chain_publish(const ChainParams& p) {
 
 template <typename T>
 __global__ void __launch_bounds__(256) k_chain(ChainParams p) {
+  COEX_PDL_ENTER();
   stamp(p.ds, SK_FUSED);
   if (skip(p.ds)) return;
   __shared__ ChainSmem<T> S;
@@ -770,6 +789,7 @@ __global__ void __launch_bounds__(256) k_chain(ChainParams p) {
 // one thread, the tolerance path reduces with warp shuffles in double.
 template <typename T, bool EXACT>
 __global__ void __launch_bounds__(256) k_chain_reduce(ChainParams p) {
+  COEX_PDL_ENTER();
   stamp(p.ds, SK_FUSED);
   if (skip(p.ds)) return;
   constexpr int CH = 1024;
@@ -826,6 +846,7 @@ struct FillParams {
 };
 template <typename T>
 __global__ void __launch_bounds__(256) k_fill(FillParams p) {
+  COEX_PDL_ENTER();
   if (skip(p.ds)) return;
   T* o = (T*)p.out.buf[0];
   publish_early(p.out, o);
@@ -836,11 +857,13 @@ __global__ void __launch_bounds__(256) k_fill(FillParams p) {
 // Convert float64 host payload (mapped) into the context precision.
 template <typename T>
 __global__ void __launch_bounds__(256) k_from_f64(const double* src, T* dst, long long n) {
+  COEX_PDL_ENTER();
   const long long stride = (long long)gridDim.x * blockDim.x;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) dst[i] = (T)src[i];
 }
 template <typename T>
 __global__ void __launch_bounds__(256) k_to_f64(const T* src, double* dst, long long n) {
+  COEX_PDL_ENTER();
   const long long stride = (long long)gridDim.x * blockDim.x;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) dst[i] = (double)src[i];
 }
@@ -858,6 +881,7 @@ struct PtrParams {
   Out out;
 };
 __global__ void k_ptr(PtrParams p) {
+  COEX_PDL_ENTER();
   stamp(p.ds, SK_PTR);
   if (skip(p.ds)) return;
   void* v;
@@ -921,6 +945,7 @@ struct SynthParams {
 
 template <typename T>
 __global__ void __launch_bounds__(kSynthThreads) k_synth(SynthParams p) {
+  COEX_PDL_ENTER();
   if (skip(p.ds)) return;
   T* o = (T*)p.out.buf[0];
   publish_early(p.out, o);
@@ -973,6 +998,7 @@ struct DecideParams {
 };
 
 __global__ void k_decide(DecideParams p) {
+  COEX_PDL_ENTER();
   DevState* ds = p.ds;
   stamp(ds, SK_DECIDE);
   if (ds->cancelled) {
@@ -1007,6 +1033,7 @@ struct GateParams {
   Mailbox* mb;
 };
 __global__ void k_commit_gate(GateParams p) {
+  COEX_PDL_ENTER();
   DevState* ds = p.ds;
   stamp(ds, SK_GATE);
   if (ds->cancelled) return;
@@ -1045,6 +1072,7 @@ struct FeedWaitParams {
 };
 
 __global__ void k_feed_wait(FeedWaitParams p) {
+  COEX_PDL_ENTER();
   DevState* ds = p.ds;
   stamp(ds, SK_FEED_WAIT);
   if (ds->cancelled) return;
@@ -1086,6 +1114,7 @@ struct FeedFillParams {
 
 template <typename T>
 __global__ void __launch_bounds__(kSynthThreads) k_feed_fill(FeedFillParams p) {
+  COEX_PDL_ENTER();
   stamp(p.ds, SK_FEED_FILL);
   if (skip(p.ds)) return;
   const int type = p.rec->type;
@@ -1128,6 +1157,7 @@ struct FetchParams {
 };
 
 __global__ void __launch_bounds__(256) k_fetch(FetchParams p) {
+  COEX_PDL_ENTER();
   DevState* ds = p.ds;
   stamp(ds, SK_FETCH);
   if (ds->cancelled) return;
@@ -1173,6 +1203,7 @@ struct BeginParams {
   int nvars;
 };
 __global__ void k_pass_begin(BeginParams p) {
+  COEX_PDL_ENTER();
   DevState* ds = p.ds;
   for (int i = threadIdx.x; i < p.nvars; i += blockDim.x) p.var_ovl[i] = nullptr;
   if (threadIdx.x == 0) {
@@ -1204,6 +1235,7 @@ struct CommitParams {
 // variable's spare buffer with 16-byte vector stores; block (0, v) flips the
 // committed pointer (nothing reads var_cur until the next pass).
 __global__ void __launch_bounds__(256) k_commit(CommitParams p) {
+  COEX_PDL_ENTER();
   stamp(p.ds, SK_COMMIT);
   if (p.ds->cancelled) return;
   const int j = blockIdx.y;
@@ -1233,6 +1265,7 @@ struct EndParams {
   int nvars;
 };
 __global__ void k_pass_end(EndParams p) {
+  COEX_PDL_ENTER();
   DevState* ds = p.ds;
   if (threadIdx.x != 0) return;
   stamp(ds, SK_END);

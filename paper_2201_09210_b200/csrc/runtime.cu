@@ -18,6 +18,7 @@
 #include <cstddef>
 #include <chrono>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -102,6 +103,16 @@ struct Launch {
     return args;
   }
 };
+
+// Blocks that each own a contiguous range of `rows` rows of `units` 16-byte units: enough
+// for ~8 rows of work per thread, at most 8 blocks per SM.
+dim3 blocks_for_rows(int64_t rows, int64_t units) {
+  const int64_t rpi = units >= 256 ? 1 : 256 / (units > 0 ? units : 1);
+  int64_t b = rows / (rpi * 8);
+  if (b > (int64_t)148 * 8) b = 148 * 8;
+  if (b < 1) b = 1;
+  return dim3((unsigned)b);
+}
 
 dim3 grid_for(int64_t n, int threads = 256, int max_per_sm = 8) {
   int64_t b = (n + threads - 1) / threads;
@@ -737,7 +748,7 @@ int build_xop_t(coex_ctx* c, const OpSpec& s, Launch* L, int* nL, size_t* ws_byt
         if (!build) break;
         ip.dst = A; ip.ld = bf16_pitch(Kc); ip.trans = 0;
         if (C % 8 == 0 && M < (1ll << 31))
-          L[(*nL)++].set((void*)k_im2col_bf16v, grid_for(M * Kc / 8), dim3(256), ip);
+          L[(*nL)++].set((void*)k_im2col_bf16v, blocks_for_rows(M, Kc / 8), dim3(256), ip);
         else if (M < (1ll << 31))
           L[(*nL)++].set((void*)k_im2col_bf16s, grid_for(M * ip.ld / 8), dim3(256), ip);
         else
@@ -785,9 +796,9 @@ int build_xop_t(coex_ctx* c, const OpSpec& s, Launch* L, int* nL, size_t* ws_byt
         if (rc) return rc;
         cp.cols = cols;
         if (F % 4 == 0 && N * Ho * Wo < (1ll << 31))
-          L[(*nL)++].set((void*)k_col2im_v<4>, grid_for(N * Ho * Wo * F / 4), dim3(256), cp);
+          L[(*nL)++].set((void*)k_col2im_v<4>, blocks_for_rows(N * Ho * Wo, F / 4), dim3(256), cp);
         else if (N * Ho * Wo < (1ll << 31))
-          L[(*nL)++].set((void*)k_col2im_v<1>, grid_for(N * Ho * Wo * F), dim3(256), cp);
+          L[(*nL)++].set((void*)k_col2im_v<1>, blocks_for_rows(N * Ho * Wo, F), dim3(256), cp);
         else
           L[(*nL)++].set((void*)k_col2im<float, float>, grid_for(N * Ho * Wo * F), dim3(256), cp);
         return COEX_OK;
@@ -820,7 +831,7 @@ int build_xop_t(coex_ctx* c, const OpSpec& s, Launch* L, int* nL, size_t* ws_byt
         if (!build) break;
         ip.dst = A; ip.ld = bf16_pitch(Kc); ip.trans = 0;
         if (C % 8 == 0 && P < (1ll << 31))
-          L[(*nL)++].set((void*)k_im2col_bf16v, grid_for(P * Kc / 8), dim3(256), ip);
+          L[(*nL)++].set((void*)k_im2col_bf16v, blocks_for_rows(P, Kc / 8), dim3(256), ip);
         else if (P < (1ll << 31))
           L[(*nL)++].set((void*)k_im2col_bf16s, grid_for(P * ip.ld / 8), dim3(256), ip);
         else
@@ -1573,6 +1584,11 @@ struct Builder {
     return bufs[i];
   }
 
+  std::unordered_map<cudaGraphNode_t, bool> kernel_nodes;   // nodes created by add_kernel
+  bool pdl = true;
+
+  // Kernel node after `*prev`.  Kernel -> kernel edges are programmatic (PDL): the node is
+  // scheduled while its predecessor's last wave drains and synchronises in COEX_PDL_ENTER.
   int add_kernel(cudaGraph_t g, cudaGraphNode_t* prev, Launch& L) {
     cudaKernelNodeParams kp = {};
     kp.func = L.fn;
@@ -1581,7 +1597,17 @@ struct Builder {
     kp.sharedMemBytes = (unsigned)L.smem;
     kp.kernelParams = L.argv();
     cudaGraphNode_t node;
-    CK(cudaGraphAddKernelNode(&node, g, *prev ? prev : nullptr, *prev ? 1 : 0, &kp));
+    if (pdl && *prev && kernel_nodes.count(*prev)) {
+      CK(cudaGraphAddKernelNode(&node, g, nullptr, 0, &kp));
+      cudaGraphEdgeData ed;
+      memset(&ed, 0, sizeof(ed));
+      ed.from_port = cudaGraphKernelNodePortProgrammatic;
+      ed.type = cudaGraphDependencyTypeProgrammatic;
+      CK(cudaGraphAddDependencies_v2(g, prev, &node, &ed, 1));
+    } else {
+      CK(cudaGraphAddKernelNode(&node, g, *prev ? prev : nullptr, *prev ? 1 : 0, &kp));
+    }
+    kernel_nodes[node] = true;
     *prev = node;
     p->n_kernel_nodes++;
     return COEX_OK;
@@ -1935,6 +1961,10 @@ int coex_prog_build(coex_ctx* c, const int64_t* plan, int64_t nwords, const doub
   coex_prog* p = new coex_prog();
   p->ctx = c;
   Builder b{c, p, plan, nwords};
+  {
+    const char* e = getenv("COEX_PDL");
+    b.pdl = !(e && e[0] == '0');
+  }
   try {
     if (b.next() != kPlanMagic || b.next() != kPlanVersion) throw std::runtime_error("bad plan header");
     const int64_t nbufs = b.next();
