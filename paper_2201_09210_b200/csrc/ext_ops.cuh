@@ -351,6 +351,78 @@ __global__ void __launch_bounds__(256) k_col2im_v(Col2imParams p) {
   publish_late(p.out, o);
 }
 
+// fp32 NHWC -> bf16 NHWC with a zero border of P pixels ([N][H+2P][W+2P][C]; the border is
+// never written -- the workspace is zeroed once), the source of the implicit-GEMM gathers:
+// TMA boxes then start at non-negative coordinates.  C % 8 == 0; 8 channels per thread.
+struct PadCvtParams {
+  DevState* ds;
+  In x;
+  __nv_bfloat16* dst;
+  long long N;
+  int H, W, C, P;
+};
+__global__ void __launch_bounds__(256) k_cvt_pad_bf16(PadCvtParams p) {
+  COEX_PDL_ENTER();
+  stamp(p.ds, SK_CVT);
+  if (skip(p.ds)) return;
+  const float* x = res<float>(p.x);
+  const int C8 = p.C / 8, Wp = p.W + 2 * p.P, Hp = p.H + 2 * p.P;
+  const long long total = p.N * p.H * p.W * C8;
+  for (long long u = (long long)blockIdx.x * blockDim.x + threadIdx.x; u < total;
+       u += (long long)gridDim.x * blockDim.x) {
+    const long long pix = u / C8;
+    const int cg = (int)(u - pix * C8);
+    const int w = (int)(pix % p.W);
+    const long long t = pix / p.W;
+    const int h = (int)(t % p.H);
+    const long long n = t / p.H;
+    const float4* src = (const float4*)(x + pix * p.C + cg * 8);
+    const float4 a = __ldg(src), b = __ldg(src + 1);
+    __nv_bfloat162 v0 = __floats2bfloat162_rn(a.x, a.y), v1 = __floats2bfloat162_rn(a.z, a.w);
+    __nv_bfloat162 v2 = __floats2bfloat162_rn(b.x, b.y), v3 = __floats2bfloat162_rn(b.z, b.w);
+    uint4 o;
+    o.x = *(uint32_t*)&v0; o.y = *(uint32_t*)&v1; o.z = *(uint32_t*)&v2; o.w = *(uint32_t*)&v3;
+    *(uint4*)(p.dst + ((n * Hp + h + p.P) * Wp + w + p.P) * p.C + cg * 8) = o;
+  }
+}
+
+// Sub-pixel conv2d_t weights: for output phase (py, px) the taps ky = ky0 + (T-1-jy)*so,
+// ky0 = (py + pad) mod so (likewise x), stacked as bf16 [phase][(jy, jx, c)][pitch(F)] -- the
+// MN-major B operand of the phase GEMMs.  w is conv2d_t's weight [k*k*F][C].
+struct WPhaseParams {
+  DevState* ds;
+  In w;
+  __nv_bfloat16* dst;
+  long long ld;              // row pitch of dst (>= F, multiple of 8)
+  int k, so, pad, T, C, F;
+};
+__global__ void __launch_bounds__(256) k_convt_wphase(WPhaseParams p) {
+  COEX_PDL_ENTER();
+  stamp(p.ds, SK_CVT);
+  if (skip(p.ds)) return;
+  const float* w = res<float>(p.w);
+  const long long krows = (long long)p.T * p.T * p.C;
+  const long long rows = (long long)p.so * p.so * krows;
+  const long long total = rows * p.ld;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long r = i / p.ld;
+    const int f = (int)(i - r * p.ld);
+    float v = 0.f;
+    if (f < p.F) {
+      const int ph = (int)(r / krows);
+      const int rem = (int)(r - (long long)ph * krows);
+      const int tap = rem / p.C, c = rem - tap * p.C;
+      const int jy = tap / p.T, jx = tap - jy * p.T;
+      const int py = ph / p.so, px = ph - py * p.so;
+      const int ky = (py + p.pad) % p.so + (p.T - 1 - jy) * p.so;
+      const int kx = (px + p.pad) % p.so + (p.T - 1 - jx) * p.so;
+      v = w[(((long long)ky * p.k + kx) * p.F + f) * p.C + c];
+    }
+    p.dst[i] = __float2bfloat16_rn(v);
+  }
+}
+
 // ------------------------------------------------------------------ column statistics
 // Per-channel (last axis) sums over all leading rows, in double, with a per-channel shift
 // K_c = x[0, c] (numerically a centred one-pass): S1 = sum(x-K), S2 = sum((x-K)^2),

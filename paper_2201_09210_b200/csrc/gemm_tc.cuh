@@ -108,8 +108,36 @@ __global__ void __launch_bounds__(256) k_cvt_bf16(CvtParams p) {
   }
 }
 
+// Implicit-GEMM convolution geometry (AMODE 2 / 3): the A operand is gathered straight from
+// the bf16 NHWC input by 4-D TMA boxes {64 channels, bw*s, bh*s, bn} with element strides
+// {1, s, s, 1} -- one box per (tap, 64-channel chunk) and pixel block; padding = TMA
+// out-of-bounds zero fill.  Pixel (n, oy, ox) of the GEMM grid reads input
+// (n, oy*s + off_y + ty, ox*s + off_x + tx) for tap (ty, tx) = (tap / taps_x, tap % taps_x).
+// conv2d_t runs as `phases` sub-pixel convolutions (stride 1, per-phase offsets, phase weights
+// stacked in B), the epilogue scattering GEMM row (n, h, w) of phase (py, px) to output row
+// (n, so*h + py, so*w + px).
+struct TcConv {
+  int C;                     // input channels (multiple of 64)
+  int taps_x;                // taps per kernel row in the K ordering (tap, channel)
+  int s;                     // element stride of the gather
+  int Hg, Wg;                // GEMM pixel grid
+  int bw, bh, bn;            // pixel block of one box (bw * bh * bn = 128 (AMODE 2) or 64 (AMODE 3))
+  int phases;                // 1, or so*so for the sub-pixel conv2d_t
+  int so, Ho, Wo;            // output grid of the scatter epilogue (phases > 1)
+  long long b_rows;          // B rows per phase (phase p reads B rows p * b_rows ...)
+  int off_y[4], off_x[4];    // lower offsets (phases == 1: index 0)
+  int pad, bord;             // phases > 1: conv2d_t padding and the bf16 copy's zero border
+};
+
+// lower input offset of output phase q (sub-pixel conv2d_t): taps ky = ky0 + (T-1-j)*so,
+// ky0 = (q + pad) mod so, input row = h + (q + pad - ky0)/so - (T-1) + j (+ border)
+__device__ __forceinline__ int phase_off(const TcConv& g, int q) {
+  const int k0 = (q + g.pad) % g.so;
+  return (q + g.pad - k0) / g.so - (g.taps_x - 1) + g.bord;
+}
+
 struct TcGemmParams {
-  CUtensorMap tmA;           // bf16 [M][ld], box {64, 128}, SWIZZLE_128B
+  CUtensorMap tmA;           // bf16 [M][ld], box {64, 128}, SWIZZLE_128B (AMODE 2/3: 4-D NHWC map)
   CUtensorMap tmB;           // bf16 [N][ld], box {64, BN}
   DevState* ds;
   In a, b;                   // original operands (ping-pong output choice only)
@@ -117,6 +145,7 @@ struct TcGemmParams {
   Out out;
   float* raw;                // non-null: write here (no publication) -- scratch / split-K slices
   int splits;                // split-K: CTA (tile, split) covers k-blocks of its slice, raw + split*M*N
+  TcConv cv;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -180,6 +209,23 @@ __host__ __device__ constexpr uint32_t idesc_bf16_f32(int M, int N, bool a_mn = 
          ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2,
+                                            int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], [%2];" ::
+          "r"(smem_u32(dst)),
+      "l"((uint64_t)map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+
+// pixel index -> (n, oy, ox) of the GEMM grid
+__device__ __forceinline__ void conv_pix(const TcConv& g, long long pix, int& n, int& oy, int& ox) {
+  ox = (int)(pix % g.Wg);
+  const long long t = pix / g.Wg;
+  oy = (int)(t % g.Hg);
+  n = (int)(t / g.Hg);
+}
+
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
@@ -188,15 +234,18 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 // grid; three pipelines: the smem ring (TMA -> MMA, `full`/`empty`), two TMEM accumulator
 // buffers (MMA -> epilogue, `tfull`/`tempty`) so the epilogue of item i overlaps the MMAs of
 // item i+1, and the static round-robin item schedule shared by all roles.
-// A_MN / B_MN: operand stored MN-major in global memory ([K][M] / [K][N] rows, e.g. an
-// im2col matrix used as A^T) -- loaded as 64 x 64 boxes and consumed through MN-major
+// AMODE: 0 = A K-major 2-D, 1 = A MN-major 2-D ([K][M] rows, e.g. an im2col matrix used as
+// A^T), 2 = implicit convolution, A K-major (conv2d / sub-pixel conv2d_t), 3 = implicit
+// convolution, A MN-major (weight gradient: M = (tap, channel), K = pixels).  B_MN: B stored
+// [K][N].  MN-major operands are loaded as 64 x 64 boxes and consumed through MN-major
 // descriptors, so no transposition pass is needed.
-template <int BN, bool A_MN, bool B_MN>
+template <int BN, int AMODE, bool B_MN>
 __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc(const __grid_constant__ TcGemmParams p) {
   COEX_PDL_ENTER();
   constexpr int STAGES = TcCfg<BN>::STAGES;
   constexpr int B_BYTES = TcCfg<BN>::B_BYTES;
   constexpr uint32_t TMEM_COLS = 2 * BN;            // two accumulator buffers
+  constexpr bool A_MN = AMODE == 1 || AMODE == 3;
   stamp(p.ds, SK_MATMUL);
   if (skip(p.ds)) return;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -213,14 +262,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc(const __grid_constant
   const long long tiles_n = (p.N + BN - 1) / BN;
   const long long tiles_m = (p.M + TC_BM - 1) / TC_BM;
   const int splits = p.splits > 1 ? p.splits : 1;
-  const long long items = tiles_m * tiles_n * splits;
+  const int phases = AMODE == 2 ? p.cv.phases : 1;
+  const long long items = tiles_m * tiles_n * splits * phases;
   const int nk_all = (int)((p.K + TC_BK - 1) / TC_BK);
   const long long group = (long long)TC_GROUP_M * tiles_n;
 
   // item -> (m0, n0, split, first k-block, k-block count); grouped rasterisation of tiles
   auto decode = [&](long long it, int& m0, int& n0, int& split, int& kb0, int& nk) {
     split = (int)(it % splits);
-    const long long t = it / splits;
+    const long long t = (it / splits) / phases;
     const long long first_m = (t / group) * TC_GROUP_M;
     const long long gm = min((long long)TC_GROUP_M, tiles_m - first_m);
     m0 = (int)((first_m + (t % group) % gm) * TC_BM);
@@ -266,24 +316,49 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc(const __grid_constant
       for (long long it = blockIdx.x; it < items; it += gridDim.x) {
         int m0, n0, split, kb0, nk;
         decode(it, m0, n0, split, kb0, nk);
+        const int cph = (int)((it / splits) % phases);     // sub-pixel phase of this item
         for (int kb = 0; kb < nk; ++kb, ++kbg) {
           const int s = (int)(kbg % STAGES);
           const uint32_t ph = (uint32_t)((kbg / STAGES) & 1);
           mbar_wait(&empty[s], ph ^ 1u);
           mbar_expect_tx(&full[s], TC_A_BYTES + B_BYTES);
-          if constexpr (A_MN) {
+          const int kk = (kb0 + kb) * TC_BK;
+          if constexpr (AMODE == 2) {                 // (tap, channel chunk) x 128-pixel block
+            const int tap = kk / p.cv.C, c0 = kk - tap * p.cv.C;
+            const int ty = tap / p.cv.taps_x, tx = tap - ty * p.cv.taps_x;
+            int pn, oy, ox;
+            conv_pix(p.cv, m0, pn, oy, ox);
+            int offy = p.cv.off_y[0], offx = p.cv.off_x[0];
+            if (phases > 1) {
+              offy = phase_off(p.cv, cph / p.cv.so);
+              offx = phase_off(p.cv, cph % p.cv.so);
+            }
+            tma_load_4d(sA + s * TC_A_BYTES, &p.tmA, &full[s], c0, ox * p.cv.s + offx + tx, oy * p.cv.s + offy + ty, pn);
+          } else if constexpr (AMODE == 3) {          // 64-pixel block x two (tap, channel) halves
+            int pn, oy, ox;
+            conv_pix(p.cv, kk, pn, oy, ox);
+#pragma unroll
+            for (int h = 0; h < TC_BM / 64; ++h) {
+              const int mm = m0 + 64 * h;
+              const int tap = mm / p.cv.C, c0 = mm - tap * p.cv.C;
+              const int ty = tap / p.cv.taps_x, tx = tap - ty * p.cv.taps_x;
+              tma_load_4d(sA + s * TC_A_BYTES + h * 8192, &p.tmA, &full[s], c0, ox * p.cv.s + p.cv.off_x[0] + tx,
+                          oy * p.cv.s + p.cv.off_y[0] + ty, pn);
+            }
+          } else if constexpr (A_MN) {
 #pragma unroll
             for (int h = 0; h < TC_BM / 64; ++h)
-              tma_load_2d(sA + s * TC_A_BYTES + h * 8192, &p.tmA, &full[s], m0 + 64 * h, (kb0 + kb) * TC_BK);
+              tma_load_2d(sA + s * TC_A_BYTES + h * 8192, &p.tmA, &full[s], m0 + 64 * h, kk);
           } else {
-            tma_load_2d(sA + s * TC_A_BYTES, &p.tmA, &full[s], (kb0 + kb) * TC_BK, m0);
+            tma_load_2d(sA + s * TC_A_BYTES, &p.tmA, &full[s], kk, m0);
           }
+          const int brow = (int)(cph * p.cv.b_rows) + kk;
           if constexpr (B_MN) {
 #pragma unroll
             for (int h = 0; h < BN / 64; ++h)
-              tma_load_2d(sB + s * B_BYTES + h * 8192, &p.tmB, &full[s], n0 + 64 * h, (kb0 + kb) * TC_BK);
+              tma_load_2d(sB + s * B_BYTES + h * 8192, &p.tmB, &full[s], n0 + 64 * h, brow);
           } else {
-            tma_load_2d(sB + s * B_BYTES, &p.tmB, &full[s], (kb0 + kb) * TC_BK, n0);
+            tma_load_2d(sB + s * B_BYTES, &p.tmB, &full[s], brow, n0);
           }
         }
       }
@@ -346,6 +421,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc(const __grid_constant
       const int a = li & 1;
       const uint32_t aph = (uint32_t)((li >> 1) & 1);
       float* C = p.raw != nullptr ? p.raw + (long long)split * p.M * p.N : Cout;
+      const int cph = (int)((it / splits) % phases);
       mbar_wait(&tfull[a], aph);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll 1
@@ -382,7 +458,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc(const __grid_constant
           const long long grow = (long long)m0 + lane_base + rr;
           if (grow < p.M && gcol < p.N) {
             const float4 v = *(const float4*)(stage + rr * TC_EPI_LD + col);
-            float* dst = C + grow * p.N + gcol;
+            long long orow = grow;
+            if (AMODE == 2 && phases > 1) {          // sub-pixel conv2d_t: scatter to the output grid
+              int pn, hy, wx;
+              conv_pix(p.cv, grow, pn, hy, wx);
+              const int py = cph / p.cv.so, px = cph - py * p.cv.so;
+              orow = ((long long)pn * p.cv.Ho + (long long)hy * p.cv.so + py) * p.cv.Wo + (long long)wx * p.cv.so + px;
+            }
+            float* dst = C + orow * p.N + gcol;
             if (vec_ok && gcol + 4 <= p.N) {
               *(float4*)dst = v;
             } else {

@@ -640,33 +640,77 @@ size_t matmul_split_ws(int64_t M, int64_t N, int64_t K) {
 }
 
 // Appends the GEMM (and its split-K reduction) to L.  `ws` = fp32 split slices (splits > 1).
+// Kernel variants: AMODE 0/1 (2-D A, K- or MN-major) x B_MN, AMODE 2/3 (implicit conv) x B_MN.
 template <int BN>
-int tc_attr3(bool amn, bool bmn) {
-  static bool done[4] = {false, false, false, false};
-  const int i = (amn ? 2 : 0) + (bmn ? 1 : 0);
+void* tc_fn(int amode, bool bmn) {
+  switch (amode) {
+    case 0: return bmn ? (void*)k_gemm_tc<BN, 0, true> : (void*)k_gemm_tc<BN, 0, false>;
+    case 1: return bmn ? (void*)k_gemm_tc<BN, 1, true> : (void*)k_gemm_tc<BN, 1, false>;
+    case 2: return (void*)k_gemm_tc<BN, 2, true>;
+    default: return (void*)k_gemm_tc<BN, 3, true>;
+  }
+}
+template <int BN>
+int tc_attr(int amode, bool bmn) {
+  static bool done[8] = {false};
+  const int i = amode * 2 + (bmn ? 1 : 0);
   if (!done[i]) {
-    const void* fn = amn ? (bmn ? (const void*)k_gemm_tc<BN, true, true> : (const void*)k_gemm_tc<BN, true, false>)
-                         : (bmn ? (const void*)k_gemm_tc<BN, false, true> : (const void*)k_gemm_tc<BN, false, false>);
-    CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, TcCfg<BN>::SMEM));
+    CK(cudaFuncSetAttribute((const void*)tc_fn<BN>(amode, bmn), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            TcCfg<BN>::SMEM));
     done[i] = true;
   }
   return COEX_OK;
 }
-template <int BN>
-void* tc_fn(bool amn, bool bmn) {
-  return amn ? (bmn ? (void*)k_gemm_tc<BN, true, true> : (void*)k_gemm_tc<BN, true, false>)
-             : (bmn ? (void*)k_gemm_tc<BN, false, true> : (void*)k_gemm_tc<BN, false, false>);
+
+// 4-D NHWC bf16 gather map for the implicit-GEMM convolutions: box {64 channels, bw*s, bh*s, bn},
+// element strides {1, s, s, 1}, 128-byte swizzle, out-of-bounds (padding) -> 0.
+int make_tmap_conv(CUtensorMap* m, void* base, int64_t N, int64_t H, int64_t W, int64_t C, int s, int bw, int bh,
+                   int bn) {
+  auto enc = tmap_encoder();
+  if (!enc) return fail(COEX_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[4] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)N};
+  cuuint64_t strides[3] = {(cuuint64_t)C * 2, (cuuint64_t)W * C * 2, (cuuint64_t)H * W * C * 2};
+  cuuint32_t box[4] = {64, (cuuint32_t)(bw * s), (cuuint32_t)(bh * s), (cuuint32_t)bn};
+  cuuint32_t es[4] = {1, (cuuint32_t)s, (cuuint32_t)s, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, base, dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(COEX_CUDA_ERROR, "cuTensorMapEncodeTiled (conv) failed: " + std::to_string((int)r));
+  return COEX_OK;
 }
 
-// a_mn / b_mn: operand stored MN-major ([K][pitch(M)] / [K][pitch(N)]) instead of K-major.
+// Pixel block {bw, bh, bn} of `pix` consecutive pixels of an Hg x Wg grid that tiles it exactly
+// (so every M tile / K block of pixels is one TMA box).
+bool conv_blocks(int64_t Hg, int64_t Wg, int pix, int* bw, int* bh, int* bn) {
+  if (Wg >= pix) {
+    if (Wg % pix) return false;
+    *bw = pix; *bh = 1; *bn = 1;
+  } else if (Hg * Wg >= pix) {
+    if (pix % Wg || Hg % (pix / Wg)) return false;
+    *bw = (int)Wg; *bh = pix / (int)Wg; *bn = 1;
+  } else {
+    if (pix % (Hg * Wg)) return false;
+    *bw = (int)Wg; *bh = (int)Hg; *bn = pix / (int)(Hg * Wg);
+  }
+  return *bw * 2 <= 256 && *bh * 2 <= 256;
+}
+
+// amode: 0 A K-major [M][pitch(K)], 1 A MN-major [K][pitch(M)], 2 / 3 implicit convolution
+// (A gathered by `conv_map` with geometry `cv`); b_mn: B stored [K][pitch(N)] instead of [N][pitch(K)].
 int tc_gemm_launches(coex_ctx* c, DevState* ds, void* a16, void* b16, int64_t M, int64_t N, int64_t K,
                      const TcPlan& t, In na, In nb, const Out& out, float* raw, float* ws, Launch* L, int* nL,
-                     bool a_mn = false, bool b_mn = false) {
+                     int amode = 0, bool b_mn = false, const TcConv* cv = nullptr,
+                     const CUtensorMap* conv_map = nullptr) {
   TcGemmParams gp;
   memset(&gp, 0, sizeof(gp));
-  int rc = a_mn ? make_tmap_mn(&gp.tmA, a16, M, K) : make_tmap(&gp.tmA, a16, M, K, TC_BM);
+  int rc = COEX_OK;
+  if (amode >= 2) gp.tmA = *conv_map;
+  else rc = amode == 1 ? make_tmap_mn(&gp.tmA, a16, M, K) : make_tmap(&gp.tmA, a16, M, K, TC_BM);
   if (rc) return rc;
-  rc = b_mn ? make_tmap_mn(&gp.tmB, b16, N, K) : make_tmap(&gp.tmB, b16, N, K, t.bn);
+  if (cv) gp.cv = *cv;
+  else gp.cv.phases = 1;
+  const int64_t brows = K * ((amode == 2 && cv) ? cv->phases : 1);    // sub-pixel phases stack their B
+  rc = b_mn ? make_tmap_mn(&gp.tmB, b16, N, brows) : make_tmap(&gp.tmB, b16, N, K, t.bn);
   if (rc) return rc;
   gp.ds = ds;
   gp.a = na;
@@ -678,11 +722,12 @@ int tc_gemm_launches(coex_ctx* c, DevState* ds, void* a16, void* b16, int64_t M,
   gp.splits = t.splits;
   gp.raw = t.splits > 1 ? ws : raw;
   Launch& G = L[(*nL)++];
-  void* fn = t.bn == 64 ? tc_fn<64>(a_mn, b_mn) : t.bn == 128 ? tc_fn<128>(a_mn, b_mn) : tc_fn<256>(a_mn, b_mn);
-  const int64_t items = t.tiles * t.splits;
+  void* fn = t.bn == 64 ? tc_fn<64>(amode, b_mn) : t.bn == 128 ? tc_fn<128>(amode, b_mn) : tc_fn<256>(amode, b_mn);
+  const int64_t items = ((M + TC_BM - 1) / TC_BM) * ((N + t.bn - 1) / t.bn) * t.splits *
+                        (amode == 2 ? gp.cv.phases : 1);
   G.set(fn, dim3((unsigned)(items < kNumSMs ? items : kNumSMs)), dim3(TC_THREADS), gp);
   G.smem = t.bn == 64 ? TcCfg<64>::SMEM : t.bn == 128 ? TcCfg<128>::SMEM : TcCfg<256>::SMEM;
-  rc = t.bn == 64 ? tc_attr3<64>(a_mn, b_mn) : t.bn == 128 ? tc_attr3<128>(a_mn, b_mn) : tc_attr3<256>(a_mn, b_mn);
+  rc = t.bn == 64 ? tc_attr<64>(amode, b_mn) : t.bn == 128 ? tc_attr<128>(amode, b_mn) : tc_attr<256>(amode, b_mn);
   if (rc) return rc;
   if (t.splits > 1) {
     SplitReduceParams r{};
@@ -701,6 +746,33 @@ int tc_gemm_launches(coex_ctx* c, DevState* ds, void* a16, void* b16, int64_t M,
     L[(*nL)++].set((void*)k_splitk_reduce, grid_for(M * N / 4 + 1), dim3(256), r);
   }
   return COEX_OK;
+}
+
+// fp32 [rows][K] -> bf16 [rows][pitch(K)] (flattened k_cvt_bf16, one operand)
+void cvt_rows_launch(DevState* ds, In src, void* dst, int64_t rows, int64_t K, Launch* L) {
+  CvtParams q{};
+  q.ds = ds; q.src[0] = src; q.rows[0] = rows; q.K = K; q.ld = bf16_pitch(K); q.trans[0] = 0;
+  q.dst[0] = (__nv_bfloat16*)dst;
+  const int64_t gx = (rows * q.ld / 8 + 255) / 256;
+  L->set((void*)k_cvt_bf16, dim3((unsigned)(gx < kNumSMs * 16 ? (gx < 1 ? 1 : gx) : kNumSMs * 16), 1), dim3(256), q);
+}
+
+// fp32 NHWC x -> zero-bordered bf16 copy (implicit-GEMM gather source)
+void cvt_pad_launch(DevState* ds, In src, void* dst, int64_t N, int64_t H, int64_t W, int64_t C, int P, Launch* L) {
+  PadCvtParams q{};
+  q.ds = ds; q.x = src; q.dst = (__nv_bfloat16*)dst; q.N = N; q.H = (int)H; q.W = (int)W; q.C = (int)C; q.P = P;
+  L->set((void*)k_cvt_pad_bf16, grid_for(N * H * W * C / 8), dim3(256), q);
+}
+
+// COEX_IMPLICIT: bitmask of implicit-GEMM convolution paths (1 conv2d, 2 conv2d_dw, 4 conv2d_t);
+// default all on.
+int implicit_mask() {
+  static int m = -1;
+  if (m < 0) {
+    const char* e = getenv("COEX_IMPLICIT");
+    m = e ? atoi(e) : 7;
+  }
+  return m;
 }
 
 struct Carve {
@@ -740,6 +812,29 @@ int build_xop_t(coex_ctx* c, const OpSpec& s, Launch* L, int* nL, size_t* ws_byt
       ip.ds = s.ds; ip.x = s.in[0];
       ip.N = N; ip.H = H; ip.W = W; ip.C = C; ip.Ho = Ho; ip.Wo = Wo;
       ip.k = (int)k; ip.s = (int)st; ip.p = (int)pd;
+      int bw, bh, bnn;
+      // implicit GEMM pays off on the larger pixel grids (measured per op on the C2 shapes:
+      // tools/cmp_implicit.py); small grids keep the materialised im2col operand
+      if (bf16 && (implicit_mask() & 1) && C % 64 == 0 && st <= 2 && Ho * Wo >= 256 &&
+          conv_blocks(Ho, Wo, 128, &bw, &bh, &bnn)) {
+        // implicit GEMM: A gathered from bf16 NHWC x by 4-D TMA boxes (no im2col matrix)
+        const TcPlan t = tc_plan(M, F, Kc, true);
+        const int P = (int)pd;
+        void* X = cv.take((size_t)N * (H + 2 * P) * (W + 2 * P) * C * 2);
+        void* B = cv.take((size_t)Kc * bf16_pitch(F) * 2);
+        float* ws = t.splits > 1 ? (float*)cv.take((size_t)t.splits * M * F * 4) : nullptr;
+        if (!build) break;
+        cvt_pad_launch(s.ds, s.in[0], X, N, H, W, C, P, &L[(*nL)++]);
+        cvt_rows_launch(s.ds, s.in[1], B, Kc, F, &L[(*nL)++]);
+        TcConv g{};
+        g.C = (int)C; g.taps_x = (int)k; g.s = (int)st; g.Hg = (int)Ho; g.Wg = (int)Wo;
+        g.bw = bw; g.bh = bh; g.bn = bnn; g.phases = 1; g.off_y[0] = g.off_x[0] = 0;   // padding is in the copy
+        CUtensorMap map;
+        int rc = make_tmap_conv(&map, X, N, H + 2 * P, W + 2 * P, C, (int)st, bw, bh, bnn);
+        if (rc) return rc;
+        return tc_gemm_launches(c, s.ds, nullptr, B, M, F, Kc, t, s.in[0], s.in[1], s.out, nullptr, ws, L, nL, 2, true,
+                                &g, &map);
+      }
       if (bf16) {
         const TcPlan t = tc_plan(M, F, Kc, true);
         void* A = cv.take((size_t)M * bf16_pitch(Kc) * 2);
@@ -759,7 +854,7 @@ int build_xop_t(coex_ctx* c, const OpSpec& s, Launch* L, int* nL, size_t* ws_byt
         const int64_t gx = (Kc * q.ld / 8 + 255) / 256;
         L[(*nL)++].set((void*)k_cvt_bf16, dim3((unsigned)(gx < kNumSMs * 16 ? (gx < 1 ? 1 : gx) : kNumSMs * 16), 1),
                        dim3(256), q);
-        return tc_gemm_launches(c, s.ds, A, B, M, F, Kc, t, s.in[0], s.in[1], s.out, nullptr, ws, L, nL, false, true);
+        return tc_gemm_launches(c, s.ds, A, B, M, F, Kc, t, s.in[0], s.in[1], s.out, nullptr, ws, L, nL, 0, true);
       }
       void* A = cv.take((size_t)M * Kc * es);
       if (!build) break;
@@ -775,6 +870,46 @@ int build_xop_t(coex_ctx* c, const OpSpec& s, Launch* L, int* nL, size_t* ws_byt
       const int64_t N = s.in_shape[0][0], H = s.in_shape[0][1], W = s.in_shape[0][2], C = s.in_shape[0][3];
       const int64_t Ho = s.out_shape[1], Wo = s.out_shape[2], F = s.out_shape[3];
       const int64_t M = N * H * W, Nc = k * k * F;
+      int bw, bh, bnn;
+      if (bf16 && (implicit_mask() & 4) && C % 64 == 0 && st >= 1 && k % st == 0 && k - 2 * pd == st &&
+          H * W >= 64 && F >= 32 && conv_blocks(H, W, 128, &bw, &bh, &bnn)) {
+        // sub-pixel decomposition: st*st stride-1 implicit GEMMs (one per output phase) over the
+        // bf16 NHWC input, epilogue scattering straight into the output -- no cols / col2im
+        const int Tp = (int)(k / st), phases = (int)(st * st);
+        const int64_t Kr = (int64_t)Tp * Tp * C;
+        const TcPlan t = tc_plan(M * phases, F, Kr, false);
+        int lo = 0, hi = 0;                          // offset range over the phases
+        for (int ph = 0; ph < phases; ++ph) {
+          const int py = ph / (int)st, ky0 = (py + (int)pd) % (int)st;
+          const int o = (py + (int)pd - ky0) / (int)st - (Tp - 1);
+          lo = o < lo ? o : lo;
+          hi = o + Tp - 1 > hi ? o + Tp - 1 : hi;
+        }
+        const int Pp = -lo > hi ? -lo : hi;          // zero border of the bf16 copy
+        void* X = cv.take((size_t)N * (H + 2 * Pp) * (W + 2 * Pp) * C * 2);
+        void* B = cv.take((size_t)phases * Kr * bf16_pitch(F) * 2);
+        if (!build) break;
+        cvt_pad_launch(s.ds, s.in[0], X, N, H, W, C, Pp, &L[(*nL)++]);
+        WPhaseParams wp{};
+        wp.ds = s.ds; wp.w = s.in[1]; wp.dst = (__nv_bfloat16*)B; wp.ld = bf16_pitch(F);
+        wp.k = (int)k; wp.so = (int)st; wp.pad = (int)pd; wp.T = Tp; wp.C = (int)C; wp.F = (int)F;
+        L[(*nL)++].set((void*)k_convt_wphase, grid_for(phases * Kr * wp.ld), dim3(256), wp);
+        TcConv g{};
+        g.C = (int)C; g.taps_x = Tp; g.s = 1; g.Hg = (int)H; g.Wg = (int)W; g.bw = bw; g.bh = bh; g.bn = bnn;
+        g.phases = phases; g.so = (int)st; g.Ho = (int)Ho; g.Wo = (int)Wo; g.b_rows = Kr; g.pad = (int)pd;
+        g.bord = Pp;
+        for (int ph = 0; ph < phases; ++ph) {
+          const int py = ph / (int)st, px = ph % (int)st;
+          const int ky0 = (py + (int)pd) % (int)st, kx0 = (px + (int)pd) % (int)st;
+          g.off_y[ph] = (py + (int)pd - ky0) / (int)st - (Tp - 1) + Pp;
+          g.off_x[ph] = (px + (int)pd - kx0) / (int)st - (Tp - 1) + Pp;
+        }
+        CUtensorMap map;
+        int rc = make_tmap_conv(&map, X, N, H + 2 * Pp, W + 2 * Pp, C, 1, bw, bh, bnn);
+        if (rc) return rc;
+        return tc_gemm_launches(c, s.ds, nullptr, B, M, F, Kr, t, s.in[0], s.in[1], s.out, nullptr, nullptr, L, nL, 2,
+                                true, &g, &map);
+      }
       Col2imParams cp{};
       cp.ds = s.ds; cp.N = N; cp.H = H; cp.W = W; cp.F = F; cp.Ho = Ho; cp.Wo = Wo;
       cp.k = (int)k; cp.s = (int)st; cp.p = (int)pd; cp.a = s.in[0]; cp.b = s.in[1]; cp.out = s.out;
@@ -821,6 +956,28 @@ int build_xop_t(coex_ctx* c, const OpSpec& s, Launch* L, int* nL, size_t* ws_byt
       ip.ds = s.ds; ip.x = s.in[0];
       ip.N = N; ip.H = H; ip.W = W; ip.C = C; ip.Ho = Ho; ip.Wo = Wo;
       ip.k = (int)k; ip.s = (int)st; ip.p = (int)pd;
+      int bw, bh, bnn;
+      if (bf16 && (implicit_mask() & 2) && C % 64 == 0 && st <= 2 && Ho * Wo >= 256 &&
+          conv_blocks(Ho, Wo, 64, &bw, &bh, &bnn)) {
+        // implicit GEMM: A = im2col(x)^T gathered from bf16 NHWC x (64-pixel K blocks,
+        // (tap, 64-channel) M halves, MN-major), B = dy [P][pitch(F)] MN-major
+        const TcPlan t = tc_plan(Kc, F, P, true);
+        const int Pd = (int)pd;
+        void* X = cv.take((size_t)N * (H + 2 * Pd) * (W + 2 * Pd) * C * 2);
+        void* B = cv.take((size_t)P * bf16_pitch(F) * 2);
+        float* ws = t.splits > 1 ? (float*)cv.take((size_t)t.splits * Kc * F * 4) : nullptr;
+        if (!build) break;
+        cvt_pad_launch(s.ds, s.in[0], X, N, H, W, C, Pd, &L[(*nL)++]);
+        cvt_rows_launch(s.ds, s.in[1], B, P, F, &L[(*nL)++]);
+        TcConv g{};
+        g.C = (int)C; g.taps_x = (int)k; g.s = (int)st; g.Hg = (int)Ho; g.Wg = (int)Wo;
+        g.bw = bw; g.bh = bh; g.bn = bnn; g.phases = 1; g.off_y[0] = g.off_x[0] = 0;   // padding is in the copy
+        CUtensorMap map;
+        int rc = make_tmap_conv(&map, X, N, H + 2 * Pd, W + 2 * Pd, C, (int)st, bw, bh, bnn);
+        if (rc) return rc;
+        return tc_gemm_launches(c, s.ds, nullptr, B, Kc, F, P, t, s.in[0], s.in[1], s.out, nullptr, ws, L, nL, 3, true,
+                                &g, &map);
+      }
       if (bf16) {
         // dW = im2col(x)^T . dy with both operands MN-major: A = im2col(x) [P][pitch(Kc)],
         // B = dy [P][pitch(F)] in bf16 -- no transposition pass
@@ -843,7 +1000,7 @@ int build_xop_t(coex_ctx* c, const OpSpec& s, Launch* L, int* nL, size_t* ws_byt
         const int64_t gx = (units + 255) / 256;
         L[(*nL)++].set((void*)k_cvt_bf16, dim3((unsigned)(gx < kNumSMs * 16 ? (gx < 1 ? 1 : gx) : kNumSMs * 16), 1),
                        dim3(256), q);
-        return tc_gemm_launches(c, s.ds, A, B, Kc, F, P, t, s.in[0], s.in[1], s.out, nullptr, ws, L, nL, true, true);
+        return tc_gemm_launches(c, s.ds, A, B, Kc, F, P, t, s.in[0], s.in[1], s.out, nullptr, ws, L, nL, 1, true);
       }
       void* A = cv.take((size_t)P * Kc * es);
       if (!build) break;

@@ -42,6 +42,14 @@ CONV = [
     (OpKind.CONV2D_DW, {"conv": (4, 2, 1)}, [rt(2, 6, 6, 4), rt(2, 3, 3, 12)]),
     (OpKind.CONV2D, {"conv": (4, 2, 1)}, [rt(2, 6, 6, 4), rt(64, 12)]),
     (OpKind.CONV2D_T, {"conv": (4, 2, 1)}, [rt(2, 3, 3, 12), rt(64, 12)]),
+    # implicit-GEMM paths (C % 64 == 0): pixel blocks spanning rows / images, padding taps
+    (OpKind.CONV2D, {"conv": (4, 2, 1)}, [rt(16, 8, 8, 64), rt(1024, 32)]),
+    (OpKind.CONV2D, {"conv": (3, 1, 1)}, [rt(2, 16, 16, 128), rt(1152, 64)]),
+    (OpKind.CONV2D, {"conv": (4, 2, 1)}, [rt(2, 6, 6, 64), rt(1024, 16)]),
+    (OpKind.CONV2D_T, {"conv": (4, 2, 1)}, [rt(16, 4, 4, 128), rt(1024, 128)]),
+    (OpKind.CONV2D_T, {"conv": (4, 2, 1)}, [rt(2, 32, 32, 64), rt(48, 64)]),
+    (OpKind.CONV2D_DW, {"conv": (4, 2, 1)}, [rt(16, 8, 8, 64), rt(16, 4, 4, 32)]),
+    (OpKind.CONV2D_DW, {"conv": (3, 1, 1)}, [rt(2, 16, 16, 128), rt(2, 16, 16, 64)]),
 ]
 MATMUL_SPLIT = [  # bf16 MatMuls whose tile grid is too small: split-K slices
     (OpKind.MATMUL, {}, [rt(128, 8192), rt(8192, 1)]),
