@@ -138,7 +138,7 @@ def main():
     from paper_2201_09210_b200.workloads import C2, dcgan_program
     be = B200Backend(precision=a.precision)
     ops = record_step_ops(be, lambda n: dcgan_program(steps=n, **C2), 2)
-    rows = profile_ops(be, ops)
+    rows = profile_ops(be, ops, reps=int(os.environ.get("STEP_OPS_REPS", "10")))
     agg = by_kernel(rows)
     tot = sum(agg.values())
     print(f"{len(rows)} distinct ops, {sum(ops.values())} op executions per D+G step pair; kernel time {tot:.3f} ms")
