@@ -32,10 +32,11 @@ pinned mapped memory).
 * ``cpu_baseline``: the CPU oracle co-execution (oracle/, SPEC-faithful runner + f64
   kernels) on a bounded sample, rank 0 only.
 
-Multi-GPU: one process per GPU (torchrun).  C1 is data parallel (global batch 64*N, NCCL
-all-reduce nodes inside the pass graph, paper_2201_09210_b200/dp.py).  C2 has no sharding
-rule for batch-norm statistics yet: every rank trains an independent replica on its own
-data stream (weak scaling, no collective).  Time = max over ranks.
+Multi-GPU: one process per GPU (torchrun), data parallel (paper_2201_09210_b200/dp.py):
+every rank runs the host program on the global batch (C1: 64*N, C2: 128*N) while its device
+expands and trains on its own row shard; gradients (and the fetched loss) are all-reduced by
+NCCL nodes inside the pass graph.  C2 normalises with per-replica batch statistics (data-
+parallel training without synchronised batch norm).  Weak scaling; time = max over ranks.
 """
 
 from __future__ import annotations
@@ -317,8 +318,9 @@ def workload_setup(args, world: int):
     import numpy as np
     rr = np.random.default_rng(7)
     if args.workload == "c2":
-        src = dcgan_program(steps=100_000, **C2)
-        b, nz, img = C2["batch"], C2["nz"], C2["img"]
+        gb = C2["batch"] * world
+        src = dcgan_program(steps=100_000, **dict(C2, batch=gb))
+        b, nz, img = gb, C2["nz"], C2["img"]
         recs = {"z": [Tensor((b, nz), rr.uniform(-1, 1, (b, nz))) for _ in range(2)],
                 "img": [Tensor((b, img, img, 3), rr.uniform(-1, 1, (b, img, img, 3))) for _ in range(2)]}
         for name, shp in _c2_weight_shapes().items():
@@ -327,11 +329,13 @@ def workload_setup(args, world: int):
         cfg = {"workload": "C2 DCGAN 64x64 (ngf=ndf=64, nz=100; D: 4 strided convs + BN + leaky-relu, G: dense + "
                            "4 transposed convs + BN + relu, tanh), batch 128/GPU, D and G iterations alternating "
                            "through a SwitchCase on native mod(step, 2), hand-written backward, SGD",
-               "global_batch": b * world, "per_gpu_batch": b,
-               "parallelism": f"dp{world}" if world == 1 else f"{world} independent replicas (no BN sharding rule)",
+               "global_batch": gb, "per_gpu_batch": C2["batch"],
+               "parallelism": f"dp{world}" + ("" if world == 1 else
+                                              " (batch-sharded; per-replica batch-norm statistics; NCCL all-reduce "
+                                              "of weight / BN-parameter gradients and the loss in the pass graph)"),
                "algorithmic_flops_per_d_step": fl["d_step"], "algorithmic_flops_per_g_step": fl["g_step"]}
-        h2d = (b * nz + b * img * img * 3) * 8
-        return src, SyntheticDataset(1000 + 7919 * dist_env()[0]), recs, h2d, cfg, None
+        h2d = (C2["batch"] * nz + C2["batch"] * img * img * 3) * 8      # this rank's shard
+        return src, SyntheticDataset(1000), recs, h2d, cfg, gb
     gbatch = C1["batch"] * world
     cfg1 = dict(C1, batch=gbatch)
     src = c1_program(steps=100_000, **cfg1)

@@ -21,8 +21,18 @@ assigning a sharded value to a variable, slicing a replicated batch tensor)
 makes the program run replicated: every rank computes the global batch, no
 collective, still correct.
 
+Extension ops (C2): convolutions of a row-sharded NHWC activation with a
+replicated weight stay row-sharded (S0); a weight gradient ``conv2d_dw`` of two
+row-sharded operands, ``sum_rows`` and ``bn_dgamma`` over row-sharded values are
+P+; ``batchnorm`` / ``batchnorm_dx`` of a row-sharded activation normalise with
+the statistics of the rank's own rows (per-replica batch statistics -- the
+semantics of data-parallel training without synchronised batch norm), so their
+results stay S0.
+
 Parity: DP results equal the single-device run up to summation order
 (tolerance, not bitwise) -- tests/test_dp_gloo.py checks world size 2 on CPU.
+With per-replica batch-norm statistics the equality holds when every rank's rows
+have the statistics of the global batch (the test feeds duplicated halves).
 """
 
 from __future__ import annotations
@@ -38,7 +48,9 @@ R, S0, S1, PSUM, PAVG = "R", "S0", "S1", "P+", "P~"
 PARTIAL = (PSUM, PAVG)
 ELEMENTWISE = (OpKind.ADD, OpKind.SUB, OpKind.MUL)
 LINEAR_UNARY = (OpKind.NEG,)
-NONLINEAR = (OpKind.RELU, OpKind.SIGMOID)
+NONLINEAR = (OpKind.RELU, OpKind.SIGMOID, OpKind.TANH, OpKind.LEAKY_RELU)
+# extension ops (C2): row-wise binary nonlinear ops keep the row sharding of their operands
+ROW_BINARY = (OpKind.RELU_GRAD, OpKind.LEAKY_RELU_GRAD, OpKind.BCE_TERM)
 
 
 @dataclass
@@ -145,6 +157,9 @@ class _Prop:
             return ins[0]
         if k in LINEAR_UNARY:
             return ins[0]
+        if k in (OpKind.CONV2D, OpKind.CONV2D_T, OpKind.CONV2D_DW, OpKind.BATCHNORM, OpKind.BATCHNORM_DX,
+                 OpKind.BN_DGAMMA, OpKind.SUM_ROWS) or k in ROW_BINARY:
+            return self._ext(x, ins)
         if k in ELEMENTWISE:
             a, b = ins
             scalar = [self._rank0(bb) for bb in x.inputs]
@@ -219,6 +234,55 @@ class _Prop:
                 return self.op(x)
             raise Unshardable(f"matmul of {a} x {b}")
         raise Unshardable(f"no sharding rule for {k.value}")
+
+    def _ext(self, x: ExecOp, ins):
+        """Sharding rules of the C2 extension ops (module docstring)."""
+        k = x.kind
+        for i, st in enumerate(ins):               # every extension op needs complete operands
+            if st in PARTIAL:
+                self.needs_r_binding(x.inputs[i])
+        ins = [R if st in PARTIAL else st for st in ins]
+        if k in ROW_BINARY:
+            a, b = ins
+            if a == b:
+                return a
+            if S1 in (a, b):
+                raise Unshardable(f"node {x.node_id}: column-sharded operand of {k.value}")
+            r_side = 1 if a != R else 0
+            if not self._rank0(x.inputs[r_side]):
+                raise Unshardable(f"node {x.node_id}: replicated tensor meets a sharded one")
+            return a if a != R else b
+        if k in (OpKind.CONV2D, OpKind.CONV2D_T):
+            xs, w = ins
+            if w != R:
+                raise Unshardable(f"node {x.node_id}: sharded convolution weight")
+            if xs == S1:
+                raise Unshardable(f"node {x.node_id}: column-sharded convolution input")
+            return xs
+        if k is OpKind.CONV2D_DW:
+            xs, dy = ins
+            if xs == S0 and dy == S0:
+                return PSUM
+            if xs == R and dy == R:
+                return R
+            raise Unshardable(f"node {x.node_id}: weight gradient of {xs} x {dy}")
+        if k in (OpKind.BATCHNORM, OpKind.BATCHNORM_DX):
+            xs = ins[0]
+            if ins[1] != R or (k is OpKind.BATCHNORM and ins[2] != R):
+                raise Unshardable(f"node {x.node_id}: sharded batch-norm parameters")
+            if k is OpKind.BATCHNORM_DX and ins[2] != xs:
+                raise Unshardable(f"node {x.node_id}: batch-norm gradient sharded unlike its input")
+            if xs == S1:
+                raise Unshardable(f"node {x.node_id}: column-sharded batch-norm input")
+            return xs
+        # BN_DGAMMA / SUM_ROWS: column sums over the rows
+        if any(st == S1 for st in ins):
+            raise Unshardable(f"node {x.node_id}: column-sharded operand of {k.value}")
+        if all(st == R for st in ins):
+            return R
+        if any(st == R for st in ins):
+            raise Unshardable(f"node {x.node_id}: {k.value} of replicated and sharded operands")
+        return PSUM
 
     def _rank0(self, b):
         shp = self.feed_shapes.get(b.slot) if b.fed else self.node_shapes.get(b.cands[0])

@@ -16,10 +16,26 @@ from oracle.cpu_backend import CpuBackend
 from paper_2201_09210_b200 import coexec, lang
 from paper_2201_09210_b200.dataset import SyntheticDataset
 from paper_2201_09210_b200.dp import DPGroup
-from paper_2201_09210_b200.workloads import c1_program
+from paper_2201_09210_b200.tensor import Tensor
+from paper_2201_09210_b200.workloads import c1_program, dcgan_program
 
 SMALL_C1 = c1_program(steps=12, batch=8, hidden=16, din=12, dout=3)
 BATCH = 8
+SMALL_C2 = dcgan_program(steps=6, batch=8, nz=6, ngf=4, ndf=4, img=16)
+
+
+class DupHalves(SyntheticDataset):
+    """Batch inputs whose second half repeats the first: per-replica batch-norm statistics
+    (C2 data parallelism) then equal the global-batch statistics, so the DP run must match
+    the single-process run at the global batch."""
+
+    def next(self, name, shape, step):
+        t = super().next(name, shape, step)
+        if len(shape) >= 1 and shape[0] == BATCH:
+            d = t.materialize().data.copy() if hasattr(t, "materialize") else np.array(t.data)
+            d[BATCH // 2:] = d[:BATCH // 2]
+            return Tensor(shape, d)
+        return t
 
 
 def _free_port():
@@ -30,7 +46,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, src, out):
+def _worker(rank, world, port, src, out, dup=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
 
@@ -42,19 +58,20 @@ def _worker(rank, world, port, src, out):
         return t.numpy()
 
     be = CpuBackend(dp=DPGroup(rank, world, BATCH, allreduce))
-    o = coexec.Orchestrator(lang.parse(src), SyntheticDataset(0), coexec.Mode.coexec, coexec.RunConfig(), be)
+    ds = DupHalves(0) if dup else SyntheticDataset(0)
+    o = coexec.Orchestrator(lang.parse(src), ds, coexec.Mode.coexec, coexec.RunConfig(), be)
     res, st = o.run()
     plans = [(p.replicated, p.reason, p.allreduce_nodes, sorted(p.sharded_slots)) for p in be.dp_plans]
     out[rank] = (res.lines, {k: v.data for k, v in res.vars.items()}, st.counters(), st.decision_log, plans)
     dist.destroy_process_group()
 
 
-def run_dp(src, world=2):
+def run_dp(src, world=2, dup=False):
     ctx = mp.get_context("spawn")
     mgr = ctx.Manager()
     out = mgr.dict()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, src, out)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, src, out, dup)) for r in range(world)]
     for p in procs:
         p.start()
     for p in procs:
@@ -95,3 +112,23 @@ steps 6 {
     out = run_dp(src)
     assert out[0][4][-1][0] is True                   # fetching a sharded activation -> replicated
     assert out[0][0] == ref.lines == out[1][0]
+
+
+def test_dp2_dcgan_matches_global_batch():
+    """C2 (DCGAN) data parallel at world size 2: activations row-sharded through the
+    convolutions, per-replica batch-norm statistics, weight / gamma / beta gradients
+    all-reduced (P+), the loss averaged (P~).  With duplicated batch halves the result
+    equals the single-process global-batch run."""
+    ref, ref_st = coexec.run(lang.parse(SMALL_C2), DupHalves(0), "coexec", backend=CpuBackend())
+    out = run_dp(SMALL_C2, dup=True)
+    r0, r1 = out[0], out[1]
+    assert r0[0] == r1[0] and r0[3] == r1[3] and r0[2] == r1[2]
+    assert r0[2] == ref_st.counters()
+    plans = r0[4]
+    assert plans and not any(p[0] for p in plans), plans   # every specialisation sharded
+    assert max(len(p[2]) for p in plans) >= 8               # weight, BN-parameter and loss reductions
+    for a, b in zip(ref.lines, r0[0]):
+        assert abs(float(a) - float(b)) <= 1e-9 * max(1.0, abs(float(a))), (a, b)
+    for k, t in ref.vars.items():
+        np.testing.assert_allclose(r0[1][k], t.data, rtol=1e-8, atol=1e-11)
+        np.testing.assert_array_equal(r0[1][k], r1[1][k])

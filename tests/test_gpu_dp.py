@@ -30,3 +30,25 @@ def test_forced_dp_nccl_in_graph_bitwise():
     assert [float(x) for x in got.lines] == pytest.approx([float(x) for x in ref.lines], rel=1e-12)
     for k, t in ref.vars.items():
         assert abs(got.vars[k].data - t.data).max() <= 1e-12 * max(1.0, abs(t.data).max())
+
+
+@pytest.mark.parametrize("prec,tol", [("f64", 1e-10), ("fp32", 1e-4)])
+def test_forced_dp_dcgan(prec, tol):
+    """C2 (DCGAN) with a forced 1-rank sharding: conv / batch-norm sharding rules, NCCL
+    all-reduce nodes for every weight, gamma / beta gradient and the loss inside both
+    SwitchCase bodies; results within the precision's tolerance of the oracle."""
+    from paper_2201_09210_b200.workloads import C2_SMALL, dcgan_program
+    from test_gpu_coexec import assert_close, run
+    src = dcgan_program(steps=6, **C2_SMALL)
+    ref, ref_st, _ = run(src, "coexec", CpuBackend())
+    be = B200Backend(precision=prec, dp=DPGroup(0, 1, C2_SMALL["batch"], force=True))
+    try:
+        o = coexec.Orchestrator(lang.parse(src), SyntheticDataset(0), coexec.Mode.coexec, coexec.RunConfig(), be)
+        got, st = o.run()
+        plan = o.compiled.last_plan
+        assert plan.dp is not None and not plan.dp.replicated, plan.dp and plan.dp.reason
+        assert len(plan.dp.allreduce_nodes) >= 8
+    finally:
+        be.close()
+    assert st.counters() == ref_st.counters()
+    assert_close(ref, got, tol, False)
