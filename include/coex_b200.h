@@ -62,6 +62,21 @@ enum coex_opkind {
   COEX_BN_DGAMMA,          /* (x, dy) -> [C] = sum_rows(dy * xhat) */
   COEX_SUM_ROWS,           /* (x [..,C]) -> [C] */
   COEX_TANH, COEX_LEAKY_RELU, COEX_RELU_GRAD, COEX_LEAKY_RELU_GRAD, COEX_BCE_TERM,
+  /* transformer extension (config C4): coex_attrs.dims[0] = vocab (embedding_dw),
+   * coex_attrs.value = softmax scale (causal_softmax, softmax_grad) */
+  COEX_TO_INDEX = 26,      /* (u, V) -> clip(floor((u+1)/2*V), 0, V-1) */
+  COEX_EMBEDDING,          /* (table [V, d], ids [..]) -> [.., d] */
+  COEX_EMBEDDING_DW,       /* (ids [..], dy [.., d]) -> [V, d] scatter-add */
+  COEX_LAYERNORM,          /* (x [.., d], gamma [d], beta [d]) */
+  COEX_LAYERNORM_DX,       /* (x, gamma, dy) -> dx */
+  COEX_LN_DGAMMA,          /* (x, dy) -> [d] */
+  COEX_BIAS_ADD,           /* (x [.., d], b [d]) */
+  COEX_GELU, COEX_GELU_GRAD,
+  COEX_BMM, COEX_BMM_NT, COEX_BMM_TN,   /* batched a.b, a.b^T, a^T.b ([B, ., .]) */
+  COEX_CAUSAL_SOFTMAX,     /* (x [.., T, T]) -> row softmax of scale*x over j <= i */
+  COEX_SOFTMAX_GRAD,       /* (y, dy) -> scale*y*(dy - sum(dy*y)) */
+  COEX_CROSS_ENTROPY,      /* (logits [R, V], ids [R]) -> mean loss */
+  COEX_CROSS_ENTROPY_GRAD, /* -> (softmax - onehot) / R */
   COEX_NUM_KINDS
 };
 

@@ -24,6 +24,16 @@ reference; written in tensor.py's style (explicit orders):
   variance of the centred values, eps = 1e-5.
 * TANH, LEAKY_RELU (slope 0.2), RELU_GRAD, LEAKY_RELU_GRAD, BCE_TERM
   (max(x,0) - x*t + log1p(exp(-|x|))) elementwise.
+* C4 (GPT-2): TO_INDEX(u, V) = clip(floor((u+1)/2*V), 0, V-1); EMBEDDING row gather
+  (ids clipped to the table); EMBEDDING_DW scatter-add in row order from +0.0;
+  LAYERNORM / LAYERNORM_DX / LN_DGAMMA over the last axis (sequential row sums,
+  eps 1e-5); BIAS_ADD (last-axis broadcast); GELU (tanh approximation) and its
+  derivative; BMM / BMM_NT / BMM_TN = per-batch MATMUL (sequential k) of a.b,
+  a.b^T, a^T.b; CAUSAL_SOFTMAX(x, scale): row softmax of scale*x over j <= i of
+  each trailing [T, T] block (masked entries 0, max-subtracted, exp then
+  sequential sum); SOFTMAX_GRAD(y, dy, scale) = scale*y*(dy - sum_j dy*y);
+  CROSS_ENTROPY(logits, ids) = mean over rows of logsumexp - logit[id];
+  CROSS_ENTROPY_GRAD = (softmax - onehot) / R.
 """
 
 from __future__ import annotations
@@ -31,7 +41,8 @@ from __future__ import annotations
 import numpy as np
 
 from paper_2201_09210_b200.errors import BadAttrs, ShapeMismatch
-from paper_2201_09210_b200.tensor import BN_EPS, LEAKY_SLOPE, OpKind, Tensor, infer_shape
+from paper_2201_09210_b200.tensor import (BN_EPS, GELU_C, LEAKY_SLOPE, LN_EPS, OpKind, Tensor,
+                                          infer_shape)
 
 
 def matmul_seq(a: np.ndarray, b: np.ndarray) -> np.ndarray:
@@ -130,6 +141,9 @@ def ext_kernel(kind: OpKind, attrs: dict, x: list, out_shape) -> np.ndarray:
         t = dy - col_sum_seq(dy) / r
         t = t - xhat * (col_sum_seq(dy * xhat) / r)
         return (t * (x[1] * rstd)).reshape(out_shape)
+    t = transformer_kernel(kind, attrs, x, out_shape)
+    if t is not None:
+        return t
     a = x[0]
     if kind is OpKind.TANH:
         return np.tanh(a)
@@ -144,6 +158,100 @@ def ext_kernel(kind: OpKind, attrs: dict, x: list, out_shape) -> np.ndarray:
         with np.errstate(over="ignore"):
             return np.broadcast_to((np.maximum(a, 0.0) - a * b) + np.log1p(np.exp(-np.abs(a))), out_shape)
     raise BadAttrs(f"unknown op kind {kind!r}")  # pragma: no cover
+
+
+def row_stats(x2: np.ndarray):
+    """Per-row mean / rstd over the last axis: sequential sums from +0.0."""
+    d = x2.shape[1]
+    mean = (np.cumsum(x2, axis=1)[:, -1] + 0.0) / d
+    dev = x2 - mean[:, None]
+    var = (np.cumsum(dev * dev, axis=1)[:, -1] + 0.0) / d
+    return dev, 1.0 / np.sqrt(var + LN_EPS)
+
+
+def _ids(idx: np.ndarray, v: int) -> np.ndarray:
+    return np.clip(np.floor(idx), 0, v - 1).astype(np.int64)
+
+
+def transformer_kernel(kind: OpKind, attrs: dict, x: list, out_shape):
+    if kind is OpKind.TO_INDEX:
+        v = np.broadcast_to(x[1], np.broadcast_shapes(x[0].shape, x[1].shape))
+        return np.clip(np.floor((x[0] + 1.0) * 0.5 * v), 0.0, v - 1.0)
+    if kind is OpKind.GELU:
+        a = x[0]
+        return 0.5 * a * (1.0 + np.tanh(GELU_C * (a + 0.044715 * a * a * a)))
+    if kind is OpKind.GELU_GRAD:
+        a, g = x
+        t = np.tanh(GELU_C * (a + 0.044715 * a * a * a))
+        d = 0.5 * (1.0 + t) + 0.5 * a * (1.0 - t * t) * GELU_C * (1.0 + 3.0 * 0.044715 * a * a)
+        return np.broadcast_to(g * d, out_shape)
+    if kind is OpKind.EMBEDDING:
+        table, idx = x
+        return table[_ids(idx, table.shape[0])]
+    if kind is OpKind.EMBEDDING_DW:
+        idx, dy = x
+        v = attrs["dims"][0]
+        ids = _ids(idx, v).reshape(-1)
+        g = dy.reshape(ids.size, -1)
+        out = np.zeros((v, g.shape[1]))
+        for r in range(ids.size):            # row order, one rounded add per row
+            out[ids[r]] += g[r]
+        return out + 0.0
+    if kind in (OpKind.LAYERNORM, OpKind.LAYERNORM_DX, OpKind.LN_DGAMMA):
+        d = x[0].shape[-1]
+        x2 = x[0].reshape(-1, d)
+        dev, rstd = row_stats(x2)
+        xhat = dev * rstd[:, None]
+        if kind is OpKind.LAYERNORM:
+            return ((xhat * x[1]) + x[2]).reshape(out_shape)
+        dy = x[-1].reshape(-1, d)
+        if kind is OpKind.LN_DGAMMA:
+            return col_sum_seq(dy * xhat)
+        dxh = dy * x[1]
+        m1 = (np.cumsum(dxh, axis=1)[:, -1] + 0.0) / d
+        m2 = (np.cumsum(dxh * xhat, axis=1)[:, -1] + 0.0) / d
+        return (((dxh - m1[:, None]) - xhat * m2[:, None]) * rstd[:, None]).reshape(out_shape)
+    if kind is OpKind.BIAS_ADD:
+        return x[0] + x[1]
+    if kind in (OpKind.BMM, OpKind.BMM_NT, OpKind.BMM_TN):
+        a, b = x
+        out = np.empty(out_shape)
+        for i in range(a.shape[0]):
+            ai = a[i].T if kind is OpKind.BMM_TN else a[i]
+            bi = b[i].T if kind is OpKind.BMM_NT else b[i]
+            out[i] = matmul_seq(np.ascontiguousarray(ai), np.ascontiguousarray(bi))
+        return out
+    if kind is OpKind.CAUSAL_SOFTMAX:
+        sc = attrs["value"]
+        t = x[0].shape[-1]
+        z = x[0].reshape(-1, t, t) * sc
+        mask = np.tril(np.ones((t, t), dtype=bool))
+        zm = np.where(mask, z, -np.inf)
+        e = np.exp(zm - zm.max(axis=2, keepdims=True))
+        s_ = np.cumsum(e, axis=2)[:, :, -1:] + 0.0
+        return (e / s_).reshape(out_shape)
+    if kind is OpKind.SOFTMAX_GRAD:
+        sc = attrs["value"]
+        y, dy = x
+        t = y.shape[-1]
+        y3, d3 = y.reshape(-1, t), dy.reshape(-1, t)
+        dot = np.cumsum(d3 * y3, axis=1)[:, -1:] + 0.0
+        return (sc * (y3 * (d3 - dot))).reshape(out_shape)
+    if kind in (OpKind.CROSS_ENTROPY, OpKind.CROSS_ENTROPY_GRAD):
+        logits, idx = x
+        r, v = logits.shape
+        ids = _ids(idx, v)
+        mx = logits.max(axis=1, keepdims=True)
+        e = np.exp(logits - mx)
+        s_ = np.cumsum(e, axis=1)[:, -1:] + 0.0
+        if kind is OpKind.CROSS_ENTROPY:
+            lse = np.log(s_[:, 0]) + mx[:, 0]
+            loss = lse - logits[np.arange(r), ids]
+            return np.array(sum_seq(loss) / r)
+        g = e / s_
+        g[np.arange(r), ids] -= 1.0
+        return g / r
+    return None
 
 
 _BINARY = {OpKind.ADD: np.add, OpKind.SUB: np.subtract, OpKind.MUL: np.multiply}

@@ -142,6 +142,11 @@ def _attrs(kind: OpKind, attrs: dict) -> CoexAttrs:
         at.value = float(attrs["value"])
     elif kind in CONV_KINDS:
         dims = attrs["conv"]
+    elif kind is OpKind.EMBEDDING_DW:
+        dims = attrs["dims"]
+    elif kind in (OpKind.CAUSAL_SOFTMAX, OpKind.SOFTMAX_GRAD):
+        dims = ()
+        at.value = float(attrs["value"])
     else:
         dims = ()
     if len(dims) > MAX_RANK:

@@ -146,6 +146,8 @@ struct TcGemmParams {
   float* raw;                // non-null: write here (no publication) -- scratch / split-K slices
   int splits;                // split-K: CTA (tile, split) covers k-blocks of its slice, raw + split*M*N
   TcConv cv;
+  int batch;                 // batched GEMM (bmm): 3-D tensor maps {inner, rows, batch}; C + b * c_bstride
+  long long c_bstride;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -209,6 +211,14 @@ __host__ __device__ constexpr uint32_t idesc_bf16_f32(int M, int N, bool a_mn = 
          ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::
+          "r"(smem_u32(dst)),
+      "l"((uint64_t)map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+
 __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2,
                                             int c3) {
   asm volatile(
@@ -263,14 +273,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc(const __grid_constant
   const long long tiles_m = (p.M + TC_BM - 1) / TC_BM;
   const int splits = p.splits > 1 ? p.splits : 1;
   const int phases = AMODE == 2 ? p.cv.phases : 1;
-  const long long items = tiles_m * tiles_n * splits * phases;
+  const int nbat = p.batch > 1 ? p.batch : 1;
+  const long long items = tiles_m * tiles_n * splits * phases * nbat;
   const int nk_all = (int)((p.K + TC_BK - 1) / TC_BK);
   const long long group = (long long)TC_GROUP_M * tiles_n;
 
   // item -> (m0, n0, split, first k-block, k-block count); grouped rasterisation of tiles
   auto decode = [&](long long it, int& m0, int& n0, int& split, int& kb0, int& nk) {
     split = (int)(it % splits);
-    const long long t = (it / splits) / phases;
+    const long long t = ((it / splits) / phases) % (tiles_m * tiles_n);
     const long long first_m = (t / group) * TC_GROUP_M;
     const long long gm = min((long long)TC_GROUP_M, tiles_m - first_m);
     m0 = (int)((first_m + (t % group) % gm) * TC_BM);
@@ -317,6 +328,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc(const __grid_constant
         int m0, n0, split, kb0, nk;
         decode(it, m0, n0, split, kb0, nk);
         const int cph = (int)((it / splits) % phases);     // sub-pixel phase of this item
+        const int bi = (int)(((it / splits) / phases) / (tiles_m * tiles_n));   // batch of this item
         for (int kb = 0; kb < nk; ++kb, ++kbg) {
           const int s = (int)(kbg % STAGES);
           const uint32_t ph = (uint32_t)((kbg / STAGES) & 1);
@@ -347,18 +359,24 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc(const __grid_constant
             }
           } else if constexpr (A_MN) {
 #pragma unroll
-            for (int h = 0; h < TC_BM / 64; ++h)
-              tma_load_2d(sA + s * TC_A_BYTES + h * 8192, &p.tmA, &full[s], m0 + 64 * h, kk);
+            for (int h = 0; h < TC_BM / 64; ++h) {
+              if (nbat > 1) tma_load_3d(sA + s * TC_A_BYTES + h * 8192, &p.tmA, &full[s], m0 + 64 * h, kk, bi);
+              else tma_load_2d(sA + s * TC_A_BYTES + h * 8192, &p.tmA, &full[s], m0 + 64 * h, kk);
+            }
           } else {
-            tma_load_2d(sA + s * TC_A_BYTES, &p.tmA, &full[s], kk, m0);
+            if (nbat > 1) tma_load_3d(sA + s * TC_A_BYTES, &p.tmA, &full[s], kk, m0, bi);
+            else tma_load_2d(sA + s * TC_A_BYTES, &p.tmA, &full[s], kk, m0);
           }
           const int brow = (int)(cph * p.cv.b_rows) + kk;
           if constexpr (B_MN) {
 #pragma unroll
-            for (int h = 0; h < BN / 64; ++h)
-              tma_load_2d(sB + s * B_BYTES + h * 8192, &p.tmB, &full[s], n0 + 64 * h, brow);
+            for (int h = 0; h < BN / 64; ++h) {
+              if (nbat > 1) tma_load_3d(sB + s * B_BYTES + h * 8192, &p.tmB, &full[s], n0 + 64 * h, brow, bi);
+              else tma_load_2d(sB + s * B_BYTES + h * 8192, &p.tmB, &full[s], n0 + 64 * h, brow);
+            }
           } else {
-            tma_load_2d(sB + s * B_BYTES, &p.tmB, &full[s], brow, n0);
+            if (nbat > 1) tma_load_3d(sB + s * B_BYTES, &p.tmB, &full[s], brow, n0, bi);
+            else tma_load_2d(sB + s * B_BYTES, &p.tmB, &full[s], brow, n0);
           }
         }
       }
@@ -420,7 +438,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc(const __grid_constant
       decode(it, m0, n0, split, kb0, nk);
       const int a = li & 1;
       const uint32_t aph = (uint32_t)((li >> 1) & 1);
-      float* C = p.raw != nullptr ? p.raw + (long long)split * p.M * p.N : Cout;
+      const int bi = (int)(((it / splits) / phases) / (tiles_m * tiles_n));
+      float* C = (p.raw != nullptr ? p.raw + (long long)split * p.M * p.N : Cout) + (long long)bi * p.c_bstride;
       const int cph = (int)((it / splits) % phases);
       mbar_wait(&tfull[a], aph);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");

@@ -179,7 +179,7 @@ __device__ __forceinline__ void publish_late(const Out& o, void* out) {
   if (threadIdx.x == 0) {
     __threadfence();
     unsigned int prev = atomicAdd(o.late, 1u);
-    if (prev == gridDim.x - 1) {
+    if (prev == gridDim.x * gridDim.y * gridDim.z - 1) {
       for (int i = 0; i < o.npub; ++i) *o.pub[i] = out;
       *o.late = 0u;
     }
@@ -198,10 +198,14 @@ __device__ __forceinline__ void count_op(DevState* ds) {
 // Extension elementwise ops (configs C2-C5, oracle/kernels.py ext_kernel): TANH, LEAKY_RELU
 // (slope 0.2), RELU_GRAD(x, dy), LEAKY_RELU_GRAD(x, dy), BCE_TERM(x, t).
 enum EwOp { EW_ADD = 0, EW_SUB = 1, EW_MUL = 2, EW_NEG = 3, EW_RELU = 4, EW_SIGMOID = 5, EW_COPY = 6,
-            EW_TANH = 7, EW_LRELU = 8, EW_RELU_GRAD = 9, EW_LRELU_GRAD = 10, EW_BCE = 11 };
+            EW_TANH = 7, EW_LRELU = 8, EW_RELU_GRAD = 9, EW_LRELU_GRAD = 10, EW_BCE = 11,
+            EW_TO_INDEX = 12, EW_GELU_GRAD = 13, EW_GELU = 14 };
+constexpr double kGeluK = 0.7978845608028654;   // sqrt(2/pi)
 constexpr double kLeakySlope = 0.2;
 
-__host__ __device__ __forceinline__ bool ew_binary(int op) { return op <= EW_MUL || op >= EW_RELU_GRAD; }
+__host__ __device__ __forceinline__ bool ew_binary(int op) {
+  return op <= EW_MUL || (op >= EW_RELU_GRAD && op <= EW_GELU_GRAD);
+}
 
 __device__ __forceinline__ double ew_apply(int op, double a, double b) {
   switch (op) {
@@ -216,6 +220,15 @@ __device__ __forceinline__ double ew_apply(int op, double a, double b) {
     case EW_RELU_GRAD: return a > 0.0 ? b : 0.0;
     case EW_LRELU_GRAD: return a > 0.0 ? b : __dmul_rn(b, kLeakySlope);
     case EW_BCE: return __dadd_rn(__dsub_rn(a > 0.0 ? a : 0.0, __dmul_rn(a, b)), log1p(exp(-fabs(a))));
+    case EW_TO_INDEX: {
+      const double v = floor((a + 1.0) * 0.5 * b);
+      return v < 0.0 ? 0.0 : (v > b - 1.0 ? b - 1.0 : v);
+    }
+    case EW_GELU: return 0.5 * a * (1.0 + tanh(kGeluK * (a + 0.044715 * a * a * a)));
+    case EW_GELU_GRAD: {
+      const double t = tanh(kGeluK * (a + 0.044715 * a * a * a));
+      return b * (0.5 * (1.0 + t) + 0.5 * a * (1.0 - t * t) * kGeluK * (1.0 + 3.0 * 0.044715 * a * a));
+    }
     default: return a;
   }
 }
@@ -232,6 +245,15 @@ __device__ __forceinline__ float ew_apply(int op, float a, float b) {
     case EW_RELU_GRAD: return a > 0.0f ? b : 0.0f;
     case EW_LRELU_GRAD: return a > 0.0f ? b : __fmul_rn(b, (float)kLeakySlope);
     case EW_BCE: return __fadd_rn(__fsub_rn(a > 0.0f ? a : 0.0f, __fmul_rn(a, b)), log1pf(expf(-fabsf(a))));
+    case EW_TO_INDEX: {
+      const float v = floorf((a + 1.0f) * 0.5f * b);
+      return v < 0.0f ? 0.0f : (v > b - 1.0f ? b - 1.0f : v);
+    }
+    case EW_GELU: return 0.5f * a * (1.0f + tanhf((float)kGeluK * (a + 0.044715f * a * a * a)));
+    case EW_GELU_GRAD: {
+      const float t = tanhf((float)kGeluK * (a + 0.044715f * a * a * a));
+      return b * (0.5f * (1.0f + t) + 0.5f * a * (1.0f - t * t) * (float)kGeluK * (1.0f + 3.0f * 0.044715f * a * a));
+    }
     default: return a;
   }
 }
@@ -424,6 +446,7 @@ struct MatmulParams {
   int trans_a, trans_b;
   long long lda, ldb;       // row stride of the stored operand
   Out out;
+  long long sa, sb, sc;     // batched (blockIdx.y = batch): element strides of A, B, C per batch
 };
 
 template <typename T, int BM, int BN, int BK, int RM, int RN, bool EXACT>
@@ -518,11 +541,14 @@ __global__ void __launch_bounds__((BM / RM) * (BN / RN)) k_matmul_pipe(MatmulPar
   COEX_PDL_ENTER();
   stamp(p.ds, SK_MATMUL);
   if (skip(p.ds)) return;
-  const T* A = res<T>(p.a);
-  const T* B = res<T>(p.b);
-  T* C = pick_out<T>(p.out, A, B);
-  publish_early(p.out, C);
-  count_op(p.ds);
+  const T* A0 = res<T>(p.a);
+  const T* B0 = res<T>(p.b);
+  T* C0 = pick_out<T>(p.out, A0, B0);
+  publish_early(p.out, C0);
+  if (blockIdx.y == 0) count_op(p.ds);
+  const T* A = A0 + blockIdx.y * p.sa;
+  const T* B = B0 + blockIdx.y * p.sb;
+  T* C = C0 + blockIdx.y * p.sc;
   constexpr int TX = BN / RN, TY = BM / RM, NT = TX * TY;
   __shared__ __align__(16) T sA[STAGES][BK][BM + 1];
   __shared__ __align__(16) T sB[STAGES][BK][BN + 1];
@@ -617,7 +643,7 @@ __global__ void __launch_bounds__((BM / RM) * (BN / RN)) k_matmul_pipe(MatmulPar
         if (gm < p.M && gn < p.N) C[gm * p.N + gn] = acc[i][j];
       }
   }
-  publish_late(p.out, C);
+  publish_late(p.out, C0);
 }
 
 // Parity SUM / MEAN with shared-memory staging: all threads stream 2048-element

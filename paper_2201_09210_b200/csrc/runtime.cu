@@ -30,6 +30,7 @@
 #include "kernels.cuh"
 #include "gemm_tc.cuh"
 #include "ext_ops.cuh"
+#include "xformer_ops.cuh"
 
 #include <cudaTypedefs.h>
 #include <dlfcn.h>
@@ -229,7 +230,8 @@ int infer_ext(int kind, const coex_attrs* at, const TRec* in, int* ndim, int64_t
 
 int infer(int kind, const coex_attrs* at, int nin, const TRec* in, int* ndim, int64_t* shape) {
   static const int arity[] = {2, 2, 2, 2, 1, 1, 1, 1, 1, 1, 1, 0, 0, 1,
-                              2, 2, 2, 3, 3, 2, 1, 1, 1, 2, 2, 2};
+                              2, 2, 2, 3, 3, 2, 1, 1, 1, 2, 2, 2,
+                              2, 2, 2, 3, 3, 2, 2, 1, 2, 2, 2, 2, 1, 2, 2, 2};
   static_assert(sizeof(arity) / sizeof(arity[0]) == COEX_NUM_KINDS, "arity table");
   if (kind < 0 || kind >= COEX_NUM_KINDS) return fail(COEX_BAD_ATTRS, "unknown op kind");
   if (nin != arity[kind]) return fail(COEX_BAD_ATTRS, "wrong number of tensor inputs");
@@ -300,11 +302,11 @@ int infer_ext(int kind, const coex_attrs* at, const TRec* in, int* ndim, int64_t
     return true;
   };
   switch (kind) {
-    case COEX_TANH: case COEX_LEAKY_RELU:
+    case COEX_TANH: case COEX_LEAKY_RELU: case COEX_GELU:
       *ndim = in[0].ndim;
       memcpy(shape, in[0].shape, sizeof(int64_t) * in[0].ndim);
       return COEX_OK;
-    case COEX_RELU_GRAD: case COEX_LEAKY_RELU_GRAD: case COEX_BCE_TERM: {
+    case COEX_RELU_GRAD: case COEX_LEAKY_RELU_GRAD: case COEX_BCE_TERM: case COEX_TO_INDEX: case COEX_GELU_GRAD: {
       const TRec &a = in[0], &b = in[1];
       if (!(same(a, b) || a.ndim == 0 || b.ndim == 0)) return fail(COEX_SHAPE_MISMATCH, "elementwise: incompatible shapes");
       const TRec& r = (same(a, b) || b.ndim == 0) ? a : b;
@@ -329,6 +331,84 @@ int infer_ext(int kind, const coex_attrs* at, const TRec* in, int* ndim, int64_t
       if (kind == COEX_BATCHNORM_DX && !same(x, in[2])) return fail(COEX_SHAPE_MISMATCH, "batchnorm_dx: dy differs from x");
       *ndim = x.ndim;
       memcpy(shape, x.shape, sizeof(int64_t) * x.ndim);
+      return COEX_OK;
+    }
+    case COEX_EMBEDDING: {
+      if (in[0].ndim != 2 || in[1].ndim + 1 > COEX_MAX_RANK) return fail(COEX_SHAPE_MISMATCH, "embedding: table [V, d] required");
+      *ndim = in[1].ndim + 1;
+      memcpy(shape, in[1].shape, sizeof(int64_t) * in[1].ndim);
+      shape[in[1].ndim] = in[0].shape[1];
+      return COEX_OK;
+    }
+    case COEX_EMBEDDING_DW: {
+      const TRec &ids = in[0], &dy = in[1];
+      if (at == nullptr || at->n != 1 || at->dims[0] < 1) return fail(COEX_BAD_ATTRS, "embedding_dw: attribute [vocab] expected");
+      bool ok = dy.ndim == ids.ndim + 1;
+      for (int i = 0; ok && i < ids.ndim; ++i) ok = dy.shape[i] == ids.shape[i];
+      if (!ok) return fail(COEX_SHAPE_MISMATCH, "embedding_dw: gradient does not match ids + [d]");
+      *ndim = 2;
+      shape[0] = at->dims[0];
+      shape[1] = dy.shape[dy.ndim - 1];
+      return COEX_OK;
+    }
+    case COEX_LAYERNORM: case COEX_LAYERNORM_DX: case COEX_LN_DGAMMA: {
+      const TRec& x = in[0];
+      if (x.ndim < 1 || x.numel == 0) return fail(COEX_SHAPE_MISMATCH, "layernorm: non-empty operand required");
+      const int64_t d = x.shape[x.ndim - 1];
+      if (kind == COEX_LN_DGAMMA) {
+        if (!same(x, in[1])) return fail(COEX_SHAPE_MISMATCH, "ln_dgamma: dy differs from x");
+        if (d > 1024) return fail(COEX_SHAPE_MISMATCH, "ln_dgamma: rows longer than 1024");
+        *ndim = 1;
+        shape[0] = d;
+        return COEX_OK;
+      }
+      if (in[1].ndim != 1 || in[1].shape[0] != d) return fail(COEX_SHAPE_MISMATCH, "layernorm: gamma must be [d]");
+      if (kind == COEX_LAYERNORM && (in[2].ndim != 1 || in[2].shape[0] != d))
+        return fail(COEX_SHAPE_MISMATCH, "layernorm: beta must be [d]");
+      if (kind == COEX_LAYERNORM_DX && !same(x, in[2])) return fail(COEX_SHAPE_MISMATCH, "layernorm_dx: dy differs from x");
+      *ndim = x.ndim;
+      memcpy(shape, x.shape, sizeof(int64_t) * x.ndim);
+      return COEX_OK;
+    }
+    case COEX_BIAS_ADD: {
+      const TRec &x = in[0], &b = in[1];
+      if (x.ndim < 1 || b.ndim != 1 || b.shape[0] != x.shape[x.ndim - 1])
+        return fail(COEX_SHAPE_MISMATCH, "bias_add: bias does not match the last dim");
+      *ndim = x.ndim;
+      memcpy(shape, x.shape, sizeof(int64_t) * x.ndim);
+      return COEX_OK;
+    }
+    case COEX_BMM: case COEX_BMM_NT: case COEX_BMM_TN: {
+      const TRec &a = in[0], &b = in[1];
+      if (a.ndim != 3 || b.ndim != 3 || a.shape[0] != b.shape[0])
+        return fail(COEX_SHAPE_MISMATCH, "bmm: rank-3 operands with equal batch required");
+      const int64_t m = kind == COEX_BMM_TN ? a.shape[2] : a.shape[1], ka = kind == COEX_BMM_TN ? a.shape[1] : a.shape[2];
+      const int64_t n = kind == COEX_BMM_NT ? b.shape[1] : b.shape[2], kb = kind == COEX_BMM_NT ? b.shape[2] : b.shape[1];
+      if (ka != kb) return fail(COEX_SHAPE_MISMATCH, "bmm: inner dimensions differ");
+      *ndim = 3;
+      shape[0] = a.shape[0]; shape[1] = m; shape[2] = n;
+      return COEX_OK;
+    }
+    case COEX_CAUSAL_SOFTMAX: case COEX_SOFTMAX_GRAD: {
+      const TRec& x = in[0];
+      if (x.ndim < 2 || x.shape[x.ndim - 1] != x.shape[x.ndim - 2])
+        return fail(COEX_SHAPE_MISMATCH, "softmax: square trailing [T, T] block required");
+      if (kind == COEX_SOFTMAX_GRAD && !same(x, in[1])) return fail(COEX_SHAPE_MISMATCH, "softmax_grad: dy differs from y");
+      *ndim = x.ndim;
+      memcpy(shape, x.shape, sizeof(int64_t) * x.ndim);
+      return COEX_OK;
+    }
+    case COEX_CROSS_ENTROPY: case COEX_CROSS_ENTROPY_GRAD: {
+      const TRec &lg = in[0], &ids = in[1];
+      if (lg.ndim != 2 || ids.ndim != 1 || ids.shape[0] != lg.shape[0] || lg.shape[0] == 0)
+        return fail(COEX_SHAPE_MISMATCH, "cross_entropy: logits [R, V] and ids [R] required");
+      if (kind == COEX_CROSS_ENTROPY) {
+        *ndim = 0;
+      } else {
+        *ndim = 2;
+        shape[0] = lg.shape[0];
+        shape[1] = lg.shape[1];
+      }
       return COEX_OK;
     }
     default: break;
@@ -387,7 +467,10 @@ struct OpSpec {
 // Plan-only kind: batchnorm_dx + bn_dgamma + sum_rows over the same (x, dy) fused into one
 // column-statistics pass (planner.py _bn_bwd_groups); three outputs dx, dgamma, dbeta.
 constexpr int kBnBwdFused = 100;
-bool is_ext_compute(int kind) { return (kind >= COEX_CONV2D && kind <= COEX_SUM_ROWS) || kind == kBnBwdFused; }
+bool is_ext_compute(int kind) {
+  return (kind >= COEX_CONV2D && kind <= COEX_SUM_ROWS) || kind == kBnBwdFused ||
+         (kind >= COEX_EMBEDDING && kind <= COEX_CROSS_ENTROPY_GRAD && kind != COEX_GELU && kind != COEX_GELU_GRAD);
+}
 int ew_code(int kind) {
   switch (kind) {
     case COEX_ADD: return EW_ADD;
@@ -400,6 +483,9 @@ int ew_code(int kind) {
     case COEX_LEAKY_RELU: return EW_LRELU;
     case COEX_RELU_GRAD: return EW_RELU_GRAD;
     case COEX_LEAKY_RELU_GRAD: return EW_LRELU_GRAD;
+    case COEX_TO_INDEX: return EW_TO_INDEX;
+    case COEX_GELU: return EW_GELU;
+    case COEX_GELU_GRAD: return EW_GELU_GRAD;
     default: return EW_BCE;
   }
 }
@@ -503,7 +589,8 @@ int build_launch_t(coex_ctx* c, const OpSpec& s, Launch* L) {
   const int64_t n = numel_of(s.out_ndim, s.out_shape);
   switch (s.kind) {
     case COEX_ADD: case COEX_SUB: case COEX_MUL: case COEX_NEG: case COEX_RELU: case COEX_SIGMOID:
-    case COEX_TANH: case COEX_LEAKY_RELU: case COEX_RELU_GRAD: case COEX_LEAKY_RELU_GRAD: case COEX_BCE_TERM: {
+    case COEX_TANH: case COEX_LEAKY_RELU: case COEX_RELU_GRAD: case COEX_LEAKY_RELU_GRAD: case COEX_BCE_TERM:
+    case COEX_TO_INDEX: case COEX_GELU: case COEX_GELU_GRAD: {
       EwParams p{};
       p.ds = s.ds;
       p.a = s.in[0];
@@ -662,6 +749,22 @@ int tc_attr(int amode, bool bmn) {
   return COEX_OK;
 }
 
+// Batched operands (bmm): 3-D maps {inner, rows, batch} over [batch][rows][pitch(inner)] bf16.
+int make_tmap3(CUtensorMap* m, void* base, int64_t rows, int64_t inner, int64_t batch, int box_inner, int box_rows) {
+  auto enc = tmap_encoder();
+  if (!enc) return fail(COEX_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable");
+  const int64_t pitch = bf16_pitch(inner > 0 ? inner : 1);
+  cuuint64_t dims[3] = {(cuuint64_t)(inner > 0 ? inner : 1), (cuuint64_t)(rows > 0 ? rows : 1), (cuuint64_t)batch};
+  cuuint64_t strides[2] = {(cuuint64_t)pitch * 2, (cuuint64_t)pitch * 2 * (rows > 0 ? rows : 1)};
+  cuuint32_t box[3] = {(cuuint32_t)box_inner, (cuuint32_t)box_rows, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, base, dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(COEX_CUDA_ERROR, "cuTensorMapEncodeTiled (3-D) failed: " + std::to_string((int)r));
+  return COEX_OK;
+}
+
 // 4-D NHWC bf16 gather map for the implicit-GEMM convolutions: box {64 channels, bw*s, bh*s, bn},
 // element strides {1, s, s, 1}, 128-byte swizzle, out-of-bounds (padding) -> 0.
 int make_tmap_conv(CUtensorMap* m, void* base, int64_t N, int64_t H, int64_t W, int64_t C, int s, int bw, int bh,
@@ -700,17 +803,21 @@ bool conv_blocks(int64_t Hg, int64_t Wg, int pix, int* bw, int* bh, int* bn) {
 int tc_gemm_launches(coex_ctx* c, DevState* ds, void* a16, void* b16, int64_t M, int64_t N, int64_t K,
                      const TcPlan& t, In na, In nb, const Out& out, float* raw, float* ws, Launch* L, int* nL,
                      int amode = 0, bool b_mn = false, const TcConv* cv = nullptr,
-                     const CUtensorMap* conv_map = nullptr) {
+                     const CUtensorMap* conv_map = nullptr, int64_t batch = 1) {
   TcGemmParams gp;
   memset(&gp, 0, sizeof(gp));
   int rc = COEX_OK;
   if (amode >= 2) gp.tmA = *conv_map;
+  else if (batch > 1) rc = amode == 1 ? make_tmap3(&gp.tmA, a16, K, M, batch, 64, TC_BK) : make_tmap3(&gp.tmA, a16, M, K, batch, TC_BK, TC_BM);
   else rc = amode == 1 ? make_tmap_mn(&gp.tmA, a16, M, K) : make_tmap(&gp.tmA, a16, M, K, TC_BM);
   if (rc) return rc;
   if (cv) gp.cv = *cv;
   else gp.cv.phases = 1;
+  gp.batch = (int)batch;
+  gp.c_bstride = M * N;
   const int64_t brows = K * ((amode == 2 && cv) ? cv->phases : 1);    // sub-pixel phases stack their B
-  rc = b_mn ? make_tmap_mn(&gp.tmB, b16, N, brows) : make_tmap(&gp.tmB, b16, N, K, t.bn);
+  if (batch > 1) rc = b_mn ? make_tmap3(&gp.tmB, b16, K, N, batch, 64, TC_BK) : make_tmap3(&gp.tmB, b16, N, K, batch, TC_BK, t.bn);
+  else rc = b_mn ? make_tmap_mn(&gp.tmB, b16, N, brows) : make_tmap(&gp.tmB, b16, N, K, t.bn);
   if (rc) return rc;
   gp.ds = ds;
   gp.a = na;
@@ -724,7 +831,7 @@ int tc_gemm_launches(coex_ctx* c, DevState* ds, void* a16, void* b16, int64_t M,
   Launch& G = L[(*nL)++];
   void* fn = t.bn == 64 ? tc_fn<64>(amode, b_mn) : t.bn == 128 ? tc_fn<128>(amode, b_mn) : tc_fn<256>(amode, b_mn);
   const int64_t items = ((M + TC_BM - 1) / TC_BM) * ((N + t.bn - 1) / t.bn) * t.splits *
-                        (amode == 2 ? gp.cv.phases : 1);
+                        (amode == 2 ? gp.cv.phases : 1) * (batch > 1 ? batch : 1);
   G.set(fn, dim3((unsigned)(items < kNumSMs ? items : kNumSMs)), dim3(TC_THREADS), gp);
   G.smem = t.bn == 64 ? TcCfg<64>::SMEM : t.bn == 128 ? TcCfg<128>::SMEM : TcCfg<256>::SMEM;
   rc = t.bn == 64 ? tc_attr<64>(amode, b_mn) : t.bn == 128 ? tc_attr<128>(amode, b_mn) : tc_attr<256>(amode, b_mn);
@@ -1066,6 +1173,117 @@ int build_xop_t(coex_ctx* c, const OpSpec& s, Launch* L, int* nL, size_t* ws_byt
         L[(*nL)++].set((void*)k_bn_apply<T>, grid_for(n), dim3(256), ap);
       }
       return COEX_OK;
+    }
+    case COEX_BMM: case COEX_BMM_NT: case COEX_BMM_TN: {
+      const int64_t Bt = s.in_shape[0][0];
+      const bool tn = s.kind == COEX_BMM_TN, nt = s.kind == COEX_BMM_NT;
+      const int64_t M = s.out_shape[1], N = s.out_shape[2];
+      const int64_t K = tn ? s.in_shape[0][1] : s.in_shape[0][2];
+      if (bf16) {
+        // operands converted as stored: A [B][M][K] (K-major) or [B][K][M] (tn: MN-major);
+        // B [B][K][N] (MN-major) or [B][N][K] (nt: K-major); 3-D TMA maps, batch = grid items
+        const TcPlan t = tc_plan(M * Bt, N, K, false);
+        const int64_t arow = tn ? K : M, acol = tn ? M : K, brow = nt ? N : K, bcol = nt ? K : N;
+        void* A = cv.take((size_t)Bt * arow * bf16_pitch(acol) * 2);
+        void* B = cv.take((size_t)Bt * brow * bf16_pitch(bcol) * 2);
+        if (!build) break;
+        cvt_rows_launch(s.ds, s.in[0], A, Bt * arow, acol, &L[(*nL)++]);
+        cvt_rows_launch(s.ds, s.in[1], B, Bt * brow, bcol, &L[(*nL)++]);
+        return tc_gemm_launches(c, s.ds, A, B, M, N, K, t, s.in[0], s.in[1], s.out, nullptr, nullptr, L, nL,
+                                tn ? 1 : 0, !nt, nullptr, nullptr, Bt);
+      }
+      if (!build) break;
+      MatmulParams mp{};
+      mp.ds = s.ds; mp.a = s.in[0]; mp.b = s.in[1]; mp.trans_a = tn; mp.trans_b = nt;
+      mp.M = M; mp.N = N; mp.K = K;
+      mp.lda = s.in_shape[0][2]; mp.ldb = s.in_shape[1][2];
+      mp.sa = s.in_shape[0][1] * s.in_shape[0][2]; mp.sb = s.in_shape[1][1] * s.in_shape[1][2]; mp.sc = M * N;
+      mp.out = s.out;
+      simt_matmul_launch<T>(c, mp, &L[*nL]);
+      L[(*nL)++].grid.y = (unsigned)Bt;
+      return COEX_OK;
+    }
+    case COEX_EMBEDDING: case COEX_EMBEDDING_DW: case COEX_LAYERNORM: case COEX_LAYERNORM_DX: case COEX_LN_DGAMMA:
+    case COEX_BIAS_ADD: case COEX_CAUSAL_SOFTMAX: case COEX_SOFTMAX_GRAD: case COEX_CROSS_ENTROPY:
+    case COEX_CROSS_ENTROPY_GRAD: {
+      RowParams rp{};
+      rp.ds = s.ds; rp.x = s.in[0]; rp.y = s.in[1];
+      rp.z = s.nin > 2 ? s.in[2] : In{nullptr, nullptr, nullptr};
+      rp.out = s.out;
+      rp.scale = s.value;
+      const int64_t xn = numel_of(s.in_ndim[0], s.in_shape[0]);
+      const int64_t d = s.in_shape[0][s.in_ndim[0] - 1];
+      auto warp_rows = [&](int64_t rows) {
+        int64_t b = (rows + 7) / 8;
+        return dim3((unsigned)(b < kNumSMs * 8 ? (b < 1 ? 1 : b) : kNumSMs * 8));
+      };
+      switch (s.kind) {
+        case COEX_EMBEDDING: {
+          if (!build) break;
+          rp.d = s.in_shape[0][1]; rp.vocab = s.in_shape[0][0];
+          rp.rows = numel_of(s.in_ndim[1], s.in_shape[1]);
+          L[(*nL)++].set(is_f64(c) ? (void*)k_embed<double> : (void*)k_embed<float>, grid_for(rp.rows * rp.d), dim3(256), rp);
+          return COEX_OK;
+        }
+        case COEX_EMBEDDING_DW: {
+          if (!build) break;
+          rp.d = s.out_shape[1]; rp.vocab = s.out_shape[0];
+          rp.rows = numel_of(s.in_ndim[0], s.in_shape[0]);
+          ZeroParams zp{};
+          zp.ds = s.ds; zp.out = s.out; zp.out.npub = 0; zp.out.late = nullptr;
+          zp.bytes = rp.vocab * rp.d * (int64_t)es; zp.a = s.in[0]; zp.b = s.in[1];
+          L[(*nL)++].set((void*)k_zero, grid_for(zp.bytes / 16 + 1), dim3(256), zp);
+          L[(*nL)++].set(is_f64(c) ? (void*)k_embed_dw<double> : (void*)k_embed_dw<float>, grid_for(rp.rows * rp.d),
+                         dim3(256), rp);
+          return COEX_OK;
+        }
+        case COEX_LAYERNORM: case COEX_LAYERNORM_DX: {
+          if (!build) break;
+          rp.d = d; rp.rows = xn / d;
+          void* fn = s.kind == COEX_LAYERNORM ? (is_f64(c) ? (void*)k_layernorm<double, 0> : (void*)k_layernorm<float, 0>)
+                                              : (is_f64(c) ? (void*)k_layernorm<double, 1> : (void*)k_layernorm<float, 1>);
+          L[(*nL)++].set(fn, warp_rows(rp.rows), dim3(256), rp);
+          return COEX_OK;
+        }
+        case COEX_LN_DGAMMA: {
+          rp.acc = (double*)cv.take((size_t)kColReplicas * d * 8);
+          rp.counter = (unsigned int*)cv.take(16);
+          if (!build) break;
+          rp.d = d; rp.rows = xn / d;
+          L[(*nL)++].set(is_f64(c) ? (void*)k_ln_dgamma<double> : (void*)k_ln_dgamma<float>, warp_rows(rp.rows / 4),
+                         dim3(256), rp);
+          return COEX_OK;
+        }
+        case COEX_BIAS_ADD: {
+          if (!build) break;
+          rp.d = d; rp.rows = xn / d;
+          L[(*nL)++].set(is_f64(c) ? (void*)k_bias_add<double> : (void*)k_bias_add<float>,
+                         grid_for(sizeof(T) == 4 && d % 4 == 0 ? xn / 4 : xn), dim3(256), rp);
+          return COEX_OK;
+        }
+        case COEX_CAUSAL_SOFTMAX: case COEX_SOFTMAX_GRAD: {
+          if (!build) break;
+          rp.d = d; rp.rows = xn / d; rp.T = (int)d;
+          void* fn = s.kind == COEX_CAUSAL_SOFTMAX ? (is_f64(c) ? (void*)k_causal_softmax<double> : (void*)k_causal_softmax<float>)
+                                                   : (is_f64(c) ? (void*)k_softmax_grad<double> : (void*)k_softmax_grad<float>);
+          L[(*nL)++].set(fn, warp_rows(rp.rows), dim3(256), rp);
+          return COEX_OK;
+        }
+        default: {   // cross-entropy (loss / gradient)
+          const int64_t R = s.in_shape[0][0];
+          if (s.kind == COEX_CROSS_ENTROPY) {
+            rp.acc = (double*)cv.take((size_t)R * 8);
+            rp.counter = (unsigned int*)cv.take(16);
+          }
+          if (!build) break;
+          rp.d = s.in_shape[0][1]; rp.rows = R; rp.vocab = rp.d;
+          void* fn = s.kind == COEX_CROSS_ENTROPY ? (is_f64(c) ? (void*)k_cross_entropy<double, 0> : (void*)k_cross_entropy<float, 0>)
+                                                  : (is_f64(c) ? (void*)k_cross_entropy<double, 1> : (void*)k_cross_entropy<float, 1>);
+          L[(*nL)++].set(fn, dim3((unsigned)(R < kNumSMs * 8 ? R : kNumSMs * 8)), dim3(256), rp);
+          return COEX_OK;
+        }
+      }
+      break;
     }
     default:
       return fail(COEX_BAD_ATTRS, "op kind has no extension kernel");
@@ -1458,6 +1676,7 @@ int eager_scratch(coex_ctx* c, OpSpec* s) {
     size_t wb = 0;
     int rc = build_xop(c, *s, tmp, &n, &wb);
     if (rc) return rc;
+    if (wb < 256) wb = 256;          // a non-null workspace marks the build pass
     CK(cudaMallocAsync((void**)&s->ws, wb, c->stream));
     CK(cudaMemsetAsync(s->ws, 0, wb, c->stream));
   }
@@ -1879,6 +2098,7 @@ struct Builder {
         size_t wb = 0;
         int rc = build_xop(c, s, L, &nL, &wb);
         if (rc) return rc;
+        if (wb < 256) wb = 256;      // a non-null workspace marks the build pass
         void* ws = nullptr;
         CK(cudaMalloc(&ws, wb));
         CK(cudaMemset(ws, 0, wb));

@@ -1,0 +1,381 @@
+// xformer_ops.cuh -- sm_100a kernels of the transformer extension op set (config C4,
+// GPT-2 small; SURVEY §2.4, §8(a) row a*).  Semantics: oracle/kernels.py
+// transformer_kernel (builder-defined, parity unpinned by the reference).
+//
+// Row kernels (layernorm, causal softmax, cross-entropy) give one warp (or one block
+// for vocabulary-wide rows) to a row, keep the row in registers / L1, and reduce with
+// warp shuffles in double.  Column sums (ln_dgamma) reuse the fp64-atomic replicated
+// accumulator scheme of k_colstats.  The batched GEMMs (bmm*) are lowered by the runtime
+// to the tcgen05 kernel (bf16 mode, 3-D tensor maps) or the batched SIMT kernel.
+#pragma once
+#include "ext_ops.cuh"
+
+namespace coex {
+
+constexpr double kLnEps = 1e-5;
+constexpr double kGeluC = 0.7978845608028654;
+
+struct RowParams {
+  DevState* ds;
+  In x, y, z;                // operands (meaning per kernel)
+  long long rows, d;         // row count, row length
+  int T;                     // causal softmax: rows per [T, T] block
+  double scale;
+  long long vocab;           // embedding / cross-entropy
+  double* acc;               // column accumulators (ln_dgamma) / per-row losses (cross-entropy)
+  unsigned int* counter;
+  Out out;
+};
+
+template <typename A>
+__device__ __forceinline__ A warp_sum(A v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+template <typename A>
+__device__ __forceinline__ A warp_max(A v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+// softmax-type rows accumulate in the storage precision's natural type (f64 parity mode:
+// double; fp32 / bf16 modes: float -- exp in double would make them ALU-bound)
+template <typename T> struct AccT { typedef float type; };
+template <> struct AccT<double> { typedef double type; };
+__device__ __forceinline__ float ex(float v) { return __expf(v); }
+__device__ __forceinline__ double ex(double v) { return exp(v); }
+
+// last-block election after every block wrote its part (threadfence + counter)
+__device__ __forceinline__ bool last_block(unsigned int* counter) {
+  __shared__ unsigned int last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = (atomicAdd(counter, 1u) == gridDim.x - 1) ? 1u : 0u;
+    if (last) __threadfence();
+  }
+  __syncthreads();
+  return last != 0;
+}
+
+// ------------------------------------------------------------------ embedding
+// out[r, :] = table[clip(ids[r]), :]   (x = table [V, d], y = ids [rows])
+template <typename T>
+__global__ void __launch_bounds__(256) k_embed(RowParams p) {
+  COEX_PDL_ENTER();
+  stamp(p.ds, SK_EW);
+  if (skip(p.ds)) return;
+  const T* tab = res<T>(p.x);
+  const T* ids = res<T>(p.y);
+  T* o = pick_out<T>(p.out, tab, ids);
+  publish_early(p.out, o);
+  count_op(p.ds);
+  const long long total = p.rows * p.d;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    const long long r = i / p.d, c = i - r * p.d;
+    double f = floor((double)ids[r]);
+    long long v = f < 0 ? 0 : (f > (double)(p.vocab - 1) ? p.vocab - 1 : (long long)f);
+    o[i] = tab[v * p.d + c];
+  }
+  publish_late(p.out, o);
+}
+
+// out[v, :] = sum over rows r with ids[r] == v of dy[r, :] (atomics; the output is zeroed
+// by the preceding k_zero launch)   (x = ids [rows], y = dy [rows, d])
+template <typename T>
+__global__ void __launch_bounds__(256) k_embed_dw(RowParams p) {
+  COEX_PDL_ENTER();
+  stamp(p.ds, SK_EW);
+  if (skip(p.ds)) return;
+  const T* ids = res<T>(p.x);
+  const T* dy = res<T>(p.y);
+  T* o = pick_out<T>(p.out, ids, dy);
+  publish_early(p.out, o);
+  count_op(p.ds);
+  const long long total = p.rows * p.d;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    const long long r = i / p.d, c = i - r * p.d;
+    double f = floor((double)ids[r]);
+    long long v = f < 0 ? 0 : (f > (double)(p.vocab - 1) ? p.vocab - 1 : (long long)f);
+    atomicAdd(o + v * p.d + c, dy[i]);
+  }
+  publish_late(p.out, o);
+}
+
+struct ZeroParams {
+  DevState* ds;
+  Out out;
+  long long bytes;
+  In a, b;
+};
+__global__ void __launch_bounds__(256) k_zero(ZeroParams p) {
+  COEX_PDL_ENTER();
+  if (skip(p.ds)) return;
+  char* o = pick_out<char>(p.out, p.a.cell || p.a.direct ? res<char>(p.a) : nullptr,
+                           p.b.cell || p.b.direct ? res<char>(p.b) : nullptr);
+  const long long n16 = p.bytes / 16;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += (long long)gridDim.x * blockDim.x)
+    ((uint4*)o)[i] = make_uint4(0u, 0u, 0u, 0u);
+  for (long long i = n16 * 16 + (long long)blockIdx.x * blockDim.x + threadIdx.x; i < p.bytes;
+       i += (long long)gridDim.x * blockDim.x)
+    o[i] = 0;
+}
+
+// ------------------------------------------------------------------ bias add
+// out = x + b[i % d]
+template <typename T>
+__global__ void __launch_bounds__(256) k_bias_add(RowParams p) {
+  COEX_PDL_ENTER();
+  stamp(p.ds, SK_EW);
+  if (skip(p.ds)) return;
+  const T* x = res<T>(p.x);
+  const T* b = res<T>(p.y);
+  T* o = pick_out<T>(p.out, x, b);
+  publish_early(p.out, o);
+  count_op(p.ds);
+  const long long total = p.rows * p.d;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  if (sizeof(T) == 4 && (p.d & 3) == 0) {
+    const long long d4 = p.d / 4;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total / 4; i += stride) {
+      const float4 v = ((const float4*)x)[i];
+      const float4 w = ((const float4*)b)[i % d4];
+      ((float4*)o)[i] = make_float4(__fadd_rn(v.x, w.x), __fadd_rn(v.y, w.y), __fadd_rn(v.z, w.z), __fadd_rn(v.w, w.w));
+    }
+  } else {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride)
+      o[i] = ew_apply(EW_ADD, x[i], b[i % p.d]);
+  }
+  publish_late(p.out, o);
+}
+
+// ------------------------------------------------------------------ layernorm
+// One warp per row; the row is read twice (mean, then centred moments) from L1/L2.
+template <typename T>
+__device__ __forceinline__ void ln_row_stats(const T* xr, long long d, int lane, double& mean, double& rstd) {
+  double s = 0.0;
+  for (long long c = lane; c < d; c += 32) s += (double)xr[c];
+  mean = warp_sum(s) / (double)d;
+  double q = 0.0;
+  for (long long c = lane; c < d; c += 32) {
+    const double v = (double)xr[c] - mean;
+    q += v * v;
+  }
+  rstd = 1.0 / sqrt(warp_sum(q) / (double)d + kLnEps);
+}
+
+// mode 0: y = xhat*g + b (x, g = y operand, b = z operand); mode 1: dx (x, g, dy = z)
+template <typename T, int MODE>
+__global__ void __launch_bounds__(256) k_layernorm(RowParams p) {
+  COEX_PDL_ENTER();
+  stamp(p.ds, SK_BNAPPLY);
+  if (skip(p.ds)) return;
+  const T* x = res<T>(p.x);
+  const T* g = res<T>(p.y);
+  const T* z = res<T>(p.z);
+  T* o = pick_out<T>(p.out, x, g);
+  publish_early(p.out, o);
+  count_op(p.ds);
+  const int lane = threadIdx.x & 31;
+  const long long warps = (long long)gridDim.x * (blockDim.x / 32);
+  for (long long r = (long long)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; r < p.rows; r += warps) {
+    const T* xr = x + r * p.d;
+    double mean, rstd;
+    ln_row_stats(xr, p.d, lane, mean, rstd);
+    if (MODE == 0) {
+      for (long long c = lane; c < p.d; c += 32)
+        o[r * p.d + c] = (T)((((double)xr[c] - mean) * rstd) * (double)g[c] + (double)z[c]);
+    } else {
+      const T* dy = z + r * p.d;
+      double m1 = 0.0, m2 = 0.0;
+      for (long long c = lane; c < p.d; c += 32) {
+        const double dxh = (double)dy[c] * (double)g[c];
+        m1 += dxh;
+        m2 += dxh * (((double)xr[c] - mean) * rstd);
+      }
+      m1 = warp_sum(m1) / (double)p.d;
+      m2 = warp_sum(m2) / (double)p.d;
+      for (long long c = lane; c < p.d; c += 32) {
+        const double xh = ((double)xr[c] - mean) * rstd;
+        o[r * p.d + c] = (T)((((double)dy[c] * (double)g[c] - m1) - xh * m2) * rstd);
+      }
+    }
+  }
+  publish_late(p.out, o);
+}
+
+// ln_dgamma: out[c] = sum over rows of dy * xhat (x, dy = y operand).  Warps take rows; each
+// lane accumulates its columns in double, blocks add into kColReplicas fp64 accumulators,
+// the last block sums the replicas, writes the output and re-zeroes the accumulators.
+template <typename T>
+__global__ void __launch_bounds__(256) k_ln_dgamma(RowParams p) {
+  COEX_PDL_ENTER();
+  stamp(p.ds, SK_COLSTATS);
+  if (skip(p.ds)) return;
+  const T* x = res<T>(p.x);
+  const T* dy = res<T>(p.y);
+  T* o = pick_out<T>(p.out, x, dy);
+  publish_early(p.out, o);
+  count_op(p.ds);
+  constexpr int MAXC = 32;                          // columns per lane (d <= 1024)
+  const int lane = threadIdx.x & 31;
+  double accl[MAXC];
+#pragma unroll
+  for (int j = 0; j < MAXC; ++j) accl[j] = 0.0;
+  const long long warps = (long long)gridDim.x * (blockDim.x / 32);
+  for (long long r = (long long)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; r < p.rows; r += warps) {
+    const T* xr = x + r * p.d;
+    double mean, rstd;
+    ln_row_stats(xr, p.d, lane, mean, rstd);
+#pragma unroll
+    for (int j = 0; j < MAXC; ++j) {
+      const long long c = lane + 32ll * j;
+      if (c < p.d) accl[j] += (double)dy[r * p.d + c] * (((double)xr[c] - mean) * rstd);
+    }
+  }
+  double* accr = p.acc + (long long)(blockIdx.x % kColReplicas) * p.d;
+#pragma unroll
+  for (int j = 0; j < MAXC; ++j) {
+    const long long c = lane + 32ll * j;
+    if (c < p.d && accl[j] != 0.0) atomicAdd(accr + c, accl[j]);
+  }
+  if (!last_block(p.counter)) return;
+  const unsigned int nrep = gridDim.x < (unsigned)kColReplicas ? gridDim.x : (unsigned)kColReplicas;
+  for (long long c = threadIdx.x; c < p.d; c += blockDim.x) {
+    double s = 0.0;
+    for (unsigned int q = 0; q < nrep; ++q) {
+      s += __ldcg(p.acc + (long long)q * p.d + c);
+      p.acc[(long long)q * p.d + c] = 0.0;
+    }
+    o[c] = (T)s;
+  }
+  if (threadIdx.x == 0) *p.counter = 0u;
+  __syncthreads();
+  if (threadIdx.x == 0 && p.out.late != nullptr)
+    for (int i = 0; i < p.out.npub; ++i) *p.out.pub[i] = o;
+}
+
+// ------------------------------------------------------------------ causal softmax
+// One warp per row of a [T, T] block: row i keeps columns j <= i; y = exp(s*x - max) / sum.
+template <typename T>
+__global__ void __launch_bounds__(256) k_causal_softmax(RowParams p) {
+  COEX_PDL_ENTER();
+  stamp(p.ds, SK_EW);
+  if (skip(p.ds)) return;
+  const T* x = res<T>(p.x);
+  T* o = pick_out<T>(p.out, x, nullptr);
+  publish_early(p.out, o);
+  count_op(p.ds);
+  const int lane = threadIdx.x & 31;
+  const long long warps = (long long)gridDim.x * (blockDim.x / 32);
+  const long long d = p.d;
+  typedef typename AccT<T>::type A;
+  const A sc = (A)p.scale;
+  for (long long r = (long long)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; r < p.rows; r += warps) {
+    const long long i = r % p.T;                    // row index inside its [T, T] block
+    const T* xr = x + r * d;
+    T* orow = o + r * d;
+    A mx = -INFINITY;
+    for (long long c = lane; c <= i; c += 32) mx = fmax(mx, (A)xr[c] * sc);
+    mx = warp_max(mx);
+    A s = 0;
+    for (long long c = lane; c <= i; c += 32) s += ex((A)xr[c] * sc - mx);
+    s = warp_sum(s);
+    const A inv = (A)1 / s;
+    for (long long c = lane; c < d; c += 32)
+      orow[c] = c <= i ? (T)(ex((A)xr[c] * sc - mx) * inv) : T(0);
+  }
+  publish_late(p.out, o);
+}
+
+// dx = scale * y * (dy - sum_j dy*y)   (x = y, y = dy operand)
+template <typename T>
+__global__ void __launch_bounds__(256) k_softmax_grad(RowParams p) {
+  COEX_PDL_ENTER();
+  stamp(p.ds, SK_EW);
+  if (skip(p.ds)) return;
+  const T* y = res<T>(p.x);
+  const T* dy = res<T>(p.y);
+  T* o = pick_out<T>(p.out, y, dy);
+  publish_early(p.out, o);
+  count_op(p.ds);
+  const int lane = threadIdx.x & 31;
+  const long long warps = (long long)gridDim.x * (blockDim.x / 32);
+  const long long d = p.d;
+  typedef typename AccT<T>::type A;
+  for (long long r = (long long)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; r < p.rows; r += warps) {
+    const T* yr = y + r * d;
+    const T* gr = dy + r * d;
+    A dot = 0;
+    for (long long c = lane; c < d; c += 32) dot += (A)gr[c] * (A)yr[c];
+    dot = warp_sum(dot);
+    for (long long c = lane; c < d; c += 32)
+      o[r * d + c] = (T)((A)p.scale * ((A)yr[c] * ((A)gr[c] - dot)));
+  }
+  publish_late(p.out, o);
+}
+
+// ------------------------------------------------------------------ cross-entropy
+// One block per row (vocabulary-wide rows).  MODE 0: loss row values into p.acc, the last
+// block writes their mean (ordered sum: deterministic); MODE 1: (softmax - onehot) / rows.
+template <typename T, int MODE>
+__global__ void __launch_bounds__(256) k_cross_entropy(RowParams p) {
+  COEX_PDL_ENTER();
+  stamp(p.ds, MODE ? SK_EW : SK_REDUCE);
+  if (skip(p.ds)) return;
+  const T* lg = res<T>(p.x);
+  const T* ids = res<T>(p.y);
+  T* o = pick_out<T>(p.out, lg, ids);
+  if (MODE == 1) publish_early(p.out, o);
+  count_op(p.ds);
+  __shared__ double red[32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const long long V = p.d;
+  for (long long r = blockIdx.x; r < p.rows; r += gridDim.x) {
+    const T* row = lg + r * V;
+    double mx = -INFINITY;
+    for (long long c = threadIdx.x; c < V; c += blockDim.x) mx = fmax(mx, (double)row[c]);
+    mx = warp_max(mx);
+    if (lane == 0) red[wid] = mx;
+    __syncthreads();
+    mx = red[0];
+    for (int w = 1; w < nw; ++w) mx = fmax(mx, red[w]);
+    __syncthreads();
+    typedef typename AccT<T>::type A;
+    A sa = 0;
+    for (long long c = threadIdx.x; c < V; c += blockDim.x) sa += ex((A)((double)row[c] - mx));
+    double s = warp_sum((double)sa);
+    if (lane == 0) red[wid] = s;
+    __syncthreads();
+    s = 0.0;
+    for (int w = 0; w < nw; ++w) s += red[w];
+    __syncthreads();
+    double f = floor((double)ids[r]);
+    const long long id = f < 0 ? 0 : (f > (double)(V - 1) ? V - 1 : (long long)f);
+    if (MODE == 0) {
+      if (threadIdx.x == 0) p.acc[r] = (log(s) + mx) - (double)row[id];
+    } else {
+      const A inv = (A)(1.0 / s), invr = (A)(1.0 / (double)p.rows);
+      for (long long c = threadIdx.x; c < V; c += blockDim.x) {
+        A g = ex((A)((double)row[c] - mx)) * inv;
+        if (c == id) g -= (A)1;
+        o[r * V + c] = (T)(g * invr);
+      }
+    }
+  }
+  if (MODE == 1) {
+    publish_late(p.out, o);
+    return;
+  }
+  if (!last_block(p.counter)) return;
+  if (threadIdx.x == 0) {
+    double acc = 0.0;
+    for (long long r = 0; r < p.rows; ++r) acc += __ldcg(p.acc + r);
+    o[0] = (T)(acc / (double)p.rows);
+    *p.counter = 0u;
+    for (int i = 0; i < p.out.npub; ++i) *p.out.pub[i] = o;
+  }
+}
+
+}  // namespace coex

@@ -35,7 +35,8 @@ from .trace_graph import (Diverged, External, Handle, LoopEnter, LoopExit,
                           LoopIterStart, OpEvent, StepEnd)
 
 OP_BY_NAME = {k.value: k for k in OpKind if k not in (OpKind.READ_VAR, OpKind.ASSIGN_VAR)}
-CONV_NAMES = frozenset(("conv2d", "conv2d_t", "conv2d_dw"))
+CONV_NAMES = frozenset(("conv2d", "conv2d_t", "conv2d_dw", "embedding_dw"))
+SCALE_NAMES = frozenset(("causal_softmax", "softmax_grad"))    # trailing host scale -> "value" attr
 
 
 class Val:
@@ -694,17 +695,31 @@ class Interp:
                 return ctx.op(kind, {"perm": tuple(perm)}, [x], loc, [shp])
             return transpose
         if name in CONV_NAMES:
-            # extension convolutions: two tensor operands + the [k, s, p] shape literal
+            # extension ops with two tensor operands + a shape literal ([k, s, p] / [vocab])
             fy = self._c_expr(e.args[1], loc)
             geo = self._c_shape(e.args[2], loc)
+            akey = "dims" if name == "embedding_dw" else "conv"
 
             def conv(ctx, env):
                 x = fx(ctx, env)
                 y = fy(ctx, env)
                 if isinstance(x, str) or isinstance(y, str):
                     raise it._err(f"{name}: string operand", e)
-                return ctx.op(kind, {"conv": tuple(geo(ctx, env))}, [x, y], loc, [shape_of(x), shape_of(y)])
+                return ctx.op(kind, {akey: tuple(geo(ctx, env))}, [x, y], loc, [shape_of(x), shape_of(y)])
             return conv
+        if name in SCALE_NAMES:
+            ftens = [fx] + [self._c_expr(a, loc) for a in e.args[1:-1]]
+            fsc = self._host_fn(self._c_expr(e.args[-1], loc), e)
+
+            def scaled(ctx, env):
+                xs = [f(ctx, env) for f in ftens]
+                if any(isinstance(v, str) for v in xs):
+                    raise it._err(f"{name}: string operand", e)
+                sc = fsc(ctx, env)
+                if isinstance(sc, bool) or not isinstance(sc, (int, float)):
+                    raise it._err(f"{name}: scale must be a number", e)
+                return ctx.op(kind, {"value": float(sc)}, xs, loc, [shape_of(v) for v in xs])
+            return scaled
         site = (kind, kind.value, loc, (loc.stmt_id, loc.loop_path))
         if len(e.args) == 3:
             fy = self._c_expr(e.args[1], loc)

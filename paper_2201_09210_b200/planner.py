@@ -28,7 +28,7 @@ from dataclasses import dataclass, field
 
 from .errors import ShapeMiss
 from .graph_gen import ExecOp, InputFeed, OutputFetch, SwitchCase, SymProgram, UnrolledLoop, While
-from .tensor import CONV_KINDS, OpKind, flops_of, infer_shape, shape_size
+from .tensor import BMM_KINDS, CONV_KINDS, OpKind, flops_of, infer_shape, shape_size
 
 MAGIC = 0xC0E8B200
 VERSION = 2
@@ -38,10 +38,13 @@ MAX_RANK = 8
 MAX_PUB = 6
 # extension compute ops (conv / batch-norm families) lowered by csrc/ext_ops.cuh: T_XOP items
 XOP = {OpKind.CONV2D, OpKind.CONV2D_T, OpKind.CONV2D_DW, OpKind.BATCHNORM, OpKind.BATCHNORM_DX,
-       OpKind.BN_DGAMMA, OpKind.SUM_ROWS}
+       OpKind.BN_DGAMMA, OpKind.SUM_ROWS,
+       OpKind.EMBEDDING, OpKind.EMBEDDING_DW, OpKind.LAYERNORM, OpKind.LAYERNORM_DX, OpKind.LN_DGAMMA,
+       OpKind.BIAS_ADD, OpKind.BMM, OpKind.BMM_NT, OpKind.BMM_TN, OpKind.CAUSAL_SOFTMAX, OpKind.SOFTMAX_GRAD,
+       OpKind.CROSS_ENTROPY, OpKind.CROSS_ENTROPY_GRAD}
 EW_CODE = {OpKind.ADD: 0, OpKind.SUB: 1, OpKind.MUL: 2, OpKind.NEG: 3, OpKind.RELU: 4, OpKind.SIGMOID: 5,
            OpKind.TANH: 7, OpKind.LEAKY_RELU: 8, OpKind.RELU_GRAD: 9, OpKind.LEAKY_RELU_GRAD: 10,
-           OpKind.BCE_TERM: 11}
+           OpKind.BCE_TERM: 11, OpKind.TO_INDEX: 12, OpKind.GELU_GRAD: 13, OpKind.GELU: 14}
 COMPUTE = {OpKind.MATMUL, OpKind.SUM, OpKind.MEAN, OpKind.TRANSPOSE} | set(EW_CODE) | XOP
 MAX_XIN = 3
 XOP_BN_BWD = 100          # fused batchnorm_dx + bn_dgamma + sum_rows (csrc COEX_BN_BWD_FUSED)
@@ -510,15 +513,15 @@ class Planner:
         in_shapes = [self._in_shape(b, shapes) for b in x.inputs]
         late = _conflicts(cells, pubs[nid])
         n_compute[0] += 1
-        attr = list(x.attrs["conv"]) if x.kind in CONV_KINDS else []
-        if x.kind in CONV_KINDS:
+        attr = list(x.attrs["conv"]) if x.kind in CONV_KINDS else list(x.attrs.get("dims", ()))
+        if x.kind in CONV_KINDS or x.kind in BMM_KINDS:
             flops[0] += flops_of(x.kind, in_shapes, x.attrs)
         out_shape = shapes[nid]
         word = [T_XOP, x.kind.code, nid, len(cells)] + cells + [-1] * (MAX_XIN - len(cells))
         for s_ in in_shapes + [()] * (MAX_XIN - len(in_shapes)):
             word += [len(s_)] + _pad(s_)
         word += [len(out_shape)] + _pad(out_shape)
-        word += [len(attr)] + _pad(attr) + [_f64_bits(0.0)]
+        word += [len(attr)] + _pad(attr) + [_f64_bits(float(x.attrs.get("value", 0.0)))]
         word += out_words(nid, late)
         return word
 
