@@ -9,6 +9,8 @@ fetched loss, a native call mid-step (``clip``, the numpy stand-in), and a
 
 from __future__ import annotations
 
+import math
+
 from .dataset import DatasetSource
 from .tensor import Tensor
 
@@ -184,6 +186,121 @@ def c1_flops(batch=64, hidden=128, din=784, dout=10) -> int:
     fwd = 2 * batch * din * hidden + 2 * batch * hidden * dout
     bwd = 2 * hidden * batch * dout + 2 * batch * dout * hidden + 2 * din * batch * hidden
     return fwd + bwd
+
+
+def gpt2_program(steps: int = 20, batch: int = 8, seq: int = 1024, d: int = 768, heads: int = 12, layers: int = 12,
+                 vocab: int = 50257, lr: float = 0.01) -> str:
+    """BASELINE.json configs[3]: GPT-2 small training on synthetic tokens.
+
+    Pre-LayerNorm decoder: token + learned position embeddings, ``layers`` blocks of causal
+    multi-head attention (bmm + causal_softmax) and a GELU MLP, final layernorm, tied LM
+    head, cross-entropy on next-token ids.  The backward pass is written out (no autodiff
+    in the language); SGD with a learning-rate scale halved by a data-dependent
+    ``while`` loop over the fetched loss (the "Python loop" of the config).  Extension ops
+    (SURVEY §2.4); parity against the builder's f64 restatement.
+    """
+    B, T, D, H, L, V = batch, seq, d, heads, layers, vocab
+    hd = D // H
+    BT, BH = B * T, B * H
+    sc = 1.0 / (hd ** 0.5)
+    v = [f"var wte = mul(input(\"wte_init\", [{V}, {D}]), 0.02)",
+         f"var wpe = mul(input(\"wpe_init\", [{T}, {D}]), 0.01)",
+         f"var gf = fill([{D}], 1.0)", f"var bfn = fill([{D}], 0.0)"]
+    for l in range(L):
+        v += [f"var g1_{l} = fill([{D}], 1.0)", f"var b1_{l} = fill([{D}], 0.0)",
+              f"var g2_{l} = fill([{D}], 1.0)", f"var b2_{l} = fill([{D}], 0.0)"]
+        for w in ("q", "k", "v", "o"):
+            v += [f"var w{w}_{l} = mul(input(\"w{w}{l}_init\", [{D}, {D}]), 0.02)",
+                  f"var c{w}_{l} = fill([{D}], 0.0)"]
+        v += [f"var wf1_{l} = mul(input(\"wf1{l}_init\", [{D}, {4 * D}]), 0.02)", f"var cf1_{l} = fill([{4 * D}], 0.0)",
+              f"var wf2_{l} = mul(input(\"wf2{l}_init\", [{4 * D}, {D}]), 0.02)", f"var cf2_{l} = fill([{D}], 0.0)"]
+
+    def heads_of(x):
+        return f"reshape(transpose(reshape({x}, [{B}, {T}, {H}, {hd}]), [0, 2, 1, 3]), [{BH}, {T}, {hd}])"
+
+    def merge(x):
+        return f"reshape(transpose(reshape({x}, [{B}, {H}, {T}, {hd}]), [0, 2, 1, 3]), [{BT}, {D}])"
+
+    b = [f"let tok = to_index(input(\"tokens\", [{B}, {T}]), {float(V)})",
+         f"let tgt = to_index(input(\"targets\", [{BT}]), {float(V)})",
+         f"let emb = embedding(wte, tok)",
+         f"let x0 = reshape(bias_add(reshape(emb, [{B}, {T * D}]), reshape(wpe, [{T * D}])), [{BT}, {D}])"]
+    for l in range(L):
+        x = f"x{l}"
+        b += [f"let h1_{l} = layernorm({x}, g1_{l}, b1_{l})"]
+        for w in ("q", "k", "v"):
+            b += [f"let {w}_{l} = bias_add(matmul(h1_{l}, w{w}_{l}), c{w}_{l})",
+                  f"let {w}h_{l} = {heads_of(f'{w}_{l}')}"]
+        b += [f"let p_{l} = causal_softmax(bmm_nt(qh_{l}, kh_{l}), {sc})",
+              f"let o_{l} = {merge(f'bmm(p_{l}, vh_{l})')}",
+              f"let xa_{l} = add({x}, bias_add(matmul(o_{l}, wo_{l}), co_{l}))",
+              f"let h2_{l} = layernorm(xa_{l}, g2_{l}, b2_{l})",
+              f"let pre_{l} = bias_add(matmul(h2_{l}, wf1_{l}), cf1_{l})",
+              f"let f_{l} = gelu(pre_{l})",
+              f"let x{l + 1} = add(xa_{l}, bias_add(matmul(f_{l}, wf2_{l}), cf2_{l}))"]
+    b += [f"let hf = layernorm(x{L}, gf, bfn)",
+          f"let logits = matmul(hf, transpose(wte))",
+          f"let loss = cross_entropy(logits, tgt)",
+          f"let dlog = cross_entropy_grad(logits, tgt)",
+          f"let dwte_h = matmul(transpose(dlog), hf)",
+          f"let dhf = matmul(dlog, wte)",
+          f"let dx{L} = layernorm_dx(x{L}, gf, dhf)",
+          f"let dgf = ln_dgamma(x{L}, dhf)",
+          f"let dbf = sum_rows(dhf)"]
+    for l in range(L - 1, -1, -1):
+        dm = f"dx{l + 1}"
+        b += [f"let dwf2_{l} = matmul(transpose(f_{l}), {dm})",
+              f"let dcf2_{l} = sum_rows({dm})",
+              f"let dpre_{l} = gelu_grad(pre_{l}, matmul({dm}, transpose(wf2_{l})))",
+              f"let dwf1_{l} = matmul(transpose(h2_{l}), dpre_{l})",
+              f"let dcf1_{l} = sum_rows(dpre_{l})",
+              f"let dh2_{l} = matmul(dpre_{l}, transpose(wf1_{l}))",
+              f"let dxa_{l} = add({dm}, layernorm_dx(xa_{l}, g2_{l}, dh2_{l}))",
+              f"let dg2_{l} = ln_dgamma(xa_{l}, dh2_{l})",
+              f"let db2_{l} = sum_rows(dh2_{l})",
+              f"let dwo_{l} = matmul(transpose(o_{l}), dxa_{l})",
+              f"let dco_{l} = sum_rows(dxa_{l})",
+              f"let doh_{l} = {heads_of(f'matmul(dxa_{l}, transpose(wo_{l}))')}",
+              f"let ds_{l} = softmax_grad(p_{l}, bmm_nt(doh_{l}, vh_{l}), {sc})",
+              f"let dq_{l} = {merge(f'bmm(ds_{l}, kh_{l})')}",
+              f"let dk_{l} = {merge(f'bmm_tn(ds_{l}, qh_{l})')}",
+              f"let dv_{l} = {merge(f'bmm_tn(p_{l}, doh_{l})')}"]
+        for w in ("q", "k", "v"):
+            b += [f"let dw{w}_{l} = matmul(transpose(h1_{l}), d{w}_{l})", f"let dc{w}_{l} = sum_rows(d{w}_{l})"]
+        b += [f"let dh1_{l} = add(add(matmul(dq_{l}, transpose(wq_{l})), matmul(dk_{l}, transpose(wk_{l}))), "
+              f"matmul(dv_{l}, transpose(wv_{l})))",
+              f"let dx{l} = add(dxa_{l}, layernorm_dx(x{l}, g1_{l}, dh1_{l}))",
+              f"let dg1_{l} = ln_dgamma(x{l}, dh1_{l})",
+              f"let db1_{l} = sum_rows(dh1_{l})"]
+    b += [f"let dwpe = reshape(sum_rows(reshape(dx0, [{B}, {T * D}])), [{T}, {D}])",
+          f"let dwte = add(dwte_h, embedding_dw(tok, reshape(dx0, [{B}, {T}, {D}]), [{V}]))",
+          f"let l = item(loss)",
+          f"let lrs = fill([], {lr})",
+          f"let k = 0",
+          f"while l > {round(math.log(V), 3)} and k < 2 {{ lrs = mul(lrs, 0.5); k = k + 1 }}",
+          f"wte = sub(wte, mul(dwte, lrs))",
+          f"wpe = sub(wpe, mul(dwpe, lrs))",
+          f"gf = sub(gf, mul(dgf, lrs))",
+          f"bfn = sub(bfn, mul(dbf, lrs))"]
+    for l in range(L):
+        for w in ("q", "k", "v", "o"):
+            b += [f"w{w}_{l} = sub(w{w}_{l}, mul(dw{w}_{l}, lrs))", f"c{w}_{l} = sub(c{w}_{l}, mul(dc{w}_{l}, lrs))"]
+        for nm in ("wf1", "cf1", "wf2", "cf2", "g1", "b1", "g2", "b2"):
+            b += [f"{nm}_{l} = sub({nm}_{l}, mul(d{nm}_{l}, lrs))"]
+    b += ["print(l)"]
+    return "\n".join(v) + f"\nsteps {steps} {{\n  " + "\n  ".join(b) + "\n}\n"
+
+
+C4 = dict(batch=8, seq=1024, d=768, heads=12, layers=12, vocab=50257)
+C4_SMALL = dict(batch=2, seq=32, d=64, heads=4, layers=2, vocab=97)
+
+
+def gpt2_flops(batch=8, seq=1024, d=768, heads=12, layers=12, vocab=50257, **_) -> int:
+    """GEMM FLOPs of one C4 training step (forward + backward, 2*M*N*K per product)."""
+    bt = batch * seq
+    per_layer_fwd = 2 * bt * d * (3 * d) + 2 * bt * d * d + 2 * bt * d * 4 * d * 2 + 2 * 2 * batch * heads * seq * seq * (d // heads)
+    head_fwd = 2 * bt * d * vocab
+    return 3 * (layers * per_layer_fwd + head_fwd)
 
 
 class InMemoryDataset(DatasetSource):
