@@ -26,6 +26,7 @@ namespace coex {
   } while (0)
 
 constexpr int kMaxRank = 8;
+constexpr int kMaxDevVars = 1024;   // variables per context (runtime.cu kMaxVars)
 constexpr int kMaxPub = 6;
 
 // ------------------------------------------------------------------ pass state
@@ -102,8 +103,9 @@ struct Mailbox {
   volatile unsigned long long stall_ns;
   volatile long long ops;
   volatile long long fetches;
-  volatile unsigned long long dirty_mask;
-  volatile int var_shape_id[64];
+  volatile unsigned long long dirty_mask;        // first 64 variables (coex_pass_stats)
+  volatile unsigned long long dirty[kMaxDevVars / 64];   // every variable committed by the pass
+  volatile int var_shape_id[kMaxDevVars];
   DecEntry dec[kDecCap];
   FeedEntry feed[kFeedCap];
   FetchEntry fetch[kFetchCap];
@@ -1295,15 +1297,20 @@ __global__ void k_pass_end(EndParams p) {
   DevState* ds = p.ds;
   if (threadIdx.x != 0) return;
   stamp(ds, SK_END);
-  unsigned long long mask = 0;
-  if (!ds->cancelled) {
-    for (int i = 0; i < p.nvars && i < 64; ++i)
-      if (p.var_ovl[i] != nullptr) {
-        mask |= 1ull << i;
-        p.mb->var_shape_id[i] = p.var_ovl_shape[i];
+  for (int w = 0; w < kMaxDevVars / 64; ++w) {
+    unsigned long long mask = 0;
+    if (!ds->cancelled) {
+      for (int b = 0; b < 64; ++b) {
+        const int i = w * 64 + b;
+        if (i < p.nvars && p.var_ovl[i] != nullptr) {
+          mask |= 1ull << b;
+          p.mb->var_shape_id[i] = p.var_ovl_shape[i];
+        }
       }
+    }
+    p.mb->dirty[w] = mask;
+    if (w == 0) p.mb->dirty_mask = mask;
   }
-  p.mb->dirty_mask = mask;
   p.mb->committed = ds->cancelled ? 0 : 1;
   p.mb->status = ds->status;
   p.mb->exec_ns = globaltimer() - ds->t_begin;

@@ -14,6 +14,7 @@
 //   decisions and fed values.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
 #include <cstddef>
 #include <chrono>
@@ -55,6 +56,7 @@ int fail(int code, const std::string& msg) {
   } while (0)
 
 constexpr int kMaxVars = 1024;
+static_assert(kMaxVars == kMaxDevVars, "variable table sizes");
 constexpr int kNumSMs = 148;
 
 struct Buf {
@@ -318,7 +320,8 @@ int infer_ext(int kind, const coex_attrs* at, const TRec* in, int* ndim, int64_t
       const TRec& x = in[0];
       if (x.ndim < 1 || x.numel == 0) return fail(COEX_SHAPE_MISMATCH, "column op: non-empty operand of rank >= 1 required");
       const int64_t C = x.shape[x.ndim - 1];
-      if (C > (int64_t)kColMaxSlots * 256) return fail(COEX_SHAPE_MISMATCH, "column op: more than 2048 channels");
+      if (kind != COEX_SUM_ROWS && C > (int64_t)kColMaxSlots * 256)
+        return fail(COEX_SHAPE_MISMATCH, "column op: more than 2048 channels");
       if (kind == COEX_SUM_ROWS || kind == COEX_BN_DGAMMA) {
         if (kind == COEX_BN_DGAMMA && !same(x, in[1])) return fail(COEX_SHAPE_MISMATCH, "bn_dgamma: dy differs from x");
         *ndim = 1;
@@ -1121,6 +1124,20 @@ int build_xop_t(coex_ctx* c, const OpSpec& s, Launch* L, int* nL, size_t* ws_byt
     }
     case COEX_BATCHNORM: case COEX_BATCHNORM_DX: case COEX_BN_DGAMMA: case COEX_SUM_ROWS: case kBnBwdFused: {
       const int64_t C = s.in_shape[0][s.in_ndim[0] - 1];
+      if (s.kind == COEX_SUM_ROWS && C > 1024) {   // wide rows: column-parallel sum
+        const int64_t Rw = numel_of(s.in_ndim[0], s.in_shape[0]) / C;
+        const int64_t gx = (C + 255) / 256;
+        int64_t gy = 1;
+        while (gy < 64 && gx * gy < kNumSMs * 4 && Rw / (gy * 2) >= 64) gy *= 2;
+        RowParams rp{};
+        rp.ds = s.ds; rp.x = s.in[0]; rp.rows = Rw; rp.d = C; rp.out = s.out;
+        if (gy > 1) rp.acc = (double*)cv.take((size_t)C * 8);
+        if (!build) break;
+        L[(*nL)++].set(is_f64(c) ? (void*)k_colsum_wide<double> : (void*)k_colsum_wide<float>,
+                       dim3((unsigned)gx, (unsigned)gy), dim3(256), rp);
+        if (gy > 1) L[(*nL)++].set(is_f64(c) ? (void*)k_acc_out<double> : (void*)k_acc_out<float>, grid_for(C), dim3(256), rp);
+        return COEX_OK;
+      }
       const int64_t n = numel_of(s.in_ndim[0], s.in_shape[0]);
       const int64_t R = n / C;
       // partial blocks: enough to stream x at full bandwidth, few enough that the last block's
@@ -2388,7 +2405,7 @@ int coex_prog_build(coex_ctx* c, const int64_t* plan, int64_t nwords, const doub
     }
     // variables committed by this program
     const int64_t ncommit = b.next();
-    if (ncommit > kMaxCommit) throw std::runtime_error("too many assigned variables");
+    if (ncommit > kMaxVars) throw std::runtime_error("too many assigned variables");
     for (int64_t i = 0; i < ncommit; ++i) {
       p->commit_vars.push_back((int)b.next());
       p->commit_bytes.push_back(b.next());
@@ -2420,13 +2437,13 @@ int coex_prog_build(coex_ctx* c, const int64_t* plan, int64_t nwords, const doub
       rc = b.add_kernel(p->graph, &prev, L);
       if (rc) throw std::runtime_error(g_err);
     }
-    if (!p->commit_vars.empty()) {
+    for (size_t base = 0; base < p->commit_vars.size(); base += kMaxCommit) {   // kMaxCommit per launch
       CommitParams cp{};
       cp.ds = c->d_state;
-      cp.n = (int)p->commit_vars.size();
+      cp.n = (int)std::min((size_t)kMaxCommit, p->commit_vars.size() - base);
       for (int i = 0; i < cp.n; ++i) {
-        cp.var_index[i] = p->commit_vars[i];
-        cp.bytes[i] = p->commit_bytes[i];
+        cp.var_index[i] = p->commit_vars[base + i];
+        cp.bytes[i] = p->commit_bytes[base + i];
       }
       cp.var_cur = c->d_var_cur;
       cp.var_ovl = c->d_var_ovl;
@@ -2685,7 +2702,7 @@ int coex_pass_wait(coex_prog* p, coex_pass_stats* st) {
     // host bookkeeping of committed variables: the spare became the value
     for (size_t i = 0; i < p->commit_vars.size(); ++i) {
       int vi = p->commit_vars[i];
-      if (vi >= 64 || !((mb->dirty_mask >> vi) & 1ull)) continue;
+      if (vi >= kMaxVars || !((mb->dirty[vi / 64] >> (vi % 64)) & 1ull)) continue;
       Var& v = c->vars[vi];
       Buf* old = v.t.buf;
       v.t.buf = v.spare;

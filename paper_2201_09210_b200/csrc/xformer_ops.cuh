@@ -378,4 +378,42 @@ __global__ void __launch_bounds__(256) k_cross_entropy(RowParams p) {
   }
 }
 
+// ------------------------------------------------------------------ wide column sums
+// sum_rows for wide rows (C > 1024, e.g. the position-embedding gradient [B, T*d] or the MLP
+// bias gradient [B*T, 4d]): each thread owns one column and adds a chunk of rows in order;
+// one chunk -> written directly, several chunks (grid.y) -> fp64 atomics into p.acc and a
+// k_acc_out pass.   (x operand, rows x d)
+template <typename T>
+__global__ void __launch_bounds__(256) k_colsum_wide(RowParams p) {
+  COEX_PDL_ENTER();
+  stamp(p.ds, SK_COLSTATS);
+  if (skip(p.ds)) return;
+  const T* x = res<T>(p.x);
+  T* o = pick_out<T>(p.out, x, nullptr);
+  if (gridDim.y == 1) publish_early(p.out, o);
+  if (blockIdx.y == 0) count_op(p.ds);
+  const long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long r0 = p.rows * blockIdx.y / gridDim.y, r1 = p.rows * (blockIdx.y + 1) / gridDim.y;
+  if (c < p.d) {
+    double acc = 0.0;
+    for (long long r = r0; r < r1; ++r) acc += (double)x[r * p.d + c];
+    if (gridDim.y == 1) o[c] = (T)acc;
+    else atomicAdd(p.acc + c, acc);
+  }
+  if (gridDim.y == 1) publish_late(p.out, o);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_acc_out(RowParams p) {
+  COEX_PDL_ENTER();
+  if (skip(p.ds)) return;
+  T* o = pick_out<T>(p.out, res<T>(p.x), nullptr);
+  publish_early(p.out, o);
+  for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < p.d; c += (long long)gridDim.x * blockDim.x) {
+    o[c] = (T)p.acc[c];
+    p.acc[c] = 0.0;                                  // re-zero for the next launch
+  }
+  publish_late(p.out, o);
+}
+
 }  // namespace coex

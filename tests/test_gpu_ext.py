@@ -71,6 +71,8 @@ BN = [
     (OpKind.SUM_ROWS, {}, [rt(4, 4, 4, 8)]),
     (OpKind.SUM_ROWS, {}, [rt(3000, 513)]),
     (OpKind.SUM_ROWS, {}, [rt(5)]),
+    (OpKind.SUM_ROWS, {}, [rt(8, 5000)]),        # wide rows: column-parallel kernel
+    (OpKind.SUM_ROWS, {}, [rt(4096, 3072)]),     # wide rows, row chunks + fp64 atomics
 ]
 
 EDGE = np.array([-800.0, -30.0, -1.0, -0.0, 0.0, 1e-30, 0.5, 30.0, 800.0, np.nan])
