@@ -236,7 +236,8 @@ class B200Backend:
     STAMP_KINDS = {0: "begin", 1: "elementwise", 2: "reduce", 3: "transpose", 4: "matmul", 5: "ptr-op",
                    6: "decide", 7: "feed-wait", 8: "feed-fill", 9: "fetch", 10: "commit-gate", 11: "commit",
                    12: "end", 13: "fused chain", 14: "im2col", 15: "col2im", 16: "bf16 cvt", 17: "colstats",
-                   18: "bn apply", 19: "split-K reduce"}
+                   18: "bn apply", 19: "split-K reduce", 20: "causal softmax", 21: "softmax grad",
+                   22: "cross-entropy", 23: "bias add", 24: "layernorm", 25: "embedding", 26: "column sum"}
 
     def set_trace(self, capacity: int):
         """Enable device-side per-kernel stamps (0 disables)."""

@@ -148,6 +148,11 @@ struct TcGemmParams {
   TcConv cv;
   int batch;                 // batched GEMM (bmm): 3-D tensor maps {inner, rows, batch}; C + b * c_bstride
   long long c_bstride;
+  // causal attention structure (planner-proven, see planner.py _tri_flags):
+  //   tri_out: only the lower triangle (col <= row) of C is ever read -> tiles strictly above
+  //            the diagonal are skipped (no MMA, no store);
+  //   tri_a:   A is lower- (1) / upper- (2) triangular in (m, k) -> K blocks outside are zero
+  int tri_out, tri_a;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -288,6 +293,17 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc(const __grid_constant
     n0 = (int)(((t % group) / gm) * BN);
     kb0 = (int)((long long)nk_all * split / splits);
     nk = (int)((long long)nk_all * (split + 1) / splits) - kb0;
+    if (p.tri_out && n0 >= m0 + TC_BM) nk = -1;               // tile above the diagonal: skipped
+    else if (p.tri_a == 1) {                                  // A[m][k] == 0 for k > m
+      const int hi = (m0 + TC_BM + TC_BK - 1) / TC_BK;
+      if (kb0 + nk > hi) nk = hi - kb0 > 0 ? hi - kb0 : 0;
+    } else if (p.tri_a == 2) {                                // A[m][k] == 0 for k < m
+      const int lo = m0 / TC_BK, end = kb0 + nk;
+      if (kb0 < lo) {
+        kb0 = lo < end ? lo : end;
+        nk = end - kb0;
+      }
+    }
   };
 
   float* Cout = nullptr;
@@ -444,7 +460,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc(const __grid_constant
       mbar_wait(&tfull[a], aph);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll 1
-      for (int c = 0; c < BN; c += 32) {
+      for (int c = 0; c < (nk < 0 ? 0 : BN); c += 32) {
         uint32_t r[32];
         if (nk > 0) {
           const uint32_t taddr = tmem + ((uint32_t)lane_base << 16) + (uint32_t)(a * BN + c);

@@ -52,7 +52,8 @@ enum StampKind {
   SK_BEGIN = 0, SK_EW = 1, SK_REDUCE = 2, SK_TRANSPOSE = 3, SK_MATMUL = 4, SK_PTR = 5, SK_DECIDE = 6,
   SK_FEED_WAIT = 7, SK_FEED_FILL = 8, SK_FETCH = 9, SK_GATE = 10, SK_COMMIT = 11, SK_END = 12,
   SK_AFTER_WAIT = 64, SK_FUSED = 13, SK_IM2COL = 14, SK_COL2IM = 15, SK_CVT = 16, SK_COLSTATS = 17,
-  SK_BNAPPLY = 18, SK_SPLITK = 19
+  SK_BNAPPLY = 18, SK_SPLITK = 19, SK_SOFTMAX = 20, SK_SOFTMAX_GRAD = 21, SK_CE = 22, SK_BIAS = 23, SK_LN = 24,
+  SK_EMBED = 25, SK_COLSUM = 26
 };
 
 // Host <-> device rings in pinned, mapped host memory.
@@ -401,6 +402,36 @@ __global__ void __launch_bounds__(256) k_transpose(TransposeParams p) {
       rem = q;
     }
     o[i] = a[src];
+  }
+  publish_late(p.out, o);
+}
+
+// Transpose that keeps the innermost axis (e.g. the attention head split [B,T,H,hd] ->
+// [B,H,T,hd]): whole rows of `inner` contiguous elements move, 16-byte vectors per thread,
+// 32-bit index arithmetic per row (rank <= 4 outer axes).
+template <typename T>
+__global__ void __launch_bounds__(256) k_transpose_rows(TransposeParams p) {
+  COEX_PDL_ENTER();
+  stamp(p.ds, SK_TRANSPOSE);
+  if (skip(p.ds)) return;
+  const T* a = res<T>(p.a);
+  T* o = pick_out<T>(p.out, a, nullptr);
+  publish_early(p.out, o);
+  count_op(p.ds);
+  constexpr int V = 16 / sizeof(T);
+  const long long inner = p.out_shape[p.rank - 1];
+  const long long vpr = inner / V;                 // vectors per row
+  const long long rows = p.n / inner;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long u = (long long)blockIdx.x * blockDim.x + threadIdx.x; u < rows * vpr; u += stride) {
+    const long long r = u / vpr, e = (u - r * vpr) * V;
+    long long rem = r, src = 0;
+    for (int d = p.rank - 2; d >= 0; --d) {
+      const long long idx = rem % p.out_shape[d];
+      rem /= p.out_shape[d];
+      src += idx * p.src_stride[d];
+    }
+    *(uint4*)(o + r * inner + e) = *(const uint4*)(a + src + e);
   }
   publish_late(p.out, o);
 }

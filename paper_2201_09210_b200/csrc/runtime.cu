@@ -464,6 +464,8 @@ struct OpSpec {
   char* ws = nullptr;                      // extension ops: workspace base (nullptr = size query)
   Out out{};
   Out out2{}, out3{};                      // fused batch-norm backward: dgamma, dbeta
+  void* shadow = nullptr;                  // bf16 copy of the output to write (softmax-type producers)
+  void* in_shadow[kMaxIn] = {nullptr, nullptr, nullptr};   // bf16 copies of inputs (batched GEMM A)
   DevState* ds = nullptr;
 };
 
@@ -640,7 +642,11 @@ int build_launch_t(coex_ctx* c, const OpSpec& s, Launch* L) {
         L->set((void*)k_transpose2d<T>, dim3((unsigned)(tiles < kNumSMs * 8 ? (tiles < 1 ? 1 : tiles) : kNumSMs * 8)),
                dim3(32, 8), p);
       } else {
-        L->set((void*)k_transpose<T>, grid_for(n), dim3(256), p);
+        const int64_t inner = s.out_shape[s.out_ndim - 1];
+        if (s.out_ndim >= 2 && s.attr_dims[s.out_ndim - 1] == s.out_ndim - 1 && inner % (16 / (int64_t)sizeof(T)) == 0)
+          L->set((void*)k_transpose_rows<T>, grid_for(n / (16 / sizeof(T))), dim3(256), p);
+        else
+          L->set((void*)k_transpose<T>, grid_for(n), dim3(256), p);
       }
       return COEX_OK;
     }
@@ -1124,8 +1130,9 @@ int build_xop_t(coex_ctx* c, const OpSpec& s, Launch* L, int* nL, size_t* ws_byt
     }
     case COEX_BATCHNORM: case COEX_BATCHNORM_DX: case COEX_BN_DGAMMA: case COEX_SUM_ROWS: case kBnBwdFused: {
       const int64_t C = s.in_shape[0][s.in_ndim[0] - 1];
-      if (s.kind == COEX_SUM_ROWS && C > 1024) {   // wide rows: column-parallel sum
-        const int64_t Rw = numel_of(s.in_ndim[0], s.in_shape[0]) / C;
+      const int64_t Rw = numel_of(s.in_ndim[0], s.in_shape[0]) / C;
+      if (s.kind == COEX_SUM_ROWS && (C > 1024 || (!is_f64(c) && Rw >= 4096 && C >= 256))) {
+        // wide rows / tall tolerance-mode sums: column-parallel sum over row chunks
         const int64_t gx = (C + 255) / 256;
         int64_t gy = 1;
         while (gy < 64 && gx * gy < kNumSMs * 4 && Rw / (gy * 2) >= 64) gy *= 2;
@@ -1201,13 +1208,22 @@ int build_xop_t(coex_ctx* c, const OpSpec& s, Launch* L, int* nL, size_t* ws_byt
         // B [B][K][N] (MN-major) or [B][N][K] (nt: K-major); 3-D TMA maps, batch = grid items
         const TcPlan t = tc_plan(M * Bt, N, K, false);
         const int64_t arow = tn ? K : M, acol = tn ? M : K, brow = nt ? N : K, bcol = nt ? K : N;
-        void* A = cv.take((size_t)Bt * arow * bf16_pitch(acol) * 2);
+        const bool a_sh = s.in_shadow[0] != nullptr && acol % 8 == 0;   // producer wrote a bf16 copy
+        void* A = a_sh ? s.in_shadow[0] : cv.take((size_t)Bt * arow * bf16_pitch(acol) * 2);
         void* B = cv.take((size_t)Bt * brow * bf16_pitch(bcol) * 2);
         if (!build) break;
-        cvt_rows_launch(s.ds, s.in[0], A, Bt * arow, acol, &L[(*nL)++]);
+        if (!a_sh) cvt_rows_launch(s.ds, s.in[0], A, Bt * arow, acol, &L[(*nL)++]);
         cvt_rows_launch(s.ds, s.in[1], B, Bt * brow, bcol, &L[(*nL)++]);
-        return tc_gemm_launches(c, s.ds, A, B, M, N, K, t, s.in[0], s.in[1], s.out, nullptr, nullptr, L, nL,
-                                tn ? 1 : 0, !nt, nullptr, nullptr, Bt);
+        const int rc = tc_gemm_launches(c, s.ds, A, B, M, N, K, t, s.in[0], s.in[1], s.out, nullptr, nullptr, L, nL,
+                                        tn ? 1 : 0, !nt, nullptr, nullptr, Bt);
+        // planner-proven causal structure (attr dims[0]: 1 = only C's lower triangle is read,
+        // 2 = A lower-triangular, 3 = A upper-triangular)
+        if (rc == COEX_OK && s.attr_n >= 1 && s.attr_dims[0] > 0) {
+          TcGemmParams* gp = (TcGemmParams*)L[*nL - 1].params;
+          if (s.attr_dims[0] == 1) gp->tri_out = 1;
+          else gp->tri_a = (int)s.attr_dims[0] - 1;
+        }
+        return rc;
       }
       if (!build) break;
       MatmulParams mp{};
@@ -1228,6 +1244,7 @@ int build_xop_t(coex_ctx* c, const OpSpec& s, Launch* L, int* nL, size_t* ws_byt
       rp.z = s.nin > 2 ? s.in[2] : In{nullptr, nullptr, nullptr};
       rp.out = s.out;
       rp.scale = s.value;
+      rp.shadow = (__nv_bfloat16*)s.shadow;
       const int64_t xn = numel_of(s.in_ndim[0], s.in_shape[0]);
       const int64_t d = s.in_shape[0][s.in_ndim[0] - 1];
       auto warp_rows = [&](int64_t rows) {
@@ -2110,6 +2127,8 @@ struct Builder {
           read_out(s.out2);
           read_out(s.out3);
         }
+        s.shadow = buf(next());
+        for (int i = 0; i < kMaxIn; ++i) s.in_shadow[i] = buf(next());
         Launch L[kMaxLaunches];
         int nL = 0;
         size_t wb = 0;

@@ -25,6 +25,7 @@ struct RowParams {
   double* acc;               // column accumulators (ln_dgamma) / per-row losses (cross-entropy)
   unsigned int* counter;
   Out out;
+  __nv_bfloat16* shadow;     // optional bf16 copy of the output (consumed by batched GEMMs)
 };
 
 template <typename A>
@@ -64,7 +65,7 @@ __device__ __forceinline__ bool last_block(unsigned int* counter) {
 template <typename T>
 __global__ void __launch_bounds__(256) k_embed(RowParams p) {
   COEX_PDL_ENTER();
-  stamp(p.ds, SK_EW);
+  stamp(p.ds, SK_EMBED);
   if (skip(p.ds)) return;
   const T* tab = res<T>(p.x);
   const T* ids = res<T>(p.y);
@@ -86,7 +87,7 @@ __global__ void __launch_bounds__(256) k_embed(RowParams p) {
 template <typename T>
 __global__ void __launch_bounds__(256) k_embed_dw(RowParams p) {
   COEX_PDL_ENTER();
-  stamp(p.ds, SK_EW);
+  stamp(p.ds, SK_EMBED);
   if (skip(p.ds)) return;
   const T* ids = res<T>(p.x);
   const T* dy = res<T>(p.y);
@@ -127,7 +128,7 @@ __global__ void __launch_bounds__(256) k_zero(ZeroParams p) {
 template <typename T>
 __global__ void __launch_bounds__(256) k_bias_add(RowParams p) {
   COEX_PDL_ENTER();
-  stamp(p.ds, SK_EW);
+  stamp(p.ds, SK_BIAS);
   if (skip(p.ds)) return;
   const T* x = res<T>(p.x);
   const T* b = res<T>(p.y);
@@ -169,7 +170,7 @@ __device__ __forceinline__ void ln_row_stats(const T* xr, long long d, int lane,
 template <typename T, int MODE>
 __global__ void __launch_bounds__(256) k_layernorm(RowParams p) {
   COEX_PDL_ENTER();
-  stamp(p.ds, SK_BNAPPLY);
+  stamp(p.ds, SK_LN);
   if (skip(p.ds)) return;
   const T* x = res<T>(p.x);
   const T* g = res<T>(p.y);
@@ -211,7 +212,7 @@ __global__ void __launch_bounds__(256) k_layernorm(RowParams p) {
 template <typename T>
 __global__ void __launch_bounds__(256) k_ln_dgamma(RowParams p) {
   COEX_PDL_ENTER();
-  stamp(p.ds, SK_COLSTATS);
+  stamp(p.ds, SK_LN);
   if (skip(p.ds)) return;
   const T* x = res<T>(p.x);
   const T* dy = res<T>(p.y);
@@ -261,7 +262,7 @@ __global__ void __launch_bounds__(256) k_ln_dgamma(RowParams p) {
 template <typename T>
 __global__ void __launch_bounds__(256) k_causal_softmax(RowParams p) {
   COEX_PDL_ENTER();
-  stamp(p.ds, SK_EW);
+  stamp(p.ds, SK_SOFTMAX);
   if (skip(p.ds)) return;
   const T* x = res<T>(p.x);
   T* o = pick_out<T>(p.out, x, nullptr);
@@ -283,8 +284,11 @@ __global__ void __launch_bounds__(256) k_causal_softmax(RowParams p) {
     for (long long c = lane; c <= i; c += 32) s += ex((A)xr[c] * sc - mx);
     s = warp_sum(s);
     const A inv = (A)1 / s;
-    for (long long c = lane; c < d; c += 32)
-      orow[c] = c <= i ? (T)(ex((A)xr[c] * sc - mx) * inv) : T(0);
+    for (long long c = lane; c < d; c += 32) {
+      const A v = c <= i ? ex((A)xr[c] * sc - mx) * inv : (A)0;
+      orow[c] = (T)v;
+      if (p.shadow) p.shadow[r * d + c] = __float2bfloat16_rn((float)v);
+    }
   }
   publish_late(p.out, o);
 }
@@ -293,7 +297,7 @@ __global__ void __launch_bounds__(256) k_causal_softmax(RowParams p) {
 template <typename T>
 __global__ void __launch_bounds__(256) k_softmax_grad(RowParams p) {
   COEX_PDL_ENTER();
-  stamp(p.ds, SK_EW);
+  stamp(p.ds, SK_SOFTMAX_GRAD);
   if (skip(p.ds)) return;
   const T* y = res<T>(p.x);
   const T* dy = res<T>(p.y);
@@ -307,11 +311,20 @@ __global__ void __launch_bounds__(256) k_softmax_grad(RowParams p) {
   for (long long r = (long long)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; r < p.rows; r += warps) {
     const T* yr = y + r * d;
     const T* gr = dy + r * d;
+    // entries with y == 0 (causal mask) contribute nothing and their dy is never read (the
+    // planner may skip computing dy there)
     A dot = 0;
-    for (long long c = lane; c < d; c += 32) dot += (A)gr[c] * (A)yr[c];
+    for (long long c = lane; c < d; c += 32) {
+      const A yv = (A)yr[c];
+      if (yv != (A)0) dot += (A)gr[c] * yv;
+    }
     dot = warp_sum(dot);
-    for (long long c = lane; c < d; c += 32)
-      o[r * d + c] = (T)((A)p.scale * ((A)yr[c] * ((A)gr[c] - dot)));
+    for (long long c = lane; c < d; c += 32) {
+      const A yv = (A)yr[c];
+      const A v = yv != (A)0 ? (A)p.scale * (yv * ((A)gr[c] - dot)) : (A)0;
+      o[r * d + c] = (T)v;
+      if (p.shadow) p.shadow[r * d + c] = __float2bfloat16_rn((float)v);
+    }
   }
   publish_late(p.out, o);
 }
@@ -322,43 +335,52 @@ __global__ void __launch_bounds__(256) k_softmax_grad(RowParams p) {
 template <typename T, int MODE>
 __global__ void __launch_bounds__(256) k_cross_entropy(RowParams p) {
   COEX_PDL_ENTER();
-  stamp(p.ds, MODE ? SK_EW : SK_REDUCE);
+  stamp(p.ds, SK_CE);
   if (skip(p.ds)) return;
+  typedef typename AccT<T>::type A;
   const T* lg = res<T>(p.x);
   const T* ids = res<T>(p.y);
   T* o = pick_out<T>(p.out, lg, ids);
   if (MODE == 1) publish_early(p.out, o);
   count_op(p.ds);
-  __shared__ double red[32];
+  __shared__ A redm[32], reds[32];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const long long V = p.d;
   for (long long r = blockIdx.x; r < p.rows; r += gridDim.x) {
     const T* row = lg + r * V;
-    double mx = -INFINITY;
-    for (long long c = threadIdx.x; c < V; c += blockDim.x) mx = fmax(mx, (double)row[c]);
-    mx = warp_max(mx);
-    if (lane == 0) red[wid] = mx;
+    // online max / sum of exponentials in one pass (rescaling the partial sum on a new max)
+    A mx = -INFINITY, sm = 0;
+    for (long long c = threadIdx.x; c < V; c += blockDim.x) {
+      const A v = (A)row[c];
+      if (v > mx) {
+        sm = sm * ex(mx - v) + (A)1;
+        mx = v;
+      } else {
+        sm += ex(v - mx);
+      }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const A om = __shfl_xor_sync(0xffffffffu, mx, off), os = __shfl_xor_sync(0xffffffffu, sm, off);
+      const A nm = fmax(mx, om);
+      sm = (mx == -INFINITY ? (A)0 : sm * ex(mx - nm)) + (om == -INFINITY ? (A)0 : os * ex(om - nm));
+      mx = nm;
+    }
+    if (lane == 0) { redm[wid] = mx; reds[wid] = sm; }
     __syncthreads();
-    mx = red[0];
-    for (int w = 1; w < nw; ++w) mx = fmax(mx, red[w]);
-    __syncthreads();
-    typedef typename AccT<T>::type A;
-    A sa = 0;
-    for (long long c = threadIdx.x; c < V; c += blockDim.x) sa += ex((A)((double)row[c] - mx));
-    double s = warp_sum((double)sa);
-    if (lane == 0) red[wid] = s;
-    __syncthreads();
-    s = 0.0;
-    for (int w = 0; w < nw; ++w) s += red[w];
+    A gm = redm[0];
+    for (int w = 1; w < nw; ++w) gm = fmax(gm, redm[w]);
+    A gs = 0;
+    for (int w = 0; w < nw; ++w) gs += redm[w] == -INFINITY ? (A)0 : reds[w] * ex(redm[w] - gm);
     __syncthreads();
     double f = floor((double)ids[r]);
     const long long id = f < 0 ? 0 : (f > (double)(V - 1) ? V - 1 : (long long)f);
     if (MODE == 0) {
-      if (threadIdx.x == 0) p.acc[r] = (log(s) + mx) - (double)row[id];
+      if (threadIdx.x == 0) p.acc[r] = ((double)log(gs) + (double)gm) - (double)row[id];
     } else {
-      const A inv = (A)(1.0 / s), invr = (A)(1.0 / (double)p.rows);
+      const A inv = (A)1 / gs, invr = (A)(1.0 / (double)p.rows);
       for (long long c = threadIdx.x; c < V; c += blockDim.x) {
-        A g = ex((A)((double)row[c] - mx)) * inv;
+        A g = ex((A)row[c] - gm) * inv;
         if (c == id) g -= (A)1;
         o[r * V + c] = (T)(g * invr);
       }
@@ -386,7 +408,7 @@ __global__ void __launch_bounds__(256) k_cross_entropy(RowParams p) {
 template <typename T>
 __global__ void __launch_bounds__(256) k_colsum_wide(RowParams p) {
   COEX_PDL_ENTER();
-  stamp(p.ds, SK_COLSTATS);
+  stamp(p.ds, SK_COLSUM);
   if (skip(p.ds)) return;
   const T* x = res<T>(p.x);
   T* o = pick_out<T>(p.out, x, nullptr);

@@ -225,6 +225,18 @@ class Planner:
                 vcell[nid] = new_cell(b0)
             else:
                 vcell[nid] = new_cell(-1)
+        # bf16 shadows: a softmax-type node whose output feeds batched GEMMs as operand A also
+        # writes a bf16 copy, which those GEMMs read instead of converting the fp32 tensor
+        self.shadow = {}
+        if self.bf16:
+            for nid, x in ops.items():
+                if x.kind not in (OpKind.CAUSAL_SOFTMAX, OpKind.SOFTMAX_GRAD) or nid not in node_buf:
+                    continue
+                if node_buf[nid][2] or shapes[nid][-1] % 8 or any(nid in s_ for s_ in multi):
+                    continue
+                if any(c.kind in (OpKind.BMM, OpKind.BMM_TN) and not c.inputs[0].fed and c.inputs[0].cands == (nid,)
+                       for c in consumers.get(nid, [])):
+                    self.shadow[nid] = new_buf(shape_size(shapes[nid]) * 2)
         for s in list(multi):
             multi[s] = new_cell(-1)
         slot_buf: dict = {}
@@ -505,7 +517,7 @@ class Planner:
         word += [len(out_shape)] + _pad(out_shape)
         word += [0] + _pad([]) + [_f64_bits(0.0)]
         word += out_words(d.node_id, late) + out_words(g.node_id, late) + out_words(sr.node_id, late)
-        return word
+        return word + [-1] * (1 + MAX_XIN)
 
     def _xop_word(self, x, shapes, in_cell, out_words, pubs, n_compute, flops) -> list:
         nid = x.node_id
@@ -514,6 +526,9 @@ class Planner:
         late = _conflicts(cells, pubs[nid])
         n_compute[0] += 1
         attr = list(x.attrs["conv"]) if x.kind in CONV_KINDS else list(x.attrs.get("dims", ()))
+        if x.kind in BMM_KINDS and self.bf16:
+            tri = self._tri_flag(x)
+            attr = [tri] if tri else []
         if x.kind in CONV_KINDS or x.kind in BMM_KINDS:
             flops[0] += flops_of(x.kind, in_shapes, x.attrs)
         out_shape = shapes[nid]
@@ -523,7 +538,47 @@ class Planner:
         word += [len(out_shape)] + _pad(out_shape)
         word += [len(attr)] + _pad(attr) + [_f64_bits(float(x.attrs.get("value", 0.0)))]
         word += out_words(nid, late)
-        return word
+        return word + self._shadow_words(x)
+
+    def _causal_prob(self, b) -> bool:
+        """Binding b is (single-candidate) a causal_softmax output, or a softmax_grad of one --
+        both are exactly zero above the diagonal of every [T, T] block."""
+        if b.fed or len(b.cands) != 1:
+            return False
+        n = self.ops.get(b.cands[0])
+        if n is None:
+            return False
+        if n.kind is OpKind.CAUSAL_SOFTMAX:
+            return True
+        return n.kind is OpKind.SOFTMAX_GRAD and self._causal_prob(n.inputs[0])
+
+    def _tri_flag(self, x) -> int:
+        """Causal structure of a batched GEMM (tcgen05 path): 1 = only the lower triangle of
+        the output is ever read (QK^T into causal_softmax, dO.V^T into softmax_grad of a causal
+        softmax), 2 / 3 = operand A lower- / upper-triangular (P or dS, as stored / transposed)."""
+        if x.kind is OpKind.BMM_NT:
+            nid = x.node_id
+            cons = self.consumers.get(nid, [])
+            if not cons or nid in self.sp.fetch_nodes or any(nid in s_ for s_ in self._multi_sets()):
+                return 0
+            for c in cons:
+                if c.kind is OpKind.CAUSAL_SOFTMAX:
+                    continue
+                if c.kind is OpKind.SOFTMAX_GRAD and c.inputs[1].cands == (nid,) and \
+                        c.inputs[0].cands != (nid,) and self._causal_prob(c.inputs[0]):
+                    continue
+                return 0
+            return 1
+        if x.kind in (OpKind.BMM, OpKind.BMM_TN) and self._causal_prob(x.inputs[0]):
+            return 2 if x.kind is OpKind.BMM else 3
+        return 0
+
+    def _shadow_words(self, x) -> list:
+        """[own bf16 shadow buffer, bf16 shadow of each input (batched-GEMM operand A only)]."""
+        ins = [-1] * MAX_XIN
+        if x.kind in (OpKind.BMM, OpKind.BMM_TN) and not x.inputs[0].fed and len(x.inputs[0].cands) == 1:
+            ins[0] = self.shadow.get(x.inputs[0].cands[0], -1)
+        return [self.shadow.get(x.node_id, -1)] + ins
 
     # ------------------------------------------------------------ pointer-op rewrites
     def _pointer_rewrites(self, consumers, multi, folded):

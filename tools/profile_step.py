@@ -28,19 +28,22 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--precision", default="f64")
     ap.add_argument("--out", default=None)
-    ap.add_argument("--workload", default="c1", choices=["c1", "c2"])
+    ap.add_argument("--workload", default="c1", choices=["c1", "c2", "c4"])
     a = ap.parse_args()
     be = B200Backend(precision=a.precision)
     if a.workload == "c2":
         from paper_2201_09210_b200.workloads import C2, dcgan_program
         src = dcgan_program(steps=100_000, **C2)
+    elif a.workload == "c4":
+        from paper_2201_09210_b200.workloads import C4, gpt2_program
+        src = gpt2_program(steps=100_000, **C4)
     else:
         src = c1_program(steps=100_000, **C1)
     o = make_orch(src, SyntheticDataset(1000), be)
     reach_coexec(o)
     for _ in range(5):
         o.step()
-    be.set_trace(16384)
+    be.set_trace(65536)
     agg = collections.defaultdict(float)
     cnt = collections.Counter()
     total = 0.0

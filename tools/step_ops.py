@@ -135,13 +135,16 @@ def main():
     ap.add_argument("--out", default=None)
     a = ap.parse_args()
     from paper_2201_09210_b200.b200 import B200Backend
-    from paper_2201_09210_b200.workloads import C2, dcgan_program
+    from paper_2201_09210_b200.workloads import C2, C4, dcgan_program, gpt2_program
     be = B200Backend(precision=a.precision)
-    ops = record_step_ops(be, lambda n: dcgan_program(steps=n, **C2), 2)
+    if a.workload == "c4":
+        ops = record_step_ops(be, lambda n: gpt2_program(steps=n, **C4), 1)
+    else:
+        ops = record_step_ops(be, lambda n: dcgan_program(steps=n, **C2), 2)
     rows = profile_ops(be, ops, reps=int(os.environ.get("STEP_OPS_REPS", "10")))
     agg = by_kernel(rows)
     tot = sum(agg.values())
-    print(f"{len(rows)} distinct ops, {sum(ops.values())} op executions per D+G step pair; kernel time {tot:.3f} ms")
+    print(f"{len(rows)} distinct ops, {sum(ops.values())} op executions per step(s); kernel time {tot:.3f} ms")
     for k, v in agg.items():
         print(f"  {v:8.3f} ms  {100 * v / tot:5.1f}%  {k}")
     for r in sorted(rows, key=lambda r: -r["count"] * sum(l["ms"] for l in r["launches"]))[:25]:
