@@ -1326,11 +1326,12 @@ struct EndParams {
 __global__ void k_pass_end(EndParams p) {
   COEX_PDL_ENTER();
   DevState* ds = p.ds;
-  if (threadIdx.x != 0) return;
-  stamp(ds, SK_END);
-  for (int w = 0; w < kMaxDevVars / 64; ++w) {
+  if (threadIdx.x == 0) stamp(ds, SK_END);
+  // one lane per 64-variable word of the dirty bitmap (only the context's defined variables)
+  const int nwords = (p.nvars + 63) / 64;
+  for (int w = threadIdx.x; w < kMaxDevVars / 64; w += blockDim.x) {
     unsigned long long mask = 0;
-    if (!ds->cancelled) {
+    if (w < nwords && !ds->cancelled) {
       for (int b = 0; b < 64; ++b) {
         const int i = w * 64 + b;
         if (i < p.nvars && p.var_ovl[i] != nullptr) {
@@ -1342,6 +1343,8 @@ __global__ void k_pass_end(EndParams p) {
     p.mb->dirty[w] = mask;
     if (w == 0) p.mb->dirty_mask = mask;
   }
+  __syncwarp();
+  if (threadIdx.x != 0) return;
   p.mb->committed = ds->cancelled ? 0 : 1;
   p.mb->status = ds->status;
   p.mb->exec_ns = globaltimer() - ds->t_begin;

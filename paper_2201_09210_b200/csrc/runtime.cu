@@ -465,7 +465,8 @@ struct OpSpec {
   Out out{};
   Out out2{}, out3{};                      // fused batch-norm backward: dgamma, dbeta
   void* shadow = nullptr;                  // bf16 copy of the output to write (softmax-type producers)
-  void* in_shadow[kMaxIn] = {nullptr, nullptr, nullptr};   // bf16 copies of inputs (batched GEMM A)
+  void* in_shadow[kMaxIn] = {nullptr, nullptr, nullptr};   // shared bf16 copies of GEMM operands
+  int in_conv[kMaxIn] = {1, 1, 1};         // 1: this op converts into in_shadow / scratch first
   DevState* ds = nullptr;
 };
 
@@ -1208,12 +1209,13 @@ int build_xop_t(coex_ctx* c, const OpSpec& s, Launch* L, int* nL, size_t* ws_byt
         // B [B][K][N] (MN-major) or [B][N][K] (nt: K-major); 3-D TMA maps, batch = grid items
         const TcPlan t = tc_plan(M * Bt, N, K, false);
         const int64_t arow = tn ? K : M, acol = tn ? M : K, brow = nt ? N : K, bcol = nt ? K : N;
-        const bool a_sh = s.in_shadow[0] != nullptr && acol % 8 == 0;   // producer wrote a bf16 copy
-        void* A = a_sh ? s.in_shadow[0] : cv.take((size_t)Bt * arow * bf16_pitch(acol) * 2);
-        void* B = cv.take((size_t)Bt * brow * bf16_pitch(bcol) * 2);
+        // shared bf16 copies from the plan (or a bf16 shadow written by the producer); eager:
+        // private copies in the workspace
+        void* A = s.in_shadow[0] ? s.in_shadow[0] : cv.take((size_t)Bt * arow * bf16_pitch(acol) * 2);
+        void* B = s.in_shadow[1] ? s.in_shadow[1] : cv.take((size_t)Bt * brow * bf16_pitch(bcol) * 2);
         if (!build) break;
-        if (!a_sh) cvt_rows_launch(s.ds, s.in[0], A, Bt * arow, acol, &L[(*nL)++]);
-        cvt_rows_launch(s.ds, s.in[1], B, Bt * brow, bcol, &L[(*nL)++]);
+        if (!s.in_shadow[0] || s.in_conv[0]) cvt_rows_launch(s.ds, s.in[0], A, Bt * arow, acol, &L[(*nL)++]);
+        if (!s.in_shadow[1] || s.in_conv[1]) cvt_rows_launch(s.ds, s.in[1], B, Bt * brow, bcol, &L[(*nL)++]);
         const int rc = tc_gemm_launches(c, s.ds, A, B, M, N, K, t, s.in[0], s.in[1], s.out, nullptr, nullptr, L, nL,
                                         tn ? 1 : 0, !nt, nullptr, nullptr, Bt);
         // planner-proven causal structure (attr dims[0]: 1 = only C's lower triangle is read,
@@ -1333,12 +1335,15 @@ constexpr int kMaxLaunches = 6;
 
 bool needs_scratch(const coex_ctx* c, int kind) { return c->prec == COEX_BF16 && kind == COEX_MATMUL; }
 
+// bf16 copies of the MatMul operands as stored ([rows][pitch(cols)]; K- or MN-major use)
 void scratch_bytes(const OpSpec& s, size_t* a, size_t* b) {
-  const int64_t M = s.trans_a ? s.in_shape[0][1] : s.in_shape[0][0];
-  const int64_t K = s.trans_a ? s.in_shape[0][0] : s.in_shape[0][1];
-  const int64_t N = s.trans_b ? s.in_shape[1][0] : s.in_shape[1][1];
-  *a = (size_t)(M > 0 ? M : 1) * bf16_pitch(K > 0 ? K : 1) * 2;
-  *b = (size_t)(N > 0 ? N : 1) * bf16_pitch(K > 0 ? K : 1) * 2;
+  const int64_t ra = s.in_shape[0][0], ca = s.in_shape[0][1], rb = s.in_shape[1][0], cb = s.in_shape[1][1];
+  const size_t a1 = (size_t)(ra > 0 ? ra : 1) * bf16_pitch(ca > 0 ? ca : 1) * 2;   // as stored
+  const size_t a2 = (size_t)(ca > 0 ? ca : 1) * bf16_pitch(ra > 0 ? ra : 1) * 2;   // transposed
+  const size_t b1 = (size_t)(rb > 0 ? rb : 1) * bf16_pitch(cb > 0 ? cb : 1) * 2;
+  const size_t b2 = (size_t)(cb > 0 ? cb : 1) * bf16_pitch(rb > 0 ? rb : 1) * 2;
+  *a = a1 > a2 ? a1 : a2;
+  *b = b1 > b2 ? b1 : b2;
 }
 
 // One op -> its launches (bf16 MatMul = operand conversion + tcgen05 GEMM; extension ops
@@ -1355,28 +1360,31 @@ int build_launches(coex_ctx* c, const OpSpec& s, Launch* L, int* nL) {
   const int64_t M = s.trans_a ? s.in_shape[0][1] : s.in_shape[0][0];
   const int64_t K = s.trans_a ? s.in_shape[0][0] : s.in_shape[0][1];
   const int64_t N = s.trans_b ? s.in_shape[1][0] : s.in_shape[1][1];
-  CvtParams cv{};
-  cv.ds = s.ds;
-  cv.src[0] = s.in[0];
-  cv.src[1] = s.in[1];
-  cv.rows[0] = M;
-  cv.rows[1] = N;
-  cv.K = K;
-  cv.ld = bf16_pitch(K);
-  cv.trans[0] = s.trans_a ? 1 : 0;     // A stored [K][M] when folded from a transpose
-  cv.trans[1] = s.trans_b ? 0 : 1;     // B stored [K][N] -> B^T read; folded: stored [N][K]
-  cv.dst[0] = (__nv_bfloat16*)s.scratch[0];
-  cv.dst[1] = (__nv_bfloat16*)s.scratch[1];
-  // direct operands: one row per block; transposed operands: one 32x32 tile per block
-  const int64_t rows_max = M > N ? M : N;
-  const int64_t tiles_max = ((rows_max + 31) / 32) * ((cv.ld + 31) / 32);
-  int64_t gx = rows_max > tiles_max ? rows_max : tiles_max;
-  if (gx > (int64_t)kNumSMs * 16) gx = (int64_t)kNumSMs * 16;
-  dim3 g((unsigned)(gx > 0 ? gx : 1), 2);
-  L[0].set((void*)k_cvt_bf16, g, dim3(256), cv);
-  *nL = 1;
+  // operands are converted as stored (no transposition): A [M][K] -> K-major, A folded from a
+  // transpose ([K][M]) -> MN-major; B [K][N] -> MN-major, B folded ([N][K]) -> K-major.  A
+  // conversion is skipped when an earlier GEMM of the pass already made this copy.
+  // conversion flag 2 (planner: narrow operand): transposed conversion into a K-major copy.
+  // Eager calls use the same narrow rule.
+  int ca = s.in_conv[0], cb = s.in_conv[1];
+  if (s.ws == nullptr && ca == 1 && cb == 1) {     // eager: no plan flags
+    if (s.trans_a && M < 64) ca = 2;
+    if (!s.trans_b && N < 64) cb = 2;
+  }
+  const bool a_mn = s.trans_a && ca != 2, b_mn = !s.trans_b && cb != 2;
+  *nL = 0;
+  if (ca == 1) cvt_rows_launch(s.ds, s.in[0], s.scratch[0], s.in_shape[0][0], s.in_shape[0][1], &L[(*nL)++]);
+  if (cb == 1) cvt_rows_launch(s.ds, s.in[1], s.scratch[1], s.in_shape[1][0], s.in_shape[1][1], &L[(*nL)++]);
+  for (int w = 0; w < 2; ++w) {
+    if ((w == 0 ? ca : cb) != 2) continue;
+    CvtParams q{};                                  // element (r, k) = src[k * R + r]
+    q.ds = s.ds; q.src[0] = s.in[w]; q.rows[0] = w == 0 ? M : N; q.K = K; q.ld = bf16_pitch(K); q.trans[0] = 1;
+    q.dst[0] = (__nv_bfloat16*)s.scratch[w];
+    const int64_t tiles = ((q.rows[0] + 31) / 32) * ((q.ld + 31) / 32);
+    L[(*nL)++].set((void*)k_cvt_bf16, dim3((unsigned)(tiles < kNumSMs * 16 ? (tiles < 1 ? 1 : tiles) : kNumSMs * 16), 1),
+                   dim3(256), q);
+  }
   return tc_gemm_launches(c, s.ds, s.scratch[0], s.scratch[1], M, N, K, tc_plan(M, N, K, s.ws != nullptr), s.in[0],
-                          s.in[1], s.out, nullptr, (float*)s.ws, L, nL);
+                          s.in[1], s.out, nullptr, (float*)s.ws, L, nL, a_mn ? 1 : 0, b_mn);
 }
 
 int launch_now(coex_ctx* c, Launch& L) {
@@ -2075,6 +2083,8 @@ struct Builder {
         s.trans_b = (int)next();
         s.scratch[0] = buf(next());
         s.scratch[1] = buf(next());
+        s.in_conv[0] = (int)next();
+        s.in_conv[1] = (int)next();
         read_out(s.out);
         s.nin = 2;
         if (needs_scratch(c, s.kind)) {           // bf16 MatMul: split-K slices when the tile grid is small
@@ -2129,6 +2139,7 @@ struct Builder {
         }
         s.shadow = buf(next());
         for (int i = 0; i < kMaxIn; ++i) s.in_shadow[i] = buf(next());
+        for (int i = 0; i < kMaxIn; ++i) s.in_conv[i] = (int)next();
         Launch L[kMaxLaunches];
         int nL = 0;
         size_t wb = 0;
@@ -2477,7 +2488,7 @@ int coex_prog_build(coex_ctx* c, const int64_t* plan, int64_t nwords, const doub
       if (rc) throw std::runtime_error(g_err);
     }
     {
-      EndParams ep{c->d_state, c->d_mb, c->d_var_ovl, c->d_var_ovl_shape, (int)kMaxVars};
+      EndParams ep{c->d_state, c->d_mb, c->d_var_ovl, c->d_var_ovl_shape, (int)c->vars.size()};
       Launch L;
       L.set((void*)k_pass_end, dim3(1), dim3(32), ep);
       rc = b.add_kernel(p->graph, &prev, L);

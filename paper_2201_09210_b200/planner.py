@@ -298,6 +298,7 @@ class Planner:
             return [T_PTR, op, nid, cin, var_idx, shape_id] + out_words(nid, False)
 
         self.consumers = consumers
+        self._copies = {}
         self.n_chains = 0
         self.chain_lates = 0
 
@@ -310,6 +311,14 @@ class Planner:
 
         def emit(insts) -> list:
             items = []
+            saved = self._copies
+            self._copies = {}
+            try:
+                return emit_list(insts, items)
+            finally:
+                self._copies = saved
+
+        def emit_list(insts, items) -> list:
             bn_groups, bn_skip = self._bn_bwd_groups(insts) if self.fuse else ({}, set())
             if self.fuse:
                 segs = self._segments(insts, shapes, folded)
@@ -333,29 +342,40 @@ class Planner:
                         items.append(self._chain_item(run, shapes, in_cell, node_buf, pubs, multi, n_compute))
                     except _TooWide:
                         items.extend(emit(run))
+                    self._invalidate([c for r in run for c in pubs[r.node_id]] +
+                                     [slot_cell[f.slot] for f in feeds if f.slot in slot_cell])
                     continue
                 x = seg
                 if isinstance(x, InputFeed):
                     it = feed_item(x)
                     if it is not None:
                         items.append(it)
+                    if x.slot in slot_cell:
+                        self._invalidate([slot_cell[x.slot]])
                 elif isinstance(x, OutputFetch):
                     shp = shapes[x.node_id]
                     items.append([T_FETCH, x.node_id, vcell[x.node_id], shape_size(shp), len(shp)] + _pad(shp))
                 elif isinstance(x, ExecOp):
                     items.extend(self._exec(x, shapes, in_cell, out_words, ptr_item, pubs, multi,
                                             folded, n_compute, flops))
+                    self._invalidate(pubs[x.node_id])
+                    if x.kind is OpKind.ASSIGN_VAR:
+                        self._invalidate([-(2000 + self.var_index[x.attrs["var_name"]])])
                 elif isinstance(x, SwitchCase):
+                    self._invalidate()
                     it = [T_SWITCH, x.branch_id, len(x.cases)]
                     for c in x.cases:
                         it += seq(c)
                     items.append(it)
                 elif isinstance(x, While):
+                    self._invalidate()
                     items.append([T_WHILE, x.loop_id] + seq(x.body))
                 elif isinstance(x, UnrolledLoop):
+                    self._invalidate()
                     for b in x.bodies:
                         items.extend(emit(b))
                 elif type(x).__name__ == "AllReduce":
+                    self._invalidate()
                     b0, b1, pp = node_buf.get(x.node_id, (-1, -1, True))
                     if b0 < 0 or pp:
                         raise NeedsReplicated(f"node {x.node_id} has no static buffer to all-reduce")
@@ -364,6 +384,7 @@ class Planner:
 
         def seq(insts) -> list:
             items = emit(insts)
+            self._invalidate()
             out = [T_SEQ, len(items)]
             for it in items:
                 out += it
@@ -442,11 +463,22 @@ class Planner:
         word += [len(out_shape)] + _pad(out_shape)
         word += [len(attr_dims)] + _pad(attr_dims) + [_f64_bits(0.0), trans[0], trans[1]]
         if k is OpKind.MATMUL and self.bf16:
-            pitch = (kk + 7) // 8 * 8
-            word += [self.new_buf(max(m, 1) * pitch * 2), self.new_buf(max(nn, 1) * pitch * 2)]
+            # narrow operands (the GEMM's M or N < 64 on an MN-major copy) are converted
+            # transposed into a private K-major copy instead (flag 2): MN-major boxes of a
+            # 1..63-wide tensor are mostly padding
+            if trans[0] and m < 64:
+                ca = (self.new_buf(max(m, 1) * ((kk + 7) // 8 * 8) * 2), 2)
+            else:
+                ca = self._copy(cells[0], in_shapes[0])
+            if not trans[1] and nn < 64:
+                cb = (self.new_buf(max(nn, 1) * ((kk + 7) // 8 * 8) * 2), 2)
+            else:
+                cb = self._copy(cells[1], in_shapes[1])
+            word += [ca[0], cb[0], ca[1], cb[1]]
         else:
-            word += [-1, -1]
+            word += [-1, -1, 0, 0]
         word += out_words(nid, late)
+        self._invalidate(pubs[nid])
         return [word]
 
     def _bn_bwd_groups(self, insts):
@@ -517,7 +549,8 @@ class Planner:
         word += [len(out_shape)] + _pad(out_shape)
         word += [0] + _pad([]) + [_f64_bits(0.0)]
         word += out_words(d.node_id, late) + out_words(g.node_id, late) + out_words(sr.node_id, late)
-        return word + [-1] * (1 + MAX_XIN)
+        self._invalidate(pubs[d.node_id] + pubs[g.node_id] + pubs[sr.node_id])
+        return word + [-1] * (1 + MAX_XIN) + [0] * MAX_XIN
 
     def _xop_word(self, x, shapes, in_cell, out_words, pubs, n_compute, flops) -> list:
         nid = x.node_id
@@ -538,7 +571,12 @@ class Planner:
         word += [len(out_shape)] + _pad(out_shape)
         word += [len(attr)] + _pad(attr) + [_f64_bits(float(x.attrs.get("value", 0.0)))]
         word += out_words(nid, late)
-        return word + self._shadow_words(x)
+        word += self._shadow_words(x, cells, in_shapes)
+        self._invalidate(pubs[nid])
+        if nid in self.shadow:                  # this node's bf16 shadow is a valid copy from here on
+            shp = shapes[nid]
+            self._copies[(pubs[nid][0], shape_size(shp[:-1]), shp[-1])] = self.shadow[nid]
+        return word
 
     def _causal_prob(self, b) -> bool:
         """Binding b is (single-candidate) a causal_softmax output, or a softmax_grad of one --
@@ -573,12 +611,46 @@ class Planner:
             return 2 if x.kind is OpKind.BMM else 3
         return 0
 
-    def _shadow_words(self, x) -> list:
-        """[own bf16 shadow buffer, bf16 shadow of each input (batched-GEMM operand A only)]."""
-        ins = [-1] * MAX_XIN
-        if x.kind in (OpKind.BMM, OpKind.BMM_TN) and not x.inputs[0].fed and len(x.inputs[0].cands) == 1:
-            ins[0] = self.shadow.get(x.inputs[0].cands[0], -1)
-        return [self.shadow.get(x.node_id, -1)] + ins
+    # ------------------------------------------------------------ shared bf16 operand copies
+    # Every tcgen05 GEMM operand is a bf16 copy [rows][pitch(cols)] of the stored tensor, a
+    # layout that serves K-major and MN-major use alike.  Within one straight-line instruction
+    # list the first GEMM that needs a tensor converts it into a shared buffer and later GEMMs
+    # reuse it, until something republishes the tensor's cell (or control flow intervenes).
+    def _copy(self, cell, shape) -> tuple:
+        """(buffer index, convert?) of the bf16 copy of the tensor behind operand cell ``cell``."""
+        shape = tuple(shape)
+        rows = shape_size(shape[:-1]) if len(shape) > 1 else 1
+        cols = shape[-1] if shape else 1
+        key = (cell, rows, cols)
+        hit = self._copies.get(key)
+        if hit is not None:
+            return hit, 0
+        buf = self.new_buf(max(rows, 1) * ((max(cols, 1) + 7) // 8 * 8) * 2)
+        if cell is not None and cell != -1:
+            self._copies[key] = buf
+        return buf, 1
+
+    def _invalidate(self, pub_codes=None):
+        """Drop copies whose source cell is republished (all copies when ``pub_codes`` is None)."""
+        if pub_codes is None:
+            self._copies.clear()
+            return
+        dead = set()
+        for c in pub_codes:
+            dead.add(c)
+            if c <= -2000:                      # a variable's overlay slot: its direct reads change
+                dead.add(-(1000 + (-2000 - c)))
+        for key in [k for k in self._copies if k[0] in dead]:
+            del self._copies[key]
+
+    def _shadow_words(self, x, in_cells=None, in_shapes=None) -> list:
+        """[own bf16 shadow buffer] + per input [bf16 copy buffer] + per input [convert?] for the
+        batched GEMMs (others: no copies)."""
+        bufs, conv = [-1] * MAX_XIN, [0] * MAX_XIN
+        if x.kind in BMM_KINDS and self.bf16 and in_cells is not None:
+            for i in range(2):
+                bufs[i], conv[i] = self._copy(in_cells[i], in_shapes[i])
+        return [self.shadow.get(x.node_id, -1)] + bufs + conv
 
     # ------------------------------------------------------------ pointer-op rewrites
     def _pointer_rewrites(self, consumers, multi, folded):
