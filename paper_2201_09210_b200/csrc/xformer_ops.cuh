@@ -180,6 +180,57 @@ __global__ void __launch_bounds__(256) k_layernorm(RowParams p) {
   count_op(p.ds);
   const int lane = threadIdx.x & 31;
   const long long warps = (long long)gridDim.x * (blockDim.x / 32);
+  if (p.d <= 768 && sizeof(T) == 4) {               // fp32 rows up to 768 held in registers
+    constexpr int PER = 24;
+    const long long d = p.d;
+    for (long long r = (long long)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; r < p.rows; r += warps) {
+      const T* xr = x + r * d;
+      float xv[PER];
+      float s1 = 0.f;
+#pragma unroll
+      for (int j = 0; j < PER; ++j) {
+        const long long c = lane + 32ll * j;
+        xv[j] = c < d ? (float)xr[c] : 0.f;
+        s1 += xv[j];
+      }
+      const float mean = warp_sum(s1) / (float)d;
+      float s2 = 0.f;
+#pragma unroll
+      for (int j = 0; j < PER; ++j) {
+        const long long c = lane + 32ll * j;
+        const float t = c < d ? xv[j] - mean : 0.f;
+        s2 += t * t;
+      }
+      const float rstd = rsqrtf(warp_sum(s2) / (float)d + (float)kLnEps);
+      if (MODE == 0) {
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+          const long long c = lane + 32ll * j;
+          if (c < d) o[r * d + c] = (T)(((xv[j] - mean) * rstd) * (float)g[c] + (float)z[c]);
+        }
+      } else {
+        const T* dyr = z + r * d;
+        float gv[PER];
+        float m1 = 0.f, m2 = 0.f;
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+          const long long c = lane + 32ll * j;
+          gv[j] = c < d ? (float)dyr[c] * (float)g[c] : 0.f;
+          m1 += gv[j];
+          m2 += c < d ? gv[j] * ((xv[j] - mean) * rstd) : 0.f;
+        }
+        m1 = warp_sum(m1) / (float)d;
+        m2 = warp_sum(m2) / (float)d;
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+          const long long c = lane + 32ll * j;
+          if (c < d) o[r * d + c] = (T)(((gv[j] - m1) - ((xv[j] - mean) * rstd) * m2) * rstd);
+        }
+      }
+    }
+    publish_late(p.out, o);
+    return;
+  }
   for (long long r = (long long)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; r < p.rows; r += warps) {
     const T* xr = x + r * p.d;
     double mean, rstd;
@@ -273,6 +324,42 @@ __global__ void __launch_bounds__(256) k_causal_softmax(RowParams p) {
   const long long d = p.d;
   typedef typename AccT<T>::type A;
   const A sc = (A)p.scale;
+  if (d <= 1024) {                                  // row held in registers: one read, one write
+    constexpr int PER = 32;
+    for (long long r = (long long)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; r < p.rows; r += warps) {
+      const long long i = r % p.T;
+      const T* xr = x + r * d;
+      T* orow = o + r * d;
+      A v[PER];
+      A mx = -INFINITY;
+#pragma unroll
+      for (int j = 0; j < PER; ++j) {
+        const long long c = lane + 32ll * j;
+        v[j] = c <= i ? (A)xr[c] * sc : -INFINITY;
+        mx = fmax(mx, v[j]);
+      }
+      mx = warp_max(mx);
+      A sm = 0;
+#pragma unroll
+      for (int j = 0; j < PER; ++j) {
+        const long long c = lane + 32ll * j;
+        v[j] = c <= i ? ex(v[j] - mx) : (A)0;
+        sm += v[j];
+      }
+      const A inv = (A)1 / warp_sum(sm);
+#pragma unroll
+      for (int j = 0; j < PER; ++j) {
+        const long long c = lane + 32ll * j;
+        if (c < d) {
+          const A y = v[j] * inv;
+          orow[c] = (T)y;
+          if (p.shadow) p.shadow[r * d + c] = __float2bfloat16_rn((float)y);
+        }
+      }
+    }
+    publish_late(p.out, o);
+    return;
+  }
   for (long long r = (long long)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; r < p.rows; r += warps) {
     const long long i = r % p.T;                    // row index inside its [T, T] block
     const T* xr = x + r * d;
@@ -308,6 +395,34 @@ __global__ void __launch_bounds__(256) k_softmax_grad(RowParams p) {
   const long long warps = (long long)gridDim.x * (blockDim.x / 32);
   const long long d = p.d;
   typedef typename AccT<T>::type A;
+  if (d <= 1024) {                                  // rows held in registers: y and dy read once
+    constexpr int PER = 32;
+    for (long long r = (long long)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; r < p.rows; r += warps) {
+      const T* yr = y + r * d;
+      const T* gr = dy + r * d;
+      A yv[PER], gv[PER];
+      A dot = 0;
+#pragma unroll
+      for (int j = 0; j < PER; ++j) {
+        const long long c = lane + 32ll * j;
+        yv[j] = c < d ? (A)yr[c] : (A)0;
+        gv[j] = yv[j] != (A)0 ? (A)gr[c] : (A)0;
+        dot += gv[j] * yv[j];
+      }
+      dot = warp_sum(dot);
+#pragma unroll
+      for (int j = 0; j < PER; ++j) {
+        const long long c = lane + 32ll * j;
+        if (c < d) {
+          const A v = yv[j] != (A)0 ? (A)p.scale * (yv[j] * (gv[j] - dot)) : (A)0;
+          o[r * d + c] = (T)v;
+          if (p.shadow) p.shadow[r * d + c] = __float2bfloat16_rn((float)v);
+        }
+      }
+    }
+    publish_late(p.out, o);
+    return;
+  }
   for (long long r = (long long)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; r < p.rows; r += warps) {
     const T* yr = y + r * d;
     const T* gr = dy + r * d;
@@ -417,8 +532,16 @@ __global__ void __launch_bounds__(256) k_colsum_wide(RowParams p) {
   const long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long r0 = p.rows * blockIdx.y / gridDim.y, r1 = p.rows * (blockIdx.y + 1) / gridDim.y;
   if (c < p.d) {
-    double acc = 0.0;
-    for (long long r = r0; r < r1; ++r) acc += (double)x[r * p.d + c];
+    // four independent accumulators (combined in a fixed order) keep four loads in flight
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    long long r = r0;
+    for (; r + 3 < r1; r += 4) {
+      const double v0 = (double)x[r * p.d + c], v1 = (double)x[(r + 1) * p.d + c];
+      const double v2 = (double)x[(r + 2) * p.d + c], v3 = (double)x[(r + 3) * p.d + c];
+      a0 += v0; a1 += v1; a2 += v2; a3 += v3;
+    }
+    for (; r < r1; ++r) a0 += (double)x[r * p.d + c];
+    const double acc = (a0 + a1) + (a2 + a3);
     if (gridDim.y == 1) o[c] = (T)acc;
     else atomicAdd(p.acc + c, acc);
   }
