@@ -702,8 +702,14 @@ TcPlan tc_plan(int64_t M, int64_t N, int64_t K, bool allow_split) {
   TcPlan best;
   double best_t = 1e30;
   const int64_t nk = (K + TC_BK - 1) / TC_BK;
+  static int force_bn = -1;
+  if (force_bn < 0) {
+    const char* e = getenv("COEX_FORCE_BN");     // tuning experiments only
+    force_bn = e ? atoi(e) : 0;
+  }
   const int bns[3] = {64, 128, 256};
   for (int bn : bns) {
+    if (force_bn && bn != force_bn) continue;
     if (bn > 64 && N <= bn / 2) continue;
     const int64_t tiles = ((M + TC_BM - 1) / TC_BM) * ((N + bn - 1) / bn);
     const int64_t smax = allow_split ? (nk / 2 < 32 ? (nk / 2 > 1 ? nk / 2 : 1) : 32) : 1;
@@ -713,13 +719,16 @@ TcPlan tc_plan(int64_t M, int64_t N, int64_t K, bool allow_split) {
       const int64_t items = (tiles < 1 ? 1 : tiles) * sp;
       const int64_t rounds = (items + kNumSMs - 1) / kNumSMs;
       const double kper = (double)((nk + sp - 1) / sp);
+      // per-SM figures fitted to measured launches (tools/ncu_ops.py qkt / gemm_8192 with
+      // COEX_FORCE_BN): ~115 GB/s of TMA operand feed, ~23.5 GB/s of epilogue stores and
+      // ~0.9 us of fixed cost per work item (barrier round trips, TMEM hand-off)
       const double mma = kper * 2.0 * TC_BM * bn * TC_BK / 10.7e12;
-      const double feed = kper * (double)(TC_BM + bn) * TC_BK * 2 / 135e9;
-      const double epi = (double)TC_BM * bn * 4 / 44e9;
+      const double feed = kper * (double)(TC_BM + bn) * TC_BK * 2 / 115e9;
+      const double epi = (double)TC_BM * bn * 4 / 23.5e9;
       double body = mma > feed ? mma : feed;
       if (epi > body) body = epi;
-      double t = rounds * body + epi + 2e-6;
-      if (sp > 1) t += (double)(sp + 1) * M * N * 4 / 5.5e12 + 2e-6;
+      double t = rounds * (body + 0.9e-6) + epi + 2e-6;
+      if (sp > 1) t += (double)(sp + 1) * M * N * 4 / 5.5e12 + 3e-6;
       if (t < best_t * 0.98) {
         best_t = t;
         best.bn = bn;

@@ -464,11 +464,23 @@ __global__ void __launch_bounds__(256) k_cross_entropy(RowParams p) {
   for (long long r = blockIdx.x; r < p.rows; r += gridDim.x) {
     const T* row = lg + r * V;
     // online max / sum of exponentials in one pass (rescaling the partial sum on a new max)
+    // groups of 4 independent loads per thread (memory-level parallelism), merged online
     A mx = -INFINITY, sm = 0;
-    for (long long c = threadIdx.x; c < V; c += blockDim.x) {
+    const long long step = blockDim.x;
+    long long c = threadIdx.x;
+    for (; c + 3 * step < V; c += 4 * step) {
+      const A v0 = (A)row[c], v1 = (A)row[c + step], v2 = (A)row[c + 2 * step], v3 = (A)row[c + 3 * step];
+      const A m4 = fmax(fmax(v0, v1), fmax(v2, v3));
+      if (m4 > mx) {
+        sm = mx == -INFINITY ? (A)0 : sm * ex(mx - m4);
+        mx = m4;
+      }
+      sm += (ex(v0 - mx) + ex(v1 - mx)) + (ex(v2 - mx) + ex(v3 - mx));
+    }
+    for (; c < V; c += step) {
       const A v = (A)row[c];
       if (v > mx) {
-        sm = sm * ex(mx - v) + (A)1;
+        sm = mx == -INFINITY ? (A)1 : sm * ex(mx - v) + (A)1;
         mx = v;
       } else {
         sm += ex(v - mx);
@@ -494,10 +506,12 @@ __global__ void __launch_bounds__(256) k_cross_entropy(RowParams p) {
       if (threadIdx.x == 0) p.acc[r] = ((double)log(gs) + (double)gm) - (double)row[id];
     } else {
       const A inv = (A)1 / gs, invr = (A)(1.0 / (double)p.rows);
-      for (long long c = threadIdx.x; c < V; c += blockDim.x) {
-        A g = ex((A)row[c] - gm) * inv;
-        if (c == id) g -= (A)1;
-        o[r * V + c] = (T)(g * invr);
+      T* orow = o + r * V;
+#pragma unroll 4
+      for (long long c2 = threadIdx.x; c2 < V; c2 += blockDim.x) {
+        A g = ex((A)row[c2] - gm) * inv;
+        if (c2 == id) g -= (A)1;
+        orow[c2] = (T)(g * invr);
       }
     }
   }

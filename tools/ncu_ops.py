@@ -21,6 +21,8 @@ OPS = {
     "bn_16x16x128": (OpKind.BATCHNORM, {}, [(128, 16, 16, 128), (128,), (128,)]),
     "mm_8192x128x1": (OpKind.MATMUL, {}, [(8192, 128), (128, 1)]),
     "gemm_8192": (OpKind.MATMUL, {}, [(8192, 8192), (8192, 8192)]),
+    "ce_grad": (OpKind.CROSS_ENTROPY_GRAD, {}, [(8192, 50257), (8192,)]),
+    "qkt": (OpKind.BMM_NT, {}, [(96, 1024, 64), (96, 1024, 64)]),
 }
 
 be = B200Backend(precision=os.environ.get("PREC", "bf16"))
