@@ -12,6 +12,8 @@ Workloads (paper_2201_09210_b200/workloads.py):
   tcgen05 convolutions / GEMMs (implicit-GEMM lowering), fp32 everything else.  A step is
   one D or one G iteration; ``value`` counts iterations of either kind.
 * ``c1`` -- configs[0], the tiny MLP the reference's own CPU path can express (f64 parity).
+* ``c4`` -- configs[3], GPT-2 small (12 layers, d=768, 12 heads, T=1024, batch 8, vocab
+  50257), hand-written backward, data-dependent ``while`` over the fetched loss; bf16.
 
 A *step* is one training iteration run by the co-execution orchestrator: the Python
 skeleton walks the step while the B200 executes the step's CUDA graph (one
@@ -57,7 +59,7 @@ from paper_2201_09210_b200.coexec import Phase  # noqa: E402
 from paper_2201_09210_b200.dataset import SyntheticDataset  # noqa: E402
 from paper_2201_09210_b200.tensor import OpKind, Tensor, shape_size  # noqa: E402
 from paper_2201_09210_b200.workloads import (C1, C2, InMemoryDataset, c1_flops, c1_program,  # noqa: E402
-                                             dcgan_flops, dcgan_program)
+                                             C4, dcgan_flops, dcgan_program, gpt2_flops, gpt2_program)
 
 METRIC = "training iterations/sec at 1/2/4/8 B200 vs ref CPU co-exec; % HBM/tensor roofline"
 UNIT = "it/s"
@@ -213,11 +215,14 @@ def tensor_gemm(peak_tflops, peak_kind, size: int = 8192):
             "ms": round(ms, 4)}
 
 
-def roofline_c2(be, hbm_peak, tflops_peak, peak_kind):
-    """Per-kernel-family breakdown of one D+G step pair (eager re-launch, CUDA events on the
-    context stream) and the roofline of the dominant family."""
+def roofline_c2(be, hbm_peak, tflops_peak, peak_kind, workload="c2"):
+    """Per-kernel-family breakdown of one D+G step pair (C2) or one step (C4) -- eager
+    re-launch, CUDA events on the context stream -- and the roofline of the dominant family."""
     from tools.step_ops import by_family, profile_ops, record_step_ops
-    ops = record_step_ops(be, lambda n: dcgan_program(steps=n, **C2), 2)
+    if workload == "c4":
+        ops = record_step_ops(be, lambda n: gpt2_program(steps=n, **C4), 1)
+    else:
+        ops = record_step_ops(be, lambda n: dcgan_program(steps=n, **C2), 2)
     rows = profile_ops(be, ops, reps=10)
     fam = by_family(rows, be.esize)
     total = sum(f["ms"] for f in fam.values())
@@ -292,11 +297,35 @@ def cpu_baseline_c2(steps: int = 2):
                       f"{C2['batch']}; host cpu_count={os.cpu_count()}"}
 
 
+def cpu_baseline_c4(steps: int = 1):
+    """CPU oracle co-execution of C4 on a bounded sample: GPT-2 small's width (d=768, 12 heads)
+    at 1 layer, batch 1, T=64, vocabulary 4096; per-step time scaled to the full step by the
+    GEMM-FLOP ratio (stated in the sample)."""
+    from oracle.cpu_backend import CpuBackend
+    small = dict(C4, batch=1, seq=64, layers=1, vocab=4096)
+    o = make_orch(gpt2_program(steps=10_000, **small), SyntheticDataset(1000), CpuBackend())
+    reach_coexec(o)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        o.step()
+    dt = (time.perf_counter() - t0) / steps
+    scale = gpt2_flops(**C4) / gpt2_flops(**small)
+    return {"value": round(1.0 / (dt * scale), 8), "unit": UNIT, "cores": 2, "kind": "port",
+            "sample": f"C4 co-exec on the CPU oracle at 1 layer, batch 1, T=64, vocab 4096 (d, heads of GPT-2 small), "
+                      f"{steps} step(s) after tracing ({dt:.1f} s/step), scaled x{scale:.0f} by the GEMM-FLOP ratio "
+                      f"to the full step; host cpu_count={os.cpu_count()}"}
+
+
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    if args.workload == "c2":
+    if args.workload == "c4":
+        k = 1
+        base = cpu_baseline_c4(1)
+        cfg = {"workload": "C4 GPT-2 small, batch 8 x 1024 tokens, coexec (CPU oracle runner, f64)",
+               "global_batch": C4["batch"]}
+    elif args.workload == "c2":
         base = cpu_baseline_c2(max(2, min(args.steps, 4)))
         k = max(2, min(args.steps, 4))
         cfg = {"workload": "C2 DCGAN 64x64 (ngf=ndf=64, nz=100), batch 128, D/G alternating, coexec (CPU oracle "
@@ -317,6 +346,25 @@ def workload_setup(args, world: int):
     """(program source, synthetic dataset, e2e host records, per-rank H2D bytes, config dict)."""
     import numpy as np
     rr = np.random.default_rng(7)
+    if args.workload == "c4":
+        gb = C4["batch"] * world
+        cfg4 = dict(C4, batch=gb)
+        src = gpt2_program(steps=100_000, **cfg4)
+        t = C4["seq"]
+        recs = {"tokens": [Tensor((gb, t), rr.uniform(-1, 1, (gb, t))) for _ in range(2)],
+                "targets": [Tensor((gb, t), rr.uniform(-1, 1, (gb, t))) for _ in range(2)]}
+        import re
+        for m in re.finditer(r'input\("(\w+_init)", \[([0-9, ]+)\]\)', gpt2_program(steps=1, **C4)):
+            shp = tuple(int(v) for v in m.group(2).split(","))
+            recs[m.group(1)] = [Tensor(shp, rr.uniform(-1, 1, shp))]
+        cfg = {"workload": "C4 GPT-2 small (12 pre-LN blocks, d=768, 12 heads, T=1024, vocab 50257, tied head), "
+                           "batch 8 sequences/GPU, hand-written backward, SGD, data-dependent while over the "
+                           "fetched loss",
+               "global_batch": gb, "per_gpu_batch": C4["batch"], "seq_len": t,
+               "parallelism": f"dp{world}" if world == 1 else f"dp{world} (batch-sharded, NCCL all-reduce)",
+               "algorithmic_flops_per_step": gpt2_flops(**C4)}
+        h2d = 2 * C4["batch"] * t * 8
+        return src, SyntheticDataset(1000), recs, h2d, cfg, gb
     if args.workload == "c2":
         gb = C2["batch"] * world
         src = dcgan_program(steps=100_000, **dict(C2, batch=gb))
@@ -395,6 +443,26 @@ def run_b200(args):
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
         t_max = float(tt.item())
     value = world * args.steps / (t_max * 1e-3)
+    st = o.stats
+    stats = {"graph_exec_ms": round(st.graph_exec_ms, 3), "graph_stall_ms": round(st.graph_stall_ms, 3),
+             "python_exec_ms": round(st.python_exec_ms, 3), "python_stall_ms": round(st.python_stall_ms, 3),
+             "counters": list(st.counters())}
+    clocks = clk.summary()
+    roof = tgemm = None
+    if rank == 0:                      # kernel evidence while this context is alive
+        if args.workload in ("c2", "c4"):
+            roof = roofline_c2(be, hbm, tfl, peak_kind, args.workload)
+            if args.workload == "c4":
+                roof["unit_of_work"] = "one training step"
+                for f in roof.get("families", {}).values():
+                    for k in list(f):
+                        if k.endswith("_per_pair"):
+                            f[k.replace("_per_pair", "_per_step")] = f.pop(k)
+        else:
+            roof = roofline(be, hbm, tfl, peak_kind)
+            tgemm = tensor_gemm(tfl, peak_kind) if not args.no_tensor_gemm else None
+    del o
+    be.close()                         # free the synthetic-input pass graph before the e2e one
 
     # e2e: host-resident inputs through the public API (H2D each step, loss D2H)
     be2 = B200Backend(device=dev, precision=args.precision, dp=dp)
@@ -411,16 +479,13 @@ def run_b200(args):
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
         e2e_max = float(tt.item())
 
+    del o2
+    be2.close()
     if rank == 0:
-        if args.workload == "c2":
-            roof = roofline_c2(be, hbm, tfl, peak_kind)
-            base = cpu_baseline_c2() if world == 1 and not args.no_cpu_baseline else None
-            tgemm = None
+        if world == 1 and not args.no_cpu_baseline:
+            base = {"c1": lambda: cpu_baseline(12), "c2": cpu_baseline_c2, "c4": cpu_baseline_c4}[args.workload]()
         else:
-            roof = roofline(be, hbm, tfl, peak_kind)
-            base = cpu_baseline(12) if world == 1 and not args.no_cpu_baseline else None
-            tgemm = tensor_gemm(tfl, peak_kind) if not args.no_tensor_gemm else None
-        st = o.stats
+            base = None
         cfg.update({"l2": "flushed (256 MiB write) between timed steps", "tracing_steps_before_coexec": pre,
                     "steps_replayed_in_timed_region": replays})
         line = {
@@ -436,16 +501,12 @@ def run_b200(args):
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 8,
                     "data": "InMemoryDataset host tensors (f64), copied through coex_pass_feed each step"},
             "gpu_launches": launches,
-            "clocks": clk.summary(),
-            "stats": {"graph_exec_ms": round(st.graph_exec_ms, 3), "graph_stall_ms": round(st.graph_stall_ms, 3),
-                      "python_exec_ms": round(st.python_exec_ms, 3), "python_stall_ms": round(st.python_stall_ms, 3),
-                      "counters": list(st.counters())},
+            "clocks": clocks,
+            "stats": stats,
         }
         if tgemm is not None:
             line["tensor_gemm"] = tgemm
         print(json.dumps(line))
-    be2.close()
-    be.close()
     if world > 1:
         torch.distributed.destroy_process_group()
 
@@ -455,7 +516,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=None)
     ap.add_argument("--warmup", type=int, default=10)
-    ap.add_argument("--workload", default="c2", choices=["c1", "c2"])
+    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c4"])
     ap.add_argument("--precision", default=None, choices=["f64", "fp32", "bf16"])
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -463,9 +524,9 @@ def main():
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.steps is None:
-        args.steps = 100 if args.workload == "c2" else 200
+        args.steps = {"c1": 200, "c2": 100, "c4": 20}[args.workload]
     if args.precision is None:
-        args.precision = "bf16" if args.workload == "c2" else "f64"
+        args.precision = "f64" if args.workload == "c1" else "bf16"
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -215,6 +215,9 @@ class B200Backend:
 
     def close(self):
         if self.ctx is not None:
+            for prog in getattr(self, "_programs", []):   # graphs, arenas and workspaces first
+                prog.close()
+            self._programs = []
             self.lib.coex_ctx_destroy(self.ctx)
             self.ctx = None
 
@@ -354,6 +357,13 @@ class B200Backend:
 
     # ------------------------------------------------------------ symbolic side
     def compile(self, sp, tg) -> "B200Program":
+        prog = self._compile(sp, tg)
+        if not hasattr(self, "_programs"):
+            self._programs = []
+        self._programs.append(prog)
+        return prog
+
+    def _compile(self, sp, tg) -> "B200Program":
         return B200Program(self, sp, tg)
 
     def begin_pass(self, prog: "B200Program", lazy: bool = False) -> "B200Pass":

@@ -222,7 +222,7 @@ def gpt2_program(steps: int = 20, batch: int = 8, seq: int = 1024, d: int = 768,
         return f"reshape(transpose(reshape({x}, [{B}, {H}, {T}, {hd}]), [0, 2, 1, 3]), [{BT}, {D}])"
 
     b = [f"let tok = to_index(input(\"tokens\", [{B}, {T}]), {float(V)})",
-         f"let tgt = to_index(input(\"targets\", [{BT}]), {float(V)})",
+         f"let tgt = reshape(to_index(input(\"targets\", [{B}, {T}]), {float(V)}), [{BT}])",
          f"let emb = embedding(wte, tok)",
          f"let x0 = reshape(bias_add(reshape(emb, [{B}, {T * D}]), reshape(wpe, [{T * D}])), [{BT}, {D}])"]
     for l in range(L):
