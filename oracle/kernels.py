@@ -250,7 +250,7 @@ def transformer_kernel(kind: OpKind, attrs: dict, x: list, out_shape):
             return np.array(sum_seq(loss) / r)
         g = e / s_
         g[np.arange(r), ids] -= 1.0
-        return g / r
+        return g / attrs.get("rows", float(r))     # data parallel: the global row count
     return None
 
 

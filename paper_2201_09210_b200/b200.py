@@ -147,6 +147,9 @@ def _attrs(kind: OpKind, attrs: dict) -> CoexAttrs:
     elif kind in (OpKind.CAUSAL_SOFTMAX, OpKind.SOFTMAX_GRAD):
         dims = ()
         at.value = float(attrs["value"])
+    elif kind is OpKind.CROSS_ENTROPY_GRAD:
+        dims = ()
+        at.value = float(attrs.get("rows", 0.0))
     else:
         dims = ()
     if len(dims) > MAX_RANK:

@@ -505,7 +505,7 @@ __global__ void __launch_bounds__(256) k_cross_entropy(RowParams p) {
     if (MODE == 0) {
       if (threadIdx.x == 0) p.acc[r] = ((double)log(gs) + (double)gm) - (double)row[id];
     } else {
-      const A inv = (A)1 / gs, invr = (A)(1.0 / (double)p.rows);
+      const A inv = (A)1 / gs, invr = (A)(1.0 / (p.scale > 0.0 ? p.scale : (double)p.rows));   // scale: global rows
       T* orow = o + r * V;
 #pragma unroll 4
       for (long long c2 = threadIdx.x; c2 < V; c2 += blockDim.x) {

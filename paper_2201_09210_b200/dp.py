@@ -29,6 +29,14 @@ the statistics of the rank's own rows (per-replica batch statistics -- the
 semantics of data-parallel training without synchronised batch norm), so their
 results stay S0.
 
+C4 ops: layernorm (rows), bias_add, causal softmax and its gradient, the batched
+GEMMs (batch = sequences x heads, sharded with the sequences) and the embedding
+gather keep S0; ``embedding_dw`` and ``ln_dgamma`` are P+; ``cross_entropy`` is
+P~ (equal row shards); ``cross_entropy_grad`` keeps S0 and is rewritten to divide
+by the global row count.  A reshape keeps S0 when its leading target dimension
+splits evenly over the ranks (row-major chunks stay contiguous); a transpose keeps
+S0 when it leaves axis 0 in place.
+
 Parity: DP results equal the single-device run up to summation order
 (tolerance, not bitwise) -- tests/test_dp_gloo.py checks world size 2 on CPU.
 With per-replica batch-norm statistics the equality holds when every rank's rows
@@ -48,9 +56,12 @@ R, S0, S1, PSUM, PAVG = "R", "S0", "S1", "P+", "P~"
 PARTIAL = (PSUM, PAVG)
 ELEMENTWISE = (OpKind.ADD, OpKind.SUB, OpKind.MUL)
 LINEAR_UNARY = (OpKind.NEG,)
-NONLINEAR = (OpKind.RELU, OpKind.SIGMOID, OpKind.TANH, OpKind.LEAKY_RELU)
-# extension ops (C2): row-wise binary nonlinear ops keep the row sharding of their operands
-ROW_BINARY = (OpKind.RELU_GRAD, OpKind.LEAKY_RELU_GRAD, OpKind.BCE_TERM)
+NONLINEAR = (OpKind.RELU, OpKind.SIGMOID, OpKind.TANH, OpKind.LEAKY_RELU, OpKind.GELU)
+# extension ops (C2 / C4): row-wise binary nonlinear ops keep the row sharding of their operands
+ROW_BINARY = (OpKind.RELU_GRAD, OpKind.LEAKY_RELU_GRAD, OpKind.BCE_TERM, OpKind.GELU_GRAD, OpKind.TO_INDEX)
+# C4 ops whose rows (or batch entries) are independent: sharded in, sharded out
+ROW_WISE = (OpKind.LAYERNORM, OpKind.LAYERNORM_DX, OpKind.BIAS_ADD, OpKind.CAUSAL_SOFTMAX, OpKind.SOFTMAX_GRAD,
+            OpKind.BMM, OpKind.BMM_NT, OpKind.BMM_TN, OpKind.EMBEDDING, OpKind.CROSS_ENTROPY_GRAD)
 
 
 @dataclass
@@ -158,7 +169,8 @@ class _Prop:
         if k in LINEAR_UNARY:
             return ins[0]
         if k in (OpKind.CONV2D, OpKind.CONV2D_T, OpKind.CONV2D_DW, OpKind.BATCHNORM, OpKind.BATCHNORM_DX,
-                 OpKind.BN_DGAMMA, OpKind.SUM_ROWS) or k in ROW_BINARY:
+                 OpKind.BN_DGAMMA, OpKind.SUM_ROWS, OpKind.EMBEDDING_DW, OpKind.LN_DGAMMA,
+                 OpKind.CROSS_ENTROPY) or k in ROW_BINARY or k in ROW_WISE:
             return self._ext(x, ins)
         if k in ELEMENTWISE:
             a, b = ins
@@ -201,8 +213,11 @@ class _Prop:
             return R
         if k is OpKind.TRANSPOSE:
             a = ins[0]
+            perm = tuple(x.attrs["perm"])
+            if a == S0 and len(perm) > 2 and perm[0] == 0:
+                return S0                            # rows stay on their rank
             if a in (S0, S1):
-                if tuple(x.attrs["perm"]) != (1, 0):
+                if perm != (1, 0):
                     raise Unshardable("transpose of a sharded tensor beyond 2-D")
                 return S1 if a == S0 else S0
             return a
@@ -212,8 +227,8 @@ class _Prop:
                 raise Unshardable("reshape of a column-sharded tensor")
             if a == S0:
                 tgt = x.attrs["target_shape"]
-                if not tgt or tgt[0] != self.batch:
-                    raise Unshardable("reshape that moves the batch dimension")
+                if not tgt or tgt[0] % self.world:
+                    raise Unshardable("reshape whose leading dimension does not split over the ranks")
             return a
         if k is OpKind.MATMUL:
             a, b = ins
@@ -252,6 +267,34 @@ class _Prop:
             if not self._rank0(x.inputs[r_side]):
                 raise Unshardable(f"node {x.node_id}: replicated tensor meets a sharded one")
             return a if a != R else b
+        if k in ROW_WISE:
+            # sharded operands: the rows / batch entries; replicated ones: parameters (gamma,
+            # beta, bias, embedding table); EMBEDDING's table is operand 0
+            sh = [st for st in ins if st != R]
+            if not sh:
+                return R
+            if any(st != S0 for st in sh):
+                raise Unshardable(f"node {x.node_id}: {k.value} of {ins}")
+            if k in (OpKind.BMM, OpKind.BMM_NT, OpKind.BMM_TN, OpKind.SOFTMAX_GRAD, OpKind.CROSS_ENTROPY_GRAD,
+                     OpKind.LAYERNORM_DX) and len(sh) != 2:
+                raise Unshardable(f"node {x.node_id}: {k.value} mixes sharded and replicated rows")
+            if k is OpKind.EMBEDDING and ins[0] != R:
+                raise Unshardable(f"node {x.node_id}: sharded embedding table")
+            if k in (OpKind.LAYERNORM, OpKind.BIAS_ADD) and ins[0] != S0:
+                raise Unshardable(f"node {x.node_id}: {k.value} of replicated rows with sharded parameters")
+            return S0
+        if k in (OpKind.EMBEDDING_DW, OpKind.LN_DGAMMA):
+            if ins == [S0, S0]:
+                return PSUM
+            if ins == [R, R]:
+                return R
+            raise Unshardable(f"node {x.node_id}: {k.value} of {ins}")
+        if k is OpKind.CROSS_ENTROPY:
+            if ins == [S0, S0]:
+                return PAVG
+            if ins == [R, R]:
+                return R
+            raise Unshardable(f"node {x.node_id}: cross_entropy of {ins}")
         if k in (OpKind.CONV2D, OpKind.CONV2D_T):
             xs, w = ins
             if w != R:
@@ -328,6 +371,9 @@ def _rewrite(insts, prop: _Prop) -> list:
                 tgt = list(x.attrs["target_shape"])
                 tgt[0] //= prop.world
                 y = ExecOp(x.node_id, x.kind, dict(x.attrs, target_shape=tuple(tgt)), x.inputs)
+            if x.kind is OpKind.CROSS_ENTROPY_GRAD and prop.state.get(x.node_id) == S0:
+                rows = prop.node_shapes[x.node_id][0]        # divide by the global row count
+                y = ExecOp(x.node_id, x.kind, dict(x.attrs, rows=float(rows)), x.inputs)
             out.append(y)
             if x.node_id in prop.reduce_at:
                 out.append(AllReduce(x.node_id, prop.reduce_at[x.node_id]))

@@ -569,7 +569,7 @@ class Planner:
         for s_ in in_shapes + [()] * (MAX_XIN - len(in_shapes)):
             word += [len(s_)] + _pad(s_)
         word += [len(out_shape)] + _pad(out_shape)
-        word += [len(attr)] + _pad(attr) + [_f64_bits(float(x.attrs.get("value", 0.0)))]
+        word += [len(attr)] + _pad(attr) + [_f64_bits(float(x.attrs.get("value", x.attrs.get("rows", 0.0))))]
         word += out_words(nid, late)
         word += self._shadow_words(x, cells, in_shapes)
         self._invalidate(pubs[nid])

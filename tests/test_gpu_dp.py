@@ -52,3 +52,32 @@ def test_forced_dp_dcgan(prec, tol):
         be.close()
     assert st.counters() == ref_st.counters()
     assert_close(ref, got, tol, False)
+
+
+@pytest.mark.parametrize("prec,tol", [("f64", 1e-10), ("bf16", 3e-2)])
+def test_forced_dp_gpt2(prec, tol):
+    """C4 (GPT-2) with a forced 1-rank sharding: all-reduce nodes for every parameter
+    gradient and the loss in the pass graph (the cross-entropy gradient rewritten to the
+    global row count); results within tolerance of the oracle."""
+    import numpy as np
+    from paper_2201_09210_b200.workloads import C4_SMALL, gpt2_program
+    from test_gpu_coexec import run
+    src = gpt2_program(steps=8, **C4_SMALL)
+    ref, ref_st, _ = run(src, "coexec", CpuBackend())
+    be = B200Backend(precision=prec, dp=DPGroup(0, 1, C4_SMALL["batch"], force=True))
+    try:
+        o = coexec.Orchestrator(lang.parse(src), SyntheticDataset(0), coexec.Mode.coexec, coexec.RunConfig(), be)
+        got, st = o.run()
+        plans = [p.last_plan for p in be._programs if p.last_plan is not None]
+        assert plans, "no pass graph ran"
+        assert all(p.dp is not None and not p.dp.replicated for p in plans), [p.dp and p.dp.reason for p in plans]
+        assert max(len(p.dp.allreduce_nodes) for p in plans) >= 20
+    finally:
+        be.close()
+    assert st.counters() == ref_st.counters()
+    for a, b in zip(ref.lines, got.lines):
+        assert abs(float(a) - float(b)) <= tol * abs(float(a))
+    keys = sorted(ref.vars)
+    w = np.concatenate([ref.vars[k].data.ravel() for k in keys])
+    g = np.concatenate([got.vars[k].data.ravel() for k in keys])
+    assert np.linalg.norm(g - w) <= min(tol, 2e-2) * np.linalg.norm(w)
