@@ -14,6 +14,9 @@ Workloads (paper_2201_09210_b200/workloads.py):
 * ``c1`` -- configs[0], the tiny MLP the reference's own CPU path can express (f64 parity).
 * ``c4`` -- configs[3], GPT-2 small (12 layers, d=768, 12 heads, T=1024, batch 8, vocab
   50257), hand-written backward, data-dependent ``while`` over the fetched loss; bf16.
+* ``c5`` -- configs[4], Music Transformer (6 layers, d=512, 8 heads, T=1024, batch 8, vocab
+  388, relative attention with the skew), generator / try-except control flow simulated
+  with natives; bf16.
 
 A *step* is one training iteration run by the co-execution orchestrator: the Python
 skeleton walks the step while the B200 executes the step's CUDA graph (one
@@ -59,7 +62,8 @@ from paper_2201_09210_b200.coexec import Phase  # noqa: E402
 from paper_2201_09210_b200.dataset import SyntheticDataset  # noqa: E402
 from paper_2201_09210_b200.tensor import OpKind, Tensor, shape_size  # noqa: E402
 from paper_2201_09210_b200.workloads import (C1, C2, InMemoryDataset, c1_flops, c1_program,  # noqa: E402
-                                             C4, dcgan_flops, dcgan_program, gpt2_flops, gpt2_program)
+                                             C4, C5, dcgan_flops, dcgan_program, gpt2_flops, gpt2_program,
+                                             music_transformer_program)
 
 METRIC = "training iterations/sec at 1/2/4/8 B200 vs ref CPU co-exec; % HBM/tensor roofline"
 UNIT = "it/s"
@@ -216,11 +220,12 @@ def tensor_gemm(peak_tflops, peak_kind, size: int = 8192):
 
 
 def roofline_c2(be, hbm_peak, tflops_peak, peak_kind, workload="c2"):
-    """Per-kernel-family breakdown of one D+G step pair (C2) or one step (C4) -- eager
+    """Per-kernel-family breakdown of one D+G step pair (C2) or one step (C4, C5) -- eager
     re-launch, CUDA events on the context stream -- and the roofline of the dominant family."""
     from tools.step_ops import by_family, profile_ops, record_step_ops
-    if workload == "c4":
-        ops = record_step_ops(be, lambda n: gpt2_program(steps=n, **C4), 1)
+    if workload in DECODERS:
+        cfg0, prog, _ = DECODERS[workload]
+        ops = record_step_ops(be, lambda n: prog(steps=n, **cfg0), 1)
     else:
         ops = record_step_ops(be, lambda n: dcgan_program(steps=n, **C2), 2)
     rows = profile_ops(be, ops, reps=10)
@@ -297,34 +302,40 @@ def cpu_baseline_c2(steps: int = 2):
                       f"{C2['batch']}; host cpu_count={os.cpu_count()}"}
 
 
-def cpu_baseline_c4(steps: int = 1):
-    """CPU oracle co-execution of C4 on a bounded sample: GPT-2 small's width (d=768, 12 heads)
-    at 1 layer, batch 1, T=64, vocabulary 4096; per-step time scaled to the full step by the
-    GEMM-FLOP ratio (stated in the sample)."""
+# decoder workloads: (full config, program builder, extra gpt2_flops keywords)
+DECODERS = {"c4": (C4, gpt2_program, {}), "c5": (C5, music_transformer_program, {"music": True})}
+
+
+def cpu_baseline_c4(steps: int = 1, workload: str = "c4"):
+    """CPU oracle co-execution of C4 (C5) on a bounded sample: the config's width (d, heads)
+    at 1 layer, batch 1, T=64 (C4: vocabulary 4096); per-step time scaled to the full step by
+    the GEMM-FLOP ratio (stated in the sample)."""
     from oracle.cpu_backend import CpuBackend
-    small = dict(C4, batch=1, seq=64, layers=1, vocab=4096)
-    o = make_orch(gpt2_program(steps=10_000, **small), SyntheticDataset(1000), CpuBackend())
+    full, prog, fk = DECODERS[workload]
+    small = dict(full, batch=1, seq=64, layers=1, vocab=min(full["vocab"], 4096))
+    o = make_orch(prog(steps=10_000, **small), SyntheticDataset(1000), CpuBackend())
     reach_coexec(o)
     t0 = time.perf_counter()
     for _ in range(steps):
         o.step()
     dt = (time.perf_counter() - t0) / steps
-    scale = gpt2_flops(**C4) / gpt2_flops(**small)
+    scale = gpt2_flops(**full, **fk) / gpt2_flops(**small, **fk)
     return {"value": round(1.0 / (dt * scale), 8), "unit": UNIT, "cores": 2, "kind": "port",
-            "sample": f"C4 co-exec on the CPU oracle at 1 layer, batch 1, T=64, vocab 4096 (d, heads of GPT-2 small), "
-                      f"{steps} step(s) after tracing ({dt:.1f} s/step), scaled x{scale:.0f} by the GEMM-FLOP ratio "
-                      f"to the full step; host cpu_count={os.cpu_count()}"}
+            "sample": f"{workload.upper()} co-exec on the CPU oracle at 1 layer, batch 1, T=64, vocab {small['vocab']} "
+                      f"(d={full['d']}, {full['heads']} heads), {steps} step(s) after tracing ({dt:.1f} s/step), "
+                      f"scaled x{scale:.0f} by the GEMM-FLOP ratio to the full step; host cpu_count={os.cpu_count()}"}
 
 
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    if args.workload == "c4":
+    if args.workload in DECODERS:
         k = 1
-        base = cpu_baseline_c4(1)
-        cfg = {"workload": "C4 GPT-2 small, batch 8 x 1024 tokens, coexec (CPU oracle runner, f64)",
-               "global_batch": C4["batch"]}
+        base = cpu_baseline_c4(1, args.workload)
+        cfg = {"workload": ("C4 GPT-2 small" if args.workload == "c4" else "C5 Music Transformer") +
+                           ", batch 8 x 1024 tokens, coexec (CPU oracle runner, f64)",
+               "global_batch": DECODERS[args.workload][0]["batch"]}
     elif args.workload == "c2":
         base = cpu_baseline_c2(max(2, min(args.steps, 4)))
         k = max(2, min(args.steps, 4))
@@ -346,24 +357,27 @@ def workload_setup(args, world: int):
     """(program source, synthetic dataset, e2e host records, per-rank H2D bytes, config dict)."""
     import numpy as np
     rr = np.random.default_rng(7)
-    if args.workload == "c4":
-        gb = C4["batch"] * world
-        cfg4 = dict(C4, batch=gb)
-        src = gpt2_program(steps=100_000, **cfg4)
-        t = C4["seq"]
+    if args.workload in DECODERS:
+        full, prog, fk = DECODERS[args.workload]
+        gb = full["batch"] * world
+        src = prog(steps=100_000, **dict(full, batch=gb))
+        t = full["seq"]
         recs = {"tokens": [Tensor((gb, t), rr.uniform(-1, 1, (gb, t))) for _ in range(2)],
                 "targets": [Tensor((gb, t), rr.uniform(-1, 1, (gb, t))) for _ in range(2)]}
         import re
-        for m in re.finditer(r'input\("(\w+_init)", \[([0-9, ]+)\]\)', gpt2_program(steps=1, **C4)):
+        for m in re.finditer(r'input\("(\w+_init)", \[([0-9, ]+)\]\)', prog(steps=1, **full)):
             shp = tuple(int(v) for v in m.group(2).split(","))
             recs[m.group(1)] = [Tensor(shp, rr.uniform(-1, 1, shp))]
-        cfg = {"workload": "C4 GPT-2 small (12 pre-LN blocks, d=768, 12 heads, T=1024, vocab 50257, tied head), "
-                           "batch 8 sequences/GPU, hand-written backward, SGD, data-dependent while over the "
-                           "fetched loss",
-               "global_batch": gb, "per_gpu_batch": C4["batch"], "seq_len": t,
+        desc = ("C4 GPT-2 small (12 pre-LN blocks, d=768, 12 heads, T=1024, vocab 50257, tied head)"
+                if args.workload == "c4" else
+                "C5 Music Transformer (6 pre-LN blocks, d=512, 8 heads, ff 2048, T=1024, vocab 388, relative "
+                "attention with the skew, untied head; generator while + try/except SwitchCase on natives)")
+        cfg = {"workload": desc + ", batch 8 sequences/GPU, hand-written backward, SGD, data-dependent while over "
+                                  "the fetched loss",
+               "global_batch": gb, "per_gpu_batch": full["batch"], "seq_len": t,
                "parallelism": f"dp{world}" if world == 1 else f"dp{world} (batch-sharded, NCCL all-reduce)",
-               "algorithmic_flops_per_step": gpt2_flops(**C4)}
-        h2d = 2 * C4["batch"] * t * 8
+               "algorithmic_flops_per_step": gpt2_flops(**full, **fk)}
+        h2d = 2 * full["batch"] * t * 8
         return src, SyntheticDataset(1000), recs, h2d, cfg, gb
     if args.workload == "c2":
         gb = C2["batch"] * world
@@ -450,9 +464,9 @@ def run_b200(args):
     clocks = clk.summary()
     roof = tgemm = None
     if rank == 0:                      # kernel evidence while this context is alive
-        if args.workload in ("c2", "c4"):
+        if args.workload in ("c2", "c4", "c5"):
             roof = roofline_c2(be, hbm, tfl, peak_kind, args.workload)
-            if args.workload == "c4":
+            if args.workload in DECODERS:
                 roof["unit_of_work"] = "one training step"
                 for f in roof.get("families", {}).values():
                     for k in list(f):
@@ -483,7 +497,8 @@ def run_b200(args):
     be2.close()
     if rank == 0:
         if world == 1 and not args.no_cpu_baseline:
-            base = {"c1": lambda: cpu_baseline(12), "c2": cpu_baseline_c2, "c4": cpu_baseline_c4}[args.workload]()
+            base = {"c1": lambda: cpu_baseline(12), "c2": cpu_baseline_c2, "c4": cpu_baseline_c4,
+                    "c5": lambda: cpu_baseline_c4(1, "c5")}[args.workload]()
         else:
             base = None
         cfg.update({"l2": "flushed (256 MiB write) between timed steps", "tracing_steps_before_coexec": pre,
@@ -516,7 +531,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=None)
     ap.add_argument("--warmup", type=int, default=10)
-    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c4"])
+    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c4", "c5"])
     ap.add_argument("--precision", default=None, choices=["f64", "fp32", "bf16"])
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -524,7 +539,7 @@ def main():
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.steps is None:
-        args.steps = {"c1": 200, "c2": 100, "c4": 20}[args.workload]
+        args.steps = {"c1": 200, "c2": 100, "c4": 20, "c5": 20}[args.workload]
     if args.precision is None:
         args.precision = "f64" if args.workload == "c1" else "bf16"
     if args.impl == "reference":

@@ -77,6 +77,9 @@ enum coex_opkind {
   COEX_SOFTMAX_GRAD,       /* (y, dy) -> scale*y*(dy - sum(dy*y)) */
   COEX_CROSS_ENTROPY,      /* (logits [R, V], ids [R]) -> mean loss */
   COEX_CROSS_ENTROPY_GRAD, /* -> (softmax - onehot) / R */
+  /* relative attention (config C5, Music Transformer) */
+  COEX_REL_SKEW = 42,      /* (x [.., T, T]) -> y[i, j] = x[i, T-1-i+j] for j <= i, else 0 */
+  COEX_REL_UNSKEW,         /* adjoint: dx[i, m] = dy[i, m-(T-1)+i] for m >= T-1-i, else 0 */
   COEX_NUM_KINDS
 };
 

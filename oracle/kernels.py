@@ -34,6 +34,9 @@ reference; written in tensor.py's style (explicit orders):
   sequential sum); SOFTMAX_GRAD(y, dy, scale) = scale*y*(dy - sum_j dy*y);
   CROSS_ENTROPY(logits, ids) = mean over rows of logsumexp - logit[id];
   CROSS_ENTROPY_GRAD = (softmax - onehot) / R.
+* C5 (Music Transformer): REL_SKEW(x)[i, j] = x[i, T-1-i+j] for j <= i else 0 (the
+  relative-attention skew of Huang et al.: column T-1-(i-j) of Q.E_r^T holds distance
+  j-i); REL_UNSKEW is its adjoint: dx[i, m] = dy[i, m-(T-1)+i] for m >= T-1-i else 0.
 """
 
 from __future__ import annotations
@@ -213,6 +216,16 @@ def transformer_kernel(kind: OpKind, attrs: dict, x: list, out_shape):
         return (((dxh - m1[:, None]) - xhat * m2[:, None]) * rstd[:, None]).reshape(out_shape)
     if kind is OpKind.BIAS_ADD:
         return x[0] + x[1]
+    if kind in (OpKind.REL_SKEW, OpKind.REL_UNSKEW):
+        t = x[0].shape[-1]
+        a = x[0].reshape(-1, t, t)
+        out = np.zeros_like(a)
+        for i in range(t):
+            if kind is OpKind.REL_SKEW:        # out[i, 0..i] = a[i, T-1-i .. T-1]
+                out[:, i, :i + 1] = a[:, i, t - 1 - i:]
+            else:                              # out[i, T-1-i .. T-1] = a[i, 0..i]
+                out[:, i, t - 1 - i:] = a[:, i, :i + 1]
+        return out.reshape(out_shape)
     if kind in (OpKind.BMM, OpKind.BMM_NT, OpKind.BMM_TN):
         a, b = x
         out = np.empty(out_shape)

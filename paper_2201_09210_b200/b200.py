@@ -243,7 +243,8 @@ class B200Backend:
                    6: "decide", 7: "feed-wait", 8: "feed-fill", 9: "fetch", 10: "commit-gate", 11: "commit",
                    12: "end", 13: "fused chain", 14: "im2col", 15: "col2im", 16: "bf16 cvt", 17: "colstats",
                    18: "bn apply", 19: "split-K reduce", 20: "causal softmax", 21: "softmax grad",
-                   22: "cross-entropy", 23: "bias add", 24: "layernorm", 25: "embedding", 26: "column sum"}
+                   22: "cross-entropy", 23: "bias add", 24: "layernorm", 25: "embedding", 26: "column sum",
+                   27: "rel skew"}
 
     def set_trace(self, capacity: int):
         """Enable device-side per-kernel stamps (0 disables)."""

@@ -233,7 +233,8 @@ int infer_ext(int kind, const coex_attrs* at, const TRec* in, int* ndim, int64_t
 int infer(int kind, const coex_attrs* at, int nin, const TRec* in, int* ndim, int64_t* shape) {
   static const int arity[] = {2, 2, 2, 2, 1, 1, 1, 1, 1, 1, 1, 0, 0, 1,
                               2, 2, 2, 3, 3, 2, 1, 1, 1, 2, 2, 2,
-                              2, 2, 2, 3, 3, 2, 2, 1, 2, 2, 2, 2, 1, 2, 2, 2};
+                              2, 2, 2, 3, 3, 2, 2, 1, 2, 2, 2, 2, 1, 2, 2, 2,
+                              1, 1};
   static_assert(sizeof(arity) / sizeof(arity[0]) == COEX_NUM_KINDS, "arity table");
   if (kind < 0 || kind >= COEX_NUM_KINDS) return fail(COEX_BAD_ATTRS, "unknown op kind");
   if (nin != arity[kind]) return fail(COEX_BAD_ATTRS, "wrong number of tensor inputs");
@@ -392,7 +393,7 @@ int infer_ext(int kind, const coex_attrs* at, const TRec* in, int* ndim, int64_t
       shape[0] = a.shape[0]; shape[1] = m; shape[2] = n;
       return COEX_OK;
     }
-    case COEX_CAUSAL_SOFTMAX: case COEX_SOFTMAX_GRAD: {
+    case COEX_CAUSAL_SOFTMAX: case COEX_SOFTMAX_GRAD: case COEX_REL_SKEW: case COEX_REL_UNSKEW: {
       const TRec& x = in[0];
       if (x.ndim < 2 || x.shape[x.ndim - 1] != x.shape[x.ndim - 2])
         return fail(COEX_SHAPE_MISMATCH, "softmax: square trailing [T, T] block required");
@@ -475,7 +476,7 @@ struct OpSpec {
 constexpr int kBnBwdFused = 100;
 bool is_ext_compute(int kind) {
   return (kind >= COEX_CONV2D && kind <= COEX_SUM_ROWS) || kind == kBnBwdFused ||
-         (kind >= COEX_EMBEDDING && kind <= COEX_CROSS_ENTROPY_GRAD && kind != COEX_GELU && kind != COEX_GELU_GRAD);
+         (kind >= COEX_EMBEDDING && kind <= COEX_REL_UNSKEW && kind != COEX_GELU && kind != COEX_GELU_GRAD);
 }
 int ew_code(int kind) {
   switch (kind) {
@@ -1249,7 +1250,7 @@ int build_xop_t(coex_ctx* c, const OpSpec& s, Launch* L, int* nL, size_t* ws_byt
     }
     case COEX_EMBEDDING: case COEX_EMBEDDING_DW: case COEX_LAYERNORM: case COEX_LAYERNORM_DX: case COEX_LN_DGAMMA:
     case COEX_BIAS_ADD: case COEX_CAUSAL_SOFTMAX: case COEX_SOFTMAX_GRAD: case COEX_CROSS_ENTROPY:
-    case COEX_CROSS_ENTROPY_GRAD: {
+    case COEX_CROSS_ENTROPY_GRAD: case COEX_REL_SKEW: case COEX_REL_UNSKEW: {
       RowParams rp{};
       rp.ds = s.ds; rp.x = s.in[0]; rp.y = s.in[1];
       rp.z = s.nin > 2 ? s.in[2] : In{nullptr, nullptr, nullptr};
@@ -1311,6 +1312,14 @@ int build_xop_t(coex_ctx* c, const OpSpec& s, Launch* L, int* nL, size_t* ws_byt
           rp.d = d; rp.rows = xn / d; rp.T = (int)d;
           void* fn = s.kind == COEX_CAUSAL_SOFTMAX ? (is_f64(c) ? (void*)k_causal_softmax<double> : (void*)k_causal_softmax<float>)
                                                    : (is_f64(c) ? (void*)k_softmax_grad<double> : (void*)k_softmax_grad<float>);
+          L[(*nL)++].set(fn, warp_rows(rp.rows), dim3(256), rp);
+          return COEX_OK;
+        }
+        case COEX_REL_SKEW: case COEX_REL_UNSKEW: {
+          if (!build) break;
+          rp.d = d; rp.rows = xn / d;
+          void* fn = s.kind == COEX_REL_SKEW ? (is_f64(c) ? (void*)k_rel_skew<double, 0> : (void*)k_rel_skew<float, 0>)
+                                             : (is_f64(c) ? (void*)k_rel_skew<double, 1> : (void*)k_rel_skew<float, 1>);
           L[(*nL)++].set(fn, warp_rows(rp.rows), dim3(256), rp);
           return COEX_OK;
         }

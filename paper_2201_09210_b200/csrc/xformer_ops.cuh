@@ -151,6 +151,35 @@ __global__ void __launch_bounds__(256) k_bias_add(RowParams p) {
   publish_late(p.out, o);
 }
 
+// ------------------------------------------------------------------ relative-attention skew (C5)
+// Rows of [.., T, T] blocks, one warp per row, i = row index inside its block, s = T-1-i:
+//   UN = 0 (rel_skew):   out[c] = c <= i ? x[c + s] : 0
+//   UN = 1 (rel_unskew): out[m] = m >= s ? x[m - s] : 0      (the adjoint)
+// Both are shifted contiguous copies: coalesced reads and writes, HBM-bound.
+template <typename T, int UN>
+__global__ void __launch_bounds__(256) k_rel_skew(RowParams p) {
+  COEX_PDL_ENTER();
+  stamp(p.ds, SK_SKEW);
+  if (skip(p.ds)) return;
+  const T* x = res<T>(p.x);
+  T* o = pick_out<T>(p.out, x, nullptr);
+  publish_early(p.out, o);
+  count_op(p.ds);
+  const int lane = threadIdx.x & 31;
+  const long long warps = (long long)gridDim.x * (blockDim.x / 32);
+  const long long d = p.d;
+  for (long long r = (long long)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; r < p.rows; r += warps) {
+    const long long i = r % d, sh = d - 1 - i;
+    const T* xr = x + r * d;
+    T* orow = o + r * d;
+    for (long long c = lane; c < d; c += 32) {
+      if (UN == 0) orow[c] = c <= i ? xr[c + sh] : T(0);
+      else orow[c] = c >= sh ? xr[c - sh] : T(0);
+    }
+  }
+  publish_late(p.out, o);
+}
+
 // ------------------------------------------------------------------ layernorm
 // One warp per row; the row is read twice (mean, then centred moments) from L1/L2.
 template <typename T>

@@ -61,7 +61,8 @@ NONLINEAR = (OpKind.RELU, OpKind.SIGMOID, OpKind.TANH, OpKind.LEAKY_RELU, OpKind
 ROW_BINARY = (OpKind.RELU_GRAD, OpKind.LEAKY_RELU_GRAD, OpKind.BCE_TERM, OpKind.GELU_GRAD, OpKind.TO_INDEX)
 # C4 ops whose rows (or batch entries) are independent: sharded in, sharded out
 ROW_WISE = (OpKind.LAYERNORM, OpKind.LAYERNORM_DX, OpKind.BIAS_ADD, OpKind.CAUSAL_SOFTMAX, OpKind.SOFTMAX_GRAD,
-            OpKind.BMM, OpKind.BMM_NT, OpKind.BMM_TN, OpKind.EMBEDDING, OpKind.CROSS_ENTROPY_GRAD)
+            OpKind.BMM, OpKind.BMM_NT, OpKind.BMM_TN, OpKind.EMBEDDING, OpKind.CROSS_ENTROPY_GRAD,
+            OpKind.REL_SKEW, OpKind.REL_UNSKEW)
 
 
 @dataclass

@@ -41,7 +41,7 @@ XOP = {OpKind.CONV2D, OpKind.CONV2D_T, OpKind.CONV2D_DW, OpKind.BATCHNORM, OpKin
        OpKind.BN_DGAMMA, OpKind.SUM_ROWS,
        OpKind.EMBEDDING, OpKind.EMBEDDING_DW, OpKind.LAYERNORM, OpKind.LAYERNORM_DX, OpKind.LN_DGAMMA,
        OpKind.BIAS_ADD, OpKind.BMM, OpKind.BMM_NT, OpKind.BMM_TN, OpKind.CAUSAL_SOFTMAX, OpKind.SOFTMAX_GRAD,
-       OpKind.CROSS_ENTROPY, OpKind.CROSS_ENTROPY_GRAD}
+       OpKind.CROSS_ENTROPY, OpKind.CROSS_ENTROPY_GRAD, OpKind.REL_SKEW, OpKind.REL_UNSKEW}
 EW_CODE = {OpKind.ADD: 0, OpKind.SUB: 1, OpKind.MUL: 2, OpKind.NEG: 3, OpKind.RELU: 4, OpKind.SIGMOID: 5,
            OpKind.TANH: 7, OpKind.LEAKY_RELU: 8, OpKind.RELU_GRAD: 9, OpKind.LEAKY_RELU_GRAD: 10,
            OpKind.BCE_TERM: 11, OpKind.TO_INDEX: 12, OpKind.GELU_GRAD: 13, OpKind.GELU: 14}

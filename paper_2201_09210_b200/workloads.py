@@ -190,6 +190,27 @@ def c1_flops(batch=64, hidden=128, din=784, dout=10) -> int:
 
 def gpt2_program(steps: int = 20, batch: int = 8, seq: int = 1024, d: int = 768, heads: int = 12, layers: int = 12,
                  vocab: int = 50257, lr: float = 0.01) -> str:
+    return _decoder_program(steps, batch, seq, d, heads, layers, vocab, lr, music=False)
+
+
+def music_transformer_program(steps: int = 20, batch: int = 8, seq: int = 1024, d: int = 512, heads: int = 8,
+                              layers: int = 6, vocab: int = 388, lr: float = 0.01) -> str:
+    """BASELINE.json configs[4]: Music Transformer training on synthetic
+    event sequences.
+
+    The GPT-2 decoder of :func:`gpt2_program` with (1) relative attention: per layer a
+    relative-position table ``er`` [T, hd] shared by the heads, logits
+    ``q.k^T + rel_skew(q.er^T)`` (the memory-efficient skew of Huang et al. 2018) and the
+    adjoint ``rel_unskew`` in the backward pass; (2) an untied output projection; (3) the
+    config's Python control features simulated with natives: a *generator* yielding a
+    host-drawn number of learning-rate decay steps (``while k < native choice(3, 2)``) and a
+    *try/except* whose except-path (``native coin(1)``) drops the relative-table update of
+    the step -- a SwitchCase with an assignment in one arm only.
+    """
+    return _decoder_program(steps, batch, seq, d, heads, layers, vocab, lr, music=True)
+
+
+def _decoder_program(steps, batch, seq, d, heads, layers, vocab, lr, music) -> str:
     """BASELINE.json configs[3]: GPT-2 small training on synthetic tokens.
 
     Pre-LayerNorm decoder: token + learned position embeddings, ``layers`` blocks of causal
@@ -214,6 +235,10 @@ def gpt2_program(steps: int = 20, batch: int = 8, seq: int = 1024, d: int = 768,
                   f"var c{w}_{l} = fill([{D}], 0.0)"]
         v += [f"var wf1_{l} = mul(input(\"wf1{l}_init\", [{D}, {4 * D}]), 0.02)", f"var cf1_{l} = fill([{4 * D}], 0.0)",
               f"var wf2_{l} = mul(input(\"wf2{l}_init\", [{4 * D}, {D}]), 0.02)", f"var cf2_{l} = fill([{D}], 0.0)"]
+        if music:
+            v += [f"var er_{l} = mul(input(\"er{l}_init\", [{T}, {hd}]), 0.02)"]
+    if music:
+        v += [f"var wout = mul(input(\"wout_init\", [{D}, {V}]), 0.02)"]
 
     def heads_of(x):
         return f"reshape(transpose(reshape({x}, [{B}, {T}, {H}, {hd}]), [0, 2, 1, 3]), [{BH}, {T}, {hd}])"
@@ -231,7 +256,12 @@ def gpt2_program(steps: int = 20, batch: int = 8, seq: int = 1024, d: int = 768,
         for w in ("q", "k", "v"):
             b += [f"let {w}_{l} = bias_add(matmul(h1_{l}, w{w}_{l}), c{w}_{l})",
                   f"let {w}h_{l} = {heads_of(f'{w}_{l}')}"]
-        b += [f"let p_{l} = causal_softmax(bmm_nt(qh_{l}, kh_{l}), {sc})",
+        if music:
+            b += [f"let qe_{l} = reshape(matmul(reshape(qh_{l}, [{BH * T}, {hd}]), transpose(er_{l})), [{BH}, {T}, {T}])",
+                  f"let p_{l} = causal_softmax(add(bmm_nt(qh_{l}, kh_{l}), rel_skew(qe_{l})), {sc})"]
+        else:
+            b += [f"let p_{l} = causal_softmax(bmm_nt(qh_{l}, kh_{l}), {sc})"]
+        b += [
               f"let o_{l} = {merge(f'bmm(p_{l}, vh_{l})')}",
               f"let xa_{l} = add({x}, bias_add(matmul(o_{l}, wo_{l}), co_{l}))",
               f"let h2_{l} = layernorm(xa_{l}, g2_{l}, b2_{l})",
@@ -239,11 +269,16 @@ def gpt2_program(steps: int = 20, batch: int = 8, seq: int = 1024, d: int = 768,
               f"let f_{l} = gelu(pre_{l})",
               f"let x{l + 1} = add(xa_{l}, bias_add(matmul(f_{l}, wf2_{l}), cf2_{l}))"]
     b += [f"let hf = layernorm(x{L}, gf, bfn)",
-          f"let logits = matmul(hf, transpose(wte))",
+          f"let logits = matmul(hf, {'wout' if music else 'transpose(wte)'})",
           f"let loss = cross_entropy(logits, tgt)",
-          f"let dlog = cross_entropy_grad(logits, tgt)",
-          f"let dwte_h = matmul(transpose(dlog), hf)",
-          f"let dhf = matmul(dlog, wte)",
+          f"let dlog = cross_entropy_grad(logits, tgt)"]
+    if music:
+        b += [f"let dwout = matmul(transpose(hf), dlog)",
+              f"let dhf = matmul(dlog, transpose(wout))"]
+    else:
+        b += [f"let dwte_h = matmul(transpose(dlog), hf)",
+              f"let dhf = matmul(dlog, wte)"]
+    b += [
           f"let dx{L} = layernorm_dx(x{L}, gf, dhf)",
           f"let dgf = ln_dgamma(x{L}, dhf)",
           f"let dbf = sum_rows(dhf)"]
@@ -261,8 +296,14 @@ def gpt2_program(steps: int = 20, batch: int = 8, seq: int = 1024, d: int = 768,
               f"let dwo_{l} = matmul(transpose(o_{l}), dxa_{l})",
               f"let dco_{l} = sum_rows(dxa_{l})",
               f"let doh_{l} = {heads_of(f'matmul(dxa_{l}, transpose(wo_{l}))')}",
-              f"let ds_{l} = softmax_grad(p_{l}, bmm_nt(doh_{l}, vh_{l}), {sc})",
-              f"let dq_{l} = {merge(f'bmm(ds_{l}, kh_{l})')}",
+              f"let ds_{l} = softmax_grad(p_{l}, bmm_nt(doh_{l}, vh_{l}), {sc})"]
+        if music:
+            b += [f"let dqe_{l} = reshape(rel_unskew(ds_{l}), [{BH * T}, {T}])",
+                  f"let der_{l} = matmul(transpose(dqe_{l}), reshape(qh_{l}, [{BH * T}, {hd}]))",
+                  f"let dq_{l} = {merge(f'add(bmm(ds_{l}, kh_{l}), reshape(matmul(dqe_{l}, er_{l}), [{BH}, {T}, {hd}]))')}"]
+        else:
+            b += [f"let dq_{l} = {merge(f'bmm(ds_{l}, kh_{l})')}"]
+        b += [
               f"let dk_{l} = {merge(f'bmm_tn(ds_{l}, qh_{l})')}",
               f"let dv_{l} = {merge(f'bmm_tn(p_{l}, doh_{l})')}"]
         for w in ("q", "k", "v"):
@@ -273,12 +314,21 @@ def gpt2_program(steps: int = 20, batch: int = 8, seq: int = 1024, d: int = 768,
               f"let dg1_{l} = ln_dgamma(x{l}, dh1_{l})",
               f"let db1_{l} = sum_rows(dh1_{l})"]
     b += [f"let dwpe = reshape(sum_rows(reshape(dx0, [{B}, {T * D}])), [{T}, {D}])",
-          f"let dwte = add(dwte_h, embedding_dw(tok, reshape(dx0, [{B}, {T}, {D}]), [{V}]))",
+          (f"let dwte = embedding_dw(tok, reshape(dx0, [{B}, {T}, {D}]), [{V}])" if music else
+           f"let dwte = add(dwte_h, embedding_dw(tok, reshape(dx0, [{B}, {T}, {D}]), [{V}]))"),
           f"let l = item(loss)",
           f"let lrs = fill([], {lr})",
           f"let k = 0",
-          f"while l > {round(math.log(V), 3)} and k < 2 {{ lrs = mul(lrs, 0.5); k = k + 1 }}",
-          f"wte = sub(wte, mul(dwte, lrs))",
+          f"while l > {round(math.log(V), 3)} and k < 2 {{ lrs = mul(lrs, 0.5); k = k + 1 }}"]
+    if music:
+        # generator: a host-drawn number of decay steps; try/except: the except arm
+        # (native coin) skips the relative-table update of this step
+        b += [f"let g = 0",
+              f"while g < native choice(3, 2) {{ lrs = mul(lrs, 0.8); g = g + 1 }}",
+              f"wout = sub(wout, mul(dwout, lrs))",
+              "if native coin(1) { print(0) } else { " +
+              "; ".join(f"er_{l} = sub(er_{l}, mul(der_{l}, lrs))" for l in range(L)) + " }"]
+    b += [f"wte = sub(wte, mul(dwte, lrs))",
           f"wpe = sub(wpe, mul(dwpe, lrs))",
           f"gf = sub(gf, mul(dgf, lrs))",
           f"bfn = sub(bfn, mul(dbf, lrs))"]
@@ -293,12 +343,17 @@ def gpt2_program(steps: int = 20, batch: int = 8, seq: int = 1024, d: int = 768,
 
 C4 = dict(batch=8, seq=1024, d=768, heads=12, layers=12, vocab=50257)
 C4_SMALL = dict(batch=2, seq=32, d=64, heads=4, layers=2, vocab=97)
+C5 = dict(batch=8, seq=1024, d=512, heads=8, layers=6, vocab=388)
+C5_SMALL = dict(batch=2, seq=16, d=32, heads=2, layers=2, vocab=29)
 
 
-def gpt2_flops(batch=8, seq=1024, d=768, heads=12, layers=12, vocab=50257, **_) -> int:
-    """GEMM FLOPs of one C4 training step (forward + backward, 2*M*N*K per product)."""
+def gpt2_flops(batch=8, seq=1024, d=768, heads=12, layers=12, vocab=50257, music=False, **_) -> int:
+    """GEMM FLOPs of one C4 (C5 with ``music``) training step (forward + backward,
+    2*M*N*K per product; C5 adds the q.er^T relative logits)."""
     bt = batch * seq
     per_layer_fwd = 2 * bt * d * (3 * d) + 2 * bt * d * d + 2 * bt * d * 4 * d * 2 + 2 * 2 * batch * heads * seq * seq * (d // heads)
+    if music:
+        per_layer_fwd += 2 * batch * heads * seq * seq * (d // heads)
     head_fwd = 2 * bt * d * vocab
     return 3 * (layers * per_layer_fwd + head_fwd)
 

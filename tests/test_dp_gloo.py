@@ -17,12 +17,13 @@ from paper_2201_09210_b200 import coexec, lang
 from paper_2201_09210_b200.dataset import SyntheticDataset
 from paper_2201_09210_b200.dp import DPGroup
 from paper_2201_09210_b200.tensor import Tensor
-from paper_2201_09210_b200.workloads import c1_program, dcgan_program, gpt2_program
+from paper_2201_09210_b200.workloads import c1_program, dcgan_program, gpt2_program, music_transformer_program
 
 SMALL_C1 = c1_program(steps=12, batch=8, hidden=16, din=12, dout=3)
 BATCH = 8
 SMALL_C2 = dcgan_program(steps=6, batch=8, nz=6, ngf=4, ndf=4, img=16)
 SMALL_C4 = gpt2_program(steps=4, batch=BATCH, seq=8, d=16, heads=2, layers=2, vocab=23)
+SMALL_C5 = music_transformer_program(steps=8, batch=BATCH, seq=8, d=16, heads=2, layers=2, vocab=23)
 
 
 class DupHalves(SyntheticDataset):
@@ -135,13 +136,16 @@ def test_dp2_dcgan_matches_global_batch():
         np.testing.assert_array_equal(r0[1][k], r1[1][k])
 
 
-def test_dp2_gpt2_matches_global_batch():
-    """C4 (GPT-2) data parallel at world size 2: sequences sharded through embeddings,
-    layernorms, attention (batch = sequences x heads) and the MLP; weight, bias, layernorm
-    and embedding gradients all-reduced (P+), the loss averaged (P~), the cross-entropy
-    gradient divided by the global row count -- equal to the global-batch run."""
-    ref, ref_st = coexec.run(lang.parse(SMALL_C4), SyntheticDataset(0), "coexec", backend=CpuBackend())
-    out = run_dp(SMALL_C4)
+@pytest.mark.parametrize("src", [SMALL_C4, SMALL_C5], ids=["gpt2", "music_transformer"])
+def test_dp2_gpt2_matches_global_batch(src):
+    """C4 (GPT-2) / C5 (Music Transformer) data parallel at world size 2: sequences sharded
+    through embeddings, layernorms, attention (batch = sequences x heads; C5's relative
+    logits q.er^T and their skew row-wise) and the MLP; weight, bias, layernorm, embedding
+    and relative-table gradients all-reduced (P+), the loss averaged (P~), the
+    cross-entropy gradient divided by the global row count -- equal to the global-batch
+    run."""
+    ref, ref_st = coexec.run(lang.parse(src), SyntheticDataset(0), "coexec", backend=CpuBackend())
+    out = run_dp(src)
     r0, r1 = out[0], out[1]
     assert r0[0] == r1[0] and r0[3] == r1[3] and r0[2] == r1[2]
     assert r0[2] == ref_st.counters()

@@ -1,0 +1,85 @@
+"""CPU checks of the builder-defined extension ops (SURVEY §8(a) row a*, parity unpinned
+by the reference) that the GPU parity tests rely on: the f64 restatements in
+oracle/kernels.py against torch autograd, and config C5 (Music Transformer) through the
+co-execution engine on the CPU backend."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle.cpu_backend import CpuBackend
+from oracle.kernels import execute_kernel
+from paper_2201_09210_b200.tensor import OpKind, Tensor
+from paper_2201_09210_b200.workloads import C5_SMALL, music_transformer_program
+from test_gpu_coexec import run
+
+RNG = np.random.default_rng(5)
+
+
+def k(kind, *xs, **attrs):
+    return execute_kernel(kind, attrs, [Tensor(x.shape, x) for x in xs])[0].data
+
+
+def t_skew(x):
+    t = x.shape[-1]
+    i = torch.arange(t).view(t, 1)
+    j = torch.arange(t).view(1, t)
+    idx = (t - 1 - i + j).clamp(max=t - 1).expand(*x.shape)
+    return torch.where(j <= i, torch.gather(x, -1, idx), torch.zeros((), dtype=x.dtype))
+
+
+@pytest.mark.parametrize("t", [1, 2, 7, 33])
+def test_rel_skew_matches_definition_and_adjoint(t):
+    x = RNG.standard_normal((3, t, t))
+    dy = RNG.standard_normal((3, t, t))
+    y = k(OpKind.REL_SKEW, x)
+    assert np.array_equal(y, t_skew(torch.from_numpy(x)).numpy())
+    for i in range(t):                       # column j of row i holds relative distance j - i
+        for j in range(t):
+            assert y[1, i, j] == (x[1, i, t - 1 - i + j] if j <= i else 0.0)
+    dx = k(OpKind.REL_UNSKEW, dy)
+    assert abs(np.sum(y * dy) - np.sum(x * dx)) <= 1e-12 * np.sum(np.abs(x * dx))
+
+
+def test_relative_attention_backward_formulas():
+    """The C5 program's hand-written attention backward (workloads._decoder_program, music)
+    equals torch autograd of softmax(sc * (q.k^T + skew(q.er^T))) . v."""
+    bh, t, hd = 3, 9, 4
+    sc = 0.5
+    q, kk, v = (RNG.standard_normal((bh, t, hd)) for _ in range(3))
+    er = RNG.standard_normal((t, hd))
+    g = RNG.standard_normal((bh, t, hd))
+    # oracle restatement, in the program's order
+    qe = k(OpKind.MATMUL, q.reshape(bh * t, hd), er.T.copy()).reshape(bh, t, t)
+    s = k(OpKind.ADD, k(OpKind.BMM_NT, q, kk), k(OpKind.REL_SKEW, qe))
+    p = k(OpKind.CAUSAL_SOFTMAX, s, value=sc)
+    ds = k(OpKind.SOFTMAX_GRAD, p, k(OpKind.BMM_NT, g, v), value=sc)
+    dqe = k(OpKind.REL_UNSKEW, ds).reshape(bh * t, t)
+    der = k(OpKind.MATMUL, dqe.T.copy(), q.reshape(bh * t, hd))
+    dq = k(OpKind.BMM, ds, kk) + k(OpKind.MATMUL, dqe, er).reshape(bh, t, hd)
+    dk = k(OpKind.BMM_TN, ds, q)
+    # torch autograd
+    tq, tk, tv, te = (torch.tensor(a, requires_grad=True) for a in (q, kk, v, er))
+    ts = tq @ tk.transpose(1, 2) + t_skew(tq @ te.T)
+    mask = torch.ones(t, t, dtype=torch.bool).tril()
+    tp = torch.softmax((sc * ts).masked_fill(~mask, -torch.inf), -1)
+    (tp @ tv * torch.from_numpy(g)).sum().backward()
+    np.testing.assert_allclose(p, tp.detach().numpy(), rtol=1e-12, atol=1e-14)
+    np.testing.assert_allclose(dq, tq.grad.numpy(), rtol=1e-10, atol=1e-12)
+    np.testing.assert_allclose(dk, tk.grad.numpy(), rtol=1e-10, atol=1e-12)
+    np.testing.assert_allclose(der, te.grad.numpy(), rtol=1e-10, atol=1e-12)
+
+
+def test_music_transformer_coexec_equals_imperative():
+    """C5 at its parity size: co-execution (graph + skeleton, natives driving the
+    generator loop and the try/except arm) prints and stores exactly what the imperative
+    run does, and the relative-attention program reaches the co-execution path."""
+    src = music_transformer_program(steps=6, **C5_SMALL)
+    ref, _, _ = run(src, "imperative", CpuBackend())
+    got, st, _ = run(src, "coexec", CpuBackend())
+    assert ref.lines == got.lines
+    for name in ref.vars:
+        assert np.array_equal(ref.vars[name].data, got.vars[name].data), name
+    assert st.counters()[1] > 0                      # passes run as graphs
+    kinds = {type(dc).__name__ for step in st.decision_log for dc in step}
+    assert kinds == {"CaseDecision", "LoopDecision"}

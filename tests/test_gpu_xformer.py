@@ -55,6 +55,11 @@ ROWS = [
     (OpKind.GELU, {}, [rt(1000, scale=3.0)]),
     (OpKind.GELU_GRAD, {}, [rt(50, 3), rt(50, 3)]),
     (OpKind.TO_INDEX, {}, [Tensor((6,), [-1.0, -0.5, 0.0, 0.3, 0.999999, 1.5]), Tensor((), 97.0)]),
+    # relative attention (C5): shifted copies, bit-exact in every precision
+    (OpKind.REL_SKEW, {}, [rt(3, 37, 37)]),
+    (OpKind.REL_SKEW, {}, [rt(1, 1)]),
+    (OpKind.REL_UNSKEW, {}, [rt(2, 2, 64, 64)]),
+    (OpKind.REL_UNSKEW, {}, [rt(4, 100, 100)]),
 ]
 
 
@@ -89,7 +94,7 @@ def test_bmm_tolerance(b200_factory, prec, tol, i):
 def test_row_ops(b200_factory, prec, tol, i):
     kind, attrs, ins = ROWS[i]
     got, want = run(b200_factory(prec), kind, attrs, ins)
-    if kind is OpKind.TO_INDEX or (kind is OpKind.EMBEDDING and prec == "f64"):
+    if kind is OpKind.TO_INDEX or (kind in (OpKind.EMBEDDING, OpKind.REL_SKEW, OpKind.REL_UNSKEW) and prec == "f64"):
         assert got.data.tobytes() == want.data.tobytes()
     else:
         assert nrel(got, want) <= tol

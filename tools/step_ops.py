@@ -63,6 +63,16 @@ def launch_work(kind, attrs, shapes, kernel: str, esize: int = 4):
     from paper_2201_09210_b200.tensor import flops_of, shape_size
     shapes = [tuple(x) for x in shapes]
     n_in = [shape_size(x) for x in shapes]
+    if kind in (OpKind.BMM, OpKind.BMM_NT, OpKind.BMM_TN) and (kernel.startswith("k_gemm_tc")
+                                                                or kernel.startswith("k_matmul")):
+        return "flops", flops_of(kind, shapes, attrs)
+    if kernel.startswith(("k_causal_softmax", "k_softmax_grad", "k_layernorm", "k_ln_dgamma", "k_cross_entropy",
+                          "k_rel_skew", "k_bias_add", "k_embed", "k_colsum_wide")):
+        # row kernels: every input read once, the output written once
+        out = shape_size(_conv_geo(kind, attrs, shapes))
+        if kind is OpKind.CROSS_ENTROPY:
+            out = 0
+        return "bytes", (sum(n_in) + out) * esize
     if kind is OpKind.MATMUL or kind in (OpKind.CONV2D, OpKind.CONV2D_T, OpKind.CONV2D_DW):
         out = _conv_geo(kind, attrs, shapes) if kind is not OpKind.MATMUL else (shapes[0][0], shapes[1][1])
         if kernel.startswith("k_gemm_tc") or kernel.startswith("k_matmul"):
@@ -111,6 +121,8 @@ def by_family(rows, esize=4):
             f["ms"] += r["count"] * ln["ms"]
             f["launches"] += r["count"]
             what, amount = launch_work(kind, r["attrs"], r["shapes"], name, esize)
+            if amount is not None and kind is OpKind.MATMUL and name.startswith("k_cvt_bf16"):
+                amount //= max(1, sum(1 for x in r["launches"] if x["kernel"].startswith("k_cvt_bf16")))
             if amount is None:
                 f["unknown_ms"] += r["count"] * ln["ms"]
             elif what == "flops":
@@ -135,10 +147,12 @@ def main():
     ap.add_argument("--out", default=None)
     a = ap.parse_args()
     from paper_2201_09210_b200.b200 import B200Backend
-    from paper_2201_09210_b200.workloads import C2, C4, dcgan_program, gpt2_program
+    from paper_2201_09210_b200.workloads import C2, C4, C5, dcgan_program, gpt2_program, music_transformer_program
     be = B200Backend(precision=a.precision)
     if a.workload == "c4":
         ops = record_step_ops(be, lambda n: gpt2_program(steps=n, **C4), 1)
+    elif a.workload == "c5":
+        ops = record_step_ops(be, lambda n: music_transformer_program(steps=n, **C5), 1)
     else:
         ops = record_step_ops(be, lambda n: dcgan_program(steps=n, **C2), 2)
     rows = profile_ops(be, ops, reps=int(os.environ.get("STEP_OPS_REPS", "10")))
