@@ -14,6 +14,8 @@ Workloads (paper_2201_09210_b200/workloads.py):
 * ``c1`` -- configs[0], the tiny MLP the reference's own CPU path can express (f64 parity).
 * ``c4`` -- configs[3], GPT-2 small (12 layers, d=768, 12 heads, T=1024, batch 8, vocab
   50257), hand-written backward, data-dependent ``while`` over the fetched loss; bf16.
+* ``c3`` -- configs[2], ResNet-50 (224x224, batch 64) with SDPoint: a 4-way SwitchCase on
+  ``native choice`` picks the stochastic downsampling point each step; bf16.
 * ``c5`` -- configs[4], Music Transformer (6 layers, d=512, 8 heads, T=1024, batch 8, vocab
   388, relative attention with the skew), generator / try-except control flow simulated
   with natives; bf16.
@@ -63,7 +65,7 @@ from paper_2201_09210_b200.dataset import SyntheticDataset  # noqa: E402
 from paper_2201_09210_b200.tensor import OpKind, Tensor, shape_size  # noqa: E402
 from paper_2201_09210_b200.workloads import (C1, C2, InMemoryDataset, c1_flops, c1_program,  # noqa: E402
                                              C4, C5, dcgan_flops, dcgan_program, gpt2_flops, gpt2_program,
-                                             music_transformer_program)
+                                             music_transformer_program, C3, resnet_flops, resnet_program)
 
 METRIC = "training iterations/sec at 1/2/4/8 B200 vs ref CPU co-exec; % HBM/tensor roofline"
 UNIT = "it/s"
@@ -135,6 +137,24 @@ def reach_coexec(o, budget: int = 40):
     while o.phase is not Phase.CoExec and n < budget:
         o.step()
         n += 1
+    return n
+
+
+def settle(o, quiet: int = 8, budget: int = 80) -> int:
+    """Untimed steps until `quiet` consecutive co-executed steps needed no retrace, replay or
+    graph (re)build -- workloads whose paths are drawn at random (C1's choice loop, C3's
+    SDPoint) discover their paths and speculative constants here, not in the timed region."""
+    def sig():
+        st = o.stats
+        graphs = getattr(o.compiled, "graphs", None)
+        return (st.counters(), st.shape_replays, id(o.compiled), len(graphs) if graphs is not None else 0)
+    n, calm, last = 0, 0, sig()
+    while calm < quiet and n < budget:
+        o.step()
+        n += 1
+        cur = sig()
+        calm = calm + 1 if (cur == last and o.phase is Phase.CoExec) else 0
+        last = cur
     return n
 
 
@@ -226,6 +246,8 @@ def roofline_c2(be, hbm_peak, tflops_peak, peak_kind, workload="c2"):
     if workload in DECODERS:
         cfg0, prog, _ = DECODERS[workload]
         ops = record_step_ops(be, lambda n: prog(steps=n, **cfg0), 1)
+    elif workload == "c3":
+        ops = record_step_ops(be, lambda n: resnet_program(steps=n, **C3), 1)
     else:
         ops = record_step_ops(be, lambda n: dcgan_program(steps=n, **C2), 2)
     rows = profile_ops(be, ops, reps=10)
@@ -302,6 +324,25 @@ def cpu_baseline_c2(steps: int = 2):
                       f"{C2['batch']}; host cpu_count={os.cpu_count()}"}
 
 
+def cpu_baseline_c3(steps: int = 1):
+    """CPU oracle co-execution of C3 on a bounded sample: the full ResNet-50 (widths, depth,
+    1000 classes) at batch 1 on 64x64 images; per-step time scaled to batch 64 at 224x224 by
+    the conv-FLOP ratio (stated in the sample)."""
+    from oracle.cpu_backend import CpuBackend
+    small = dict(C3, batch=1, img=64)
+    o = make_orch(resnet_program(steps=10_000, **small), SyntheticDataset(1000), CpuBackend())
+    reach_coexec(o)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        o.step()
+    dt = (time.perf_counter() - t0) / steps
+    scale = resnet_flops(**C3) / resnet_flops(**small)
+    return {"value": round(1.0 / (dt * scale), 8), "unit": UNIT, "cores": 2, "kind": "port",
+            "sample": f"C3 co-exec on the CPU oracle, full ResNet-50 at batch 1 on 64x64 images, {steps} step(s) "
+                      f"after tracing ({dt:.1f} s/step), scaled x{scale:.0f} by the conv-FLOP ratio to batch 64 at "
+                      f"224x224; host cpu_count={os.cpu_count()}"}
+
+
 # decoder workloads: (full config, program builder, extra gpt2_flops keywords)
 DECODERS = {"c4": (C4, gpt2_program, {}), "c5": (C5, music_transformer_program, {"music": True})}
 
@@ -330,7 +371,12 @@ def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    if args.workload in DECODERS:
+    if args.workload == "c3":
+        k = 1
+        base = cpu_baseline_c3(1)
+        cfg = {"workload": "C3 ResNet-50 + SDPoint, batch 64 x 224x224, coexec (CPU oracle runner, f64)",
+               "global_batch": C3["batch"]}
+    elif args.workload in DECODERS:
         k = 1
         base = cpu_baseline_c4(1, args.workload)
         cfg = {"workload": ("C4 GPT-2 small" if args.workload == "c4" else "C5 Music Transformer") +
@@ -378,6 +424,26 @@ def workload_setup(args, world: int):
                "parallelism": f"dp{world}" if world == 1 else f"dp{world} (batch-sharded, NCCL all-reduce)",
                "algorithmic_flops_per_step": gpt2_flops(**full, **fk)}
         h2d = 2 * full["batch"] * t * 8
+        return src, SyntheticDataset(1000), recs, h2d, cfg, gb
+    if args.workload == "c3":
+        gb = C3["batch"] * world
+        src = resnet_program(steps=100_000, **dict(C3, batch=gb))
+        b, img = gb, C3["img"]
+        recs = {"img": [Tensor((b, img, img, 3), rr.uniform(-1, 1, (b, img, img, 3))) for _ in range(2)],
+                "labels": [Tensor((b,), rr.uniform(-1, 1, (b,))) for _ in range(2)]}
+        import re
+        for m in re.finditer(r'input\("(\w+_init)", \[([0-9, ]+)\]\)', resnet_program(steps=1, **C3)):
+            shp = tuple(int(v) for v in m.group(2).split(","))
+            recs[m.group(1)] = [Tensor(shp, rr.uniform(-1, 1, shp))]
+        cfg = {"workload": "C3 ResNet-50 v1.5 (bottlenecks 3-4-6-3, BN, projection shortcuts, 1000 classes) with "
+                           "SDPoint: a 4-way SwitchCase on native choice picks none or a 2x2 average pool after "
+                           "stage 1/2/3 each step (path-dependent activation shapes), hand-written backward, SGD",
+               "global_batch": gb, "per_gpu_batch": C3["batch"], "image": [C3["img"], C3["img"], 3],
+               "parallelism": f"dp{world}" + ("" if world == 1 else
+                                              " (batch-sharded; per-replica batch-norm statistics; NCCL all-reduce "
+                                              "of weight / BN-parameter gradients and the loss in the pass graph)"),
+               "algorithmic_flops_per_step_without_downsampling": resnet_flops(**C3)}
+        h2d = (C3["batch"] * img * img * 3 + C3["batch"]) * 8
         return src, SyntheticDataset(1000), recs, h2d, cfg, gb
     if args.workload == "c2":
         gb = C2["batch"] * world
@@ -440,6 +506,7 @@ def run_b200(args):
     be = B200Backend(device=dev, precision=args.precision, dp=dp)
     o = make_orch(src, dataset, be)
     pre = reach_coexec(o)
+    settled = settle(o)
     for _ in range(args.warmup):
         o.step()
     if world > 1:
@@ -464,9 +531,9 @@ def run_b200(args):
     clocks = clk.summary()
     roof = tgemm = None
     if rank == 0:                      # kernel evidence while this context is alive
-        if args.workload in ("c2", "c4", "c5"):
+        if args.workload in ("c2", "c3", "c4", "c5"):
             roof = roofline_c2(be, hbm, tfl, peak_kind, args.workload)
-            if args.workload in DECODERS:
+            if args.workload != "c2":
                 roof["unit_of_work"] = "one training step"
                 for f in roof.get("families", {}).values():
                     for k in list(f):
@@ -482,6 +549,7 @@ def run_b200(args):
     be2 = B200Backend(device=dev, precision=args.precision, dp=dp)
     o2 = make_orch(src, InMemoryDataset(recs), be2)
     reach_coexec(o2)
+    settle(o2)
     for _ in range(args.warmup):
         o2.step()
     if world > 1:
@@ -497,11 +565,12 @@ def run_b200(args):
     be2.close()
     if rank == 0:
         if world == 1 and not args.no_cpu_baseline:
-            base = {"c1": lambda: cpu_baseline(12), "c2": cpu_baseline_c2, "c4": cpu_baseline_c4,
+            base = {"c1": lambda: cpu_baseline(12), "c2": cpu_baseline_c2, "c3": cpu_baseline_c3, "c4": cpu_baseline_c4,
                     "c5": lambda: cpu_baseline_c4(1, "c5")}[args.workload]()
         else:
             base = None
         cfg.update({"l2": "flushed (256 MiB write) between timed steps", "tracing_steps_before_coexec": pre,
+                    "settle_steps_before_warmup": settled,
                     "steps_replayed_in_timed_region": replays})
         line = {
             "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -531,7 +600,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=None)
     ap.add_argument("--warmup", type=int, default=10)
-    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c4", "c5"])
+    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--precision", default=None, choices=["f64", "fp32", "bf16"])
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -539,7 +608,7 @@ def main():
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.steps is None:
-        args.steps = {"c1": 200, "c2": 100, "c4": 20, "c5": 20}[args.workload]
+        args.steps = {"c1": 200, "c2": 100, "c3": 20, "c4": 20, "c5": 20}[args.workload]
     if args.precision is None:
         args.precision = "f64" if args.workload == "c1" else "bf16"
     if args.impl == "reference":

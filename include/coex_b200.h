@@ -80,6 +80,14 @@ enum coex_opkind {
   /* relative attention (config C5, Music Transformer) */
   COEX_REL_SKEW = 42,      /* (x [.., T, T]) -> y[i, j] = x[i, T-1-i+j] for j <= i, else 0 */
   COEX_REL_UNSKEW,         /* adjoint: dx[i, m] = dy[i, m-(T-1)+i] for m >= T-1-i, else 0 */
+  /* ResNet-50 / SDPoint (config C3): coex_attrs.dims = [kernel, stride, pad] */
+  COEX_CONV2D_DX = 44,     /* (dy, w [k*k*C, F], x [N,H,W,C]) -> conv2d's input gradient, x's shape */
+  COEX_MAXPOOL,            /* (x) -> [N,Ho,Wo,C], -inf padding */
+  COEX_MAXPOOL_GRAD,       /* (x, dy) -> dy routed to each window's first argmax */
+  COEX_AVGPOOL,            /* (x) -> window sum / k^2, zero padding */
+  COEX_AVGPOOL_GRAD,       /* (x, dy) -> covering dy sum / k^2 */
+  COEX_GLOBAL_AVGPOOL,     /* (x [N,H,W,C]) -> [N,C] */
+  COEX_GLOBAL_AVGPOOL_GRAD,/* (x, dy [N,C]) -> dy / (H*W) broadcast */
   COEX_NUM_KINDS
 };
 

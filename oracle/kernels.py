@@ -37,6 +37,13 @@ reference; written in tensor.py's style (explicit orders):
 * C5 (Music Transformer): REL_SKEW(x)[i, j] = x[i, T-1-i+j] for j <= i else 0 (the
   relative-attention skew of Huang et al.: column T-1-(i-j) of Q.E_r^T holds distance
   j-i); REL_UNSKEW is its adjoint: dx[i, m] = dy[i, m-(T-1)+i] for m >= T-1-i else 0.
+* C3 (ResNet-50 / SDPoint): CONV2D_DX(dy, w, x) = col2im(MATMUL(dy, w^T)) onto x's
+  geometry (conv2d's input gradient; unlike CONV2D_T it also covers strides whose
+  forward rounding left input rows without a window); MAXPOOL (-inf padding, the first
+  maximum in (ky, kx) order wins) and MAXPOOL_GRAD (dy routed to that argmax, summed over
+  windows in ascending (oy, ox) order from +0.0); AVGPOOL = (window sum in (ky, kx) order,
+  zero padding) / k^2; AVGPOOL_GRAD = (sum of covering dy in (oy, ox) order) / k^2;
+  GLOBAL_AVGPOOL = (row-major sum over H, W) / (H*W); GLOBAL_AVGPOOL_GRAD = dy / (H*W).
 """
 
 from __future__ import annotations
@@ -114,7 +121,72 @@ def bn_stats(x2: np.ndarray):
     return d, rstd
 
 
+def _windows(h, w, k, s, p, ho, wo):
+    """(oy, ox, [(ky, kx, iy, ix) in (ky, kx) order, in-bounds taps only])."""
+    for oy in range(ho):
+        for ox in range(wo):
+            taps = [(ky, kx, oy * s - p + ky, ox * s - p + kx) for ky in range(k) for kx in range(k)]
+            yield oy, ox, [t for t in taps if 0 <= t[2] < h and 0 <= t[3] < w]
+
+
+def pool_kernel(kind: OpKind, attrs: dict, x: list, out_shape) -> np.ndarray:
+    if kind is OpKind.GLOBAL_AVGPOOL:
+        n, h, w, c = x[0].shape
+        acc = np.zeros((n, c))
+        for i in range(h):
+            for j in range(w):
+                acc = acc + x[0][:, i, j, :]
+        return acc / (h * w)
+    if kind is OpKind.GLOBAL_AVGPOOL_GRAD:
+        n, h, w, c = x[0].shape
+        return np.broadcast_to((x[1] / (h * w))[:, None, None, :], (n, h, w, c)).copy()
+    k, s, p = attrs["conv"]
+    n, h, w, c = x[0].shape
+    if kind in (OpKind.MAXPOOL, OpKind.AVGPOOL):
+        _, ho, wo, _ = out_shape
+        out = np.zeros(out_shape)
+        for oy, ox, taps in _windows(h, w, k, s, p, ho, wo):
+            if kind is OpKind.MAXPOOL:
+                m = np.full((n, c), -np.inf)
+                for _, _, iy, ix in taps:
+                    m = np.where(x[0][:, iy, ix, :] > m, x[0][:, iy, ix, :], m)
+                out[:, oy, ox, :] = m
+            else:
+                acc = np.zeros((n, c))
+                for _, _, iy, ix in taps:
+                    acc = acc + x[0][:, iy, ix, :]
+                out[:, oy, ox, :] = acc / (k * k)
+        return out
+    dy = x[1]
+    _, ho, wo, _ = dy.shape
+    acc = np.zeros((n, h, w, c))
+    for oy, ox, taps in _windows(h, w, k, s, p, ho, wo):   # ascending (oy, ox)
+        if kind is OpKind.AVGPOOL_GRAD:
+            for _, _, iy, ix in taps:
+                acc[:, iy, ix, :] = acc[:, iy, ix, :] + dy[:, oy, ox, :]
+            continue
+        m = np.full((n, c), -np.inf)
+        arg = np.zeros((n, c), dtype=np.int64)
+        for t, (_, _, iy, ix) in enumerate(taps):
+            better = x[0][:, iy, ix, :] > m
+            m = np.where(better, x[0][:, iy, ix, :], m)
+            arg = np.where(better, t, arg)
+        for t, (_, _, iy, ix) in enumerate(taps):
+            acc[:, iy, ix, :] = acc[:, iy, ix, :] + np.where(arg == t, dy[:, oy, ox, :], 0.0)
+    if kind is OpKind.AVGPOOL_GRAD:
+        return acc / (k * k)
+    return acc
+
+
 def ext_kernel(kind: OpKind, attrs: dict, x: list, out_shape) -> np.ndarray:
+    if kind in (OpKind.MAXPOOL, OpKind.MAXPOOL_GRAD, OpKind.AVGPOOL, OpKind.AVGPOOL_GRAD, OpKind.GLOBAL_AVGPOOL,
+                OpKind.GLOBAL_AVGPOOL_GRAD):
+        return pool_kernel(kind, attrs, x, out_shape)
+    if kind is OpKind.CONV2D_DX:
+        k, s, p = attrs["conv"]
+        f = x[0].shape[3]
+        cols = matmul_seq(x[0].reshape(-1, f), np.ascontiguousarray(x[1].T))
+        return col2im(cols, x[0].shape, k, s, p, out_shape)
     if kind is OpKind.CONV2D:
         k, s, p = attrs["conv"]
         return matmul_seq(im2col(x[0], k, s, p), x[1]).reshape(out_shape)

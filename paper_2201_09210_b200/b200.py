@@ -25,7 +25,7 @@ from .dataset import SyntheticTensor
 from .errors import STATUS, ChannelClosed, CoexError, DeviceError, ShapeMiss
 from .planner import Planner, slot_code
 from .runner_api import PassResult
-from .tensor import CONV_KINDS, OpKind, Tensor, shape_size
+from .tensor import CONV_ATTR_KINDS, OpKind, Tensor, shape_size
 from .trace_graph import CaseDecision, LoopDecision
 
 _F64 = struct.Struct("<d")
@@ -140,7 +140,7 @@ def _attrs(kind: OpKind, attrs: dict) -> CoexAttrs:
     elif kind is OpKind.FILL:
         dims = attrs["shape"]
         at.value = float(attrs["value"])
-    elif kind in CONV_KINDS:
+    elif kind in CONV_ATTR_KINDS:
         dims = attrs["conv"]
     elif kind is OpKind.EMBEDDING_DW:
         dims = attrs["dims"]
@@ -244,7 +244,7 @@ class B200Backend:
                    12: "end", 13: "fused chain", 14: "im2col", 15: "col2im", 16: "bf16 cvt", 17: "colstats",
                    18: "bn apply", 19: "split-K reduce", 20: "causal softmax", 21: "softmax grad",
                    22: "cross-entropy", 23: "bias add", 24: "layernorm", 25: "embedding", 26: "column sum",
-                   27: "rel skew"}
+                   27: "rel skew", 28: "pooling"}
 
     def set_trace(self, capacity: int):
         """Enable device-side per-kernel stamps (0 disables)."""
@@ -364,6 +364,10 @@ class B200Backend:
         prog = self._compile(sp, tg)
         if not hasattr(self, "_programs"):
             self._programs = []
+        # a regenerated SymProgram supersedes the earlier ones: release their graphs and
+        # device memory now (a program asked for a pass again rebuilds on demand)
+        for old in self._programs:
+            old.close()
         self._programs.append(prog)
         return prog
 

@@ -367,6 +367,26 @@ __global__ void __launch_bounds__(256) k_cvt_pad_bf16(PadCvtParams p) {
   if (skip(p.ds)) return;
   const float* x = res<float>(p.x);
   const int C8 = p.C / 8, Wp = p.W + 2 * p.P, Hp = p.H + 2 * p.P;
+  // the zero border is rewritten every pass: the destination is shared scratch
+  if (p.P > 0) {
+    const int P2 = 2 * p.P;
+    const long long tb = p.N * P2 * Wp * C8;             // top / bottom border rows
+    const long long sd = p.N * p.H * P2 * C8;            // left / right border columns
+    for (long long u = (long long)blockIdx.x * blockDim.x + threadIdx.x; u < tb + sd;
+         u += (long long)gridDim.x * blockDim.x) {
+      long long pix;
+      if (u < tb) {
+        const long long q = u / C8, r = q / Wp;
+        const int i = (int)(r % P2);
+        pix = ((r / P2) * Hp + (i < p.P ? i : p.H + i)) * Wp + q % Wp;
+      } else {
+        const long long q = (u - tb) / C8, r = q / P2;
+        const int j = (int)(q % P2);
+        pix = ((r / p.H) * Hp + r % p.H + p.P) * Wp + (j < p.P ? j : p.W + j);
+      }
+      *(uint4*)(p.dst + pix * p.C + (u % C8) * 8) = make_uint4(0, 0, 0, 0);
+    }
+  }
   const long long total = p.N * p.H * p.W * C8;
   for (long long u = (long long)blockIdx.x * blockDim.x + threadIdx.x; u < total;
        u += (long long)gridDim.x * blockDim.x) {
@@ -722,6 +742,109 @@ __global__ void __launch_bounds__(256) k_bn_apply_v4(BnApplyParams p) {
       r.w = fmaf(gv.w, coef[c + 3], fmaf(xv.w, coef[C + c + 3], coef[2 * C + c + 3]));
     }
     ((float4*)o)[u] = r;
+  }
+  publish_late(p.out, o);
+}
+
+// ------------------------------------------------------------------ pooling (config C3)
+// NHWC, channels innermost (coalesced).  MODE 0 maxpool, 2 avgpool: one thread per output
+// element, taps in (ky, kx) order (max: strict '>' so the first maximum wins, -inf padding;
+// avg: zero padding, sum / k^2).  MODE 1 maxpool_grad, 3 avgpool_grad: one thread per INPUT
+// element gathering the covering windows in ascending (oy, ox) order (max: the window's
+// argmax recomputed; no atomics, deterministic).  MODE 4 global average pool (thread per
+// (n, c), row-major sequential sum / (H*W)), MODE 5 its gradient -- oracle/kernels.py
+// pool_kernel.
+struct PoolParams {
+  DevState* ds;
+  In x, dy;
+  Out out;
+  long long N, H, W, C, Ho, Wo;
+  int k, s, p;
+};
+
+template <typename T, int MODE>
+__global__ void __launch_bounds__(256) k_pool(PoolParams p) {
+  COEX_PDL_ENTER();
+  stamp(p.ds, SK_POOL);
+  if (skip(p.ds)) return;
+  const T* x = res<T>(p.x);
+  const T* dy = (MODE & 1) ? res<T>(p.dy) : nullptr;       // modes 1, 3, 5 take (x, dy)
+  T* o = pick_out<T>(p.out, x, dy);
+  publish_early(p.out, o);
+  count_op(p.ds);
+  const long long C = p.C;
+  const int k = p.k, s = p.s, pd = p.p;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  if (MODE == 4) {                       // global average pool: thread per (n, c)
+    const long long hw = p.H * p.W;
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < p.N * C; e += stride) {
+      const T* xp = x + (e / C) * hw * C + e % C;
+      T acc = (T)0;
+      for (long long i = 0; i < hw; ++i) acc = acc + xp[i * C];
+      o[e] = acc / (T)hw;
+    }
+  } else if (MODE == 5) {                // its gradient: dy[n, c] / (H*W) broadcast
+    const long long hw = p.H * p.W, total = p.N * hw * C;
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += stride)
+      o[e] = dy[(e / (hw * C)) * C + e % C] / (T)hw;
+  } else if (MODE == 0 || MODE == 2) {
+    const long long total = p.N * p.Ho * p.Wo * C;
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += stride) {
+      const long long c = e % C, pix = e / C;
+      const long long ox = pix % p.Wo, oy = (pix / p.Wo) % p.Ho, n = pix / (p.Wo * p.Ho);
+      T acc = MODE == 0 ? (T)-INFINITY : (T)0;
+      for (int ky = 0; ky < k; ++ky) {
+        const long long iy = oy * s - pd + ky;
+        if (iy < 0 || iy >= p.H) continue;
+        for (int kx = 0; kx < k; ++kx) {
+          const long long ix = ox * s - pd + kx;
+          if (ix < 0 || ix >= p.W) continue;
+          const T v = x[((n * p.H + iy) * p.W + ix) * C + c];
+          if (MODE == 0) { if (v > acc) acc = v; }
+          else acc = acc + v;
+        }
+      }
+      o[e] = MODE == 0 ? acc : acc / (T)(k * k);
+    }
+  } else {
+    const long long total = p.N * p.H * p.W * C;
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += stride) {
+      const long long c = e % C, pix = e / C;
+      const long long ix = pix % p.W, iy = (pix / p.W) % p.H, n = pix / (p.W * p.H);
+      // windows oy with oy*s - p <= iy <= oy*s - p + k - 1
+      long long oy0 = iy + pd - k + 1;
+      oy0 = oy0 <= 0 ? 0 : (oy0 + s - 1) / s;
+      long long oy1 = (iy + pd) / s;
+      if (oy1 > p.Ho - 1) oy1 = p.Ho - 1;
+      long long ox0 = ix + pd - k + 1;
+      ox0 = ox0 <= 0 ? 0 : (ox0 + s - 1) / s;
+      long long ox1 = (ix + pd) / s;
+      if (ox1 > p.Wo - 1) ox1 = p.Wo - 1;
+      T acc = (T)0;
+      for (long long oy = oy0; oy <= oy1; ++oy) {
+        for (long long ox = ox0; ox <= ox1; ++ox) {
+          const T g = dy[((n * p.Ho + oy) * p.Wo + ox) * C + c];
+          if (MODE == 3) { acc = acc + g; continue; }
+          // argmax: strict '>' from -inf; no tap above -inf -> the first in-bounds tap
+          T m = (T)-INFINITY;
+          long long ay = -1, ax = -1, fy = -1, fx = -1;
+          for (int ky = 0; ky < k; ++ky) {
+            const long long yy = oy * s - pd + ky;
+            if (yy < 0 || yy >= p.H) continue;
+            for (int kx = 0; kx < k; ++kx) {
+              const long long xx = ox * s - pd + kx;
+              if (xx < 0 || xx >= p.W) continue;
+              const T v = x[((n * p.H + yy) * p.W + xx) * C + c];
+              if (fy < 0) { fy = yy; fx = xx; }
+              if (v > m) { m = v; ay = yy; ax = xx; }
+            }
+          }
+          if (ay < 0) { ay = fy; ax = fx; }
+          if (ay == iy && ax == ix) acc = acc + g;
+        }
+      }
+      o[e] = MODE == 3 ? acc / (T)(k * k) : acc;
+    }
   }
   publish_late(p.out, o);
 }

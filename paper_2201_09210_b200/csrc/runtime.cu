@@ -234,7 +234,7 @@ int infer(int kind, const coex_attrs* at, int nin, const TRec* in, int* ndim, in
   static const int arity[] = {2, 2, 2, 2, 1, 1, 1, 1, 1, 1, 1, 0, 0, 1,
                               2, 2, 2, 3, 3, 2, 1, 1, 1, 2, 2, 2,
                               2, 2, 2, 3, 3, 2, 2, 1, 2, 2, 2, 2, 1, 2, 2, 2,
-                              1, 1};
+                              1, 1, 3, 1, 2, 1, 2, 1, 2};
   static_assert(sizeof(arity) / sizeof(arity[0]) == COEX_NUM_KINDS, "arity table");
   if (kind < 0 || kind >= COEX_NUM_KINDS) return fail(COEX_BAD_ATTRS, "unknown op kind");
   if (nin != arity[kind]) return fail(COEX_BAD_ATTRS, "wrong number of tensor inputs");
@@ -415,7 +415,50 @@ int infer_ext(int kind, const coex_attrs* at, const TRec* in, int* ndim, int64_t
       }
       return COEX_OK;
     }
+    case COEX_GLOBAL_AVGPOOL: case COEX_GLOBAL_AVGPOOL_GRAD: {
+      const TRec& x = in[0];
+      if (x.ndim != 4 || numel_of(x.ndim, x.shape) == 0) return fail(COEX_SHAPE_MISMATCH, "global_avgpool: rank-4 NHWC input required");
+      if (kind == COEX_GLOBAL_AVGPOOL) {
+        *ndim = 2; shape[0] = x.shape[0]; shape[1] = x.shape[3];
+        return COEX_OK;
+      }
+      if (in[1].ndim != 2 || in[1].shape[0] != x.shape[0] || in[1].shape[1] != x.shape[3])
+        return fail(COEX_SHAPE_MISMATCH, "global_avgpool_grad: gradient does not match [N, C]");
+      *ndim = 4; memcpy(shape, x.shape, sizeof(int64_t) * 4);
+      return COEX_OK;
+    }
     default: break;
+  }
+  if (kind == COEX_CONV2D_DX) {          // (dy, w, x): x's shape; dy must be conv2d(x, w)'s output
+    int nd; int64_t sh[COEX_MAX_RANK];
+    const TRec xw[2] = {in[2], in[1]};
+    int rc = infer_ext(COEX_CONV2D, at, xw, &nd, sh);
+    if (rc) return rc;
+    if (!(in[0].ndim == 4 && sh[0] == in[0].shape[0] && sh[1] == in[0].shape[1] && sh[2] == in[0].shape[2] &&
+          sh[3] == in[0].shape[3]))
+      return fail(COEX_SHAPE_MISMATCH, "conv2d_dx: gradient is not conv2d(x, w)'s output");
+    *ndim = 4; memcpy(shape, in[2].shape, sizeof(int64_t) * 4);
+    return COEX_OK;
+  }
+  if (kind >= COEX_MAXPOOL && kind <= COEX_AVGPOOL_GRAD) {
+    if (at == nullptr || at->n != 3 || at->dims[0] < 1 || at->dims[1] < 1 || at->dims[2] < 0)
+      return fail(COEX_BAD_ATTRS, "pool: attribute [kernel, stride, pad] expected");
+    const int64_t k = at->dims[0], st = at->dims[1], pd = at->dims[2];
+    const TRec& x = in[0];
+    if (x.ndim != 4 || numel_of(x.ndim, x.shape) == 0) return fail(COEX_SHAPE_MISMATCH, "pool: rank-4 NHWC input required");
+    if (pd >= k || x.shape[1] + 2 * pd < k || x.shape[2] + 2 * pd < k)
+      return fail(COEX_SHAPE_MISMATCH, "pool: window does not fit the input");
+    const int64_t o[4] = {x.shape[0], (x.shape[1] + 2 * pd - k) / st + 1, (x.shape[2] + 2 * pd - k) / st + 1, x.shape[3]};
+    *ndim = 4;
+    if (kind == COEX_MAXPOOL || kind == COEX_AVGPOOL) {
+      memcpy(shape, o, sizeof(o));
+      return COEX_OK;
+    }
+    const TRec& g = in[1];
+    if (g.ndim != 4 || g.shape[0] != o[0] || g.shape[1] != o[1] || g.shape[2] != o[2] || g.shape[3] != o[3])
+      return fail(COEX_SHAPE_MISMATCH, "pool grad: gradient does not match the pooled geometry");
+    memcpy(shape, x.shape, sizeof(int64_t) * 4);
+    return COEX_OK;
   }
   // convolutions
   if (at == nullptr || at->n != 3 || at->dims[0] < 1 || at->dims[1] < 1 || at->dims[2] < 0)
@@ -462,7 +505,8 @@ struct OpSpec {
   double value = 0.0;
   int trans_a = 0, trans_b = 0;
   void* scratch[2] = {nullptr, nullptr};   // bf16 K-major operand copies (tcgen05 path)
-  char* ws = nullptr;                      // extension ops: workspace base (nullptr = size query)
+  char* ws = nullptr;                      // extension ops: scratch workspace base (nullptr = size query)
+  char* pz = nullptr;                      // extension ops: the op's persistent zeroed state
   Out out{};
   Out out2{}, out3{};                      // fused batch-norm backward: dgamma, dbeta
   void* shadow = nullptr;                  // bf16 copy of the output to write (softmax-type producers)
@@ -476,7 +520,7 @@ struct OpSpec {
 constexpr int kBnBwdFused = 100;
 bool is_ext_compute(int kind) {
   return (kind >= COEX_CONV2D && kind <= COEX_SUM_ROWS) || kind == kBnBwdFused ||
-         (kind >= COEX_EMBEDDING && kind <= COEX_REL_UNSKEW && kind != COEX_GELU && kind != COEX_GELU_GRAD);
+         (kind >= COEX_EMBEDDING && kind <= COEX_GLOBAL_AVGPOOL_GRAD && kind != COEX_GELU && kind != COEX_GELU_GRAD);
 }
 int ew_code(int kind) {
   switch (kind) {
@@ -920,11 +964,15 @@ Out private_out(void* buf) {
   return o;
 }
 
-// Extension ops (conv family, batch-norm family): up to 5 launches per op, workspace carved
-// from s.ws.  With s.ws == nullptr only the workspace size is computed (*ws_bytes).
+// Extension ops (conv family, batch-norm family): up to 5 launches per op.  Two workspaces:
+// s.ws = scratch, fully rewritten by the op before it is read (im2col / bf16 operand copies,
+// split-K partials, cols) -- shared by every op of a program (ops run in stream order); s.pz =
+// the op's own persistent state (fp64 atomic accumulators, block counters: zero at rest, reset
+// by the op itself).  With s.ws == nullptr only the sizes are computed (*ws_bytes, *pz_bytes).
 template <typename T>
-int build_xop_t(coex_ctx* c, const OpSpec& s, Launch* L, int* nL, size_t* ws_bytes) {
+int build_xop_t(coex_ctx* c, const OpSpec& s, Launch* L, int* nL, size_t* ws_bytes, size_t* pz_bytes) {
   Carve cv(s.ws);
+  Carve pv(s.pz);
   const bool build = s.ws != nullptr;
   const bool bf16 = c->prec == COEX_BF16;
   const size_t es = sizeof(T);
@@ -993,12 +1041,17 @@ int build_xop_t(coex_ctx* c, const OpSpec& s, Launch* L, int* nL, size_t* ws_byt
       simt_matmul_launch<T>(c, mp, &L[(*nL)++]);
       return COEX_OK;
     }
-    case COEX_CONV2D_T: {
+    case COEX_CONV2D_T: case COEX_CONV2D_DX: {
+      // conv2d_dx(dy, w, x) is conv2d_t(dy, w) onto x's geometry (out_shape): the output may
+      // exceed the transposed-convolution size by up to s-1 rows / columns (no window
+      // reached them in the forward pass) -- those stay zero; only the exact geometry takes
+      // the sub-pixel implicit path
       const int64_t N = s.in_shape[0][0], H = s.in_shape[0][1], W = s.in_shape[0][2], C = s.in_shape[0][3];
       const int64_t Ho = s.out_shape[1], Wo = s.out_shape[2], F = s.out_shape[3];
       const int64_t M = N * H * W, Nc = k * k * F;
       int bw, bh, bnn;
       if (bf16 && (implicit_mask() & 4) && C % 64 == 0 && st >= 1 && k % st == 0 && k - 2 * pd == st &&
+          Ho == (H - 1) * st - 2 * pd + k && Wo == (W - 1) * st - 2 * pd + k &&
           H * W >= 64 && F >= 32 && conv_blocks(H, W, 128, &bw, &bh, &bnn)) {
         // sub-pixel decomposition: st*st stride-1 implicit GEMMs (one per output phase) over the
         // bf16 NHWC input, epilogue scattering straight into the output -- no cols / col2im
@@ -1075,6 +1128,38 @@ int build_xop_t(coex_ctx* c, const OpSpec& s, Launch* L, int* nL, size_t* ws_byt
       L[(*nL)++].set((void*)k_col2im<T, T>, grid_for(N * Ho * Wo * F), dim3(256), cp);
       return COEX_OK;
     }
+    case COEX_MAXPOOL: case COEX_MAXPOOL_GRAD: case COEX_AVGPOOL: case COEX_AVGPOOL_GRAD: case COEX_GLOBAL_AVGPOOL:
+    case COEX_GLOBAL_AVGPOOL_GRAD: {
+      if (!build) break;
+      PoolParams pp{};
+      pp.ds = s.ds; pp.x = s.in[0]; pp.dy = s.nin > 1 ? s.in[1] : In{nullptr, nullptr, nullptr}; pp.out = s.out;
+      pp.N = s.in_shape[0][0]; pp.H = s.in_shape[0][1]; pp.W = s.in_shape[0][2]; pp.C = s.in_shape[0][3];
+      pp.k = (int)k; pp.s = (int)st; pp.p = (int)pd;
+      const bool f64 = is_f64(c);
+      void* fn = nullptr;
+      int64_t work = pp.N * pp.H * pp.W * pp.C;
+      switch (s.kind) {
+        case COEX_MAXPOOL: case COEX_AVGPOOL:
+          pp.Ho = s.out_shape[1]; pp.Wo = s.out_shape[2];
+          work = pp.N * pp.Ho * pp.Wo * pp.C;
+          fn = s.kind == COEX_MAXPOOL ? (f64 ? (void*)k_pool<double, 0> : (void*)k_pool<float, 0>)
+                                      : (f64 ? (void*)k_pool<double, 2> : (void*)k_pool<float, 2>);
+          break;
+        case COEX_MAXPOOL_GRAD: case COEX_AVGPOOL_GRAD:
+          pp.Ho = s.in_shape[1][1]; pp.Wo = s.in_shape[1][2];
+          fn = s.kind == COEX_MAXPOOL_GRAD ? (f64 ? (void*)k_pool<double, 1> : (void*)k_pool<float, 1>)
+                                           : (f64 ? (void*)k_pool<double, 3> : (void*)k_pool<float, 3>);
+          break;
+        case COEX_GLOBAL_AVGPOOL:
+          work = pp.N * pp.C;
+          fn = f64 ? (void*)k_pool<double, 4> : (void*)k_pool<float, 4>;
+          break;
+        default:
+          fn = f64 ? (void*)k_pool<double, 5> : (void*)k_pool<float, 5>;
+      }
+      L[(*nL)++].set(fn, grid_for(work), dim3(256), pp);
+      return COEX_OK;
+    }
     case COEX_CONV2D_DW: {
       const int64_t N = s.in_shape[0][0], H = s.in_shape[0][1], W = s.in_shape[0][2], C = s.in_shape[0][3];
       const int64_t Ho = s.in_shape[1][1], Wo = s.in_shape[1][2], F = s.in_shape[1][3];
@@ -1149,7 +1234,7 @@ int build_xop_t(coex_ctx* c, const OpSpec& s, Launch* L, int* nL, size_t* ws_byt
         while (gy < 64 && gx * gy < kNumSMs * 4 && Rw / (gy * 2) >= 64) gy *= 2;
         RowParams rp{};
         rp.ds = s.ds; rp.x = s.in[0]; rp.rows = Rw; rp.d = C; rp.out = s.out;
-        if (gy > 1) rp.acc = (double*)cv.take((size_t)C * 8);
+        if (gy > 1) rp.acc = (double*)pv.take((size_t)C * 8);
         if (!build) break;
         L[(*nL)++].set(is_f64(c) ? (void*)k_colsum_wide<double> : (void*)k_colsum_wide<float>,
                        dim3((unsigned)gx, (unsigned)gy), dim3(256), rp);
@@ -1176,9 +1261,9 @@ int build_xop_t(coex_ctx* c, const OpSpec& s, Launch* L, int* nL, size_t* ws_byt
       ColStatsParams cp{};
       cp.ds = s.ds; cp.x = s.in[0]; cp.R = R; cp.C = C;
       cp.atomic = atomic ? 1 : 0;
-      cp.part = (double*)cv.take((size_t)(atomic ? kColReplicas : G) * C * 4 * 8);
-      cp.stats = (double*)cv.take((size_t)C * 4 * 8);
-      cp.counter = (unsigned int*)cv.take(16);
+      cp.part = (double*)pv.take((size_t)(atomic ? kColReplicas : G) * C * 4 * 8);
+      cp.stats = (double*)pv.take((size_t)C * 4 * 8);
+      cp.counter = (unsigned int*)pv.take(16);
       cp.a = s.in[0];
       cp.b = s.nin > 1 ? s.in[1] : In{nullptr, nullptr, nullptr};
       if (!build) break;
@@ -1292,8 +1377,8 @@ int build_xop_t(coex_ctx* c, const OpSpec& s, Launch* L, int* nL, size_t* ws_byt
           return COEX_OK;
         }
         case COEX_LN_DGAMMA: {
-          rp.acc = (double*)cv.take((size_t)kColReplicas * d * 8);
-          rp.counter = (unsigned int*)cv.take(16);
+          rp.acc = (double*)pv.take((size_t)kColReplicas * d * 8);
+          rp.counter = (unsigned int*)pv.take(16);
           if (!build) break;
           rp.d = d; rp.rows = xn / d;
           L[(*nL)++].set(is_f64(c) ? (void*)k_ln_dgamma<double> : (void*)k_ln_dgamma<float>, warp_rows(rp.rows / 4),
@@ -1326,8 +1411,8 @@ int build_xop_t(coex_ctx* c, const OpSpec& s, Launch* L, int* nL, size_t* ws_byt
         default: {   // cross-entropy (loss / gradient)
           const int64_t R = s.in_shape[0][0];
           if (s.kind == COEX_CROSS_ENTROPY) {
-            rp.acc = (double*)cv.take((size_t)R * 8);
-            rp.counter = (unsigned int*)cv.take(16);
+            rp.acc = (double*)pv.take((size_t)R * 8);
+            rp.counter = (unsigned int*)pv.take(16);
           }
           if (!build) break;
           rp.d = s.in_shape[0][1]; rp.rows = R; rp.vocab = rp.d;
@@ -1343,11 +1428,13 @@ int build_xop_t(coex_ctx* c, const OpSpec& s, Launch* L, int* nL, size_t* ws_byt
       return fail(COEX_BAD_ATTRS, "op kind has no extension kernel");
   }
   *ws_bytes = cv.off;
+  if (pz_bytes) *pz_bytes = pv.off;
   return COEX_OK;
 }
 
-int build_xop(coex_ctx* c, const OpSpec& s, Launch* L, int* nL, size_t* ws_bytes) {
-  return is_f64(c) ? build_xop_t<double>(c, s, L, nL, ws_bytes) : build_xop_t<float>(c, s, L, nL, ws_bytes);
+int build_xop(coex_ctx* c, const OpSpec& s, Launch* L, int* nL, size_t* ws_bytes, size_t* pz_bytes = nullptr) {
+  return is_f64(c) ? build_xop_t<double>(c, s, L, nL, ws_bytes, pz_bytes)
+                   : build_xop_t<float>(c, s, L, nL, ws_bytes, pz_bytes);
 }
 constexpr int kMaxLaunches = 6;
 
@@ -1733,12 +1820,15 @@ int eager_scratch(coex_ctx* c, OpSpec* s) {
   if (is_ext_compute(s->kind)) {
     Launch tmp[kMaxLaunches];
     int n = 0;
-    size_t wb = 0;
-    int rc = build_xop(c, *s, tmp, &n, &wb);
+    size_t wb = 0, pzb = 0;
+    int rc = build_xop(c, *s, tmp, &n, &wb, &pzb);
     if (rc) return rc;
     if (wb < 256) wb = 256;          // a non-null workspace marks the build pass
     CK(cudaMallocAsync((void**)&s->ws, wb, c->stream));
-    CK(cudaMemsetAsync(s->ws, 0, wb, c->stream));
+    if (pzb) {
+      CK(cudaMallocAsync((void**)&s->pz, pzb, c->stream));
+      CK(cudaMemsetAsync(s->pz, 0, pzb, c->stream));
+    }
   }
   return COEX_OK;
 }
@@ -1747,8 +1837,9 @@ void eager_free(coex_ctx* c, OpSpec* s) {
   if (s->scratch[0]) cudaFreeAsync(s->scratch[0], c->stream);
   if (s->scratch[1]) cudaFreeAsync(s->scratch[1], c->stream);
   if (s->ws) cudaFreeAsync(s->ws, c->stream);
+  if (s->pz) cudaFreeAsync(s->pz, c->stream);
   s->scratch[0] = s->scratch[1] = nullptr;
-  s->ws = nullptr;
+  s->ws = s->pz = nullptr;
 }
 }  // namespace
 
@@ -1980,6 +2071,31 @@ struct Builder {
   std::vector<char*> bufs;
   int64_t n_late = 0;
   std::string err;
+  char* scratch = nullptr;         // scratch shared by the program's ops (they run in stream order)
+  size_t scratch_cap = 0;
+
+  // A scratch region of >= bytes; grows geometrically (earlier ops keep the smaller region
+  // they were built with, so the total stays below twice the largest request).
+  char* shared_scratch(size_t bytes) {
+    if (bytes < 256) bytes = 256;
+    if (bytes > scratch_cap) {
+      size_t cap = scratch_cap * 2 > bytes ? scratch_cap * 2 : bytes;
+      void* q = nullptr;
+      if (cudaMalloc(&q, cap) != cudaSuccess) {
+        cudaGetLastError();
+        cap = bytes;
+        if (cudaMalloc(&q, cap) != cudaSuccess) {
+          cudaGetLastError();
+          throw std::runtime_error("cudaMalloc(shared scratch): out of memory");
+        }
+      }
+      p->workspaces.push_back(q);
+      p->ws_bytes += cap;
+      scratch = (char*)q;
+      scratch_cap = cap;
+    }
+    return scratch;
+  }
 
   int64_t next() {
     if (pos >= n) throw std::runtime_error("plan truncated");
@@ -2110,13 +2226,7 @@ struct Builder {
           const int64_t K = s.trans_a ? s.in_shape[0][0] : s.in_shape[0][1];
           const int64_t N = s.trans_b ? s.in_shape[1][0] : s.in_shape[1][1];
           const size_t wb = matmul_split_ws(M, N, K);
-          if (wb) {
-            void* ws = nullptr;
-            CK(cudaMalloc(&ws, wb));
-            p->workspaces.push_back(ws);
-            p->ws_bytes += wb;
-            s.ws = (char*)ws;
-          }
+          if (wb) s.ws = shared_scratch(wb);
         }
         Launch L[kMaxLaunches];
         int nL = 0;
@@ -2160,17 +2270,19 @@ struct Builder {
         for (int i = 0; i < kMaxIn; ++i) s.in_conv[i] = (int)next();
         Launch L[kMaxLaunches];
         int nL = 0;
-        size_t wb = 0;
-        int rc = build_xop(c, s, L, &nL, &wb);
+        size_t wb = 0, pzb = 0;
+        int rc = build_xop(c, s, L, &nL, &wb, &pzb);
         if (rc) return rc;
-        if (wb < 256) wb = 256;      // a non-null workspace marks the build pass
-        void* ws = nullptr;
-        CK(cudaMalloc(&ws, wb));
-        CK(cudaMemset(ws, 0, wb));
-        p->workspaces.push_back(ws);
-        p->ws_bytes += wb;
-        s.ws = (char*)ws;
-        rc = build_xop(c, s, L, &nL, &wb);
+        s.ws = shared_scratch(wb);   // non-null: marks the build pass
+        if (pzb) {
+          void* pz = nullptr;
+          CK(cudaMalloc(&pz, pzb));
+          CK(cudaMemset(pz, 0, pzb));
+          p->workspaces.push_back(pz);
+          p->ws_bytes += pzb;
+          s.pz = (char*)pz;
+        }
+        rc = build_xop(c, s, L, &nL, &wb, &pzb);
         if (rc) return rc;
         p->n_compute += nL;
         for (int i = 0; i < nL; ++i) {

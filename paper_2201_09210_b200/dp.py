@@ -62,7 +62,10 @@ ROW_BINARY = (OpKind.RELU_GRAD, OpKind.LEAKY_RELU_GRAD, OpKind.BCE_TERM, OpKind.
 # C4 ops whose rows (or batch entries) are independent: sharded in, sharded out
 ROW_WISE = (OpKind.LAYERNORM, OpKind.LAYERNORM_DX, OpKind.BIAS_ADD, OpKind.CAUSAL_SOFTMAX, OpKind.SOFTMAX_GRAD,
             OpKind.BMM, OpKind.BMM_NT, OpKind.BMM_TN, OpKind.EMBEDDING, OpKind.CROSS_ENTROPY_GRAD,
-            OpKind.REL_SKEW, OpKind.REL_UNSKEW)
+            OpKind.REL_SKEW, OpKind.REL_UNSKEW,
+            # C3: per-image pooling and conv2d's input gradient (weight replicated)
+            OpKind.CONV2D_DX, OpKind.MAXPOOL, OpKind.MAXPOOL_GRAD, OpKind.AVGPOOL, OpKind.AVGPOOL_GRAD,
+            OpKind.GLOBAL_AVGPOOL, OpKind.GLOBAL_AVGPOOL_GRAD)
 
 
 @dataclass
@@ -277,7 +280,8 @@ class _Prop:
             if any(st != S0 for st in sh):
                 raise Unshardable(f"node {x.node_id}: {k.value} of {ins}")
             if k in (OpKind.BMM, OpKind.BMM_NT, OpKind.BMM_TN, OpKind.SOFTMAX_GRAD, OpKind.CROSS_ENTROPY_GRAD,
-                     OpKind.LAYERNORM_DX) and len(sh) != 2:
+                     OpKind.LAYERNORM_DX, OpKind.CONV2D_DX, OpKind.MAXPOOL_GRAD, OpKind.AVGPOOL_GRAD,
+                     OpKind.GLOBAL_AVGPOOL_GRAD) and len(sh) != 2:
                 raise Unshardable(f"node {x.node_id}: {k.value} mixes sharded and replicated rows")
             if k is OpKind.EMBEDDING and ins[0] != R:
                 raise Unshardable(f"node {x.node_id}: sharded embedding table")

@@ -35,7 +35,8 @@ from .trace_graph import (Diverged, External, Handle, LoopEnter, LoopExit,
                           LoopIterStart, OpEvent, StepEnd)
 
 OP_BY_NAME = {k.value: k for k in OpKind if k not in (OpKind.READ_VAR, OpKind.ASSIGN_VAR)}
-CONV_NAMES = frozenset(("conv2d", "conv2d_t", "conv2d_dw", "embedding_dw"))
+CONV_NAMES = frozenset(("conv2d", "conv2d_t", "conv2d_dw", "embedding_dw", "conv2d_dx", "maxpool", "maxpool_grad",
+                        "avgpool", "avgpool_grad"))
 SCALE_NAMES = frozenset(("causal_softmax", "softmax_grad"))    # trailing host scale -> "value" attr
 
 
@@ -695,17 +696,16 @@ class Interp:
                 return ctx.op(kind, {"perm": tuple(perm)}, [x], loc, [shp])
             return transpose
         if name in CONV_NAMES:
-            # extension ops with two tensor operands + a shape literal ([k, s, p] / [vocab])
-            fy = self._c_expr(e.args[1], loc)
-            geo = self._c_shape(e.args[2], loc)
+            # extension ops with tensor operands + a trailing shape literal ([k, s, p] / [vocab])
+            ftens = [fx] + [self._c_expr(a, loc) for a in e.args[1:-1]]
+            geo = self._c_shape(e.args[-1], loc)
             akey = "dims" if name == "embedding_dw" else "conv"
 
             def conv(ctx, env):
-                x = fx(ctx, env)
-                y = fy(ctx, env)
-                if isinstance(x, str) or isinstance(y, str):
+                xs = [f(ctx, env) for f in ftens]
+                if any(isinstance(v, str) for v in xs):
                     raise it._err(f"{name}: string operand", e)
-                return ctx.op(kind, {akey: tuple(geo(ctx, env))}, [x, y], loc, [shape_of(x), shape_of(y)])
+                return ctx.op(kind, {akey: tuple(geo(ctx, env))}, xs, loc, [shape_of(v) for v in xs])
             return conv
         if name in SCALE_NAMES:
             ftens = [fx] + [self._c_expr(a, loc) for a in e.args[1:-1]]

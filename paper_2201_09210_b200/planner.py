@@ -28,7 +28,7 @@ from dataclasses import dataclass, field
 
 from .errors import ShapeMiss
 from .graph_gen import ExecOp, InputFeed, OutputFetch, SwitchCase, SymProgram, UnrolledLoop, While
-from .tensor import BMM_KINDS, CONV_KINDS, OpKind, flops_of, infer_shape, shape_size
+from .tensor import BMM_KINDS, CONV_ATTR_KINDS, CONV_KINDS, OpKind, flops_of, infer_shape, shape_size
 
 MAGIC = 0xC0E8B200
 VERSION = 2
@@ -41,7 +41,9 @@ XOP = {OpKind.CONV2D, OpKind.CONV2D_T, OpKind.CONV2D_DW, OpKind.BATCHNORM, OpKin
        OpKind.BN_DGAMMA, OpKind.SUM_ROWS,
        OpKind.EMBEDDING, OpKind.EMBEDDING_DW, OpKind.LAYERNORM, OpKind.LAYERNORM_DX, OpKind.LN_DGAMMA,
        OpKind.BIAS_ADD, OpKind.BMM, OpKind.BMM_NT, OpKind.BMM_TN, OpKind.CAUSAL_SOFTMAX, OpKind.SOFTMAX_GRAD,
-       OpKind.CROSS_ENTROPY, OpKind.CROSS_ENTROPY_GRAD, OpKind.REL_SKEW, OpKind.REL_UNSKEW}
+       OpKind.CROSS_ENTROPY, OpKind.CROSS_ENTROPY_GRAD, OpKind.REL_SKEW, OpKind.REL_UNSKEW,
+       OpKind.CONV2D_DX, OpKind.MAXPOOL, OpKind.MAXPOOL_GRAD, OpKind.AVGPOOL, OpKind.AVGPOOL_GRAD,
+       OpKind.GLOBAL_AVGPOOL, OpKind.GLOBAL_AVGPOOL_GRAD}
 EW_CODE = {OpKind.ADD: 0, OpKind.SUB: 1, OpKind.MUL: 2, OpKind.NEG: 3, OpKind.RELU: 4, OpKind.SIGMOID: 5,
            OpKind.TANH: 7, OpKind.LEAKY_RELU: 8, OpKind.RELU_GRAD: 9, OpKind.LEAKY_RELU_GRAD: 10,
            OpKind.BCE_TERM: 11, OpKind.TO_INDEX: 12, OpKind.GELU_GRAD: 13, OpKind.GELU: 14}
@@ -558,7 +560,7 @@ class Planner:
         in_shapes = [self._in_shape(b, shapes) for b in x.inputs]
         late = _conflicts(cells, pubs[nid])
         n_compute[0] += 1
-        attr = list(x.attrs["conv"]) if x.kind in CONV_KINDS else list(x.attrs.get("dims", ()))
+        attr = list(x.attrs["conv"]) if x.kind in CONV_ATTR_KINDS else list(x.attrs.get("dims", ()))
         if x.kind in BMM_KINDS and self.bf16:
             tri = self._tri_flag(x)
             attr = [tri] if tri else []

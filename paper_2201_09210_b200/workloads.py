@@ -341,6 +341,155 @@ def _decoder_program(steps, batch, seq, d, heads, layers, vocab, lr, music) -> s
     return "\n".join(v) + f"\nsteps {steps} {{\n  " + "\n  ".join(b) + "\n}\n"
 
 
+def resnet_program(steps: int = 20, batch: int = 64, img: int = 224, width: int = 64,
+                   blocks: tuple = (3, 4, 6, 3), classes: int = 1000, lr: float = 0.01) -> str:
+    """BASELINE.json configs[2]: ResNet-50 with SDPoint on synthetic NHWC
+    images.
+
+    Bottleneck ResNet (v1.5: the stride sits on the 3x3 conv; projection shortcuts with
+    batch-norm on the first block of each stage): stem 7x7/2 conv + BN + ReLU + 3x3/2 max
+    pool, stages of ``blocks`` bottlenecks (widths width*2^i, expansion 4), global average
+    pool, fully connected classifier, cross-entropy on host-drawn labels.  SDPoint
+    (stochastic downsampling point): every step ``native choice(4, 5)`` picks the
+    downsampling point -- none, or a 2x2 average pool after stage 1, 2 or 3 -- and a 4-way
+    SwitchCase runs that path's forward, backward and update: every activation after the
+    point has a path-dependent spatial size, static inside its case (one CUDA-graph body
+    per shape class).  Backward written out with conv2d_dw / conv2d_dx, batch-norm backward,
+    ReLU masks from the post-activation values; SGD on shape-invariant parameters.
+    Extension ops.
+    """
+    decls: list = []
+
+    def network(sdpoint: int) -> list:
+        v, fwd, units = [], [], []
+        cnt = [0]
+
+        def conv_bn(x, cin, cout, k, s, p, relu, need_dx=True):
+            i = cnt[0]
+            cnt[0] += 1
+            fan = k * k * cin
+            v.extend([f"var w{i} = mul(input(\"w{i}_init\", [{fan}, {cout}]), {math.sqrt(6.0 / fan):.6f})",
+                      f"var g{i} = fill([{cout}], 1.0)", f"var b{i} = fill([{cout}], 0.0)"])
+            fwd.extend([f"let c{i} = conv2d({x}, w{i}, [{k}, {s}, {p}])",
+                        f"let n{i} = batchnorm(c{i}, g{i}, b{i})"])
+            out = f"n{i}"
+            if relu:
+                fwd.append(f"let a{i} = relu(n{i})")
+                out = f"a{i}"
+            units.append(dict(i=i, x=x, k=k, s=s, p=p, relu=relu, need_dx=need_dx))
+            return i, out
+
+        def back(u, d, bwd):
+            i = u["i"]
+            if u["relu"]:
+                bwd.append(f"let dn{i} = relu_grad(a{i}, {d})")
+                d = f"dn{i}"
+            geo = f"[{u['k']}, {u['s']}, {u['p']}]"
+            bwd.extend([f"let dc{i} = batchnorm_dx(c{i}, g{i}, {d})", f"let dg{i} = bn_dgamma(c{i}, {d})",
+                        f"let db{i} = sum_rows({d})", f"let dw{i} = conv2d_dw({u['x']}, dc{i}, {geo})"])
+            if not u["need_dx"]:
+                return None
+            bwd.append(f"let dx{i} = conv2d_dx(dc{i}, w{i}, {u['x']}, {geo})")
+            return f"dx{i}"
+
+        stem, a_stem = conv_bn("x", 3, width, 7, 2, 3, True, need_dx=False)
+        fwd.append(f"let mp = maxpool({a_stem}, [3, 2, 1])")
+        cur, cin = "mp", width
+        plan = []
+        for si, nb in enumerate(blocks):
+            mid = width << si
+            cout = mid * 4
+            stage = []
+            for bi in range(nb):
+                stride = 2 if (bi == 0 and si > 0) else 1
+                u1 = conv_bn(cur, cin, mid, 1, 1, 0, True)
+                u2 = conv_bn(u1[1], mid, mid, 3, stride, 1, True)
+                u3 = conv_bn(u2[1], mid, cout, 1, 1, 0, False)
+                us = conv_bn(cur, cin, cout, 1, stride, 0, False) if bi == 0 else None
+                y = f"y{si}_{bi}"
+                fwd.append(f"let {y} = relu(add({u3[1]}, {us[1] if us else cur}))")
+                stage.append((u1[0], u2[0], u3[0], us[0] if us else None, y))
+                cur, cin = y, cout
+            pre = None
+            if si + 1 == sdpoint:           # the SDPoint: 2x2 average pool after this stage
+                pre, cur = cur, f"sp{si}"
+                fwd.append(f"let {cur} = avgpool({pre}, [2, 2, 0])")
+            plan.append((stage, pre))
+        v.extend([f"var wfc = mul(input(\"wfc_init\", [{cin}, {classes}]), {math.sqrt(3.0 / cin):.6f})",
+                  f"var bfc = fill([{classes}], 0.0)"])
+        fwd.extend([f"let gp = global_avgpool({cur})",
+                    "let logits = bias_add(matmul(gp, wfc), bfc)",
+                    "let loss = cross_entropy(logits, lab)"])
+        by_i = {u["i"]: u for u in units}
+        bwd = ["let dlog = cross_entropy_grad(logits, lab)",
+               "let dwfc = matmul(transpose(gp), dlog)",
+               "let dbfc = sum_rows(dlog)",
+               f"let dtop = global_avgpool_grad({cur}, matmul(dlog, transpose(wfc)))"]
+        d = "dtop"
+        for si in range(len(plan) - 1, -1, -1):
+            stage, pre = plan[si]
+            if pre is not None:
+                bwd.append(f"let dsp = avgpool_grad({pre}, {d}, [2, 2, 0])")
+                d = "dsp"
+            for (i1, i2, i3, isc, y) in reversed(stage):
+                bwd.append(f"let dz_{y} = relu_grad({y}, {d})")
+                dz = f"dz_{y}"
+                gx = back(by_i[i1], back(by_i[i2], back(by_i[i3], dz, bwd), bwd), bwd)
+                gs = back(by_i[isc], dz, bwd) if isc is not None else dz
+                bwd.append(f"let dxb_{y} = add({gx}, {gs})")
+                d = f"dxb_{y}"
+        bwd.append(f"let dstem = maxpool_grad({a_stem}, {d}, [3, 2, 1])")
+        back(by_i[stem], "dstem", bwd)
+        upd = ["let l = item(loss)", f"let lrs = fill([], {lr})",
+               "wfc = sub(wfc, mul(dwfc, lrs))", "bfc = sub(bfc, mul(dbfc, lrs))"]
+        for u in units:
+            i = u["i"]
+            upd += [f"w{i} = sub(w{i}, mul(dw{i}, lrs))", f"g{i} = sub(g{i}, mul(dg{i}, lrs))",
+                    f"b{i} = sub(b{i}, mul(db{i}, lrs))"]
+        upd.append("print(l)")
+        if not decls:
+            decls.extend(v)
+        return fwd + bwd + upd
+
+    def arm(j, ind):
+        pad = "  " * ind
+        return ("{\n" + "\n".join(pad + "  " + ln for ln in network(j)) + "\n" + pad + "}")
+
+    head = [f"let x = input(\"img\", [{batch}, {img}, {img}, 3])",
+            f"let lab = to_index(input(\"labels\", [{batch}]), {float(classes)})",
+            "let sd = native choice(4, 5)"]
+    sw = (f"if sd == 0 {arm(0, 1)} else {{\n    if sd == 1 {arm(1, 2)} else {{\n      "
+          f"if sd == 2 {arm(2, 3)} else {arm(3, 3)}\n    }}\n  }}")
+    return "\n".join(decls) + f"\nsteps {steps} {{\n  " + "\n  ".join(head) + "\n  " + sw + "\n}\n"
+
+
+C3 = dict(batch=64, img=224, width=64, blocks=(3, 4, 6, 3), classes=1000)
+C3_SMALL = dict(batch=8, img=64, width=4, blocks=(1, 1, 1, 1), classes=10)
+
+
+def resnet_flops(batch=64, img=224, width=64, blocks=(3, 4, 6, 3), classes=1000, **_) -> int:
+    """Conv + FC FLOPs of one C3 step without SDPoint downsampling (forward + weight and input
+    gradients, 2*M*N*K per product; the stem's input gradient is not computed)."""
+    def conv(h, cin, cout, k, s, p):
+        ho = (h + 2 * p - k) // s + 1
+        return ho, 2 * batch * ho * ho * k * k * cin * cout
+    h, f = conv(img, 3, width, 7, 2, 3)
+    total = 2 * f                                         # forward + weight gradient
+    h = (h + 2 - 3) // 2 + 1
+    cin = width
+    for si, nb in enumerate(blocks):
+        mid = width << si
+        for bi in range(nb):
+            s = 2 if (bi == 0 and si > 0) else 1
+            _, f1 = conv(h, cin, mid, 1, 1, 0)
+            h2, f2 = conv(h, mid, mid, 3, s, 1)
+            _, f3 = conv(h2, mid, mid * 4, 1, 1, 0)
+            fs = conv(h, cin, mid * 4, 1, s, 0)[1] if bi == 0 else 0
+            total += 3 * (f1 + f2 + f3 + fs)
+            h, cin = h2, mid * 4
+    return total + 3 * 2 * batch * cin * classes
+
+
 C4 = dict(batch=8, seq=1024, d=768, heads=12, layers=12, vocab=50257)
 C4_SMALL = dict(batch=2, seq=32, d=64, heads=4, layers=2, vocab=97)
 C5 = dict(batch=8, seq=1024, d=512, heads=8, layers=6, vocab=388)

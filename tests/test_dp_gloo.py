@@ -17,12 +17,14 @@ from paper_2201_09210_b200 import coexec, lang
 from paper_2201_09210_b200.dataset import SyntheticDataset
 from paper_2201_09210_b200.dp import DPGroup
 from paper_2201_09210_b200.tensor import Tensor
-from paper_2201_09210_b200.workloads import c1_program, dcgan_program, gpt2_program, music_transformer_program
+from paper_2201_09210_b200.workloads import (c1_program, dcgan_program, gpt2_program, music_transformer_program,
+                                             resnet_program)
 
 SMALL_C1 = c1_program(steps=12, batch=8, hidden=16, din=12, dout=3)
 BATCH = 8
 SMALL_C2 = dcgan_program(steps=6, batch=8, nz=6, ngf=4, ndf=4, img=16)
 SMALL_C4 = gpt2_program(steps=4, batch=BATCH, seq=8, d=16, heads=2, layers=2, vocab=23)
+SMALL_C3 = resnet_program(steps=14, batch=BATCH, img=32, width=2, blocks=(1, 1, 1, 1), classes=5, lr=1e-3)
 SMALL_C5 = music_transformer_program(steps=8, batch=BATCH, seq=8, d=16, heads=2, layers=2, vocab=23)
 
 
@@ -116,13 +118,17 @@ steps 6 {
     assert out[0][0] == ref.lines == out[1][0]
 
 
-def test_dp2_dcgan_matches_global_batch():
-    """C2 (DCGAN) data parallel at world size 2: activations row-sharded through the
-    convolutions, per-replica batch-norm statistics, weight / gamma / beta gradients
-    all-reduced (P+), the loss averaged (P~).  With duplicated batch halves the result
-    equals the single-process global-batch run."""
-    ref, ref_st = coexec.run(lang.parse(SMALL_C2), DupHalves(0), "coexec", backend=CpuBackend())
-    out = run_dp(SMALL_C2, dup=True)
+@pytest.mark.parametrize("src,tol", [(SMALL_C2, 1e-9), (SMALL_C3, 1e-8)], ids=["dcgan", "resnet_sdpoint"])
+def test_dp2_dcgan_matches_global_batch(src, tol):
+    """C2 (DCGAN) / C3 (ResNet-50 + SDPoint) data parallel at world size 2: activations
+    row-sharded through the convolutions, pooling and (C3) the path-dependent SDPoint tail,
+    per-replica batch-norm statistics, weight / gamma / beta gradients all-reduced (P+), the
+    loss averaged (P~).  With duplicated batch halves the result equals the single-process
+    global-batch run (C3 within 1e-8: the 4- vs 8-row batch-norm summation orders differ at
+    f64 rounding level, and the tiny network's training dynamics amplify that ~10x per step
+    -- measured 1e-16 at step 4 growing to 2e-10 at step 14)."""
+    ref, ref_st = coexec.run(lang.parse(src), DupHalves(0), "coexec", backend=CpuBackend())
+    out = run_dp(src, dup=True)
     r0, r1 = out[0], out[1]
     assert r0[0] == r1[0] and r0[3] == r1[3] and r0[2] == r1[2]
     assert r0[2] == ref_st.counters()
@@ -130,9 +136,9 @@ def test_dp2_dcgan_matches_global_batch():
     assert plans and not any(p[0] for p in plans), plans   # every specialisation sharded
     assert max(len(p[2]) for p in plans) >= 8               # weight, BN-parameter and loss reductions
     for a, b in zip(ref.lines, r0[0]):
-        assert abs(float(a) - float(b)) <= 1e-9 * max(1.0, abs(float(a))), (a, b)
+        assert abs(float(a) - float(b)) <= tol * max(1.0, abs(float(a))), (a, b)
     for k, t in ref.vars.items():
-        np.testing.assert_allclose(r0[1][k], t.data, rtol=1e-8, atol=1e-11)
+        np.testing.assert_allclose(r0[1][k], t.data, rtol=tol * 10, atol=tol * 1e-2)
         np.testing.assert_array_equal(r0[1][k], r1[1][k])
 
 

@@ -10,7 +10,7 @@ import torch
 from oracle.cpu_backend import CpuBackend
 from oracle.kernels import execute_kernel
 from paper_2201_09210_b200.tensor import OpKind, Tensor
-from paper_2201_09210_b200.workloads import C5_SMALL, music_transformer_program
+from paper_2201_09210_b200.workloads import C3_SMALL, C5_SMALL, music_transformer_program, resnet_program
 from test_gpu_coexec import run
 
 RNG = np.random.default_rng(5)
@@ -83,3 +83,66 @@ def test_music_transformer_coexec_equals_imperative():
     assert st.counters()[1] > 0                      # passes run as graphs
     kinds = {type(dc).__name__ for step in st.decision_log for dc in step}
     assert kinds == {"CaseDecision", "LoopDecision"}
+
+
+def _nchw(x):
+    return x.permute(0, 3, 1, 2)
+
+
+def _nhwc(x):
+    return x.permute(0, 2, 3, 1)
+
+
+@pytest.mark.parametrize("k,s,p", [(3, 2, 1), (2, 2, 0), (3, 1, 1), (1, 2, 0), (7, 2, 3)])
+def test_pooling_and_conv_dx_match_torch(k, s, p):
+    """C3 ops against torch autograd: maxpool / avgpool (count_include_pad) and their
+    gradients, conv2d_dx as conv2d's input gradient (including strides whose forward
+    rounding leaves input rows without a window), global average pooling."""
+    h = 8 if k < 7 else 9
+    x = RNG.standard_normal((2, h, h, 3))
+    tx = torch.tensor(x, requires_grad=True)
+    tm = _nhwc(torch.nn.functional.max_pool2d(_nchw(tx), k, s, p)) if p <= k // 2 else None
+    if tm is not None:
+        m = k_(OpKind.MAXPOOL, x, conv=(k, s, p))
+        dy = RNG.standard_normal(m.shape)
+        (tm * torch.from_numpy(dy)).sum().backward()
+        np.testing.assert_array_equal(m, tm.detach().numpy())
+        np.testing.assert_array_equal(k_(OpKind.MAXPOOL_GRAD, x, dy, conv=(k, s, p)), tx.grad.numpy())
+        tx = torch.tensor(x, requires_grad=True)
+        ta = _nhwc(torch.nn.functional.avg_pool2d(_nchw(tx), k, s, p, count_include_pad=True))
+        (ta * torch.from_numpy(dy)).sum().backward()
+        np.testing.assert_allclose(k_(OpKind.AVGPOOL, x, conv=(k, s, p)), ta.detach().numpy(), rtol=1e-14)
+        np.testing.assert_allclose(k_(OpKind.AVGPOOL_GRAD, x, dy, conv=(k, s, p)), tx.grad.numpy(), rtol=1e-13, atol=1e-16)
+    w = RNG.standard_normal((k * k * 3, 4))
+    tx = torch.tensor(x, requires_grad=True)
+    ty = _nhwc(torch.nn.functional.conv2d(_nchw(tx), torch.tensor(w).reshape(k, k, 3, 4).permute(3, 2, 0, 1),
+                                          stride=s, padding=p))
+    y = k_(OpKind.CONV2D, x, w, conv=(k, s, p))
+    dy = RNG.standard_normal(y.shape)
+    (ty * torch.from_numpy(dy)).sum().backward()
+    np.testing.assert_allclose(y, ty.detach().numpy(), rtol=1e-12, atol=1e-12)
+    np.testing.assert_allclose(k_(OpKind.CONV2D_DX, dy, w, x, conv=(k, s, p)), tx.grad.numpy(),
+                               rtol=1e-12, atol=1e-12)
+    tx = torch.tensor(x, requires_grad=True)
+    g = RNG.standard_normal((2, 3))
+    (tx.mean((1, 2)) * torch.from_numpy(g)).sum().backward()
+    np.testing.assert_allclose(k_(OpKind.GLOBAL_AVGPOOL, x), x.mean((1, 2)), rtol=1e-14)
+    np.testing.assert_allclose(k_(OpKind.GLOBAL_AVGPOOL_GRAD, x, g), tx.grad.numpy(), rtol=1e-13, atol=1e-16)
+
+
+def k_(kind, *xs, **attrs):
+    return execute_kernel(kind, attrs, [Tensor(x.shape, x) for x in xs])[0].data
+
+
+def test_resnet_sdpoint_coexec_equals_imperative():
+    """C3 at its parity size: the 4-way SDPoint SwitchCase (static shapes per arm) runs as
+    graphs once its paths are traced; co-execution prints and stores exactly what the
+    imperative run does."""
+    src = resnet_program(steps=12, lr=1e-3, **C3_SMALL)
+    ref, _, _ = run(src, "imperative", CpuBackend())
+    got, st, _ = run(src, "coexec", CpuBackend())
+    assert ref.lines == got.lines
+    for name in ref.vars:
+        assert np.array_equal(ref.vars[name].data, got.vars[name].data), name
+    assert st.counters()[1] > 1 and st.shape_replays == 0
+    assert len({dc.case_index for step in st.decision_log for dc in step}) >= 2

@@ -51,6 +51,22 @@ CONV = [
     (OpKind.CONV2D_DW, {"conv": (4, 2, 1)}, [rt(16, 8, 8, 64), rt(16, 4, 4, 32)]),
     (OpKind.CONV2D_DW, {"conv": (3, 1, 1)}, [rt(2, 16, 16, 128), rt(2, 16, 16, 64)]),
 ]
+# C3: conv2d's input gradient onto the forward geometry (strided shapes whose forward
+# rounding leaves rows without a window: conv2d_t's size would differ) -- (dy, w, x)
+def _dx_case(n, h, c, f, k, s, p):
+    ho = (h + 2 * p - k) // s + 1
+    return (OpKind.CONV2D_DX, {"conv": (k, s, p)}, [rt(n, ho, ho, f), rt(k * k * c, f), rt(n, h, h, c)])
+
+
+CONV += [
+    _dx_case(2, 8, 3, 5, 3, 2, 1),       # even input, 3x3/2: one row past conv2d_t's size
+    _dx_case(2, 7, 4, 6, 3, 2, 1),       # odd input: exact conv2d_t geometry
+    _dx_case(2, 8, 4, 6, 1, 2, 0),       # 1x1/2 projection shortcut
+    _dx_case(2, 9, 3, 8, 7, 2, 3),       # 7x7/2 stem
+    _dx_case(2, 8, 64, 64, 3, 1, 1),     # 3x3/1: sub-pixel implicit path (bf16)
+    _dx_case(4, 14, 128, 64, 3, 2, 1),   # strided, explicit path
+    _dx_case(2, 16, 64, 256, 1, 1, 0),   # 1x1/1 expansion
+]
 MATMUL_SPLIT = [  # bf16 MatMuls whose tile grid is too small: split-K slices
     (OpKind.MATMUL, {}, [rt(128, 8192), rt(8192, 1)]),
     (OpKind.MATMUL, {}, [rt(8192, 128), rt(128, 1)]),
@@ -73,6 +89,22 @@ BN = [
     (OpKind.SUM_ROWS, {}, [rt(5)]),
     (OpKind.SUM_ROWS, {}, [rt(8, 5000)]),        # wide rows: column-parallel kernel
     (OpKind.SUM_ROWS, {}, [rt(4096, 3072)]),     # wide rows, row chunks + fp64 atomics
+]
+
+POOL = [
+    (OpKind.MAXPOOL, {"conv": (3, 2, 1)}, [rt(2, 9, 9, 5)]),
+    (OpKind.MAXPOOL, {"conv": (3, 2, 1)}, [rt(4, 16, 16, 64)]),
+    (OpKind.MAXPOOL, {"conv": (2, 2, 0)}, [Tensor((1, 4, 4, 2), np.repeat(np.arange(16.0), 2).reshape(1, 4, 4, 2) % 3)]),
+    (OpKind.MAXPOOL_GRAD, {"conv": (3, 2, 1)}, [rt(2, 9, 9, 5), rt(2, 5, 5, 5)]),
+    (OpKind.MAXPOOL_GRAD, {"conv": (3, 2, 1)}, [rt(4, 16, 16, 64), rt(4, 8, 8, 64)]),
+    (OpKind.MAXPOOL_GRAD, {"conv": (2, 2, 0)},   # ties: the first maximum takes the gradient
+     [Tensor((1, 4, 4, 2), np.repeat(np.arange(16.0), 2).reshape(1, 4, 4, 2) % 3), rt(1, 2, 2, 2)]),
+    (OpKind.AVGPOOL, {"conv": (2, 2, 0)}, [rt(2, 7, 7, 6)]),
+    (OpKind.AVGPOOL, {"conv": (3, 1, 1)}, [rt(2, 5, 5, 3)]),
+    (OpKind.AVGPOOL_GRAD, {"conv": (2, 2, 0)}, [rt(2, 7, 7, 6), rt(2, 3, 3, 6)]),
+    (OpKind.AVGPOOL_GRAD, {"conv": (3, 1, 1)}, [rt(2, 5, 5, 3), rt(2, 5, 5, 3)]),
+    (OpKind.GLOBAL_AVGPOOL, {}, [rt(3, 7, 7, 33)]),
+    (OpKind.GLOBAL_AVGPOOL_GRAD, {}, [rt(3, 7, 7, 33), rt(3, 33)]),
 ]
 
 EDGE = np.array([-800.0, -30.0, -1.0, -0.0, 0.0, 1e-30, 0.5, 30.0, 800.0, np.nan])
@@ -136,6 +168,18 @@ def test_elementwise_ext(b200_factory, prec, tol, i):
     kind, attrs, ins = EW[i]
     got, want = run(b200_factory(prec), kind, attrs, ins)
     if prec == "f64" and kind in (OpKind.LEAKY_RELU, OpKind.RELU_GRAD, OpKind.LEAKY_RELU_GRAD):
+        assert got.data.tobytes() == want.data.tobytes()
+    else:
+        assert nrel(got, want) <= tol
+
+
+@pytest.mark.parametrize("prec,tol", [("f64", 0.0), ("fp32", 1e-6), ("bf16", 1e-6)])
+@pytest.mark.parametrize("i", range(len(POOL)))
+def test_pooling(b200_factory, prec, tol, i):
+    """Pooling (C3): f64 bit-exact (same tap / window order as the oracle); fp32 storage
+    (the bf16 mode stores activations in fp32) within 1e-6."""
+    got, want = run(b200_factory(prec), *POOL[i])
+    if prec == "f64":
         assert got.data.tobytes() == want.data.tobytes()
     else:
         assert nrel(got, want) <= tol

@@ -28,7 +28,7 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--precision", default="f64")
     ap.add_argument("--out", default=None)
-    ap.add_argument("--workload", default="c1", choices=["c1", "c2", "c4", "c5"])
+    ap.add_argument("--workload", default="c1", choices=["c1", "c2", "c3", "c4", "c5"])
     a = ap.parse_args()
     be = B200Backend(precision=a.precision)
     if a.workload == "c2":
@@ -37,6 +37,9 @@ def main():
     elif a.workload == "c4":
         from paper_2201_09210_b200.workloads import C4, gpt2_program
         src = gpt2_program(steps=100_000, **C4)
+    elif a.workload == "c3":
+        from paper_2201_09210_b200.workloads import C3, resnet_program
+        src = resnet_program(steps=100_000, **C3)
     elif a.workload == "c5":
         from paper_2201_09210_b200.workloads import C5, music_transformer_program
         src = music_transformer_program(steps=100_000, **C5)

@@ -151,6 +151,9 @@ def main():
     be = B200Backend(precision=a.precision)
     if a.workload == "c4":
         ops = record_step_ops(be, lambda n: gpt2_program(steps=n, **C4), 1)
+    elif a.workload == "c3":
+        from paper_2201_09210_b200.workloads import C3, resnet_program
+        ops = record_step_ops(be, lambda n: resnet_program(steps=n, **C3), 1)
     elif a.workload == "c5":
         ops = record_step_ops(be, lambda n: music_transformer_program(steps=n, **C5), 1)
     else:
