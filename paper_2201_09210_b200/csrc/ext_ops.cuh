@@ -465,11 +465,26 @@ struct ColStatsParams {
   Out out;                   // [C] result (COL_SUM_ROWS, COL_BN_DGAMMA)
   int extra;                 // COL_BN_DX fused backward: also write dgamma / dbeta [C]
   Out out_g, out_b;
+  long long chunk_rows;      // BULK: rows per streamed chunk (a multiple of the rows per pass)
 };
+
+// 1-D bulk copy global -> shared, completion counted on an mbarrier (BULK column statistics)
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"((uint64_t)src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+constexpr int kColStages = 4;      // BULK: chunks in flight per block
 
 // V = channels per thread (4: float4 loads when C % 4 == 0 and T = float; else 1); rows
 // unrolled by 4 so each thread keeps several independent loads in flight.
-template <typename T, int V, int S, bool DY>
+//
+// BULK (float, V = 4, S = 1): the block's rows are one contiguous range, streamed through a
+// kColStages-deep shared-memory ring by 1-D bulk copies (thread 0 issues, mbarriers count the
+// bytes) -- the bytes in flight no longer depend on registers per thread, so large tensors
+// run at HBM rate with two blocks per SM.
+template <typename T, int V, int S, bool DY, bool BULK = false>
 __global__ void __launch_bounds__(256) k_colstats(ColStatsParams p) {
   COEX_PDL_ENTER();
   stamp(p.ds, SK_COLSTATS);
@@ -500,7 +515,59 @@ __global__ void __launch_bounds__(256) k_colstats(ColStatsParams p) {
       const long long c = (cc + (long long)j * L) * V + v;
       sh[j][v] = (p.mode != COL_SUM_ROWS && j < slots && c < C) ? (double)x[c] : 0.0;
     }
-  if (rr < rpi) {
+  if constexpr (BULK) {
+    extern __shared__ __align__(128) unsigned char col_dsm[];
+    __shared__ uint64_t full[kColStages];
+    const long long cr = p.chunk_rows, cf = cr * C;
+    float* xs = (float*)col_dsm;
+    float* gs = xs + kColStages * cf;
+    const long long nch = (r_end - r_begin + cr - 1) / cr;
+    if (t == 0) {
+      for (int q = 0; q < kColStages; ++q) mbar_init(&full[q], 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    auto issue = [&](long long i) {
+      const int q = (int)(i % kColStages);
+      const long long r0 = r_begin + i * cr;
+      const long long nr = r_end - r0 < cr ? r_end - r0 : cr;
+      const uint32_t bytes = (uint32_t)(nr * C * 4);
+      mbar_expect_tx(&full[q], with_dy ? 2 * bytes : bytes);
+      bulk_g2s(xs + q * cf, x + r0 * C, bytes, &full[q]);
+      if (with_dy) bulk_g2s(gs + q * cf, dy + r0 * C, bytes, &full[q]);
+    };
+    if (t == 0)
+      for (long long i = 0; i < nch && i < kColStages; ++i) issue(i);
+    const long long c0 = (long long)cc * V;
+    for (long long i = 0; i < nch; ++i) {
+      const int q = (int)(i % kColStages);
+      mbar_wait(&full[q], (uint32_t)((i / kColStages) & 1));
+      const long long nr = r_end - (r_begin + i * cr) < cr ? r_end - (r_begin + i * cr) : cr;
+      if (rr < rpi && c0 < C) {
+        for (long long r = rr; r < nr; r += rpi) {
+          const float4 f = *(const float4*)(xs + q * cf + r * C + c0);
+          const float xv[4] = {f.x, f.y, f.z, f.w};
+          float gv[4] = {0.f, 0.f, 0.f, 0.f};
+          if (with_dy) {
+            const float4 g = *(const float4*)(gs + q * cf + r * C + c0);
+            gv[0] = g.x; gv[1] = g.y; gv[2] = g.z; gv[3] = g.w;
+          }
+#pragma unroll
+          for (int v = 0; v < V; ++v) {
+            const double d = (double)xv[v] - sh[0][v];
+            a1[0][v] += d;
+            a2[0][v] += d * d;
+            if (with_dy) {
+              a3[0][v] += (double)gv[v];
+              a4[0][v] += (double)gv[v] * d;
+            }
+          }
+        }
+      }
+      __syncthreads();                      // stage q consumed by every thread
+      if (t == 0 && i + kColStages < nch) issue(i + kColStages);
+    }
+  } else if (rr < rpi) {
 #pragma unroll
     for (int j = 0; j < S; ++j) {
       if (j >= slots) break;
@@ -751,7 +818,8 @@ __global__ void __launch_bounds__(256) k_bn_apply_v4(BnApplyParams p) {
 // element, taps in (ky, kx) order (max: strict '>' so the first maximum wins, -inf padding;
 // avg: zero padding, sum / k^2).  MODE 1 maxpool_grad, 3 avgpool_grad: one thread per INPUT
 // element gathering the covering windows in ascending (oy, ox) order (max: the window's
-// argmax recomputed; no atomics, deterministic).  MODE 4 global average pool (thread per
+// argmax recomputed, or read from the per-window tap indices MODE 6 wrote; no atomics,
+// deterministic).  MODE 4 global average pool (thread per
 // (n, c), row-major sequential sum / (H*W)), MODE 5 its gradient -- oracle/kernels.py
 // pool_kernel.
 struct PoolParams {
@@ -760,6 +828,7 @@ struct PoolParams {
   Out out;
   long long N, H, W, C, Ho, Wo;
   int k, s, p;
+  unsigned char* idx;        // maxpool_grad: per-window argmax tap (ky*k + kx), written by MODE 6
 };
 
 template <typename T, int MODE>
@@ -769,6 +838,29 @@ __global__ void __launch_bounds__(256) k_pool(PoolParams p) {
   if (skip(p.ds)) return;
   const T* x = res<T>(p.x);
   const T* dy = (MODE & 1) ? res<T>(p.dy) : nullptr;       // modes 1, 3, 5 take (x, dy)
+  if (MODE == 6) {                       // maxpool_grad pass 1: argmax tap of every window
+    const long long total = p.N * p.Ho * p.Wo * p.C;
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+      const long long c = e % p.C, pix = e / p.C;
+      const long long ox = pix % p.Wo, oy = (pix / p.Wo) % p.Ho, n = pix / (p.Wo * p.Ho);
+      T m = (T)-INFINITY;
+      int arg = -1, first = -1;
+      for (int ky = 0; ky < p.k; ++ky) {
+        const long long iy = oy * p.s - p.p + ky;
+        if (iy < 0 || iy >= p.H) continue;
+        for (int kx = 0; kx < p.k; ++kx) {
+          const long long ix = ox * p.s - p.p + kx;
+          if (ix < 0 || ix >= p.W) continue;
+          const T v = x[((n * p.H + iy) * p.W + ix) * p.C + c];
+          if (first < 0) first = ky * p.k + kx;
+          if (v > m) { m = v; arg = ky * p.k + kx; }
+        }
+      }
+      p.idx[e] = (unsigned char)(arg < 0 ? first : arg);
+    }
+    return;
+  }
   T* o = pick_out<T>(p.out, x, dy);
   publish_early(p.out, o);
   count_op(p.ds);
@@ -823,8 +915,13 @@ __global__ void __launch_bounds__(256) k_pool(PoolParams p) {
       T acc = (T)0;
       for (long long oy = oy0; oy <= oy1; ++oy) {
         for (long long ox = ox0; ox <= ox1; ++ox) {
-          const T g = dy[((n * p.Ho + oy) * p.Wo + ox) * C + c];
-          if (MODE == 3) { acc = acc + g; continue; }
+          const long long w = ((n * p.Ho + oy) * p.Wo + ox) * C + c;
+          if (MODE == 3) { acc = acc + dy[w]; continue; }
+          if (p.idx != nullptr) {          // argmax from pass 1
+            if (p.idx[w] == (unsigned char)((iy - (oy * s - pd)) * k + (ix - (ox * s - pd)))) acc = acc + dy[w];
+            continue;
+          }
+          const T g = dy[w];
           // argmax: strict '>' from -inf; no tap above -inf -> the first in-bounds tap
           T m = (T)-INFINITY;
           long long ay = -1, ax = -1, fy = -1, fx = -1;

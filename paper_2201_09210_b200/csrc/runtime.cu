@@ -946,6 +946,16 @@ int implicit_mask() {
   return m;
 }
 
+// COEX_COL_BULK=0 keeps the register-pipelined column statistics (A/B measurement)
+bool col_bulk() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("COEX_COL_BULK");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 struct Carve {
   char* base;
   size_t off = 0;
@@ -1130,6 +1140,10 @@ int build_xop_t(coex_ctx* c, const OpSpec& s, Launch* L, int* nL, size_t* ws_byt
     }
     case COEX_MAXPOOL: case COEX_MAXPOOL_GRAD: case COEX_AVGPOOL: case COEX_AVGPOOL_GRAD: case COEX_GLOBAL_AVGPOOL:
     case COEX_GLOBAL_AVGPOOL_GRAD: {
+      // maxpool_grad: pass 1 stores every window's argmax tap (1 byte) in scratch, pass 2
+      // gathers -- instead of recomputing up to ceil(k/s)^2 window maxima per input element
+      unsigned char* idx = nullptr;
+      if (s.kind == COEX_MAXPOOL_GRAD) idx = (unsigned char*)cv.take((size_t)numel_of(s.in_ndim[1], s.in_shape[1]));
       if (!build) break;
       PoolParams pp{};
       pp.ds = s.ds; pp.x = s.in[0]; pp.dy = s.nin > 1 ? s.in[1] : In{nullptr, nullptr, nullptr}; pp.out = s.out;
@@ -1147,6 +1161,13 @@ int build_xop_t(coex_ctx* c, const OpSpec& s, Launch* L, int* nL, size_t* ws_byt
           break;
         case COEX_MAXPOOL_GRAD: case COEX_AVGPOOL_GRAD:
           pp.Ho = s.in_shape[1][1]; pp.Wo = s.in_shape[1][2];
+          if (s.kind == COEX_MAXPOOL_GRAD) {
+            pp.idx = idx;
+            PoolParams p1 = pp;
+            p1.out = Out{};
+            L[(*nL)++].set(f64 ? (void*)k_pool<double, 6> : (void*)k_pool<float, 6>,
+                           grid_for(pp.N * pp.Ho * pp.Wo * pp.C), dim3(256), p1);
+          }
           fn = s.kind == COEX_MAXPOOL_GRAD ? (f64 ? (void*)k_pool<double, 1> : (void*)k_pool<float, 1>)
                                            : (f64 ? (void*)k_pool<double, 3> : (void*)k_pool<float, 3>);
           break;
@@ -1258,8 +1279,27 @@ int build_xop_t(coex_ctx* c, const OpSpec& s, Launch* L, int* nL, size_t* ws_byt
       if (v4 && C <= 1024) colfn = dy ? (void*)k_colstats<float, 4, 1, true> : (void*)k_colstats<float, 4, 1, false>;
       else if (v4) colfn = dy ? (void*)k_colstats<float, 4, 2, true> : (void*)k_colstats<float, 4, 2, false>;
       else colfn = dy ? (void*)k_colstats<T, 1, kColMaxSlots, true> : (void*)k_colstats<T, 1, kColMaxSlots, false>;
+      // bulk-streamed statistics (tolerance modes, C <= 1024): rows of 16 KB chunks
+      size_t bulk_smem = 0;
+      if (atomic && v4 && C <= 1024 && col_bulk()) {
+        const int64_t rpi = 256 / (C / 4 < 256 ? C / 4 : 256);
+        const int64_t cr = (4096 / C > rpi ? 4096 / C : rpi) / rpi * rpi;
+        bulk_smem = (size_t)kColStages * cr * C * 4 * (dy ? 2 : 1);
+        colfn = dy ? (void*)k_colstats<float, 4, 1, true, true> : (void*)k_colstats<float, 4, 1, false, true>;
+        static int occ[2] = {0, 0};
+        int& oc = occ[dy ? 1 : 0];
+        if (oc == 0) {
+          CK(cudaFuncSetAttribute(colfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bulk_smem));
+          if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oc, colfn, 256, bulk_smem) != cudaSuccess || oc < 1) {
+            cudaGetLastError();
+            oc = 1;
+          }
+        }
+        if (G > (int64_t)oc * kNumSMs) G = (int64_t)oc * kNumSMs;
+      }
       ColStatsParams cp{};
       cp.ds = s.ds; cp.x = s.in[0]; cp.R = R; cp.C = C;
+      if (bulk_smem) cp.chunk_rows = (int64_t)(bulk_smem / ((size_t)kColStages * C * 4 * (dy ? 2 : 1)));
       cp.atomic = atomic ? 1 : 0;
       cp.part = (double*)pv.take((size_t)(atomic ? kColReplicas : G) * C * 4 * 8);
       cp.stats = (double*)pv.take((size_t)C * 4 * 8);
@@ -1271,7 +1311,8 @@ int build_xop_t(coex_ctx* c, const OpSpec& s, Launch* L, int* nL, size_t* ws_byt
         cp.mode = s.kind == COEX_SUM_ROWS ? COL_SUM_ROWS : COL_BN_DGAMMA;
         if (s.kind == COEX_BN_DGAMMA) cp.dy = s.in[1];
         cp.out = s.out;
-        L[(*nL)++].set(colfn, dim3((unsigned)G), dim3(256), cp);
+        L[*nL].set(colfn, dim3((unsigned)G), dim3(256), cp);
+        L[(*nL)++].smem = bulk_smem;
         return COEX_OK;
       }
       cp.mode = s.kind == COEX_BATCHNORM ? COL_BN : COL_BN_DX;
@@ -1282,7 +1323,8 @@ int build_xop_t(coex_ctx* c, const OpSpec& s, Launch* L, int* nL, size_t* ws_byt
         cp.out_g = s.out2;
         cp.out_b = s.out3;
       }
-      L[(*nL)++].set(colfn, dim3((unsigned)G), dim3(256), cp);
+      L[*nL].set(colfn, dim3((unsigned)G), dim3(256), cp);
+      L[(*nL)++].smem = bulk_smem;
       BnApplyParams ap{};
       ap.ds = s.ds; ap.x = s.in[0]; ap.g = s.in[1]; ap.third = s.in[2]; ap.stats = cp.stats;
       ap.n = n; ap.C = C; ap.dx = s.kind != COEX_BATCHNORM; ap.out = s.out;

@@ -19,6 +19,9 @@ OPS = {
     "dw_32x32x64": (OpKind.CONV2D_DW, {"conv": (4, 2, 1)}, [(128, 32, 32, 64), (128, 16, 16, 128)]),
     "conv_16x16x128": (OpKind.CONV2D, {"conv": (4, 2, 1)}, [(128, 16, 16, 128), (2048, 256)]),
     "bn_16x16x128": (OpKind.BATCHNORM, {}, [(128, 16, 16, 128), (128,), (128,)]),
+    "bn_4x4x512": (OpKind.BATCHNORM, {}, [(128, 4, 4, 512), (512,), (512,)]),
+    "bn_32x32x64": (OpKind.BATCHNORM, {}, [(128, 32, 32, 64), (64,), (64,)]),
+    "bndx_8x8x256": (OpKind.BATCHNORM_DX, {}, [(128, 8, 8, 256), (256,), (128, 8, 8, 256)]),
     "mm_8192x128x1": (OpKind.MATMUL, {}, [(8192, 128), (128, 1)]),
     "gemm_8192": (OpKind.MATMUL, {}, [(8192, 8192), (8192, 8192)]),
     "ce_grad": (OpKind.CROSS_ENTROPY_GRAD, {}, [(8192, 50257), (8192,)]),
