@@ -276,7 +276,17 @@ def roofline_c2(be, hbm_peak, tflops_peak, peak_kind, workload="c2"):
         ach = f["bytes"] / (known * 1e-3) / 1e9
         roof = {"bound": "hbm", "kernel": top, "achieved": round(ach, 1), "peak": hbm_peak, "unit": "GB/s",
                 "frac": round(ach / hbm_peak, 4), "algorithmic_bytes_per_pair": f["bytes"]}
-    roof.update({"traffic": None, "peak_source": peak_kind, "kernel_ms_per_pair": round(f["ms"], 4),
+    traffic, tnote = None, None
+    if workload == "c2" and top == "k_gemm_tc":
+        # DRAM read + write of one representative launch of the family, from the committed
+        # `ncu --set full` capture (the implicit conv2d [128,32,32,64] x [1024,128], 8.6 GFLOP;
+        # algorithmic bytes of that launch: bf16 x copy 17 MB + weights 0.26 MB + fp32 output
+        # 16.8 MB -- the output stays in L2 under ncu's serialised replay)
+        traffic = 19.26e6
+        tnote = ("bytes per launch of k_gemm_tc<128, 2, 1> (conv2d [128,32,32,64]x[1024,128]) from "
+                 "profiles/round1_ncu_c2_conv_gemm.ncu-rep, dram__bytes_read.sum + dram__bytes_write.sum")
+    roof.update({"traffic": traffic, "traffic_note": tnote, "peak_source": peak_kind,
+                 "kernel_ms_per_pair": round(f["ms"], 4),
                  "share_of_step": round(f["ms"] / total, 4), "kernel_sum_ms_per_pair": round(total, 4),
                  "families": fams,
                  "method": "every distinct op of one D+G step pair re-launched eagerly with the step's shapes, "
