@@ -177,7 +177,11 @@ def timed_steps(o, be, k: int, flush: bool = True):
         be.event(0)
         o.step()
         be.event(1)
-        tot += be.elapsed_ms(0, 1)
+        ms = be.elapsed_ms(0, 1)
+        tot += ms
+        if os.environ.get("BENCH_VERBOSE"):
+            print(f"[bench] step {ms:.3f} ms counters {o.stats.counters()} shape_replays {o.stats.shape_replays}",
+                  file=sys.stderr, flush=True)
     return tot, be.kernel_count() - ops0
 
 
