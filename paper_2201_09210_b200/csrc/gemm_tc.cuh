@@ -459,9 +459,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc(const __grid_constant
       const int cph = (int)((it / splits) % phases);
       mbar_wait(&tfull[a], aph);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-#pragma unroll 1
-      for (int c = 0; c < (nk < 0 ? 0 : BN); c += 32) {
-        uint32_t r[32];
+      // TMEM loads software-pipelined one 32-column chunk ahead: chunk c+32 streams out of
+      // TMEM while chunk c goes through the smem transpose and the global stores
+      auto tload = [&](uint32_t (&r)[32], int c) {
         if (nk > 0) {
           const uint32_t taddr = tmem + ((uint32_t)lane_base << 16) + (uint32_t)(a * BN + c);
           asm volatile(
@@ -473,12 +473,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc(const __grid_constant
                 "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]),
                 "=r"(r[30]), "=r"(r[31])
               : "r"(taddr));
-          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         } else {
 #pragma unroll
           for (int i = 0; i < 32; ++i) r[i] = 0u;
         }
-        if (n0 + c >= p.N) break;                    // chunk entirely past the last column
+      };
+      auto tstore = [&](const uint32_t (&r)[32], int c) {
+        if (n0 + c >= p.N) return;                   // chunk entirely past the last column
         float* srow = stage + lane * TC_EPI_LD;
 #pragma unroll
         for (int i = 0; i < 32; i += 4)
@@ -512,6 +513,22 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc(const __grid_constant
           }
         }
         __syncwarp();
+      };
+      if (nk >= 0) {
+        uint32_t ra[32], rb[32];
+        tload(ra, 0);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 64) {
+          if (c + 32 < BN) tload(rb, c + 32);
+          tstore(ra, c);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          if (c + 32 < BN) {
+            if (c + 64 < BN) tload(ra, c + 64);
+            tstore(rb, c + 32);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          }
+        }
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();

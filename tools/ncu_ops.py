@@ -21,6 +21,10 @@ OPS = {
     "bn_16x16x128": (OpKind.BATCHNORM, {}, [(128, 16, 16, 128), (128,), (128,)]),
     "bn_4x4x512": (OpKind.BATCHNORM, {}, [(128, 4, 4, 512), (512,), (512,)]),
     "bn_32x32x64": (OpKind.BATCHNORM, {}, [(128, 32, 32, 64), (64,), (64,)]),
+    "c3s1_c64": (OpKind.CONV2D, {"conv": (3, 1, 1)}, [(32, 32, 32, 64), (576, 128)]),
+    "c3s1_c128": (OpKind.CONV2D, {"conv": (3, 1, 1)}, [(32, 32, 32, 128), (1152, 64)]),
+    "c3s1_c256": (OpKind.CONV2D, {"conv": (3, 1, 1)}, [(32, 32, 32, 256), (2304, 32)]),
+    "c4s2_c64": (OpKind.CONV2D, {"conv": (4, 2, 1)}, [(32, 64, 64, 64), (1024, 128)]),
     "bndx_8x8x256": (OpKind.BATCHNORM_DX, {}, [(128, 8, 8, 256), (256,), (128, 8, 8, 256)]),
     "mm_8192x128x1": (OpKind.MATMUL, {}, [(8192, 128), (128, 1)]),
     "gemm_8192": (OpKind.MATMUL, {}, [(8192, 8192), (8192, 8192)]),
