@@ -88,6 +88,13 @@ enum coex_opkind {
   COEX_AVGPOOL_GRAD,       /* (x, dy) -> covering dy sum / k^2 */
   COEX_GLOBAL_AVGPOOL,     /* (x [N,H,W,C]) -> [N,C] */
   COEX_GLOBAL_AVGPOOL_GRAD,/* (x, dy [N,C]) -> dy / (H*W) broadcast */
+  /* general extension ops: Adam's elementwise sqrt / div; data movement; axis reductions
+   * (coex_attrs.dims = [axis, start, length] for slice, [axis] for concat / sum_axis) */
+  COEX_SQRT = 51,          /* (x) -> sqrt(x) */
+  COEX_DIV,                /* (a, b) -> a / b, rank-0 broadcast */
+  COEX_SLICE,              /* (x) -> x[.., start:start+length, ..] along axis */
+  COEX_CONCAT,             /* (a, b) -> joined along axis */
+  COEX_SUM_AXIS,           /* (x) -> sequential sum along axis (axis removed) */
   COEX_NUM_KINDS
 };
 

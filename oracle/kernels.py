@@ -44,6 +44,9 @@ reference; written in tensor.py's style (explicit orders):
   windows in ascending (oy, ox) order from +0.0); AVGPOOL = (window sum in (ky, kx) order,
   zero padding) / k^2; AVGPOOL_GRAD = (sum of covering dy in (oy, ox) order) / k^2;
   GLOBAL_AVGPOOL = (row-major sum over H, W) / (H*W); GLOBAL_AVGPOOL_GRAD = dy / (H*W).
+* General: SQRT (IEEE, NaN for negatives), DIV (IEEE, rank-0 broadcast) -- Adam's update;
+  SLICE(x, [axis, start, length]), CONCAT(a, b, [axis]); SUM_AXIS(x, [axis]) = sequential sum
+  along the axis from +0.0.
 """
 
 from __future__ import annotations
@@ -179,6 +182,20 @@ def pool_kernel(kind: OpKind, attrs: dict, x: list, out_shape) -> np.ndarray:
 
 
 def ext_kernel(kind: OpKind, attrs: dict, x: list, out_shape) -> np.ndarray:
+    if kind is OpKind.SQRT:
+        with np.errstate(invalid="ignore"):
+            return np.sqrt(x[0])
+    if kind is OpKind.SLICE:
+        ax, start, length = attrs["dims"]
+        return np.take(x[0], np.arange(start, start + length), axis=ax).reshape(out_shape)
+    if kind is OpKind.CONCAT:
+        return np.concatenate([x[0], x[1]], axis=attrs["dims"][0])
+    if kind is OpKind.SUM_AXIS:
+        ax = attrs["dims"][0]
+        acc = np.zeros(out_shape)
+        for j in range(x[0].shape[ax]):
+            acc = acc + np.take(x[0], j, axis=ax)
+        return acc + 0.0
     if kind in (OpKind.MAXPOOL, OpKind.MAXPOOL_GRAD, OpKind.AVGPOOL, OpKind.AVGPOOL_GRAD, OpKind.GLOBAL_AVGPOOL,
                 OpKind.GLOBAL_AVGPOOL_GRAD):
         return pool_kernel(kind, attrs, x, out_shape)
@@ -339,7 +356,12 @@ def transformer_kernel(kind: OpKind, attrs: dict, x: list, out_shape):
     return None
 
 
-_BINARY = {OpKind.ADD: np.add, OpKind.SUB: np.subtract, OpKind.MUL: np.multiply}
+def _div(a, b):
+    with np.errstate(divide="ignore", invalid="ignore"):
+        return np.divide(a, b)
+
+
+_BINARY = {OpKind.ADD: np.add, OpKind.SUB: np.subtract, OpKind.MUL: np.multiply, OpKind.DIV: _div}
 
 
 EXT = frozenset(tuple(OpKind)[14:])

@@ -142,7 +142,7 @@ def _attrs(kind: OpKind, attrs: dict) -> CoexAttrs:
         at.value = float(attrs["value"])
     elif kind in CONV_ATTR_KINDS:
         dims = attrs["conv"]
-    elif kind is OpKind.EMBEDDING_DW:
+    elif kind in (OpKind.EMBEDDING_DW, OpKind.SLICE, OpKind.CONCAT, OpKind.SUM_AXIS):
         dims = attrs["dims"]
     elif kind in (OpKind.CAUSAL_SOFTMAX, OpKind.SOFTMAX_GRAD):
         dims = ()
@@ -244,7 +244,7 @@ class B200Backend:
                    12: "end", 13: "fused chain", 14: "im2col", 15: "col2im", 16: "bf16 cvt", 17: "colstats",
                    18: "bn apply", 19: "split-K reduce", 20: "causal softmax", 21: "softmax grad",
                    22: "cross-entropy", 23: "bias add", 24: "layernorm", 25: "embedding", 26: "column sum",
-                   27: "rel skew", 28: "pooling"}
+                   27: "rel skew", 28: "pooling", 29: "axis op"}
 
     def set_trace(self, capacity: int):
         """Enable device-side per-kernel stamps (0 disables)."""

@@ -53,7 +53,7 @@ enum StampKind {
   SK_FEED_WAIT = 7, SK_FEED_FILL = 8, SK_FETCH = 9, SK_GATE = 10, SK_COMMIT = 11, SK_END = 12,
   SK_AFTER_WAIT = 64, SK_FUSED = 13, SK_IM2COL = 14, SK_COL2IM = 15, SK_CVT = 16, SK_COLSTATS = 17,
   SK_BNAPPLY = 18, SK_SPLITK = 19, SK_SOFTMAX = 20, SK_SOFTMAX_GRAD = 21, SK_CE = 22, SK_BIAS = 23, SK_LN = 24,
-  SK_EMBED = 25, SK_COLSUM = 26, SK_SKEW = 27, SK_POOL = 28
+  SK_EMBED = 25, SK_COLSUM = 26, SK_SKEW = 27, SK_POOL = 28, SK_AXIS = 29
 };
 
 // Host <-> device rings in pinned, mapped host memory.
@@ -202,12 +202,12 @@ __device__ __forceinline__ void count_op(DevState* ds) {
 // (slope 0.2), RELU_GRAD(x, dy), LEAKY_RELU_GRAD(x, dy), BCE_TERM(x, t).
 enum EwOp { EW_ADD = 0, EW_SUB = 1, EW_MUL = 2, EW_NEG = 3, EW_RELU = 4, EW_SIGMOID = 5, EW_COPY = 6,
             EW_TANH = 7, EW_LRELU = 8, EW_RELU_GRAD = 9, EW_LRELU_GRAD = 10, EW_BCE = 11,
-            EW_TO_INDEX = 12, EW_GELU_GRAD = 13, EW_GELU = 14 };
+            EW_TO_INDEX = 12, EW_GELU_GRAD = 13, EW_GELU = 14, EW_SQRT = 15, EW_DIV = 16 };
 constexpr double kGeluK = 0.7978845608028654;   // sqrt(2/pi)
 constexpr double kLeakySlope = 0.2;
 
 __host__ __device__ __forceinline__ bool ew_binary(int op) {
-  return op <= EW_MUL || (op >= EW_RELU_GRAD && op <= EW_GELU_GRAD);
+  return op <= EW_MUL || (op >= EW_RELU_GRAD && op <= EW_GELU_GRAD) || op == EW_DIV;
 }
 
 __device__ __forceinline__ double ew_apply(int op, double a, double b) {
@@ -232,6 +232,8 @@ __device__ __forceinline__ double ew_apply(int op, double a, double b) {
       const double t = tanh(kGeluK * (a + 0.044715 * a * a * a));
       return b * (0.5 * (1.0 + t) + 0.5 * a * (1.0 - t * t) * kGeluK * (1.0 + 3.0 * 0.044715 * a * a));
     }
+    case EW_SQRT: return __dsqrt_rn(a);
+    case EW_DIV: return __ddiv_rn(a, b);
     default: return a;
   }
 }
@@ -257,6 +259,8 @@ __device__ __forceinline__ float ew_apply(int op, float a, float b) {
       const float t = tanhf((float)kGeluK * (a + 0.044715f * a * a * a));
       return b * (0.5f * (1.0f + t) + 0.5f * a * (1.0f - t * t) * (float)kGeluK * (1.0f + 3.0f * 0.044715f * a * a));
     }
+    case EW_SQRT: return __fsqrt_rn(a);
+    case EW_DIV: return __fdiv_rn(a, b);
     default: return a;
   }
 }

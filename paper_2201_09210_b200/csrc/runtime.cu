@@ -234,7 +234,8 @@ int infer(int kind, const coex_attrs* at, int nin, const TRec* in, int* ndim, in
   static const int arity[] = {2, 2, 2, 2, 1, 1, 1, 1, 1, 1, 1, 0, 0, 1,
                               2, 2, 2, 3, 3, 2, 1, 1, 1, 2, 2, 2,
                               2, 2, 2, 3, 3, 2, 2, 1, 2, 2, 2, 2, 1, 2, 2, 2,
-                              1, 1, 3, 1, 2, 1, 2, 1, 2};
+                              1, 1, 3, 1, 2, 1, 2, 1, 2,
+                              1, 2, 1, 2, 1};
   static_assert(sizeof(arity) / sizeof(arity[0]) == COEX_NUM_KINDS, "arity table");
   if (kind < 0 || kind >= COEX_NUM_KINDS) return fail(COEX_BAD_ATTRS, "unknown op kind");
   if (nin != arity[kind]) return fail(COEX_BAD_ATTRS, "wrong number of tensor inputs");
@@ -305,11 +306,12 @@ int infer_ext(int kind, const coex_attrs* at, const TRec* in, int* ndim, int64_t
     return true;
   };
   switch (kind) {
-    case COEX_TANH: case COEX_LEAKY_RELU: case COEX_GELU:
+    case COEX_TANH: case COEX_LEAKY_RELU: case COEX_GELU: case COEX_SQRT:
       *ndim = in[0].ndim;
       memcpy(shape, in[0].shape, sizeof(int64_t) * in[0].ndim);
       return COEX_OK;
-    case COEX_RELU_GRAD: case COEX_LEAKY_RELU_GRAD: case COEX_BCE_TERM: case COEX_TO_INDEX: case COEX_GELU_GRAD: {
+    case COEX_RELU_GRAD: case COEX_LEAKY_RELU_GRAD: case COEX_BCE_TERM: case COEX_TO_INDEX: case COEX_GELU_GRAD:
+    case COEX_DIV: {
       const TRec &a = in[0], &b = in[1];
       if (!(same(a, b) || a.ndim == 0 || b.ndim == 0)) return fail(COEX_SHAPE_MISMATCH, "elementwise: incompatible shapes");
       const TRec& r = (same(a, b) || b.ndim == 0) ? a : b;
@@ -412,6 +414,30 @@ int infer_ext(int kind, const coex_attrs* at, const TRec* in, int* ndim, int64_t
         *ndim = 2;
         shape[0] = lg.shape[0];
         shape[1] = lg.shape[1];
+      }
+      return COEX_OK;
+    }
+    case COEX_SLICE: case COEX_CONCAT: case COEX_SUM_AXIS: {
+      const int want = kind == COEX_SLICE ? 3 : 1;
+      if (at == nullptr || at->n != want) return fail(COEX_BAD_ATTRS, "axis op: [axis(, start, length)] expected");
+      const TRec& x = in[0];
+      const int64_t ax = at->dims[0];
+      if (ax < 0 || ax >= x.ndim) return fail(COEX_SHAPE_MISMATCH, "axis op: axis out of range");
+      *ndim = x.ndim;
+      memcpy(shape, x.shape, sizeof(int64_t) * x.ndim);
+      if (kind == COEX_SLICE) {
+        if (at->dims[1] < 0 || at->dims[2] < 0 || at->dims[1] + at->dims[2] > x.shape[ax])
+          return fail(COEX_SHAPE_MISMATCH, "slice: range exceeds the axis");
+        shape[ax] = at->dims[2];
+      } else if (kind == COEX_SUM_AXIS) {
+        for (int i = (int)ax; i + 1 < x.ndim; ++i) shape[i] = x.shape[i + 1];
+        *ndim = x.ndim - 1;
+      } else {
+        const TRec& y = in[1];
+        if (y.ndim != x.ndim) return fail(COEX_SHAPE_MISMATCH, "concat: ranks differ");
+        for (int i = 0; i < x.ndim; ++i)
+          if (i != ax && y.shape[i] != x.shape[i]) return fail(COEX_SHAPE_MISMATCH, "concat: shapes differ off the axis");
+        shape[ax] = x.shape[ax] + y.shape[ax];
       }
       return COEX_OK;
     }
@@ -520,7 +546,8 @@ struct OpSpec {
 constexpr int kBnBwdFused = 100;
 bool is_ext_compute(int kind) {
   return (kind >= COEX_CONV2D && kind <= COEX_SUM_ROWS) || kind == kBnBwdFused ||
-         (kind >= COEX_EMBEDDING && kind <= COEX_GLOBAL_AVGPOOL_GRAD && kind != COEX_GELU && kind != COEX_GELU_GRAD);
+         (kind >= COEX_EMBEDDING && kind <= COEX_GLOBAL_AVGPOOL_GRAD && kind != COEX_GELU && kind != COEX_GELU_GRAD) ||
+         (kind >= COEX_SLICE && kind <= COEX_SUM_AXIS);
 }
 int ew_code(int kind) {
   switch (kind) {
@@ -537,6 +564,8 @@ int ew_code(int kind) {
     case COEX_TO_INDEX: return EW_TO_INDEX;
     case COEX_GELU: return EW_GELU;
     case COEX_GELU_GRAD: return EW_GELU_GRAD;
+    case COEX_SQRT: return EW_SQRT;
+    case COEX_DIV: return EW_DIV;
     default: return EW_BCE;
   }
 }
@@ -641,7 +670,7 @@ int build_launch_t(coex_ctx* c, const OpSpec& s, Launch* L) {
   switch (s.kind) {
     case COEX_ADD: case COEX_SUB: case COEX_MUL: case COEX_NEG: case COEX_RELU: case COEX_SIGMOID:
     case COEX_TANH: case COEX_LEAKY_RELU: case COEX_RELU_GRAD: case COEX_LEAKY_RELU_GRAD: case COEX_BCE_TERM:
-    case COEX_TO_INDEX: case COEX_GELU: case COEX_GELU_GRAD: {
+    case COEX_TO_INDEX: case COEX_GELU: case COEX_GELU_GRAD: case COEX_SQRT: case COEX_DIV: {
       EwParams p{};
       p.ds = s.ds;
       p.a = s.in[0];
@@ -1136,6 +1165,22 @@ int build_xop_t(coex_ctx* c, const OpSpec& s, Launch* L, int* nL, size_t* ws_byt
       simt_matmul_launch<T>(c, mp, &L[(*nL)++]);
       cp.cols = cols;
       L[(*nL)++].set((void*)k_col2im<T, T>, grid_for(N * Ho * Wo * F), dim3(256), cp);
+      return COEX_OK;
+    }
+    case COEX_SLICE: case COEX_CONCAT: case COEX_SUM_AXIS: {
+      if (!build) break;
+      AxisParams ap{};
+      ap.ds = s.ds; ap.a = s.in[0]; ap.b = s.nin > 1 ? s.in[1] : In{nullptr, nullptr, nullptr}; ap.out = s.out;
+      const int ax = (int)s.attr_dims[0];
+      ap.outer = 1; ap.inner = 1;
+      for (int i = 0; i < ax; ++i) ap.outer *= s.in_shape[0][i];
+      for (int i = ax + 1; i < s.in_ndim[0]; ++i) ap.inner *= s.in_shape[0][i];
+      ap.A = s.in_shape[0][ax];
+      ap.A2 = s.nin > 1 ? s.in_shape[1][ax] : 0;
+      ap.start = s.attr_dims[1]; ap.length = s.attr_dims[2];
+      ap.mode = s.kind == COEX_SLICE ? 0 : s.kind == COEX_CONCAT ? 1 : 2;
+      const int64_t work = ap.mode == 2 ? ap.outer * ap.inner : numel_of(s.out_ndim, s.out_shape);
+      L[(*nL)++].set(is_f64(c) ? (void*)k_axis<double> : (void*)k_axis<float>, grid_for(work < 1 ? 1 : work), dim3(256), ap);
       return COEX_OK;
     }
     case COEX_MAXPOOL: case COEX_MAXPOOL_GRAD: case COEX_AVGPOOL: case COEX_AVGPOOL_GRAD: case COEX_GLOBAL_AVGPOOL:

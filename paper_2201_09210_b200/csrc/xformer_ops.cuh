@@ -604,4 +604,48 @@ __global__ void __launch_bounds__(256) k_acc_out(RowParams p) {
   publish_late(p.out, o);
 }
 
+// ------------------------------------------------------------------ axis ops (general)
+// x viewed as [outer][A][inner] around the axis.  slice: out[o][j][i] = x[o][start + j][i];
+// concat: out[o][j][i] = j < A ? a[o][j][i] : b[o][j - A][i]; sum_axis: out[o][i] = sequential
+// sum over j from +0 (thread per output element, coalesced over i).
+struct AxisParams {
+  DevState* ds;
+  In a, b;
+  Out out;
+  long long outer, A, A2, inner, start, length;
+  int mode;                  // 0 slice, 1 concat, 2 sum_axis
+};
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_axis(AxisParams p) {
+  COEX_PDL_ENTER();
+  stamp(p.ds, SK_AXIS);
+  if (skip(p.ds)) return;
+  const T* a = res<T>(p.a);
+  const T* b = p.mode == 1 ? res<T>(p.b) : nullptr;
+  T* o = pick_out<T>(p.out, a, b);
+  publish_early(p.out, o);
+  count_op(p.ds);
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  if (p.mode == 2) {
+    const long long total = p.outer * p.inner;
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += stride) {
+      const long long i = e % p.inner, ob = e / p.inner;
+      const T* src = a + ob * p.A * p.inner + i;
+      T acc = (T)0;
+      for (long long j = 0; j < p.A; ++j) acc = acc + src[j * p.inner];
+      o[e] = acc + (T)0;
+    }
+  } else {
+    const long long L = p.mode == 0 ? p.length : p.A + p.A2;
+    const long long total = p.outer * L * p.inner;
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += stride) {
+      const long long i = e % p.inner, t = e / p.inner, j = t % L, ob = t / L;
+      if (p.mode == 0) o[e] = a[(ob * p.A + p.start + j) * p.inner + i];
+      else o[e] = j < p.A ? a[(ob * p.A + j) * p.inner + i] : b[(ob * p.A2 + j - p.A) * p.inner + i];
+    }
+  }
+  publish_late(p.out, o);
+}
+
 }  // namespace coex

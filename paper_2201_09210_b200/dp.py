@@ -54,9 +54,9 @@ from .tensor import OpKind, Tensor, shape_size
 
 R, S0, S1, PSUM, PAVG = "R", "S0", "S1", "P+", "P~"
 PARTIAL = (PSUM, PAVG)
-ELEMENTWISE = (OpKind.ADD, OpKind.SUB, OpKind.MUL)
+ELEMENTWISE = (OpKind.ADD, OpKind.SUB, OpKind.MUL, OpKind.DIV)
 LINEAR_UNARY = (OpKind.NEG,)
-NONLINEAR = (OpKind.RELU, OpKind.SIGMOID, OpKind.TANH, OpKind.LEAKY_RELU, OpKind.GELU)
+NONLINEAR = (OpKind.RELU, OpKind.SIGMOID, OpKind.TANH, OpKind.LEAKY_RELU, OpKind.GELU, OpKind.SQRT)
 # extension ops (C2 / C4): row-wise binary nonlinear ops keep the row sharding of their operands
 ROW_BINARY = (OpKind.RELU_GRAD, OpKind.LEAKY_RELU_GRAD, OpKind.BCE_TERM, OpKind.GELU_GRAD, OpKind.TO_INDEX)
 # C4 ops whose rows (or batch entries) are independent: sharded in, sharded out
@@ -138,6 +138,11 @@ class _Prop:
     def need_r(self, nid):
         """A consumer needs node ``nid`` replicated: schedule its all-reduce."""
         st = self.state.get(nid)
+        x = self.kind.get(nid)
+        if st in PARTIAL and x is not None and x.kind is OpKind.RESHAPE and not x.inputs[0].fed \
+                and len(x.inputs[0].cands) == 1 and self.state.get(x.inputs[0].cands[0]) == st:
+            # a reshape is a view with no buffer of its own: reduce its producer in place
+            return self.need_r(x.inputs[0].cands[0])
         if st in PARTIAL:
             self.reduce_at[nid] = st == PAVG
             return True
@@ -176,6 +181,18 @@ class _Prop:
                  OpKind.BN_DGAMMA, OpKind.SUM_ROWS, OpKind.EMBEDDING_DW, OpKind.LN_DGAMMA,
                  OpKind.CROSS_ENTROPY) or k in ROW_BINARY or k in ROW_WISE:
             return self._ext(x, ins)
+        if k in (OpKind.SLICE, OpKind.CONCAT, OpKind.SUM_AXIS):
+            # linear data movement / reduction along one axis: states pass through unless the
+            # axis is the sharded one
+            ax = x.attrs["dims"][0]
+            if any(st == S1 for st in ins) or (ax == 0 and any(st == S0 for st in ins)):
+                raise Unshardable(f"node {x.node_id}: {k.value} along the sharded axis")
+            if len(set(ins)) > 1:
+                raise Unshardable(f"node {x.node_id}: {k.value} of {ins}")
+            return ins[0]
+        if k is OpKind.DIV and ins[1] in PARTIAL:
+            self.needs_r_binding(x.inputs[1])        # a / P is not linear in P
+            ins = [ins[0], R]
         if k in ELEMENTWISE:
             a, b = ins
             scalar = [self._rank0(bb) for bb in x.inputs]
@@ -192,7 +209,7 @@ class _Prop:
                 return R
             if pa or pb:
                 other = b if pa else a
-                if k is OpKind.MUL and other == R:
+                if k in (OpKind.MUL, OpKind.DIV) and other == R:
                     return a if pa else b       # scaling by a replicated value is linear
                 self.needs_r_binding(x.inputs[0 if pa else 1])
                 a, b = (R, b) if pa else (a, R)
@@ -361,8 +378,13 @@ class _Prop:
 
     def run(self):
         for _ in range(8):
-            n_red = len(self.reduce_at)
-            if not self.walk(self.sp.body) and len(self.reduce_at) == n_red:
+            before = dict(self.reduce_at)
+            changed = self.walk(self.sp.body)
+            # a node marked for all-reduce on an earlier walk may have become replicated since
+            # (its own partial input got reduced in place for another consumer): its mark is
+            # stale -- all-reducing a replicated value would multiply it by the world size
+            self.reduce_at = {n: v for n, v in self.reduce_at.items() if self.state.get(n) in PARTIAL}
+            if not changed and self.reduce_at == before:
                 return
         raise Unshardable("sharding states did not converge")
 

@@ -36,7 +36,8 @@ from .trace_graph import (Diverged, External, Handle, LoopEnter, LoopExit,
 
 OP_BY_NAME = {k.value: k for k in OpKind if k not in (OpKind.READ_VAR, OpKind.ASSIGN_VAR)}
 CONV_NAMES = frozenset(("conv2d", "conv2d_t", "conv2d_dw", "embedding_dw", "conv2d_dx", "maxpool", "maxpool_grad",
-                        "avgpool", "avgpool_grad"))
+                        "avgpool", "avgpool_grad", "slice", "concat", "sum_axis"))
+DIMS_NAMES = frozenset(("embedding_dw", "slice", "concat", "sum_axis"))     # literal -> "dims" attr
 SCALE_NAMES = frozenset(("causal_softmax", "softmax_grad"))    # trailing host scale -> "value" attr
 
 
@@ -699,7 +700,7 @@ class Interp:
             # extension ops with tensor operands + a trailing shape literal ([k, s, p] / [vocab])
             ftens = [fx] + [self._c_expr(a, loc) for a in e.args[1:-1]]
             geo = self._c_shape(e.args[-1], loc)
-            akey = "dims" if name == "embedding_dw" else "conv"
+            akey = "dims" if name in DIMS_NAMES else "conv"
 
             def conv(ctx, env):
                 xs = [f(ctx, env) for f in ftens]

@@ -43,10 +43,11 @@ XOP = {OpKind.CONV2D, OpKind.CONV2D_T, OpKind.CONV2D_DW, OpKind.BATCHNORM, OpKin
        OpKind.BIAS_ADD, OpKind.BMM, OpKind.BMM_NT, OpKind.BMM_TN, OpKind.CAUSAL_SOFTMAX, OpKind.SOFTMAX_GRAD,
        OpKind.CROSS_ENTROPY, OpKind.CROSS_ENTROPY_GRAD, OpKind.REL_SKEW, OpKind.REL_UNSKEW,
        OpKind.CONV2D_DX, OpKind.MAXPOOL, OpKind.MAXPOOL_GRAD, OpKind.AVGPOOL, OpKind.AVGPOOL_GRAD,
-       OpKind.GLOBAL_AVGPOOL, OpKind.GLOBAL_AVGPOOL_GRAD}
+       OpKind.GLOBAL_AVGPOOL, OpKind.GLOBAL_AVGPOOL_GRAD, OpKind.SLICE, OpKind.CONCAT, OpKind.SUM_AXIS}
 EW_CODE = {OpKind.ADD: 0, OpKind.SUB: 1, OpKind.MUL: 2, OpKind.NEG: 3, OpKind.RELU: 4, OpKind.SIGMOID: 5,
            OpKind.TANH: 7, OpKind.LEAKY_RELU: 8, OpKind.RELU_GRAD: 9, OpKind.LEAKY_RELU_GRAD: 10,
-           OpKind.BCE_TERM: 11, OpKind.TO_INDEX: 12, OpKind.GELU_GRAD: 13, OpKind.GELU: 14}
+           OpKind.BCE_TERM: 11, OpKind.TO_INDEX: 12, OpKind.GELU_GRAD: 13, OpKind.GELU: 14,
+           OpKind.SQRT: 15, OpKind.DIV: 16}
 COMPUTE = {OpKind.MATMUL, OpKind.SUM, OpKind.MEAN, OpKind.TRANSPOSE} | set(EW_CODE) | XOP
 MAX_XIN = 3
 XOP_BN_BWD = 100          # fused batchnorm_dx + bn_dgamma + sum_rows (csrc COEX_BN_BWD_FUSED)

@@ -10,6 +10,7 @@ fetched loss, a native call mid-step (``clip``, the numpy stand-in), and a
 from __future__ import annotations
 
 import math
+import re
 
 from .dataset import DatasetSource
 from .tensor import Tensor
@@ -189,12 +190,13 @@ def c1_flops(batch=64, hidden=128, din=784, dout=10) -> int:
 
 
 def gpt2_program(steps: int = 20, batch: int = 8, seq: int = 1024, d: int = 768, heads: int = 12, layers: int = 12,
-                 vocab: int = 50257, lr: float = 0.01) -> str:
-    return _decoder_program(steps, batch, seq, d, heads, layers, vocab, lr, music=False)
+                 vocab: int = 50257, lr: float = 0.01, optimizer: str = "sgd") -> str:
+    src = _decoder_program(steps, batch, seq, d, heads, layers, vocab, lr, music=False)
+    return adam_program(src) if optimizer == "adam" else src
 
 
 def music_transformer_program(steps: int = 20, batch: int = 8, seq: int = 1024, d: int = 512, heads: int = 8,
-                              layers: int = 6, vocab: int = 388, lr: float = 0.01) -> str:
+                              layers: int = 6, vocab: int = 388, lr: float = 0.01, optimizer: str = "sgd") -> str:
     """BASELINE.json configs[4]: Music Transformer training on synthetic
     event sequences.
 
@@ -207,7 +209,48 @@ def music_transformer_program(steps: int = 20, batch: int = 8, seq: int = 1024, 
     *try/except* whose except-path (``native coin(1)``) drops the relative-table update of
     the step -- a SwitchCase with an assignment in one arm only.
     """
-    return _decoder_program(steps, batch, seq, d, heads, layers, vocab, lr, music=True)
+    src = _decoder_program(steps, batch, seq, d, heads, layers, vocab, lr, music=True)
+    return adam_program(src) if optimizer == "adam" else src
+
+
+_SGD_LINE = re.compile(r"^(\s*)(\w+) = sub\(\2, mul\((\w+), lrs\)\)$")
+_VAR_SHAPE = re.compile(r"^var (\w+) = .*?\[([0-9, ]*)\]")
+
+
+def adam_program(src: str, b1: float = 0.9, b2: float = 0.999, eps: float = 1e-8) -> str:
+    """Rewrite a program's SGD updates ``p = sub(p, mul(dp, lrs))`` into Adam (Kingma & Ba):
+    per parameter two state variables, ``m = b1*m + (1-b1)*g``, ``v = b2*v + (1-b2)*g^2``,
+    ``p -= lrs * (m / (1-b1^t)) / (sqrt(v / (1-b2^t)) + eps)`` -- bias corrections from two
+    rank-0 variables advanced every step; elementwise sqrt / div (extension ops).  The
+    arithmetic fuses into the planner's elementwise chains."""
+    shapes = {}
+    for ln in src.splitlines():
+        m = _VAR_SHAPE.match(ln.strip())
+        if m:
+            shapes[m.group(1)] = [int(t) for t in m.group(2).split(",") if t.strip()]
+    head, body = src.split("\nsteps ", 1)
+    decls = [head]
+    out = []
+    first = True
+    for ln in body.splitlines():
+        m = _SGD_LINE.match(ln)
+        if not m or m.group(2) not in shapes:
+            out.append(ln)
+            continue
+        ind, name, grad = m.groups()
+        if first:                                   # bias corrections, once per step
+            out += [f"{ind}adam_b1 = mul(adam_b1, {b1})", f"{ind}adam_b2 = mul(adam_b2, {b2})",
+                    f"{ind}let adam_c1 = sub(fill([], 1.0), adam_b1)",
+                    f"{ind}let adam_c2 = sub(fill([], 1.0), adam_b2)"]
+            decls += ["var adam_b1 = fill([], 1.0)", "var adam_b2 = fill([], 1.0)"]
+            first = False
+        shp = shapes[name]
+        decls += [f"var m_{name} = fill({shp}, 0.0)", f"var v_{name} = fill({shp}, 0.0)"]
+        out += [f"{ind}m_{name} = add(mul(m_{name}, {b1}), mul({grad}, {round(1 - b1, 12)}))",
+                f"{ind}v_{name} = add(mul(v_{name}, {b2}), mul(mul({grad}, {grad}), {round(1 - b2, 12)}))",
+                f"{ind}{name} = sub({name}, mul(div(div(m_{name}, adam_c1), "
+                f"add(sqrt(div(v_{name}, adam_c2)), {eps})), lrs))"]
+    return "\n".join(decls) + "\nsteps " + "\n".join(out) + "\n"
 
 
 def _decoder_program(steps, batch, seq, d, heads, layers, vocab, lr, music) -> str:

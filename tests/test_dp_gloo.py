@@ -25,6 +25,7 @@ BATCH = 8
 SMALL_C2 = dcgan_program(steps=6, batch=8, nz=6, ngf=4, ndf=4, img=16)
 SMALL_C4 = gpt2_program(steps=4, batch=BATCH, seq=8, d=16, heads=2, layers=2, vocab=23)
 SMALL_C3 = resnet_program(steps=14, batch=BATCH, img=32, width=2, blocks=(1, 1, 1, 1), classes=5, lr=1e-3)
+SMALL_C4_ADAM = gpt2_program(steps=4, batch=BATCH, seq=8, d=16, heads=2, layers=2, vocab=23, optimizer="adam")
 SMALL_C5 = music_transformer_program(steps=8, batch=BATCH, seq=8, d=16, heads=2, layers=2, vocab=23)
 
 
@@ -142,7 +143,7 @@ def test_dp2_dcgan_matches_global_batch(src, tol):
         np.testing.assert_array_equal(r0[1][k], r1[1][k])
 
 
-@pytest.mark.parametrize("src", [SMALL_C4, SMALL_C5], ids=["gpt2", "music_transformer"])
+@pytest.mark.parametrize("src", [SMALL_C4, SMALL_C4_ADAM, SMALL_C5], ids=["gpt2", "gpt2_adam", "music_transformer"])
 def test_dp2_gpt2_matches_global_batch(src):
     """C4 (GPT-2) / C5 (Music Transformer) data parallel at world size 2: sequences sharded
     through embeddings, layernorms, attention (batch = sequences x heads; C5's relative

@@ -10,7 +10,8 @@ import torch
 from oracle.cpu_backend import CpuBackend
 from oracle.kernels import execute_kernel
 from paper_2201_09210_b200.tensor import OpKind, Tensor
-from paper_2201_09210_b200.workloads import C3_SMALL, C5_SMALL, music_transformer_program, resnet_program
+from paper_2201_09210_b200.workloads import (C3_SMALL, C4_SMALL, C5_SMALL, gpt2_program, music_transformer_program,
+                                             resnet_program)
 from test_gpu_coexec import run
 
 RNG = np.random.default_rng(5)
@@ -146,3 +147,41 @@ def test_resnet_sdpoint_coexec_equals_imperative():
         assert np.array_equal(ref.vars[name].data, got.vars[name].data), name
     assert st.counters()[1] > 1 and st.shape_replays == 0
     assert len({dc.case_index for step in st.decision_log for dc in step}) >= 2
+
+
+def test_axis_ops_and_adam_elementwise():
+    """slice / concat / sum_axis against numpy (sum_axis bit-exact to a sequential loop),
+    sqrt / div IEEE (NaN / inf cases)."""
+    x = RNG.standard_normal((3, 5, 4))
+    y = RNG.standard_normal((3, 2, 4))
+    np.testing.assert_array_equal(k_(OpKind.SLICE, x, dims=(1, 1, 3)), x[:, 1:4, :])
+    np.testing.assert_array_equal(k_(OpKind.SLICE, x, dims=(2, 0, 0)), x[:, :, :0])
+    np.testing.assert_array_equal(k_(OpKind.CONCAT, x, y, dims=(1,)), np.concatenate([x, y], 1))
+    seq = x[:, 0, :] + 0.0
+    for j in range(1, 5):
+        seq = seq + x[:, j, :]
+    np.testing.assert_array_equal(k_(OpKind.SUM_AXIS, x, dims=(1,)), seq)
+    np.testing.assert_allclose(k_(OpKind.SUM_AXIS, x, dims=(0,)), x.sum(0), rtol=1e-14)
+    v = np.array([4.0, 0.0, -0.0, -1.0, np.inf, 2.0])
+    got = k_(OpKind.SQRT, v)
+    assert got[0] == 2.0 and got[1] == 0.0 and np.signbit(got[2]) and np.isnan(got[3]) and got[4] == np.inf
+    d = k_(OpKind.DIV, v, np.array(0.0))
+    assert d[0] == np.inf and np.isnan(d[1]) and d[3] == -np.inf
+    with pytest.raises(Exception):
+        k_(OpKind.SLICE, x, dims=(1, 3, 3))
+    with pytest.raises(Exception):
+        k_(OpKind.CONCAT, x, RNG.standard_normal((3, 2, 5)), dims=(1,))
+
+
+def test_adam_program_coexec_equals_imperative():
+    """GPT-2 at its parity size with the Adam rewrite (workloads.adam_program): co-execution
+    equals the imperative run bit for bit; the update differs from SGD's."""
+    src = gpt2_program(steps=6, optimizer="adam", **C4_SMALL)
+    assert "sqrt(div(v_wte, adam_c2))" in src
+    ref, _, _ = run(src, "imperative", CpuBackend())
+    got, st, _ = run(src, "coexec", CpuBackend())
+    assert ref.lines == got.lines and st.counters()[1] > 0
+    for name in ref.vars:
+        assert np.array_equal(ref.vars[name].data, got.vars[name].data), name
+    sgd, _, _ = run(gpt2_program(steps=6, **C4_SMALL), "imperative", CpuBackend())
+    assert sgd.lines[0] == ref.lines[0] and sgd.lines[1:] != ref.lines[1:]

@@ -55,7 +55,7 @@ def test_forced_dp_dcgan(prec, tol):
 
 
 @pytest.mark.parametrize("prec,tol", [("f64", 1e-10), ("bf16", 3e-2)])
-@pytest.mark.parametrize("cfg", ["c4", "c5"])
+@pytest.mark.parametrize("cfg", ["c4", "c4_adam", "c5"])
 def test_forced_dp_gpt2(prec, tol, cfg):
     """C4 (GPT-2) / C5 (Music Transformer) with a forced 1-rank sharding: all-reduce nodes
     for every parameter gradient and the loss in the pass graph (the cross-entropy gradient
@@ -63,9 +63,11 @@ def test_forced_dp_gpt2(prec, tol, cfg):
     import numpy as np
     from paper_2201_09210_b200.workloads import C4_SMALL, C5_SMALL, gpt2_program, music_transformer_program
     from test_gpu_coexec import run
-    src = gpt2_program(steps=8, **C4_SMALL) if cfg == "c4" else music_transformer_program(steps=8, **C5_SMALL)
+    src = (gpt2_program(steps=8, **C4_SMALL) if cfg == "c4" else
+           gpt2_program(steps=8, optimizer="adam", **C4_SMALL) if cfg == "c4_adam" else
+           music_transformer_program(steps=8, **C5_SMALL))
     ref, ref_st, _ = run(src, "coexec", CpuBackend())
-    be = B200Backend(precision=prec, dp=DPGroup(0, 1, (C4_SMALL if cfg == "c4" else C5_SMALL)["batch"], force=True))
+    be = B200Backend(precision=prec, dp=DPGroup(0, 1, (C5_SMALL if cfg == "c5" else C4_SMALL)["batch"], force=True))
     try:
         o = coexec.Orchestrator(lang.parse(src), SyntheticDataset(0), coexec.Mode.coexec, coexec.RunConfig(), be)
         got, st = o.run()

@@ -118,6 +118,10 @@ EW = [
     (OpKind.LEAKY_RELU_GRAD, {}, [Tensor(EDGE.shape, EDGE), rt(10)]),
     (OpKind.BCE_TERM, {}, [Tensor(EDGE.shape, EDGE), Tensor((), 1.0)]),
     (OpKind.BCE_TERM, {}, [rt(64, 1, scale=4.0), Tensor((), 0.0)]),
+    (OpKind.SQRT, {}, [Tensor(EDGE.shape, EDGE)]),
+    (OpKind.SQRT, {}, [Tensor((300,), np.abs(RNG.standard_normal(300)))]),
+    (OpKind.DIV, {}, [Tensor(EDGE.shape, EDGE), Tensor((), 3.0)]),
+    (OpKind.DIV, {}, [rt(37, 41), rt(37, 41)]),
 ]
 
 
@@ -167,7 +171,7 @@ def test_batchnorm_family(b200_factory, prec, tol, i):
 def test_elementwise_ext(b200_factory, prec, tol, i):
     kind, attrs, ins = EW[i]
     got, want = run(b200_factory(prec), kind, attrs, ins)
-    if prec == "f64" and kind in (OpKind.LEAKY_RELU, OpKind.RELU_GRAD, OpKind.LEAKY_RELU_GRAD):
+    if prec == "f64" and kind in (OpKind.LEAKY_RELU, OpKind.RELU_GRAD, OpKind.LEAKY_RELU_GRAD, OpKind.SQRT, OpKind.DIV):
         assert got.data.tobytes() == want.data.tobytes()
     else:
         assert nrel(got, want) <= tol

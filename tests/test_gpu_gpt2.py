@@ -20,6 +20,7 @@ from test_gpu_coexec import run
 pytestmark = pytest.mark.gpu
 
 SRC = gpt2_program(steps=5, **C4_SMALL)
+SRC_ADAM = gpt2_program(steps=5, optimizer="adam", **C4_SMALL)
 
 
 @pytest.fixture(scope="module")
@@ -39,6 +40,24 @@ def test_gpt2_parity(b200_factory, oracle_run, prec, tol):
     assert st.decision_log == ref_st.decision_log
     assert to_json_text(o.tg) == to_json_text(ref_o.tg)
     assert len(ref.lines) == len(got.lines)
+    for a, b in zip(ref.lines, got.lines):
+        assert math.isclose(float(a), float(b), rel_tol=tol), (a, b)
+    keys = sorted(ref.vars)
+    w = np.concatenate([ref.vars[k].data.ravel() for k in keys])
+    g = np.concatenate([got.vars[k].data.ravel() for k in keys])
+    assert np.linalg.norm(g - w) / np.linalg.norm(w) <= min(tol, 2e-2)
+
+
+@pytest.mark.parametrize("prec,tol", [("f64", 1e-10), ("bf16", 3e-2)])
+def test_gpt2_adam_parity(b200_factory, prec, tol):
+    """The Adam rewrite (sqrt / div elementwise, fused into chains) against the oracle."""
+    ref, ref_st, _ = run(SRC_ADAM, "coexec", CpuBackend())
+    be = b200_factory(prec, fresh=True)
+    try:
+        got, st, _ = run(SRC_ADAM, "coexec", be)
+    finally:
+        be.close()
+    assert st.counters() == ref_st.counters()
     for a, b in zip(ref.lines, got.lines):
         assert math.isclose(float(a), float(b), rel_tol=tol), (a, b)
     keys = sorted(ref.vars)

@@ -60,6 +60,13 @@ ROWS = [
     (OpKind.REL_SKEW, {}, [rt(1, 1)]),
     (OpKind.REL_UNSKEW, {}, [rt(2, 2, 64, 64)]),
     (OpKind.REL_UNSKEW, {}, [rt(4, 100, 100)]),
+    # general axis ops: bit-exact in every precision except sum_axis (fp32 accumulation)
+    (OpKind.SLICE, {"dims": (1, 3, 17)}, [rt(4, 30, 7)]),
+    (OpKind.SLICE, {"dims": (0, 2, 3)}, [rt(9, 5)]),
+    (OpKind.CONCAT, {"dims": (1,)}, [rt(4, 30, 7), rt(4, 2, 7)]),
+    (OpKind.CONCAT, {"dims": (2,)}, [rt(3, 5, 64), rt(3, 5, 64)]),
+    (OpKind.SUM_AXIS, {"dims": (1,)}, [rt(6, 300, 33)]),
+    (OpKind.SUM_AXIS, {"dims": (0,)}, [rt(1000, 17)]),
 ]
 
 
@@ -94,7 +101,8 @@ def test_bmm_tolerance(b200_factory, prec, tol, i):
 def test_row_ops(b200_factory, prec, tol, i):
     kind, attrs, ins = ROWS[i]
     got, want = run(b200_factory(prec), kind, attrs, ins)
-    if kind is OpKind.TO_INDEX or (kind in (OpKind.EMBEDDING, OpKind.REL_SKEW, OpKind.REL_UNSKEW) and prec == "f64"):
+    if kind is OpKind.TO_INDEX or (kind in (OpKind.EMBEDDING, OpKind.REL_SKEW, OpKind.REL_UNSKEW, OpKind.SLICE,
+                                            OpKind.CONCAT, OpKind.SUM_AXIS) and prec == "f64"):
         assert got.data.tobytes() == want.data.tobytes()
     else:
         assert nrel(got, want) <= tol
