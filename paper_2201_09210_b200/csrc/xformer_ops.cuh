@@ -235,7 +235,11 @@ __global__ void __launch_bounds__(256) k_layernorm(RowParams p) {
 #pragma unroll
         for (int j = 0; j < PER; ++j) {
           const long long c = lane + 32ll * j;
-          if (c < d) o[r * d + c] = (T)(((xv[j] - mean) * rstd) * (float)g[c] + (float)z[c]);
+          if (c < d) {
+            const T v = (T)(((xv[j] - mean) * rstd) * (float)g[c] + (float)z[c]);
+            o[r * d + c] = v;
+            if (p.shadow) p.shadow[r * d + c] = __float2bfloat16_rn((float)v);   // GEMM operand copy
+          }
         }
       } else {
         const T* dyr = z + r * d;
@@ -265,8 +269,11 @@ __global__ void __launch_bounds__(256) k_layernorm(RowParams p) {
     double mean, rstd;
     ln_row_stats(xr, p.d, lane, mean, rstd);
     if (MODE == 0) {
-      for (long long c = lane; c < p.d; c += 32)
-        o[r * p.d + c] = (T)((((double)xr[c] - mean) * rstd) * (double)g[c] + (double)z[c]);
+      for (long long c = lane; c < p.d; c += 32) {
+        const T v = (T)((((double)xr[c] - mean) * rstd) * (double)g[c] + (double)z[c]);
+        o[r * p.d + c] = v;
+        if (p.shadow) p.shadow[r * p.d + c] = __float2bfloat16_rn((float)v);
+      }
     } else {
       const T* dy = z + r * p.d;
       double m1 = 0.0, m2 = 0.0;

@@ -232,10 +232,25 @@ class Planner:
         # writes a bf16 copy, which those GEMMs read instead of converting the fp32 tensor
         self.shadow = {}
         if self.bf16:
+            def gemm_use(nid):
+                """nid's output is a MatMul operand (directly or through a folded transpose)."""
+                for c in consumers.get(nid, []):
+                    if c.kind is OpKind.MATMUL:
+                        return True
+                    if c.kind is OpKind.TRANSPOSE and c.node_id in folded:
+                        return True
+                return False
+
             for nid, x in ops.items():
-                if x.kind not in (OpKind.CAUSAL_SOFTMAX, OpKind.SOFTMAX_GRAD) or nid not in node_buf:
+                if x.kind not in (OpKind.CAUSAL_SOFTMAX, OpKind.SOFTMAX_GRAD, OpKind.LAYERNORM) or nid not in node_buf:
                     continue
                 if node_buf[nid][2] or shapes[nid][-1] % 8 or any(nid in s_ for s_ in multi):
+                    continue
+                if x.kind is OpKind.LAYERNORM:
+                    # layernorm outputs feed the q/k/v, MLP-in and LM-head GEMMs (and their
+                    # weight gradients through transposes): written once in bf16 by the producer
+                    if gemm_use(nid):
+                        self.shadow[nid] = new_buf(shape_size(shapes[nid]) * 2)
                     continue
                 if any(c.kind in (OpKind.BMM, OpKind.BMM_TN) and not c.inputs[0].fed and c.inputs[0].cands == (nid,)
                        for c in consumers.get(nid, [])):
