@@ -32,8 +32,11 @@ constexpr int TC_EPI_LD = 36;       // epilogue staging row pitch (floats): 32 c
 constexpr int TC_EPI_BYTES = 4 * 32 * TC_EPI_LD * 4;   // four epilogue warps x 32 rows
 // Narrow-N variants (convolution GEMMs have N = Cout in 64..512): BN in {64, 128, 256};
 // the stage count grows as the B tile shrinks so every variant keeps ~192 KB in flight.
-template <int BN> struct TcCfg {
-  static constexpr int STAGES = BN == 256 ? 4 : BN == 128 ? 6 : 8;
+// DUO: a shallow-pipeline variant small enough for two CTAs per SM (BN <= 128; two TMEM
+// accumulator pairs fit the 512 columns) -- for short-K GEMMs on under two waves of tiles,
+// where per-tile latency rather than operand bandwidth bounds the launch.
+template <int BN, bool DUO = false> struct TcCfg {
+  static constexpr int STAGES = DUO ? (BN == 64 ? 3 : 2) : BN == 256 ? 4 : BN == 128 ? 6 : 8;
   static constexpr int B_BYTES = BN * TC_BK * 2;
   static constexpr int SMEM = STAGES * (TC_A_BYTES + B_BYTES) + 1024 /*align*/ + 256 /*barriers, tmem slot*/ +
                                TC_EPI_BYTES;
@@ -254,11 +257,11 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 // convolution, A MN-major (weight gradient: M = (tap, channel), K = pixels).  B_MN: B stored
 // [K][N].  MN-major operands are loaded as 64 x 64 boxes and consumed through MN-major
 // descriptors, so no transposition pass is needed.
-template <int BN, int AMODE, bool B_MN>
-__global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc(const __grid_constant__ TcGemmParams p) {
+template <int BN, int AMODE, bool B_MN, bool DUO = false>
+__global__ void __launch_bounds__(TC_THREADS, DUO ? 2 : 1) k_gemm_tc(const __grid_constant__ TcGemmParams p) {
   COEX_PDL_ENTER();
-  constexpr int STAGES = TcCfg<BN>::STAGES;
-  constexpr int B_BYTES = TcCfg<BN>::B_BYTES;
+  constexpr int STAGES = TcCfg<BN, DUO>::STAGES;
+  constexpr int B_BYTES = TcCfg<BN, DUO>::B_BYTES;
   constexpr uint32_t TMEM_COLS = 2 * BN;            // two accumulator buffers
   constexpr bool A_MN = AMODE == 1 || AMODE == 3;
   stamp(p.ds, SK_MATMUL);

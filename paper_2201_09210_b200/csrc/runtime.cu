@@ -821,25 +821,34 @@ size_t matmul_split_ws(int64_t M, int64_t N, int64_t K) {
 
 // Appends the GEMM (and its split-K reduction) to L.  `ws` = fp32 split slices (splits > 1).
 // Kernel variants: AMODE 0/1 (2-D A, K- or MN-major) x B_MN, AMODE 2/3 (implicit conv) x B_MN.
-template <int BN>
+template <int BN, bool DUO = false>
 void* tc_fn(int amode, bool bmn) {
   switch (amode) {
-    case 0: return bmn ? (void*)k_gemm_tc<BN, 0, true> : (void*)k_gemm_tc<BN, 0, false>;
-    case 1: return bmn ? (void*)k_gemm_tc<BN, 1, true> : (void*)k_gemm_tc<BN, 1, false>;
-    case 2: return (void*)k_gemm_tc<BN, 2, true>;
-    default: return (void*)k_gemm_tc<BN, 3, true>;
+    case 0: return bmn ? (void*)k_gemm_tc<BN, 0, true, DUO> : (void*)k_gemm_tc<BN, 0, false, DUO>;
+    case 1: return bmn ? (void*)k_gemm_tc<BN, 1, true, DUO> : (void*)k_gemm_tc<BN, 1, false, DUO>;
+    case 2: return (void*)k_gemm_tc<BN, 2, true, DUO>;
+    default: return (void*)k_gemm_tc<BN, 3, true, DUO>;
   }
 }
-template <int BN>
+template <int BN, bool DUO = false>
 int tc_attr(int amode, bool bmn) {
   static bool done[8] = {false};
   const int i = amode * 2 + (bmn ? 1 : 0);
   if (!done[i]) {
-    CK(cudaFuncSetAttribute((const void*)tc_fn<BN>(amode, bmn), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            TcCfg<BN>::SMEM));
+    CK(cudaFuncSetAttribute((const void*)tc_fn<BN, DUO>(amode, bmn), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            TcCfg<BN, DUO>::SMEM));
     done[i] = true;
   }
   return COEX_OK;
+}
+// COEX_DUO: 0 never / 1 always (BN <= 128) / unset: the cost-model policy in tc_gemm_launches
+int duo_mode() {
+  static int m = -2;
+  if (m == -2) {
+    const char* e = getenv("COEX_DUO");
+    m = e ? atoi(e) : -1;
+  }
+  return m;
 }
 
 // Batched operands (bmm): 3-D maps {inner, rows, batch} over [batch][rows][pitch(inner)] bf16.
@@ -922,12 +931,29 @@ int tc_gemm_launches(coex_ctx* c, DevState* ds, void* a16, void* b16, int64_t M,
   gp.splits = t.splits;
   gp.raw = t.splits > 1 ? ws : raw;
   Launch& G = L[(*nL)++];
-  void* fn = t.bn == 64 ? tc_fn<64>(amode, b_mn) : t.bn == 128 ? tc_fn<128>(amode, b_mn) : tc_fn<256>(amode, b_mn);
   const int64_t items = ((M + TC_BM - 1) / TC_BM) * ((N + t.bn - 1) / t.bn) * t.splits *
                         (amode == 2 ? gp.cv.phases : 1) * (batch > 1 ? batch : 1);
-  G.set(fn, dim3((unsigned)(items < kNumSMs ? items : kNumSMs)), dim3(TC_THREADS), gp);
-  G.smem = t.bn == 64 ? TcCfg<64>::SMEM : t.bn == 128 ? TcCfg<128>::SMEM : TcCfg<256>::SMEM;
-  rc = t.bn == 64 ? tc_attr<64>(amode, b_mn) : t.bn == 128 ? tc_attr<128>(amode, b_mn) : tc_attr<256>(amode, b_mn);
+  // two CTAs per SM for short-K launches that do not fill two waves of single CTAs
+  const int64_t kblocks = (K + TC_BK - 1) / TC_BK / (t.splits > 0 ? t.splits : 1);
+  const int dm = duo_mode();
+  static int kmax = -1;
+  if (kmax < 0) {
+    const char* e = getenv("COEX_DUO_KMAX");
+    kmax = e ? atoi(e) : 32;
+  }
+  const bool duo = t.bn <= 128 && (dm == 1 || (dm < 0 && kblocks <= kmax));
+  void* fn;
+  if (duo) {
+    fn = t.bn == 64 ? tc_fn<64, true>(amode, b_mn) : tc_fn<128, true>(amode, b_mn);
+    G.set(fn, dim3((unsigned)(items < 2 * kNumSMs ? items : 2 * kNumSMs)), dim3(TC_THREADS), gp);
+    G.smem = t.bn == 64 ? TcCfg<64, true>::SMEM : TcCfg<128, true>::SMEM;
+    rc = t.bn == 64 ? tc_attr<64, true>(amode, b_mn) : tc_attr<128, true>(amode, b_mn);
+  } else {
+    fn = t.bn == 64 ? tc_fn<64>(amode, b_mn) : t.bn == 128 ? tc_fn<128>(amode, b_mn) : tc_fn<256>(amode, b_mn);
+    G.set(fn, dim3((unsigned)(items < kNumSMs ? items : kNumSMs)), dim3(TC_THREADS), gp);
+    G.smem = t.bn == 64 ? TcCfg<64>::SMEM : t.bn == 128 ? TcCfg<128>::SMEM : TcCfg<256>::SMEM;
+    rc = t.bn == 64 ? tc_attr<64>(amode, b_mn) : t.bn == 128 ? tc_attr<128>(amode, b_mn) : tc_attr<256>(amode, b_mn);
+  }
   if (rc) return rc;
   if (t.splits > 1) {
     SplitReduceParams r{};
