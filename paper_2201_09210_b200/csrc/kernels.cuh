@@ -24,6 +24,12 @@ namespace coex {
     asm volatile("griddepcontrol.wait;" ::: "memory");          \
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); \
   } while (0)
+// Cancellable entry (compute kernels): the cancel flag is loaded right after the dependency
+// wait but tested only once the kernel has loaded its operand pointers (res / pick_out), so
+// the flag's round trip overlaps theirs; every data access still follows the test.
+#define COEX_PDL_ENTER_CANCEL(ds)                               \
+  COEX_PDL_ENTER();                                             \
+  const bool coex_cancelled_ = skip(ds)
 
 constexpr int kMaxRank = 8;
 constexpr int kMaxDevVars = 1024;   // variables per context (runtime.cu kMaxVars)
@@ -276,12 +282,12 @@ struct EwParams {
 
 template <typename T>
 __global__ void __launch_bounds__(256) k_elementwise(EwParams p) {
-  COEX_PDL_ENTER();
+  COEX_PDL_ENTER_CANCEL(p.ds);
   stamp(p.ds, SK_EW);
-  if (skip(p.ds)) return;
   const T* a = res<T>(p.a);
   const T* b = ew_binary(p.op) ? res<T>(p.b) : nullptr;
   T* o = pick_out<T>(p.out, a, b);
+  if (coex_cancelled_) return;
   publish_early(p.out, o);
   count_op(p.ds);
   const long long n = p.n;
@@ -329,11 +335,11 @@ struct ReduceParams {
 // Parity path: one warp streams the data, lane 0 accumulates strictly in order.
 template <typename T>
 __global__ void __launch_bounds__(32) k_reduce_seq(ReduceParams p) {
-  COEX_PDL_ENTER();
+  COEX_PDL_ENTER_CANCEL(p.ds);
   stamp(p.ds, SK_REDUCE);
-  if (skip(p.ds)) return;
   const T* a = res<T>(p.a);
   T* o = pick_out<T>(p.out, a, nullptr);
+  if (coex_cancelled_) return;
   publish_early(p.out, o);
   count_op(p.ds);
   const int lane = threadIdx.x;
@@ -354,11 +360,11 @@ __global__ void __launch_bounds__(32) k_reduce_seq(ReduceParams p) {
 // Tolerance path (fp32 / bf16 contexts): warp-shuffle tree in double, one block.
 template <typename T>
 __global__ void __launch_bounds__(1024) k_reduce_tree(ReduceParams p) {
-  COEX_PDL_ENTER();
+  COEX_PDL_ENTER_CANCEL(p.ds);
   stamp(p.ds, SK_REDUCE);
-  if (skip(p.ds)) return;
   const T* a = res<T>(p.a);
   T* o = pick_out<T>(p.out, a, nullptr);
+  if (coex_cancelled_) return;
   publish_early(p.out, o);
   count_op(p.ds);
   __shared__ double part[32];
@@ -389,11 +395,11 @@ struct TransposeParams {
 
 template <typename T>
 __global__ void __launch_bounds__(256) k_transpose(TransposeParams p) {
-  COEX_PDL_ENTER();
+  COEX_PDL_ENTER_CANCEL(p.ds);
   stamp(p.ds, SK_TRANSPOSE);
-  if (skip(p.ds)) return;
   const T* a = res<T>(p.a);
   T* o = pick_out<T>(p.out, a, nullptr);
+  if (coex_cancelled_) return;
   publish_early(p.out, o);
   count_op(p.ds);
   const long long stride = (long long)gridDim.x * blockDim.x;
@@ -415,11 +421,11 @@ __global__ void __launch_bounds__(256) k_transpose(TransposeParams p) {
 // 32-bit index arithmetic per row (rank <= 4 outer axes).
 template <typename T>
 __global__ void __launch_bounds__(256) k_transpose_rows(TransposeParams p) {
-  COEX_PDL_ENTER();
+  COEX_PDL_ENTER_CANCEL(p.ds);
   stamp(p.ds, SK_TRANSPOSE);
-  if (skip(p.ds)) return;
   const T* a = res<T>(p.a);
   T* o = pick_out<T>(p.out, a, nullptr);
+  if (coex_cancelled_) return;
   publish_early(p.out, o);
   count_op(p.ds);
   constexpr int V = 16 / sizeof(T);
@@ -443,11 +449,11 @@ __global__ void __launch_bounds__(256) k_transpose_rows(TransposeParams p) {
 // 2-D transpose through a padded shared-memory tile (coalesced on both sides).
 template <typename T>
 __global__ void __launch_bounds__(256) k_transpose2d(TransposeParams p) {
-  COEX_PDL_ENTER();
+  COEX_PDL_ENTER_CANCEL(p.ds);
   stamp(p.ds, SK_TRANSPOSE);
-  if (skip(p.ds)) return;
   const T* a = res<T>(p.a);
   T* o = pick_out<T>(p.out, a, nullptr);
+  if (coex_cancelled_) return;
   publish_early(p.out, o);
   count_op(p.ds);
   __shared__ T tile[32][33];
@@ -488,12 +494,12 @@ struct MatmulParams {
 
 template <typename T, int BM, int BN, int BK, int RM, int RN, bool EXACT>
 __global__ void __launch_bounds__((BM / RM) * (BN / RN)) k_matmul_simt(MatmulParams p) {
-  COEX_PDL_ENTER();
+  COEX_PDL_ENTER_CANCEL(p.ds);
   stamp(p.ds, SK_MATMUL);
-  if (skip(p.ds)) return;
   const T* A = res<T>(p.a);
   const T* B = res<T>(p.b);
   T* C = pick_out<T>(p.out, A, B);
+  if (coex_cancelled_) return;
   publish_early(p.out, C);
   count_op(p.ds);
   constexpr int TX = BN / RN, TY = BM / RM, NT = TX * TY;
@@ -575,12 +581,12 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 
 template <typename T, int BM, int BN, int BK, int RM, int RN, bool EXACT, int STAGES>
 __global__ void __launch_bounds__((BM / RM) * (BN / RN)) k_matmul_pipe(MatmulParams p) {
-  COEX_PDL_ENTER();
+  COEX_PDL_ENTER_CANCEL(p.ds);
   stamp(p.ds, SK_MATMUL);
-  if (skip(p.ds)) return;
   const T* A0 = res<T>(p.a);
   const T* B0 = res<T>(p.b);
   T* C0 = pick_out<T>(p.out, A0, B0);
+  if (coex_cancelled_) return;
   publish_early(p.out, C0);
   if (blockIdx.y == 0) count_op(p.ds);
   const T* A = A0 + blockIdx.y * p.sa;
@@ -688,13 +694,13 @@ __global__ void __launch_bounds__((BM / RM) * (BN / RN)) k_matmul_pipe(MatmulPar
 // order (unrolled so loads run ahead of the dependent add chain).
 template <typename T>
 __global__ void __launch_bounds__(256) k_reduce_seq_smem(ReduceParams p) {
-  COEX_PDL_ENTER();
+  COEX_PDL_ENTER_CANCEL(p.ds);
   stamp(p.ds, SK_REDUCE);
-  if (skip(p.ds)) return;
   constexpr int CH = 2048;
   __shared__ T buf[2][CH];
   const T* a = res<T>(p.a);
   T* o = pick_out<T>(p.out, a, nullptr);
+  if (coex_cancelled_) return;
   publish_early(p.out, o);
   count_op(p.ds);
   double acc = 0.0;
@@ -822,9 +828,9 @@ __device__ __forceinline__ void chain_publish(const ChainParams& p) {
 
 template <typename T>
 __global__ void __launch_bounds__(256) k_chain(ChainParams p) {
-  COEX_PDL_ENTER();
+  COEX_PDL_ENTER_CANCEL(p.ds);
   stamp(p.ds, SK_FUSED);
-  if (skip(p.ds)) return;
+  if (coex_cancelled_) return;
   __shared__ ChainSmem<T> S;
   chain_load(p, S);
   if (p.late == nullptr && blockIdx.x == 0 && threadIdx.x == 0) chain_publish(p);
@@ -852,9 +858,9 @@ __global__ void __launch_bounds__(256) k_chain(ChainParams p) {
 // one thread, the tolerance path reduces with warp shuffles in double.
 template <typename T, bool EXACT>
 __global__ void __launch_bounds__(256) k_chain_reduce(ChainParams p) {
-  COEX_PDL_ENTER();
+  COEX_PDL_ENTER_CANCEL(p.ds);
   stamp(p.ds, SK_FUSED);
-  if (skip(p.ds)) return;
+  if (coex_cancelled_) return;
   constexpr int CH = 1024;
   __shared__ T vals[CH];
   __shared__ double part[8];
@@ -909,9 +915,9 @@ struct FillParams {
 };
 template <typename T>
 __global__ void __launch_bounds__(256) k_fill(FillParams p) {
-  COEX_PDL_ENTER();
-  if (skip(p.ds)) return;
+  COEX_PDL_ENTER_CANCEL(p.ds);
   T* o = (T*)p.out.buf[0];
+  if (coex_cancelled_) return;
   publish_early(p.out, o);
   const long long stride = (long long)gridDim.x * blockDim.x;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < p.n; i += stride) o[i] = (T)p.value;

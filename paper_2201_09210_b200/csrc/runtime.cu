@@ -781,12 +781,18 @@ TcPlan tc_plan(int64_t M, int64_t N, int64_t K, bool allow_split) {
     const char* e = getenv("COEX_FORCE_BN");     // tuning experiments only
     force_bn = e ? atoi(e) : 0;
   }
+  static int max_split = -1;
+  if (max_split < 0) {
+    const char* e = getenv("COEX_MAX_SPLIT");     // tuning experiments only
+    max_split = e ? atoi(e) : 32;
+  }
   const int bns[3] = {64, 128, 256};
   for (int bn : bns) {
     if (force_bn && bn != force_bn) continue;
     if (bn > 64 && N <= bn / 2) continue;
     const int64_t tiles = ((M + TC_BM - 1) / TC_BM) * ((N + bn - 1) / bn);
-    const int64_t smax = allow_split ? (nk / 2 < 32 ? (nk / 2 > 1 ? nk / 2 : 1) : 32) : 1;
+    int64_t smax = allow_split ? (nk / 2 < 32 ? (nk / 2 > 1 ? nk / 2 : 1) : 32) : 1;
+    if (smax > max_split) smax = max_split < 1 ? 1 : max_split;
     for (int64_t sp = 1; sp <= smax; ++sp) {
       // persistent CTAs: items per CTA run back to back, the epilogue of one item overlapping
       // the MMAs of the next (two TMEM accumulators)
@@ -1001,6 +1007,17 @@ int implicit_mask() {
   return m;
 }
 
+// smallest output pixel grid (per image) that takes the implicit-GEMM convolution paths
+// (COEX_IMPLICIT_MINPIX; conv2d_t uses a quarter of it on its input grid)
+int64_t implicit_minpix() {
+  static int64_t m = -1;
+  if (m < 0) {
+    const char* e = getenv("COEX_IMPLICIT_MINPIX");
+    m = e ? atoll(e) : 256;
+  }
+  return m;
+}
+
 // COEX_COL_BULK=0 keeps the register-pipelined column statistics (A/B measurement)
 bool col_bulk() {
   static int v = -1;
@@ -1055,7 +1072,7 @@ int build_xop_t(coex_ctx* c, const OpSpec& s, Launch* L, int* nL, size_t* ws_byt
       int bw, bh, bnn;
       // implicit GEMM pays off on the larger pixel grids (measured per op on the C2 shapes:
       // tools/cmp_implicit.py); small grids keep the materialised im2col operand
-      if (bf16 && (implicit_mask() & 1) && C % 64 == 0 && st <= 2 && Ho * Wo >= 256 &&
+      if (bf16 && (implicit_mask() & 1) && C % 64 == 0 && st <= 2 && Ho * Wo >= implicit_minpix() &&
           conv_blocks(Ho, Wo, 128, &bw, &bh, &bnn)) {
         // implicit GEMM: A gathered from bf16 NHWC x by 4-D TMA boxes (no im2col matrix)
         const TcPlan t = tc_plan(M, F, Kc, true);
@@ -1117,7 +1134,7 @@ int build_xop_t(coex_ctx* c, const OpSpec& s, Launch* L, int* nL, size_t* ws_byt
       int bw, bh, bnn;
       if (bf16 && (implicit_mask() & 4) && C % 64 == 0 && st >= 1 && k % st == 0 && k - 2 * pd == st &&
           Ho == (H - 1) * st - 2 * pd + k && Wo == (W - 1) * st - 2 * pd + k &&
-          H * W >= 64 && F >= 32 && conv_blocks(H, W, 128, &bw, &bh, &bnn)) {
+          H * W >= implicit_minpix() / 4 && F >= 32 && conv_blocks(H, W, 128, &bw, &bh, &bnn)) {
         // sub-pixel decomposition: st*st stride-1 implicit GEMMs (one per output phase) over the
         // bf16 NHWC input, epilogue scattering straight into the output -- no cols / col2im
         const int Tp = (int)(k / st), phases = (int)(st * st);
@@ -1261,7 +1278,7 @@ int build_xop_t(coex_ctx* c, const OpSpec& s, Launch* L, int* nL, size_t* ws_byt
       ip.N = N; ip.H = H; ip.W = W; ip.C = C; ip.Ho = Ho; ip.Wo = Wo;
       ip.k = (int)k; ip.s = (int)st; ip.p = (int)pd;
       int bw, bh, bnn;
-      if (bf16 && (implicit_mask() & 2) && C % 64 == 0 && st <= 2 && Ho * Wo >= 256 &&
+      if (bf16 && (implicit_mask() & 2) && C % 64 == 0 && st <= 2 && Ho * Wo >= implicit_minpix() &&
           conv_blocks(Ho, Wo, 64, &bw, &bh, &bnn)) {
         // implicit GEMM: A = im2col(x)^T gathered from bf16 NHWC x (64-pixel K blocks,
         // (tap, 64-channel) M halves, MN-major), B = dy [P][pitch(F)] MN-major

@@ -256,7 +256,10 @@ class Planner:
                        for c in consumers.get(nid, [])):
                     self.shadow[nid] = new_buf(shape_size(shapes[nid]) * 2)
         for s in list(multi):
-            multi[s] = new_cell(-1)
+            # start pointing at a candidate's buffer (same shape for every candidate): a
+            # cancelled pass that skipped every producer still hands its readers valid memory
+            init = next((node_buf[c][0] for c in sorted(s) if c in node_buf), -1)
+            multi[s] = new_cell(init)
         slot_buf: dict = {}
         slot_cell: dict = {}
         slot_rec: dict = {}
