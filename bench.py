@@ -29,8 +29,9 @@ pinned mapped memory).
   bracketing each step; synthetic inputs expanded on the device from the generator state
   (no host data), L2 flushed (256 MiB write) between steps outside the timed region.
 * ``e2e``: the same metric through the public API with host-resident inputs
-  (``InMemoryDataset``): every step copies the step's inputs host->device through the C-ABI
-  feed path and reads the printed loss back.
+  (``InMemoryDataset`` over pinned host memory, ``B200Backend.pin``): every step moves the
+  step's inputs host->device (the feed kernel reads them across the bus, converting to the
+  compute precision) and reads the printed loss back.
 * ``roofline``: every distinct op of one D+G step pair re-launched eagerly with the step's
   shapes, launch by launch, between CUDA events on the same stream (coex_exec_op_profile);
   kernels grouped by family; the family with the largest share of step time is the
@@ -561,6 +562,10 @@ def run_b200(args):
 
     # e2e: host-resident inputs through the public API (H2D each step, loss D2H)
     be2 = B200Backend(device=dev, precision=args.precision, dp=dp)
+    for name, lst in recs.items():        # per-step inputs live in pinned (registered) host memory
+        if not name.endswith("_init"):
+            for t in lst:
+                be2.pin(t.data)
     o2 = make_orch(src, InMemoryDataset(recs), be2)
     reach_coexec(o2)
     settle(o2)
@@ -597,7 +602,8 @@ def run_b200(args):
             "cpu_baseline": base,
             "e2e": {"value": round(world * args.steps / (e2e_max * 1e-3), 3), "unit": UNIT,
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 8,
-                    "data": "InMemoryDataset host tensors (f64), copied through coex_pass_feed each step"},
+                    "data": "InMemoryDataset host tensors (f64) in pinned host memory (coex_host_register), read "
+                            "in place by the feed kernel each step (coex_pass_feed_mapped)"},
             "gpu_launches": launches,
             "clocks": clocks,
             "stats": stats,

@@ -192,6 +192,13 @@ int coex_pass_loop(coex_prog* prog, int64_t loop_id, int32_t cont);
 int coex_pass_feed(coex_prog* prog, int64_t slot, int ndim, const int64_t* shape, const double* data);
 int coex_pass_feed_synth(coex_prog* prog, int64_t slot, uint64_t state, int ndim, const int64_t* shape);
 int coex_pass_feed_tensor(coex_prog* prog, int64_t slot, int64_t tensor_id);
+/* Host payload already in registered (pinned, mapped) memory: the feed kernel reads it in
+ * place over the bus -- no staging copy into the feed arena.  `data` must lie inside a range
+ * registered with coex_host_register. */
+int coex_pass_feed_mapped(coex_prog* prog, int64_t slot, int ndim, const int64_t* shape, const double* data);
+/* Page-lock and map a host range for coex_pass_feed_mapped (cudaHostRegister, read-only). */
+int coex_host_register(coex_ctx* ctx, void* ptr, int64_t bytes);
+int coex_host_unregister(coex_ctx* ctx, void* ptr);
 int coex_pass_fetch(coex_prog* prog, int64_t node_id, int64_t occurrence, double* out, int64_t cap,
                     int* ndim, int64_t* shape);
 int coex_pass_cancel(coex_prog* prog);

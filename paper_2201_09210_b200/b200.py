@@ -89,6 +89,9 @@ SIGNATURES = {
     "coex_pass_feed": (ctypes.c_int, [_P, _I64, ctypes.c_int, _I64P, _DP]),
     "coex_pass_feed_synth": (ctypes.c_int, [_P, _I64, ctypes.c_uint64, ctypes.c_int, _I64P]),
     "coex_pass_feed_tensor": (ctypes.c_int, [_P, _I64, _I64]),
+    "coex_pass_feed_mapped": (ctypes.c_int, [_P, _I64, ctypes.c_int, _I64P, _DP]),
+    "coex_host_register": (ctypes.c_int, [_P, ctypes.c_void_p, _I64]),
+    "coex_host_unregister": (ctypes.c_int, [_P, ctypes.c_void_p]),
     "coex_pass_fetch": (ctypes.c_int, [_P, _I64, _I64, _DP, _I64, _IP, _I64P]),
     "coex_pass_cancel": (ctypes.c_int, [_P]),
     "coex_pass_wait": (ctypes.c_int, [_P, ctypes.POINTER(CoexPassStats)]),
@@ -221,8 +224,9 @@ class B200Backend:
             for prog in getattr(self, "_programs", []):   # graphs, arenas and workspaces first
                 prog.close()
             self._programs = []
-            self.lib.coex_ctx_destroy(self.ctx)
+            self.lib.coex_ctx_destroy(self.ctx)      # also unregisters pinned host ranges
             self.ctx = None
+            self._pinned = []
 
     def kernel_count(self) -> int:
         return int(self.lib.coex_ctx_kernel_count(self.ctx))
@@ -349,6 +353,24 @@ class B200Backend:
 
     def var_shapes(self) -> dict:
         return dict(self._vshape)
+
+    # ------------------------------------------------------------ pinned host inputs
+    def pin(self, array) -> None:
+        """Page-lock and map a host f64 array (cudaHostRegister) so that feeding it in a pass
+        is one bus crossing read by the feed kernel instead of a staging copy plus a read.
+        The array must stay alive (the backend keeps a reference) and unchanged while passes
+        may read it."""
+        a = np.asarray(array)
+        if a.dtype != np.float64 or not a.flags["C_CONTIGUOUS"] or a.nbytes == 0:
+            raise CoexError("pin: a non-empty C-contiguous float64 array is required")
+        if not hasattr(self, "_pinned"):
+            self._pinned = []
+        _check(self.lib.coex_host_register(self.ctx, ctypes.c_void_p(a.ctypes.data), a.nbytes))
+        self._pinned.append((a.ctypes.data, a.nbytes, a))
+
+    def is_pinned(self, a) -> bool:
+        p, n = a.ctypes.data, a.nbytes
+        return any(b <= p and p + n <= b + m for b, m, _ in getattr(self, "_pinned", ()))
 
     def snapshot_vars(self) -> dict:
         if self.active is not None:
@@ -535,7 +557,11 @@ class B200Pass:
         else:
             data = np.ascontiguousarray(v.data, dtype=np.float64)
             self.keep.append(data)
-            self._do(self.lib.coex_pass_feed, code, len(shape), _shape_arr(shape), data.ctypes.data_as(_DP))
+            if self.be.is_pinned(data):      # registered host memory: read in place by the feed kernel
+                self._do(self.lib.coex_pass_feed_mapped, code, len(shape), _shape_arr(shape),
+                         data.ctypes.data_as(_DP))
+            else:
+                self._do(self.lib.coex_pass_feed, code, len(shape), _shape_arr(shape), data.ctypes.data_as(_DP))
 
     def fetch(self, nid: int, k: int) -> Tensor:
         if self.lazy:

@@ -74,7 +74,7 @@ struct DecEntry {
   int value;    // case index / continue flag
 };
 
-enum FeedType { FEED_SCALAR = 0, FEED_HOST = 1, FEED_SYNTH = 2, FEED_DEVICE = 3 };
+enum FeedType { FEED_SCALAR = 0, FEED_HOST = 1, FEED_SYNTH = 2, FEED_DEVICE = 3, FEED_MAPPED = 4 };
 
 struct FeedEntry {
   volatile unsigned long long seq;
@@ -85,7 +85,7 @@ struct FeedEntry {
   unsigned long long state;    // FEED_SYNTH generator state
   double scalar;               // FEED_SCALAR value
   unsigned long long off;      // FEED_HOST payload offset in the feed arena (doubles)
-  const void* dptr;            // FEED_DEVICE pointer (already in the context precision)
+  const void* dptr;            // FEED_DEVICE pointer (context precision) / FEED_MAPPED host f64 payload
 };
 
 struct FetchEntry {
@@ -1188,10 +1188,22 @@ __global__ void __launch_bounds__(kSynthThreads) k_feed_fill(FeedFillParams p) {
   if (skip(p.ds)) return;
   const int type = p.rec->type;
   T* o = (T*)p.buf;
-  if (type == FEED_HOST) {
-    const double* src = p.arena + p.rec->off;
+  if (type == FEED_HOST || type == FEED_MAPPED) {
+    // FEED_HOST: the staged payload in the mapped feed arena; FEED_MAPPED: the caller's own
+    // registered host buffer, read in place (one bus crossing, no host staging copy)
+    const double* src = type == FEED_HOST ? p.arena + p.rec->off : (const double*)p.rec->dptr;
     const long long stride = (long long)gridDim.x * blockDim.x;
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < p.n; i += stride) o[i] = (T)src[i];
+    if ((((uintptr_t)src) & 15) == 0) {
+      const long long n2 = p.n / 2;
+      for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n2; i += stride) {
+        const double2 v = ((const double2*)src)[i];
+        o[2 * i] = (T)v.x;
+        o[2 * i + 1] = (T)v.y;
+      }
+      if (blockIdx.x == 0 && threadIdx.x == 0 && (p.n & 1)) o[p.n - 1] = (T)src[p.n - 1];
+    } else {
+      for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < p.n; i += stride) o[i] = (T)src[i];
+    }
   } else if (type == FEED_SYNTH) {
     __shared__ T stage[kSynthThreads * kSynthRun];
     const unsigned long long s0 = p.rec->state;

@@ -127,6 +127,7 @@ dim3 grid_for(int64_t n, int threads = 256, int max_per_sm = 8) {
 }  // namespace
 
 struct coex_ctx {
+  std::vector<std::pair<char*, size_t>> pinned;   // coex_host_register ranges
   int device = 0;
   int prec = COEX_F64;
   size_t esize = 8;
@@ -1707,6 +1708,8 @@ int coex_ctx_create(int device, int precision, coex_ctx** out) {
 int coex_ctx_destroy(coex_ctx* c) {
   if (c == nullptr) return COEX_OK;
   cudaStreamSynchronize(c->stream);
+  for (auto& r : c->pinned) cudaHostUnregister(r.first);
+  c->pinned.clear();
   for (auto& kv : c->tensors) release(c, kv.second.buf);
   for (auto& v : c->vars) {
     release(c, v.t.buf);
@@ -2897,6 +2900,36 @@ static int push_feed(coex_prog* p, int64_t slot, int type, int ndim, const int64
 
 int coex_pass_feed(coex_prog* p, int64_t slot, int ndim, const int64_t* shape, const double* data) {
   return push_feed(p, slot, FEED_HOST, ndim, shape, data, 0, nullptr);
+}
+int coex_pass_feed_mapped(coex_prog* p, int64_t slot, int ndim, const int64_t* shape, const double* data) {
+  coex_ctx* c = p->ctx;
+  const char* d = (const char*)data;
+  const size_t bytes = (size_t)numel_of(ndim, shape) * sizeof(double);
+  for (const auto& r : c->pinned) {
+    if (d >= r.first && d + bytes <= r.first + r.second) {
+      void* dev = nullptr;
+      CK(cudaHostGetDevicePointer(&dev, r.first, 0));
+      return push_feed(p, slot, FEED_MAPPED, ndim, shape, nullptr, 0, (const char*)dev + (d - r.first));
+    }
+  }
+  return fail(COEX_INVALID, "coex_pass_feed_mapped: payload is not inside a registered host range");
+}
+int coex_host_register(coex_ctx* c, void* ptr, int64_t bytes) {
+  if (ptr == nullptr || bytes <= 0) return fail(COEX_INVALID, "coex_host_register: empty range");
+  CK(cudaHostRegister(ptr, (size_t)bytes, cudaHostRegisterMapped | cudaHostRegisterReadOnly));
+  c->pinned.emplace_back((char*)ptr, (size_t)bytes);
+  return COEX_OK;
+}
+int coex_host_unregister(coex_ctx* c, void* ptr) {
+  for (size_t i = 0; i < c->pinned.size(); ++i) {
+    if (c->pinned[i].first == (char*)ptr) {
+      cudaStreamSynchronize(c->stream);
+      CK(cudaHostUnregister(ptr));
+      c->pinned.erase(c->pinned.begin() + (long)i);
+      return COEX_OK;
+    }
+  }
+  return fail(COEX_INVALID, "coex_host_unregister: range not registered");
 }
 int coex_pass_feed_synth(coex_prog* p, int64_t slot, uint64_t state, int ndim, const int64_t* shape) {
   return push_feed(p, slot, FEED_SYNTH, ndim, shape, nullptr, state, nullptr);
