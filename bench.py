@@ -423,8 +423,11 @@ def workload_setup(args, world: int):
         gb = full["batch"] * world
         src = prog(steps=100_000, **dict(full, batch=gb))
         t = full["seq"]
-        recs = {"tokens": [Tensor((gb, t), rr.uniform(-1, 1, (gb, t))) for _ in range(2)],
-                "targets": [Tensor((gb, t), rr.uniform(-1, 1, (gb, t))) for _ in range(2)]}
+        # 64 distinct host batches: with only a couple the model memorises them within the run,
+        # the loss drops below the while loop's threshold and the e2e leg would time a retrace
+        nrec = 64
+        recs = {"tokens": [Tensor((gb, t), rr.uniform(-1, 1, (gb, t))) for _ in range(nrec)],
+                "targets": [Tensor((gb, t), rr.uniform(-1, 1, (gb, t))) for _ in range(nrec)]}
         import re
         for m in re.finditer(r'input\("(\w+_init)", \[([0-9, ]+)\]\)', prog(steps=1, **full)):
             shp = tuple(int(v) for v in m.group(2).split(","))
