@@ -232,6 +232,45 @@ __global__ void __launch_bounds__(256) k_im2col_bf16s(Im2colParams p) {
   }
 }
 
+// Few-channel bf16 im2col (C and k compile-time: the image layers, C = 3): one thread per
+// output row builds the whole k*k*C row in registers (no per-element index division) and
+// stores it as 16-byte units; the row pitch's tail is zeroed.
+template <int C, int K>
+__global__ void __launch_bounds__(256) k_im2col_small(Im2colParams p) {
+  COEX_PDL_ENTER_CANCEL(p.ds);
+  stamp(p.ds, SK_IM2COL);
+  if (coex_cancelled_) return;
+  const float* x = res<float>(p.x);
+  constexpr int KC = K * K * C, KP = (KC + 7) / 8 * 8;
+  const int H = (int)p.H, W = (int)p.W, Ho = (int)p.Ho, Wo = (int)p.Wo;
+  const long long M = p.N * p.Ho * p.Wo;
+  for (long long m = (long long)blockIdx.x * blockDim.x + threadIdx.x; m < M; m += (long long)gridDim.x * blockDim.x) {
+    const int ox = (int)(m % Wo);
+    const long long r = m / Wo;
+    const int oy = (int)(r % Ho);
+    const long long n = r / Ho;
+    __align__(16) __nv_bfloat16 v[KP];
+#pragma unroll
+    for (int ky = 0; ky < K; ++ky) {
+      const int iy = oy * p.s - p.p + ky;
+#pragma unroll
+      for (int kx = 0; kx < K; ++kx) {
+        const int ix = ox * p.s - p.p + kx;
+        const bool ok = iy >= 0 && iy < H && ix >= 0 && ix < W;
+        const float* src = x + ((n * H + (ok ? iy : 0)) * W + (ok ? ix : 0)) * C;
+#pragma unroll
+        for (int c = 0; c < C; ++c) v[(ky * K + kx) * C + c] = __float2bfloat16_rn(ok ? __ldg(src + c) : 0.f);
+      }
+    }
+#pragma unroll
+    for (int j = KC; j < KP; ++j) v[j] = __float2bfloat16_rn(0.f);
+    __nv_bfloat16* d = (__nv_bfloat16*)p.dst + m * p.ld;
+#pragma unroll
+    for (int q = 0; q < KP / 8; ++q) *(uint4*)(d + q * 8) = *(const uint4*)(v + q * 8);
+    for (long long j = KP; j < p.ld; j += 8) *(uint4*)(d + j) = make_uint4(0, 0, 0, 0);
+  }
+}
+
 // f64 parity path for the transposed operand is not needed: the SIMT GEMM reads the
 // row-major im2col buffer with trans_a (element-exact), so only float tiles go through smem.
 
@@ -289,6 +328,48 @@ __global__ void __launch_bounds__(256) k_col2im(Col2imParams p) {
 // only the (ky, kx) taps congruent with the output position are visited, ascending.  Blocks
 // own contiguous pixel ranges; threads keep their channel group and walk pixels
 // incrementally (no divisions in the loop).
+// Few-channel col2im (F compile-time, the image-producing conv2d_t): one thread per output
+// pixel accumulates its F channels over the taps in ascending (ky, kx) order from +0 -- the
+// same per-element order as k_col2im_v -- reading each tap's F floats contiguously.
+template <int F>
+__global__ void __launch_bounds__(256) k_col2im_px(Col2imParams p) {
+  COEX_PDL_ENTER_CANCEL(p.ds);
+  stamp(p.ds, SK_COL2IM);
+  float* o = pick_out<float>(p.out, res<float>(p.a), res<float>(p.b));
+  if (coex_cancelled_) return;
+  publish_early(p.out, o);
+  count_op(p.ds);
+  const float* cols = (const float*)p.cols;
+  const int k = p.k, s = p.s, pd = p.p, H = (int)p.H, W = (int)p.W, Ho = (int)p.Ho, Wo = (int)p.Wo;
+  const long long kkF = (long long)k * k * F;
+  const long long P = p.N * p.Ho * p.Wo;
+  for (long long pix = (long long)blockIdx.x * blockDim.x + threadIdx.x; pix < P;
+       pix += (long long)gridDim.x * blockDim.x) {
+    const int ox = (int)(pix % Wo);
+    const long long tq = pix / Wo;
+    const int oy = (int)(tq % Ho);
+    const long long n = tq / Ho;
+    float acc[F];
+#pragma unroll
+    for (int f = 0; f < F; ++f) acc[f] = 0.f;
+    const int ty0 = oy + pd, tx0 = ox + pd;
+    for (int ky = ty0 % s; ky < k; ky += s) {
+      const int iy = (ty0 - ky) / s;
+      if (ty0 - ky < 0 || iy >= H) continue;
+      for (int kx = tx0 % s; kx < k; kx += s) {
+        const int ix = (tx0 - kx) / s;
+        if (tx0 - kx < 0 || ix >= W) continue;
+        const float* src = cols + ((n * H + iy) * W + ix) * kkF + ((long long)ky * k + kx) * F;
+#pragma unroll
+        for (int f = 0; f < F; ++f) acc[f] = __fadd_rn(acc[f], __ldg(src + f));
+      }
+    }
+#pragma unroll
+    for (int f = 0; f < F; ++f) o[pix * F + f] = acc[f];
+  }
+  publish_late(p.out, o);
+}
+
 template <int V>
 __global__ void __launch_bounds__(256) k_col2im_v(Col2imParams p) {
   COEX_PDL_ENTER_CANCEL(p.ds);

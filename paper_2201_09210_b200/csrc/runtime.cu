@@ -1019,6 +1019,24 @@ int64_t implicit_minpix() {
   return m;
 }
 
+// narrowest conv2d_t output (channels) that takes the sub-pixel implicit path (COEX_CONVT_MINF)
+int64_t convt_min_f() {
+  static int64_t m = -1;
+  if (m < 0) {
+    const char* e = getenv("COEX_CONVT_MINF");
+    m = e ? atoll(e) : 32;
+  }
+  return m;
+}
+
+// few-channel im2col specialisations (image layers)
+void* im2col_small_fn(int64_t C, int64_t k) {
+  if (C == 3 && k == 4) return (void*)k_im2col_small<3, 4>;
+  if (C == 3 && k == 7) return (void*)k_im2col_small<3, 7>;
+  if (C == 3 && k == 3) return (void*)k_im2col_small<3, 3>;
+  return nullptr;
+}
+
 // COEX_COL_BULK=0 keeps the register-pipelined column statistics (A/B measurement)
 bool col_bulk() {
   static int v = -1;
@@ -1103,7 +1121,8 @@ int build_xop_t(coex_ctx* c, const OpSpec& s, Launch* L, int* nL, size_t* ws_byt
         if (C % 8 == 0 && M < (1ll << 31))
           L[(*nL)++].set((void*)k_im2col_bf16v, blocks_for_rows(M, Kc / 8), dim3(256), ip);
         else if (M < (1ll << 31))
-          L[(*nL)++].set((void*)k_im2col_bf16s, grid_for(M * ip.ld / 8), dim3(256), ip);
+          L[(*nL)++].set(im2col_small_fn(C, k) ? im2col_small_fn(C, k) : (void*)k_im2col_bf16s,
+                         im2col_small_fn(C, k) ? grid_for(M) : grid_for(M * ip.ld / 8), dim3(256), ip);
         else
           L[(*nL)++].set((void*)k_im2col<float, __nv_bfloat16>, grid_for(M * ip.ld / 8), dim3(256), ip);
         CvtParams q{};
@@ -1135,7 +1154,7 @@ int build_xop_t(coex_ctx* c, const OpSpec& s, Launch* L, int* nL, size_t* ws_byt
       int bw, bh, bnn;
       if (bf16 && (implicit_mask() & 4) && C % 64 == 0 && st >= 1 && k % st == 0 && k - 2 * pd == st &&
           Ho == (H - 1) * st - 2 * pd + k && Wo == (W - 1) * st - 2 * pd + k &&
-          H * W >= implicit_minpix() / 4 && F >= 32 && conv_blocks(H, W, 128, &bw, &bh, &bnn)) {
+          H * W >= implicit_minpix() / 4 && F >= convt_min_f() && conv_blocks(H, W, 128, &bw, &bh, &bnn)) {
         // sub-pixel decomposition: st*st stride-1 implicit GEMMs (one per output phase) over the
         // bf16 NHWC input, epilogue scattering straight into the output -- no cols / col2im
         const int Tp = (int)(k / st), phases = (int)(st * st);
@@ -1196,7 +1215,8 @@ int build_xop_t(coex_ctx* c, const OpSpec& s, Launch* L, int* nL, size_t* ws_byt
         if (F % 4 == 0 && N * Ho * Wo < (1ll << 31))
           L[(*nL)++].set((void*)k_col2im_v<4>, blocks_for_rows(N * Ho * Wo, F / 4), dim3(256), cp);
         else if (N * Ho * Wo < (1ll << 31))
-          L[(*nL)++].set((void*)k_col2im_v<1>, blocks_for_rows(N * Ho * Wo, F), dim3(256), cp);
+          L[(*nL)++].set(F == 3 ? (void*)k_col2im_px<3> : (void*)k_col2im_v<1>,
+                         F == 3 ? grid_for(N * Ho * Wo) : blocks_for_rows(N * Ho * Wo, F), dim3(256), cp);
         else
           L[(*nL)++].set((void*)k_col2im<float, float>, grid_for(N * Ho * Wo * F), dim3(256), cp);
         return COEX_OK;
@@ -1312,7 +1332,8 @@ int build_xop_t(coex_ctx* c, const OpSpec& s, Launch* L, int* nL, size_t* ws_byt
         if (C % 8 == 0 && P < (1ll << 31))
           L[(*nL)++].set((void*)k_im2col_bf16v, blocks_for_rows(P, Kc / 8), dim3(256), ip);
         else if (P < (1ll << 31))
-          L[(*nL)++].set((void*)k_im2col_bf16s, grid_for(P * ip.ld / 8), dim3(256), ip);
+          L[(*nL)++].set(im2col_small_fn(C, k) ? im2col_small_fn(C, k) : (void*)k_im2col_bf16s,
+                         im2col_small_fn(C, k) ? grid_for(P) : grid_for(P * ip.ld / 8), dim3(256), ip);
         else
           L[(*nL)++].set((void*)k_im2col<float, __nv_bfloat16>, grid_for(P * ip.ld / 8), dim3(256), ip);
         CvtParams q{};
