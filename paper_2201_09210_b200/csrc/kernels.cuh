@@ -826,18 +826,15 @@ __device__ __forceinline__ void chain_publish(const ChainParams& p) {
   }
 }
 
+// One chain over blocks [b, b + nb) of the launch (k_chain: the whole grid; k_chain_multi:
+// this chain's share of a grid that runs several independent chains).
 template <typename T>
-__global__ void __launch_bounds__(256) k_chain(ChainParams p) {
-  COEX_PDL_ENTER_CANCEL(p.ds);
-  stamp(p.ds, SK_FUSED);
-  if (coex_cancelled_) return;
-  __shared__ ChainSmem<T> S;
+__device__ __forceinline__ void chain_run(const ChainParams& p, ChainSmem<T>& S, long long b, long long nb) {
   chain_load(p, S);
-  if (p.late == nullptr && blockIdx.x == 0 && threadIdx.x == 0) chain_publish(p);
-  count_op(p.ds);
+  if (p.late == nullptr && b == 0 && threadIdx.x == 0) chain_publish(p);
   const int nops = p.nops, nout = p.nout;
-  const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < p.n; i += stride) {
+  const long long stride = nb * blockDim.x;
+  for (long long i = b * blockDim.x + threadIdx.x; i < p.n; i += stride) {
     chain_eval(S, nops, i);
     for (int j = 0; j < nout; ++j) S.out_buf[j][i] = S.r[S.out_reg[j]][threadIdx.x];
   }
@@ -845,12 +842,44 @@ __global__ void __launch_bounds__(256) k_chain(ChainParams p) {
     __syncthreads();
     if (threadIdx.x == 0) {
       __threadfence();
-      if (atomicAdd(p.late, 1u) == gridDim.x - 1) {
+      if (atomicAdd(p.late, 1u) == (unsigned)(nb - 1)) {
         chain_publish(p);
         *p.late = 0u;
       }
     }
   }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_chain(ChainParams p) {
+  COEX_PDL_ENTER_CANCEL(p.ds);
+  stamp(p.ds, SK_FUSED);
+  if (coex_cancelled_) return;
+  __shared__ ChainSmem<T> S;
+  count_op(p.ds);
+  chain_run(p, S, blockIdx.x, gridDim.x);
+}
+
+// Several independent elementwise chains in one launch (e.g. every parameter's SGD update
+// of a step): block ranges [off[j], off[j+1]) run chain j.  The planner groups only chains
+// that neither read what another publishes nor publish late.
+constexpr int kMaxMultiChain = 8;
+struct MultiChainParams {
+  DevState* ds;
+  int count;
+  int off[kMaxMultiChain + 1];
+  ChainParams c[kMaxMultiChain];
+};
+template <typename T>
+__global__ void __launch_bounds__(256) k_chain_multi(const __grid_constant__ MultiChainParams mp) {
+  COEX_PDL_ENTER_CANCEL(mp.ds);
+  stamp(mp.ds, SK_FUSED);
+  if (coex_cancelled_) return;
+  __shared__ ChainSmem<T> S;
+  count_op(mp.ds);
+  int j = 0;
+  while (j + 1 < mp.count && (int)blockIdx.x >= mp.off[j + 1]) ++j;
+  chain_run(mp.c[j], S, (long long)blockIdx.x - mp.off[j], (long long)(mp.off[j + 1] - mp.off[j]));
 }
 
 // Chain closed by SUM / MEAN: one block evaluates the chain in 2048-element

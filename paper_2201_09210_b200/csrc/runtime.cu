@@ -89,7 +89,7 @@ struct Launch {
   void* fn = nullptr;
   dim3 grid{1}, block{1};
   size_t smem = 0;
-  alignas(64) unsigned char params[2048];
+  alignas(64) unsigned char params[8192];     // k_chain_multi carries up to 8 chain programs
   size_t psize = 0;
   void* args[1];
   template <typename P>
@@ -2174,7 +2174,7 @@ int coex_var_rollback(coex_ctx* c) {
 namespace {
 
 enum PlanTag : int64_t { T_SEQ = 1, T_OP = 2, T_PTR = 3, T_FEED = 4, T_FETCH = 5, T_SWITCH = 6, T_WHILE = 7, T_CHAIN = 8,
-                         T_ALLREDUCE = 9, T_XOP = 10 };
+                         T_ALLREDUCE = 9, T_XOP = 10, T_MCHAIN = 11 };
 constexpr int64_t kPlanMagic = 0xC0E8B200;
 constexpr int64_t kPlanVersion = 2;
 
@@ -2249,6 +2249,47 @@ struct Builder {
       scratch_cap = cap;
     }
     return scratch;
+  }
+
+  // One chain program (T_CHAIN word after its tag) into q.
+  void parse_chain(ChainParams& q) {
+    memset(&q, 0, sizeof(q));
+    q.ds = c->d_state;
+    q.n = next();
+    q.red = (int)next();
+    q.red_reg = (int)next();
+    q.red_buf = buf(next());
+    q.red_npub = (int)next();
+    for (int i = 0; i < kChainPub; ++i) {
+      int64_t ci = next();
+      q.red_pub[i] = i < q.red_npub ? pubcell(ci) : nullptr;
+    }
+    const int64_t late = next();
+    q.nin = (int)next();
+    for (int i = 0; i < kChainIn; ++i) {
+      int64_t ci = next();
+      q.in[i] = (i < q.nin) ? operand(ci) : In{nullptr, nullptr, nullptr};
+      q.in_scalar[i] = (unsigned char)next();
+    }
+    q.nops = (int)next();
+    for (int i = 0; i < kChainOps; ++i) {
+      q.ops[i].op = (unsigned char)next();
+      q.ops[i].dst = (unsigned char)next();
+      q.ops[i].a = (unsigned char)next();
+      q.ops[i].b = (unsigned char)next();
+    }
+    q.nout = (int)next();
+    for (int j = 0; j < kChainOut; ++j) {
+      q.out_reg[j] = (unsigned char)next();
+      q.out_buf[j] = buf(next());
+      q.npub[j] = (unsigned char)next();
+      for (int i = 0; i < kChainPub; ++i) {
+        int64_t ci = next();
+        q.pub[j][i] = (j < q.nout && i < q.npub[j]) ? pubcell(ci) : nullptr;
+      }
+    }
+    if (q.nin > kChainIn || q.nops > kChainOps || q.nout > kChainOut) throw std::runtime_error("chain too wide");
+    q.late = late ? p->late + (n_late++) : nullptr;
   }
 
   int64_t next() {
@@ -2445,45 +2486,32 @@ struct Builder {
         }
         return COEX_OK;
       }
+      case T_MCHAIN: {                              // independent chains, one launch
+        const int64_t cnt = next();
+        if (cnt < 1 || cnt > kMaxMultiChain) throw std::runtime_error("bad multi-chain count");
+        MultiChainParams* mq = new MultiChainParams();
+        memset(mq, 0, sizeof(*mq));
+        mq->ds = c->d_state;
+        mq->count = (int)cnt;
+        int64_t blocks = 0;
+        for (int64_t j = 0; j < cnt; ++j) {
+          if (next() != T_CHAIN) throw std::runtime_error("multi-chain member is not a chain");
+          parse_chain(mq->c[j]);
+          if (mq->c[j].red) throw std::runtime_error("multi-chain member reduces");
+          mq->off[j] = (int)blocks;
+          blocks += grid_for(mq->c[j].n).x;
+        }
+        mq->off[cnt] = (int)blocks;
+        Launch L;
+        if (is_f64(c)) L.set((void*)k_chain_multi<double>, dim3((unsigned)blocks), dim3(256), *mq);
+        else L.set((void*)k_chain_multi<float>, dim3((unsigned)blocks), dim3(256), *mq);
+        delete mq;
+        p->n_compute++;
+        return add_kernel(g, prev, L);
+      }
       case T_CHAIN: {
         ChainParams q;
-        memset(&q, 0, sizeof(q));
-        q.ds = c->d_state;
-        q.n = next();
-        q.red = (int)next();
-        q.red_reg = (int)next();
-        q.red_buf = buf(next());
-        q.red_npub = (int)next();
-        for (int i = 0; i < kChainPub; ++i) {
-          int64_t ci = next();
-          q.red_pub[i] = i < q.red_npub ? pubcell(ci) : nullptr;
-        }
-        const int64_t late = next();
-        q.nin = (int)next();
-        for (int i = 0; i < kChainIn; ++i) {
-          int64_t ci = next();
-          q.in[i] = (i < q.nin) ? operand(ci) : In{nullptr, nullptr, nullptr};
-          q.in_scalar[i] = (unsigned char)next();
-        }
-        q.nops = (int)next();
-        for (int i = 0; i < kChainOps; ++i) {
-          q.ops[i].op = (unsigned char)next();
-          q.ops[i].dst = (unsigned char)next();
-          q.ops[i].a = (unsigned char)next();
-          q.ops[i].b = (unsigned char)next();
-        }
-        q.nout = (int)next();
-        for (int j = 0; j < kChainOut; ++j) {
-          q.out_reg[j] = (unsigned char)next();
-          q.out_buf[j] = buf(next());
-          q.npub[j] = (unsigned char)next();
-          for (int i = 0; i < kChainPub; ++i) {
-            int64_t ci = next();
-            q.pub[j][i] = (j < q.nout && i < q.npub[j]) ? pubcell(ci) : nullptr;
-          }
-        }
-        if (q.nin > kChainIn || q.nops > kChainOps || q.nout > kChainOut) throw std::runtime_error("chain too wide");
-        q.late = late ? p->late + (n_late++) : nullptr;
+        parse_chain(q);
         Launch L;
         if (q.red) {
           if (is_f64(c)) L.set((void*)k_chain_reduce<double, true>, dim3(1), dim3(256), q);

@@ -32,7 +32,8 @@ from .tensor import BMM_KINDS, CONV_ATTR_KINDS, CONV_KINDS, OpKind, flops_of, in
 
 MAGIC = 0xC0E8B200
 VERSION = 2
-T_SEQ, T_OP, T_PTR, T_FEED, T_FETCH, T_SWITCH, T_WHILE, T_CHAIN, T_ALLREDUCE, T_XOP = 1, 2, 3, 4, 5, 6, 7, 8, 9, 10
+T_SEQ, T_OP, T_PTR, T_FEED, T_FETCH, T_SWITCH, T_WHILE, T_CHAIN, T_ALLREDUCE, T_XOP, T_MCHAIN = 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11
+MAX_MCHAIN = 8            # chains per k_chain_multi launch (csrc kMaxMultiChain)
 PTR_ALIAS, PTR_READ_VAR, PTR_ASSIGN_VAR = 0, 1, 2
 MAX_RANK = 8
 MAX_PUB = 6
@@ -321,7 +322,9 @@ class Planner:
         self.consumers = consumers
         self._copies = {}
         self.n_chains = 0
+        self.n_mchains = 0
         self.chain_lates = 0
+        self._chain_meta = {}
 
         def feed_item(x):
             if x.slot in self.const_slots:
@@ -401,7 +404,7 @@ class Planner:
                     if b0 < 0 or pp:
                         raise NeedsReplicated(f"node {x.node_id} has no static buffer to all-reduce")
                     items.append([T_ALLREDUCE, b0, shape_size(shapes[x.node_id]), int(x.avg)])
-            return items
+            return self._group_chains(items) if self.fuse else items
 
         def seq(insts) -> list:
             items = emit(insts)
@@ -752,6 +755,41 @@ class Planner:
         flush()
         return segs
 
+    def _group_chains(self, items: list) -> list:
+        """Adjacent elementwise chains that neither read what another one publishes (cells,
+        variable overlay slots) nor reduce run as one k_chain_multi launch (T_MCHAIN) -- e.g.
+        every parameter update of a step; each keeps its own late-publication counter."""
+        out, group = [], []
+
+        def flush():
+            if len(group) == 1:
+                out.append(group[0])
+            elif group:
+                w = [T_MCHAIN, len(group)]
+                for g in group:
+                    w += g
+                out.append(w)
+                self.n_mchains += 1
+            group.clear()
+
+        for it in items:
+            meta = self._chain_meta.get(id(it))
+            if meta is None or meta[0] is not it or meta[3]:     # (ids of dropped words get reused)
+                flush()
+                out.append(it)
+                continue
+            ok = len(group) < MAX_MCHAIN
+            for g in group:
+                gm = self._chain_meta[id(g)]
+                if _conflicts(meta[1], gm[2]) or _conflicts(gm[1], meta[2]):
+                    ok = False
+                    break
+            if not ok:
+                flush()
+            group.append(it)
+        flush()
+        return out
+
     def _chain_item(self, run, shapes, in_cell, node_buf, pubs, multi, n_compute) -> list:
         red = run[-1] if run[-1].kind in (OpKind.SUM, OpKind.MEAN) else None
         ew = run[:-1] if red is not None else run
@@ -812,6 +850,7 @@ class Planner:
         w += [len(outs)]
         for reg, buf, p in outs + [(0, -1, [])] * (CHAIN_OUT - len(outs)):
             w += [reg, buf, len(p)] + list(p) + [0] * (CHAIN_PUB - len(p))
+        self._chain_meta[id(w)] = (w, [c for c, _ in inputs], sorted(pub_cells), red is not None)
         return w
 
     def _must_store(self, nid, run, pos) -> bool:
