@@ -816,6 +816,8 @@ struct BnApplyParams {
   long long n, C;
   int dx;                    // 0: y = ((x-mean)*rstd)*g + b; 1: dx = (dy - m(dy) - xhat*m(dy*xhat)) * (g*rstd)
   Out out;
+  int act;                   // >= 0: also write act(y) (EW_RELU / EW_LRELU) to out2
+  Out out2;
 };
 
 template <typename T>
@@ -826,8 +828,10 @@ __global__ void __launch_bounds__(256) k_bn_apply(BnApplyParams p) {
   const T* g = res<T>(p.g);
   const T* z = res<T>(p.third);
   T* o = pick_out<T>(p.out, x, g);
+  T* o2 = p.act >= 0 ? pick_out<T>(p.out2, x, g) : nullptr;
   if (coex_cancelled_) return;
   publish_early(p.out, o);
+  if (o2) publish_early(p.out2, o2);
   count_op(p.ds);
   const long long stride = (long long)gridDim.x * blockDim.x;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < p.n; i += stride) {
@@ -838,8 +842,10 @@ __global__ void __launch_bounds__(256) k_bn_apply(BnApplyParams p) {
     if (!p.dx) r = xhat * (double)g[c] + (double)z[c];
     else r = (((double)z[i] - st[2]) - xhat * st[3]) * ((double)g[c] * st[1]);
     o[i] = (T)r;
+    if (o2) o2[i] = ew_apply(p.act, (T)r, (T)0);
   }
   publish_late(p.out, o);
+  if (o2) publish_late(p.out2, o2);
 }
 
 // Vectorised apply (float, C % 4 == 0): per-channel affine coefficients in shared memory,
@@ -853,8 +859,10 @@ __global__ void __launch_bounds__(256) k_bn_apply_v4(BnApplyParams p) {
   const float* g = res<float>(p.g);
   const float* z = res<float>(p.third);
   float* o = pick_out<float>(p.out, x, g);
+  float* o2 = p.act >= 0 ? pick_out<float>(p.out2, x, g) : nullptr;
   if (coex_cancelled_) return;
   publish_early(p.out, o);
+  if (o2) publish_early(p.out2, o2);
   count_op(p.ds);
   const int C = (int)p.C;
   for (int c = threadIdx.x; c < C; c += blockDim.x) {
@@ -890,8 +898,14 @@ __global__ void __launch_bounds__(256) k_bn_apply_v4(BnApplyParams p) {
       r.w = fmaf(gv.w, coef[c + 3], fmaf(xv.w, coef[C + c + 3], coef[2 * C + c + 3]));
     }
     ((float4*)o)[u] = r;
+    if (o2) {
+      const int a = p.act;
+      ((float4*)o2)[u] = make_float4(ew_apply(a, r.x, 0.f), ew_apply(a, r.y, 0.f), ew_apply(a, r.z, 0.f),
+                                     ew_apply(a, r.w, 0.f));
+    }
   }
   publish_late(p.out, o);
+  if (o2) publish_late(p.out2, o2);
 }
 
 // ------------------------------------------------------------------ pooling (config C3)

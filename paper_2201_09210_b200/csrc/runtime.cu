@@ -545,8 +545,11 @@ struct OpSpec {
 // Plan-only kind: batchnorm_dx + bn_dgamma + sum_rows over the same (x, dy) fused into one
 // column-statistics pass (planner.py _bn_bwd_groups); three outputs dx, dgamma, dbeta.
 constexpr int kBnBwdFused = 100;
+// Plan-only kind: batchnorm whose apply pass also writes relu / leaky_relu of its output
+// (planner.py _bn_act_pairs; attr dims[0] = the activation's EW code; second output out2).
+constexpr int kBnAct = 101;
 bool is_ext_compute(int kind) {
-  return (kind >= COEX_CONV2D && kind <= COEX_SUM_ROWS) || kind == kBnBwdFused ||
+  return (kind >= COEX_CONV2D && kind <= COEX_SUM_ROWS) || kind == kBnBwdFused || kind == kBnAct ||
          (kind >= COEX_EMBEDDING && kind <= COEX_GLOBAL_AVGPOOL_GRAD && kind != COEX_GELU && kind != COEX_GELU_GRAD) ||
          (kind >= COEX_SLICE && kind <= COEX_SUM_AXIS);
 }
@@ -1355,7 +1358,8 @@ int build_xop_t(coex_ctx* c, const OpSpec& s, Launch* L, int* nL, size_t* ws_byt
       simt_matmul_launch<T>(c, mp, &L[(*nL)++]);
       return COEX_OK;
     }
-    case COEX_BATCHNORM: case COEX_BATCHNORM_DX: case COEX_BN_DGAMMA: case COEX_SUM_ROWS: case kBnBwdFused: {
+    case COEX_BATCHNORM: case COEX_BATCHNORM_DX: case COEX_BN_DGAMMA: case COEX_SUM_ROWS: case kBnBwdFused:
+    case kBnAct: {
       const int64_t C = s.in_shape[0][s.in_ndim[0] - 1];
       const int64_t Rw = numel_of(s.in_ndim[0], s.in_shape[0]) / C;
       if (s.kind == COEX_SUM_ROWS && (C > 1024 || (!is_f64(c) && Rw >= 4096 && C >= 256))) {
@@ -1425,7 +1429,7 @@ int build_xop_t(coex_ctx* c, const OpSpec& s, Launch* L, int* nL, size_t* ws_byt
         L[(*nL)++].smem = bulk_smem;
         return COEX_OK;
       }
-      cp.mode = s.kind == COEX_BATCHNORM ? COL_BN : COL_BN_DX;
+      cp.mode = (s.kind == COEX_BATCHNORM || s.kind == kBnAct) ? COL_BN : COL_BN_DX;
       if (s.kind == COEX_BATCHNORM_DX || s.kind == kBnBwdFused) cp.dy = s.in[2];
       cp.out = Out{};
       if (s.kind == kBnBwdFused) {
@@ -1437,7 +1441,9 @@ int build_xop_t(coex_ctx* c, const OpSpec& s, Launch* L, int* nL, size_t* ws_byt
       L[(*nL)++].smem = bulk_smem;
       BnApplyParams ap{};
       ap.ds = s.ds; ap.x = s.in[0]; ap.g = s.in[1]; ap.third = s.in[2]; ap.stats = cp.stats;
-      ap.n = n; ap.C = C; ap.dx = s.kind != COEX_BATCHNORM; ap.out = s.out;
+      ap.n = n; ap.C = C; ap.dx = s.kind != COEX_BATCHNORM && s.kind != kBnAct; ap.out = s.out;
+      ap.act = s.kind == kBnAct ? (int)s.attr_dims[0] : -1;
+      if (s.kind == kBnAct) ap.out2 = s.out2;
       if (v4) {
         L[*nL].set((void*)k_bn_apply_v4, grid_for(n / 4), dim3(256), ap);
         L[(*nL)++].smem = (size_t)3 * C * sizeof(float);
@@ -2459,6 +2465,8 @@ struct Builder {
         if (s.kind == kBnBwdFused) {
           read_out(s.out2);
           read_out(s.out3);
+        } else if (s.kind == kBnAct) {
+          read_out(s.out2);
         }
         s.shadow = buf(next());
         for (int i = 0; i < kMaxIn; ++i) s.in_shadow[i] = buf(next());

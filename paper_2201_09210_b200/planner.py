@@ -52,6 +52,7 @@ EW_CODE = {OpKind.ADD: 0, OpKind.SUB: 1, OpKind.MUL: 2, OpKind.NEG: 3, OpKind.RE
 COMPUTE = {OpKind.MATMUL, OpKind.SUM, OpKind.MEAN, OpKind.TRANSPOSE} | set(EW_CODE) | XOP
 MAX_XIN = 3
 XOP_BN_BWD = 100          # fused batchnorm_dx + bn_dgamma + sum_rows (csrc COEX_BN_BWD_FUSED)
+XOP_BN_ACT = 101          # batchnorm also writing relu / leaky_relu of its output (csrc kBnAct)
 CHAIN_IN, CHAIN_OPS, CHAIN_OUT, CHAIN_PUB, CHAIN_REGS = 8, 16, 8, 4, 16
 
 
@@ -323,6 +324,7 @@ class Planner:
         self._copies = {}
         self.n_chains = 0
         self.n_mchains = 0
+        self._act_for = {}
         self.chain_lates = 0
         self._chain_meta = {}
 
@@ -343,6 +345,10 @@ class Planner:
                 self._copies = saved
 
         def emit_list(insts, items) -> list:
+            act_of = self._bn_act_pairs(insts) if (self.fuse and self.bf16) else {}
+            if act_of:
+                gone = {a.node_id for a in act_of.values()}
+                insts = [y for y in insts if not (isinstance(y, ExecOp) and y.node_id in gone)]
             bn_groups, bn_skip = self._bn_bwd_groups(insts) if self.fuse else ({}, set())
             if self.fuse:
                 segs = self._segments(insts, shapes, folded)
@@ -505,6 +511,35 @@ class Planner:
         self._invalidate(pubs[nid])
         return [word]
 
+    def _bn_act_pairs(self, insts) -> dict:
+        """batchnorm -> relu / leaky_relu of its output in the same instruction list: the
+        normalisation kernel also writes the activation (one pass over the data instead of
+        two, one launch less).  The activation must read the batchnorm output as its only
+        candidate and be a plain stored node (not fetched, merged, pinned, folded or
+        self-dependent); the fused op publishes both nodes at the batchnorm's position."""
+        multi_nodes = {n for s_ in self._multi_sets() for n in s_}
+        banned = set(self.sp.fetch_nodes) | multi_nodes | set(self.force_store) | set(self.folded_assigns.values())
+        pos = {x.node_id: i for i, x in enumerate(insts) if isinstance(x, ExecOp)}
+        out = {}
+        taken = set()
+        for x in insts:
+            if not isinstance(x, ExecOp) or x.kind not in (OpKind.RELU, OpKind.LEAKY_RELU):
+                continue
+            b = x.inputs[0]
+            if b.fed or len(b.cands) != 1 or x.node_id in banned:
+                continue
+            bn = self.ops.get(b.cands[0])
+            if bn is None or bn.kind is not OpKind.BATCHNORM or bn.node_id in banned or bn.node_id in taken:
+                continue
+            if bn.node_id not in pos or pos[bn.node_id] > pos[x.node_id]:
+                continue
+            if any((not bb.fed) and x.node_id in bb.cands for bb in x.inputs):
+                continue
+            out[bn.node_id] = x
+            taken.add(bn.node_id)
+        self._act_for.update(out)
+        return out
+
     def _bn_bwd_groups(self, insts):
         """Batch-norm backward triples in one instruction list -- batchnorm_dx(x, g, dy),
         bn_dgamma(x, dy), sum_rows(dy) with identical x / dy bindings -- run as ONE column-
@@ -589,12 +624,20 @@ class Planner:
         if x.kind in CONV_KINDS or x.kind in BMM_KINDS:
             flops[0] += flops_of(x.kind, in_shapes, x.attrs)
         out_shape = shapes[nid]
-        word = [T_XOP, x.kind.code, nid, len(cells)] + cells + [-1] * (MAX_XIN - len(cells))
+        act = self._act_for.get(nid)
+        kind_code = x.kind.code
+        if act is not None:                     # batchnorm + activation in one apply pass
+            kind_code = XOP_BN_ACT
+            attr = [EW_CODE[act.kind]]
+        word = [T_XOP, kind_code, nid, len(cells)] + cells + [-1] * (MAX_XIN - len(cells))
         for s_ in in_shapes + [()] * (MAX_XIN - len(in_shapes)):
             word += [len(s_)] + _pad(s_)
         word += [len(out_shape)] + _pad(out_shape)
         word += [len(attr)] + _pad(attr) + [_f64_bits(float(x.attrs.get("value", x.attrs.get("rows", 0.0))))]
         word += out_words(nid, late)
+        if act is not None:
+            word += out_words(act.node_id, _conflicts(cells, pubs[act.node_id]))
+            self._invalidate(pubs[act.node_id])
         word += self._shadow_words(x, cells, in_shapes)
         self._invalidate(pubs[nid])
         if nid in self.shadow:                  # this node's bf16 shadow is a valid copy from here on
