@@ -1022,6 +1022,16 @@ int64_t implicit_minpix() {
   return m;
 }
 
+// smallest conv2d_t input grid (per image) on the sub-pixel implicit path (COEX_CONVT_MINPIX)
+int64_t convt_minpix() {
+  static int64_t m = -1;
+  if (m < 0) {
+    const char* e = getenv("COEX_CONVT_MINPIX");
+    m = e ? atoll(e) : implicit_minpix() / 4;
+  }
+  return m;
+}
+
 // narrowest conv2d_t output (channels) that takes the sub-pixel implicit path (COEX_CONVT_MINF)
 int64_t convt_min_f() {
   static int64_t m = -1;
@@ -1157,7 +1167,7 @@ int build_xop_t(coex_ctx* c, const OpSpec& s, Launch* L, int* nL, size_t* ws_byt
       int bw, bh, bnn;
       if (bf16 && (implicit_mask() & 4) && C % 64 == 0 && st >= 1 && k % st == 0 && k - 2 * pd == st &&
           Ho == (H - 1) * st - 2 * pd + k && Wo == (W - 1) * st - 2 * pd + k &&
-          H * W >= implicit_minpix() / 4 && F >= convt_min_f() && conv_blocks(H, W, 128, &bw, &bh, &bnn)) {
+          H * W >= convt_minpix() && F >= convt_min_f() && conv_blocks(H, W, 128, &bw, &bh, &bnn)) {
         // sub-pixel decomposition: st*st stride-1 implicit GEMMs (one per output phase) over the
         // bf16 NHWC input, epilogue scattering straight into the output -- no cols / col2im
         const int Tp = (int)(k / st), phases = (int)(st * st);
@@ -1383,6 +1393,12 @@ int build_xop_t(coex_ctx* c, const OpSpec& s, Launch* L, int* nL, size_t* ws_byt
       // tolerance modes accumulate with fp64 atomics (no merge of per-block partials)
       const bool atomic = !is_f64(c);
       int64_t G = n / 16384;
+      static int64_t gmin = -1;                      // COEX_COL_MINBLOCKS (tuning experiments)
+      if (gmin < 0) {
+        const char* e = getenv("COEX_COL_MINBLOCKS");
+        gmin = e ? atoll(e) : 0;
+      }
+      if (atomic && G < gmin) G = gmin;
       if (!atomic && G > 32768 / C) G = 32768 / C;
       if (G > kNumSMs * 2) G = kNumSMs * 2;
       if (G > R) G = R;
