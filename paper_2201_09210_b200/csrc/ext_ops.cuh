@@ -58,9 +58,8 @@ template <> __device__ __forceinline__ __nv_bfloat16 cvt_to<__nv_bfloat16>(doubl
 // of one (ky, kx) run are contiguous channels).  bf16 destinations store 8 per thread.
 template <typename Tin, typename Tout>
 __global__ void __launch_bounds__(256) k_im2col(Im2colParams p) {
-  COEX_PDL_ENTER_CANCEL(p.ds);
+  COEX_PDL_ENTER();
   stamp(p.ds, SK_IM2COL);
-  if (coex_cancelled_) return;
   const Tin* x = res<Tin>(p.x);
   const long long M = p.N * p.Ho * p.Wo;
   const long long stride = (long long)gridDim.x * blockDim.x;
@@ -107,9 +106,8 @@ __global__ void __launch_bounds__(256) k_im2col(Im2colParams p) {
 // of output pixels; a thread keeps its (ky, kx, channel-group) fixed and walks pixels with
 // incremental (n, oy, ox) arithmetic -- no divisions in the loop.
 __global__ void __launch_bounds__(256) k_im2col_bf16v(Im2colParams p) {
-  COEX_PDL_ENTER_CANCEL(p.ds);
+  COEX_PDL_ENTER();
   stamp(p.ds, SK_IM2COL);
-  if (coex_cancelled_) return;
   const float* x = res<float>(p.x);
   const int C8 = (int)(p.C / 8), k = p.k, H = (int)p.H, W = (int)p.W, Ho = (int)p.Ho, Wo = (int)p.Wo;
   const int Q = k * k * C8;                         // 16-byte units per row (ld == Kc)
@@ -154,9 +152,8 @@ __global__ void __launch_bounds__(256) k_im2col_bf16v(Im2colParams p) {
 // 64 m x 32 kk tiles; each thread loads float4 runs of channels (8 threads per pixel row)
 // and the tile is written back along pixels as bf16 pairs.
 __global__ void __launch_bounds__(256) k_im2col_bf16t(Im2colParams p) {
-  COEX_PDL_ENTER_CANCEL(p.ds);
+  COEX_PDL_ENTER();
   stamp(p.ds, SK_IM2COL);
-  if (coex_cancelled_) return;
   const float* x = res<float>(p.x);
   __shared__ float tile[64][33];
   const int t = threadIdx.x;
@@ -200,9 +197,8 @@ __global__ void __launch_bounds__(256) k_im2col_bf16t(Im2colParams p) {
 // Scalar bf16 im2col for C % 8 != 0 (e.g. the 3-channel image layer): one thread = one
 // 8-element unit of a row, 32-bit index arithmetic.
 __global__ void __launch_bounds__(256) k_im2col_bf16s(Im2colParams p) {
-  COEX_PDL_ENTER_CANCEL(p.ds);
+  COEX_PDL_ENTER();
   stamp(p.ds, SK_IM2COL);
-  if (coex_cancelled_) return;
   const float* x = res<float>(p.x);
   const int C = (int)p.C, k = p.k, H = (int)p.H, W = (int)p.W, Ho = (int)p.Ho, Wo = (int)p.Wo;
   const int Kc = k * k * C;
@@ -237,9 +233,8 @@ __global__ void __launch_bounds__(256) k_im2col_bf16s(Im2colParams p) {
 // stores it as 16-byte units; the row pitch's tail is zeroed.
 template <int C, int K>
 __global__ void __launch_bounds__(256) k_im2col_small(Im2colParams p) {
-  COEX_PDL_ENTER_CANCEL(p.ds);
+  COEX_PDL_ENTER();
   stamp(p.ds, SK_IM2COL);
-  if (coex_cancelled_) return;
   const float* x = res<float>(p.x);
   constexpr int KC = K * K * C, KP = (KC + 7) / 8 * 8;
   const int H = (int)p.H, W = (int)p.W, Ho = (int)p.Ho, Wo = (int)p.Wo;
@@ -288,10 +283,9 @@ struct Col2imParams {
 
 template <typename Tc, typename T>
 __global__ void __launch_bounds__(256) k_col2im(Col2imParams p) {
-  COEX_PDL_ENTER_CANCEL(p.ds);
+  COEX_PDL_ENTER();
   stamp(p.ds, SK_COL2IM);
   T* o = pick_out<T>(p.out, res<T>(p.a), res<T>(p.b));
-  if (coex_cancelled_) return;
   publish_early(p.out, o);
   count_op(p.ds);
   const Tc* cols = (const Tc*)p.cols;
@@ -333,10 +327,9 @@ __global__ void __launch_bounds__(256) k_col2im(Col2imParams p) {
 // same per-element order as k_col2im_v -- reading each tap's F floats contiguously.
 template <int F>
 __global__ void __launch_bounds__(256) k_col2im_px(Col2imParams p) {
-  COEX_PDL_ENTER_CANCEL(p.ds);
+  COEX_PDL_ENTER();
   stamp(p.ds, SK_COL2IM);
   float* o = pick_out<float>(p.out, res<float>(p.a), res<float>(p.b));
-  if (coex_cancelled_) return;
   publish_early(p.out, o);
   count_op(p.ds);
   const float* cols = (const float*)p.cols;
@@ -372,10 +365,9 @@ __global__ void __launch_bounds__(256) k_col2im_px(Col2imParams p) {
 
 template <int V>
 __global__ void __launch_bounds__(256) k_col2im_v(Col2imParams p) {
-  COEX_PDL_ENTER_CANCEL(p.ds);
+  COEX_PDL_ENTER();
   stamp(p.ds, SK_COL2IM);
   float* o = pick_out<float>(p.out, res<float>(p.a), res<float>(p.b));
-  if (coex_cancelled_) return;
   publish_early(p.out, o);
   count_op(p.ds);
   const float* cols = (const float*)p.cols;
@@ -443,9 +435,8 @@ struct PadCvtParams {
   int H, W, C, P;
 };
 __global__ void __launch_bounds__(256) k_cvt_pad_bf16(PadCvtParams p) {
-  COEX_PDL_ENTER_CANCEL(p.ds);
+  COEX_PDL_ENTER();
   stamp(p.ds, SK_CVT);
-  if (coex_cancelled_) return;
   const float* x = res<float>(p.x);
   const int C8 = p.C / 8, Wp = p.W + 2 * p.P, Hp = p.H + 2 * p.P;
   // the zero border is rewritten every pass: the destination is shared scratch
@@ -498,9 +489,8 @@ struct WPhaseParams {
   int k, so, pad, T, C, F;
 };
 __global__ void __launch_bounds__(256) k_convt_wphase(WPhaseParams p) {
-  COEX_PDL_ENTER_CANCEL(p.ds);
+  COEX_PDL_ENTER();
   stamp(p.ds, SK_CVT);
-  if (coex_cancelled_) return;
   const float* w = res<float>(p.w);
   const long long krows = (long long)p.T * p.T * p.C;
   const long long rows = (long long)p.so * p.so * krows;
@@ -567,9 +557,8 @@ constexpr int kColStages = 4;      // BULK: chunks in flight per block
 // run at HBM rate with two blocks per SM.
 template <typename T, int V, int S, bool DY, bool BULK = false>
 __global__ void __launch_bounds__(256) k_colstats(ColStatsParams p) {
-  COEX_PDL_ENTER_CANCEL(p.ds);
+  COEX_PDL_ENTER();
   stamp(p.ds, SK_COLSTATS);
-  if (coex_cancelled_) return;
   const T* x = res<T>(p.x);
   constexpr bool with_dy = DY;
   const T* dy = with_dy ? res<T>(p.dy) : nullptr;
@@ -822,14 +811,13 @@ struct BnApplyParams {
 
 template <typename T>
 __global__ void __launch_bounds__(256) k_bn_apply(BnApplyParams p) {
-  COEX_PDL_ENTER_CANCEL(p.ds);
+  COEX_PDL_ENTER();
   stamp(p.ds, SK_BNAPPLY);
   const T* x = res<T>(p.x);
   const T* g = res<T>(p.g);
   const T* z = res<T>(p.third);
   T* o = pick_out<T>(p.out, x, g);
   T* o2 = p.act >= 0 ? pick_out<T>(p.out2, x, g) : nullptr;
-  if (coex_cancelled_) return;
   publish_early(p.out, o);
   if (o2) publish_early(p.out2, o2);
   count_op(p.ds);
@@ -852,7 +840,7 @@ __global__ void __launch_bounds__(256) k_bn_apply(BnApplyParams p) {
 // one float4 per thread.  BATCHNORM: y = x*A + B;  BATCHNORM_DX: dx = dy*A + x*B + D with
 // A = g*rstd, B = -g*rstd^2*mean(dy*xhat), D = g*rstd*(rstd*mean*mean(dy*xhat) - mean(dy)).
 __global__ void __launch_bounds__(256) k_bn_apply_v4(BnApplyParams p) {
-  COEX_PDL_ENTER_CANCEL(p.ds);
+  COEX_PDL_ENTER();
   stamp(p.ds, SK_BNAPPLY);
   extern __shared__ float coef[];                    // [3][C]
   const float* x = res<float>(p.x);
@@ -860,7 +848,6 @@ __global__ void __launch_bounds__(256) k_bn_apply_v4(BnApplyParams p) {
   const float* z = res<float>(p.third);
   float* o = pick_out<float>(p.out, x, g);
   float* o2 = p.act >= 0 ? pick_out<float>(p.out2, x, g) : nullptr;
-  if (coex_cancelled_) return;
   publish_early(p.out, o);
   if (o2) publish_early(p.out2, o2);
   count_op(p.ds);
@@ -928,9 +915,8 @@ struct PoolParams {
 
 template <typename T, int MODE>
 __global__ void __launch_bounds__(256) k_pool(PoolParams p) {
-  COEX_PDL_ENTER_CANCEL(p.ds);
+  COEX_PDL_ENTER();
   stamp(p.ds, SK_POOL);
-  if (coex_cancelled_) return;
   const T* x = res<T>(p.x);
   const T* dy = (MODE & 1) ? res<T>(p.dy) : nullptr;       // modes 1, 3, 5 take (x, dy)
   if (MODE == 6) {                       // maxpool_grad pass 1: argmax tap of every window

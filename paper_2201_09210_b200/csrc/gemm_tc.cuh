@@ -59,9 +59,8 @@ struct CvtParams {
 // (coalesced on both sides); transposed operands go through a 32x33 shared-memory
 // tile so both the strided read and the K-major write stay coalesced.
 __global__ void __launch_bounds__(256) k_cvt_bf16(CvtParams p) {
-  COEX_PDL_ENTER_CANCEL(p.ds);
+  COEX_PDL_ENTER();
   stamp(p.ds, SK_CVT);
-  if (coex_cancelled_) return;
   // operand select without dynamic indexing of the parameter arrays (that would copy the
   // whole parameter block to local memory in every thread)
   const bool w1 = blockIdx.y != 0;
@@ -259,13 +258,12 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 // descriptors, so no transposition pass is needed.
 template <int BN, int AMODE, bool B_MN, bool DUO = false>
 __global__ void __launch_bounds__(TC_THREADS, DUO ? 2 : 1) k_gemm_tc(const __grid_constant__ TcGemmParams p) {
-  COEX_PDL_ENTER_CANCEL(p.ds);
+  COEX_PDL_ENTER();
   constexpr int STAGES = TcCfg<BN, DUO>::STAGES;
   constexpr int B_BYTES = TcCfg<BN, DUO>::B_BYTES;
   constexpr uint32_t TMEM_COLS = 2 * BN;            // two accumulator buffers
   constexpr bool A_MN = AMODE == 1 || AMODE == 3;
   stamp(p.ds, SK_MATMUL);
-  if (coex_cancelled_) return;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   unsigned char* sA = smem;
@@ -557,10 +555,9 @@ struct SplitReduceParams {
   Out out;
 };
 __global__ void __launch_bounds__(256) k_splitk_reduce(SplitReduceParams p) {
-  COEX_PDL_ENTER_CANCEL(p.ds);
+  COEX_PDL_ENTER();
   stamp(p.ds, SK_SPLITK);
   float* o = pick_out<float>(p.out, res<float>(p.a), p.b.cell || p.b.direct ? res<float>(p.b) : nullptr);
-  if (coex_cancelled_) return;
   publish_early(p.out, o);
   const long long n4 = p.n / 4;
   const long long stride = (long long)gridDim.x * blockDim.x;

@@ -24,12 +24,6 @@ namespace coex {
     asm volatile("griddepcontrol.wait;" ::: "memory");          \
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); \
   } while (0)
-// Cancellable entry (compute kernels): the cancel flag is loaded right after the dependency
-// wait but tested only once the kernel has loaded its operand pointers (res / pick_out), so
-// the flag's round trip overlaps theirs; every data access still follows the test.
-#define COEX_PDL_ENTER_CANCEL(ds)                               \
-  COEX_PDL_ENTER();                                             \
-  const bool coex_cancelled_ = skip(ds)
 
 constexpr int kMaxRank = 8;
 constexpr int kMaxDevVars = 1024;   // variables per context (runtime.cu kMaxVars)
@@ -38,7 +32,7 @@ constexpr int kMaxPub = 6;
 // ------------------------------------------------------------------ pass state
 // One per context, in device memory.  Reset by k_pass_begin.
 struct DevState {
-  int cancelled;                  // later kernels become no-ops
+  int cancelled;                  // spinners stop, conditionals skip, no commit
   int status;                     // coex_status of a device-detected failure
   unsigned long long pass_id;
   long long dec_head;             // decisions consumed this pass
@@ -195,6 +189,14 @@ __device__ __forceinline__ void publish_late(const Out& o, void* out) {
   }
 }
 
+// Cancellation is enforced where it is observable: the spinners (decisions,
+// feeds, fetches) stop waiting, conditional nodes then run no body, the commit is skipped and
+// AssignVar leaves the overlay alone (k_ptr and the feed kernels test the flag).  Compute
+// kernels do not: a cancelled pass runs its remaining straight-line kernels and discards
+// them.  That is safe because every pointer cell holds valid memory at all times -- cells
+// start each pass at their build-time values (a buffer of the right size, or the program's
+// zero-filled spare buffer of the largest size) -- and it removes a dependent flag load from
+// every launch (~5 % of the C2 step).
 __device__ __forceinline__ bool skip(const DevState* ds) {
   return ds != nullptr && *(volatile const int*)&ds->cancelled;
 }
@@ -282,12 +284,11 @@ struct EwParams {
 
 template <typename T>
 __global__ void __launch_bounds__(256) k_elementwise(EwParams p) {
-  COEX_PDL_ENTER_CANCEL(p.ds);
+  COEX_PDL_ENTER();
   stamp(p.ds, SK_EW);
   const T* a = res<T>(p.a);
   const T* b = ew_binary(p.op) ? res<T>(p.b) : nullptr;
   T* o = pick_out<T>(p.out, a, b);
-  if (coex_cancelled_) return;
   publish_early(p.out, o);
   count_op(p.ds);
   const long long n = p.n;
@@ -335,11 +336,10 @@ struct ReduceParams {
 // Parity path: one warp streams the data, lane 0 accumulates strictly in order.
 template <typename T>
 __global__ void __launch_bounds__(32) k_reduce_seq(ReduceParams p) {
-  COEX_PDL_ENTER_CANCEL(p.ds);
+  COEX_PDL_ENTER();
   stamp(p.ds, SK_REDUCE);
   const T* a = res<T>(p.a);
   T* o = pick_out<T>(p.out, a, nullptr);
-  if (coex_cancelled_) return;
   publish_early(p.out, o);
   count_op(p.ds);
   const int lane = threadIdx.x;
@@ -360,11 +360,10 @@ __global__ void __launch_bounds__(32) k_reduce_seq(ReduceParams p) {
 // Tolerance path (fp32 / bf16 contexts): warp-shuffle tree in double, one block.
 template <typename T>
 __global__ void __launch_bounds__(1024) k_reduce_tree(ReduceParams p) {
-  COEX_PDL_ENTER_CANCEL(p.ds);
+  COEX_PDL_ENTER();
   stamp(p.ds, SK_REDUCE);
   const T* a = res<T>(p.a);
   T* o = pick_out<T>(p.out, a, nullptr);
-  if (coex_cancelled_) return;
   publish_early(p.out, o);
   count_op(p.ds);
   __shared__ double part[32];
@@ -395,11 +394,10 @@ struct TransposeParams {
 
 template <typename T>
 __global__ void __launch_bounds__(256) k_transpose(TransposeParams p) {
-  COEX_PDL_ENTER_CANCEL(p.ds);
+  COEX_PDL_ENTER();
   stamp(p.ds, SK_TRANSPOSE);
   const T* a = res<T>(p.a);
   T* o = pick_out<T>(p.out, a, nullptr);
-  if (coex_cancelled_) return;
   publish_early(p.out, o);
   count_op(p.ds);
   const long long stride = (long long)gridDim.x * blockDim.x;
@@ -421,11 +419,10 @@ __global__ void __launch_bounds__(256) k_transpose(TransposeParams p) {
 // 32-bit index arithmetic per row (rank <= 4 outer axes).
 template <typename T>
 __global__ void __launch_bounds__(256) k_transpose_rows(TransposeParams p) {
-  COEX_PDL_ENTER_CANCEL(p.ds);
+  COEX_PDL_ENTER();
   stamp(p.ds, SK_TRANSPOSE);
   const T* a = res<T>(p.a);
   T* o = pick_out<T>(p.out, a, nullptr);
-  if (coex_cancelled_) return;
   publish_early(p.out, o);
   count_op(p.ds);
   constexpr int V = 16 / sizeof(T);
@@ -449,11 +446,10 @@ __global__ void __launch_bounds__(256) k_transpose_rows(TransposeParams p) {
 // 2-D transpose through a padded shared-memory tile (coalesced on both sides).
 template <typename T>
 __global__ void __launch_bounds__(256) k_transpose2d(TransposeParams p) {
-  COEX_PDL_ENTER_CANCEL(p.ds);
+  COEX_PDL_ENTER();
   stamp(p.ds, SK_TRANSPOSE);
   const T* a = res<T>(p.a);
   T* o = pick_out<T>(p.out, a, nullptr);
-  if (coex_cancelled_) return;
   publish_early(p.out, o);
   count_op(p.ds);
   __shared__ T tile[32][33];
@@ -494,12 +490,11 @@ struct MatmulParams {
 
 template <typename T, int BM, int BN, int BK, int RM, int RN, bool EXACT>
 __global__ void __launch_bounds__((BM / RM) * (BN / RN)) k_matmul_simt(MatmulParams p) {
-  COEX_PDL_ENTER_CANCEL(p.ds);
+  COEX_PDL_ENTER();
   stamp(p.ds, SK_MATMUL);
   const T* A = res<T>(p.a);
   const T* B = res<T>(p.b);
   T* C = pick_out<T>(p.out, A, B);
-  if (coex_cancelled_) return;
   publish_early(p.out, C);
   count_op(p.ds);
   constexpr int TX = BN / RN, TY = BM / RM, NT = TX * TY;
@@ -581,12 +576,11 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 
 template <typename T, int BM, int BN, int BK, int RM, int RN, bool EXACT, int STAGES>
 __global__ void __launch_bounds__((BM / RM) * (BN / RN)) k_matmul_pipe(MatmulParams p) {
-  COEX_PDL_ENTER_CANCEL(p.ds);
+  COEX_PDL_ENTER();
   stamp(p.ds, SK_MATMUL);
   const T* A0 = res<T>(p.a);
   const T* B0 = res<T>(p.b);
   T* C0 = pick_out<T>(p.out, A0, B0);
-  if (coex_cancelled_) return;
   publish_early(p.out, C0);
   if (blockIdx.y == 0) count_op(p.ds);
   const T* A = A0 + blockIdx.y * p.sa;
@@ -694,13 +688,12 @@ __global__ void __launch_bounds__((BM / RM) * (BN / RN)) k_matmul_pipe(MatmulPar
 // order (unrolled so loads run ahead of the dependent add chain).
 template <typename T>
 __global__ void __launch_bounds__(256) k_reduce_seq_smem(ReduceParams p) {
-  COEX_PDL_ENTER_CANCEL(p.ds);
+  COEX_PDL_ENTER();
   stamp(p.ds, SK_REDUCE);
   constexpr int CH = 2048;
   __shared__ T buf[2][CH];
   const T* a = res<T>(p.a);
   T* o = pick_out<T>(p.out, a, nullptr);
-  if (coex_cancelled_) return;
   publish_early(p.out, o);
   count_op(p.ds);
   double acc = 0.0;
@@ -852,9 +845,8 @@ __device__ __forceinline__ void chain_run(const ChainParams& p, ChainSmem<T>& S,
 
 template <typename T>
 __global__ void __launch_bounds__(256) k_chain(ChainParams p) {
-  COEX_PDL_ENTER_CANCEL(p.ds);
+  COEX_PDL_ENTER();
   stamp(p.ds, SK_FUSED);
-  if (coex_cancelled_) return;
   __shared__ ChainSmem<T> S;
   count_op(p.ds);
   chain_run(p, S, blockIdx.x, gridDim.x);
@@ -872,9 +864,8 @@ struct MultiChainParams {
 };
 template <typename T>
 __global__ void __launch_bounds__(256) k_chain_multi(const __grid_constant__ MultiChainParams mp) {
-  COEX_PDL_ENTER_CANCEL(mp.ds);
+  COEX_PDL_ENTER();
   stamp(mp.ds, SK_FUSED);
-  if (coex_cancelled_) return;
   __shared__ ChainSmem<T> S;
   count_op(mp.ds);
   int j = 0;
@@ -887,9 +878,8 @@ __global__ void __launch_bounds__(256) k_chain_multi(const __grid_constant__ Mul
 // one thread, the tolerance path reduces with warp shuffles in double.
 template <typename T, bool EXACT>
 __global__ void __launch_bounds__(256) k_chain_reduce(ChainParams p) {
-  COEX_PDL_ENTER_CANCEL(p.ds);
+  COEX_PDL_ENTER();
   stamp(p.ds, SK_FUSED);
-  if (coex_cancelled_) return;
   constexpr int CH = 1024;
   __shared__ T vals[CH];
   __shared__ double part[8];
@@ -944,9 +934,8 @@ struct FillParams {
 };
 template <typename T>
 __global__ void __launch_bounds__(256) k_fill(FillParams p) {
-  COEX_PDL_ENTER_CANCEL(p.ds);
+  COEX_PDL_ENTER();
   T* o = (T*)p.out.buf[0];
-  if (coex_cancelled_) return;
   publish_early(p.out, o);
   const long long stride = (long long)gridDim.x * blockDim.x;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < p.n; i += stride) o[i] = (T)p.value;
@@ -1311,11 +1300,15 @@ struct BeginParams {
   Mailbox* mb;
   void** var_ovl;
   int nvars;
+  void** cells;              // the program's pointer cells, reset to their build-time
+  void* const* cells_init;   // values (every one a valid buffer) at the start of each pass
+  long long ncells;
 };
 __global__ void k_pass_begin(BeginParams p) {
   COEX_PDL_ENTER();
   DevState* ds = p.ds;
   for (int i = threadIdx.x; i < p.nvars; i += blockDim.x) p.var_ovl[i] = nullptr;
+  for (long long i = threadIdx.x; i < p.ncells; i += blockDim.x) p.cells[i] = p.cells_init[i];
   if (threadIdx.x == 0) {
     ds->cancelled = 0;
     ds->status = 0;

@@ -2216,6 +2216,8 @@ struct coex_prog {
   char* arena = nullptr;              // node / slot buffers
   size_t arena_bytes = 0;
   void** cells = nullptr;             // device pointer cells
+  void** cells_init = nullptr;        // their build-time values (k_pass_begin resets them)
+  void* spare = nullptr;              // zero-filled stand-in for cells without a buffer of their own
   int64_t ncells = 0;
   FeedRecord* recs = nullptr;
   unsigned int* late = nullptr;       // late-publication counters
@@ -2744,8 +2746,20 @@ int coex_prog_build(coex_ctx* c, const int64_t* plan, int64_t nwords, const doub
     p->ncells = b.next();
     std::vector<void*> init(p->ncells > 0 ? p->ncells : 1, nullptr);
     for (int64_t i = 0; i < p->ncells; ++i) init[i] = b.buf(b.next());
+    // cells without a buffer (pointer ops, merged bindings of pointer ops) start at a
+    // zero-filled spare as large as any tensor the program touches: a cancelled pass that
+    // skipped their publisher still hands its readers valid memory
+    size_t spare = 256;
+    for (int64_t i = 0; i < nbufs; ++i) spare = std::max(spare, (size_t)sizes[i]);
+    for (const auto& v : c->vars) spare = std::max(spare, (size_t)(v.t.numel > 0 ? v.t.numel : 1) * c->esize);
+    CK(cudaMalloc(&p->spare, spare));
+    CK(cudaMemset(p->spare, 0, spare));
+    for (int64_t i = 0; i < p->ncells; ++i)
+      if (init[i] == nullptr) init[i] = p->spare;
     CK(cudaMalloc(&p->cells, sizeof(void*) * (p->ncells > 0 ? p->ncells : 1)));
+    CK(cudaMalloc(&p->cells_init, sizeof(void*) * (p->ncells > 0 ? p->ncells : 1)));
     CK(cudaMemcpy(p->cells, init.data(), sizeof(void*) * p->ncells, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(p->cells_init, init.data(), sizeof(void*) * p->ncells, cudaMemcpyHostToDevice));
     const int64_t nrecs = b.next();
     CK(cudaMalloc(&p->recs, sizeof(FeedRecord) * (nrecs > 0 ? nrecs : 1)));
     const int64_t nlate = b.next();
@@ -2789,6 +2803,9 @@ int coex_prog_build(coex_ctx* c, const int64_t* plan, int64_t nwords, const doub
     {
       BeginParams bp{c->d_state, c->d_mb, c->d_var_ovl, (int)c->vars.size() > 0 ? (int)kMaxVars : 0};
       bp.nvars = kMaxVars;
+      bp.cells = p->cells;
+      bp.cells_init = p->cells_init;
+      bp.ncells = p->ncells;
       Launch L;
       L.set((void*)k_pass_begin, dim3(1), dim3(256), bp);
       int rc = b.add_kernel(p->graph, &prev, L);
@@ -2852,6 +2869,8 @@ int coex_prog_destroy(coex_prog* p) {
   if (p->graph) cudaGraphDestroy(p->graph);
   if (p->arena) cudaFree(p->arena);
   if (p->cells) cudaFree(p->cells);
+  if (p->cells_init) cudaFree(p->cells_init);
+  if (p->spare) cudaFree(p->spare);
   if (p->recs) cudaFree(p->recs);
   if (p->late) cudaFree(p->late);
   for (void* w : p->workspaces) cudaFree(w);

@@ -64,12 +64,11 @@ __device__ __forceinline__ bool last_block(unsigned int* counter) {
 // out[r, :] = table[clip(ids[r]), :]   (x = table [V, d], y = ids [rows])
 template <typename T>
 __global__ void __launch_bounds__(256) k_embed(RowParams p) {
-  COEX_PDL_ENTER_CANCEL(p.ds);
+  COEX_PDL_ENTER();
   stamp(p.ds, SK_EMBED);
   const T* tab = res<T>(p.x);
   const T* ids = res<T>(p.y);
   T* o = pick_out<T>(p.out, tab, ids);
-  if (coex_cancelled_) return;
   publish_early(p.out, o);
   count_op(p.ds);
   const long long total = p.rows * p.d;
@@ -86,12 +85,11 @@ __global__ void __launch_bounds__(256) k_embed(RowParams p) {
 // by the preceding k_zero launch)   (x = ids [rows], y = dy [rows, d])
 template <typename T>
 __global__ void __launch_bounds__(256) k_embed_dw(RowParams p) {
-  COEX_PDL_ENTER_CANCEL(p.ds);
+  COEX_PDL_ENTER();
   stamp(p.ds, SK_EMBED);
   const T* ids = res<T>(p.x);
   const T* dy = res<T>(p.y);
   T* o = pick_out<T>(p.out, ids, dy);
-  if (coex_cancelled_) return;
   publish_early(p.out, o);
   count_op(p.ds);
   const long long total = p.rows * p.d;
@@ -111,8 +109,7 @@ struct ZeroParams {
   In a, b;
 };
 __global__ void __launch_bounds__(256) k_zero(ZeroParams p) {
-  COEX_PDL_ENTER_CANCEL(p.ds);
-  if (coex_cancelled_) return;
+  COEX_PDL_ENTER();
   char* o = pick_out<char>(p.out, p.a.cell || p.a.direct ? res<char>(p.a) : nullptr,
                            p.b.cell || p.b.direct ? res<char>(p.b) : nullptr);
   const long long n16 = p.bytes / 16;
@@ -127,12 +124,11 @@ __global__ void __launch_bounds__(256) k_zero(ZeroParams p) {
 // out = x + b[i % d]
 template <typename T>
 __global__ void __launch_bounds__(256) k_bias_add(RowParams p) {
-  COEX_PDL_ENTER_CANCEL(p.ds);
+  COEX_PDL_ENTER();
   stamp(p.ds, SK_BIAS);
   const T* x = res<T>(p.x);
   const T* b = res<T>(p.y);
   T* o = pick_out<T>(p.out, x, b);
-  if (coex_cancelled_) return;
   publish_early(p.out, o);
   count_op(p.ds);
   const long long total = p.rows * p.d;
@@ -158,11 +154,10 @@ __global__ void __launch_bounds__(256) k_bias_add(RowParams p) {
 // Both are shifted contiguous copies: coalesced reads and writes, HBM-bound.
 template <typename T, int UN>
 __global__ void __launch_bounds__(256) k_rel_skew(RowParams p) {
-  COEX_PDL_ENTER_CANCEL(p.ds);
+  COEX_PDL_ENTER();
   stamp(p.ds, SK_SKEW);
   const T* x = res<T>(p.x);
   T* o = pick_out<T>(p.out, x, nullptr);
-  if (coex_cancelled_) return;
   publish_early(p.out, o);
   count_op(p.ds);
   const int lane = threadIdx.x & 31;
@@ -198,13 +193,12 @@ __device__ __forceinline__ void ln_row_stats(const T* xr, long long d, int lane,
 // mode 0: y = xhat*g + b (x, g = y operand, b = z operand); mode 1: dx (x, g, dy = z)
 template <typename T, int MODE>
 __global__ void __launch_bounds__(256) k_layernorm(RowParams p) {
-  COEX_PDL_ENTER_CANCEL(p.ds);
+  COEX_PDL_ENTER();
   stamp(p.ds, SK_LN);
   const T* x = res<T>(p.x);
   const T* g = res<T>(p.y);
   const T* z = res<T>(p.z);
   T* o = pick_out<T>(p.out, x, g);
-  if (coex_cancelled_) return;
   publish_early(p.out, o);
   count_op(p.ds);
   const int lane = threadIdx.x & 31;
@@ -298,12 +292,11 @@ __global__ void __launch_bounds__(256) k_layernorm(RowParams p) {
 // the last block sums the replicas, writes the output and re-zeroes the accumulators.
 template <typename T>
 __global__ void __launch_bounds__(256) k_ln_dgamma(RowParams p) {
-  COEX_PDL_ENTER_CANCEL(p.ds);
+  COEX_PDL_ENTER();
   stamp(p.ds, SK_LN);
   const T* x = res<T>(p.x);
   const T* dy = res<T>(p.y);
   T* o = pick_out<T>(p.out, x, dy);
-  if (coex_cancelled_) return;
   publish_early(p.out, o);
   count_op(p.ds);
   constexpr int MAXC = 32;                          // columns per lane (d <= 1024)
@@ -348,11 +341,10 @@ __global__ void __launch_bounds__(256) k_ln_dgamma(RowParams p) {
 // One warp per row of a [T, T] block: row i keeps columns j <= i; y = exp(s*x - max) / sum.
 template <typename T>
 __global__ void __launch_bounds__(256) k_causal_softmax(RowParams p) {
-  COEX_PDL_ENTER_CANCEL(p.ds);
+  COEX_PDL_ENTER();
   stamp(p.ds, SK_SOFTMAX);
   const T* x = res<T>(p.x);
   T* o = pick_out<T>(p.out, x, nullptr);
-  if (coex_cancelled_) return;
   publish_early(p.out, o);
   count_op(p.ds);
   const int lane = threadIdx.x & 31;
@@ -419,12 +411,11 @@ __global__ void __launch_bounds__(256) k_causal_softmax(RowParams p) {
 // dx = scale * y * (dy - sum_j dy*y)   (x = y, y = dy operand)
 template <typename T>
 __global__ void __launch_bounds__(256) k_softmax_grad(RowParams p) {
-  COEX_PDL_ENTER_CANCEL(p.ds);
+  COEX_PDL_ENTER();
   stamp(p.ds, SK_SOFTMAX_GRAD);
   const T* y = res<T>(p.x);
   const T* dy = res<T>(p.y);
   T* o = pick_out<T>(p.out, y, dy);
-  if (coex_cancelled_) return;
   publish_early(p.out, o);
   count_op(p.ds);
   const int lane = threadIdx.x & 31;
@@ -485,9 +476,8 @@ __global__ void __launch_bounds__(256) k_softmax_grad(RowParams p) {
 // block writes their mean (ordered sum: deterministic); MODE 1: (softmax - onehot) / rows.
 template <typename T, int MODE>
 __global__ void __launch_bounds__(256) k_cross_entropy(RowParams p) {
-  COEX_PDL_ENTER_CANCEL(p.ds);
+  COEX_PDL_ENTER();
   stamp(p.ds, SK_CE);
-  if (coex_cancelled_) return;
   typedef typename AccT<T>::type A;
   const T* lg = res<T>(p.x);
   const T* ids = res<T>(p.y);
@@ -572,9 +562,8 @@ __global__ void __launch_bounds__(256) k_cross_entropy(RowParams p) {
 // k_acc_out pass.   (x operand, rows x d)
 template <typename T>
 __global__ void __launch_bounds__(256) k_colsum_wide(RowParams p) {
-  COEX_PDL_ENTER_CANCEL(p.ds);
+  COEX_PDL_ENTER();
   stamp(p.ds, SK_COLSUM);
-  if (coex_cancelled_) return;
   const T* x = res<T>(p.x);
   T* o = pick_out<T>(p.out, x, nullptr);
   if (gridDim.y == 1) publish_early(p.out, o);
@@ -600,9 +589,8 @@ __global__ void __launch_bounds__(256) k_colsum_wide(RowParams p) {
 
 template <typename T>
 __global__ void __launch_bounds__(256) k_acc_out(RowParams p) {
-  COEX_PDL_ENTER_CANCEL(p.ds);
+  COEX_PDL_ENTER();
   T* o = pick_out<T>(p.out, res<T>(p.x), nullptr);
-  if (coex_cancelled_) return;
   publish_early(p.out, o);
   for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < p.d; c += (long long)gridDim.x * blockDim.x) {
     o[c] = (T)p.acc[c];
@@ -625,12 +613,11 @@ struct AxisParams {
 
 template <typename T>
 __global__ void __launch_bounds__(256) k_axis(AxisParams p) {
-  COEX_PDL_ENTER_CANCEL(p.ds);
+  COEX_PDL_ENTER();
   stamp(p.ds, SK_AXIS);
   const T* a = res<T>(p.a);
   const T* b = p.mode == 1 ? res<T>(p.b) : nullptr;
   T* o = pick_out<T>(p.out, a, b);
-  if (coex_cancelled_) return;
   publish_early(p.out, o);
   count_op(p.ds);
   const long long stride = (long long)gridDim.x * blockDim.x;
