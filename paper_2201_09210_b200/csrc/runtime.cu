@@ -776,6 +776,23 @@ struct TcPlan {
 // bounded by its MMA time or its L2->SMEM operand stream, plus the fp32 epilogue store and a
 // fixed prologue; split-K adds the slice reduction.  (Per-SM figures: 1/148 of the measured
 // bf16 peak, ~135 GB/s of L2 operand bandwidth, ~44 GB/s of concurrent store bandwidth.)
+int duo_kmax() {
+  static int kmax = -1;
+  if (kmax < 0) {
+    const char* e = getenv("COEX_DUO_KMAX");
+    kmax = e ? atoi(e) : 32;
+  }
+  return kmax;
+}
+// COEX_DUO_MODEL=0: the cost model ignores the two-CTA slots (A/B)
+bool duo_model() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("COEX_DUO_MODEL");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
 TcPlan tc_plan(int64_t M, int64_t N, int64_t K, bool allow_split) {
   TcPlan best;
   double best_t = 1e30;
@@ -801,8 +818,10 @@ TcPlan tc_plan(int64_t M, int64_t N, int64_t K, bool allow_split) {
       // persistent CTAs: items per CTA run back to back, the epilogue of one item overlapping
       // the MMAs of the next (two TMEM accumulators)
       const int64_t items = (tiles < 1 ? 1 : tiles) * sp;
-      const int64_t rounds = (items + kNumSMs - 1) / kNumSMs;
       const double kper = (double)((nk + sp - 1) / sp);
+      // launches the DUO variant takes (tc_gemm_launches) hold two CTAs per SM
+      const int64_t slots = duo_model() && bn <= 128 && kper <= duo_kmax() ? 2 * kNumSMs : kNumSMs;
+      const int64_t rounds = (items + slots - 1) / slots;
       // per-SM figures fitted to measured launches (tools/ncu_ops.py qkt / gemm_8192 with
       // COEX_FORCE_BN): ~115 GB/s of TMA operand feed, ~23.5 GB/s of epilogue stores and
       // ~0.9 us of fixed cost per work item (barrier round trips, TMEM hand-off)
@@ -946,12 +965,7 @@ int tc_gemm_launches(coex_ctx* c, DevState* ds, void* a16, void* b16, int64_t M,
   // two CTAs per SM for short-K launches that do not fill two waves of single CTAs
   const int64_t kblocks = (K + TC_BK - 1) / TC_BK / (t.splits > 0 ? t.splits : 1);
   const int dm = duo_mode();
-  static int kmax = -1;
-  if (kmax < 0) {
-    const char* e = getenv("COEX_DUO_KMAX");
-    kmax = e ? atoi(e) : 32;
-  }
-  const bool duo = t.bn <= 128 && (dm == 1 || (dm < 0 && kblocks <= kmax));
+  const bool duo = t.bn <= 128 && (dm == 1 || (dm < 0 && kblocks <= duo_kmax()));
   void* fn;
   if (duo) {
     fn = t.bn == 64 ? tc_fn<64, true>(amode, b_mn) : tc_fn<128, true>(amode, b_mn);
