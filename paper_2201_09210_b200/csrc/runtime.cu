@@ -1665,8 +1665,20 @@ int build_launches(coex_ctx* c, const OpSpec& s, Launch* L, int* nL) {
   }
   const bool a_mn = s.trans_a && ca != 2, b_mn = !s.trans_b && cb != 2;
   *nL = 0;
-  if (ca == 1) cvt_rows_launch(s.ds, s.in[0], s.scratch[0], s.in_shape[0][0], s.in_shape[0][1], &L[(*nL)++]);
-  if (cb == 1) cvt_rows_launch(s.ds, s.in[1], s.scratch[1], s.in_shape[1][0], s.in_shape[1][1], &L[(*nL)++]);
+  if (ca == 1 && cb == 1) {                         // both operands as stored: one launch
+    CvtParams q{};
+    q.ds = s.ds; q.src[0] = s.in[0]; q.src[1] = s.in[1];
+    q.rows[0] = s.in_shape[0][0]; q.K = s.in_shape[0][1]; q.ld = bf16_pitch(q.K);
+    q.rows[1] = s.in_shape[1][0]; q.Kb = s.in_shape[1][1]; q.ldb = bf16_pitch(q.Kb);
+    q.dst[0] = (__nv_bfloat16*)s.scratch[0]; q.dst[1] = (__nv_bfloat16*)s.scratch[1];
+    const int64_t ga = (q.rows[0] * q.ld / 8 + 255) / 256, gb = (q.rows[1] * q.ldb / 8 + 255) / 256;
+    int64_t gx = ga > gb ? ga : gb;
+    if (gx > kNumSMs * 16) gx = kNumSMs * 16;
+    L[(*nL)++].set((void*)k_cvt_bf16, dim3((unsigned)(gx < 1 ? 1 : gx), 2), dim3(256), q);
+  } else {
+    if (ca == 1) cvt_rows_launch(s.ds, s.in[0], s.scratch[0], s.in_shape[0][0], s.in_shape[0][1], &L[(*nL)++]);
+    if (cb == 1) cvt_rows_launch(s.ds, s.in[1], s.scratch[1], s.in_shape[1][0], s.in_shape[1][1], &L[(*nL)++]);
+  }
   for (int w = 0; w < 2; ++w) {
     if ((w == 0 ? ca : cb) != 2) continue;
     CvtParams q{};                                  // element (r, k) = src[k * R + r]
