@@ -58,9 +58,54 @@ from paper_2201_09210_b200.tensor import (BN_EPS, GELU_C, LEAKY_SLOPE, LN_EPS, O
                                           infer_shape)
 
 
+# Tolerance-mode switch (tests only): when True, MATMUL and every product built on it
+# (conv, bmm) use numpy's BLAS f64 product instead of the sequential-k loop.  The two
+# differ by f64 rounding in the summation order only (<= ~K * 2^-53 relative, pinned by
+# tests/test_ext_oracle_cpu.py::test_fast_matmul_matches_sequential), which is 8+ orders
+# of magnitude below the fp32 (1e-5) and bf16 (2e-2) bars it is used to check; the
+# bit-exact f64 parity tests never set it.
+FAST_MATMUL = False
+
+
+# Host threads for the sequential-k product (bench.py's CPU reference arm sets it to the
+# host's core count).  Output tiles are independent: every element still accumulates
+# a[i,0]*b[0,j], a[i,1]*b[1,j], ... in k order from +0.0, so the result is bit-identical to
+# the single-threaded loop (tests/test_ext_oracle_cpu.py::test_threaded_matmul_bitwise).
+THREADS = 1
+_POOL = None
+
+
+def _seq_tile(a, b, acc, r0, r1, c0, c1):
+    at = np.ascontiguousarray(a[r0:r1].T)          # k-major rows of the tile's A block
+    blk = acc[r0:r1, c0:c1]
+    tmp = np.empty_like(blk)
+    for k in range(a.shape[1]):
+        np.multiply(at[k][:, None], b[k:k + 1, c0:c1], out=tmp)
+        blk += tmp
+
+
 def matmul_seq(a: np.ndarray, b: np.ndarray) -> np.ndarray:
+    if FAST_MATMUL:
+        return np.matmul(a, b) + 0.0
     m, kk = a.shape
-    acc = np.zeros((m, b.shape[1]), dtype=np.float64)
+    n = b.shape[1]
+    acc = np.zeros((m, n), dtype=np.float64)
+    if THREADS > 1 and m * n >= 2 * 65536:
+        global _POOL
+        if _POOL is None or _POOL._max_workers != THREADS:
+            from concurrent.futures import ThreadPoolExecutor
+            _POOL = ThreadPoolExecutor(THREADS)
+        # one large block per thread (the k loop's numpy calls then run long enough between
+        # GIL handoffs to overlap): split rows when there are enough, else columns
+        t = min(THREADS, max(1, m * n // 65536))       # blocks of >= 64 Ki outputs
+        if m >= 4 * t:
+            e = [m * i // t for i in range(t + 1)]
+            tiles = [(e[i], e[i + 1], 0, n) for i in range(t) if e[i] < e[i + 1]]
+        else:
+            e = [n * i // t for i in range(t + 1)]
+            tiles = [(0, m, e[i], e[i + 1]) for i in range(t) if e[i] < e[i + 1]]
+        list(_POOL.map(lambda t: _seq_tile(a, b, acc, *t), tiles))
+        return acc
     for k in range(kk):
         acc += a[:, k:k + 1] * b[k:k + 1, :]
     return acc

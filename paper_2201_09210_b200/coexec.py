@@ -235,6 +235,21 @@ class Orchestrator:
         self.stats.per_step.append({"step": step, "phase": phase.value, "ms": dt * 1e3})
         return phase
 
+    def margins(self) -> list:
+        """Value-driven comparisons evaluated so far (the latest evaluation per step and
+        source position): {"step", "line", "col", "op", "a", "b", "rel_margin"} with
+        rel_margin = |a - b| / max(|a|, |b|).  A decision whose margin is below the precision
+        mode's tolerance may legitimately differ from the f64 oracle's."""
+        last = {}
+        for st, ln, col, op, a, b in self.it.margin_log:
+            last[(st, ln, col)] = (op, a, b)
+        out = []
+        for (st, ln, col), (op, a, b) in sorted(last.items()):
+            den = max(abs(a), abs(b))
+            out.append({"step": st, "line": ln, "col": col, "op": op, "a": a, "b": b,
+                        "rel_margin": abs(a - b) / den if den > 0 else 0.0})
+        return out
+
     def result(self) -> RunResult:
         return RunResult(list(self.it.out), self.be.snapshot_vars(), self.step_times)
 

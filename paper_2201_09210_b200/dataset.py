@@ -23,7 +23,7 @@ import json
 import numpy as np
 
 from .errors import DatasetExhausted, EvalError
-from .rng import MASK64, XS_MULT, seeded_state, xs_step
+from .rng import MASK64, XS_MULT, jump_state, seeded_state, xs_step
 from .tensor import Tensor, shape_size
 
 OCC_MIX = 0x9E3779B97F4A7C15
@@ -33,49 +33,32 @@ def synth_values(state: int, n: int) -> np.ndarray:
     """Host expansion of ``n`` draws from generator ``state`` mapped to [-1, 1).
 
     Bit-identical to ``gen.next_unit() * 2.0 - 1.0`` repeated n times
-    (dataset.py:49-50): the sequential xorshift walk is done on uint64 lanes of
-    64 interleaved sub-streams (each lane jumps 64 states at a time)."""
+    (dataset.py:49-50): the draws are cut into ``lanes`` contiguous chunks of
+    ``rows`` draws; each chunk's first state is reached by the O(log n) GF(2)
+    jump-ahead (rng.jump_state) and the chunks then step xorshift64 in lockstep
+    on uint64 vectors -- ``rows`` vector steps instead of n scalar ones."""
     out = np.empty(n, dtype=np.float64)
     if n == 0:
         return out
-    lanes = min(n, 64)
-    starts = np.empty(lanes, dtype=np.uint64)
-    x = state
-    for i in range(lanes):
-        x = xs_step(x)
-        starts[i] = x
+    lanes = max(1, min(4096, n // 32))
     rows = -(-n // lanes)
-    states = np.empty((rows, lanes), dtype=np.uint64)
-    states[0] = starts
-    if rows > 1:
-        from .rng import jump_columns
-        cols = np.array(jump_columns(6) if lanes == 64 else _cols_for(lanes), dtype=np.uint64)
-        cur = starts.copy()
-        for r in range(1, rows):
-            cur = _apply_matrix(cols, cur)
-            states[r] = cur
+    starts = np.empty(lanes, dtype=np.uint64)
+    x = xs_step(state)
+    for i in range(lanes):
+        starts[i] = x
+        x = jump_state(x, rows)
+    states = np.empty((lanes, rows), dtype=np.uint64)
+    cur = starts
+    s12, s25, s27 = np.uint64(12), np.uint64(25), np.uint64(27)
+    for r in range(rows):
+        states[:, r] = cur
+        cur = cur ^ (cur >> s12)
+        cur = cur ^ (cur << s25)
+        cur = cur ^ (cur >> s27)
     flat = states.reshape(-1)[:n]
     prod = flat * np.uint64(XS_MULT)
     out[:] = (prod >> np.uint64(11)).astype(np.float64) * (2.0 ** -53) * 2.0 - 1.0
     return out
-
-
-def _cols_for(k: int) -> list:
-    cols = []
-    for b in range(64):
-        v = 1 << b
-        for _ in range(k):
-            v = xs_step(v)
-        cols.append(v)
-    return cols
-
-
-def _apply_matrix(cols: np.ndarray, v: np.ndarray) -> np.ndarray:
-    r = np.zeros_like(v)
-    for b in range(64):
-        bit = (v >> np.uint64(b)) & np.uint64(1)
-        r ^= cols[b] * bit
-    return r
 
 
 class SyntheticTensor:

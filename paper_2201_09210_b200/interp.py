@@ -373,6 +373,11 @@ class Interp:
         self.out: list = []            # flushed printed lines
         self.prologue_env: dict = {}
         self.step = -1
+        # value-branch margins: every ordered comparison with a float operand
+        # -- the conditions a fetched value can drive -- logs (step, line, col, op, a, b);
+        # a decision is robust to the precision mode's error when |a-b| / max(|a|,|b|)
+        # exceeds that mode's tolerance (Orchestrator.margins())
+        self.margin_log: list = []
         self._body = self._c_block(program.body, False)
 
     # ------------------------------------------------------------------ driver API
@@ -624,6 +629,8 @@ class Interp:
         if op == "!=":
             return lambda ctx, env: fa(ctx, env) != fb(ctx, env)
         impl = _BINOPS[op]
+        ordered = op in ("<", "<=", ">", ">=")
+        line, col = e.pos.line, e.pos.col
 
         def arith(ctx, env):
             a = fa(ctx, env)
@@ -632,6 +639,8 @@ class Interp:
             if (ta is int or ta is float) and (tb is int or tb is float):
                 if op == "/" and b == 0:
                     raise it._err("division by zero", e)
+                if ordered and (ta is float or tb is float):
+                    it.margin_log.append((it.step, line, col, op, a, b))
                 return impl(a, b)
             if ta is str and tb is str and op in ("+", "<", "<=", ">", ">="):
                 return impl(a, b)

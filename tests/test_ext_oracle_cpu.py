@@ -185,3 +185,36 @@ def test_adam_program_coexec_equals_imperative():
         assert np.array_equal(ref.vars[name].data, got.vars[name].data), name
     sgd, _, _ = run(gpt2_program(steps=6, **C4_SMALL), "imperative", CpuBackend())
     assert sgd.lines[0] == ref.lines[0] and sgd.lines[1:] != ref.lines[1:]
+
+
+def test_fast_matmul_matches_sequential():
+    """oracle.kernels.FAST_MATMUL (BLAS f64, used only by the tolerance-mode contract tests
+    at full model width) agrees with the sequential-k restatement to f64 rounding."""
+    from oracle import kernels as K
+    r = np.random.default_rng(3)
+    for m, k, n in ((64, 784, 128), (128, 3072, 96), (33, 50257 // 16, 17)):
+        a, b = r.uniform(-1, 1, (m, k)), r.uniform(-1, 1, (k, n))
+        ref = K.matmul_seq(a, b)
+        K.FAST_MATMUL = True
+        try:
+            fast = K.matmul_seq(a, b)
+        finally:
+            K.FAST_MATMUL = False
+        assert np.linalg.norm(fast - ref) / np.linalg.norm(ref) <= k * 2.0 ** -52
+
+
+def test_threaded_matmul_bitwise():
+    """oracle.kernels.THREADS > 1 (bench.py's CPU reference arm) tiles the output across
+    host threads; each element keeps the reference's sequential-k order: bit-identical."""
+    from oracle import kernels as K
+    r = np.random.default_rng(4)
+    for m, k, n in ((130, 300, 2500), (64, 784, 128), (1, 4096, 5000)):
+        a, b = r.uniform(-1, 1, (m, k)), r.uniform(-1, 1, (k, n))
+        a[0, 0] = -0.0
+        ref = K.matmul_seq(a, b)
+        K.THREADS = 4
+        try:
+            par = K.matmul_seq(a, b)
+        finally:
+            K.THREADS = 1
+        assert par.tobytes() == ref.tobytes()
