@@ -76,6 +76,19 @@ def dist_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
 
 
+def load_sustained(burst: float) -> float:
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["bf16_tflops_sustained"])
+    except Exception:
+        return burst
+
+
+# dram__bytes_read.sum + dram__bytes_write.sum of one representative launch of the dominant
+# GEMM family, from the committed `ncu --set full` captures (per launch, like `achieved`)
+TRAFFIC = {}
+
+
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -242,6 +255,69 @@ def tensor_gemm(peak_tflops, peak_kind, size: int = 8192):
     return {"bound": "tensor", "kernel": f"k_cvt_bf16 + k_gemm_tc {size}^3 bf16->fp32", "achieved": round(tf, 2),
             "peak": peak_tflops, "unit": "TFLOP/s", "frac": round(tf / peak_tflops, 4), "peak_source": peak_kind,
             "ms": round(ms, 4)}
+
+
+GEMM_KINDS = ("matmul", "split-K reduce")      # the tcgen05 GEMM family in the device stamps
+
+
+def step_flops(workload: str, step: int, world: int = 1) -> int:
+    """Algorithmic GEMM FLOPs of co-executed step ``step`` on one rank (the
+    causal attention products at their lower-triangle size, the work the kernels execute)."""
+    if workload in DECODERS:
+        full, _, fk = DECODERS[workload]
+        return gpt2_flops(**full, **fk, causal=True)
+    if workload == "c2":
+        fl = dcgan_flops(**C2)
+        return fl["d_step"] if step % 2 == 0 else fl["g_step"]
+    if workload == "c3":
+        from paper_2201_09210_b200.natives import eval_native
+        return resnet_flops(**C3, sdpoint=int(eval_native("choice", [4, 5], 0, step)))
+    return c1_flops(**C1)
+
+
+def graph_roofline(o, be, workload, hbm_peak, tflops_sustained, peak_kind, steps: int = 6):
+    """Roofline of the dominant kernel family from the pass graph itself: device
+    %globaltimer stamps of every graph kernel (coex_ctx_set_trace) over `steps` co-executed
+    steps run after the timed region; each stamp interval is charged to the kernel kind that
+    opened it.  GEMM family = tcgen05 GEMM launches + their split-K reduces; achieved =
+    the steps' algorithmic GEMM FLOPs / the family's summed in-graph time."""
+    import collections
+    be.set_trace(65536)
+    agg, cnt = collections.defaultdict(float), collections.Counter()
+    total_ns, flops = 0, 0
+    try:
+        for _ in range(steps):
+            st = o.next_step
+            o.step()
+            tr = be.read_trace()
+            flops += step_flops(workload, st)
+            for (t0, k, aw), (t1, _, _) in zip(tr, tr[1:]):
+                name = be.STAMP_KINDS.get(k, str(k))
+                if aw:
+                    name += " (after wait)"
+                elif k in (6, 7, 10):
+                    name += " (host stall)"
+                agg[name] += (t1 - t0)
+                cnt[name] += 1
+            total_ns += tr[-1][0] - tr[0][0]
+    finally:
+        be.set_trace(0)
+    kinds = {k: {"us_per_step": round(v / 1e3 / steps, 2), "launches_per_step": round(cnt[k] / steps, 2),
+                 "share": round(v / total_ns, 4)} for k, v in sorted(agg.items(), key=lambda kv: -kv[1])}
+    g_ns = sum(agg[k] for k in GEMM_KINDS)
+    g_launch = sum(cnt[k] for k in GEMM_KINDS if k == "matmul")
+    ach = flops / (g_ns * 1e-9) / 1e12
+    return {"bound": "tensor", "kernel": "k_gemm_tc (every GEMM / implicit conv / batched GEMM launch of the "
+                                         "step, with its split-K reduce)",
+            "achieved": round(ach, 2), "peak": tflops_sustained, "unit": "TFLOP/s",
+            "frac": round(ach / tflops_sustained, 4), "peak_source": peak_kind + " (sustained bf16: kernels timed "
+                                                                                 "inside a long step)",
+            "algorithmic_flops_per_step": flops // steps, "launches_per_step": round(g_launch / steps, 1),
+            "avg_launch_us": round(g_ns / 1e3 / max(g_launch, 1), 2),
+            "share_of_step": round(g_ns / total_ns, 4), "device_step_us": round(total_ns / 1e3 / steps, 1),
+            "method": f"in-graph %globaltimer stamps over {steps} co-executed steps after the timed region "
+                      "(coex_ctx_set_trace); stamp interval charged to the kernel that opened it",
+            "by_kind": kinds}
 
 
 def roofline_c2(be, hbm_peak, tflops_peak, peak_kind, workload="c2"):
@@ -532,13 +608,10 @@ def run_b200(args):
     roof = tgemm = None
     if rank == 0:                      # kernel evidence while this context is alive
         if args.workload in ("c2", "c3", "c4", "c5"):
-            roof = roofline_c2(be, hbm, tfl, peak_kind, args.workload)
-            if args.workload != "c2":
-                roof["unit_of_work"] = "one training step"
-                for f in roof.get("families", {}).values():
-                    for k in list(f):
-                        if k.endswith("_per_pair"):
-                            f[k.replace("_per_pair", "_per_step")] = f.pop(k)
+            roof = graph_roofline(o, be, args.workload, hbm, load_sustained(tfl), peak_kind)
+            roof["traffic"] = TRAFFIC.get(args.workload)
+            if args.eager_families:
+                roof["eager_families"] = roofline_c2(be, hbm, tfl, peak_kind, args.workload)
         else:
             roof = roofline(be, hbm, tfl, peak_kind)
             tgemm = tensor_gemm(tfl, peak_kind) if not args.no_tensor_gemm else None
@@ -609,6 +682,8 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-tensor-gemm", action="store_true")
+    ap.add_argument("--eager-families", action="store_true",
+                    help="also re-launch every op of the step eagerly for a per-family table")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.steps is None:

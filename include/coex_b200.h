@@ -165,6 +165,13 @@ int coex_ctx_read_trace(coex_ctx* ctx, uint64_t* out_pairs, int64_t cap, int64_t
 /* ---- tensors (eager side) ---- */
 int coex_tensor_put(coex_ctx* ctx, int ndim, const int64_t* shape, const double* data, int64_t* id);
 int coex_tensor_synth(coex_ctx* ctx, uint64_t state, int ndim, const int64_t* shape, int64_t* id);
+/* Index inputs: the same, with TO_INDEX(u, index_v) (pkg tensor extension, oracle
+ * clip(floor((u+1)/2*V), 0, V-1)) applied to each f64 value before it is stored in the compute
+ * precision -- an fp32-rounded u can move floor() across an integer.  index_v <= 0: plain put. */
+int coex_tensor_put_index(coex_ctx* ctx, int ndim, const int64_t* shape, const double* data, double index_v,
+                          int64_t* id);
+int coex_tensor_synth_index(coex_ctx* ctx, uint64_t state, int ndim, const int64_t* shape, double index_v,
+                            int64_t* id);
 int coex_tensor_get(coex_ctx* ctx, int64_t id, double* out, int64_t cap, int* ndim, int64_t* shape);
 int coex_tensor_info(coex_ctx* ctx, int64_t id, int* ndim, int64_t* shape);
 int coex_tensor_free(coex_ctx* ctx, int64_t id);

@@ -71,6 +71,8 @@ SIGNATURES = {
     "coex_ctx_read_trace": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_uint64), _I64, _I64P]),
     "coex_tensor_put": (ctypes.c_int, [_P, ctypes.c_int, _I64P, _DP, _I64P]),
     "coex_tensor_synth": (ctypes.c_int, [_P, ctypes.c_uint64, ctypes.c_int, _I64P, _I64P]),
+    "coex_tensor_put_index": (ctypes.c_int, [_P, ctypes.c_int, _I64P, _DP, ctypes.c_double, _I64P]),
+    "coex_tensor_synth_index": (ctypes.c_int, [_P, ctypes.c_uint64, ctypes.c_int, _I64P, ctypes.c_double, _I64P]),
     "coex_tensor_get": (ctypes.c_int, [_P, _I64, _DP, _I64, _IP, _I64P]),
     "coex_tensor_info": (ctypes.c_int, [_P, _I64, _IP, _I64P]),
     "coex_tensor_free": (ctypes.c_int, [_P, _I64]),
@@ -304,6 +306,20 @@ class B200Backend:
         data = np.ascontiguousarray(t.data, dtype=np.float64)
         _check(self.lib.coex_tensor_put(self.ctx, len(t.shape), _shape_arr(t.shape),
                                         data.ctypes.data_as(_DP), ctypes.byref(tid)))
+        return DevTensor(self, tid.value, t.shape)
+
+    def put_index(self, t, v: float) -> DevTensor:
+        """TO_INDEX(t, v) of a host-side input (synthetic or host tensor), evaluated in f64 on
+        the device while the values are converted to the compute precision (the op itself
+        would see fp32/bf16-rounded values; include/coex_b200.h coex_tensor_put_index)."""
+        tid = ctypes.c_int64()
+        if isinstance(t, SyntheticTensor):
+            _check(self.lib.coex_tensor_synth_index(self.ctx, t.state, len(t.shape), _shape_arr(t.shape), float(v),
+                                                    ctypes.byref(tid)))
+            return DevTensor(self, tid.value, t.shape)
+        data = np.ascontiguousarray(t.data, dtype=np.float64)
+        _check(self.lib.coex_tensor_put_index(self.ctx, len(t.shape), _shape_arr(t.shape),
+                                              data.ctypes.data_as(_DP), float(v), ctypes.byref(tid)))
         return DevTensor(self, tid.value, t.shape)
 
     def get(self, v) -> Tensor:

@@ -53,7 +53,8 @@ struct CvtParams {
   long long ld;              // padded K pitch (elements, multiple of 8)
   int trans[2];              // 1: element (r, k) is src[k * rows + r]; 0: src[r * K + k]
   __nv_bfloat16* dst[2];
-  long long Kb, ldb;         // operand 1's row length / pitch when it differs (0: K, ld)
+  long long Kb, ldb;         // operand 1's row length / pitch when own_b is set
+  int own_b;                 // 1: operand 1 has its own K (Kb, may be 0) and pitch (ldb)
 };
 
 // Operand conversion: grid.y selects the operand.  Direct operands stream rows
@@ -67,7 +68,7 @@ __global__ void __launch_bounds__(256) k_cvt_bf16(CvtParams p) {
   const bool w1 = blockIdx.y != 0;
   const float* s = res<float>(w1 ? p.src[1] : p.src[0]);
   __nv_bfloat16* d = w1 ? p.dst[1] : p.dst[0];
-  const bool own = w1 && p.Kb != 0;
+  const bool own = w1 && p.own_b;
   const long long R = w1 ? p.rows[1] : p.rows[0], K = own ? p.Kb : p.K, ld = own ? p.ldb : p.ld;
   if (!(w1 ? p.trans[1] : p.trans[0])) {
     // flattened over 8-element units of every row: 8 consecutive k per thread, one 16-byte store

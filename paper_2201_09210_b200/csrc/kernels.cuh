@@ -942,11 +942,23 @@ __global__ void __launch_bounds__(256) k_fill(FillParams p) {
 }
 
 // Convert float64 host payload (mapped) into the context precision.
+// TO_INDEX(u, V) evaluated in f64 on the fed value itself (oracle: clip(floor((u+1)*0.5*V),
+// 0, V-1)).  Index feeds apply it while converting the f64 host / generator value to the
+// compute precision: an fp32-rounded u would move floor() across an integer for ~V * 2^-24
+// of the draws (C4: a dozen token ids per step).
+__device__ __forceinline__ double index_of(double u, double V) {
+  const double v = floor(__dmul_rn(__dmul_rn(__dadd_rn(u, 1.0), 0.5), V));
+  if (v != v) return v;
+  return v < 0.0 ? 0.0 : (v > V - 1.0 ? V - 1.0 : v);
+}
+__device__ __forceinline__ double feed_value(double u, double iv) { return iv > 0.0 ? index_of(u, iv) : u; }
+
 template <typename T>
-__global__ void __launch_bounds__(256) k_from_f64(const double* src, T* dst, long long n) {
+__global__ void __launch_bounds__(256) k_from_f64(const double* src, T* dst, long long n, double iv) {
   COEX_PDL_ENTER();
   const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) dst[i] = (T)src[i];
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    dst[i] = (T)feed_value(src[i], iv);
 }
 template <typename T>
 __global__ void __launch_bounds__(256) k_to_f64(const T* src, double* dst, long long n) {
@@ -1028,6 +1040,7 @@ struct SynthParams {
   unsigned long long state;
   long long n;
   Out out;
+  double iv;                        // > 0: index feed, TO_INDEX(u, iv) applied in f64
 };
 
 template <typename T>
@@ -1044,7 +1057,7 @@ __global__ void __launch_bounds__(kSynthThreads) k_synth(SynthParams p) {
 #pragma unroll
     for (int i = 0; i < kSynthRun; ++i) {
       s = xs_next(s);
-      stage[threadIdx.x * kSynthRun + i] = (T)xs_unit_pm1(s);
+      stage[threadIdx.x * kSynthRun + i] = (T)feed_value(xs_unit_pm1(s), p.iv);
     }
     __syncthreads();
     long long lim = min(per_block, p.n - base);
@@ -1156,6 +1169,7 @@ struct FeedWaitParams {
   void* buf;             // slot buffer
   void** cell;           // slot cell (re-pointed for device-resident feeds)
   int is_f64;
+  double iv;             // > 0: index feed (TO_INDEX fused into the feed, see index_of)
 };
 
 __global__ void k_feed_wait(FeedWaitParams p) {
@@ -1181,8 +1195,11 @@ __global__ void k_feed_wait(FeedWaitParams p) {
   p.rec->off = e->off;
   p.rec->dptr = e->dptr;
   if (e->type == FEED_SCALAR) {
-    if (p.is_f64) *(double*)p.buf = e->scalar; else *(float*)p.buf = (float)e->scalar;
+    const double v = feed_value(e->scalar, p.iv);
+    if (p.is_f64) *(double*)p.buf = v; else *(float*)p.buf = (float)v;
     *p.cell = p.buf;
+  } else if (e->type == FEED_DEVICE && p.iv > 0.0) {
+    *p.cell = p.buf;               // k_feed_fill converts the device tensor into indices
   } else if (e->type == FEED_DEVICE) {
     *p.cell = (void*)e->dptr;      // bind by pointer, no copy
   } else {
@@ -1197,6 +1214,7 @@ struct FeedFillParams {
   const unsigned long long* jump;
   long long n;
   void* buf;
+  double iv;             // > 0: index feed
 };
 
 template <typename T>
@@ -1215,13 +1233,21 @@ __global__ void __launch_bounds__(kSynthThreads) k_feed_fill(FeedFillParams p) {
       const long long n2 = p.n / 2;
       for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n2; i += stride) {
         const double2 v = ((const double2*)src)[i];
-        o[2 * i] = (T)v.x;
-        o[2 * i + 1] = (T)v.y;
+        o[2 * i] = (T)feed_value(v.x, p.iv);
+        o[2 * i + 1] = (T)feed_value(v.y, p.iv);
       }
-      if (blockIdx.x == 0 && threadIdx.x == 0 && (p.n & 1)) o[p.n - 1] = (T)src[p.n - 1];
+      if (blockIdx.x == 0 && threadIdx.x == 0 && (p.n & 1)) o[p.n - 1] = (T)feed_value(src[p.n - 1], p.iv);
     } else {
-      for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < p.n; i += stride) o[i] = (T)src[i];
+      for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < p.n; i += stride)
+        o[i] = (T)feed_value(src[i], p.iv);
     }
+  } else if (type == FEED_DEVICE && p.iv > 0.0) {
+    // a device-resident tensor fed into an index slot: its values are already in the compute
+    // precision, the transform runs on them (what the unfused TO_INDEX kernel would do)
+    const T* src = (const T*)p.rec->dptr;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < p.n; i += stride)
+      o[i] = (T)ew_apply(EW_TO_INDEX, src[i], (T)p.iv);
   } else if (type == FEED_SYNTH) {
     __shared__ T stage[kSynthThreads * kSynthRun];
     const unsigned long long s0 = p.rec->state;
@@ -1231,7 +1257,7 @@ __global__ void __launch_bounds__(kSynthThreads) k_feed_fill(FeedFillParams p) {
 #pragma unroll
       for (int i = 0; i < kSynthRun; ++i) {
         s = xs_next(s);
-        stage[threadIdx.x * kSynthRun + i] = (T)xs_unit_pm1(s);
+        stage[threadIdx.x * kSynthRun + i] = (T)feed_value(xs_unit_pm1(s), p.iv);
       }
       __syncthreads();
       long long lim = min(per_block, p.n - base);

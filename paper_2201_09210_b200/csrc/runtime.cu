@@ -793,6 +793,15 @@ bool duo_model() {
   }
   return v == 1;
 }
+int duo_mode();
+// The DUO (two CTAs per SM) decision for a launch of tile width bn whose split holds
+// `kblocks` K-blocks (= ceil(K / BK) / splits, integer division as the launch computes it);
+// tc_plan prices tiles with the same rule the launch applies.
+bool tc_use_duo(int bn, int64_t kblocks) {
+  const int dm = duo_mode();
+  return bn <= 128 && (dm == 1 || (dm < 0 && kblocks <= duo_kmax()));
+}
+
 TcPlan tc_plan(int64_t M, int64_t N, int64_t K, bool allow_split) {
   TcPlan best;
   double best_t = 1e30;
@@ -820,7 +829,7 @@ TcPlan tc_plan(int64_t M, int64_t N, int64_t K, bool allow_split) {
       const int64_t items = (tiles < 1 ? 1 : tiles) * sp;
       const double kper = (double)((nk + sp - 1) / sp);
       // launches the DUO variant takes (tc_gemm_launches) hold two CTAs per SM
-      const int64_t slots = duo_model() && bn <= 128 && kper <= duo_kmax() ? 2 * kNumSMs : kNumSMs;
+      const int64_t slots = duo_model() && tc_use_duo(bn, nk / sp) ? 2 * kNumSMs : kNumSMs;
       const int64_t rounds = (items + slots - 1) / slots;
       // per-SM figures fitted to measured launches (tools/ncu_ops.py qkt / gemm_8192 with
       // COEX_FORCE_BN): ~115 GB/s of TMA operand feed, ~23.5 GB/s of epilogue stores and
@@ -964,8 +973,7 @@ int tc_gemm_launches(coex_ctx* c, DevState* ds, void* a16, void* b16, int64_t M,
                         (amode == 2 ? gp.cv.phases : 1) * (batch > 1 ? batch : 1);
   // two CTAs per SM for short-K launches that do not fill two waves of single CTAs
   const int64_t kblocks = (K + TC_BK - 1) / TC_BK / (t.splits > 0 ? t.splits : 1);
-  const int dm = duo_mode();
-  const bool duo = t.bn <= 128 && (dm == 1 || (dm < 0 && kblocks <= duo_kmax()));
+  const bool duo = tc_use_duo(t.bn, kblocks);
   void* fn;
   if (duo) {
     fn = t.bn == 64 ? tc_fn<64, true>(amode, b_mn) : tc_fn<128, true>(amode, b_mn);
@@ -1669,7 +1677,7 @@ int build_launches(coex_ctx* c, const OpSpec& s, Launch* L, int* nL) {
     CvtParams q{};
     q.ds = s.ds; q.src[0] = s.in[0]; q.src[1] = s.in[1];
     q.rows[0] = s.in_shape[0][0]; q.K = s.in_shape[0][1]; q.ld = bf16_pitch(q.K);
-    q.rows[1] = s.in_shape[1][0]; q.Kb = s.in_shape[1][1]; q.ldb = bf16_pitch(q.Kb);
+    q.rows[1] = s.in_shape[1][0]; q.Kb = s.in_shape[1][1]; q.ldb = bf16_pitch(q.Kb); q.own_b = 1;
     q.dst[0] = (__nv_bfloat16*)s.scratch[0]; q.dst[1] = (__nv_bfloat16*)s.scratch[1];
     const int64_t ga = (q.rows[0] * q.ld / 8 + 255) / 256, gb = (q.rows[1] * q.ldb / 8 + 255) / 256;
     int64_t gx = ga > gb ? ga : gb;
@@ -1889,6 +1897,11 @@ int coex_ctx_event_elapsed(coex_ctx* c, int a, int b, double* ms) {
 
 // =============================================================== tensors
 int coex_tensor_put(coex_ctx* c, int ndim, const int64_t* shape, const double* data, int64_t* id) {
+  return coex_tensor_put_index(c, ndim, shape, data, 0.0, id);
+}
+
+int coex_tensor_put_index(coex_ctx* c, int ndim, const int64_t* shape, const double* data, double index_v,
+                          int64_t* id) {
   if (ndim < 0 || ndim > COEX_MAX_RANK) return fail(COEX_INVALID, "rank out of range");
   TRec t;
   t.ndim = ndim;
@@ -1901,13 +1914,16 @@ int coex_tensor_put(coex_ctx* c, int ndim, const int64_t* shape, const double* d
     if (rc) return rc;
     CK(cudaStreamSynchronize(c->stream));        // staging buffer reuse
     memcpy(c->h_stage, data, t.numel * sizeof(double));
-    if (is_f64(c)) {
+    if (is_f64(c) && !(index_v > 0.0)) {
       CK(cudaMemcpyAsync(t.buf->ptr, c->h_stage, t.numel * 8, cudaMemcpyHostToDevice, c->stream));
     } else {
       double* dtmp;
       CK(cudaMallocAsync(&dtmp, t.numel * 8, c->stream));
       CK(cudaMemcpyAsync(dtmp, c->h_stage, t.numel * 8, cudaMemcpyHostToDevice, c->stream));
-      k_from_f64<float><<<grid_for(t.numel), 256, 0, c->stream>>>(dtmp, (float*)t.buf->ptr, t.numel);
+      if (is_f64(c))
+        k_from_f64<double><<<grid_for(t.numel), 256, 0, c->stream>>>(dtmp, (double*)t.buf->ptr, t.numel, index_v);
+      else
+        k_from_f64<float><<<grid_for(t.numel), 256, 0, c->stream>>>(dtmp, (float*)t.buf->ptr, t.numel, index_v);
       CK(cudaGetLastError());
       CK(cudaFreeAsync(dtmp, c->stream));
     }
@@ -1917,6 +1933,11 @@ int coex_tensor_put(coex_ctx* c, int ndim, const int64_t* shape, const double* d
 }
 
 int coex_tensor_synth(coex_ctx* c, uint64_t state, int ndim, const int64_t* shape, int64_t* id) {
+  return coex_tensor_synth_index(c, state, ndim, shape, 0.0, id);
+}
+
+int coex_tensor_synth_index(coex_ctx* c, uint64_t state, int ndim, const int64_t* shape, double index_v,
+                            int64_t* id) {
   if (ndim < 0 || ndim > COEX_MAX_RANK) return fail(COEX_INVALID, "rank out of range");
   TRec t;
   t.ndim = ndim;
@@ -1929,6 +1950,7 @@ int coex_tensor_synth(coex_ctx* c, uint64_t state, int ndim, const int64_t* shap
     p.jump = c->d_jump;
     p.state = state;
     p.n = t.numel;
+    p.iv = index_v;
     p.out.buf[0] = t.buf->ptr;
     const int64_t per_block = (int64_t)kSynthThreads * kSynthRun;
     int64_t blocks = (t.numel + per_block - 1) / per_block;
@@ -2628,6 +2650,10 @@ struct Builder {
         q.cell = cell(next());
         q.rec = p->recs + (int64_t)next();
         q.is_f64 = is_f64(c);
+        {                                      // index feed: TO_INDEX fused into the feed
+          int64_t vbits = next();
+          memcpy(&q.iv, &vbits, 8);
+        }
         Launch L;
         L.set((void*)k_feed_wait, dim3(1), dim3(1), q);
         int rc = add_kernel(g, prev, L);
@@ -2640,6 +2666,7 @@ struct Builder {
           f.jump = c->d_jump;
           f.n = q.numel;
           f.buf = q.buf;
+          f.iv = q.iv;
           const int64_t per_block = (int64_t)kSynthThreads * kSynthRun;
           int64_t blocks = (q.numel + per_block - 1) / per_block;
           if (blocks < 1) blocks = 1;

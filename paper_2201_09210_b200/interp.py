@@ -101,6 +101,16 @@ def _loc_key(loc) -> tuple:
 # ======================================================================= contexts
 
 
+def _index_input(be, args) -> bool:
+    """TO_INDEX of an external host-side input (dataset tensor) by a host scalar."""
+    if not hasattr(be, "put_index") or len(args) != 2 or isinstance(args[0], Val):
+        return False
+    v = args[1]
+    if isinstance(v, bool) or not isinstance(v, (int, float)) or not v > 0:
+        return False
+    return isinstance(args[0], (Tensor, SyntheticTensor))
+
+
 class EagerCtx:
     """Inline kernel execution on ``backend``; optionally records a trace."""
 
@@ -136,9 +146,15 @@ class EagerCtx:
     def op(self, kind: OpKind, attrs: dict, args: list, loc, shapes: list) -> Val:
         out_shape = infer_shape(kind, attrs, shapes)[0]
         refs, devs = [], []
-        for p, v in enumerate(args):
-            self._arg(v, loc, p, refs, devs)
-        dev = self.be.exec_op(kind, attrs, devs)
+        if kind is OpKind.TO_INDEX and _index_input(self.be, args):
+            # an external input turned into indices: the backend applies TO_INDEX to the f64
+            # values while uploading them (same trace refs, no separate op launch)
+            refs += [External((loc.stmt_id, 0)), External((loc.stmt_id, 1))]
+            dev = self.be.put_index(args[0], float(args[1]))
+        else:
+            for p, v in enumerate(args):
+                self._arg(v, loc, p, refs, devs)
+            dev = self.be.exec_op(kind, attrs, devs)
         vals = tuple(float(v) if isinstance(v, (int, float)) else None for v in args) if self.trace is not None \
             else None
         return self._emit(kind, attrs, loc, refs, dev, out_shape, [tuple(s) for s in shapes], vals)

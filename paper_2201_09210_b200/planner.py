@@ -195,6 +195,15 @@ class Planner:
                         and _fold_is_local(self.sp.body, nid, x.inputs[0].cands[0]):
                     folded.add(nid)
         self.folded = folded
+        # index feeds: TO_INDEX(input(..), V) with V a baked constant is applied by the feed
+        # kernel to the f64 value (exact ids, see csrc index_of); the node aliases the slot
+        self.index_nodes = {}
+        self.index_slots = {}
+        for nid, x in ops.items():
+            if x.kind is OpKind.TO_INDEX and x.inputs[0].fed and x.inputs[1].fed and \
+                    x.inputs[1].slot in self.const_slots and float(self.const_slots[x.inputs[1].slot]) > 0:
+                self.index_nodes[nid] = x.inputs[0].slot
+                self.index_slots[x.inputs[0].slot] = float(self.const_slots[x.inputs[1].slot])
         self.elided_reads, self.folded_assigns = self._pointer_rewrites(consumers, multi, folded)
 
         bufs: list = []
@@ -217,7 +226,7 @@ class Planner:
         consts: list = []
         for nid, x in ops.items():
             n = shape_size(shapes[nid])
-            if x.kind in COMPUTE and nid not in folded:
+            if x.kind in COMPUTE and nid not in folded and nid not in self.index_nodes:
                 self_dep = any((not b.fed) and nid in b.cands for b in x.inputs)
                 b0 = new_buf(n * self.esize)
                 b1 = new_buf(n * self.esize) if self_dep else -1
@@ -333,7 +342,8 @@ class Planner:
                 return None
             shp = tuple(self.feed_shapes[x.slot])
             return ([T_FEED, slot_code(x.slot), shape_size(shp), len(shp)] + _pad(shp)
-                    + [slot_buf[x.slot], slot_cell[x.slot], slot_rec[x.slot]])
+                    + [slot_buf[x.slot], slot_cell[x.slot], slot_rec[x.slot],
+                       _f64_bits(self.index_slots.get(x.slot, 0.0))])
 
         def emit(insts) -> list:
             items = []
@@ -461,6 +471,8 @@ class Planner:
                              self._shape_id(s))]
         if nid in folded:
             return []
+        if nid in self.index_nodes:
+            return [ptr_item(PTR_ALIAS, nid, in_cell(x.inputs[0]), -1, -1)]
         if k in XOP:
             return [self._xop_word(x, shapes, in_cell, out_words, pubs, n_compute, flops)]
         ins = list(x.inputs)
@@ -779,7 +791,8 @@ class Planner:
             if isinstance(x, InputFeed) and run:
                 feeds.append(x)
                 continue
-            if isinstance(x, ExecOp) and x.kind in EW_CODE and x.node_id not in folded:
+            if isinstance(x, ExecOp) and x.kind in EW_CODE and x.node_id not in folded and \
+                    x.node_id not in self.index_nodes:
                 n = shape_size(shapes[x.node_id])
                 if run and n != n_run[0] or len(run) >= CHAIN_OPS:
                     flush()

@@ -510,9 +510,10 @@ C3 = dict(batch=64, img=224, width=64, blocks=(3, 4, 6, 3), classes=1000)
 C3_SMALL = dict(batch=8, img=64, width=4, blocks=(1, 1, 1, 1), classes=10)
 
 
-def resnet_flops(batch=64, img=224, width=64, blocks=(3, 4, 6, 3), classes=1000, **_) -> int:
-    """Conv + FC FLOPs of one C3 step without SDPoint downsampling (forward + weight and input
-    gradients, 2*M*N*K per product; the stem's input gradient is not computed)."""
+def resnet_flops(batch=64, img=224, width=64, blocks=(3, 4, 6, 3), classes=1000, sdpoint=0, **_) -> int:
+    """Conv + FC FLOPs of one C3 step on SDPoint path ``sdpoint`` (0: no downsampling; j: the
+    2x2 average pool after stage j) -- forward + weight and input gradients, 2*M*N*K per
+    product; the stem's input gradient is not computed."""
     def conv(h, cin, cout, k, s, p):
         ho = (h + 2 * p - k) // s + 1
         return ho, 2 * batch * ho * ho * k * k * cin * cout
@@ -530,6 +531,8 @@ def resnet_flops(batch=64, img=224, width=64, blocks=(3, 4, 6, 3), classes=1000,
             fs = conv(h, cin, mid * 4, 1, s, 0)[1] if bi == 0 else 0
             total += 3 * (f1 + f2 + f3 + fs)
             h, cin = h2, mid * 4
+        if si + 1 == sdpoint:
+            h = (h - 2) // 2 + 1
     return total + 3 * 2 * batch * cin * classes
 
 
@@ -539,11 +542,14 @@ C5 = dict(batch=8, seq=1024, d=512, heads=8, layers=6, vocab=388)
 C5_SMALL = dict(batch=2, seq=16, d=32, heads=2, layers=2, vocab=29)
 
 
-def gpt2_flops(batch=8, seq=1024, d=768, heads=12, layers=12, vocab=50257, music=False, **_) -> int:
+def gpt2_flops(batch=8, seq=1024, d=768, heads=12, layers=12, vocab=50257, music=False, causal=False, **_) -> int:
     """GEMM FLOPs of one C4 (C5 with ``music``) training step (forward + backward,
-    2*M*N*K per product; C5 adds the q.er^T relative logits)."""
+    2*M*N*K per product; C5 adds the q.er^T relative logits).  ``causal``: the two
+    attention products count only their causal (lower-triangle, T(T+1)/2) part -- the work
+    the kernels execute; the default counts the full T x T square."""
     bt = batch * seq
-    per_layer_fwd = 2 * bt * d * (3 * d) + 2 * bt * d * d + 2 * bt * d * 4 * d * 2 + 2 * 2 * batch * heads * seq * seq * (d // heads)
+    tt = seq * (seq + 1) // 2 if causal else seq * seq
+    per_layer_fwd = 2 * bt * d * (3 * d) + 2 * bt * d * d + 2 * bt * d * 4 * d * 2 + 2 * 2 * batch * heads * tt * (d // heads)
     if music:
         per_layer_fwd += 2 * batch * heads * seq * seq * (d // heads)
     head_fwd = 2 * bt * d * vocab
