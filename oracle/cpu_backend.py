@@ -35,9 +35,10 @@ from paper_2201_09210_b200.runner_api import PassResult
 from paper_2201_09210_b200.tensor import OpKind, Tensor
 from paper_2201_09210_b200.trace_graph import CaseDecision, LoopDecision
 
-from .kernels import execute_kernel
+from .kernels import bn_sync, execute_kernel
 
 _NEED = object()
+SYNC_BN = (OpKind.BATCHNORM, OpKind.BATCHNORM_DX, OpKind.BN_DGAMMA)
 
 
 class ChannelSet:
@@ -152,7 +153,11 @@ class _Runner:
             out = self.vs.read(x.attrs["var_name"])
         else:
             ins = [self._resolve(b) for b in x.inputs]
-            out = execute_kernel(x.kind, x.attrs, ins)[0]
+            if self.dp is not None and "rows" in x.attrs and x.kind in SYNC_BN:
+                # synchronised batch norm of a row shard (dp.py marks it with the global rows)
+                out = Tensor._wrap(bn_sync(x.kind, [t.data for t in ins], x.attrs["rows"], self.dp.allreduce))
+            else:
+                out = execute_kernel(x.kind, x.attrs, ins)[0]
             if x.kind is OpKind.ASSIGN_VAR:
                 self.vs.overlay[x.attrs["var_name"]] = out
         self.tick += 1

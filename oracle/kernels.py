@@ -169,6 +169,37 @@ def bn_stats(x2: np.ndarray):
     return d, rstd
 
 
+def bn_sync(kind, x, global_rows: float, allreduce) -> np.ndarray:
+    """Synchronised batch norm of one rank's row shard (data parallel; the device's
+    k_colstats raw mode + all-reduce + k_bn_finalize): rank-local column sums of x, x^2, dy,
+    dy*x summed over the ranks by ``allreduce``, statistics over the GLOBAL batch
+    (``global_rows``), then the local rows normalised with them.  Equals BATCHNORM /
+    BATCHNORM_DX / BN_DGAMMA of the concatenated global batch up to summation order."""
+    c = x[0].shape[-1]
+    x2 = x[0].reshape(-1, c)
+    dy = None if kind is OpKind.BATCHNORM else x[-1].reshape(-1, c)
+    raw = np.zeros((4, c))
+    raw[0] = col_sum_seq(x2)
+    raw[1] = col_sum_seq(x2 * x2)
+    if dy is not None:
+        raw[2] = col_sum_seq(dy)
+        raw[3] = col_sum_seq(dy * x2)
+    raw = np.asarray(allreduce(raw.reshape(-1), False)).reshape(4, c)
+    r = float(global_rows)
+    mean = raw[0] / r
+    var = np.maximum(raw[1] / r - mean * mean, 0.0)
+    rstd = 1.0 / np.sqrt(var + BN_EPS)
+    xhat = (x2 - mean) * rstd
+    if kind is OpKind.BATCHNORM:
+        return ((xhat * x[1]) + x[2]).reshape(x[0].shape)
+    sdx = rstd * (raw[3] - mean * raw[2])                 # global sum(dy * xhat)
+    if kind is OpKind.BN_DGAMMA:
+        return sdx
+    t = dy - raw[2] / r
+    t = t - xhat * (sdx / r)
+    return (t * (x[1] * rstd)).reshape(x[0].shape)
+
+
 def _windows(h, w, k, s, p, ho, wo):
     """(oy, ox, [(ky, kx, iy, ix) in (ky, kx) order, in-bounds taps only])."""
     for oy in range(ho):

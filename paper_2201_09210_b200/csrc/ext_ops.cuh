@@ -537,6 +537,9 @@ struct ColStatsParams {
   int extra;                 // COL_BN_DX fused backward: also write dgamma / dbeta [C]
   Out out_g, out_b;
   long long chunk_rows;      // BULK: rows per streamed chunk (a multiple of the rows per pass)
+  int raw;                   // synchronised batch norm (data parallel): no shift; the last block
+                             // writes the raw [C][4] sums sum(x), sum(x^2), sum(dy), sum(dy*x) to
+                             // `stats` for the cross-rank all-reduce and k_bn_finalize
 };
 
 // 1-D bulk copy global -> shared, completion counted on an mbarrier (BULK column statistics)
@@ -583,7 +586,7 @@ __global__ void __launch_bounds__(256) k_colstats(ColStatsParams p) {
     for (int v = 0; v < V; ++v) {
       a1[j][v] = a2[j][v] = a3[j][v] = a4[j][v] = 0.0;
       const long long c = (cc + (long long)j * L) * V + v;
-      sh[j][v] = (p.mode != COL_SUM_ROWS && j < slots && c < C) ? (double)x[c] : 0.0;
+      sh[j][v] = (p.mode != COL_SUM_ROWS && !p.raw && j < slots && c < C) ? (double)x[c] : 0.0;
     }
   if constexpr (BULK) {
     extern __shared__ __align__(128) unsigned char col_dsm[];
@@ -758,6 +761,14 @@ __global__ void __launch_bounds__(256) k_colstats(ColStatsParams p) {
       o[c] = (T)s1;
       continue;
     }
+    if (p.raw) {                                    // rank-local sums: all-reduced, then finalised
+      double* st = p.stats + c * 4;
+      st[0] = s1;
+      st[1] = s2;
+      st[2] = d1;
+      st[3] = d2;
+      continue;
+    }
     const double m1 = s1 / (double)R;
     const double mean = (double)x[c] + m1;
     double var = s2 / (double)R - m1 * m1;
@@ -795,6 +806,49 @@ __global__ void __launch_bounds__(256) k_colstats(ColStatsParams p) {
     if (t == 0 && p.out.late != nullptr)   // single finishing block publishes
       for (int i = 0; i < p.out.npub; ++i) *p.out.pub[i] = o;
   }
+}
+
+// Synchronised batch norm (data parallel): the all-reduced raw sums of every
+// rank's rows -> mean, rstd, mean(dy), mean(dy*xhat) over the GLOBAL batch (R = global rows),
+// the same finalisation as k_colstats with shift 0.  BN_DGAMMA writes sum(dy*xhat) (global,
+// replicated).  One block.
+struct BnFinalizeParams {
+  DevState* ds;
+  double* stats;             // [C][4] in: raw global sums; out: mean, rstd, mean(dy), mean(dy*xhat)
+  long long C;
+  double R;
+  int mode;                  // COL_BN, COL_BN_DX, COL_BN_DGAMMA
+  In a, b;                   // node operands (ping-pong output choice only)
+  Out out;                   // COL_BN_DGAMMA: [C]
+};
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_bn_finalize(BnFinalizeParams p) {
+  COEX_PDL_ENTER();
+  stamp(p.ds, SK_COLSTATS);
+  T* o = nullptr;
+  if (p.mode == COL_BN_DGAMMA) {
+    o = pick_out<T>(p.out, res<T>(p.a), p.b.cell || p.b.direct ? res<T>(p.b) : nullptr);
+    publish_early(p.out, o);
+  }
+  for (long long c = threadIdx.x; c < p.C; c += blockDim.x) {
+    double* st = p.stats + c * 4;
+    const double s1 = st[0], s2 = st[1], d1 = st[2], d2 = st[3];
+    const double mean = s1 / p.R;
+    double var = s2 / p.R - mean * mean;
+    if (var < 0.0) var = 0.0;
+    const double rstd = 1.0 / sqrt(var + kBnEps);
+    const double sdx = rstd * (d2 - mean * d1);      // sum(dy * xhat)
+    if (p.mode == COL_BN_DGAMMA) {
+      o[c] = (T)sdx;
+      continue;
+    }
+    st[0] = mean;
+    st[1] = rstd;
+    st[2] = d1 / p.R;
+    st[3] = sdx / p.R;
+  }
+  if (o) publish_late(p.out, o);
 }
 
 // ------------------------------------------------------------------ batch-norm apply

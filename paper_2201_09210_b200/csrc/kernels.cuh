@@ -53,7 +53,7 @@ enum StampKind {
   SK_FEED_WAIT = 7, SK_FEED_FILL = 8, SK_FETCH = 9, SK_GATE = 10, SK_COMMIT = 11, SK_END = 12,
   SK_AFTER_WAIT = 64, SK_FUSED = 13, SK_IM2COL = 14, SK_COL2IM = 15, SK_CVT = 16, SK_COLSTATS = 17,
   SK_BNAPPLY = 18, SK_SPLITK = 19, SK_SOFTMAX = 20, SK_SOFTMAX_GRAD = 21, SK_CE = 22, SK_BIAS = 23, SK_LN = 24,
-  SK_EMBED = 25, SK_COLSUM = 26, SK_SKEW = 27, SK_POOL = 28, SK_AXIS = 29
+  SK_EMBED = 25, SK_COLSUM = 26, SK_SKEW = 27, SK_POOL = 28, SK_AXIS = 29, SK_GUARD = 30
 };
 
 // Host <-> device rings in pinned, mapped host memory.
@@ -189,14 +189,16 @@ __device__ __forceinline__ void publish_late(const Out& o, void* out) {
   }
 }
 
-// Cancellation is enforced where it is observable: the spinners (decisions,
-// feeds, fetches) stop waiting, conditional nodes then run no body, the commit is skipped and
-// AssignVar leaves the overlay alone (k_ptr and the feed kernels test the flag).  Compute
-// kernels do not: a cancelled pass runs its remaining straight-line kernels and discards
-// them.  That is safe because every pointer cell holds valid memory at all times -- cells
-// start each pass at their build-time values (a buffer of the right size, or the program's
-// zero-filled spare buffer of the largest size) -- and it removes a dependent flag load from
-// every launch (~5 % of the C2 step).
+// Cancellation ("after cancel the pass stops within one kernel execution"):
+// the spinners (decisions, feeds, fetches) stop waiting, conditional nodes then run no body,
+// the commit is skipped and AssignVar leaves the overlay alone (k_ptr and the feed kernels
+// test the flag).  Compute kernels do not test it themselves (a dependent flag load at every
+// launch cost ~5 % of the C2 step); instead the builder cuts every straight-line list into
+// guarded segments: a one-thread k_guard reads the host's cancel word and sets an IF
+// conditional whose body is the next segment (COEX_CANCEL_EVERY kernels, default 16), so a
+// cancelled pass skips every later segment and runs at most the one in flight.  Cells start
+// each pass at their build-time values (a buffer of the right size, or the program's
+// zero-filled spare buffer of the largest size), so any prefix of kernels reads valid memory.
 __device__ __forceinline__ bool skip(const DevState* ds) {
   return ds != nullptr && *(volatile const int*)&ds->cancelled;
 }
@@ -1122,6 +1124,20 @@ __global__ void k_decide(DecideParams p) {
   ds->dec_head = idx + 1;
   p.mb->dec_consumed = idx + 1;
   cudaGraphSetConditional(p.handle, (unsigned)v);
+}
+
+// Segment guard: runs the next straight-line segment (an IF body) unless the pass is cancelled.
+struct GuardParams {
+  DevState* ds;
+  Mailbox* mb;
+  cudaGraphConditionalHandle handle;
+};
+__global__ void k_guard(GuardParams p) {
+  COEX_PDL_ENTER();
+  DevState* ds = p.ds;
+  stamp(ds, SK_GUARD);
+  if (!ds->cancelled && p.mb->cancel == ds->pass_id) ds->cancelled = 1;
+  cudaGraphSetConditional(p.handle, ds->cancelled ? 0u : 1u);
 }
 
 // Commit gate: the overlay may only be committed once the skeleton has

@@ -92,6 +92,17 @@ struct Launch {
   alignas(64) unsigned char params[8192];     // k_chain_multi carries up to 8 chain programs
   size_t psize = 0;
   void* args[1];
+  // collective instead of a kernel (fn == nullptr): in-place sum all-reduce of ar_count
+  // elements at ar_buf over the context's communicator (synchronised batch norm)
+  void* ar_buf = nullptr;
+  int64_t ar_count = 0;
+  int ar_f64 = 1;
+  void allreduce(void* b, int64_t n, bool f64) {
+    fn = nullptr;
+    ar_buf = b;
+    ar_count = n;
+    ar_f64 = f64 ? 1 : 0;
+  }
   template <typename P>
   void set(void* f, dim3 g, dim3 b, const P& p) {
     static_assert(sizeof(P) <= sizeof(params), "kernel params too large");
@@ -1458,8 +1469,31 @@ int build_xop_t(coex_ctx* c, const OpSpec& s, Launch* L, int* nL, size_t* ws_byt
       cp.counter = (unsigned int*)pv.take(16);
       cp.a = s.in[0];
       cp.b = s.nin > 1 ? s.in[1] : In{nullptr, nullptr, nullptr};
+      // synchronised batch norm (data parallel: dp.py marks a row-sharded batchnorm /
+      // batchnorm_dx / bn_dgamma with the GLOBAL row count): rank-local raw sums, an in-place
+      // all-reduce of the [C][4] doubles over the context's communicator, finalisation over
+      // the global batch, then the usual apply pass
+      const bool sync = s.value > 0.0 && s.kind != COEX_SUM_ROWS && s.kind != kBnBwdFused;
       if (!build) break;
-      if (s.kind == COEX_SUM_ROWS || s.kind == COEX_BN_DGAMMA) {
+      if (sync) {
+        if (c->comm == nullptr) return fail(COEX_BAD_ATTRS, "synchronised batch norm without a communicator");
+        cp.raw = 1;
+        cp.mode = s.kind == COEX_BATCHNORM || s.kind == kBnAct ? COL_BN
+                  : s.kind == COEX_BN_DGAMMA ? COL_BN_DGAMMA : COL_BN_DX;
+        if (s.kind == COEX_BN_DGAMMA) cp.dy = s.in[1];
+        else if (s.kind == COEX_BATCHNORM_DX) cp.dy = s.in[2];
+        cp.out = Out{};
+        L[*nL].set(colfn, dim3((unsigned)G), dim3(256), cp);
+        L[(*nL)++].smem = bulk_smem;
+        L[(*nL)++].allreduce(cp.stats, 4 * C, true);
+        BnFinalizeParams fp{};
+        fp.ds = s.ds; fp.stats = cp.stats; fp.C = C; fp.R = s.value; fp.mode = cp.mode;
+        fp.a = cp.a; fp.b = cp.b;
+        if (s.kind == COEX_BN_DGAMMA) fp.out = s.out;
+        L[(*nL)++].set(is_f64(c) ? (void*)k_bn_finalize<double> : (void*)k_bn_finalize<float>, dim3(1), dim3(256), fp);
+        if (s.kind == COEX_BN_DGAMMA) return COEX_OK;
+      }
+      if (!sync && (s.kind == COEX_SUM_ROWS || s.kind == COEX_BN_DGAMMA)) {
         cp.mode = s.kind == COEX_SUM_ROWS ? COL_SUM_ROWS : COL_BN_DGAMMA;
         if (s.kind == COEX_BN_DGAMMA) cp.dy = s.in[1];
         cp.out = s.out;
@@ -1467,16 +1501,18 @@ int build_xop_t(coex_ctx* c, const OpSpec& s, Launch* L, int* nL, size_t* ws_byt
         L[(*nL)++].smem = bulk_smem;
         return COEX_OK;
       }
-      cp.mode = (s.kind == COEX_BATCHNORM || s.kind == kBnAct) ? COL_BN : COL_BN_DX;
-      if (s.kind == COEX_BATCHNORM_DX || s.kind == kBnBwdFused) cp.dy = s.in[2];
-      cp.out = Out{};
-      if (s.kind == kBnBwdFused) {
-        cp.extra = 1;
-        cp.out_g = s.out2;
-        cp.out_b = s.out3;
+      if (!sync) {
+        cp.mode = (s.kind == COEX_BATCHNORM || s.kind == kBnAct) ? COL_BN : COL_BN_DX;
+        if (s.kind == COEX_BATCHNORM_DX || s.kind == kBnBwdFused) cp.dy = s.in[2];
+        cp.out = Out{};
+        if (s.kind == kBnBwdFused) {
+          cp.extra = 1;
+          cp.out_g = s.out2;
+          cp.out_b = s.out3;
+        }
+        L[*nL].set(colfn, dim3((unsigned)G), dim3(256), cp);
+        L[(*nL)++].smem = bulk_smem;
       }
-      L[*nL].set(colfn, dim3((unsigned)G), dim3(256), cp);
-      L[(*nL)++].smem = bulk_smem;
       BnApplyParams ap{};
       ap.ds = s.ds; ap.x = s.in[0]; ap.g = s.in[1]; ap.third = s.in[2]; ap.stats = cp.stats;
       ap.n = n; ap.C = C; ap.dx = s.kind != COEX_BATCHNORM && s.kind != kBnAct; ap.out = s.out;
@@ -1701,6 +1737,14 @@ int build_launches(coex_ctx* c, const OpSpec& s, Launch* L, int* nL) {
 }
 
 int launch_now(coex_ctx* c, Launch& L) {
+  if (L.fn == nullptr && L.ar_buf != nullptr) {
+    NcclApi& n = nccl();
+    if (!n.ok || c->comm == nullptr) return fail(COEX_CUDA_ERROR, "collective launch without a communicator");
+    if (n.all_reduce(L.ar_buf, L.ar_buf, (size_t)L.ar_count, L.ar_f64 ? kNcclDouble : kNcclFloat, kNcclSum, c->comm,
+                     c->stream))
+      return fail(COEX_CUDA_ERROR, "ncclAllReduce failed");
+    return COEX_OK;
+  }
   CK(cudaLaunchKernel(L.fn, L.grid, L.block, L.argv(), L.smem, c->stream));
   c->kernel_count++;
   return COEX_OK;
@@ -2269,7 +2313,7 @@ struct coex_prog {
   int64_t ncells = 0;
   FeedRecord* recs = nullptr;
   unsigned int* late = nullptr;       // late-publication counters
-  int64_t n_kernel_nodes = 0, n_cond_nodes = 0, n_compute = 0, n_collectives = 0;
+  int64_t n_kernel_nodes = 0, n_cond_nodes = 0, n_compute = 0, n_collectives = 0, n_guards = 0;
   std::vector<int> commit_vars;
   std::vector<int64_t> commit_bytes;
   std::unordered_map<int, std::vector<int64_t>> var_shapes;   // shape id -> dims
@@ -2405,10 +2449,31 @@ struct Builder {
 
   std::unordered_map<cudaGraphNode_t, bool> kernel_nodes;   // nodes created by add_kernel
   bool pdl = true;
+  int64_t cancel_every = 16;        // kernel nodes per cancel-guarded segment (0: no guards)
 
   // Kernel node after `*prev`.  Kernel -> kernel edges are programmatic (PDL): the node is
   // scheduled while its predecessor's last wave drains and synchronises in COEX_PDL_ENTER.
+  // NCCL all-reduce captured on a side stream into a child graph node after *prev.
+  int add_allreduce(cudaGraph_t g, cudaGraphNode_t* prev, void* b, int64_t count, int dtype, int op) {
+    NcclApi& n = nccl();
+    if (!n.ok || c->comm == nullptr) throw std::runtime_error("all-reduce in a plan without a communicator");
+    cudaGraph_t child;
+    CK(cudaStreamBeginCapture(c->cap_stream, cudaStreamCaptureModeRelaxed));
+    int r = n.all_reduce(b, b, (size_t)count, dtype, op, c->comm, c->cap_stream);
+    cudaError_t ce = cudaStreamEndCapture(c->cap_stream, &child);
+    if (r || ce != cudaSuccess) throw std::runtime_error("capturing ncclAllReduce failed");
+    cudaGraphNode_t node;
+    ce = cudaGraphAddChildGraphNode(&node, g, *prev ? prev : nullptr, *prev ? 1 : 0, child);
+    cudaGraphDestroy(child);
+    if (ce != cudaSuccess) throw std::runtime_error(std::string("child graph node: ") + cudaGetErrorString(ce));
+    *prev = node;
+    p->n_collectives++;
+    return COEX_OK;
+  }
+
   int add_kernel(cudaGraph_t g, cudaGraphNode_t* prev, Launch& L) {
+    if (L.fn == nullptr && L.ar_buf != nullptr)
+      return add_allreduce(g, prev, L.ar_buf, L.ar_count, L.ar_f64 ? kNcclDouble : kNcclFloat, kNcclSum);
     cudaKernelNodeParams kp = {};
     kp.func = L.fn;
     kp.gridDim = L.grid;
@@ -2448,14 +2513,56 @@ struct Builder {
     o.late = late ? p->late + (n_late++) : nullptr;
   }
 
+  // A straight-line list.  With cancel guards on (COEX_CANCEL_EVERY > 0, default 16) the
+  // list is cut into segments of about that many kernel nodes, each the body of an IF
+  // conditional set by a k_guard that reads the host's cancel word: a cancelled pass skips
+  // every later segment.  All-reduce child graphs stay at the list's own level.
   int seq(cudaGraph_t g, cudaGraphNode_t* prev) {
     if (next() != T_SEQ) throw std::runtime_error("expected SEQ");
     int64_t items = next();
+    cudaGraph_t body = nullptr;
+    cudaGraphNode_t bprev = nullptr;
+    int64_t seg0 = 0;
+    auto close = [&]() -> int {
+      if (body && bprev == nullptr) {            // segment without nodes: keep the body non-empty
+        cudaGraphNode_t e;
+        CK(cudaGraphAddEmptyNode(&e, body, nullptr, 0));
+      }
+      body = nullptr;
+      return COEX_OK;
+    };
     for (int64_t i = 0; i < items; ++i) {
-      int rc = item(g, prev);
+      const int64_t tag = pos < n ? w[pos] : -1;
+      const bool guardable = cancel_every > 0 && tag != T_ALLREDUCE;
+      if (body && (!guardable || p->n_kernel_nodes - seg0 >= cancel_every)) {
+        int rc = close();
+        if (rc) return rc;
+      }
+      if (guardable && !body) {
+        cudaGraphConditionalHandle h;
+        CK(cudaGraphConditionalHandleCreate(&h, g, 0, 0));
+        GuardParams gp{c->d_state, c->d_mb, h};
+        Launch L;
+        L.set((void*)k_guard, dim3(1), dim3(1), gp);
+        int rc = add_kernel(g, prev, L);
+        if (rc) return rc;
+        cudaGraphNodeParams cp = {};
+        cp.type = cudaGraphNodeTypeConditional;
+        cp.conditional.handle = h;
+        cp.conditional.type = cudaGraphCondTypeIf;
+        cp.conditional.size = 1;
+        cudaGraphNode_t node;
+        CK(cudaGraphAddNode(&node, g, prev, 1, &cp));
+        p->n_guards++;
+        *prev = node;
+        body = cp.conditional.phGraph_out[0];
+        bprev = nullptr;
+        seg0 = p->n_kernel_nodes;
+      }
+      int rc = body ? item(body, &bprev) : item(g, prev);
       if (rc) return rc;
     }
-    return COEX_OK;
+    return close();
   }
 
   int item(cudaGraph_t g, cudaGraphNode_t* prev) {
@@ -2601,23 +2708,9 @@ struct Builder {
         void* b = buf(next());
         const int64_t count = next();
         const int64_t avg = next();
-        NcclApi& n = nccl();
-        if (!n.ok || c->comm == nullptr) throw std::runtime_error("all-reduce in a plan without a communicator");
-        // Capture the collective on a side stream into a child graph (stream capture into
-        // an existing graph would also work; a child node keeps conditional bodies simple).
-        cudaGraph_t child;
-        CK(cudaStreamBeginCapture(c->cap_stream, cudaStreamCaptureModeRelaxed));
-        int r = n.all_reduce(b, b, (size_t)count, is_f64(c) ? kNcclDouble : kNcclFloat, avg ? kNcclAvg : kNcclSum,
-                             c->comm, c->cap_stream);
-        cudaError_t ce = cudaStreamEndCapture(c->cap_stream, &child);
-        if (r || ce != cudaSuccess) throw std::runtime_error("capturing ncclAllReduce failed");
-        cudaGraphNode_t node;
-        ce = cudaGraphAddChildGraphNode(&node, g, *prev ? prev : nullptr, *prev ? 1 : 0, child);
-        cudaGraphDestroy(child);
-        if (ce != cudaSuccess) throw std::runtime_error(std::string("child graph node: ") + cudaGetErrorString(ce));
-        *prev = node;
-        p->n_collectives++;
-        return COEX_OK;
+        // the collective is captured on a side stream into a child graph node (a child node
+        // keeps conditional bodies simple)
+        return add_allreduce(g, prev, b, count, is_f64(c) ? kNcclDouble : kNcclFloat, avg ? kNcclAvg : kNcclSum);
       }
       case T_PTR: {
         PtrParams q{};
@@ -2779,6 +2872,12 @@ int coex_prog_build(coex_ctx* c, const int64_t* plan, int64_t nwords, const doub
   {
     const char* e = getenv("COEX_PDL");
     b.pdl = !(e && e[0] == '0');
+    const char* ce = getenv("COEX_CANCEL_EVERY");
+    if (ce) b.cancel_every = atoll(ce);
+    // data parallel over several ranks: every rank must run every collective it reaches, so
+    // straight-line segments are not guarded (a rank that observes its cancel earlier than
+    // its peers would skip an all-reduce they already entered); spinners still stop
+    if (c->comm != nullptr && c->world > 1) b.cancel_every = 0;
   }
   try {
     if (b.next() != kPlanMagic || b.next() != kPlanVersion) throw std::runtime_error("bad plan header");

@@ -24,10 +24,13 @@ collective, still correct.
 Extension ops (C2): convolutions of a row-sharded NHWC activation with a
 replicated weight stay row-sharded (S0); a weight gradient ``conv2d_dw`` of two
 row-sharded operands, ``sum_rows`` and ``bn_dgamma`` over row-sharded values are
-P+; ``batchnorm`` / ``batchnorm_dx`` of a row-sharded activation normalise with
-the statistics of the rank's own rows (per-replica batch statistics -- the
-semantics of data-parallel training without synchronised batch norm), so their
-results stay S0.
+P+; ``batchnorm`` / ``batchnorm_dx`` / ``bn_dgamma`` of a row-sharded activation
+are *synchronised*: the rewrite stamps them with the global row count (attr
+``rows``) and the device computes rank-local raw column sums, all-reduces them
+(NCCL, inside the op's launch sequence) and normalises with the statistics of
+the GLOBAL batch -- the single-device math (SPEC.md:466 sequential-order
+equality, up to summation order).  ``batchnorm`` / ``batchnorm_dx`` stay S0;
+``bn_dgamma`` is R (already the global sum).
 
 C4 ops: layernorm (rows), bias_add, causal softmax and its gradient, the batched
 GEMMs (batch = sequences x heads, sharded with the sequences) and the embedding
@@ -38,9 +41,8 @@ splits evenly over the ranks (row-major chunks stay contiguous); a transpose kee
 S0 when it leaves axis 0 in place.
 
 Parity: DP results equal the single-device run up to summation order
-(tolerance, not bitwise) -- tests/test_dp_gloo.py checks world size 2 on CPU.
-With per-replica batch-norm statistics the equality holds when every rank's rows
-have the statistics of the global batch (the test feeds duplicated halves).
+(tolerance, not bitwise) -- tests/test_dp_gloo.py checks world size 2 on CPU
+(distinct row shards, batch norm included).
 """
 
 from __future__ import annotations
@@ -115,6 +117,7 @@ class _Prop:
                         if len(shp) >= 1 and shp[0] == batch and batch % world == 0}
         self.state: dict = {}
         self.reduce_at: dict = {}       # node id -> avg flag
+        self.sync_bn: set = set()       # batch-norm family nodes over row shards (synchronised)
         self.kind: dict = {}
         for x in _iter(sp.body):
             if isinstance(x, ExecOp):
@@ -339,6 +342,11 @@ class _Prop:
                 raise Unshardable(f"node {x.node_id}: batch-norm gradient sharded unlike its input")
             if xs == S1:
                 raise Unshardable(f"node {x.node_id}: column-sharded batch-norm input")
+            if xs == S0:
+                self.sync_bn.add(x.node_id)     # synchronised batch statistics
+            elif xs in PARTIAL:
+                self.needs_r_binding(x.inputs[0])
+                return R
             return xs
         # BN_DGAMMA / SUM_ROWS: column sums over the rows
         if any(st == S1 for st in ins):
@@ -347,10 +355,17 @@ class _Prop:
             return R
         if any(st == R for st in ins):
             raise Unshardable(f"node {x.node_id}: {k.value} of replicated and sharded operands")
+        if k is OpKind.BN_DGAMMA:
+            self.sync_bn.add(x.node_id)         # synchronised: the global sum(dy * xhat)
+            return R
         return PSUM
 
+    def shape_of(self, b):
+        """Global shape of binding b."""
+        return self.feed_shapes.get(b.slot) if b.fed else self.node_shapes.get(b.cands[0])
+
     def _rank0(self, b):
-        shp = self.feed_shapes.get(b.slot) if b.fed else self.node_shapes.get(b.cands[0])
+        shp = self.shape_of(b)
         return shp is not None and shape_size(shp) == 1
 
     def walk(self, insts):
@@ -379,6 +394,7 @@ class _Prop:
     def run(self):
         for _ in range(8):
             before = dict(self.reduce_at)
+            self.sync_bn = set()            # recomputed by every walk: the last one is exact
             changed = self.walk(self.sp.body)
             # a node marked for all-reduce on an earlier walk may have become replicated since
             # (its own partial input got reduced in place for another consumer): its mark is
@@ -400,6 +416,10 @@ def _rewrite(insts, prop: _Prop) -> list:
                 y = ExecOp(x.node_id, x.kind, dict(x.attrs, target_shape=tuple(tgt)), x.inputs)
             if x.kind is OpKind.CROSS_ENTROPY_GRAD and prop.state.get(x.node_id) == S0:
                 rows = prop.node_shapes[x.node_id][0]        # divide by the global row count
+                y = ExecOp(x.node_id, x.kind, dict(x.attrs, rows=float(rows)), x.inputs)
+            if x.node_id in prop.sync_bn:
+                shp = prop.shape_of(x.inputs[0])             # normalise over the global rows
+                rows = shape_size(shp) // shp[-1]
                 y = ExecOp(x.node_id, x.kind, dict(x.attrs, rows=float(rows)), x.inputs)
             out.append(y)
             if x.node_id in prop.reduce_at:

@@ -568,7 +568,7 @@ class Planner:
         used = set()
         for d in dxs:
             xb, gb, dyb = d.inputs
-            if xb.fed or dyb.fed:
+            if xb.fed or dyb.fed or "rows" in d.attrs:     # synchronised (data parallel): unfused
                 continue
             g = next((y for y in insts if isinstance(y, ExecOp) and y.kind is OpKind.BN_DGAMMA
                       and y.node_id not in used and y.inputs[0] == xb and y.inputs[1] == dyb), None)

@@ -29,20 +29,6 @@ SMALL_C4_ADAM = gpt2_program(steps=4, batch=BATCH, seq=8, d=16, heads=2, layers=
 SMALL_C5 = music_transformer_program(steps=8, batch=BATCH, seq=8, d=16, heads=2, layers=2, vocab=23)
 
 
-class DupHalves(SyntheticDataset):
-    """Batch inputs whose second half repeats the first: per-replica batch-norm statistics
-    (C2 data parallelism) then equal the global-batch statistics, so the DP run must match
-    the single-process run at the global batch."""
-
-    def next(self, name, shape, step):
-        t = super().next(name, shape, step)
-        if len(shape) >= 1 and shape[0] == BATCH:
-            d = t.materialize().data.copy() if hasattr(t, "materialize") else np.array(t.data)
-            d[BATCH // 2:] = d[:BATCH // 2]
-            return Tensor(shape, d)
-        return t
-
-
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -51,7 +37,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, src, out, dup=False):
+def _worker(rank, world, port, src, out):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
 
@@ -63,7 +49,7 @@ def _worker(rank, world, port, src, out, dup=False):
         return t.numpy()
 
     be = CpuBackend(dp=DPGroup(rank, world, BATCH, allreduce))
-    ds = DupHalves(0) if dup else SyntheticDataset(0)
+    ds = SyntheticDataset(0)
     o = coexec.Orchestrator(lang.parse(src), ds, coexec.Mode.coexec, coexec.RunConfig(), be)
     res, st = o.run()
     plans = [(p.replicated, p.reason, p.allreduce_nodes, sorted(p.sharded_slots)) for p in be.dp_plans]
@@ -71,12 +57,12 @@ def _worker(rank, world, port, src, out, dup=False):
     dist.destroy_process_group()
 
 
-def run_dp(src, world=2, dup=False):
+def run_dp(src, world=2):
     ctx = mp.get_context("spawn")
     mgr = ctx.Manager()
     out = mgr.dict()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, src, out, dup)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, src, out)) for r in range(world)]
     for p in procs:
         p.start()
     for p in procs:
@@ -121,21 +107,21 @@ steps 6 {
 
 @pytest.mark.parametrize("src,tol", [(SMALL_C2, 1e-9), (SMALL_C3, 1e-8)], ids=["dcgan", "resnet_sdpoint"])
 def test_dp2_dcgan_matches_global_batch(src, tol):
-    """C2 (DCGAN) / C3 (ResNet-50 + SDPoint) data parallel at world size 2: activations
-    row-sharded through the convolutions, pooling and (C3) the path-dependent SDPoint tail,
-    per-replica batch-norm statistics, weight / gamma / beta gradients all-reduced (P+), the
-    loss averaged (P~).  With duplicated batch halves the result equals the single-process
-    global-batch run (C3 within 1e-8: the 4- vs 8-row batch-norm summation orders differ at
-    f64 rounding level, and the tiny network's training dynamics amplify that ~10x per step
-    -- measured 1e-16 at step 4 growing to 2e-10 at step 14)."""
-    ref, ref_st = coexec.run(lang.parse(src), DupHalves(0), "coexec", backend=CpuBackend())
-    out = run_dp(src, dup=True)
+    """C2 (DCGAN) / C3 (ResNet-50 + SDPoint) data parallel at world size 2 on distinct row
+    shards: activations row-sharded through the convolutions, pooling and (C3) the
+    path-dependent SDPoint tail; batch norm SYNCHRONISED (rank-local raw column sums
+    all-reduced, statistics of the global batch); weight / beta gradients all-reduced (P+),
+    gamma gradients already global, the loss averaged (P~).  Equal to the single-process
+    global-batch run up to summation order (C3 within 1e-8: the tiny network's training
+    dynamics amplify f64 rounding-order differences ~10x per step)."""
+    ref, ref_st = coexec.run(lang.parse(src), SyntheticDataset(0), "coexec", backend=CpuBackend())
+    out = run_dp(src)
     r0, r1 = out[0], out[1]
     assert r0[0] == r1[0] and r0[3] == r1[3] and r0[2] == r1[2]
     assert r0[2] == ref_st.counters()
     plans = r0[4]
     assert plans and not any(p[0] for p in plans), plans   # every specialisation sharded
-    assert max(len(p[2]) for p in plans) >= 8               # weight, BN-parameter and loss reductions
+    assert max(len(p[2]) for p in plans) >= 6               # weight, BN-shift and loss reductions
     for a, b in zip(ref.lines, r0[0]):
         assert abs(float(a) - float(b)) <= tol * max(1.0, abs(float(a))), (a, b)
     for k, t in ref.vars.items():
