@@ -195,7 +195,7 @@ __device__ __forceinline__ void publish_late(const Out& o, void* out) {
 // test the flag).  Compute kernels do not test it themselves (a dependent flag load at every
 // launch cost ~5 % of the C2 step); instead the builder cuts every straight-line list into
 // guarded segments: a one-thread k_guard reads the host's cancel word and sets an IF
-// conditional whose body is the next segment (COEX_CANCEL_EVERY kernels, default 16), so a
+// conditional whose body is the next segment (COEX_CANCEL_EVERY kernels, default 64), so a
 // cancelled pass skips every later segment and runs at most the one in flight.  Cells start
 // each pass at their build-time values (a buffer of the right size, or the program's
 // zero-filled spare buffer of the largest size), so any prefix of kernels reads valid memory.

@@ -559,8 +559,11 @@ constexpr int kBnBwdFused = 100;
 // Plan-only kind: batchnorm whose apply pass also writes relu / leaky_relu of its output
 // (planner.py _bn_act_pairs; attr dims[0] = the activation's EW code; second output out2).
 constexpr int kBnAct = 101;
+// Plan-only kind: cross_entropy + cross_entropy_grad of the same logits / ids in one pass
+// (planner.py _ce_pairs; out = the gradient, out2 = the loss; value = global rows or 0).
+constexpr int kCeFused = 102;
 bool is_ext_compute(int kind) {
-  return (kind >= COEX_CONV2D && kind <= COEX_SUM_ROWS) || kind == kBnBwdFused || kind == kBnAct ||
+  return (kind >= COEX_CONV2D && kind <= COEX_SUM_ROWS) || kind == kBnBwdFused || kind == kBnAct || kind == kCeFused ||
          (kind >= COEX_EMBEDDING && kind <= COEX_GLOBAL_AVGPOOL_GRAD && kind != COEX_GELU && kind != COEX_GELU_GRAD) ||
          (kind >= COEX_SLICE && kind <= COEX_SUM_AXIS);
 }
@@ -1567,7 +1570,7 @@ int build_xop_t(coex_ctx* c, const OpSpec& s, Launch* L, int* nL, size_t* ws_byt
     }
     case COEX_EMBEDDING: case COEX_EMBEDDING_DW: case COEX_LAYERNORM: case COEX_LAYERNORM_DX: case COEX_LN_DGAMMA:
     case COEX_BIAS_ADD: case COEX_CAUSAL_SOFTMAX: case COEX_SOFTMAX_GRAD: case COEX_CROSS_ENTROPY:
-    case COEX_CROSS_ENTROPY_GRAD: case COEX_REL_SKEW: case COEX_REL_UNSKEW: {
+    case COEX_CROSS_ENTROPY_GRAD: case COEX_REL_SKEW: case COEX_REL_UNSKEW: case kCeFused: {
       RowParams rp{};
       rp.ds = s.ds; rp.x = s.in[0]; rp.y = s.in[1];
       rp.z = s.nin > 2 ? s.in[2] : In{nullptr, nullptr, nullptr};
@@ -1638,6 +1641,40 @@ int build_xop_t(coex_ctx* c, const OpSpec& s, Launch* L, int* nL, size_t* ws_byt
           void* fn = s.kind == COEX_REL_SKEW ? (is_f64(c) ? (void*)k_rel_skew<double, 0> : (void*)k_rel_skew<float, 0>)
                                              : (is_f64(c) ? (void*)k_rel_skew<double, 1> : (void*)k_rel_skew<float, 1>);
           L[(*nL)++].set(fn, warp_rows(rp.rows), dim3(256), rp);
+          return COEX_OK;
+        }
+        case kCeFused: {   // loss + gradient (+ bf16 shadow) in one pass over the logits
+          const int64_t R = s.in_shape[0][0], V = s.in_shape[0][1];
+          rp.acc = (double*)pv.take((size_t)R * 8);
+          rp.counter = (unsigned int*)pv.take(16);
+          if (!build) break;
+          rp.d = V; rp.rows = R; rp.vocab = V;
+          rp.spitch = (V + 7) / 8 * 8;
+          rp.skip_f32 = (int)s.attr_dims[0];
+          rp.out2 = s.out2;
+          const size_t smem = (size_t)V * 4;
+          if (is_f64(c) || smem > 220 * 1024) {      // f64 parity / very wide rows: two passes
+            rp.shadow = nullptr;
+            rp.skip_f32 = 0;
+            RowParams lp = rp;
+            lp.out = s.out2;
+            L[(*nL)++].set(is_f64(c) ? (void*)k_cross_entropy<double, 0> : (void*)k_cross_entropy<float, 0>,
+                           dim3((unsigned)(R < kNumSMs * 8 ? R : kNumSMs * 8)), dim3(256), lp);
+            L[(*nL)++].set(is_f64(c) ? (void*)k_cross_entropy<double, 1> : (void*)k_cross_entropy<float, 1>,
+                           dim3((unsigned)(R < kNumSMs * 8 ? R : kNumSMs * 8)), dim3(256), rp);
+            return COEX_OK;
+          }
+          const bool wide = V >= 8192;
+          void* fn = wide ? (void*)k_ce_fused<1024> : (void*)k_ce_fused<128>;
+          static bool attr_set = false;
+          if (!attr_set) {
+            CK(cudaFuncSetAttribute((void*)k_ce_fused<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+            CK(cudaFuncSetAttribute((void*)k_ce_fused<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+            attr_set = true;
+          }
+          const int64_t per_sm = wide ? 1 : 8;
+          L[*nL].set(fn, dim3((unsigned)(R < kNumSMs * per_sm ? R : kNumSMs * per_sm)), dim3(wide ? 1024 : 128), rp);
+          L[(*nL)++].smem = smem;
           return COEX_OK;
         }
         default: {   // cross-entropy (loss / gradient)
@@ -2449,7 +2486,7 @@ struct Builder {
 
   std::unordered_map<cudaGraphNode_t, bool> kernel_nodes;   // nodes created by add_kernel
   bool pdl = true;
-  int64_t cancel_every = 16;        // kernel nodes per cancel-guarded segment (0: no guards)
+  int64_t cancel_every = 64;        // kernel nodes per cancel-guarded segment (0: no guards)
 
   // Kernel node after `*prev`.  Kernel -> kernel edges are programmatic (PDL): the node is
   // scheduled while its predecessor's last wave drains and synchronises in COEX_PDL_ENTER.
@@ -2513,7 +2550,7 @@ struct Builder {
     o.late = late ? p->late + (n_late++) : nullptr;
   }
 
-  // A straight-line list.  With cancel guards on (COEX_CANCEL_EVERY > 0, default 16) the
+  // A straight-line list.  With cancel guards on (COEX_CANCEL_EVERY > 0, default 64) the
   // list is cut into segments of about that many kernel nodes, each the body of an IF
   // conditional set by a k_guard that reads the host's cancel word: a cancelled pass skips
   // every later segment.  All-reduce child graphs stay at the list's own level.
@@ -2638,7 +2675,7 @@ struct Builder {
         if (s.kind == kBnBwdFused) {
           read_out(s.out2);
           read_out(s.out3);
-        } else if (s.kind == kBnAct) {
+        } else if (s.kind == kBnAct || s.kind == kCeFused) {
           read_out(s.out2);
         }
         s.shadow = buf(next());

@@ -26,6 +26,9 @@ struct RowParams {
   unsigned int* counter;
   Out out;
   __nv_bfloat16* shadow;     // optional bf16 copy of the output (consumed by batched GEMMs)
+  Out out2;                  // fused cross-entropy: the loss (out = the gradient)
+  long long spitch;          // shadow row pitch (elements; >= d, multiple of 8)
+  int skip_f32;              // fused cross-entropy: the fp32 gradient has no reader (GEMMs read the shadow)
 };
 
 template <typename A>
@@ -552,6 +555,98 @@ __global__ void __launch_bounds__(256) k_cross_entropy(RowParams p) {
     o[0] = (T)(acc / (double)p.rows);
     *p.counter = 0u;
     for (int i = 0; i < p.out.npub; ++i) *p.out.pub[i] = o;
+  }
+}
+
+// Fused cross-entropy (planner: cross_entropy + cross_entropy_grad of the same logits and
+// ids; tolerance modes).  One block per row; the row is staged in shared memory on its one
+// HBM read (max on the fly), its exponentials cached in place, and the gradient
+// (softmax - onehot) / rows written from shared memory -- in fp32 (unless no reader needs
+// it) and as the bf16 GEMM-operand shadow [rows][spitch] the LM-head weight / input
+// gradient GEMMs read.  Row losses go to acc; the last block writes their mean in row order.
+// HBM: logits once in, gradient out (vs. two full reads and a conversion pass unfused).
+template <int NT>
+__device__ __forceinline__ float block_reduce(float v, bool is_max, float* red) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    const float o = __shfl_xor_sync(0xffffffffu, v, off);
+    v = is_max ? fmaxf(v, o) : v + o;
+  }
+  if (lane == 0) red[wid] = v;
+  __syncthreads();
+  float r = red[0];
+  for (int w = 1; w < NT / 32; ++w) r = is_max ? fmaxf(r, red[w]) : r + red[w];
+  __syncthreads();
+  return r;
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT) k_ce_fused(RowParams p) {
+  COEX_PDL_ENTER();
+  stamp(p.ds, SK_CE);
+  extern __shared__ float srow[];
+  __shared__ float red[NT / 32];
+  const float* lg = res<float>(p.x);
+  const float* ids = res<float>(p.y);
+  float* o = pick_out<float>(p.out, lg, ids);
+  float* lo = pick_out<float>(p.out2, lg, ids);
+  publish_early(p.out, o);
+  count_op(p.ds);
+  const long long V = p.d;
+  const float invr = (float)(1.0 / (p.scale > 0.0 ? p.scale : (double)p.rows));   // scale: global rows
+  for (long long r = blockIdx.x; r < p.rows; r += gridDim.x) {
+    const float* row = lg + r * V;
+    float mx = -INFINITY;
+    long long c = threadIdx.x;
+    for (; c + 7 * NT < V; c += 8 * NT) {            // eight independent loads in flight
+      float v[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) v[q] = __ldcs(row + c + q * NT);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        srow[c + q * NT] = v[q];
+        mx = fmaxf(mx, v[q]);
+      }
+    }
+    for (; c < V; c += NT) {
+      const float v = __ldcs(row + c);
+      srow[c] = v;
+      mx = fmaxf(mx, v);
+    }
+    const float gm = block_reduce<NT>(mx, true, red);
+    float sm = 0.f;
+    for (long long k = threadIdx.x; k < V; k += NT) {
+      const float e = __expf(srow[k] - gm);
+      srow[k] = e;
+      sm += e;
+    }
+    const float gs = block_reduce<NT>(sm, false, red);
+    const double f = floor((double)ids[r]);
+    const long long id = f < 0 ? 0 : (f > (double)(V - 1) ? V - 1 : (long long)f);
+    if (threadIdx.x == 0) p.acc[r] = ((double)logf(gs) + (double)gm) - (double)row[id];
+    const float inv = 1.f / gs;
+    float* orow = o + r * V;
+    __nv_bfloat16* srow16 = p.shadow ? p.shadow + r * p.spitch : nullptr;
+    for (long long k = threadIdx.x; k < V; k += NT) {
+      float g = srow[k] * inv;
+      if (k == id) g -= 1.f;
+      g *= invr;
+      if (!p.skip_f32) __stcs(orow + k, g);
+      if (srow16) srow16[k] = __float2bfloat16_rn(g);
+    }
+    if (srow16)
+      for (long long k = V + threadIdx.x; k < p.spitch; k += NT) srow16[k] = __float2bfloat16_rn(0.f);
+    __syncthreads();                                  // srow reused by the next row
+  }
+  publish_late(p.out, o);
+  if (!last_block(p.counter)) return;
+  if (threadIdx.x == 0) {
+    double acc = 0.0;
+    for (long long r = 0; r < p.rows; ++r) acc += __ldcg(p.acc + r);
+    lo[0] = (float)(acc / (double)p.rows);
+    *p.counter = 0u;
+    for (int i = 0; i < p.out2.npub; ++i) *p.out2.pub[i] = lo;
   }
 }
 

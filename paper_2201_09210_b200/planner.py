@@ -53,6 +53,7 @@ COMPUTE = {OpKind.MATMUL, OpKind.SUM, OpKind.MEAN, OpKind.TRANSPOSE} | set(EW_CO
 MAX_XIN = 3
 XOP_BN_BWD = 100          # fused batchnorm_dx + bn_dgamma + sum_rows (csrc COEX_BN_BWD_FUSED)
 XOP_BN_ACT = 101          # batchnorm also writing relu / leaky_relu of its output (csrc kBnAct)
+XOP_CE_FUSED = 102        # cross_entropy + cross_entropy_grad in one pass (csrc kCeFused)
 CHAIN_IN, CHAIN_OPS, CHAIN_OUT, CHAIN_PUB, CHAIN_REGS = 8, 16, 8, 4, 16
 
 
@@ -253,6 +254,13 @@ class Planner:
                 return False
 
             for nid, x in ops.items():
+                if x.kind is OpKind.CROSS_ENTROPY_GRAD and nid in node_buf and not node_buf[nid][2] and \
+                        gemm_use(nid) and not any(nid in s_ for s_ in multi) and \
+                        any(y.kind is OpKind.CROSS_ENTROPY and y.inputs == x.inputs for y in ops.values()):
+                    # the fused cross-entropy writes the gradient's bf16 copy ([rows][pitch 8])
+                    shp = shapes[nid]
+                    self.shadow[nid] = new_buf(shape_size(shp[:-1]) * ((shp[-1] + 7) // 8 * 8) * 2)
+                    continue
                 if x.kind not in (OpKind.CAUSAL_SOFTMAX, OpKind.SOFTMAX_GRAD, OpKind.LAYERNORM) or nid not in node_buf:
                     continue
                 if node_buf[nid][2] or shapes[nid][-1] % 8 or any(nid in s_ for s_ in multi):
@@ -334,6 +342,9 @@ class Planner:
         self.n_chains = 0
         self.n_mchains = 0
         self._act_for = {}
+        self._ce_loss = {}                       # fused cross-entropy: gradient node -> loss node
+        self._skip_f32 = {}                      # gradient node -> (plan word, attr index): 1 = no fp32 reader
+        self._skip_cell = {}                     # its output cell -> gradient node
         self.chain_lates = 0
         self._chain_meta = {}
 
@@ -359,6 +370,11 @@ class Planner:
             if act_of:
                 gone = {a.node_id for a in act_of.values()}
                 insts = [y for y in insts if not (isinstance(y, ExecOp) and y.node_id in gone)]
+            ce_of = self._ce_pairs(insts) if self.fuse else {}
+            if ce_of:                               # the gradient moves up to the loss's position
+                grads = {g.node_id for g in ce_of.values()}
+                insts = [ce_of.get(y.node_id, y) if isinstance(y, ExecOp) else y for y in insts
+                         if not (isinstance(y, ExecOp) and y.node_id in grads)]
             bn_groups, bn_skip = self._bn_bwd_groups(insts) if self.fuse else ({}, set())
             if self.fuse:
                 segs = self._segments(insts, shapes, folded)
@@ -399,6 +415,7 @@ class Planner:
                     items.extend(self._exec(x, shapes, in_cell, out_words, ptr_item, pubs, multi,
                                             folded, n_compute, flops))
                     self._invalidate(pubs[x.node_id])
+                    self._register_shadow(x, pubs, shapes)
                     if x.kind is OpKind.ASSIGN_VAR:
                         self._invalidate([-(2000 + self.var_index[x.attrs["var_name"]])])
                 elif isinstance(x, SwitchCase):
@@ -516,6 +533,8 @@ class Planner:
                 cb = (self.new_buf(max(nn, 1) * ((kk + 7) // 8 * 8) * 2), 2)
             else:
                 cb = self._copy(cells[1], in_shapes[1])
+            self._need_f32(cells[0], ca[1])
+            self._need_f32(cells[1], cb[1])
             word += [ca[0], cb[0], ca[1], cb[1]]
         else:
             word += [-1, -1, 0, 0]
@@ -550,6 +569,36 @@ class Planner:
             out[bn.node_id] = x
             taken.add(bn.node_id)
         self._act_for.update(out)
+        return out
+
+    def _ce_pairs(self, insts) -> dict:
+        """cross_entropy(lg, ids) and cross_entropy_grad(lg, ids) over the same bindings in one
+        instruction list: one kernel computes both (the logits are read once).  The fused op
+        takes the loss's position; legal when nothing in between re-produces an input and
+        neither node is merged, pinned or self-dependent.  Returns {loss node: grad node}."""
+        multi_nodes = {n for s_ in self._multi_sets() for n in s_}
+        banned = multi_nodes | set(self.folded_assigns.values())
+        pos = {x.node_id: i for i, x in enumerate(insts) if isinstance(x, ExecOp)}
+        out = {}
+        for x in insts:
+            if not isinstance(x, ExecOp) or x.kind is not OpKind.CROSS_ENTROPY or x.node_id in banned:
+                continue
+            g = next((y for y in insts if isinstance(y, ExecOp) and y.kind is OpKind.CROSS_ENTROPY_GRAD
+                      and y.inputs == x.inputs and y.node_id not in banned and y.node_id not in self.force_store
+                      and pos[y.node_id] > pos[x.node_id]), None)
+            if g is None or g in out.values():
+                continue
+            ids = {x.node_id, g.node_id}
+            if any((not b.fed) and (set(b.cands) & ids) for b in x.inputs):
+                continue
+            lo, hi = pos[x.node_id], pos[g.node_id]
+            srcs = {c for b in x.inputs if not b.fed for c in b.cands}
+            fed = {b.slot for b in x.inputs if b.fed}
+            if any((isinstance(y, ExecOp) and y.node_id in srcs) or (isinstance(y, InputFeed) and y.slot in fed)
+                   or not isinstance(y, (ExecOp, InputFeed, OutputFetch)) for y in insts[lo + 1:hi]):
+                continue
+            out[x.node_id] = g
+            self._ce_loss[g.node_id] = x
         return out
 
     def _bn_bwd_groups(self, insts):
@@ -637,25 +686,67 @@ class Planner:
             flops[0] += flops_of(x.kind, in_shapes, x.attrs)
         out_shape = shapes[nid]
         act = self._act_for.get(nid)
+        ce_loss = self._ce_loss.get(nid)
         kind_code = x.kind.code
         if act is not None:                     # batchnorm + activation in one apply pass
             kind_code = XOP_BN_ACT
             attr = [EW_CODE[act.kind]]
+        skip = 0
+        if ce_loss is not None:                 # loss + gradient in one pass over the logits
+            kind_code = XOP_CE_FUSED
+            skip = int(nid in self.shadow and self._gemm_only(nid))
+            attr = [skip]
         word = [T_XOP, kind_code, nid, len(cells)] + cells + [-1] * (MAX_XIN - len(cells))
         for s_ in in_shapes + [()] * (MAX_XIN - len(in_shapes)):
             word += [len(s_)] + _pad(s_)
         word += [len(out_shape)] + _pad(out_shape)
+        attr_at = len(word) + 1
         word += [len(attr)] + _pad(attr) + [_f64_bits(float(x.attrs.get("value", x.attrs.get("rows", 0.0))))]
         word += out_words(nid, late)
         if act is not None:
             word += out_words(act.node_id, _conflicts(cells, pubs[act.node_id]))
             self._invalidate(pubs[act.node_id])
+        if ce_loss is not None:
+            word += out_words(ce_loss.node_id, _conflicts(cells, pubs[ce_loss.node_id]))
+            self._invalidate(pubs[ce_loss.node_id])
+            if skip:                            # cleared if any GEMM has to convert the fp32 tensor
+                self._skip_f32[nid] = (word, attr_at)
+                self._skip_cell[pubs[nid][0]] = nid
         word += self._shadow_words(x, cells, in_shapes)
         self._invalidate(pubs[nid])
-        if nid in self.shadow:                  # this node's bf16 shadow is a valid copy from here on
+        return word
+
+    def _register_shadow(self, x, pubs, shapes):
+        """After x's publication: its bf16 shadow (written by its kernel) is the valid bf16
+        copy of its output for later GEMMs of the same list."""
+        nid = x.node_id
+        if nid in self.shadow and (x.kind is not OpKind.CROSS_ENTROPY_GRAD or nid in self._ce_loss):
             shp = shapes[nid]
             self._copies[(pubs[nid][0], shape_size(shp[:-1]), shp[-1])] = self.shadow[nid]
-        return word
+
+    def _gemm_only(self, nid) -> bool:
+        """Every reader of nid's output is a MatMul operand (directly or through a folded
+        transpose) and the value is not fetched, merged, pinned or assigned."""
+        if nid in self.sp.fetch_nodes or nid in self.force_store or nid in self.folded_assigns.values():
+            return False
+        if any(nid in s_ for s_ in self._multi_sets()):
+            return False
+        for c in self.consumers.get(nid, []):
+            if c.kind is OpKind.MATMUL:
+                continue
+            if c.kind is OpKind.TRANSPOSE and c.node_id in self.folded and \
+                    all(cc.kind is OpKind.MATMUL for cc in self.consumers.get(c.node_id, [])):
+                continue
+            return False
+        return True
+
+    def _need_f32(self, cell, conv):
+        """A GEMM operand read from ``cell`` needs the fp32 tensor (its copy is converted):
+        the producer must write it after all."""
+        nid = self._skip_cell.get(cell)
+        if nid is not None and conv:
+            word, at = self._skip_f32[nid]
+            word[at] = 0
 
     def _causal_prob(self, b) -> bool:
         """Binding b is (single-candidate) a causal_softmax output, or a softmax_grad of one --
@@ -729,6 +820,7 @@ class Planner:
         if x.kind in BMM_KINDS and self.bf16 and in_cells is not None:
             for i in range(2):
                 bufs[i], conv[i] = self._copy(in_cells[i], in_shapes[i])
+                self._need_f32(in_cells[i], conv[i])
         return [self.shadow.get(x.node_id, -1)] + bufs + conv
 
     # ------------------------------------------------------------ pointer-op rewrites

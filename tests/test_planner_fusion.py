@@ -72,3 +72,18 @@ def test_layernorm_shadows():
     pl, _ = _planner(gpt2_program(steps=6, **C4_SMALL))
     kinds = {pl.ops[n].kind for n in pl.shadow}
     assert OpKind.LAYERNORM in kinds and OpKind.CAUSAL_SOFTMAX in kinds
+
+
+def test_cross_entropy_fused_with_shadow_only_gradient():
+    """C4: cross_entropy + cross_entropy_grad of the same logits become one plan op (kind
+    102); the gradient's only readers are the LM-head GEMMs, which read its bf16 shadow, so
+    the fp32 gradient is never written (attr 1)."""
+    from paper_2201_09210_b200.planner import XOP_CE_FUSED
+    pl, plan = _planner(gpt2_program(steps=6, **C4_SMALL))
+    assert pl._ce_loss
+    for g, lo in pl._ce_loss.items():
+        assert pl.ops[g].kind is OpKind.CROSS_ENTROPY_GRAD and lo.kind is OpKind.CROSS_ENTROPY
+        assert g in pl.shadow
+    assert pl._skip_f32 and all(w[at] == 1 for w, at in pl._skip_f32.values())
+    w = plan.words
+    assert any(w[i] == XOP_CE_FUSED and w[i - 1] == 10 for i in range(1, len(w)))
