@@ -250,7 +250,8 @@ class B200Backend:
                    12: "end", 13: "fused chain", 14: "im2col", 15: "col2im", 16: "bf16 cvt", 17: "colstats",
                    18: "bn apply", 19: "split-K reduce", 20: "causal softmax", 21: "softmax grad",
                    22: "cross-entropy", 23: "bias add", 24: "layernorm", 25: "embedding", 26: "column sum",
-                   27: "rel skew", 28: "pooling", 29: "axis op"}
+                   27: "rel skew", 28: "pooling", 29: "axis op", 30: "cancel guard",
+                   31: "attention"}
 
     def set_trace(self, capacity: int):
         """Enable device-side per-kernel stamps (0 disables)."""

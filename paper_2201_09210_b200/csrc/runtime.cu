@@ -32,6 +32,7 @@
 #include "gemm_tc.cuh"
 #include "ext_ops.cuh"
 #include "xformer_ops.cuh"
+#include "attn_tc.cuh"
 
 #include <cudaTypedefs.h>
 #include <dlfcn.h>
@@ -2325,7 +2326,7 @@ int coex_var_rollback(coex_ctx* c) {
 namespace {
 
 enum PlanTag : int64_t { T_SEQ = 1, T_OP = 2, T_PTR = 3, T_FEED = 4, T_FETCH = 5, T_SWITCH = 6, T_WHILE = 7, T_CHAIN = 8,
-                         T_ALLREDUCE = 9, T_XOP = 10, T_MCHAIN = 11 };
+                         T_ALLREDUCE = 9, T_XOP = 10, T_MCHAIN = 11, T_ATTN = 12 };
 constexpr int64_t kPlanMagic = 0xC0E8B200;
 constexpr int64_t kPlanVersion = 2;
 
@@ -2703,6 +2704,60 @@ struct Builder {
           if (rc) return rc;
         }
         return COEX_OK;
+      }
+      case T_ATTN: {                                // fused causal attention (attn_tc.cuh)
+        const int64_t mode = next();
+        FaParams fp{};
+        fp.ds = c->d_state;
+        fp.BH = (int)next();
+        fp.T = (int)next();
+        {
+          int64_t sb = next();
+          double sc;
+          memcpy(&sc, &sb, 8);
+          fp.scale = (float)sc;
+        }
+        fp.lse = (float*)buf(next());
+        fp.delta = (float*)buf(next());
+        fp.q = operand(next());
+        fp.k = operand(next());
+        fp.v = operand(next());
+        fp.o = operand(next());
+        fp.dout = operand(next());
+        fp.pa = fp.q;
+        fp.pb = fp.k;
+        if (is_f64(c) || fp.T % FA_BLK != 0) throw std::runtime_error("flash attention: bf16 mode, T % 128 only");
+        static bool attr_set = false;
+        if (!attr_set) {
+          CK(cudaFuncSetAttribute((void*)k_fa_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFaFwdSmem));
+          CK(cudaFuncSetAttribute((void*)k_fa_bwd_kv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFaKvSmem));
+          CK(cudaFuncSetAttribute((void*)k_fa_bwd_q, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFaQSmem));
+          attr_set = true;
+        }
+        const unsigned blocks = (unsigned)(fp.BH * (fp.T / FA_BLK));
+        p->n_compute++;
+        if (mode == 0) {
+          read_out(fp.out);
+          Launch L;
+          L.set((void*)k_fa_fwd, dim3(blocks), dim3(128), fp);
+          L.smem = kFaFwdSmem;
+          return add_kernel(g, prev, L);
+        }
+        read_out(fp.out);
+        read_out(fp.out2);
+        read_out(fp.out3);
+        Launch L0, L1, L2;
+        const int64_t rows = (int64_t)fp.BH * fp.T;
+        const int64_t db = (rows * 16 + 255) / 256;
+        L0.set((void*)k_fa_delta, dim3((unsigned)(db < kNumSMs * 8 ? db : kNumSMs * 8)), dim3(256), fp);
+        L1.set((void*)k_fa_bwd_kv, dim3(blocks), dim3(256), fp);
+        L1.smem = kFaKvSmem;
+        L2.set((void*)k_fa_bwd_q, dim3(blocks), dim3(256), fp);
+        L2.smem = kFaQSmem;
+        int rc = add_kernel(g, prev, L0);
+        if (!rc) rc = add_kernel(g, prev, L1);
+        if (!rc) rc = add_kernel(g, prev, L2);
+        return rc;
       }
       case T_MCHAIN: {                              // independent chains, one launch
         const int64_t cnt = next();

@@ -23,6 +23,7 @@ is not fetched) is not materialised -- the MatMul reads the operand transposed.
 
 from __future__ import annotations
 
+import os
 import struct
 from dataclasses import dataclass, field
 
@@ -33,6 +34,7 @@ from .tensor import BMM_KINDS, CONV_ATTR_KINDS, CONV_KINDS, OpKind, flops_of, in
 MAGIC = 0xC0E8B200
 VERSION = 2
 T_SEQ, T_OP, T_PTR, T_FEED, T_FETCH, T_SWITCH, T_WHILE, T_CHAIN, T_ALLREDUCE, T_XOP, T_MCHAIN = 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11
+T_ATTN = 12               # fused causal attention (csrc attn_tc.cuh): forward / backward of one layer
 MAX_MCHAIN = 8            # chains per k_chain_multi launch (csrc kMaxMultiChain)
 PTR_ALIAS, PTR_READ_VAR, PTR_ASSIGN_VAR = 0, 1, 2
 MAX_RANK = 8
@@ -54,6 +56,19 @@ MAX_XIN = 3
 XOP_BN_BWD = 100          # fused batchnorm_dx + bn_dgamma + sum_rows (csrc COEX_BN_BWD_FUSED)
 XOP_BN_ACT = 101          # batchnorm also writing relu / leaky_relu of its output (csrc kBnAct)
 XOP_CE_FUSED = 102        # cross_entropy + cross_entropy_grad in one pass (csrc kCeFused)
+FA_HEAD = 64              # flash attention: head dim and query / key block of the tcgen05 kernels
+FA_BLOCK = 128
+
+
+class _Attn:
+    """Stands in for one layer's attention nodes in an instruction list: mode 0 = the forward
+    (S = bmm_nt(q, k), P = causal_softmax(S), O = bmm(P, v)) at O's position, mode 1 = the
+    backward (dP = bmm_nt(dO, v), dS = softmax_grad(P, dP), dQ = bmm(dS, k), dK = bmm_tn(dS, q),
+    dV = bmm_tn(P, dO)) at dS's position."""
+
+    def __init__(self, mode: int, g: dict):
+        self.mode = mode
+        self.g = g
 CHAIN_IN, CHAIN_OPS, CHAIN_OUT, CHAIN_PUB, CHAIN_REGS = 8, 16, 8, 4, 16
 
 
@@ -222,6 +237,7 @@ class Planner:
             return len(cell_init) - 1
 
         node_buf: dict = {}
+        self._node_buf = node_buf
         vcell: dict = {}
         fills: list = []
         consts: list = []
@@ -345,6 +361,7 @@ class Planner:
         self._ce_loss = {}                       # fused cross-entropy: gradient node -> loss node
         self._skip_f32 = {}                      # gradient node -> (plan word, attr index): 1 = no fp32 reader
         self._skip_cell = {}                     # its output cell -> gradient node
+        self.n_attn = 0                          # flash-attention groups (forward + backward)
         self.chain_lates = 0
         self._chain_meta = {}
 
@@ -370,6 +387,18 @@ class Planner:
             if act_of:
                 gone = {a.node_id for a in act_of.values()}
                 insts = [y for y in insts if not (isinstance(y, ExecOp) and y.node_id in gone)]
+            groups = self._attn_groups(insts, shapes) if (self.fuse and self.bf16) else []
+            if groups:                              # flash attention: S, P, dP, dS never stored
+                repl, gone = {}, set()
+                for g in groups:
+                    repl[g["O"].node_id] = _Attn(0, g)
+                    repl[g["G"].node_id] = _Attn(1, g)
+                    gone |= {g[k].node_id for k in ("S", "P", "dP", "DQ", "DK", "DV")}
+                    g["lse"] = self.new_buf(g["BH"] * g["T"] * 4)
+                    g["delta"] = self.new_buf(g["BH"] * g["T"] * 4)
+                    self.n_attn += 1
+                insts = [repl.get(y.node_id, y) if isinstance(y, ExecOp) else y for y in insts
+                         if not (isinstance(y, ExecOp) and y.node_id in gone)]
             ce_of = self._ce_pairs(insts) if self.fuse else {}
             if ce_of:                               # the gradient moves up to the loss's position
                 grads = {g.node_id for g in ce_of.values()}
@@ -411,6 +440,8 @@ class Planner:
                 elif isinstance(x, OutputFetch):
                     shp = shapes[x.node_id]
                     items.append([T_FETCH, x.node_id, vcell[x.node_id], shape_size(shp), len(shp)] + _pad(shp))
+                elif isinstance(x, _Attn):
+                    items.append(self._attn_word(x, in_cell, out_words, pubs, n_compute, flops, shapes))
                 elif isinstance(x, ExecOp):
                     items.extend(self._exec(x, shapes, in_cell, out_words, ptr_item, pubs, multi,
                                             folded, n_compute, flops))
@@ -570,6 +601,99 @@ class Planner:
             taken.add(bn.node_id)
         self._act_for.update(out)
         return out
+
+    def _attn_groups(self, insts, shapes) -> list:
+        """One layer's causal attention, forward and backward, in one instruction list (the
+        C4 program's hand-written attention; oracle/kernels.py BMM / CAUSAL_SOFTMAX /
+        SOFTMAX_GRAD): S = bmm_nt(q, k) -> P = causal_softmax(S) -> O = bmm(P, v);
+        dP = bmm_nt(dO, v) -> dS = softmax_grad(P, dP) -> dQ = bmm(dS, k), dK = bmm_tn(dS, q);
+        dV = bmm_tn(P, dO).  S, P, dP and dS must have no other reader (not fetched, merged or
+        pinned), the head dim is 64 and T a multiple of 128.  COEX_FLASH=0 disables it."""
+        if os.environ.get("COEX_FLASH", "1") == "0":
+            return []
+        ex = {x.node_id: x for x in insts if isinstance(x, ExecOp)}
+        pos = {x.node_id: i for i, x in enumerate(insts) if isinstance(x, ExecOp)}
+        multi_nodes = {n for s_ in self._multi_sets() for n in s_}
+        banned = set(self.sp.fetch_nodes) | multi_nodes | set(self.force_store) | set(self.folded_assigns.values())
+
+        def single(b):
+            return (not b.fed) and len(b.cands) == 1
+
+        def only(nid):
+            return [c.node_id for c in self.consumers.get(nid, [])]
+
+        out = []
+        for P in insts:
+            if not isinstance(P, ExecOp) or P.kind is not OpKind.CAUSAL_SOFTMAX or not single(P.inputs[0]):
+                continue
+            S = ex.get(P.inputs[0].cands[0])
+            if S is None or S.kind is not OpKind.BMM_NT or only(S.node_id) != [P.node_id]:
+                continue
+            q, k = S.inputs
+            pc = self.consumers.get(P.node_id, [])
+            O = [c for c in pc if c.kind is OpKind.BMM and single(c.inputs[0]) and c.inputs[0].cands == (P.node_id,)]
+            G = [c for c in pc if c.kind is OpKind.SOFTMAX_GRAD and single(c.inputs[0])
+                 and c.inputs[0].cands == (P.node_id,)]
+            DV = [c for c in pc if c.kind is OpKind.BMM_TN and single(c.inputs[0]) and c.inputs[0].cands == (P.node_id,)]
+            if len(pc) != 3 or len(O) != 1 or len(G) != 1 or len(DV) != 1:
+                continue
+            O, G, DV = O[0], G[0], DV[0]
+            v = O.inputs[1]
+            if not single(G.inputs[1]):
+                continue
+            dP = ex.get(G.inputs[1].cands[0])
+            if dP is None or dP.kind is not OpKind.BMM_NT or dP.inputs[1] != v or only(dP.node_id) != [G.node_id]:
+                continue
+            do = dP.inputs[0]
+            if DV.inputs[1] != do:
+                continue
+            gc = self.consumers.get(G.node_id, [])
+            DQ = [c for c in gc if c.kind is OpKind.BMM and c.inputs[0].cands == (G.node_id,) and c.inputs[1] == k]
+            DK = [c for c in gc if c.kind is OpKind.BMM_TN and c.inputs[0].cands == (G.node_id,) and c.inputs[1] == q]
+            if len(gc) != 2 or len(DQ) != 1 or len(DK) != 1:
+                continue
+            DQ, DK = DQ[0], DK[0]
+            nodes = {"S": S, "P": P, "O": O, "dP": dP, "G": G, "DQ": DQ, "DK": DK, "DV": DV}
+            if any(n.node_id in banned or n.node_id not in ex for n in nodes.values()):
+                continue
+            if not all(single(b) for b in (q, k, v, do)):
+                continue
+            shp = tuple(self._in_shape(q, shapes))
+            if len(shp) != 3 or shp[2] != FA_HEAD or shp[1] % FA_BLOCK or shp[1] == 0 or \
+                    any(tuple(self._in_shape(b, shapes)) != shp for b in (k, v, do)):
+                continue
+            if float(P.attrs["value"]) != float(G.attrs["value"]):
+                continue
+            if any(self._node_buf.get(n.node_id, (-1, -1, True))[2] for n in (O, DQ, DK, DV)):
+                continue                            # ping-pong outputs (self-dependent): not here
+            if not (pos[S.node_id] < pos[P.node_id] < pos[O.node_id] and pos[dP.node_id] < pos[G.node_id]
+                    and min(pos[DQ.node_id], pos[DK.node_id], pos[DV.node_id]) > pos[G.node_id]):
+                continue
+            g = dict(nodes, q=q, k=k, v=v, do=do, BH=shp[0], T=shp[1], scale=float(P.attrs["value"]))
+            out.append(g)
+        return out
+
+    def _attn_word(self, a, in_cell, out_words, pubs, n_compute, flops, shapes) -> list:
+        """[T_ATTN, mode, BH, T, scale bits, lse buf, delta buf, cells q k v o dO, outputs]"""
+        g = a.g
+        o_cell = pubs[g["O"].node_id][0]
+        if a.mode == 0:
+            cells = [in_cell(g["q"]), in_cell(g["k"]), in_cell(g["v"]), -1, -1]
+            outs = [g["O"].node_id]
+            members = ("S", "O")
+        else:
+            cells = [in_cell(g["q"]), in_cell(g["k"]), in_cell(g["v"]), o_cell, in_cell(g["do"])]
+            outs = [g["DQ"].node_id, g["DK"].node_id, g["DV"].node_id]
+            members = ("dP", "DQ", "DK", "DV")
+        for m in members:
+            x = g[m]
+            flops[0] += flops_of(x.kind, [tuple(self._in_shape(b, shapes)) for b in x.inputs], x.attrs)
+        n_compute[0] += 1
+        word = [T_ATTN, a.mode, g["BH"], g["T"], _f64_bits(g["scale"]), g["lse"], g["delta"]] + cells
+        for nid in outs:
+            word += out_words(nid, _conflicts(cells, pubs[nid]))
+            self._invalidate(pubs[nid])
+        return word
 
     def _ce_pairs(self, insts) -> dict:
         """cross_entropy(lg, ids) and cross_entropy_grad(lg, ids) over the same bindings in one

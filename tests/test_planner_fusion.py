@@ -87,3 +87,14 @@ def test_cross_entropy_fused_with_shadow_only_gradient():
     assert pl._skip_f32 and all(w[at] == 1 for w, at in pl._skip_f32.values())
     w = plan.words
     assert any(w[i] == XOP_CE_FUSED and w[i - 1] == 10 for i in range(1, len(w)))
+
+
+def test_flash_attention_groups():
+    """C4 at a flash-eligible shape (head dim 64, T = 128): every layer's attention forward and
+    backward become two T_ATTN items; the scores / probabilities are never computed."""
+    from paper_2201_09210_b200.planner import T_ATTN
+    cfg = dict(batch=2, seq=128, d=128, heads=2, layers=2, vocab=97)
+    pl, plan = _planner(gpt2_program(steps=6, **cfg))
+    assert pl.n_attn == 2
+    w = plan.words
+    assert sum(1 for i in range(1, len(w)) if w[i] == T_ATTN and w[i + 1] in (0, 1) and w[i + 2] == 4) >= 4
