@@ -257,7 +257,10 @@ def tensor_gemm(peak_tflops, peak_kind, size: int = 8192):
             "ms": round(ms, 4)}
 
 
-GEMM_KINDS = ("matmul", "split-K reduce")      # the tcgen05 GEMM family in the device stamps
+# the tcgen05 family in the device stamps: GEMMs (with their split-K reduces) and the fused
+# flash-attention kernels (the attention contractions of C4 run inside them)
+GEMM_KINDS = ("matmul", "split-K reduce", "attention fwd", "attention delta", "attention dK/dV", "attention dQ")
+TC_LAUNCH_KINDS = ("matmul", "attention fwd", "attention dK/dV", "attention dQ")
 
 
 def step_flops(workload: str, step: int, world: int = 1) -> int:
@@ -305,10 +308,10 @@ def graph_roofline(o, be, workload, hbm_peak, tflops_sustained, peak_kind, steps
     kinds = {k: {"us_per_step": round(v / 1e3 / steps, 2), "launches_per_step": round(cnt[k] / steps, 2),
                  "share": round(v / total_ns, 4)} for k, v in sorted(agg.items(), key=lambda kv: -kv[1])}
     g_ns = sum(agg[k] for k in GEMM_KINDS)
-    g_launch = sum(cnt[k] for k in GEMM_KINDS if k == "matmul")
+    g_launch = sum(cnt[k] for k in TC_LAUNCH_KINDS)
     ach = flops / (g_ns * 1e-9) / 1e12
-    return {"bound": "tensor", "kernel": "k_gemm_tc (every GEMM / implicit conv / batched GEMM launch of the "
-                                         "step, with its split-K reduce)",
+    return {"bound": "tensor", "kernel": "k_gemm_tc + k_fa_* (every GEMM / implicit conv / batched GEMM launch "
+                                         "of the step with its split-K reduce, and the flash-attention kernels)",
             "achieved": round(ach, 2), "peak": tflops_sustained, "unit": "TFLOP/s",
             "frac": round(ach / tflops_sustained, 4), "peak_source": peak_kind + " (sustained bf16: kernels timed "
                                                                                  "inside a long step)",

@@ -132,140 +132,174 @@ __device__ __forceinline__ void fa_mma_k64(uint32_t d, const unsigned char* a, c
     fa_mma(d, fa_desc(a, 16) + 2 * k, fa_desc(b, 16) + 2 * k, idesc, (acc0 || k > 0) ? 1u : 0u);
 }
 
+// named barrier over `count` threads (id 0 is __syncthreads)
+__device__ __forceinline__ void fa_bar(int id, int count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fa_tmem_alloc(uint32_t* slot, uint32_t cols) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(slot)), "r"(cols)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void fa_tmem_free(uint32_t tmem, uint32_t cols) {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(cols) : "memory");
+}
+// loader side of a tile hand-off: the 128 loader threads' generic-proxy stores become visible
+// to the tensor core's async proxy, then each arrives on the `full` barrier (count 128)
+__device__ __forceinline__ void fa_publish(uint64_t* full) {
+  fa_proxy_fence();
+  mbar_arrive(full);
+}
+
+// Every kernel is warp-specialised: the LAST warpgroup (128 threads) converts the next tiles
+// (fp32 global -> bf16 swizzled shared memory) into a second buffer while the compute
+// warpgroups run softmax-type math on the current block and one thread issues the MMAs, so
+// global-load latency hides behind the block in flight.
+
 // ============================================================== forward
-__global__ void __launch_bounds__(128, 2) k_fa_fwd(const __grid_constant__ FaParams p) {
+// 256 threads: warps 0-3 = the 128 query rows (TMEM lanes), warps 4-7 = loader.
+__global__ void __launch_bounds__(256, 1) k_fa_fwd(const __grid_constant__ FaParams p) {
   COEX_PDL_ENTER();
   stamp(p.ds, SK_ATTN);
   extern __shared__ __align__(1024) unsigned char fa_raw[];
   unsigned char* sm = (unsigned char*)(((uintptr_t)fa_raw + 1023) & ~(uintptr_t)1023);
   unsigned char* sQ = sm;
-  unsigned char* sK = sm + FA_TILE;
-  unsigned char* sV = sm + 2 * FA_TILE;
-  unsigned char* sP = sm + 3 * FA_TILE;          // two sub-tiles
-  uint64_t* bar = (uint64_t*)(sm + 5 * FA_TILE);  // [0] S done, [1] PV done
-  uint32_t* tslot = (uint32_t*)(bar + 2);
+  unsigned char* sK = sm + FA_TILE;              // [2] K buffers, then [2] V buffers
+  unsigned char* sV = sm + 3 * FA_TILE;
+  unsigned char* sP = sm + 5 * FA_TILE;          // two sub-tiles
+  uint64_t* bar = (uint64_t*)(sm + 7 * FA_TILE);
+  uint64_t *kv_full = bar, *kv_empty = bar + 2, *q_full = bar + 4, *s_done = bar + 5, *o_done = bar + 6;
+  uint32_t* tslot = (uint32_t*)(bar + 8);
   const int tid = threadIdx.x, warp = tid >> 5;
   const int nqb = p.T / FA_BLK;
   const int qb = nqb - 1 - (int)(blockIdx.x / p.BH);   // heaviest query blocks first
   const int bh = (int)(blockIdx.x % p.BH);
   const long long hoff = (long long)bh * p.T * FA_D;
-  const float* Q = res<float>(p.q) + hoff;
-  const float* K = res<float>(p.k) + hoff;
-  const float* V = res<float>(p.v) + hoff;
   float* O = pick_out<float>(p.out, res<float>(p.pa), res<float>(p.pb));
   publish_early(p.out, O);
   count_op(p.ds);
   if (tid == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&kv_full[i], 128);
+      mbar_init(&kv_empty[i], 1);
+    }
+    mbar_init(q_full, 128);
+    mbar_init(s_done, 1);
+    mbar_init(o_done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)), "r"(256)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
-  }
-  fa_load<128>(sQ, Q, qb * FA_BLK);
+  if (warp == 0) fa_tmem_alloc(tslot, 256);
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tslot;
-  const uint32_t lane = (uint32_t)(warp * 32) << 16;
-  const uint32_t tS = tmem, tO = tmem + 128;
-  constexpr uint32_t idS = idesc_bf16_f32(128, 128, false, false);
-  constexpr uint32_t idO = idesc_bf16_f32(128, 64, false, true);
-  const float sc2 = p.scale * FA_LOG2E;
-  float o[FA_D];
-#pragma unroll
-  for (int e = 0; e < FA_D; ++e) o[e] = 0.f;
-  float m = -INFINITY, l = 0.f;
-  for (int j = 0; j <= qb; ++j) {
-    fa_load<128>(sK, K, j * FA_BLK);
-    fa_load<128>(sV, V, j * FA_BLK);
-    fa_proxy_fence();
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
-    if (tid == 0) {
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      fa_mma_k64(tS, sQ, sK, idS, false);
-      fa_commit(&bar[0]);
+  if (tid >= 128) {                                  // ===== loader warpgroup
+    const float* K = res<float>(p.k) + hoff;
+    const float* V = res<float>(p.v) + hoff;
+    fa_load<128>(sQ, res<float>(p.q) + hoff, qb * FA_BLK);
+    fa_publish(q_full);
+    for (int j = 0; j <= qb; ++j) {
+      const int b = j & 1;
+      if (j >= 2) mbar_wait(&kv_empty[b], (uint32_t)(((j - 2) >> 1) & 1));
+      fa_load<128>(sK + b * FA_TILE, K, j * FA_BLK);
+      fa_load<128>(sV + b * FA_TILE, V, j * FA_BLK);
+      fa_publish(&kv_full[b]);
     }
-    mbar_wait(&bar[0], (uint32_t)(j & 1));
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const bool diag = j == qb;
-    float mx = m;
-    float v[32];
-#pragma unroll 1
-    for (int c = 0; c < 128; c += 32) {
-      fa_ld32(tS + lane + c, v);
+  } else {                                           // ===== softmax rows + MMA issuer
+    const uint32_t lane = (uint32_t)(warp * 32) << 16;
+    const uint32_t tS = tmem, tO = tmem + 128;
+    constexpr uint32_t idS = idesc_bf16_f32(128, 128, false, false);
+    constexpr uint32_t idO = idesc_bf16_f32(128, 64, false, true);
+    const float sc2 = p.scale * FA_LOG2E;
+    float o[FA_D];
 #pragma unroll
-      for (int i = 0; i < 32; ++i)
-        if (!diag || c + i <= tid) mx = fmaxf(mx, v[i] * sc2);
-    }
-    const float alpha = exp2f(m - mx);           // m == -inf on the first block: alpha = 0
-    float rs = 0.f;
-#pragma unroll 1
-    for (int c = 0; c < 128; c += 32) {
-      fa_ld32(tS + lane + c, v);
-#pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        const float e = (!diag || c + i <= tid) ? exp2f(v[i] * sc2 - mx) : 0.f;
-        v[i] = e;
-        rs += e;
+    for (int e = 0; e < FA_D; ++e) o[e] = 0.f;
+    float m = -INFINITY, l = 0.f;
+    mbar_wait(q_full, 0);
+    for (int j = 0; j <= qb; ++j) {
+      const int b = j & 1;
+      if (tid == 0) {
+        mbar_wait(&kv_full[b], (uint32_t)((j >> 1) & 1));
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        fa_mma_k64(tS, sQ, sK + b * FA_TILE, idS, false);
+        fa_commit(s_done);
       }
-      fa_store_row32(sP, tid, c, v);
-    }
-    l = l * alpha + rs;
-    m = mx;
-    fa_proxy_fence();
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
-    if (tid == 0) {
+      mbar_wait(s_done, (uint32_t)(j & 1));
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      // O_blk = P . V: K = 128 keys in two 64-key sub-tiles of P; V is an MN-major B operand
-      // ([keys][64] rows: K steps of 16 keys = 2048 B)
+      const bool diag = j == qb;
+      float mx = m;
+      float v[32];
+#pragma unroll 1
+      for (int c = 0; c < 128; c += 32) {
+        fa_ld32(tS + lane + c, v);
 #pragma unroll
-      for (int k = 0; k < FA_BLK / 16; ++k)
-        fa_mma(tO, fa_desc(sP + (k >> 2) * FA_TILE, 16) + 2 * (k & 3), fa_desc(sV, 8192) + 128 * k, idO,
-               k > 0 ? 1u : 0u);
-      fa_commit(&bar[1]);
+        for (int i = 0; i < 32; ++i)
+          if (!diag || c + i <= tid) mx = fmaxf(mx, v[i] * sc2);
+      }
+      const float alpha = exp2f(m - mx);           // m == -inf on the first block: alpha = 0
+      float rs = 0.f;
+#pragma unroll 1
+      for (int c = 0; c < 128; c += 32) {
+        fa_ld32(tS + lane + c, v);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const float e = (!diag || c + i <= tid) ? exp2f(v[i] * sc2 - mx) : 0.f;
+          v[i] = e;
+          rs += e;
+        }
+        fa_store_row32(sP, tid, c, v);
+      }
+      l = l * alpha + rs;
+      m = mx;
+      fa_proxy_fence();
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      fa_bar(1, 128);
+      if (tid == 0) {
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        // O_blk = P . V: K = 128 keys in two 64-key sub-tiles of P; V is an MN-major B operand
+        // ([keys][64] rows: K steps of 16 keys = 2048 B)
+        const unsigned char* vb = sV + b * FA_TILE;
+#pragma unroll
+        for (int k = 0; k < FA_BLK / 16; ++k)
+          fa_mma(tO, fa_desc(sP + (k >> 2) * FA_TILE, 16) + 2 * (k & 3), fa_desc(vb, 8192) + 128 * k, idO,
+                 k > 0 ? 1u : 0u);
+        fa_commit(o_done);
+        fa_commit(&kv_empty[b]);                   // K / V buffer b free once these MMAs retire
+      }
+      mbar_wait(o_done, (uint32_t)(j & 1));
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+      for (int c = 0; c < FA_D; c += 32) {
+        fa_ld32(tO + lane + c, v);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) o[c + i] = o[c + i] * alpha + v[i];
+      }
     }
-    mbar_wait(&bar[1], (uint32_t)(j & 1));
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    // epilogue: O / l through shared memory (coalesced row stores), lse = m + log2(l)
+    const float inv = 1.f / l;
+    p.lse[(long long)bh * p.T + qb * FA_BLK + tid] = m + log2f(l);
+    float* stage = (float*)sK;                     // [128][68] fp32 over the K / V buffers (64 KB)
 #pragma unroll
-    for (int c = 0; c < FA_D; c += 32) {
-      fa_ld32(tO + lane + c, v);
-#pragma unroll
-      for (int i = 0; i < 32; ++i) o[c + i] = o[c + i] * alpha + v[i];
+    for (int e = 0; e < FA_D; e += 4)
+      *(float4*)(stage + tid * 68 + e) = make_float4(o[e] * inv, o[e + 1] * inv, o[e + 2] * inv, o[e + 3] * inv);
+    fa_bar(1, 128);
+    float* Ob = O + hoff + (long long)qb * FA_BLK * FA_D;
+    for (int u = tid; u < FA_BLK * 16; u += 128) {
+      const int r = u >> 4, c4 = u & 15;
+      *(float4*)(Ob + r * FA_D + c4 * 4) = *(const float4*)(stage + r * 68 + c4 * 4);
     }
-  }
-  // epilogue: O / l through shared memory (coalesced row stores), lse = m + log2(l)
-  const float inv = 1.f / l;
-  p.lse[(long long)bh * p.T + qb * FA_BLK + tid] = m + log2f(l);
-  __syncthreads();
-  float* stage = (float*)sK;                     // [128][68] fp32 over sK, sV, sP (80 KB free)
-#pragma unroll
-  for (int e = 0; e < FA_D; e += 4)
-    *(float4*)(stage + tid * 68 + e) = make_float4(o[e] * inv, o[e + 1] * inv, o[e + 2] * inv, o[e + 3] * inv);
-  __syncthreads();
-  float* Ob = O + hoff + (long long)qb * FA_BLK * FA_D;
-  for (int u = tid; u < FA_BLK * 16; u += 128) {
-    const int r = u >> 4, c4 = u & 15;
-    *(float4*)(Ob + r * FA_D + c4 * 4) = *(const float4*)(stage + r * 68 + c4 * 4);
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if (warp == 0) {
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256) : "memory");
-  }
+  if (warp == 0) fa_tmem_free(tmem, 256);
   publish_late(p.out, O);
 }
 
 // ============================================================== delta = rowsum(dO * O)
 __global__ void __launch_bounds__(256) k_fa_delta(const __grid_constant__ FaParams p) {
   COEX_PDL_ENTER();
-  stamp(p.ds, SK_ATTN);
+  stamp(p.ds, SK_ATTN_DELTA);
   const float* dO = res<float>(p.dout);
   const float* O = res<float>(p.o);
   const long long rows = (long long)p.BH * p.T;
@@ -302,225 +336,250 @@ __device__ __forceinline__ void fa_pds(uint32_t tS, uint32_t tdP, uint32_t lane,
 }
 
 // ============================================================== backward: dK, dV per key block
-__global__ void __launch_bounds__(256, 1) k_fa_bwd_kv(const __grid_constant__ FaParams p) {
+// 384 threads: warps 0-7 = (query row r, key half h) of the S / dP tiles, warps 8-11 = loader
+// of the next query block's Q and dO tiles (double-buffered).
+__global__ void __launch_bounds__(384, 1) k_fa_bwd_kv(const __grid_constant__ FaParams p) {
   COEX_PDL_ENTER();
-  stamp(p.ds, SK_ATTN);
+  stamp(p.ds, SK_ATTN_KV);
   extern __shared__ __align__(1024) unsigned char fa_raw[];
   unsigned char* sm = (unsigned char*)(((uintptr_t)fa_raw + 1023) & ~(uintptr_t)1023);
-  unsigned char* sQ = sm;
-  unsigned char* sdO = sm + FA_TILE;
-  unsigned char* sK = sm + 2 * FA_TILE;
-  unsigned char* sV = sm + 3 * FA_TILE;
-  unsigned char* sP = sm + 4 * FA_TILE;          // [128 q][128 keys] (two sub-tiles)
-  unsigned char* sdS = sm + 6 * FA_TILE;         // same
-  uint64_t* bar = (uint64_t*)(sm + 8 * FA_TILE);
-  uint32_t* tslot = (uint32_t*)(bar + 2);
-  const int tid = threadIdx.x, warp = tid >> 5, r = tid & 127, h = tid >> 7;
+  unsigned char* sK = sm;
+  unsigned char* sV = sm + FA_TILE;
+  unsigned char* sQ = sm + 2 * FA_TILE;          // [2]
+  unsigned char* sdO = sm + 4 * FA_TILE;         // [2]
+  unsigned char* sP = sm + 6 * FA_TILE;          // [128 q][128 keys] (two sub-tiles)
+  unsigned char* sdS = sm + 8 * FA_TILE;         // same
+  uint64_t* bar = (uint64_t*)(sm + 10 * FA_TILE);
+  uint64_t *qd_full = bar, *qd_empty = bar + 2, *kv_full = bar + 4, *s_done = bar + 5, *o_done = bar + 6;
+  uint32_t* tslot = (uint32_t*)(bar + 8);
+  const int tid = threadIdx.x, warp = tid >> 5;
   const int nb = p.T / FA_BLK;
   const int kb = (int)(blockIdx.x / p.BH);       // key block (low = most query blocks: first)
   const int bh = (int)(blockIdx.x % p.BH);
   const long long hoff = (long long)bh * p.T * FA_D;
-  const float* Q = res<float>(p.q) + hoff;
-  const float* K = res<float>(p.k) + hoff;
-  const float* V = res<float>(p.v) + hoff;
-  const float* dO = res<float>(p.dout) + hoff;
   float* dK = pick_out<float>(p.out2, res<float>(p.pa), res<float>(p.pb));
   float* dV = pick_out<float>(p.out3, res<float>(p.pa), res<float>(p.pb));
   publish_early(p.out2, dK);
   publish_early(p.out3, dV);
   count_op(p.ds);
   if (tid == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&qd_full[i], 128);
+      mbar_init(&qd_empty[i], 1);
+    }
+    mbar_init(kv_full, 128);
+    mbar_init(s_done, 1);
+    mbar_init(o_done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)), "r"(512)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
-  }
-  fa_load<256>(sK, K, kb * FA_BLK);
-  fa_load<256>(sV, V, kb * FA_BLK);
+  if (warp == 0) fa_tmem_alloc(tslot, 512);
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tslot;
-  const uint32_t lane = (uint32_t)((warp & 3) * 32) << 16;
   const uint32_t tS = tmem, tdP = tmem + 128, tdV = tmem + 256, tdK = tmem + 320;
-  constexpr uint32_t idS = idesc_bf16_f32(128, 128, false, false);
-  constexpr uint32_t idKV = idesc_bf16_f32(128, 64, true, true);
-  const float sc2 = p.scale * FA_LOG2E;
-  int it = 0;
-  for (int qb = kb; qb < nb; ++qb, ++it) {
-    fa_load<256>(sQ, Q, qb * FA_BLK);
-    fa_load<256>(sdO, dO, qb * FA_BLK);
-    const long long row = (long long)bh * p.T + qb * FA_BLK + r;
-    const float lse2 = p.lse[row], dl = p.delta[row];
-    fa_proxy_fence();
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
-    if (tid == 0) {
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      fa_mma_k64(tS, sQ, sK, idS, false);        // S = Q . K^T
-      fa_mma_k64(tdP, sdO, sV, idS, false);      // dP = dO . V^T
-      fa_commit(&bar[0]);
+  if (tid >= 256) {                                  // ===== loader warpgroup
+    const float* Q = res<float>(p.q) + hoff;
+    const float* dO = res<float>(p.dout) + hoff;
+    fa_load<128>(sK, res<float>(p.k) + hoff, kb * FA_BLK);
+    fa_load<128>(sV, res<float>(p.v) + hoff, kb * FA_BLK);
+    fa_publish(kv_full);
+    int it = 0;
+    for (int qb = kb; qb < nb; ++qb, ++it) {
+      const int b = it & 1;
+      if (it >= 2) mbar_wait(&qd_empty[b], (uint32_t)(((it - 2) >> 1) & 1));
+      fa_load<128>(sQ + b * FA_TILE, Q, qb * FA_BLK);
+      fa_load<128>(sdO + b * FA_TILE, dO, qb * FA_BLK);
+      fa_publish(&qd_full[b]);
     }
-    mbar_wait(&bar[0], (uint32_t)(it & 1));
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    fa_pds<true>(tS, tdP, lane, r, h, qb == kb, lse2, dl, sc2, p.scale, sP, sdS);
-    fa_proxy_fence();
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
-    if (tid == 0) {
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      // dV += P^T . dO, dK += dS^T . Q: A = the [q][keys] tile read MN-major (M = keys in two
-      // 64-key blocks 16 KB apart, K = query rows: steps of 16 rows = 2048 B); B = the
-      // [q][64] tile read MN-major (N = head dim)
-#pragma unroll
-      for (int k = 0; k < FA_BLK / 16; ++k) {
-        const uint32_t acc = (it > 0 || k > 0) ? 1u : 0u;
-        fa_mma(tdV, fa_desc(sP, FA_TILE) + 128 * k, fa_desc(sdO, 8192) + 128 * k, idKV, acc);
-        fa_mma(tdK, fa_desc(sdS, FA_TILE) + 128 * k, fa_desc(sQ, 8192) + 128 * k, idKV, acc);
+  } else {                                           // ===== compute warpgroups + MMA issuer
+    const int r = tid & 127, h = tid >> 7;
+    const uint32_t lane = (uint32_t)((warp & 3) * 32) << 16;
+    constexpr uint32_t idS = idesc_bf16_f32(128, 128, false, false);
+    constexpr uint32_t idKV = idesc_bf16_f32(128, 64, true, true);
+    const float sc2 = p.scale * FA_LOG2E;
+    if (tid == 0) mbar_wait(kv_full, 0);
+    int it = 0;
+    for (int qb = kb; qb < nb; ++qb, ++it) {
+      const int b = it & 1;
+      const long long row = (long long)bh * p.T + qb * FA_BLK + r;
+      const float lse2 = p.lse[row], dl = p.delta[row];
+      if (tid == 0) {
+        mbar_wait(&qd_full[b], (uint32_t)((it >> 1) & 1));
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        fa_mma_k64(tS, sQ + b * FA_TILE, sK, idS, false);      // S = Q . K^T
+        fa_mma_k64(tdP, sdO + b * FA_TILE, sV, idS, false);    // dP = dO . V^T
+        fa_commit(s_done);
       }
-      fa_commit(&bar[1]);
-    }
-    mbar_wait(&bar[1], (uint32_t)(it & 1));
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  }
-  // epilogue: warps 0-3 dV, warps 4-7 dK (row = key), staged through shared memory
-  float* stage = (float*)sm + h * (FA_BLK * 68);  // two [128][68] fp32 stages (68 KB of the 128 KB)
-  {
-    float v[32];
-    const uint32_t tacc = h ? tdK : tdV;
-#pragma unroll 1
-    for (int c = 0; c < FA_D; c += 32) {
-      fa_ld32(tacc + lane + c, v);
+      // s_done also retires the previous block's dV / dK MMAs (issued earlier by the same
+      // thread): sP / sdS are free to overwrite
+      mbar_wait(s_done, (uint32_t)(it & 1));
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      fa_pds<true>(tS, tdP, lane, r, h, qb == kb, lse2, dl, sc2, p.scale, sP, sdS);
+      fa_proxy_fence();
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      fa_bar(1, 256);
+      if (tid == 0) {
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        // dV += P^T . dO, dK += dS^T . Q: A = the [q][keys] tile read MN-major (M = keys in two
+        // 64-key blocks 16 KB apart, K = query rows: steps of 16 rows = 2048 B); B = the
+        // [q][64] tile read MN-major (N = head dim)
+        const unsigned char* qbuf = sQ + b * FA_TILE;
+        const unsigned char* obuf = sdO + b * FA_TILE;
 #pragma unroll
-      for (int i = 0; i < 32; i += 4)
-        *(float4*)(stage + r * 68 + c + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+        for (int k = 0; k < FA_BLK / 16; ++k) {
+          const uint32_t acc = (it > 0 || k > 0) ? 1u : 0u;
+          fa_mma(tdV, fa_desc(sP, FA_TILE) + 128 * k, fa_desc(obuf, 8192) + 128 * k, idKV, acc);
+          fa_mma(tdK, fa_desc(sdS, FA_TILE) + 128 * k, fa_desc(qbuf, 8192) + 128 * k, idKV, acc);
+        }
+        fa_commit(&qd_empty[b]);
+      }
     }
-  }
-  __syncthreads();
-  for (int u = tid; u < 2 * FA_BLK * 16; u += 256) {
-    const int w = u / (FA_BLK * 16), rr = (u >> 4) & 127, c4 = u & 15;
-    float* dst = (w ? dK : dV) + hoff + (long long)(kb * FA_BLK + rr) * FA_D + c4 * 4;
-    *(float4*)dst = *(const float4*)((float*)sm + w * (FA_BLK * 68) + rr * 68 + c4 * 4);
+    if (tid == 0) fa_commit(o_done);
+    mbar_wait(o_done, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    // epilogue: warps 0-3 dV, warps 4-7 dK (row = key), staged through shared memory
+    float* stage = (float*)sQ + h * (FA_BLK * 68);  // two [128][68] fp32 stages (68 KB of sQ..sdS)
+    {
+      float v[32];
+      const uint32_t tacc = h ? tdK : tdV;
+#pragma unroll 1
+      for (int c = 0; c < FA_D; c += 32) {
+        fa_ld32(tacc + lane + c, v);
+#pragma unroll
+        for (int i = 0; i < 32; i += 4)
+          *(float4*)(stage + r * 68 + c + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+      }
+    }
+    fa_bar(1, 256);
+    for (int u = tid; u < 2 * FA_BLK * 16; u += 256) {
+      const int w = u / (FA_BLK * 16), rr = (u >> 4) & 127, c4 = u & 15;
+      float* dst = (w ? dK : dV) + hoff + (long long)(kb * FA_BLK + rr) * FA_D + c4 * 4;
+      *(float4*)dst = *(const float4*)((float*)sQ + w * (FA_BLK * 68) + rr * 68 + c4 * 4);
+    }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if (warp == 0) {
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512) : "memory");
-  }
+  if (warp == 0) fa_tmem_free(tmem, 512);
   publish_late(p.out2, dK);
   publish_late(p.out3, dV);
 }
 
 // ============================================================== backward: dQ per query block
-__global__ void __launch_bounds__(256, 1) k_fa_bwd_q(const __grid_constant__ FaParams p) {
+// 384 threads: warps 0-7 compute, warps 8-11 load the next key block's K and V tiles.
+__global__ void __launch_bounds__(384, 1) k_fa_bwd_q(const __grid_constant__ FaParams p) {
   COEX_PDL_ENTER();
-  stamp(p.ds, SK_ATTN);
+  stamp(p.ds, SK_ATTN_Q);
   extern __shared__ __align__(1024) unsigned char fa_raw[];
   unsigned char* sm = (unsigned char*)(((uintptr_t)fa_raw + 1023) & ~(uintptr_t)1023);
   unsigned char* sQ = sm;
   unsigned char* sdO = sm + FA_TILE;
-  unsigned char* sK = sm + 2 * FA_TILE;
-  unsigned char* sV = sm + 3 * FA_TILE;
-  unsigned char* sdS = sm + 4 * FA_TILE;         // [128 q][128 keys]
-  uint64_t* bar = (uint64_t*)(sm + 6 * FA_TILE);
-  uint32_t* tslot = (uint32_t*)(bar + 2);
-  const int tid = threadIdx.x, warp = tid >> 5, r = tid & 127, h = tid >> 7;
+  unsigned char* sK = sm + 2 * FA_TILE;          // [2]
+  unsigned char* sV = sm + 4 * FA_TILE;          // [2]
+  unsigned char* sdS = sm + 6 * FA_TILE;         // [128 q][128 keys]
+  uint64_t* bar = (uint64_t*)(sm + 8 * FA_TILE);
+  uint64_t *kv_full = bar, *kv_empty = bar + 2, *q_full = bar + 4, *s_done = bar + 5, *o_done = bar + 6;
+  uint32_t* tslot = (uint32_t*)(bar + 8);
+  const int tid = threadIdx.x, warp = tid >> 5;
   const int nb = p.T / FA_BLK;
   const int qb = nb - 1 - (int)(blockIdx.x / p.BH);
   const int bh = (int)(blockIdx.x % p.BH);
   const long long hoff = (long long)bh * p.T * FA_D;
-  const float* Q = res<float>(p.q) + hoff;
-  const float* K = res<float>(p.k) + hoff;
-  const float* V = res<float>(p.v) + hoff;
-  const float* dO = res<float>(p.dout) + hoff;
   float* dQ = pick_out<float>(p.out, res<float>(p.pa), res<float>(p.pb));
   publish_early(p.out, dQ);
   count_op(p.ds);
   if (tid == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&kv_full[i], 128);
+      mbar_init(&kv_empty[i], 1);
+    }
+    mbar_init(q_full, 128);
+    mbar_init(s_done, 1);
+    mbar_init(o_done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)), "r"(512)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
-  }
-  fa_load<256>(sQ, Q, qb * FA_BLK);
-  fa_load<256>(sdO, dO, qb * FA_BLK);
+  if (warp == 0) fa_tmem_alloc(tslot, 512);
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tslot;
-  const uint32_t lane = (uint32_t)((warp & 3) * 32) << 16;
   const uint32_t tS = tmem, tdP = tmem + 128, tdQ = tmem + 256;
-  constexpr uint32_t idS = idesc_bf16_f32(128, 128, false, false);
-  constexpr uint32_t idQ = idesc_bf16_f32(128, 64, false, true);
-  const float sc2 = p.scale * FA_LOG2E;
-  const long long row = (long long)bh * p.T + qb * FA_BLK + r;
-  const float lse2 = p.lse[row], dl = p.delta[row];
-  for (int kb = 0; kb <= qb; ++kb) {
-    fa_load<256>(sK, K, kb * FA_BLK);
-    fa_load<256>(sV, V, kb * FA_BLK);
-    fa_proxy_fence();
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
-    if (tid == 0) {
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      fa_mma_k64(tS, sQ, sK, idS, false);
-      fa_mma_k64(tdP, sdO, sV, idS, false);
-      fa_commit(&bar[0]);
+  if (tid >= 256) {                                  // ===== loader warpgroup
+    const float* K = res<float>(p.k) + hoff;
+    const float* V = res<float>(p.v) + hoff;
+    fa_load<128>(sQ, res<float>(p.q) + hoff, qb * FA_BLK);
+    fa_load<128>(sdO, res<float>(p.dout) + hoff, qb * FA_BLK);
+    fa_publish(q_full);
+    for (int kb = 0; kb <= qb; ++kb) {
+      const int b = kb & 1;
+      if (kb >= 2) mbar_wait(&kv_empty[b], (uint32_t)(((kb - 2) >> 1) & 1));
+      fa_load<128>(sK + b * FA_TILE, K, kb * FA_BLK);
+      fa_load<128>(sV + b * FA_TILE, V, kb * FA_BLK);
+      fa_publish(&kv_full[b]);
     }
-    mbar_wait(&bar[0], (uint32_t)(kb & 1));
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    fa_pds<false>(tS, tdP, lane, r, h, kb == qb, lse2, dl, sc2, p.scale, nullptr, sdS);
-    fa_proxy_fence();
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
-    if (tid == 0) {
+  } else {                                           // ===== compute warpgroups + MMA issuer
+    const int r = tid & 127, h = tid >> 7;
+    const uint32_t lane = (uint32_t)((warp & 3) * 32) << 16;
+    constexpr uint32_t idS = idesc_bf16_f32(128, 128, false, false);
+    constexpr uint32_t idQ = idesc_bf16_f32(128, 64, false, true);
+    const float sc2 = p.scale * FA_LOG2E;
+    const long long row = (long long)bh * p.T + qb * FA_BLK + r;
+    const float lse2 = p.lse[row], dl = p.delta[row];
+    if (tid == 0) mbar_wait(q_full, 0);
+    for (int kb = 0; kb <= qb; ++kb) {
+      const int b = kb & 1;
+      if (tid == 0) {
+        mbar_wait(&kv_full[b], (uint32_t)((kb >> 1) & 1));
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        fa_mma_k64(tS, sQ, sK + b * FA_TILE, idS, false);
+        fa_mma_k64(tdP, sdO, sV + b * FA_TILE, idS, false);
+        fa_commit(s_done);
+      }
+      mbar_wait(s_done, (uint32_t)(kb & 1));        // (also retires the previous dQ MMAs: sdS free)
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      // dQ += dS . K: A = dS K-major (K = keys, two sub-tiles), B = K tile MN-major (N = 64)
+      fa_pds<false>(tS, tdP, lane, r, h, kb == qb, lse2, dl, sc2, p.scale, nullptr, sdS);
+      fa_proxy_fence();
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      fa_bar(1, 256);
+      if (tid == 0) {
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        // dQ += dS . K: A = dS K-major (K = keys, two sub-tiles), B = K tile MN-major (N = 64)
+        const unsigned char* kbuf = sK + b * FA_TILE;
 #pragma unroll
-      for (int k = 0; k < FA_BLK / 16; ++k)
-        fa_mma(tdQ, fa_desc(sdS + (k >> 2) * FA_TILE, 16) + 2 * (k & 3), fa_desc(sK, 8192) + 128 * k, idQ,
-               (kb > 0 || k > 0) ? 1u : 0u);
-      fa_commit(&bar[1]);
+        for (int k = 0; k < FA_BLK / 16; ++k)
+          fa_mma(tdQ, fa_desc(sdS + (k >> 2) * FA_TILE, 16) + 2 * (k & 3), fa_desc(kbuf, 8192) + 128 * k, idQ,
+                 (kb > 0 || k > 0) ? 1u : 0u);
+        fa_commit(&kv_empty[b]);
+      }
     }
-    mbar_wait(&bar[1], (uint32_t)(kb & 1));
+    if (tid == 0) fa_commit(o_done);
+    mbar_wait(o_done, 0);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  }
-  float* stage = (float*)sm;                     // [128][68] fp32 (34 KB of the 96 KB)
-  if (h == 0) {
-    float v[32];
+    float* stage = (float*)sK;                     // [128][68] fp32 over the K / V buffers
+    if (h == 0) {
+      float v[32];
 #pragma unroll 1
-    for (int c = 0; c < FA_D; c += 32) {
-      fa_ld32(tdQ + lane + c, v);
+      for (int c = 0; c < FA_D; c += 32) {
+        fa_ld32(tdQ + lane + c, v);
 #pragma unroll
-      for (int i = 0; i < 32; i += 4)
-        *(float4*)(stage + r * 68 + c + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+        for (int i = 0; i < 32; i += 4)
+          *(float4*)(stage + r * 68 + c + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+      }
     }
-  }
-  __syncthreads();
-  for (int u = tid; u < FA_BLK * 16; u += 256) {
-    const int rr = u >> 4, c4 = u & 15;
-    *(float4*)(dQ + hoff + (long long)(qb * FA_BLK + rr) * FA_D + c4 * 4) = *(const float4*)(stage + rr * 68 + c4 * 4);
+    fa_bar(1, 256);
+    for (int u = tid; u < FA_BLK * 16; u += 256) {
+      const int rr = u >> 4, c4 = u & 15;
+      *(float4*)(dQ + hoff + (long long)(qb * FA_BLK + rr) * FA_D + c4 * 4) = *(const float4*)(stage + rr * 68 + c4 * 4);
+    }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if (warp == 0) {
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512) : "memory");
-  }
+  if (warp == 0) fa_tmem_free(tmem, 512);
   publish_late(p.out, dQ);
 }
 
-constexpr size_t kFaFwdSmem = 5 * FA_TILE + 1024 + 64;
-constexpr size_t kFaKvSmem = 8 * FA_TILE + 1024 + 64;
-constexpr size_t kFaQSmem = 7 * FA_TILE + 1024 + 64;   // one CTA per SM (its TMEM takes all 512 columns)
+constexpr size_t kFaFwdSmem = 7 * FA_TILE + 1024 + 128;
+constexpr size_t kFaKvSmem = 10 * FA_TILE + 1024 + 128;
+constexpr size_t kFaQSmem = 8 * FA_TILE + 1024 + 128;
 
 }  // namespace coex

@@ -53,7 +53,8 @@ enum StampKind {
   SK_FEED_WAIT = 7, SK_FEED_FILL = 8, SK_FETCH = 9, SK_GATE = 10, SK_COMMIT = 11, SK_END = 12,
   SK_AFTER_WAIT = 64, SK_FUSED = 13, SK_IM2COL = 14, SK_COL2IM = 15, SK_CVT = 16, SK_COLSTATS = 17,
   SK_BNAPPLY = 18, SK_SPLITK = 19, SK_SOFTMAX = 20, SK_SOFTMAX_GRAD = 21, SK_CE = 22, SK_BIAS = 23, SK_LN = 24,
-  SK_EMBED = 25, SK_COLSUM = 26, SK_SKEW = 27, SK_POOL = 28, SK_AXIS = 29, SK_GUARD = 30, SK_ATTN = 31
+  SK_EMBED = 25, SK_COLSUM = 26, SK_SKEW = 27, SK_POOL = 28, SK_AXIS = 29, SK_GUARD = 30, SK_ATTN = 31,
+  SK_ATTN_DELTA = 32, SK_ATTN_KV = 33, SK_ATTN_Q = 34
 };
 
 // Host <-> device rings in pinned, mapped host memory.

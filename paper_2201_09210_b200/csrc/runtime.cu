@@ -2739,7 +2739,7 @@ struct Builder {
         if (mode == 0) {
           read_out(fp.out);
           Launch L;
-          L.set((void*)k_fa_fwd, dim3(blocks), dim3(128), fp);
+          L.set((void*)k_fa_fwd, dim3(blocks), dim3(256), fp);
           L.smem = kFaFwdSmem;
           return add_kernel(g, prev, L);
         }
@@ -2750,9 +2750,9 @@ struct Builder {
         const int64_t rows = (int64_t)fp.BH * fp.T;
         const int64_t db = (rows * 16 + 255) / 256;
         L0.set((void*)k_fa_delta, dim3((unsigned)(db < kNumSMs * 8 ? db : kNumSMs * 8)), dim3(256), fp);
-        L1.set((void*)k_fa_bwd_kv, dim3(blocks), dim3(256), fp);
+        L1.set((void*)k_fa_bwd_kv, dim3(blocks), dim3(384), fp);
         L1.smem = kFaKvSmem;
-        L2.set((void*)k_fa_bwd_q, dim3(blocks), dim3(256), fp);
+        L2.set((void*)k_fa_bwd_q, dim3(blocks), dim3(384), fp);
         L2.smem = kFaQSmem;
         int rc = add_kernel(g, prev, L0);
         if (!rc) rc = add_kernel(g, prev, L1);

@@ -111,6 +111,7 @@ class Plan:
     node_shapes: dict = field(default_factory=dict)
     feed_shapes: dict = field(default_factory=dict)
     folded: set = field(default_factory=set)
+    n_attn: int = 0                      # flash-attention groups (one forward + one backward item each)
 
 
 class Planner:
@@ -494,7 +495,7 @@ class Planner:
         w += body
         sig = (tuple(sorted((k, tuple(v)) for k, v in self.var_shapes.items())),
                tuple(sorted((k, tuple(v)) for k, v in self.feed_shapes.items())))
-        plan = Plan(w, consts, sig, n_compute[0], flops[0], shapes, dict(self.feed_shapes), folded)
+        plan = Plan(w, consts, sig, n_compute[0], flops[0], shapes, dict(self.feed_shapes), folded, self.n_attn)
         plan.const_slots = dict(self.const_slots)
         return plan
 
