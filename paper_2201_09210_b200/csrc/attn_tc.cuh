@@ -91,7 +91,7 @@ __device__ __forceinline__ void fa_ld32(uint32_t taddr, float (&v)[32]) {
 template <int NT>
 __device__ __forceinline__ void fa_load(unsigned char* dst, const float* src, int t0) {
 #pragma unroll 4
-  for (int u = threadIdx.x; u < FA_BLK * 8; u += NT) {
+  for (int u = threadIdx.x % NT; u < FA_BLK * 8; u += NT) {     // (loader warpgroup: its own index)
     const int r = u >> 3, c = u & 7;
     const float* s = src + (long long)(t0 + r) * FA_D + c * 8;
     const float4 a = *(const float4*)s, b = *(const float4*)(s + 4);
