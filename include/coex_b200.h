@@ -157,6 +157,16 @@ int coex_exec_op_timed(coex_ctx* ctx, int kind, const coex_attrs* attrs, int nin
 int coex_exec_op_profile(coex_ctx* ctx, int kind, const coex_attrs* attrs, int nin, const int64_t* in_ids,
                          int reps, double* ms, int* nlaunch, char* names, int name_cap);
 
+/* Fused causal attention (csrc/attn_tc.cuh, tcgen05; fp32 / bf16 modes) outside a graph: the
+ * kernels the step graph runs for a planner attention group (T_ATTN) -- SURVEY §8(f)2; no
+ * reference counterpart (its op set is closed, pkg/src/coex/tensor.py:30-44), parity is against
+ * the unfused composition bmm_nt -> causal_softmax -> bmm (oracle/kernels.py).  Head dim 64, T a
+ * multiple of 128, fp32 [BH][T][64] operands.  backward = 0: in {q, k, v} -> out {O, lse [BH][T]}
+ * (lse in log2 units of scale*q.k); backward = 1: in {q, k, v, O, dO, lse} -> out {dQ, dK, dV}.
+ * reps > 0 re-launches the kernels reps times between CUDA events: *avg_ms per repetition. */
+int coex_flash_attn(coex_ctx* ctx, int backward, const int64_t* in_ids, int BH, int T, double scale, int reps,
+                    int64_t* out_ids, double* avg_ms);
+
 /* Device-side per-kernel stamps (%globaltimer, kernel kind) for the next passes (0 = off).
  * coex_ctx_read_trace returns n (time_ns, kind) pairs of the last pass. */
 int coex_ctx_set_trace(coex_ctx* ctx, int capacity);

@@ -65,6 +65,8 @@ SIGNATURES = {
     "coex_exec_op_profile": (ctypes.c_int, [_P, ctypes.c_int, ctypes.POINTER(CoexAttrs), ctypes.c_int, _I64P,
                                             ctypes.c_int, _DP, ctypes.POINTER(ctypes.c_int), ctypes.c_char_p,
                                             ctypes.c_int]),
+    "coex_flash_attn": (ctypes.c_int, [_P, ctypes.c_int, _I64P, ctypes.c_int, ctypes.c_int, ctypes.c_double,
+                                       ctypes.c_int, _I64P, _DP]),
     "coex_nccl_unique_id": (ctypes.c_int, [ctypes.c_char_p]),
     "coex_ctx_init_comm": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int, ctypes.c_char_p]),
     "coex_ctx_set_trace": (ctypes.c_int, [_P, ctypes.c_int]),
@@ -274,6 +276,23 @@ class B200Backend:
         _check(self.lib.coex_exec_op_timed(self.ctx, kind.code, ctypes.byref(at), len(devs), ids, reps,
                                            ctypes.byref(ms)))
         return ms.value
+
+    def flash_attention(self, values: list, scale: float, backward: bool = False, reps: int = 0):
+        """Fused causal attention (csrc/attn_tc.cuh) eagerly: forward ``[q, k, v]`` -> ``(O, lse)``,
+        backward ``[q, k, v, O, dO, lse]`` -> ``(dQ, dK, dV)``; fp32 ``[BH, T, 64]`` operands.
+        With ``reps`` > 0 also the average device ms of one (re-launched) repetition."""
+        devs = [v if isinstance(v, DevTensor) else self.put(v) for v in values]
+        BH, T = devs[0].shape[0], devs[0].shape[1]
+        ids = (ctypes.c_int64 * 6)(*[d.id for d in devs], *([0] * (6 - len(devs))))
+        outs = (ctypes.c_int64 * 3)()
+        ms = ctypes.c_double()
+        _check(self.lib.coex_flash_attn(self.ctx, 1 if backward else 0, ids, BH, T, float(scale), reps, outs,
+                                        ctypes.byref(ms)))
+        if backward:
+            res = tuple(DevTensor(self, outs[i], (BH, T, 64)) for i in range(3))
+        else:
+            res = (DevTensor(self, outs[0], (BH, T, 64)), DevTensor(self, outs[1], (BH, T)))
+        return (res, ms.value) if reps > 0 else res
 
     def profile_op(self, kind: OpKind, attrs: dict, values: list, reps: int = 20) -> list:
         """[(kernel name, average device ms)] for every launch of the op's lowering."""

@@ -37,6 +37,8 @@ struct FaParams {
   DevState* ds;
   In q, k, v, o, dout;       // fp32 [BH][T][64] (element (bh, t, e) at bh*T*64 + t*64 + e)
   int BH, T;
+  int H;                     // heads per row of the operand layout (1: [BH][T][64])
+  long long rs;              // row pitch in floats (64, or H * 64 for the merged layout)
   float scale;               // logits = scale * q.k
   float* lse;                // [BH][T] log2-domain row log-sum-exp of scale*q.k (fwd -> bwd)
   float* delta;              // [BH][T] rowsum(dO * O)
@@ -86,21 +88,76 @@ __device__ __forceinline__ void fa_ld32(uint32_t taddr, float (&v)[32]) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-// rows [t0, t0 + 128) of a fp32 [T][64] matrix -> bf16 swizzled tile; NT threads, coalesced
-// (8 consecutive threads cover one 256-byte row)
-template <int NT>
-__device__ __forceinline__ void fa_load(unsigned char* dst, const float* src, int t0) {
+// issue-only TMEM load of 32 columns (completion: fa_ld_wait, then fa_ld_dep on the registers)
+__device__ __forceinline__ void fa_ld32_issue(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void fa_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+// empty volatile asm "redefining" the registers after the wait: their uses cannot move above it
+__device__ __forceinline__ void fa_ld_dep(uint32_t (&r)[32]) {
+  asm volatile(""
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                 "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]), "+r"(r[15]),
+                 "+r"(r[16]), "+r"(r[17]), "+r"(r[18]), "+r"(r[19]), "+r"(r[20]), "+r"(r[21]), "+r"(r[22]),
+                 "+r"(r[23]), "+r"(r[24]), "+r"(r[25]), "+r"(r[26]), "+r"(r[27]), "+r"(r[28]), "+r"(r[29]),
+                 "+r"(r[30]), "+r"(r[31]));
+}
+
+// row t of head bh: [BH][T][64] (H == 1, rs == 64) or the merged [B][T][H*64] layout of the
+// projections the heads are split from (H heads, row pitch rs = H * 64)
+template <typename F>
+__device__ __forceinline__ F* fa_row(F* base, const FaParams& p, int bh, long long t) {
+  return base + ((long long)(bh / p.H) * p.T + t) * p.rs + (long long)(bh % p.H) * FA_D;
+}
+
+// ---- fp32 tile staging through the bulk-copy (TMA) engine.  The operands are fp32 rows
+// reached through runtime cells (no static tensor map), so the loader warpgroup issues 1-D
+// cp.async.bulk copies -- one 32 KB copy per tile when the head's rows are contiguous, else
+// one 256-byte copy per row -- into a fp32 staging tile that completes on an mbarrier; the
+// copies for block j+1 fly while block j is converted (smem -> bf16 swizzled smem) and used.
+constexpr int FA_STG = FA_BLK * FA_D * 4;       // one fp32 [128][64] staging tile: 32 KB
+
+__device__ __forceinline__ void fa_bulk(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+// loader thread lt (0..127): rows [t0, t0 + 128) of head bh -> fp32 staging tile
+__device__ __forceinline__ void fa_stage_issue(unsigned char* stg, const FaParams& p, const float* base, int bh,
+                                               int t0, uint64_t* full, int lt) {
+  if (p.rs == FA_D) {
+    if (lt == 0) fa_bulk(stg, fa_row(base, p, bh, t0), FA_STG, full);
+  } else {
+    fa_bulk(stg + lt * (FA_D * 4), fa_row(base, p, bh, t0 + lt), FA_D * 4, full);
+  }
+}
+// fp32 staging tile -> bf16 128-B-swizzled tile (128 loader threads; conflict-free both sides)
+__device__ __forceinline__ void fa_convert(unsigned char* dst, const unsigned char* stg, int lt) {
 #pragma unroll 4
-  for (int u = threadIdx.x % NT; u < FA_BLK * 8; u += NT) {     // (loader warpgroup: its own index)
+  for (int u = lt; u < FA_BLK * 8; u += 128) {
     const int r = u >> 3, c = u & 7;
-    const float* s = src + (long long)(t0 + r) * FA_D + c * 8;
-    const float4 a = *(const float4*)s, b = *(const float4*)(s + 4);
+    const float4 a = *(const float4*)(stg + r * 256 + c * 32), b = *(const float4*)(stg + r * 256 + c * 32 + 16);
     __nv_bfloat162 v0 = __floats2bfloat162_rn(a.x, a.y), v1 = __floats2bfloat162_rn(a.z, a.w);
     __nv_bfloat162 v2 = __floats2bfloat162_rn(b.x, b.y), v3 = __floats2bfloat162_rn(b.z, b.w);
     uint4 o;
     o.x = *(uint32_t*)&v0; o.y = *(uint32_t*)&v1; o.z = *(uint32_t*)&v2; o.w = *(uint32_t*)&v3;
     *(uint4*)(dst + fa_sw(r, c)) = o;
   }
+}
+// one staged pair of tiles (a, b) for the next phase of `full`: expect, then issue
+__device__ __forceinline__ void fa_stage_pair(unsigned char* stg, const FaParams& p, const float* a, const float* b,
+                                              int bh, int ta, int tb, uint64_t* full, int lt) {
+  if (lt == 0) mbar_expect_tx(full, (b ? 2 : 1) * FA_STG);
+  fa_stage_issue(stg, p, a, bh, ta, full, lt);
+  if (b) fa_stage_issue(stg + FA_STG, p, b, bh, tb, full, lt);
 }
 
 // 32 consecutive keys [k0, k0 + 32) of one row r of a [128][128] bf16 probability-type tile
@@ -158,24 +215,105 @@ __device__ __forceinline__ void fa_publish(uint64_t* full) {
 // global-load latency hides behind the block in flight.
 
 // ============================================================== forward
-// 256 threads: warps 0-3 = the 128 query rows (TMEM lanes), warps 4-7 = loader.
-__global__ void __launch_bounds__(256, 1) k_fa_fwd(const __grid_constant__ FaParams p) {
+// One CTA per (head, PAIR of 128-query tiles 2i / 2i+1): the two tiles share every K / V block
+// and run as a ping-pong on the tensor core -- while one softmax warpgroup works on its S
+// block, the single MMA thread computes the other tile's S and P.V.  416 threads:
+//   warps 0-3  softmax of tile A (query tile 2i, rows = TMEM lanes), warps 4-7 tile B (2i+1);
+//   warps 8-11 loader (fp32 rows -> bf16 128-B-swizzled tiles, K / V double-buffered);
+//   warp 12    MMA issuer (one elected thread).
+// O accumulates in TMEM (P.V with accumulate); the running row max is kept lazily (log2
+// domain, rescale of O / l only when a block raises it by more than FA_RESCALE, warp-uniform),
+// so un-normalised probabilities stay below 2^FA_RESCALE.
+// TMEM (512 columns): S_A 0-127 | S_B 128-255 | O_A 256-319 | O_B 320-383.
+constexpr float FA_RESCALE = 8.f;
+
+__device__ __forceinline__ float fa_ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ void fa_st32(uint32_t taddr, const float (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]), "f"(v[8]), "f"(v[9]),
+      "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]), "f"(v[15]), "f"(v[16]), "f"(v[17]), "f"(v[18]),
+      "f"(v[19]), "f"(v[20]), "f"(v[21]), "f"(v[22]), "f"(v[23]), "f"(v[24]), "f"(v[25]), "f"(v[26]), "f"(v[27]),
+      "f"(v[28]), "f"(v[29]), "f"(v[30]), "f"(v[31])
+      : "memory");
+}
+
+// pass 1 over one S row (128 keys in TMEM, two 32-column loads per wait): raw maximum over
+// the unmasked keys
+template <bool DIAG>
+__device__ __forceinline__ float fa_rowmax(uint32_t tS, int r) {
+  float mx = -INFINITY;
+#pragma unroll 1
+  for (int c = 0; c < FA_BLK; c += 64) {
+    uint32_t a[32], b[32];
+    fa_ld32_issue(tS + c, a);
+    fa_ld32_issue(tS + c + 32, b);
+    fa_ld_wait();
+    fa_ld_dep(a);
+    fa_ld_dep(b);
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      if (!DIAG || c + i <= r) mx = fmaxf(mx, __uint_as_float(a[i]));
+      if (!DIAG || c + 32 + i <= r) mx = fmaxf(mx, __uint_as_float(b[i]));
+    }
+  }
+  return mx;
+}
+// pass 2: P = 2^(s * sc2 - m) (bf16 into the swizzled P tile), returns the row sum
+template <bool DIAG>
+__device__ __forceinline__ float fa_rowexp(uint32_t tS, int r, float sc2, float m, unsigned char* sP) {
+  float rs0 = 0.f, rs1 = 0.f;
+#pragma unroll 1
+  for (int c = 0; c < FA_BLK; c += 64) {
+    uint32_t a[32], b[32];
+    fa_ld32_issue(tS + c, a);
+    fa_ld32_issue(tS + c + 32, b);
+    fa_ld_wait();
+    fa_ld_dep(a);
+    fa_ld_dep(b);
+    float v[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      v[i] = (!DIAG || c + i <= r) ? fa_ex2(fmaf(__uint_as_float(a[i]), sc2, -m)) : 0.f;
+      rs0 += v[i];
+    }
+    fa_store_row32(sP, r, c, v);
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      v[i] = (!DIAG || c + 32 + i <= r) ? fa_ex2(fmaf(__uint_as_float(b[i]), sc2, -m)) : 0.f;
+      rs1 += v[i];
+    }
+    fa_store_row32(sP, r, c + 32, v);
+  }
+  return rs0 + rs1;
+}
+
+__global__ void __launch_bounds__(416, 1) k_fa_fwd(const __grid_constant__ FaParams p) {
   COEX_PDL_ENTER();
   stamp(p.ds, SK_ATTN);
   extern __shared__ __align__(1024) unsigned char fa_raw[];
   unsigned char* sm = (unsigned char*)(((uintptr_t)fa_raw + 1023) & ~(uintptr_t)1023);
-  unsigned char* sQ = sm;
-  unsigned char* sK = sm + FA_TILE;              // [2] K buffers, then [2] V buffers
-  unsigned char* sV = sm + 3 * FA_TILE;
-  unsigned char* sP = sm + 5 * FA_TILE;          // two sub-tiles
-  uint64_t* bar = (uint64_t*)(sm + 7 * FA_TILE);
-  uint64_t *kv_full = bar, *kv_empty = bar + 2, *q_full = bar + 4, *s_done = bar + 5, *o_done = bar + 6;
-  uint32_t* tslot = (uint32_t*)(bar + 8);
+  unsigned char* sQ = sm;                        // [2 tiles]
+  unsigned char* sK = sm + 2 * FA_TILE;          // [2 buffers]
+  unsigned char* sV = sm + 4 * FA_TILE;          // [2 buffers]
+  unsigned char* sP = sm + 6 * FA_TILE;          // [2 tiles] x two 64-key sub-tiles
+  unsigned char* stg = sm + 10 * FA_TILE;        // fp32 staging: K | V (first Q_A | Q_B)
+  uint64_t* bar = (uint64_t*)(sm + 14 * FA_TILE);
+  uint64_t *kv_full = bar, *kv_empty = bar + 2, *q_full = bar + 4, *s_full = bar + 5, *p_full = bar + 7,
+           *o_done = bar + 9, *stg_full = bar + 11;
+  uint32_t* tslot = (uint32_t*)(bar + 12);
   const int tid = threadIdx.x, warp = tid >> 5;
-  const int nqb = p.T / FA_BLK;
-  const int qb = nqb - 1 - (int)(blockIdx.x / p.BH);   // heaviest query blocks first
+  const int nqb = p.T / FA_BLK, npair = (nqb + 1) / 2;
+  const int pi = npair - 1 - (int)(blockIdx.x / p.BH);   // heaviest pairs first
   const int bh = (int)(blockIdx.x % p.BH);
-  const long long hoff = (long long)bh * p.T * FA_D;
+  const int qA = 2 * pi;
+  const bool hasB = qA + 1 < nqb;
+  const int nk = hasB ? qA + 2 : qA + 1;                 // key blocks of the pair (tile t: qA + t + 1)
   float* O = pick_out<float>(p.out, res<float>(p.pa), res<float>(p.pb));
   publish_early(p.out, O);
   count_op(p.ds);
@@ -183,116 +321,142 @@ __global__ void __launch_bounds__(256, 1) k_fa_fwd(const __grid_constant__ FaPar
     for (int i = 0; i < 2; ++i) {
       mbar_init(&kv_full[i], 128);
       mbar_init(&kv_empty[i], 1);
+      mbar_init(&s_full[i], 1);
+      mbar_init(&p_full[i], 128);
+      mbar_init(&o_done[i], 1);
     }
     mbar_init(q_full, 128);
-    mbar_init(s_done, 1);
-    mbar_init(o_done, 1);
+    mbar_init(stg_full, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 0) fa_tmem_alloc(tslot, 256);
+  if (warp == 0) fa_tmem_alloc(tslot, 512);
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tslot;
-  if (tid >= 128) {                                  // ===== loader warpgroup
-    const float* K = res<float>(p.k) + hoff;
-    const float* V = res<float>(p.v) + hoff;
-    fa_load<128>(sQ, res<float>(p.q) + hoff, qb * FA_BLK);
+  if (warp >= 8 && warp < 12) {                      // ===== loader warpgroup
+    const float* Q = res<float>(p.q);
+    const float* K = res<float>(p.k);
+    const float* V = res<float>(p.v);
+    const int lt = tid & 127;
+    fa_stage_pair(stg, p, Q, hasB ? Q : nullptr, bh, qA * FA_BLK, (qA + 1) * FA_BLK, stg_full, lt);
+    mbar_wait(stg_full, 0);
+    fa_convert(sQ, stg, lt);
+    if (hasB) fa_convert(sQ + FA_TILE, stg + FA_STG, lt);
+    fa_bar(4, 128);                                  // staging drained
+    fa_stage_pair(stg, p, K, V, bh, 0, 0, stg_full, lt);
     fa_publish(q_full);
-    for (int j = 0; j <= qb; ++j) {
+    for (int j = 0; j < nk; ++j) {
       const int b = j & 1;
+      mbar_wait(stg_full, (uint32_t)((j + 1) & 1));
       if (j >= 2) mbar_wait(&kv_empty[b], (uint32_t)(((j - 2) >> 1) & 1));
-      fa_load<128>(sK + b * FA_TILE, K, j * FA_BLK);
-      fa_load<128>(sV + b * FA_TILE, V, j * FA_BLK);
+      fa_convert(sK + b * FA_TILE, stg, lt);
+      fa_convert(sV + b * FA_TILE, stg + FA_STG, lt);
       fa_publish(&kv_full[b]);
+      fa_bar(4, 128);
+      if (j + 1 < nk) fa_stage_pair(stg, p, K, V, bh, (j + 1) * FA_BLK, (j + 1) * FA_BLK, stg_full, lt);
     }
-  } else {                                           // ===== softmax rows + MMA issuer
-    const uint32_t lane = (uint32_t)(warp * 32) << 16;
-    const uint32_t tS = tmem, tO = tmem + 128;
-    constexpr uint32_t idS = idesc_bf16_f32(128, 128, false, false);
-    constexpr uint32_t idO = idesc_bf16_f32(128, 64, false, true);
-    const float sc2 = p.scale * FA_LOG2E;
-    float o[FA_D];
-#pragma unroll
-    for (int e = 0; e < FA_D; ++e) o[e] = 0.f;
-    float m = -INFINITY, l = 0.f;
-    mbar_wait(q_full, 0);
-    for (int j = 0; j <= qb; ++j) {
-      const int b = j & 1;
-      if (tid == 0) {
-        mbar_wait(&kv_full[b], (uint32_t)((j >> 1) & 1));
+  } else if (warp == 12) {                           // ===== MMA issuer
+    if ((tid & 31) == 0) {
+      constexpr uint32_t idS = idesc_bf16_f32(128, 128, false, false);
+      constexpr uint32_t idO = idesc_bf16_f32(128, 64, false, true);
+      const int ntile[2] = {qA + 1, qA + 2};
+      auto pv = [&](int t, int j) {                  // O_t += P_t . V(j)
+        mbar_wait(&p_full[t], (uint32_t)(j & 1));
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        fa_mma_k64(tS, sQ, sK + b * FA_TILE, idS, false);
-        fa_commit(s_done);
-      }
-      mbar_wait(s_done, (uint32_t)(j & 1));
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const bool diag = j == qb;
-      float mx = m;
-      float v[32];
-#pragma unroll 1
-      for (int c = 0; c < 128; c += 32) {
-        fa_ld32(tS + lane + c, v);
-#pragma unroll
-        for (int i = 0; i < 32; ++i)
-          if (!diag || c + i <= tid) mx = fmaxf(mx, v[i] * sc2);
-      }
-      const float alpha = exp2f(m - mx);           // m == -inf on the first block: alpha = 0
-      float rs = 0.f;
-#pragma unroll 1
-      for (int c = 0; c < 128; c += 32) {
-        fa_ld32(tS + lane + c, v);
-#pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const float e = (!diag || c + i <= tid) ? exp2f(v[i] * sc2 - mx) : 0.f;
-          v[i] = e;
-          rs += e;
-        }
-        fa_store_row32(sP, tid, c, v);
-      }
-      l = l * alpha + rs;
-      m = mx;
-      fa_proxy_fence();
-      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-      fa_bar(1, 128);
-      if (tid == 0) {
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        // O_blk = P . V: K = 128 keys in two 64-key sub-tiles of P; V is an MN-major B operand
-        // ([keys][64] rows: K steps of 16 keys = 2048 B)
-        const unsigned char* vb = sV + b * FA_TILE;
+        const unsigned char* pt = sP + t * 2 * FA_TILE;
+        const unsigned char* vb = sV + (j & 1) * FA_TILE;
 #pragma unroll
         for (int k = 0; k < FA_BLK / 16; ++k)
-          fa_mma(tO, fa_desc(sP + (k >> 2) * FA_TILE, 16) + 2 * (k & 3), fa_desc(vb, 8192) + 128 * k, idO,
-                 k > 0 ? 1u : 0u);
-        fa_commit(o_done);
-        fa_commit(&kv_empty[b]);                   // K / V buffer b free once these MMAs retire
+          fa_mma(tmem + 256 + 64 * t, fa_desc(pt + (k >> 2) * FA_TILE, 16) + 2 * (k & 3), fa_desc(vb, 8192) + 128 * k,
+                 idO, (j > 0 || k > 0) ? 1u : 0u);
+        fa_commit(&o_done[t]);
+      };
+      mbar_wait(q_full, 0);
+      for (int j = 0; j < nk; ++j) {
+        const int b = j & 1;
+        mbar_wait(&kv_full[b], (uint32_t)((j >> 1) & 1));
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        for (int t = 0; t < (hasB ? 2 : 1); ++t) {
+          if (j > 0 && j - 1 < ntile[t]) pv(t, j - 1);
+          if (j < ntile[t]) {
+            fa_mma_k64(tmem + 128 * t, sQ + t * FA_TILE, sK + b * FA_TILE, idS, false);
+            fa_commit(&s_full[t]);
+          }
+        }
+        if (j > 0) fa_commit(&kv_empty[(j - 1) & 1]);
       }
-      mbar_wait(o_done, (uint32_t)(j & 1));
+      for (int t = 0; t < (hasB ? 2 : 1); ++t)
+        if (ntile[t] == nk) pv(t, nk - 1);
+    }
+  } else if (warp < 4 || hasB) {                     // ===== softmax warpgroup t
+    const int t = warp >> 2, r = tid & 127, qb = qA + t;
+    const uint32_t lane = (uint32_t)((warp & 3) * 32) << 16;
+    const uint32_t tS = tmem + lane + 128 * t, tO = tmem + lane + 256 + 64 * t;
+    unsigned char* sPt = sP + t * 2 * FA_TILE;
+    const float sc2 = p.scale * FA_LOG2E;
+    float m = -INFINITY, l = 0.f;
+    for (int j = 0; j <= qb; ++j) {
+      mbar_wait(&s_full[t], (uint32_t)(j & 1));
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const bool diag = j == qb;
+      const float mx = (diag ? fa_rowmax<true>(tS, r) : fa_rowmax<false>(tS, r)) * sc2;
+      bool waited = false;
+      if (j == 0) {
+        m = mx;
+      } else {
+        const bool need = mx > m + FA_RESCALE;
+        if (__any_sync(0xffffffffu, need)) {         // warp-uniform: tcgen05.ld / st are collective
+          mbar_wait(&o_done[t], (uint32_t)((j - 1) & 1));
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          waited = true;
+          const float alpha = need ? fa_ex2(m - mx) : 1.f;
+          float v[32];
+#pragma unroll
+          for (int c = 0; c < FA_D; c += 32) {
+            fa_ld32(tO + c, v);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] *= alpha;
+            fa_st32(tO + c, v);
+          }
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+          l *= alpha;
+          if (need) m = mx;
+        }
+      }
+      if (j > 0 && !waited) mbar_wait(&o_done[t], (uint32_t)((j - 1) & 1));   // P_t free again
+      l += diag ? fa_rowexp<true>(tS, r, sc2, m, sPt) : fa_rowexp<false>(tS, r, sc2, m, sPt);
+      fa_proxy_fence();
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      mbar_arrive(&p_full[t]);
+    }
+    mbar_wait(&o_done[t], (uint32_t)(qb & 1));         // the last P.V
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    // epilogue: O / l through this tile's P buffer (free now; 128 x 64 fp32 = 32 KB, float4
+    // slots XOR-swizzled by row), coalesced row stores; lse = m + log2(l)
+    const float inv = 1.f / l;
+    p.lse[(long long)bh * p.T + qb * FA_BLK + r] = m + log2f(l);
+    float4* stage = (float4*)sPt;
+    {
+      float v[32];
 #pragma unroll
       for (int c = 0; c < FA_D; c += 32) {
-        fa_ld32(tO + lane + c, v);
+        fa_ld32(tO + c, v);
 #pragma unroll
-        for (int i = 0; i < 32; ++i) o[c + i] = o[c + i] * alpha + v[i];
+        for (int i = 0; i < 32; i += 4)
+          stage[r * 16 + (((c + i) >> 2) ^ (r & 15))] = make_float4(v[i] * inv, v[i + 1] * inv, v[i + 2] * inv,
+                                                                     v[i + 3] * inv);
       }
     }
-    // epilogue: O / l through shared memory (coalesced row stores), lse = m + log2(l)
-    const float inv = 1.f / l;
-    p.lse[(long long)bh * p.T + qb * FA_BLK + tid] = m + log2f(l);
-    float* stage = (float*)sK;                     // [128][68] fp32 over the K / V buffers (64 KB)
-#pragma unroll
-    for (int e = 0; e < FA_D; e += 4)
-      *(float4*)(stage + tid * 68 + e) = make_float4(o[e] * inv, o[e + 1] * inv, o[e + 2] * inv, o[e + 3] * inv);
-    fa_bar(1, 128);
-    float* Ob = O + hoff + (long long)qb * FA_BLK * FA_D;
-    for (int u = tid; u < FA_BLK * 16; u += 128) {
-      const int r = u >> 4, c4 = u & 15;
-      *(float4*)(Ob + r * FA_D + c4 * 4) = *(const float4*)(stage + r * 68 + c4 * 4);
+    fa_bar(1 + t, 128);
+    for (int u = r; u < FA_BLK * 16; u += 128) {
+      const int rr = u >> 4, c4 = u & 15;
+      *(float4*)(fa_row(O, p, bh, qb * FA_BLK + rr) + c4 * 4) = stage[rr * 16 + (c4 ^ (rr & 15))];
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if (warp == 0) fa_tmem_free(tmem, 256);
+  if (warp == 0) fa_tmem_free(tmem, 512);
   publish_late(p.out, O);
 }
 
@@ -306,7 +470,9 @@ __global__ void __launch_bounds__(256) k_fa_delta(const __grid_constant__ FaPara
   const int lane = threadIdx.x & 15;             // 16 threads per 64-wide row (one float4 each)
   for (long long r = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 4; r < rows;
        r += ((long long)gridDim.x * blockDim.x) >> 4) {
-    const float4 a = *(const float4*)(dO + r * FA_D + lane * 4), b = *(const float4*)(O + r * FA_D + lane * 4);
+    const int bh = (int)(r / p.T);
+    const long long t = r - (long long)bh * p.T;
+    const float4 a = *(const float4*)(fa_row(dO, p, bh, t) + lane * 4), b = *(const float4*)(fa_row(O, p, bh, t) + lane * 4);
     float s = a.x * b.x + a.y * b.y + a.z * b.z + a.w * b.w;
 #pragma unroll
     for (int off = 8; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
@@ -315,24 +481,35 @@ __global__ void __launch_bounds__(256) k_fa_delta(const __grid_constant__ FaPara
 }
 
 // P and dS of one (query block, key block) pair from the S / dP accumulators: thread (row r,
-// column half h) handles 64 keys; writes bf16 P and dS rows into the two [128][128] tiles
-template <bool WANT_P>
-__device__ __forceinline__ void fa_pds(uint32_t tS, uint32_t tdP, uint32_t lane, int r, int h, bool diag, float lse2,
-                                       float dl, float sc2, float scale, unsigned char* sP, unsigned char* sdS) {
-  float s[32], d[32];
-#pragma unroll 1
-  for (int c = h * 64; c < h * 64 + 64; c += 32) {
-    fa_ld32(tS + lane + c, s);
-    fa_ld32(tdP + lane + c, d);
+// column half h) handles 64 keys -- the four 32-column TMEM loads (S, dP) issued together, one
+// wait -- and writes bf16 P and dS rows into the two [128][128] tiles
+template <bool WANT_P, bool DIAG>
+__device__ __forceinline__ void fa_pds(uint32_t tS, uint32_t tdP, int r, int h, float lse2, float dl, float sc2,
+                                       float scale, unsigned char* sP, unsigned char* sdS) {
+  uint32_t s0[32], s1[32], d0[32], d1[32];
+  const int c0 = h * 64;
+  fa_ld32_issue(tS + c0, s0);
+  fa_ld32_issue(tdP + c0, d0);
+  fa_ld32_issue(tS + c0 + 32, s1);
+  fa_ld32_issue(tdP + c0 + 32, d1);
+  fa_ld_wait();
+  fa_ld_dep(s0);
+  fa_ld_dep(d0);
+  fa_ld_dep(s1);
+  fa_ld_dep(d1);
+  auto half = [&](uint32_t (&sr)[32], uint32_t (&dr)[32], int c) {
+    float pv[32], dv[32];
 #pragma unroll
     for (int i = 0; i < 32; ++i) {
-      const float pr = (!diag || c + i <= r) ? exp2f(s[i] * sc2 - lse2) : 0.f;
-      s[i] = pr;
-      d[i] = scale * pr * (d[i] - dl);
+      const float pr = (!DIAG || c + i <= r) ? fa_ex2(fmaf(__uint_as_float(sr[i]), sc2, -lse2)) : 0.f;
+      pv[i] = pr;
+      dv[i] = (scale * pr) * (__uint_as_float(dr[i]) - dl);
     }
-    if (WANT_P) fa_store_row32(sP, r, c, s);
-    fa_store_row32(sdS, r, c, d);
-  }
+    if (WANT_P) fa_store_row32(sP, r, c, pv);
+    fa_store_row32(sdS, r, c, dv);
+  };
+  half(s0, d0, c0);
+  half(s1, d1, c0 + 32);
 }
 
 // ============================================================== backward: dK, dV per key block
@@ -349,14 +526,15 @@ __global__ void __launch_bounds__(384, 1) k_fa_bwd_kv(const __grid_constant__ Fa
   unsigned char* sdO = sm + 4 * FA_TILE;         // [2]
   unsigned char* sP = sm + 6 * FA_TILE;          // [128 q][128 keys] (two sub-tiles)
   unsigned char* sdS = sm + 8 * FA_TILE;         // same
-  uint64_t* bar = (uint64_t*)(sm + 10 * FA_TILE);
-  uint64_t *qd_full = bar, *qd_empty = bar + 2, *kv_full = bar + 4, *s_done = bar + 5, *o_done = bar + 6;
+  unsigned char* stg = sm + 10 * FA_TILE;        // fp32 staging: Q | dO (first K | V)
+  uint64_t* bar = (uint64_t*)(sm + 14 * FA_TILE);
+  uint64_t *qd_full = bar, *qd_empty = bar + 2, *kv_full = bar + 4, *s_done = bar + 5, *o_done = bar + 6,
+           *stg_full = bar + 7;
   uint32_t* tslot = (uint32_t*)(bar + 8);
   const int tid = threadIdx.x, warp = tid >> 5;
   const int nb = p.T / FA_BLK;
   const int kb = (int)(blockIdx.x / p.BH);       // key block (low = most query blocks: first)
   const int bh = (int)(blockIdx.x % p.BH);
-  const long long hoff = (long long)bh * p.T * FA_D;
   float* dK = pick_out<float>(p.out2, res<float>(p.pa), res<float>(p.pb));
   float* dV = pick_out<float>(p.out3, res<float>(p.pa), res<float>(p.pb));
   publish_early(p.out2, dK);
@@ -370,6 +548,7 @@ __global__ void __launch_bounds__(384, 1) k_fa_bwd_kv(const __grid_constant__ Fa
     mbar_init(kv_full, 128);
     mbar_init(s_done, 1);
     mbar_init(o_done, 1);
+    mbar_init(stg_full, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) fa_tmem_alloc(tslot, 512);
@@ -379,18 +558,26 @@ __global__ void __launch_bounds__(384, 1) k_fa_bwd_kv(const __grid_constant__ Fa
   const uint32_t tmem = *tslot;
   const uint32_t tS = tmem, tdP = tmem + 128, tdV = tmem + 256, tdK = tmem + 320;
   if (tid >= 256) {                                  // ===== loader warpgroup
-    const float* Q = res<float>(p.q) + hoff;
-    const float* dO = res<float>(p.dout) + hoff;
-    fa_load<128>(sK, res<float>(p.k) + hoff, kb * FA_BLK);
-    fa_load<128>(sV, res<float>(p.v) + hoff, kb * FA_BLK);
+    const float* Q = res<float>(p.q);
+    const float* dO = res<float>(p.dout);
+    const int lt = tid & 127;
+    fa_stage_pair(stg, p, res<float>(p.k), res<float>(p.v), bh, kb * FA_BLK, kb * FA_BLK, stg_full, lt);
+    mbar_wait(stg_full, 0);
+    fa_convert(sK, stg, lt);
+    fa_convert(sV, stg + FA_STG, lt);
+    fa_bar(4, 128);
+    fa_stage_pair(stg, p, Q, dO, bh, kb * FA_BLK, kb * FA_BLK, stg_full, lt);
     fa_publish(kv_full);
     int it = 0;
     for (int qb = kb; qb < nb; ++qb, ++it) {
       const int b = it & 1;
+      mbar_wait(stg_full, (uint32_t)((it + 1) & 1));
       if (it >= 2) mbar_wait(&qd_empty[b], (uint32_t)(((it - 2) >> 1) & 1));
-      fa_load<128>(sQ + b * FA_TILE, Q, qb * FA_BLK);
-      fa_load<128>(sdO + b * FA_TILE, dO, qb * FA_BLK);
+      fa_convert(sQ + b * FA_TILE, stg, lt);
+      fa_convert(sdO + b * FA_TILE, stg + FA_STG, lt);
       fa_publish(&qd_full[b]);
+      fa_bar(4, 128);
+      if (qb + 1 < nb) fa_stage_pair(stg, p, Q, dO, bh, (qb + 1) * FA_BLK, (qb + 1) * FA_BLK, stg_full, lt);
     }
   } else {                                           // ===== compute warpgroups + MMA issuer
     const int r = tid & 127, h = tid >> 7;
@@ -415,7 +602,8 @@ __global__ void __launch_bounds__(384, 1) k_fa_bwd_kv(const __grid_constant__ Fa
       // thread): sP / sdS are free to overwrite
       mbar_wait(s_done, (uint32_t)(it & 1));
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      fa_pds<true>(tS, tdP, lane, r, h, qb == kb, lse2, dl, sc2, p.scale, sP, sdS);
+      if (qb == kb) fa_pds<true, true>(tS + lane, tdP + lane, r, h, lse2, dl, sc2, p.scale, sP, sdS);
+      else fa_pds<true, false>(tS + lane, tdP + lane, r, h, lse2, dl, sc2, p.scale, sP, sdS);
       fa_proxy_fence();
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       fa_bar(1, 256);
@@ -454,7 +642,7 @@ __global__ void __launch_bounds__(384, 1) k_fa_bwd_kv(const __grid_constant__ Fa
     fa_bar(1, 256);
     for (int u = tid; u < 2 * FA_BLK * 16; u += 256) {
       const int w = u / (FA_BLK * 16), rr = (u >> 4) & 127, c4 = u & 15;
-      float* dst = (w ? dK : dV) + hoff + (long long)(kb * FA_BLK + rr) * FA_D + c4 * 4;
+      float* dst = fa_row(w ? dK : dV, p, bh, kb * FA_BLK + rr) + c4 * 4;
       *(float4*)dst = *(const float4*)((float*)sQ + w * (FA_BLK * 68) + rr * 68 + c4 * 4);
     }
   }
@@ -477,14 +665,15 @@ __global__ void __launch_bounds__(384, 1) k_fa_bwd_q(const __grid_constant__ FaP
   unsigned char* sK = sm + 2 * FA_TILE;          // [2]
   unsigned char* sV = sm + 4 * FA_TILE;          // [2]
   unsigned char* sdS = sm + 6 * FA_TILE;         // [128 q][128 keys]
-  uint64_t* bar = (uint64_t*)(sm + 8 * FA_TILE);
-  uint64_t *kv_full = bar, *kv_empty = bar + 2, *q_full = bar + 4, *s_done = bar + 5, *o_done = bar + 6;
+  unsigned char* stg = sm + 8 * FA_TILE;         // fp32 staging: K | V (first Q | dO)
+  uint64_t* bar = (uint64_t*)(sm + 12 * FA_TILE);
+  uint64_t *kv_full = bar, *kv_empty = bar + 2, *q_full = bar + 4, *s_done = bar + 5, *o_done = bar + 6,
+           *stg_full = bar + 7;
   uint32_t* tslot = (uint32_t*)(bar + 8);
   const int tid = threadIdx.x, warp = tid >> 5;
   const int nb = p.T / FA_BLK;
   const int qb = nb - 1 - (int)(blockIdx.x / p.BH);
   const int bh = (int)(blockIdx.x % p.BH);
-  const long long hoff = (long long)bh * p.T * FA_D;
   float* dQ = pick_out<float>(p.out, res<float>(p.pa), res<float>(p.pb));
   publish_early(p.out, dQ);
   count_op(p.ds);
@@ -496,6 +685,7 @@ __global__ void __launch_bounds__(384, 1) k_fa_bwd_q(const __grid_constant__ FaP
     mbar_init(q_full, 128);
     mbar_init(s_done, 1);
     mbar_init(o_done, 1);
+    mbar_init(stg_full, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) fa_tmem_alloc(tslot, 512);
@@ -505,17 +695,25 @@ __global__ void __launch_bounds__(384, 1) k_fa_bwd_q(const __grid_constant__ FaP
   const uint32_t tmem = *tslot;
   const uint32_t tS = tmem, tdP = tmem + 128, tdQ = tmem + 256;
   if (tid >= 256) {                                  // ===== loader warpgroup
-    const float* K = res<float>(p.k) + hoff;
-    const float* V = res<float>(p.v) + hoff;
-    fa_load<128>(sQ, res<float>(p.q) + hoff, qb * FA_BLK);
-    fa_load<128>(sdO, res<float>(p.dout) + hoff, qb * FA_BLK);
+    const float* K = res<float>(p.k);
+    const float* V = res<float>(p.v);
+    const int lt = tid & 127;
+    fa_stage_pair(stg, p, res<float>(p.q), res<float>(p.dout), bh, qb * FA_BLK, qb * FA_BLK, stg_full, lt);
+    mbar_wait(stg_full, 0);
+    fa_convert(sQ, stg, lt);
+    fa_convert(sdO, stg + FA_STG, lt);
+    fa_bar(4, 128);
+    fa_stage_pair(stg, p, K, V, bh, 0, 0, stg_full, lt);
     fa_publish(q_full);
     for (int kb = 0; kb <= qb; ++kb) {
       const int b = kb & 1;
+      mbar_wait(stg_full, (uint32_t)((kb + 1) & 1));
       if (kb >= 2) mbar_wait(&kv_empty[b], (uint32_t)(((kb - 2) >> 1) & 1));
-      fa_load<128>(sK + b * FA_TILE, K, kb * FA_BLK);
-      fa_load<128>(sV + b * FA_TILE, V, kb * FA_BLK);
+      fa_convert(sK + b * FA_TILE, stg, lt);
+      fa_convert(sV + b * FA_TILE, stg + FA_STG, lt);
       fa_publish(&kv_full[b]);
+      fa_bar(4, 128);
+      if (kb + 1 <= qb) fa_stage_pair(stg, p, K, V, bh, (kb + 1) * FA_BLK, (kb + 1) * FA_BLK, stg_full, lt);
     }
   } else {                                           // ===== compute warpgroups + MMA issuer
     const int r = tid & 127, h = tid >> 7;
@@ -537,7 +735,8 @@ __global__ void __launch_bounds__(384, 1) k_fa_bwd_q(const __grid_constant__ FaP
       }
       mbar_wait(s_done, (uint32_t)(kb & 1));        // (also retires the previous dQ MMAs: sdS free)
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      fa_pds<false>(tS, tdP, lane, r, h, kb == qb, lse2, dl, sc2, p.scale, nullptr, sdS);
+      if (kb == qb) fa_pds<false, true>(tS + lane, tdP + lane, r, h, lse2, dl, sc2, p.scale, nullptr, sdS);
+      else fa_pds<false, false>(tS + lane, tdP + lane, r, h, lse2, dl, sc2, p.scale, nullptr, sdS);
       fa_proxy_fence();
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       fa_bar(1, 256);
@@ -569,7 +768,7 @@ __global__ void __launch_bounds__(384, 1) k_fa_bwd_q(const __grid_constant__ FaP
     fa_bar(1, 256);
     for (int u = tid; u < FA_BLK * 16; u += 256) {
       const int rr = u >> 4, c4 = u & 15;
-      *(float4*)(dQ + hoff + (long long)(qb * FA_BLK + rr) * FA_D + c4 * 4) = *(const float4*)(stage + rr * 68 + c4 * 4);
+      *(float4*)(fa_row(dQ, p, bh, qb * FA_BLK + rr) + c4 * 4) = *(const float4*)(stage + rr * 68 + c4 * 4);
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -578,8 +777,11 @@ __global__ void __launch_bounds__(384, 1) k_fa_bwd_q(const __grid_constant__ FaP
   publish_late(p.out, dQ);
 }
 
-constexpr size_t kFaFwdSmem = 7 * FA_TILE + 1024 + 128;
-constexpr size_t kFaKvSmem = 10 * FA_TILE + 1024 + 128;
-constexpr size_t kFaQSmem = 8 * FA_TILE + 1024 + 128;
+// forward grid: one CTA per (head, pair of query tiles)
+inline unsigned fa_fwd_blocks(const FaParams& p) { return (unsigned)(p.BH * ((p.T / FA_BLK + 1) / 2)); }
+
+constexpr size_t kFaFwdSmem = 14 * FA_TILE + 1024 + 128;
+constexpr size_t kFaKvSmem = 14 * FA_TILE + 1024 + 128;
+constexpr size_t kFaQSmem = 12 * FA_TILE + 1024 + 128;
 
 }  // namespace coex

@@ -1788,6 +1788,16 @@ int launch_now(coex_ctx* c, Launch& L) {
   return COEX_OK;
 }
 
+int fa_set_attrs() {
+  static bool done = false;
+  if (done) return COEX_OK;
+  CK(cudaFuncSetAttribute((void*)k_fa_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFaFwdSmem));
+  CK(cudaFuncSetAttribute((void*)k_fa_bwd_kv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFaKvSmem));
+  CK(cudaFuncSetAttribute((void*)k_fa_bwd_q, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFaQSmem));
+  done = true;
+  return COEX_OK;
+}
+
 TRec* get_t(coex_ctx* c, int64_t id) {
   auto it = c->tensors.find(id);
   return it == c->tensors.end() ? nullptr : &it->second;
@@ -2265,6 +2275,97 @@ int coex_exec_op_profile(coex_ctx* c, int kind, const coex_attrs* attrs, int nin
   return rc;
 }
 
+// Fused causal attention outside a graph (kernel-level parity and ncu captures of
+// attn_tc.cuh; the step graph reaches the same kernels through T_ATTN).  Forward: in = {q, k,
+// v} fp32 [BH][T][64] -> out = {O [BH][T][64], lse [BH][T]}.  Backward: in = {q, k, v, O, dO,
+// lse} -> out = {dQ, dK, dV}.  reps > 0: the kernels are re-launched reps times between CUDA
+// events after the first run and *avg_ms receives the per-repetition time.
+int coex_flash_attn(coex_ctx* c, int backward, const int64_t* in_ids, int BH, int T, double scale, int reps,
+                    int64_t* out_ids, double* avg_ms) {
+  if (c->active) return fail(COEX_IN_FLIGHT_PASS, "eager op while a pass is in flight");
+  if (c->esize != 4) return fail(COEX_BAD_ATTRS, "flash attention: fp32 / bf16 precision modes only");
+  if (BH < 1 || T < FA_BLK || T % FA_BLK) return fail(COEX_BAD_ATTRS, "flash attention: T a multiple of 128");
+  const int nin = backward ? 6 : 3;
+  const float* ptr[6];
+  for (int i = 0; i < nin; ++i) {
+    TRec* t = get_t(c, in_ids[i]);
+    const int64_t want = (int64_t)BH * T * (i == 5 ? 1 : FA_D);
+    if (!t || t->numel != want) return fail(COEX_SHAPE_MISMATCH, "flash attention: operand size");
+    ptr[i] = (const float*)t->buf->ptr;
+  }
+  if (int e = fa_set_attrs()) return e;
+  auto in_of = [](const void* p) { In x{}; x.direct = p; return x; };
+  auto out_of = [](void* p) { Out o{}; o.buf[0] = p; return o; };
+  const int nout = backward ? 3 : 2;
+  TRec o[3];
+  for (int i = 0; i < nout; ++i) {
+    const bool lse = !backward && i == 1;
+    o[i].ndim = lse ? 2 : 3;
+    o[i].shape[0] = BH;
+    o[i].shape[1] = T;
+    o[i].shape[2] = FA_D;
+    o[i].numel = (int64_t)BH * T * (lse ? 1 : FA_D);
+    int rc = alloc_buf(c, o[i].numel * 4, &o[i].buf);
+    if (rc) return rc;
+  }
+  FaParams fp{};
+  fp.ds = c->d_state;
+  fp.BH = BH;
+  fp.T = T;
+  fp.H = 1;
+  fp.rs = FA_D;
+  fp.scale = (float)scale;
+  fp.q = in_of(ptr[0]);
+  fp.k = in_of(ptr[1]);
+  fp.v = in_of(ptr[2]);
+  Buf* delta = nullptr;
+  const unsigned blocks = (unsigned)(BH * (T / FA_BLK));
+  Launch L[3];
+  int nL = 0;
+  if (!backward) {
+    fp.lse = (float*)o[1].buf->ptr;
+    fp.out = out_of(o[0].buf->ptr);
+    L[nL].set((void*)k_fa_fwd, dim3(fa_fwd_blocks(fp)), dim3(416), fp);
+    L[nL++].smem = kFaFwdSmem;
+  } else {
+    int rc = alloc_buf(c, (int64_t)BH * T * 4, &delta);
+    if (rc) return rc;
+    fp.o = in_of(ptr[3]);
+    fp.dout = in_of(ptr[4]);
+    fp.lse = (float*)ptr[5];
+    fp.delta = (float*)delta->ptr;
+    fp.out = out_of(o[0].buf->ptr);
+    fp.out2 = out_of(o[1].buf->ptr);
+    fp.out3 = out_of(o[2].buf->ptr);
+    const int64_t db = ((int64_t)BH * T * 16 + 255) / 256;
+    L[nL++].set((void*)k_fa_delta, dim3((unsigned)(db < kNumSMs * 8 ? db : kNumSMs * 8)), dim3(256), fp);
+    L[nL].set((void*)k_fa_bwd_kv, dim3(blocks), dim3(384), fp);
+    L[nL++].smem = kFaKvSmem;
+    L[nL].set((void*)k_fa_bwd_q, dim3(blocks), dim3(384), fp);
+    L[nL++].smem = kFaQSmem;
+  }
+  int rc = COEX_OK;
+  for (int i = 0; rc == COEX_OK && i < nL; ++i) rc = launch_now(c, L[i]);
+  if (rc == COEX_OK && reps > 0) {
+    rc = coex_ctx_event_record(c, 62);
+    for (int r = 0; rc == COEX_OK && r < reps; ++r)
+      for (int i = 0; rc == COEX_OK && i < nL; ++i) rc = launch_now(c, L[i]);
+    if (rc == COEX_OK) rc = coex_ctx_event_record(c, 63);
+    double ms = 0;
+    if (rc == COEX_OK) rc = coex_ctx_event_elapsed(c, 62, 63, &ms);
+    if (avg_ms) *avg_ms = ms / reps;
+  }
+  if (delta) release(c, delta);
+  for (int i = 0; i < nout; ++i) {
+    if (rc) {
+      release(c, o[i].buf);
+      continue;
+    }
+    out_ids[i] = new_handle(c, o[i]);
+  }
+  return rc;
+}
+
 // =============================================================== variables
 int coex_var_define(coex_ctx* c, const char* name, int64_t tid, int* var_index) {
   TRec* t = get_t(c, tid);
@@ -2711,6 +2812,8 @@ struct Builder {
         fp.ds = c->d_state;
         fp.BH = (int)next();
         fp.T = (int)next();
+        fp.H = 1;
+        fp.rs = FA_D;
         {
           int64_t sb = next();
           double sc;
@@ -2727,19 +2830,13 @@ struct Builder {
         fp.pa = fp.q;
         fp.pb = fp.k;
         if (is_f64(c) || fp.T % FA_BLK != 0) throw std::runtime_error("flash attention: bf16 mode, T % 128 only");
-        static bool attr_set = false;
-        if (!attr_set) {
-          CK(cudaFuncSetAttribute((void*)k_fa_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFaFwdSmem));
-          CK(cudaFuncSetAttribute((void*)k_fa_bwd_kv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFaKvSmem));
-          CK(cudaFuncSetAttribute((void*)k_fa_bwd_q, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFaQSmem));
-          attr_set = true;
-        }
+        if (int e = fa_set_attrs()) return e;
         const unsigned blocks = (unsigned)(fp.BH * (fp.T / FA_BLK));
         p->n_compute++;
         if (mode == 0) {
           read_out(fp.out);
           Launch L;
-          L.set((void*)k_fa_fwd, dim3(blocks), dim3(256), fp);
+          L.set((void*)k_fa_fwd, dim3(fa_fwd_blocks(fp)), dim3(416), fp);
           L.smem = kFaFwdSmem;
           return add_kernel(g, prev, L);
         }

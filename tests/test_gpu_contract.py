@@ -20,7 +20,8 @@
   one (measured: tests report kappa per tensor).  There the bound is 4 x max(kappa of the
   tensor, median kappa of the case) -- the B200 result must be as close to the f64 answer
   as one rounding of the weights moves the f64 answer itself (a single perturbation flips
-  masks stochastically, so a tensor it left calm falls back to the case's median).  Printed losses always meet the literal bar.  The per-op
+  masks stochastically: kappa is the largest over KAPPA_DRAWS independent perturbations, and a
+  tensor they all left calm falls back to the case's median).  Printed losses always meet the literal bar.  The per-op
   bar at the same full shapes is literal for every op (tests/test_gpu_opsweep.py).
 
 The oracle runs in f64 with numpy's BLAS product for MATMUL (oracle.kernels.FAST_MATMUL,
@@ -51,6 +52,9 @@ pytestmark = pytest.mark.gpu
 
 TOL = {"fp32": 1e-5, "bf16": 2e-2}
 CALIBRATED_FACTOR = 4.0
+# independent one-rounding perturbations per sensitivity estimate (per tensor: the largest):
+# a mask flip is a rare event per draw, one draw under-samples it
+KAPPA_DRAWS = 3
 
 
 def _report(rec):
@@ -136,15 +140,16 @@ def _oracle(case):
 class _Perturbed(SyntheticDataset):
     """The synthetic dataset with every ``*_init`` weight tensor multiplied by (1 + u*N(0,1))."""
 
-    def __init__(self, seed, u):
+    def __init__(self, seed, u, draw=0):
         super().__init__(seed, lazy=False)
         self.u = u
+        self.draw = draw
 
     def next(self, name, shape, step):
         t = super().next(name, shape, step)
         if not name.endswith("_init"):
             return t
-        r = np.random.default_rng(zlib.crc32(name.encode()))
+        r = np.random.default_rng((zlib.crc32(name.encode()), self.draw))
         return Tensor(tuple(shape), t.data * (1.0 + self.u * r.standard_normal(t.data.shape)))
 
 
@@ -158,14 +163,18 @@ def _kappa(case, prec):
     key = (case, prec)
     if key not in _KAPPA:
         src, grads, ref = _oracle(case)[:3]
+        kap = {}
         OK.FAST_MATMUL = True
         try:
-            o = coexec.Orchestrator(lang.parse(src), _Perturbed(0, UNIT[prec]), coexec.Mode.coexec,
-                                    coexec.RunConfig(), CpuBackend())
-            pert, _ = o.run()
+            for draw in range(KAPPA_DRAWS):
+                o = coexec.Orchestrator(lang.parse(src), _Perturbed(0, UNIT[prec], draw), coexec.Mode.coexec,
+                                        coexec.RunConfig(), CpuBackend())
+                pert, _ = o.run()
+                for k, e in compare(ref, pert, 0.0, grads, ZERO.get(case))[0].items():
+                    kap[k] = max(kap.get(k, 0.0), e)
         finally:
             OK.FAST_MATMUL = False
-        _KAPPA[key] = compare(ref, pert, 0.0, grads, ZERO.get(case))[0]
+        _KAPPA[key] = kap
     return _KAPPA[key]
 
 

@@ -5,6 +5,7 @@ forward / backward as tcgen05 flash-attention kernels.  One co-executed grad-pro
 tensor within the bf16 bar (2e-2), like the unfused bf16 path (COEX_FLASH=0) does; TraceGraph,
 decisions and counters bit-exact."""
 
+import numpy as np
 import pytest
 
 from contract import compare, grad_probe
@@ -49,3 +50,46 @@ def test_flash_attention_gradients(b200_factory, oracle_run, monkeypatch, flash)
     errs, bad = compare(ref, got, 2e-2, grads, {f"ck_{l}": f"cq_{l}" for l in range(CFG["layers"])})
     print("flash" if flash == "1" else "unfused", sorted(errs.items(), key=lambda kv: -kv[1])[:4])
     assert not bad, bad
+
+
+# ---------------------------------------------------------------- kernel level (coex_flash_attn)
+def _attn_ref(q, k, v, do, scale):
+    """f64 causal attention forward / backward (the unfused composition bmm_nt ->
+    causal_softmax -> bmm of oracle/kernels.py and its hand-written backward)."""
+    T = q.shape[1]
+    s = np.einsum("bte,bse->bts", q, k) * scale
+    s = np.where(np.tril(np.ones((T, T), bool)), s, -np.inf)
+    p = np.exp(s - s.max(-1, keepdims=True))
+    p /= p.sum(-1, keepdims=True)
+    o = np.einsum("bts,bse->bte", p, v)
+    dp = np.einsum("bte,bse->bts", do, v)
+    ds = p * (dp - (dp * p).sum(-1, keepdims=True)) * scale
+    return o, np.einsum("bts,bse->bte", ds, k), np.einsum("bts,bte->bse", ds, q), np.einsum("bts,bte->bse", p, do)
+
+
+def _rel(a, b):
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+@pytest.mark.parametrize("BH,T", [(3, 128), (4, 512), (2, 1024)])
+def test_flash_kernels_vs_f64(b200_factory, BH, T):
+    """Each k_fa_* kernel against f64 causal attention: bf16 operands, fp32 accumulation --
+    within the bf16 bar (2e-2 relative, norm-wise per output tensor)."""
+    from paper_2201_09210_b200.tensor import Tensor
+    r = np.random.default_rng(BH * T)
+    q, k, v, do = (r.standard_normal((BH, T, 64)) for _ in range(4))
+    scale = 0.125
+    o_ref, dq_ref, dk_ref, dv_ref = _attn_ref(q, k, v, do, scale)
+    be = b200_factory("bf16", fresh=True)
+    try:
+        dq_, dk_, dv_ = (be.put(Tensor(x.shape, x)) for x in (q, k, v))
+        o, lse = be.flash_attention([dq_, dk_, dv_], scale)
+        o_np = be.get(o).data.reshape(BH, T, 64)
+        dq, dk, dv = be.flash_attention([dq_, dk_, dv_, o, be.put(Tensor(do.shape, do)), lse], scale, backward=True)
+        got = [be.get(t).data.reshape(BH, T, 64) for t in (dq, dk, dv)]
+    finally:
+        be.close()
+    errs = {"O": _rel(o_np, o_ref), "dQ": _rel(got[0], dq_ref), "dK": _rel(got[1], dk_ref),
+            "dV": _rel(got[2], dv_ref)}
+    print(BH, T, errs)
+    assert all(e <= 2e-2 for e in errs.values()), errs

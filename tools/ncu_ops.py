@@ -30,6 +30,15 @@ OPS = {
     "gemm_8192": (OpKind.MATMUL, {}, [(8192, 8192), (8192, 8192)]),
     "ce_grad": (OpKind.CROSS_ENTROPY_GRAD, {}, [(8192, 50257), (8192,)]),
     "qkt": (OpKind.BMM_NT, {}, [(96, 1024, 64), (96, 1024, 64)]),
+    # C4 (GPT-2 small, batch 8 x 1024 tokens): the step's GEMM shapes
+    "c4_qkv": (OpKind.MATMUL, {}, [(8192, 768), (768, 768)]),
+    "c4_fc1": (OpKind.MATMUL, {}, [(8192, 768), (768, 3072)]),
+    "c4_fc2": (OpKind.MATMUL, {}, [(8192, 3072), (3072, 768)]),
+    "c4_head": (OpKind.MATMUL, {}, [(8192, 768), (768, 50257)]),
+    "c4_dhead": (OpKind.MATMUL, {}, [(8192, 50257), (50257, 768)]),
+    "c4_dw768": (OpKind.MATMUL, {}, [(768, 8192), (8192, 768)]),
+    "c4_dw3072": (OpKind.MATMUL, {}, [(768, 8192), (8192, 3072)]),
+    "c4_dwte": (OpKind.MATMUL, {}, [(50257, 8192), (8192, 768)]),
 }
 
 be = B200Backend(precision=os.environ.get("PREC", "bf16"))
@@ -39,5 +48,11 @@ for name in sys.argv[1:]:
     ins = [be.put(Tensor(s, r.uniform(-1, 1, s))) for s in shapes]
     for _ in range(3):
         be.exec_op(kind, attrs, ins)
-    print(name, be.profile_op(kind, attrs, ins, reps=5))
+    prof = be.profile_op(kind, attrs, ins, reps=5)
+    flops = 0
+    if kind in (OpKind.MATMUL,):
+        (m, kk), (_, n) = shapes
+        flops = 2 * m * n * kk
+    gemm_ms = sum(ms for nm, ms in prof if "gemm" in nm or "splitk" in nm)
+    print(name, prof, f"gemm {gemm_ms:.4f} ms" + (f" {flops / gemm_ms / 1e9:.1f} TFLOP/s" if flops else ""))
 be.sync()
