@@ -259,7 +259,7 @@ def tensor_gemm(peak_tflops, peak_kind, size: int = 8192):
 
 # the tcgen05 family in the device stamps: GEMMs (with their split-K reduces) and the fused
 # flash-attention kernels (the attention contractions of C4 run inside them)
-GEMM_KINDS = ("matmul", "split-K reduce", "attention fwd", "attention delta", "attention dK/dV", "attention dQ")
+GEMM_KINDS = ("matmul", "split-K reduce", "attention fwd", "attention dK/dV", "attention dQ")
 TC_LAUNCH_KINDS = ("matmul", "attention fwd", "attention dK/dV", "attention dQ")
 
 

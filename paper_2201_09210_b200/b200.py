@@ -253,7 +253,7 @@ class B200Backend:
                    18: "bn apply", 19: "split-K reduce", 20: "causal softmax", 21: "softmax grad",
                    22: "cross-entropy", 23: "bias add", 24: "layernorm", 25: "embedding", 26: "column sum",
                    27: "rel skew", 28: "pooling", 29: "axis op", 30: "cancel guard",
-                   31: "attention fwd", 32: "attention delta", 33: "attention dK/dV", 34: "attention dQ"}
+                   31: "attention fwd", 32: "attention prep", 33: "attention dK/dV", 34: "attention dQ"}
 
     def set_trace(self, capacity: int):
         """Enable device-side per-kernel stamps (0 disables)."""

@@ -246,6 +246,14 @@ __device__ __forceinline__ void conv_pix(const TcConv& g, long long pix, int& n,
   n = (int)(t / g.Hg);
 }
 
+// tcgen05.commit from one elected lane of a converged warp
+__device__ __forceinline__ void tc_commit_elect(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(bar))
+      : "memory");
+}
+
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
@@ -402,7 +410,10 @@ __global__ void __launch_bounds__(TC_THREADS, DUO ? 2 : 1) k_gemm_tc(const __gri
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {                                // ===== MMA issuer
+    {                                               // ===== MMA issuer: the whole warp runs the
+      // loop (descriptors stay warp-uniform, on the uniform datapath) and one elected lane
+      // issues each tcgen05.mma / commit -- a single-lane issuer pays ~82 cycles per MMA, more
+      // than the tensor pipe's own 64 cycles at BN = 128 (probes/mma_probe.cu)
       constexpr uint32_t idesc = idesc_bf16_f32(TC_BM, BN, A_MN, B_MN);
       long long kbg = 0;
       int li = 0;                                   // local item index
@@ -428,22 +439,20 @@ __global__ void __launch_bounds__(TC_THREADS, DUO ? 2 : 1) k_gemm_tc(const __gri
           for (int k = 0; k < TC_BK / 16; ++k) {
             const uint32_t acc = (kb > 0 || k > 0) ? 1u : 0u;
             asm volatile(
-                "{\n\t.reg .pred p;\n\t"
+                "{\n\t.reg .pred p, e;\n\t"
+                "elect.sync _|e, 0xffffffff;\n\t"
                 "setp.ne.b32 p, %4, 0;\n\t"
-                "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(acc_addr),
+                "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(acc_addr),
                 "l"(da + stepA * k), "l"(db + stepB * k), "r"(idesc), "r"(acc)
                 : "memory");
           }
-          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                           smem_u32(&empty[s]))
-                       : "memory");
+          tc_commit_elect(&empty[s]);
         }
         if (nk > 0)
-          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                           smem_u32(&tfull[a]))
-                       : "memory");
-        else
+          tc_commit_elect(&tfull[a]);
+        else if (lane == 0)
           mbar_arrive(&tfull[a]);                   // empty K slice: the epilogue writes zeros
+        __syncwarp();
       }
     }
   } else {                                          // ===== epilogue: warps 2..5

@@ -397,6 +397,7 @@ class Planner:
                     gone |= {g[k].node_id for k in ("S", "P", "dP", "DQ", "DK", "DV")}
                     g["lse"] = self.new_buf(g["BH"] * g["T"] * 4)
                     g["delta"] = self.new_buf(g["BH"] * g["T"] * 4)
+                    g["tiles"] = self.new_buf(4 * g["BH"] * g["T"] * FA_HEAD * 2)   # bf16 q | k | v | dO tiles
                     self.n_attn += 1
                 insts = [repl.get(y.node_id, y) if isinstance(y, ExecOp) else y for y in insts
                          if not (isinstance(y, ExecOp) and y.node_id in gone)]
@@ -675,7 +676,8 @@ class Planner:
         return out
 
     def _attn_word(self, a, in_cell, out_words, pubs, n_compute, flops, shapes) -> list:
-        """[T_ATTN, mode, BH, T, scale bits, lse buf, delta buf, cells q k v o dO, outputs]"""
+        """[T_ATTN, mode, BH, T, H, row pitch, scale bits, lse buf, delta buf, tiles buf, cells q k v o dO,
+        outputs]"""
         g = a.g
         o_cell = pubs[g["O"].node_id][0]
         if a.mode == 0:
@@ -690,7 +692,8 @@ class Planner:
             x = g[m]
             flops[0] += flops_of(x.kind, [tuple(self._in_shape(b, shapes)) for b in x.inputs], x.attrs)
         n_compute[0] += 1
-        word = [T_ATTN, a.mode, g["BH"], g["T"], _f64_bits(g["scale"]), g["lse"], g["delta"]] + cells
+        word = [T_ATTN, a.mode, g["BH"], g["T"], g.get("H", 1), g.get("rs", FA_HEAD), _f64_bits(g["scale"]), g["lse"],
+                g["delta"], g["tiles"]] + cells
         for nid in outs:
             word += out_words(nid, _conflicts(cells, pubs[nid]))
             self._invalidate(pubs[nid])
