@@ -363,6 +363,8 @@ class Planner:
         self._skip_f32 = {}                      # gradient node -> (plan word, attr index): 1 = no fp32 reader
         self._skip_cell = {}                     # its output cell -> gradient node
         self.n_attn = 0                          # flash-attention groups (forward + backward)
+        self.n_head_fold = 0                     # ... of which read / write the merged head layout
+        self._emitted = set()                    # node ids emitted as their own plan items
         self.chain_lates = 0
         self._chain_meta = {}
 
@@ -395,6 +397,8 @@ class Planner:
                     repl[g["O"].node_id] = _Attn(0, g)
                     repl[g["G"].node_id] = _Attn(1, g)
                     gone |= {g[k].node_id for k in ("S", "P", "dP", "DQ", "DK", "DV")}
+                    gone |= g.get("fold_gone", set())
+                    self.n_head_fold += 1 if "fold_gone" in g else 0
                     g["lse"] = self.new_buf(g["BH"] * g["T"] * 4)
                     g["delta"] = self.new_buf(g["BH"] * g["T"] * 4)
                     g["tiles"] = self.new_buf(4 * g["BH"] * g["T"] * FA_HEAD * 2)   # bf16 q | k | v | dO tiles
@@ -502,6 +506,7 @@ class Planner:
 
     def _exec(self, x, shapes, in_cell, out_words, ptr_item, pubs, multi, folded, n_compute, flops) -> list:
         nid = x.node_id
+        self._emitted.add(nid)
         k = x.kind
         if k is OpKind.FILL:
             if any(nid in s for s in multi):
@@ -672,21 +677,109 @@ class Planner:
                     and min(pos[DQ.node_id], pos[DK.node_id], pos[DV.node_id]) > pos[G.node_id]):
                 continue
             g = dict(nodes, q=q, k=k, v=v, do=do, BH=shp[0], T=shp[1], scale=float(P.attrs["value"]))
+            members = {n.node_id for n in nodes.values()}
+            fold = self._head_fold(g, ex, members, banned, shapes)
+            if fold is not None:
+                g.update(fold)
             out.append(g)
         return out
+
+    def _head_fold(self, g, ex, members, banned, shapes):
+        """Head split / merge folded into the attention kernels (C4's ``heads_of`` / ``merge``):
+        every operand q, k, v, dO is reshape(transpose(reshape(src, [B, T, H, hd]), [0, 2, 1, 3]),
+        [B*H, T, hd]) of a merged [B*T, H*hd] tensor, and every output O, dQ, dK, dV is consumed
+        only by reshape(transpose(reshape(., [B, H, T, hd]), [0, 2, 1, 3])).  The kernels then
+        read the merged rows of src directly (row pitch H*hd, head offset h*hd) and write their
+        outputs straight into the merge transposes' buffers: the eight [B*T, H*hd] transposes of
+        the layer are never launched.  All or nothing (one operand layout per attention word).
+        Returns {"H", "rs", "src": {name: binding}, "dst": {name: transpose node}, "fold_gone"}
+        or None."""
+        if os.environ.get("COEX_HEAD_FOLD", "1") == "0":
+            return None
+        BH, T = g["BH"], g["T"]
+        cons = self.consumers
+
+        def only(nid):
+            return [c.node_id for c in cons.get(nid, [])]
+
+        def node_of(b):
+            if b.fed or len(b.cands) != 1:
+                return None
+            return ex.get(b.cands[0])
+
+        def split(b):                                # operand binding -> (src binding, H, nodes)
+            r2 = node_of(b)
+            if r2 is None or r2.kind is not OpKind.RESHAPE or not set(only(r2.node_id)) <= members:
+                return None
+            x = node_of(r2.inputs[0])
+            if x is None or x.kind is not OpKind.TRANSPOSE or tuple(x.attrs["perm"]) != (0, 2, 1, 3) or \
+                    only(x.node_id) != [r2.node_id]:
+                return None
+            r1 = node_of(x.inputs[0])
+            if r1 is None or r1.kind is not OpKind.RESHAPE or only(r1.node_id) != [x.node_id]:
+                return None
+            b_, t_, h_, d_ = shapes[r1.node_id]
+            if t_ != T or d_ != FA_HEAD or b_ * h_ != BH:
+                return None
+            src = r1.inputs[0]
+            if src.fed or len(src.cands) != 1 or shape_size(self._in_shape(src, shapes)) != BH * T * FA_HEAD:
+                return None
+            return src, h_, {r2.node_id, x.node_id, r1.node_id}
+
+        def merge(o):                                # output node -> (merge transpose, H, nodes)
+            r3 = only(o.node_id)
+            if len(r3) != 1 or r3[0] not in ex or ex[r3[0]].kind is not OpKind.RESHAPE:
+                return None
+            r3 = ex[r3[0]]
+            x = only(r3.node_id)
+            if len(x) != 1 or x[0] not in ex:
+                return None
+            x = ex[x[0]]
+            if x.kind is not OpKind.TRANSPOSE or tuple(x.attrs["perm"]) != (0, 2, 1, 3) or len(shapes[r3.node_id]) != 4:
+                return None
+            b_, h_, t_, d_ = shapes[r3.node_id]
+            if t_ != T or d_ != FA_HEAD or b_ * h_ != BH:
+                return None
+            if self._node_buf.get(x.node_id, (-1, -1, True))[2] or x.node_id not in self._node_buf:
+                return None
+            return x, h_, {r3.node_id}
+
+        src, dst, gone, hs = {}, {}, set(), set()
+        for name in ("q", "k", "v", "do"):
+            r = split(g[name])
+            if r is None:
+                return None
+            src[name], h, nodes = r
+            hs.add(h)
+            gone |= nodes
+        for name in ("O", "DQ", "DK", "DV"):
+            r = merge(g[name])
+            if r is None:
+                return None
+            dst[name], h, nodes = r
+            hs.add(h)
+            gone |= nodes | {dst[name].node_id}
+        if len(hs) != 1 or gone & banned:
+            return None
+        H = hs.pop()
+        return {"H": H, "rs": H * FA_HEAD, "src": src, "dst": dst, "fold_gone": gone}
 
     def _attn_word(self, a, in_cell, out_words, pubs, n_compute, flops, shapes) -> list:
         """[T_ATTN, mode, BH, T, H, row pitch, scale bits, lse buf, delta buf, tiles buf, cells q k v o dO,
         outputs]"""
         g = a.g
-        o_cell = pubs[g["O"].node_id][0]
+        src = g.get("src", {})
+        dst = {k: v.node_id for k, v in g.get("dst", {}).items()}
+        opnd = {k: in_cell(src.get(k, g[k])) for k in ("q", "k", "v", "do")}
+        out_node = {k: dst.get(k, g[k].node_id) for k in ("O", "DQ", "DK", "DV")}
+        o_cell = pubs[out_node["O"]][0]
         if a.mode == 0:
-            cells = [in_cell(g["q"]), in_cell(g["k"]), in_cell(g["v"]), -1, -1]
-            outs = [g["O"].node_id]
+            cells = [opnd["q"], opnd["k"], opnd["v"], -1, -1]
+            outs = [out_node["O"]]
             members = ("S", "O")
         else:
-            cells = [in_cell(g["q"]), in_cell(g["k"]), in_cell(g["v"]), o_cell, in_cell(g["do"])]
-            outs = [g["DQ"].node_id, g["DK"].node_id, g["DV"].node_id]
+            cells = [opnd["q"], opnd["k"], opnd["v"], o_cell, opnd["do"]]
+            outs = [out_node["DQ"], out_node["DK"], out_node["DV"]]
             members = ("dP", "DQ", "DK", "DV")
         for m in members:
             x = g[m]

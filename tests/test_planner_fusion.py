@@ -98,3 +98,10 @@ def test_flash_attention_groups():
     assert pl.n_attn == 2
     w = plan.words
     assert sum(1 for i in range(1, len(w)) if w[i] == T_ATTN and w[i + 1] in (0, 1) and w[i + 2] == 4) >= 4
+    # the head split / merge transposes fold into the attention words: merged rows of the
+    # [B*T, H*hd] projections (H = 2, row pitch 128); no 4-D transpose is launched
+    assert pl.n_head_fold == 2
+    assert sum(1 for i in range(1, len(w) - 5) if w[i] == T_ATTN and w[i + 1] in (0, 1) and w[i + 2] == 4
+               and w[i + 3] == 128 and w[i + 4] == 2 and w[i + 5] == 128) >= 4
+    emitted = {y.node_id for y in pl.ops.values() if y.kind is OpKind.TRANSPOSE and len(y.attrs["perm"]) == 4}
+    assert emitted and all(n not in pl._emitted for n in emitted)
