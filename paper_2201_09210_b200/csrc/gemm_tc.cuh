@@ -571,7 +571,7 @@ __global__ void __launch_bounds__(256) k_splitk_reduce(SplitReduceParams p) {
   stamp(p.ds, SK_SPLITK);
   float* o = pick_out<float>(p.out, res<float>(p.a), p.b.cell || p.b.direct ? res<float>(p.b) : nullptr);
   publish_early(p.out, o);
-  const long long n4 = p.n / 4;
+  const long long n4 = (p.n % 4) == 0 ? p.n / 4 : 0;   // slices start 16-byte aligned only when 4 | n
   const long long stride = (long long)gridDim.x * blockDim.x;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
     float4 acc = ((const float4*)p.ws)[i];

@@ -30,6 +30,7 @@
 #include "../../include/coex_b200.h"
 #include "kernels.cuh"
 #include "gemm_tc.cuh"
+#include "gemm_tf32.cuh"
 #include "ext_ops.cuh"
 #include "xformer_ops.cuh"
 #include "attn_tc.cuh"
@@ -181,6 +182,17 @@ struct coex_ctx {
 namespace {
 
 bool is_f64(const coex_ctx* c) { return c->prec == COEX_F64; }
+// COEX_TF32=0: fp32-mode MatMuls on the SIMT FFMA kernel instead of 3xTF32 tcgen05 (A/B only)
+bool tf32_on() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("COEX_TF32");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+bool tf32_path(const coex_ctx* c) { return c->prec == COEX_F32 && tf32_on(); }
+
 
 int alloc_buf(coex_ctx* c, size_t bytes, Buf** out) {
   Buf* b = new Buf();
@@ -870,6 +882,112 @@ TcPlan tc_plan(int64_t M, int64_t N, int64_t K, bool allow_split) {
 size_t matmul_split_ws(int64_t M, int64_t N, int64_t K) {
   const TcPlan t = tc_plan(M, N, K, true);
   return t.splits > 1 ? (size_t)t.splits * M * N * 4 : 0;
+}
+
+// 3xTF32 launch shape: BN 64 for narrow outputs, else 128; split-K when the tile grid covers
+// under half of the SMs and each slice keeps >= 8 K blocks of 32
+TcPlan tf32_plan(int64_t M, int64_t N, int64_t K, bool allow_split) {
+  TcPlan t;
+  t.bn = N <= 64 ? 64 : 128;
+  t.tiles = ((M + TC_BM - 1) / TC_BM) * ((N + t.bn - 1) / t.bn);
+  if (t.tiles < 1) t.tiles = 1;
+  const int64_t nk = (K + TF_BK - 1) / TF_BK;
+  t.splits = 1;
+  if (allow_split && t.tiles * 2 <= kNumSMs) {
+    int64_t sp = kNumSMs / t.tiles;
+    if (sp > nk / 8) sp = nk / 8;
+    if (sp > 16) sp = 16;
+    t.splits = sp > 1 ? (int)sp : 1;
+  }
+  return t;
+}
+size_t matmul_split_ws_c(const coex_ctx* c, int64_t M, int64_t N, int64_t K) {
+  if (!tf32_path(c)) return matmul_split_ws(M, N, K);
+  const TcPlan t = tf32_plan(M, N, K, true);
+  return t.splits > 1 ? (size_t)t.splits * M * N * 4 : 0;
+}
+
+// fp32 hi / lo planes [2][rows][ld]: 3-D map {ld, rows, 2}, box {32, box_rows, 1}, 128-byte swizzle
+int make_tmap_tf32(CUtensorMap* m, void* base, int64_t rows, int64_t ld, int box_rows) {
+  auto enc = tmap_encoder();
+  if (!enc) return fail(COEX_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[3] = {(cuuint64_t)ld, (cuuint64_t)(rows > 0 ? rows : 1), 2};
+  cuuint64_t strides[2] = {(cuuint64_t)ld * 4, (cuuint64_t)ld * 4 * (rows > 0 ? rows : 1)};
+  cuuint32_t box[3] = {(cuuint32_t)TF_BK, (cuuint32_t)box_rows, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, base, dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(COEX_CUDA_ERROR, "cuTensorMapEncodeTiled (tf32) failed: " + std::to_string((int)r));
+  return COEX_OK;
+}
+
+// fp32-mode MatMul: operand split (k_cvt_tf32, one launch for both operands) + k_gemm_tf32
+// (+ split-K reduction)
+int tf32_gemm_launches(coex_ctx* c, const OpSpec& s, int64_t M, int64_t N, int64_t K, Launch* L, int* nL) {
+  const int64_t ld = tf32_pitch(K > 0 ? K : 1);
+  TfCvtParams q{};
+  q.ds = s.ds;
+  q.src[0] = s.in[0];
+  q.src[1] = s.in[1];
+  q.rows[0] = M;
+  q.rows[1] = N;
+  q.K = K;
+  q.ld = ld;
+  q.trans[0] = s.trans_a ? 1 : 0;                  // A stored [K][M] when folded from a transpose
+  q.trans[1] = s.trans_b ? 0 : 1;                  // B^T rows: B stored [K][N] unless folded
+  q.dst[0] = (float*)s.scratch[0];
+  q.dst[1] = (float*)s.scratch[1];
+  const int64_t units = (M > N ? M : N) * ld / 4;
+  int64_t gx = (units + 255) / 256;
+  if (q.trans[0] || q.trans[1]) {
+    const int64_t tiles = (((M > N ? M : N) + 31) / 32) * ((ld + 31) / 32);
+    if (tiles > gx) gx = tiles;
+  }
+  if (gx > kNumSMs * 16) gx = kNumSMs * 16;
+  *nL = 0;
+  L[(*nL)++].set((void*)k_cvt_tf32, dim3((unsigned)(gx < 1 ? 1 : gx), 2), dim3(256), q);
+  const TcPlan t = tf32_plan(M, N, K, s.ws != nullptr);
+  TcGemmParams gp;
+  memset(&gp, 0, sizeof(gp));
+  int rc = make_tmap_tf32(&gp.tmA, s.scratch[0], M, ld, TC_BM);
+  if (!rc) rc = make_tmap_tf32(&gp.tmB, s.scratch[1], N, ld, t.bn);
+  if (rc) return rc;
+  gp.ds = s.ds;
+  gp.a = s.in[0];
+  gp.b = s.in[1];
+  gp.M = M;
+  gp.N = N;
+  gp.K = K;
+  gp.out = s.out;
+  gp.splits = t.splits;
+  gp.raw = t.splits > 1 ? (float*)s.ws : nullptr;
+  gp.cv.phases = 1;
+  gp.batch = 1;
+  const int64_t items = t.tiles * t.splits;
+  Launch& G = L[(*nL)++];
+  G.set(t.bn == 64 ? (void*)k_gemm_tf32<64> : (void*)k_gemm_tf32<128>,
+        dim3((unsigned)(items < kNumSMs ? items : kNumSMs)), dim3(TC_THREADS), gp);
+  G.smem = t.bn == 64 ? TfCfg<64>::SMEM : TfCfg<128>::SMEM;
+  static bool attr = false;
+  if (!attr) {
+    CK(cudaFuncSetAttribute((const void*)k_gemm_tf32<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, TfCfg<64>::SMEM));
+    CK(cudaFuncSetAttribute((const void*)k_gemm_tf32<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            TfCfg<128>::SMEM));
+    attr = true;
+  }
+  if (t.splits > 1) {
+    SplitReduceParams r{};
+    r.ds = s.ds;
+    r.ws = (float*)s.ws;
+    r.n = M * N;
+    r.splits = t.splits;
+    r.a = s.in[0];
+    r.b = s.in[1];
+    r.out = s.out;
+    L[(*nL)++].set((void*)k_splitk_reduce, grid_for(M * N / 4 + 1), dim3(256), r);
+  }
+  return COEX_OK;
 }
 
 // Appends the GEMM (and its split-K reduction) to L.  `ws` = fp32 split slices (splits > 1).
@@ -1708,11 +1826,20 @@ int build_xop(coex_ctx* c, const OpSpec& s, Launch* L, int* nL, size_t* ws_bytes
 }
 constexpr int kMaxLaunches = 6;
 
-bool needs_scratch(const coex_ctx* c, int kind) { return c->prec == COEX_BF16 && kind == COEX_MATMUL; }
+bool needs_scratch(const coex_ctx* c, int kind) {
+  return (c->prec == COEX_BF16 || tf32_path(c)) && kind == COEX_MATMUL;
+}
 
-// bf16 copies of the MatMul operands as stored ([rows][pitch(cols)]; K- or MN-major use)
-void scratch_bytes(const OpSpec& s, size_t* a, size_t* b) {
+// bf16 copies of the MatMul operands as stored ([rows][pitch(cols)]; K- or MN-major use);
+// 3xTF32: hi / lo fp32 planes of the K-major operands (A [M][K], B^T [N][K])
+void scratch_bytes(const coex_ctx* c, const OpSpec& s, size_t* a, size_t* b) {
   const int64_t ra = s.in_shape[0][0], ca = s.in_shape[0][1], rb = s.in_shape[1][0], cb = s.in_shape[1][1];
+  if (tf32_path(c)) {
+    const int64_t M = s.trans_a ? ca : ra, K = s.trans_a ? ra : ca, N = s.trans_b ? rb : cb;
+    *a = (size_t)2 * (M > 0 ? M : 1) * tf32_pitch(K > 0 ? K : 1) * 4;
+    *b = (size_t)2 * (N > 0 ? N : 1) * tf32_pitch(K > 0 ? K : 1) * 4;
+    return;
+  }
   const size_t a1 = (size_t)(ra > 0 ? ra : 1) * bf16_pitch(ca > 0 ? ca : 1) * 2;   // as stored
   const size_t a2 = (size_t)(ca > 0 ? ca : 1) * bf16_pitch(ra > 0 ? ra : 1) * 2;   // transposed
   const size_t b1 = (size_t)(rb > 0 ? rb : 1) * bf16_pitch(cb > 0 ? cb : 1) * 2;
@@ -1735,6 +1862,7 @@ int build_launches(coex_ctx* c, const OpSpec& s, Launch* L, int* nL) {
   const int64_t M = s.trans_a ? s.in_shape[0][1] : s.in_shape[0][0];
   const int64_t K = s.trans_a ? s.in_shape[0][0] : s.in_shape[0][1];
   const int64_t N = s.trans_b ? s.in_shape[1][0] : s.in_shape[1][1];
+  if (tf32_path(c)) return tf32_gemm_launches(c, s, M, N, K, L, nL);
   // operands are converted as stored (no transposition): A [M][K] -> K-major, A folded from a
   // transpose ([K][M]) -> MN-major; B [K][N] -> MN-major, B folded ([N][K]) -> K-major.  A
   // conversion is skipped when an earlier GEMM of the pass already made this copy.
@@ -2124,13 +2252,13 @@ int eager_spec(coex_ctx* c, int kind, const coex_attrs* attrs, int nin, const TR
 int eager_scratch(coex_ctx* c, OpSpec* s) {
   if (needs_scratch(c, s->kind)) {
     size_t ba, bb;
-    scratch_bytes(*s, &ba, &bb);
+    scratch_bytes(c, *s, &ba, &bb);
     CK(cudaMallocAsync(&s->scratch[0], ba, c->stream));
     CK(cudaMallocAsync(&s->scratch[1], bb, c->stream));
     const int64_t M = s->trans_a ? s->in_shape[0][1] : s->in_shape[0][0];
     const int64_t K = s->trans_a ? s->in_shape[0][0] : s->in_shape[0][1];
     const int64_t N = s->trans_b ? s->in_shape[1][0] : s->in_shape[1][1];
-    const size_t wb = matmul_split_ws(M, N, K);
+    const size_t wb = matmul_split_ws_c(c, M, N, K);
     if (wb) CK(cudaMallocAsync((void**)&s->ws, wb, c->stream));
   }
   if (is_ext_compute(s->kind)) {
@@ -2768,7 +2896,7 @@ struct Builder {
           const int64_t M = s.trans_a ? s.in_shape[0][1] : s.in_shape[0][0];
           const int64_t K = s.trans_a ? s.in_shape[0][0] : s.in_shape[0][1];
           const int64_t N = s.trans_b ? s.in_shape[1][0] : s.in_shape[1][1];
-          const size_t wb = matmul_split_ws(M, N, K);
+          const size_t wb = matmul_split_ws_c(c, M, N, K);
           if (wb) s.ws = shared_scratch(wb);
         }
         Launch L[kMaxLaunches];

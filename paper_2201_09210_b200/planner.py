@@ -127,6 +127,10 @@ class Planner:
         self.var_shapes = dict(var_shapes)
         self.feed_shapes = dict(feed_shapes)
         self.esize = esize
+        # fp32 mode: MatMuls run as 3xTF32 on the tensor cores (csrc/gemm_tf32.cuh) with hi / lo
+        # operand planes in per-op scratch; COEX_TF32=0 keeps the SIMT kernel (same switch as
+        # the runtime's tf32_on)
+        self.tf32 = (not bf16) and esize == 4 and os.environ.get("COEX_TF32", "1") != "0"
         self.ops = {}           # node id -> ExecOp (first instance)
         for x in walk(sp.body):
             if isinstance(x, ExecOp) and x.node_id not in self.ops:
@@ -574,6 +578,9 @@ class Planner:
             self._need_f32(cells[0], ca[1])
             self._need_f32(cells[1], cb[1])
             word += [ca[0], cb[0], ca[1], cb[1]]
+        elif k is OpKind.MATMUL and self.tf32:
+            p4 = (max(kk, 1) + 3) // 4 * 4
+            word += [self.new_buf(2 * max(m, 1) * p4 * 4), self.new_buf(2 * max(nn, 1) * p4 * 4), 1, 1]
         else:
             word += [-1, -1, 0, 0]
         word += out_words(nid, late)
