@@ -331,6 +331,8 @@ class CpuPass:
             self.thread.join()
         if self.error is not None and not self.ch.cancelled:
             return PassResult(False, error=repr(self.error))
+        if self.result is None:             # cancelled pass whose runner raised before returning
+            return PassResult(False, error=repr(self.error))
         return self.result
 
 

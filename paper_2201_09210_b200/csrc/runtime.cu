@@ -2585,9 +2585,9 @@ int coex_var_rollback(coex_ctx* c) {
 namespace {
 
 enum PlanTag : int64_t { T_SEQ = 1, T_OP = 2, T_PTR = 3, T_FEED = 4, T_FETCH = 5, T_SWITCH = 6, T_WHILE = 7, T_CHAIN = 8,
-                         T_ALLREDUCE = 9, T_XOP = 10, T_MCHAIN = 11, T_ATTN = 12 };
+                         T_ALLREDUCE = 9, T_XOP = 10, T_MCHAIN = 11, T_ATTN = 12, T_JOIN = 13 };
 constexpr int64_t kPlanMagic = 0xC0E8B200;
-constexpr int64_t kPlanVersion = 2;
+constexpr int64_t kPlanVersion = 3;
 
 struct FeedSlot {
   int64_t slot;
@@ -2747,6 +2747,7 @@ struct Builder {
   std::unordered_map<cudaGraphNode_t, bool> kernel_nodes;   // nodes created by add_kernel
   bool pdl = true;
   int64_t cancel_every = 64;        // kernel nodes per cancel-guarded segment (0: no guards)
+  std::vector<std::pair<cudaGraph_t, cudaGraphNode_t>> pending_ar;   // async collectives not yet joined
 
   // Kernel node after `*prev`.  Kernel -> kernel edges are programmatic (PDL): the node is
   // scheduled while its predecessor's last wave drains and synchronises in COEX_PDL_ENTER.
@@ -2830,7 +2831,7 @@ struct Builder {
     };
     for (int64_t i = 0; i < items; ++i) {
       const int64_t tag = pos < n ? w[pos] : -1;
-      const bool guardable = cancel_every > 0 && tag != T_ALLREDUCE;
+      const bool guardable = cancel_every > 0 && tag != T_ALLREDUCE && tag != T_JOIN;
       if (body && (!guardable || p->n_kernel_nodes - seg0 >= cancel_every)) {
         int rc = close();
         if (rc) return rc;
@@ -3059,9 +3060,33 @@ struct Builder {
         void* b = buf(next());
         const int64_t count = next();
         const int64_t avg = next();
+        const int64_t async = next();
         // the collective is captured on a side stream into a child graph node (a child node
-        // keeps conditional bodies simple)
-        return add_allreduce(g, prev, b, count, is_f64(c) ? kNcclDouble : kNcclFloat, avg ? kNcclAvg : kNcclSum);
+        // keeps conditional bodies simple).  async (gradient buckets): a side branch off the
+        // chain -- the following compute does not wait for it; a later T_JOIN (placed by the
+        // planner before the first reader) does
+        if (!async)
+          return add_allreduce(g, prev, b, count, is_f64(c) ? kNcclDouble : kNcclFloat, avg ? kNcclAvg : kNcclSum);
+        cudaGraphNode_t branch = *prev;
+        int rc = add_allreduce(g, &branch, b, count, is_f64(c) ? kNcclDouble : kNcclFloat, avg ? kNcclAvg : kNcclSum);
+        if (rc) return rc;
+        pending_ar.push_back({g, branch});
+        return COEX_OK;
+      }
+      case T_JOIN: {                                // chain += every pending collective of this graph
+        std::vector<cudaGraphNode_t> deps;
+        if (*prev) deps.push_back(*prev);
+        std::vector<std::pair<cudaGraph_t, cudaGraphNode_t>> keep;
+        for (auto& pr : pending_ar) {
+          if (pr.first == g) deps.push_back(pr.second);
+          else keep.push_back(pr);
+        }
+        pending_ar.swap(keep);
+        if (deps.size() <= 1) return COEX_OK;
+        cudaGraphNode_t node;
+        CK(cudaGraphAddEmptyNode(&node, g, deps.data(), deps.size()));
+        *prev = node;
+        return COEX_OK;
       }
       case T_PTR: {
         PtrParams q{};

@@ -119,9 +119,14 @@ class _Prop:
         self.reduce_at: dict = {}       # node id -> avg flag
         self.sync_bn: set = set()       # batch-norm family nodes over row shards (synchronised)
         self.kind: dict = {}
+        self.consumers: dict = {}       # node id -> ids of the ops reading it
         for x in _iter(sp.body):
             if isinstance(x, ExecOp):
                 self.kind[x.node_id] = x
+                for b in x.inputs:
+                    if not b.fed:
+                        for c in b.cands:
+                            self.consumers.setdefault(c, set()).add(x.node_id)
 
     def bind(self, b):
         if b.fed:
@@ -138,14 +143,38 @@ class _Prop:
         st = self.state[nid]
         return R if (st in PARTIAL and nid in self.reduce_at) else st
 
+    def _sole_partial(self, b, st, nid):
+        """binding b is one partial producer of kind st read only by node nid"""
+        return (not b.fed and len(b.cands) == 1 and self.state.get(b.cands[0]) == st
+                and self.consumers.get(b.cands[0], set()) == {nid})
+
     def need_r(self, nid):
-        """A consumer needs node ``nid`` replicated: schedule its all-reduce."""
+        """A consumer needs node ``nid`` replicated: schedule its all-reduce.  The collective is
+        hoisted to the earliest partial producer it can move to -- through a reshape (a view),
+        a scaling by a replicated value (the learning-rate product of an update), a negation or
+        a sum of partials each read only here -- so the gradient is reduced where the backward
+        pass produces it and the planner can overlap it with the rest of the backward
+        (planner._bucket_allreduce).  Sums are linear, so the result is the same up to
+        summation order."""
         st = self.state.get(nid)
         x = self.kind.get(nid)
         if st in PARTIAL and x is not None and x.kind is OpKind.RESHAPE and not x.inputs[0].fed \
                 and len(x.inputs[0].cands) == 1 and self.state.get(x.inputs[0].cands[0]) == st:
             # a reshape is a view with no buffer of its own: reduce its producer in place
             return self.need_r(x.inputs[0].cands[0])
+        if st in PARTIAL and x is not None and nid not in self.reduce_at:
+            ins = x.inputs
+            if x.kind is OpKind.MUL and len(ins) == 2:
+                for i in (0, 1):
+                    other = ins[1 - i]
+                    if self._sole_partial(ins[i], st, nid) and self.bind(other) == R:
+                        return self.need_r(ins[i].cands[0])
+            if x.kind in LINEAR_UNARY and self._sole_partial(ins[0], st, nid):
+                return self.need_r(ins[0].cands[0])
+            if x.kind is OpKind.ADD and len(ins) == 2 and all(self._sole_partial(b, st, nid) for b in ins) \
+                    and ins[0].cands != ins[1].cands:
+                self.need_r(ins[0].cands[0])
+                return self.need_r(ins[1].cands[0])
         if st in PARTIAL:
             self.reduce_at[nid] = st == PAVG
             return True

@@ -32,9 +32,11 @@ from .graph_gen import ExecOp, InputFeed, OutputFetch, SwitchCase, SymProgram, U
 from .tensor import BMM_KINDS, CONV_ATTR_KINDS, CONV_KINDS, OpKind, flops_of, infer_shape, shape_size
 
 MAGIC = 0xC0E8B200
-VERSION = 2
+VERSION = 3
 T_SEQ, T_OP, T_PTR, T_FEED, T_FETCH, T_SWITCH, T_WHILE, T_CHAIN, T_ALLREDUCE, T_XOP, T_MCHAIN = 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11
 T_ATTN = 12               # fused causal attention (csrc attn_tc.cuh): forward / backward of one layer
+T_JOIN = 13               # the chain waits for every asynchronous all-reduce issued so far in its list
+AR_BUCKET_BYTES = int(os.environ.get("COEX_AR_BUCKET_MB", "64")) << 20
 MAX_MCHAIN = 8            # chains per k_chain_multi launch (csrc kMaxMultiChain)
 PTR_ALIAS, PTR_READ_VAR, PTR_ASSIGN_VAR = 0, 1, 2
 MAX_RANK = 8
@@ -58,6 +60,18 @@ XOP_BN_ACT = 101          # batchnorm also writing relu / leaky_relu of its outp
 XOP_CE_FUSED = 102        # cross_entropy + cross_entropy_grad in one pass (csrc kCeFused)
 FA_HEAD = 64              # flash attention: head dim and query / key block of the tcgen05 kernels
 FA_BLOCK = 128
+
+
+class _ARBucket:
+    """Consecutive AllReduce items of one instruction list whose node buffers are adjacent in
+    the arena: ONE collective over the span (gradient bucketing), issued asynchronously."""
+
+    def __init__(self, members: list):
+        self.members = members
+
+
+class _Join:
+    """The chain waits for the list's asynchronous all-reduces (before their first reader)."""
 
 
 class _Attn:
@@ -246,7 +260,16 @@ class Planner:
         vcell: dict = {}
         fills: list = []
         consts: list = []
-        for nid, x in ops.items():
+        # all-reduced (data-parallel gradient) nodes get adjacent buffers in program order, so
+        # consecutive all-reduces of a list can run as one collective over the span
+        ar_order = []
+        for x in walk(self.sp.body):
+            if type(x).__name__ == "AllReduce" and x.node_id not in ar_order and x.node_id in ops:
+                ar_order.append(x.node_id)
+        self._ar_pos = {nid: i for i, nid in enumerate(ar_order)}
+        ar_set = set(ar_order)
+        for nid in ar_order + [n for n in ops if n not in ar_set]:
+            x = ops[nid]
             n = shape_size(shapes[nid])
             if x.kind in COMPUTE and nid not in folded and nid not in self.index_nodes:
                 self_dep = any((not b.fed) and nid in b.cands for b in x.inputs)
@@ -368,6 +391,8 @@ class Planner:
         self._skip_cell = {}                     # its output cell -> gradient node
         self.n_attn = 0                          # flash-attention groups (forward + backward)
         self.n_head_fold = 0                     # ... of which read / write the merged head layout
+        self.n_ar_buckets = 0                    # asynchronous bucketed all-reduces
+        self._ar_lists = []                      # instruction lists after bucketing (inspection)
         self._emitted = set()                    # node ids emitted as their own plan items
         self.chain_lates = 0
         self._chain_meta = {}
@@ -414,6 +439,7 @@ class Planner:
                 grads = {g.node_id for g in ce_of.values()}
                 insts = [ce_of.get(y.node_id, y) if isinstance(y, ExecOp) else y for y in insts
                          if not (isinstance(y, ExecOp) and y.node_id in grads)]
+            insts = self._bucket_allreduce(insts, node_buf, shapes)
             bn_groups, bn_skip = self._bn_bwd_groups(insts) if self.fuse else ({}, set())
             if self.fuse:
                 segs = self._segments(insts, shapes, folded)
@@ -477,7 +503,19 @@ class Planner:
                     b0, b1, pp = node_buf.get(x.node_id, (-1, -1, True))
                     if b0 < 0 or pp:
                         raise NeedsReplicated(f"node {x.node_id} has no static buffer to all-reduce")
-                    items.append([T_ALLREDUCE, b0, shape_size(shapes[x.node_id]), int(x.avg)])
+                    items.append([T_ALLREDUCE, b0, shape_size(shapes[x.node_id]), int(x.avg), 0])
+                elif isinstance(x, _ARBucket):
+                    self._invalidate()
+                    first = node_buf[x.members[0].node_id][0]
+                    # span of the adjacent arena buffers (each padded to 256 bytes, csrc plan load)
+                    span = 0
+                    for i, m in enumerate(x.members):
+                        nbytes = shape_size(shapes[m.node_id]) * self.esize
+                        span += nbytes if i == len(x.members) - 1 else (max(nbytes, 16) + 255) // 256 * 256
+                    items.append([T_ALLREDUCE, first, span // self.esize, int(x.members[0].avg), 1])
+                    self.n_ar_buckets += 1
+                elif isinstance(x, _Join):
+                    items.append([T_JOIN])
             return self._group_chains(items) if self.fuse else items
 
         def seq(insts) -> list:
@@ -1130,6 +1168,62 @@ class Planner:
             segs.append(("inst", x))
         flush()
         return segs
+
+    def _bucket_allreduce(self, insts, node_buf, shapes) -> list:
+        """Data-parallel gradient all-reduces (dp.py AllReduce items) of one instruction list,
+        bucketed and overlapped: consecutive all-reduces whose buffers are adjacent in the
+        arena (build() allocates all-reduced nodes in program order) and share sum / average
+        form one collective (up to AR_BUCKET_BYTES), issued as a side branch of the graph
+        (T_ALLREDUCE async); the compute that follows does not wait.  A _Join goes in front of
+        the first instruction that reads a value whose collective is pending or issued
+        (typically the parameter updates at the end of the backward pass), in front of any
+        control flow, and at the end of the list.  COEX_AR_BUCKET_MB=0 keeps one synchronous
+        collective per gradient."""
+        if AR_BUCKET_BYTES <= 0 or not any(type(x).__name__ == "AllReduce" for x in insts):
+            return insts
+        out, pending, issued = [], [], set()
+        nbytes = [0]
+
+        def flush():
+            if pending:
+                out.append(_ARBucket(list(pending)))
+                issued.update(m.node_id for m in pending)
+                pending.clear()
+                nbytes[0] = 0
+
+        def join():
+            flush()
+            if issued:
+                out.append(_Join())
+                issued.clear()
+
+        for x in insts:
+            if type(x).__name__ == "AllReduce":
+                b0 = node_buf.get(x.node_id, (-1, -1, True))
+                if b0[0] < 0 or b0[2]:
+                    raise NeedsReplicated(f"node {x.node_id} has no static buffer to all-reduce")
+                if pending:
+                    last = node_buf[pending[-1].node_id][0]
+                    if b0[0] != last + 1 or x.avg != pending[-1].avg:
+                        flush()
+                pending.append(x)
+                nbytes[0] += shape_size(shapes[x.node_id]) * self.esize
+                if nbytes[0] >= AR_BUCKET_BYTES:
+                    flush()
+                continue
+            waiting = issued | {m.node_id for m in pending}
+            if isinstance(x, ExecOp):
+                if waiting and any((not b.fed) and any(c in waiting for c in b.cands) for b in x.inputs):
+                    join()
+            elif isinstance(x, OutputFetch):
+                if x.node_id in waiting:
+                    join()
+            elif not isinstance(x, InputFeed):
+                join()                                   # control flow: everything settles first
+            out.append(x)
+        join()
+        self._ar_lists.append(out)
+        return out
 
     def _group_chains(self, items: list) -> list:
         """Adjacent elementwise chains that neither read what another one publishes (cells,

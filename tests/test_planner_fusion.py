@@ -105,3 +105,49 @@ def test_flash_attention_groups():
                and w[i + 3] == 128 and w[i + 4] == 2 and w[i + 5] == 128) >= 4
     emitted = {y.node_id for y in pl.ops.values() if y.kind is OpKind.TRANSPOSE and len(y.attrs["perm"]) == 4}
     assert emitted and all(n not in pl._emitted for n in emitted)
+
+
+@pytest.mark.parametrize("which", ["c2", "c4"])
+def test_dp_allreduce_buckets(which):
+    """Data-parallel gradient all-reduces are bucketed and asynchronous: consecutive
+    all-reduces of adjacent buffers form one collective (T_ALLREDUCE async), and a T_JOIN
+    precedes the first instruction reading any pending value (the parameter updates)."""
+    from paper_2201_09210_b200.dp import local_feed_shapes, shard_program
+    from paper_2201_09210_b200.graph_gen import ExecOp
+    from paper_2201_09210_b200.planner import T_ALLREDUCE, T_JOIN, _ARBucket, _Join
+    src = dcgan_program(steps=8, **C2_SMALL) if which == "c2" else gpt2_program(steps=6, **C4_SMALL)
+    o = make_orch(src, SyntheticDataset(0), CpuBackend())
+    for _ in range(5):
+        o.step()
+    feed = {(n.id, p): tuple(s) for n in o.tg.all_nodes() if n.typ == "op" for p, s in n.feed_shapes.items()}
+    vs = o.be.var_shapes()
+    vi = {k: j for j, k in enumerate(sorted(vs))}
+    gshapes = Planner(o.sp, o.tg, vi, vs, feed, 4).infer_shapes()
+    batch = (C2_SMALL if which == "c2" else C4_SMALL)["batch"]
+    dplan = shard_program(o.sp, feed, gshapes, batch, 2)
+    assert not dplan.replicated, dplan.reason
+    pl = Planner(dplan.sp, o.tg, vi, vs, local_feed_shapes(feed, dplan), 4, bf16=True,
+                 force_store=dplan.allreduce_nodes)
+    plan = pl.build()
+    assert pl.n_ar_buckets >= 1
+    n_ar = len([n for n in dplan.allreduce_nodes])
+    w = plan.words
+    assert T_JOIN in w and T_ALLREDUCE in w
+    for lst in pl._ar_lists:
+        pending = set()
+        members = [m.node_id for x in lst if isinstance(x, _ARBucket) for m in x.members]
+        assert len(members) == len(set(members))
+        for x in lst:
+            if isinstance(x, _ARBucket):
+                bufs = [pl._node_buf[m.node_id][0] for m in x.members]
+                assert bufs == list(range(bufs[0], bufs[0] + len(bufs)))     # adjacent in the arena
+                pending |= {m.node_id for m in x.members}
+            elif isinstance(x, _Join):
+                pending.clear()
+            elif isinstance(x, ExecOp):
+                reads = {c for b in x.inputs if not b.fed for c in b.cands}
+                assert not (reads & pending), (x.kind, reads & pending)
+        assert not pending
+    # fewer collectives than gradients: bucketing merged some
+    n_coll = sum(len(x.members) > 0 for lst in pl._ar_lists for x in lst if isinstance(x, _ARBucket))
+    assert n_coll < n_ar, (n_coll, n_ar)
