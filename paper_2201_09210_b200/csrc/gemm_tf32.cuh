@@ -9,6 +9,13 @@
 // accumulates  A_hi.B_hi + A_hi.B_lo + A_lo.B_hi  in the fp32 TMEM accumulator (the dropped
 // A_lo.B_lo term is ~2^-22 relative): three tcgen05.mma kind::tf32 per K step.
 //
+// Measured (tools/tf32_err.py, B200): 2.1e-6 relative per op for K <= 3072 -- a floor set by
+// the tensor core's own fp32 accumulation (adding the A_lo.B_lo term does not move it),
+// growing with the accumulation length (2.3e-5 at K = 50257 in one chain, 7.5e-6 with chains
+// of <= 1024: COEX_TF32_MAXK splits K).  FFMA: 5e-7.  The fp32 mode therefore keeps the SIMT
+// kernel by default (the 1e-5 end-to-end gradient bar fails by ~2x with this path);
+// COEX_TF32=1 selects it (~190-260 TFLOP/s vs the FFMA kernel's SIMT rate).
+//
 //   k_cvt_tf32   fp32 operand (as stored, or transposed through a 32 x 33 shared tile) ->
 //                hi / lo planes [2][rows][pitch4(K)], K-major (B is written as B^T [N][K]).
 //   k_gemm_tf32  the warp-specialised persistent GEMM of gemm_tc.cuh (TMA producer warp, MMA

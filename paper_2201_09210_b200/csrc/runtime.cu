@@ -182,14 +182,14 @@ struct coex_ctx {
 namespace {
 
 bool is_f64(const coex_ctx* c) { return c->prec == COEX_F64; }
-// COEX_TF32=0: fp32-mode MatMuls on the SIMT FFMA kernel instead of 3xTF32 tcgen05 (A/B only)
+// COEX_TF32=1: fp32-mode MatMuls as 3xTF32 on tcgen05 (csrc/gemm_tf32.cuh) instead of the
+// SIMT FFMA kernel.  Off by default: the tensor core's fp32 accumulation carries ~2^-19
+// relative error per MMA (measured, tools/tf32_err.py: 2.1e-6 per op at K <= 3072 vs 5e-7
+// for FFMA), which the north_star's 1e-5 end-to-end gradient bar does not absorb
+// (tests/test_gpu_contract.py fp32 cases).  Read per call: the planner reads the same variable.
 bool tf32_on() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("COEX_TF32");
-    v = (e && e[0] == '0') ? 0 : 1;
-  }
-  return v == 1;
+  const char* e = getenv("COEX_TF32");
+  return e && e[0] == '1';
 }
 bool tf32_path(const coex_ctx* c) { return c->prec == COEX_F32 && tf32_on(); }
 
@@ -898,6 +898,17 @@ TcPlan tf32_plan(int64_t M, int64_t N, int64_t K, bool allow_split) {
     if (sp > nk / 8) sp = nk / 8;
     if (sp > 16) sp = 16;
     t.splits = sp > 1 ? (int)sp : 1;
+  }
+  // accuracy: one TMEM accumulation chain covers at most COEX_TF32_MAXK K elements (slices are
+  // summed in IEEE fp32 by k_splitk_reduce)
+  static int64_t maxk = -1;
+  if (maxk < 0) {
+    const char* e = getenv("COEX_TF32_MAXK");
+    maxk = e ? atoll(e) : 1024;
+  }
+  if (allow_split && maxk > 0) {
+    const int64_t need = (K + maxk - 1) / maxk;
+    if (need > t.splits) t.splits = (int)(need < 64 ? need : 64);
   }
   return t;
 }

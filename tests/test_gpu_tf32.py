@@ -1,10 +1,11 @@
-"""fp32-mode MatMul as 3xTF32 on the tcgen05 tensor cores (csrc/gemm_tf32.cuh) against the
-float64 oracle (oracle.kernels.execute_kernel <- tensor.py:228-236).
+"""fp32-mode MatMul as 3xTF32 on the tcgen05 tensor cores (csrc/gemm_tf32.cuh, COEX_TF32=1)
+against the float64 oracle (oracle.kernels.execute_kernel <- tensor.py:228-236).
 
-Contract (BASELINE.json north_star): fp32 outputs agree within 1e-5 relative.  A single TF32
-product would miss it (~5e-4); the hi / lo split keeps the error at the fp32-accumulation
-level, checked here per op (norm-wise and element-wise against the operand scale) over
-aligned and ragged shapes, split-K launches, folded transposes and a co-executed program."""
+A single TF32 product would miss the fp32 bar (~5e-4); the hi / lo split brings a single op
+to the tensor core's fp32-accumulation floor (~2e-6, measured), checked here per op against
+1e-5 (norm-wise and element-wise against the operand scale) over aligned and ragged shapes,
+split-K launches, folded transposes and a co-executed program.  The fp32 mode's default stays
+the SIMT kernel: end to end, that floor exceeds the contract's 1e-5 gradient bar."""
 
 import numpy as np
 import pytest
@@ -13,6 +14,11 @@ from oracle.kernels import execute_kernel
 from paper_2201_09210_b200.tensor import OpKind, Tensor
 
 pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(autouse=True)
+def _tf32(monkeypatch):
+    monkeypatch.setenv("COEX_TF32", "1")
 
 
 @pytest.mark.parametrize("m,k,n", [(128, 64, 128), (64, 784, 128), (1, 1, 1), (130, 70, 250), (1000, 300, 700),
