@@ -129,6 +129,9 @@ typedef struct coex_pass_stats {
 
 const char* coex_last_error(void);
 const char* coex_version(void);
+/* Launch shape of the tcgen05 bf16 GEMM for an [M,K] x [K,N] MatMul (tile width bn, split-K
+ * count, 1 = two CTAs per SM): host-only query for tests / tuning (no context needed). */
+int coex_gemm_plan(int64_t M, int64_t N, int64_t K, int allow_split, int* bn, int* splits, int* duo);
 
 /* ---- context ---- */
 int coex_ctx_create(int device, int precision, coex_ctx** out);

@@ -53,6 +53,8 @@ _IP = ctypes.POINTER(ctypes.c_int)
 SIGNATURES = {
     "coex_last_error": (ctypes.c_char_p, []),
     "coex_version": (ctypes.c_char_p, []),
+    "coex_gemm_plan": (ctypes.c_int, [_I64, _I64, _I64, ctypes.c_int, ctypes.POINTER(ctypes.c_int),
+                                      ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]),
     "coex_ctx_create": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.POINTER(_P)]),
     "coex_ctx_destroy": (ctypes.c_int, [_P]),
     "coex_ctx_sync": (ctypes.c_int, [_P]),
@@ -165,6 +167,14 @@ def _attrs(kind: OpKind, attrs: dict) -> CoexAttrs:
     for i, d in enumerate(dims):
         at.dims[i] = int(d)
     return at
+
+
+def gemm_plan(M: int, N: int, K: int, allow_split: bool = True) -> tuple:
+    """(tile width, split-K count, two-CTA variant) the runtime picks for a bf16 MatMul."""
+    lib = load_library()
+    bn, sp, duo = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+    _check(lib.coex_gemm_plan(M, N, K, int(allow_split), ctypes.byref(bn), ctypes.byref(sp), ctypes.byref(duo)))
+    return bn.value, sp.value, bool(duo.value)
 
 
 class DevTensor:

@@ -821,6 +821,22 @@ bool duo_model() {
   return v == 1;
 }
 int duo_mode();
+double bn256_bias() {
+  static double v = -1;
+  if (v < 0) {
+    const char* e = getenv("COEX_BN256_BIAS");
+    v = e ? atof(e) : 0.9;
+  }
+  return v;
+}
+double duo_penalty() {
+  static double v = -1;
+  if (v < 0) {
+    const char* e = getenv("COEX_DUO_PENALTY");
+    v = e ? atof(e) : 1.7;
+  }
+  return v;
+}
 // The DUO (two CTAs per SM) decision for a launch of tile width bn whose split holds
 // `kblocks` K-blocks (= ceil(K / BK) / splits, integer division as the launch computes it);
 // tc_plan prices tiles with the same rule the launch applies.
@@ -866,8 +882,12 @@ TcPlan tc_plan(int64_t M, int64_t N, int64_t K, bool allow_split) {
       const double epi = (double)TC_BM * bn * 4 / 23.5e9;
       double body = mma > feed ? mma : feed;
       if (epi > body) body = epi;
+      // the DUO variant's two-stage ring leaves TMA latency exposed: measured per-item cost
+      // (tools/ncu_ops.py c4_* with COEX_DUO / COEX_FORCE_BN) ~1.7x the single-CTA model
+      if (slots > kNumSMs) body *= duo_penalty();
       double t = rounds * (body + 0.9e-6) + epi + 2e-6;
       if (sp > 1) t += (double)(sp + 1) * M * N * 4 / 5.5e12 + 3e-6;
+      if (bn == 256) t *= bn256_bias();           // measured: the wide tile beats the model
       if (t < best_t * 0.98) {
         best_t = t;
         best.bn = bn;
@@ -1955,6 +1975,16 @@ extern "C" {
 
 const char* coex_last_error(void) { return g_err.c_str(); }
 const char* coex_version(void) { return "coexb200 0.1.0 sm_100a"; }
+
+// The tcgen05 GEMM launch shape the runtime picks for an [M, K] x [K, N] bf16 MatMul (tile
+// width, split-K count, two-CTA-per-SM variant) -- host-only, for tests and tuning tools.
+int coex_gemm_plan(int64_t M, int64_t N, int64_t K, int allow_split, int* bn, int* splits, int* duo) {
+  const TcPlan t = tc_plan(M, N, K, allow_split != 0);
+  *bn = t.bn;
+  *splits = t.splits;
+  *duo = tc_use_duo(t.bn, (K + TC_BK - 1) / TC_BK / (t.splits > 0 ? t.splits : 1)) ? 1 : 0;
+  return COEX_OK;
+}
 
 int coex_ctx_create(int device, int precision, coex_ctx** out) {
   if (precision < COEX_F64 || precision > COEX_BF16) return fail(COEX_INVALID, "bad precision");
