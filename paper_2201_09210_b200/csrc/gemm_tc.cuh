@@ -158,6 +158,8 @@ struct TcGemmParams {
   //            the diagonal are skipped (no MMA, no store);
   //   tri_a:   A is lower- (1) / upper- (2) triangular in (m, k) -> K blocks outside are zero
   int tri_out, tri_a;
+  In bias;                   // has_bias: C[m][n] += bias[n] in the epilogue (fused bias_add)
+  int has_bias;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -461,6 +463,7 @@ __global__ void __launch_bounds__(TC_THREADS, DUO ? 2 : 1) k_gemm_tc(const __gri
     const int lane_base = 32 * (warp % 4);          // TMEM lanes of this warp
     float* stage = (float*)(tmem_slot + 4) + (warp - 2) * (32 * TC_EPI_LD);
     const bool vec_ok = (p.N % 4) == 0;
+    const float* bias = p.has_bias ? res<float>(p.bias) : nullptr;
     int li = 0;
     for (long long it = blockIdx.x; it < items; it += gridDim.x, ++li) {
       int m0, n0, split, kb0, nk;
@@ -501,12 +504,24 @@ __global__ void __launch_bounds__(TC_THREADS, DUO ? 2 : 1) k_gemm_tc(const __gri
         __syncwarp();
         const int sub = lane >> 3, col = (lane & 7) * 4;   // 4 rows x 8 float4 per instruction
         const long long gcol = (long long)n0 + c + col;
+        // fused bias_add: this lane's four columns, loaded once per chunk (not per row)
+        float4 bv = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (bias != nullptr && gcol < p.N) {
+          if (vec_ok && gcol + 4 <= p.N) {
+            bv = __ldg((const float4*)(bias + gcol));
+          } else {
+            bv.x = __ldg(bias + gcol);
+            if (gcol + 1 < p.N) bv.y = __ldg(bias + gcol + 1);
+            if (gcol + 2 < p.N) bv.z = __ldg(bias + gcol + 2);
+            if (gcol + 3 < p.N) bv.w = __ldg(bias + gcol + 3);
+          }
+        }
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
           const int rr = q * 4 + sub;
           const long long grow = (long long)m0 + lane_base + rr;
           if (grow < p.M && gcol < p.N) {
-            const float4 v = *(const float4*)(stage + rr * TC_EPI_LD + col);
+            float4 v = *(const float4*)(stage + rr * TC_EPI_LD + col);
             long long orow = grow;
             if (AMODE == 2 && phases > 1) {          // sub-pixel conv2d_t: scatter to the output grid
               int pn, hy, wx;
@@ -515,6 +530,7 @@ __global__ void __launch_bounds__(TC_THREADS, DUO ? 2 : 1) k_gemm_tc(const __gri
               orow = ((long long)pn * p.cv.Ho + (long long)hy * p.cv.so + py) * p.cv.Wo + (long long)wx * p.cv.so + px;
             }
             float* dst = C + orow * p.N + gcol;
+            v.x += bv.x; v.y += bv.y; v.z += bv.z; v.w += bv.w;
             if (vec_ok && gcol + 4 <= p.N) {
               *(float4*)dst = v;
             } else {
@@ -565,13 +581,18 @@ struct SplitReduceParams {
   int splits;
   In a, b;                   // node operands (ping-pong output choice only)
   Out out;
+  In bias;                   // has_bias: out[m][c] += bias[c] (fused bias_add), ncols = N
+  int has_bias;
+  long long ncols;
 };
 __global__ void __launch_bounds__(256) k_splitk_reduce(SplitReduceParams p) {
   COEX_PDL_ENTER();
   stamp(p.ds, SK_SPLITK);
   float* o = pick_out<float>(p.out, res<float>(p.a), p.b.cell || p.b.direct ? res<float>(p.b) : nullptr);
   publish_early(p.out, o);
-  const long long n4 = (p.n % 4) == 0 ? p.n / 4 : 0;   // slices start 16-byte aligned only when 4 | n
+  const float* bias = p.has_bias ? res<float>(p.bias) : nullptr;
+  // slices start 16-byte aligned only when 4 | n; the bias's column groups need 4 | ncols
+  const long long n4 = ((p.n % 4) == 0 && (bias == nullptr || p.ncols % 4 == 0)) ? p.n / 4 : 0;
   const long long stride = (long long)gridDim.x * blockDim.x;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
     float4 acc = ((const float4*)p.ws)[i];
@@ -579,11 +600,16 @@ __global__ void __launch_bounds__(256) k_splitk_reduce(SplitReduceParams p) {
       const float4 v = ((const float4*)(p.ws + (long long)s * p.n))[i];
       acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
     }
+    if (bias != nullptr) {
+      const float4 bv = *(const float4*)(bias + (i * 4) % p.ncols);
+      acc.x += bv.x; acc.y += bv.y; acc.z += bv.z; acc.w += bv.w;
+    }
     ((float4*)o)[i] = acc;
   }
   for (long long i = n4 * 4 + (long long)blockIdx.x * blockDim.x + threadIdx.x; i < p.n; i += stride) {
     float acc = p.ws[i];
     for (int s = 1; s < p.splits; ++s) acc += p.ws[(long long)s * p.n + i];
+    if (bias != nullptr) acc += bias[i % p.ncols];
     o[i] = acc;
   }
   publish_late(p.out, o);

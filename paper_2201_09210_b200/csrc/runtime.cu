@@ -563,6 +563,7 @@ struct OpSpec {
   void* shadow = nullptr;                  // bf16 copy of the output to write (softmax-type producers)
   void* in_shadow[kMaxIn] = {nullptr, nullptr, nullptr};   // shared bf16 copies of GEMM operands
   int in_conv[kMaxIn] = {1, 1, 1};         // 1: this op converts into in_shadow / scratch first
+  int bias = 0;                            // MatMul: in[2] is a [N] bias added by the epilogue
   DevState* ds = nullptr;
 };
 
@@ -1107,9 +1108,14 @@ bool conv_blocks(int64_t Hg, int64_t Wg, int pix, int* bw, int* bh, int* bn) {
 int tc_gemm_launches(coex_ctx* c, DevState* ds, void* a16, void* b16, int64_t M, int64_t N, int64_t K,
                      const TcPlan& t, In na, In nb, const Out& out, float* raw, float* ws, Launch* L, int* nL,
                      int amode = 0, bool b_mn = false, const TcConv* cv = nullptr,
-                     const CUtensorMap* conv_map = nullptr, int64_t batch = 1) {
+                     const CUtensorMap* conv_map = nullptr, int64_t batch = 1, const In* bias = nullptr) {
   TcGemmParams gp;
   memset(&gp, 0, sizeof(gp));
+  if (bias) {
+    if (amode >= 2 || batch > 1) return fail(COEX_INVALID, "GEMM bias epilogue: plain 2-D MatMul only");
+    gp.bias = *bias;
+    gp.has_bias = t.splits > 1 ? 0 : 1;          // split-K: the slice reduction adds it
+  }
   int rc = COEX_OK;
   if (amode >= 2) gp.tmA = *conv_map;
   else if (batch > 1) rc = amode == 1 ? make_tmap3(&gp.tmA, a16, K, M, batch, 64, TC_BK) : make_tmap3(&gp.tmA, a16, M, K, batch, TC_BK, TC_BM);
@@ -1159,6 +1165,11 @@ int tc_gemm_launches(coex_ctx* c, DevState* ds, void* a16, void* b16, int64_t M,
     r.splits = t.splits;
     r.a = na;
     r.b = nb;
+    if (bias) {
+      r.bias = *bias;
+      r.has_bias = 1;
+      r.ncols = N;
+    }
     if (raw != nullptr) {            // reduce into scratch: a private, never-published Out
       r.out = Out{};
       r.out.buf[0] = raw;
@@ -1930,7 +1941,8 @@ int build_launches(coex_ctx* c, const OpSpec& s, Launch* L, int* nL) {
                    dim3(256), q);
   }
   return tc_gemm_launches(c, s.ds, s.scratch[0], s.scratch[1], M, N, K, tc_plan(M, N, K, s.ws != nullptr), s.in[0],
-                          s.in[1], s.out, nullptr, (float*)s.ws, L, nL, a_mn ? 1 : 0, b_mn);
+                          s.in[1], s.out, nullptr, (float*)s.ws, L, nL, a_mn ? 1 : 0, b_mn, nullptr, nullptr, 1,
+                          s.bias ? &s.in[2] : nullptr);
 }
 
 int launch_now(coex_ctx* c, Launch& L) {
@@ -2932,6 +2944,13 @@ struct Builder {
         s.scratch[1] = buf(next());
         s.in_conv[0] = (int)next();
         s.in_conv[1] = (int)next();
+        {
+          const int64_t bc = next();                // fused bias_add (GEMM epilogue), -1: none
+          if (bc != -1) {
+            s.in[2] = operand(bc);
+            s.bias = 1;
+          }
+        }
         read_out(s.out);
         s.nin = 2;
         if (needs_scratch(c, s.kind)) {           // bf16 MatMul: split-K slices when the tile grid is small

@@ -392,6 +392,8 @@ class Planner:
         self.n_attn = 0                          # flash-attention groups (forward + backward)
         self.n_head_fold = 0                     # ... of which read / write the merged head layout
         self.n_ar_buckets = 0                    # asynchronous bucketed all-reduces
+        self._bias_for = {}                      # MatMul node -> bias_add fused into its epilogue
+        self.n_bias_fused = 0
         self._ar_lists = []                      # instruction lists after bucketing (inspection)
         self._emitted = set()                    # node ids emitted as their own plan items
         self.chain_lates = 0
@@ -434,6 +436,12 @@ class Planner:
                     self.n_attn += 1
                 insts = [repl.get(y.node_id, y) if isinstance(y, ExecOp) else y for y in insts
                          if not (isinstance(y, ExecOp) and y.node_id in gone)]
+            bias_of = self._bias_pairs(insts) if (self.fuse and self.bf16) else {}
+            if bias_of:                             # bias_add folded into its GEMM's epilogue
+                gone_b = {y.node_id for y in bias_of.values()}
+                insts = [y for y in insts if not (isinstance(y, ExecOp) and y.node_id in gone_b)]
+                self._bias_for.update(bias_of)
+                self.n_bias_fused += len(bias_of)
             ce_of = self._ce_pairs(insts) if self.fuse else {}
             if ce_of:                               # the gradient moves up to the loss's position
                 grads = {g.node_id for g in ce_of.values()}
@@ -588,7 +596,10 @@ class Planner:
         while len(cells) < 2:
             cells.append(-1)
             in_shapes.append(())
-        late = _conflicts(cells, pubs[nid])
+        ba = self._bias_for.get(nid) if k is OpKind.MATMUL else None
+        bias_cell = in_cell(ba.inputs[1]) if ba is not None else -1
+        out_nid = ba.node_id if ba is not None else nid
+        late = _conflicts(cells + ([bias_cell] if ba is not None else []), pubs[out_nid])
         attr_dims = list(x.attrs.get("perm", ()))
         out_shape = shapes[nid]
         n_compute[0] += 1
@@ -621,8 +632,11 @@ class Planner:
             word += [self.new_buf(2 * max(m, 1) * p4 * 4), self.new_buf(2 * max(nn, 1) * p4 * 4), 1, 1]
         else:
             word += [-1, -1, 0, 0]
-        word += out_words(nid, late)
-        self._invalidate(pubs[nid])
+        word += [bias_cell]
+        word += out_words(out_nid, late)
+        self._invalidate(pubs[out_nid])
+        if ba is not None:
+            self._invalidate(pubs[nid])
         return [word]
 
     def _bn_act_pairs(self, insts) -> dict:
@@ -836,6 +850,42 @@ class Planner:
             word += out_words(nid, _conflicts(cells, pubs[nid]))
             self._invalidate(pubs[nid])
         return word
+
+    def _bias_pairs(self, insts) -> dict:
+        """bias_add(matmul(a, b), c) in one instruction list (C4 / C5 projections): the GEMM
+        epilogue adds the bias (split-K: the slice reduction does) and writes the bias_add's
+        output directly -- no separate pass over the [rows, N] product.  Legal when the
+        MatMul's only reader is the bias_add, neither node is fetched / merged / pinned /
+        self-dependent, and the bias binding is produced before the MatMul (or fed).
+        Returns {matmul node: bias_add node}."""
+        if os.environ.get("COEX_BIAS_FUSE", "1") == "0":
+            return {}
+        multi_nodes = {n for s_ in self._multi_sets() for n in s_}
+        banned = set(self.sp.fetch_nodes) | multi_nodes | set(self.force_store) | set(self.folded_assigns.values())
+        pos = {x.node_id: i for i, x in enumerate(insts) if isinstance(x, ExecOp)}
+        out = {}
+        for x in insts:
+            if not isinstance(x, ExecOp) or x.kind is not OpKind.BIAS_ADD or x.node_id in banned:
+                continue
+            a, c = x.inputs
+            if a.fed or len(a.cands) != 1 or a.cands[0] not in pos:
+                continue
+            m = self.ops[a.cands[0]]
+            if m.kind is not OpKind.MATMUL or m.node_id in banned or m.node_id in out:
+                continue
+            if [y.node_id for y in self.consumers.get(m.node_id, [])] != [x.node_id]:
+                continue
+            if self._node_buf.get(x.node_id, (-1, -1, True))[2] or x.node_id not in self._node_buf:
+                continue
+            if any((not b.fed) and x.node_id in b.cands for b in x.inputs):
+                continue
+            if not c.fed and any(cc in pos and pos[cc] > pos[m.node_id] and cc not in self.elided_reads
+                                 for cc in c.cands):
+                continue                            # (an elided variable read has no position)
+            if not c.fed and any(cc == m.node_id for cc in c.cands):
+                continue
+            out[m.node_id] = x
+        return out
 
     def _ce_pairs(self, insts) -> dict:
         """cross_entropy(lg, ids) and cross_entropy_grad(lg, ids) over the same bindings in one

@@ -151,3 +151,13 @@ def test_dp_allreduce_buckets(which):
     # fewer collectives than gradients: bucketing merged some
     n_coll = sum(len(x.members) > 0 for lst in pl._ar_lists for x in lst if isinstance(x, _ARBucket))
     assert n_coll < n_ar, (n_coll, n_ar)
+
+
+def test_bias_add_fused_into_gemm():
+    """C4: every projection's bias_add(matmul(a, w), c) becomes the GEMM's epilogue (one plan
+    op publishing the bias_add's output); the bias_add is never launched on its own."""
+    pl, plan = _planner(gpt2_program(steps=6, **C4_SMALL))
+    assert pl.n_bias_fused == 6 * C4_SMALL["layers"]
+    for m, ba in pl._bias_for.items():
+        assert pl.ops[m].kind is OpKind.MATMUL and ba.kind is OpKind.BIAS_ADD
+        assert ba.node_id not in pl._emitted and m in pl._emitted

@@ -1,0 +1,4 @@
+#!/bin/bash
+mkdir -p gpurun_out
+timeout 1500 python -m pytest tests/test_gpu_gpt2.py tests/test_gpu_music.py tests/test_gpu_tc.py tests/test_gpu_flash.py tests/test_gpu_xformer.py "tests/test_gpu_contract.py::test_full_width_gradients[c4-bf16]" "tests/test_gpu_contract.py::test_full_width_gradients[c5-bf16]" -q --tb=short > gpurun_out/bias_tests.log 2>&1; echo rc=$? >> gpurun_out/bias_tests.log
+timeout 900 python bench.py --no-cpu-baseline > gpurun_out/bias_c4.json 2> gpurun_out/bias_c4.err
