@@ -1247,6 +1247,14 @@ void* im2col_small_fn(int64_t C, int64_t k) {
   return nullptr;
 }
 
+// COEX_CE_STREAM=1: the streaming two-pass cross-entropy for wide rows instead of the
+// shared-memory-staged one (measured slower on C4: 2.34 vs 1.32 ms per step -- the second pass
+// re-reads rows that no longer fit in L2 with ~600 rows in flight; kept for A/B)
+bool ce_stream() {
+  const char* e = getenv("COEX_CE_STREAM");
+  return e && e[0] == '1';
+}
+
 // COEX_COL_BULK=0 keeps the register-pipelined column statistics (A/B measurement)
 bool col_bulk() {
   static int v = -1;
@@ -1569,6 +1577,19 @@ int build_xop_t(coex_ctx* c, const OpSpec& s, Launch* L, int* nL, size_t* ws_byt
     case kBnAct: {
       const int64_t C = s.in_shape[0][s.in_ndim[0] - 1];
       const int64_t Rw = numel_of(s.in_ndim[0], s.in_shape[0]) / C;
+      if (s.kind == COEX_SUM_ROWS && !is_f64(c) && C % 4 == 0 && (C > 1024 || (Rw >= 4096 && C >= 256))) {
+        // tolerance modes, 4 | C: 16-byte column groups, row chunks sized to fill the SMs
+        const int64_t gx = (C + 255) / 256;
+        int64_t gy = 1;
+        while (gy < 256 && gx * gy < kNumSMs * 4 && Rw / (gy * 2) >= 64) gy *= 2;
+        RowParams rp{};
+        rp.ds = s.ds; rp.x = s.in[0]; rp.rows = Rw; rp.d = C; rp.out = s.out;
+        if (gy > 1) rp.acc = (double*)pv.take((size_t)C * 8);
+        if (!build) break;
+        L[(*nL)++].set((void*)k_colsum_v4, dim3((unsigned)gx, (unsigned)gy), dim3(256), rp);
+        if (gy > 1) L[(*nL)++].set((void*)k_acc_out<float>, grid_for(C), dim3(256), rp);
+        return COEX_OK;
+      }
       if (s.kind == COEX_SUM_ROWS && (C > 1024 || (!is_f64(c) && Rw >= 4096 && C >= 256))) {
         // wide rows / tall tolerance-mode sums: column-parallel sum over row chunks
         const int64_t gx = (C + 255) / 256;
@@ -1769,6 +1790,14 @@ int build_xop_t(coex_ctx* c, const OpSpec& s, Launch* L, int* nL, size_t* ws_byt
           rp.d = d; rp.rows = xn / d;
           void* fn = s.kind == COEX_LAYERNORM ? (is_f64(c) ? (void*)k_layernorm<double, 0> : (void*)k_layernorm<float, 0>)
                                               : (is_f64(c) ? (void*)k_layernorm<double, 1> : (void*)k_layernorm<float, 1>);
+          if (!is_f64(c) && d % 4 == 0 && d <= 1024) {   // 16-byte rows: PER float4 groups per lane
+            const bool fw = s.kind == COEX_LAYERNORM;
+            const int per = (int)((d / 4 + 31) / 32);
+            fn = per <= 2 ? (fw ? (void*)k_layernorm_v4<0, 2> : (void*)k_layernorm_v4<1, 2>)
+                 : per <= 4 ? (fw ? (void*)k_layernorm_v4<0, 4> : (void*)k_layernorm_v4<1, 4>)
+                 : per <= 6 ? (fw ? (void*)k_layernorm_v4<0, 6> : (void*)k_layernorm_v4<1, 6>)
+                            : (fw ? (void*)k_layernorm_v4<0, 8> : (void*)k_layernorm_v4<1, 8>);
+          }
           L[(*nL)++].set(fn, warp_rows(rp.rows), dim3(256), rp);
           return COEX_OK;
         }
@@ -1823,6 +1852,10 @@ int build_xop_t(coex_ctx* c, const OpSpec& s, Launch* L, int* nL, size_t* ws_byt
                            dim3((unsigned)(R < kNumSMs * 8 ? R : kNumSMs * 8)), dim3(256), lp);
             L[(*nL)++].set(is_f64(c) ? (void*)k_cross_entropy<double, 1> : (void*)k_cross_entropy<float, 1>,
                            dim3((unsigned)(R < kNumSMs * 8 ? R : kNumSMs * 8)), dim3(256), rp);
+            return COEX_OK;
+          }
+          if (V >= 8192 && ce_stream()) {             // wide vocabulary: streaming two-pass kernel
+            L[(*nL)++].set((void*)k_ce_stream, dim3((unsigned)(R < kNumSMs * 4 ? R : kNumSMs * 4)), dim3(256), rp);
             return COEX_OK;
           }
           const bool wide = V >= 8192;

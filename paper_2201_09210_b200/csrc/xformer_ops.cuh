@@ -290,6 +290,103 @@ __global__ void __launch_bounds__(256) k_layernorm(RowParams p) {
   publish_late(p.out, o);
 }
 
+// fp32 rows with 4 | d <= 1024 (C4 / C5: 768 / 512): one warp per row, 16-byte accesses --
+// lane l holds float4 groups l, l+32, ... (PER = d / 128 of them) -- so a row is a handful of
+// coalesced 512-byte instructions per operand; the bf16 shadow leaves as 8-byte stores.
+// mode 0: y = xhat*g + b (+ shadow); mode 1: dx from (x, g, dy).  Same math as k_layernorm.
+template <int MODE, int PER>
+__global__ void __launch_bounds__(256) k_layernorm_v4(RowParams p) {
+  COEX_PDL_ENTER();
+  stamp(p.ds, SK_LN);
+  const float* x = res<float>(p.x);
+  const float* g = res<float>(p.y);
+  const float* z = res<float>(p.z);
+  float* o = pick_out<float>(p.out, x, g);
+  publish_early(p.out, o);
+  count_op(p.ds);
+  const int lane = threadIdx.x & 31;
+  const long long warps = (long long)gridDim.x * (blockDim.x / 32);
+  const long long d = p.d, d4 = d / 4;
+  const float4* g4 = (const float4*)g;
+  const float4* z4 = (const float4*)z;
+  for (long long r = (long long)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; r < p.rows; r += warps) {
+    const float4* xr = (const float4*)(x + r * d);
+    float4 xv[PER];
+    float s1 = 0.f;
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+      const long long c = lane + 32ll * j;
+      xv[j] = c < d4 ? __ldcs(xr + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+      s1 += (xv[j].x + xv[j].y) + (xv[j].z + xv[j].w);
+    }
+    const float mean = warp_sum(s1) / (float)d;
+    float s2 = 0.f;
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+      const long long c = lane + 32ll * j;
+      if (c < d4) {
+        const float a = xv[j].x - mean, b = xv[j].y - mean, e = xv[j].z - mean, f = xv[j].w - mean;
+        s2 += (a * a + b * b) + (e * e + f * f);
+      }
+    }
+    const float rstd = rsqrtf(warp_sum(s2) / (float)d + (float)kLnEps);
+    if (MODE == 0) {
+      float4* orow = (float4*)(o + r * d);
+      uint2* srow = p.shadow ? (uint2*)(p.shadow + r * d) : nullptr;
+#pragma unroll
+      for (int j = 0; j < PER; ++j) {
+        const long long c = lane + 32ll * j;
+        if (c < d4) {
+          const float4 gg = __ldg(g4 + c), bb = __ldg(z4 + c);
+          float4 v;
+          v.x = ((xv[j].x - mean) * rstd) * gg.x + bb.x;
+          v.y = ((xv[j].y - mean) * rstd) * gg.y + bb.y;
+          v.z = ((xv[j].z - mean) * rstd) * gg.z + bb.z;
+          v.w = ((xv[j].w - mean) * rstd) * gg.w + bb.w;
+          orow[c] = v;
+          if (srow) {
+            __nv_bfloat162 w0 = __floats2bfloat162_rn(v.x, v.y), w1 = __floats2bfloat162_rn(v.z, v.w);
+            srow[c] = make_uint2(*(uint32_t*)&w0, *(uint32_t*)&w1);
+          }
+        }
+      }
+    } else {
+      const float4* dyr = (const float4*)(z + r * d);
+      float4 gv[PER];
+      float m1 = 0.f, m2 = 0.f;
+#pragma unroll
+      for (int j = 0; j < PER; ++j) {
+        const long long c = lane + 32ll * j;
+        if (c < d4) {
+          const float4 dy = __ldcs(dyr + c), gg = __ldg(g4 + c);
+          gv[j] = make_float4(dy.x * gg.x, dy.y * gg.y, dy.z * gg.z, dy.w * gg.w);
+          m1 += (gv[j].x + gv[j].y) + (gv[j].z + gv[j].w);
+          m2 += (gv[j].x * ((xv[j].x - mean) * rstd) + gv[j].y * ((xv[j].y - mean) * rstd)) +
+                (gv[j].z * ((xv[j].z - mean) * rstd) + gv[j].w * ((xv[j].w - mean) * rstd));
+        } else {
+          gv[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      }
+      m1 = warp_sum(m1) / (float)d;
+      m2 = warp_sum(m2) / (float)d;
+      float4* orow = (float4*)(o + r * d);
+#pragma unroll
+      for (int j = 0; j < PER; ++j) {
+        const long long c = lane + 32ll * j;
+        if (c < d4) {
+          float4 v;
+          v.x = ((gv[j].x - m1) - ((xv[j].x - mean) * rstd) * m2) * rstd;
+          v.y = ((gv[j].y - m1) - ((xv[j].y - mean) * rstd) * m2) * rstd;
+          v.z = ((gv[j].z - m1) - ((xv[j].z - mean) * rstd) * m2) * rstd;
+          v.w = ((gv[j].w - m1) - ((xv[j].w - mean) * rstd) * m2) * rstd;
+          orow[c] = v;
+        }
+      }
+    }
+  }
+  publish_late(p.out, o);
+}
+
 // ln_dgamma: out[c] = sum over rows of dy * xhat (x, dy = y operand).  Warps take rows; each
 // lane accumulates its columns in double, blocks add into kColReplicas fp64 accumulators,
 // the last block sums the replicas, writes the output and re-zeroes the accumulators.
@@ -650,6 +747,130 @@ __global__ void __launch_bounds__(NT) k_ce_fused(RowParams p) {
   }
 }
 
+// Streaming fused cross-entropy for wide vocabularies (C4: 50257): no shared-memory row --
+// pass 1 reads the row once with 16-byte loads (online max / sum of exponentials per thread,
+// merged across the block), pass 2 re-reads it (L2-resident: a few rows per SM in flight)
+// and writes the gradient 8 columns per thread: the bf16 shadow as one 16-byte store, the
+// fp32 gradient only when a reader needs it.  256 threads per row, several rows per SM, so
+// HBM latency hides behind other rows instead of behind one 200 KB staging copy.
+__device__ __forceinline__ void ce_merge(float& m, float& s, float m2, float s2) {
+  const float mn = fmaxf(m, m2);
+  s = (m == -INFINITY ? 0.f : s * __expf(m - mn)) + (m2 == -INFINITY ? 0.f : s2 * __expf(m2 - mn));
+  m = mn;
+}
+__global__ void __launch_bounds__(256) k_ce_stream(RowParams p) {
+  COEX_PDL_ENTER();
+  stamp(p.ds, SK_CE);
+  __shared__ float red_m[8], red_s[8];
+  const float* lg = res<float>(p.x);
+  const float* ids = res<float>(p.y);
+  float* o = pick_out<float>(p.out, lg, ids);
+  float* lo = pick_out<float>(p.out2, lg, ids);
+  publish_early(p.out, o);
+  count_op(p.ds);
+  const long long V = p.d;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const float invr = (float)(1.0 / (p.scale > 0.0 ? p.scale : (double)p.rows));
+  for (long long r = blockIdx.x; r < p.rows; r += gridDim.x) {
+    const float* row = lg + r * V;
+    // ---- pass 1: online (max, sum exp) over the row; 16-byte aligned body
+    const int head = (int)((16 - ((uintptr_t)row & 15)) & 15) / 4;   // scalars before alignment
+    const long long h = head < V ? head : V;
+    const long long nv = (V - h) / 4;
+    float m = -INFINITY, sm = 0.f;
+    if (tid < h) {
+      const float v = __ldcs(row + tid);
+      m = v;
+      sm = 1.f;
+    }
+    const float4* body = (const float4*)(row + h);
+    long long i = tid;
+    for (; i + 3 * 256 < nv; i += 4 * 256) {           // four 16-byte loads in flight
+      float4 q[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) q[u] = __ldcs(body + i + u * 256);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const float mx = fmaxf(fmaxf(q[u].x, q[u].y), fmaxf(q[u].z, q[u].w));
+        const float s4 = __expf(q[u].x - mx) + __expf(q[u].y - mx) + __expf(q[u].z - mx) + __expf(q[u].w - mx);
+        ce_merge(m, sm, mx, s4);
+      }
+    }
+    for (; i < nv; i += 256) {
+      const float4 q = __ldcs(body + i);
+      const float mx = fmaxf(fmaxf(q.x, q.y), fmaxf(q.z, q.w));
+      ce_merge(m, sm, mx, __expf(q.x - mx) + __expf(q.y - mx) + __expf(q.z - mx) + __expf(q.w - mx));
+    }
+    for (long long k = h + nv * 4 + tid; k < V; k += 256) ce_merge(m, sm, __ldcs(row + k), 1.f);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const float m2 = __shfl_xor_sync(0xffffffffu, m, off), s2 = __shfl_xor_sync(0xffffffffu, sm, off);
+      ce_merge(m, sm, m2, s2);
+    }
+    if (lane == 0) {
+      red_m[wid] = m;
+      red_s[wid] = sm;
+    }
+    __syncthreads();
+    float gm = red_m[0], gs = red_s[0];
+    for (int w = 1; w < 8; ++w) ce_merge(gm, gs, red_m[w], red_s[w]);
+    __syncthreads();                                   // red_* reused by the next row
+    const double f = floor((double)ids[r]);
+    const long long id = f < 0 ? 0 : (f > (double)(V - 1) ? V - 1 : (long long)f);
+    if (tid == 0) p.acc[r] = ((double)logf(gs) + (double)gm) - (double)row[id];
+    // ---- pass 2: gradient, 8 columns per thread (one 16-byte bf16 shadow store)
+    const float inv = 1.f / gs;
+    float* orow = o + r * V;
+    __nv_bfloat16* srow16 = p.shadow ? p.shadow + r * p.spitch : nullptr;
+    const long long pitch = p.shadow ? p.spitch : (V + 7) / 8 * 8;
+    // four 8-column chunks per iteration: all 32 loads issued before any use (L2 latency
+    // overlapped instead of paid once per chunk)
+    for (long long k00 = (long long)tid * 8; k00 < pitch; k00 += 4 * 256 * 8) {
+      float g[4][8];
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const long long k = k00 + q * 2048 + u;
+          g[q][u] = k < V ? __ldg(row + k) : 0.f;
+        }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const long long k0 = k00 + q * 2048;
+        if (k0 >= pitch) break;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const long long k = k0 + u;
+          float v = 0.f;
+          if (k < V) {
+            v = __expf(g[q][u] - gm) * inv;
+            if (k == id) v -= 1.f;
+            v *= invr;
+            if (!p.skip_f32) __stcs(orow + k, v);
+          }
+          g[q][u] = v;
+        }
+        if (srow16) {
+          __nv_bfloat162 w0 = __floats2bfloat162_rn(g[q][0], g[q][1]), w1 = __floats2bfloat162_rn(g[q][2], g[q][3]);
+          __nv_bfloat162 w2 = __floats2bfloat162_rn(g[q][4], g[q][5]), w3 = __floats2bfloat162_rn(g[q][6], g[q][7]);
+          uint4 pk;
+          pk.x = *(uint32_t*)&w0; pk.y = *(uint32_t*)&w1; pk.z = *(uint32_t*)&w2; pk.w = *(uint32_t*)&w3;
+          *(uint4*)(srow16 + k0) = pk;
+        }
+      }
+    }
+  }
+  publish_late(p.out, o);
+  if (!last_block(p.counter)) return;
+  if (threadIdx.x == 0) {
+    double acc = 0.0;
+    for (long long r = 0; r < p.rows; ++r) acc += __ldcg(p.acc + r);
+    lo[0] = (float)(acc / (double)p.rows);
+    *p.counter = 0u;
+    for (int i = 0; i < p.out2.npub; ++i) *p.out2.pub[i] = lo;
+  }
+}
+
 // ------------------------------------------------------------------ wide column sums
 // sum_rows for wide rows (C > 1024, e.g. the position-embedding gradient [B, T*d] or the MLP
 // bias gradient [B*T, 4d]): each thread owns one column and adds a chunk of rows in order;
@@ -678,6 +899,54 @@ __global__ void __launch_bounds__(256) k_colsum_wide(RowParams p) {
     const double acc = (a0 + a1) + (a2 + a3);
     if (gridDim.y == 1) o[c] = (T)acc;
     else atomicAdd(p.acc + c, acc);
+  }
+  if (gridDim.y == 1) publish_late(p.out, o);
+}
+
+// fp32, 4 | d: each thread owns FOUR columns (one 16-byte load per row) and a quarter of the
+// block's rows (4 row lanes x 64 column groups = 256 columns per block), eight loads in
+// flight; fp64 accumulation, the four row lanes combined in shared memory in a fixed order,
+// then written (one row chunk) or added with fp64 atomics into p.acc (k_acc_out pass).
+__global__ void __launch_bounds__(256) k_colsum_v4(RowParams p) {
+  COEX_PDL_ENTER();
+  stamp(p.ds, SK_COLSUM);
+  __shared__ double part[4][64][4];
+  const float* x = res<float>(p.x);
+  float* o = pick_out<float>(p.out, x, nullptr);
+  if (gridDim.y == 1) publish_early(p.out, o);
+  if (blockIdx.y == 0 && blockIdx.x == 0) count_op(p.ds);
+  const int cg = threadIdx.x & 63, rl = threadIdx.x >> 6;
+  const long long c = ((long long)blockIdx.x * 64 + cg) * 4;
+  const long long r0 = p.rows * blockIdx.y / gridDim.y, r1 = p.rows * (blockIdx.y + 1) / gridDim.y;
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  if (c < p.d) {
+    const float* col = x + c;
+    long long r = r0 + rl;
+    for (; r + 28 < r1; r += 32) {                   // eight rows of this lane in flight
+      float4 q[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) q[u] = __ldcs((const float4*)(col + (r + 4 * u) * p.d));
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        a0 += (double)q[u].x; a1 += (double)q[u].y; a2 += (double)q[u].z; a3 += (double)q[u].w;
+      }
+    }
+    for (; r < r1; r += 4) {
+      const float4 q = __ldcs((const float4*)(col + r * p.d));
+      a0 += (double)q.x; a1 += (double)q.y; a2 += (double)q.z; a3 += (double)q.w;
+    }
+  }
+  part[rl][cg][0] = a0;
+  part[rl][cg][1] = a1;
+  part[rl][cg][2] = a2;
+  part[rl][cg][3] = a3;
+  __syncthreads();
+  if (rl == 0 && c < p.d) {
+    for (int k = 0; k < 4; ++k) {
+      const double v = (part[0][cg][k] + part[1][cg][k]) + (part[2][cg][k] + part[3][cg][k]);
+      if (gridDim.y == 1) o[c + k] = (float)v;
+      else atomicAdd(p.acc + c + k, v);
+    }
   }
   if (gridDim.y == 1) publish_late(p.out, o);
 }
