@@ -307,20 +307,65 @@ def graph_roofline(o, be, workload, hbm_peak, tflops_sustained, peak_kind, steps
         be.set_trace(0)
     kinds = {k: {"us_per_step": round(v / 1e3 / steps, 2), "launches_per_step": round(cnt[k] / steps, 2),
                  "share": round(v / total_ns, 4)} for k, v in sorted(agg.items(), key=lambda kv: -kv[1])}
+    method = (f"in-graph %globaltimer stamps over {steps} co-executed steps after the timed region "
+              "(coex_ctx_set_trace); stamp interval charged to the kernel that opened it")
+    if be.precision != "bf16":
+        # f64 parity / fp32 modes: the MatMuls run on the SIMT FMA pipes -- roofline against the
+        # measured FMA peak of that pipe (probes/fma_peak.cu -> profiles/round2_simt_peaks.json)
+        pk = simt_peaks()
+        key = "fp64_fma_tflops" if be.precision == "f64" else "fp32_fma_tflops"
+        m_ns = agg.get("matmul", 0.0)
+        ach = flops / max(m_ns * 1e-9, 1e-12) / 1e12
+        return {"bound": "fp64" if be.precision == "f64" else "fp32", "kernel": "k_matmul_pipe (SIMT MatMul)",
+                "achieved": round(ach, 3), "peak": pk.get(key), "unit": "TFLOP/s",
+                "frac": round(ach / pk[key], 4) if pk.get(key) else None,
+                "peak_source": "measured SIMT FMA peak (profiles/round2_simt_peaks.json, probes/fma_peak.cu)",
+                "algorithmic_flops_per_step": flops // steps, "share_of_step": round(m_ns / total_ns, 4),
+                "device_step_us": round(total_ns / 1e3 / steps, 1), "method": method, "by_kind": kinds}
     g_ns = sum(agg[k] for k in GEMM_KINDS)
     g_launch = sum(cnt[k] for k in TC_LAUNCH_KINDS)
     ach = flops / (g_ns * 1e-9) / 1e12
-    return {"bound": "tensor", "kernel": "k_gemm_tc + k_fa_* (every GEMM / implicit conv / batched GEMM launch "
-                                         "of the step with its split-K reduce, and the flash-attention kernels)",
-            "achieved": round(ach, 2), "peak": tflops_sustained, "unit": "TFLOP/s",
-            "frac": round(ach / tflops_sustained, 4), "peak_source": peak_kind + " (sustained bf16: kernels timed "
-                                                                                 "inside a long step)",
-            "algorithmic_flops_per_step": flops // steps, "launches_per_step": round(g_launch / steps, 1),
-            "avg_launch_us": round(g_ns / 1e3 / max(g_launch, 1), 2),
-            "share_of_step": round(g_ns / total_ns, 4), "device_step_us": round(total_ns / 1e3 / steps, 1),
-            "method": f"in-graph %globaltimer stamps over {steps} co-executed steps after the timed region "
-                      "(coex_ctx_set_trace); stamp interval charged to the kernel that opened it",
-            "by_kind": kinds}
+    # the dominant kernel alone: k_gemm_tc (+ its split-K reduces) over the GEMM FLOPs, the
+    # attention products (run inside k_fa_* when the planner fused them) taken out
+    fa_ns = sum(agg.get(k, 0.0) for k in ("attention fwd", "attention dK/dV", "attention dQ"))
+    a_fl = attn_flops(workload) * steps if fa_ns > 0 else 0
+    mm_ns = agg.get("matmul", 0.0) + agg.get("split-K reduce", 0.0)
+    mm_ach = (flops - a_fl) / max(mm_ns * 1e-9, 1e-12) / 1e12
+    fam = {"kernel": "k_gemm_tc + k_fa_* (every tcgen05 launch: GEMMs with their split-K reduces and the "
+                     "flash-attention kernels)", "achieved": round(ach, 2), "frac": round(ach / tflops_sustained, 4),
+           "share_of_step": round(g_ns / total_ns, 4), "launches_per_step": round(g_launch / steps, 1)}
+    if fa_ns > 0:
+        fam["flash_attention"] = {"achieved": round(a_fl / max(fa_ns * 1e-9, 1e-12) / 1e12, 2),
+                                  "frac": round(a_fl / max(fa_ns * 1e-9, 1e-12) / 1e12 / tflops_sustained, 4),
+                                  "algorithmic_flops_per_step": a_fl // steps,
+                                  "us_per_step": round(fa_ns / 1e3 / steps, 1)}
+    return {"bound": "tensor", "kernel": "k_gemm_tc (every GEMM / implicit conv / batched GEMM launch of the step "
+                                         "with its split-K reduce; attention FLOPs excluded when flash-fused)",
+            "achieved": round(mm_ach, 2), "peak": tflops_sustained, "unit": "TFLOP/s",
+            "frac": round(mm_ach / tflops_sustained, 4), "peak_source": peak_kind + " (sustained bf16: kernels timed "
+                                                                                    "inside a long step)",
+            "algorithmic_flops_per_step": (flops - a_fl) // steps,
+            "launches_per_step": round(cnt.get("matmul", 0) / steps, 1),
+            "avg_launch_us": round(mm_ns / 1e3 / max(cnt.get("matmul", 0), 1), 2),
+            "share_of_step": round(mm_ns / total_ns, 4), "device_step_us": round(total_ns / 1e3 / steps, 1),
+            "tcgen05_family": fam, "method": method, "by_kind": kinds}
+
+
+def simt_peaks() -> dict:
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "round2_simt_peaks.json")
+    try:
+        return json.load(open(path))
+    except OSError:
+        return {}
+
+
+def attn_flops(workload: str) -> int:
+    """Causal attention FLOPs (QK^T and P.V, forward + backward = 3x) of one decoder step."""
+    if workload not in DECODERS:
+        return 0
+    full, _, _ = DECODERS[workload]
+    b, t, d, h, L = full["batch"], full["seq"], full["d"], full["heads"], full["layers"]
+    return 3 * L * 2 * 2 * b * h * (t * (t + 1) // 2) * (d // h)
 
 
 def roofline_c2(be, hbm_peak, tflops_peak, peak_kind, workload="c2"):
