@@ -570,6 +570,9 @@ struct OpSpec {
 // Plan-only kind: batchnorm_dx + bn_dgamma + sum_rows over the same (x, dy) fused into one
 // column-statistics pass (planner.py _bn_bwd_groups); three outputs dx, dgamma, dbeta.
 constexpr int kBnBwdFused = 100;
+// Plan-only kind: layernorm_dx + ln_dgamma + sum_rows over the same (x, dy) in one pass
+// (planner.py _bn_bwd_groups; outputs dx, dgamma, dbeta; fp32 / bf16 modes, 4 | d <= 1024).
+constexpr int kLnBwdFused = 103;
 // Plan-only kind: batchnorm whose apply pass also writes relu / leaky_relu of its output
 // (planner.py _bn_act_pairs; attr dims[0] = the activation's EW code; second output out2).
 constexpr int kBnAct = 101;
@@ -578,6 +581,7 @@ constexpr int kBnAct = 101;
 constexpr int kCeFused = 102;
 bool is_ext_compute(int kind) {
   return (kind >= COEX_CONV2D && kind <= COEX_SUM_ROWS) || kind == kBnBwdFused || kind == kBnAct || kind == kCeFused ||
+         kind == kLnBwdFused ||
          (kind >= COEX_EMBEDDING && kind <= COEX_GLOBAL_AVGPOOL_GRAD && kind != COEX_GELU && kind != COEX_GELU_GRAD) ||
          (kind >= COEX_SLICE && kind <= COEX_SUM_AXIS);
 }
@@ -1752,7 +1756,7 @@ int build_xop_t(coex_ctx* c, const OpSpec& s, Launch* L, int* nL, size_t* ws_byt
     }
     case COEX_EMBEDDING: case COEX_EMBEDDING_DW: case COEX_LAYERNORM: case COEX_LAYERNORM_DX: case COEX_LN_DGAMMA:
     case COEX_BIAS_ADD: case COEX_CAUSAL_SOFTMAX: case COEX_SOFTMAX_GRAD: case COEX_CROSS_ENTROPY:
-    case COEX_CROSS_ENTROPY_GRAD: case COEX_REL_SKEW: case COEX_REL_UNSKEW: case kCeFused: {
+    case COEX_CROSS_ENTROPY_GRAD: case COEX_REL_SKEW: case COEX_REL_UNSKEW: case kCeFused: case kLnBwdFused: {
       RowParams rp{};
       rp.ds = s.ds; rp.x = s.in[0]; rp.y = s.in[1];
       rp.z = s.nin > 2 ? s.in[2] : In{nullptr, nullptr, nullptr};
@@ -1799,6 +1803,24 @@ int build_xop_t(coex_ctx* c, const OpSpec& s, Launch* L, int* nL, size_t* ws_byt
                             : (fw ? (void*)k_layernorm_v4<0, 8> : (void*)k_layernorm_v4<1, 8>);
           }
           L[(*nL)++].set(fn, warp_rows(rp.rows), dim3(256), rp);
+          return COEX_OK;
+        }
+        case kLnBwdFused: {
+          rp.acc = (double*)pv.take((size_t)2 * kColReplicas * d * 8);
+          rp.counter = (unsigned int*)pv.take(16);
+          if (!build) break;
+          if (is_f64(c) || d % 4 || d > 1024) return fail(COEX_INVALID, "fused layernorm backward: fp32 rows, 4 | d <= 1024");
+          rp.d = d; rp.rows = xn / d;
+          LnBwdParams lp{};
+          lp.p = rp;
+          lp.out_g = s.out2;
+          lp.out_b = s.out3;
+          const int per = (int)((d / 4 + 31) / 32);
+          void* fn = per <= 2 ? (void*)k_ln_bwd_v4<2> : per <= 4 ? (void*)k_ln_bwd_v4<4>
+                   : per <= 6 ? (void*)k_ln_bwd_v4<6> : (void*)k_ln_bwd_v4<8>;
+          int64_t blocks = (rp.rows + 7) / 8;
+          if (blocks > kNumSMs * 2) blocks = kNumSMs * 2;
+          L[(*nL)++].set(fn, dim3((unsigned)(blocks < 1 ? 1 : blocks)), dim3(256), lp);
           return COEX_OK;
         }
         case COEX_LN_DGAMMA: {
@@ -3026,7 +3048,7 @@ struct Builder {
         int64_t vbits = next();
         memcpy(&s.value, &vbits, 8);
         read_out(s.out);
-        if (s.kind == kBnBwdFused) {
+        if (s.kind == kBnBwdFused || s.kind == kLnBwdFused) {
           read_out(s.out2);
           read_out(s.out3);
         } else if (s.kind == kBnAct || s.kind == kCeFused) {

@@ -387,6 +387,143 @@ __global__ void __launch_bounds__(256) k_layernorm_v4(RowParams p) {
   publish_late(p.out, o);
 }
 
+// Fused layernorm backward (planner _bn_bwd_groups, plan kind 103): layernorm_dx(x, g, dy),
+// ln_dgamma(x, dy) and sum_rows(dy) over the same (x, dy) in ONE pass -- fp32, 4 | d <= 1024.
+// Warps take rows (16-byte accesses as k_layernorm_v4) and write dx; every lane keeps its
+// columns' sum(dy * xhat) and sum(dy) in registers over its rows, the block combines its
+// warps in shared memory (fp64), adds into kColReplicas fp64 accumulator replicas, and the
+// last block sums the replicas in order, writes dgamma / dbeta and re-zeroes them.
+// (out = dx, out2 = dgamma, out3 = dbeta; p.acc = 2 * kColReplicas * d doubles)
+struct LnBwdParams {
+  RowParams p;
+  Out out_g, out_b;
+};
+template <int PER>
+__global__ void __launch_bounds__(256) k_ln_bwd_v4(const __grid_constant__ LnBwdParams lp) {
+  COEX_PDL_ENTER();
+  const RowParams& p = lp.p;
+  const Out& out_g = lp.out_g;
+  const Out& out_b = lp.out_b;
+  stamp(p.ds, SK_LN);
+  __shared__ double red[2][1024];
+  const float* x = res<float>(p.x);
+  const float* g = res<float>(p.y);
+  const float* z = res<float>(p.z);
+  float* o = pick_out<float>(p.out, x, g);
+  float* og = pick_out<float>(out_g, x, g);
+  float* ob = pick_out<float>(out_b, x, g);
+  publish_early(p.out, o);
+  publish_early(out_g, og);
+  publish_early(out_b, ob);
+  count_op(p.ds);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const long long warps = (long long)gridDim.x * (blockDim.x / 32);
+  const long long d = p.d, d4 = d / 4;
+  const float4* g4 = (const float4*)g;
+  float4 ag[PER], ab[PER];
+#pragma unroll
+  for (int j = 0; j < PER; ++j) {
+    ag[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+    ab[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  for (int i = threadIdx.x; i < 2 * 1024; i += blockDim.x) (&red[0][0])[i] = 0.0;
+  for (long long r = (long long)blockIdx.x * (blockDim.x / 32) + wid; r < p.rows; r += warps) {
+    const float4* xr = (const float4*)(x + r * d);
+    const float4* dyr = (const float4*)(z + r * d);
+    float4 xv[PER], dv[PER];
+    float s1 = 0.f;
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+      const long long c = lane + 32ll * j;
+      xv[j] = c < d4 ? __ldcs(xr + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+      dv[j] = c < d4 ? __ldcs(dyr + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+      s1 += (xv[j].x + xv[j].y) + (xv[j].z + xv[j].w);
+    }
+    const float mean = warp_sum(s1) / (float)d;
+    float s2 = 0.f;
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+      const long long c = lane + 32ll * j;
+      if (c < d4) {
+        xv[j] = make_float4(xv[j].x - mean, xv[j].y - mean, xv[j].z - mean, xv[j].w - mean);
+        s2 += (xv[j].x * xv[j].x + xv[j].y * xv[j].y) + (xv[j].z * xv[j].z + xv[j].w * xv[j].w);
+      }
+    }
+    const float rstd = rsqrtf(warp_sum(s2) / (float)d + (float)kLnEps);
+    float m1 = 0.f, m2 = 0.f;
+    float4 gv[PER];
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+      const long long c = lane + 32ll * j;
+      if (c < d4) {
+        const float4 gg = __ldg(g4 + c);
+        const float4 xh = make_float4(xv[j].x * rstd, xv[j].y * rstd, xv[j].z * rstd, xv[j].w * rstd);
+        xv[j] = xh;
+        gv[j] = make_float4(dv[j].x * gg.x, dv[j].y * gg.y, dv[j].z * gg.z, dv[j].w * gg.w);
+        m1 += (gv[j].x + gv[j].y) + (gv[j].z + gv[j].w);
+        m2 += (gv[j].x * xh.x + gv[j].y * xh.y) + (gv[j].z * xh.z + gv[j].w * xh.w);
+        ag[j].x += dv[j].x * xh.x; ag[j].y += dv[j].y * xh.y; ag[j].z += dv[j].z * xh.z; ag[j].w += dv[j].w * xh.w;
+        ab[j].x += dv[j].x; ab[j].y += dv[j].y; ab[j].z += dv[j].z; ab[j].w += dv[j].w;
+      } else {
+        gv[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+    m1 = warp_sum(m1) / (float)d;
+    m2 = warp_sum(m2) / (float)d;
+    float4* orow = (float4*)(o + r * d);
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+      const long long c = lane + 32ll * j;
+      if (c < d4)
+        orow[c] = make_float4(((gv[j].x - m1) - xv[j].x * m2) * rstd, ((gv[j].y - m1) - xv[j].y * m2) * rstd,
+                              ((gv[j].z - m1) - xv[j].z * m2) * rstd, ((gv[j].w - m1) - xv[j].w * m2) * rstd);
+    }
+  }
+  publish_late(p.out, o);
+  __syncthreads();                                   // red zeroed
+  // warps of the block in order (fixed order per block): fp64 column partials
+  for (int w = 0; w < 8; ++w) {
+    if (wid == w) {
+#pragma unroll
+      for (int j = 0; j < PER; ++j) {
+        const long long c = lane + 32ll * j;
+        if (c < d4) {
+          red[0][4 * c] += ag[j].x; red[0][4 * c + 1] += ag[j].y; red[0][4 * c + 2] += ag[j].z; red[0][4 * c + 3] += ag[j].w;
+          red[1][4 * c] += ab[j].x; red[1][4 * c + 1] += ab[j].y; red[1][4 * c + 2] += ab[j].z; red[1][4 * c + 3] += ab[j].w;
+        }
+      }
+    }
+    __syncthreads();
+  }
+  double* acc = p.acc + (long long)(blockIdx.x % kColReplicas) * 2 * d;
+  for (long long c = threadIdx.x; c < d; c += blockDim.x) {
+    atomicAdd(acc + c, red[0][c]);
+    atomicAdd(acc + d + c, red[1][c]);
+  }
+  if (!last_block(p.counter)) return;
+  const unsigned int nrep = gridDim.x < (unsigned)kColReplicas ? gridDim.x : (unsigned)kColReplicas;
+  for (long long c = threadIdx.x; c < d; c += blockDim.x) {
+    double sg = 0.0, sb = 0.0;
+    for (unsigned int q = 0; q < nrep; ++q) {
+      double* a = p.acc + (long long)q * 2 * d;
+      sg += __ldcg(a + c);
+      sb += __ldcg(a + d + c);
+      a[c] = 0.0;
+      a[d + c] = 0.0;
+    }
+    og[c] = (float)sg;
+    ob[c] = (float)sb;
+  }
+  if (threadIdx.x == 0) *p.counter = 0u;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (out_g.late != nullptr)
+      for (int i = 0; i < out_g.npub; ++i) *out_g.pub[i] = og;
+    if (out_b.late != nullptr)
+      for (int i = 0; i < out_b.npub; ++i) *out_b.pub[i] = ob;
+  }
+}
+
 // ln_dgamma: out[c] = sum over rows of dy * xhat (x, dy = y operand).  Warps take rows; each
 // lane accumulates its columns in double, blocks add into kColReplicas fp64 accumulators,
 // the last block sums the replicas, writes the output and re-zeroes the accumulators.

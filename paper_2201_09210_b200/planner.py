@@ -58,6 +58,7 @@ MAX_XIN = 3
 XOP_BN_BWD = 100          # fused batchnorm_dx + bn_dgamma + sum_rows (csrc COEX_BN_BWD_FUSED)
 XOP_BN_ACT = 101          # batchnorm also writing relu / leaky_relu of its output (csrc kBnAct)
 XOP_CE_FUSED = 102        # cross_entropy + cross_entropy_grad in one pass (csrc kCeFused)
+XOP_LN_BWD = 103          # fused layernorm_dx + ln_dgamma + sum_rows (csrc kLnBwdFused)
 FA_HEAD = 64              # flash attention: head dim and query / key block of the tcgen05 kernels
 FA_BLOCK = 128
 
@@ -448,7 +449,7 @@ class Planner:
                 insts = [ce_of.get(y.node_id, y) if isinstance(y, ExecOp) else y for y in insts
                          if not (isinstance(y, ExecOp) and y.node_id in grads)]
             insts = self._bucket_allreduce(insts, node_buf, shapes)
-            bn_groups, bn_skip = self._bn_bwd_groups(insts) if self.fuse else ({}, set())
+            bn_groups, bn_skip = self._bn_bwd_groups(insts, shapes) if self.fuse else ({}, set())
             if self.fuse:
                 segs = self._segments(insts, shapes, folded)
             else:
@@ -917,7 +918,7 @@ class Planner:
             self._ce_loss[g.node_id] = x
         return out
 
-    def _bn_bwd_groups(self, insts):
+    def _bn_bwd_groups(self, insts, shapes=None):
         """Batch-norm backward triples in one instruction list -- batchnorm_dx(x, g, dy),
         bn_dgamma(x, dy), sum_rows(dy) with identical x / dy bindings -- run as ONE column-
         statistics pass (all three need sum(dy) and sum(dy * xhat)).  The fused op sits at the
@@ -929,13 +930,21 @@ class Planner:
             if isinstance(x, ExecOp):
                 pos.setdefault(x.node_id, i)
         multi_nodes = {n for s_ in self._multi_sets() for n in s_}
-        dxs = [x for x in insts if isinstance(x, ExecOp) and x.kind is OpKind.BATCHNORM_DX]
+        # batch norm (any precision) and -- fp32 storage, 4 | d <= 1024 -- layernorm
+        ln_ok = self.esize == 4 and os.environ.get("COEX_LN_BWD_FUSE", "1") != "0"
+        dxs = [x for x in insts if isinstance(x, ExecOp) and
+               (x.kind is OpKind.BATCHNORM_DX or (ln_ok and x.kind is OpKind.LAYERNORM_DX))]
         used = set()
         for d in dxs:
             xb, gb, dyb = d.inputs
             if xb.fed or dyb.fed or "rows" in d.attrs:     # synchronised (data parallel): unfused
                 continue
-            g = next((y for y in insts if isinstance(y, ExecOp) and y.kind is OpKind.BN_DGAMMA
+            gkind = OpKind.BN_DGAMMA if d.kind is OpKind.BATCHNORM_DX else OpKind.LN_DGAMMA
+            if d.kind is OpKind.LAYERNORM_DX:
+                dd = self._in_shape(xb, shapes)[-1] if shapes is not None else 0
+                if dd % 4 or dd > 1024 or dd == 0:
+                    continue
+            g = next((y for y in insts if isinstance(y, ExecOp) and y.kind is gkind
                       and y.node_id not in used and y.inputs[0] == xb and y.inputs[1] == dyb), None)
             sr = next((y for y in insts if isinstance(y, ExecOp) and y.kind is OpKind.SUM_ROWS
                        and y.node_id not in used and y.inputs[0] == dyb), None)
@@ -964,11 +973,25 @@ class Planner:
                        for m in mem):
                     ok = False
                     break
+            at = insts[hi]
             if not ok:
-                continue
-            last = insts[hi]
-            groups[last.node_id] = (d, g, sr)
-            skip |= ids - {last.node_id}
+                # alternatively at the FIRST member's position (the layernorm's dx feeds a
+                # residual add before ln_dgamma / sum_rows run): every member reads only
+                # (x, g, dy), so that is legal when nothing up to the last member re-produces
+                # x, dy or the first member's own inputs, and there is no control flow between
+                first = insts[lo]
+                srcs = {c for m in mem for b in m.inputs if not b.fed for c in b.cands}
+                ok = all(isinstance(y, (ExecOp, InputFeed)) and
+                         not (isinstance(y, ExecOp) and y.node_id not in ids and y.node_id in srcs)
+                         for y in insts[lo:hi + 1])
+                # the members' own inputs must all exist at the first position
+                ok = ok and all(not b.fed and all(pos.get(c, -1) < lo or c not in pos for c in b.cands)
+                                or b.fed for m in mem for b in m.inputs)
+                if not ok:
+                    continue
+                at = first
+            groups[at.node_id] = (d, g, sr)
+            skip |= ids - {at.node_id}
             used |= ids
         return groups, skip
 
@@ -979,7 +1002,7 @@ class Planner:
         late = _conflicts(cells, pubs[d.node_id] + pubs[g.node_id] + pubs[sr.node_id])
         n_compute[0] += 1
         out_shape = shapes[d.node_id]
-        word = [T_XOP, XOP_BN_BWD, d.node_id, 3] + cells
+        word = [T_XOP, XOP_LN_BWD if d.kind is OpKind.LAYERNORM_DX else XOP_BN_BWD, d.node_id, 3] + cells
         for s_ in in_shapes:
             word += [len(s_)] + _pad(s_)
         word += [len(out_shape)] + _pad(out_shape)

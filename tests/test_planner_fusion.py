@@ -161,3 +161,13 @@ def test_bias_add_fused_into_gemm():
     for m, ba in pl._bias_for.items():
         assert pl.ops[m].kind is OpKind.MATMUL and ba.kind is OpKind.BIAS_ADD
         assert ba.node_id not in pl._emitted and m in pl._emitted
+
+
+def test_layernorm_backward_fused():
+    """C4: layernorm_dx + ln_dgamma + sum_rows over the same (x, dy) become one plan op
+    (kind 103, one pass over x and dy) -- two per layer plus the final layernorm."""
+    from paper_2201_09210_b200.planner import T_XOP, XOP_LN_BWD
+    pl, plan = _planner(gpt2_program(steps=6, **C4_SMALL))
+    w = plan.words
+    n = sum(1 for i in range(len(w) - 1) if w[i] == T_XOP and w[i + 1] == XOP_LN_BWD)
+    assert n == 2 * C4_SMALL["layers"] + 1, n
