@@ -160,6 +160,8 @@ struct TcGemmParams {
   int tri_out, tri_a;
   In bias;                   // has_bias: C[m][n] += bias[n] in the epilogue (fused bias_add)
   int has_bias;
+  In resid;                  // has_resid: C[m][n] += resid[m][n] (fused residual add, [M][N])
+  int has_resid;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -464,6 +466,7 @@ __global__ void __launch_bounds__(TC_THREADS, DUO ? 2 : 1) k_gemm_tc(const __gri
     float* stage = (float*)(tmem_slot + 4) + (warp - 2) * (32 * TC_EPI_LD);
     const bool vec_ok = (p.N % 4) == 0;
     const float* bias = p.has_bias ? res<float>(p.bias) : nullptr;
+    const float* resid = p.has_resid ? res<float>(p.resid) : nullptr;
     int li = 0;
     for (long long it = blockIdx.x; it < items; it += gridDim.x, ++li) {
       int m0, n0, split, kb0, nk;
@@ -504,6 +507,27 @@ __global__ void __launch_bounds__(TC_THREADS, DUO ? 2 : 1) k_gemm_tc(const __gri
         __syncwarp();
         const int sub = lane >> 3, col = (lane & 7) * 4;   // 4 rows x 8 float4 per instruction
         const long long gcol = (long long)n0 + c + col;
+        // fused residual add: the chunk's eight rows of this lane issued together, before any
+        // store (one memory latency per chunk, not one per row)
+        float4 rq[8];
+        if (resid != nullptr) {
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const long long grow = (long long)m0 + lane_base + q * 4 + sub;
+            rq[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (grow < p.M && gcol < p.N) {
+              const float* rr_ = resid + grow * p.N + gcol;
+              if (vec_ok && gcol + 4 <= p.N) {
+                rq[q] = __ldcs((const float4*)rr_);
+              } else {
+                rq[q].x = rr_[0];
+                if (gcol + 1 < p.N) rq[q].y = rr_[1];
+                if (gcol + 2 < p.N) rq[q].z = rr_[2];
+                if (gcol + 3 < p.N) rq[q].w = rr_[3];
+              }
+            }
+          }
+        }
         // fused bias_add: this lane's four columns, loaded once per chunk (not per row)
         float4 bv = make_float4(0.f, 0.f, 0.f, 0.f);
         if (bias != nullptr && gcol < p.N) {
@@ -531,6 +555,9 @@ __global__ void __launch_bounds__(TC_THREADS, DUO ? 2 : 1) k_gemm_tc(const __gri
             }
             float* dst = C + orow * p.N + gcol;
             v.x += bv.x; v.y += bv.y; v.z += bv.z; v.w += bv.w;
+            if (resid != nullptr) {
+              v.x += rq[q].x; v.y += rq[q].y; v.z += rq[q].z; v.w += rq[q].w;
+            }
             if (vec_ok && gcol + 4 <= p.N) {
               *(float4*)dst = v;
             } else {
@@ -584,6 +611,8 @@ struct SplitReduceParams {
   In bias;                   // has_bias: out[m][c] += bias[c] (fused bias_add), ncols = N
   int has_bias;
   long long ncols;
+  In resid;                  // has_resid: out[i] += resid[i] (fused residual add)
+  int has_resid;
 };
 __global__ void __launch_bounds__(256) k_splitk_reduce(SplitReduceParams p) {
   COEX_PDL_ENTER();
@@ -591,6 +620,7 @@ __global__ void __launch_bounds__(256) k_splitk_reduce(SplitReduceParams p) {
   float* o = pick_out<float>(p.out, res<float>(p.a), p.b.cell || p.b.direct ? res<float>(p.b) : nullptr);
   publish_early(p.out, o);
   const float* bias = p.has_bias ? res<float>(p.bias) : nullptr;
+  const float* resid = p.has_resid ? res<float>(p.resid) : nullptr;
   // slices start 16-byte aligned only when 4 | n; the bias's column groups need 4 | ncols
   const long long n4 = ((p.n % 4) == 0 && (bias == nullptr || p.ncols % 4 == 0)) ? p.n / 4 : 0;
   const long long stride = (long long)gridDim.x * blockDim.x;
@@ -604,12 +634,17 @@ __global__ void __launch_bounds__(256) k_splitk_reduce(SplitReduceParams p) {
       const float4 bv = *(const float4*)(bias + (i * 4) % p.ncols);
       acc.x += bv.x; acc.y += bv.y; acc.z += bv.z; acc.w += bv.w;
     }
+    if (resid != nullptr) {
+      const float4 q = ((const float4*)resid)[i];
+      acc.x += q.x; acc.y += q.y; acc.z += q.z; acc.w += q.w;
+    }
     ((float4*)o)[i] = acc;
   }
   for (long long i = n4 * 4 + (long long)blockIdx.x * blockDim.x + threadIdx.x; i < p.n; i += stride) {
     float acc = p.ws[i];
     for (int s = 1; s < p.splits; ++s) acc += p.ws[(long long)s * p.n + i];
     if (bias != nullptr) acc += bias[i % p.ncols];
+    if (resid != nullptr) acc += resid[i];
     o[i] = acc;
   }
   publish_late(p.out, o);

@@ -564,6 +564,8 @@ struct OpSpec {
   void* in_shadow[kMaxIn] = {nullptr, nullptr, nullptr};   // shared bf16 copies of GEMM operands
   int in_conv[kMaxIn] = {1, 1, 1};         // 1: this op converts into in_shadow / scratch first
   int bias = 0;                            // MatMul: in[2] is a [N] bias added by the epilogue
+  In resid{nullptr, nullptr, nullptr};     // MatMul: [M, N] residual added by the epilogue
+  int has_resid = 0;
   DevState* ds = nullptr;
 };
 
@@ -1112,13 +1114,20 @@ bool conv_blocks(int64_t Hg, int64_t Wg, int pix, int* bw, int* bh, int* bn) {
 int tc_gemm_launches(coex_ctx* c, DevState* ds, void* a16, void* b16, int64_t M, int64_t N, int64_t K,
                      const TcPlan& t, In na, In nb, const Out& out, float* raw, float* ws, Launch* L, int* nL,
                      int amode = 0, bool b_mn = false, const TcConv* cv = nullptr,
-                     const CUtensorMap* conv_map = nullptr, int64_t batch = 1, const In* bias = nullptr) {
+                     const CUtensorMap* conv_map = nullptr, int64_t batch = 1, const In* bias = nullptr,
+                     const In* resid = nullptr) {
   TcGemmParams gp;
   memset(&gp, 0, sizeof(gp));
-  if (bias) {
-    if (amode >= 2 || batch > 1) return fail(COEX_INVALID, "GEMM bias epilogue: plain 2-D MatMul only");
-    gp.bias = *bias;
-    gp.has_bias = t.splits > 1 ? 0 : 1;          // split-K: the slice reduction adds it
+  if (bias || resid) {
+    if (amode >= 2 || batch > 1) return fail(COEX_INVALID, "GEMM epilogue fusion: plain 2-D MatMul only");
+    if (bias) {
+      gp.bias = *bias;
+      gp.has_bias = t.splits > 1 ? 0 : 1;        // split-K: the slice reduction adds it
+    }
+    if (resid) {
+      gp.resid = *resid;
+      gp.has_resid = t.splits > 1 ? 0 : 1;
+    }
   }
   int rc = COEX_OK;
   if (amode >= 2) gp.tmA = *conv_map;
@@ -1173,6 +1182,10 @@ int tc_gemm_launches(coex_ctx* c, DevState* ds, void* a16, void* b16, int64_t M,
       r.bias = *bias;
       r.has_bias = 1;
       r.ncols = N;
+    }
+    if (resid) {
+      r.resid = *resid;
+      r.has_resid = 1;
     }
     if (raw != nullptr) {            // reduce into scratch: a private, never-published Out
       r.out = Out{};
@@ -1997,7 +2010,7 @@ int build_launches(coex_ctx* c, const OpSpec& s, Launch* L, int* nL) {
   }
   return tc_gemm_launches(c, s.ds, s.scratch[0], s.scratch[1], M, N, K, tc_plan(M, N, K, s.ws != nullptr), s.in[0],
                           s.in[1], s.out, nullptr, (float*)s.ws, L, nL, a_mn ? 1 : 0, b_mn, nullptr, nullptr, 1,
-                          s.bias ? &s.in[2] : nullptr);
+                          s.bias ? &s.in[2] : nullptr, s.has_resid ? &s.resid : nullptr);
 }
 
 int launch_now(coex_ctx* c, Launch& L) {
@@ -3004,6 +3017,11 @@ struct Builder {
           if (bc != -1) {
             s.in[2] = operand(bc);
             s.bias = 1;
+          }
+          const int64_t rc_ = next();               // fused residual add (GEMM epilogue), -1: none
+          if (rc_ != -1) {
+            s.resid = operand(rc_);
+            s.has_resid = 1;
           }
         }
         read_out(s.out);

@@ -395,6 +395,8 @@ class Planner:
         self.n_ar_buckets = 0                    # asynchronous bucketed all-reduces
         self._bias_for = {}                      # MatMul node -> bias_add fused into its epilogue
         self.n_bias_fused = 0
+        self._resid_for = {}                     # MatMul node -> (add node, residual binding)
+        self.n_resid_fused = 0
         self._ar_lists = []                      # instruction lists after bucketing (inspection)
         self._emitted = set()                    # node ids emitted as their own plan items
         self.chain_lates = 0
@@ -443,6 +445,12 @@ class Planner:
                 insts = [y for y in insts if not (isinstance(y, ExecOp) and y.node_id in gone_b)]
                 self._bias_for.update(bias_of)
                 self.n_bias_fused += len(bias_of)
+            resid_of = self._resid_pairs(insts, shapes) if (self.fuse and self.bf16) else {}
+            if resid_of:                            # residual add folded into its GEMM's epilogue
+                gone_r = {y[0].node_id for y in resid_of.values()}
+                insts = [y for y in insts if not (isinstance(y, ExecOp) and y.node_id in gone_r)]
+                self._resid_for.update(resid_of)
+                self.n_resid_fused += len(resid_of)
             ce_of = self._ce_pairs(insts) if self.fuse else {}
             if ce_of:                               # the gradient moves up to the loss's position
                 grads = {g.node_id for g in ce_of.values()}
@@ -600,7 +608,11 @@ class Planner:
         ba = self._bias_for.get(nid) if k is OpKind.MATMUL else None
         bias_cell = in_cell(ba.inputs[1]) if ba is not None else -1
         out_nid = ba.node_id if ba is not None else nid
-        late = _conflicts(cells + ([bias_cell] if ba is not None else []), pubs[out_nid])
+        rs = self._resid_for.get(nid) if k is OpKind.MATMUL else None
+        resid_cell = in_cell(rs[1]) if rs is not None else -1
+        if rs is not None:
+            out_nid = rs[0].node_id
+        late = _conflicts(cells + [c for c in (bias_cell, resid_cell) if c != -1], pubs[out_nid])
         attr_dims = list(x.attrs.get("perm", ()))
         out_shape = shapes[nid]
         n_compute[0] += 1
@@ -633,11 +645,13 @@ class Planner:
             word += [self.new_buf(2 * max(m, 1) * p4 * 4), self.new_buf(2 * max(nn, 1) * p4 * 4), 1, 1]
         else:
             word += [-1, -1, 0, 0]
-        word += [bias_cell]
+        word += [bias_cell, resid_cell]
         word += out_words(out_nid, late)
         self._invalidate(pubs[out_nid])
-        if ba is not None:
+        if ba is not None or rs is not None:
             self._invalidate(pubs[nid])
+        if ba is not None and rs is not None:
+            self._invalidate(pubs[ba.node_id])
         return [word]
 
     def _bn_act_pairs(self, insts) -> dict:
@@ -886,6 +900,49 @@ class Planner:
             if not c.fed and any(cc == m.node_id for cc in c.cands):
                 continue
             out[m.node_id] = x
+        return out
+
+    def _resid_pairs(self, insts, shapes) -> dict:
+        """add(r, G) / add(G, r) where G is a GEMM's output -- the MatMul itself or its fused
+        bias_add -- read only by the add (C4: the residual stream x + proj(...) and the q / k /
+        v input-gradient sum): the GEMM epilogue adds r (split-K: the slice reduction does) and
+        writes the add's output.  r must have the add's shape and be produced before the
+        MatMul; nothing fetched / merged / pinned / self-dependent.  {matmul: (add, r)}"""
+        if os.environ.get("COEX_RESID_FUSE", "1") == "0":
+            return {}
+        multi_nodes = {n for s_ in self._multi_sets() for n in s_}
+        banned = set(self.sp.fetch_nodes) | multi_nodes | set(self.force_store) | set(self.folded_assigns.values())
+        pos = {x.node_id: i for i, x in enumerate(insts) if isinstance(x, ExecOp)}
+        gemm_of = {x.node_id: x.node_id for x in insts if isinstance(x, ExecOp) and x.kind is OpKind.MATMUL}
+        for m, ba in self._bias_for.items():
+            if m in pos:
+                gemm_of[ba.node_id] = m
+        out = {}
+        for x in insts:
+            if not isinstance(x, ExecOp) or x.kind is not OpKind.ADD or x.node_id in banned or len(x.inputs) != 2:
+                continue
+            if self._node_buf.get(x.node_id, (-1, -1, True))[2] or x.node_id not in self._node_buf:
+                continue
+            if any((not b.fed) and x.node_id in b.cands for b in x.inputs):
+                continue
+            for i in (0, 1):
+                b, r = x.inputs[i], x.inputs[1 - i]
+                if b.fed or len(b.cands) != 1 or r.fed:
+                    continue
+                src = b.cands[0]
+                m = gemm_of.get(src)
+                if m is None or m in out or src in banned or m in banned:
+                    continue
+                if [y.node_id for y in self.consumers.get(src, [])] != [x.node_id]:
+                    continue
+                if tuple(self._in_shape(r, shapes)) != tuple(shapes[x.node_id]) or \
+                        tuple(shapes[src]) != tuple(shapes[x.node_id]):
+                    continue
+                if any(c in (m, src) or (c in pos and pos[c] > pos[m] and c not in self.elided_reads)
+                       for c in r.cands):
+                    continue
+                out[m] = (x, r)
+                break
         return out
 
     def _ce_pairs(self, insts) -> dict:

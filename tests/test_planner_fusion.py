@@ -171,3 +171,13 @@ def test_layernorm_backward_fused():
     w = plan.words
     n = sum(1 for i in range(len(w) - 1) if w[i] == T_XOP and w[i + 1] == XOP_LN_BWD)
     assert n == 2 * C4_SMALL["layers"] + 1, n
+
+
+def test_residual_add_fused_into_gemm():
+    """C4: the residual stream adds (x + proj(...)) and the q / k / v input-gradient sums
+    run in the GEMM epilogues (the add's output written by the GEMM) -- four per layer."""
+    pl, plan = _planner(gpt2_program(steps=6, **C4_SMALL))
+    assert pl.n_resid_fused == 4 * C4_SMALL["layers"]
+    for m, (add, r) in pl._resid_for.items():
+        assert pl.ops[m].kind is OpKind.MATMUL and add.kind is OpKind.ADD
+        assert add.node_id not in pl._emitted
