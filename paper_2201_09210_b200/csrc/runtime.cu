@@ -1109,6 +1109,28 @@ bool conv_blocks(int64_t Hg, int64_t Wg, int pix, int* bw, int* bh, int* bn) {
   return *bw * 2 <= 256 && *bh * 2 <= 256;
 }
 
+// fp32 [slices][rows][N] output of a GEMM: 3-D map {N, rows, slices}, box {32, 32, 1}, 128-byte
+// swizzle (the TMA-store epilogue's boxes); rows / columns past the tensor are clipped
+int make_tmap_c(CUtensorMap* m, void* base, int64_t rows, int64_t N, int64_t slices) {
+  auto enc = tmap_encoder();
+  if (!enc) return fail(COEX_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[3] = {(cuuint64_t)N, (cuuint64_t)rows, (cuuint64_t)slices};
+  cuuint64_t strides[2] = {(cuuint64_t)N * 4, (cuuint64_t)N * 4 * rows};
+  cuuint32_t box[3] = {32, 32, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, base, dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(COEX_CUDA_ERROR, "cuTensorMapEncodeTiled (C) failed: " + std::to_string((int)r));
+  return COEX_OK;
+}
+// COEX_TMA_STORE=1: the TMA-store epilogue (opt-in: measured slower than the LSU epilogue on
+// C4 -- GEMM family 7.88 -> 8.44 ms per step -- and C2, 534 -> 496 it/s)
+bool tma_store_on() {
+  const char* e = getenv("COEX_TMA_STORE");
+  return e && e[0] == '1';
+}
+
 // amode: 0 A K-major [M][pitch(K)], 1 A MN-major [K][pitch(M)], 2 / 3 implicit convolution
 // (A gathered by `conv_map` with geometry `cv`); b_mn: B stored [K][pitch(N)] instead of [N][pitch(K)].
 int tc_gemm_launches(coex_ctx* c, DevState* ds, void* a16, void* b16, int64_t M, int64_t N, int64_t K,
@@ -1151,6 +1173,19 @@ int tc_gemm_launches(coex_ctx* c, DevState* ds, void* a16, void* b16, int64_t M,
   gp.out = out;
   gp.splits = t.splits;
   gp.raw = t.splits > 1 ? ws : raw;
+  // TMA-store epilogue: plain row-major outputs (no conv2d_t scatter, no batch), 4 | N, M > 0
+  if (tma_store_on() && batch == 1 && (amode != 2 || gp.cv.phases == 1) && N % 4 == 0 && M > 0 && N > 0 &&
+      !gp.has_resid && !(resid && t.splits > 1)) {
+    if (gp.raw != nullptr) {
+      rc = make_tmap_c(&gp.tmC0, gp.raw, M, N, t.splits > 1 ? t.splits : 1);
+      gp.tma_c = rc == COEX_OK;
+    } else if (out.buf[0] != nullptr && (!out.pingpong || out.buf[1] != nullptr)) {
+      rc = make_tmap_c(&gp.tmC0, out.buf[0], M, N, 1);
+      if (!rc && out.pingpong) rc = make_tmap_c(&gp.tmC1, out.buf[1], M, N, 1);
+      gp.tma_c = rc == COEX_OK;
+    }
+    if (rc) return rc;
+  }
   Launch& G = L[(*nL)++];
   const int64_t items = ((M + TC_BM - 1) / TC_BM) * ((N + t.bn - 1) / t.bn) * t.splits *
                         (amode == 2 ? gp.cv.phases : 1) * (batch > 1 ? batch : 1);
