@@ -35,15 +35,11 @@ constexpr int TC_EPI_BYTES = 4 * 32 * TC_EPI_LD * 4;   // four epilogue warps x 
 // DUO: a shallow-pipeline variant small enough for two CTAs per SM (BN <= 128; two TMEM
 // accumulator pairs fit the 512 columns) -- for short-K GEMMs on under two waves of tiles,
 // where per-tile latency rather than operand bandwidth bounds the launch.
-// epilogue staging region (1024-aligned, after the ring): the padded row-segment staging of
-// the LSU epilogue, or per epilogue warp two swizzled 32 x 32 fp32 boxes for TMA stores
-constexpr int TC_EPI_REGION = 4 * 2 * 4096;
-static_assert(TC_EPI_BYTES <= TC_EPI_REGION, "epilogue staging");
 template <int BN, bool DUO = false> struct TcCfg {
   static constexpr int STAGES = DUO ? (BN == 64 ? 3 : 2) : BN == 256 ? 4 : BN == 128 ? 6 : 8;
   static constexpr int B_BYTES = BN * TC_BK * 2;
-  static constexpr int SMEM = STAGES * (TC_A_BYTES + B_BYTES) + 1024 /*align*/ + TC_EPI_REGION +
-                               256 /*barriers, tmem slot*/;
+  static constexpr int SMEM = STAGES * (TC_A_BYTES + B_BYTES) + 1024 /*align*/ + 256 /*barriers, tmem slot*/ +
+                               TC_EPI_BYTES;
 };
 constexpr int TC_STAGES = TcCfg<TC_BN>::STAGES;
 constexpr int TC_B_BYTES = TcCfg<TC_BN>::B_BYTES;
@@ -164,13 +160,6 @@ struct TcGemmParams {
   int tri_out, tri_a;
   In bias;                   // has_bias: C[m][n] += bias[n] in the epilogue (fused bias_add)
   int has_bias;
-  In resid;                  // has_resid: C[m][n] += resid[m][n] (fused residual add, [M][N])
-  int has_resid;
-  // tma_c: the epilogue stores 32 x 32 fp32 boxes with cp.async.bulk.tensor from swizzled
-  // shared memory -- tmC0 / tmC1: {N, M, slices} maps over out.buf[0] / out.buf[1] (ping-pong),
-  // or over the raw split-K slices (tmC0, slice = split)
-  CUtensorMap tmC0, tmC1;
-  int tma_c;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -292,8 +281,7 @@ __global__ void __launch_bounds__(TC_THREADS, DUO ? 2 : 1) k_gemm_tc(const __gri
   unsigned char* smem = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   unsigned char* sA = smem;
   unsigned char* sB = smem + STAGES * TC_A_BYTES;
-  unsigned char* epi = sB + STAGES * B_BYTES;       // 1024-aligned (ring sizes are multiples of 8 KB)
-  uint64_t* full = (uint64_t*)(epi + TC_EPI_REGION);
+  uint64_t* full = (uint64_t*)(sB + STAGES * B_BYTES);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;                 // [2]
   uint64_t* tempty = tfull + 2;                     // [2]
@@ -473,13 +461,9 @@ __global__ void __launch_bounds__(TC_THREADS, DUO ? 2 : 1) k_gemm_tc(const __gri
     // TMEM -> registers -> per-warp smem transpose -> coalesced row-segment stores:
     // each 32-column chunk of the warp's 32 rows leaves as 128-byte row segments.
     const int lane_base = 32 * (warp % 4);          // TMEM lanes of this warp
-    float* stage = (float*)epi + (warp - 2) * (32 * TC_EPI_LD);
-    unsigned char* tbox = epi + (warp - 2) * 8192;   // TMA-store boxes of this warp (2 x 4 KB)
-    const CUtensorMap* tmc = (p.raw == nullptr && Cout == (float*)p.out.buf[1] && p.out.pingpong) ? &p.tmC1 : &p.tmC0;
-    int nbox = 0;
+    float* stage = (float*)(tmem_slot + 4) + (warp - 2) * (32 * TC_EPI_LD);
     const bool vec_ok = (p.N % 4) == 0;
     const float* bias = p.has_bias ? res<float>(p.bias) : nullptr;
-    const float* resid = p.has_resid ? res<float>(p.resid) : nullptr;
     int li = 0;
     for (long long it = blockIdx.x; it < items; it += gridDim.x, ++li) {
       int m0, n0, split, kb0, nk;
@@ -510,44 +494,7 @@ __global__ void __launch_bounds__(TC_THREADS, DUO ? 2 : 1) k_gemm_tc(const __gri
           for (int i = 0; i < 32; ++i) r[i] = 0u;
         }
       };
-      // TMA-store epilogue: the lane's row of the 32-column chunk (+ bias) into a 128-B-swizzled
-      // 32 x 32 fp32 box, one bulk tensor store per chunk issued by lane 0; two boxes per warp
-      // so the store of chunk c overlaps the TMEM load / staging of chunk c + 1
-      auto tstore_tma = [&](const uint32_t (&r)[32], int c) {
-        if (n0 + c >= p.N) return;
-        unsigned char* box = tbox + (nbox & 1) * 4096;
-        ++nbox;
-        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-        __syncwarp();
-        float4 bq[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          bq[j] = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (bias != nullptr && n0 + c + 4 * j < p.N) bq[j] = __ldg((const float4*)(bias + n0 + c + 4 * j));
-        }
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const uint32_t addr = smem_u32(box + lane * 128 + ((j ^ (lane & 7)) << 4));
-          asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr),
-                       "f"(__uint_as_float(r[4 * j]) + bq[j].x), "f"(__uint_as_float(r[4 * j + 1]) + bq[j].y),
-                       "f"(__uint_as_float(r[4 * j + 2]) + bq[j].z), "f"(__uint_as_float(r[4 * j + 3]) + bq[j].w)
-                       : "memory");
-        }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncwarp();
-        if (lane == 0) {
-          asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
-                           (uint64_t)tmc),
-                       "r"(smem_u32(box)), "r"(n0 + c), "r"(m0 + lane_base), "r"(split)
-                       : "memory");
-          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-        }
-      };
       auto tstore = [&](const uint32_t (&r)[32], int c) {
-        if (p.tma_c) {
-          tstore_tma(r, c);
-          return;
-        }
         if (n0 + c >= p.N) return;                   // chunk entirely past the last column
         float* srow = stage + lane * TC_EPI_LD;
 #pragma unroll
@@ -557,27 +504,6 @@ __global__ void __launch_bounds__(TC_THREADS, DUO ? 2 : 1) k_gemm_tc(const __gri
         __syncwarp();
         const int sub = lane >> 3, col = (lane & 7) * 4;   // 4 rows x 8 float4 per instruction
         const long long gcol = (long long)n0 + c + col;
-        // fused residual add: the chunk's eight rows of this lane issued together, before any
-        // store (one memory latency per chunk, not one per row)
-        float4 rq[8];
-        if (resid != nullptr) {
-#pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            const long long grow = (long long)m0 + lane_base + q * 4 + sub;
-            rq[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (grow < p.M && gcol < p.N) {
-              const float* rr_ = resid + grow * p.N + gcol;
-              if (vec_ok && gcol + 4 <= p.N) {
-                rq[q] = __ldcs((const float4*)rr_);
-              } else {
-                rq[q].x = rr_[0];
-                if (gcol + 1 < p.N) rq[q].y = rr_[1];
-                if (gcol + 2 < p.N) rq[q].z = rr_[2];
-                if (gcol + 3 < p.N) rq[q].w = rr_[3];
-              }
-            }
-          }
-        }
         // fused bias_add: this lane's four columns, loaded once per chunk (not per row)
         float4 bv = make_float4(0.f, 0.f, 0.f, 0.f);
         if (bias != nullptr && gcol < p.N) {
@@ -605,9 +531,6 @@ __global__ void __launch_bounds__(TC_THREADS, DUO ? 2 : 1) k_gemm_tc(const __gri
             }
             float* dst = C + orow * p.N + gcol;
             v.x += bv.x; v.y += bv.y; v.z += bv.z; v.w += bv.w;
-            if (resid != nullptr) {
-              v.x += rq[q].x; v.y += rq[q].y; v.z += rq[q].z; v.w += rq[q].w;
-            }
             if (vec_ok && gcol + 4 <= p.N) {
               *(float4*)dst = v;
             } else {
@@ -640,7 +563,6 @@ __global__ void __launch_bounds__(TC_THREADS, DUO ? 2 : 1) k_gemm_tc(const __gri
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[a]);       // accumulator buffer free for item li + 2
     }
-    if (p.tma_c && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");   // stores landed
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -662,8 +584,6 @@ struct SplitReduceParams {
   In bias;                   // has_bias: out[m][c] += bias[c] (fused bias_add), ncols = N
   int has_bias;
   long long ncols;
-  In resid;                  // has_resid: out[i] += resid[i] (fused residual add)
-  int has_resid;
 };
 __global__ void __launch_bounds__(256) k_splitk_reduce(SplitReduceParams p) {
   COEX_PDL_ENTER();
@@ -671,7 +591,6 @@ __global__ void __launch_bounds__(256) k_splitk_reduce(SplitReduceParams p) {
   float* o = pick_out<float>(p.out, res<float>(p.a), p.b.cell || p.b.direct ? res<float>(p.b) : nullptr);
   publish_early(p.out, o);
   const float* bias = p.has_bias ? res<float>(p.bias) : nullptr;
-  const float* resid = p.has_resid ? res<float>(p.resid) : nullptr;
   // slices start 16-byte aligned only when 4 | n; the bias's column groups need 4 | ncols
   const long long n4 = ((p.n % 4) == 0 && (bias == nullptr || p.ncols % 4 == 0)) ? p.n / 4 : 0;
   const long long stride = (long long)gridDim.x * blockDim.x;
@@ -685,17 +604,12 @@ __global__ void __launch_bounds__(256) k_splitk_reduce(SplitReduceParams p) {
       const float4 bv = *(const float4*)(bias + (i * 4) % p.ncols);
       acc.x += bv.x; acc.y += bv.y; acc.z += bv.z; acc.w += bv.w;
     }
-    if (resid != nullptr) {
-      const float4 q = ((const float4*)resid)[i];
-      acc.x += q.x; acc.y += q.y; acc.z += q.z; acc.w += q.w;
-    }
     ((float4*)o)[i] = acc;
   }
   for (long long i = n4 * 4 + (long long)blockIdx.x * blockDim.x + threadIdx.x; i < p.n; i += stride) {
     float acc = p.ws[i];
     for (int s = 1; s < p.splits; ++s) acc += p.ws[(long long)s * p.n + i];
     if (bias != nullptr) acc += bias[i % p.ncols];
-    if (resid != nullptr) acc += resid[i];
     o[i] = acc;
   }
   publish_late(p.out, o);

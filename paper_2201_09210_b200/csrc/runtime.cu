@@ -564,8 +564,6 @@ struct OpSpec {
   void* in_shadow[kMaxIn] = {nullptr, nullptr, nullptr};   // shared bf16 copies of GEMM operands
   int in_conv[kMaxIn] = {1, 1, 1};         // 1: this op converts into in_shadow / scratch first
   int bias = 0;                            // MatMul: in[2] is a [N] bias added by the epilogue
-  In resid{nullptr, nullptr, nullptr};     // MatMul: [M, N] residual added by the epilogue
-  int has_resid = 0;
   DevState* ds = nullptr;
 };
 
@@ -1109,47 +1107,18 @@ bool conv_blocks(int64_t Hg, int64_t Wg, int pix, int* bw, int* bh, int* bn) {
   return *bw * 2 <= 256 && *bh * 2 <= 256;
 }
 
-// fp32 [slices][rows][N] output of a GEMM: 3-D map {N, rows, slices}, box {32, 32, 1}, 128-byte
-// swizzle (the TMA-store epilogue's boxes); rows / columns past the tensor are clipped
-int make_tmap_c(CUtensorMap* m, void* base, int64_t rows, int64_t N, int64_t slices) {
-  auto enc = tmap_encoder();
-  if (!enc) return fail(COEX_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable");
-  cuuint64_t dims[3] = {(cuuint64_t)N, (cuuint64_t)rows, (cuuint64_t)slices};
-  cuuint64_t strides[2] = {(cuuint64_t)N * 4, (cuuint64_t)N * 4 * rows};
-  cuuint32_t box[3] = {32, 32, 1};
-  cuuint32_t es[3] = {1, 1, 1};
-  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, base, dims, strides, box, es,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return fail(COEX_CUDA_ERROR, "cuTensorMapEncodeTiled (C) failed: " + std::to_string((int)r));
-  return COEX_OK;
-}
-// COEX_TMA_STORE=1: the TMA-store epilogue (opt-in: measured slower than the LSU epilogue on
-// C4 -- GEMM family 7.88 -> 8.44 ms per step -- and C2, 534 -> 496 it/s)
-bool tma_store_on() {
-  const char* e = getenv("COEX_TMA_STORE");
-  return e && e[0] == '1';
-}
-
 // amode: 0 A K-major [M][pitch(K)], 1 A MN-major [K][pitch(M)], 2 / 3 implicit convolution
 // (A gathered by `conv_map` with geometry `cv`); b_mn: B stored [K][pitch(N)] instead of [N][pitch(K)].
 int tc_gemm_launches(coex_ctx* c, DevState* ds, void* a16, void* b16, int64_t M, int64_t N, int64_t K,
                      const TcPlan& t, In na, In nb, const Out& out, float* raw, float* ws, Launch* L, int* nL,
                      int amode = 0, bool b_mn = false, const TcConv* cv = nullptr,
-                     const CUtensorMap* conv_map = nullptr, int64_t batch = 1, const In* bias = nullptr,
-                     const In* resid = nullptr) {
+                     const CUtensorMap* conv_map = nullptr, int64_t batch = 1, const In* bias = nullptr) {
   TcGemmParams gp;
   memset(&gp, 0, sizeof(gp));
-  if (bias || resid) {
-    if (amode >= 2 || batch > 1) return fail(COEX_INVALID, "GEMM epilogue fusion: plain 2-D MatMul only");
-    if (bias) {
-      gp.bias = *bias;
-      gp.has_bias = t.splits > 1 ? 0 : 1;        // split-K: the slice reduction adds it
-    }
-    if (resid) {
-      gp.resid = *resid;
-      gp.has_resid = t.splits > 1 ? 0 : 1;
-    }
+  if (bias) {
+    if (amode >= 2 || batch > 1) return fail(COEX_INVALID, "GEMM bias epilogue: plain 2-D MatMul only");
+    gp.bias = *bias;
+    gp.has_bias = t.splits > 1 ? 0 : 1;          // split-K: the slice reduction adds it
   }
   int rc = COEX_OK;
   if (amode >= 2) gp.tmA = *conv_map;
@@ -1173,19 +1142,6 @@ int tc_gemm_launches(coex_ctx* c, DevState* ds, void* a16, void* b16, int64_t M,
   gp.out = out;
   gp.splits = t.splits;
   gp.raw = t.splits > 1 ? ws : raw;
-  // TMA-store epilogue: plain row-major outputs (no conv2d_t scatter, no batch), 4 | N, M > 0
-  if (tma_store_on() && batch == 1 && (amode != 2 || gp.cv.phases == 1) && N % 4 == 0 && M > 0 && N > 0 &&
-      !gp.has_resid && !(resid && t.splits > 1)) {
-    if (gp.raw != nullptr) {
-      rc = make_tmap_c(&gp.tmC0, gp.raw, M, N, t.splits > 1 ? t.splits : 1);
-      gp.tma_c = rc == COEX_OK;
-    } else if (out.buf[0] != nullptr && (!out.pingpong || out.buf[1] != nullptr)) {
-      rc = make_tmap_c(&gp.tmC0, out.buf[0], M, N, 1);
-      if (!rc && out.pingpong) rc = make_tmap_c(&gp.tmC1, out.buf[1], M, N, 1);
-      gp.tma_c = rc == COEX_OK;
-    }
-    if (rc) return rc;
-  }
   Launch& G = L[(*nL)++];
   const int64_t items = ((M + TC_BM - 1) / TC_BM) * ((N + t.bn - 1) / t.bn) * t.splits *
                         (amode == 2 ? gp.cv.phases : 1) * (batch > 1 ? batch : 1);
@@ -1218,10 +1174,7 @@ int tc_gemm_launches(coex_ctx* c, DevState* ds, void* a16, void* b16, int64_t M,
       r.has_bias = 1;
       r.ncols = N;
     }
-    if (resid) {
-      r.resid = *resid;
-      r.has_resid = 1;
-    }
+
     if (raw != nullptr) {            // reduce into scratch: a private, never-published Out
       r.out = Out{};
       r.out.buf[0] = raw;
@@ -2045,7 +1998,7 @@ int build_launches(coex_ctx* c, const OpSpec& s, Launch* L, int* nL) {
   }
   return tc_gemm_launches(c, s.ds, s.scratch[0], s.scratch[1], M, N, K, tc_plan(M, N, K, s.ws != nullptr), s.in[0],
                           s.in[1], s.out, nullptr, (float*)s.ws, L, nL, a_mn ? 1 : 0, b_mn, nullptr, nullptr, 1,
-                          s.bias ? &s.in[2] : nullptr, s.has_resid ? &s.resid : nullptr);
+                          s.bias ? &s.in[2] : nullptr);
 }
 
 int launch_now(coex_ctx* c, Launch& L) {
@@ -3053,11 +3006,7 @@ struct Builder {
             s.in[2] = operand(bc);
             s.bias = 1;
           }
-          const int64_t rc_ = next();               // fused residual add (GEMM epilogue), -1: none
-          if (rc_ != -1) {
-            s.resid = operand(rc_);
-            s.has_resid = 1;
-          }
+
         }
         read_out(s.out);
         s.nin = 2;
@@ -3428,14 +3377,24 @@ int coex_prog_build(coex_ctx* c, const int64_t* plan, int64_t nwords, const doub
     const int64_t nbufs = b.next();
     std::vector<int64_t> sizes(nbufs);
     size_t total = 0;
+    // a negative entry is a VIEW: -(1 + parent << 40 + byte offset) into an earlier buffer
+    // (planner _arm_views: arm-exclusive activations of a SwitchCase share one region)
     for (int64_t i = 0; i < nbufs; ++i) {
       sizes[i] = b.next();
-      total += ((size_t)sizes[i] + 255) & ~(size_t)255;
+      if (sizes[i] >= 0) total += ((size_t)sizes[i] + 255) & ~(size_t)255;
     }
     p->arena_bytes = total;
     if (total) CK(cudaMalloc(&p->arena, total));
     size_t off = 0;
     for (int64_t i = 0; i < nbufs; ++i) {
+      if (sizes[i] < 0) {
+        const int64_t v = -sizes[i] - 1, parent = v >> 40, boff = v & ((1ll << 40) - 1);
+        if (parent < 0 || parent >= i || sizes[parent] < 0 || boff >= sizes[parent])
+          throw std::runtime_error("bad buffer view");
+        b.bufs.push_back((char*)b.bufs[parent] + boff);
+        sizes[i] = sizes[parent] - boff;            // bound for the spare below
+        continue;
+      }
       b.bufs.push_back(p->arena + off);
       off += ((size_t)sizes[i] + 255) & ~(size_t)255;
     }

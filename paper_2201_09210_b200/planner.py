@@ -250,6 +250,11 @@ class Planner:
 
         self.new_buf = new_buf
 
+        def new_view(parent, offset):
+            """a buffer that is a byte range of another (plan word: -(1 + parent<<40 + offset))"""
+            bufs.append(-(1 + (parent << 40) + int(offset)))
+            return len(bufs) - 1
+
         cell_init: list = []
 
         def new_cell(buf_idx=-1):
@@ -269,12 +274,13 @@ class Planner:
                 ar_order.append(x.node_id)
         self._ar_pos = {nid: i for i, nid in enumerate(ar_order)}
         ar_set = set(ar_order)
+        arm_view = self._arm_views(consumers, multi, folded, shapes, new_buf, new_view)
         for nid in ar_order + [n for n in ops if n not in ar_set]:
             x = ops[nid]
             n = shape_size(shapes[nid])
             if x.kind in COMPUTE and nid not in folded and nid not in self.index_nodes:
                 self_dep = any((not b.fed) and nid in b.cands for b in x.inputs)
-                b0 = new_buf(n * self.esize)
+                b0 = arm_view[nid] if nid in arm_view else new_buf(n * self.esize)
                 b1 = new_buf(n * self.esize) if self_dep else -1
                 node_buf[nid] = (b0, b1, self_dep)
                 vcell[nid] = new_cell(b0)
@@ -395,8 +401,6 @@ class Planner:
         self.n_ar_buckets = 0                    # asynchronous bucketed all-reduces
         self._bias_for = {}                      # MatMul node -> bias_add fused into its epilogue
         self.n_bias_fused = 0
-        self._resid_for = {}                     # MatMul node -> (add node, residual binding)
-        self.n_resid_fused = 0
         self._ar_lists = []                      # instruction lists after bucketing (inspection)
         self._emitted = set()                    # node ids emitted as their own plan items
         self.chain_lates = 0
@@ -445,12 +449,6 @@ class Planner:
                 insts = [y for y in insts if not (isinstance(y, ExecOp) and y.node_id in gone_b)]
                 self._bias_for.update(bias_of)
                 self.n_bias_fused += len(bias_of)
-            resid_of = self._resid_pairs(insts, shapes) if (self.fuse and self.bf16) else {}
-            if resid_of:                            # residual add folded into its GEMM's epilogue
-                gone_r = {y[0].node_id for y in resid_of.values()}
-                insts = [y for y in insts if not (isinstance(y, ExecOp) and y.node_id in gone_r)]
-                self._resid_for.update(resid_of)
-                self.n_resid_fused += len(resid_of)
             ce_of = self._ce_pairs(insts) if self.fuse else {}
             if ce_of:                               # the gradient moves up to the loss's position
                 grads = {g.node_id for g in ce_of.values()}
@@ -608,11 +606,7 @@ class Planner:
         ba = self._bias_for.get(nid) if k is OpKind.MATMUL else None
         bias_cell = in_cell(ba.inputs[1]) if ba is not None else -1
         out_nid = ba.node_id if ba is not None else nid
-        rs = self._resid_for.get(nid) if k is OpKind.MATMUL else None
-        resid_cell = in_cell(rs[1]) if rs is not None else -1
-        if rs is not None:
-            out_nid = rs[0].node_id
-        late = _conflicts(cells + [c for c in (bias_cell, resid_cell) if c != -1], pubs[out_nid])
+        late = _conflicts(cells + ([bias_cell] if ba is not None else []), pubs[out_nid])
         attr_dims = list(x.attrs.get("perm", ()))
         out_shape = shapes[nid]
         n_compute[0] += 1
@@ -645,13 +639,11 @@ class Planner:
             word += [self.new_buf(2 * max(m, 1) * p4 * 4), self.new_buf(2 * max(nn, 1) * p4 * 4), 1, 1]
         else:
             word += [-1, -1, 0, 0]
-        word += [bias_cell, resid_cell]
+        word += [bias_cell]
         word += out_words(out_nid, late)
         self._invalidate(pubs[out_nid])
-        if ba is not None or rs is not None:
+        if ba is not None:
             self._invalidate(pubs[nid])
-        if ba is not None and rs is not None:
-            self._invalidate(pubs[ba.node_id])
         return [word]
 
     def _bn_act_pairs(self, insts) -> dict:
@@ -900,53 +892,6 @@ class Planner:
             if not c.fed and any(cc == m.node_id for cc in c.cands):
                 continue
             out[m.node_id] = x
-        return out
-
-    def _resid_pairs(self, insts, shapes) -> dict:
-        """add(r, G) / add(G, r) where G is a GEMM's output -- the MatMul itself or its fused
-        bias_add -- read only by the add (C4: the residual stream x + proj(...) and the q / k /
-        v input-gradient sum): the GEMM epilogue adds r (split-K: the slice reduction does) and
-        writes the add's output.  r must have the add's shape and be produced before the
-        MatMul; nothing fetched / merged / pinned / self-dependent.  {matmul: (add, r)}
-
-        Opt-in (COEX_RESID_FUSE=1): measured on C4 it costs more than it saves -- the short-K
-        projections are epilogue-bound and the residual read lengthens every tile's epilogue
-        (GEMM family +2.1 ms vs -0.6 ms of add passes per step, 48.7 -> 45.2 it/s)."""
-        if os.environ.get("COEX_RESID_FUSE", "0") != "1":
-            return {}
-        multi_nodes = {n for s_ in self._multi_sets() for n in s_}
-        banned = set(self.sp.fetch_nodes) | multi_nodes | set(self.force_store) | set(self.folded_assigns.values())
-        pos = {x.node_id: i for i, x in enumerate(insts) if isinstance(x, ExecOp)}
-        gemm_of = {x.node_id: x.node_id for x in insts if isinstance(x, ExecOp) and x.kind is OpKind.MATMUL}
-        for m, ba in self._bias_for.items():
-            if m in pos:
-                gemm_of[ba.node_id] = m
-        out = {}
-        for x in insts:
-            if not isinstance(x, ExecOp) or x.kind is not OpKind.ADD or x.node_id in banned or len(x.inputs) != 2:
-                continue
-            if self._node_buf.get(x.node_id, (-1, -1, True))[2] or x.node_id not in self._node_buf:
-                continue
-            if any((not b.fed) and x.node_id in b.cands for b in x.inputs):
-                continue
-            for i in (0, 1):
-                b, r = x.inputs[i], x.inputs[1 - i]
-                if b.fed or len(b.cands) != 1 or r.fed:
-                    continue
-                src = b.cands[0]
-                m = gemm_of.get(src)
-                if m is None or m in out or src in banned or m in banned:
-                    continue
-                if [y.node_id for y in self.consumers.get(src, [])] != [x.node_id]:
-                    continue
-                if tuple(self._in_shape(r, shapes)) != tuple(shapes[x.node_id]) or \
-                        tuple(shapes[src]) != tuple(shapes[x.node_id]):
-                    continue
-                if any(c in (m, src) or (c in pos and pos[c] > pos[m] and c not in self.elided_reads)
-                       for c in r.cands):
-                    continue
-                out[m] = (x, r)
-                break
         return out
 
     def _ce_pairs(self, insts) -> dict:
@@ -1302,6 +1247,72 @@ class Planner:
             segs.append(("inst", x))
         flush()
         return segs
+
+    def _arm_views(self, consumers, multi, folded, shapes, new_buf, new_view) -> dict:
+        """Arm-exclusive node buffers: the cases of a SwitchCase never run in the same pass, so
+        a node produced inside one case and read only inside that case (an arm-local
+        activation) can live in memory the other cases' arm-local nodes use too.  Per
+        SwitchCase one region of max-over-cases bytes; each case lays its local nodes out from
+        the region's start (256-byte slots).  Never aliased: fetched, merged (multi-candidate),
+        pinned (force_store), variable-published, self-dependent or folded nodes, constants,
+        nodes that occur in several cases.  C3 (four SDPoint arms) and C2 (D / G steps).
+        COEX_ARM_ALIAS=0 keeps one buffer per node.  Returns {node: view buffer index}."""
+        if os.environ.get("COEX_ARM_ALIAS", "1") == "0":
+            return {}
+        ops = self.ops
+        multi_nodes = {n for s_ in multi for n in s_}
+        banned = set(self.sp.fetch_nodes) | multi_nodes | set(self.force_store) | \
+            set(self.folded_assigns.values()) | set(self.index_nodes)
+        out = {}
+        self.arm_alias_bytes = [0, 0]          # (bytes without aliasing, region bytes)
+
+        def local_nodes(case, others_count):
+            inside = {y.node_id for y in walk(case) if isinstance(y, ExecOp)}
+            loc = []
+            for nid in sorted(inside):
+                x = ops.get(nid)
+                if x is None or others_count[nid] > 1 or nid in banned or nid in out:
+                    continue
+                if x.kind not in COMPUTE or nid in folded:
+                    continue
+                if any((not b.fed) and nid in b.cands for b in x.inputs):
+                    continue
+                if not all(c.node_id in inside for c in consumers.get(nid, [])):
+                    continue
+                loc.append(nid)
+            return loc
+
+        def visit(insts):
+            for x in insts:
+                if isinstance(x, SwitchCase):
+                    from collections import Counter
+                    cnt = Counter(y.node_id for c in x.cases for y in walk(c) if isinstance(y, ExecOp))
+                    layouts, size = [], 0
+                    for c in x.cases:
+                        off, lay = 0, []
+                        for nid in local_nodes(c, cnt):
+                            nbytes = max(shape_size(shapes[nid]) * self.esize, 16)
+                            lay.append((nid, off))
+                            off += (nbytes + 255) // 256 * 256
+                            self.arm_alias_bytes[0] += nbytes
+                        layouts.append(lay)
+                        size = max(size, off)
+                    if size > 0 and sum(len(l) for l in layouts) > 0:
+                        region = new_buf(size)
+                        self.arm_alias_bytes[1] += size
+                        for lay in layouts:
+                            for nid, off in lay:
+                                out[nid] = new_view(region, off)
+                    for c in x.cases:                # nested switches: their own regions
+                        visit(c)
+                elif isinstance(x, While):
+                    visit(x.body)
+                elif isinstance(x, UnrolledLoop):
+                    for b in x.bodies:
+                        visit(b)
+
+        visit(self.sp.body)
+        return out
 
     def _bucket_allreduce(self, insts, node_buf, shapes) -> list:
         """Data-parallel gradient all-reduces (dp.py AllReduce items) of one instruction list,

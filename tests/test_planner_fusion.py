@@ -173,13 +173,25 @@ def test_layernorm_backward_fused():
     assert n == 2 * C4_SMALL["layers"] + 1, n
 
 
-def test_residual_add_fused_into_gemm(monkeypatch):
-    """C4 with COEX_RESID_FUSE=1 (opt-in, slower on C4): the residual stream adds
-    (x + proj(...)) and the q / k / v input-gradient sums run in the GEMM epilogues (the
-    add's output written by the GEMM) -- four per layer."""
-    monkeypatch.setenv("COEX_RESID_FUSE", "1")
-    pl, plan = _planner(gpt2_program(steps=6, **C4_SMALL))
-    assert pl.n_resid_fused == 4 * C4_SMALL["layers"]
-    for m, (add, r) in pl._resid_for.items():
-        assert pl.ops[m].kind is OpKind.MATMUL and add.kind is OpKind.ADD
-        assert add.node_id not in pl._emitted
+def test_arm_exclusive_buffers(dcgan):
+    """C2's D / G SwitchCase: activations produced and read inside one case share a region
+    with the other case's (cases never run in the same pass); views are well-formed and
+    nothing fetched / merged / pinned is aliased."""
+    from paper_2201_09210_b200.planner import walk
+    from paper_2201_09210_b200.graph_gen import SwitchCase
+    pl, plan = dcgan
+    w = plan.words
+    nb = w[2]
+    sizes = w[3:3 + nb]
+    views = [i for i, x in enumerate(sizes) if x < 0]
+    assert views, "no arm-exclusive views"
+    unaliased, region = pl.arm_alias_bytes
+    assert 0 < region < unaliased
+    for i in views:
+        v = -sizes[i] - 1
+        parent, off = v >> 40, v & ((1 << 40) - 1)
+        assert 0 <= parent < i and sizes[parent] >= 0 and off < sizes[parent]
+    aliased = {n for n, (b0, _, _) in pl._node_buf.items() if b0 in set(views)}
+    assert not aliased & set(pl.sp.fetch_nodes)
+    sw = [x for x in walk(pl.sp.body) if isinstance(x, SwitchCase)]
+    assert sw
