@@ -351,6 +351,19 @@ def graph_roofline(o, be, workload, hbm_peak, tflops_sustained, peak_kind, steps
             "tcgen05_family": fam, "method": method, "by_kind": kinds}
 
 
+def graph_memory(o) -> dict:
+    """Device bytes of the pass graphs' arenas (node buffers, shared scratch) per shape
+    specialisation -- planner._arm_views lets the cases of a SwitchCase share activation
+    memory (C2 D / G, C3 SDPoint arms)."""
+    try:
+        prog = o.compiled
+        arenas = [prog.info(h)["arena_bytes"] for h, _ in prog.graphs.values()]
+        return {"graphs": len(arenas), "arena_bytes_max": max(arenas) if arenas else 0,
+                "arena_bytes_total": sum(arenas)}
+    except Exception as e:                       # noqa: BLE001 -- diagnostics only
+        return {"error": repr(e)}
+
+
 def simt_peaks() -> dict:
     path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "round2_simt_peaks.json")
     try:
@@ -654,14 +667,14 @@ def run_b200(args):
              "counters": list(st.counters())}
     clocks = clk.summary()
     roof = tgemm = None
+    mem = graph_memory(o)
     if rank == 0:                      # kernel evidence while this context is alive
-        if args.workload in ("c2", "c3", "c4", "c5"):
-            roof = graph_roofline(o, be, args.workload, hbm, load_sustained(tfl), peak_kind)
-            roof["traffic"] = TRAFFIC.get(args.workload)
-            if args.eager_families:
-                roof["eager_families"] = roofline_c2(be, hbm, tfl, peak_kind, args.workload)
-        else:
-            roof = roofline(be, hbm, tfl, peak_kind)
+        roof = graph_roofline(o, be, args.workload, hbm, load_sustained(tfl), peak_kind)
+        roof["traffic"] = TRAFFIC.get(args.workload)
+        if args.eager_families and args.workload != "c1":
+            roof["eager_families"] = roofline_c2(be, hbm, tfl, peak_kind, args.workload)
+        if args.workload == "c1":
+            roof["eager_hbm"] = roofline(be, hbm, tfl, peak_kind)
             tgemm = tensor_gemm(tfl, peak_kind) if not args.no_tensor_gemm else None
     del o
     be.close()                         # free the synthetic-input pass graph before the e2e one
@@ -712,6 +725,7 @@ def run_b200(args):
             "gpu_launches": launches,
             "clocks": clocks,
             "stats": stats,
+            "memory": mem,
         }
         if tgemm is not None:
             line["tensor_gemm"] = tgemm
