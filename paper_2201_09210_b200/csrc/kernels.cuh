@@ -11,6 +11,7 @@
 // each kernel cites the lines it reproduces.
 #pragma once
 #include <cuda_runtime.h>
+#include <cuda_bf16.h>
 #include <stdint.h>
 
 namespace coex {
@@ -283,6 +284,8 @@ struct EwParams {
   int a_scalar, b_scalar;   // broadcast rank-0 operand
   long long n;
   Out out;
+  __nv_bfloat16* shadow;    // bf16 mode: also write the bf16 copy later GEMMs read (GELU / GELU_GRAD)
+  int skip_f32;             // the fp32 output has no reader (only GEMMs, through the shadow)
 };
 
 template <typename T>
@@ -312,7 +315,11 @@ __global__ void __launch_bounds__(256) k_elementwise(EwParams p) {
         r.y = ew_apply(p.op, x4.y, y4.y);
         r.z = ew_apply(p.op, x4.z, y4.z);
         r.w = ew_apply(p.op, x4.w, y4.w);
-        ((float4*)o)[i] = r;
+        if (!p.skip_f32) ((float4*)o)[i] = r;
+        if (p.shadow) {
+          __nv_bfloat162 h0 = __floats2bfloat162_rn(r.x, r.y), h1 = __floats2bfloat162_rn(r.z, r.w);
+          ((uint2*)p.shadow)[i] = make_uint2(*(uint32_t*)&h0, *(uint32_t*)&h1);
+        }
       }
       publish_late(p.out, o);
       return;
@@ -321,7 +328,9 @@ __global__ void __launch_bounds__(256) k_elementwise(EwParams p) {
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
     T x = p.a_scalar ? as : a[i];
     T y = (b == nullptr) ? T(0) : (p.b_scalar ? bs : b[i]);
-    o[i] = ew_apply(p.op, x, y);
+    const T v = ew_apply(p.op, x, y);
+    if (!p.skip_f32) o[i] = v;
+    if (p.shadow) p.shadow[i] = __float2bfloat16_rn((float)v);
   }
   publish_late(p.out, o);
 }

@@ -564,6 +564,7 @@ struct OpSpec {
   void* in_shadow[kMaxIn] = {nullptr, nullptr, nullptr};   // shared bf16 copies of GEMM operands
   int in_conv[kMaxIn] = {1, 1, 1};         // 1: this op converts into in_shadow / scratch first
   int bias = 0;                            // MatMul: in[2] is a [N] bias added by the epilogue
+  int skip_f32 = 0;                        // elementwise with a shadow: the fp32 output has no reader
   DevState* ds = nullptr;
 };
 
@@ -717,6 +718,8 @@ int build_launch_t(coex_ctx* c, const OpSpec& s, Launch* L) {
       p.b_scalar = binary && s.in_ndim[1] == 0 && n != 1;
       p.n = n;
       p.out = s.out;
+      p.shadow = (__nv_bfloat16*)s.shadow;
+      p.skip_f32 = s.shadow ? s.skip_f32 : 0;
       L->set((void*)k_elementwise<T>, grid_for(sizeof(T) == 4 && n % 4 == 0 ? n / 4 : n), dim3(256), p);
       return COEX_OK;
     }
@@ -3006,6 +3009,8 @@ struct Builder {
             s.in[2] = operand(bc);
             s.bias = 1;
           }
+          s.shadow = buf(next());                   // elementwise: bf16 GEMM-operand copy, -1: none
+          s.skip_f32 = (int)next();
 
         }
         read_out(s.out);

@@ -312,6 +312,13 @@ class Planner:
                     shp = shapes[nid]
                     self.shadow[nid] = new_buf(shape_size(shp[:-1]) * ((shp[-1] + 7) // 8 * 8) * 2)
                     continue
+                if x.kind in (OpKind.GELU, OpKind.GELU_GRAD) and nid in node_buf and not node_buf[nid][2] and \
+                        shapes[nid] and shapes[nid][-1] % 8 == 0 and not any(nid in s_ for s_ in multi) and \
+                        gemm_use(nid) and os.environ.get("COEX_EW_SHADOW", "1") != "0":
+                    # the elementwise pass writes the bf16 copy its GEMM readers use (and skips
+                    # the fp32 output when only GEMMs read it, _exec)
+                    self.shadow[nid] = new_buf(shape_size(shapes[nid]) * 2)
+                    continue
                 if x.kind not in (OpKind.CAUSAL_SOFTMAX, OpKind.SOFTMAX_GRAD, OpKind.LAYERNORM) or nid not in node_buf:
                     continue
                 if node_buf[nid][2] or shapes[nid][-1] % 8 or any(nid in s_ for s_ in multi):
@@ -639,7 +646,8 @@ class Planner:
             word += [self.new_buf(2 * max(m, 1) * p4 * 4), self.new_buf(2 * max(nn, 1) * p4 * 4), 1, 1]
         else:
             word += [-1, -1, 0, 0]
-        word += [bias_cell]
+        sh = self.shadow.get(nid, -1) if k in (OpKind.GELU, OpKind.GELU_GRAD) else -1
+        word += [bias_cell, sh, int(sh != -1 and self._gemm_only(nid))]
         word += out_words(out_nid, late)
         self._invalidate(pubs[out_nid])
         if ba is not None:
