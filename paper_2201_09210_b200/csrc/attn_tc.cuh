@@ -56,6 +56,7 @@ struct FaParams {
   Out out, out2, out3;       // fwd: O | bwd_kv: dK (out2), dV (out3) | bwd_q: dQ (out)
   In pa, pb;                 // ping-pong output choice of the node being written
   long long* dbg;            // non-null (COEX_FA_DBG, eager only): CTA 0 event clocks
+  __nv_bfloat16* sh[3];      // bf16 copies for GEMM-only readers (fwd: O | bwd: dQ, dK, dV), same rows
 };
 
 // global tile (tensor w in q, k, v, dO = 0..3; head bh; block j)
@@ -69,6 +70,16 @@ __device__ __forceinline__ unsigned char* fa_tile(const FaParams& p, int w, int 
 template <typename F>
 __device__ __forceinline__ F* fa_row(F* base, const FaParams& p, int bh, long long t) {
   return base + ((long long)(bh / p.H) * p.T + t) * p.rs + (long long)(bh % p.H) * FA_D;
+}
+
+// fp32 float4 of row t, columns 4*c4.. -> the output and, when present, its bf16 copy
+__device__ __forceinline__ void fa_store4(float* out, __nv_bfloat16* sh, const FaParams& p, int bh, long long t, int c4,
+                                          float4 v) {
+  *(float4*)(fa_row(out, p, bh, t) + c4 * 4) = v;
+  if (sh != nullptr) {
+    __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y), b = __floats2bfloat162_rn(v.z, v.w);
+    *(uint2*)(fa_row(sh, p, bh, t) + c4 * 4) = make_uint2(*(uint32_t*)&a, *(uint32_t*)&b);
+  }
 }
 
 // 128-B swizzle of a [rows][64 bf16] tile: 16-byte chunk c of row r at chunk c ^ (r & 7)
@@ -494,7 +505,7 @@ __global__ void __launch_bounds__(320, 1) k_fa_fwd(const __grid_constant__ FaPar
     fa_bar(1 + t, 128);
     for (int u = r; u < FA_BLK * 16; u += 128) {
       const int rr = u >> 4, c4 = u & 15;
-      *(float4*)(fa_row(O, p, bh, qb * FA_BLK + rr) + c4 * 4) = stage[rr * 16 + (c4 ^ (rr & 15))];
+      fa_store4(O, p.sh[0], p, bh, qb * FA_BLK + rr, c4, stage[rr * 16 + (c4 ^ (rr & 15))]);
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -669,8 +680,8 @@ __global__ void __launch_bounds__(320, 1) k_fa_bwd_kv(const __grid_constant__ Fa
     fa_bar(1, 256);
     for (int u = tid; u < 2 * FA_BLK * 16; u += 256) {
       const int w = u / (FA_BLK * 16), rr = (u >> 4) & 127, c4 = u & 15;
-      float* dst = fa_row(w ? dK : dV, p, bh, kb * FA_BLK + rr) + c4 * 4;
-      *(float4*)dst = *(const float4*)((float*)sQ + w * (FA_BLK * 68) + rr * 68 + c4 * 4);
+      fa_store4(w ? dK : dV, w ? p.sh[1] : p.sh[2], p, bh, kb * FA_BLK + rr, c4,
+                *(const float4*)((float*)sQ + w * (FA_BLK * 68) + rr * 68 + c4 * 4));
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -797,7 +808,7 @@ __global__ void __launch_bounds__(320, 1) k_fa_bwd_q(const __grid_constant__ FaP
     fa_bar(1, 256);
     for (int u = tid; u < FA_BLK * 16; u += 256) {
       const int rr = u >> 4, c4 = u & 15;
-      *(float4*)(fa_row(dQ, p, bh, qb * FA_BLK + rr) + c4 * 4) = *(const float4*)(stage + rr * 68 + c4 * 4);
+      fa_store4(dQ, p.sh[0], p, bh, qb * FA_BLK + rr, c4, *(const float4*)(stage + rr * 68 + c4 * 4));
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");

@@ -3104,6 +3104,7 @@ struct Builder {
         fp.lse = (float*)buf(next());
         fp.delta = (float*)buf(next());
         fp.tiles = (unsigned char*)buf(next());
+        for (int i = 0; i < 3; ++i) fp.sh[i] = (__nv_bfloat16*)buf(next());   // -1 -> nullptr
         fp.q = operand(next());
         fp.k = operand(next());
         fp.v = operand(next());

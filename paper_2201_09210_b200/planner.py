@@ -410,6 +410,7 @@ class Planner:
         self.n_bias_fused = 0
         self._ar_lists = []                      # instruction lists after bucketing (inspection)
         self._emitted = set()                    # node ids emitted as their own plan items
+        self._fa_shadow = {}                     # attention output node -> its bf16 copy buffer
         self.chain_lates = 0
         self._chain_meta = {}
 
@@ -447,6 +448,17 @@ class Planner:
                     g["lse"] = self.new_buf(g["BH"] * g["T"] * 4)
                     g["delta"] = self.new_buf(g["BH"] * g["T"] * 4)
                     g["tiles"] = self.new_buf(4 * g["BH"] * g["T"] * FA_HEAD * 2)   # bf16 q | k | v | dO tiles
+                    # folded outputs read only by GEMMs (through their [B*T, H*hd] reshape): the
+                    # attention epilogue also writes the bf16 copy those GEMMs use
+                    if "dst" in g and os.environ.get("COEX_FA_SHADOW", "1") != "0":
+                        g["shadow"] = {}
+                        for name, xnode in g["dst"].items():
+                            r4 = [c.node_id for c in self.consumers.get(xnode.node_id, [])]
+                            if len(r4) == 1 and self.ops[r4[0]].kind is OpKind.RESHAPE and \
+                                    len(shapes[r4[0]]) == 2 and self._gemm_reader(r4[0]):
+                                b_ = self.new_buf(shape_size(shapes[r4[0]]) * 2)
+                                g["shadow"][name] = b_
+                                self._fa_shadow[xnode.node_id] = b_
                     self.n_attn += 1
                 insts = [repl.get(y.node_id, y) if isinstance(y, ExecOp) else y for y in insts
                          if not (isinstance(y, ExecOp) and y.node_id in gone)]
@@ -859,8 +871,10 @@ class Planner:
             x = g[m]
             flops[0] += flops_of(x.kind, [tuple(self._in_shape(b, shapes)) for b in x.inputs], x.attrs)
         n_compute[0] += 1
+        sh = g.get("shadow", {})
+        shw = [sh.get("O", -1), -1, -1] if a.mode == 0 else [sh.get("DQ", -1), sh.get("DK", -1), sh.get("DV", -1)]
         word = [T_ATTN, a.mode, g["BH"], g["T"], g.get("H", 1), g.get("rs", FA_HEAD), _f64_bits(g["scale"]), g["lse"],
-                g["delta"], g["tiles"]] + cells
+                g["delta"], g["tiles"]] + shw + cells
         for nid in outs:
             word += out_words(nid, _conflicts(cells, pubs[nid]))
             self._invalidate(pubs[nid])
@@ -1071,11 +1085,27 @@ class Planner:
 
     def _register_shadow(self, x, pubs, shapes):
         """After x's publication: its bf16 shadow (written by its kernel) is the valid bf16
-        copy of its output for later GEMMs of the same list."""
+        copy of its output for later GEMMs of the same list.  A 2-D reshape of an attention
+        output with a bf16 copy (written by the attention epilogue) registers that copy."""
         nid = x.node_id
+        if x.kind is OpKind.RESHAPE and not x.inputs[0].fed and len(x.inputs[0].cands) == 1 and \
+                x.inputs[0].cands[0] in self._fa_shadow and len(shapes[nid]) == 2:
+            shp = shapes[nid]
+            self._copies[(pubs[nid][0], shp[0], shp[1])] = self._fa_shadow[x.inputs[0].cands[0]]
+            return
         if nid in self.shadow and (x.kind is not OpKind.CROSS_ENTROPY_GRAD or nid in self._ce_loss):
             shp = shapes[nid]
             self._copies[(pubs[nid][0], shape_size(shp[:-1]), shp[-1])] = self.shadow[nid]
+
+    def _gemm_reader(self, nid) -> bool:
+        """Some reader of nid's output is a MatMul operand (directly or through a folded
+        transpose) -- a bf16 copy written by the producer saves that GEMM a conversion."""
+        for c in self.consumers.get(nid, []):
+            if c.kind is OpKind.MATMUL:
+                return True
+            if c.kind is OpKind.TRANSPOSE and c.node_id in self.folded:
+                return True
+        return False
 
     def _gemm_only(self, nid) -> bool:
         """Every reader of nid's output is a MatMul operand (directly or through a folded
