@@ -778,6 +778,9 @@ struct ChainSmem {
   unsigned char in_scalar[kChainIn];
   unsigned char out_reg[kChainOut];
   T* out_buf[kChainOut];
+  // fp32 update fast path: the program is  t = g * s ; y = w - t  (every parameter's SGD step):
+  // axpy = 1, ax_w / ax_g = vector inputs, ax_s = the scalar input; 16-byte aligned, 4 | n
+  int axpy, ax_w, ax_g, ax_s;
   T r[kChainRegs][256];
 };
 
@@ -797,6 +800,20 @@ __device__ __forceinline__ void chain_load(const ChainParams& p, ChainSmem<T>& S
     for (int j = 0; j < kChainOut; ++j) {
       S.out_reg[j] = p.out_reg[j];
       S.out_buf[j] = (T*)p.out_buf[j];
+    }
+    S.axpy = 0;
+    if (sizeof(T) == 4 && p.nops == 2 && p.nout == 1 && (p.n & 3) == 0 && p.ops[0].op == EW_MUL &&
+        p.ops[1].op == EW_SUB && p.ops[1].b == p.ops[0].dst && p.out_reg[0] == p.ops[1].dst &&
+        p.ops[1].a >= kChainRegs && p.ops[0].a >= kChainRegs && p.ops[0].b >= kChainRegs) {
+      const int w = p.ops[1].a - kChainRegs, x = p.ops[0].a - kChainRegs, y = p.ops[0].b - kChainRegs;
+      const int g = p.in_scalar[x] ? y : x, sc = p.in_scalar[x] ? x : y;
+      if (!p.in_scalar[w] && !p.in_scalar[g] && p.in_scalar[sc] && !(((uintptr_t)S.ip[w] | (uintptr_t)S.ip[g] |
+                                                                      (uintptr_t)S.out_buf[0]) & 15)) {
+        S.axpy = 1;
+        S.ax_w = w;
+        S.ax_g = g;
+        S.ax_s = sc;
+      }
     }
   }
   __syncthreads();
@@ -839,9 +856,23 @@ __device__ __forceinline__ void chain_run(const ChainParams& p, ChainSmem<T>& S,
   if (p.late == nullptr && b == 0 && threadIdx.x == 0) chain_publish(p);
   const int nops = p.nops, nout = p.nout;
   const long long stride = nb * blockDim.x;
-  for (long long i = b * blockDim.x + threadIdx.x; i < p.n; i += stride) {
-    chain_eval(S, nops, i);
-    for (int j = 0; j < nout; ++j) S.out_buf[j][i] = S.r[S.out_reg[j]][threadIdx.x];
+  if (sizeof(T) == 4 && S.axpy) {
+    // the SGD update without the interpreter: 16-byte loads / stores, the same two roundings
+    // (product, then difference) as the op-by-op program
+    const float4* w4 = (const float4*)S.ip[S.ax_w];
+    const float4* g4 = (const float4*)S.ip[S.ax_g];
+    float4* o4 = (float4*)S.out_buf[0];
+    const float sc = (float)S.sv[S.ax_s];
+    for (long long i = b * blockDim.x + threadIdx.x; i < p.n / 4; i += stride) {
+      const float4 w = w4[i], g = g4[i];
+      o4[i] = make_float4(__fsub_rn(w.x, __fmul_rn(g.x, sc)), __fsub_rn(w.y, __fmul_rn(g.y, sc)),
+                          __fsub_rn(w.z, __fmul_rn(g.z, sc)), __fsub_rn(w.w, __fmul_rn(g.w, sc)));
+    }
+  } else {
+    for (long long i = b * blockDim.x + threadIdx.x; i < p.n; i += stride) {
+      chain_eval(S, nops, i);
+      for (int j = 0; j < nout; ++j) S.out_buf[j][i] = S.r[S.out_reg[j]][threadIdx.x];
+    }
   }
   if (p.late != nullptr) {
     __syncthreads();
