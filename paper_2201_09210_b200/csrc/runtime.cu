@@ -1592,10 +1592,12 @@ int build_xop_t(coex_ctx* c, const OpSpec& s, Launch* L, int* nL, size_t* ws_byt
         while (gy < 256 && gx * gy < kNumSMs * 4 && Rw / (gy * 2) >= 64) gy *= 2;
         RowParams rp{};
         rp.ds = s.ds; rp.x = s.in[0]; rp.rows = Rw; rp.d = C; rp.out = s.out;
-        if (gy > 1) rp.acc = (double*)pv.take((size_t)C * 8);
+        if (gy > 1) {
+          rp.acc = (double*)pv.take((size_t)C * 8);
+          rp.counter = (unsigned int*)pv.take(16);
+        }
         if (!build) break;
         L[(*nL)++].set((void*)k_colsum_v4, dim3((unsigned)gx, (unsigned)gy), dim3(256), rp);
-        if (gy > 1) L[(*nL)++].set((void*)k_acc_out<float>, grid_for(C), dim3(256), rp);
         return COEX_OK;
       }
       if (s.kind == COEX_SUM_ROWS && (C > 1024 || (!is_f64(c) && Rw >= 4096 && C >= 256))) {

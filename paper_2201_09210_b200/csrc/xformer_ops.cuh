@@ -1085,7 +1085,31 @@ __global__ void __launch_bounds__(256) k_colsum_v4(RowParams p) {
       else atomicAdd(p.acc + c + k, v);
     }
   }
-  if (gridDim.y == 1) publish_late(p.out, o);
+  if (gridDim.y == 1) {
+    publish_late(p.out, o);
+    return;
+  }
+  // several row chunks: the last block to finish writes the output from the fp64
+  // accumulators and re-zeroes them (no separate k_acc_out launch)
+  __shared__ unsigned int last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(p.counter, 1u) == gridDim.x * gridDim.y - 1 ? 1u : 0u;
+    if (last) __threadfence();
+  }
+  __syncthreads();
+  if (!last) return;
+  for (long long k = threadIdx.x; k < p.d; k += blockDim.x) {
+    o[k] = (float)__ldcg(p.acc + k);
+    p.acc[k] = 0.0;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    *p.counter = 0u;
+    __threadfence();
+    for (int i = 0; i < p.out.npub; ++i) *p.out.pub[i] = o;
+  }
 }
 
 template <typename T>

@@ -659,7 +659,13 @@ class Planner:
         else:
             word += [-1, -1, 0, 0]
         sh = self.shadow.get(nid, -1) if k in (OpKind.GELU, OpKind.GELU_GRAD) else -1
-        word += [bias_cell, sh, int(sh != -1 and self._gemm_only(nid))]
+        skip = int(sh != -1 and self._gemm_only(nid))
+        word += [bias_cell, sh, skip]
+        if skip:
+            # a GEMM reader that ends up converting the fp32 tensor after all (its copy lookup
+            # missed, e.g. after a collective invalidated the copies) re-enables the fp32 write
+            self._skip_f32[nid] = (word, len(word) - 1)
+            self._skip_cell[pubs[nid][0]] = nid
         word += out_words(out_nid, late)
         self._invalidate(pubs[out_nid])
         if ba is not None:
