@@ -288,6 +288,27 @@ struct EwParams {
   int skip_f32;             // the fp32 output has no reader (only GEMMs, through the shadow)
 };
 
+// fp32 float4 body with the op fixed at compile time (no per-element dispatch)
+template <int OP>
+__device__ __forceinline__ void ew_body4(const EwParams& p, const float* a, const float* b, float* o, float as,
+                                         float bs, long long n4, long long stride) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
+    const float4 x4 = p.a_scalar ? make_float4(as, as, as, as) : ((const float4*)a)[i];
+    float4 y4 = make_float4(bs, bs, bs, bs);
+    if (b != nullptr && !p.b_scalar) y4 = ((const float4*)b)[i];
+    float4 r;
+    r.x = ew_apply(OP, x4.x, y4.x);
+    r.y = ew_apply(OP, x4.y, y4.y);
+    r.z = ew_apply(OP, x4.z, y4.z);
+    r.w = ew_apply(OP, x4.w, y4.w);
+    if (!p.skip_f32) ((float4*)o)[i] = r;
+    if (p.shadow) {
+      __nv_bfloat162 h0 = __floats2bfloat162_rn(r.x, r.y), h1 = __floats2bfloat162_rn(r.z, r.w);
+      ((uint2*)p.shadow)[i] = make_uint2(*(uint32_t*)&h0, *(uint32_t*)&h1);
+    }
+  }
+}
+
 template <typename T>
 __global__ void __launch_bounds__(256) k_elementwise(EwParams p) {
   COEX_PDL_ENTER();
@@ -306,6 +327,22 @@ __global__ void __launch_bounds__(256) k_elementwise(EwParams p) {
     const bool va = p.a_scalar || (((uintptr_t)a & 15) == 0);
     const bool vb = b == nullptr || p.b_scalar || (((uintptr_t)b & 15) == 0);
     if ((n & 3) == 0 && va && vb && (((uintptr_t)o & 15) == 0)) {
+      const float* af = (const float*)a;
+      const float* bf = (const float*)b;
+      float* of = (float*)o;
+      bool done = true;
+      switch (p.op) {                                // hot ops: op-specialised loops
+        case EW_ADD: ew_body4<EW_ADD>(p, af, bf, of, (float)as, (float)bs, n / 4, stride); break;
+        case EW_SUB: ew_body4<EW_SUB>(p, af, bf, of, (float)as, (float)bs, n / 4, stride); break;
+        case EW_MUL: ew_body4<EW_MUL>(p, af, bf, of, (float)as, (float)bs, n / 4, stride); break;
+        case EW_GELU: ew_body4<EW_GELU>(p, af, bf, of, (float)as, (float)bs, n / 4, stride); break;
+        case EW_GELU_GRAD: ew_body4<EW_GELU_GRAD>(p, af, bf, of, (float)as, (float)bs, n / 4, stride); break;
+        default: done = false;
+      }
+      if (done) {
+        publish_late(p.out, o);
+        return;
+      }
       for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n / 4; i += stride) {
         const float4 x4 = p.a_scalar ? make_float4(as, as, as, as) : ((const float4*)a)[i];
         float4 y4 = make_float4(bs, bs, bs, bs);
