@@ -148,6 +148,27 @@ int64_t coex_ctx_kernel_count(coex_ctx* ctx);
 int coex_nccl_unique_id(uint8_t* out128);
 int coex_ctx_init_comm(coex_ctx* ctx, int rank, int world, const uint8_t* uid128);
 
+/* ---- GEMM -> all-reduce fusion over NVLink SHARP multicast (csrc/nvls.cuh) ----
+ * Replaces the NCCL gradient buckets of a data-parallel plan (the reference has no
+ * distributed path).  Set-up, once per context, with a host
+ * barrier (torch.distributed) between the steps:
+ *   rank 0: coex_nvls_create(bytes, world) -> {pid, fd, rounded bytes} (broadcast them);
+ *   every rank: coex_nvls_attach(pid, fd, bytes, world); barrier; coex_nvls_bind; barrier.
+ * Plans built afterwards place sum-reduced gradient buckets in the region: their GEMM
+ * producers add into the multicast alias from the epilogue (multimem.red), other members
+ * are reduced by a one-shot multimem.ld_reduce / multimem.st kernel. */
+int coex_nvls_supported(coex_ctx* ctx, int* out);          /* CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED */
+int coex_nvls_create(coex_ctx* ctx, int64_t bytes, int world, int64_t* out_pid_fd_bytes);
+int coex_nvls_attach(coex_ctx* ctx, int64_t pid, int64_t fd, int64_t bytes, int world);
+int coex_nvls_bind(coex_ctx* ctx);
+int coex_nvls_info(coex_ctx* ctx, int64_t* out3);          /* {usable bytes (0: none), world, mode 1 MC / 2 P2P} */
+/* Same protocol without a multicast object (cuMulticastCreate unavailable): each rank's
+ * region is a cudaMalloc exported by CUDA IPC; the epilogues add into every peer's copy over
+ * NVLink.  rank: coex_p2p_create -> 64-byte handle; all-gather; coex_p2p_open(all handles). */
+int coex_p2p_create(coex_ctx* ctx, int64_t bytes, uint8_t* out_handle64);
+int coex_p2p_open(coex_ctx* ctx, const uint8_t* handles, int world);
+int coex_prog_nvls(coex_prog* prog, int64_t* fused_gemms); /* GEMMs reducing in their epilogue */
+
 /* ---- timing on the context's stream (bench.py; CUDA events, not host clocks) ---- */
 int coex_ctx_event_record(coex_ctx* ctx, int slot);               /* slot in [0, 64) */
 int coex_ctx_event_elapsed(coex_ctx* ctx, int a, int b, double* ms);

@@ -71,6 +71,14 @@ SIGNATURES = {
                                        ctypes.c_int, _I64P, _DP]),
     "coex_nccl_unique_id": (ctypes.c_int, [ctypes.c_char_p]),
     "coex_ctx_init_comm": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int, ctypes.c_char_p]),
+    "coex_nvls_supported": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_int)]),
+    "coex_nvls_create": (ctypes.c_int, [_P, ctypes.c_int64, ctypes.c_int, ctypes.POINTER(ctypes.c_int64)]),
+    "coex_nvls_attach": (ctypes.c_int, [_P, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int]),
+    "coex_nvls_bind": (ctypes.c_int, [_P]),
+    "coex_nvls_info": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_int64)]),
+    "coex_prog_nvls": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_int64)]),
+    "coex_p2p_create": (ctypes.c_int, [_P, ctypes.c_int64, ctypes.c_char_p]),
+    "coex_p2p_open": (ctypes.c_int, [_P, ctypes.c_char_p, ctypes.c_int]),
     "coex_ctx_set_trace": (ctypes.c_int, [_P, ctypes.c_int]),
     "coex_ctx_read_trace": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_uint64), _I64, _I64P]),
     "coex_tensor_put": (ctypes.c_int, [_P, ctypes.c_int, _I64P, _DP, _I64P]),
@@ -216,8 +224,69 @@ class B200Backend:
         self._vshape: dict = {}
         self.active = None
         self.op_log = None            # list: record (kind, attrs, input shapes) of eager ops
+        self.nvls_bytes = 0           # NVLS gradient region (csrc/nvls.cuh); 0 = NCCL buckets
+        self.nvls_mode = "none"
         if dp is not None and (dp.world > 1 or dp.force):
             self._init_comm()
+            if precision != "f64" and self._nvls_wanted():
+                self._init_nvls(int(os.environ.get("COEX_NVLS_MB", "1024")) << 20)
+
+    def _nvls_wanted(self) -> bool:
+        """COEX_NVLS=0: off; 1: on (multicast, else the P2P transport -- also for a forced
+        1-rank group); p2p: the P2P transport; unset: on when the group spans several GPUs and
+        a multicast object can be created (P2P reductions send R x the bytes of the
+        switch-reduced path, so the default then falls back to the NCCL buckets)."""
+        mode = os.environ.get("COEX_NVLS", "")
+        if mode == "0":
+            return False
+        if mode in ("1", "p2p"):
+            return True
+        ok = ctypes.c_int(0)
+        _check(self.lib.coex_nvls_supported(self.ctx, ctypes.byref(ok)))
+        return bool(ok.value) and self.dp.world > 1
+
+    def _init_nvls(self, nbytes: int):
+        """GEMM -> all-reduce fusion region over the data-parallel group (csrc/nvls.cuh,
+        include/coex_b200.h).  Multicast: rank 0 creates the object and exports a POSIX fd,
+        every rank imports it (pidfd_getfd) and adds its device, then binds its own copy, with
+        host barriers between the phases.  P2P: every rank exports its region by CUDA IPC and
+        opens the others'."""
+        world, mode = self.dp.world, os.environ.get("COEX_NVLS", "")
+        if world > 1:                 # (torch is already up under torchrun; a 1-rank group never imports it)
+            import torch.distributed as dist
+        info = (ctypes.c_int64 * 3)()
+        vals = [0, 0, 0, 0]
+        if mode != "p2p" and self.dp.rank == 0:
+            if self.lib.coex_nvls_create(self.ctx, nbytes, world, info) == 0:
+                vals = [1, int(info[0]), int(info[1]), int(info[2])]
+        if world > 1:
+            obj = [vals]
+            dist.broadcast_object_list(obj, src=0)
+            vals = obj[0]
+        if vals[0]:
+            _check(self.lib.coex_nvls_attach(self.ctx, vals[1], vals[2], vals[3], world))
+            if world > 1:
+                dist.barrier()
+            _check(self.lib.coex_nvls_bind(self.ctx))
+            if world > 1:
+                dist.barrier()
+        elif mode in ("1", "p2p"):
+            h = ctypes.create_string_buffer(64)
+            _check(self.lib.coex_p2p_create(self.ctx, nbytes, h))
+            handles = [bytes(h.raw)]
+            if world > 1:
+                handles = [None] * world
+                dist.all_gather_object(handles, bytes(h.raw))
+            allh = ctypes.create_string_buffer(b"".join(handles), 64 * world)
+            _check(self.lib.coex_p2p_open(self.ctx, allh, world))
+            if world > 1:
+                dist.barrier()
+        else:
+            return                                   # no multicast: NCCL buckets
+        out = (ctypes.c_int64 * 3)()
+        _check(self.lib.coex_nvls_info(self.ctx, out))
+        self.nvls_bytes = int(out[0])
+        self.nvls_mode = {1: "multicast", 2: "p2p"}.get(int(out[2]), "none")
 
     def _init_comm(self):
         """NCCL communicator over the caller's torch.distributed group (rank 0 makes the id)."""
@@ -263,7 +332,8 @@ class B200Backend:
                    18: "bn apply", 19: "split-K reduce", 20: "causal softmax", 21: "softmax grad",
                    22: "cross-entropy", 23: "bias add", 24: "layernorm", 25: "embedding", 26: "column sum",
                    27: "rel skew", 28: "pooling", 29: "axis op", 30: "cancel guard",
-                   31: "attention fwd", 32: "attention prep", 33: "attention dK/dV", 34: "attention dQ"}
+                   31: "attention fwd", 32: "attention prep", 33: "attention dK/dV", 34: "attention dQ",
+                   35: "nvls all-reduce"}
 
     def set_trace(self, capacity: int):
         """Enable device-side per-kernel stamps (0 disables)."""
@@ -509,7 +579,7 @@ class B200Program:
                 try:
                     plan = Planner(dplan.sp, self.tg, be.var_idx, vsh, local_feed_shapes(self.feed_shape, dplan),
                                    be.esize, bf16=bf16, force_store=dplan.allreduce_nodes,
-                                   const_slots=self.consts).build()
+                                   const_slots=self.consts, nvls_bytes=be.nvls_bytes).build()
                     plan.feed_shapes = dict(self.feed_shape)        # host checks global shapes
                     plan.sharded = set(dplan.sharded_slots)
                     plan.dp = dplan
@@ -520,9 +590,11 @@ class B200Program:
                        const_slots=self.consts).build()
 
     def info(self, handle) -> dict:
-        nk, nc, ab = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        nk, nc, ab, nv = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
         self.be.lib.coex_prog_info(handle, ctypes.byref(nk), ctypes.byref(nc), ctypes.byref(ab))
-        return {"kernel_nodes": nk.value, "conditional_nodes": nc.value, "arena_bytes": ab.value}
+        self.be.lib.coex_prog_nvls(handle, ctypes.byref(nv))
+        return {"kernel_nodes": nk.value, "conditional_nodes": nc.value, "arena_bytes": ab.value,
+                "nvls_fused_gemms": nv.value}
 
     def close(self):
         for handle, _ in self.graphs.values():

@@ -160,6 +160,9 @@ struct TcGemmParams {
   int tri_out, tri_a;
   In bias;                   // has_bias: C[m][n] += bias[n] in the epilogue (fused bias_add)
   int has_bias;
+  // GEMM -> all-reduce fusion (nvls.cuh): mode != RED_NONE -- the epilogue adds every tile
+  // into the team's copies (multimem.red or per-peer red) instead of storing it
+  RedTarget red;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -531,7 +534,10 @@ __global__ void __launch_bounds__(TC_THREADS, DUO ? 2 : 1) k_gemm_tc(const __gri
             }
             float* dst = C + orow * p.N + gcol;
             v.x += bv.x; v.y += bv.y; v.z += bv.z; v.w += bv.w;
-            if (vec_ok && gcol + 4 <= p.N) {
+            if (p.red.mode != RED_NONE) {           // gradient bucket member: reduce across ranks
+              const int nv = (int)(p.N - gcol < 4 ? p.N - gcol : 4);
+              red_store4(p.red, dst, v, vec_ok && gcol + 4 <= p.N, nv);
+            } else if (vec_ok && gcol + 4 <= p.N) {
               *(float4*)dst = v;
             } else {
               dst[0] = v.x;

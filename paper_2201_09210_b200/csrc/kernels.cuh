@@ -55,7 +55,7 @@ enum StampKind {
   SK_AFTER_WAIT = 64, SK_FUSED = 13, SK_IM2COL = 14, SK_COL2IM = 15, SK_CVT = 16, SK_COLSTATS = 17,
   SK_BNAPPLY = 18, SK_SPLITK = 19, SK_SOFTMAX = 20, SK_SOFTMAX_GRAD = 21, SK_CE = 22, SK_BIAS = 23, SK_LN = 24,
   SK_EMBED = 25, SK_COLSUM = 26, SK_SKEW = 27, SK_POOL = 28, SK_AXIS = 29, SK_GUARD = 30, SK_ATTN = 31,
-  SK_ATTN_DELTA = 32, SK_ATTN_KV = 33, SK_ATTN_Q = 34
+  SK_ATTN_DELTA = 32, SK_ATTN_KV = 33, SK_ATTN_Q = 34, SK_NVLS = 35
 };
 
 // Host <-> device rings in pinned, mapped host memory.

@@ -29,6 +29,7 @@
 
 #include "../../include/coex_b200.h"
 #include "kernels.cuh"
+#include "nvls.cuh"
 #include "gemm_tc.cuh"
 #include "gemm_tf32.cuh"
 #include "ext_ops.cuh"
@@ -37,6 +38,9 @@
 
 #include <cudaTypedefs.h>
 #include <dlfcn.h>
+#include <cerrno>
+#include <sys/syscall.h>
+#include <unistd.h>
 
 using namespace coex;
 
@@ -99,6 +103,9 @@ struct Launch {
   void* ar_buf = nullptr;
   int64_t ar_count = 0;
   int ar_f64 = 1;
+  // tcgen05 GEMM whose result lands in the op's Out (1: the GEMM itself, 2: its split-K
+  // reduction) -- the NVLS fusion retargets these (Builder::nvls_fuse)
+  int tc_dest = 0;
   void allreduce(void* b, int64_t n, bool f64) {
     fn = nullptr;
     ar_buf = b;
@@ -177,6 +184,18 @@ struct coex_ctx {
   void* comm = nullptr;                  // ncclComm_t
   int rank = 0, world = 1;
   cudaStream_t cap_stream = nullptr;     // side stream used to capture collectives into graphs
+  // NVLS gradient region (nvls.cuh): this rank's copy and the team's multicast alias of the
+  // same bytes; the first kNvlsFlagBytes hold the barrier flags
+  char* nv_local = nullptr;
+  char* nv_mc = nullptr;
+  size_t nv_bytes = 0;
+  unsigned long long nv_mc_handle = 0, nv_mem_handle = 0;
+  int nv_world = 0, nv_creator = 0, nv_attached = 0;
+  unsigned int* nv_gen = nullptr;        // barrier generations (ordinary device memory)
+  int nv_next_slot = 0;
+  int nv_mode = 0;                       // RedMode: RED_MC (multicast) / RED_P2P (IPC-opened peers)
+  char* nv_peer[kMaxPeers] = {nullptr};  // RED_P2P: every rank's region (own = nv_local)
+  bool nv_p2p_own = false;               // RED_P2P: nv_local from cudaMalloc (freed here)
 };
 
 namespace {
@@ -1146,6 +1165,7 @@ int tc_gemm_launches(coex_ctx* c, DevState* ds, void* a16, void* b16, int64_t M,
   gp.splits = t.splits;
   gp.raw = t.splits > 1 ? ws : raw;
   Launch& G = L[(*nL)++];
+  G.tc_dest = raw == nullptr ? 1 : 0;
   const int64_t items = ((M + TC_BM - 1) / TC_BM) * ((N + t.bn - 1) / t.bn) * t.splits *
                         (amode == 2 ? gp.cv.phases : 1) * (batch > 1 ? batch : 1);
   // two CTAs per SM for short-K launches that do not fill two waves of single CTAs
@@ -1184,6 +1204,7 @@ int tc_gemm_launches(coex_ctx* c, DevState* ds, void* a16, void* b16, int64_t M,
     } else {
       r.out = out;
     }
+    L[*nL].tc_dest = raw == nullptr ? 2 : 0;
     L[(*nL)++].set((void*)k_splitk_reduce, grid_for(M * N / 4 + 1), dim3(256), r);
   }
   return COEX_OK;
@@ -2044,6 +2065,10 @@ int set_var_cur(coex_ctx* c, int idx) {
 }  // namespace
 
 // =============================================================== C-ABI: context
+namespace {
+void nvls_release(coex_ctx* c);
+}  // namespace
+
 extern "C" {
 
 const char* coex_last_error(void) { return g_err.c_str(); }
@@ -2141,6 +2166,7 @@ int coex_ctx_destroy(coex_ctx* c) {
   if (c->h_stage) cudaFreeHost(c->h_stage);
   for (auto& ev : c->events)
     if (ev) cudaEventDestroy(ev);
+  nvls_release(c);
   if (c->comm && nccl().ok) nccl().comm_destroy(c->comm);
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   cudaStreamDestroy(c->stream);
@@ -2159,6 +2185,245 @@ int coex_ctx_set_timeout(coex_ctx* c, double seconds) {
 }
 
 int64_t coex_ctx_kernel_count(coex_ctx* c) { return c ? c->kernel_count : 0; }
+
+// ---- NVLS multicast region (nvls.cuh) through the driver API, resolved at run time ----
+}  // extern "C"
+namespace {
+struct CuApi {
+  bool ok = false;
+  CUresult (*mc_create)(CUmemGenericAllocationHandle*, const CUmulticastObjectProp*) = nullptr;
+  CUresult (*mc_add_device)(CUmemGenericAllocationHandle, CUdevice) = nullptr;
+  CUresult (*mc_bind_mem)(CUmemGenericAllocationHandle, size_t, CUmemGenericAllocationHandle, size_t, size_t,
+                          unsigned long long) = nullptr;
+  CUresult (*mc_unbind)(CUmemGenericAllocationHandle, CUdevice, size_t, size_t) = nullptr;
+  CUresult (*mc_granularity)(size_t*, const CUmulticastObjectProp*, CUmulticastGranularity_flags) = nullptr;
+  CUresult (*mem_create)(CUmemGenericAllocationHandle*, size_t, const CUmemAllocationProp*, unsigned long long) = nullptr;
+  CUresult (*mem_release)(CUmemGenericAllocationHandle) = nullptr;
+  CUresult (*mem_granularity)(size_t*, const CUmemAllocationProp*, CUmemAllocationGranularity_flags) = nullptr;
+  CUresult (*addr_reserve)(CUdeviceptr*, size_t, size_t, CUdeviceptr, unsigned long long) = nullptr;
+  CUresult (*addr_free)(CUdeviceptr, size_t) = nullptr;
+  CUresult (*mem_map)(CUdeviceptr, size_t, size_t, CUmemGenericAllocationHandle, unsigned long long) = nullptr;
+  CUresult (*mem_unmap)(CUdeviceptr, size_t) = nullptr;
+  CUresult (*set_access)(CUdeviceptr, size_t, const CUmemAccessDesc*, size_t) = nullptr;
+  CUresult (*export_handle)(void*, CUmemGenericAllocationHandle, CUmemAllocationHandleType, unsigned long long) = nullptr;
+  CUresult (*import_handle)(CUmemGenericAllocationHandle*, void*, CUmemAllocationHandleType) = nullptr;
+  CUresult (*dev_attr)(int*, CUdevice_attribute, CUdevice) = nullptr;
+};
+CuApi& cuapi() {
+  static CuApi a;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    auto get = [](const char* name, void** fn) {
+      cudaDriverEntryPointQueryResult q;
+      return cudaGetDriverEntryPoint(name, fn, cudaEnableDefault, &q) == cudaSuccess && q == cudaDriverEntryPointSuccess;
+    };
+    bool ok = true;
+    ok &= get("cuMulticastCreate", (void**)&a.mc_create);
+    ok &= get("cuMulticastAddDevice", (void**)&a.mc_add_device);
+    ok &= get("cuMulticastBindMem", (void**)&a.mc_bind_mem);
+    ok &= get("cuMulticastUnbind", (void**)&a.mc_unbind);
+    ok &= get("cuMulticastGetGranularity", (void**)&a.mc_granularity);
+    ok &= get("cuMemCreate", (void**)&a.mem_create);
+    ok &= get("cuMemRelease", (void**)&a.mem_release);
+    ok &= get("cuMemGetAllocationGranularity", (void**)&a.mem_granularity);
+    ok &= get("cuMemAddressReserve", (void**)&a.addr_reserve);
+    ok &= get("cuMemAddressFree", (void**)&a.addr_free);
+    ok &= get("cuMemMap", (void**)&a.mem_map);
+    ok &= get("cuMemUnmap", (void**)&a.mem_unmap);
+    ok &= get("cuMemSetAccess", (void**)&a.set_access);
+    ok &= get("cuMemExportToShareableHandle", (void**)&a.export_handle);
+    ok &= get("cuMemImportFromShareableHandle", (void**)&a.import_handle);
+    ok &= get("cuDeviceGetAttribute", (void**)&a.dev_attr);
+    a.ok = ok;
+    cudaGetLastError();
+  }
+  return a;
+}
+#define CU(call)                                                                                  \
+  do {                                                                                            \
+    CUresult r_ = (call);                                                                         \
+    if (r_ != CUDA_SUCCESS)                                                                       \
+      return fail(COEX_CUDA_ERROR, std::string(#call) + ": CUresult " + std::to_string((int)r_)); \
+  } while (0)
+
+CUmulticastObjectProp nvls_prop(size_t bytes, int world) {
+  CUmulticastObjectProp mp;
+  memset(&mp, 0, sizeof(mp));
+  mp.numDevices = (unsigned)world;
+  mp.size = bytes;
+  mp.handleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+  return mp;
+}
+void nvls_release(coex_ctx* c) {
+  if (c->nv_mode == RED_P2P) {
+    for (int r = 0; r < c->nv_world && r < kMaxPeers; ++r)
+      if (c->nv_peer[r] && c->nv_peer[r] != c->nv_local) cudaIpcCloseMemHandle(c->nv_peer[r]);
+    if (c->nv_p2p_own && c->nv_local) cudaFree(c->nv_local);
+    if (c->nv_gen) cudaFree(c->nv_gen);
+    return;
+  }
+  if (c->nv_local || c->nv_mc_handle) {           // NVLS region: unmap both aliases, unbind, release
+    CuApi& a = cuapi();
+    if (c->nv_mc) { a.mem_unmap((CUdeviceptr)c->nv_mc, c->nv_bytes); a.addr_free((CUdeviceptr)c->nv_mc, c->nv_bytes); }
+    if (c->nv_local) {
+      a.mem_unmap((CUdeviceptr)c->nv_local, c->nv_bytes);
+      a.addr_free((CUdeviceptr)c->nv_local, c->nv_bytes);
+      a.mc_unbind(c->nv_mc_handle, (CUdevice)c->device, 0, c->nv_bytes);
+    }
+    if (c->nv_mem_handle) a.mem_release(c->nv_mem_handle);
+    if (c->nv_mc_handle) a.mem_release(c->nv_mc_handle);
+    if (c->nv_gen) cudaFree(c->nv_gen);
+  }
+}
+}  // namespace
+extern "C" {
+
+int coex_nvls_supported(coex_ctx* c, int* out) {
+  *out = 0;
+  CuApi& a = cuapi();
+  if (!a.ok) return COEX_OK;
+  int v = 0;
+  if (a.dev_attr(&v, CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED, (CUdevice)c->device) == CUDA_SUCCESS) *out = v;
+  return COEX_OK;
+}
+
+// Rank 0: the team's multicast object (world devices, >= bytes per device, rounded to the
+// recommended granularity), exported as a POSIX fd for the other ranks (pidfd_getfd).
+int coex_nvls_create(coex_ctx* c, int64_t bytes, int world, int64_t* out_pid_fd) {
+  CuApi& a = cuapi();
+  if (!a.ok) return fail(COEX_CUDA_ERROR, "driver multicast API not available");
+  if (c->nv_mc_handle) return fail(COEX_INVALID, "NVLS region already created");
+  CK(cudaSetDevice(c->device));
+  size_t want = (size_t)bytes + kNvlsFlagBytes, gran = 0;
+  CUmulticastObjectProp mp = nvls_prop(want, world);
+  CU(a.mc_granularity(&gran, &mp, CU_MULTICAST_GRANULARITY_RECOMMENDED));
+  want = (want + gran - 1) / gran * gran;
+  mp.size = want;
+  CUmemGenericAllocationHandle h;
+  CU(a.mc_create(&h, &mp));
+  c->nv_mc_handle = h;
+  c->nv_bytes = want;
+  c->nv_world = world;
+  c->nv_creator = 1;
+  int fd = -1;
+  CU(a.export_handle(&fd, h, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, 0));
+  out_pid_fd[0] = (int64_t)getpid();
+  out_pid_fd[1] = fd;
+  out_pid_fd[2] = (int64_t)want;
+  return COEX_OK;
+}
+
+// Every rank: join the team (ranks > 0 import the creator's fd first), add this device.
+int coex_nvls_attach(coex_ctx* c, int64_t pid, int64_t fd, int64_t bytes, int world) {
+  CuApi& a = cuapi();
+  if (!a.ok) return fail(COEX_CUDA_ERROR, "driver multicast API not available");
+  CK(cudaSetDevice(c->device));
+  if (!c->nv_creator) {
+    const int pfd = (int)syscall(434 /* pidfd_open */, (pid_t)pid, 0);
+    if (pfd < 0) return fail(COEX_CUDA_ERROR, "pidfd_open failed: " + std::string(strerror(errno)));
+    const int lfd = (int)syscall(438 /* pidfd_getfd */, pfd, (int)fd, 0);
+    close(pfd);
+    if (lfd < 0) return fail(COEX_CUDA_ERROR, "pidfd_getfd failed: " + std::string(strerror(errno)));
+    CUmemGenericAllocationHandle h;
+    CUresult r = a.import_handle(&h, (void*)(uintptr_t)lfd, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR);
+    close(lfd);
+    if (r != CUDA_SUCCESS) return fail(COEX_CUDA_ERROR, "cuMemImportFromShareableHandle: " + std::to_string((int)r));
+    c->nv_mc_handle = h;
+    c->nv_bytes = (size_t)bytes;
+    c->nv_world = world;
+  }
+  CU(a.mc_add_device(c->nv_mc_handle, (CUdevice)c->device));
+  c->nv_attached = 1;
+  return COEX_OK;
+}
+
+// Every rank, after all ranks attached: this rank's physical copy bound to the object, both
+// mapped (unicast + multicast), flags zeroed.  The host barrier after it precedes any pass.
+int coex_nvls_bind(coex_ctx* c) {
+  CuApi& a = cuapi();
+  if (!c->nv_attached) return fail(COEX_INVALID, "coex_nvls_bind before coex_nvls_attach");
+  CK(cudaSetDevice(c->device));
+  CUmemAllocationProp ap;
+  memset(&ap, 0, sizeof(ap));
+  ap.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+  ap.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  ap.location.id = c->device;
+  size_t g = 0;
+  CU(a.mem_granularity(&g, &ap, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED));
+  if (c->nv_bytes % g) return fail(COEX_INVALID, "NVLS size not a multiple of the allocation granularity");
+  CUmemGenericAllocationHandle mem;
+  CU(a.mem_create(&mem, c->nv_bytes, &ap, 0));
+  c->nv_mem_handle = mem;
+  CUmemAccessDesc ad;
+  memset(&ad, 0, sizeof(ad));
+  ad.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  ad.location.id = c->device;
+  ad.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+  CUdeviceptr uc = 0, mc = 0;
+  CU(a.addr_reserve(&uc, c->nv_bytes, g, 0, 0));
+  CU(a.mem_map(uc, c->nv_bytes, 0, mem, 0));
+  CU(a.set_access(uc, c->nv_bytes, &ad, 1));
+  CU(a.mc_bind_mem(c->nv_mc_handle, 0, mem, 0, c->nv_bytes, 0));
+  CU(a.addr_reserve(&mc, c->nv_bytes, g, 0, 0));
+  CU(a.mem_map(mc, c->nv_bytes, 0, c->nv_mc_handle, 0));
+  CU(a.set_access(mc, c->nv_bytes, &ad, 1));
+  c->nv_local = (char*)uc;
+  c->nv_mc = (char*)mc;
+  c->nv_mode = RED_MC;
+  CK(cudaMalloc(&c->nv_gen, sizeof(unsigned int) * kNvlsSlots));
+  CK(cudaMemset(c->nv_gen, 0, sizeof(unsigned int) * kNvlsSlots));
+  CK(cudaMemset(c->nv_local, 0, c->nv_bytes));
+  CK(cudaDeviceSynchronize());
+  return COEX_OK;
+}
+
+int coex_nvls_info(coex_ctx* c, int64_t* out3) {
+  out3[0] = c->nv_local != nullptr ? (int64_t)(c->nv_bytes - kNvlsFlagBytes) : 0;
+  out3[1] = c->nv_world;
+  out3[2] = c->nv_mode;
+  return COEX_OK;
+}
+
+// RED_P2P transport (no multicast object): this rank's region (flags zeroed), exported as a
+// CUDA IPC handle (64 bytes) for the peers.
+int coex_p2p_create(coex_ctx* c, int64_t bytes, uint8_t* out_handle64) {
+  if (c->nv_local) return fail(COEX_INVALID, "gradient region already set up");
+  CK(cudaSetDevice(c->device));
+  const size_t want = ((size_t)bytes + kNvlsFlagBytes + 255) & ~(size_t)255;
+  CK(cudaMalloc(&c->nv_local, want));
+  c->nv_p2p_own = true;
+  c->nv_bytes = want;
+  CK(cudaMemset(c->nv_local, 0, want));
+  cudaIpcMemHandle_t h;
+  CK(cudaIpcGetMemHandle(&h, c->nv_local));
+  memcpy(out_handle64, &h, sizeof(h) < 64 ? sizeof(h) : 64);
+  return COEX_OK;
+}
+
+// Every rank, with all ranks' handles (rank order, 64 bytes each): open the peers' regions.
+int coex_p2p_open(coex_ctx* c, const uint8_t* handles, int world) {
+  if (!c->nv_local || !c->nv_p2p_own) return fail(COEX_INVALID, "coex_p2p_open before coex_p2p_create");
+  if (world < 1 || world > kMaxPeers) return fail(COEX_INVALID, "P2P gradient region: 1..8 ranks");
+  CK(cudaSetDevice(c->device));
+  for (int r = 0; r < world; ++r) {
+    if (r == c->rank) {
+      c->nv_peer[r] = c->nv_local;
+      continue;
+    }
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handles + 64 * r, sizeof(h));
+    void* ptr = nullptr;
+    CK(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    c->nv_peer[r] = (char*)ptr;
+  }
+  c->nv_world = world;
+  c->nv_mode = RED_P2P;
+  CK(cudaMalloc(&c->nv_gen, sizeof(unsigned int) * kNvlsSlots));
+  CK(cudaMemset(c->nv_gen, 0, sizeof(unsigned int) * kNvlsSlots));
+  CK(cudaDeviceSynchronize());
+  return COEX_OK;
+}
 
 int coex_nccl_unique_id(uint8_t* out128) {
   NcclApi& n = nccl();
@@ -2699,9 +2964,10 @@ int coex_var_rollback(coex_ctx* c) {
 namespace {
 
 enum PlanTag : int64_t { T_SEQ = 1, T_OP = 2, T_PTR = 3, T_FEED = 4, T_FETCH = 5, T_SWITCH = 6, T_WHILE = 7, T_CHAIN = 8,
-                         T_ALLREDUCE = 9, T_XOP = 10, T_MCHAIN = 11, T_ATTN = 12, T_JOIN = 13 };
+                         T_ALLREDUCE = 9, T_XOP = 10, T_MCHAIN = 11, T_ATTN = 12, T_JOIN = 13,
+                         T_NVLS_AR = 14, T_NVLS_ZERO = 15 };
 constexpr int64_t kPlanMagic = 0xC0E8B200;
-constexpr int64_t kPlanVersion = 3;
+constexpr int64_t kPlanVersion = 4;
 
 struct FeedSlot {
   int64_t slot;
@@ -2725,6 +2991,7 @@ struct coex_prog {
   FeedRecord* recs = nullptr;
   unsigned int* late = nullptr;       // late-publication counters
   int64_t n_kernel_nodes = 0, n_cond_nodes = 0, n_compute = 0, n_collectives = 0, n_guards = 0;
+  int64_t n_nvls_fused = 0;           // GEMMs whose epilogue reduces into the NVLS region
   std::vector<int> commit_vars;
   std::vector<int64_t> commit_bytes;
   std::unordered_map<int, std::vector<int64_t>> var_shapes;   // shape id -> dims
@@ -2750,6 +3017,8 @@ struct Builder {
   int64_t n;
   int64_t pos = 0;
   std::vector<char*> bufs;
+  std::vector<int64_t> sizes;      // buffer bytes (views: bytes to the parent's end)
+  std::vector<std::pair<char*, char*>> nv_red;   // NVLS: output ranges reduced by GEMM epilogues
   int64_t n_late = 0;
   std::string err;
   char* scratch = nullptr;         // scratch shared by the program's ops (they run in stream order)
@@ -2883,6 +3152,62 @@ struct Builder {
     return COEX_OK;
   }
 
+  // ---- NVLS fusion (nvls.cuh) ----
+  bool in_nv(const void* q) const {
+    return c->nv_local != nullptr && (const char*)q >= c->nv_local + kNvlsFlagBytes &&
+           (const char*)q < c->nv_local + c->nv_bytes;
+  }
+  // An op whose Out is an NVLS bucket member and whose result comes from ONE tcgen05 GEMM
+  // (plain or split-K, no bias, no scatter / batch / triangle): the GEMM epilogue adds its
+  // tiles into the multicast alias, the split-K reduction launch is dropped (every K slice
+  // adds), and the range is recorded as already reduced for the bucket's all-reduce.
+  void nvls_fuse(const Out& o, Launch* L, int* nL) {
+    if (!in_nv(o.buf[0]) || o.pingpong) return;
+    int gi = -1, ng = 0;
+    for (int i = 0; i < *nL; ++i)
+      if (L[i].tc_dest == 1) { gi = i; ++ng; }
+    if (ng != 1) return;
+    TcGemmParams* gp = (TcGemmParams*)L[gi].params;
+    if (gp->has_bias || gp->cv.phases > 1 || gp->batch > 1 || gp->tri_out || gp->tri_a) return;
+    for (int i = 0; i < *nL; ++i)
+      if (L[i].tc_dest == 2 && ((SplitReduceParams*)L[i].params)->has_bias) return;
+    const size_t bytes = (size_t)gp->M * (size_t)gp->N * 4;
+    char* lo = (char*)o.buf[0];
+    if (lo + bytes > c->nv_local + c->nv_bytes) return;
+    gp->red.mode = c->nv_mode;
+    if (c->nv_mode == RED_MC) {
+      gp->red.npeers = 1;
+      gp->red.delta[0] = (long long)(c->nv_mc - c->nv_local);
+    } else {
+      gp->red.npeers = c->nv_world;
+      for (int r = 0; r < c->nv_world; ++r) gp->red.delta[r] = (long long)(c->nv_peer[r] - c->nv_local);
+    }
+    gp->raw = nullptr;
+    int k = 0;
+    for (int i = 0; i < *nL; ++i)
+      if (L[i].tc_dest != 2) {
+        if (k != i) L[k] = L[i];
+        ++k;
+      }
+    *nL = k;
+    nv_red.push_back({lo, lo + bytes});
+    p->n_nvls_fused++;
+  }
+  int nvls_barrier(cudaGraph_t g, cudaGraphNode_t* prev) {
+    const int slot = c->nv_next_slot++ % kNvlsSlots;
+    NvlsBarrierParams q{};
+    q.ds = c->d_state;
+    q.mode = c->nv_mode;
+    q.world = c->nv_world;
+    if (c->nv_mode == RED_MC) q.flag_arrive[0] = (unsigned int*)c->nv_mc + slot;
+    else for (int r = 0; r < c->nv_world; ++r) q.flag_arrive[r] = (unsigned int*)c->nv_peer[r] + slot;
+    q.flag_local = (unsigned int*)c->nv_local + slot;
+    q.gen = c->nv_gen + slot;
+    Launch L;
+    L.set((void*)k_nvls_barrier, dim3(1), dim3(32), q);
+    return add_kernel(g, prev, L);
+  }
+
   int add_kernel(cudaGraph_t g, cudaGraphNode_t* prev, Launch& L) {
     if (L.fn == nullptr && L.ar_buf != nullptr)
       return add_allreduce(g, prev, L.ar_buf, L.ar_count, L.ar_f64 ? kNcclDouble : kNcclFloat, kNcclSum);
@@ -2945,7 +3270,8 @@ struct Builder {
     };
     for (int64_t i = 0; i < items; ++i) {
       const int64_t tag = pos < n ? w[pos] : -1;
-      const bool guardable = cancel_every > 0 && tag != T_ALLREDUCE && tag != T_JOIN;
+      const bool guardable = cancel_every > 0 && tag != T_ALLREDUCE && tag != T_JOIN && tag != T_NVLS_AR &&
+                             tag != T_NVLS_ZERO;
       if (body && (!guardable || p->n_kernel_nodes - seg0 >= cancel_every)) {
         int rc = close();
         if (rc) return rc;
@@ -3028,6 +3354,7 @@ struct Builder {
         int nL = 0;
         int rc = build_launches(c, s, L, &nL);
         if (rc) return rc;
+        nvls_fuse(s.out, L, &nL);
         p->n_compute += nL;
         for (int i = 0; i < nL; ++i) {
           rc = add_kernel(g, prev, L[i]);
@@ -3082,6 +3409,7 @@ struct Builder {
         }
         rc = build_xop(c, s, L, &nL, &wb, &pzb);
         if (rc) return rc;
+        nvls_fuse(s.out, L, &nL);
         p->n_compute += nL;
         for (int i = 0; i < nL; ++i) {
           rc = add_kernel(g, prev, L[i]);
@@ -3196,6 +3524,73 @@ struct Builder {
         int rc = add_allreduce(g, &branch, b, count, is_f64(c) ? kNcclDouble : kNcclFloat, avg ? kNcclAvg : kNcclSum);
         if (rc) return rc;
         pending_ar.push_back({g, branch});
+        return COEX_OK;
+      }
+      case T_NVLS_ZERO: {                           // list start: red targets zeroed on every rank
+        char* lo = buf(next());
+        const int64_t last = next();
+        if (last < 0 || last >= (int64_t)bufs.size()) throw std::runtime_error("bad NVLS zero range");
+        char* hi = bufs[last] + sizes[last];
+        if (!in_nv(lo) || !in_nv(hi - 1) || hi <= lo) throw std::runtime_error("NVLS zero range outside the region");
+        NvlsZeroParams q{};
+        q.ds = c->d_state;
+        q.p = (float4*)lo;
+        q.n4 = (int64_t)((hi - lo + 15) / 16);
+        Launch L;
+        L.set((void*)k_nvls_zero, grid_for(q.n4), dim3(256), q);
+        int rc = add_kernel(g, prev, L);
+        if (rc) return rc;
+        return nvls_barrier(g, prev);               // no rank adds before every copy is zero
+      }
+      case T_NVLS_AR: {                             // bucket over the multicast region
+        char* lo = buf(next());
+        const int64_t count = next();
+        const int64_t avg = next();
+        const int64_t async = next();
+        char* hi = lo + count * 4;
+        if (is_f64(c) || !in_nv(lo) || !in_nv(hi - 1)) throw std::runtime_error("bad NVLS bucket");
+        // spans of the bucket the GEMM epilogues did not reduce (other producers' outputs)
+        std::vector<std::pair<char*, char*>> red;
+        for (auto& r : nv_red)
+          if (r.second > lo && r.first < hi) red.push_back(r);
+        std::sort(red.begin(), red.end());
+        if (avg && !red.empty()) throw std::runtime_error("NVLS average bucket with GEMM-reduced members");
+        std::vector<NvlsSpan> spans;
+        char* cur = lo;
+        for (auto& r : red) {
+          if (r.first > cur) spans.push_back({(long long)((cur - c->nv_local) / 4), (long long)((r.first - cur) / 4)});
+          if (r.second > cur) cur = (char*)(((uintptr_t)r.second + 15) & ~(uintptr_t)15);   // padding to the next buffer
+        }
+        if (cur < hi) spans.push_back({(long long)((cur - c->nv_local) / 4), (long long)((hi - cur + 3) / 4)});
+        cudaGraphNode_t branch = *prev;
+        cudaGraphNode_t* at = async ? &branch : prev;
+        int rc = nvls_barrier(g, at);               // every rank's producers (and reds) are done
+        if (rc) return rc;
+        if (!spans.empty()) {
+          for (size_t s0 = 0; s0 < spans.size(); s0 += kNvlsMaxSpans) {
+            NvlsAllReduceParams q{};
+            q.ds = c->d_state;
+            q.mode = c->nv_mode;
+            if (c->nv_mode == RED_MC) q.base[0] = (float*)c->nv_mc;
+            else for (int r = 0; r < c->nv_world; ++r) q.base[r] = (float*)c->nv_peer[r];
+            q.rank = c->rank;
+            q.world = c->nv_world;
+            q.scale = avg ? 1.0f / (float)c->nv_world : 1.0f;
+            long long tot = 0;
+            for (size_t j = s0; j < spans.size() && j < s0 + kNvlsMaxSpans; ++j) {
+              q.spans[q.nspans++] = spans[j];
+              tot += spans[j].n;
+            }
+            Launch L;
+            L.set((void*)k_nvls_allreduce, grid_for(tot / 4 / (c->nv_world > 0 ? c->nv_world : 1) + 1), dim3(256), q);
+            rc = add_kernel(g, at, L);
+            if (rc) return rc;
+          }
+          rc = nvls_barrier(g, at);                 // every rank's stores landed
+          if (rc) return rc;
+        }
+        p->n_collectives++;
+        if (async) pending_ar.push_back({g, branch});
         return COEX_OK;
       }
       case T_JOIN: {                                // chain += every pending collective of this graph
@@ -3387,11 +3782,21 @@ int coex_prog_build(coex_ctx* c, const int64_t* plan, int64_t nwords, const doub
     size_t total = 0;
     // a negative entry is a VIEW: -(1 + parent << 40 + byte offset) into an earlier buffer
     // (planner _arm_views: arm-exclusive activations of a SwitchCase share one region)
-    for (int64_t i = 0; i < nbufs; ++i) {
-      sizes[i] = b.next();
-      if (sizes[i] >= 0) total += ((size_t)sizes[i] + 255) & ~(size_t)255;
+    for (int64_t i = 0; i < nbufs; ++i) sizes[i] = b.next();
+    // NVLS plans: the listed buffers (sum-reduced gradient bucket members) live in the
+    // context's multicast-mapped region instead of the arena, in index order
+    const int64_t n_nv = b.next();
+    std::vector<char> in_nv(nbufs, 0);
+    for (int64_t i = 0; i < n_nv; ++i) {
+      const int64_t bi = b.next();
+      if (bi < 0 || bi >= nbufs || sizes[bi] < 0) throw std::runtime_error("bad NVLS buffer");
+      in_nv[bi] = 1;
     }
+    if (n_nv > 0 && c->nv_local == nullptr) throw std::runtime_error("NVLS plan without an NVLS region");
+    for (int64_t i = 0; i < nbufs; ++i)
+      if (sizes[i] >= 0 && !in_nv[i]) total += ((size_t)sizes[i] + 255) & ~(size_t)255;
     p->arena_bytes = total;
+    size_t nv_off = kNvlsFlagBytes;
     if (total) CK(cudaMalloc(&p->arena, total));
     size_t off = 0;
     for (int64_t i = 0; i < nbufs; ++i) {
@@ -3403,9 +3808,16 @@ int coex_prog_build(coex_ctx* c, const int64_t* plan, int64_t nwords, const doub
         sizes[i] = sizes[parent] - boff;            // bound for the spare below
         continue;
       }
+      if (in_nv[i]) {
+        if (nv_off + (size_t)sizes[i] > c->nv_bytes) throw std::runtime_error("NVLS region too small for the plan");
+        b.bufs.push_back(c->nv_local + nv_off);
+        nv_off += ((size_t)sizes[i] + 255) & ~(size_t)255;
+        continue;
+      }
       b.bufs.push_back(p->arena + off);
       off += ((size_t)sizes[i] + 255) & ~(size_t)255;
     }
+    b.sizes = sizes;
     p->ncells = b.next();
     std::vector<void*> init(p->ncells > 0 ? p->ncells : 1, nullptr);
     for (int64_t i = 0; i < p->ncells; ++i) init[i] = b.buf(b.next());
@@ -3538,6 +3950,11 @@ int coex_prog_destroy(coex_prog* p) {
   if (p->late) cudaFree(p->late);
   for (void* w : p->workspaces) cudaFree(w);
   delete p;
+  return COEX_OK;
+}
+
+int coex_prog_nvls(coex_prog* p, int64_t* fused) {
+  *fused = p ? p->n_nvls_fused : 0;
   return COEX_OK;
 }
 

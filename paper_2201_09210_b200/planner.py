@@ -32,10 +32,12 @@ from .graph_gen import ExecOp, InputFeed, OutputFetch, SwitchCase, SymProgram, U
 from .tensor import BMM_KINDS, CONV_ATTR_KINDS, CONV_KINDS, OpKind, flops_of, infer_shape, shape_size
 
 MAGIC = 0xC0E8B200
-VERSION = 3
+VERSION = 4
 T_SEQ, T_OP, T_PTR, T_FEED, T_FETCH, T_SWITCH, T_WHILE, T_CHAIN, T_ALLREDUCE, T_XOP, T_MCHAIN = 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11
 T_ATTN = 12               # fused causal attention (csrc attn_tc.cuh): forward / backward of one layer
 T_JOIN = 13               # the chain waits for every asynchronous all-reduce issued so far in its list
+T_NVLS_AR = 14            # gradient bucket over the NVLS multicast region (csrc/nvls.cuh)
+T_NVLS_ZERO = 15          # list start: the region's red targets zeroed on every rank + barrier
 AR_BUCKET_BYTES = int(os.environ.get("COEX_AR_BUCKET_MB", "64")) << 20
 MAX_MCHAIN = 8            # chains per k_chain_multi launch (csrc kMaxMultiChain)
 PTR_ALIAS, PTR_READ_VAR, PTR_ASSIGN_VAR = 0, 1, 2
@@ -73,6 +75,14 @@ class _ARBucket:
 
 class _Join:
     """The chain waits for the list's asynchronous all-reduces (before their first reader)."""
+
+
+class _NvlsZero:
+    """List start of an NVLS plan: zero the list's bucket buffers [first, last] on every rank
+    and barrier, before any GEMM epilogue adds into them (csrc/nvls.cuh)."""
+
+    def __init__(self, first: int, last: int):
+        self.first, self.last = first, last
 
 
 class _Attn:
@@ -131,8 +141,11 @@ class Plan:
 
 class Planner:
     def __init__(self, sp: SymProgram, tg, var_index: dict, var_shapes: dict, feed_shapes: dict, esize: int,
-                 bf16: bool = False, fuse: bool = True, force_store=(), const_slots=None):
+                 bf16: bool = False, fuse: bool = True, force_store=(), const_slots=None, nvls_bytes: int = 0):
         self.force_store = set(force_store)
+        # data parallel over an NVLS region of this many bytes (B200Backend._init_nvls): sum
+        # all-reduced gradients live there, reduced by their GEMM epilogues (csrc/nvls.cuh)
+        self.nvls_bytes = int(nvls_bytes) if esize == 4 else 0
         self.const_slots = dict(const_slots or {})
         self.bf16 = bf16
         self.fuse = fuse
@@ -207,8 +220,24 @@ class Planner:
         return shapes
 
     # ------------------------------------------------------------ plan
+    def _nvls_lists_ok(self, insts) -> bool:
+        """Every sum all-reduce of a list has its producer inside that list (so the list-start
+        zeroing of the NVLS buffers precedes every epilogue that adds into them)."""
+        made = {x.node_id for x in walk(insts) if isinstance(x, ExecOp)}
+        for x in insts:
+            if type(x).__name__ == "AllReduce" and not x.avg and x.node_id not in made:
+                return False
+            subs = (x.cases if isinstance(x, SwitchCase) else [x.body] if isinstance(x, While)
+                    else x.bodies if isinstance(x, UnrolledLoop) else [])
+            if not all(self._nvls_lists_ok(b) for b in subs):
+                return False
+        return True
+
     def build(self) -> Plan:
         shapes = self.infer_shapes()
+        # NVLS: sum all-reduced (gradient) nodes get buffers in the multicast region
+        self.nvls = self.nvls_bytes > 0 and AR_BUCKET_BYTES > 0 and self._nvls_lists_ok(self.sp.body)
+        self.nvls_bufs = []
         ops = self.ops
         # consumers of every node id (over all bindings)
         consumers: dict = {}
@@ -274,13 +303,18 @@ class Planner:
                 ar_order.append(x.node_id)
         self._ar_pos = {nid: i for i, nid in enumerate(ar_order)}
         ar_set = set(ar_order)
+        ar_sum = {x.node_id for x in walk(self.sp.body) if type(x).__name__ == "AllReduce" and not x.avg}
         arm_view = self._arm_views(consumers, multi, folded, shapes, new_buf, new_view)
         for nid in ar_order + [n for n in ops if n not in ar_set]:
             x = ops[nid]
             n = shape_size(shapes[nid])
             if x.kind in COMPUTE and nid not in folded and nid not in self.index_nodes:
                 self_dep = any((not b.fed) and nid in b.cands for b in x.inputs)
-                b0 = arm_view[nid] if nid in arm_view else new_buf(n * self.esize)
+                if self.nvls and nid in ar_sum and not self_dep:
+                    b0 = new_buf(n * self.esize)            # own buffer in the multicast region
+                    self.nvls_bufs.append(b0)
+                else:
+                    b0 = arm_view[nid] if nid in arm_view else new_buf(n * self.esize)
                 b1 = new_buf(n * self.esize) if self_dep else -1
                 node_buf[nid] = (b0, b1, self_dep)
                 vcell[nid] = new_cell(b0)
@@ -291,6 +325,9 @@ class Planner:
                 vcell[nid] = new_cell(b0)
             else:
                 vcell[nid] = new_cell(-1)
+        if self.nvls and sum((max(bufs[b], 16) + 255) // 256 * 256 for b in self.nvls_bufs) > self.nvls_bytes:
+            self.nvls, self.nvls_bufs = False, []            # does not fit: NCCL buckets in the arena
+        self.nvls_set = set(self.nvls_bufs)
         # bf16 shadows: a softmax-type node whose output feeds batched GEMMs as operand A also
         # writes a bf16 copy, which those GEMMs read instead of converting the fp32 tensor
         self.shadow = {}
@@ -538,6 +575,8 @@ class Planner:
                     if b0 < 0 or pp:
                         raise NeedsReplicated(f"node {x.node_id} has no static buffer to all-reduce")
                     items.append([T_ALLREDUCE, b0, shape_size(shapes[x.node_id]), int(x.avg), 0])
+                elif isinstance(x, _NvlsZero):
+                    items.append([T_NVLS_ZERO, x.first, x.last])
                 elif isinstance(x, _ARBucket):
                     self._invalidate()
                     first = node_buf[x.members[0].node_id][0]
@@ -546,7 +585,8 @@ class Planner:
                     for i, m in enumerate(x.members):
                         nbytes = shape_size(shapes[m.node_id]) * self.esize
                         span += nbytes if i == len(x.members) - 1 else (max(nbytes, 16) + 255) // 256 * 256
-                    items.append([T_ALLREDUCE, first, span // self.esize, int(x.members[0].avg), 1])
+                    tag = T_NVLS_AR if first in self.nvls_set else T_ALLREDUCE
+                    items.append([tag, first, span // self.esize, int(x.members[0].avg), 1])
                     self.n_ar_buckets += 1
                 elif isinstance(x, _Join):
                     items.append([T_JOIN])
@@ -562,6 +602,7 @@ class Planner:
 
         body = seq(self.sp.body)
         w += [MAGIC, VERSION, len(bufs)] + bufs
+        w += [len(self.nvls_bufs)] + self.nvls_bufs
         w += [len(cell_init)] + cell_init
         w += [len(slot_rec), late_count[0] + self.chain_lates]
         w += [len(fills)]
@@ -578,6 +619,9 @@ class Planner:
                tuple(sorted((k, tuple(v)) for k, v in self.feed_shapes.items())))
         plan = Plan(w, consts, sig, n_compute[0], flops[0], shapes, dict(self.feed_shapes), folded, self.n_attn)
         plan.const_slots = dict(self.const_slots)
+        plan.nvls_bufs = len(self.nvls_bufs)         # gradient buffers in the NVLS region
+        plan.nvls_buckets = sum(1 for lst in self._ar_lists for x in lst if isinstance(x, _ARBucket)
+                                and self._node_buf[x.members[0].node_id][0] in self.nvls_set)
         return plan
 
     def _exec(self, x, shapes, in_cell, out_words, ptr_item, pubs, multi, folded, n_compute, flops) -> list:
@@ -1411,6 +1455,11 @@ class Planner:
                 join()                                   # control flow: everything settles first
             out.append(x)
         join()
+        # NVLS: the list's bucket buffers are zeroed (every rank) before anything adds into them
+        nv = [node_buf[m.node_id][0] for x in out if isinstance(x, _ARBucket) for m in x.members
+              if node_buf[m.node_id][0] in self.nvls_set]
+        if nv:
+            out.insert(0, _NvlsZero(min(nv), max(nv)))
         self._ar_lists.append(out)
         return out
 

@@ -153,6 +153,60 @@ def test_dp_allreduce_buckets(which):
     assert n_coll < n_ar, (n_coll, n_ar)
 
 
+@pytest.mark.parametrize("which", ["c2", "c4"])
+def test_dp_nvls_buckets(which):
+    """NVLS plans (csrc/nvls.cuh): every sum all-reduced gradient gets a buffer in the
+    multicast region (the plan header's NVLS list), every bucket over them is a T_NVLS_AR
+    item, and each list holding such buckets starts with ONE T_NVLS_ZERO over its bucket
+    buffers -- before any producer (the GEMM epilogues add into zeroed copies).  Average
+    all-reduces (the loss) stay NCCL buckets in the arena; a region too small for the
+    plan's gradients falls back to NCCL entirely."""
+    from paper_2201_09210_b200.dp import local_feed_shapes, shard_program
+    from paper_2201_09210_b200.graph_gen import ExecOp
+    from paper_2201_09210_b200.planner import MAGIC, _ARBucket, _NvlsZero, walk
+    src = dcgan_program(steps=8, **C2_SMALL) if which == "c2" else gpt2_program(steps=6, **C4_SMALL)
+    o = make_orch(src, SyntheticDataset(0), CpuBackend())
+    for _ in range(5):
+        o.step()
+    feed = {(n.id, p): tuple(s) for n in o.tg.all_nodes() if n.typ == "op" for p, s in n.feed_shapes.items()}
+    vs = o.be.var_shapes()
+    vi = {k: j for j, k in enumerate(sorted(vs))}
+    gshapes = Planner(o.sp, o.tg, vi, vs, feed, 4).infer_shapes()
+    batch = (C2_SMALL if which == "c2" else C4_SMALL)["batch"]
+    dplan = shard_program(o.sp, feed, gshapes, batch, 2)
+    assert not dplan.replicated, dplan.reason
+
+    def build(nbytes):
+        pl = Planner(dplan.sp, o.tg, vi, vs, local_feed_shapes(feed, dplan), 4, bf16=True,
+                     force_store=dplan.allreduce_nodes, nvls_bytes=nbytes)
+        return pl, pl.build()
+
+    pl, plan = build(1 << 30)
+    sums = {x.node_id for x in walk(dplan.sp.body) if type(x).__name__ == "AllReduce" and not x.avg}
+    assert sums and plan.nvls_bufs == len(sums) and plan.nvls_buckets >= 1
+    w = plan.words
+    assert w[0] == MAGIC and w[3 + w[2]] == len(pl.nvls_bufs)
+    assert w[4 + w[2]: 4 + w[2] + len(pl.nvls_bufs)] == pl.nvls_bufs
+    assert {pl._node_buf[n][0] for n in sums} == set(pl.nvls_bufs)
+    for lst in pl._ar_lists:
+        nv = [x for x in lst if isinstance(x, _ARBucket) and pl._node_buf[x.members[0].node_id][0] in pl.nvls_set]
+        zeros = [i for i, x in enumerate(lst) if isinstance(x, _NvlsZero)]
+        if not nv:
+            assert not zeros
+            continue
+        assert zeros == [0]
+        z = lst[0]
+        for x in nv:
+            assert all(not m.avg for m in x.members)
+            for m in x.members:
+                assert z.first <= pl._node_buf[m.node_id][0] <= z.last
+        produced = [i for i, x in enumerate(lst) if isinstance(x, ExecOp) and x.node_id in sums]
+        assert produced and min(produced) > 0
+    # too small a region: the whole plan keeps NCCL buckets
+    pl2, plan2 = build(4096)
+    assert plan2.nvls_bufs == 0 and plan2.nvls_buckets == 0 and pl2.n_ar_buckets >= 1
+
+
 def test_bias_add_fused_into_gemm():
     """C4: every projection's bias_add(matmul(a, w), c) becomes the GEMM's epilogue (one plan
     op publishing the bias_add's output); the bias_add is never launched on its own."""
