@@ -639,6 +639,8 @@ def run_b200(args):
     from paper_2201_09210_b200.dp import DPGroup
     src, dataset, recs, h2d, cfg, gbatch = workload_setup(args, world)
     dp = DPGroup(rank, world, gbatch) if (world > 1 and gbatch is not None) else None
+    if dp is None and args.force_dp and gbatch is not None:
+        dp = DPGroup(0, 1, gbatch, force=True)     # 1-rank sharded program: the DP graph's cost on one GPU
     dev = local if world > 1 else 0
     be = B200Backend(device=dev, precision=args.precision, dp=dp)
     o = make_orch(src, dataset, be)
@@ -709,6 +711,13 @@ def run_b200(args):
         cfg.update({"l2": "flushed (256 MiB write) between timed steps", "tracing_steps_before_coexec": pre,
                     "settle_steps_before_warmup": settled,
                     "steps_replayed_in_timed_region": replays})
+        if dp is not None:
+            cfg["gradient_reduction"] = (
+                "GEMM-epilogue reduction into the shared gradient region (" + be.nvls_mode
+                + " transport, csrc/nvls.cuh)" if be.nvls_bytes else
+                "NCCL all-reduce buckets captured into the pass graph")
+            if dp.force:
+                cfg["parallelism"] = "forced 1-rank data-parallel program (collective path measured on one GPU)"
         line = {
             "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(t_max / args.steps, 5), "higher_is_better": True,
@@ -744,6 +753,9 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-tensor-gemm", action="store_true")
+    ap.add_argument("--force-dp", action="store_true",
+                    help="N=1: run the data-parallel program on a forced 1-rank group (collectives in the graph; "
+                         "COEX_NVLS=0/1 selects NCCL buckets or the GEMM-epilogue reduction)")
     ap.add_argument("--eager-families", action="store_true",
                     help="also re-launch every op of the step eagerly for a per-family table")
     args = ap.parse_args()
