@@ -570,7 +570,7 @@ class Planner:
                     for b in x.bodies:
                         items.extend(emit(b))
                 elif type(x).__name__ == "AllReduce":
-                    self._invalidate()
+                    self._invalidate(pubs[x.node_id])      # only the reduced value changes
                     b0, b1, pp = node_buf.get(x.node_id, (-1, -1, True))
                     if b0 < 0 or pp:
                         raise NeedsReplicated(f"node {x.node_id} has no static buffer to all-reduce")
@@ -578,7 +578,9 @@ class Planner:
                 elif isinstance(x, _NvlsZero):
                     items.append([T_NVLS_ZERO, x.first, x.last])
                 elif isinstance(x, _ARBucket):
-                    self._invalidate()
+                    # only the members' values change (shared bf16 operand copies of anything
+                    # else stay valid across the collective)
+                    self._invalidate([c for m in x.members for c in pubs[m.node_id]])
                     first = node_buf[x.members[0].node_id][0]
                     # span of the adjacent arena buffers (each padded to 256 bytes, csrc plan load)
                     span = 0
@@ -989,8 +991,11 @@ class Planner:
             lo, hi = pos[x.node_id], pos[g.node_id]
             srcs = {c for b in x.inputs if not b.fed for c in b.cands}
             fed = {b.slot for b in x.inputs if b.fed}
+            # (data parallel: the loss's all-reduce sits between them -- it reads the loss only)
             if any((isinstance(y, ExecOp) and y.node_id in srcs) or (isinstance(y, InputFeed) and y.slot in fed)
-                   or not isinstance(y, (ExecOp, InputFeed, OutputFetch)) for y in insts[lo + 1:hi]):
+                   or not (isinstance(y, (ExecOp, InputFeed, OutputFetch))
+                           or (type(y).__name__ == "AllReduce" and y.node_id not in srcs))
+                   for y in insts[lo + 1:hi]):
                 continue
             out[x.node_id] = g
             self._ce_loss[g.node_id] = x
@@ -1030,7 +1035,10 @@ class Planner:
                 continue
             mem = [d, g, sr]
             ids = {m.node_id for m in mem}
-            if any(n in self.sp.fetch_nodes or n in multi_nodes or n in self.force_store for n in ids):
+            # all-reduced (pinned) members are fine: the fused op writes every member's own
+            # buffer, and a bucket holding a member between the positions forces the first-
+            # member placement below (everything is produced before the collective)
+            if any(n in self.sp.fetch_nodes or n in multi_nodes for n in ids):
                 continue
             lo = min(pos[m.node_id] for m in mem)
             hi = max(pos[m.node_id] for m in mem)
@@ -1059,7 +1067,9 @@ class Planner:
                 # x, dy or the first member's own inputs, and there is no control flow between
                 first = insts[lo]
                 srcs = {c for m in mem for b in m.inputs if not b.fed for c in b.cands}
-                ok = all(isinstance(y, (ExecOp, InputFeed)) and
+                ok = all((isinstance(y, (ExecOp, InputFeed)) or
+                          (isinstance(y, _ARBucket) and not any(m.node_id in srcs for m in y.members))
+                          or isinstance(y, _Join)) and
                          not (isinstance(y, ExecOp) and y.node_id not in ids and y.node_id in srcs)
                          for y in insts[lo:hi + 1])
                 # the members' own inputs must all exist at the first position
