@@ -272,7 +272,9 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 // convolution, A MN-major (weight gradient: M = (tap, channel), K = pixels).  B_MN: B stored
 // [K][N].  MN-major operands are loaded as 64 x 64 boxes and consumed through MN-major
 // descriptors, so no transposition pass is needed.
-template <int BN, int AMODE, bool B_MN, bool DUO = false>
+// RED: the epilogue adds into the data-parallel gradient region (nvls.cuh) instead of
+// storing -- a separate instantiation so the plain epilogue's code is untouched
+template <int BN, int AMODE, bool B_MN, bool DUO = false, bool RED = false>
 __global__ void __launch_bounds__(TC_THREADS, DUO ? 2 : 1) k_gemm_tc(const __grid_constant__ TcGemmParams p) {
   COEX_PDL_ENTER();
   constexpr int STAGES = TcCfg<BN, DUO>::STAGES;
@@ -534,7 +536,7 @@ __global__ void __launch_bounds__(TC_THREADS, DUO ? 2 : 1) k_gemm_tc(const __gri
             }
             float* dst = C + orow * p.N + gcol;
             v.x += bv.x; v.y += bv.y; v.z += bv.z; v.w += bv.w;
-            if (p.red.mode != RED_NONE) {           // gradient bucket member: reduce across ranks
+            if constexpr (RED) {                     // gradient bucket member: reduce across ranks
               const int nv = (int)(p.N - gcol < 4 ? p.N - gcol : 4);
               red_store4(p.red, dst, v, vec_ok && gcol + 4 <= p.N, nv);
             } else if (vec_ok && gcol + 4 <= p.N) {

@@ -106,6 +106,9 @@ struct Launch {
   // tcgen05 GEMM whose result lands in the op's Out (1: the GEMM itself, 2: its split-K
   // reduction) -- the NVLS fusion retargets these (Builder::nvls_fuse)
   int tc_dest = 0;
+  void* fn_red = nullptr;      // the GEMM's epilogue-reduction instantiation (nullptr: none)
+  unsigned red_grid = 0;       // its grid / dynamic shared memory (single-CTA-per-SM variant)
+  size_t red_smem = 0;
   void allreduce(void* b, int64_t n, bool f64) {
     fn = nullptr;
     ar_buf = b;
@@ -1059,6 +1062,27 @@ void* tc_fn(int amode, bool bmn) {
     default: return (void*)k_gemm_tc<BN, 3, true, DUO>;
   }
 }
+// epilogue-reduction variants (nvls.cuh) of the single-CTA kernels; nullptr: none (amode 2)
+template <int BN>
+void* tc_fn_red(int amode, bool bmn) {
+  switch (amode) {
+    case 0: return bmn ? (void*)k_gemm_tc<BN, 0, true, false, true> : (void*)k_gemm_tc<BN, 0, false, false, true>;
+    case 1: return bmn ? (void*)k_gemm_tc<BN, 1, true, false, true> : (void*)k_gemm_tc<BN, 1, false, false, true>;
+    case 3: return (void*)k_gemm_tc<BN, 3, true, false, true>;
+    default: return nullptr;
+  }
+}
+template <int BN>
+int tc_attr_red(int amode, bool bmn) {
+  static bool done[8] = {false};
+  const int i = amode * 2 + (bmn ? 1 : 0);
+  void* f = tc_fn_red<BN>(amode, bmn);
+  if (f && !done[i]) {
+    CK(cudaFuncSetAttribute((const void*)f, cudaFuncAttributeMaxDynamicSharedMemorySize, TcCfg<BN>::SMEM));
+    done[i] = true;
+  }
+  return COEX_OK;
+}
 template <int BN, bool DUO = false>
 int tc_attr(int amode, bool bmn) {
   static bool done[8] = {false};
@@ -1179,11 +1203,23 @@ int tc_gemm_launches(coex_ctx* c, DevState* ds, void* a16, void* b16, int64_t M,
     rc = t.bn == 64 ? tc_attr<64, true>(amode, b_mn) : tc_attr<128, true>(amode, b_mn);
   } else {
     fn = t.bn == 64 ? tc_fn<64>(amode, b_mn) : t.bn == 128 ? tc_fn<128>(amode, b_mn) : tc_fn<256>(amode, b_mn);
+
     G.set(fn, dim3((unsigned)(items < kNumSMs ? items : kNumSMs)), dim3(TC_THREADS), gp);
     G.smem = t.bn == 64 ? TcCfg<64>::SMEM : t.bn == 128 ? TcCfg<128>::SMEM : TcCfg<256>::SMEM;
     rc = t.bn == 64 ? tc_attr<64>(amode, b_mn) : t.bn == 128 ? tc_attr<128>(amode, b_mn) : tc_attr<256>(amode, b_mn);
   }
   if (rc) return rc;
+  // a possible gradient-region output (Builder::nvls_fuse): the single-CTA epilogue-reduction
+  // instantiation of the same tile width (a DUO launch is retargeted to it)
+  if (raw == nullptr && c->nv_local != nullptr) {
+    G.fn_red = t.bn == 64 ? tc_fn_red<64>(amode, b_mn) : t.bn == 128 ? tc_fn_red<128>(amode, b_mn)
+                                                         : tc_fn_red<256>(amode, b_mn);
+    rc = t.bn == 64 ? tc_attr_red<64>(amode, b_mn) : t.bn == 128 ? tc_attr_red<128>(amode, b_mn)
+                                                   : tc_attr_red<256>(amode, b_mn);
+    if (rc) return rc;
+    G.red_grid = (unsigned)(items < kNumSMs ? items : kNumSMs);
+    G.red_smem = t.bn == 64 ? TcCfg<64>::SMEM : t.bn == 128 ? TcCfg<128>::SMEM : TcCfg<256>::SMEM;
+  }
   if (t.splits > 1) {
     SplitReduceParams r{};
     r.ds = ds;
@@ -3166,7 +3202,7 @@ struct Builder {
     int gi = -1, ng = 0;
     for (int i = 0; i < *nL; ++i)
       if (L[i].tc_dest == 1) { gi = i; ++ng; }
-    if (ng != 1) return;
+    if (ng != 1 || L[gi].fn_red == nullptr) return;
     TcGemmParams* gp = (TcGemmParams*)L[gi].params;
     if (gp->has_bias || gp->cv.phases > 1 || gp->batch > 1 || gp->tri_out || gp->tri_a) return;
     for (int i = 0; i < *nL; ++i)
@@ -3174,6 +3210,9 @@ struct Builder {
     const size_t bytes = (size_t)gp->M * (size_t)gp->N * 4;
     char* lo = (char*)o.buf[0];
     if (lo + bytes > c->nv_local + c->nv_bytes) return;
+    L[gi].fn = L[gi].fn_red;
+    L[gi].grid = dim3(L[gi].red_grid);
+    L[gi].smem = L[gi].red_smem;
     gp->red.mode = c->nv_mode;
     if (c->nv_mode == RED_MC) {
       gp->red.npeers = 1;
