@@ -1944,6 +1944,20 @@ int build_xop_t(coex_ctx* c, const OpSpec& s, Launch* L, int* nL, size_t* ws_byt
             return COEX_OK;
           }
           const bool wide = V >= 8192;
+          // wide rows whose halves fit 110 KB: a CTA pair per row, two pairs' CTAs per SM
+          // (COEX_CE_PAIR=0: one 1024-thread CTA per row)
+          const char* cpe = getenv("COEX_CE_PAIR");
+          if (wide && (size_t)((V + 1) / 2 + 8) * 4 <= 110 * 1024 && !(cpe && cpe[0] == '0')) {
+            static bool pair_attr = false;
+            if (!pair_attr) {
+              CK(cudaFuncSetAttribute((void*)k_ce_pair<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024));
+              pair_attr = true;
+            }
+            const int64_t pairs = R < kNumSMs ? R : kNumSMs;
+            L[*nL].set((void*)k_ce_pair<512>, dim3((unsigned)(2 * pairs)), dim3(512), rp);
+            L[(*nL)++].smem = (size_t)((V + 1) / 2 + 8) * 4;
+            return COEX_OK;
+          }
           void* fn = wide ? (void*)k_ce_fused<1024> : (void*)k_ce_fused<128>;
           static bool attr_set = false;
           if (!attr_set) {

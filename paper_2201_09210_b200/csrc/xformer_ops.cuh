@@ -8,6 +8,7 @@
 // accumulator scheme of k_colstats.  The batched GEMMs (bmm*) are lowered by the runtime
 // to the tcgen05 kernel (bf16 mode, 3-D tensor maps) or the batched SIMT kernel.
 #pragma once
+#include <cooperative_groups.h>
 #include "ext_ops.cuh"
 
 namespace coex {
@@ -873,6 +874,142 @@ __global__ void __launch_bounds__(NT) k_ce_fused(RowParams p) {
       for (long long k = V + threadIdx.x; k < p.spitch; k += NT) srow16[k] = __float2bfloat16_rn(0.f);
     __syncthreads();                                  // srow reused by the next row
   }
+  publish_late(p.out, o);
+  if (!last_block(p.counter)) return;
+  if (threadIdx.x == 0) {
+    double acc = 0.0;
+    for (long long r = 0; r < p.rows; ++r) acc += __ldcg(p.acc + r);
+    lo[0] = (float)(acc / (double)p.rows);
+    *p.counter = 0u;
+    for (int i = 0; i < p.out2.npub; ++i) *p.out2.pub[i] = lo;
+  }
+}
+
+// Fused cross-entropy over a CTA PAIR per row (wide vocabularies, C4: 50257): each CTA of a
+// 2-CTA cluster stages one half of the row in shared memory (100 KB, so two CTAs -- two rows
+// -- are resident per SM and one row's load phase overlaps the other's exp / store phases,
+// where the one-CTA-per-row kernel leaves HBM idle); the pair combines its max and sum of
+// exponentials through distributed shared memory (two cluster barriers per row).  Same
+// arithmetic per element as k_ce_fused; the row sum is the two halves' sums added.
+template <int NT>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT) k_ce_pair(RowParams p) {
+  COEX_PDL_ENTER();
+  stamp(p.ds, SK_CE);
+  extern __shared__ float srow[];
+  __shared__ float red[NT / 32];
+  __shared__ float xch[2];                          // this CTA's (max, sum) for the peer
+  __shared__ __align__(8) uint64_t lbar;            // bulk-copy completion of the staged half row
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  const unsigned crank = cl.block_rank();
+  const float* peer = cl.map_shared_rank(&xch[0], crank ^ 1u);
+  const float* lg = res<float>(p.x);
+  const float* ids = res<float>(p.y);
+  float* o = pick_out<float>(p.out, lg, ids);
+  float* lo = pick_out<float>(p.out2, lg, ids);
+  publish_early(p.out, o);
+  count_op(p.ds);
+  const long long V = p.d, half = (V + 1) / 2;
+  const long long c0 = crank * half, cn = (c0 + half < V ? c0 + half : V) - c0;
+  const float invr = (float)(1.0 / (p.scale > 0.0 ? p.scale : (double)p.rows));
+  const long long pairs = gridDim.x / 2;
+  uint32_t lphase = 0;
+  if (threadIdx.x == 0) {
+    mbar_init(&lbar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  for (long long r = blockIdx.x / 2; r < p.rows; r += pairs) {
+    // stage the half row: its 16-byte-aligned body by ONE bulk copy (the copy engine keeps
+    // the whole 100 KB in flight; the other resident CTA computes meanwhile), the <= 3 head /
+    // tail scalars by plain loads.  Element k lives at srow[k + sh], sh = 4 - head, so the
+    // body lands 16-byte aligned at srow[4].
+    const float* row = lg + r * V + c0;
+    const int head = (int)(((16 - ((uintptr_t)row & 15)) & 15) / 4) < cn ? (int)(((16 - ((uintptr_t)row & 15)) & 15) / 4)
+                                                                           : (int)cn;
+    const long long nb4 = (cn - head) / 4;            // 16-byte body groups
+    const int sh = 4 - head;
+    float* st = srow + sh;
+    if (threadIdx.x == 0 && nb4 > 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic smem use of the last row
+      mbar_expect_tx(&lbar, (uint32_t)(nb4 * 16));
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       smem_u32(srow + 4)),
+                   "l"(row + head), "r"((uint32_t)(nb4 * 16)), "r"(smem_u32(&lbar))
+                   : "memory");
+    }
+    if (threadIdx.x < head) st[threadIdx.x] = __ldcs(row + threadIdx.x);
+    for (long long k = head + nb4 * 4 + threadIdx.x; k < cn; k += NT) st[k] = __ldcs(row + k);
+    if (nb4 > 0) {
+      mbar_wait(&lbar, lphase);
+      lphase ^= 1u;
+    }
+    __syncthreads();
+    // smem passes over the staged half: the aligned body as float4 (srow[4 ..]), the head
+    // (srow[sh .. 3]) and tail scalars apart -- a quarter of the instructions per element
+    const int n4 = (int)nb4;
+    const int tail0 = head + 4 * n4, ncn = (int)cn;
+    float4* body4 = (float4*)(srow + 4);
+    float mx = -INFINITY;
+    for (int q = threadIdx.x; q < n4; q += NT) {
+      const float4 v = body4[q];
+      mx = fmaxf(mx, fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w)));
+    }
+    if (threadIdx.x < head) mx = fmaxf(mx, st[threadIdx.x]);
+    for (int k = tail0 + threadIdx.x; k < ncn; k += NT) mx = fmaxf(mx, st[k]);
+    float lm = block_reduce<NT>(mx, true, red);
+    if (threadIdx.x == 0) xch[0] = lm;
+    cl.sync();
+    const float gm = fmaxf(lm, peer[0]);
+    float sm = 0.f;
+    for (int q = threadIdx.x; q < n4; q += NT) {
+      float4 v = body4[q];
+      v.x = __expf(v.x - gm); v.y = __expf(v.y - gm); v.z = __expf(v.z - gm); v.w = __expf(v.w - gm);
+      body4[q] = v;
+      sm += (v.x + v.y) + (v.z + v.w);
+    }
+    if (threadIdx.x < head) {
+      const float e = __expf(st[threadIdx.x] - gm);
+      st[threadIdx.x] = e;
+      sm += e;
+    }
+    for (int k = tail0 + threadIdx.x; k < ncn; k += NT) {
+      const float e = __expf(st[k] - gm);
+      st[k] = e;
+      sm += e;
+    }
+    const float ls = block_reduce<NT>(sm, false, red);
+    if (threadIdx.x == 0) xch[1] = ls;
+    cl.sync();
+    const float gs = crank == 0 ? ls + peer[1] : peer[1] + ls;   // same order on both CTAs
+    const double f = floor((double)ids[r]);
+    const long long id = f < 0 ? 0 : (f > (double)(V - 1) ? V - 1 : (long long)f);
+    if (crank == 0 && threadIdx.x == 0) p.acc[r] = ((double)logf(gs) + (double)gm) - (double)lg[r * V + id];
+    const float inv = 1.f / gs;
+    float* orow = o + r * V + c0;
+    __nv_bfloat16* srow16 = p.shadow ? p.shadow + r * p.spitch + c0 : nullptr;
+    const long long lid = id - c0;
+    auto grad = [&](int k) {
+      float g = st[k] * inv;
+      if (k == lid) g -= 1.f;
+      return g * invr;
+    };
+    if (!p.skip_f32)
+      for (int k = threadIdx.x; k < ncn; k += NT) __stcs(orow + k, grad(k));
+    if (srow16) {
+      // bf16 shadow as 4-byte column pairs on even absolute columns (the shadow row pitch
+      // is a multiple of 8); an odd first / last column of this half goes alone
+      const int k0 = (int)(c0 & 1);                  // first k whose absolute column is even
+      if (k0 && threadIdx.x == 0) srow16[0] = __float2bfloat16_rn(grad(0));
+      for (int k = k0 + 2 * threadIdx.x; k + 1 < ncn; k += 2 * NT)
+        *(__nv_bfloat162*)(srow16 + k) = __floats2bfloat162_rn(grad(k), grad(k + 1));
+      if (((ncn - k0) & 1) && threadIdx.x == 0) srow16[ncn - 1] = __float2bfloat16_rn(grad(ncn - 1));
+    }
+    if (srow16 && crank == 1)
+      for (long long k = cn + threadIdx.x; k < p.spitch - c0; k += NT) srow16[k] = __float2bfloat16_rn(0.f);
+    __syncthreads();                                  // srow reused by the next row
+  }
+  cl.sync();                                          // no CTA leaves while its peer reads xch
   publish_late(p.out, o);
   if (!last_block(p.counter)) return;
   if (threadIdx.x == 0) {
