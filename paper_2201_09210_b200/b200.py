@@ -263,13 +263,21 @@ class B200Backend:
             obj = [vals]
             dist.broadcast_object_list(obj, src=0)
             vals = obj[0]
-        if vals[0]:
-            _check(self.lib.coex_nvls_attach(self.ctx, vals[1], vals[2], vals[3], world))
-            if world > 1:
-                dist.barrier()
-            _check(self.lib.coex_nvls_bind(self.ctx))
-            if world > 1:
-                dist.barrier()
+        def agree(ok: bool) -> bool:
+            """every rank's verdict (a rank that cannot import the fd -- e.g. pidfd_getfd
+            refused by the ptrace policy -- sends the whole group back to NCCL)"""
+            if world == 1:
+                return ok
+            flags = [None] * world
+            dist.all_gather_object(flags, bool(ok))
+            return all(flags)
+
+        if vals[0] and agree(self.lib.coex_nvls_attach(self.ctx, vals[1], vals[2], vals[3], world) == 0):
+            if not agree(self.lib.coex_nvls_bind(self.ctx) == 0):
+                raise DeviceError("NVLS multicast bind failed on some rank: " +
+                                  self.lib.coex_last_error().decode(errors="replace"))
+        elif vals[0] and mode != "1":
+            return                                   # multicast unusable on some rank: NCCL buckets
         elif mode in ("1", "p2p"):
             h = ctypes.create_string_buffer(64)
             _check(self.lib.coex_p2p_create(self.ctx, nbytes, h))

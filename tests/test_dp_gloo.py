@@ -153,3 +153,92 @@ def test_dp2_gpt2_matches_global_batch(src):
     g1 = np.concatenate([r1[1][k].ravel() for k in keys])
     assert np.linalg.norm(g0 - w) <= 1e-9 * np.linalg.norm(w)
     np.testing.assert_array_equal(g0, g1)
+
+
+class _FakeNvlsLib:
+    """Stands in for libcoexb200.so's gradient-region entry points (no GPU here): records
+    the calls, fails the ones listed in `fail` on this rank."""
+
+    def __init__(self, rank, fail):
+        self.rank, self.fail, self.calls = rank, set(fail), []
+
+    def _rc(self, name):
+        self.calls.append(name)
+        return 8 if name in self.fail else 0
+
+    def coex_nvls_create(self, ctx, nbytes, world, info):
+        info[0], info[1], info[2] = 4242, 17, nbytes
+        return self._rc("create")
+
+    def coex_nvls_attach(self, ctx, pid, fd, nbytes, world):
+        assert (pid, fd, nbytes) == (4242, 17, 1 << 20)     # rank 0's export reached every rank
+        return self._rc("attach")
+
+    def coex_nvls_bind(self, ctx):
+        return self._rc("bind")
+
+    def coex_p2p_create(self, ctx, nbytes, h):
+        h.raw = bytes([self.rank]) * 64
+        return self._rc("p2p_create")
+
+    def coex_p2p_open(self, ctx, allh, world):
+        assert allh.raw[:64] == bytes([0]) * 64 and allh.raw[64:128] == bytes([1]) * 64
+        return self._rc("p2p_open")
+
+    def coex_nvls_info(self, ctx, out):
+        mode = 2 if "p2p_open" in self.calls else 1
+        out[0], out[1], out[2] = 1 << 20, 2, mode
+        return 0
+
+    def coex_last_error(self):
+        return b"fake"
+
+
+def _nvls_worker(rank, world, port, mode, fail, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    if mode is None:
+        os.environ.pop("COEX_NVLS", None)
+    else:
+        os.environ["COEX_NVLS"] = mode
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2201_09210_b200.b200 import B200Backend
+    be = object.__new__(B200Backend)            # host logic only: no context, no device
+    be.ctx, be.dp = None, DPGroup(rank, world, BATCH)
+    be.lib = _FakeNvlsLib(rank, fail.get(rank, ()))
+    be.nvls_bytes, be.nvls_mode = 0, "none"
+    be._init_nvls(1 << 20)
+    out[rank] = (be.nvls_bytes, be.nvls_mode, list(be.lib.calls))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("mode,fail,want", [
+    (None, {}, ("multicast", [["create", "attach", "bind"], ["attach", "bind"]])),
+    # a rank that cannot import the multicast fd sends the whole group back to NCCL
+    (None, {1: ("attach",)}, ("none", [["create", "attach"], ["attach"]])),
+    # ... or, with COEX_NVLS=1, to the P2P transport
+    ("1", {1: ("attach",)}, ("p2p", [["create", "attach", "p2p_create", "p2p_open"],
+                                     ["attach", "p2p_create", "p2p_open"]])),
+    # no multicast object at all (the one-GPU boxes): NCCL by default
+    (None, {0: ("create",)}, ("none", [["create"], []])),
+    ("p2p", {}, ("p2p", [["p2p_create", "p2p_open"], ["p2p_create", "p2p_open"]])),
+], ids=["multicast", "attach_fails_nccl", "attach_fails_p2p", "no_multicast", "forced_p2p"])
+def test_dp2_gradient_region_setup(mode, fail, want):
+    """World-2 host logic of the GEMM -> all-reduce fusion set-up (B200Backend._init_nvls):
+    rank 0's multicast export is broadcast, every rank's attach verdict is agreed on before
+    anyone binds, and every rank ends in the same transport."""
+    ctx = mp.get_context("spawn")
+    mgr = ctx.Manager()
+    out = mgr.dict()
+    port = _free_port()
+    procs = [ctx.Process(target=_nvls_worker, args=(r, 2, port, mode, fail, out)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+        assert p.exitcode == 0
+    res = dict(out)
+    tr, calls = want
+    for r in range(2):
+        nbytes, got_mode, got_calls = res[r]
+        assert got_mode == tr and got_calls == calls[r], (r, res[r])
+        assert (nbytes > 0) == (tr != "none")
