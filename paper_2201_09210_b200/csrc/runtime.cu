@@ -596,6 +596,7 @@ constexpr int kBnBwdFused = 100;
 // Plan-only kind: layernorm_dx + ln_dgamma + sum_rows over the same (x, dy) in one pass
 // (planner.py _bn_bwd_groups; outputs dx, dgamma, dbeta; fp32 / bf16 modes, 4 | d <= 1024).
 constexpr int kLnBwdFused = 103;
+constexpr int kSkewAdd = 104;      // add(a, rel_skew(x)) in one pass (planner _skew_pairs)
 // Plan-only kind: batchnorm whose apply pass also writes relu / leaky_relu of its output
 // (planner.py _bn_act_pairs; attr dims[0] = the activation's EW code; second output out2).
 constexpr int kBnAct = 101;
@@ -604,7 +605,7 @@ constexpr int kBnAct = 101;
 constexpr int kCeFused = 102;
 bool is_ext_compute(int kind) {
   return (kind >= COEX_CONV2D && kind <= COEX_SUM_ROWS) || kind == kBnBwdFused || kind == kBnAct || kind == kCeFused ||
-         kind == kLnBwdFused ||
+         kind == kLnBwdFused || kind == kSkewAdd ||
          (kind >= COEX_EMBEDDING && kind <= COEX_GLOBAL_AVGPOOL_GRAD && kind != COEX_GELU && kind != COEX_GELU_GRAD) ||
          (kind >= COEX_SLICE && kind <= COEX_SUM_AXIS);
 }
@@ -1819,7 +1820,8 @@ int build_xop_t(coex_ctx* c, const OpSpec& s, Launch* L, int* nL, size_t* ws_byt
     }
     case COEX_EMBEDDING: case COEX_EMBEDDING_DW: case COEX_LAYERNORM: case COEX_LAYERNORM_DX: case COEX_LN_DGAMMA:
     case COEX_BIAS_ADD: case COEX_CAUSAL_SOFTMAX: case COEX_SOFTMAX_GRAD: case COEX_CROSS_ENTROPY:
-    case COEX_CROSS_ENTROPY_GRAD: case COEX_REL_SKEW: case COEX_REL_UNSKEW: case kCeFused: case kLnBwdFused: {
+    case COEX_CROSS_ENTROPY_GRAD: case COEX_REL_SKEW: case COEX_REL_UNSKEW: case kCeFused: case kLnBwdFused:
+    case kSkewAdd: {
       RowParams rp{};
       rp.ds = s.ds; rp.x = s.in[0]; rp.y = s.in[1];
       rp.z = s.nin > 2 ? s.in[2] : In{nullptr, nullptr, nullptr};
@@ -1910,8 +1912,21 @@ int build_xop_t(coex_ctx* c, const OpSpec& s, Launch* L, int* nL, size_t* ws_byt
           L[(*nL)++].set(fn, warp_rows(rp.rows), dim3(256), rp);
           return COEX_OK;
         }
+        case kSkewAdd: {
+          if (!build) break;
+          if (is_f64(c) || d % 4) return fail(COEX_INVALID, "fused rel_skew + add: fp32 rows, 4 | T");
+          rp.d = d; rp.rows = xn / d;
+          L[(*nL)++].set((void*)k_rel_skew_v4<0, true>, warp_rows(rp.rows), dim3(256), rp);
+          return COEX_OK;
+        }
         case COEX_REL_SKEW: case COEX_REL_UNSKEW: {
           if (!build) break;
+          if (!is_f64(c) && d % 4 == 0) {           // 16-byte row stores
+            rp.d = d; rp.rows = xn / d;
+            L[(*nL)++].set(s.kind == COEX_REL_SKEW ? (void*)k_rel_skew_v4<0, false> : (void*)k_rel_skew_v4<1, false>,
+                           warp_rows(rp.rows), dim3(256), rp);
+            return COEX_OK;
+          }
           rp.d = d; rp.rows = xn / d;
           void* fn = s.kind == COEX_REL_SKEW ? (is_f64(c) ? (void*)k_rel_skew<double, 0> : (void*)k_rel_skew<float, 0>)
                                              : (is_f64(c) ? (void*)k_rel_skew<double, 1> : (void*)k_rel_skew<float, 1>);

@@ -179,6 +179,55 @@ __global__ void __launch_bounds__(256) k_rel_skew(RowParams p) {
   publish_late(p.out, o);
 }
 
+// fp32 rows of 4 | d floats: the same shifted row copies four columns per lane per step --
+// 16-byte stores, four scalar (shifted, unaligned) loads in flight, zero columns not read.
+// FUSED (planner _skew_pairs, plan kind 104): out = a + rel_skew(x), the attention logits'
+// add of the skewed relative term (y operand a = q.k^T) -- the skewed [BH, T, T] tensor never
+// reaches HBM.  Same per-element additions as rel_skew followed by add.
+template <int UN, bool FUSED>
+__global__ void __launch_bounds__(256) k_rel_skew_v4(RowParams p) {
+  COEX_PDL_ENTER();
+  stamp(p.ds, SK_SKEW);
+  const float* x = res<float>(p.x);
+  const float* a = FUSED ? res<float>(p.y) : nullptr;
+  float* o = pick_out<float>(p.out, x, a);
+  publish_early(p.out, o);
+  count_op(p.ds);
+  const int lane = threadIdx.x & 31;
+  const long long warps = (long long)gridDim.x * (blockDim.x / 32);
+  const int d = (int)p.d, d4 = d / 4;
+  for (long long r = (long long)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; r < p.rows; r += warps) {
+    const int i = (int)(r % d), sh = d - 1 - i;
+    const float* xr = x + r * d;
+    float4* orow = (float4*)(o + r * d);
+    const float4* ar = FUSED ? (const float4*)(a + r * d) : nullptr;
+    for (int q0 = lane; q0 < d4; q0 += 128) {      // four 16-byte groups per lane in flight
+      float v[4][4];
+      float4 av[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int q = q0 + 32 * u;
+        if (FUSED) av[u] = q < d4 ? ar[q] : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int c = 4 * q + e;
+          const bool in = q < d4 && (UN == 0 ? c <= i : c >= sh);
+          v[u][e] = in ? xr[UN == 0 ? c + sh : c - sh] : 0.f;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int q = q0 + 32 * u;
+        if (q >= d4) break;
+        float4 w = make_float4(v[u][0], v[u][1], v[u][2], v[u][3]);
+        if (FUSED) w = make_float4(av[u].x + w.x, av[u].y + w.y, av[u].z + w.z, av[u].w + w.w);
+        orow[q] = w;
+      }
+    }
+  }
+  publish_late(p.out, o);
+}
+
 // ------------------------------------------------------------------ layernorm
 // One warp per row; the row is read twice (mean, then centred moments) from L1/L2.
 template <typename T>

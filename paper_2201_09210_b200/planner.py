@@ -61,6 +61,7 @@ XOP_BN_BWD = 100          # fused batchnorm_dx + bn_dgamma + sum_rows (csrc COEX
 XOP_BN_ACT = 101          # batchnorm also writing relu / leaky_relu of its output (csrc kBnAct)
 XOP_CE_FUSED = 102        # cross_entropy + cross_entropy_grad in one pass (csrc kCeFused)
 XOP_LN_BWD = 103          # fused layernorm_dx + ln_dgamma + sum_rows (csrc kLnBwdFused)
+XOP_SKEW_ADD = 104        # add(a, rel_skew(x)) in one pass (csrc kSkewAdd)
 FA_HEAD = 64              # flash attention: head dim and query / key block of the tcgen05 kernels
 FA_BLOCK = 128
 
@@ -438,6 +439,7 @@ class Planner:
         self.n_mchains = 0
         self._act_for = {}
         self._ce_loss = {}                       # fused cross-entropy: gradient node -> loss node
+        self._skew_add = set()                   # adds fused with their rel_skew operand (kind 104)
         self._skip_f32 = {}                      # gradient node -> (plan word, attr index): 1 = no fp32 reader
         self._skip_cell = {}                     # its output cell -> gradient node
         self.n_attn = 0                          # flash-attention groups (forward + backward)
@@ -505,6 +507,11 @@ class Planner:
                 insts = [y for y in insts if not (isinstance(y, ExecOp) and y.node_id in gone_b)]
                 self._bias_for.update(bias_of)
                 self.n_bias_fused += len(bias_of)
+            skew_of = self._skew_pairs(insts) if (self.fuse and self.esize == 4) else {}
+            if skew_of:                             # the skewed relative term is added on the fly
+                gone_s = {sk.node_id for _, sk in skew_of.values()}
+                insts = [skew_of[y.node_id][0] if isinstance(y, ExecOp) and y.node_id in skew_of else y
+                         for y in insts if not (isinstance(y, ExecOp) and y.node_id in gone_s)]
             ce_of = self._ce_pairs(insts) if self.fuse else {}
             if ce_of:                               # the gradient moves up to the loss's position
                 grads = {g.node_id for g in ce_of.values()}
@@ -968,6 +975,39 @@ class Planner:
             out[m.node_id] = x
         return out
 
+    def _skew_pairs(self, insts) -> dict:
+        """add(a, rel_skew(x)) (C5's attention logits, q.k^T + skew(q.er^T)) where the skew's
+        only reader is that add, in one instruction list: ONE row pass computes the sum
+        (csrc k_rel_skew_v4<0, true>, plan kind 104), the skewed [BH, T, T] tensor is never
+        stored.  The skew must be a plain stored node (not fetched, merged, pinned or
+        assigned) and nothing between the two re-produces x.  Returns {add node: (fused
+        ExecOp, skew node)}; the fused op sits at the add's position."""
+        multi_nodes = {n for s_ in self._multi_sets() for n in s_}
+        banned = set(self.sp.fetch_nodes) | multi_nodes | set(self.force_store) | set(self.folded_assigns.values())
+        pos = {x.node_id: i for i, x in enumerate(insts) if isinstance(x, ExecOp)}
+        out = {}
+        for x in insts:
+            if not isinstance(x, ExecOp) or x.kind is not OpKind.ADD or x.node_id in banned:
+                continue
+            for j in (1, 0):
+                b, a = x.inputs[j], x.inputs[1 - j]
+                if b.fed or len(b.cands) != 1 or b.cands[0] not in pos:
+                    continue
+                sk = self.ops[b.cands[0]]
+                if sk.kind is not OpKind.REL_SKEW or sk.node_id in banned or pos[sk.node_id] > pos[x.node_id]:
+                    continue
+                if [c.node_id for c in self.consumers.get(sk.node_id, [])] != [x.node_id]:
+                    continue
+                xb = sk.inputs[0]
+                srcs = set(xb.cands) if not xb.fed else set()
+                if any(isinstance(y, ExecOp) and y.node_id in srcs for y in insts[pos[sk.node_id] + 1:pos[x.node_id]]):
+                    continue
+                fused = ExecOp(x.node_id, OpKind.REL_SKEW, {}, [xb, a])
+                self._skew_add.add(x.node_id)
+                out[x.node_id] = (fused, sk)
+                break
+        return out
+
     def _ce_pairs(self, insts) -> dict:
         """cross_entropy(lg, ids) and cross_entropy_grad(lg, ids) over the same bindings in one
         instruction list: one kernel computes both (the logits are read once).  The fused op
@@ -1119,6 +1159,8 @@ class Planner:
             kind_code = XOP_BN_ACT
             attr = [EW_CODE[act.kind]]
         skip = 0
+        if nid in self._skew_add:               # add(a, rel_skew(x))
+            kind_code = XOP_SKEW_ADD
         if ce_loss is not None:                 # loss + gradient in one pass over the logits
             kind_code = XOP_CE_FUSED
             skip = int(nid in self.shadow and self._gemm_only(nid))

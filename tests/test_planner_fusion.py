@@ -249,3 +249,30 @@ def test_arm_exclusive_buffers(dcgan):
     assert not aliased & set(pl.sp.fetch_nodes)
     sw = [x for x in walk(pl.sp.body) if isinstance(x, SwitchCase)]
     assert sw
+
+
+def test_rel_skew_add_fused():
+    """C5's attention logits add(q.k^T, rel_skew(q.er^T)): the skew's only reader is the add,
+    so the planner emits ONE plan kind 104 item per layer at the add's position (csrc
+    k_rel_skew_v4<0, true>) and the skew node itself disappears; f64 parity mode keeps the
+    two ops."""
+    from paper_2201_09210_b200.planner import T_XOP, XOP_SKEW_ADD
+    from paper_2201_09210_b200.workloads import C5_SMALL, music_transformer_program
+    src = music_transformer_program(steps=6, **C5_SMALL)
+    o = make_orch(src, SyntheticDataset(0), CpuBackend())
+    for _ in range(5):
+        o.step()
+    feed = {(n.id, p): tuple(s) for n in o.tg.all_nodes() if n.typ == "op" for p, s in n.feed_shapes.items()}
+    vs = o.be.var_shapes()
+    vi = {k: j for j, k in enumerate(sorted(vs))}
+    layers = C5_SMALL.get("layers", 2)
+    for esize, want in ((4, layers), (8, 0)):
+        pl = Planner(o.sp, o.tg, vi, vs, feed, esize, bf16=esize == 4)
+        w = pl.build().words
+        n = sum(1 for i in range(len(w) - 1) if w[i] == T_XOP and w[i + 1] == XOP_SKEW_ADD)
+        assert n == want == len(pl._skew_add), (esize, n)
+        for nid in pl._skew_add:
+            assert pl.ops[nid].kind is OpKind.ADD
+            skews = [c for b in pl.ops[nid].inputs if not b.fed for c in b.cands
+                     if pl.ops[c].kind is OpKind.REL_SKEW]
+            assert skews and all(c not in pl._emitted for c in skews)
