@@ -222,6 +222,10 @@ __global__ void __launch_bounds__(256) k_rel_skew_v4(RowParams p) {
         float4 w = make_float4(v[u][0], v[u][1], v[u][2], v[u][3]);
         if (FUSED) w = make_float4(av[u].x + w.x, av[u].y + w.y, av[u].z + w.z, av[u].w + w.w);
         orow[q] = w;
+        if (p.shadow) {                               // bf16 GEMM-operand copy (C5 unskew)
+          __nv_bfloat162 h0 = __floats2bfloat162_rn(w.x, w.y), h1 = __floats2bfloat162_rn(w.z, w.w);
+          ((uint2*)(p.shadow + r * d))[q] = make_uint2(*(uint32_t*)&h0, *(uint32_t*)&h1);
+        }
       }
     }
   }

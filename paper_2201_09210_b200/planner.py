@@ -357,6 +357,14 @@ class Planner:
                     # the fp32 output when only GEMMs read it, _exec)
                     self.shadow[nid] = new_buf(shape_size(shapes[nid]) * 2)
                     continue
+                if x.kind is OpKind.REL_UNSKEW and nid in node_buf and not node_buf[nid][2] and \
+                        shapes[nid][-1] % 8 == 0 and not any(nid in s_ for s_ in multi) and \
+                        any(c.kind is OpKind.RESHAPE and len(shapes[c.node_id]) == 2 and gemm_use(c.node_id)
+                            for c in consumers.get(nid, [])):
+                    # C5: the unskewed logits gradient feeds the relative-table GEMMs through a
+                    # 2-D reshape; the unskew pass writes their bf16 copy
+                    self.shadow[nid] = new_buf(shape_size(shapes[nid]) * 2)
+                    continue
                 if x.kind not in (OpKind.CAUSAL_SOFTMAX, OpKind.SOFTMAX_GRAD, OpKind.LAYERNORM) or nid not in node_buf:
                     continue
                 if node_buf[nid][2] or shapes[nid][-1] % 8 or any(nid in s_ for s_ in multi):
@@ -1194,6 +1202,14 @@ class Planner:
                 x.inputs[0].cands[0] in self._fa_shadow and len(shapes[nid]) == 2:
             shp = shapes[nid]
             self._copies[(pubs[nid][0], shp[0], shp[1])] = self._fa_shadow[x.inputs[0].cands[0]]
+            return
+        if x.kind is OpKind.RESHAPE and not x.inputs[0].fed and len(x.inputs[0].cands) == 1 and \
+                len(shapes[nid]) == 2 and self.ops[x.inputs[0].cands[0]].kind is OpKind.REL_UNSKEW and \
+                x.inputs[0].cands[0] in self.shadow and x.inputs[0].cands[0] in self._emitted:
+            # the unskew kernel's bf16 copy ([rows][T], T % 8 == 0: no padding) under the
+            # reshape's cell -- the relative-table GEMMs read it instead of converting
+            shp = shapes[nid]
+            self._copies[(pubs[nid][0], shp[0], shp[1])] = self.shadow[x.inputs[0].cands[0]]
             return
         if nid in self.shadow and (x.kind is not OpKind.CROSS_ENTROPY_GRAD or nid in self._ce_loss):
             shp = shapes[nid]
