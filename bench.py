@@ -86,7 +86,14 @@ def load_sustained(burst: float) -> float:
 
 # dram__bytes_read.sum + dram__bytes_write.sum of one representative launch of the dominant
 # GEMM family, from the committed `ncu --set full` captures (per launch, like `achieved`)
-TRAFFIC = {}
+# dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant kernel from one
+# committed `ncu --set full` capture (graph kernels inside conditional nodes cannot be
+# profiled, so the capture is of the same launch run eagerly): workload -> (bytes, note)
+TRAFFIC = {
+    "c4": (59.0e6, "k_gemm_tc MLP down-projection [8192,3072]x[3072,768] (BN 256): 55.2 MB read + 3.8 MB "
+                   "written per launch vs 80.2 MB algorithmic (A, B in bf16, C in fp32), "
+                   "profiles/round2_ncu_c4_gemm_fc2.ncu-rep"),
+}
 
 
 def load_peaks():
@@ -672,7 +679,10 @@ def run_b200(args):
     mem = graph_memory(o)
     if rank == 0:                      # kernel evidence while this context is alive
         roof = graph_roofline(o, be, args.workload, hbm, load_sustained(tfl), peak_kind)
-        roof["traffic"] = TRAFFIC.get(args.workload)
+        if args.workload in TRAFFIC:
+            roof["traffic"], roof["traffic_note"] = TRAFFIC[args.workload]
+        else:
+            roof["traffic"] = None
         if args.eager_families and args.workload != "c1":
             roof["eager_families"] = roofline_c2(be, hbm, tfl, peak_kind, args.workload)
         if args.workload == "c1":
