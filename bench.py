@@ -3,17 +3,16 @@
 Metric (BASELINE.json): training iterations/s at 1/2/4/8 B200, next to the reference CPU
 co-execution path, with the dominant kernel's roofline fraction.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2|c1]
-                    [--precision f64|fp32|bf16] [--impl b200|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c1|c2|c3|c4|c5]
+                    [--precision f64|fp32|bf16] [--impl b200|reference] [--force-dp]
 
-Workloads (paper_2201_09210_b200/workloads.py):
-* ``c2`` (default) -- BASELINE.json configs[1], DCGAN 64x64, batch 128, generator /
-  discriminator steps alternating through a SwitchCase on ``native mod(step, 2)``; bf16
-  tcgen05 convolutions / GEMMs (implicit-GEMM lowering), fp32 everything else.  A step is
-  one D or one G iteration; ``value`` counts iterations of either kind.
+Workloads (paper_2201_09210_b200/workloads.py).  BASELINE.json's metric names no
+configuration, so the default is the largest one that fits one GPU:
+* ``c4`` (default) -- configs[3], GPT-2 small (12 layers, d=768, 12 heads, T=1024, batch 8,
+  vocab 50257), hand-written backward, data-dependent ``while`` over the fetched loss; bf16.
 * ``c1`` -- configs[0], the tiny MLP the reference's own CPU path can express (f64 parity).
-* ``c4`` -- configs[3], GPT-2 small (12 layers, d=768, 12 heads, T=1024, batch 8, vocab
-  50257), hand-written backward, data-dependent ``while`` over the fetched loss; bf16.
+* ``c2`` -- configs[1], DCGAN 64x64, batch 128, generator / discriminator steps alternating
+  through a SwitchCase on ``native mod(step, 2)``; a step is one D or one G iteration.
 * ``c3`` -- configs[2], ResNet-50 (224x224, batch 64) with SDPoint: a 4-way SwitchCase on
   ``native choice`` picks the stochastic downsampling point each step; bf16.
 * ``c5`` -- configs[4], Music Transformer (6 layers, d=512, 8 heads, T=1024, batch 8, vocab
@@ -32,19 +31,20 @@ pinned mapped memory).
   (``InMemoryDataset`` over pinned host memory, ``B200Backend.pin``): every step moves the
   step's inputs host->device (the feed kernel reads them across the bus, converting to the
   compute precision) and reads the printed loss back.
-* ``roofline``: every distinct op of one D+G step pair re-launched eagerly with the step's
-  shapes, launch by launch, between CUDA events on the same stream (coex_exec_op_profile);
-  kernels grouped by family; the family with the largest share of step time is the
-  dominant kernel, its achieved FLOP/s (tensor-bound) or GB/s (memory-bound) over the
-  algorithmic work stated in DESIGN.md.
-* ``cpu_baseline``: the CPU oracle co-execution (oracle/, SPEC-faithful runner + f64
-  kernels) on a bounded sample, rank 0 only.
+* ``roofline``: from the pass graph itself -- device ``%globaltimer`` stamps of every graph
+  kernel over co-executed steps after the timed region; the dominant kernel (``k_gemm_tc``
+  for the bf16 workloads) achieved = the step's algorithmic FLOPs / its summed in-graph
+  time, against MEASURED_PEAKS.json; ``traffic`` from the committed ncu
+  capture of a representative launch.
+* ``cpu_baseline`` / ``--impl reference``: the CPU oracle co-execution (oracle/,
+  SPEC-faithful runner + f64 kernels) measured on a stated sample, rank 0 only.
 
 Multi-GPU: one process per GPU (torchrun), data parallel (paper_2201_09210_b200/dp.py):
-every rank runs the host program on the global batch (C1: 64*N, C2: 128*N) while its device
-expands and trains on its own row shard; gradients (and the fetched loss) are all-reduced by
-NCCL nodes inside the pass graph.  C2 normalises with per-replica batch statistics (data-
-parallel training without synchronised batch norm).  Weak scaling; time = max over ranks.
+every rank runs the host program on the global batch while its device expands and trains
+on its own row shard; batch norm is synchronised, gradients are reduced in their GEMM
+epilogues into a multicast region when the box provides one (csrc/nvls.cuh) and otherwise
+all-reduced by bucketed NCCL nodes inside the pass graph.  Weak scaling; time = max over
+ranks.  ``--force-dp`` runs the data-parallel program on a forced 1-rank group.
 """
 
 from __future__ import annotations
@@ -84,8 +84,6 @@ def load_sustained(burst: float) -> float:
         return burst
 
 
-# dram__bytes_read.sum + dram__bytes_write.sum of one representative launch of the dominant
-# GEMM family, from the committed `ncu --set full` captures (per launch, like `achieved`)
 # dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant kernel from one
 # committed `ncu --set full` capture (graph kernels inside conditional nodes cannot be
 # profiled, so the capture is of the same launch run eagerly): workload -> (bytes, note)
