@@ -479,6 +479,24 @@ __global__ void __launch_bounds__(256) k_transpose_rows(TransposeParams p) {
   const long long vpr = inner / V;                 // vectors per row
   const long long rows = p.n / inner;
   const long long stride = (long long)gridDim.x * blockDim.x;
+  if (rows * vpr < (1ll << 31) && p.n < (1ll << 31)) {
+    // 32-bit index arithmetic (the 64-bit div / mod chain per 16 bytes made the copy
+    // instruction-bound: C5 head splits at ~40 % of HBM)
+    const unsigned total = (unsigned)(rows * vpr), uv = (unsigned)vpr, uin = (unsigned)inner;
+    for (unsigned u = blockIdx.x * blockDim.x + threadIdx.x; u < total; u += (unsigned)stride) {
+      const unsigned r = u / uv, e = (u - r * uv) * V;
+      unsigned rem = r, src = 0;
+      for (int d = p.rank - 2; d >= 0; --d) {
+        const unsigned sd = (unsigned)p.out_shape[d];
+        const unsigned q = rem / sd;
+        src += (rem - q * sd) * (unsigned)p.src_stride[d];
+        rem = q;
+      }
+      *(uint4*)(o + (size_t)r * uin + e) = *(const uint4*)(a + src + e);
+    }
+    publish_late(p.out, o);
+    return;
+  }
   for (long long u = (long long)blockIdx.x * blockDim.x + threadIdx.x; u < rows * vpr; u += stride) {
     const long long r = u / vpr, e = (u - r * vpr) * V;
     long long rem = r, src = 0;
