@@ -1866,6 +1866,11 @@ int build_xop_t(coex_ctx* c, const OpSpec& s, Launch* L, int* nL, size_t* ws_byt
                  : per <= 4 ? (fw ? (void*)k_layernorm_v4<0, 4> : (void*)k_layernorm_v4<1, 4>)
                  : per <= 6 ? (fw ? (void*)k_layernorm_v4<0, 6> : (void*)k_layernorm_v4<1, 6>)
                             : (fw ? (void*)k_layernorm_v4<0, 8> : (void*)k_layernorm_v4<1, 8>);
+            // 128-thread blocks (4 rows each): 7 resident per SM at 72 registers instead of 3 of
+            // 256 threads -- fewer partial waves (ncu: 2.31 waves, 33 % warps active before)
+            const int64_t b = (rp.rows + 3) / 4;
+            L[(*nL)++].set(fn, dim3((unsigned)(b < kNumSMs * 16 ? (b < 1 ? 1 : b) : kNumSMs * 16)), dim3(128), rp);
+            return COEX_OK;
           }
           L[(*nL)++].set(fn, warp_rows(rp.rows), dim3(256), rp);
           return COEX_OK;
