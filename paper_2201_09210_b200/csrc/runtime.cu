@@ -1888,9 +1888,11 @@ int build_xop_t(coex_ctx* c, const OpSpec& s, Launch* L, int* nL, size_t* ws_byt
           const int per = (int)((d / 4 + 31) / 32);
           void* fn = per <= 2 ? (void*)k_ln_bwd_v4<2> : per <= 4 ? (void*)k_ln_bwd_v4<4>
                    : per <= 6 ? (void*)k_ln_bwd_v4<6> : (void*)k_ln_bwd_v4<8>;
-          int64_t blocks = (rp.rows + 7) / 8;
-          if (blocks > kNumSMs * 2) blocks = kNumSMs * 2;
-          L[(*nL)++].set(fn, dim3((unsigned)(blocks < 1 ? 1 : blocks)), dim3(256), lp);
+          // 128-thread blocks: at ~135 registers three are resident per SM (one of 256 threads
+          // before), one wave of blocks
+          int64_t blocks = (rp.rows + 3) / 4;
+          if (blocks > kNumSMs * 3) blocks = kNumSMs * 3;
+          L[(*nL)++].set(fn, dim3((unsigned)(blocks < 1 ? 1 : blocks)), dim3(128), lp);
           return COEX_OK;
         }
         case COEX_LN_DGAMMA: {
