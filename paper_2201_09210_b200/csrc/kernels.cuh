@@ -380,6 +380,8 @@ struct ReduceParams {
   long long n;
   int mean;
   Out out;
+  double* part;              // k_reduce_multi: per-block partials (context scratch)
+  unsigned int* counter;     // k_reduce_multi: last-block election
 };
 
 // Parity path: one warp streams the data, lane 0 accumulates strictly in order.
@@ -404,6 +406,59 @@ __global__ void __launch_bounds__(32) k_reduce_seq(ReduceParams p) {
   }
   if (lane == 0) o[0] = (T)(p.mean ? __ddiv_rn(acc, (double)p.n) : acc);
   publish_late(p.out, o);
+}
+
+// Tolerance path, large inputs: every block sums a contiguous chunk in double (16-byte loads
+// when aligned) into part[block]; the last block to finish adds the partials in block order
+// (deterministic for a given grid) and re-arms the counter.  The context owns part / counter
+// (kernels of one context run in stream order; PDL dependents wait for the grid).
+constexpr int kReduceMaxBlocks = 1024;
+template <typename T>
+__global__ void __launch_bounds__(256) k_reduce_multi(ReduceParams p) {
+  COEX_PDL_ENTER();
+  stamp(p.ds, SK_REDUCE);
+  const T* a = res<T>(p.a);
+  T* o = pick_out<T>(p.out, a, nullptr);
+  publish_early(p.out, o);
+  count_op(p.ds);
+  __shared__ double red[8];
+  __shared__ unsigned int last;
+  const long long lo = p.n * blockIdx.x / gridDim.x, hi = p.n * (blockIdx.x + 1) / gridDim.x;
+  double acc = 0.0;
+  long long i = lo + threadIdx.x;
+  if constexpr (sizeof(T) == 4) {
+    const long long a0 = (lo + 3) & ~3ll, a1 = hi & ~3ll;      // 16-byte aligned body (a is)
+    if (((uintptr_t)a & 15) == 0 && a1 > a0) {
+      for (long long j = lo + threadIdx.x; j < a0; j += blockDim.x) acc += (double)a[j];
+      const float4* a4 = (const float4*)(a + a0);
+      const long long n4 = (a1 - a0) / 4;
+      for (long long q = threadIdx.x; q < n4; q += blockDim.x) {
+        const float4 v = __ldcs(a4 + q);
+        acc += ((double)v.x + (double)v.y) + ((double)v.z + (double)v.w);
+      }
+      i = a1 + threadIdx.x;
+    }
+  }
+  for (; i < hi; i += blockDim.x) acc += (double)a[i];
+  for (int s = 16; s > 0; s >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double b = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) b += red[w];
+    p.part[blockIdx.x] = b;
+    __threadfence();
+    last = atomicAdd(p.counter, 1u) == gridDim.x - 1 ? 1u : 0u;
+    if (last) {
+      __threadfence();
+      double s = 0.0;
+      for (unsigned int k = 0; k < gridDim.x; ++k) s += __ldcg(p.part + k);
+      o[0] = (T)(p.mean ? s / (double)p.n : s);
+      *p.counter = 0u;
+    }
+  }
+  __syncthreads();
+  if (last) publish_late(p.out, o);
 }
 
 // Tolerance path (fp32 / bf16 contexts): warp-shuffle tree in double, one block.

@@ -197,6 +197,8 @@ struct coex_ctx {
   unsigned int* nv_gen = nullptr;        // barrier generations (ordinary device memory)
   int nv_next_slot = 0;
   int nv_mode = 0;                       // RedMode: RED_MC (multicast) / RED_P2P (IPC-opened peers)
+  double* d_red_part = nullptr;          // k_reduce_multi partials / counter (context scratch)
+  unsigned int* d_red_counter = nullptr;
   char* nv_peer[kMaxPeers] = {nullptr};  // RED_P2P: every rank's region (own = nv_local)
   bool nv_p2p_own = false;               // RED_P2P: nv_local from cudaMalloc (freed here)
 };
@@ -753,8 +755,18 @@ int build_launch_t(coex_ctx* c, const OpSpec& s, Launch* L) {
       p.n = numel_of(s.in_ndim[0], s.in_shape[0]);
       p.mean = s.kind == COEX_MEAN;
       p.out = s.out;
-      if (is_f64(c)) L->set((void*)k_reduce_seq_smem<T>, dim3(1), dim3(256), p);
-      else L->set((void*)k_reduce_tree<T>, dim3(1), dim3(1024), p);
+      if (is_f64(c)) {
+        L->set((void*)k_reduce_seq_smem<T>, dim3(1), dim3(256), p);
+      } else if (p.n >= (1 << 20) && c->d_red_part != nullptr) {
+        // large tolerance-mode sums: every SM (was one block of 1024 threads)
+        int64_t g = p.n / 16384;
+        g = g < 2 * kNumSMs ? g : 2 * kNumSMs;
+        p.part = c->d_red_part;
+        p.counter = c->d_red_counter;
+        L->set((void*)k_reduce_multi<T>, dim3((unsigned)(g < 2 ? 2 : g)), dim3(256), p);
+      } else {
+        L->set((void*)k_reduce_tree<T>, dim3(1), dim3(1024), p);
+      }
       return COEX_OK;
     }
     case COEX_TRANSPOSE: {
@@ -2185,6 +2197,9 @@ int coex_ctx_create(int device, int precision, coex_ctx** out) {
   memset((void*)c->mb, 0, sizeof(Mailbox));
   CK(cudaHostGetDevicePointer((void**)&c->d_mb, c->mb, 0));
   c->feed_cap = (size_t)32 << 20;   // doubles (256 MiB)
+  CK(cudaMalloc(&c->d_red_part, sizeof(double) * kReduceMaxBlocks + 64));
+  c->d_red_counter = (unsigned int*)(c->d_red_part + kReduceMaxBlocks);
+  CK(cudaMemset(c->d_red_part, 0, sizeof(double) * kReduceMaxBlocks + 64));
   CK(cudaHostAlloc((void**)&c->feed_arena, c->feed_cap * sizeof(double), cudaHostAllocMapped));
   CK(cudaHostGetDevicePointer((void**)&c->d_feed_arena, c->feed_arena, 0));
   c->fetch_cap = (size_t)64 << 20;  // bytes
@@ -2235,6 +2250,7 @@ int coex_ctx_destroy(coex_ctx* c) {
   cudaFreeHost(c->feed_arena);
   cudaFreeHost(c->fetch_arena);
   cudaFree(c->d_jump);
+  if (c->d_red_part) cudaFree(c->d_red_part);
   if (c->h_stage) cudaFreeHost(c->h_stage);
   for (auto& ev : c->events)
     if (ev) cudaEventDestroy(ev);

@@ -27,6 +27,8 @@ CASES = [
     (OpKind.RELU, {}, [Tensor((6,), [-1.0, -0.0, 0.0, 2.5, float("nan"), -3.0])]),
     (OpKind.SUM, {}, [rt(64, 10)]),
     (OpKind.SUM, {}, [rt(1000, 1000)]),
+    (OpKind.SUM, {}, [rt(2048, 2049)]),          # tolerance modes: multi-block k_reduce_multi
+    (OpKind.MEAN, {}, [rt(3, 1 << 20)]),
     (OpKind.SUM, {}, [Tensor((3,), [-0.0, -0.0, -0.0])]),
     (OpKind.SUM, {}, [Tensor((0,), [])]),
     (OpKind.MEAN, {}, [rt(33, 17)]),
